@@ -1,0 +1,364 @@
+#!/usr/bin/env python
+"""Headline benchmark: samples·epochs/s of batch-SOM training (K=1024, D=50).
+
+Workload (BASELINE.json configs[1]): 32x32 hexagonal lattice (1024 nodes),
+10,000,000 x 50 synthetic Gaussian-mixture rows per GPU,
+full sampling.  One *step* = one training epoch over all rows: influence(σ)
+→ BMU search (K1) → exact near-tie re-check → per-BMU accumulation (K2) →
+reduce [+ NCCL allreduce for N>1] → FP64 smoothing (K3) → apply_update.
+
+  value : device-timed epochs with the rows resident in HBM (CUDA events on
+          the engine stream, max over ranks); inputs (2 GB/GPU) exceed L2.
+  e2e   : the reference's own training loop (train_with_executor) with the
+          B200 CudaExecutor, from a host DataMatrix: the timed region includes
+          the host→device upload of the rows, every epoch's codebook/influence
+          upload and accumulator download (wall clock).
+  --impl reference : the reference CPU implementation (oracle/_ref =
+          /root/reference headers compiled, train_parallel on all host cores)
+          on a bounded sample of the same workload.
+
+Usage: python bench.py [--gpus N] [--steps K] [--warmup W] [--impl reference]
+"""
+from __future__ import annotations
+
+import argparse
+import json
+import math
+import os
+import statistics
+import subprocess
+import sys
+import threading
+import time
+
+ROOT = os.path.dirname(os.path.abspath(__file__))
+sys.path.insert(0, ROOT)
+
+METRIC = "samples·epochs/sec (1024 nodes, D=50) at 1/2/4/8 B200; % roofline; QE vs CPU"
+UNIT = "samples·epochs/s"
+P_GRID = (32, 32)
+P = P_GRID[0] * P_GRID[1]
+D = 50
+N_PER_GPU = 10_000_000
+SEED = 2602  # seed = 2604 + config number - 2 ... config c2
+EPOCHS = 10
+
+
+def peaks():
+    try:
+        with open(os.path.join(ROOT, "MEASURED_PEAKS.json")) as f:
+            return json.load(f), "measured"
+    except Exception:
+        return {"hbm_gbs": 6650.0, "bf16_tflops": 1590.0, "bf16_tflops_sustained": 1400.0}, \
+            "fallback"
+
+
+class ClockSampler:
+    """nvidia-smi clocks + throttle reasons during the timed region."""
+
+    def __init__(self, index=0):
+        self.index = index
+        self.samples = []
+        self._stop = threading.Event()
+        self._proc = None
+
+    def __enter__(self):
+        q = ("clocks.sm,clocks.max.sm,power.draw,clocks_event_reasons.active,"
+             "clocks_event_reasons.hw_slowdown,clocks_event_reasons.hw_thermal_slowdown,"
+             "clocks_event_reasons.sw_thermal_slowdown,clocks_event_reasons.sw_power_cap")
+        try:
+            self._proc = subprocess.Popen(
+                ["nvidia-smi", "-i", str(self.index), f"--query-gpu={q}", "--format=csv,noheader,nounits",
+                 "-lms", "100"], stdout=subprocess.PIPE, stderr=subprocess.DEVNULL, text=True)
+            self._t = threading.Thread(target=self._read, daemon=True)
+            self._t.start()
+        except Exception:
+            self._proc = None
+        return self
+
+    def _read(self):
+        for line in self._proc.stdout:
+            parts = [p.strip() for p in line.split(",")]
+            if len(parts) >= 8:
+                self.samples.append(parts)
+
+    def __exit__(self, *exc):
+        if self._proc:
+            self._proc.terminate()
+            try:
+                self._proc.wait(timeout=5)
+            except Exception:
+                self._proc.kill()
+
+    def summary(self):
+        if not self.samples:
+            return {"sm_mhz": None, "sm_max_mhz": None, "reasons": ["unsampled"]}
+        sm = [float(s[0]) for s in self.samples if s[0].replace(".", "").isdigit()]
+        mx = [float(s[1]) for s in self.samples if s[1].replace(".", "").isdigit()]
+        names = ["hw_slowdown", "hw_thermal_slowdown", "sw_thermal_slowdown", "sw_power_cap"]
+        reasons = sorted({names[i] for s in self.samples for i in range(4)
+                          if s[4 + i].lower() == "active"})
+        return {"sm_mhz": statistics.median(sm) if sm else None,
+                "sm_max_mhz": max(mx) if mx else None, "reasons": reasons,
+                "samples": len(self.samples)}
+
+
+def dist_env():
+    world = int(os.environ.get("WORLD_SIZE", "1"))
+    rank = int(os.environ.get("RANK", "0"))
+    local = int(os.environ.get("LOCAL_RANK", "0"))
+    return world, rank, local
+
+
+# ---------------------------------------------------------------------------
+# CPU reference (oracle/_ref: the reference headers compiled) on a bounded sample
+# ---------------------------------------------------------------------------
+
+def cpu_reference(step_seconds=6.0, steps=1, warmup=0):
+    """Time the reference's train_parallel (all host cores) on a bounded sample
+    of the headline workload: 32x32 hex, D=50, full sampling; each step = one
+    epoch.  Returns (samples·epochs/s, cores, kind, sample description)."""
+    import numpy as np
+
+    import oracle
+    chk = oracle.best()
+    cores = os.cpu_count() or 1
+    # calibrate rows so one epoch takes ~step_seconds
+    probe_rows = 256 * cores
+    x = chk.synth_gmm(probe_rows, D, SEED)
+    cfg = oracle.SomConfig(topology="hex", grid_w=P_GRID[0], grid_h=P_GRID[1], n_iters=1,
+                           seed=SEED, n_threads=cores)
+    t0 = time.perf_counter()
+    chk.train(cfg, x)
+    rate = probe_rows / max(time.perf_counter() - t0, 1e-6)
+    rows = int(min(max(rate * step_seconds, probe_rows), 400_000))
+    x = chk.synth_gmm(rows, D, SEED)
+    cfg.n_iters = 1
+    for _ in range(warmup):
+        chk.train(cfg, x)
+    times = []
+    for _ in range(max(steps, 1)):
+        t0 = time.perf_counter()
+        chk.train(cfg, x)
+        times.append(time.perf_counter() - t0)
+    value = rows / statistics.mean(times)
+    sample = (f"{rows} of the {N_PER_GPU} rows (same GMM generator), 32x32 hex, D=50, 1 epoch "
+              f"per step incl. init; train_parallel G={cores}")
+    return value, cores, chk.kind, sample, statistics.mean(times)
+
+
+def run_reference_arm(args):
+    world, rank, _ = dist_env()
+    if rank != 0:
+        return 0
+    steps = max(1, min(args.steps, 5))
+    value, cores, kind, sample, t = cpu_reference(step_seconds=4.0, steps=steps,
+                                                  warmup=min(args.warmup, 1))
+    line = {
+        "metric": METRIC, "value": value, "unit": UNIT, "n_gpus": args.gpus, "steps": steps,
+        "warmup": min(args.warmup, 1), "ms_per_step": t * 1e3, "higher_is_better": True,
+        "scaling": "weak", "vs_baseline": None, "dtype": "f64", "data": "synthetic",
+        "impl": "reference",
+        "config": {"workload": "c2: 32x32 hex SOM (1024 nodes), D=50, GMM rows, full sampling "
+                               "(bounded CPU sample)", "model": "batch-SOM"},
+        "cpu_baseline": {"value": value, "unit": UNIT, "cores": cores, "kind": kind,
+                         "sample": sample},
+        "e2e": {"value": value, "unit": UNIT, "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0},
+    }
+    print(json.dumps(line), flush=True)
+    return 0
+
+
+# ---------------------------------------------------------------------------
+# GPU arm
+# ---------------------------------------------------------------------------
+
+def host_gmm_rows(n, seed):
+    """Host (pinned) GMM rows of the SURVEY §8(d) shape: centres from the
+    reference Rng(seed, synth), component + unit noise drawn on the GPU with
+    torch (values do not change dense-loop cost; parity runs use the
+    reference generator)."""
+    import numpy as np
+    import torch
+
+    from paper_2604_26555_b200.hostref import Rng
+    r = Rng(seed, "synth")
+    centres = np.array([[-4.0 + 8.0 * r.real01() for _ in range(D)] for _ in range(16)],
+                       np.float32)
+    g = torch.Generator(device="cuda").manual_seed(seed)
+    comp = torch.randint(0, 16, (n,), device="cuda", generator=g)
+    x = torch.randn((n, D), device="cuda", generator=g, dtype=torch.float32)
+    x += torch.from_numpy(centres).cuda()[comp]
+    host = torch.empty((n, D), dtype=torch.float32, pin_memory=True)
+    host.copy_(x)
+    del x, comp
+    torch.cuda.empty_cache()
+    return host.numpy()
+
+
+def run_gpu_arm(args):
+    import numpy as np
+    import torch
+    import torch.distributed as dist
+
+    import paper_2604_26555_b200 as tsom
+    from paper_2604_26555_b200 import _lib
+    from paper_2604_26555_b200.hostref import (init_sample_draw, lattice_dist,
+                                               resolved_sigma0, schedule_value)
+
+    world, rank, local = dist_env()
+    torch.cuda.set_device(local)
+    if world > 1:
+        dist.init_process_group("gloo")
+    n = N_PER_GPU
+
+    # this rank's shard of the workload (weak scaling: n rows per GPU)
+    host = host_gmm_rows(n, SEED + rank)
+    eng = tsom.Engine(P, D, device=local)
+    if args.kernel:
+        eng.set_option(_lib.TSOM_OPT_BMU_KERNEL, args.kernel)
+    eng.bind(host)
+    if world > 1:
+        uid = [eng.comm_unique_id() if rank == 0 else None]
+        dist.broadcast_object_list(uid, src=0)
+        eng.comm_init(uid[0], rank, world)
+    # init_weights(sample_draw) (trainer.hpp:192-211) over rank 0's rows, same on every rank
+    w0 = init_sample_draw(host_gmm_rows(n, SEED) if rank else host, P, SEED)
+    eng.set_codebook(w0)
+    eng.set_topology_distance(lattice_dist("hex", *P_GRID))
+    sigma0 = resolved_sigma0("hex", *P_GRID)
+
+    def epoch(t):
+        tt = t % EPOCHS
+        eta = schedule_value(0.5, "linear", tt, EPOCHS, 1e-4)
+        sigma = schedule_value(sigma0, "linear", tt, EPOCHS, 0.3)
+        eng.train_epoch(eta, sigma)
+
+    for t in range(args.warmup):
+        epoch(t)
+    stream = torch.cuda.ExternalStream(eng.stream, device=f"cuda:{local}")
+    ev0, ev1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    launches0 = _lib.kernel_launches()
+    k1_ms, total_ms, rechecks = [], [], []
+    if world > 1:
+        dist.barrier()
+    torch.cuda.synchronize()
+    with ClockSampler(local) as clk:
+        ev0.record(stream)
+        for t in range(args.warmup, args.warmup + args.steps):
+            epoch(t)
+            det = eng.timing_detail()
+            k1_ms.append(det["k1_ms"])
+            total_ms.append(det["total_ms"])
+            rechecks.append(eng.last_recheck_count)
+        ev1.record(stream)
+        torch.cuda.synchronize()
+    launches = _lib.kernel_launches() - launches0
+    elapsed = ev0.elapsed_time(ev1)
+    if world > 1:
+        tmax = torch.tensor([elapsed], dtype=torch.float64)
+        dist.all_reduce(tmax, op=dist.ReduceOp.MAX)
+        elapsed = float(tmax.item())
+        dist.barrier()
+    ms = elapsed / args.steps
+    value = n * world / (ms / 1e3)
+    s, c = eng.qe()
+    qe_gpu = s / c
+
+    # e2e through the public C++ API (reference loop + CudaExecutor), rank 0 only
+    e2e = None
+    if rank == 0 and world == 1 and not args.no_e2e:
+        from paper_2604_26555_b200 import dropin
+        if dropin.available():
+            eng.close()
+            cfg = dropin.TrainConfig(topology="hex", grid_w=P_GRID[0], grid_h=P_GRID[1],
+                                     n_iters=EPOCHS, seed=SEED)
+            warm = dropin.TrainConfig(topology="hex", grid_w=P_GRID[0], grid_h=P_GRID[1],
+                                      n_iters=1, seed=SEED)
+            dropin.train_cuda(warm, host[:200_000], device=local)
+            _, _, _, secs = dropin.train_cuda(cfg, host, device=local)
+            h2d = n * D * 4 + EPOCHS * (P * D * 4 + P * P * 8)
+            d2h = EPOCHS * (P * D * 8 + P * 8)
+            e2e = {"value": n * EPOCHS / secs, "unit": UNIT,
+                   "h2d_bytes_per_step": int(h2d / EPOCHS), "d2h_bytes_per_step": int(d2h / EPOCHS),
+                   "path": "toposom::train_with_executor + toposom_b200::CudaExecutor "
+                           "(libtsom_dropin.so), host DataMatrix, 10 epochs per call, wall clock",
+                   "seconds_per_call": secs}
+            eng = None
+    pk, pk_kind = peaks()
+    k1 = statistics.mean(k1_ms) if k1_ms else float("nan")
+    flops = 2.0 * P * D * n
+    tf32_peak = pk["bf16_tflops"] / 2.0
+    achieved = flops / (k1 / 1e3) / 1e12 if k1 > 0 else 0.0
+    roof = {"bound": "tensor", "kernel": "k1 BMU (" + ("tcgen05 3xTF32" if args.kernel != 1 and
+                                                      tsom_tc_active() else "SIMT FP32") + ")",
+            "achieved": achieved, "peak": tf32_peak / 3.0, "unit": "TFLOP/s",
+            "frac": achieved / (tf32_peak / 3.0),
+            "traffic": None,
+            "note": (f"achieved = 2*K*D*N useful flop per launch / mean K1 event time; peak = "
+                     f"{pk_kind} bf16 {pk['bf16_tflops']} TF/s / 2 (TF32) / 3 (3xTF32 split)"),
+            "k1_ms": k1, "epoch_ms": statistics.mean(total_ms) if total_ms else None}
+    line = {
+        "metric": METRIC, "value": value, "unit": UNIT, "n_gpus": world, "steps": args.steps,
+        "warmup": args.warmup, "ms_per_step": ms, "higher_is_better": True, "scaling": "weak",
+        "vs_baseline": None, "dtype": "f32 (3xTF32 BMU) + f64 accumulate/update",
+        "data": "synthetic Gaussian mixture (16 comps, U[-4,4] centres, unit noise), random-init "
+                "codebook by sample_draw",
+        "config": {"workload": "c2: 32x32 hex SOM (1024 nodes), 1e7 x 50 rows per GPU, full "
+                               "sampling, resident in HBM", "model": "batch-SOM",
+                   "nodes": P, "dims": D, "rows_per_gpu": n, "global_rows": n * world,
+                   "parallelism": f"dp{world}", "l2": "inputs (2 GB/GPU) > L2 (126 MB); no flush"},
+        "roofline": roof,
+        "clocks": clk.summary(),
+        "gpu_launches": int(launches),
+        "qe_gpu_after": qe_gpu,
+        "rechecked_rows_per_epoch": statistics.mean(rechecks) if rechecks else None,
+    }
+    if e2e:
+        line["e2e"] = e2e
+    if rank == 0 and world == 1 and not args.no_cpu:
+        v, cores, kind, sample, _ = cpu_reference(step_seconds=6.0)
+        line["cpu_baseline"] = {"value": v, "unit": UNIT, "cores": cores, "kind": kind,
+                                "sample": sample}
+    if rank == 0:
+        print(json.dumps(line), flush=True)
+    if world > 1:
+        dist.destroy_process_group()
+    return 0
+
+
+def tsom_tc_active():
+    from paper_2604_26555_b200 import _lib
+    L = _lib.load()
+    return b"tcgen05" in L.tsom_version() and _tc_probe()
+
+
+def _tc_probe():
+    import paper_2604_26555_b200 as tsom
+    from paper_2604_26555_b200 import _lib
+    try:
+        e = tsom.Engine(256, D)
+        e.set_option(_lib.TSOM_OPT_BMU_KERNEL, 2)
+        e.close()
+        return True
+    except Exception:
+        return False
+
+
+def main():
+    ap = argparse.ArgumentParser()
+    ap.add_argument("--gpus", type=int, default=1)
+    ap.add_argument("--steps", type=int, default=20)
+    ap.add_argument("--warmup", type=int, default=3)
+    ap.add_argument("--impl", default="b200", choices=["b200", "reference"])
+    ap.add_argument("--kernel", type=int, default=0, help="0 auto, 1 SIMT, 2 tcgen05")
+    ap.add_argument("--no-e2e", action="store_true")
+    ap.add_argument("--no-cpu", action="store_true")
+    args = ap.parse_args()
+    if args.impl == "reference":
+        return run_reference_arm(args)
+    return run_gpu_arm(args)
+
+
+if __name__ == "__main__":
+    sys.exit(main())

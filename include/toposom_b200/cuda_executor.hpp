@@ -1,0 +1,186 @@
+// cuda_executor.hpp — B200 drop-in for the toposom Executor seam.
+//
+// The reference training loop train_with_executor<Executor>
+// (toposom/trainer.hpp:466-523) calls executor.run_iteration(...) exactly once
+// per epoch (:506-508) and applies the returned IterationAccumulators with
+// apply_update (:510).  CudaExecutor satisfies that concept (same signature as
+// SerialExecutor, trainer.hpp:440-460, and ThreadedExecutor,
+// parallel.hpp:99-140) and runs the whole data pass — BMU search,
+// accumulation, reduce, neighbourhood smoothing — on a B200 through the C-ABI
+// in tsom_b200.h.  A maintainer switches a run to the GPU with
+//
+//     #include <toposom_b200/cuda_executor.hpp>
+//     auto [model, log] = toposom_b200::train_cuda(config, data, sampler);
+//
+// exactly where they would call toposom::train / train_parallel.  Exceptions
+// keep the reference's types and message prefixes.
+#pragma once
+
+#include <cmath>
+#include <cstdint>
+#include <memory>
+#include <stdexcept>
+#include <string>
+#include <vector>
+
+#include "toposom/metrics.hpp"
+#include "toposom/trainer.hpp"
+#include "tsom_b200.h"
+
+namespace toposom_b200 {
+
+using toposom::DataMatrix;
+using toposom::DataSourceRef;
+using toposom::IterationAccumulators;
+
+/// Map a C-ABI status to the reference's exception types.
+inline void throw_status(int status, const char* msg) {
+    const std::string m = msg ? msg : "";
+    switch (status) {
+        case TSOM_OK: return;
+        case TSOM_ERR_INVALID: throw std::invalid_argument(m);
+        case TSOM_ERR_RANGE: throw std::out_of_range(m);
+        case TSOM_ERR_NUMERICAL: throw std::runtime_error(m);
+        default: throw std::runtime_error("toposom_b200: " + m);
+    }
+}
+
+struct Engine {
+    tsom_engine* h = nullptr;
+    Engine(int device, std::size_t nodes, std::size_t dims) {
+        const int st = tsom_create(device, static_cast<uint32_t>(nodes), static_cast<uint32_t>(dims), &h);
+        if (st) throw_status(st, "tsom_create failed (no sm_100 device?)");
+    }
+    ~Engine() { tsom_destroy(h); }
+    Engine(const Engine&) = delete;
+    Engine& operator=(const Engine&) = delete;
+    void check(int st) const { throw_status(st, tsom_last_error(h)); }
+};
+
+/// Whether run_iteration fills the per-row distance vector (the adaptive
+/// sampler needs it, trainer.hpp:511; full/random sampling ignores it).
+enum class Distances { always, never };
+
+struct CudaOptions {
+    int device = 0;
+    bool streamed = false;            // keep rows in host memory, stream every epoch
+    Distances distances = Distances::always;
+    int bmu_kernel = 0;               // 0 auto (tcgen05), 1 SIMT, 2 tcgen05
+};
+
+/// Convert the engine's float64 U/H into the reference's fixed-point
+/// accumulators (accum.hpp:45-53): value * 2^40 rounded to nearest.
+inline toposom::AccumInt to_fixed(double v) {
+    if (!std::isfinite(v))
+        throw std::runtime_error("numerical fault: accumulation term out of range (|term| >= 2^22)");
+    const double q = std::nearbyint(v * toposom::kAccumScale);
+    return static_cast<toposom::AccumInt>(q);
+}
+
+class CudaExecutor {
+public:
+    CudaExecutor(const DataSourceRef& data, std::size_t nodes, const CudaOptions& opts = {})
+        : opts_(opts), eng_(std::make_unique<Engine>(opts.device, nodes, data.cols())),
+          nodes_(nodes), dims_(data.cols()) {
+        if (opts.bmu_kernel) eng_->check(tsom_set_option(eng_->h, TSOM_OPT_BMU_KERNEL, opts.bmu_kernel));
+        if (data.in_memory()) {
+            rows_ = data.matrix();
+        } else {
+            // Shard-backed source: materialise once in host memory (the engine
+            // then streams or uploads it); the per-epoch rescans of
+            // DataSourceRef::fetch_rows (dataset.hpp:400-415) disappear.
+            owned_ = std::make_unique<DataMatrix>(0, data.cols());
+            data.for_each_row([&](std::size_t, const float* r) {
+                owned_->values.insert(owned_->values.end(), r, r + data.cols());
+                ++owned_->rows;
+            });
+            rows_ = owned_.get();
+        }
+        eng_->check(tsom_bind_host_data(eng_->h, rows_->values.data(), rows_->rows,
+                                        opts.streamed ? TSOM_BIND_STREAMED : TSOM_BIND_COPY));
+    }
+
+    /// Executor::run_iteration (trainer.hpp:446-453): one accumulation pass
+    /// plus the single reduce.  n_chunks is result-invariant by contract
+    /// (test_trainer.cpp:315-333) and therefore not used.
+    IterationAccumulators run_iteration(const std::vector<std::uint32_t>& selected,
+                                        const DataMatrix& weights,
+                                        const std::vector<double>& influence, double eta,
+                                        std::size_t /*n_chunks*/, std::vector<double>& distances) {
+        if (weights.rows != nodes_ || weights.cols != dims_)
+            throw std::invalid_argument("accumulate: accumulator shape mismatch");
+        if (influence.size() != nodes_ * nodes_)
+            throw std::invalid_argument("accumulate: influence shape mismatch");
+        eng_->check(tsom_set_codebook(eng_->h, weights.values.data()));
+        eng_->check(tsom_set_influence(eng_->h, influence.data(), -1));
+        u_.resize(nodes_ * dims_);
+        h_.resize(nodes_);
+        distances.clear();
+        double* dist_out = nullptr;
+        if (opts_.distances == Distances::always) {
+            distances.resize(selected.size());
+            dist_out = distances.data();
+        }
+        static const std::uint32_t kNone = 0;  // non-null + n_sel 0 = empty selection
+        const std::uint32_t* sel = selected.empty() ? &kNone : selected.data();
+        eng_->check(tsom_epoch(eng_->h, sel, selected.size(), eta, u_.data(), h_.data(), dist_out));
+        IterationAccumulators acc(nodes_, dims_);
+        for (std::size_t i = 0; i < u_.size(); ++i) acc.u[i] = to_fixed(u_[i]);
+        for (std::size_t j = 0; j < nodes_; ++j) acc.h[j] = to_fixed(h_[j]);
+        return acc;
+    }
+
+    std::size_t workers() const { return 1; }
+    double barrier_wait_s() const { return 0.0; }
+    tsom_engine* engine() const { return eng_->h; }
+
+private:
+    CudaOptions opts_;
+    std::unique_ptr<Engine> eng_;
+    std::size_t nodes_, dims_;
+    const DataMatrix* rows_ = nullptr;
+    std::unique_ptr<DataMatrix> owned_;
+    std::vector<double> u_, h_;
+};
+
+/// GPU analogue of toposom::train / train_parallel (trainer.hpp:526-530,
+/// parallel.hpp:145-152).  Distances are only produced when the sampler needs
+/// them (adaptive), unless the caller forces them.
+inline std::pair<toposom::SomModel, toposom::RunLog> train_cuda(
+    const toposom::SomConfig& config, const DataSourceRef& data, toposom::Sampler& sampler,
+    CudaOptions opts = {}, const toposom::TrainOptions& options = {}) {
+    if (sampler.kind() != toposom::SamplingKind::adaptive) opts.distances = Distances::never;
+    if (data.rows() < 1) throw std::invalid_argument("train: empty training data");
+    CudaExecutor executor(data, config.nodes(), opts);
+    return toposom::train_with_executor(config, data, sampler, executor, options);
+}
+
+/// find_bmus (trainer.hpp:282-308) on the GPU; bit-identical BMU indices.
+inline void find_bmus_cuda(const DataMatrix& chunk, const DataMatrix& weights,
+                           std::vector<std::uint32_t>& bmus, std::vector<double>& distances,
+                           int device = 0) {
+    if (chunk.cols != weights.cols) throw std::invalid_argument("find_bmus: dimension mismatch");
+    bmus.resize(chunk.rows);
+    distances.resize(chunk.rows);
+    if (chunk.rows == 0) return;
+    Engine eng(device, weights.rows, weights.cols);
+    eng.check(tsom_set_codebook(eng.h, weights.values.data()));
+    eng.check(tsom_bmu(eng.h, chunk.values.data(), chunk.rows, bmus.data(), distances.data()));
+}
+
+/// quantization_error (metrics.hpp:28-30) on the GPU.
+inline double quantization_error_cuda(const toposom::SomModel& model, const DataMatrix& data,
+                                      int device = 0) {
+    if (data.cols != model.weights.cols)
+        throw std::invalid_argument("mean_bmu_distance: dimension mismatch");
+    if (data.rows == 0) throw std::invalid_argument("mean_bmu_distance: empty data");
+    Engine eng(device, model.weights.rows, model.weights.cols);
+    eng.check(tsom_set_codebook(eng.h, model.weights.values.data()));
+    eng.check(tsom_bind_host_data(eng.h, data.values.data(), data.rows, TSOM_BIND_COPY));
+    double sum = 0.0;
+    uint64_t count = 0;
+    eng.check(tsom_qe(eng.h, nullptr, 0, &sum, &count));
+    return sum / static_cast<double>(count);
+}
+
+}  // namespace toposom_b200

@@ -1,0 +1,162 @@
+/*
+ * tsom_b200.h — C-ABI of the B200-native batch-SOM epoch engine.
+ *
+ * This is the drop-in boundary for the hot path of the toposom reference
+ * (paths below are relative to /root/reference/proj/include/toposom).  The
+ * reference's only seam is the Executor concept consumed by
+ * train_with_executor<Executor> (trainer.hpp:466-470, called at :506-508):
+ *
+ *     IterationAccumulators run_iteration(selected, weights, influence, eta,
+ *                                         n_chunks, distances);
+ *
+ * include/toposom_b200/cuda_executor.hpp implements that concept on top of
+ * the functions declared here, so the reference training loop runs unchanged
+ * with every per-epoch data pass on the GPU.  The free functions find_bmus /
+ * map_samples / mean_bmu_distance / quantization_error map onto tsom_bmu and
+ * tsom_qe.
+ *
+ * Conventions:
+ *   - every call returns an int status (TSOM_OK .. TSOM_ERR_TIMEOUT);
+ *     tsom_last_error() holds the message, whose prefix matches the
+ *     reference's exception text so the C++ adapter can rethrow the same type;
+ *   - plain pointers and sizes only; host buffers are borrowed for the call;
+ *   - the engine owns all device memory, streams and the NCCL communicator;
+ *   - an engine is not re-entrant (one training run, one thread).
+ *
+ * Layouts: samples and codebooks are row-major float32 (DataMatrix,
+ * matrix.hpp:12-29); influence is P x P float64 row-major, row b = influence
+ * of BMU b on every node (trainer.hpp:326); accumulators U (P x d) and H (P)
+ * are float64 values of the IterationAccumulators (accum.hpp:45-69).
+ */
+#ifndef TSOM_B200_H
+#define TSOM_B200_H
+
+#include <stddef.h>
+#include <stdint.h>
+
+#ifdef __cplusplus
+extern "C" {
+#endif
+
+/* Status codes. */
+#define TSOM_OK 0
+#define TSOM_ERR_INVALID 1   /* std::invalid_argument */
+#define TSOM_ERR_NUMERICAL 2 /* std::runtime_error "numerical fault: ..." */
+#define TSOM_ERR_RANGE 3     /* std::out_of_range */
+#define TSOM_ERR_CUDA 4
+#define TSOM_ERR_NCCL 5
+#define TSOM_ERR_TIMEOUT 6
+
+/* tsom_bind_host_data flags */
+#define TSOM_BIND_COPY 0u      /* copy rows into HBM once (resident mode)      */
+#define TSOM_BIND_STREAMED 1u  /* keep rows in (pinned) host memory; every epoch
+                                  streams them through double-buffered chunks */
+
+/* tsom_set_option keys */
+#define TSOM_OPT_BMU_KERNEL 1      /* 0 = auto (tcgen05 when supported), 1 = SIMT, 2 = tcgen05 */
+#define TSOM_OPT_TIE_TAU 2         /* value*2^-30: relative tie window for the exact re-check */
+#define TSOM_OPT_STREAM_CHUNK 3    /* rows per streamed chunk */
+#define TSOM_OPT_DETERMINISTIC 4   /* reserved */
+
+typedef struct tsom_engine tsom_engine;
+
+/* Engine lifetime ---------------------------------------------------------- */
+
+/* Create an engine for a P-node, d-dimensional codebook on CUDA `device`. */
+int tsom_create(int device, uint32_t nodes, uint32_t dims, tsom_engine** out);
+int tsom_destroy(tsom_engine* eng);
+const char* tsom_last_error(const tsom_engine* eng);
+const char* tsom_version(void);
+int tsom_set_option(tsom_engine* eng, int key, int64_t value);
+
+/* Data binding (DataSourceRef, dataset.hpp:362-421) ------------------------ */
+
+/* Bind n_rows x dims row-major float32 host rows.  TSOM_BIND_COPY uploads once
+ * and keeps the rows resident in HBM; TSOM_BIND_STREAMED re-streams them from
+ * host memory every epoch (the caller keeps `rows` alive until rebind/destroy).
+ * Replaces the executor's DataSourceRef (trainer.hpp:442, parallel.hpp:101). */
+int tsom_bind_host_data(tsom_engine* eng, const float* rows, uint64_t n_rows, uint32_t flags);
+/* Bind rows that already live in this device's memory (borrowed). */
+int tsom_bind_device_data(tsom_engine* eng, const float* d_rows, uint64_t n_rows);
+/* Fill the bound dataset with the SURVEY.md §8(d) Gaussian mixture generated
+ * on the device (centres from the reference Rng on the host, noise from a
+ * counter-based generator).  Used for throughput runs at N >= 1e7. */
+int tsom_bind_synthetic_gmm(tsom_engine* eng, uint64_t n_rows, uint64_t seed, uint32_t n_comp,
+                            uint64_t row_offset);
+uint64_t tsom_rows(const tsom_engine* eng);
+
+/* Per-epoch state ---------------------------------------------------------- */
+
+/* Codebook P x d (SomModel::weights, trainer.hpp:106). */
+int tsom_set_codebook(tsom_engine* eng, const float* weights);
+int tsom_get_codebook(tsom_engine* eng, float* weights);
+/* Influence P x P float64 (cached_influence, topology.hpp:406-418).  key is the
+ * caller's cache key (e.g. influence_cache_key(sigma) mixed with the topology
+ * refresh count); an unchanged non-negative key skips the upload. */
+int tsom_set_influence(tsom_engine* eng, const double* influence, int64_t key);
+
+/*
+ * One iteration's accumulation pass: Executor::run_iteration
+ * (trainer.hpp:446-453, parallel.hpp:107-130) plus the single reduce.
+ *   selected : sorted distinct row ids, or NULL for all bound rows
+ *   u_out    : P x d float64 U_j = eta * sum_i h[b_i][j] (x_i - w_j)  (may be NULL)
+ *   h_out    : P float64     H_j = sum_i h[b_i][j]                    (may be NULL)
+ *   dist_out : one BMU distance per selected row, selection order (may be NULL)
+ * With a communicator attached (tsom_comm_init) each rank passes its own
+ * rows/selection and receives the globally reduced U/H.
+ */
+int tsom_epoch(tsom_engine* eng, const uint32_t* selected, uint64_t n_sel, double eta,
+               double* u_out, double* h_out, double* dist_out);
+
+/* BMU search on caller rows (find_bmus trainer.hpp:282-308 / map_samples
+ * :534-541).  bmu: n uint32; dist: n float64 or NULL. */
+int tsom_bmu(tsom_engine* eng, const float* rows, uint64_t n, uint32_t* bmu, double* dist);
+/* BMU search over the bound rows (or a selection of them). */
+int tsom_bmu_bound(tsom_engine* eng, const uint32_t* selected, uint64_t n_sel, uint32_t* bmu,
+                   double* dist);
+/* Quantisation error over bound rows (mean_bmu_distance trainer.hpp:377-398,
+ * quantization_error metrics.hpp:28-30): returns the distance sum and count. */
+int tsom_qe(tsom_engine* eng, const uint32_t* selected, uint64_t n_sel, double* dist_sum,
+            uint64_t* count);
+
+/* Device-resident training (no per-epoch host traffic) -------------------- */
+
+/* Static neighbourhood distances P x P (lattice_dist topology.hpp:137-149, or
+ * hop counts topology.hpp:292-325 widened to float64); the influence for each
+ * sigma is then built on the device exactly as influence_matrix (:342-364). */
+int tsom_set_topology_distance(tsom_engine* eng, const double* dist);
+/* One full epoch on the device: influence(sigma) -> BMU -> accumulate ->
+ * (allreduce) -> smoothing -> apply_update (trainer.hpp:341-369) with the
+ * reference's H floor, momentum and non-finite guards.  flags bit0 = momentum
+ * on.  Weights stay on the device (read with tsom_get_codebook). */
+int tsom_train_epoch(tsom_engine* eng, double eta, double sigma, double momentum,
+                     uint32_t flags);
+/* Number of rows re-checked in exact FP64 by the last BMU pass (tie window). */
+uint64_t tsom_last_recheck_count(const tsom_engine* eng);
+
+/* Multi-GPU (one process per GPU) ---------------------------------------- */
+
+/* 128-byte ncclUniqueId produced by rank 0 and broadcast by the caller. */
+int tsom_comm_unique_id(tsom_engine* eng, uint8_t id_out[128]);
+/* Attach an NCCL communicator; every epoch then ends with exactly one
+ * ncclAllReduce(sum, float64) of the packed [S | c | sum dist | count] buffer
+ * (parallel.hpp:90-95 reduce). */
+int tsom_comm_init(tsom_engine* eng, const uint8_t id[128], int rank, int world);
+
+/* Timing of the last epoch (device events), milliseconds. */
+int tsom_last_timing(const tsom_engine* eng, float* bmu_ms, float* accum_ms, float* smooth_ms,
+                     float* total_ms);
+/* Detail of the last epoch (ms): [0] BMU kernel (K1) alone, [1] BMU phase incl.
+ * merge + exact re-check, [2] accumulation + reduce (+ allreduce), [3] smoothing,
+ * [4] device update (tsom_train_epoch), [5] total. */
+int tsom_last_timing_detail(const tsom_engine* eng, float out[8]);
+/* Number of CUDA kernels this library has launched in this process. */
+uint64_t tsom_kernel_launches(void);
+/* The CUDA stream all engine work is issued on (cudaStream_t as void*). */
+void* tsom_stream(tsom_engine* eng);
+
+#ifdef __cplusplus
+}
+#endif
+
+#endif /* TSOM_B200_H */

@@ -1,0 +1,167 @@
+"""Reference-shaped Python API over the B200 engine.
+
+Mirrors the toposom free functions and the Executor seam (paths relative to
+/root/reference/proj/include/toposom):
+
+* :func:`find_bmus`            — trainer.hpp:282-308
+* :func:`map_samples`          — trainer.hpp:534-541
+* :func:`mean_bmu_distance`    — trainer.hpp:377-398 (= quantization_error, metrics.hpp:28-30)
+* :class:`CudaExecutor`        — the Executor concept (trainer.hpp:440-460, parallel.hpp:99-140)
+* :func:`train_resident`       — train_with_executor (trainer.hpp:466-523) for lattice
+                                 topologies with every per-epoch step on the device
+
+Errors follow the reference's exception types: ``ValueError`` for
+std::invalid_argument, ``IndexError`` for std::out_of_range and
+:class:`NumericalFault` (a RuntimeError) for "numerical fault: ...".
+"""
+from __future__ import annotations
+
+import math
+from dataclasses import dataclass
+
+import numpy as np
+
+from ._lib import Engine, InvalidArgument, NumericalFault, OutOfRange  # noqa: F401
+from .hostref import (Rng, init_sample_draw, lattice_dist, resolved_sigma0,  # noqa: F401
+                      schedule_value)
+
+
+def _as_rows(a) -> np.ndarray:
+    a = np.ascontiguousarray(a, np.float32)
+    if a.ndim != 2:
+        raise InvalidArgument(1, "DataMatrix: expected a 2-D rows x cols array")
+    return a
+
+
+def find_bmus(chunk, weights, device: int = 0):
+    """BMU index (ties → lowest node) and Euclidean distance per row."""
+    chunk, weights = _as_rows(chunk), _as_rows(weights)
+    if chunk.shape[1] != weights.shape[1]:
+        raise InvalidArgument(1, "find_bmus: dimension mismatch")
+    with Engine(weights.shape[0], weights.shape[1], device) as eng:
+        eng.set_codebook(weights)
+        return eng.bmu(chunk, want_dist=True)
+
+
+def map_samples(weights, data, device: int = 0):
+    data = _as_rows(data)
+    if data.shape[0] == 0:
+        return np.empty(0, np.uint32), np.empty(0)
+    return find_bmus(data, weights, device)
+
+
+def mean_bmu_distance(data, weights, device: int = 0) -> float:
+    data, weights = _as_rows(data), _as_rows(weights)
+    if data.shape[1] != weights.shape[1]:
+        raise InvalidArgument(1, "mean_bmu_distance: dimension mismatch")
+    if data.shape[0] == 0:
+        raise InvalidArgument(1, "mean_bmu_distance: empty data")
+    with Engine(weights.shape[0], weights.shape[1], device) as eng:
+        eng.set_codebook(weights)
+        eng.bind(data)
+        s, c = eng.qe()
+    return s / c
+
+
+quantization_error = mean_bmu_distance
+
+
+@dataclass
+class Accumulators:
+    """Float64 view of ``IterationAccumulators`` (accum.hpp:45-69)."""
+
+    u: np.ndarray  # P x d
+    h: np.ndarray  # P
+
+    def u_value(self, node: int, k: int) -> float:
+        return float(self.u[node, k])
+
+    def h_value(self, node: int) -> float:
+        return float(self.h[node])
+
+
+class CudaExecutor:
+    """Drop-in for SerialExecutor / ThreadedExecutor (trainer.hpp:440-460).
+
+    ``run_iteration`` has the reference call shape; ``n_chunks`` is accepted and
+    ignored because the result is chunk-invariant by contract (test_trainer.cpp:315-333).
+    """
+
+    def __init__(self, data, nodes: int, device: int = 0, streamed: bool = False):
+        data = _as_rows(data)
+        self.engine = Engine(nodes, data.shape[1], device)
+        self.engine.bind(data, streamed=streamed)
+        self._infl_id = None
+
+    def run_iteration(self, selected, weights, influence, eta, n_chunks=1, distances=None):
+        eng = self.engine
+        eng.set_codebook(weights)
+        key = id(influence)
+        if key != self._infl_id:
+            eng.set_influence(influence, -1)
+            self._infl_id = key
+        want = distances is not None
+        sel = None if selected is None else np.asarray(selected, np.uint32)
+        u, h, d = eng.epoch(eta, sel, want_dist=want)
+        if want:
+            distances.clear()
+            distances.extend(d.tolist())
+        return Accumulators(u, h)
+
+    def workers(self) -> int:
+        return 1
+
+    def barrier_wait_s(self) -> float:
+        return 0.0
+
+
+@dataclass
+class ResidentConfig:
+    """Subset of SomConfig (trainer.hpp:58-99) the device-resident loop supports."""
+
+    topology: str = "hex"       # "rect" | "hex"
+    grid_w: int = 32
+    grid_h: int = 32
+    n_iters: int = 10
+    eta0: float = 0.5
+    lr_decay: str = "linear"
+    sigma0: float = 0.0
+    radius_decay: str = "linear"
+    sigma_min: float = 0.3
+    use_momentum: bool = False
+    momentum: float = 0.5
+    seed: int = 0
+
+    @property
+    def nodes(self) -> int:
+        return self.grid_w * self.grid_h
+
+
+def train_resident(cfg: ResidentConfig, engine: Engine, init_weights=None, log_qe=False):
+    """train_with_executor (trainer.hpp:466-523) with full sampling on a lattice:
+    every epoch (influence, BMU, accumulate, allreduce, smoothing, update) runs on
+    the device; the host only evaluates the two schedules.  Returns the log."""
+    if cfg.topology not in ("rect", "rectangular", "hex", "hexagonal"):
+        raise InvalidArgument(1, "train_resident: lattice topologies only")
+    if init_weights is None:
+        raise InvalidArgument(1, "train_resident: pass init weights (init_sample_draw)")
+    engine.set_codebook(init_weights)
+    engine.set_topology_distance(lattice_dist(cfg.topology, cfg.grid_w, cfg.grid_h))
+    sigma0 = resolved_sigma0(cfg.topology, cfg.grid_w, cfg.grid_h, cfg.sigma0)
+    log = []
+    for t in range(cfg.n_iters):
+        eta = schedule_value(cfg.eta0, cfg.lr_decay, t, cfg.n_iters, 1e-4)
+        sigma = schedule_value(sigma0, cfg.radius_decay, t, cfg.n_iters, cfg.sigma_min)
+        engine.train_epoch(eta, sigma, cfg.momentum, cfg.use_momentum)
+        entry = {"iter": t, "eta": eta, "sigma": sigma}
+        if log_qe:
+            s, c = engine.qe()
+            entry["qe_train"] = s / c
+        log.append(entry)
+    return log
+
+
+__all__ = ["find_bmus", "map_samples", "mean_bmu_distance", "quantization_error",
+           "CudaExecutor", "Accumulators", "ResidentConfig", "train_resident", "Engine",
+           "NumericalFault", "InvalidArgument", "OutOfRange", "Rng", "init_sample_draw",
+           "schedule_value", "lattice_dist", "math"]

@@ -1,0 +1,796 @@
+// capi.cu — the tsom_* C-ABI (include/tsom_b200.h) over the B200 kernels.
+//
+// One engine = one GPU = one training run.  Every call is synchronous from the
+// caller's point of view (it returns after its results are in the caller's
+// buffers), all device work is issued on the engine stream.  There is no CPU
+// fallback: if a kernel cannot run, the call fails with TSOM_ERR_CUDA.
+#include <cuda_runtime.h>
+#include <dlfcn.h>
+#include <nccl.h>
+
+#include <algorithm>
+#include <climits>
+#include <cmath>
+#include <cstdio>
+#include <cstring>
+#include <random>
+#include <string>
+#include <vector>
+
+#include "engine.h"
+
+using tsom::DevBuf;
+using tsom::Engine;
+
+struct tsom_engine : public Engine {};
+
+namespace tsom {
+
+std::atomic<uint64_t> g_launches{0};
+
+cudaError_t DevBuf::ensure(size_t need) {
+    if (need <= bytes && p) return cudaSuccess;
+    release();
+    if (need == 0) return cudaSuccess;
+    cudaError_t e = cudaMalloc(&p, need);
+    if (e != cudaSuccess) {
+        p = nullptr;
+        bytes = 0;
+        return e;
+    }
+    bytes = need;
+    owned = true;
+    return cudaSuccess;
+}
+
+void DevBuf::release() {
+    if (p && owned) cudaFree(p);
+    p = nullptr;
+    bytes = 0;
+    owned = true;
+}
+
+}  // namespace tsom
+
+namespace {
+
+const char* kVersion = "toposom-b200 0.1 (sm_100a; tcgen05 3xTF32 BMU, smem-privatised accumulation)";
+
+struct Fail {
+    int code;
+};
+
+#define CU(expr)                                                                          \
+    do {                                                                                  \
+        cudaError_t _e = (expr);                                                          \
+        if (_e != cudaSuccess) {                                                          \
+            eng->last_error = std::string("cuda: ") + cudaGetErrorString(_e) + " at " #expr; \
+            throw Fail{TSOM_ERR_CUDA};                                                    \
+        }                                                                                 \
+    } while (0)
+
+#define REQUIRE(cond, code, msg)        \
+    do {                                \
+        if (!(cond)) {                  \
+            eng->last_error = (msg);    \
+            throw Fail{code};           \
+        }                               \
+    } while (0)
+
+template <typename F>
+int guarded(Engine* eng, F&& f) {
+    if (!eng) return TSOM_ERR_INVALID;
+    try {
+        f();
+        return TSOM_OK;
+    } catch (const Fail& fl) {
+        return fl.code;
+    } catch (const std::exception& ex) {
+        eng->last_error = ex.what();
+        return TSOM_ERR_INVALID;
+    }
+}
+
+// ---- NCCL, loaded lazily (single-GPU use never needs it) -------------------
+struct NcclApi {
+    void* h = nullptr;
+    ncclResult_t (*getUniqueId)(ncclUniqueId*) = nullptr;
+    ncclResult_t (*commInitRank)(ncclComm_t*, int, ncclUniqueId, int) = nullptr;
+    ncclResult_t (*allReduce)(const void*, void*, size_t, ncclDataType_t, ncclRedOp_t, ncclComm_t,
+                              cudaStream_t) = nullptr;
+    ncclResult_t (*commDestroy)(ncclComm_t) = nullptr;
+    const char* (*errStr)(ncclResult_t) = nullptr;
+    bool load(std::string& err) {
+        if (h) return true;
+        const char* names[] = {"libnccl.so.2", "libnccl.so"};
+        for (const char* n : names)
+            if ((h = dlopen(n, RTLD_NOW | RTLD_GLOBAL))) break;
+        if (!h) {
+            err = std::string("nccl: cannot load libnccl.so.2: ") + dlerror();
+            return false;
+        }
+        getUniqueId = (decltype(getUniqueId))dlsym(h, "ncclGetUniqueId");
+        commInitRank = (decltype(commInitRank))dlsym(h, "ncclCommInitRank");
+        allReduce = (decltype(allReduce))dlsym(h, "ncclAllReduce");
+        commDestroy = (decltype(commDestroy))dlsym(h, "ncclCommDestroy");
+        errStr = (decltype(errStr))dlsym(h, "ncclGetErrorString");
+        if (!getUniqueId || !commInitRank || !allReduce || !commDestroy) {
+            err = "nccl: missing symbols";
+            return false;
+        }
+        return true;
+    }
+};
+NcclApi g_nccl;
+
+size_t slot_len(const Engine* e) { return (size_t)e->P * e->D + e->P + 2; }
+
+uint32_t ppad(const Engine* e) { return (e->P + 63) / 64 * 64; }
+
+bool use_tc(const Engine* e) {
+    if (e->bmu_kernel == 1) return false;
+    return tsom::tc_supported(e->P, e->D);
+}
+
+void ensure_rows(Engine* eng, uint64_t n) {
+    CU(eng->bmu.ensure(std::max<uint64_t>(n, 1) * sizeof(uint32_t)));
+    CU(eng->dist.ensure(std::max<uint64_t>(n, 1) * sizeof(double)));
+    CU(eng->flags.ensure((std::max<uint64_t>(n, 1) + 1) * sizeof(uint32_t)));
+}
+
+void prep_codebook(Engine* eng) {
+    REQUIRE(eng->codebook_set, TSOM_ERR_INVALID, "engine: codebook not set (tsom_set_codebook)");
+    if (eng->codebook_prepped) return;
+    const bool tc = use_tc(eng);
+    const uint32_t groups = (eng->P + tsom::kTcGroupN - 1) / tsom::kTcGroupN;
+    if (tc)
+        CU(eng->wsplit.ensure((size_t)groups * 2 * tsom::kTcGroupN * tsom::kTcKPad * sizeof(float)));
+    tsom::launch_prep_codebook(eng->w.as<float>(), eng->P, eng->D, eng->w2.as<double>(),
+                               eng->w2max.as<float>(), eng->wt.as<float>(), ppad(eng),
+                               tc ? eng->wsplit.as<float>() : nullptr, eng->stream);
+    CU(cudaGetLastError());
+    eng->codebook_prepped = true;
+}
+
+// K1 + exact re-check over rows `x` (selection `sel` of length n, or first n rows).
+// `tiles` = pre-split tcgen05 operand for exactly these n rows (or nullptr to build).
+void run_bmu(Engine* eng, const float* x, const uint32_t* sel, uint64_t n, const float* x2max,
+             const float* tiles) {
+    CU(cudaMemsetAsync(eng->flags.p, 0, sizeof(uint32_t), eng->stream));
+    if (n == 0) return;
+    if (use_tc(eng)) {
+        const uint32_t groups = (eng->P + tsom::kTcGroupN - 1) / tsom::kTcGroupN;
+        if (!tiles) {
+            const uint64_t ntiles = (n + tsom::kTcTileM - 1) / tsom::kTcTileM;
+            CU(eng->gsplit.ensure(ntiles * 2 * tsom::kTcTileM * tsom::kTcKPad * sizeof(float)));
+            tsom::launch_split_rows(x, sel, n, eng->D, eng->gsplit.as<float>(), eng->stream);
+            tiles = eng->gsplit.as<float>();
+        }
+        CU(eng->part.ensure((size_t)groups * 3 * n * sizeof(float)));
+        CU(cudaEventRecord(eng->ev[8], eng->stream));
+        CU(tsom::launch_bmu_tc(tiles, n, eng->P, eng->wsplit.as<float>(), eng->part.as<float>(),
+                               eng->sm_count, eng->stream));
+        CU(cudaEventRecord(eng->ev[9], eng->stream));
+        eng->k1_timed = true;
+        tsom::launch_merge_partials(eng->part.as<float>(), n, groups, x2max, eng->w2max.as<float>(),
+                                    (float)eng->tau_tc, eng->bmu.as<uint32_t>(),
+                                    eng->flags.as<uint32_t>(), eng->stream);
+    } else {
+        CU(cudaEventRecord(eng->ev[8], eng->stream));
+        tsom::launch_bmu_simt(x, sel, n, eng->D, eng->wt.as<float>(), eng->P, ppad(eng), x2max,
+                              eng->w2max.as<float>(), (float)eng->tau_simt, eng->bmu.as<uint32_t>(),
+                              eng->flags.as<uint32_t>(), eng->sm_count, eng->stream);
+        CU(cudaEventRecord(eng->ev[9], eng->stream));
+        eng->k1_timed = true;
+    }
+    CU(cudaGetLastError());
+    tsom::launch_rescan(x, sel, eng->w.as<float>(), eng->P, eng->D, eng->flags.as<uint32_t>(), n,
+                        eng->bmu.as<uint32_t>(), eng->stream);
+    CU(cudaGetLastError());
+}
+
+// Validate a selection against the bound rows (fetch_rows, dataset.hpp:393-416)
+// and reduce the identity selection to "all rows".
+const uint32_t* normalise_selection(Engine* eng, const uint32_t* sel, uint64_t n_sel) {
+    if (!sel) {
+        REQUIRE(n_sel == 0 || n_sel == eng->n_rows, TSOM_ERR_INVALID,
+                "epoch: NULL selection means all rows (n_sel must be 0 or tsom_rows())");
+        return nullptr;
+    }
+    if (n_sel == 0) return sel;
+    // contract: sorted, distinct (Sampler::select, sampling.hpp:42-43) ⇒ the
+    // last id is the largest, and size N spanning [0, N-1] is the identity
+    REQUIRE(sel[n_sel - 1] < eng->n_rows && sel[0] <= sel[n_sel - 1], TSOM_ERR_RANGE,
+            "fetch_rows: row index beyond data size");
+    if (n_sel == eng->n_rows && sel[0] == 0 && sel[n_sel - 1] == eng->n_rows - 1) return nullptr;
+    return sel;
+}
+
+// Accumulate the bound rows (resident or streamed) for one epoch into slots,
+// then reduce (+allreduce) into sums.  dist_dev: per-position distances or null.
+void accumulate_epoch(Engine* eng, const uint32_t* sel_host, uint64_t n_sel, bool want_dist,
+                      bool accumulate) {
+    const int nslots = tsom::accumulate_slots(eng->P, eng->D, eng->smem_optin, eng->sm_count);
+    CU(eng->slots.ensure((size_t)nslots * slot_len(eng) * sizeof(double)));
+    CU(eng->sums.ensure(slot_len(eng) * sizeof(double)));
+    const uint32_t* sel = normalise_selection(eng, sel_host, n_sel);
+    const uint64_t n = sel ? n_sel : eng->n_rows;
+    ensure_rows(eng, n);
+    if (sel) {
+        CU(eng->sel.ensure(std::max<uint64_t>(n, 1) * sizeof(uint32_t)));
+        CU(cudaMemcpyAsync(eng->sel.p, sel, n * sizeof(uint32_t), cudaMemcpyHostToDevice,
+                           eng->stream));
+    }
+    const uint32_t* dsel = sel ? eng->sel.as<uint32_t>() : nullptr;
+    prep_codebook(eng);
+    eng->last_recheck = 0;
+    eng->recheck_from_chunks = false;
+    eng->k1_timed = false;
+    eng->update_timed = false;
+    CU(cudaEventRecord(eng->ev[0], eng->stream));
+    if (!eng->streamed) {
+        const float* tiles = nullptr;
+        if (use_tc(eng) && !sel) {
+            if (!eng->xsplit_valid) {
+                const uint64_t ntiles = (eng->n_rows + tsom::kTcTileM - 1) / tsom::kTcTileM;
+                CU(eng->xsplit.ensure(ntiles * 2 * tsom::kTcTileM * tsom::kTcKPad * sizeof(float)));
+                tsom::launch_split_rows(eng->x.as<float>(), nullptr, eng->n_rows, eng->D,
+                                        eng->xsplit.as<float>(), eng->stream);
+                eng->xsplit_valid = true;
+            }
+            tiles = eng->xsplit.as<float>();
+        }
+        run_bmu(eng, eng->x.as<float>(), dsel, n, eng->x2max.as<float>(), tiles);
+        CU(cudaEventRecord(eng->ev[1], eng->stream));
+        tsom::launch_accumulate(eng->x.as<float>(), dsel, n, eng->D, eng->w.as<float>(), eng->P,
+                                eng->bmu.as<uint32_t>(),
+                                want_dist ? eng->dist.as<double>() : nullptr,
+                                eng->slots.as<double>(), nslots, accumulate, true,
+                                eng->smem_optin, eng->stream);
+        CU(cudaGetLastError());
+        eng->chunk_counts.assign(1, 0u);
+        eng->recheck_from_chunks = true;
+        CU(cudaMemcpyAsync(&eng->chunk_counts[0], eng->flags.p, sizeof(uint32_t),
+                           cudaMemcpyDeviceToHost, eng->stream));
+    } else {
+        // Streamed: rows live in host memory; chunks of stream_chunk_rows rows
+        // are copied on copy_stream into two device stages, compute on stream.
+        const uint64_t C = eng->stream_chunk_rows;
+        CU(eng->stage[0].ensure(C * eng->D * sizeof(float)));
+        CU(eng->stage[1].ensure(C * eng->D * sizeof(float)));
+        CU(eng->x2max.ensure(2 * sizeof(float)));
+        uint64_t pos0 = 0;  // selection cursor
+        bool first = true;
+        const uint64_t nchunks = (eng->n_rows + C - 1) / C;
+        eng->chunk_counts.assign(nchunks, 0u);
+        // events: ev[2+s] = stage s filled, ev[4+s] = stage s consumed.  No host
+        // sync inside the loop: the copy stream runs ahead into the free stage
+        // while the compute stream works on the other one.
+        uint64_t issued = 0;
+        for (uint64_t c = 0; c < nchunks; ++c) {
+            const uint64_t r0 = c * C, r1 = std::min(eng->n_rows, r0 + C);
+            uint64_t p0 = pos0, p1 = pos0;
+            if (sel) {
+                p1 = (uint64_t)(std::lower_bound(sel + p0, sel + n, (uint32_t)r1) - sel);
+                if (p1 == p0) continue;  // nothing selected in this chunk
+            }
+            const int s = (int)(issued & 1);
+            if (issued >= 2) CU(cudaStreamWaitEvent(eng->copy_stream, eng->ev[4 + s], 0));
+            CU(cudaMemcpyAsync(eng->stage[s].p, eng->host_rows + r0 * eng->D,
+                               (r1 - r0) * eng->D * sizeof(float), cudaMemcpyHostToDevice,
+                               eng->copy_stream));
+            CU(cudaEventRecord(eng->ev[2 + s], eng->copy_stream));
+            CU(cudaStreamWaitEvent(eng->stream, eng->ev[2 + s], 0));
+            ++issued;
+            const float* xs = eng->stage[s].as<float>();
+            float* xmax = eng->x2max.as<float>() + 1;
+            tsom::launch_row_norm_max(xs, r1 - r0, eng->D, xmax, eng->stream);
+            tsom::launch_fold_max(eng->x2max.as<float>(), eng->stream);
+            // selected rows of this chunk are addressed as (row - r0): shift the base
+            const float* xbase = xs - (ptrdiff_t)(r0 * eng->D);
+            const uint64_t cn = sel ? (p1 - p0) : (r1 - r0);
+            const uint32_t* csel = sel ? dsel + p0 : nullptr;
+            const uint64_t out0 = sel ? p0 : r0;
+            run_bmu(eng, sel ? xbase : xs, csel, cn, xmax, nullptr);
+            CU(cudaMemcpyAsync(&eng->chunk_counts[c], eng->flags.p, sizeof(uint32_t),
+                               cudaMemcpyDeviceToHost, eng->stream));
+            tsom::launch_accumulate(sel ? xbase : xs, csel, cn, eng->D, eng->w.as<float>(), eng->P,
+                                    eng->bmu.as<uint32_t>(),
+                                    want_dist ? eng->dist.as<double>() + out0 : nullptr,
+                                    eng->slots.as<double>(), nslots, accumulate, first,
+                                    eng->smem_optin, eng->stream);
+            CU(cudaGetLastError());
+            CU(cudaEventRecord(eng->ev[4 + s], eng->stream));
+            first = false;
+            pos0 = p1;
+        }
+        if (first) CU(cudaMemsetAsync(eng->slots.p, 0, (size_t)nslots * slot_len(eng) * sizeof(double), eng->stream));
+        eng->recheck_from_chunks = true;
+        CU(cudaEventRecord(eng->ev[1], eng->stream));
+    }
+    if (n == 0 && !eng->streamed)
+        CU(cudaMemsetAsync(eng->slots.p, 0, (size_t)nslots * slot_len(eng) * sizeof(double),
+                           eng->stream));
+    tsom::launch_reduce_slots(eng->slots.as<double>(), nslots, slot_len(eng),
+                              eng->sums.as<double>(), eng->stream);
+    CU(cudaGetLastError());
+    if (eng->nccl_comm) {
+        ncclResult_t r = g_nccl.allReduce(eng->sums.p, eng->sums.p, slot_len(eng), ncclFloat64, ncclSum,
+                                          (ncclComm_t)eng->nccl_comm, eng->stream);
+        REQUIRE(r == ncclSuccess, TSOM_ERR_NCCL,
+                std::string("nccl: allreduce failed: ") + (g_nccl.errStr ? g_nccl.errStr(r) : "?"));
+    }
+    CU(cudaEventRecord(eng->ev[2 + 4], eng->stream));
+}
+
+// Guard of quantize_term (accum.hpp:34-38): every term eta*h*(x - w) must stay
+// below 2^22.  Conservative bound |eta*h*(x - w)| <= eta*max|h|*(max||x|| + max||w||),
+// evaluated after the pass (streamed mode learns max||x|| while streaming).
+void check_term_guard(Engine* eng, double eta) {
+    float hx[2] = {0, 0};
+    CU(cudaMemcpy(&hx[0], eng->x2max.p, sizeof(float), cudaMemcpyDeviceToHost));
+    CU(cudaMemcpy(&hx[1], eng->w2max.p, sizeof(float), cudaMemcpyDeviceToHost));
+    const double bound =
+        std::fabs(eta) * eng->max_h * (std::sqrt((double)hx[0]) + std::sqrt((double)hx[1]));
+    REQUIRE(eng->max_h < 4194304.0 && bound < 4194304.0, TSOM_ERR_NUMERICAL,
+            "numerical fault: accumulation term out of range (|term| >= 2^22)");
+}
+
+void finish_recheck(Engine* eng) {
+    if (eng->recheck_from_chunks) {
+        uint64_t t = 0;
+        for (uint32_t c : eng->chunk_counts) t += c;
+        eng->last_recheck = t;
+    }
+}
+
+void smooth(Engine* eng, double eta) {
+    tsom::launch_smooth(eng->infl.as<double>(), eng->sums.as<double>(), eng->w.as<float>(), eng->P,
+                        eng->D, eta, eng->U.as<double>(), eng->H.as<double>(), eng->stream);
+    CU(cudaGetLastError());
+    CU(cudaEventRecord(eng->ev[7], eng->stream));
+}
+
+void record_timing(Engine* eng) {
+    eng->t_k1 = 0.0f;
+    eng->t_update = 0.0f;
+    if (eng->k1_timed) cudaEventElapsedTime(&eng->t_k1, eng->ev[8], eng->ev[9]);
+    if (eng->update_timed) cudaEventElapsedTime(&eng->t_update, eng->ev[7], eng->ev[10]);
+    cudaEventElapsedTime(&eng->t_bmu, eng->ev[0], eng->ev[1]);
+    cudaEventElapsedTime(&eng->t_accum, eng->ev[1], eng->ev[6]);
+    cudaEventElapsedTime(&eng->t_smooth, eng->ev[6], eng->ev[7]);
+    cudaEventElapsedTime(&eng->t_total, eng->ev[0], eng->ev[7]);
+}
+
+}  // namespace
+
+extern "C" {
+
+const char* tsom_version(void) { return kVersion; }
+
+int tsom_create(int device, uint32_t nodes, uint32_t dims, tsom_engine** out) {
+    if (!out) return TSOM_ERR_INVALID;
+    *out = nullptr;
+    if (nodes < 1 || dims < 1) return TSOM_ERR_INVALID;
+    auto* eng = new tsom_engine();
+    eng->device = device;
+    eng->P = nodes;
+    eng->D = dims;
+    int rc = guarded(eng, [&] {
+        int ndev = 0;
+        CU(cudaGetDeviceCount(&ndev));
+        REQUIRE(device >= 0 && device < ndev, TSOM_ERR_CUDA, "cuda: no such device");
+        CU(cudaSetDevice(device));
+        cudaDeviceProp prop;
+        CU(cudaGetDeviceProperties(&prop, device));
+        REQUIRE(prop.major >= 10, TSOM_ERR_CUDA,
+                std::string("cuda: device ") + prop.name + " is not sm_100 (B200) class");
+        eng->sm_count = prop.multiProcessorCount;
+        eng->smem_optin = prop.sharedMemPerBlockOptin;
+        CU(cudaStreamCreateWithFlags(&eng->stream, cudaStreamNonBlocking));
+        CU(cudaStreamCreateWithFlags(&eng->copy_stream, cudaStreamNonBlocking));
+        for (auto& ev : eng->ev) CU(cudaEventCreate(&ev));
+        const size_t P = nodes, D = dims;
+        CU(eng->w.ensure(P * D * sizeof(float)));
+        CU(eng->prev.ensure(P * D * sizeof(float)));
+        CU(cudaMemset(eng->prev.p, 0, P * D * sizeof(float)));
+        CU(eng->wt.ensure((size_t)(D + 1) * ppad(eng) * sizeof(float)));
+        CU(eng->w2.ensure(P * sizeof(double)));
+        CU(eng->w2max.ensure(sizeof(float)));
+        CU(eng->x2max.ensure(2 * sizeof(float)));
+        CU(cudaMemset(eng->x2max.p, 0, 2 * sizeof(float)));
+        CU(eng->infl.ensure(P * P * sizeof(double)));
+        CU(eng->U.ensure((P * D + P * (D + 1)) * sizeof(double)));
+        CU(eng->H.ensure(P * sizeof(double)));
+        CU(eng->status.ensure(4 * sizeof(int)));
+        ensure_rows(eng, 1);
+    });
+    if (rc != TSOM_OK) {
+        std::fprintf(stderr, "tsom_create: %s\n", eng->last_error.c_str());
+        tsom_destroy(eng);
+        return rc;
+    }
+    *out = eng;
+    return TSOM_OK;
+}
+
+int tsom_destroy(tsom_engine* eng) {
+    if (!eng) return TSOM_OK;
+    cudaSetDevice(eng->device);
+    if (eng->stream) cudaStreamSynchronize(eng->stream);
+    if (eng->nccl_comm && g_nccl.commDestroy) g_nccl.commDestroy((ncclComm_t)eng->nccl_comm);
+    if (eng->host_registered) cudaHostUnregister(const_cast<float*>(eng->host_rows));
+    for (DevBuf* b : {&eng->x, &eng->xsplit, &eng->x2max, &eng->w, &eng->wt, &eng->wsplit, &eng->w2,
+                      &eng->w2max, &eng->prev, &eng->infl, &eng->topo_dist, &eng->sel,
+                      &eng->rows_scratch, &eng->gsplit, &eng->bmu, &eng->dist, &eng->part,
+                      &eng->flags, &eng->slots, &eng->sums, &eng->U, &eng->H, &eng->status,
+                      &eng->stage[0], &eng->stage[1]})
+        b->release();
+    for (auto& ev : eng->ev)
+        if (ev) cudaEventDestroy(ev);
+    if (eng->stream) cudaStreamDestroy(eng->stream);
+    if (eng->copy_stream) cudaStreamDestroy(eng->copy_stream);
+    delete eng;
+    return TSOM_OK;
+}
+
+const char* tsom_last_error(const tsom_engine* eng) {
+    return eng ? eng->last_error.c_str() : "null engine";
+}
+
+int tsom_set_option(tsom_engine* eng, int key, int64_t value) {
+    return guarded(eng, [&] {
+        switch (key) {
+            case TSOM_OPT_BMU_KERNEL:
+                REQUIRE(value >= 0 && value <= 2, TSOM_ERR_INVALID, "option: bmu kernel 0..2");
+                REQUIRE(value != 2 || tsom::tc_supported(eng->P, eng->D), TSOM_ERR_INVALID,
+                        "option: tcgen05 BMU kernel needs d <= 54");
+                eng->bmu_kernel = (int)value;
+                eng->codebook_prepped = false;
+                break;
+            case TSOM_OPT_TIE_TAU:
+                REQUIRE(value >= 0, TSOM_ERR_INVALID, "option: tau must be >= 0");
+                eng->tau_simt = eng->tau_tc = (double)value * std::ldexp(1.0, -30);
+                break;
+            case TSOM_OPT_STREAM_CHUNK:
+                REQUIRE(value >= 128, TSOM_ERR_INVALID, "option: stream chunk >= 128 rows");
+                eng->stream_chunk_rows = (uint64_t)value;
+                break;
+            default:
+                REQUIRE(false, TSOM_ERR_INVALID, "option: unknown key");
+        }
+    });
+}
+
+int tsom_bind_host_data(tsom_engine* eng, const float* rows, uint64_t n_rows, uint32_t flags) {
+    return guarded(eng, [&] {
+        CU(cudaSetDevice(eng->device));
+        REQUIRE(rows || n_rows == 0, TSOM_ERR_INVALID, "bind: null rows");
+        REQUIRE(n_rows < (1ull << 32), TSOM_ERR_INVALID, "bind: row ids are uint32 (n < 2^32)");
+        if (eng->host_registered) {
+            cudaHostUnregister(const_cast<float*>(eng->host_rows));
+            eng->host_registered = false;
+        }
+        eng->xsplit_valid = false;
+        eng->n_rows = n_rows;
+        if (flags & TSOM_BIND_STREAMED) {
+            eng->streamed = true;
+            eng->host_rows = rows;
+            eng->x.release();
+            // pin in place for async DMA; pageable memory still works (slower)
+            if (n_rows && cudaHostRegister(const_cast<float*>(rows), n_rows * eng->D * sizeof(float),
+                                           cudaHostRegisterReadOnly) == cudaSuccess)
+                eng->host_registered = true;
+            else
+                cudaGetLastError();
+            return;
+        }
+        eng->streamed = false;
+        eng->host_rows = nullptr;
+        const size_t bytes = n_rows * eng->D * sizeof(float);
+        CU(eng->x.ensure(std::max<size_t>(bytes, 4)));
+        if (bytes) CU(cudaMemcpy(eng->x.p, rows, bytes, cudaMemcpyHostToDevice));
+        tsom::launch_row_norm_max(eng->x.as<float>(), n_rows, eng->D, eng->x2max.as<float>(),
+                                  eng->stream);
+        CU(cudaGetLastError());
+        CU(cudaStreamSynchronize(eng->stream));
+    });
+}
+
+int tsom_bind_device_data(tsom_engine* eng, const float* d_rows, uint64_t n_rows) {
+    return guarded(eng, [&] {
+        CU(cudaSetDevice(eng->device));
+        REQUIRE(n_rows < (1ull << 32), TSOM_ERR_INVALID, "bind: row ids are uint32 (n < 2^32)");
+        eng->x.release();
+        eng->x.p = const_cast<float*>(d_rows);
+        eng->x.bytes = n_rows * eng->D * sizeof(float);
+        eng->x.owned = false;
+        eng->n_rows = n_rows;
+        eng->streamed = false;
+        eng->xsplit_valid = false;
+        tsom::launch_row_norm_max(d_rows, n_rows, eng->D, eng->x2max.as<float>(), eng->stream);
+        CU(cudaGetLastError());
+        CU(cudaStreamSynchronize(eng->stream));
+    });
+}
+
+int tsom_bind_synthetic_gmm(tsom_engine* eng, uint64_t n_rows, uint64_t seed, uint32_t n_comp,
+                            uint64_t row_offset) {
+    return guarded(eng, [&] {
+        CU(cudaSetDevice(eng->device));
+        REQUIRE(n_comp >= 1, TSOM_ERR_INVALID, "synth: n_comp >= 1");
+        REQUIRE(n_rows < (1ull << 32), TSOM_ERR_INVALID, "bind: row ids are uint32 (n < 2^32)");
+        // centres from the reference Rng (rng.hpp:12-91): Rng(seed, SeedStream::synth),
+        // real(-4, 4) in (component, feature) order.
+        uint64_t z = seed + 0x9e3779b97f4a7c15ULL * (4 + 1);
+        z = (z ^ (z >> 30)) * 0xbf58476d1ce4e5b9ULL;
+        z = (z ^ (z >> 27)) * 0x94d049bb133111ebULL;
+        std::mt19937_64 gen(z ^ (z >> 31));
+        std::vector<float> centres((size_t)n_comp * eng->D);
+        for (auto& c : centres) c = (float)(-4.0 + 8.0 * ((double)(gen() >> 11) * 0x1.0p-53));
+        DevBuf dc;
+        CU(dc.ensure(centres.size() * sizeof(float)));
+        CU(cudaMemcpy(dc.p, centres.data(), centres.size() * sizeof(float), cudaMemcpyHostToDevice));
+        const size_t bytes = n_rows * eng->D * sizeof(float);
+        CU(eng->x.ensure(std::max<size_t>(bytes, 4)));
+        tsom::launch_synth_gmm(eng->x.as<float>(), n_rows, eng->D, dc.as<float>(), n_comp, seed,
+                               row_offset, eng->stream);
+        CU(cudaGetLastError());
+        eng->n_rows = n_rows;
+        eng->streamed = false;
+        eng->xsplit_valid = false;
+        tsom::launch_row_norm_max(eng->x.as<float>(), n_rows, eng->D, eng->x2max.as<float>(),
+                                  eng->stream);
+        CU(cudaStreamSynchronize(eng->stream));
+        dc.release();
+    });
+}
+
+uint64_t tsom_rows(const tsom_engine* eng) { return eng ? eng->n_rows : 0; }
+
+int tsom_set_codebook(tsom_engine* eng, const float* weights) {
+    return guarded(eng, [&] {
+        CU(cudaSetDevice(eng->device));
+        REQUIRE(weights, TSOM_ERR_INVALID, "set_codebook: null weights");
+        CU(cudaMemcpyAsync(eng->w.p, weights, (size_t)eng->P * eng->D * sizeof(float),
+                           cudaMemcpyHostToDevice, eng->stream));
+        eng->codebook_set = true;
+        eng->codebook_prepped = false;
+        prep_codebook(eng);
+        CU(cudaStreamSynchronize(eng->stream));
+    });
+}
+
+int tsom_get_codebook(tsom_engine* eng, float* weights) {
+    return guarded(eng, [&] {
+        CU(cudaSetDevice(eng->device));
+        REQUIRE(eng->codebook_set, TSOM_ERR_INVALID, "get_codebook: codebook not set");
+        CU(cudaMemcpyAsync(weights, eng->w.p, (size_t)eng->P * eng->D * sizeof(float),
+                           cudaMemcpyDeviceToHost, eng->stream));
+        CU(cudaStreamSynchronize(eng->stream));
+    });
+}
+
+int tsom_set_influence(tsom_engine* eng, const double* influence, int64_t key) {
+    return guarded(eng, [&] {
+        CU(cudaSetDevice(eng->device));
+        REQUIRE(influence, TSOM_ERR_INVALID, "set_influence: null matrix");
+        if (key >= 0 && eng->infl_set && key == eng->infl_key) return;
+        const size_t n = (size_t)eng->P * eng->P;
+        double mh = 0.0;
+        for (size_t i = 0; i < n; ++i) mh = std::max(mh, std::fabs(influence[i]));
+        eng->max_h = mh;
+        CU(cudaMemcpyAsync(eng->infl.p, influence, n * sizeof(double), cudaMemcpyHostToDevice,
+                           eng->stream));
+        CU(cudaStreamSynchronize(eng->stream));
+        eng->infl_key = key;
+        eng->infl_set = true;
+    });
+}
+
+int tsom_epoch(tsom_engine* eng, const uint32_t* selected, uint64_t n_sel, double eta,
+               double* u_out, double* h_out, double* dist_out) {
+    return guarded(eng, [&] {
+        CU(cudaSetDevice(eng->device));
+        REQUIRE(eng->infl_set, TSOM_ERR_INVALID, "epoch: influence not set");
+        REQUIRE(eng->n_rows > 0 || (selected && n_sel == 0) || eng->nccl_comm, TSOM_ERR_INVALID,
+                "epoch: no data bound");
+        prep_codebook(eng);
+        accumulate_epoch(eng, selected, n_sel, dist_out != nullptr, true);
+        smooth(eng, eta);
+        const size_t P = eng->P, D = eng->D;
+        if (u_out)
+            CU(cudaMemcpyAsync(u_out, eng->U.p, P * D * sizeof(double), cudaMemcpyDeviceToHost,
+                               eng->stream));
+        if (h_out)
+            CU(cudaMemcpyAsync(h_out, eng->H.p, P * sizeof(double), cudaMemcpyDeviceToHost,
+                               eng->stream));
+        const uint64_t n = selected ? n_sel : eng->n_rows;
+        if (dist_out && n)
+            CU(cudaMemcpyAsync(dist_out, eng->dist.p, n * sizeof(double), cudaMemcpyDeviceToHost,
+                               eng->stream));
+        CU(cudaStreamSynchronize(eng->stream));
+        finish_recheck(eng);
+        record_timing(eng);
+        if (n) check_term_guard(eng, eta);
+    });
+}
+
+int tsom_bmu(tsom_engine* eng, const float* rows, uint64_t n, uint32_t* bmu, double* dist) {
+    return guarded(eng, [&] {
+        CU(cudaSetDevice(eng->device));
+        REQUIRE(rows || n == 0, TSOM_ERR_INVALID, "find_bmus: null rows");
+        prep_codebook(eng);
+        if (n == 0) return;
+        CU(eng->rows_scratch.ensure(n * eng->D * sizeof(float)));
+        CU(cudaMemcpyAsync(eng->rows_scratch.p, rows, n * eng->D * sizeof(float),
+                           cudaMemcpyHostToDevice, eng->stream));
+        ensure_rows(eng, n);
+        const int nslots = tsom::accumulate_slots(eng->P, eng->D, eng->smem_optin, eng->sm_count);
+        CU(eng->slots.ensure((size_t)nslots * slot_len(eng) * sizeof(double)));
+        float* xm = eng->x2max.as<float>() + 1;
+        tsom::launch_row_norm_max(eng->rows_scratch.as<float>(), n, eng->D, xm, eng->stream);
+        run_bmu(eng, eng->rows_scratch.as<float>(), nullptr, n, xm, nullptr);
+        if (dist)
+            tsom::launch_accumulate(eng->rows_scratch.as<float>(), nullptr, n, eng->D,
+                                    eng->w.as<float>(), eng->P, eng->bmu.as<uint32_t>(),
+                                    eng->dist.as<double>(), eng->slots.as<double>(), nslots, false,
+                                    true, eng->smem_optin, eng->stream);
+        CU(cudaGetLastError());
+        CU(cudaMemcpyAsync(bmu, eng->bmu.p, n * sizeof(uint32_t), cudaMemcpyDeviceToHost,
+                           eng->stream));
+        if (dist)
+            CU(cudaMemcpyAsync(dist, eng->dist.p, n * sizeof(double), cudaMemcpyDeviceToHost,
+                               eng->stream));
+        uint32_t cnt = 0;
+        CU(cudaMemcpyAsync(&cnt, eng->flags.p, sizeof(uint32_t), cudaMemcpyDeviceToHost,
+                           eng->stream));
+        CU(cudaStreamSynchronize(eng->stream));
+        eng->last_recheck = cnt;
+    });
+}
+
+int tsom_bmu_bound(tsom_engine* eng, const uint32_t* selected, uint64_t n_sel, uint32_t* bmu,
+                   double* dist) {
+    return guarded(eng, [&] {
+        CU(cudaSetDevice(eng->device));
+        REQUIRE(!eng->streamed, TSOM_ERR_INVALID, "bmu_bound: resident data only");
+        accumulate_epoch(eng, selected, n_sel, dist != nullptr, false);
+        const uint64_t n = selected ? n_sel : eng->n_rows;
+        if (n) {
+            CU(cudaMemcpyAsync(bmu, eng->bmu.p, n * sizeof(uint32_t), cudaMemcpyDeviceToHost,
+                               eng->stream));
+            if (dist)
+                CU(cudaMemcpyAsync(dist, eng->dist.p, n * sizeof(double), cudaMemcpyDeviceToHost,
+                                   eng->stream));
+        }
+        CU(cudaStreamSynchronize(eng->stream));
+    });
+}
+
+int tsom_qe(tsom_engine* eng, const uint32_t* selected, uint64_t n_sel, double* dist_sum,
+            uint64_t* count) {
+    return guarded(eng, [&] {
+        CU(cudaSetDevice(eng->device));
+        accumulate_epoch(eng, selected, n_sel, false, false);
+        double tail[2] = {0, 0};
+        CU(cudaMemcpyAsync(tail, eng->sums.as<double>() + (size_t)eng->P * eng->D + eng->P,
+                           2 * sizeof(double), cudaMemcpyDeviceToHost, eng->stream));
+        CU(cudaStreamSynchronize(eng->stream));
+        finish_recheck(eng);
+        if (dist_sum) *dist_sum = tail[0];
+        if (count) *count = (uint64_t)tail[1];
+    });
+}
+
+int tsom_set_topology_distance(tsom_engine* eng, const double* dist) {
+    return guarded(eng, [&] {
+        CU(cudaSetDevice(eng->device));
+        REQUIRE(dist, TSOM_ERR_INVALID, "topology: null distance matrix");
+        const size_t n = (size_t)eng->P * eng->P;
+        CU(eng->topo_dist.ensure(n * sizeof(double)));
+        CU(cudaMemcpyAsync(eng->topo_dist.p, dist, n * sizeof(double), cudaMemcpyHostToDevice,
+                           eng->stream));
+        CU(cudaStreamSynchronize(eng->stream));
+        eng->topo_set = true;
+        eng->infl_key = -2;
+    });
+}
+
+int tsom_train_epoch(tsom_engine* eng, double eta, double sigma, double momentum, uint32_t flags) {
+    return guarded(eng, [&] {
+        CU(cudaSetDevice(eng->device));
+        REQUIRE(eng->topo_set, TSOM_ERR_INVALID, "train_epoch: topology distance not set");
+        REQUIRE(sigma > 0.0, TSOM_ERR_INVALID, "influence_matrix: sigma must be > 0");
+        const bool momentum_on = (flags & 1u) != 0;
+        // influence(sigma) on the device (topology.hpp:342-364); the device
+        // path keys its cache on sigma exactly like influence_cache_key (:399-401)
+        const int64_t key = (int64_t)std::llround(sigma * 1e6);
+        if (!(eng->infl_set && eng->infl_key == key)) {
+            const double inv = 1.0 / (2.0 * sigma * sigma);
+            tsom::launch_influence(eng->topo_dist.as<double>(), (size_t)eng->P * eng->P, inv,
+                                   eng->infl.as<double>(), eng->stream);
+            CU(cudaGetLastError());
+            eng->infl_key = key;
+            eng->infl_set = true;
+            eng->max_h = 1.0;
+        }
+        prep_codebook(eng);
+        accumulate_epoch(eng, nullptr, eng->n_rows, false, true);
+        smooth(eng, eta);
+        int ok = INT_MAX;
+        CU(cudaMemcpyAsync(eng->status.p, &ok, sizeof(int), cudaMemcpyHostToDevice, eng->stream));
+        tsom::launch_apply_update(eng->w.as<float>(), eng->prev.as<float>(), eng->P, eng->D,
+                                  eng->U.as<double>(), eng->H.as<double>(), momentum_on, momentum,
+                                  eng->status.as<int>(), eng->stream);
+        CU(cudaGetLastError());
+        CU(cudaEventRecord(eng->ev[10], eng->stream));
+        eng->update_timed = true;
+        eng->codebook_prepped = false;
+        prep_codebook(eng);
+        int st = INT_MAX;
+        CU(cudaMemcpyAsync(&st, eng->status.p, sizeof(int), cudaMemcpyDeviceToHost, eng->stream));
+        CU(cudaStreamSynchronize(eng->stream));
+        finish_recheck(eng);
+        record_timing(eng);
+        check_term_guard(eng, eta);
+        REQUIRE(st == INT_MAX, TSOM_ERR_NUMERICAL,
+                "numerical fault: non-finite weight update at node " + std::to_string(st));
+    });
+}
+
+uint64_t tsom_last_recheck_count(const tsom_engine* eng) { return eng ? eng->last_recheck : 0; }
+
+int tsom_comm_unique_id(tsom_engine* eng, uint8_t id_out[128]) {
+    return guarded(eng, [&] {
+        std::string err;
+        REQUIRE(g_nccl.load(err), TSOM_ERR_NCCL, err);
+        ncclUniqueId id;
+        ncclResult_t r = g_nccl.getUniqueId(&id);
+        REQUIRE(r == ncclSuccess, TSOM_ERR_NCCL, "nccl: ncclGetUniqueId failed");
+        static_assert(sizeof(id) == 128, "ncclUniqueId is 128 bytes");
+        std::memcpy(id_out, &id, 128);
+    });
+}
+
+int tsom_comm_init(tsom_engine* eng, const uint8_t id[128], int rank, int world) {
+    return guarded(eng, [&] {
+        CU(cudaSetDevice(eng->device));
+        REQUIRE(world >= 1 && rank >= 0 && rank < world, TSOM_ERR_INVALID, "comm: bad rank/world");
+        std::string err;
+        REQUIRE(g_nccl.load(err), TSOM_ERR_NCCL, err);
+        ncclUniqueId uid;
+        std::memcpy(&uid, id, 128);
+        ncclComm_t comm;
+        ncclResult_t r = g_nccl.commInitRank(&comm, world, uid, rank);
+        REQUIRE(r == ncclSuccess, TSOM_ERR_NCCL,
+                std::string("nccl: ncclCommInitRank failed: ") + (g_nccl.errStr ? g_nccl.errStr(r) : "?"));
+        eng->nccl_comm = comm;
+        eng->rank = rank;
+        eng->world = world;
+    });
+}
+
+int tsom_last_timing(const tsom_engine* eng, float* bmu_ms, float* accum_ms, float* smooth_ms,
+                     float* total_ms) {
+    if (!eng) return TSOM_ERR_INVALID;
+    if (bmu_ms) *bmu_ms = eng->t_bmu;
+    if (accum_ms) *accum_ms = eng->t_accum;
+    if (smooth_ms) *smooth_ms = eng->t_smooth;
+    if (total_ms) *total_ms = eng->t_total;
+    return TSOM_OK;
+}
+
+int tsom_last_timing_detail(const tsom_engine* eng, float out[8]) {
+    if (!eng || !out) return TSOM_ERR_INVALID;
+    const float v[8] = {eng->t_k1,    eng->t_bmu,    eng->t_accum, eng->t_smooth,
+                        eng->t_update, eng->t_total, 0.0f,         0.0f};
+    std::memcpy(out, v, sizeof(v));
+    return TSOM_OK;
+}
+
+uint64_t tsom_kernel_launches(void) { return tsom::g_launches.load(); }
+
+void* tsom_stream(tsom_engine* eng) { return eng ? (void*)eng->stream : nullptr; }
+
+}  // extern "C"

@@ -1,0 +1,144 @@
+// dropin.cpp — the reference training loop driving the B200 engine.
+//
+// Built only where the reference headers exist (the maintainer's build): it
+// instantiates toposom::train_with_executor (trainer.hpp:466-523) with
+// toposom_b200::CudaExecutor (include/toposom_b200/cuda_executor.hpp) and
+// exports a flat C entry with the same config layout as oracle/_ref's
+// ref_train, so tests and bench.py can run the identical reference loop with
+// the GPU executor swapped in.  No kernel code lives here.
+#include <cstdint>
+#include <cstring>
+#include <stdexcept>
+#include <string>
+
+#include "toposom_b200/cuda_executor.hpp"
+
+using namespace toposom;
+
+namespace {
+thread_local std::string g_err;
+
+template <typename F>
+int guarded(F&& f) {
+    try {
+        f();
+        return 0;
+    } catch (const std::invalid_argument& e) {
+        g_err = e.what();
+        return 1;
+    } catch (const std::out_of_range& e) {
+        g_err = e.what();
+        return 3;
+    } catch (const std::runtime_error& e) {
+        g_err = e.what();
+        return 2;
+    } catch (const std::exception& e) {
+        g_err = e.what();
+        return 9;
+    }
+}
+}  // namespace
+
+struct dropin_config {  // layout shared with oracle/_ref ref_config
+    int topology;
+    std::uint64_t grid_w, grid_h, nodes;
+    std::uint64_t n_iters;
+    double eta0;
+    int lr_exponential;
+    double sigma0;
+    int radius_exponential;
+    double sigma_min;
+    int init_method;
+    int use_momentum;
+    double momentum;
+    std::uint64_t refresh_warmup;
+    double refresh_growth;
+    std::uint64_t refresh_max_interval;
+    std::uint64_t n_chunks;
+    std::uint64_t seed;
+    int sampling;
+    int budget_fixed;
+    std::uint64_t m0;
+    double rho;
+    double alpha, beta;
+    int n_threads;
+};
+
+extern "C" {
+
+const char* tsom_dropin_last_error() { return g_err.c_str(); }
+std::size_t tsom_dropin_config_sizeof() { return sizeof(dropin_config); }
+
+// flags: bit0 streamed, bits1-2 bmu kernel (0 auto, 1 simt, 2 tc), bit3 force distances
+int tsom_dropin_train(const dropin_config* rc, const float* data, std::size_t n, std::size_t d,
+                      float* weights_out, double* qe_log, std::uint8_t* refresh_log, int device,
+                      unsigned flags, double* seconds_out) {
+    return guarded([&] {
+        SomConfig c;
+        const auto kind = static_cast<TopologyKind>(rc->topology);
+        c.topology = is_lattice(kind) ? TopologySpec::lattice(kind, rc->grid_w, rc->grid_h)
+                                      : TopologySpec::graph(kind, rc->nodes);
+        c.n_iters = rc->n_iters;
+        c.eta0 = rc->eta0;
+        c.lr_decay = rc->lr_exponential ? DecayKind::exponential : DecayKind::linear;
+        c.sigma0 = rc->sigma0;
+        c.radius_decay = rc->radius_exponential ? DecayKind::exponential : DecayKind::linear;
+        c.sigma_min = rc->sigma_min;
+        c.init_method = rc->init_method == 1 ? InitMethod::uniform_box
+                        : rc->init_method == 2 ? InitMethod::pca_plane
+                                               : InitMethod::sample_draw;
+        c.use_momentum = rc->use_momentum != 0;
+        c.momentum = rc->momentum;
+        c.refresh.warmup_iters = rc->refresh_warmup;
+        c.refresh.growth = rc->refresh_growth;
+        c.refresh.max_interval = rc->refresh_max_interval;
+        c.n_chunks = rc->n_chunks;
+        c.seed = rc->seed;
+        SamplingBudget b;
+        b.mode = rc->budget_fixed ? BudgetMode::fixed : BudgetMode::proportional;
+        b.m0 = rc->m0;
+        b.rho = rc->rho;
+        Sampler sampler(static_cast<SamplingKind>(rc->sampling), b, n, c.seed, rc->alpha, rc->beta);
+        // DataMatrix over the caller's rows (one host copy, as DataSourceRef needs a matrix)
+        DataMatrix mat(n, d, std::vector<float>(data, data + n * d));
+        toposom_b200::CudaOptions opts;
+        opts.device = device;
+        opts.streamed = (flags & 1u) != 0;
+        opts.bmu_kernel = static_cast<int>((flags >> 1) & 3u);
+        TrainOptions to;
+        to.log_qe = qe_log != nullptr;
+        const auto t0 = std::chrono::steady_clock::now();
+        std::pair<SomModel, RunLog> result;
+        if (flags & 8u) {
+            opts.distances = toposom_b200::Distances::always;
+            toposom_b200::CudaExecutor ex(mat, c.nodes(), opts);
+            result = train_with_executor(c, mat, sampler, ex, to);
+        } else {
+            result = toposom_b200::train_cuda(c, mat, sampler, opts, to);
+        }
+        const std::chrono::duration<double> dt = std::chrono::steady_clock::now() - t0;
+        if (seconds_out) *seconds_out = dt.count();
+        std::memcpy(weights_out, result.first.weights.values.data(),
+                    result.first.weights.values.size() * sizeof(float));
+        for (std::size_t t = 0; t < result.second.iterations.size(); ++t) {
+            if (qe_log) qe_log[t] = *result.second.iterations[t].qe_train;
+            if (refresh_log) refresh_log[t] = result.second.iterations[t].refreshed ? 1 : 0;
+        }
+    });
+}
+
+// find_bmus through the drop-in helper
+int tsom_dropin_find_bmus(const float* x, std::size_t n, const float* w, std::size_t p,
+                          std::size_t d, std::uint32_t* bmus, double* dists, int device) {
+    return guarded([&] {
+        DataMatrix chunk(n, d, std::vector<float>(x, x + n * d));
+        DataMatrix weights(p, d, std::vector<float>(w, w + p * d));
+        std::vector<std::uint32_t> b;
+        std::vector<double> dd;
+        toposom_b200::find_bmus_cuda(chunk, weights, b, dd, device);
+        std::memcpy(bmus, b.data(), n * sizeof(std::uint32_t));
+        std::memcpy(dists, dd.data(), n * sizeof(double));
+    });
+}
+
+}  // extern "C"

@@ -1,0 +1,176 @@
+// engine.h — internal state of the B200 batch-SOM epoch engine.
+//
+// Data layout in HBM:
+//   x        n_rows x d   f32 row-major   bound samples (resident mode)
+//   xs       tiles of 128 rows, [hi|lo] x [14 k-cores][128 rows][4 f32]
+//            pre-split TF32 operands for the tcgen05 BMU kernel (k1_bmu_tc.cu)
+//   w        P x d        f32             codebook (updated in place by the
+//                                         device-resident loop)
+//   wt       (d+1) x Ppad f32             SIMT operand: -2 w^T and ||w||^2 row
+//   ws       P/256 groups of [hi|lo] x [14][256][4] f32  tcgen05 B operand
+//   infl     P x P        f64             influence h[b][j]
+//   slots    nslot x (P*d + P + 2) f64    per-CTA accumulation partials
+//   sums     P*d + P + 2  f64             reduced [R | c | sum dist | count]
+//                                         (the one allreduce buffer)
+//   U, H     P*d, P       f64             smoothed accumulators (K3 output)
+#pragma once
+
+#include <cuda_runtime.h>
+
+#include <atomic>
+#include <cstdint>
+#include <string>
+#include <vector>
+
+#include "../../include/tsom_b200.h"
+
+namespace tsom {
+
+// Kernel launches issued by this library (tsom_kernel_launches): the bench
+// reports it so a silent host fallback would be visible.
+extern std::atomic<uint64_t> g_launches;
+#define TSOM_LAUNCH(...) (++::tsom::g_launches, __VA_ARGS__)
+
+struct DevBuf {
+    void* p = nullptr;
+    size_t bytes = 0;
+    bool owned = true;
+    cudaError_t ensure(size_t need);
+    void release();
+    template <typename T>
+    T* as() const { return static_cast<T*>(p); }
+};
+
+struct Error {
+    int code;
+    std::string msg;
+};
+
+// Threshold for the exact FP64 re-check of near-ties (see k1 kernels):
+// a row is re-scanned when second_best - best <= tau * (max||x||^2 + max||w||^2).
+constexpr double kDefaultTauSimt = 1.0 / 65536.0;   // 2^-16
+constexpr double kDefaultTauTc = 1.0 / 16384.0;     // 2^-14 (3xTF32 error is larger)
+
+constexpr int kTcTileM = 128;   // samples per tcgen05 tile (TMEM lanes)
+constexpr int kTcGroupN = 256;  // nodes per CTA-resident codebook group
+constexpr int kTcKPad = 56;     // d + 1 (norm column) padded to 7 tf32 k-steps
+
+struct Engine {
+    int device = 0;
+    uint32_t P = 0, D = 0;
+    cudaStream_t stream = nullptr;
+    cudaStream_t copy_stream = nullptr;
+    std::string last_error;
+    int sm_count = 148;
+    size_t smem_optin = 0;
+
+    // options
+    int bmu_kernel = 0;  // 0 auto, 1 simt, 2 tc
+    double tau_simt = kDefaultTauSimt;
+    double tau_tc = kDefaultTauTc;
+    uint64_t stream_chunk_rows = 1u << 20;
+
+    // bound data
+    DevBuf x;           // resident rows
+    uint64_t n_rows = 0;
+    bool streamed = false;
+    const float* host_rows = nullptr;  // streamed mode source
+    bool host_registered = false;
+    DevBuf xsplit;      // pre-split tf32 tiles for the tensor-core kernel (all rows)
+    bool xsplit_valid = false;
+    DevBuf x2max;       // float: max ||x||^2 over bound rows
+
+    // codebook
+    DevBuf w, wt, wsplit, w2, w2max, prev;
+    bool codebook_set = false;
+    bool codebook_prepped = false;
+
+    // influence
+    DevBuf infl;
+    int64_t infl_key = -1;
+    bool infl_set = false;
+    DevBuf topo_dist;
+    bool topo_set = false;
+
+    // per-epoch scratch
+    DevBuf sel;
+    DevBuf rows_scratch;   // caller rows for tsom_bmu / gathered split tiles
+    DevBuf gsplit;         // split tiles of a gathered selection
+    DevBuf bmu;
+    DevBuf dist;
+    DevBuf part;           // tcgen05 per-group partial top-2 [groups][n] (b1, i1, b2)
+    DevBuf flags;          // [0] = count, then positions
+    DevBuf slots;
+    DevBuf sums;
+    DevBuf U, H;
+    DevBuf status;         // device error word(s)
+    DevBuf stage[2];       // streamed-mode device chunks
+    float* pinned[2] = {nullptr, nullptr};
+    cudaEvent_t ev[12] = {};  // 0 start, 1 bmu end, 6 accum end, 7 smooth end, 8/9 K1 kernel, 10 update end
+    uint64_t last_recheck = 0;
+    std::vector<uint32_t> chunk_counts;  // per-chunk re-check counts (async D2H targets)
+    bool recheck_from_chunks = false;
+    double max_h = 1.0;                  // max |influence| of the bound matrix
+    float t_bmu = 0, t_accum = 0, t_smooth = 0, t_total = 0, t_k1 = 0, t_update = 0;
+    bool k1_timed = false, update_timed = false;
+
+    // multi-GPU
+    void* nccl_comm = nullptr;
+    int rank = 0, world = 1;
+};
+
+// ---------------------------------------------------------------------------
+// Kernel launchers (all asynchronous on `st`)
+// ---------------------------------------------------------------------------
+
+// codebook prep: w2 (f64 ||w_j||^2), w2max, SIMT operand wt, tcgen05 operand wsplit
+void launch_prep_codebook(const float* w, uint32_t P, uint32_t D, double* w2, float* w2max,
+                          float* wt, uint32_t Ppad, float* wsplit, cudaStream_t st);
+// max ||x||^2 over rows (f32 atomic max on non-negative floats)
+void launch_row_norm_max(const float* x, uint64_t n, uint32_t D, float* out, cudaStream_t st);
+// a[0] = max(a[0], a[1])
+void launch_fold_max(float* a, cudaStream_t st);
+// split rows (optionally gathered through sel) into tcgen05 tiles
+void launch_split_rows(const float* x, const uint32_t* sel, uint64_t n, uint32_t D, float* tiles,
+                       cudaStream_t st);
+bool tc_supported(uint32_t P, uint32_t D);
+
+// K1: BMU candidates.  SIMT variant writes final bmu + flags directly.
+void launch_bmu_simt(const float* x, const uint32_t* sel, uint64_t n, uint32_t D, const float* wt,
+                     uint32_t P, uint32_t Ppad, const float* x2max, const float* w2max, float tau,
+                     uint32_t* bmu, uint32_t* flags, int sm_count, cudaStream_t st);
+// tcgen05 variant writes per-group partials; merge writes bmu + flags.
+cudaError_t launch_bmu_tc(const float* tiles, uint64_t n, uint32_t P, const float* wsplit,
+                          float* part, int sm_count, cudaStream_t st);
+void launch_merge_partials(const float* part, uint64_t n, uint32_t groups, const float* x2max,
+                           const float* w2max, float tau, uint32_t* bmu, uint32_t* flags,
+                           cudaStream_t st);
+// exact FP64 re-scan of flagged rows (reference loop order)
+void launch_rescan(const float* x, const uint32_t* sel, const float* w, uint32_t P, uint32_t D,
+                   const uint32_t* flags, uint64_t n, uint32_t* bmu, cudaStream_t st);
+
+// K2: accumulation of residual sums per BMU + counts + exact distances.
+//     accumulate=false → distances / distance sum only.
+void launch_accumulate(const float* x, const uint32_t* sel, uint64_t n, uint32_t D,
+                       const float* w, uint32_t P, const uint32_t* bmu, double* dist_out,
+                       double* slots, int nslots, bool accumulate, bool first_pass,
+                       size_t smem_optin, cudaStream_t st);
+int accumulate_slots(uint32_t P, uint32_t D, size_t smem_optin, int sm_count);
+void launch_reduce_slots(const double* slots, int nslots, size_t len, double* sums,
+                         cudaStream_t st);
+
+// K3: smoothing num = H^T S, den = H^T c; U = eta (num - w den), H = den
+void launch_smooth(const double* infl, const double* sums, const float* w, uint32_t P, uint32_t D,
+                   double eta, double* U, double* H, cudaStream_t st);
+// apply_update on device (trainer.hpp:341-369); status[0] = first bad node + 1
+void launch_apply_update(float* w, float* prev, uint32_t P, uint32_t D, const double* U,
+                         const double* H, bool use_momentum, double momentum, int* status,
+                         cudaStream_t st);
+// influence_matrix (topology.hpp:342-364) from a P x P distance matrix
+void launch_influence(const double* dist, size_t n, double inv_two_sigma_sq, double* out,
+                      cudaStream_t st);
+// synthetic Gaussian mixture rows
+void launch_synth_gmm(float* x, uint64_t n, uint32_t D, const float* centres, uint32_t n_comp,
+                      uint64_t seed, uint64_t row_offset, cudaStream_t st);
+
+}  // namespace tsom

@@ -1,0 +1,419 @@
+// k_bmu.cu — BMU search support kernels (SIMT path, exact re-check, codebook prep).
+//
+// Reference semantics (trainer.hpp:282-308 find_bmus): for each row,
+//   best_j = argmin_j  sum_k (double(x_k) - w_jk)^2   (strict <, ties -> lowest j)
+// computed in FP64.  The GPU evaluates the Gram form ||w_j||^2 - 2 x.w_j in
+// FP32 (SIMT here, 3xTF32 tcgen05 in k1_bmu_tc.cu), keeps the best and
+// second-best value per row, and re-scans in exact FP64 — with the reference's
+// loop order and no FMA contraction — every row whose top-2 gap is within the
+// FP32 error bound tau * (max||x||^2 + max||w||^2).  Rows outside that window
+// have a unique FP64 argmin equal to the FP32 one, so BMU indices are
+// bit-identical to the reference for every row.
+#include <cuda_runtime.h>
+#include <math_constants.h>
+
+#include <cstdint>
+
+#include "engine.h"
+
+namespace tsom {
+
+// ---------------------------------------------------------------------------
+// Codebook prep (once per codebook change)
+// ---------------------------------------------------------------------------
+
+// tf32 truncation: keep 10 explicit mantissa bits (the MMA ignores the low 13)
+__device__ __forceinline__ float tf32_hi(float v) {
+    return __uint_as_float(__float_as_uint(v) & 0xFFFFE000u);
+}
+
+// Split an augmented row (values v[0..kpad)) into tcgen05 K-major core-matrix
+// layout: element (row r, k) of a [rows]-row tile lives at
+//   ((k / 4) * rows + r) * 4 + (k % 4)      (hi part; lo part follows after rows*kpad)
+__global__ void k_prep_codebook(const float* __restrict__ w, uint32_t P, uint32_t D,
+                                double* __restrict__ w2, float* __restrict__ w2max,
+                                float* __restrict__ wt, uint32_t Ppad,
+                                float* __restrict__ wsplit) {
+    const uint32_t j = blockIdx.x * blockDim.x + threadIdx.x;
+    if (j >= Ppad) return;
+    if (j >= P) {  // padding node: never wins
+        for (uint32_t k = 0; k < D; ++k) wt[(size_t)k * Ppad + j] = 0.0f;
+        wt[(size_t)D * Ppad + j] = CUDART_INF_F;
+        return;
+    }
+    const float* wj = w + (size_t)j * D;
+    double s = 0.0;
+    for (uint32_t k = 0; k < D; ++k) s = __dadd_rn(s, __dmul_rn((double)wj[k], (double)wj[k]));
+    w2[j] = s;
+    atomicMax(reinterpret_cast<int*>(w2max), __float_as_int((float)s));
+    for (uint32_t k = 0; k < D; ++k) wt[(size_t)k * Ppad + j] = -2.0f * wj[k];
+    wt[(size_t)D * Ppad + j] = (float)s;
+    if (wsplit) {
+        // group g = j / 256 holds [hi: 14 x 256 x 4][lo: 14 x 256 x 4].  Columns
+        // k < D carry -2 w_jk split hi/lo; columns D and D+1 carry ||w_j||^2 as
+        // three tf32-exact pieces (p1 hi/p2 lo in column D, p3 hi in column D+1)
+        // so the norm enters the MMA with ~33 significant bits.
+        const uint32_t g = j / kTcGroupN, r = j % kTcGroupN;
+        float* base = wsplit + (size_t)g * 2 * kTcGroupN * kTcKPad;
+        const float p1 = tf32_hi((float)s);
+        const float p2 = tf32_hi((float)(s - (double)p1));
+        const float p3 = tf32_hi((float)(s - (double)p1 - (double)p2));
+        for (uint32_t k = 0; k < kTcKPad; ++k) {
+            float hi, lo;
+            if (k < D) {
+                const float v = -2.0f * wj[k];
+                hi = tf32_hi(v);
+                lo = v - hi;
+            } else if (k == D) {
+                hi = p1;
+                lo = p2;
+            } else if (k == D + 1) {
+                hi = p3;
+                lo = 0.0f;
+            } else {
+                hi = 0.0f;
+                lo = 0.0f;
+            }
+            const size_t off = ((size_t)(k / 4) * kTcGroupN + r) * 4 + (k % 4);
+            base[off] = hi;
+            base[(size_t)kTcGroupN * kTcKPad + off] = lo;
+        }
+    }
+}
+
+__global__ void k_prep_pad_groups(uint32_t P, uint32_t D, float* __restrict__ wsplit,
+                                  uint32_t groups) {
+    // padding nodes of the last tcgen05 group: norm column = 3e38 (finite, so
+    // 0 * v never makes a NaN inside the MMA), everything else 0 => never wins
+    const uint32_t j = P + blockIdx.x * blockDim.x + threadIdx.x;
+    if (j >= groups * kTcGroupN) return;
+    const uint32_t g = j / kTcGroupN, r = j % kTcGroupN;
+    float* base = wsplit + (size_t)g * 2 * kTcGroupN * kTcKPad;
+    for (uint32_t k = 0; k < kTcKPad; ++k) {
+        const size_t off = ((size_t)(k / 4) * kTcGroupN + r) * 4 + (k % 4);
+        base[off] = k == D ? tf32_hi(3.0e38f) : 0.0f;
+        base[(size_t)kTcGroupN * kTcKPad + off] = 0.0f;
+    }
+}
+
+void launch_prep_codebook(const float* w, uint32_t P, uint32_t D, double* w2, float* w2max,
+                          float* wt, uint32_t Ppad, float* wsplit, cudaStream_t st) {
+    cudaMemsetAsync(w2max, 0, sizeof(float), st);
+    TSOM_LAUNCH(k_prep_codebook<<<(Ppad + 127) / 128, 128, 0, st>>>(w, P, D, w2, w2max, wt, Ppad, wsplit));
+    if (wsplit) {
+        const uint32_t groups = (P + kTcGroupN - 1) / kTcGroupN;
+        const uint32_t pad = groups * kTcGroupN - P;
+        if (pad) TSOM_LAUNCH(k_prep_pad_groups<<<(pad + 127) / 128, 128, 0, st>>>(P, D, wsplit, groups));
+    }
+}
+
+// ---------------------------------------------------------------------------
+// max ||x||^2 (bound once per dataset)
+// ---------------------------------------------------------------------------
+
+__global__ void k_row_norm_max(const float* __restrict__ x, uint64_t n, uint32_t D,
+                               float* __restrict__ out) {
+    float best = 0.0f;
+    for (uint64_t i = blockIdx.x * (uint64_t)blockDim.x + threadIdx.x; i < n;
+         i += (uint64_t)gridDim.x * blockDim.x) {
+        const float* r = x + i * D;
+        double s = 0.0;
+        for (uint32_t k = 0; k < D; ++k) s += (double)r[k] * (double)r[k];
+        best = fmaxf(best, (float)s * 1.0000002f);
+    }
+    for (int o = 16; o; o >>= 1) best = fmaxf(best, __shfl_xor_sync(0xffffffffu, best, o));
+    if ((threadIdx.x & 31) == 0) atomicMax(reinterpret_cast<int*>(out), __float_as_int(best));
+}
+
+void launch_row_norm_max(const float* x, uint64_t n, uint32_t D, float* out, cudaStream_t st) {
+    cudaMemsetAsync(out, 0, sizeof(float), st);
+    if (n == 0) return;
+    uint64_t blocks = (n + 255) / 256;
+    if (blocks > 148 * 16) blocks = 148 * 16;
+    TSOM_LAUNCH(k_row_norm_max<<<(unsigned)blocks, 256, 0, st>>>(x, n, D, out));
+}
+
+__global__ void k_fold_max(float* a) { a[0] = fmaxf(a[0], a[1]); }
+
+void launch_fold_max(float* a, cudaStream_t st) { TSOM_LAUNCH(k_fold_max<<<1, 1, 0, st>>>(a)); }
+
+// ---------------------------------------------------------------------------
+// K1 (SIMT): FP32 Gram distances, per-row top-2 over all nodes, flag near-ties
+// ---------------------------------------------------------------------------
+//
+// Block = 256 threads = 16 (node lanes, tx) x 16 (row lanes, ty); tile = 128
+// rows x 64-node chunks.  Thread (tx, ty) owns rows ty*8..+7 and nodes
+// tx*4..+3 of each chunk: 32 FP32 accumulators, 3 LDS.128 per 32 FFMA.
+
+constexpr int SIMT_TM = 128;
+constexpr int SIMT_TN = 64;
+constexpr int SIMT_XS = SIMT_TM + 4;  // padded row stride of the transposed x tile
+
+__device__ __forceinline__ void top2_merge(float& b1, uint32_t& i1, float& b2, float ob1,
+                                           uint32_t oi1, float ob2) {
+    if (ob1 < b1 || (ob1 == b1 && oi1 < i1)) {
+        b2 = fminf(b1, ob2);
+        b1 = ob1;
+        i1 = oi1;
+    } else {
+        b2 = fminf(b2, ob1);
+    }
+}
+
+__global__ void __launch_bounds__(256) k1_bmu_simt(
+    const float* __restrict__ x, const uint32_t* __restrict__ sel, uint64_t n, uint32_t D,
+    const float* __restrict__ wt, uint32_t P, uint32_t Ppad, const float* __restrict__ x2max,
+    const float* __restrict__ w2max, float tau, uint32_t* __restrict__ bmu,
+    uint32_t* __restrict__ flags) {
+    extern __shared__ __align__(16) float sm[];
+    const uint32_t Dp = D + 1;
+    float* xs = sm;                        // [Dp][SIMT_XS]
+    float* ws = sm + (size_t)Dp * SIMT_XS; // [Dp][SIMT_TN]
+    const int tid = threadIdx.x, tx = tid & 15, ty = tid >> 4;
+    const float thr = tau * (__ldg(x2max) + __ldg(w2max));
+
+    for (uint64_t tile = blockIdx.x; tile * SIMT_TM < n; tile += gridDim.x) {
+        const uint64_t row0 = tile * SIMT_TM;
+        __syncthreads();
+        // transposed x tile; column Dp-1 = 1 (multiplies the ||w||^2 row)
+        for (uint32_t e = tid; e < SIMT_TM * D; e += 256) {
+            const uint32_t r = e / D, k = e - r * D;
+            const uint64_t pos = row0 + r;
+            float v = 0.0f;
+            if (pos < n) {
+                const uint64_t row = sel ? (uint64_t)sel[pos] : pos;
+                v = x[row * D + k];
+            }
+            xs[k * SIMT_XS + r] = v;
+        }
+        for (int r = tid; r < SIMT_TM; r += 256) xs[D * SIMT_XS + r] = 1.0f;
+
+        float b1[8], b2[8];
+        uint32_t i1[8];
+#pragma unroll
+        for (int s = 0; s < 8; ++s) {
+            b1[s] = CUDART_INF_F;
+            b2[s] = CUDART_INF_F;
+            i1[s] = 0;
+        }
+        for (uint32_t c0 = 0; c0 < Ppad; c0 += SIMT_TN) {
+            __syncthreads();
+            for (uint32_t e = tid; e < Dp * SIMT_TN; e += 256) {
+                const uint32_t k = e / SIMT_TN, nn = e % SIMT_TN;
+                ws[k * SIMT_TN + nn] = wt[(size_t)k * Ppad + c0 + nn];
+            }
+            __syncthreads();
+            float acc[8][4];
+#pragma unroll
+            for (int s = 0; s < 8; ++s)
+#pragma unroll
+                for (int q = 0; q < 4; ++q) acc[s][q] = 0.0f;
+            for (uint32_t k = 0; k < Dp; ++k) {
+                const float4 xa = *reinterpret_cast<const float4*>(&xs[k * SIMT_XS + ty * 8]);
+                const float4 xb = *reinterpret_cast<const float4*>(&xs[k * SIMT_XS + ty * 8 + 4]);
+                const float4 wv = *reinterpret_cast<const float4*>(&ws[k * SIMT_TN + tx * 4]);
+                const float xr[8] = {xa.x, xa.y, xa.z, xa.w, xb.x, xb.y, xb.z, xb.w};
+                const float wr[4] = {wv.x, wv.y, wv.z, wv.w};
+#pragma unroll
+                for (int s = 0; s < 8; ++s)
+#pragma unroll
+                    for (int q = 0; q < 4; ++q) acc[s][q] = fmaf(xr[s], wr[q], acc[s][q]);
+            }
+#pragma unroll
+            for (int s = 0; s < 8; ++s)
+#pragma unroll
+                for (int q = 0; q < 4; ++q) {
+                    const float v = acc[s][q];
+                    if (v < b2[s]) {
+                        if (v < b1[s]) {
+                            b2[s] = b1[s];
+                            b1[s] = v;
+                            i1[s] = c0 + tx * 4 + q;
+                        } else {
+                            b2[s] = v;
+                        }
+                    }
+                }
+        }
+        // merge the 16 node lanes of each row group (lanes differ in tx only)
+#pragma unroll
+        for (int s = 0; s < 8; ++s) {
+#pragma unroll
+            for (int o = 1; o < 16; o <<= 1) {
+                const float ob1 = __shfl_xor_sync(0xffffffffu, b1[s], o);
+                const uint32_t oi1 = __shfl_xor_sync(0xffffffffu, i1[s], o);
+                const float ob2 = __shfl_xor_sync(0xffffffffu, b2[s], o);
+                top2_merge(b1[s], i1[s], b2[s], ob1, oi1, ob2);
+            }
+        }
+        if (tx == 0) {
+#pragma unroll
+            for (int s = 0; s < 8; ++s) {
+                const uint64_t pos = row0 + ty * 8 + s;
+                if (pos < n) {
+                    bmu[pos] = i1[s];
+                    if (!(b2[s] - b1[s] > thr)) {
+                        const uint32_t slot = atomicAdd(&flags[0], 1u);
+                        flags[1 + slot] = (uint32_t)pos;
+                    }
+                }
+            }
+        }
+    }
+}
+
+void launch_bmu_simt(const float* x, const uint32_t* sel, uint64_t n, uint32_t D, const float* wt,
+                     uint32_t P, uint32_t Ppad, const float* x2max, const float* w2max, float tau,
+                     uint32_t* bmu, uint32_t* flags, int sm_count, cudaStream_t st) {
+    if (n == 0) return;
+    const size_t smem = (size_t)(D + 1) * (SIMT_XS + SIMT_TN) * sizeof(float);
+    static bool attr_set = false;
+    if (!attr_set) {
+        cudaFuncSetAttribute(k1_bmu_simt, cudaFuncAttributeMaxDynamicSharedMemorySize, 200 * 1024);
+        attr_set = true;
+    }
+    uint64_t tiles = (n + SIMT_TM - 1) / SIMT_TM;
+    uint64_t grid = (uint64_t)sm_count * 8;
+    if (grid > tiles) grid = tiles;
+    TSOM_LAUNCH(k1_bmu_simt<<<(unsigned)grid, 256, smem, st>>>(x, sel, n, D, wt, P, Ppad, x2max, w2max, tau, bmu,
+                                                   flags));
+}
+
+// ---------------------------------------------------------------------------
+// Merge per-group top-2 partials of the tcgen05 kernel
+// ---------------------------------------------------------------------------
+
+__global__ void k_merge_partials(const float* __restrict__ part, uint64_t n, uint32_t groups,
+                                 const float* __restrict__ x2max, const float* __restrict__ w2max,
+                                 float tau, uint32_t* __restrict__ bmu,
+                                 uint32_t* __restrict__ flags) {
+    const uint64_t i = blockIdx.x * (uint64_t)blockDim.x + threadIdx.x;
+    if (i >= n) return;
+    const float thr = tau * (__ldg(x2max) + __ldg(w2max));
+    float b1 = CUDART_INF_F, b2 = CUDART_INF_F;
+    uint32_t i1 = 0;
+    for (uint32_t g = 0; g < groups; ++g) {
+        const float* pg = part + (size_t)g * 3 * n;
+        const float ob1 = pg[i];
+        const uint32_t oi1 = __float_as_uint(pg[n + i]);
+        const float ob2 = pg[2 * n + i];
+        top2_merge(b1, i1, b2, ob1, oi1, ob2);
+    }
+    bmu[i] = i1;
+    if (!(b2 - b1 > thr)) {
+        const uint32_t slot = atomicAdd(&flags[0], 1u);
+        flags[1 + slot] = (uint32_t)i;
+    }
+}
+
+void launch_merge_partials(const float* part, uint64_t n, uint32_t groups, const float* x2max,
+                           const float* w2max, float tau, uint32_t* bmu, uint32_t* flags,
+                           cudaStream_t st) {
+    if (n == 0) return;
+    TSOM_LAUNCH(k_merge_partials<<<(unsigned)((n + 255) / 256), 256, 0, st>>>(part, n, groups, x2max, w2max,
+                                                                  tau, bmu, flags));
+}
+
+// ---------------------------------------------------------------------------
+// Exact re-scan (one warp per flagged row), reference order and rounding
+// ---------------------------------------------------------------------------
+
+__global__ void __launch_bounds__(256) k_rescan(const float* __restrict__ x,
+                                                const uint32_t* __restrict__ sel,
+                                                const float* __restrict__ w, uint32_t P,
+                                                uint32_t D, const uint32_t* __restrict__ flags,
+                                                uint32_t* __restrict__ bmu) {
+    extern __shared__ float xrow_all[];
+    const uint32_t count = flags[0];
+    const int lane = threadIdx.x & 31, wib = threadIdx.x >> 5;
+    float* xrow = xrow_all + wib * D;
+    for (uint32_t f = blockIdx.x * 8 + wib; f < count; f += gridDim.x * 8) {
+        const uint32_t pos = flags[1 + f];
+        const uint64_t row = sel ? (uint64_t)sel[pos] : pos;
+        __syncwarp();
+        for (uint32_t k = lane; k < D; k += 32) xrow[k] = x[row * D + k];
+        __syncwarp();
+        double best = CUDART_INF;
+        uint32_t best_j = 0xFFFFFFFFu;
+        for (uint32_t j = lane; j < P; j += 32) {
+            const float* wj = w + (size_t)j * D;
+            double acc = 0.0;
+            for (uint32_t k = 0; k < D; ++k) {
+                const double diff = __dsub_rn((double)xrow[k], (double)wj[k]);
+                acc = __dadd_rn(acc, __dmul_rn(diff, diff));
+            }
+            if (acc < best) {  // ascending j within a lane: strict < keeps lowest
+                best = acc;
+                best_j = j;
+            }
+        }
+        for (int o = 16; o; o >>= 1) {
+            const double ob = __shfl_xor_sync(0xffffffffu, best, o);
+            const uint32_t oj = __shfl_xor_sync(0xffffffffu, best_j, o);
+            if (ob < best || (ob == best && oj < best_j)) {
+                best = ob;
+                best_j = oj;
+            }
+        }
+        if (lane == 0) bmu[pos] = best_j == 0xFFFFFFFFu ? 0u : best_j;
+    }
+}
+
+void launch_rescan(const float* x, const uint32_t* sel, const float* w, uint32_t P, uint32_t D,
+                   const uint32_t* flags, uint64_t n, uint32_t* bmu, cudaStream_t st) {
+    if (n == 0) return;
+    // grid sized for the worst case is wasteful; flagged rows are rare, the
+    // kernel grid-strides over the device-side count.
+    TSOM_LAUNCH(k_rescan<<<148 * 4, 256, 8 * D * sizeof(float), st>>>(x, sel, w, P, D, flags, bmu));
+}
+
+// ---------------------------------------------------------------------------
+// Split (optionally gathered) rows into tcgen05 operand tiles
+// ---------------------------------------------------------------------------
+//
+// Tile t (rows 128t..128t+127) occupies 2*128*56 floats: hi part then lo part,
+// each in K-major core-matrix order ((k/4)*128 + r)*4 + k%4.  Augmented
+// columns: k < D -> x_k, k == D and D+1 -> 1 (pairs with the two ||w||^2
+// pieces), else 0.  Rows past n are zero (their results are ignored).
+
+__global__ void k_split_rows(const float* __restrict__ x, const uint32_t* __restrict__ sel,
+                             uint64_t n, uint32_t D, float* __restrict__ tiles) {
+    const uint64_t tile = blockIdx.x;
+    const int r = threadIdx.x;  // 128 threads, one row each
+    const uint64_t pos = tile * kTcTileM + r;
+    float* base = tiles + tile * 2 * kTcTileM * kTcKPad;
+    const bool valid = pos < n;
+    const float* src = nullptr;
+    if (valid) src = x + (sel ? (uint64_t)sel[pos] : pos) * D;
+    for (uint32_t kc = 0; kc < kTcKPad / 4; ++kc) {
+        float hi[4], lo[4];
+#pragma unroll
+        for (int q = 0; q < 4; ++q) {
+            const uint32_t k = kc * 4 + q;
+            float val;
+            if (!valid)
+                val = 0.0f;
+            else if (k < D)
+                val = src[k];
+            else if (k == D || k == D + 1)
+                val = 1.0f;
+            else
+                val = 0.0f;
+            hi[q] = tf32_hi(val);
+            lo[q] = val - hi[q];
+        }
+        const size_t off = ((size_t)kc * kTcTileM + r) * 4;
+        *reinterpret_cast<float4*>(base + off) = make_float4(hi[0], hi[1], hi[2], hi[3]);
+        *reinterpret_cast<float4*>(base + (size_t)kTcTileM * kTcKPad + off) =
+            make_float4(lo[0], lo[1], lo[2], lo[3]);
+    }
+}
+
+void launch_split_rows(const float* x, const uint32_t* sel, uint64_t n, uint32_t D, float* tiles,
+                       cudaStream_t st) {
+    if (n == 0) return;
+    const uint64_t tiles_n = (n + kTcTileM - 1) / kTcTileM;
+    TSOM_LAUNCH(k_split_rows<<<(unsigned)tiles_n, kTcTileM, 0, st>>>(x, sel, n, D, tiles));
+}
+
+}  // namespace tsom

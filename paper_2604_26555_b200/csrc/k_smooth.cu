@@ -1,0 +1,180 @@
+// k_smooth.cu — K3 neighbourhood smoothing + update, influence, synthetic data.
+//
+//   U_j = eta * ( sum_b h[b][j] S_b  -  w_j * sum_b h[b][j] c_b )
+//   H_j = sum_b h[b][j] c_b
+// (trainer.hpp:318-336 regrouped by BMU; h[b][j] = influence row b, :326),
+// then apply_update (trainer.hpp:341-369).  All in FP64: the GEMM is
+// P x P x (d+1) = 1.07e8 flop per epoch at P=1024, d=50 — noise next to K1.
+#include <cuda_runtime.h>
+#include <math_constants.h>
+
+#include <cstdint>
+
+#include "engine.h"
+
+namespace tsom {
+
+// S_aug[b][k] = R_b[k] + c_b * w_b[k] (k < d), S_aug[b][d] = c_b
+__global__ void k_build_saug(const double* __restrict__ sums, const float* __restrict__ w,
+                             uint32_t P, uint32_t D, double* __restrict__ saug) {
+    const size_t e = blockIdx.x * (size_t)blockDim.x + threadIdx.x;
+    const uint32_t Dp = D + 1;
+    if (e >= (size_t)P * Dp) return;
+    const uint32_t b = (uint32_t)(e / Dp), k = (uint32_t)(e % Dp);
+    const double c = sums[(size_t)P * D + b];
+    saug[e] = k < D ? sums[(size_t)b * D + k] + c * (double)w[(size_t)b * D + k] : c;
+}
+
+// H_j = sum_b infl[b][j] c_b   (one thread per node; coalesced over j)
+__global__ void k_smooth_den(const double* __restrict__ infl, const double* __restrict__ sums,
+                             uint32_t P, uint32_t D, double* __restrict__ H) {
+    const uint32_t j = blockIdx.x * blockDim.x + threadIdx.x;
+    if (j >= P) return;
+    const double* c = sums + (size_t)P * D;
+    double acc = 0.0;
+    for (uint32_t b = 0; b < P; ++b) acc = fma(infl[(size_t)b * P + j], c[b], acc);
+    H[j] = acc;
+}
+
+// U[j][k] = eta * (sum_b infl[b][j] * saug[b][k] - w[j][k] * H_j), k < d.
+// Block: 32 nodes j x 64 columns k; b tiled by 32 through shared memory.
+constexpr int SM_TJ = 32, SM_TB = 32, SM_KG = 8, SM_KC = SM_KG * 8;
+__global__ void __launch_bounds__(256) k_smooth_gemm(const double* __restrict__ infl,
+                                                     const double* __restrict__ saug, uint32_t P,
+                                                     uint32_t D, const float* __restrict__ w,
+                                                     double eta, const double* __restrict__ H,
+                                                     double* __restrict__ U) {
+    __shared__ double hs[SM_TB * SM_TJ];
+    __shared__ double ss[SM_TB * SM_KC];
+    const uint32_t Dp = D + 1;
+    const int tj = threadIdx.x % SM_TJ, kg = threadIdx.x / SM_TJ;
+    const uint32_t j0 = blockIdx.x * SM_TJ, j = j0 + tj;
+    const uint32_t k0 = blockIdx.y * SM_KC;
+    double acc[8];
+#pragma unroll
+    for (int q = 0; q < 8; ++q) acc[q] = 0.0;
+    for (uint32_t b0 = 0; b0 < P; b0 += SM_TB) {
+        __syncthreads();
+        for (int e = threadIdx.x; e < SM_TB * SM_TJ; e += 256) {
+            const uint32_t bb = b0 + e / SM_TJ, jj = j0 + e % SM_TJ;
+            hs[e] = (bb < P && jj < P) ? infl[(size_t)bb * P + jj] : 0.0;
+        }
+        for (int e = threadIdx.x; e < SM_TB * SM_KC; e += 256) {
+            const uint32_t bb = b0 + e / SM_KC, kk = k0 + e % SM_KC;
+            ss[e] = (bb < P && kk < D) ? saug[(size_t)bb * Dp + kk] : 0.0;
+        }
+        __syncthreads();
+#pragma unroll 4
+        for (int bb = 0; bb < SM_TB; ++bb) {
+            const double hv = hs[bb * SM_TJ + tj];
+#pragma unroll
+            for (int q = 0; q < 8; ++q) acc[q] = fma(hv, ss[bb * SM_KC + kg + q * SM_KG], acc[q]);
+        }
+    }
+    if (j >= P) return;
+    const double hj = H[j];
+#pragma unroll
+    for (int q = 0; q < 8; ++q) {
+        const uint32_t k = k0 + kg + q * SM_KG;
+        if (k < D) U[(size_t)j * D + k] = eta * (acc[q] - (double)w[(size_t)j * D + k] * hj);
+    }
+}
+
+void launch_smooth(const double* infl, const double* sums, const float* w, uint32_t P, uint32_t D,
+                   double eta, double* U, double* H, cudaStream_t st) {
+    // saug scratch lives right after U (engine allocates U with room: P*d + P*(d+1))
+    double* saug = U + (size_t)P * D;
+    const size_t n = (size_t)P * (D + 1);
+    TSOM_LAUNCH(k_build_saug<<<(unsigned)((n + 255) / 256), 256, 0, st>>>(sums, w, P, D, saug));
+    TSOM_LAUNCH(k_smooth_den<<<(P + 127) / 128, 128, 0, st>>>(infl, sums, P, D, H));
+    dim3 grid((P + SM_TJ - 1) / SM_TJ, (D + SM_KC - 1) / SM_KC);
+    TSOM_LAUNCH(k_smooth_gemm<<<grid, 256, 0, st>>>(infl, saug, P, D, w, eta, H, U));
+}
+
+// apply_update (trainer.hpp:341-369): H < 1e-12 → node frozen (momentum memory
+// zeroed); else delta = U/H (+ beta*prev); non-finite → numerical fault.
+__global__ void k_apply_update(float* __restrict__ w, float* __restrict__ prev, uint32_t P,
+                               uint32_t D, const double* __restrict__ U,
+                               const double* __restrict__ H, int use_momentum, double momentum,
+                               int* __restrict__ status) {
+    const size_t e = blockIdx.x * (size_t)blockDim.x + threadIdx.x;
+    if (e >= (size_t)P * D) return;
+    const uint32_t j = (uint32_t)(e / D);
+    const double h = H[j];
+    if (h < 1e-12) {
+        if (use_momentum) prev[e] = 0.0f;
+        return;
+    }
+    double delta = U[e] / h;
+    if (use_momentum) delta += momentum * (double)prev[e];
+    const double updated = (double)w[e] + delta;
+    if (!isfinite(delta) || !isfinite(updated)) {
+        atomicMin(status, (int)j);  // lowest failing node, like the reference's loop
+        return;
+    }
+    w[e] = (float)updated;
+    if (use_momentum) prev[e] = (float)delta;
+}
+
+void launch_apply_update(float* w, float* prev, uint32_t P, uint32_t D, const double* U,
+                         const double* H, bool use_momentum, double momentum, int* status,
+                         cudaStream_t st) {
+    const size_t n = (size_t)P * D;
+    TSOM_LAUNCH(k_apply_update<<<(unsigned)((n + 255) / 256), 256, 0, st>>>(w, prev, P, D, U, H,
+                                                                use_momentum ? 1 : 0, momentum,
+                                                                status));
+}
+
+// influence_matrix (topology.hpp:342-364): z = (d*d)*inv, h = z > 57.6 ? 0 : exp(-z)
+__global__ void k_influence(const double* __restrict__ dist, size_t n, double inv,
+                            double* __restrict__ out) {
+    const size_t i = blockIdx.x * (size_t)blockDim.x + threadIdx.x;
+    if (i >= n) return;
+    const double d = dist[i];
+    const double z = __dmul_rn(__dmul_rn(d, d), inv);
+    out[i] = z > 57.6 ? 0.0 : exp(-z);
+}
+
+void launch_influence(const double* dist, size_t n, double inv_two_sigma_sq, double* out,
+                      cudaStream_t st) {
+    TSOM_LAUNCH(k_influence<<<(unsigned)((n + 255) / 256), 256, 0, st>>>(dist, n, inv_two_sigma_sq, out));
+}
+
+// Synthetic Gaussian mixture: component and unit normal noise
+// from a counter-based hash (splitmix64 of (seed, row, k)) + Box-Muller.
+__device__ __forceinline__ uint64_t smix(uint64_t z) {
+    z += 0x9e3779b97f4a7c15ULL;
+    z = (z ^ (z >> 30)) * 0xbf58476d1ce4e5b9ULL;
+    z = (z ^ (z >> 27)) * 0x94d049bb133111ebULL;
+    return z ^ (z >> 31);
+}
+
+__global__ void k_synth_gmm(float* __restrict__ x, uint64_t n, uint32_t D,
+                            const float* __restrict__ centres, uint32_t n_comp, uint64_t seed,
+                            uint64_t row_offset) {
+    const uint64_t i = blockIdx.x * (uint64_t)blockDim.x + threadIdx.x;
+    if (i >= n) return;
+    const uint64_t g = row_offset + i;
+    const uint64_t base = smix(seed ^ smix(g));
+    const uint32_t m = (uint32_t)(base % n_comp);
+    float* row = x + i * D;
+    for (uint32_t k = 0; k < D; k += 2) {
+        const uint64_t h = smix(base + k);
+        const float u1 = 1.0f - (float)(h >> 40) * 0x1.0p-24f;  // (0, 1]
+        const float u2 = (float)(h & 0xFFFFFFu) * 0x1.0p-24f;
+        const float r = sqrtf(-2.0f * logf(u1));
+        float s, c;
+        sincospif(2.0f * u2, &s, &c);
+        row[k] = centres[m * D + k] + r * c;
+        if (k + 1 < D) row[k + 1] = centres[m * D + k + 1] + r * s;
+    }
+}
+
+void launch_synth_gmm(float* x, uint64_t n, uint32_t D, const float* centres, uint32_t n_comp,
+                      uint64_t seed, uint64_t row_offset, cudaStream_t st) {
+    if (n == 0) return;
+    TSOM_LAUNCH(k_synth_gmm<<<(unsigned)((n + 255) / 256), 256, 0, st>>>(x, n, D, centres, n_comp, seed,
+                                                            row_offset));
+}
+
+}  // namespace tsom

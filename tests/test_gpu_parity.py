@@ -1,0 +1,299 @@
+"""GPU parity: the B200 engine (through the C-ABI) against the CPU oracle.
+
+Bars:
+  * BMU indices: bit-exact for every row (near-ties are re-checked in exact FP64);
+  * per-row distances: rtol 1e-12 (FP64, summation order differs);
+  * U, H accumulators of one epoch: rtol 1e-9 of max|U| (FP64 smoothing of
+    FP32-per-CTA residual sums flushed to FP64);
+  * whole runs: codebook relative max-norm <= 1e-4, QE relative <= 1e-5.
+"""
+import math
+import os
+
+import numpy as np
+import pytest
+
+import oracle
+
+pytestmark = pytest.mark.gpu
+
+GOLDEN = os.path.join(os.path.dirname(__file__), "golden")
+KERNELS = [1, 2]  # SIMT, tcgen05
+
+
+@pytest.fixture(scope="module")
+def pkg():
+    import paper_2604_26555_b200 as p
+    return p
+
+
+def engine(pkg, p, d, kernel=0):
+    e = pkg.Engine(p, d)
+    if kernel == 2:
+        from paper_2604_26555_b200 import _lib
+        try:
+            e.set_option(_lib.TSOM_OPT_BMU_KERNEL, 2)
+        except pkg.InvalidArgument:
+            pytest.skip("tcgen05 kernel unsupported for this shape")
+    elif kernel == 1:
+        from paper_2604_26555_b200 import _lib
+        e.set_option(_lib.TSOM_OPT_BMU_KERNEL, 1)
+    return e
+
+
+def rel_maxnorm(a, b):
+    return float(np.max(np.abs(a.astype(np.float64) - b)) / max(np.max(np.abs(b)), 1e-300))
+
+
+# --- reference KATs through the engine -------------------------------------
+
+@pytest.mark.parametrize("kernel", KERNELS)
+def test_find_bmus_kat(pkg, kernel):
+    # test_trainer.cpp:213-222
+    e = engine(pkg, 3, 2, kernel)
+    e.set_codebook(np.array([[0, 0], [5, 0], [0, 5]], np.float32))
+    b, d = e.bmu(np.array([[1, 1], [4.5, 0.5]], np.float32))
+    assert b.tolist() == [0, 1]
+    assert d[0] == pytest.approx(math.sqrt(2.0), rel=1e-14)
+    assert d[1] == pytest.approx(math.sqrt(0.5), rel=1e-14)
+
+
+@pytest.mark.parametrize("kernel", KERNELS)
+def test_bmu_ties_lowest_index(pkg, kernel):
+    # test_trainer.cpp:224-232: equidistant nodes -> node 0, distance 5
+    e = engine(pkg, 3, 1, kernel)
+    e.set_codebook(np.array([[2.0], [2.0], [2.0]], np.float32))
+    b, d = e.bmu(np.array([[7.0]], np.float32))
+    assert b[0] == 0 and d[0] == pytest.approx(5.0)
+
+
+def test_map_samples_and_qe_kats(pkg):
+    # test_trainer.cpp:453-462 and test_metrics.cpp:11-17
+    w = np.array([[0.0], [10.0]], np.float32)
+    b, d = pkg.map_samples(w, np.array([[1.0], [9.0], [4.0]], np.float32))
+    assert b.tolist() == [0, 1, 0] and d[2] == pytest.approx(4.0)
+    assert pkg.quantization_error(np.array([[1.0], [-1.0], [9.0], [12.0]], np.float32), w) == \
+        pytest.approx(1.25)
+    with pytest.raises(ValueError, match="dimension mismatch"):
+        pkg.find_bmus(np.zeros((1, 2), np.float32), np.zeros((2, 3), np.float32))
+
+
+def test_hand_computed_batch_step(pkg):
+    # test_trainer.cpp:246-277: U0 = 1.1, H0 = 1.5, U1 = -1.1, H1 = 1.5
+    e = pkg.Engine(2, 1)
+    e.bind(np.array([[1.0], [9.0]], np.float32))
+    e.set_codebook(np.array([[0.0], [10.0]], np.float32))
+    e.set_influence(np.array([[1.0, 0.5], [0.5, 1.0]]))
+    u, h, _ = e.epoch(0.2)
+    assert u[0, 0] == pytest.approx(1.1, rel=1e-12) and h[0] == pytest.approx(1.5, rel=1e-12)
+    assert u[1, 0] == pytest.approx(-1.1, rel=1e-12) and h[1] == pytest.approx(1.5, rel=1e-12)
+
+
+def test_device_update_hand_step_and_safeguard(pkg):
+    # same step through the device-resident update (apply_update on the GPU):
+    # influence exp(-d^2/2) = 0.5 at d = sqrt(2 ln 2)
+    e = pkg.Engine(2, 1)
+    e.bind(np.array([[1.0], [9.0]], np.float32))
+    e.set_codebook(np.array([[0.0], [10.0]], np.float32))
+    dd = math.sqrt(2 * math.log(2.0))
+    e.set_topology_distance(np.array([[0.0, dd], [dd, 0.0]]))
+    e.train_epoch(0.2, 1.0)
+    w = e.get_codebook()
+    assert w[0, 0] == pytest.approx(1.1 / 1.5, rel=1e-6)
+    assert w[1, 0] == pytest.approx(10.0 - 1.1 / 1.5, rel=1e-6)
+    # H floor (trainer.hpp:349-353): a node with no support does not move
+    e2 = pkg.Engine(2, 1)
+    e2.bind(np.array([[1.0]], np.float32))
+    e2.set_codebook(np.array([[0.0], [100.0]], np.float32))
+    e2.set_topology_distance(np.array([[0.0, 100.0], [100.0, 0.0]]))
+    e2.train_epoch(0.5, 1.0)
+    w2 = e2.get_codebook()
+    assert w2[1, 0] == 100.0 and w2[0, 0] == pytest.approx(1.0)
+
+
+# --- BMU bit-exactness at scale ----------------------------------------------
+
+@pytest.mark.parametrize("kernel", KERNELS)
+@pytest.mark.parametrize("p,n", [(100, 20000), (1024, 20000), (300, 7777)])
+def test_bmu_bit_exact_vs_oracle(pkg, oracle_port, kernel, p, n):
+    x = oracle_port.synth_gmm(n, 50, 2600 + p)
+    w = x[np.linspace(0, n - 1, p).astype(int)] * np.float32(0.9) + np.float32(0.05)
+    e = engine(pkg, p, 50, kernel)
+    e.set_codebook(w)
+    b, d = e.bmu(x)
+    bo, do = oracle_port.find_bmus(x, w)
+    assert (b == bo).all(), f"{int((b != bo).sum())} BMU mismatches"
+    np.testing.assert_allclose(d, do, rtol=1e-12, atol=0)
+
+
+@pytest.mark.parametrize("kernel", KERNELS)
+def test_bmu_exact_ties_and_duplicates(pkg, oracle_port, kernel):
+    """Duplicated codebook rows create exact FP64 ties: lowest index must win."""
+    rng = np.random.default_rng(5)
+    base = rng.standard_normal((64, 50)).astype(np.float32)
+    w = np.concatenate([base, base, base[::-1]], 0)  # every node has an exact twin
+    x = np.concatenate([base + rng.standard_normal((64, 50)).astype(np.float32) * 0.1,
+                        rng.standard_normal((4000, 50)).astype(np.float32)], 0)
+    e = engine(pkg, w.shape[0], 50, kernel)
+    e.set_codebook(w)
+    b, _ = e.bmu(x)
+    bo, _ = oracle_port.find_bmus(x, w)
+    assert (b == bo).all()
+    assert e.last_recheck_count >= x.shape[0]  # every row had an exact tie
+
+
+def test_golden_hot_path(pkg):
+    """Reference outputs (tests/golden/hot_path.npz, made from oracle/_ref)."""
+    g = np.load(os.path.join(GOLDEN, "hot_path.npz"))
+    e = pkg.Engine(100, 50)
+    e.set_codebook(g["w"])
+    b, d = e.bmu(g["x"])
+    assert (b == g["bmu"]).all()
+    np.testing.assert_allclose(d, g["dist"], rtol=1e-12)
+    e.bind(g["x"])
+    e.set_influence(g["infl"])
+    u, h, dist = e.epoch(float(g["eta"]), g["sel"], want_dist=True)
+    scale = np.max(np.abs(g["u"]))
+    assert np.max(np.abs(u - g["u"])) <= 1e-9 * scale
+    np.testing.assert_allclose(h, g["h"], rtol=1e-9)
+    np.testing.assert_allclose(dist, g["sel_dist"], rtol=1e-12)
+
+
+# --- one epoch: accumulators ------------------------------------------------
+
+@pytest.mark.parametrize("kernel", KERNELS)
+@pytest.mark.parametrize("sampling", ["full", "random"])
+def test_epoch_accumulators_vs_oracle(pkg, oracle_port, kernel, sampling):
+    n, p = 30000, 256
+    x = oracle_port.synth_gmm(n, 50, 2611)
+    w = x[np.linspace(0, n - 1, p).astype(int)].copy()
+    infl = oracle_port.influence_from_dist(oracle_port.lattice_dist("hex", 16, 16), 4.0)
+    if sampling == "full":
+        sel = np.arange(n, dtype=np.uint32)
+    else:
+        sel = np.sort(np.random.default_rng(1).choice(n, n // 3, replace=False)).astype(np.uint32)
+    e = engine(pkg, p, 50, kernel)
+    e.bind(x)
+    e.set_codebook(w)
+    e.set_influence(infl)
+    u, h, dist = e.epoch(0.45, sel, want_dist=True)
+    uo, ho, _, _, do = oracle_port.run_iteration(x, sel, w, infl, 0.45, 1, 8)
+    assert np.max(np.abs(u - uo)) <= 1e-9 * np.max(np.abs(uo))
+    np.testing.assert_allclose(h, ho, rtol=1e-9)
+    np.testing.assert_allclose(dist, do, rtol=1e-12)
+
+
+def test_streamed_equals_resident(pkg, oracle_port):
+    n, p = 50000, 128
+    x = oracle_port.synth_gmm(n, 50, 2612)
+    w = x[:p].copy()
+    infl = oracle_port.influence_from_dist(oracle_port.lattice_dist("rect", 16, 8), 3.0)
+    out = []
+    for streamed in (False, True):
+        e = pkg.Engine(p, 50)
+        from paper_2604_26555_b200 import _lib
+        e.set_option(_lib.TSOM_OPT_STREAM_CHUNK, 7000)  # ragged chunks
+        e.bind(x, streamed=streamed)
+        e.set_codebook(w)
+        e.set_influence(infl)
+        sel = np.arange(1, n, 3, dtype=np.uint32)
+        out.append(e.epoch(0.3, sel, want_dist=True))
+    (u0, h0, d0), (u1, h1, d1) = out
+    assert np.max(np.abs(u0 - u1)) <= 1e-10 * np.max(np.abs(u0))
+    np.testing.assert_allclose(h0, h1, rtol=1e-12)
+    np.testing.assert_allclose(d0, d1, rtol=1e-14)
+
+
+# --- error behaviour (the reference's exception types / messages) ----------
+
+def test_errors(pkg):
+    e = pkg.Engine(4, 2)
+    e.bind(np.zeros((10, 2), np.float32))
+    e.set_codebook(np.zeros((4, 2), np.float32))
+    e.set_influence(np.eye(4))
+    with pytest.raises(IndexError, match="fetch_rows: row index beyond data size"):
+        e.epoch(0.1, np.array([3, 10], np.uint32))
+    with pytest.raises(pkg.NumericalFault, match="numerical fault"):
+        e.bind(np.full((10, 2), 3e6, np.float32))
+        e.epoch(2.0)
+    u, h, _ = e.epoch(0.1, np.array([], np.uint32))  # empty selection: zero accumulators
+    assert not u.any() and not h.any()
+
+
+# --- whole runs --------------------------------------------------------------
+
+def test_resident_training_config1_shape(pkg, oracle_port):
+    """Config-1 shape (10x10 rect, D=50, 10 epochs) on 20k rows vs the reference run."""
+    g = np.load(os.path.join(GOLDEN, "config1_20k.npz"))
+    x = oracle_port.synth_gmm(int(g["n"]), 50, int(g["seed"]))
+    cfg = pkg.ResidentConfig(topology="rect", grid_w=10, grid_h=10, n_iters=10,
+                             seed=int(g["seed"]))
+    e = pkg.Engine(100, 50)
+    e.bind(x)
+    w0 = pkg.api.init_sample_draw(x, 100, cfg.seed)
+    log = pkg.train_resident(cfg, e, w0, log_qe=True)
+    w = e.get_codebook()
+    assert rel_maxnorm(w, g["w"]) <= 1e-4
+    qe = np.array([r["qe_train"] for r in log])
+    np.testing.assert_allclose(qe, g["qe"], rtol=1e-5)
+
+
+DROPIN_CONFIGS = [
+    dict(topology="hex", grid_w=4, grid_h=4, n_iters=8, seed=17),
+    dict(topology="mst", nodes=16, n_iters=8, seed=17),
+    dict(topology="rng", nodes=12, n_iters=6, seed=4, sampling="adaptive", rho=0.3),
+    dict(topology="rect", grid_w=5, grid_h=3, n_iters=6, seed=23, sampling="random", rho=0.5,
+         use_momentum=True, momentum=0.4),
+]
+
+
+@pytest.mark.parametrize("kw", DROPIN_CONFIGS, ids=lambda k: f"{k['topology']}")
+def test_dropin_train_vs_golden(pkg, kw):
+    """The reference loop + CudaExecutor vs the reference loop + SerialExecutor."""
+    from paper_2604_26555_b200 import dropin
+    if not dropin.available():
+        pytest.skip("libtsom_dropin.so not built")
+    g = np.load(os.path.join(GOLDEN, "train_runs.npz"))
+    i = DROPIN_CONFIGS.index(kw)
+    cfg = dropin.TrainConfig(**kw)
+    w, qe, _, _ = dropin.train_cuda(cfg, g["x"], log_qe=True)
+    assert rel_maxnorm(w, g[f"w{i}"]) <= 1e-4
+    np.testing.assert_allclose(qe, g[f"qe{i}"], rtol=1e-5)
+
+
+def test_dropin_config1_run(pkg, oracle_port):
+    from paper_2604_26555_b200 import dropin
+    if not dropin.available():
+        pytest.skip("libtsom_dropin.so not built")
+    g = np.load(os.path.join(GOLDEN, "config1_20k.npz"))
+    x = oracle_port.synth_gmm(int(g["n"]), 50, int(g["seed"]))
+    cfg = dropin.TrainConfig(topology="rect", grid_w=10, grid_h=10, n_iters=10,
+                             seed=int(g["seed"]))
+    w, qe, _, _ = dropin.train_cuda(cfg, x, log_qe=True)
+    assert rel_maxnorm(w, g["w"]) <= 1e-4
+    np.testing.assert_allclose(qe, g["qe"], rtol=1e-5)
+
+
+# --- BASELINE-size properties (1e7 x 50, K = 1024) --------------------------
+
+@pytest.mark.slow
+def test_full_size_properties(pkg, oracle_port):
+    n, p = 10_000_000, 1024
+    e = pkg.Engine(p, 50)
+    e.bind_synthetic_gmm(n, 2602)
+    # codebook: 1024 rows of a host GMM sample (same centres)
+    w = oracle_port.synth_gmm(p, 50, 2602) + np.float32(0.01)
+    e.set_codebook(w)
+    dist = pkg.api.lattice_dist("hex", 32, 32)
+    infl = oracle_port.influence_from_dist(dist, 16.0)
+    e.set_influence(infl)
+    u, h, _ = e.epoch(0.5)
+    assert np.isfinite(u).all() and np.isfinite(h).all()
+    s, c = e.qe()
+    assert c == n
+    # checksum of checksums: sum_j H_j = sum_b c_b * sum_j h[b][j]
+    b, _ = e.bmu_bound(None, want_dist=False)
+    counts = np.bincount(b, minlength=p).astype(np.float64)
+    assert counts.sum() == n
+    np.testing.assert_allclose(h, infl.T @ counts, rtol=1e-12)
+    np.testing.assert_allclose(h.sum(), (infl.sum(1) * counts).sum(), rtol=1e-12)
