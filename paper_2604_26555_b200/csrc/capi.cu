@@ -142,9 +142,9 @@ void prep_codebook(Engine* eng) {
     REQUIRE(eng->codebook_set, TSOM_ERR_INVALID, "engine: codebook not set (tsom_set_codebook)");
     if (eng->codebook_prepped) return;
     const bool tc = use_tc(eng);
-    const uint32_t groups = (eng->P + tsom::kTcGroupN - 1) / tsom::kTcGroupN;
-    if (tc)
-        CU(eng->wsplit.ensure((size_t)groups * 2 * tsom::kTcGroupN * tsom::kTcKPad * sizeof(float)));
+    const uint32_t gn = tsom::tc_group_width(eng->P);
+    const uint32_t groups = (eng->P + gn - 1) / gn;
+    if (tc) CU(eng->wsplit.ensure((size_t)groups * 2 * gn * tsom::kTcKPad * sizeof(float)));
     tsom::launch_prep_codebook(eng->w.as<float>(), eng->P, eng->D, eng->w2.as<double>(),
                                eng->w2max.as<float>(), eng->wt.as<float>(), ppad(eng),
                                tc ? eng->wsplit.as<float>() : nullptr, eng->stream);
@@ -159,7 +159,8 @@ void run_bmu(Engine* eng, const float* x, const uint32_t* sel, uint64_t n, const
     CU(cudaMemsetAsync(eng->flags.p, 0, sizeof(uint32_t), eng->stream));
     if (n == 0) return;
     if (use_tc(eng)) {
-        const uint32_t groups = (eng->P + tsom::kTcGroupN - 1) / tsom::kTcGroupN;
+        const uint32_t gn = tsom::tc_group_width(eng->P);
+        const uint32_t groups = (eng->P + gn - 1) / gn;
         if (!tiles) {
             const uint64_t ntiles = (n + tsom::kTcTileM - 1) / tsom::kTcTileM;
             CU(eng->gsplit.ensure(ntiles * 2 * tsom::kTcTileM * tsom::kTcKPad * sizeof(float)));

@@ -7,7 +7,7 @@
 //   w        P x d        f32             codebook (updated in place by the
 //                                         device-resident loop)
 //   wt       (d+1) x Ppad f32             SIMT operand: -2 w^T and ||w||^2 row
-//   ws       P/256 groups of [hi|lo] x [14][256][4] f32  tcgen05 B operand
+//   ws       ceil(P/gn) groups of [hi|lo] x [14][gn][4] f32  tcgen05 B operand (gn <= 256)
 //   infl     P x P        f64             influence h[b][j]
 //   slots    nslot x (P*d + P + 2) f64    per-CTA accumulation partials
 //   sums     P*d + P + 2  f64             reduced [R | c | sum dist | count]
@@ -134,6 +134,10 @@ void launch_fold_max(float* a, cudaStream_t st);
 void launch_split_rows(const float* x, const uint32_t* sel, uint64_t n, uint32_t D, float* tiles,
                        cudaStream_t st);
 bool tc_supported(uint32_t P, uint32_t D);
+// nodes per CTA-resident codebook group (multiple of 16, <= 256)
+__host__ __device__ inline uint32_t tc_group_width(uint32_t P) {
+    return P >= (uint32_t)kTcGroupN ? (uint32_t)kTcGroupN : (P + 15u) / 16u * 16u;
+}
 
 // K1: BMU candidates.  SIMT variant writes final bmu + flags directly.
 void launch_bmu_simt(const float* x, const uint32_t* sel, uint64_t n, uint32_t D, const float* wt,

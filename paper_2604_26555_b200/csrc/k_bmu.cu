@@ -53,8 +53,9 @@ __global__ void k_prep_codebook(const float* __restrict__ w, uint32_t P, uint32_
         // k < D carry -2 w_jk split hi/lo; columns D and D+1 carry ||w_j||^2 as
         // three tf32-exact pieces (p1 hi/p2 lo in column D, p3 hi in column D+1)
         // so the norm enters the MMA with ~33 significant bits.
-        const uint32_t g = j / kTcGroupN, r = j % kTcGroupN;
-        float* base = wsplit + (size_t)g * 2 * kTcGroupN * kTcKPad;
+        const uint32_t gn = tc_group_width(P);
+        const uint32_t g = j / gn, r = j % gn;
+        float* base = wsplit + (size_t)g * 2 * gn * kTcKPad;
         const float p1 = tf32_hi((float)s);
         const float p2 = tf32_hi((float)(s - (double)p1));
         const float p3 = tf32_hi((float)(s - (double)p1 - (double)p2));
@@ -74,9 +75,9 @@ __global__ void k_prep_codebook(const float* __restrict__ w, uint32_t P, uint32_
                 hi = 0.0f;
                 lo = 0.0f;
             }
-            const size_t off = ((size_t)(k / 4) * kTcGroupN + r) * 4 + (k % 4);
+            const size_t off = ((size_t)(k / 4) * gn + r) * 4 + (k % 4);
             base[off] = hi;
-            base[(size_t)kTcGroupN * kTcKPad + off] = lo;
+            base[(size_t)gn * kTcKPad + off] = lo;
         }
     }
 }
@@ -85,14 +86,15 @@ __global__ void k_prep_pad_groups(uint32_t P, uint32_t D, float* __restrict__ ws
                                   uint32_t groups) {
     // padding nodes of the last tcgen05 group: norm column = 3e38 (finite, so
     // 0 * v never makes a NaN inside the MMA), everything else 0 => never wins
+    const uint32_t gn = tc_group_width(P);
     const uint32_t j = P + blockIdx.x * blockDim.x + threadIdx.x;
-    if (j >= groups * kTcGroupN) return;
-    const uint32_t g = j / kTcGroupN, r = j % kTcGroupN;
-    float* base = wsplit + (size_t)g * 2 * kTcGroupN * kTcKPad;
+    if (j >= groups * gn) return;
+    const uint32_t g = j / gn, r = j % gn;
+    float* base = wsplit + (size_t)g * 2 * gn * kTcKPad;
     for (uint32_t k = 0; k < kTcKPad; ++k) {
-        const size_t off = ((size_t)(k / 4) * kTcGroupN + r) * 4 + (k % 4);
+        const size_t off = ((size_t)(k / 4) * gn + r) * 4 + (k % 4);
         base[off] = k == D ? tf32_hi(3.0e38f) : 0.0f;
-        base[(size_t)kTcGroupN * kTcKPad + off] = 0.0f;
+        base[(size_t)gn * kTcKPad + off] = 0.0f;
     }
 }
 
@@ -101,8 +103,9 @@ void launch_prep_codebook(const float* w, uint32_t P, uint32_t D, double* w2, fl
     cudaMemsetAsync(w2max, 0, sizeof(float), st);
     TSOM_LAUNCH(k_prep_codebook<<<(Ppad + 127) / 128, 128, 0, st>>>(w, P, D, w2, w2max, wt, Ppad, wsplit));
     if (wsplit) {
-        const uint32_t groups = (P + kTcGroupN - 1) / kTcGroupN;
-        const uint32_t pad = groups * kTcGroupN - P;
+        const uint32_t gn = tc_group_width(P);
+        const uint32_t groups = (P + gn - 1) / gn;
+        const uint32_t pad = groups * gn - P;
         if (pad) TSOM_LAUNCH(k_prep_pad_groups<<<(pad + 127) / 128, 128, 0, st>>>(P, D, wsplit, groups));
     }
 }

@@ -108,7 +108,8 @@ def test_device_update_hand_step_and_safeguard(pkg):
     e2.set_topology_distance(np.array([[0.0, 100.0], [100.0, 0.0]]))
     e2.train_epoch(0.5, 1.0)
     w2 = e2.get_codebook()
-    assert w2[1, 0] == 100.0 and w2[0, 0] == pytest.approx(1.0)
+    # node 0: H = 1, U = 0.5 * (1 - 0) -> moves halfway; node 1: h = exp(-5000) cut to 0
+    assert w2[1, 0] == 100.0 and w2[0, 0] == pytest.approx(0.5)
 
 
 # --- BMU bit-exactness at scale ----------------------------------------------
