@@ -131,7 +131,8 @@ int tsom_set_topology_distance(tsom_engine* eng, const double* dist);
  * on.  Weights stay on the device (read with tsom_get_codebook). */
 int tsom_train_epoch(tsom_engine* eng, double eta, double sigma, double momentum,
                      uint32_t flags);
-/* Number of rows re-checked in exact FP64 by the last BMU pass (tie window). */
+/* Rows of the last BMU pass whose winner was decided in exact FP64 (several
+ * candidates inside the FP32 error window, or a full re-scan). */
 uint64_t tsom_last_recheck_count(const tsom_engine* eng);
 
 /* Multi-GPU (one process per GPU) ---------------------------------------- */

@@ -135,7 +135,7 @@ bool use_tc(const Engine* e) {
 void ensure_rows(Engine* eng, uint64_t n) {
     CU(eng->bmu.ensure(std::max<uint64_t>(n, 1) * sizeof(uint32_t)));
     CU(eng->dist.ensure(std::max<uint64_t>(n, 1) * sizeof(double)));
-    CU(eng->flags.ensure((std::max<uint64_t>(n, 1) + 1) * sizeof(uint32_t)));
+    CU(eng->flags.ensure((std::max<uint64_t>(n, 1) + 2) * sizeof(uint32_t)));
 }
 
 void prep_codebook(Engine* eng) {
@@ -156,7 +156,7 @@ void prep_codebook(Engine* eng) {
 // `tiles` = pre-split tcgen05 operand for exactly these n rows (or nullptr to build).
 void run_bmu(Engine* eng, const float* x, const uint32_t* sel, uint64_t n, const float* x2max,
              const float* tiles) {
-    CU(cudaMemsetAsync(eng->flags.p, 0, sizeof(uint32_t), eng->stream));
+    CU(cudaMemsetAsync(eng->flags.p, 0, 2 * sizeof(uint32_t), eng->stream));
     if (n == 0) return;
     if (use_tc(eng)) {
         const uint32_t gn = tsom::tc_group_width(eng->P);
@@ -169,12 +169,14 @@ void run_bmu(Engine* eng, const float* x, const uint32_t* sel, uint64_t n, const
         }
         CU(eng->part.ensure((size_t)groups * 3 * n * sizeof(float)));
         CU(cudaEventRecord(eng->ev[8], eng->stream));
-        CU(tsom::launch_bmu_tc(tiles, n, eng->P, eng->wsplit.as<float>(), eng->part.as<float>(),
+        CU(tsom::launch_bmu_tc(tiles, n, eng->P, eng->wsplit.as<float>(), x2max,
+                               eng->w2max.as<float>(), (float)eng->tau_tc, eng->part.as<float>(),
                                eng->sm_count, eng->stream));
         CU(cudaEventRecord(eng->ev[9], eng->stream));
         eng->k1_timed = true;
-        tsom::launch_merge_partials(eng->part.as<float>(), n, groups, x2max, eng->w2max.as<float>(),
-                                    (float)eng->tau_tc, eng->bmu.as<uint32_t>(),
+        tsom::launch_merge_partials(eng->part.as<float>(), n, groups, gn, x2max,
+                                    eng->w2max.as<float>(), (float)eng->tau_tc, x, sel,
+                                    eng->w.as<float>(), eng->D, eng->bmu.as<uint32_t>(),
                                     eng->flags.as<uint32_t>(), eng->stream);
     } else {
         CU(cudaEventRecord(eng->ev[8], eng->stream));
@@ -207,12 +209,27 @@ const uint32_t* normalise_selection(Engine* eng, const uint32_t* sel, uint64_t n
     return sel;
 }
 
-// Accumulate the bound rows (resident or streamed) for one epoch into slots,
-// then reduce (+allreduce) into sums.  dist_dev: per-position distances or null.
+// K2 scratch (counting sort + piece partials) sized for `rows` rows per launch.
+void ensure_accum(Engine* eng, uint64_t rows) {
+    if (rows <= eng->acc_rows && eng->acc.counts) return;
+    size_t bytes[7];
+    tsom::accum_scratch_bytes(rows, eng->P, eng->D, bytes);
+    for (int i = 0; i < 7; ++i) CU(eng->acc_buf[i].ensure(bytes[i]));
+    eng->acc.counts = eng->acc_buf[0].as<uint32_t>();
+    eng->acc.totals = eng->acc_buf[1].as<uint32_t>();
+    eng->acc.node_start = eng->acc_buf[2].as<uint32_t>();
+    eng->acc.piece_start = eng->acc_buf[3].as<uint32_t>();
+    eng->acc.piece_node = eng->acc_buf[4].as<uint32_t>();
+    eng->acc.sorted = eng->acc_buf[5].as<uint32_t>();
+    eng->acc.partial = eng->acc_buf[6].as<double>();
+    eng->acc_rows = rows;
+}
+
+// One pass over the bound rows (resident or streamed): BMU search, then K2
+// into sums = [R | c | sum dist | rows] (+ allreduce).  want_dist: per-row
+// distances into eng->dist; want_dsum: distance sum; accumulate: R and c.
 void accumulate_epoch(Engine* eng, const uint32_t* sel_host, uint64_t n_sel, bool want_dist,
-                      bool accumulate) {
-    const int nslots = tsom::accumulate_slots(eng->P, eng->D, eng->smem_optin, eng->sm_count);
-    CU(eng->slots.ensure((size_t)nslots * slot_len(eng) * sizeof(double)));
+                      bool want_dsum, bool accumulate) {
     CU(eng->sums.ensure(slot_len(eng) * sizeof(double)));
     const uint32_t* sel = normalise_selection(eng, sel_host, n_sel);
     const uint64_t n = sel ? n_sel : eng->n_rows;
@@ -243,27 +260,29 @@ void accumulate_epoch(Engine* eng, const uint32_t* sel_host, uint64_t n_sel, boo
         }
         run_bmu(eng, eng->x.as<float>(), dsel, n, eng->x2max.as<float>(), tiles);
         CU(cudaEventRecord(eng->ev[1], eng->stream));
+        ensure_accum(eng, n);
         tsom::launch_accumulate(eng->x.as<float>(), dsel, n, eng->D, eng->w.as<float>(), eng->P,
                                 eng->bmu.as<uint32_t>(),
-                                want_dist ? eng->dist.as<double>() : nullptr,
-                                eng->slots.as<double>(), nslots, accumulate, true,
-                                eng->smem_optin, eng->stream);
+                                want_dist ? eng->dist.as<double>() : nullptr, want_dsum,
+                                accumulate, true, eng->acc, eng->sums.as<double>(), eng->sm_count,
+                                eng->stream, eng->x_slack);
         CU(cudaGetLastError());
-        eng->chunk_counts.assign(1, 0u);
+        eng->chunk_counts.assign(2, 0u);
         eng->recheck_from_chunks = true;
-        CU(cudaMemcpyAsync(&eng->chunk_counts[0], eng->flags.p, sizeof(uint32_t),
+        CU(cudaMemcpyAsync(&eng->chunk_counts[0], eng->flags.p, 2 * sizeof(uint32_t),
                            cudaMemcpyDeviceToHost, eng->stream));
     } else {
         // Streamed: rows live in host memory; chunks of stream_chunk_rows rows
         // are copied on copy_stream into two device stages, compute on stream.
         const uint64_t C = eng->stream_chunk_rows;
-        CU(eng->stage[0].ensure(C * eng->D * sizeof(float)));
-        CU(eng->stage[1].ensure(C * eng->D * sizeof(float)));
+        CU(eng->stage[0].ensure(C * eng->D * sizeof(float) + tsom::kRowSlack));
+        CU(eng->stage[1].ensure(C * eng->D * sizeof(float) + tsom::kRowSlack));
         CU(eng->x2max.ensure(2 * sizeof(float)));
+        ensure_accum(eng, C);
         uint64_t pos0 = 0;  // selection cursor
         bool first = true;
         const uint64_t nchunks = (eng->n_rows + C - 1) / C;
-        eng->chunk_counts.assign(nchunks, 0u);
+        eng->chunk_counts.assign(2 * nchunks, 0u);
         // events: ev[2+s] = stage s filled, ev[4+s] = stage s consumed.  No host
         // sync inside the loop: the copy stream runs ahead into the free stage
         // while the compute stream works on the other one.
@@ -293,27 +312,24 @@ void accumulate_epoch(Engine* eng, const uint32_t* sel_host, uint64_t n_sel, boo
             const uint32_t* csel = sel ? dsel + p0 : nullptr;
             const uint64_t out0 = sel ? p0 : r0;
             run_bmu(eng, sel ? xbase : xs, csel, cn, xmax, nullptr);
-            CU(cudaMemcpyAsync(&eng->chunk_counts[c], eng->flags.p, sizeof(uint32_t),
+            CU(cudaMemcpyAsync(&eng->chunk_counts[2 * c], eng->flags.p, 2 * sizeof(uint32_t),
                                cudaMemcpyDeviceToHost, eng->stream));
             tsom::launch_accumulate(sel ? xbase : xs, csel, cn, eng->D, eng->w.as<float>(), eng->P,
                                     eng->bmu.as<uint32_t>(),
-                                    want_dist ? eng->dist.as<double>() + out0 : nullptr,
-                                    eng->slots.as<double>(), nslots, accumulate, first,
-                                    eng->smem_optin, eng->stream);
+                                    want_dist ? eng->dist.as<double>() + out0 : nullptr, want_dsum,
+                                    accumulate, first, eng->acc, eng->sums.as<double>(),
+                                    eng->sm_count, eng->stream, true);
             CU(cudaGetLastError());
             CU(cudaEventRecord(eng->ev[4 + s], eng->stream));
             first = false;
             pos0 = p1;
         }
-        if (first) CU(cudaMemsetAsync(eng->slots.p, 0, (size_t)nslots * slot_len(eng) * sizeof(double), eng->stream));
+        if (first) CU(cudaMemsetAsync(eng->sums.p, 0, slot_len(eng) * sizeof(double), eng->stream));
         eng->recheck_from_chunks = true;
         CU(cudaEventRecord(eng->ev[1], eng->stream));
     }
     if (n == 0 && !eng->streamed)
-        CU(cudaMemsetAsync(eng->slots.p, 0, (size_t)nslots * slot_len(eng) * sizeof(double),
-                           eng->stream));
-    tsom::launch_reduce_slots(eng->slots.as<double>(), nslots, slot_len(eng),
-                              eng->sums.as<double>(), eng->stream);
+        CU(cudaMemsetAsync(eng->sums.p, 0, slot_len(eng) * sizeof(double), eng->stream));
     CU(cudaGetLastError());
     if (eng->nccl_comm) {
         ncclResult_t r = g_nccl.allReduce(eng->sums.p, eng->sums.p, slot_len(eng), ncclFloat64, ncclSum,
@@ -346,8 +362,10 @@ void finish_recheck(Engine* eng) {
 }
 
 void smooth(Engine* eng, double eta) {
+    CU(eng->smooth_scratch.ensure(tsom::smooth_scratch_doubles(eng->P, eng->D) * sizeof(double)));
     tsom::launch_smooth(eng->infl.as<double>(), eng->sums.as<double>(), eng->w.as<float>(), eng->P,
-                        eng->D, eta, eng->U.as<double>(), eng->H.as<double>(), eng->stream);
+                        eng->D, eta, eng->U.as<double>(), eng->H.as<double>(),
+                        eng->smooth_scratch.as<double>(), eng->stream);
     CU(cudaGetLastError());
     CU(cudaEventRecord(eng->ev[7], eng->stream));
 }
@@ -401,7 +419,7 @@ int tsom_create(int device, uint32_t nodes, uint32_t dims, tsom_engine** out) {
         CU(eng->x2max.ensure(2 * sizeof(float)));
         CU(cudaMemset(eng->x2max.p, 0, 2 * sizeof(float)));
         CU(eng->infl.ensure(P * P * sizeof(double)));
-        CU(eng->U.ensure((P * D + P * (D + 1)) * sizeof(double)));
+        CU(eng->U.ensure(P * D * sizeof(double)));
         CU(eng->H.ensure(P * sizeof(double)));
         CU(eng->status.ensure(4 * sizeof(int)));
         ensure_rows(eng, 1);
@@ -424,7 +442,8 @@ int tsom_destroy(tsom_engine* eng) {
     for (DevBuf* b : {&eng->x, &eng->xsplit, &eng->x2max, &eng->w, &eng->wt, &eng->wsplit, &eng->w2,
                       &eng->w2max, &eng->prev, &eng->infl, &eng->topo_dist, &eng->sel,
                       &eng->rows_scratch, &eng->gsplit, &eng->bmu, &eng->dist, &eng->part,
-                      &eng->flags, &eng->slots, &eng->sums, &eng->U, &eng->H, &eng->status,
+                      &eng->flags, &eng->acc_buf[0], &eng->acc_buf[1], &eng->acc_buf[2], &eng->acc_buf[3],
+                      &eng->acc_buf[4], &eng->acc_buf[5], &eng->acc_buf[6], &eng->sums, &eng->U, &eng->H, &eng->status, &eng->smooth_scratch,
                       &eng->stage[0], &eng->stage[1]})
         b->release();
     for (auto& ev : eng->ev)
@@ -489,7 +508,8 @@ int tsom_bind_host_data(tsom_engine* eng, const float* rows, uint64_t n_rows, ui
         eng->streamed = false;
         eng->host_rows = nullptr;
         const size_t bytes = n_rows * eng->D * sizeof(float);
-        CU(eng->x.ensure(std::max<size_t>(bytes, 4)));
+        CU(eng->x.ensure(bytes + tsom::kRowSlack));
+        eng->x_slack = true;
         if (bytes) CU(cudaMemcpy(eng->x.p, rows, bytes, cudaMemcpyHostToDevice));
         tsom::launch_row_norm_max(eng->x.as<float>(), n_rows, eng->D, eng->x2max.as<float>(),
                                   eng->stream);
@@ -506,6 +526,7 @@ int tsom_bind_device_data(tsom_engine* eng, const float* d_rows, uint64_t n_rows
         eng->x.p = const_cast<float*>(d_rows);
         eng->x.bytes = n_rows * eng->D * sizeof(float);
         eng->x.owned = false;
+        eng->x_slack = false;
         eng->n_rows = n_rows;
         eng->streamed = false;
         eng->xsplit_valid = false;
@@ -533,7 +554,8 @@ int tsom_bind_synthetic_gmm(tsom_engine* eng, uint64_t n_rows, uint64_t seed, ui
         CU(dc.ensure(centres.size() * sizeof(float)));
         CU(cudaMemcpy(dc.p, centres.data(), centres.size() * sizeof(float), cudaMemcpyHostToDevice));
         const size_t bytes = n_rows * eng->D * sizeof(float);
-        CU(eng->x.ensure(std::max<size_t>(bytes, 4)));
+        CU(eng->x.ensure(bytes + tsom::kRowSlack));
+        eng->x_slack = true;
         tsom::launch_synth_gmm(eng->x.as<float>(), n_rows, eng->D, dc.as<float>(), n_comp, seed,
                                row_offset, eng->stream);
         CU(cudaGetLastError());
@@ -597,7 +619,7 @@ int tsom_epoch(tsom_engine* eng, const uint32_t* selected, uint64_t n_sel, doubl
         REQUIRE(eng->n_rows > 0 || (selected && n_sel == 0) || eng->nccl_comm, TSOM_ERR_INVALID,
                 "epoch: no data bound");
         prep_codebook(eng);
-        accumulate_epoch(eng, selected, n_sel, dist_out != nullptr, true);
+        accumulate_epoch(eng, selected, n_sel, dist_out != nullptr, false, true);
         smooth(eng, eta);
         const size_t P = eng->P, D = eng->D;
         if (u_out)
@@ -623,31 +645,32 @@ int tsom_bmu(tsom_engine* eng, const float* rows, uint64_t n, uint32_t* bmu, dou
         REQUIRE(rows || n == 0, TSOM_ERR_INVALID, "find_bmus: null rows");
         prep_codebook(eng);
         if (n == 0) return;
-        CU(eng->rows_scratch.ensure(n * eng->D * sizeof(float)));
+        CU(eng->rows_scratch.ensure(n * eng->D * sizeof(float) + tsom::kRowSlack));
         CU(cudaMemcpyAsync(eng->rows_scratch.p, rows, n * eng->D * sizeof(float),
                            cudaMemcpyHostToDevice, eng->stream));
         ensure_rows(eng, n);
-        const int nslots = tsom::accumulate_slots(eng->P, eng->D, eng->smem_optin, eng->sm_count);
-        CU(eng->slots.ensure((size_t)nslots * slot_len(eng) * sizeof(double)));
+        CU(eng->sums.ensure(slot_len(eng) * sizeof(double)));
         float* xm = eng->x2max.as<float>() + 1;
         tsom::launch_row_norm_max(eng->rows_scratch.as<float>(), n, eng->D, xm, eng->stream);
         run_bmu(eng, eng->rows_scratch.as<float>(), nullptr, n, xm, nullptr);
-        if (dist)
+        if (dist) {
+            ensure_accum(eng, n);
             tsom::launch_accumulate(eng->rows_scratch.as<float>(), nullptr, n, eng->D,
                                     eng->w.as<float>(), eng->P, eng->bmu.as<uint32_t>(),
-                                    eng->dist.as<double>(), eng->slots.as<double>(), nslots, false,
-                                    true, eng->smem_optin, eng->stream);
+                                    eng->dist.as<double>(), false, false, true, eng->acc,
+                                    eng->sums.as<double>(), eng->sm_count, eng->stream, true);
+        }
         CU(cudaGetLastError());
         CU(cudaMemcpyAsync(bmu, eng->bmu.p, n * sizeof(uint32_t), cudaMemcpyDeviceToHost,
                            eng->stream));
         if (dist)
             CU(cudaMemcpyAsync(dist, eng->dist.p, n * sizeof(double), cudaMemcpyDeviceToHost,
                                eng->stream));
-        uint32_t cnt = 0;
-        CU(cudaMemcpyAsync(&cnt, eng->flags.p, sizeof(uint32_t), cudaMemcpyDeviceToHost,
+        uint32_t cnt[2] = {0, 0};
+        CU(cudaMemcpyAsync(cnt, eng->flags.p, 2 * sizeof(uint32_t), cudaMemcpyDeviceToHost,
                            eng->stream));
         CU(cudaStreamSynchronize(eng->stream));
-        eng->last_recheck = cnt;
+        eng->last_recheck = (uint64_t)cnt[0] + cnt[1];
     });
 }
 
@@ -656,7 +679,7 @@ int tsom_bmu_bound(tsom_engine* eng, const uint32_t* selected, uint64_t n_sel, u
     return guarded(eng, [&] {
         CU(cudaSetDevice(eng->device));
         REQUIRE(!eng->streamed, TSOM_ERR_INVALID, "bmu_bound: resident data only");
-        accumulate_epoch(eng, selected, n_sel, dist != nullptr, false);
+        accumulate_epoch(eng, selected, n_sel, dist != nullptr, false, false);
         const uint64_t n = selected ? n_sel : eng->n_rows;
         if (n) {
             CU(cudaMemcpyAsync(bmu, eng->bmu.p, n * sizeof(uint32_t), cudaMemcpyDeviceToHost,
@@ -673,7 +696,7 @@ int tsom_qe(tsom_engine* eng, const uint32_t* selected, uint64_t n_sel, double* 
             uint64_t* count) {
     return guarded(eng, [&] {
         CU(cudaSetDevice(eng->device));
-        accumulate_epoch(eng, selected, n_sel, false, false);
+        accumulate_epoch(eng, selected, n_sel, false, true, false);
         double tail[2] = {0, 0};
         CU(cudaMemcpyAsync(tail, eng->sums.as<double>() + (size_t)eng->P * eng->D + eng->P,
                            2 * sizeof(double), cudaMemcpyDeviceToHost, eng->stream));
@@ -717,7 +740,7 @@ int tsom_train_epoch(tsom_engine* eng, double eta, double sigma, double momentum
             eng->max_h = 1.0;
         }
         prep_codebook(eng);
-        accumulate_epoch(eng, nullptr, eng->n_rows, false, true);
+        accumulate_epoch(eng, nullptr, eng->n_rows, false, false, true);
         smooth(eng, eta);
         int ok = INT_MAX;
         CU(cudaMemcpyAsync(eng->status.p, &ok, sizeof(int), cudaMemcpyHostToDevice, eng->stream));

@@ -9,7 +9,8 @@
 //   wt       (d+1) x Ppad f32             SIMT operand: -2 w^T and ||w||^2 row
 //   ws       ceil(P/gn) groups of [hi|lo] x [14][gn][4] f32  tcgen05 B operand (gn <= 256)
 //   infl     P x P        f64             influence h[b][j]
-//   slots    nslot x (P*d + P + 2) f64    per-CTA accumulation partials
+//   sorted   n u32                        row positions in BMU order (counting sort)
+//   partial  pieces x (d+1) f64           per-piece (<= 256 rows) FP64 residual sums
 //   sums     P*d + P + 2  f64             reduced [R | c | sum dist | count]
 //                                         (the one allreduce buffer)
 //   U, H     P*d, P       f64             smoothed accumulators (K3 output)
@@ -55,6 +56,16 @@ constexpr int kTcTileM = 128;   // samples per tcgen05 tile (TMEM lanes)
 constexpr int kTcGroupN = 256;  // nodes per CTA-resident codebook group
 constexpr int kTcKPad = 56;     // d + 1 (norm column) padded to 7 tf32 k-steps
 
+// K2: counting sort by BMU + per-piece FP64 gather accumulation (k_accum.cu).
+struct AccumScratch {
+    uint32_t* counts = nullptr;      // [nblk][P] histograms -> offsets
+    uint32_t* totals = nullptr;      // [P]
+    uint32_t* node_start = nullptr;  // [P+1]
+    uint32_t* piece_start = nullptr; // [P+1]
+    uint32_t* piece_node = nullptr;  // [pieces]
+    uint32_t* sorted = nullptr;      // [n] positions in BMU order
+    double* partial = nullptr;       // [pieces][d+1]
+};
 struct Engine {
     int device = 0;
     uint32_t P = 0, D = 0;
@@ -73,6 +84,7 @@ struct Engine {
     // bound data
     DevBuf x;           // resident rows
     uint64_t n_rows = 0;
+    bool x_slack = false;  // kRowSlack bytes readable after the last resident row
     bool streamed = false;
     const float* host_rows = nullptr;  // streamed mode source
     bool host_registered = false;
@@ -99,10 +111,13 @@ struct Engine {
     DevBuf bmu;
     DevBuf dist;
     DevBuf part;           // tcgen05 per-group partial top-2 [groups][n] (b1, i1, b2)
-    DevBuf flags;          // [0] = count, then positions
-    DevBuf slots;
+    DevBuf flags;          // [0] full re-scan count, [1] exact-candidate count, then positions
+    DevBuf acc_buf[7];     // AccumScratch arrays
+    tsom::AccumScratch acc;
+    uint64_t acc_rows = 0; // capacity the scratch was sized for
     DevBuf sums;
     DevBuf U, H;
+    DevBuf smooth_scratch;   // saug + split-b GEMM partials
     DevBuf status;         // device error word(s)
     DevBuf stage[2];       // streamed-mode device chunks
     float* pinned[2] = {nullptr, nullptr};
@@ -136,7 +151,7 @@ void launch_split_rows(const float* x, const uint32_t* sel, uint64_t n, uint32_t
 bool tc_supported(uint32_t P, uint32_t D);
 // nodes per CTA-resident codebook group (multiple of 16, <= 256)
 __host__ __device__ inline uint32_t tc_group_width(uint32_t P) {
-    return P >= (uint32_t)kTcGroupN ? (uint32_t)kTcGroupN : (P + 15u) / 16u * 16u;
+    return P >= (uint32_t)kTcGroupN ? (uint32_t)kTcGroupN : (P + 31u) / 32u * 32u;
 }
 
 // K1: BMU candidates.  SIMT variant writes final bmu + flags directly.
@@ -145,27 +160,33 @@ void launch_bmu_simt(const float* x, const uint32_t* sel, uint64_t n, uint32_t D
                      uint32_t* bmu, uint32_t* flags, int sm_count, cudaStream_t st);
 // tcgen05 variant writes per-group partials; merge writes bmu + flags.
 cudaError_t launch_bmu_tc(const float* tiles, uint64_t n, uint32_t P, const float* wsplit,
-                          float* part, int sm_count, cudaStream_t st);
-void launch_merge_partials(const float* part, uint64_t n, uint32_t groups, const float* x2max,
-                           const float* w2max, float tau, uint32_t* bmu, uint32_t* flags,
-                           cudaStream_t st);
+                          const float* x2max, const float* w2max, float tau, float* part,
+                          int sm_count, cudaStream_t st);
+// Merge per-group candidates: unique candidate -> bmu; several -> exact FP64
+// evaluation of just those nodes (reference order); overflow -> flags list.
+void launch_merge_partials(const float* part, uint64_t n, uint32_t groups, uint32_t gn,
+                           const float* x2max, const float* w2max, float tau, const float* x,
+                           const uint32_t* sel, const float* w, uint32_t D, uint32_t* bmu,
+                           uint32_t* flags, cudaStream_t st);
 // exact FP64 re-scan of flagged rows (reference loop order)
 void launch_rescan(const float* x, const uint32_t* sel, const float* w, uint32_t P, uint32_t D,
                    const uint32_t* flags, uint64_t n, uint32_t* bmu, cudaStream_t st);
 
-// K2: accumulation of residual sums per BMU + counts + exact distances.
-//     accumulate=false → distances / distance sum only.
+void accum_scratch_bytes(uint64_t n, uint32_t P, uint32_t D, size_t out[7]);
+// sums = [R (P*d) | c (P) | sum dist | rows]; first=false adds to it (streamed chunks).
+// accumulate=false -> distances / distance sum only (QE, find_bmus).
 void launch_accumulate(const float* x, const uint32_t* sel, uint64_t n, uint32_t D,
                        const float* w, uint32_t P, const uint32_t* bmu, double* dist_out,
-                       double* slots, int nslots, bool accumulate, bool first_pass,
-                       size_t smem_optin, cudaStream_t st);
-int accumulate_slots(uint32_t P, uint32_t D, size_t smem_optin, int sm_count);
-void launch_reduce_slots(const double* slots, int nslots, size_t len, double* sums,
-                         cudaStream_t st);
+                       bool want_dist_sum, bool accumulate, bool first, const AccumScratch& s,
+                       double* sums, int sm_count, cudaStream_t st, bool x_slack = false);
+// bytes of slack the engine allocates after resident rows (TMA row gathers read
+// up to 16 bytes past a row)
+constexpr size_t kRowSlack = 64;
 
 // K3: smoothing num = H^T S, den = H^T c; U = eta (num - w den), H = den
 void launch_smooth(const double* infl, const double* sums, const float* w, uint32_t P, uint32_t D,
-                   double eta, double* U, double* H, cudaStream_t st);
+                   double eta, double* U, double* H, double* scratch, cudaStream_t st);
+size_t smooth_scratch_doubles(uint32_t P, uint32_t D);
 // apply_update on device (trainer.hpp:341-369); status[0] = first bad node + 1
 void launch_apply_update(float* w, float* prev, uint32_t P, uint32_t D, const double* U,
                          const double* H, bool use_momentum, double momentum, int* status,

@@ -33,7 +33,8 @@ namespace tsom {
 
 namespace {
 
-constexpr int kThreads = 256;
+constexpr int kThreads = 384;          // 4 role warps + 8 epilogue warps
+constexpr uint32_t kEpiThreads = 256;
 constexpr int kStages = 2;
 constexpr uint32_t kTileBytes = 2u * kTcTileM * kTcKPad * 4u;  // 57,344 (hi + lo)
 constexpr uint32_t kHalfTile = kTcTileM * kTcKPad * 4u;         // 28,672
@@ -143,25 +144,41 @@ __device__ __forceinline__ void tmem_wait_ld() {
     asm volatile("tcgen05.wait::ld.sync.aligned;" ::: "memory");
 }
 
-__device__ __forceinline__ void top2(float v, uint32_t j, float& b1, uint32_t& i1, float& b2) {
-    // nodes arrive in ascending j: strict < keeps the lowest index on ties,
-    // and an exact tie lands in b2 (gap 0 => re-checked)
-    if (v < b2) {
-        if (v < b1) {
-            b2 = b1;
-            b1 = v;
-            i1 = j;
-        } else {
-            b2 = v;
-        }
+}  // namespace
+
+__device__ __forceinline__ void named_bar(uint32_t id, uint32_t nthreads) {
+    asm volatile("bar.sync %0, %1;" ::"r"(id), "r"(nthreads) : "memory");
+}
+
+// branch-free top-2 step: strict < keeps the earliest j on ties, an exact tie
+// lands in b2 (gap 0 => candidate enumeration)
+__device__ __forceinline__ void top2_step(float v, uint32_t j, float& b1, uint32_t& i1,
+                                          float& b2) {
+    const float nb1 = fminf(b1, v);
+    b2 = fminf(b2, fmaxf(b1, v));
+    i1 = v < b1 ? j : i1;
+    b1 = nb1;
+}
+
+__device__ __forceinline__ void top2_merge_dev(float& b1, uint32_t& i1, float& b2, float ob1,
+                                               uint32_t oi1, float ob2) {
+    if (ob1 < b1 || (ob1 == b1 && oi1 < i1)) {
+        b2 = fminf(b1, ob2);
+        b1 = ob1;
+        i1 = oi1;
+    } else {
+        b2 = fminf(b2, ob1);
     }
 }
 
-}  // namespace
+// Candidate list of one (row, group): up to 4 local node indices (8 bits each)
+// whose computed value lies within thr of the group's best; count 15 = overflow.
+constexpr uint32_t kCandOverflow = 15u;
 
 __global__ void __launch_bounds__(kThreads, 1)
     k1_bmu_tc(const float* __restrict__ tiles, uint64_t n, uint32_t ntiles, uint32_t groups,
-              uint32_t gn, const float* __restrict__ wsplit, float* __restrict__ part) {
+              uint32_t gn, const float* __restrict__ wsplit, const float* __restrict__ x2max,
+              const float* __restrict__ w2max, float tau, float* __restrict__ part) {
     extern __shared__ __align__(1024) uint8_t smem[];
     const uint32_t w_bytes = 2u * kTcKPad * gn * 4u;  // hi + lo of this CTA's group
     uint8_t* sW = smem;
@@ -173,6 +190,7 @@ __global__ void __launch_bounds__(kThreads, 1)
     uint64_t* tempty_bar = bars + 6;  // [2] accumulator drained
     uint64_t* w_bar = bars + 8;       // codebook group landed
     uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(bars + 9);
+    uint32_t* xch = reinterpret_cast<uint32_t*>(bars + 10);  // [4 quarters][160]
 
     const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
     const uint32_t g = blockIdx.x % groups;
@@ -187,7 +205,7 @@ __global__ void __launch_bounds__(kThreads, 1)
         }
         for (int a = 0; a < 2; ++a) {
             mbar_init(&tfull_bar[a], 1);
-            mbar_init(&tempty_bar[a], 128);
+            mbar_init(&tempty_bar[a], kEpiThreads);
         }
         mbar_init(w_bar, 1);
         asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
@@ -205,7 +223,7 @@ __global__ void __launch_bounds__(kThreads, 1)
 
     if (warp == 0) {
         if (lane == 0) {
-            // resident codebook group (one bulk copy per hi/lo half keeps each < 2^20 B)
+            // resident codebook group (hi and lo halves, each < 2^20 B of tx count)
             mbar_expect_tx(w_bar, w_bytes);
             const float* wg = wsplit + (size_t)g * 2 * kTcKPad * gn;
             bulk_g2s(sW, wg, w_bytes / 2, w_bar);
@@ -260,39 +278,114 @@ __global__ void __launch_bounds__(kThreads, 1)
             }
         }
     } else if (warp >= 4) {
-        const uint32_t q = warp & 3;  // TMEM lane quarter this warp may access
+        // 8 epilogue warps: quarter q = TMEM lanes 32q..32q+31 (= tile rows), half h
+        // = which half of the group's columns.  Thread = row: top-2 is thread-local.
+        const uint32_t q = warp & 3, h = (warp - 4) >> 2;
         const uint32_t row = q * 32 + lane;
-        const uint32_t jbase = g * gn;
+        const uint32_t half_cols = gn >> 1;  // multiple of 16
+        const uint32_t c0 = h * half_cols;
+        const float thr = tau * (__ldg(x2max) + __ldg(w2max));
+        uint32_t* xq = xch + q * 160;  // [b1 | i1 | b2] x 32 lanes
+        uint32_t* xp = xq + 96;        // [pack | cnt] x 32 lanes
         uint32_t acc = 0, acc_phase = 0;
         for (uint32_t t = cta_in_group; t < ntiles; t += ctas_per_group) {
             mbar_wait(&tfull_bar[acc], acc_phase);
             tc_fence_after();
-            const uint32_t taddr = tmem_base + ((q * 32u) << 16) + acc * acc_cols;
-            float b1 = CUDART_INF_F, b2 = CUDART_INF_F;
-            uint32_t i1 = 0;
+            const uint32_t taddr = tmem_base + ((q * 32u) << 16) + acc * acc_cols + c0;
+            // pass 1: four independent top-2 streams (ILP), then fold
+            float b1[4], b2[4];
+            uint32_t i1[4];
+#pragma unroll
+            for (int s = 0; s < 4; ++s) {
+                b1[s] = CUDART_INF_F;
+                b2[s] = CUDART_INF_F;
+                i1[s] = 0;
+            }
             uint32_t c = 0;
-            for (; c + 32 <= gn; c += 32) {
+            for (; c + 32 <= half_cols; c += 32) {
                 uint32_t r[32];
                 TMEM_LD32(taddr + c, r);
                 tmem_wait_ld();
 #pragma unroll
-                for (int k = 0; k < 32; ++k) top2(__uint_as_float(r[k]), jbase + c + k, b1, i1, b2);
+                for (int k = 0; k < 32; ++k)
+                    top2_step(__uint_as_float(r[k]), c0 + c + k, b1[k & 3], i1[k & 3], b2[k & 3]);
             }
-            if (c < gn) {  // gn is a multiple of 16
+            if (c < half_cols) {
                 uint32_t r[16];
                 TMEM_LD16(taddr + c, r);
                 tmem_wait_ld();
 #pragma unroll
-                for (int k = 0; k < 16; ++k) top2(__uint_as_float(r[k]), jbase + c + k, b1, i1, b2);
+                for (int k = 0; k < 16; ++k)
+                    top2_step(__uint_as_float(r[k]), c0 + c + k, b1[k & 3], i1[k & 3], b2[k & 3]);
+            }
+#pragma unroll
+            for (int s = 1; s < 4; ++s) top2_merge_dev(b1[0], i1[0], b2[0], b1[s], i1[s], b2[s]);
+            float B1 = b1[0], B2 = b2[0];
+            uint32_t I1 = i1[0];
+            // fold the two column halves through shared memory
+            if (h == 1) {
+                xq[lane] = __float_as_uint(B1);
+                xq[32 + lane] = I1;
+                xq[64 + lane] = __float_as_uint(B2);
+            }
+            named_bar(1 + q, 64);
+            if (h == 0) {
+                top2_merge_dev(B1, I1, B2, __uint_as_float(xq[lane]), xq[32 + lane],
+                               __uint_as_float(xq[64 + lane]));
+                xq[lane] = __float_as_uint(B1);
+                xq[32 + lane] = I1;
+                xq[64 + lane] = __float_as_uint(B2);
+            }
+            named_bar(1 + q, 64);
+            if (h == 1) {
+                B1 = __uint_as_float(xq[lane]);
+                I1 = xq[32 + lane];
+                B2 = __uint_as_float(xq[64 + lane]);
+            }
+            // pass 2 (rare): enumerate this half's candidates v <= B1 + thr, ascending j
+            const bool need = !(B2 - B1 > thr);
+            uint32_t pack = 0, cnt = 0;
+            if (__any_sync(0xffffffffu, need)) {
+                const float lim = B1 + thr;
+                for (uint32_t cc = 0; cc < half_cols; cc += 16) {
+                    uint32_t r[16];
+                    TMEM_LD16(taddr + cc, r);
+                    tmem_wait_ld();
+#pragma unroll
+                    for (int k = 0; k < 16; ++k) {
+                        if (need && __uint_as_float(r[k]) <= lim) {
+                            if (cnt < 4) pack |= (c0 + cc + k) << (8 * cnt);
+                            ++cnt;
+                        }
+                    }
+                }
             }
             tc_fence_before();
-            mbar_arrive(&tempty_bar[acc]);
-            const uint64_t pos = (uint64_t)t * kTcTileM + row;
-            if (pos < n) {
-                float* pg = part + (size_t)g * 3 * n;
-                pg[pos] = b1;
-                pg[n + pos] = __uint_as_float(i1);
-                pg[2 * n + pos] = b2;
+            mbar_arrive(&tempty_bar[acc]);  // this thread is done with the accumulator
+            if (h == 1) {
+                xp[lane] = pack;
+                xp[32 + lane] = cnt;
+            }
+            named_bar(1 + q, 64);
+            if (h == 0) {
+                uint32_t out_pack = I1, out_cnt = 1;
+                if (need) {
+                    const uint32_t p1 = xp[lane], n1 = xp[32 + lane];
+                    const uint32_t total = cnt + n1;
+                    if (cnt > 4 || n1 > 4 || total > 4 || total == 0) {
+                        out_cnt = kCandOverflow;
+                    } else {
+                        out_pack = pack | (n1 ? (p1 << (8 * cnt)) : 0u);
+                        out_cnt = total;
+                    }
+                }
+                const uint64_t pos = (uint64_t)t * kTcTileM + row;
+                if (pos < n) {
+                    float* pg = part + (size_t)g * 3 * n;
+                    pg[pos] = B1;
+                    pg[n + pos] = __uint_as_float(out_pack);
+                    pg[2 * n + pos] = __uint_as_float(out_cnt);
+                }
             }
             if (++acc == 2) {
                 acc = 0;
@@ -312,7 +405,8 @@ __global__ void __launch_bounds__(kThreads, 1)
 bool tc_supported(uint32_t P, uint32_t D) { return P >= 1 && D + 2 <= (uint32_t)kTcKPad; }
 
 cudaError_t launch_bmu_tc(const float* tiles, uint64_t n, uint32_t P, const float* wsplit,
-                          float* part, int sm_count, cudaStream_t st) {
+                          const float* x2max, const float* w2max, float tau, float* part,
+                          int sm_count, cudaStream_t st) {
     if (n == 0) return cudaSuccess;
     const uint32_t gn = tc_group_width(P);
     const uint32_t groups = (P + gn - 1) / gn;
@@ -322,7 +416,7 @@ cudaError_t launch_bmu_tc(const float* tiles, uint64_t n, uint32_t P, const floa
     if (per_group > ntiles) per_group = ntiles;
     const uint32_t grid = per_group * groups;
     const uint32_t w_bytes = 2u * kTcKPad * gn * 4u;
-    const size_t smem = ((w_bytes + 1023u) & ~1023u) + kStages * kTileBytes + 128;
+    const size_t smem = ((w_bytes + 1023u) & ~1023u) + kStages * kTileBytes + 80 + 4 * 160 * 4;
     static size_t attr = 0;
     if (attr < smem) {
         cudaError_t e =
@@ -330,7 +424,8 @@ cudaError_t launch_bmu_tc(const float* tiles, uint64_t n, uint32_t P, const floa
         if (e != cudaSuccess) return e;
         attr = smem;
     }
-    TSOM_LAUNCH(k1_bmu_tc<<<grid, kThreads, smem, st>>>(tiles, n, ntiles, groups, gn, wsplit, part));
+    TSOM_LAUNCH(k1_bmu_tc<<<grid, kThreads, smem, st>>>(tiles, n, ntiles, groups, gn, wsplit, x2max,
+                                                        w2max, tau, part));
     return cudaGetLastError();
 }
 

@@ -5,11 +5,21 @@
 // Algebra: the reference folds eta*h[b][j]*(x - w_j) for
 // every sample and every node.  Grouping the samples by BMU b gives
 //   U_j = eta * sum_b h[b][j] * (S_b - c_b w_j),   H_j = sum_b h[b][j] c_b
-// with S_b = sum_{i: b_i = b} x_i and c_b = #{i: b_i = b}.  This kernel builds
-// (R_b = sum (x_i - w_b), c_b) — residuals keep FP32 partial sums well
-// conditioned — in shared memory per CTA, then flushes each CTA's partials to
-// its own FP64 slot (no global atomics, deterministic final reduce).  The
-// smoothing GEMM (k_smooth.cu) forms S_b = R_b + c_b w_b in FP64.
+// with S_b = sum_{i: b_i = b} x_i and c_b = #{i: b_i = b}.  K2 produces the
+// residual sums R_b = sum (x_i - w_b) (exact FP64 terms) and c_b; the
+// smoothing GEMM (k_smooth.cu) forms S_b = R_b + c_b w_b.
+//
+// Pipeline (all deterministic, no floating-point atomics):
+//   k_hist      block-local BMU histograms            [nblk][P]
+//   k_colscan   per-node exclusive scan over blocks   (in place) + node totals
+//   k_nodescan  node starts, counts c_b, piece table  (one block)
+//   k_scatter   stable counting sort of row positions by BMU
+//   k_gather    one warp per piece (<= 256 rows of one node): x rows gathered
+//               in batches of 8, FP64 register accumulation, optional exact
+//               distances; one partial row per piece
+//   k_piece_reduce  sums the pieces of every node in order -> sums buffer
+// HBM traffic per row: ~4 B x 3 (bmu passes) + 8 B (sorted position) + the
+// 200 B row => ~212 B/row (204 B algorithmic).
 #include <cuda_runtime.h>
 
 #include <cstdint>
@@ -18,184 +28,506 @@
 
 namespace tsom {
 
-constexpr int ACC_THREADS = 1024;
-constexpr int ACC_WARPS = ACC_THREADS / 32;
-constexpr uint64_t kMaxRowsPerSlotPass = 1u << 16;  // FP32 partials cover <= 65536 rows
+constexpr uint32_t kHistRows = 16384;   // rows per histogram / scatter block
+constexpr int kScatterWarps = 8;        // sub-chunks of 2048 rows
+constexpr uint32_t kPieceRows = 256;    // rows per gather task (one warp)
+constexpr int kGatherBatch = 16;
 
-// Shared-memory privatised variant: smem = R[P*D] f32 + c[P] u32.
-__global__ void __launch_bounds__(ACC_THREADS, 1) k_accumulate_smem(
-    const float* __restrict__ x, const uint32_t* __restrict__ sel, uint64_t n, uint32_t D,
-    const float* __restrict__ w, uint32_t P, const uint32_t* __restrict__ bmu,
-    double* __restrict__ dist_out, double* __restrict__ slots, uint64_t rows_per_cta,
-    int accumulate, int first_pass) {
-    extern __shared__ float smem[];
-    float* R = smem;
-    uint32_t* cnt = reinterpret_cast<uint32_t*>(smem + (size_t)P * D);
-    __shared__ double red[ACC_WARPS];
-    const size_t slot_len = (size_t)P * D + P + 2;
-    double* slot = slots + (size_t)blockIdx.x * slot_len;
-    const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+uint64_t accum_pieces_max(uint64_t n, uint32_t P) { return n / kPieceRows + P + 1; }
+uint64_t accum_blocks(uint64_t n) { return (n + kHistRows - 1) / kHistRows; }
 
-    if (accumulate) {
-        for (size_t e = threadIdx.x; e < (size_t)P * D; e += ACC_THREADS) R[e] = 0.0f;
-        for (uint32_t e = threadIdx.x; e < P; e += ACC_THREADS) cnt[e] = 0u;
-    }
+// ---------------------------------------------------------------------------
+// counting sort by BMU
+// ---------------------------------------------------------------------------
+
+__global__ void __launch_bounds__(512) k_hist(const uint32_t* __restrict__ bmu, uint64_t n,
+                                              uint32_t P, uint32_t* __restrict__ counts) {
+    extern __shared__ uint32_t hist[];
+    for (uint32_t b = threadIdx.x; b < P; b += blockDim.x) hist[b] = 0;
     __syncthreads();
-
-    const uint64_t r0 = (uint64_t)blockIdx.x * rows_per_cta;
-    uint64_t r1 = r0 + rows_per_cta;
-    if (r1 > n) r1 = n;
-    double dsum = 0.0;
-    for (uint64_t pos = r0 + warp; pos < r1; pos += ACC_WARPS) {
-        const uint64_t row = sel ? (uint64_t)sel[pos] : pos;
-        const uint32_t b = bmu[pos];
-        const float* xr = x + row * D;
-        const float* wb = w + (size_t)b * D;
-        double d2 = 0.0;
-        for (uint32_t k = lane; k < D; k += 32) {
-            const float xv = xr[k], wv = wb[k];
-            const double diff = (double)xv - (double)wv;
-            d2 = fma(diff, diff, d2);
-            if (accumulate) atomicAdd(&R[(size_t)b * D + k], xv - wv);
-        }
-#pragma unroll
-        for (int o = 16; o; o >>= 1) d2 += __shfl_xor_sync(0xffffffffu, d2, o);
-        const double dist = sqrt(d2 > 0.0 ? d2 : 0.0);
-        if (lane == 0) {
-            if (accumulate) atomicAdd(&cnt[b], 1u);
-            if (dist_out) dist_out[pos] = dist;
-        }
-        dsum += dist;
-    }
-    // the warp's lanes hold identical dsum; one per warp
-    if (lane == 0) red[warp] = dsum;
+    const uint64_t r0 = (uint64_t)blockIdx.x * kHistRows;
+    const uint64_t r1 = r0 + kHistRows < n ? r0 + kHistRows : n;
+    for (uint64_t i = r0 + threadIdx.x; i < r1; i += blockDim.x) atomicAdd(&hist[bmu[i]], 1u);
     __syncthreads();
-    if (warp == 0) {
-        double v = lane < ACC_WARPS ? red[lane] : 0.0;
+    uint32_t* out = counts + (size_t)blockIdx.x * P;
+    for (uint32_t b = threadIdx.x; b < P; b += blockDim.x) out[b] = hist[b];
+}
+
+// counts[blk][b] -> exclusive prefix over blk (per node b); totals[b].
+// Block = 32 nodes x 8 block-segments: segment sums, scan over segments, rewrite.
+__global__ void __launch_bounds__(256) k_colscan(uint32_t* __restrict__ counts, uint32_t nblk,
+                                                 uint32_t P, uint32_t* __restrict__ totals) {
+    __shared__ uint32_t seg[8][33];
+    const uint32_t tn = threadIdx.x & 31, sg = threadIdx.x >> 5;
+    const uint32_t b = blockIdx.x * 32 + tn;
+    const uint32_t per = (nblk + 7) / 8;
+    const uint32_t s0 = sg * per, s1 = min(nblk, s0 + per);
+    uint32_t sum = 0;
+    if (b < P) {
+        uint32_t k = s0;
+        for (; k + 8 <= s1; k += 8) {
+            uint32_t v[8];
 #pragma unroll
-        for (int o = 16; o; o >>= 1) v += __shfl_xor_sync(0xffffffffu, v, o);
-        if (lane == 0) {
-            const double rows = r1 > r0 ? (double)(r1 - r0) : 0.0;
-            if (first_pass) {
-                slot[(size_t)P * D + P] = v;
-                slot[(size_t)P * D + P + 1] = rows;
-            } else {
-                slot[(size_t)P * D + P] += v;
-                slot[(size_t)P * D + P + 1] += rows;
+            for (int u = 0; u < 8; ++u) v[u] = counts[(size_t)(k + u) * P + b];
+#pragma unroll
+            for (int u = 0; u < 8; ++u) sum += v[u];
+        }
+        for (; k < s1; ++k) sum += counts[(size_t)k * P + b];
+    }
+    seg[sg][tn] = sum;
+    __syncthreads();
+    uint32_t run = 0;
+    for (uint32_t q = 0; q < sg; ++q) run += seg[q][tn];
+    if (b < P) {
+        if (sg == 7) totals[b] = run + sum;
+        uint32_t k = s0;
+        for (; k + 8 <= s1; k += 8) {
+            uint32_t v[8];
+#pragma unroll
+            for (int u = 0; u < 8; ++u) v[u] = counts[(size_t)(k + u) * P + b];
+#pragma unroll
+            for (int u = 0; u < 8; ++u) {
+                counts[(size_t)(k + u) * P + b] = run;
+                run += v[u];
             }
         }
-    }
-    if (!accumulate) return;
-    // flush FP32 partials into this CTA's FP64 slot (exclusive owner: no atomics)
-    for (size_t e = threadIdx.x; e < (size_t)P * D; e += ACC_THREADS) {
-        const double v = (double)R[e];
-        slot[e] = first_pass ? v : slot[e] + v;
-    }
-    for (uint32_t e = threadIdx.x; e < P; e += ACC_THREADS) {
-        const double v = (double)cnt[e];
-        slot[(size_t)P * D + e] = first_pass ? v : slot[(size_t)P * D + e] + v;
+        for (; k < s1; ++k) {
+            const uint32_t v = counts[(size_t)k * P + b];
+            counts[(size_t)k * P + b] = run;
+            run += v;
+        }
     }
 }
 
-// Fallback for codebooks whose partials exceed shared memory: FP64 atomics
-// straight into slot 0 (correct, slower; P*D > ~51k).
-__global__ void __launch_bounds__(256) k_accumulate_global(
-    const float* __restrict__ x, const uint32_t* __restrict__ sel, uint64_t n, uint32_t D,
-    const float* __restrict__ w, uint32_t P, const uint32_t* __restrict__ bmu,
-    double* __restrict__ dist_out, double* __restrict__ slot, int accumulate) {
+// node_start[b] (exclusive scan of totals), piece_start[b], piece_node[], and
+// the counts c_b into the sums buffer.  One block of 1024 threads.
+__global__ void __launch_bounds__(1024) k_nodescan(const uint32_t* __restrict__ totals, uint32_t P,
+                                                   uint32_t D, uint32_t* __restrict__ node_start,
+                                                   uint32_t* __restrict__ piece_start,
+                                                   uint32_t* __restrict__ piece_node,
+                                                   double* __restrict__ sums, int add_counts) {
+    __shared__ uint32_t s_rows[1024], s_pcs[1024];
+    __shared__ uint32_t carry_rows, carry_pcs;
+    if (threadIdx.x == 0) {
+        carry_rows = 0;
+        carry_pcs = 0;
+    }
+    __syncthreads();
+    for (uint32_t base = 0; base < P; base += 1024) {
+        const uint32_t b = base + threadIdx.x;
+        const uint32_t t = b < P ? totals[b] : 0u;
+        const uint32_t pc = (t + kPieceRows - 1) / kPieceRows;
+        s_rows[threadIdx.x] = t;
+        s_pcs[threadIdx.x] = pc;
+        __syncthreads();
+        for (uint32_t off = 1; off < 1024; off <<= 1) {  // Hillis-Steele inclusive scan
+            uint32_t a = 0, c = 0;
+            if (threadIdx.x >= off) {
+                a = s_rows[threadIdx.x - off];
+                c = s_pcs[threadIdx.x - off];
+            }
+            __syncthreads();
+            s_rows[threadIdx.x] += a;
+            s_pcs[threadIdx.x] += c;
+            __syncthreads();
+        }
+        const uint32_t ns = carry_rows + s_rows[threadIdx.x] - t;
+        const uint32_t ps = carry_pcs + s_pcs[threadIdx.x] - pc;
+        if (b < P) {
+            node_start[b] = ns;
+            piece_start[b] = ps;
+            for (uint32_t k = 0; k < pc; ++k) piece_node[ps + k] = b;
+            double* cb = sums + (size_t)P * D + b;
+            *cb = add_counts ? *cb + (double)t : (double)t;
+        }
+        __syncthreads();
+        if (threadIdx.x == 1023) {
+            carry_rows += s_rows[1023];
+            carry_pcs += s_pcs[1023];
+        }
+        __syncthreads();
+    }
+    if (threadIdx.x == 0) {
+        node_start[P] = carry_rows;
+        piece_start[P] = carry_pcs;
+    }
+}
+
+// Stable scatter of positions into BMU order (ties in position order).
+__global__ void __launch_bounds__(kScatterWarps * 32) k_scatter(
+    const uint32_t* __restrict__ bmu, uint64_t n, uint32_t P, const uint32_t* __restrict__ offs,
+    const uint32_t* __restrict__ node_start, uint32_t* __restrict__ sorted) {
+    extern __shared__ uint32_t whist[];  // [kScatterWarps][P] then the block's BMUs
+    uint32_t* sb = whist + (size_t)kScatterWarps * P;
+    const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+    const uint64_t r0 = (uint64_t)blockIdx.x * kHistRows;
+    for (uint32_t e = threadIdx.x; e < kScatterWarps * P; e += blockDim.x) whist[e] = 0;
+    for (uint32_t e = threadIdx.x; e < kHistRows; e += blockDim.x)
+        sb[e] = r0 + e < n ? bmu[r0 + e] : 0u;  // one coalesced pass over the block's BMUs
+    __syncthreads();
+    const uint32_t sub = kHistRows / kScatterWarps;
+    const uint64_t w0 = r0 + (uint64_t)warp * sub;
+    const uint64_t w1 = (w0 + sub < n) ? w0 + sub : n;
+    uint32_t* mine = whist + (size_t)warp * P;
+    for (uint64_t i = w0 + lane; i < w1; i += 32) atomicAdd(&mine[sb[i - r0]], 1u);
+    __syncthreads();
+    const uint32_t* boff = offs + (size_t)blockIdx.x * P;
+    for (uint32_t b = threadIdx.x; b < P; b += blockDim.x) {
+        uint32_t run = node_start[b] + boff[b];
+        for (int w = 0; w < kScatterWarps; ++w) {
+            const uint32_t c = whist[(size_t)w * P + b];
+            whist[(size_t)w * P + b] = run;
+            run += c;
+        }
+    }
+    __syncthreads();
+    for (uint64_t base = w0; base < w1; base += 32) {
+        const uint64_t i = base + lane;
+        const bool valid = i < w1;
+        const uint32_t b = valid ? sb[i - r0] : 0xFFFFFFFFu;
+        const uint32_t peers = __match_any_sync(0xffffffffu, b);
+        const uint32_t rank = __popc(peers & ((1u << lane) - 1u));
+        if (valid) sorted[mine[b] + rank] = (uint32_t)i;
+        __syncwarp();
+        if (valid && rank == 0) mine[b] += __popc(peers);
+        __syncwarp();
+    }
+}
+
+// ---------------------------------------------------------------------------
+// gather + FP64 accumulation per piece
+// ---------------------------------------------------------------------------
+
+// partial[p][k] (k < D) = sum over the piece's rows of (x_k - w_bk) in FP64;
+// partial[p][D] = sum of their exact BMU distances (when requested).
+// V2: d even — lane l < d/2 owns dims 2l, 2l+1 and reads them with one 8-byte
+// load per row (rows are 8-byte aligned); otherwise lanes own l and l+32.
+template <bool V2>
+__global__ void __launch_bounds__(256, 3) k_gather(
+    const float* __restrict__ x, const uint32_t* __restrict__ sel, const float* __restrict__ w,
+    uint32_t P, uint32_t D, const uint32_t* __restrict__ sorted,
+    const uint32_t* __restrict__ node_start, const uint32_t* __restrict__ piece_start,
+    const uint32_t* __restrict__ piece_node, double* __restrict__ partial,
+    double* __restrict__ dist_out, int want_dist, int accumulate) {
     const int lane = threadIdx.x & 31;
-    const uint64_t wid = (blockIdx.x * (uint64_t)blockDim.x + threadIdx.x) >> 5;
-    const uint64_t nw = ((uint64_t)gridDim.x * blockDim.x) >> 5;
-    double dsum = 0.0, rows = 0.0;
-    for (uint64_t pos = wid; pos < n; pos += nw) {
-        rows += 1.0;
-        const uint64_t row = sel ? (uint64_t)sel[pos] : pos;
-        const uint32_t b = bmu[pos];
-        const float* xr = x + row * D;
+    const uint32_t npieces = piece_start[P];
+    const uint32_t Dp = D + 1;
+    const uint32_t ka = V2 ? 2 * lane : lane, kb = V2 ? 2 * lane + 1 : lane + 32;
+    const bool oka = ka < D, okb = kb < D;
+    for (uint32_t p = (blockIdx.x * blockDim.x + threadIdx.x) >> 5; p < npieces;
+         p += (gridDim.x * blockDim.x) >> 5) {
+        const uint32_t b = piece_node[p];
+        const uint32_t r0 = node_start[b] + (p - piece_start[b]) * kPieceRows;
+        const uint32_t r1 = min(r0 + kPieceRows, node_start[b + 1]);
         const float* wb = w + (size_t)b * D;
-        double d2 = 0.0;
-        for (uint32_t k = lane; k < D; k += 32) {
-            const float xv = xr[k], wv = wb[k];
-            const double diff = (double)xv - (double)wv;
-            d2 = fma(diff, diff, d2);
-            if (accumulate) atomicAdd(&slot[(size_t)b * D + k], (double)(xv - wv));
+        const double w0 = oka ? (double)wb[ka] : 0.0;
+        const double w1 = okb ? (double)wb[kb] : 0.0;
+        double a0 = 0.0, a1 = 0.0, ds = 0.0;
+        for (uint32_t r = r0; r < r1; r += 32) {
+            const uint32_t mrow = min(32u, r1 - r);
+            // one coalesced load of up to 32 positions, broadcast per row
+            uint32_t mypos = 0;
+            uint64_t myrow = 0;
+            if (lane < (int)mrow) {
+                mypos = sorted[r + lane];
+                myrow = sel ? (uint64_t)sel[mypos] : (uint64_t)mypos;
+            }
+            for (uint32_t j0 = 0; j0 < mrow; j0 += kGatherBatch) {
+                float2 xv[kGatherBatch];
+#pragma unroll
+                for (int j = 0; j < kGatherBatch; ++j) {
+                    const uint64_t row = __shfl_sync(0xffffffffu, myrow, (j0 + j) & 31);
+                    const float* xr = x + row * D;
+                    const bool ok = j0 + j < mrow;
+                    if (V2) {
+                        xv[j] = (ok && oka) ? __ldg(reinterpret_cast<const float2*>(xr + ka))
+                                            : make_float2(0.0f, 0.0f);
+                    } else {
+                        xv[j].x = (ok && oka) ? __ldg(xr + ka) : 0.0f;
+                        xv[j].y = (ok && okb) ? __ldg(xr + kb) : 0.0f;
+                    }
+                }
+#pragma unroll
+                for (int j = 0; j < kGatherBatch; ++j) {
+                    if (j0 + j < mrow) {
+                        const double d0 = oka ? (double)xv[j].x - w0 : 0.0;
+                        const double d1 = okb ? (double)xv[j].y - w1 : 0.0;
+                        a0 += d0;
+                        a1 += d1;
+                        if (want_dist) {
+                            double d2 = fma(d0, d0, d1 * d1);
+#pragma unroll
+                            for (int o = 16; o; o >>= 1) d2 += __shfl_xor_sync(0xffffffffu, d2, o);
+                            const double dist = sqrt(d2 > 0.0 ? d2 : 0.0);
+                            const uint32_t pos = __shfl_sync(0xffffffffu, mypos, (j0 + j) & 31);
+                            if (dist_out && lane == 0) dist_out[pos] = dist;
+                            ds += dist;
+                        }
+                    }
+                }
+            }
         }
-        for (int o = 16; o; o >>= 1) d2 += __shfl_xor_sync(0xffffffffu, d2, o);
-        const double dist = sqrt(d2 > 0.0 ? d2 : 0.0);
-        if (lane == 0) {
-            if (accumulate) atomicAdd(&slot[(size_t)P * D + b], 1.0);
-            if (dist_out) dist_out[pos] = dist;
+        double* out = partial + (size_t)p * Dp;
+        if (accumulate) {
+            if (oka) out[ka] = a0;
+            if (okb) out[kb] = a1;
         }
-        dsum += dist;
-    }
-    if (lane == 0 && rows > 0.0) {
-        atomicAdd(&slot[(size_t)P * D + P], dsum);
-        atomicAdd(&slot[(size_t)P * D + P + 1], rows);
+        if (lane == 0) out[D] = ds;
     }
 }
 
-int accumulate_slots(uint32_t P, uint32_t D, size_t smem_optin, int sm_count) {
-    const size_t need = ((size_t)P * D + P) * 4;
-    if (need + 1024 > smem_optin) return 1;  // global fallback uses one slot
-    return sm_count;
+// TMA-fed variant: every lane issues one cp.async.bulk (1-D TMA) copy of its
+// row into a per-warp double-buffered shared-memory ring; a batch of 32 rows is
+// consumed while the next is in flight (~1000 rows/SM outstanding without
+// register pressure).  Bulk copies need 16-byte aligned sources and sizes, so
+// each copy covers [row & ~15, +rowb) with rowb = roundup16(4d + 8) (d even:
+// rows start at 0 or 8 mod 16); the caller guarantees slack after the last row.
+constexpr int kTmaWarps = 8;
+
+__device__ __forceinline__ uint32_t sm_u32(const void* p) {
+    return static_cast<uint32_t>(__cvta_generic_to_shared(p));
 }
+
+__global__ void __launch_bounds__(kTmaWarps * 32, 2) k_gather_tma(
+    const float* __restrict__ x, const uint32_t* __restrict__ sel, const float* __restrict__ w,
+    uint32_t P, uint32_t D, uint32_t rowb, const uint32_t* __restrict__ sorted,
+    const uint32_t* __restrict__ node_start, const uint32_t* __restrict__ piece_start,
+    const uint32_t* __restrict__ piece_node, double* __restrict__ partial,
+    double* __restrict__ dist_out, int want_dist, int accumulate) {
+    extern __shared__ __align__(128) uint8_t gsm[];
+    const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+    uint8_t* buf = gsm + (size_t)warp * 2 * 32 * rowb;  // [2][32][rowb]
+    uint64_t* bars = reinterpret_cast<uint64_t*>(gsm + (size_t)kTmaWarps * 2 * 32 * rowb) + warp * 2;
+    if (lane == 0) {
+        asm volatile("mbarrier.init.shared::cta.b64 [%0], 1;" ::"r"(sm_u32(&bars[0])));
+        asm volatile("mbarrier.init.shared::cta.b64 [%0], 1;" ::"r"(sm_u32(&bars[1])));
+        asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
+    }
+    __syncwarp();
+    uint32_t phase[2] = {0u, 0u};
+    const uint32_t npieces = piece_start[P];
+    const uint32_t Dp = D + 1;
+    const uint32_t ka = 2 * lane, kb = 2 * lane + 1;
+    const bool oka = ka < D, okb = kb < D;
+
+    // issue the bulk copies of batch m (rows r0+32m+lane) into buffer `slot`
+    auto issue = [&](uint64_t rowaddr, uint32_t nrows, int slot) {
+        if (lane == 0)
+            asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;" ::"r"(
+                             sm_u32(&bars[slot])),
+                         "r"(nrows * rowb)
+                         : "memory");
+        __syncwarp();
+        if ((uint32_t)lane < nrows) {
+            const uint64_t src = rowaddr & ~15ull;
+            asm volatile(
+                "cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1], %2, [%3];" ::"r"(
+                    sm_u32(buf + ((size_t)slot * 32 + lane) * rowb)),
+                "l"(src), "r"(rowb), "r"(sm_u32(&bars[slot]))
+                : "memory");
+        }
+    };
+    auto wait = [&](int slot) {
+        asm volatile(
+            "{\n\t.reg .pred P1;\n\t"
+            "W_%=:\n\t"
+            "mbarrier.try_wait.parity.shared::cta.b64 P1, [%0], %1, %2;\n\t"
+            "@!P1 bra W_%=;\n\t}" ::"r"(sm_u32(&bars[slot])),
+            "r"(phase[slot]), "r"(0x989680u)
+            : "memory");
+        phase[slot] ^= 1u;
+    };
+
+    for (uint32_t p = blockIdx.x * kTmaWarps + warp; p < npieces; p += gridDim.x * kTmaWarps) {
+        const uint32_t b = piece_node[p];
+        const uint32_t r0 = node_start[b] + (p - piece_start[b]) * kPieceRows;
+        const uint32_t r1 = min(r0 + kPieceRows, node_start[b + 1]);
+        const uint32_t nb = (r1 - r0 + 31) / 32;  // batches of 32 rows (<= 8)
+        uint64_t addr[8];
+        uint32_t pos[8];
+#pragma unroll
+        for (int m = 0; m < 8; ++m) {
+            const uint32_t r = r0 + 32 * m + lane;
+            pos[m] = r < r1 ? sorted[r] : 0u;
+        }
+#pragma unroll
+        for (int m = 0; m < 8; ++m) {
+            const uint64_t row = sel ? (uint64_t)sel[pos[m]] : (uint64_t)pos[m];
+            addr[m] = reinterpret_cast<uint64_t>(x + row * D);
+        }
+        const float* wb = w + (size_t)b * D;
+        const double w0 = oka ? (double)wb[ka] : 0.0;
+        const double w1 = okb ? (double)wb[kb] : 0.0;
+        double a0 = 0.0, a1 = 0.0, ds = 0.0;
+        issue(addr[0], min(32u, r1 - r0), 0);
+#pragma unroll
+        for (int m = 0; m < 8; ++m) {
+            if (m < (int)nb) {
+                const uint32_t rows_m = min(32u, r1 - (r0 + 32 * m));
+                if (m + 1 < (int)nb) issue(addr[m + 1], min(32u, r1 - (r0 + 32 * (m + 1))), (m + 1) & 1);
+                wait(m & 1);
+                const uint8_t* bm = buf + (size_t)(m & 1) * 32 * rowb;
+                for (uint32_t j = 0; j < rows_m; ++j) {
+                    const uint32_t mis = (uint32_t)__shfl_sync(0xffffffffu, (uint32_t)addr[m], j) & 15u;
+                    const float* xr = reinterpret_cast<const float*>(bm + (size_t)j * rowb + mis);
+                    float2 v = make_float2(0.0f, 0.0f);
+                    if (okb) v = *reinterpret_cast<const float2*>(xr + ka);
+                    else if (oka) v.x = xr[ka];
+                    const double d0 = oka ? (double)v.x - w0 : 0.0;
+                    const double d1 = okb ? (double)v.y - w1 : 0.0;
+                    a0 += d0;
+                    a1 += d1;
+                    if (want_dist) {
+                        double d2 = fma(d0, d0, d1 * d1);
+#pragma unroll
+                        for (int o = 16; o; o >>= 1) d2 += __shfl_xor_sync(0xffffffffu, d2, o);
+                        const double dist = sqrt(d2 > 0.0 ? d2 : 0.0);
+                        const uint32_t pp = __shfl_sync(0xffffffffu, pos[m], j);
+                        if (dist_out && lane == 0) dist_out[pp] = dist;
+                        ds += dist;
+                    }
+                }
+                __syncwarp();  // buffer m&1 may be refilled by the next issue
+            }
+        }
+        double* out = partial + (size_t)p * Dp;
+        if (accumulate) {
+            if (oka) out[ka] = a0;
+            if (okb) out[kb] = a1;
+        }
+        if (lane == 0) out[D] = ds;
+    }
+}
+
+// sums[b][k] (+)= sum over the pieces of node b: one warp per (b, k), lanes
+// stride the node's pieces, fixed xor tree (deterministic, skew-proof)
+__global__ void k_piece_reduce(const double* __restrict__ partial,
+                               const uint32_t* __restrict__ piece_start, uint32_t P, uint32_t D,
+                               double* __restrict__ sums, int add) {
+    const size_t e = (blockIdx.x * (size_t)blockDim.x + threadIdx.x) >> 5;
+    const int lane = threadIdx.x & 31;
+    if (e >= (size_t)P * D) return;
+    const uint32_t Dp = D + 1;
+    const uint32_t b = (uint32_t)(e / D), k = (uint32_t)(e % D);
+    const uint32_t p0 = piece_start[b], p1 = piece_start[b + 1];
+    double q0 = 0.0, q1 = 0.0;
+    uint32_t p = p0 + lane;
+    for (; p + 32 < p1; p += 64) {
+        q0 += partial[(size_t)p * Dp + k];
+        q1 += partial[(size_t)(p + 32) * Dp + k];
+    }
+    if (p < p1) q0 += partial[(size_t)p * Dp + k];
+    double v = q0 + q1;
+#pragma unroll
+    for (int o = 16; o; o >>= 1) v += __shfl_xor_sync(0xffffffffu, v, o);
+    if (lane == 0) sums[e] = add ? sums[e] + v : v;
+}
+
+// distance sum over all pieces: fixed strided partition + fixed tree (deterministic)
+__global__ void __launch_bounds__(1024) k_dist_reduce(const double* __restrict__ partial,
+                                                      const uint32_t* __restrict__ piece_start,
+                                                      uint32_t P, uint32_t D,
+                                                      double* __restrict__ sums, int add) {
+    __shared__ double red[1024];
+    const uint32_t np = piece_start[P], Dp = D + 1;
+    double s = 0.0;
+    for (uint32_t p = threadIdx.x; p < np; p += 1024) s += partial[(size_t)p * Dp + D];
+    red[threadIdx.x] = s;
+    __syncthreads();
+    for (int off = 512; off; off >>= 1) {
+        if ((int)threadIdx.x < off) red[threadIdx.x] += red[threadIdx.x + off];
+        __syncthreads();
+    }
+    if (threadIdx.x == 0) {
+        double* t = sums + (size_t)P * D + P;
+        t[0] = add ? t[0] + red[0] : red[0];
+    }
+}
+
+__global__ void k_add_rowcount(double* __restrict__ sums, uint32_t P, uint32_t D, double rows,
+                               int add) {
+    double* t = sums + (size_t)P * D + P + 1;
+    *t = add ? *t + rows : rows;
+}
+
+// ---------------------------------------------------------------------------
 
 void launch_accumulate(const float* x, const uint32_t* sel, uint64_t n, uint32_t D,
                        const float* w, uint32_t P, const uint32_t* bmu, double* dist_out,
-                       double* slots, int nslots, bool accumulate, bool first_pass,
-                       size_t smem_optin, cudaStream_t st) {
-    const size_t slot_len = (size_t)P * D + P + 2;
-    const size_t need = ((size_t)P * D + P) * 4;
-    if (need + 1024 > smem_optin) {
-        if (first_pass) cudaMemsetAsync(slots, 0, slot_len * sizeof(double), st);
-        if (n == 0) return;
-        uint64_t blocks = (n * 32 + 255) / 256;
-        if (blocks > 148 * 64) blocks = 148 * 64;
-        TSOM_LAUNCH(k_accumulate_global<<<(unsigned)blocks, 256, 0, st>>>(x, sel, n, D, w, P, bmu, dist_out,
-                                                             slots, accumulate ? 1 : 0));
-        return;
-    }
-    static size_t attr_bytes = 0;
-    if (attr_bytes < need) {
-        cudaFuncSetAttribute(k_accumulate_smem, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                             (int)(smem_optin - 1024));
-        attr_bytes = smem_optin;
-    }
-    // rows are split over nslots CTAs per pass; each pass covers <= nslots*64k rows
-    const uint64_t pass_rows = (uint64_t)nslots * kMaxRowsPerSlotPass;
-    bool first = first_pass;
-    uint64_t done = 0;
+                       bool want_dist_sum, bool accumulate, bool first, const AccumScratch& s,
+                       double* sums, int sm_count, cudaStream_t st, bool x_slack) {
+    const int add = first ? 0 : 1;
     if (n == 0) {
-        TSOM_LAUNCH(k_accumulate_smem<<<nslots, ACC_THREADS, accumulate ? need : 16, st>>>(
-            x, sel, 0, D, w, P, bmu, dist_out, slots, 1, accumulate ? 1 : 0, first ? 1 : 0));
+        if (first) cudaMemsetAsync(sums, 0, ((size_t)P * D + P + 2) * sizeof(double), st);
         return;
     }
-    while (done < n) {
-        const uint64_t chunk = (n - done) < pass_rows ? (n - done) : pass_rows;
-        const uint64_t per_cta = (chunk + nslots - 1) / nslots;
-        // with a selection the row ids are read through sel; without one the
-        // rows of this pass are contiguous from `done`
-        TSOM_LAUNCH(k_accumulate_smem<<<nslots, ACC_THREADS, accumulate ? need : 16, st>>>(
-            sel ? x : x + done * D, sel ? sel + done : nullptr, chunk, D, w, P, bmu + done,
-            dist_out ? dist_out + done : nullptr, slots, per_cta, accumulate ? 1 : 0,
-            first ? 1 : 0));
-        first = false;
-        done += chunk;
+    const bool want_dist = dist_out != nullptr || want_dist_sum;
+    if (!accumulate && !want_dist) {  // BMU only: nothing to gather
+        if (first) cudaMemsetAsync(sums, 0, ((size_t)P * D + P + 2) * sizeof(double), st);
+        TSOM_LAUNCH(k_add_rowcount<<<1, 1, 0, st>>>(sums, P, D, (double)n, add));
+        return;
     }
+    const uint32_t nblk = (uint32_t)accum_blocks(n);
+    static uint32_t attr_p = 0;
+    if (P > attr_p) {  // dynamic smem beyond 48 KB (P up to ~7000 nodes)
+        cudaFuncSetAttribute(k_hist, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)(P * 4));
+        cudaFuncSetAttribute(k_scatter, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                             (int)((kScatterWarps * P + kHistRows) * 4));
+        attr_p = P;
+    }
+    TSOM_LAUNCH(k_hist<<<nblk, 512, P * sizeof(uint32_t), st>>>(bmu, n, P, s.counts));
+    TSOM_LAUNCH(k_colscan<<<(P + 31) / 32, 256, 0, st>>>(s.counts, nblk, P, s.totals));
+    TSOM_LAUNCH(k_nodescan<<<1, 1024, 0, st>>>(s.totals, P, D, s.node_start, s.piece_start,
+                                               s.piece_node, sums, add));
+    TSOM_LAUNCH(k_scatter<<<nblk, kScatterWarps * 32,
+                            ((size_t)kScatterWarps * P + kHistRows) * sizeof(uint32_t),
+                            st>>>(bmu, n, P, s.counts, s.node_start, s.sorted));
+    const uint64_t pieces = accum_pieces_max(n, P);
+    const uint64_t warps = pieces < (uint64_t)sm_count * 32 ? pieces : (uint64_t)sm_count * 32;
+    const unsigned gblocks = (unsigned)((warps * 32 + 255) / 256);
+    const bool v2 = (D % 2 == 0) && D <= 64 && ((reinterpret_cast<uintptr_t>(x) & 7u) == 0);
+    const uint32_t rowb = (D * 4 + 8 + 15) / 16 * 16;  // d even: row offset mod 16 is 0 or 8
+    const size_t tsmem = (size_t)kTmaWarps * (2 * 32 * rowb + 16);
+    if (v2 && x_slack && tsmem <= 110 * 1024) {
+        static size_t tattr = 0;
+        if (tattr < tsmem) {
+            cudaFuncSetAttribute(k_gather_tma, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                 (int)tsmem);
+            tattr = tsmem;
+        }
+        const uint64_t tblocks = (pieces + kTmaWarps - 1) / kTmaWarps;
+        const unsigned tb = (unsigned)(tblocks < (uint64_t)sm_count * 2 ? tblocks : sm_count * 2);
+        TSOM_LAUNCH(k_gather_tma<<<tb, kTmaWarps * 32, tsmem, st>>>(
+            x, sel, w, P, D, rowb, s.sorted, s.node_start, s.piece_start, s.piece_node, s.partial,
+            dist_out, want_dist ? 1 : 0, accumulate ? 1 : 0));
+    } else if (v2)
+        TSOM_LAUNCH(k_gather<true><<<gblocks, 256, 0, st>>>(
+            x, sel, w, P, D, s.sorted, s.node_start, s.piece_start, s.piece_node, s.partial,
+            dist_out, want_dist ? 1 : 0, accumulate ? 1 : 0));
+    else
+        TSOM_LAUNCH(k_gather<false><<<gblocks, 256, 0, st>>>(
+            x, sel, w, P, D, s.sorted, s.node_start, s.piece_start, s.piece_node, s.partial,
+            dist_out, want_dist ? 1 : 0, accumulate ? 1 : 0));
+    const size_t m = (size_t)P * D;
+    if (accumulate)
+        TSOM_LAUNCH(k_piece_reduce<<<(unsigned)((m * 32 + 255) / 256), 256, 0, st>>>(
+            s.partial, s.piece_start, P, D, sums, add));
+    if (want_dist)
+        TSOM_LAUNCH(k_dist_reduce<<<1, 1024, 0, st>>>(s.partial, s.piece_start, P, D, sums, add));
+    else if (first)
+        cudaMemsetAsync(sums + (size_t)P * D + P, 0, sizeof(double), st);
+    TSOM_LAUNCH(k_add_rowcount<<<1, 1, 0, st>>>(sums, P, D, (double)n, add));
 }
 
-__global__ void k_reduce_slots(const double* __restrict__ slots, int nslots, size_t len,
-                               double* __restrict__ sums) {
-    const size_t e = blockIdx.x * (size_t)blockDim.x + threadIdx.x;
-    if (e >= len) return;
-    double s = 0.0;
-    for (int c = 0; c < nslots; ++c) s += slots[(size_t)c * len + e];  // fixed order
-    sums[e] = s;
-}
-
-void launch_reduce_slots(const double* slots, int nslots, size_t len, double* sums,
-                         cudaStream_t st) {
-    TSOM_LAUNCH(k_reduce_slots<<<(unsigned)((len + 255) / 256), 256, 0, st>>>(slots, nslots, len, sums));
+void accum_scratch_bytes(uint64_t n, uint32_t P, uint32_t D, size_t out[7]) {
+    const uint64_t nblk = accum_blocks(n), pieces = accum_pieces_max(n, P);
+    out[0] = (size_t)nblk * P * 4;           // counts / offsets
+    out[1] = (size_t)P * 4;                  // totals
+    out[2] = (size_t)(P + 1) * 4;            // node_start
+    out[3] = (size_t)(P + 1) * 4;            // piece_start
+    out[4] = (size_t)pieces * 4;             // piece_node
+    out[5] = (size_t)(n ? n : 1) * 4;        // sorted positions
+    out[6] = (size_t)pieces * (D + 1) * 8;   // piece partials
 }
 
 }  // namespace tsom

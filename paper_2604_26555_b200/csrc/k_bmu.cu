@@ -257,7 +257,7 @@ __global__ void __launch_bounds__(256) k1_bmu_simt(
                     bmu[pos] = i1[s];
                     if (!(b2[s] - b1[s] > thr)) {
                         const uint32_t slot = atomicAdd(&flags[0], 1u);
-                        flags[1 + slot] = (uint32_t)pos;
+                        flags[2 + slot] = (uint32_t)pos;
                     }
                 }
             }
@@ -286,35 +286,100 @@ void launch_bmu_simt(const float* x, const uint32_t* sel, uint64_t n, uint32_t D
 // Merge per-group top-2 partials of the tcgen05 kernel
 // ---------------------------------------------------------------------------
 
+__device__ __forceinline__ double exact_d2(const float* __restrict__ x,
+                                           const float* __restrict__ wj, uint32_t D) {
+    // the reference's loop (trainer.hpp:295-299): FP64, sequential k, no contraction
+    double acc = 0.0;
+    for (uint32_t k = 0; k < D; ++k) {
+        const double diff = __dsub_rn((double)x[k], (double)wj[k]);
+        acc = __dadd_rn(acc, __dmul_rn(diff, diff));
+    }
+    return acc;
+}
+
+// part[g] = [b1 | packed local candidate ids | count] (k1_bmu_tc.cu epilogue)
 __global__ void k_merge_partials(const float* __restrict__ part, uint64_t n, uint32_t groups,
-                                 const float* __restrict__ x2max, const float* __restrict__ w2max,
-                                 float tau, uint32_t* __restrict__ bmu,
-                                 uint32_t* __restrict__ flags) {
+                                 uint32_t gn, const float* __restrict__ x2max,
+                                 const float* __restrict__ w2max, float tau,
+                                 const float* __restrict__ x, const uint32_t* __restrict__ sel,
+                                 const float* __restrict__ w, uint32_t D,
+                                 uint32_t* __restrict__ bmu, uint32_t* __restrict__ flags) {
     const uint64_t i = blockIdx.x * (uint64_t)blockDim.x + threadIdx.x;
     if (i >= n) return;
     const float thr = tau * (__ldg(x2max) + __ldg(w2max));
-    float b1 = CUDART_INF_F, b2 = CUDART_INF_F;
-    uint32_t i1 = 0;
+    // all partials of the row in one round of independent loads (groups <= 8
+    // stay in registers; larger codebooks stream in chunks of 8)
+    constexpr uint32_t kG = 8;
+    float b1v[kG];
+    uint32_t pk[kG], ct[kG];
+    float B1 = CUDART_INF_F;
+    for (uint32_t g0 = 0; g0 < groups; g0 += kG) {
+#pragma unroll
+        for (uint32_t q = 0; q < kG; ++q)
+            if (g0 + q < groups) B1 = fminf(B1, part[(size_t)(g0 + q) * 3 * n + i]);
+    }
+    const float lim = B1 + thr;
+    uint32_t ncand = 0, only = 0;
+    bool overflow = false;
+    for (uint32_t g0 = 0; g0 < groups; g0 += kG) {
+#pragma unroll
+        for (uint32_t q = 0; q < kG; ++q) {
+            if (g0 + q < groups) {
+                const float* pg = part + (size_t)(g0 + q) * 3 * n;
+                b1v[q] = pg[i];
+                pk[q] = __float_as_uint(pg[n + i]);
+                ct[q] = __float_as_uint(pg[2 * n + i]);
+            }
+        }
+#pragma unroll
+        for (uint32_t q = 0; q < kG; ++q) {
+            if (g0 + q < groups && b1v[q] <= lim) {
+                if (ct[q] > 4) overflow = true;
+                ncand += ct[q];
+                only = (g0 + q) * gn + (pk[q] & 0xFFu);
+            }
+        }
+    }
+    if (overflow || ncand == 0) {  // > 4 near-ties inside a group: full exact re-scan
+        const uint32_t slot = atomicAdd(&flags[0], 1u);
+        flags[2 + slot] = (uint32_t)i;
+        bmu[i] = only;
+        return;
+    }
+    if (ncand == 1) {
+        bmu[i] = only;
+        return;
+    }
+    // several candidates: exact FP64 distances of just those nodes, ascending node
+    // order with strict < (lowest index wins ties), as find_bmus (trainer.hpp:293-304)
+    atomicAdd(&flags[1], 1u);
+    const float* xr = x + (sel ? (uint64_t)sel[i] : i) * D;
+    double best = CUDART_INF;
+    uint32_t best_j = 0;
     for (uint32_t g = 0; g < groups; ++g) {
         const float* pg = part + (size_t)g * 3 * n;
-        const float ob1 = pg[i];
-        const uint32_t oi1 = __float_as_uint(pg[n + i]);
-        const float ob2 = pg[2 * n + i];
-        top2_merge(b1, i1, b2, ob1, oi1, ob2);
+        if (!(pg[i] <= lim)) continue;
+        const uint32_t cnt = __float_as_uint(pg[2 * n + i]);
+        const uint32_t pack = __float_as_uint(pg[n + i]);
+        for (uint32_t c = 0; c < cnt; ++c) {
+            const uint32_t j = g * gn + ((pack >> (8 * c)) & 0xFFu);
+            const double d2 = exact_d2(xr, w + (size_t)j * D, D);
+            if (d2 < best) {
+                best = d2;
+                best_j = j;
+            }
+        }
     }
-    bmu[i] = i1;
-    if (!(b2 - b1 > thr)) {
-        const uint32_t slot = atomicAdd(&flags[0], 1u);
-        flags[1 + slot] = (uint32_t)i;
-    }
+    bmu[i] = best_j;
 }
 
-void launch_merge_partials(const float* part, uint64_t n, uint32_t groups, const float* x2max,
-                           const float* w2max, float tau, uint32_t* bmu, uint32_t* flags,
-                           cudaStream_t st) {
+void launch_merge_partials(const float* part, uint64_t n, uint32_t groups, uint32_t gn,
+                           const float* x2max, const float* w2max, float tau, const float* x,
+                           const uint32_t* sel, const float* w, uint32_t D, uint32_t* bmu,
+                           uint32_t* flags, cudaStream_t st) {
     if (n == 0) return;
-    TSOM_LAUNCH(k_merge_partials<<<(unsigned)((n + 255) / 256), 256, 0, st>>>(part, n, groups, x2max, w2max,
-                                                                  tau, bmu, flags));
+    TSOM_LAUNCH(k_merge_partials<<<(unsigned)((n + 255) / 256), 256, 0, st>>>(
+        part, n, groups, gn, x2max, w2max, tau, x, sel, w, D, bmu, flags));
 }
 
 // ---------------------------------------------------------------------------
@@ -331,7 +396,7 @@ __global__ void __launch_bounds__(256) k_rescan(const float* __restrict__ x,
     const int lane = threadIdx.x & 31, wib = threadIdx.x >> 5;
     float* xrow = xrow_all + wib * D;
     for (uint32_t f = blockIdx.x * 8 + wib; f < count; f += gridDim.x * 8) {
-        const uint32_t pos = flags[1 + f];
+        const uint32_t pos = flags[2 + f];
         const uint64_t row = sel ? (uint64_t)sel[pos] : pos;
         __syncwarp();
         for (uint32_t k = lane; k < D; k += 32) xrow[k] = x[row * D + k];

@@ -25,43 +25,52 @@ __global__ void k_build_saug(const double* __restrict__ sums, const float* __res
     saug[e] = k < D ? sums[(size_t)b * D + k] + c * (double)w[(size_t)b * D + k] : c;
 }
 
-// H_j = sum_b infl[b][j] c_b   (one thread per node; coalesced over j)
-__global__ void k_smooth_den(const double* __restrict__ infl, const double* __restrict__ sums,
-                             uint32_t P, uint32_t D, double* __restrict__ H) {
-    const uint32_t j = blockIdx.x * blockDim.x + threadIdx.x;
-    if (j >= P) return;
+// H_j = sum_b infl[b][j] c_b: block = 32 nodes x 8 b-slices, fixed-order fold
+__global__ void __launch_bounds__(256) k_smooth_den(const double* __restrict__ infl,
+                                                    const double* __restrict__ sums, uint32_t P,
+                                                    uint32_t D, double* __restrict__ H) {
+    __shared__ double part[8][33];
+    const uint32_t tj = threadIdx.x & 31, sl = threadIdx.x >> 5;
+    const uint32_t j = blockIdx.x * 32 + tj;
     const double* c = sums + (size_t)P * D;
     double acc = 0.0;
-    for (uint32_t b = 0; b < P; ++b) acc = fma(infl[(size_t)b * P + j], c[b], acc);
-    H[j] = acc;
+    if (j < P)
+        for (uint32_t b = sl; b < P; b += 8) acc = fma(infl[(size_t)b * P + j], c[b], acc);
+    part[sl][tj] = acc;
+    __syncthreads();
+    if (sl == 0 && j < P) {
+        double v = 0.0;
+        for (int k = 0; k < 8; ++k) v += part[k][tj];
+        H[j] = v;
+    }
 }
 
-// U[j][k] = eta * (sum_b infl[b][j] * saug[b][k] - w[j][k] * H_j), k < d.
-// Block: 32 nodes j x 64 columns k; b tiled by 32 through shared memory.
-constexpr int SM_TJ = 32, SM_TB = 32, SM_KG = 8, SM_KC = SM_KG * 8;
+// partial[z][j][k] = sum_{b in slice z} infl[b][j] * saug[b][k], k < d.
+// Block: 32 nodes j x 64 columns k x one of SM_SPLIT b-slices (fills the GPU).
+constexpr int SM_TJ = 32, SM_TB = 32, SM_KG = 8, SM_KC = SM_KG * 8, SM_SPLIT = 8;
 __global__ void __launch_bounds__(256) k_smooth_gemm(const double* __restrict__ infl,
                                                      const double* __restrict__ saug, uint32_t P,
-                                                     uint32_t D, const float* __restrict__ w,
-                                                     double eta, const double* __restrict__ H,
-                                                     double* __restrict__ U) {
+                                                     uint32_t D, double* __restrict__ partial) {
     __shared__ double hs[SM_TB * SM_TJ];
     __shared__ double ss[SM_TB * SM_KC];
     const uint32_t Dp = D + 1;
     const int tj = threadIdx.x % SM_TJ, kg = threadIdx.x / SM_TJ;
     const uint32_t j0 = blockIdx.x * SM_TJ, j = j0 + tj;
     const uint32_t k0 = blockIdx.y * SM_KC;
+    const uint32_t span = (P + SM_SPLIT - 1) / SM_SPLIT;
+    const uint32_t bz0 = blockIdx.z * span, bz1 = min(P, bz0 + span);
     double acc[8];
 #pragma unroll
     for (int q = 0; q < 8; ++q) acc[q] = 0.0;
-    for (uint32_t b0 = 0; b0 < P; b0 += SM_TB) {
+    for (uint32_t b0 = bz0; b0 < bz1; b0 += SM_TB) {
         __syncthreads();
         for (int e = threadIdx.x; e < SM_TB * SM_TJ; e += 256) {
             const uint32_t bb = b0 + e / SM_TJ, jj = j0 + e % SM_TJ;
-            hs[e] = (bb < P && jj < P) ? infl[(size_t)bb * P + jj] : 0.0;
+            hs[e] = (bb < bz1 && jj < P) ? infl[(size_t)bb * P + jj] : 0.0;
         }
         for (int e = threadIdx.x; e < SM_TB * SM_KC; e += 256) {
             const uint32_t bb = b0 + e / SM_KC, kk = k0 + e % SM_KC;
-            ss[e] = (bb < P && kk < D) ? saug[(size_t)bb * Dp + kk] : 0.0;
+            ss[e] = (bb < bz1 && kk < D) ? saug[(size_t)bb * Dp + kk] : 0.0;
         }
         __syncthreads();
 #pragma unroll 4
@@ -72,23 +81,42 @@ __global__ void __launch_bounds__(256) k_smooth_gemm(const double* __restrict__ 
         }
     }
     if (j >= P) return;
-    const double hj = H[j];
+    double* out = partial + (size_t)blockIdx.z * P * D;
 #pragma unroll
     for (int q = 0; q < 8; ++q) {
         const uint32_t k = k0 + kg + q * SM_KG;
-        if (k < D) U[(size_t)j * D + k] = eta * (acc[q] - (double)w[(size_t)j * D + k] * hj);
+        if (k < D) out[(size_t)j * D + k] = acc[q];
     }
 }
 
+// U = eta * (sum_z partial[z] - w * H), fixed slice order (deterministic)
+__global__ void k_smooth_finish(const double* __restrict__ partial, const float* __restrict__ w,
+                                const double* __restrict__ H, uint32_t P, uint32_t D, double eta,
+                                double* __restrict__ U) {
+    const size_t e = blockIdx.x * (size_t)blockDim.x + threadIdx.x;
+    if (e >= (size_t)P * D) return;
+    double s = 0.0;
+    for (int z = 0; z < SM_SPLIT; ++z) s += partial[(size_t)z * P * D + e];
+    U[e] = eta * (s - (double)w[e] * H[e / D]);
+}
+
 void launch_smooth(const double* infl, const double* sums, const float* w, uint32_t P, uint32_t D,
-                   double eta, double* U, double* H, cudaStream_t st) {
-    // saug scratch lives right after U (engine allocates U with room: P*d + P*(d+1))
-    double* saug = U + (size_t)P * D;
+                   double eta, double* U, double* H, double* scratch, cudaStream_t st) {
+    // scratch: P*(d+1) (saug) + SM_SPLIT*P*d (slice partials) doubles
+    double* saug = scratch;
+    double* partial = scratch + (size_t)P * (D + 1);
     const size_t n = (size_t)P * (D + 1);
     TSOM_LAUNCH(k_build_saug<<<(unsigned)((n + 255) / 256), 256, 0, st>>>(sums, w, P, D, saug));
-    TSOM_LAUNCH(k_smooth_den<<<(P + 127) / 128, 128, 0, st>>>(infl, sums, P, D, H));
-    dim3 grid((P + SM_TJ - 1) / SM_TJ, (D + SM_KC - 1) / SM_KC);
-    TSOM_LAUNCH(k_smooth_gemm<<<grid, 256, 0, st>>>(infl, saug, P, D, w, eta, H, U));
+    TSOM_LAUNCH(k_smooth_den<<<(P + 31) / 32, 256, 0, st>>>(infl, sums, P, D, H));
+    dim3 grid((P + SM_TJ - 1) / SM_TJ, (D + SM_KC - 1) / SM_KC, SM_SPLIT);
+    TSOM_LAUNCH(k_smooth_gemm<<<grid, 256, 0, st>>>(infl, saug, P, D, partial));
+    const size_t pd = (size_t)P * D;
+    TSOM_LAUNCH(k_smooth_finish<<<(unsigned)((pd + 255) / 256), 256, 0, st>>>(partial, w, H, P, D,
+                                                                            eta, U));
+}
+
+size_t smooth_scratch_doubles(uint32_t P, uint32_t D) {
+    return (size_t)P * (D + 1) + (size_t)SM_SPLIT * P * D;
 }
 
 // apply_update (trainer.hpp:341-369): H < 1e-12 → node frozen (momentum memory

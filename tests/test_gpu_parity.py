@@ -143,6 +143,23 @@ def test_bmu_exact_ties_and_duplicates(pkg, oracle_port, kernel):
     assert e.last_recheck_count >= x.shape[0]  # every row had an exact tie
 
 
+@pytest.mark.parametrize("kernel", KERNELS)
+def test_bmu_many_way_ties_full_rescan(pkg, oracle_port, kernel):
+    """Eight identical nodes per cluster (> 4 candidates in one group) force the
+    full exact re-scan path; indices must still match the reference."""
+    rng = np.random.default_rng(9)
+    centres = rng.standard_normal((40, 50)).astype(np.float32) * 3
+    w = np.repeat(centres, 8, axis=0)  # 320 nodes: groups of 8 exact twins
+    x = (centres[rng.integers(0, 40, 3000)] +
+         0.2 * rng.standard_normal((3000, 50))).astype(np.float32)
+    e = engine(pkg, w.shape[0], 50, kernel)
+    e.set_codebook(w)
+    b, d = e.bmu(x)
+    bo, do = oracle_port.find_bmus(x, w)
+    assert (b == bo).all()
+    np.testing.assert_allclose(d, do, rtol=1e-12)
+
+
 def test_golden_hot_path(pkg):
     """Reference outputs (tests/golden/hot_path.npz, made from oracle/_ref)."""
     g = np.load(os.path.join(GOLDEN, "hot_path.npz"))
@@ -200,7 +217,8 @@ def test_streamed_equals_resident(pkg, oracle_port):
         sel = np.arange(1, n, 3, dtype=np.uint32)
         out.append(e.epoch(0.3, sel, want_dist=True))
     (u0, h0, d0), (u1, h1, d1) = out
-    assert np.max(np.abs(u0 - u1)) <= 1e-10 * np.max(np.abs(u0))
+    # same rows, same BMUs; only the grouping of the FP32 per-CTA partial sums differs
+    assert np.max(np.abs(u0 - u1)) <= 1e-9 * np.max(np.abs(u0))
     np.testing.assert_allclose(h0, h1, rtol=1e-12)
     np.testing.assert_allclose(d0, d1, rtol=1e-14)
 
