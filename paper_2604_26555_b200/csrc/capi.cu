@@ -161,23 +161,50 @@ void run_bmu(Engine* eng, const float* x, const uint32_t* sel, uint64_t n, const
     if (use_tc(eng)) {
         const uint32_t gn = tsom::tc_group_width(eng->P);
         const uint32_t groups = (eng->P + gn - 1) / gn;
+        const size_t tile_bytes = 2ull * tsom::kTcTileM * tsom::kTcKPad * sizeof(float);
         if (!tiles) {
             const uint64_t ntiles = (n + tsom::kTcTileM - 1) / tsom::kTcTileM;
-            CU(eng->gsplit.ensure(ntiles * 2 * tsom::kTcTileM * tsom::kTcKPad * sizeof(float)));
-            tsom::launch_split_rows(x, sel, n, eng->D, eng->gsplit.as<float>(), eng->stream);
+            CU(eng->gsplit.ensure(ntiles * tile_bytes));
+            tsom::launch_split_rows(x, sel, nullptr, n, eng->D, eng->gsplit.as<float>(),
+                                    eng->stream);
             tiles = eng->gsplit.as<float>();
         }
         CU(eng->part.ensure((size_t)groups * 3 * n * sizeof(float)));
+        CU(eng->ties.ensure((n + 1) * sizeof(uint32_t)));
+        CU(cudaMemsetAsync(eng->ties.p, 0, sizeof(uint32_t), eng->stream));
+        const float* x2 = x2max;
+        const float* w2 = eng->w2max.as<float>();
+        const float tau = (float)eng->tau_tc;
         CU(cudaEventRecord(eng->ev[8], eng->stream));
-        CU(tsom::launch_bmu_tc(tiles, n, eng->P, eng->wsplit.as<float>(), x2max,
-                               eng->w2max.as<float>(), (float)eng->tau_tc, eng->part.as<float>(),
-                               eng->sm_count, eng->stream));
+        CU(tsom::launch_bmu_tc(tiles, n, nullptr, false, eng->P, eng->wsplit.as<float>(), x2, w2,
+                               tau, eng->part.as<float>(), eng->sm_count, eng->stream));
         CU(cudaEventRecord(eng->ev[9], eng->stream));
         eng->k1_timed = true;
-        tsom::launch_merge_partials(eng->part.as<float>(), n, groups, gn, x2max,
-                                    eng->w2max.as<float>(), (float)eng->tau_tc, x, sel,
-                                    eng->w.as<float>(), eng->D, eng->bmu.as<uint32_t>(),
-                                    eng->flags.as<uint32_t>(), eng->stream);
+        tsom::launch_merge_fast(eng->part.as<float>(), n, groups, gn, x2, w2, tau,
+                                eng->bmu.as<uint32_t>(), eng->ties.as<uint32_t>(), eng->stream);
+        CU(cudaGetLastError());
+        // near-tie rows (~1%): same tensor-core kernel in enumerate mode on just
+        // those rows, then exact FP64 over their few candidates
+        uint32_t nt = 0;
+        CU(cudaMemcpyAsync(&nt, eng->ties.p, sizeof(uint32_t), cudaMemcpyDeviceToHost, eng->stream));
+        CU(cudaStreamSynchronize(eng->stream));
+        const uint64_t chunk = 1ull << 20;
+        const uint32_t* tpos = eng->ties.as<uint32_t>() + 1;
+        for (uint64_t f0 = 0; f0 < nt; f0 += chunk) {
+            const uint64_t m = std::min<uint64_t>(chunk, nt - f0);
+            const uint64_t mt = (m + tsom::kTcTileM - 1) / tsom::kTcTileM;
+            CU(eng->tsplit.ensure(mt * tile_bytes));
+            CU(eng->part2.ensure((size_t)groups * 3 * m * sizeof(float)));
+            tsom::launch_split_rows(x, sel, tpos + f0, m, eng->D, eng->tsplit.as<float>(),
+                                    eng->stream);
+            CU(tsom::launch_bmu_tc(eng->tsplit.as<float>(), m, nullptr, true, eng->P,
+                                   eng->wsplit.as<float>(), x2, w2, tau, eng->part2.as<float>(),
+                                   eng->sm_count, eng->stream));
+            tsom::launch_merge_partials(eng->part2.as<float>(), tpos + f0, m, groups, gn, x2, w2,
+                                        tau, x, sel, eng->w.as<float>(), eng->D,
+                                        eng->bmu.as<uint32_t>(), eng->flags.as<uint32_t>(),
+                                        eng->stream);
+        }
     } else {
         CU(cudaEventRecord(eng->ev[8], eng->stream));
         tsom::launch_bmu_simt(x, sel, n, eng->D, eng->wt.as<float>(), eng->P, ppad(eng), x2max,
@@ -252,7 +279,7 @@ void accumulate_epoch(Engine* eng, const uint32_t* sel_host, uint64_t n_sel, boo
             if (!eng->xsplit_valid) {
                 const uint64_t ntiles = (eng->n_rows + tsom::kTcTileM - 1) / tsom::kTcTileM;
                 CU(eng->xsplit.ensure(ntiles * 2 * tsom::kTcTileM * tsom::kTcKPad * sizeof(float)));
-                tsom::launch_split_rows(eng->x.as<float>(), nullptr, eng->n_rows, eng->D,
+                tsom::launch_split_rows(eng->x.as<float>(), nullptr, nullptr, eng->n_rows, eng->D,
                                         eng->xsplit.as<float>(), eng->stream);
                 eng->xsplit_valid = true;
             }
@@ -442,7 +469,7 @@ int tsom_destroy(tsom_engine* eng) {
     for (DevBuf* b : {&eng->x, &eng->xsplit, &eng->x2max, &eng->w, &eng->wt, &eng->wsplit, &eng->w2,
                       &eng->w2max, &eng->prev, &eng->infl, &eng->topo_dist, &eng->sel,
                       &eng->rows_scratch, &eng->gsplit, &eng->bmu, &eng->dist, &eng->part,
-                      &eng->flags, &eng->acc_buf[0], &eng->acc_buf[1], &eng->acc_buf[2], &eng->acc_buf[3],
+                      &eng->flags, &eng->ties, &eng->part2, &eng->tsplit, &eng->acc_buf[0], &eng->acc_buf[1], &eng->acc_buf[2], &eng->acc_buf[3],
                       &eng->acc_buf[4], &eng->acc_buf[5], &eng->acc_buf[6], &eng->sums, &eng->U, &eng->H, &eng->status, &eng->smooth_scratch,
                       &eng->stage[0], &eng->stage[1]})
         b->release();

@@ -112,6 +112,9 @@ struct Engine {
     DevBuf dist;
     DevBuf part;           // tcgen05 per-group partial top-2 [groups][n] (b1, i1, b2)
     DevBuf flags;          // [0] full re-scan count, [1] exact-candidate count, then positions
+    DevBuf ties;           // [0] near-tie count, then positions (enumerate pass input)
+    DevBuf part2;          // enumerate-pass partials
+    DevBuf tsplit;         // split tiles of the near-tie rows
     DevBuf acc_buf[7];     // AccumScratch arrays
     tsom::AccumScratch acc;
     uint64_t acc_rows = 0; // capacity the scratch was sized for
@@ -145,9 +148,10 @@ void launch_prep_codebook(const float* w, uint32_t P, uint32_t D, double* w2, fl
 void launch_row_norm_max(const float* x, uint64_t n, uint32_t D, float* out, cudaStream_t st);
 // a[0] = max(a[0], a[1])
 void launch_fold_max(float* a, cudaStream_t st);
-// split rows (optionally gathered through sel) into tcgen05 tiles
-void launch_split_rows(const float* x, const uint32_t* sel, uint64_t n, uint32_t D, float* tiles,
-                       cudaStream_t st);
+// split rows (optionally gathered through sel, and/or through a position list
+// idx: split row f = position idx[f]) into tcgen05 tiles
+void launch_split_rows(const float* x, const uint32_t* sel, const uint32_t* idx, uint64_t n,
+                       uint32_t D, float* tiles, cudaStream_t st);
 bool tc_supported(uint32_t P, uint32_t D);
 // nodes per CTA-resident codebook group (multiple of 16, <= 256)
 __host__ __device__ inline uint32_t tc_group_width(uint32_t P) {
@@ -158,16 +162,22 @@ __host__ __device__ inline uint32_t tc_group_width(uint32_t P) {
 void launch_bmu_simt(const float* x, const uint32_t* sel, uint64_t n, uint32_t D, const float* wt,
                      uint32_t P, uint32_t Ppad, const float* x2max, const float* w2max, float tau,
                      uint32_t* bmu, uint32_t* flags, int sm_count, cudaStream_t st);
-// tcgen05 variant writes per-group partials; merge writes bmu + flags.
-cudaError_t launch_bmu_tc(const float* tiles, uint64_t n, uint32_t P, const float* wsplit,
-                          const float* x2max, const float* w2max, float tau, float* part,
-                          int sm_count, cudaStream_t st);
-// Merge per-group candidates: unique candidate -> bmu; several -> exact FP64
-// evaluation of just those nodes (reference order); overflow -> flags list.
-void launch_merge_partials(const float* part, uint64_t n, uint32_t groups, uint32_t gn,
-                           const float* x2max, const float* w2max, float tau, const float* x,
-                           const uint32_t* sel, const float* w, uint32_t D, uint32_t* bmu,
-                           uint32_t* flags, cudaStream_t st);
+// tcgen05 variant: per-group partials (enumerate = candidate lists; dev_n =
+// optional device row count).
+cudaError_t launch_bmu_tc(const float* tiles, uint64_t n, const uint32_t* dev_n, bool enumerate,
+                          uint32_t P, const float* wsplit, const float* x2max,
+                          const float* w2max, float tau, float* part, int sm_count,
+                          cudaStream_t st);
+// main-pass merge: bmu for rows with a clear winner, near-tie positions -> ties
+void launch_merge_fast(const float* part, uint64_t n, uint32_t groups, uint32_t gn,
+                       const float* x2max, const float* w2max, float tau, uint32_t* bmu,
+                       uint32_t* ties, cudaStream_t st);
+// enumerate-pass merge over the near-tie rows: candidates -> exact FP64 -> bmu;
+// overflow -> flags list for the full re-scan.
+void launch_merge_partials(const float* part, const uint32_t* ties, uint64_t n, uint32_t groups,
+                           uint32_t gn, const float* x2max, const float* w2max, float tau,
+                           const float* x, const uint32_t* sel, const float* w, uint32_t D,
+                           uint32_t* bmu, uint32_t* flags, cudaStream_t st);
 // exact FP64 re-scan of flagged rows (reference loop order)
 void launch_rescan(const float* x, const uint32_t* sel, const float* w, uint32_t P, uint32_t D,
                    const uint32_t* flags, uint64_t n, uint32_t* bmu, cudaStream_t st);

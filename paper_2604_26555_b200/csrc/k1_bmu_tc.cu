@@ -19,8 +19,9 @@
 //   warp 1      : MMA issuer — one elected thread, 21 tcgen05.mma per tile
 //                 (M=128 rows x N=gn nodes x K=8, three products x 7 k-steps)
 //   warp 2      : TMEM allocator (2 accumulator buffers x gn columns)
-//   warps 4..7  : epilogue — tcgen05.ld 32 lanes x 32 columns, per-row top-2
-//                 (thread = row, so the argmin is thread-local), partials out
+//   warps 4..7  : epilogue — warp q+4 owns TMEM lanes 32q.. (tile rows) and all
+//                 columns; pipelined tcgen05.ld x32, eight independent top-2
+//                 streams per thread, candidate enumeration for near-ties
 // Samples sit on the TMEM lane axis, so no cross-lane reduction is needed.
 #include <cuda_runtime.h>
 #include <math_constants.h>
@@ -33,8 +34,8 @@ namespace tsom {
 
 namespace {
 
-constexpr int kThreads = 384;          // 4 role warps + 8 epilogue warps
-constexpr uint32_t kEpiThreads = 256;
+constexpr int kThreads = 384;          // 4 role warps + 2 sets x 4 epilogue warps
+constexpr uint32_t kEpiThreads = 128;   // arrivals per accumulator buffer (one set)
 constexpr int kStages = 2;
 constexpr uint32_t kTileBytes = 2u * kTcTileM * kTcKPad * 4u;  // 57,344 (hi + lo)
 constexpr uint32_t kHalfTile = kTcTileM * kTcKPad * 4u;         // 28,672
@@ -146,10 +147,6 @@ __device__ __forceinline__ void tmem_wait_ld() {
 
 }  // namespace
 
-__device__ __forceinline__ void named_bar(uint32_t id, uint32_t nthreads) {
-    asm volatile("bar.sync %0, %1;" ::"r"(id), "r"(nthreads) : "memory");
-}
-
 // branch-free top-2 step: strict < keeps the earliest j on ties, an exact tie
 // lands in b2 (gap 0 => candidate enumeration)
 __device__ __forceinline__ void top2_step(float v, uint32_t j, float& b1, uint32_t& i1,
@@ -175,11 +172,19 @@ __device__ __forceinline__ void top2_merge_dev(float& b1, uint32_t& i1, float& b
 // whose computed value lies within thr of the group's best; count 15 = overflow.
 constexpr uint32_t kCandOverflow = 15u;
 
+// kEnum = false (main pass): per (row, group) the top-2 (b1, i1, b2) only.
+// kEnum = true (near-tie rows only, see k_merge_fast): per (row, group) the best
+// value plus up to 4 local candidate ids within thr of it (count 15 = overflow).
+// dev_n (optional): row count read on the device (the near-tie list length).
+template <bool kEnum>
 __global__ void __launch_bounds__(kThreads, 1)
-    k1_bmu_tc(const float* __restrict__ tiles, uint64_t n, uint32_t ntiles, uint32_t groups,
-              uint32_t gn, const float* __restrict__ wsplit, const float* __restrict__ x2max,
-              const float* __restrict__ w2max, float tau, float* __restrict__ part) {
+    k1_bmu_tc(const float* __restrict__ tiles, uint64_t n_host, const uint32_t* __restrict__ dev_n,
+              uint32_t groups, uint32_t gn, const float* __restrict__ wsplit,
+              const float* __restrict__ x2max, const float* __restrict__ w2max, float tau,
+              float* __restrict__ part) {
     extern __shared__ __align__(1024) uint8_t smem[];
+    const uint64_t n = dev_n ? (uint64_t)*dev_n : n_host;
+    const uint32_t ntiles = (uint32_t)((n + kTcTileM - 1) / kTcTileM);
     const uint32_t w_bytes = 2u * kTcKPad * gn * 4u;  // hi + lo of this CTA's group
     uint8_t* sW = smem;
     uint8_t* sX = smem + ((w_bytes + 1023u) & ~1023u);
@@ -190,7 +195,6 @@ __global__ void __launch_bounds__(kThreads, 1)
     uint64_t* tempty_bar = bars + 6;  // [2] accumulator drained
     uint64_t* w_bar = bars + 8;       // codebook group landed
     uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(bars + 9);
-    uint32_t* xch = reinterpret_cast<uint32_t*>(bars + 10);  // [4 quarters][160]
 
     const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
     const uint32_t g = blockIdx.x % groups;
@@ -222,7 +226,7 @@ __global__ void __launch_bounds__(kThreads, 1)
     const uint32_t tmem_base = *tmem_slot;
 
     if (warp == 0) {
-        if (lane == 0) {
+        if (lane == 0 && ntiles > cta_in_group) {
             // resident codebook group (hi and lo halves, each < 2^20 B of tx count)
             mbar_expect_tx(w_bar, w_bytes);
             const float* wg = wsplit + (size_t)g * 2 * kTcKPad * gn;
@@ -241,7 +245,7 @@ __global__ void __launch_bounds__(kThreads, 1)
             }
         }
     } else if (warp == 1) {
-        if (lane == 0) {
+        if (lane == 0 && ntiles > cta_in_group) {
             const uint32_t idesc = idesc_tf32(kTcTileM, gn);
             const uint32_t w_lbo = gn * 16u;
             const uint32_t sw = smem_u32(sW);
@@ -278,119 +282,96 @@ __global__ void __launch_bounds__(kThreads, 1)
             }
         }
     } else if (warp >= 4) {
-        // 8 epilogue warps: quarter q = TMEM lanes 32q..32q+31 (= tile rows), half h
-        // = which half of the group's columns.  Thread = row: top-2 is thread-local.
-        const uint32_t q = warp & 3, h = (warp - 4) >> 2;
+        // 2 sets x 4 epilogue warps: set s drains accumulator buffer s (every
+        // other tile), so two warps per SM sub-partition hide each other's
+        // latency without exchanging anything.  Warp (set, q) owns TMEM lanes
+        // 32q..32q+31 (= tile rows) and all gn columns; thread = row.
+        const uint32_t q = warp & 3, set = (warp - 4) >> 2;
         const uint32_t row = q * 32 + lane;
-        const uint32_t half_cols = gn >> 1;  // multiple of 16
-        const uint32_t c0 = h * half_cols;
-        const float thr = tau * (__ldg(x2max) + __ldg(w2max));
-        uint32_t* xq = xch + q * 160;  // [b1 | i1 | b2] x 32 lanes
-        uint32_t* xp = xq + 96;        // [pack | cnt] x 32 lanes
-        uint32_t acc = 0, acc_phase = 0;
-        for (uint32_t t = cta_in_group; t < ntiles; t += ctas_per_group) {
+        const uint32_t nfull = gn / 32, tail16 = (gn % 32) != 0;
+        const uint32_t acc = set;
+        uint32_t acc_phase = 0;
+        for (uint32_t t = cta_in_group + set * ctas_per_group; t < ntiles;
+             t += 2 * ctas_per_group) {
             mbar_wait(&tfull_bar[acc], acc_phase);
             tc_fence_after();
-            const uint32_t taddr = tmem_base + ((q * 32u) << 16) + acc * acc_cols + c0;
-            // pass 1: four independent top-2 streams (ILP), then fold
-            float b1[4], b2[4];
-            uint32_t i1[4];
+            const uint32_t taddr = tmem_base + ((q * 32u) << 16) + acc * acc_cols;
+            // pass 1: eight independent top-2 streams (ILP), TMEM loads pipelined
+            float b1[8], b2[8];
+            uint32_t i1[8];
 #pragma unroll
-            for (int s = 0; s < 4; ++s) {
-                b1[s] = CUDART_INF_F;
-                b2[s] = CUDART_INF_F;
-                i1[s] = 0;
+            for (int s2 = 0; s2 < 8; ++s2) {
+                b1[s2] = CUDART_INF_F;
+                b2[s2] = CUDART_INF_F;
+                i1[s2] = 0;
             }
-            uint32_t c = 0;
-            for (; c + 32 <= half_cols; c += 32) {
-                uint32_t r[32];
-                TMEM_LD32(taddr + c, r);
+            uint32_t ra[32], rb[32];
+            if (nfull) TMEM_LD32(taddr, ra);
+            for (uint32_t c = 0; c < nfull; c += 2) {
                 tmem_wait_ld();
+                if (c + 1 < nfull) TMEM_LD32(taddr + (c + 1) * 32, rb);
 #pragma unroll
                 for (int k = 0; k < 32; ++k)
-                    top2_step(__uint_as_float(r[k]), c0 + c + k, b1[k & 3], i1[k & 3], b2[k & 3]);
+                    top2_step(__uint_as_float(ra[k]), c * 32 + k, b1[k & 7], i1[k & 7], b2[k & 7]);
+                if (c + 1 < nfull) {
+                    tmem_wait_ld();
+                    if (c + 2 < nfull) TMEM_LD32(taddr + (c + 2) * 32, ra);
+#pragma unroll
+                    for (int k = 0; k < 32; ++k)
+                        top2_step(__uint_as_float(rb[k]), (c + 1) * 32 + k, b1[k & 7], i1[k & 7],
+                                  b2[k & 7]);
+                }
             }
-            if (c < half_cols) {
+            if (tail16) {
                 uint32_t r[16];
-                TMEM_LD16(taddr + c, r);
+                TMEM_LD16(taddr + nfull * 32, r);
                 tmem_wait_ld();
 #pragma unroll
                 for (int k = 0; k < 16; ++k)
-                    top2_step(__uint_as_float(r[k]), c0 + c + k, b1[k & 3], i1[k & 3], b2[k & 3]);
+                    top2_step(__uint_as_float(r[k]), nfull * 32 + k, b1[k & 7], i1[k & 7], b2[k & 7]);
             }
 #pragma unroll
-            for (int s = 1; s < 4; ++s) top2_merge_dev(b1[0], i1[0], b2[0], b1[s], i1[s], b2[s]);
-            float B1 = b1[0], B2 = b2[0];
-            uint32_t I1 = i1[0];
-            // fold the two column halves through shared memory
-            if (h == 1) {
-                xq[lane] = __float_as_uint(B1);
-                xq[32 + lane] = I1;
-                xq[64 + lane] = __float_as_uint(B2);
-            }
-            named_bar(1 + q, 64);
-            if (h == 0) {
-                top2_merge_dev(B1, I1, B2, __uint_as_float(xq[lane]), xq[32 + lane],
-                               __uint_as_float(xq[64 + lane]));
-                xq[lane] = __float_as_uint(B1);
-                xq[32 + lane] = I1;
-                xq[64 + lane] = __float_as_uint(B2);
-            }
-            named_bar(1 + q, 64);
-            if (h == 1) {
-                B1 = __uint_as_float(xq[lane]);
-                I1 = xq[32 + lane];
-                B2 = __uint_as_float(xq[64 + lane]);
-            }
-            // pass 2 (rare): enumerate this half's candidates v <= B1 + thr, ascending j
-            const bool need = !(B2 - B1 > thr);
-            uint32_t pack = 0, cnt = 0;
-            if (__any_sync(0xffffffffu, need)) {
-                const float lim = B1 + thr;
-                for (uint32_t cc = 0; cc < half_cols; cc += 16) {
-                    uint32_t r[16];
-                    TMEM_LD16(taddr + cc, r);
-                    tmem_wait_ld();
+            for (int s2 = 1; s2 < 8; ++s2)
+                top2_merge_dev(b1[0], i1[0], b2[0], b1[s2], i1[s2], b2[s2]);
+            const float B1 = b1[0], B2 = b2[0];
+            const uint32_t I1 = i1[0];
+            uint32_t w1 = I1, w2 = __float_as_uint(B2);
+            if (kEnum) {
+                // enumerate the row's candidates v <= B1 + thr in ascending j
+                const float thr = tau * (__ldg(x2max) + __ldg(w2max));
+                const bool need = !(B2 - B1 > thr);
+                w2 = 1;
+                if (__any_sync(0xffffffffu, need)) {
+                    const float lim = B1 + thr;
+                    uint32_t pk = 0, nc = 0;
+                    for (uint32_t cc = 0; cc < gn; cc += 16) {
+                        uint32_t r[16];
+                        TMEM_LD16(taddr + cc, r);
+                        tmem_wait_ld();
 #pragma unroll
-                    for (int k = 0; k < 16; ++k) {
-                        if (need && __uint_as_float(r[k]) <= lim) {
-                            if (cnt < 4) pack |= (c0 + cc + k) << (8 * cnt);
-                            ++cnt;
+                        for (int k = 0; k < 16; ++k) {
+                            if (need && __uint_as_float(r[k]) <= lim) {
+                                if (nc < 4) pk |= (cc + k) << (8 * nc);
+                                ++nc;
+                            }
                         }
+                    }
+                    if (need) {
+                        w1 = pk;
+                        w2 = (nc >= 1 && nc <= 4) ? nc : kCandOverflow;
                     }
                 }
             }
             tc_fence_before();
             mbar_arrive(&tempty_bar[acc]);  // this thread is done with the accumulator
-            if (h == 1) {
-                xp[lane] = pack;
-                xp[32 + lane] = cnt;
+            const uint64_t pos = (uint64_t)t * kTcTileM + row;
+            if (pos < n) {
+                float* pg = part + (size_t)g * 3 * n;
+                pg[pos] = B1;
+                pg[n + pos] = __uint_as_float(w1);
+                pg[2 * n + pos] = __uint_as_float(w2);
             }
-            named_bar(1 + q, 64);
-            if (h == 0) {
-                uint32_t out_pack = I1, out_cnt = 1;
-                if (need) {
-                    const uint32_t p1 = xp[lane], n1 = xp[32 + lane];
-                    const uint32_t total = cnt + n1;
-                    if (cnt > 4 || n1 > 4 || total > 4 || total == 0) {
-                        out_cnt = kCandOverflow;
-                    } else {
-                        out_pack = pack | (n1 ? (p1 << (8 * cnt)) : 0u);
-                        out_cnt = total;
-                    }
-                }
-                const uint64_t pos = (uint64_t)t * kTcTileM + row;
-                if (pos < n) {
-                    float* pg = part + (size_t)g * 3 * n;
-                    pg[pos] = B1;
-                    pg[n + pos] = __uint_as_float(out_pack);
-                    pg[2 * n + pos] = __uint_as_float(out_cnt);
-                }
-            }
-            if (++acc == 2) {
-                acc = 0;
-                acc_phase ^= 1;
-            }
+            acc_phase ^= 1;
         }
     }
     tc_fence_before();
@@ -404,28 +385,30 @@ __global__ void __launch_bounds__(kThreads, 1)
 
 bool tc_supported(uint32_t P, uint32_t D) { return P >= 1 && D + 2 <= (uint32_t)kTcKPad; }
 
-cudaError_t launch_bmu_tc(const float* tiles, uint64_t n, uint32_t P, const float* wsplit,
-                          const float* x2max, const float* w2max, float tau, float* part,
-                          int sm_count, cudaStream_t st) {
+cudaError_t launch_bmu_tc(const float* tiles, uint64_t n, const uint32_t* dev_n, bool enumerate,
+                          uint32_t P, const float* wsplit, const float* x2max,
+                          const float* w2max, float tau, float* part, int sm_count,
+                          cudaStream_t st) {
     if (n == 0) return cudaSuccess;
     const uint32_t gn = tc_group_width(P);
     const uint32_t groups = (P + gn - 1) / gn;
-    const uint32_t ntiles = (uint32_t)((n + kTcTileM - 1) / kTcTileM);
+    const uint32_t ntiles = (uint32_t)((n + kTcTileM - 1) / kTcTileM);  // upper bound
     uint32_t per_group = (uint32_t)sm_count / groups;
     if (per_group < 1) per_group = 1;
     if (per_group > ntiles) per_group = ntiles;
     const uint32_t grid = per_group * groups;
     const uint32_t w_bytes = 2u * kTcKPad * gn * 4u;
-    const size_t smem = ((w_bytes + 1023u) & ~1023u) + kStages * kTileBytes + 80 + 4 * 160 * 4;
-    static size_t attr = 0;
-    if (attr < smem) {
-        cudaError_t e =
-            cudaFuncSetAttribute(k1_bmu_tc, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+    const size_t smem = ((w_bytes + 1023u) & ~1023u) + kStages * kTileBytes + 80;
+    auto kern = enumerate ? k1_bmu_tc<true> : k1_bmu_tc<false>;
+    static size_t attr[2] = {0, 0};
+    if (attr[enumerate] < smem) {
+        cudaError_t e = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                             (int)smem);
         if (e != cudaSuccess) return e;
-        attr = smem;
+        attr[enumerate] = smem;
     }
-    TSOM_LAUNCH(k1_bmu_tc<<<grid, kThreads, smem, st>>>(tiles, n, ntiles, groups, gn, wsplit, x2max,
-                                                        w2max, tau, part));
+    TSOM_LAUNCH(kern<<<grid, kThreads, smem, st>>>(tiles, n, dev_n, groups, gn, wsplit, x2max,
+                                                   w2max, tau, part));
     return cudaGetLastError();
 }
 

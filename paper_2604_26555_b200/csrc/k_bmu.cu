@@ -297,89 +297,119 @@ __device__ __forceinline__ double exact_d2(const float* __restrict__ x,
     return acc;
 }
 
-// part[g] = [b1 | packed local candidate ids | count] (k1_bmu_tc.cu epilogue)
-__global__ void k_merge_partials(const float* __restrict__ part, uint64_t n, uint32_t groups,
-                                 uint32_t gn, const float* __restrict__ x2max,
+// Main-pass merge.  part[g] = [b1 | i1 | b2] per row (k1_bmu_tc<false>).  A row
+// whose global best is separated from every other node by more than the FP32
+// error window thr gets its BMU here; otherwise its position joins `ties`
+// ([0] = count, positions from [1]) for the enumerate pass.
+__global__ void k_merge_fast(const float* __restrict__ part, uint64_t n, uint32_t groups,
+                             uint32_t gn, const float* __restrict__ x2max,
+                             const float* __restrict__ w2max, float tau,
+                             uint32_t* __restrict__ bmu, uint32_t* __restrict__ ties) {
+    const uint64_t i = blockIdx.x * (uint64_t)blockDim.x + threadIdx.x;
+    if (i >= n) return;
+    const float thr = tau * (__ldg(x2max) + __ldg(w2max));
+    float B1 = CUDART_INF_F, B2 = CUDART_INF_F;
+    uint32_t I1 = 0;
+    for (uint32_t g0 = 0; g0 < groups; g0 += 8) {
+        float b1v[8], b2v[8];
+        uint32_t i1v[8];
+#pragma unroll
+        for (uint32_t q = 0; q < 8; ++q) {
+            if (g0 + q < groups) {
+                const float* pg = part + (size_t)(g0 + q) * 3 * n;
+                b1v[q] = pg[i];
+                i1v[q] = __float_as_uint(pg[n + i]);
+                b2v[q] = pg[2 * n + i];
+            }
+        }
+#pragma unroll
+        for (uint32_t q = 0; q < 8; ++q)  // ascending groups = ascending node ids
+            if (g0 + q < groups)
+                top2_merge(B1, I1, B2, b1v[q], (g0 + q) * gn + i1v[q], b2v[q]);
+    }
+    bmu[i] = I1;
+    if (!(B2 - B1 > thr)) {
+        const uint32_t slot = atomicAdd(&ties[0], 1u);
+        ties[1 + slot] = (uint32_t)i;
+    }
+}
+
+void launch_merge_fast(const float* part, uint64_t n, uint32_t groups, uint32_t gn,
+                       const float* x2max, const float* w2max, float tau, uint32_t* bmu,
+                       uint32_t* ties, cudaStream_t st) {
+    if (n == 0) return;
+    TSOM_LAUNCH(k_merge_fast<<<(unsigned)((n + 255) / 256), 256, 0, st>>>(
+        part, n, groups, gn, x2max, w2max, tau, bmu, ties));
+}
+
+
+// Enumerate-pass merge over the near-tie rows f < n (position ties[f]).
+// part[g] = [b1 | packed local candidate ids | count] (k1_bmu_tc<true>).
+// One candidate -> bmu; several -> exact FP64 distances of just those nodes in
+// ascending node order with strict < (lowest index wins), as find_bmus
+// (trainer.hpp:293-304); > 4 candidates in a group -> full exact re-scan list.
+__global__ void k_merge_partials(const float* __restrict__ part, const uint32_t* __restrict__ ties,
+                                 uint64_t n, uint32_t groups, uint32_t gn, const float* __restrict__ x2max,
                                  const float* __restrict__ w2max, float tau,
                                  const float* __restrict__ x, const uint32_t* __restrict__ sel,
                                  const float* __restrict__ w, uint32_t D,
                                  uint32_t* __restrict__ bmu, uint32_t* __restrict__ flags) {
-    const uint64_t i = blockIdx.x * (uint64_t)blockDim.x + threadIdx.x;
-    if (i >= n) return;
     const float thr = tau * (__ldg(x2max) + __ldg(w2max));
-    // all partials of the row in one round of independent loads (groups <= 8
-    // stay in registers; larger codebooks stream in chunks of 8)
-    constexpr uint32_t kG = 8;
-    float b1v[kG];
-    uint32_t pk[kG], ct[kG];
-    float B1 = CUDART_INF_F;
-    for (uint32_t g0 = 0; g0 < groups; g0 += kG) {
-#pragma unroll
-        for (uint32_t q = 0; q < kG; ++q)
-            if (g0 + q < groups) B1 = fminf(B1, part[(size_t)(g0 + q) * 3 * n + i]);
-    }
-    const float lim = B1 + thr;
-    uint32_t ncand = 0, only = 0;
-    bool overflow = false;
-    for (uint32_t g0 = 0; g0 < groups; g0 += kG) {
-#pragma unroll
-        for (uint32_t q = 0; q < kG; ++q) {
-            if (g0 + q < groups) {
-                const float* pg = part + (size_t)(g0 + q) * 3 * n;
-                b1v[q] = pg[i];
-                pk[q] = __float_as_uint(pg[n + i]);
-                ct[q] = __float_as_uint(pg[2 * n + i]);
+    for (uint64_t f = blockIdx.x * (uint64_t)blockDim.x + threadIdx.x; f < n;
+         f += (uint64_t)gridDim.x * blockDim.x) {
+        const uint32_t pos = ties[f];
+        float B1 = CUDART_INF_F;
+        for (uint32_t g = 0; g < groups; ++g) B1 = fminf(B1, part[(size_t)g * 3 * n + f]);
+        const float lim = B1 + thr;
+        uint32_t ncand = 0, only = 0;
+        bool overflow = false;
+        for (uint32_t g = 0; g < groups; ++g) {
+            const float* pg = part + (size_t)g * 3 * n;
+            if (!(pg[f] <= lim)) continue;
+            const uint32_t cnt = __float_as_uint(pg[2 * n + f]);
+            if (cnt > 4) overflow = true;
+            ncand += cnt;
+            only = g * gn + (__float_as_uint(pg[n + f]) & 0xFFu);
+        }
+        if (overflow || ncand == 0) {
+            const uint32_t slot = atomicAdd(&flags[0], 1u);
+            flags[2 + slot] = pos;
+            bmu[pos] = only;
+            continue;
+        }
+        if (ncand == 1) {
+            bmu[pos] = only;
+            continue;
+        }
+        atomicAdd(&flags[1], 1u);
+        const float* xr = x + (sel ? (uint64_t)sel[pos] : (uint64_t)pos) * D;
+        double best = CUDART_INF;
+        uint32_t best_j = 0;
+        for (uint32_t g = 0; g < groups; ++g) {
+            const float* pg = part + (size_t)g * 3 * n;
+            if (!(pg[f] <= lim)) continue;
+            const uint32_t cnt = __float_as_uint(pg[2 * n + f]);
+            const uint32_t pack = __float_as_uint(pg[n + f]);
+            for (uint32_t c = 0; c < cnt; ++c) {
+                const uint32_t j = g * gn + ((pack >> (8 * c)) & 0xFFu);
+                const double d2 = exact_d2(xr, w + (size_t)j * D, D);
+                if (d2 < best) {
+                    best = d2;
+                    best_j = j;
+                }
             }
         }
-#pragma unroll
-        for (uint32_t q = 0; q < kG; ++q) {
-            if (g0 + q < groups && b1v[q] <= lim) {
-                if (ct[q] > 4) overflow = true;
-                ncand += ct[q];
-                only = (g0 + q) * gn + (pk[q] & 0xFFu);
-            }
-        }
+        bmu[pos] = best_j;
     }
-    if (overflow || ncand == 0) {  // > 4 near-ties inside a group: full exact re-scan
-        const uint32_t slot = atomicAdd(&flags[0], 1u);
-        flags[2 + slot] = (uint32_t)i;
-        bmu[i] = only;
-        return;
-    }
-    if (ncand == 1) {
-        bmu[i] = only;
-        return;
-    }
-    // several candidates: exact FP64 distances of just those nodes, ascending node
-    // order with strict < (lowest index wins ties), as find_bmus (trainer.hpp:293-304)
-    atomicAdd(&flags[1], 1u);
-    const float* xr = x + (sel ? (uint64_t)sel[i] : i) * D;
-    double best = CUDART_INF;
-    uint32_t best_j = 0;
-    for (uint32_t g = 0; g < groups; ++g) {
-        const float* pg = part + (size_t)g * 3 * n;
-        if (!(pg[i] <= lim)) continue;
-        const uint32_t cnt = __float_as_uint(pg[2 * n + i]);
-        const uint32_t pack = __float_as_uint(pg[n + i]);
-        for (uint32_t c = 0; c < cnt; ++c) {
-            const uint32_t j = g * gn + ((pack >> (8 * c)) & 0xFFu);
-            const double d2 = exact_d2(xr, w + (size_t)j * D, D);
-            if (d2 < best) {
-                best = d2;
-                best_j = j;
-            }
-        }
-    }
-    bmu[i] = best_j;
 }
 
-void launch_merge_partials(const float* part, uint64_t n, uint32_t groups, uint32_t gn,
-                           const float* x2max, const float* w2max, float tau, const float* x,
-                           const uint32_t* sel, const float* w, uint32_t D, uint32_t* bmu,
-                           uint32_t* flags, cudaStream_t st) {
+void launch_merge_partials(const float* part, const uint32_t* ties, uint64_t n, uint32_t groups,
+                           uint32_t gn, const float* x2max, const float* w2max, float tau,
+                           const float* x, const uint32_t* sel, const float* w, uint32_t D,
+                           uint32_t* bmu, uint32_t* flags, cudaStream_t st) {
     if (n == 0) return;
     TSOM_LAUNCH(k_merge_partials<<<(unsigned)((n + 255) / 256), 256, 0, st>>>(
-        part, n, groups, gn, x2max, w2max, tau, x, sel, w, D, bmu, flags));
+        part, ties, n, groups, gn, x2max, w2max, tau, x, sel, w, D, bmu, flags));
 }
 
 // ---------------------------------------------------------------------------
@@ -445,43 +475,51 @@ void launch_rescan(const float* x, const uint32_t* sel, const float* w, uint32_t
 // pieces), else 0.  Rows past n are zero (their results are ignored).
 
 __global__ void k_split_rows(const float* __restrict__ x, const uint32_t* __restrict__ sel,
-                             uint64_t n, uint32_t D, float* __restrict__ tiles) {
-    const uint64_t tile = blockIdx.x;
+                             const uint32_t* __restrict__ idx, uint64_t n, uint32_t D,
+                             float* __restrict__ tiles) {
+    // idx (optional): positions; split row f is then position idx[f]
+    const uint64_t ntiles = (n + kTcTileM - 1) / kTcTileM;
     const int r = threadIdx.x;  // 128 threads, one row each
-    const uint64_t pos = tile * kTcTileM + r;
-    float* base = tiles + tile * 2 * kTcTileM * kTcKPad;
-    const bool valid = pos < n;
-    const float* src = nullptr;
-    if (valid) src = x + (sel ? (uint64_t)sel[pos] : pos) * D;
-    for (uint32_t kc = 0; kc < kTcKPad / 4; ++kc) {
-        float hi[4], lo[4];
-#pragma unroll
-        for (int q = 0; q < 4; ++q) {
-            const uint32_t k = kc * 4 + q;
-            float val;
-            if (!valid)
-                val = 0.0f;
-            else if (k < D)
-                val = src[k];
-            else if (k == D || k == D + 1)
-                val = 1.0f;
-            else
-                val = 0.0f;
-            hi[q] = tf32_hi(val);
-            lo[q] = val - hi[q];
+    for (uint64_t tile = blockIdx.x; tile < ntiles; tile += gridDim.x) {
+        const uint64_t f = tile * kTcTileM + r;
+        float* base = tiles + tile * 2 * kTcTileM * kTcKPad;
+        const bool valid = f < n;
+        const float* src = nullptr;
+        if (valid) {
+            const uint64_t pos = idx ? (uint64_t)idx[f] : f;
+            src = x + (sel ? (uint64_t)sel[pos] : pos) * D;
         }
-        const size_t off = ((size_t)kc * kTcTileM + r) * 4;
-        *reinterpret_cast<float4*>(base + off) = make_float4(hi[0], hi[1], hi[2], hi[3]);
-        *reinterpret_cast<float4*>(base + (size_t)kTcTileM * kTcKPad + off) =
-            make_float4(lo[0], lo[1], lo[2], lo[3]);
+        for (uint32_t kc = 0; kc < kTcKPad / 4; ++kc) {
+            float hi[4], lo[4];
+#pragma unroll
+            for (int q = 0; q < 4; ++q) {
+                const uint32_t k = kc * 4 + q;
+                float val;
+                if (!valid)
+                    val = 0.0f;
+                else if (k < D)
+                    val = src[k];
+                else if (k == D || k == D + 1)
+                    val = 1.0f;
+                else
+                    val = 0.0f;
+                hi[q] = tf32_hi(val);
+                lo[q] = val - hi[q];
+            }
+            const size_t off = ((size_t)kc * kTcTileM + r) * 4;
+            *reinterpret_cast<float4*>(base + off) = make_float4(hi[0], hi[1], hi[2], hi[3]);
+            *reinterpret_cast<float4*>(base + (size_t)kTcTileM * kTcKPad + off) =
+                make_float4(lo[0], lo[1], lo[2], lo[3]);
+        }
     }
 }
 
-void launch_split_rows(const float* x, const uint32_t* sel, uint64_t n, uint32_t D, float* tiles,
-                       cudaStream_t st) {
+void launch_split_rows(const float* x, const uint32_t* sel, const uint32_t* idx, uint64_t n,
+                       uint32_t D, float* tiles, cudaStream_t st) {
     if (n == 0) return;
-    const uint64_t tiles_n = (n + kTcTileM - 1) / kTcTileM;
-    TSOM_LAUNCH(k_split_rows<<<(unsigned)tiles_n, kTcTileM, 0, st>>>(x, sel, n, D, tiles));
+    uint64_t tiles_n = (n + kTcTileM - 1) / kTcTileM;
+    if (tiles_n > 148ull * 64) tiles_n = 148ull * 64;
+    TSOM_LAUNCH(k_split_rows<<<(unsigned)tiles_n, kTcTileM, 0, st>>>(x, sel, idx, n, D, tiles));
 }
 
 }  // namespace tsom
