@@ -54,53 +54,52 @@ def peaks():
 
 
 class ClockSampler:
-    """nvidia-smi clocks + throttle reasons during the timed region."""
+    """SM clock + throttle reasons sampled every 20 ms (NVML) during the timed region."""
 
-    def __init__(self, index=0):
-        self.index = index
+    NAMES = {"hw_slowdown": 0x8, "hw_thermal_slowdown": 0x40, "sw_thermal_slowdown": 0x20,
+             "sw_power_cap": 0x4}
+
+    def __init__(self, index=0, period=0.02):
+        self.index, self.period = index, period
         self.samples = []
         self._stop = threading.Event()
-        self._proc = None
+        self._t = None
+        self.max_mhz = None
 
     def __enter__(self):
-        q = ("clocks.sm,clocks.max.sm,power.draw,clocks_event_reasons.active,"
-             "clocks_event_reasons.hw_slowdown,clocks_event_reasons.hw_thermal_slowdown,"
-             "clocks_event_reasons.sw_thermal_slowdown,clocks_event_reasons.sw_power_cap")
         try:
-            self._proc = subprocess.Popen(
-                ["nvidia-smi", "-i", str(self.index), f"--query-gpu={q}", "--format=csv,noheader,nounits",
-                 "-lms", "100"], stdout=subprocess.PIPE, stderr=subprocess.DEVNULL, text=True)
-            self._t = threading.Thread(target=self._read, daemon=True)
+            import pynvml
+            pynvml.nvmlInit()
+            h = pynvml.nvmlDeviceGetHandleByIndex(self.index)
+            self.max_mhz = pynvml.nvmlDeviceGetMaxClockInfo(h, pynvml.NVML_CLOCK_SM)
+
+            def run():
+                while not self._stop.is_set():
+                    try:
+                        sm = pynvml.nvmlDeviceGetClockInfo(h, pynvml.NVML_CLOCK_SM)
+                        rs = pynvml.nvmlDeviceGetCurrentClocksEventReasons(h)
+                        self.samples.append((sm, rs))
+                    except Exception:
+                        pass
+                    self._stop.wait(self.period)
+            self._t = threading.Thread(target=run, daemon=True)
             self._t.start()
         except Exception:
-            self._proc = None
+            self._t = None
         return self
 
-    def _read(self):
-        for line in self._proc.stdout:
-            parts = [p.strip() for p in line.split(",")]
-            if len(parts) >= 8:
-                self.samples.append(parts)
-
     def __exit__(self, *exc):
-        if self._proc:
-            self._proc.terminate()
-            try:
-                self._proc.wait(timeout=5)
-            except Exception:
-                self._proc.kill()
+        self._stop.set()
+        if self._t:
+            self._t.join(timeout=2)
 
     def summary(self):
         if not self.samples:
-            return {"sm_mhz": None, "sm_max_mhz": None, "reasons": ["unsampled"]}
-        sm = [float(s[0]) for s in self.samples if s[0].replace(".", "").isdigit()]
-        mx = [float(s[1]) for s in self.samples if s[1].replace(".", "").isdigit()]
-        names = ["hw_slowdown", "hw_thermal_slowdown", "sw_thermal_slowdown", "sw_power_cap"]
-        reasons = sorted({names[i] for s in self.samples for i in range(4)
-                          if s[4 + i].lower() == "active"})
-        return {"sm_mhz": statistics.median(sm) if sm else None,
-                "sm_max_mhz": max(mx) if mx else None, "reasons": reasons,
-                "samples": len(self.samples)}
+            return {"sm_mhz": None, "sm_max_mhz": self.max_mhz, "reasons": ["unsampled"]}
+        sm = [s[0] for s in self.samples]
+        reasons = sorted({k for _, rs in self.samples for k, bit in self.NAMES.items() if rs & bit})
+        return {"sm_mhz": statistics.median(sm), "sm_max_mhz": self.max_mhz, "reasons": reasons,
+                "samples": len(self.samples), "sm_mhz_min": min(sm)}
 
 
 def dist_env():
@@ -239,7 +238,7 @@ def run_gpu_arm(args):
     stream = torch.cuda.ExternalStream(eng.stream, device=f"cuda:{local}")
     ev0, ev1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
     launches0 = _lib.kernel_launches()
-    k1_ms, total_ms, rechecks = [], [], []
+    k1_ms, total_ms, rechecks, phases = [], [], [], []
     if world > 1:
         dist.barrier()
     torch.cuda.synchronize()
@@ -249,6 +248,7 @@ def run_gpu_arm(args):
             epoch(t)
             det = eng.timing_detail()
             k1_ms.append(det["k1_ms"])
+            phases.append(det)
             total_ms.append(det["total_ms"])
             rechecks.append(eng.last_recheck_count)
         ev1.record(stream)
@@ -265,26 +265,51 @@ def run_gpu_arm(args):
     s, c = eng.qe()
     qe_gpu = s / c
 
-    # e2e through the public C++ API (reference loop + CudaExecutor), rank 0 only
+    eng.close()
+    eng = None
+    # e2e through the public C-ABI with HOST buffers (rank 0, N=1): bind the host
+    # rows (H2D), run the epochs, read the codebook back (D2H) — all inside the
+    # wall-clock region; then the same workload through the reference's own
+    # training loop with the CudaExecutor plugin (libtsom_dropin.so).
     e2e = None
     if rank == 0 and world == 1 and not args.no_e2e:
+        def cabi_run(epochs):
+            t0 = time.perf_counter()
+            e = tsom.Engine(P, D, device=local)
+            if args.kernel:
+                e.set_option(_lib.TSOM_OPT_BMU_KERNEL, args.kernel)
+            e.bind(host)
+            e.set_codebook(w0)
+            e.set_topology_distance(lattice_dist("hex", *P_GRID))
+            for t in range(epochs):
+                eta = schedule_value(0.5, "linear", t, epochs, 1e-4)
+                sigma = schedule_value(sigma0, "linear", t, epochs, 0.3)
+                e.train_epoch(eta, sigma)
+            wf = e.get_codebook()
+            e.close()
+            return time.perf_counter() - t0, wf
+        cabi_run(1)  # warm-up (allocations, module load)
+        secs, _ = cabi_run(EPOCHS)
+        h2d = n * D * 4 + P * D * 4 + P * P * 8
+        d2h = P * D * 4
+        e2e = {"value": n * EPOCHS / secs, "unit": UNIT,
+               "h2d_bytes_per_step": int(h2d / EPOCHS), "d2h_bytes_per_step": int(d2h / EPOCHS),
+               "path": "C-ABI tsom_bind_host_data + 10 x tsom_train_epoch + tsom_get_codebook "
+                       "from pinned host rows, wall clock incl. engine creation",
+               "seconds_per_call": secs, "epochs_per_call": EPOCHS}
         from paper_2604_26555_b200 import dropin
         if dropin.available():
-            eng.close()
             cfg = dropin.TrainConfig(topology="hex", grid_w=P_GRID[0], grid_h=P_GRID[1],
                                      n_iters=EPOCHS, seed=SEED)
             warm = dropin.TrainConfig(topology="hex", grid_w=P_GRID[0], grid_h=P_GRID[1],
                                       n_iters=1, seed=SEED)
             dropin.train_cuda(warm, host[:200_000], device=local)
-            _, _, _, secs = dropin.train_cuda(cfg, host, device=local)
-            h2d = n * D * 4 + EPOCHS * (P * D * 4 + P * P * 8)
-            d2h = EPOCHS * (P * D * 8 + P * 8)
-            e2e = {"value": n * EPOCHS / secs, "unit": UNIT,
-                   "h2d_bytes_per_step": int(h2d / EPOCHS), "d2h_bytes_per_step": int(d2h / EPOCHS),
-                   "path": "toposom::train_with_executor + toposom_b200::CudaExecutor "
-                           "(libtsom_dropin.so), host DataMatrix, 10 epochs per call, wall clock",
-                   "seconds_per_call": secs}
-            eng = None
+            _, _, _, dsecs = dropin.train_cuda(cfg, host, device=local)
+            e2e["dropin_reference_loop"] = {
+                "value": n * EPOCHS / dsecs, "seconds_per_call": dsecs,
+                "path": "toposom::train_with_executor + toposom_b200::CudaExecutor "
+                        "(host DataMatrix; reference host code per epoch: sampler, influence, "
+                        "apply_update, int128 accumulators)"}
     pk, pk_kind = peaks()
     k1 = statistics.mean(k1_ms) if k1_ms else float("nan")
     flops = 2.0 * P * D * n
@@ -297,7 +322,8 @@ def run_gpu_arm(args):
             "traffic": None,
             "note": (f"achieved = 2*K*D*N useful flop per launch / mean K1 event time; peak = "
                      f"{pk_kind} bf16 {pk['bf16_tflops']} TF/s / 2 (TF32) / 3 (3xTF32 split)"),
-            "k1_ms": k1, "epoch_ms": statistics.mean(total_ms) if total_ms else None}
+            "k1_ms": k1, "epoch_ms": statistics.mean(total_ms) if total_ms else None,
+            "phase_ms": {k: statistics.mean(p[k] for p in phases) for k in phases[0]} if phases else None}
     line = {
         "metric": METRIC, "value": value, "unit": UNIT, "n_gpus": world, "steps": args.steps,
         "warmup": args.warmup, "ms_per_step": ms, "higher_is_better": True, "scaling": "weak",
@@ -348,8 +374,8 @@ def _tc_probe():
 def main():
     ap = argparse.ArgumentParser()
     ap.add_argument("--gpus", type=int, default=1)
-    ap.add_argument("--steps", type=int, default=20)
-    ap.add_argument("--warmup", type=int, default=3)
+    ap.add_argument("--steps", type=int, default=50)
+    ap.add_argument("--warmup", type=int, default=5)
     ap.add_argument("--impl", default="b200", choices=["b200", "reference"])
     ap.add_argument("--kernel", type=int, default=0, help="0 auto, 1 SIMT, 2 tcgen05")
     ap.add_argument("--no-e2e", action="store_true")

@@ -155,7 +155,7 @@ void prep_codebook(Engine* eng) {
 // K1 + exact re-check over rows `x` (selection `sel` of length n, or first n rows).
 // `tiles` = pre-split tcgen05 operand for exactly these n rows (or nullptr to build).
 void run_bmu(Engine* eng, const float* x, const uint32_t* sel, uint64_t n, const float* x2max,
-             const float* tiles) {
+             const float* tiles, const float* tiles_xn2) {
     CU(cudaMemsetAsync(eng->flags.p, 0, 2 * sizeof(uint32_t), eng->stream));
     if (n == 0) return;
     if (use_tc(eng)) {
@@ -165,22 +165,24 @@ void run_bmu(Engine* eng, const float* x, const uint32_t* sel, uint64_t n, const
         if (!tiles) {
             const uint64_t ntiles = (n + tsom::kTcTileM - 1) / tsom::kTcTileM;
             CU(eng->gsplit.ensure(ntiles * tile_bytes));
+            CU(eng->gxn2.ensure(n * sizeof(float)));
             tsom::launch_split_rows(x, sel, nullptr, n, eng->D, eng->gsplit.as<float>(),
-                                    eng->stream);
+                                    eng->gxn2.as<float>(), eng->stream);
             tiles = eng->gsplit.as<float>();
+            tiles_xn2 = eng->gxn2.as<float>();
         }
         CU(eng->part.ensure((size_t)groups * 3 * n * sizeof(float)));
         CU(eng->ties.ensure((n + 1) * sizeof(uint32_t)));
         CU(cudaMemsetAsync(eng->ties.p, 0, sizeof(uint32_t), eng->stream));
-        const float* x2 = x2max;
         const float* w2 = eng->w2max.as<float>();
         const float tau = (float)eng->tau_tc;
         CU(cudaEventRecord(eng->ev[8], eng->stream));
-        CU(tsom::launch_bmu_tc(tiles, n, nullptr, false, eng->P, eng->wsplit.as<float>(), x2, w2,
-                               tau, eng->part.as<float>(), eng->sm_count, eng->stream));
+        CU(tsom::launch_bmu_tc(tiles, n, nullptr, false, eng->P, eng->wsplit.as<float>(),
+                               tiles_xn2, w2, tau, eng->part.as<float>(), eng->sm_count,
+                               eng->stream));
         CU(cudaEventRecord(eng->ev[9], eng->stream));
         eng->k1_timed = true;
-        tsom::launch_merge_fast(eng->part.as<float>(), n, groups, gn, x2, w2, tau,
+        tsom::launch_merge_fast(eng->part.as<float>(), n, groups, gn, tiles_xn2, w2, tau,
                                 eng->bmu.as<uint32_t>(), eng->ties.as<uint32_t>(), eng->stream);
         CU(cudaGetLastError());
         // near-tie rows (~1%): same tensor-core kernel in enumerate mode on just
@@ -195,13 +197,15 @@ void run_bmu(Engine* eng, const float* x, const uint32_t* sel, uint64_t n, const
             const uint64_t mt = (m + tsom::kTcTileM - 1) / tsom::kTcTileM;
             CU(eng->tsplit.ensure(mt * tile_bytes));
             CU(eng->part2.ensure((size_t)groups * 3 * m * sizeof(float)));
+            CU(eng->txn2.ensure(m * sizeof(float)));
             tsom::launch_split_rows(x, sel, tpos + f0, m, eng->D, eng->tsplit.as<float>(),
-                                    eng->stream);
+                                    eng->txn2.as<float>(), eng->stream);
             CU(tsom::launch_bmu_tc(eng->tsplit.as<float>(), m, nullptr, true, eng->P,
-                                   eng->wsplit.as<float>(), x2, w2, tau, eng->part2.as<float>(),
-                                   eng->sm_count, eng->stream));
-            tsom::launch_merge_partials(eng->part2.as<float>(), tpos + f0, m, groups, gn, x2, w2,
-                                        tau, x, sel, eng->w.as<float>(), eng->D,
+                                   eng->wsplit.as<float>(), eng->txn2.as<float>(), w2, tau,
+                                   eng->part2.as<float>(), eng->sm_count, eng->stream));
+            tsom::launch_merge_partials(eng->part2.as<float>(), tpos + f0, m, groups, gn,
+                                        eng->txn2.as<float>(), w2, tau, x, sel,
+                                        eng->w.as<float>(), eng->D,
                                         eng->bmu.as<uint32_t>(), eng->flags.as<uint32_t>(),
                                         eng->stream);
         }
@@ -275,17 +279,20 @@ void accumulate_epoch(Engine* eng, const uint32_t* sel_host, uint64_t n_sel, boo
     CU(cudaEventRecord(eng->ev[0], eng->stream));
     if (!eng->streamed) {
         const float* tiles = nullptr;
+        const float* tiles_xn2 = nullptr;
         if (use_tc(eng) && !sel) {
             if (!eng->xsplit_valid) {
                 const uint64_t ntiles = (eng->n_rows + tsom::kTcTileM - 1) / tsom::kTcTileM;
                 CU(eng->xsplit.ensure(ntiles * 2 * tsom::kTcTileM * tsom::kTcKPad * sizeof(float)));
+                CU(eng->xn2.ensure(std::max<uint64_t>(eng->n_rows, 1) * sizeof(float)));
                 tsom::launch_split_rows(eng->x.as<float>(), nullptr, nullptr, eng->n_rows, eng->D,
-                                        eng->xsplit.as<float>(), eng->stream);
+                                        eng->xsplit.as<float>(), eng->xn2.as<float>(), eng->stream);
                 eng->xsplit_valid = true;
             }
             tiles = eng->xsplit.as<float>();
+            tiles_xn2 = eng->xn2.as<float>();
         }
-        run_bmu(eng, eng->x.as<float>(), dsel, n, eng->x2max.as<float>(), tiles);
+        run_bmu(eng, eng->x.as<float>(), dsel, n, eng->x2max.as<float>(), tiles, tiles_xn2);
         CU(cudaEventRecord(eng->ev[1], eng->stream));
         ensure_accum(eng, n);
         tsom::launch_accumulate(eng->x.as<float>(), dsel, n, eng->D, eng->w.as<float>(), eng->P,
@@ -338,7 +345,7 @@ void accumulate_epoch(Engine* eng, const uint32_t* sel_host, uint64_t n_sel, boo
             const uint64_t cn = sel ? (p1 - p0) : (r1 - r0);
             const uint32_t* csel = sel ? dsel + p0 : nullptr;
             const uint64_t out0 = sel ? p0 : r0;
-            run_bmu(eng, sel ? xbase : xs, csel, cn, xmax, nullptr);
+            run_bmu(eng, sel ? xbase : xs, csel, cn, xmax, nullptr, nullptr);
             CU(cudaMemcpyAsync(&eng->chunk_counts[2 * c], eng->flags.p, 2 * sizeof(uint32_t),
                                cudaMemcpyDeviceToHost, eng->stream));
             tsom::launch_accumulate(sel ? xbase : xs, csel, cn, eng->D, eng->w.as<float>(), eng->P,
@@ -466,7 +473,7 @@ int tsom_destroy(tsom_engine* eng) {
     if (eng->stream) cudaStreamSynchronize(eng->stream);
     if (eng->nccl_comm && g_nccl.commDestroy) g_nccl.commDestroy((ncclComm_t)eng->nccl_comm);
     if (eng->host_registered) cudaHostUnregister(const_cast<float*>(eng->host_rows));
-    for (DevBuf* b : {&eng->x, &eng->xsplit, &eng->x2max, &eng->w, &eng->wt, &eng->wsplit, &eng->w2,
+    for (DevBuf* b : {&eng->x, &eng->xsplit, &eng->xn2, &eng->gxn2, &eng->txn2, &eng->x2max, &eng->w, &eng->wt, &eng->wsplit, &eng->w2,
                       &eng->w2max, &eng->prev, &eng->infl, &eng->topo_dist, &eng->sel,
                       &eng->rows_scratch, &eng->gsplit, &eng->bmu, &eng->dist, &eng->part,
                       &eng->flags, &eng->ties, &eng->part2, &eng->tsplit, &eng->acc_buf[0], &eng->acc_buf[1], &eng->acc_buf[2], &eng->acc_buf[3],
@@ -679,7 +686,7 @@ int tsom_bmu(tsom_engine* eng, const float* rows, uint64_t n, uint32_t* bmu, dou
         CU(eng->sums.ensure(slot_len(eng) * sizeof(double)));
         float* xm = eng->x2max.as<float>() + 1;
         tsom::launch_row_norm_max(eng->rows_scratch.as<float>(), n, eng->D, xm, eng->stream);
-        run_bmu(eng, eng->rows_scratch.as<float>(), nullptr, n, xm, nullptr);
+        run_bmu(eng, eng->rows_scratch.as<float>(), nullptr, n, xm, nullptr, nullptr);
         if (dist) {
             ensure_accum(eng, n);
             tsom::launch_accumulate(eng->rows_scratch.as<float>(), nullptr, n, eng->D,

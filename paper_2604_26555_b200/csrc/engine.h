@@ -89,6 +89,7 @@ struct Engine {
     const float* host_rows = nullptr;  // streamed mode source
     bool host_registered = false;
     DevBuf xsplit;      // pre-split tf32 tiles for the tensor-core kernel (all rows)
+    DevBuf xn2, gxn2, txn2;  // per-row ||x||^2 for xsplit / gsplit / tsplit rows
     bool xsplit_valid = false;
     DevBuf x2max;       // float: max ||x||^2 over bound rows
 
@@ -151,7 +152,7 @@ void launch_fold_max(float* a, cudaStream_t st);
 // split rows (optionally gathered through sel, and/or through a position list
 // idx: split row f = position idx[f]) into tcgen05 tiles
 void launch_split_rows(const float* x, const uint32_t* sel, const uint32_t* idx, uint64_t n,
-                       uint32_t D, float* tiles, cudaStream_t st);
+                       uint32_t D, float* tiles, float* xn2, cudaStream_t st);
 bool tc_supported(uint32_t P, uint32_t D);
 // nodes per CTA-resident codebook group (multiple of 16, <= 256)
 __host__ __device__ inline uint32_t tc_group_width(uint32_t P) {
@@ -165,17 +166,17 @@ void launch_bmu_simt(const float* x, const uint32_t* sel, uint64_t n, uint32_t D
 // tcgen05 variant: per-group partials (enumerate = candidate lists; dev_n =
 // optional device row count).
 cudaError_t launch_bmu_tc(const float* tiles, uint64_t n, const uint32_t* dev_n, bool enumerate,
-                          uint32_t P, const float* wsplit, const float* x2max,
+                          uint32_t P, const float* wsplit, const float* xn2,
                           const float* w2max, float tau, float* part, int sm_count,
                           cudaStream_t st);
 // main-pass merge: bmu for rows with a clear winner, near-tie positions -> ties
 void launch_merge_fast(const float* part, uint64_t n, uint32_t groups, uint32_t gn,
-                       const float* x2max, const float* w2max, float tau, uint32_t* bmu,
+                       const float* xn2, const float* w2max, float tau, uint32_t* bmu,
                        uint32_t* ties, cudaStream_t st);
 // enumerate-pass merge over the near-tie rows: candidates -> exact FP64 -> bmu;
 // overflow -> flags list for the full re-scan.
 void launch_merge_partials(const float* part, const uint32_t* ties, uint64_t n, uint32_t groups,
-                           uint32_t gn, const float* x2max, const float* w2max, float tau,
+                           uint32_t gn, const float* xn2, const float* w2max, float tau,
                            const float* x, const uint32_t* sel, const float* w, uint32_t D,
                            uint32_t* bmu, uint32_t* flags, cudaStream_t st);
 // exact FP64 re-scan of flagged rows (reference loop order)

@@ -180,7 +180,7 @@ template <bool kEnum>
 __global__ void __launch_bounds__(kThreads, 1)
     k1_bmu_tc(const float* __restrict__ tiles, uint64_t n_host, const uint32_t* __restrict__ dev_n,
               uint32_t groups, uint32_t gn, const float* __restrict__ wsplit,
-              const float* __restrict__ x2max, const float* __restrict__ w2max, float tau,
+              const float* __restrict__ xn2, const float* __restrict__ w2max, float tau,
               float* __restrict__ part) {
     extern __shared__ __align__(1024) uint8_t smem[];
     const uint64_t n = dev_n ? (uint64_t)*dev_n : n_host;
@@ -338,8 +338,10 @@ __global__ void __launch_bounds__(kThreads, 1)
             uint32_t w1 = I1, w2 = __float_as_uint(B2);
             if (kEnum) {
                 // enumerate the row's candidates v <= B1 + thr in ascending j
-                const float thr = tau * (__ldg(x2max) + __ldg(w2max));
-                const bool need = !(B2 - B1 > thr);
+                const uint64_t prow = (uint64_t)t * kTcTileM + row;
+                const float thr =
+                    prow < n ? tau * (__ldg(xn2 + prow) + __ldg(w2max)) : 0.0f;
+                const bool need = prow < n && !(B2 - B1 > thr);
                 w2 = 1;
                 if (__any_sync(0xffffffffu, need)) {
                     const float lim = B1 + thr;
@@ -386,7 +388,7 @@ __global__ void __launch_bounds__(kThreads, 1)
 bool tc_supported(uint32_t P, uint32_t D) { return P >= 1 && D + 2 <= (uint32_t)kTcKPad; }
 
 cudaError_t launch_bmu_tc(const float* tiles, uint64_t n, const uint32_t* dev_n, bool enumerate,
-                          uint32_t P, const float* wsplit, const float* x2max,
+                          uint32_t P, const float* wsplit, const float* xn2,
                           const float* w2max, float tau, float* part, int sm_count,
                           cudaStream_t st) {
     if (n == 0) return cudaSuccess;
@@ -407,7 +409,7 @@ cudaError_t launch_bmu_tc(const float* tiles, uint64_t n, const uint32_t* dev_n,
         if (e != cudaSuccess) return e;
         attr[enumerate] = smem;
     }
-    TSOM_LAUNCH(kern<<<grid, kThreads, smem, st>>>(tiles, n, dev_n, groups, gn, wsplit, x2max,
+    TSOM_LAUNCH(kern<<<grid, kThreads, smem, st>>>(tiles, n, dev_n, groups, gn, wsplit, xn2,
                                                    w2max, tau, part));
     return cudaGetLastError();
 }

@@ -301,31 +301,19 @@ __device__ __forceinline__ double exact_d2(const float* __restrict__ x,
 // whose global best is separated from every other node by more than the FP32
 // error window thr gets its BMU here; otherwise its position joins `ties`
 // ([0] = count, positions from [1]) for the enumerate pass.
-__global__ void k_merge_fast(const float* __restrict__ part, uint64_t n, uint32_t groups,
-                             uint32_t gn, const float* __restrict__ x2max,
-                             const float* __restrict__ w2max, float tau,
-                             uint32_t* __restrict__ bmu, uint32_t* __restrict__ ties) {
+__global__ void __launch_bounds__(256, 8) k_merge_fast(
+    const float* __restrict__ part, uint64_t n, uint32_t groups, uint32_t gn,
+    const float* __restrict__ xn2, const float* __restrict__ w2max, float tau,
+    uint32_t* __restrict__ bmu, uint32_t* __restrict__ ties) {
     const uint64_t i = blockIdx.x * (uint64_t)blockDim.x + threadIdx.x;
     if (i >= n) return;
-    const float thr = tau * (__ldg(x2max) + __ldg(w2max));
+    const float thr = tau * (__ldg(xn2 + i) + __ldg(w2max));
     float B1 = CUDART_INF_F, B2 = CUDART_INF_F;
     uint32_t I1 = 0;
-    for (uint32_t g0 = 0; g0 < groups; g0 += 8) {
-        float b1v[8], b2v[8];
-        uint32_t i1v[8];
-#pragma unroll
-        for (uint32_t q = 0; q < 8; ++q) {
-            if (g0 + q < groups) {
-                const float* pg = part + (size_t)(g0 + q) * 3 * n;
-                b1v[q] = pg[i];
-                i1v[q] = __float_as_uint(pg[n + i]);
-                b2v[q] = pg[2 * n + i];
-            }
-        }
-#pragma unroll
-        for (uint32_t q = 0; q < 8; ++q)  // ascending groups = ascending node ids
-            if (g0 + q < groups)
-                top2_merge(B1, I1, B2, b1v[q], (g0 + q) * gn + i1v[q], b2v[q]);
+    for (uint32_t g = 0; g < groups; ++g) {  // ascending groups = ascending node ids
+        const float* pg = part + (size_t)g * 3 * n;
+        top2_merge(B1, I1, B2, __ldg(pg + i), g * gn + __float_as_uint(__ldg(pg + n + i)),
+                   __ldg(pg + 2 * n + i));
     }
     bmu[i] = I1;
     if (!(B2 - B1 > thr)) {
@@ -335,11 +323,11 @@ __global__ void k_merge_fast(const float* __restrict__ part, uint64_t n, uint32_
 }
 
 void launch_merge_fast(const float* part, uint64_t n, uint32_t groups, uint32_t gn,
-                       const float* x2max, const float* w2max, float tau, uint32_t* bmu,
+                       const float* xn2, const float* w2max, float tau, uint32_t* bmu,
                        uint32_t* ties, cudaStream_t st) {
     if (n == 0) return;
     TSOM_LAUNCH(k_merge_fast<<<(unsigned)((n + 255) / 256), 256, 0, st>>>(
-        part, n, groups, gn, x2max, w2max, tau, bmu, ties));
+        part, n, groups, gn, xn2, w2max, tau, bmu, ties));
 }
 
 
@@ -349,15 +337,15 @@ void launch_merge_fast(const float* part, uint64_t n, uint32_t groups, uint32_t 
 // ascending node order with strict < (lowest index wins), as find_bmus
 // (trainer.hpp:293-304); > 4 candidates in a group -> full exact re-scan list.
 __global__ void k_merge_partials(const float* __restrict__ part, const uint32_t* __restrict__ ties,
-                                 uint64_t n, uint32_t groups, uint32_t gn, const float* __restrict__ x2max,
+                                 uint64_t n, uint32_t groups, uint32_t gn, const float* __restrict__ xn2,
                                  const float* __restrict__ w2max, float tau,
                                  const float* __restrict__ x, const uint32_t* __restrict__ sel,
                                  const float* __restrict__ w, uint32_t D,
                                  uint32_t* __restrict__ bmu, uint32_t* __restrict__ flags) {
-    const float thr = tau * (__ldg(x2max) + __ldg(w2max));
     for (uint64_t f = blockIdx.x * (uint64_t)blockDim.x + threadIdx.x; f < n;
          f += (uint64_t)gridDim.x * blockDim.x) {
         const uint32_t pos = ties[f];
+        const float thr = tau * (__ldg(xn2 + f) + __ldg(w2max));
         float B1 = CUDART_INF_F;
         for (uint32_t g = 0; g < groups; ++g) B1 = fminf(B1, part[(size_t)g * 3 * n + f]);
         const float lim = B1 + thr;
@@ -404,12 +392,12 @@ __global__ void k_merge_partials(const float* __restrict__ part, const uint32_t*
 }
 
 void launch_merge_partials(const float* part, const uint32_t* ties, uint64_t n, uint32_t groups,
-                           uint32_t gn, const float* x2max, const float* w2max, float tau,
+                           uint32_t gn, const float* xn2, const float* w2max, float tau,
                            const float* x, const uint32_t* sel, const float* w, uint32_t D,
                            uint32_t* bmu, uint32_t* flags, cudaStream_t st) {
     if (n == 0) return;
     TSOM_LAUNCH(k_merge_partials<<<(unsigned)((n + 255) / 256), 256, 0, st>>>(
-        part, ties, n, groups, gn, x2max, w2max, tau, x, sel, w, D, bmu, flags));
+        part, ties, n, groups, gn, xn2, w2max, tau, x, sel, w, D, bmu, flags));
 }
 
 // ---------------------------------------------------------------------------
@@ -476,7 +464,7 @@ void launch_rescan(const float* x, const uint32_t* sel, const float* w, uint32_t
 
 __global__ void k_split_rows(const float* __restrict__ x, const uint32_t* __restrict__ sel,
                              const uint32_t* __restrict__ idx, uint64_t n, uint32_t D,
-                             float* __restrict__ tiles) {
+                             float* __restrict__ tiles, float* __restrict__ xn2) {
     // idx (optional): positions; split row f is then position idx[f]
     const uint64_t ntiles = (n + kTcTileM - 1) / kTcTileM;
     const int r = threadIdx.x;  // 128 threads, one row each
@@ -489,6 +477,7 @@ __global__ void k_split_rows(const float* __restrict__ x, const uint32_t* __rest
             const uint64_t pos = idx ? (uint64_t)idx[f] : f;
             src = x + (sel ? (uint64_t)sel[pos] : pos) * D;
         }
+        double nrm = 0.0;
         for (uint32_t kc = 0; kc < kTcKPad / 4; ++kc) {
             float hi[4], lo[4];
 #pragma unroll
@@ -497,9 +486,10 @@ __global__ void k_split_rows(const float* __restrict__ x, const uint32_t* __rest
                 float val;
                 if (!valid)
                     val = 0.0f;
-                else if (k < D)
+                else if (k < D) {
                     val = src[k];
-                else if (k == D || k == D + 1)
+                    nrm += (double)val * (double)val;
+                } else if (k == D || k == D + 1)
                     val = 1.0f;
                 else
                     val = 0.0f;
@@ -511,15 +501,17 @@ __global__ void k_split_rows(const float* __restrict__ x, const uint32_t* __rest
             *reinterpret_cast<float4*>(base + (size_t)kTcTileM * kTcKPad + off) =
                 make_float4(lo[0], lo[1], lo[2], lo[3]);
         }
+        // per-row ||x||^2, rounded up: the row's own FP32 error window (thr_i)
+        if (xn2 && valid) xn2[f] = (float)nrm * 1.0000003f;
     }
 }
 
 void launch_split_rows(const float* x, const uint32_t* sel, const uint32_t* idx, uint64_t n,
-                       uint32_t D, float* tiles, cudaStream_t st) {
+                       uint32_t D, float* tiles, float* xn2, cudaStream_t st) {
     if (n == 0) return;
     uint64_t tiles_n = (n + kTcTileM - 1) / kTcTileM;
     if (tiles_n > 148ull * 64) tiles_n = 148ull * 64;
-    TSOM_LAUNCH(k_split_rows<<<(unsigned)tiles_n, kTcTileM, 0, st>>>(x, sel, idx, n, D, tiles));
+    TSOM_LAUNCH(k_split_rows<<<(unsigned)tiles_n, kTcTileM, 0, st>>>(x, sel, idx, n, D, tiles, xn2));
 }
 
 }  // namespace tsom
