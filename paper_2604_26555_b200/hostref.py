@@ -10,6 +10,7 @@ compute fallback: none of them touches samples.
 * :func:`schedule_value`    — trainer.hpp:132-139
 * :func:`resolved_sigma0`   — trainer.hpp:75-80
 * :func:`lattice_dist`      — topology.hpp:114-149
+* :func:`assign_shards`     — parallel.hpp:28-41 (row shards per rank/GPU)
 """
 from __future__ import annotations
 
@@ -128,4 +129,18 @@ def lattice_dist(kind: str, width: int, height: int) -> np.ndarray:
     dy = xy[:, None, 1] - xy[None, :, 1]
     out = np.sqrt(dx * dx + dy * dy)
     np.fill_diagonal(out, 0.0)
+    return out
+
+
+def assign_shards(n: int, workers: int) -> list[tuple[int, int]]:
+    """Contiguous near-equal partition (parallel.hpp:28-41): the first n % G
+    slices get one extra item; a slice may be empty when G > n."""
+    if workers < 1:
+        raise ValueError("assign_shards: G must be >= 1")
+    base, extra = divmod(n, workers)
+    out, begin = [], 0
+    for g in range(workers):
+        cnt = base + (1 if g < extra else 0)
+        out.append((begin, begin + cnt))
+        begin += cnt
     return out
