@@ -173,17 +173,19 @@ void run_bmu(Engine* eng, const float* x, const uint32_t* sel, uint64_t n, const
         }
         CU(eng->part.ensure((size_t)groups * 3 * n * sizeof(float)));
         CU(eng->ties.ensure((n + 1) * sizeof(uint32_t)));
+        CU(eng->tmask.ensure(std::max<uint64_t>(n, 1) * sizeof(uint32_t)));
         CU(cudaMemsetAsync(eng->ties.p, 0, sizeof(uint32_t), eng->stream));
         const float* w2 = eng->w2max.as<float>();
         const float tau = (float)eng->tau_tc;
         CU(cudaEventRecord(eng->ev[8], eng->stream));
         CU(tsom::launch_bmu_tc(tiles, n, nullptr, false, eng->P, eng->wsplit.as<float>(),
-                               tiles_xn2, w2, tau, eng->part.as<float>(), eng->sm_count,
-                               eng->stream));
+                               tiles_xn2, w2, tau, nullptr, eng->part.as<float>(),
+                               eng->sm_count, eng->stream));
         CU(cudaEventRecord(eng->ev[9], eng->stream));
         eng->k1_timed = true;
         tsom::launch_merge_fast(eng->part.as<float>(), n, groups, gn, tiles_xn2, w2, tau,
-                                eng->bmu.as<uint32_t>(), eng->ties.as<uint32_t>(), eng->stream);
+                                eng->bmu.as<uint32_t>(), eng->ties.as<uint32_t>(),
+                                eng->tmask.as<uint32_t>(), eng->stream);
         CU(cudaGetLastError());
         // near-tie rows (~1%): same tensor-core kernel in enumerate mode on just
         // those rows, then exact FP64 over their few candidates
@@ -196,13 +198,14 @@ void run_bmu(Engine* eng, const float* x, const uint32_t* sel, uint64_t n, const
             const uint64_t m = std::min<uint64_t>(chunk, nt - f0);
             const uint64_t mt = (m + tsom::kTcTileM - 1) / tsom::kTcTileM;
             CU(eng->tsplit.ensure(mt * tile_bytes));
-            CU(eng->part2.ensure((size_t)groups * 3 * m * sizeof(float)));
+            CU(eng->part2.ensure((size_t)groups * 4 * m * sizeof(float)));
             CU(eng->txn2.ensure(m * sizeof(float)));
             tsom::launch_split_rows(x, sel, tpos + f0, m, eng->D, eng->tsplit.as<float>(),
                                     eng->txn2.as<float>(), eng->stream);
             CU(tsom::launch_bmu_tc(eng->tsplit.as<float>(), m, nullptr, true, eng->P,
                                    eng->wsplit.as<float>(), eng->txn2.as<float>(), w2, tau,
-                                   eng->part2.as<float>(), eng->sm_count, eng->stream));
+                                   eng->tmask.as<uint32_t>() + f0, eng->part2.as<float>(),
+                                   eng->sm_count, eng->stream));
             tsom::launch_merge_partials(eng->part2.as<float>(), tpos + f0, m, groups, gn,
                                         eng->txn2.as<float>(), w2, tau, x, sel,
                                         eng->w.as<float>(), eng->D,
@@ -476,7 +479,7 @@ int tsom_destroy(tsom_engine* eng) {
     for (DevBuf* b : {&eng->x, &eng->xsplit, &eng->xn2, &eng->gxn2, &eng->txn2, &eng->x2max, &eng->w, &eng->wt, &eng->wsplit, &eng->w2,
                       &eng->w2max, &eng->prev, &eng->infl, &eng->topo_dist, &eng->sel,
                       &eng->rows_scratch, &eng->gsplit, &eng->bmu, &eng->dist, &eng->part,
-                      &eng->flags, &eng->ties, &eng->part2, &eng->tsplit, &eng->acc_buf[0], &eng->acc_buf[1], &eng->acc_buf[2], &eng->acc_buf[3],
+                      &eng->flags, &eng->ties, &eng->tmask, &eng->part2, &eng->tsplit, &eng->acc_buf[0], &eng->acc_buf[1], &eng->acc_buf[2], &eng->acc_buf[3],
                       &eng->acc_buf[4], &eng->acc_buf[5], &eng->acc_buf[6], &eng->sums, &eng->U, &eng->H, &eng->status, &eng->smooth_scratch,
                       &eng->stage[0], &eng->stage[1]})
         b->release();

@@ -10,8 +10,8 @@
 //   ws       ceil(P/gn) groups of [hi|lo] x [14][gn][4] f32  tcgen05 B operand (gn <= 256)
 //   infl     P x P        f64             influence h[b][j]
 //   sorted   n u32                        row positions in BMU order (counting sort)
-//   partial  pieces x (d+1) f64           per-piece (<= 256 rows) FP64 residual sums
-//   sums     P*d + P + 2  f64             reduced [R | c | sum dist | count]
+//   partial  pieces x (d+1) f64           per-piece (<= 256 rows) FP64 row sums
+//   sums     P*d + P + 2  f64             reduced [S | c | sum dist | count]
 //                                         (the one allreduce buffer)
 //   U, H     P*d, P       f64             smoothed accumulators (K3 output)
 #pragma once
@@ -114,6 +114,7 @@ struct Engine {
     DevBuf part;           // tcgen05 per-group partial top-2 [groups][n] (b1, i1, b2)
     DevBuf flags;          // [0] full re-scan count, [1] exact-candidate count, then positions
     DevBuf ties;           // [0] near-tie count, then positions (enumerate pass input)
+    DevBuf tmask;          // per near-tie row: bitmask of groups inside the window
     DevBuf part2;          // enumerate-pass partials
     DevBuf tsplit;         // split tiles of the near-tie rows
     DevBuf acc_buf[7];     // AccumScratch arrays
@@ -167,12 +168,12 @@ void launch_bmu_simt(const float* x, const uint32_t* sel, uint64_t n, uint32_t D
 // optional device row count).
 cudaError_t launch_bmu_tc(const float* tiles, uint64_t n, const uint32_t* dev_n, bool enumerate,
                           uint32_t P, const float* wsplit, const float* xn2,
-                          const float* w2max, float tau, float* part, int sm_count,
-                          cudaStream_t st);
+                          const float* w2max, float tau, const uint32_t* rmask, float* part,
+                          int sm_count, cudaStream_t st);
 // main-pass merge: bmu for rows with a clear winner, near-tie positions -> ties
 void launch_merge_fast(const float* part, uint64_t n, uint32_t groups, uint32_t gn,
                        const float* xn2, const float* w2max, float tau, uint32_t* bmu,
-                       uint32_t* ties, cudaStream_t st);
+                       uint32_t* ties, uint32_t* tmask, cudaStream_t st);
 // enumerate-pass merge over the near-tie rows: candidates -> exact FP64 -> bmu;
 // overflow -> flags list for the full re-scan.
 void launch_merge_partials(const float* part, const uint32_t* ties, uint64_t n, uint32_t groups,

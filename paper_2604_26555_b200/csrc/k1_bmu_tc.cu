@@ -174,14 +174,15 @@ constexpr uint32_t kCandOverflow = 15u;
 
 // kEnum = false (main pass): per (row, group) the top-2 (b1, i1, b2) only.
 // kEnum = true (near-tie rows only, see k_merge_fast): per (row, group) the best
-// value plus up to 4 local candidate ids within thr of it (count 15 = overflow).
+// value plus up to 8 local candidate ids within thr of it (count 15 = overflow),
+// enumerated only in the groups flagged relevant for the row (rmask).
 // dev_n (optional): row count read on the device (the near-tie list length).
 template <bool kEnum>
 __global__ void __launch_bounds__(kThreads, 1)
     k1_bmu_tc(const float* __restrict__ tiles, uint64_t n_host, const uint32_t* __restrict__ dev_n,
               uint32_t groups, uint32_t gn, const float* __restrict__ wsplit,
               const float* __restrict__ xn2, const float* __restrict__ w2max, float tau,
-              float* __restrict__ part) {
+              const uint32_t* __restrict__ rmask, float* __restrict__ part) {
     extern __shared__ __align__(1024) uint8_t smem[];
     const uint64_t n = dev_n ? (uint64_t)*dev_n : n_host;
     const uint32_t ntiles = (uint32_t)((n + kTcTileM - 1) / kTcTileM);
@@ -335,17 +336,17 @@ __global__ void __launch_bounds__(kThreads, 1)
                 top2_merge_dev(b1[0], i1[0], b2[0], b1[s2], i1[s2], b2[s2]);
             const float B1 = b1[0], B2 = b2[0];
             const uint32_t I1 = i1[0];
-            uint32_t w1 = I1, w2 = __float_as_uint(B2);
+            uint32_t w1 = I1, w2 = __float_as_uint(B2), w3 = 1;
             if (kEnum) {
                 // enumerate the row's candidates v <= B1 + thr in ascending j
                 const uint64_t prow = (uint64_t)t * kTcTileM + row;
-                const float thr =
-                    prow < n ? tau * (__ldg(xn2 + prow) + __ldg(w2max)) : 0.0f;
-                const bool need = prow < n && !(B2 - B1 > thr);
-                w2 = 1;
+                const bool relevant = prow < n && ((__ldg(rmask + prow) >> (g & 31)) & 1u);
+                const float thr = relevant ? tau * (__ldg(xn2 + prow) + __ldg(w2max)) : 0.0f;
+                const bool need = relevant && !(B2 - B1 > thr);
+                w2 = 0;
                 if (__any_sync(0xffffffffu, need)) {
                     const float lim = B1 + thr;
-                    uint32_t pk = 0, nc = 0;
+                    uint32_t pk0 = 0, pk1 = 0, nc = 0;
                     for (uint32_t cc = 0; cc < gn; cc += 16) {
                         uint32_t r[16];
                         TMEM_LD16(taddr + cc, r);
@@ -353,14 +354,17 @@ __global__ void __launch_bounds__(kThreads, 1)
 #pragma unroll
                         for (int k = 0; k < 16; ++k) {
                             if (need && __uint_as_float(r[k]) <= lim) {
-                                if (nc < 4) pk |= (cc + k) << (8 * nc);
+                                const uint32_t id = (cc + k) << (8 * (nc & 3));
+                                if (nc < 4) pk0 |= id;
+                                else if (nc < 8) pk1 |= id;
                                 ++nc;
                             }
                         }
                     }
                     if (need) {
-                        w1 = pk;
-                        w2 = (nc >= 1 && nc <= 4) ? nc : kCandOverflow;
+                        w1 = pk0;
+                        w2 = pk1;
+                        w3 = (nc >= 1 && nc <= 8) ? nc : kCandOverflow;
                     }
                 }
             }
@@ -368,10 +372,11 @@ __global__ void __launch_bounds__(kThreads, 1)
             mbar_arrive(&tempty_bar[acc]);  // this thread is done with the accumulator
             const uint64_t pos = (uint64_t)t * kTcTileM + row;
             if (pos < n) {
-                float* pg = part + (size_t)g * 3 * n;
+                float* pg = part + (size_t)g * (kEnum ? 4 : 3) * n;
                 pg[pos] = B1;
                 pg[n + pos] = __uint_as_float(w1);
                 pg[2 * n + pos] = __uint_as_float(w2);
+                if (kEnum) pg[3 * n + pos] = __uint_as_float(w3);
             }
             acc_phase ^= 1;
         }
@@ -389,8 +394,8 @@ bool tc_supported(uint32_t P, uint32_t D) { return P >= 1 && D + 2 <= (uint32_t)
 
 cudaError_t launch_bmu_tc(const float* tiles, uint64_t n, const uint32_t* dev_n, bool enumerate,
                           uint32_t P, const float* wsplit, const float* xn2,
-                          const float* w2max, float tau, float* part, int sm_count,
-                          cudaStream_t st) {
+                          const float* w2max, float tau, const uint32_t* rmask, float* part,
+                          int sm_count, cudaStream_t st) {
     if (n == 0) return cudaSuccess;
     const uint32_t gn = tc_group_width(P);
     const uint32_t groups = (P + gn - 1) / gn;
@@ -410,7 +415,7 @@ cudaError_t launch_bmu_tc(const float* tiles, uint64_t n, const uint32_t* dev_n,
         attr[enumerate] = smem;
     }
     TSOM_LAUNCH(kern<<<grid, kThreads, smem, st>>>(tiles, n, dev_n, groups, gn, wsplit, xn2,
-                                                   w2max, tau, part));
+                                                   w2max, tau, rmask, part));
     return cudaGetLastError();
 }
 

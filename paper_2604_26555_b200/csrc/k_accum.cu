@@ -5,9 +5,8 @@
 // Algebra: the reference folds eta*h[b][j]*(x - w_j) for
 // every sample and every node.  Grouping the samples by BMU b gives
 //   U_j = eta * sum_b h[b][j] * (S_b - c_b w_j),   H_j = sum_b h[b][j] c_b
-// with S_b = sum_{i: b_i = b} x_i and c_b = #{i: b_i = b}.  K2 produces the
-// residual sums R_b = sum (x_i - w_b) (exact FP64 terms) and c_b; the
-// smoothing GEMM (k_smooth.cu) forms S_b = R_b + c_b w_b.
+// with S_b = sum_{i: b_i = b} x_i and c_b = #{i: b_i = b}.  K2 produces S_b
+// (FP64 register sums of exact FP64 terms, no float atomics) and c_b.
 //
 // Pipeline (all deterministic, no floating-point atomics):
 //   k_hist      block-local BMU histograms            [nblk][P]
@@ -198,7 +197,7 @@ __global__ void __launch_bounds__(kScatterWarps * 32) k_scatter(
 // gather + FP64 accumulation per piece
 // ---------------------------------------------------------------------------
 
-// partial[p][k] (k < D) = sum over the piece's rows of (x_k - w_bk) in FP64;
+// partial[p][k] (k < D) = sum over the piece's rows of x_k in FP64;
 // partial[p][D] = sum of their exact BMU distances (when requested).
 // V2: d even — lane l < d/2 owns dims 2l, 2l+1 and reads them with one 8-byte
 // load per row (rows are 8-byte aligned); otherwise lanes own l and l+32.
@@ -252,8 +251,8 @@ __global__ void __launch_bounds__(256, 3) k_gather(
                     if (j0 + j < mrow) {
                         const double d0 = oka ? (double)xv[j].x - w0 : 0.0;
                         const double d1 = okb ? (double)xv[j].y - w1 : 0.0;
-                        a0 += d0;
-                        a1 += d1;
+                        a0 += (double)xv[j].x;
+                        a1 += (double)xv[j].y;
                         if (want_dist) {
                             double d2 = fma(d0, d0, d1 * d1);
 #pragma unroll
@@ -276,69 +275,44 @@ __global__ void __launch_bounds__(256, 3) k_gather(
     }
 }
 
-// TMA-fed variant: every lane issues one cp.async.bulk (1-D TMA) copy of its
-// row into a per-warp double-buffered shared-memory ring; a batch of 32 rows is
-// consumed while the next is in flight (~1000 rows/SM outstanding without
-// register pressure).  Bulk copies need 16-byte aligned sources and sizes, so
-// each copy covers [row & ~15, +rowb) with rowb = roundup16(4d + 8) (d even:
-// rows start at 0 or 8 mod 16); the caller guarantees slack after the last row.
-constexpr int kTmaWarps = 8;
+// Async-copy gather: a warp copies 32 rows per batch into a double-buffered
+// shared-memory ring with cp.async (LDGSTS, 8 bytes per lane: one instruction
+// moves a whole 200-B row), so ~2 x 32 rows per warp are in flight without
+// holding registers; then it accumulates S_b = sum x in FP64 registers.
+// Requires d even (8-byte aligned rows).  partial[p][D] = sum of exact
+// distances when requested (needs w_b: d = x - w).
+constexpr int kAsyncWarps = 8;
 
-__device__ __forceinline__ uint32_t sm_u32(const void* p) {
-    return static_cast<uint32_t>(__cvta_generic_to_shared(p));
-}
-
-__global__ void __launch_bounds__(kTmaWarps * 32, 2) k_gather_tma(
+__global__ void __launch_bounds__(kAsyncWarps * 32, 2) k_gather_async(
     const float* __restrict__ x, const uint32_t* __restrict__ sel, const float* __restrict__ w,
-    uint32_t P, uint32_t D, uint32_t rowb, const uint32_t* __restrict__ sorted,
+    uint32_t P, uint32_t D, const uint32_t* __restrict__ sorted,
     const uint32_t* __restrict__ node_start, const uint32_t* __restrict__ piece_start,
     const uint32_t* __restrict__ piece_node, double* __restrict__ partial,
     double* __restrict__ dist_out, int want_dist, int accumulate) {
-    extern __shared__ __align__(128) uint8_t gsm[];
+    extern __shared__ __align__(16) float gbuf[];
     const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
-    uint8_t* buf = gsm + (size_t)warp * 2 * 32 * rowb;  // [2][32][rowb]
-    uint64_t* bars = reinterpret_cast<uint64_t*>(gsm + (size_t)kTmaWarps * 2 * 32 * rowb) + warp * 2;
-    if (lane == 0) {
-        asm volatile("mbarrier.init.shared::cta.b64 [%0], 1;" ::"r"(sm_u32(&bars[0])));
-        asm volatile("mbarrier.init.shared::cta.b64 [%0], 1;" ::"r"(sm_u32(&bars[1])));
-        asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
-    }
-    __syncwarp();
-    uint32_t phase[2] = {0u, 0u};
+    const uint32_t rowf = D;                                   // floats per smem row
+    float* buf = gbuf + (size_t)warp * 2 * 32 * rowf;          // [2][32][D]
     const uint32_t npieces = piece_start[P];
     const uint32_t Dp = D + 1;
     const uint32_t ka = 2 * lane, kb = 2 * lane + 1;
     const bool oka = ka < D, okb = kb < D;
 
-    // issue the bulk copies of batch m (rows r0+32m+lane) into buffer `slot`
-    auto issue = [&](uint64_t rowaddr, uint32_t nrows, int slot) {
-        if (lane == 0)
-            asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;" ::"r"(
-                             sm_u32(&bars[slot])),
-                         "r"(nrows * rowb)
-                         : "memory");
-        __syncwarp();
-        if ((uint32_t)lane < nrows) {
-            const uint64_t src = rowaddr & ~15ull;
-            asm volatile(
-                "cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1], %2, [%3];" ::"r"(
-                    sm_u32(buf + ((size_t)slot * 32 + lane) * rowb)),
-                "l"(src), "r"(rowb), "r"(sm_u32(&bars[slot]))
-                : "memory");
+    auto issue = [&](const uint64_t* rowaddr_reg, uint32_t nrows, int slot) {
+        float* dst = buf + (size_t)slot * 32 * rowf;
+        for (uint32_t j = 0; j < nrows; ++j) {
+            const uint64_t a = __shfl_sync(0xffffffffu, *rowaddr_reg, j);
+            if (okb) {
+                const uint32_t sdst = (uint32_t)__cvta_generic_to_shared(dst + j * rowf + ka);
+                asm volatile("cp.async.ca.shared.global [%0], [%1], 8;" ::"r"(sdst),
+                             "l"(a + 4ull * ka)
+                             : "memory");
+            }
         }
-    };
-    auto wait = [&](int slot) {
-        asm volatile(
-            "{\n\t.reg .pred P1;\n\t"
-            "W_%=:\n\t"
-            "mbarrier.try_wait.parity.shared::cta.b64 P1, [%0], %1, %2;\n\t"
-            "@!P1 bra W_%=;\n\t}" ::"r"(sm_u32(&bars[slot])),
-            "r"(phase[slot]), "r"(0x989680u)
-            : "memory");
-        phase[slot] ^= 1u;
+        asm volatile("cp.async.commit_group;" ::: "memory");
     };
 
-    for (uint32_t p = blockIdx.x * kTmaWarps + warp; p < npieces; p += gridDim.x * kTmaWarps) {
+    for (uint32_t p = blockIdx.x * kAsyncWarps + warp; p < npieces; p += gridDim.x * kAsyncWarps) {
         const uint32_t b = piece_node[p];
         const uint32_t r0 = node_start[b] + (p - piece_start[b]) * kPieceRows;
         const uint32_t r1 = min(r0 + kPieceRows, node_start[b + 1]);
@@ -355,29 +329,35 @@ __global__ void __launch_bounds__(kTmaWarps * 32, 2) k_gather_tma(
             const uint64_t row = sel ? (uint64_t)sel[pos[m]] : (uint64_t)pos[m];
             addr[m] = reinterpret_cast<uint64_t>(x + row * D);
         }
-        const float* wb = w + (size_t)b * D;
-        const double w0 = oka ? (double)wb[ka] : 0.0;
-        const double w1 = okb ? (double)wb[kb] : 0.0;
+        double w0 = 0.0, w1 = 0.0;
+        if (want_dist) {
+            const float* wb = w + (size_t)b * D;
+            w0 = oka ? (double)wb[ka] : 0.0;
+            w1 = okb ? (double)wb[kb] : 0.0;
+        }
         double a0 = 0.0, a1 = 0.0, ds = 0.0;
-        issue(addr[0], min(32u, r1 - r0), 0);
+        issue(&addr[0], min(32u, r1 - r0), 0);
 #pragma unroll
         for (int m = 0; m < 8; ++m) {
             if (m < (int)nb) {
                 const uint32_t rows_m = min(32u, r1 - (r0 + 32 * m));
-                if (m + 1 < (int)nb) issue(addr[m + 1], min(32u, r1 - (r0 + 32 * (m + 1))), (m + 1) & 1);
-                wait(m & 1);
-                const uint8_t* bm = buf + (size_t)(m & 1) * 32 * rowb;
+                if (m + 1 < (int)nb) {
+                    issue(&addr[m + 1], min(32u, r1 - (r0 + 32 * (m + 1))), (m + 1) & 1);
+                    asm volatile("cp.async.wait_group 1;" ::: "memory");
+                } else {
+                    asm volatile("cp.async.wait_group 0;" ::: "memory");
+                }
+                __syncwarp();
+                const float* bm = buf + (size_t)(m & 1) * 32 * rowf;
+#pragma unroll 4
                 for (uint32_t j = 0; j < rows_m; ++j) {
-                    const uint32_t mis = (uint32_t)__shfl_sync(0xffffffffu, (uint32_t)addr[m], j) & 15u;
-                    const float* xr = reinterpret_cast<const float*>(bm + (size_t)j * rowb + mis);
                     float2 v = make_float2(0.0f, 0.0f);
-                    if (okb) v = *reinterpret_cast<const float2*>(xr + ka);
-                    else if (oka) v.x = xr[ka];
-                    const double d0 = oka ? (double)v.x - w0 : 0.0;
-                    const double d1 = okb ? (double)v.y - w1 : 0.0;
-                    a0 += d0;
-                    a1 += d1;
+                    if (okb) v = *reinterpret_cast<const float2*>(bm + j * rowf + ka);
+                    a0 += (double)v.x;
+                    a1 += (double)v.y;
                     if (want_dist) {
+                        const double d0 = oka ? (double)v.x - w0 : 0.0;
+                        const double d1 = okb ? (double)v.y - w1 : 0.0;
                         double d2 = fma(d0, d0, d1 * d1);
 #pragma unroll
                         for (int o = 16; o; o >>= 1) d2 += __shfl_xor_sync(0xffffffffu, d2, o);
@@ -486,19 +466,18 @@ void launch_accumulate(const float* x, const uint32_t* sel, uint64_t n, uint32_t
     const uint64_t warps = pieces < (uint64_t)sm_count * 32 ? pieces : (uint64_t)sm_count * 32;
     const unsigned gblocks = (unsigned)((warps * 32 + 255) / 256);
     const bool v2 = (D % 2 == 0) && D <= 64 && ((reinterpret_cast<uintptr_t>(x) & 7u) == 0);
-    const uint32_t rowb = (D * 4 + 8 + 15) / 16 * 16;  // d even: row offset mod 16 is 0 or 8
-    const size_t tsmem = (size_t)kTmaWarps * (2 * 32 * rowb + 16);
-    if (v2 && x_slack && tsmem <= 110 * 1024) {
-        static size_t tattr = 0;
-        if (tattr < tsmem) {
-            cudaFuncSetAttribute(k_gather_tma, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                                 (int)tsmem);
-            tattr = tsmem;
+    const size_t asmem = (size_t)kAsyncWarps * 2 * 32 * D * sizeof(float);
+    if (v2 && D <= 64 && asmem <= 110 * 1024) {
+        static size_t aattr = 0;
+        if (aattr < asmem) {
+            cudaFuncSetAttribute(k_gather_async, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                 (int)asmem);
+            aattr = asmem;
         }
-        const uint64_t tblocks = (pieces + kTmaWarps - 1) / kTmaWarps;
-        const unsigned tb = (unsigned)(tblocks < (uint64_t)sm_count * 2 ? tblocks : sm_count * 2);
-        TSOM_LAUNCH(k_gather_tma<<<tb, kTmaWarps * 32, tsmem, st>>>(
-            x, sel, w, P, D, rowb, s.sorted, s.node_start, s.piece_start, s.piece_node, s.partial,
+        const uint64_t ablocks = (pieces + kAsyncWarps - 1) / kAsyncWarps;
+        const unsigned ab = (unsigned)(ablocks < (uint64_t)sm_count * 2 ? ablocks : sm_count * 2);
+        TSOM_LAUNCH(k_gather_async<<<ab, kAsyncWarps * 32, asmem, st>>>(
+            x, sel, w, P, D, s.sorted, s.node_start, s.piece_start, s.piece_node, s.partial,
             dist_out, want_dist ? 1 : 0, accumulate ? 1 : 0));
     } else if (v2)
         TSOM_LAUNCH(k_gather<true><<<gblocks, 256, 0, st>>>(

@@ -304,7 +304,7 @@ __device__ __forceinline__ double exact_d2(const float* __restrict__ x,
 __global__ void __launch_bounds__(256, 8) k_merge_fast(
     const float* __restrict__ part, uint64_t n, uint32_t groups, uint32_t gn,
     const float* __restrict__ xn2, const float* __restrict__ w2max, float tau,
-    uint32_t* __restrict__ bmu, uint32_t* __restrict__ ties) {
+    uint32_t* __restrict__ bmu, uint32_t* __restrict__ ties, uint32_t* __restrict__ tmask) {
     const uint64_t i = blockIdx.x * (uint64_t)blockDim.x + threadIdx.x;
     if (i >= n) return;
     const float thr = tau * (__ldg(xn2 + i) + __ldg(w2max));
@@ -317,45 +317,55 @@ __global__ void __launch_bounds__(256, 8) k_merge_fast(
     }
     bmu[i] = I1;
     if (!(B2 - B1 > thr)) {
+        // groups whose best lies inside the window (bit g; > 32 groups: all)
+        uint32_t mask = 0xFFFFFFFFu;
+        if (groups <= 32) {
+            mask = 0;
+            const float lim = B1 + thr;
+            for (uint32_t g = 0; g < groups; ++g)
+                if (__ldg(part + (size_t)g * 3 * n + i) <= lim) mask |= 1u << g;
+        }
         const uint32_t slot = atomicAdd(&ties[0], 1u);
         ties[1 + slot] = (uint32_t)i;
+        tmask[slot] = mask;
     }
 }
 
 void launch_merge_fast(const float* part, uint64_t n, uint32_t groups, uint32_t gn,
                        const float* xn2, const float* w2max, float tau, uint32_t* bmu,
-                       uint32_t* ties, cudaStream_t st) {
+                       uint32_t* ties, uint32_t* tmask, cudaStream_t st) {
     if (n == 0) return;
     TSOM_LAUNCH(k_merge_fast<<<(unsigned)((n + 255) / 256), 256, 0, st>>>(
-        part, n, groups, gn, xn2, w2max, tau, bmu, ties));
+        part, n, groups, gn, xn2, w2max, tau, bmu, ties, tmask));
 }
 
 
 // Enumerate-pass merge over the near-tie rows f < n (position ties[f]).
-// part[g] = [b1 | packed local candidate ids | count] (k1_bmu_tc<true>).
+// part[g] = [b1 | ids 0-3 | ids 4-7 | count] (k1_bmu_tc<true>, 8-bit local ids).
 // One candidate -> bmu; several -> exact FP64 distances of just those nodes in
 // ascending node order with strict < (lowest index wins), as find_bmus
-// (trainer.hpp:293-304); > 4 candidates in a group -> full exact re-scan list.
+// (trainer.hpp:293-304); > 8 candidates in a group -> full exact re-scan list.
 __global__ void k_merge_partials(const float* __restrict__ part, const uint32_t* __restrict__ ties,
-                                 uint64_t n, uint32_t groups, uint32_t gn, const float* __restrict__ xn2,
-                                 const float* __restrict__ w2max, float tau,
-                                 const float* __restrict__ x, const uint32_t* __restrict__ sel,
-                                 const float* __restrict__ w, uint32_t D,
-                                 uint32_t* __restrict__ bmu, uint32_t* __restrict__ flags) {
+                                 uint64_t n, uint32_t groups, uint32_t gn,
+                                 const float* __restrict__ xn2, const float* __restrict__ w2max,
+                                 float tau, const float* __restrict__ x,
+                                 const uint32_t* __restrict__ sel, const float* __restrict__ w,
+                                 uint32_t D, uint32_t* __restrict__ bmu,
+                                 uint32_t* __restrict__ flags) {
     for (uint64_t f = blockIdx.x * (uint64_t)blockDim.x + threadIdx.x; f < n;
          f += (uint64_t)gridDim.x * blockDim.x) {
         const uint32_t pos = ties[f];
         const float thr = tau * (__ldg(xn2 + f) + __ldg(w2max));
         float B1 = CUDART_INF_F;
-        for (uint32_t g = 0; g < groups; ++g) B1 = fminf(B1, part[(size_t)g * 3 * n + f]);
+        for (uint32_t g = 0; g < groups; ++g) B1 = fminf(B1, part[(size_t)g * 4 * n + f]);
         const float lim = B1 + thr;
         uint32_t ncand = 0, only = 0;
         bool overflow = false;
         for (uint32_t g = 0; g < groups; ++g) {
-            const float* pg = part + (size_t)g * 3 * n;
+            const float* pg = part + (size_t)g * 4 * n;
             if (!(pg[f] <= lim)) continue;
-            const uint32_t cnt = __float_as_uint(pg[2 * n + f]);
-            if (cnt > 4) overflow = true;
+            const uint32_t cnt = __float_as_uint(pg[3 * n + f]);
+            if (cnt > 8) overflow = true;
             ncand += cnt;
             only = g * gn + (__float_as_uint(pg[n + f]) & 0xFFu);
         }
@@ -374,12 +384,13 @@ __global__ void k_merge_partials(const float* __restrict__ part, const uint32_t*
         double best = CUDART_INF;
         uint32_t best_j = 0;
         for (uint32_t g = 0; g < groups; ++g) {
-            const float* pg = part + (size_t)g * 3 * n;
+            const float* pg = part + (size_t)g * 4 * n;
             if (!(pg[f] <= lim)) continue;
-            const uint32_t cnt = __float_as_uint(pg[2 * n + f]);
-            const uint32_t pack = __float_as_uint(pg[n + f]);
+            const uint32_t cnt = __float_as_uint(pg[3 * n + f]);
+            const uint32_t pk0 = __float_as_uint(pg[n + f]), pk1 = __float_as_uint(pg[2 * n + f]);
             for (uint32_t c = 0; c < cnt; ++c) {
-                const uint32_t j = g * gn + ((pack >> (8 * c)) & 0xFFu);
+                const uint32_t pk = c < 4 ? pk0 : pk1;
+                const uint32_t j = g * gn + ((pk >> (8 * (c & 3))) & 0xFFu);
                 const double d2 = exact_d2(xr, w + (size_t)j * D, D);
                 if (d2 < best) {
                     best = d2;

@@ -14,7 +14,7 @@
 
 namespace tsom {
 
-// S_aug[b][k] = R_b[k] + c_b * w_b[k] (k < d), S_aug[b][d] = c_b
+// S_aug[b][k] = S_b[k] (k < d), S_aug[b][d] = c_b   (sums = [S | c | ...])
 __global__ void k_build_saug(const double* __restrict__ sums, const float* __restrict__ w,
                              uint32_t P, uint32_t D, double* __restrict__ saug) {
     const size_t e = blockIdx.x * (size_t)blockDim.x + threadIdx.x;
@@ -22,7 +22,7 @@ __global__ void k_build_saug(const double* __restrict__ sums, const float* __res
     if (e >= (size_t)P * Dp) return;
     const uint32_t b = (uint32_t)(e / Dp), k = (uint32_t)(e % Dp);
     const double c = sums[(size_t)P * D + b];
-    saug[e] = k < D ? sums[(size_t)b * D + k] + c * (double)w[(size_t)b * D + k] : c;
+    saug[e] = k < D ? sums[(size_t)b * D + k] : c;
 }
 
 // H_j = sum_b infl[b][j] c_b: block = 32 nodes x 8 b-slices, fixed-order fold

@@ -1,7 +1,7 @@
 """Multi-rank (data-parallel) host logic on CPU with gloo, world size 2.
 
 The engine's N>1 path: each rank reduces its own row shard to
-the packed sums [R_b | c_b | sum dist | rows], one allreduce(sum) combines
+the packed sums [S_b | c_b | sum dist | rows], one allreduce(sum) combines
 them, and every rank runs the identical FP64 smoothing.  Here the per-rank K2
 sums are restated in numpy from the oracle's BMUs, combined with a real gloo
 allreduce, smoothed with the K3 algebra, and compared with the single-process
@@ -30,20 +30,19 @@ def test_assign_shards_matches_reference():
 
 
 def shard_sums(x, w, bmu):
-    """K2 restated: residual sums R_b = sum (x_i - w_b), counts c_b (FP64)."""
+    """K2 restated: row sums S_b = sum x_i, counts c_b (FP64)."""
     P, D = w.shape
-    R = np.zeros((P, D))
-    np.add.at(R, bmu, x.astype(np.float64) - w[bmu].astype(np.float64))
+    S = np.zeros((P, D))
+    np.add.at(S, bmu, x.astype(np.float64))
     c = np.bincount(bmu, minlength=P).astype(np.float64)
-    return np.concatenate([R.ravel(), c, [0.0, float(len(bmu))]])
+    return np.concatenate([S.ravel(), c, [0.0, float(len(bmu))]])
 
 
 def smooth(sums, w, infl, eta):
-    """K3 restated: S_b = R_b + c_b w_b; U = eta (h^T S - w H); H = h^T c."""
+    """K3 restated: U = eta (h^T S - w H); H = h^T c."""
     P, D = w.shape
-    R = sums[:P * D].reshape(P, D)
+    S = sums[:P * D].reshape(P, D)
     c = sums[P * D:P * D + P]
-    S = R + c[:, None] * w.astype(np.float64)
     H = infl.T @ c
     U = eta * (infl.T @ S - w.astype(np.float64) * H[:, None])
     return U, H
