@@ -131,6 +131,17 @@ int tsom_set_topology_distance(tsom_engine* eng, const double* dist);
  * on.  Weights stay on the device (read with tsom_get_codebook). */
 int tsom_train_epoch(tsom_engine* eng, double eta, double sigma, double momentum,
                      uint32_t flags);
+/* Topology refresh on the device (refresh_topology topology.hpp:439-451) from
+ * the engine's current codebook: FP64 Gram (pairwise_sq_dists :81-108), then
+ * kind 2 = MST (build_mst :192-220) or 3 = RNG (build_rng_graph :229-258), then
+ * all-pairs hop counts (hop_distances :292-325) which become the distance
+ * matrix of the device-resident loop.  edges_out (optional): (i, j) pairs, i < j,
+ * lexicographic; hops_out (optional): P x P uint16.  Errors: "hop_distances:
+ * graph is disconnected" (TSOM_ERR_NUMERICAL). */
+int tsom_refresh_topology(tsom_engine* eng, int kind, uint32_t* edges_out, uint64_t edges_cap,
+                          uint64_t* n_edges, uint16_t* hops_out);
+/* pairwise_sq_dists (topology.hpp:81-108) of the current codebook, P x P f64. */
+int tsom_pairwise_sq_dists(tsom_engine* eng, double* out);
 /* Rows of the last BMU pass whose winner was decided in exact FP64 (several
  * candidates inside the FP32 error window, or a full re-scan). */
 uint64_t tsom_last_recheck_count(const tsom_engine* eng);

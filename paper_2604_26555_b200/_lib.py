@@ -36,7 +36,8 @@ EXPORTS = [
     "tsom_set_codebook", "tsom_get_codebook", "tsom_set_influence", "tsom_epoch", "tsom_bmu",
     "tsom_bmu_bound", "tsom_qe", "tsom_set_topology_distance", "tsom_train_epoch",
     "tsom_last_recheck_count", "tsom_comm_unique_id", "tsom_comm_init", "tsom_last_timing",
-    "tsom_stream", "tsom_last_timing_detail", "tsom_kernel_launches",
+    "tsom_stream", "tsom_last_timing_detail", "tsom_kernel_launches", "tsom_refresh_topology",
+    "tsom_pairwise_sq_dists",
 ]
 
 
@@ -107,6 +108,8 @@ def load():
     L.tsom_last_timing.argtypes = [_vp] + [C.POINTER(C.c_float)] * 4
     L.tsom_last_timing_detail.argtypes = [_vp, C.POINTER(C.c_float)]
     L.tsom_kernel_launches.restype = u64
+    L.tsom_refresh_topology.argtypes = [_vp, i32, _vp, u64, C.POINTER(u64), _vp]
+    L.tsom_pairwise_sq_dists.argtypes = [_vp, _vp]
     L.tsom_stream.argtypes = [_vp]
     L.tsom_stream.restype = _vp
     for name in EXPORTS:
@@ -253,6 +256,23 @@ class Engine:
         self._check(self.L.tsom_last_timing(self.h, *[C.byref(x) for x in v]))
         return {"bmu_ms": v[0].value, "accum_ms": v[1].value, "smooth_ms": v[2].value,
                 "total_ms": v[3].value}
+
+    def refresh_topology(self, kind: str, want_hops: bool = False):
+        """Device refresh_topology: returns (edges [m, 2] uint32, hops [P, P] or None)."""
+        k = {"mst": 2, "rng": 3}[kind]
+        P = self.nodes
+        cap = max(1, P * (P - 1) // 2)
+        edges = np.empty(2 * cap, np.uint32)
+        ne = C.c_uint64()
+        hops = np.empty((P, P), np.uint16) if want_hops else None
+        self._check(self.L.tsom_refresh_topology(self.h, k, _ptr(edges), cap, C.byref(ne),
+                                                 _ptr(hops)))
+        return edges[: 2 * ne.value].reshape(-1, 2).copy(), hops
+
+    def pairwise_sq_dists(self) -> np.ndarray:
+        out = np.empty((self.nodes, self.nodes))
+        self._check(self.L.tsom_pairwise_sq_dists(self.h, _ptr(out)))
+        return out
 
     def timing_detail(self):
         v = (C.c_float * 8)()

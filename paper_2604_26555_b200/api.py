@@ -22,8 +22,8 @@ from dataclasses import dataclass
 import numpy as np
 
 from ._lib import Engine, InvalidArgument, NumericalFault, OutOfRange  # noqa: F401
-from .hostref import (Rng, init_sample_draw, lattice_dist, resolved_sigma0,  # noqa: F401
-                      schedule_value)
+from .hostref import (RefreshState, Rng, init_sample_draw, lattice_dist,  # noqa: F401
+                      resolved_sigma0, schedule_value)
 
 
 def _as_rows(a) -> np.ndarray:
@@ -117,11 +117,16 @@ class CudaExecutor:
 
 @dataclass
 class ResidentConfig:
-    """Subset of SomConfig (trainer.hpp:58-99) the device-resident loop supports."""
+    """Subset of SomConfig (trainer.hpp:58-99) the device-resident loop supports
+    (full sampling; lattices, or MST/RNG graphs refreshed on the device)."""
 
-    topology: str = "hex"       # "rect" | "hex"
+    topology: str = "hex"       # "rect" | "hex" | "mst" | "rng"
     grid_w: int = 32
     grid_h: int = 32
+    graph_nodes: int = 0        # graph kinds: node count
+    refresh_warmup: int = 0     # 0 = auto: 10% of n_iters (trainer.hpp:81-85)
+    refresh_growth: float = 1.5
+    refresh_max_interval: int = 25
     n_iters: int = 10
     eta0: float = 0.5
     lr_decay: str = "linear"
@@ -133,27 +138,42 @@ class ResidentConfig:
     seed: int = 0
 
     @property
+    def lattice(self) -> bool:
+        return self.topology in ("rect", "rectangular", "hex", "hexagonal")
+
+    @property
     def nodes(self) -> int:
-        return self.grid_w * self.grid_h
+        return self.grid_w * self.grid_h if self.lattice else self.graph_nodes
 
 
 def train_resident(cfg: ResidentConfig, engine: Engine, init_weights=None, log_qe=False):
-    """train_with_executor (trainer.hpp:466-523) with full sampling on a lattice:
-    every epoch (influence, BMU, accumulate, allreduce, smoothing, update) runs on
-    the device; the host only evaluates the two schedules.  Returns the log."""
-    if cfg.topology not in ("rect", "rectangular", "hex", "hexagonal"):
-        raise InvalidArgument(1, "train_resident: lattice topologies only")
+    """train_with_executor (trainer.hpp:466-523) with full sampling, every epoch on
+    the device: topology refresh (graphs, on the schedule of should_refresh),
+    influence, BMU, accumulate, allreduce, smoothing, update.  The host only
+    evaluates the schedules.  Returns the per-iteration log."""
     if init_weights is None:
         raise InvalidArgument(1, "train_resident: pass init weights (init_sample_draw)")
     engine.set_codebook(init_weights)
-    engine.set_topology_distance(lattice_dist(cfg.topology, cfg.grid_w, cfg.grid_h))
+    refresh = None
+    if cfg.lattice:
+        engine.set_topology_distance(lattice_dist(cfg.topology, cfg.grid_w, cfg.grid_h))
+    elif cfg.topology in ("mst", "rng"):
+        warm = cfg.refresh_warmup if cfg.refresh_warmup else cfg.n_iters // 10
+        refresh = RefreshState(warm, cfg.refresh_growth, cfg.refresh_max_interval)
+    else:
+        raise InvalidArgument(1, f"unknown topology kind: '{cfg.topology}'")
     sigma0 = resolved_sigma0(cfg.topology, cfg.grid_w, cfg.grid_h, cfg.sigma0)
     log = []
     for t in range(cfg.n_iters):
+        refreshed = False
+        if refresh is not None and refresh.should_refresh(t):
+            engine.refresh_topology(cfg.topology)  # from the current device codebook
+            refresh.mark(t)
+            refreshed = True
         eta = schedule_value(cfg.eta0, cfg.lr_decay, t, cfg.n_iters, 1e-4)
         sigma = schedule_value(sigma0, cfg.radius_decay, t, cfg.n_iters, cfg.sigma_min)
         engine.train_epoch(eta, sigma, cfg.momentum, cfg.use_momentum)
-        entry = {"iter": t, "eta": eta, "sigma": sigma}
+        entry = {"iter": t, "eta": eta, "sigma": sigma, "refreshed": refreshed}
         if log_qe:
             s, c = engine.qe()
             entry["qe_train"] = s / c

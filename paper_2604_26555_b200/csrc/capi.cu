@@ -480,7 +480,11 @@ int tsom_destroy(tsom_engine* eng) {
                       &eng->w2max, &eng->prev, &eng->infl, &eng->topo_dist, &eng->sel,
                       &eng->rows_scratch, &eng->gsplit, &eng->bmu, &eng->dist, &eng->part,
                       &eng->flags, &eng->ties, &eng->tmask, &eng->part2, &eng->tsplit, &eng->acc_buf[0], &eng->acc_buf[1], &eng->acc_buf[2], &eng->acc_buf[3],
-                      &eng->acc_buf[4], &eng->acc_buf[5], &eng->acc_buf[6], &eng->sums, &eng->U, &eng->H, &eng->status, &eng->smooth_scratch,
+                      &eng->acc_buf[4], &eng->acc_buf[5], &eng->acc_buf[6], &eng->sums,
+                      &eng->topo_buf[0], &eng->topo_buf[1], &eng->topo_buf[2], &eng->topo_buf[3],
+                      &eng->topo_buf[4], &eng->topo_buf[5], &eng->topo_buf[6], &eng->topo_buf[7],
+                      &eng->topo_buf[8], &eng->topo_buf[9], &eng->topo_buf[10], &eng->topo_buf[11],
+                      &eng->topo_buf[12], &eng->topo_buf[13], &eng->topo_buf[14], &eng->U, &eng->H, &eng->status, &eng->smooth_scratch,
                       &eng->stage[0], &eng->stage[1]})
         b->release();
     for (auto& ev : eng->ev)
@@ -755,6 +759,92 @@ int tsom_set_topology_distance(tsom_engine* eng, const double* dist) {
         CU(cudaStreamSynchronize(eng->stream));
         eng->topo_set = true;
         eng->infl_key = -2;
+    });
+}
+
+}  // extern "C"
+
+namespace {
+void ensure_topo(Engine* eng) {
+    const size_t P = eng->P;
+    if (eng->topo_p == P && eng->topo.d2) return;
+    const size_t sizes[15] = {P * 8,     P * P * 8,         P * 4,     2 * P * 8, 2 * P * 4,
+                              2 * P * 4, P * P,             P * 4,     P * (P > 1 ? P - 1 : 1) * 4 + 8,
+                              4,         (P + 1) * 4,       P * (P > 1 ? P - 1 : 1) * 4 + 8,
+                              P * P * 2, P * P * 8,         4};
+    for (int i = 0; i < 15; ++i) CU(eng->topo_buf[i].ensure(sizes[i]));
+    tsom::TopoScratch& t = eng->topo;
+    t.norms = eng->topo_buf[0].as<double>();
+    t.d2 = eng->topo_buf[1].as<double>();
+    t.comp = eng->topo_buf[2].as<uint32_t>();
+    t.bw = eng->topo_buf[3].as<double>();
+    t.ba = eng->topo_buf[4].as<uint32_t>();
+    t.bb = eng->topo_buf[5].as<uint32_t>();
+    t.keep = eng->topo_buf[6].as<uint8_t>();
+    t.rowcnt = eng->topo_buf[7].as<uint32_t>();
+    t.edges = eng->topo_buf[8].as<uint32_t>();
+    t.ne = eng->topo_buf[9].as<uint32_t>();
+    t.deg = eng->topo_buf[10].as<uint32_t>();
+    t.adj = eng->topo_buf[11].as<uint32_t>();
+    t.hops = eng->topo_buf[12].as<uint16_t>();
+    t.hopd = eng->topo_buf[13].as<double>();
+    t.status = eng->topo_buf[14].as<uint32_t>();
+    eng->topo_p = (uint32_t)P;
+}
+}  // namespace
+
+extern "C" {
+
+int tsom_refresh_topology(tsom_engine* eng, int kind, uint32_t* edges_out, uint64_t edges_cap,
+                          uint64_t* n_edges, uint16_t* hops_out) {
+    return guarded(eng, [&] {
+        CU(cudaSetDevice(eng->device));
+        REQUIRE(kind == 2 || kind == 3, TSOM_ERR_INVALID,
+                "refresh_topology: kind must be 2 (mst) or 3 (rng)");
+        REQUIRE(eng->codebook_set, TSOM_ERR_INVALID, "engine: codebook not set (tsom_set_codebook)");
+        REQUIRE(kind != 3 || eng->P >= 2, TSOM_ERR_INVALID, "build_rng_graph: P must be >= 2");
+        REQUIRE(eng->P <= 8192, TSOM_ERR_INVALID, "refresh_topology: P <= 8192 on the device");
+        ensure_topo(eng);
+        tsom::launch_refresh_topology(eng->w.as<float>(), eng->P, eng->D, kind, eng->topo,
+                                      eng->stream);
+        CU(cudaGetLastError());
+        uint32_t st = 0, ne = 0;
+        CU(cudaMemcpyAsync(&st, eng->topo.status, 4, cudaMemcpyDeviceToHost, eng->stream));
+        CU(cudaMemcpyAsync(&ne, eng->topo.ne, 4, cudaMemcpyDeviceToHost, eng->stream));
+        CU(cudaStreamSynchronize(eng->stream));
+        REQUIRE(!(st & 2u), TSOM_ERR_RANGE, "hop_distances: edge index out of range");
+        REQUIRE(!(st & 1u), TSOM_ERR_NUMERICAL, "hop_distances: graph is disconnected");
+        if (n_edges) *n_edges = ne;
+        if (edges_out) {
+            REQUIRE(edges_cap >= ne, TSOM_ERR_INVALID, "refresh_topology: edge buffer too small");
+            CU(cudaMemcpy(edges_out, eng->topo.edges, (size_t)ne * 2 * sizeof(uint32_t),
+                          cudaMemcpyDeviceToHost));
+        }
+        if (hops_out)
+            CU(cudaMemcpy(hops_out, eng->topo.hops, (size_t)eng->P * eng->P * sizeof(uint16_t),
+                          cudaMemcpyDeviceToHost));
+        // the device-resident loop builds its influence from these hop counts
+        const size_t nn = (size_t)eng->P * eng->P;
+        CU(eng->topo_dist.ensure(nn * sizeof(double)));
+        CU(cudaMemcpyAsync(eng->topo_dist.p, eng->topo.hopd, nn * sizeof(double),
+                           cudaMemcpyDeviceToDevice, eng->stream));
+        CU(cudaStreamSynchronize(eng->stream));
+        eng->topo_set = true;
+        eng->infl_key = -2;  // influence cache cleared on refresh (topology.hpp:447)
+    });
+}
+
+int tsom_pairwise_sq_dists(tsom_engine* eng, double* out) {
+    return guarded(eng, [&] {
+        CU(cudaSetDevice(eng->device));
+        REQUIRE(eng->codebook_set, TSOM_ERR_INVALID, "engine: codebook not set (tsom_set_codebook)");
+        ensure_topo(eng);
+        // the Gram alone (kind 0: no graph)
+        tsom::launch_gram_only(eng->w.as<float>(), eng->P, eng->D, eng->topo, eng->stream);
+        CU(cudaGetLastError());
+        CU(cudaMemcpyAsync(out, eng->topo.d2, (size_t)eng->P * eng->P * sizeof(double),
+                           cudaMemcpyDeviceToHost, eng->stream));
+        CU(cudaStreamSynchronize(eng->stream));
     });
 }
 

@@ -66,6 +66,29 @@ struct AccumScratch {
     uint32_t* sorted = nullptr;      // [n] positions in BMU order
     double* partial = nullptr;       // [pieces][d+1]
 };
+// Topology refresh scratch (k_topology.cu), P x P arrays on the device.
+struct TopoScratch {
+    double* norms = nullptr;   // [P]
+    double* d2 = nullptr;      // [P*P] pairwise squared distances (FP64 Gram)
+    uint32_t* comp = nullptr;  // [P]
+    double* bw = nullptr;      // [2P]
+    uint32_t* ba = nullptr;    // [2P]
+    uint32_t* bb = nullptr;    // [2P]
+    uint8_t* keep = nullptr;   // [P*P] edge mask (a < b)
+    uint32_t* rowcnt = nullptr;// [P]
+    uint32_t* edges = nullptr; // [P*(P-1)] (i, j) pairs, lexicographic
+    uint32_t* ne = nullptr;    // [1]
+    uint32_t* deg = nullptr;   // [P+1] CSR offsets
+    uint32_t* adj = nullptr;   // [2 * edges]
+    uint16_t* hops = nullptr;  // [P*P]
+    double* hopd = nullptr;    // [P*P] hop counts widened (influence input)
+    uint32_t* status = nullptr;// bit0 disconnected, bit1 edge out of range
+};
+// refresh_topology (topology.hpp:439-451) for kind 2 (MST) / 3 (RNG)
+int launch_refresh_topology(const float* w, uint32_t P, uint32_t D, int kind, TopoScratch& s,
+                            cudaStream_t st);
+void launch_gram_only(const float* w, uint32_t P, uint32_t D, TopoScratch& s, cudaStream_t st);
+
 struct Engine {
     int device = 0;
     uint32_t P = 0, D = 0;
@@ -104,6 +127,9 @@ struct Engine {
     bool infl_set = false;
     DevBuf topo_dist;
     bool topo_set = false;
+    DevBuf topo_buf[15];
+    tsom::TopoScratch topo;
+    uint32_t topo_p = 0;  // P the scratch was sized for
 
     // per-epoch scratch
     DevBuf sel;

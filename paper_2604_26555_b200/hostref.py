@@ -11,6 +11,7 @@ compute fallback: none of them touches samples.
 * :func:`resolved_sigma0`   — trainer.hpp:75-80
 * :func:`lattice_dist`      — topology.hpp:114-149
 * :func:`assign_shards`     — parallel.hpp:28-41 (row shards per rank/GPU)
+* :class:`RefreshState`     — should_refresh / refresh bookkeeping, topology.hpp:68-72, 423-451
 """
 from __future__ import annotations
 
@@ -144,3 +145,30 @@ def assign_shards(n: int, workers: int) -> list[tuple[int, int]]:
         out.append((begin, begin + cnt))
         begin += cnt
     return out
+
+
+class RefreshState:
+    """Graph refresh schedule (RefreshPolicy topology.hpp:68-72; should_refresh
+    :423-435; the counters refresh_topology updates :447-450)."""
+
+    def __init__(self, warmup_iters: int, growth: float = 1.5, max_interval: int = 25):
+        if not growth > 1.0:
+            raise ValueError("config: refresh growth must be > 1")
+        self.warmup, self.growth, self.max_interval = warmup_iters, growth, max_interval
+        self.last_refresh_iter = -1
+        self.refresh_count = 0
+        self.post_warmup_refreshes = 0
+
+    def should_refresh(self, it: int) -> bool:
+        if it < self.warmup:
+            return True
+        raw = math.ceil(math.pow(self.growth, float(self.post_warmup_refreshes)))
+        interval = self.max_interval if raw >= float(self.max_interval) else int(raw)
+        interval = min(self.max_interval, interval)
+        return it - self.last_refresh_iter >= interval
+
+    def mark(self, it: int):
+        self.last_refresh_iter = it
+        self.refresh_count += 1
+        if it >= self.warmup:
+            self.post_warmup_refreshes += 1

@@ -44,3 +44,23 @@ def test_schedule_values(oracle_port):
     assert hostref.schedule_value(0.001, "linear", 99, 100, 1e-4) == 1e-4
     assert hostref.resolved_sigma0("hex", 32, 32) == 16.0
     assert hostref.resolved_sigma0("mst", 0, 0) == 3.0
+
+
+def test_refresh_schedule_matches_reference():
+    # test_topology.cpp:351-367: growth 2, warmup 10 -> 0..9, 10, 12, 16, 24
+    st = hostref.RefreshState(10, 2.0, 25)
+    got = []
+    for it in range(30):
+        if st.should_refresh(it):
+            st.mark(it)
+            got.append(it)
+    assert got == [0, 1, 2, 3, 4, 5, 6, 7, 8, 9, 10, 12, 16, 24]
+    assert st.post_warmup_refreshes == 4
+    # test_topology.cpp:369-383: saturation at max_interval
+    st = hostref.RefreshState(1, 10.0, 5)
+    got = []
+    for it in range(25):
+        if st.should_refresh(it):
+            st.mark(it)
+            got.append(it)
+    assert got == [0, 1, 6, 11, 16, 21]
