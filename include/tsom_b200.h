@@ -62,7 +62,9 @@ typedef struct tsom_engine tsom_engine;
 
 /* Engine lifetime ---------------------------------------------------------- */
 
-/* Create an engine for a P-node, d-dimensional codebook on CUDA `device`. */
+/* Create an engine for a P-node, d-dimensional codebook on CUDA `device`
+ * (1 <= d <= 256; the tensor-core BMU kernel covers d <= 54, larger d uses the
+ * SIMT kernel). */
 int tsom_create(int device, uint32_t nodes, uint32_t dims, tsom_engine** out);
 int tsom_destroy(tsom_engine* eng);
 const char* tsom_last_error(const tsom_engine* eng);

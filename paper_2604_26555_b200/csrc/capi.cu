@@ -214,8 +214,10 @@ void run_bmu(Engine* eng, const float* x, const uint32_t* sel, uint64_t n, const
         }
     } else {
         CU(cudaEventRecord(eng->ev[8], eng->stream));
+        // the FP32 accumulation bound grows with the d+1 terms of each dot product
+        const double tau_s = eng->tau_simt * std::max(1.0, (eng->D + 1) / 51.0);
         tsom::launch_bmu_simt(x, sel, n, eng->D, eng->wt.as<float>(), eng->P, ppad(eng), x2max,
-                              eng->w2max.as<float>(), (float)eng->tau_simt, eng->bmu.as<uint32_t>(),
+                              eng->w2max.as<float>(), (float)tau_s, eng->bmu.as<uint32_t>(),
                               eng->flags.as<uint32_t>(), eng->sm_count, eng->stream);
         CU(cudaEventRecord(eng->ev[9], eng->stream));
         eng->k1_timed = true;
@@ -427,7 +429,7 @@ const char* tsom_version(void) { return kVersion; }
 int tsom_create(int device, uint32_t nodes, uint32_t dims, tsom_engine** out) {
     if (!out) return TSOM_ERR_INVALID;
     *out = nullptr;
-    if (nodes < 1 || dims < 1) return TSOM_ERR_INVALID;
+    if (nodes < 1 || dims < 1 || dims > 256) return TSOM_ERR_INVALID;  // d <= 256 (K2 lanes)
     auto* eng = new tsom_engine();
     eng->device = device;
     eng->P = nodes;

@@ -197,64 +197,69 @@ __global__ void __launch_bounds__(kScatterWarps * 32) k_scatter(
 // gather + FP64 accumulation per piece
 // ---------------------------------------------------------------------------
 
-// partial[p][k] (k < D) = sum over the piece's rows of x_k in FP64;
-// partial[p][D] = sum of their exact BMU distances (when requested).
-// V2: d even — lane l < d/2 owns dims 2l, 2l+1 and reads them with one 8-byte
-// load per row (rows are 8-byte aligned); otherwise lanes own l and l+32.
-template <bool V2>
-__global__ void __launch_bounds__(256, 3) k_gather(
+// Generic gather (any d <= 256): lane l owns features l, l+32, ... (NQ slots),
+// rows loaded through registers in batches of 8.  partial[p][k] (k < D) =
+// sum over the piece's rows of x_k in FP64; partial[p][D] = sum of exact
+// distances (when requested).
+template <int NQ>
+__global__ void __launch_bounds__(256) k_gather_any(
     const float* __restrict__ x, const uint32_t* __restrict__ sel, const float* __restrict__ w,
     uint32_t P, uint32_t D, const uint32_t* __restrict__ sorted,
     const uint32_t* __restrict__ node_start, const uint32_t* __restrict__ piece_start,
     const uint32_t* __restrict__ piece_node, double* __restrict__ partial,
     double* __restrict__ dist_out, int want_dist, int accumulate) {
+    constexpr int B = 8;
     const int lane = threadIdx.x & 31;
     const uint32_t npieces = piece_start[P];
     const uint32_t Dp = D + 1;
-    const uint32_t ka = V2 ? 2 * lane : lane, kb = V2 ? 2 * lane + 1 : lane + 32;
-    const bool oka = ka < D, okb = kb < D;
     for (uint32_t p = (blockIdx.x * blockDim.x + threadIdx.x) >> 5; p < npieces;
          p += (gridDim.x * blockDim.x) >> 5) {
         const uint32_t b = piece_node[p];
         const uint32_t r0 = node_start[b] + (p - piece_start[b]) * kPieceRows;
         const uint32_t r1 = min(r0 + kPieceRows, node_start[b + 1]);
         const float* wb = w + (size_t)b * D;
-        const double w0 = oka ? (double)wb[ka] : 0.0;
-        const double w1 = okb ? (double)wb[kb] : 0.0;
-        double a0 = 0.0, a1 = 0.0, ds = 0.0;
+        double wv[NQ], acc[NQ];
+#pragma unroll
+        for (int q = 0; q < NQ; ++q) {
+            const uint32_t k = lane + 32 * q;
+            wv[q] = k < D ? (double)wb[k] : 0.0;
+            acc[q] = 0.0;
+        }
+        double ds = 0.0;
         for (uint32_t r = r0; r < r1; r += 32) {
             const uint32_t mrow = min(32u, r1 - r);
-            // one coalesced load of up to 32 positions, broadcast per row
             uint32_t mypos = 0;
             uint64_t myrow = 0;
             if (lane < (int)mrow) {
                 mypos = sorted[r + lane];
                 myrow = sel ? (uint64_t)sel[mypos] : (uint64_t)mypos;
             }
-            for (uint32_t j0 = 0; j0 < mrow; j0 += kGatherBatch) {
-                float2 xv[kGatherBatch];
+            for (uint32_t j0 = 0; j0 < mrow; j0 += B) {
+                float xv[B][NQ];
 #pragma unroll
-                for (int j = 0; j < kGatherBatch; ++j) {
+                for (int j = 0; j < B; ++j) {
                     const uint64_t row = __shfl_sync(0xffffffffu, myrow, (j0 + j) & 31);
                     const float* xr = x + row * D;
                     const bool ok = j0 + j < mrow;
-                    if (V2) {
-                        xv[j] = (ok && oka) ? __ldg(reinterpret_cast<const float2*>(xr + ka))
-                                            : make_float2(0.0f, 0.0f);
-                    } else {
-                        xv[j].x = (ok && oka) ? __ldg(xr + ka) : 0.0f;
-                        xv[j].y = (ok && okb) ? __ldg(xr + kb) : 0.0f;
+#pragma unroll
+                    for (int q = 0; q < NQ; ++q) {
+                        const uint32_t k = lane + 32 * q;
+                        xv[j][q] = (ok && k < D) ? __ldg(xr + k) : 0.0f;
                     }
                 }
 #pragma unroll
-                for (int j = 0; j < kGatherBatch; ++j) {
+                for (int j = 0; j < B; ++j) {
                     if (j0 + j < mrow) {
-                        const double d0 = oka ? (double)xv[j].x - w0 : 0.0;
-                        const double d1 = okb ? (double)xv[j].y - w1 : 0.0;
-                        a0 += (double)xv[j].x;
-                        a1 += (double)xv[j].y;
+                        double d2 = 0.0;
+#pragma unroll
+                        for (int q = 0; q < NQ; ++q) {
+                            acc[q] += (double)xv[j][q];
+                            if (want_dist && lane + 32 * q < D) {
+                                const double dd = (double)xv[j][q] - wv[q];
+                                d2 = fma(dd, dd, d2);
+                            }
+                        }
                         if (want_dist) {
-                            double d2 = fma(d0, d0, d1 * d1);
 #pragma unroll
                             for (int o = 16; o; o >>= 1) d2 += __shfl_xor_sync(0xffffffffu, d2, o);
                             const double dist = sqrt(d2 > 0.0 ? d2 : 0.0);
@@ -268,8 +273,9 @@ __global__ void __launch_bounds__(256, 3) k_gather(
         }
         double* out = partial + (size_t)p * Dp;
         if (accumulate) {
-            if (oka) out[ka] = a0;
-            if (okb) out[kb] = a1;
+#pragma unroll
+            for (int q = 0; q < NQ; ++q)
+                if (lane + 32 * q < D) out[lane + 32 * q] = acc[q];
         }
         if (lane == 0) out[D] = ds;
     }
@@ -479,14 +485,24 @@ void launch_accumulate(const float* x, const uint32_t* sel, uint64_t n, uint32_t
         TSOM_LAUNCH(k_gather_async<<<ab, kAsyncWarps * 32, asmem, st>>>(
             x, sel, w, P, D, s.sorted, s.node_start, s.piece_start, s.piece_node, s.partial,
             dist_out, want_dist ? 1 : 0, accumulate ? 1 : 0));
-    } else if (v2)
-        TSOM_LAUNCH(k_gather<true><<<gblocks, 256, 0, st>>>(
-            x, sel, w, P, D, s.sorted, s.node_start, s.piece_start, s.piece_node, s.partial,
-            dist_out, want_dist ? 1 : 0, accumulate ? 1 : 0));
-    else
-        TSOM_LAUNCH(k_gather<false><<<gblocks, 256, 0, st>>>(
-            x, sel, w, P, D, s.sorted, s.node_start, s.piece_start, s.piece_node, s.partial,
-            dist_out, want_dist ? 1 : 0, accumulate ? 1 : 0));
+    } else {
+        const int nq = (int)((D + 31) / 32);
+#define TSOM_GATHER_ANY(NQ)                                                                     \
+    TSOM_LAUNCH(k_gather_any<NQ><<<gblocks, 256, 0, st>>>(                                     \
+        x, sel, w, P, D, s.sorted, s.node_start, s.piece_start, s.piece_node, s.partial,       \
+        dist_out, want_dist ? 1 : 0, accumulate ? 1 : 0))
+        switch (nq) {
+            case 1: TSOM_GATHER_ANY(1); break;
+            case 2: TSOM_GATHER_ANY(2); break;
+            case 3: TSOM_GATHER_ANY(3); break;
+            case 4: TSOM_GATHER_ANY(4); break;
+            case 5: TSOM_GATHER_ANY(5); break;
+            case 6: TSOM_GATHER_ANY(6); break;
+            case 7: TSOM_GATHER_ANY(7); break;
+            default: TSOM_GATHER_ANY(8); break;
+        }
+#undef TSOM_GATHER_ANY
+    }
     const size_t m = (size_t)P * D;
     if (accumulate)
         TSOM_LAUNCH(k_piece_reduce<<<(unsigned)((m * 32 + 255) / 256), 256, 0, st>>>(
