@@ -85,19 +85,20 @@ public:
         if (opts.bmu_kernel) eng_->check(tsom_set_option(eng_->h, TSOM_OPT_BMU_KERNEL, opts.bmu_kernel));
         if (data.in_memory()) {
             rows_ = data.matrix();
+            eng_->check(tsom_bind_host_data(eng_->h, rows_->values.data(), rows_->rows,
+                                            opts.streamed ? TSOM_BIND_STREAMED : TSOM_BIND_COPY));
         } else {
-            // Shard-backed source: materialise once in host memory (the engine
-            // then streams or uploads it); the per-epoch rescans of
-            // DataSourceRef::fetch_rows (dataset.hpp:400-415) disappear.
-            owned_ = std::make_unique<DataMatrix>(0, data.cols());
-            data.for_each_row([&](std::size_t, const float* r) {
-                owned_->values.insert(owned_->values.end(), r, r + data.cols());
-                ++owned_->rows;
-            });
-            rows_ = owned_.get();
+            // Shard-backed source: the engine reads the FSOMSHRD files itself
+            // (copied once into HBM, or streamed from disk every epoch through
+            // pinned staging), replacing the per-epoch rescans of
+            // DataSourceRef::fetch_rows (dataset.hpp:400-415).
+            std::vector<std::string> names;
+            for (const auto& p : data.shards()->shard_paths) names.push_back(p.string());
+            std::vector<const char*> cpaths;
+            for (const auto& n : names) cpaths.push_back(n.c_str());
+            eng_->check(tsom_bind_shards(eng_->h, cpaths.data(), (std::uint32_t)cpaths.size(),
+                                         opts.streamed ? TSOM_BIND_STREAMED : TSOM_BIND_COPY));
         }
-        eng_->check(tsom_bind_host_data(eng_->h, rows_->values.data(), rows_->rows,
-                                        opts.streamed ? TSOM_BIND_STREAMED : TSOM_BIND_COPY));
     }
 
     /// Executor::run_iteration (trainer.hpp:446-453): one accumulation pass
@@ -139,7 +140,6 @@ private:
     std::unique_ptr<Engine> eng_;
     std::size_t nodes_, dims_;
     const DataMatrix* rows_ = nullptr;
-    std::unique_ptr<DataMatrix> owned_;
     std::vector<double> u_, h_;
 };
 

@@ -57,6 +57,8 @@ extern "C" {
 #define TSOM_OPT_TIE_TAU 2         /* value*2^-30: relative tie window for the exact re-check */
 #define TSOM_OPT_STREAM_CHUNK 3    /* rows per streamed chunk */
 #define TSOM_OPT_DETERMINISTIC 4   /* reserved */
+#define TSOM_OPT_HOST_REGISTER 5   /* streamed host rows: 1 (default) page-lock the caller's
+                                      buffer for direct DMA, 0 copy through pinned staging */
 
 typedef struct tsom_engine tsom_engine;
 
@@ -78,6 +80,17 @@ int tsom_set_option(tsom_engine* eng, int key, int64_t value);
  * host memory every epoch (the caller keeps `rows` alive until rebind/destroy).
  * Replaces the executor's DataSourceRef (trainer.hpp:442, parallel.hpp:101). */
 int tsom_bind_host_data(tsom_engine* eng, const float* rows, uint64_t n_rows, uint32_t flags);
+/* Bind FSOMSHRD shard files (dataset.hpp:171-344: 24-byte header "FSOMSHRD",
+ * u32 version 1, u64 rows, u32 cols, then row-major f32), rows in the order of
+ * `paths` (open_shards sorts part-*.shard by name, :277-301).  TSOM_BIND_COPY
+ * reads them once into HBM; TSOM_BIND_STREAMED keeps them on disk and every
+ * epoch preads chunks into pinned staging, overlapped with the GPU work of the
+ * previous chunk (the out-of-core path; replaces ChunkReader :305-344 and the
+ * per-chunk rescans of DataSourceRef::fetch_rows :400-415).  Header errors keep
+ * the reference's messages ("not a shard file (bad magic): ...", "truncated or
+ * corrupt shard: ...", "shard column count mismatch in ..."). */
+int tsom_bind_shards(tsom_engine* eng, const char* const* paths, uint32_t n_paths,
+                     uint32_t flags);
 /* Bind rows that already live in this device's memory (borrowed). */
 int tsom_bind_device_data(tsom_engine* eng, const float* d_rows, uint64_t n_rows);
 /* Fill the bound dataset with the SURVEY.md §8(d) Gaussian mixture generated

@@ -28,6 +28,7 @@ TSOM_BIND_STREAMED = 1
 TSOM_OPT_BMU_KERNEL = 1
 TSOM_OPT_TIE_TAU = 2
 TSOM_OPT_STREAM_CHUNK = 3
+TSOM_OPT_HOST_REGISTER = 5
 
 # Every symbol include/tsom_b200.h declares (checked by tests/test_abi.py).
 EXPORTS = [
@@ -37,7 +38,7 @@ EXPORTS = [
     "tsom_bmu_bound", "tsom_qe", "tsom_set_topology_distance", "tsom_train_epoch",
     "tsom_last_recheck_count", "tsom_comm_unique_id", "tsom_comm_init", "tsom_last_timing",
     "tsom_stream", "tsom_last_timing_detail", "tsom_kernel_launches", "tsom_refresh_topology",
-    "tsom_pairwise_sq_dists",
+    "tsom_pairwise_sq_dists", "tsom_bind_shards",
 ]
 
 
@@ -110,6 +111,7 @@ def load():
     L.tsom_kernel_launches.restype = u64
     L.tsom_refresh_topology.argtypes = [_vp, i32, _vp, u64, C.POINTER(u64), _vp]
     L.tsom_pairwise_sq_dists.argtypes = [_vp, _vp]
+    L.tsom_bind_shards.argtypes = [_vp, C.POINTER(C.c_char_p), u32, u32]
     L.tsom_stream.argtypes = [_vp]
     L.tsom_stream.restype = _vp
     for name in EXPORTS:
@@ -174,6 +176,12 @@ class Engine:
         flags = TSOM_BIND_STREAMED if streamed else TSOM_BIND_COPY
         self._keep = rows if streamed else None
         self._check(self.L.tsom_bind_host_data(self.h, _ptr(rows), rows.shape[0], flags))
+
+    def bind_shards(self, paths, streamed: bool = True):
+        """FSOMSHRD files (dataset.hpp:171-344), rows in the given order."""
+        arr = (C.c_char_p * len(paths))(*[os.fsencode(p) for p in paths])
+        flags = TSOM_BIND_STREAMED if streamed else TSOM_BIND_COPY
+        self._check(self.L.tsom_bind_shards(self.h, arr, len(paths), flags))
 
     def bind_device(self, ptr: int, n_rows: int):
         self._check(self.L.tsom_bind_device_data(self.h, ptr, n_rows))

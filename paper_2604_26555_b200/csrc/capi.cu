@@ -6,6 +6,8 @@
 // fallback: if a kernel cannot run, the call fails with TSOM_ERR_CUDA.
 #include <cuda_runtime.h>
 #include <dlfcn.h>
+#include <fcntl.h>
+#include <unistd.h>
 #include <nccl.h>
 
 #include <algorithm>
@@ -245,6 +247,65 @@ const uint32_t* normalise_selection(Engine* eng, const uint32_t* sel, uint64_t n
     return sel;
 }
 
+// Host side of one streamed chunk [r0, r1): returns a host pointer the copy
+// engine can DMA from.  Registered caller memory is used in place; shard files
+// (pread) and pageable caller memory go through the two pinned staging
+// buffers, reusing slot s only after its previous H2D has completed.
+void close_shards(Engine* eng) {
+    for (auto& f : eng->shards)
+        if (f.fd >= 0) ::close(f.fd);
+    eng->shards.clear();
+}
+
+void ensure_pinned(Engine* eng, uint64_t rows) {
+    if (eng->pinned_rows >= rows && eng->pinned[0]) return;
+    for (int s = 0; s < 2; ++s) {
+        if (eng->pin_busy[s]) CU(cudaEventSynchronize(eng->ev_pin[s]));
+        if (eng->pinned[s]) cudaFreeHost(eng->pinned[s]);
+        eng->pinned[s] = nullptr;
+        CU(cudaMallocHost(&eng->pinned[s], rows * eng->D * sizeof(float)));
+        if (!eng->ev_pin[s]) CU(cudaEventCreateWithFlags(&eng->ev_pin[s], cudaEventDisableTiming));
+        eng->pin_busy[s] = false;
+    }
+    eng->pinned_rows = rows;
+}
+
+void read_shard_rows(Engine* eng, uint64_t r0, uint64_t r1, float* dst) {
+    const size_t rowb = (size_t)eng->D * sizeof(float);
+    for (const auto& f : eng->shards) {
+        const uint64_t a = std::max(r0, f.row0), b = std::min(r1, f.row0 + f.rows);
+        if (a >= b) continue;
+        char* out = reinterpret_cast<char*>(dst + (a - r0) * eng->D);
+        size_t left = (b - a) * rowb;
+        off_t off = (off_t)(24 + (a - f.row0) * rowb);
+        while (left) {
+            const ssize_t got = ::pread(f.fd, out, left, off);
+            REQUIRE(got > 0, TSOM_ERR_NUMERICAL, "shard read failed: " + f.path);
+            out += got;
+            off += got;
+            left -= (size_t)got;
+        }
+    }
+}
+
+const float* host_chunk_source(Engine* eng, uint64_t r0, uint64_t r1, int s) {
+    if (eng->shards.empty() && eng->host_registered) return eng->host_rows + r0 * eng->D;
+    ensure_pinned(eng, eng->stream_chunk_rows);
+    if (eng->pin_busy[s]) CU(cudaEventSynchronize(eng->ev_pin[s]));
+    if (!eng->shards.empty())
+        read_shard_rows(eng, r0, r1, eng->pinned[s]);
+    else
+        std::memcpy(eng->pinned[s], eng->host_rows + r0 * eng->D,
+                    (r1 - r0) * eng->D * sizeof(float));
+    return eng->pinned[s];
+}
+
+void note_pinned_copy(Engine* eng, int s) {
+    if (eng->shards.empty() && eng->host_registered) return;
+    CU(cudaEventRecord(eng->ev_pin[s], eng->copy_stream));
+    eng->pin_busy[s] = true;
+}
+
 // K2 scratch (counting sort + piece partials) sized for `rows` rows per launch.
 void ensure_accum(Engine* eng, uint64_t rows) {
     if (rows <= eng->acc_rows && eng->acc.counts) return;
@@ -334,10 +395,12 @@ void accumulate_epoch(Engine* eng, const uint32_t* sel_host, uint64_t n_sel, boo
                 if (p1 == p0) continue;  // nothing selected in this chunk
             }
             const int s = (int)(issued & 1);
+            // host read of this chunk overlaps the GPU work already queued
+            const float* src = host_chunk_source(eng, r0, r1, s);
             if (issued >= 2) CU(cudaStreamWaitEvent(eng->copy_stream, eng->ev[4 + s], 0));
-            CU(cudaMemcpyAsync(eng->stage[s].p, eng->host_rows + r0 * eng->D,
-                               (r1 - r0) * eng->D * sizeof(float), cudaMemcpyHostToDevice,
-                               eng->copy_stream));
+            CU(cudaMemcpyAsync(eng->stage[s].p, src, (r1 - r0) * eng->D * sizeof(float),
+                               cudaMemcpyHostToDevice, eng->copy_stream));
+            note_pinned_copy(eng, s);
             CU(cudaEventRecord(eng->ev[2 + s], eng->copy_stream));
             CU(cudaStreamWaitEvent(eng->stream, eng->ev[2 + s], 0));
             ++issued;
@@ -478,6 +541,11 @@ int tsom_destroy(tsom_engine* eng) {
     if (eng->stream) cudaStreamSynchronize(eng->stream);
     if (eng->nccl_comm && g_nccl.commDestroy) g_nccl.commDestroy((ncclComm_t)eng->nccl_comm);
     if (eng->host_registered) cudaHostUnregister(const_cast<float*>(eng->host_rows));
+    close_shards(eng);
+    for (int s2 = 0; s2 < 2; ++s2) {
+        if (eng->pinned[s2]) cudaFreeHost(eng->pinned[s2]);
+        if (eng->ev_pin[s2]) cudaEventDestroy(eng->ev_pin[s2]);
+    }
     for (DevBuf* b : {&eng->x, &eng->xsplit, &eng->xn2, &eng->gxn2, &eng->txn2, &eng->x2max, &eng->w, &eng->wt, &eng->wsplit, &eng->w2,
                       &eng->w2max, &eng->prev, &eng->infl, &eng->topo_dist, &eng->sel,
                       &eng->rows_scratch, &eng->gsplit, &eng->bmu, &eng->dist, &eng->part,
@@ -519,6 +587,9 @@ int tsom_set_option(tsom_engine* eng, int key, int64_t value) {
                 REQUIRE(value >= 128, TSOM_ERR_INVALID, "option: stream chunk >= 128 rows");
                 eng->stream_chunk_rows = (uint64_t)value;
                 break;
+            case TSOM_OPT_HOST_REGISTER:
+                eng->host_register = value != 0;
+                break;
             default:
                 REQUIRE(false, TSOM_ERR_INVALID, "option: unknown key");
         }
@@ -534,6 +605,7 @@ int tsom_bind_host_data(tsom_engine* eng, const float* rows, uint64_t n_rows, ui
             cudaHostUnregister(const_cast<float*>(eng->host_rows));
             eng->host_registered = false;
         }
+        close_shards(eng);
         eng->xsplit_valid = false;
         eng->n_rows = n_rows;
         if (flags & TSOM_BIND_STREAMED) {
@@ -541,7 +613,7 @@ int tsom_bind_host_data(tsom_engine* eng, const float* rows, uint64_t n_rows, ui
             eng->host_rows = rows;
             eng->x.release();
             // pin in place for async DMA; pageable memory still works (slower)
-            if (n_rows && cudaHostRegister(const_cast<float*>(rows), n_rows * eng->D * sizeof(float),
+            if (n_rows && eng->host_register && cudaHostRegister(const_cast<float*>(rows), n_rows * eng->D * sizeof(float),
                                            cudaHostRegisterReadOnly) == cudaSuccess)
                 eng->host_registered = true;
             else
@@ -555,6 +627,79 @@ int tsom_bind_host_data(tsom_engine* eng, const float* rows, uint64_t n_rows, ui
         eng->x_slack = true;
         if (bytes) CU(cudaMemcpy(eng->x.p, rows, bytes, cudaMemcpyHostToDevice));
         tsom::launch_row_norm_max(eng->x.as<float>(), n_rows, eng->D, eng->x2max.as<float>(),
+                                  eng->stream);
+        CU(cudaGetLastError());
+        CU(cudaStreamSynchronize(eng->stream));
+    });
+}
+
+int tsom_bind_shards(tsom_engine* eng, const char* const* paths, uint32_t n_paths,
+                     uint32_t flags) {
+    return guarded(eng, [&] {
+        CU(cudaSetDevice(eng->device));
+        REQUIRE(paths && n_paths >= 1, TSOM_ERR_INVALID, "no .shard files given");
+        if (eng->host_registered) {
+            cudaHostUnregister(const_cast<float*>(eng->host_rows));
+            eng->host_registered = false;
+        }
+        close_shards(eng);
+        eng->host_rows = nullptr;
+        uint64_t total = 0;
+        for (uint32_t i = 0; i < n_paths; ++i) {
+            Engine::ShardFile f;
+            f.path = paths[i];
+            f.fd = ::open(paths[i], O_RDONLY);
+            if (f.fd < 0) {
+                close_shards(eng);
+                REQUIRE(false, TSOM_ERR_NUMERICAL, "cannot open shard: " + f.path);
+            }
+            eng->shards.push_back(f);
+            // FSOMSHRD header (dataset.hpp:171-183, read_shard_header :221-233)
+            unsigned char h[24] = {0};
+            const ssize_t got = ::pread(f.fd, h, 24, 0);
+            REQUIRE(got >= 8 && std::memcmp(h, "FSOMSHRD", 8) == 0, TSOM_ERR_NUMERICAL,
+                    "not a shard file (bad magic): " + f.path);
+            uint32_t ver, cols;
+            uint64_t rows;
+            std::memcpy(&ver, h + 8, 4);
+            std::memcpy(&rows, h + 12, 8);
+            std::memcpy(&cols, h + 20, 4);
+            REQUIRE(got < 12 || ver == 1, TSOM_ERR_NUMERICAL,
+                    "unsupported shard version " + std::to_string(ver) + " in " + f.path);
+            REQUIRE(got == 24, TSOM_ERR_NUMERICAL, "truncated shard header: " + f.path);
+            REQUIRE(cols == eng->D, TSOM_ERR_NUMERICAL, "shard column count mismatch in " + f.path);
+            const off_t want = (off_t)(24 + rows * cols * sizeof(float));
+            REQUIRE(::lseek(f.fd, 0, SEEK_END) == want, TSOM_ERR_NUMERICAL,
+                    "truncated or corrupt shard: " + f.path);
+            eng->shards.back().row0 = total;
+            eng->shards.back().rows = rows;
+            total += rows;
+        }
+        REQUIRE(total < (1ull << 32), TSOM_ERR_INVALID, "bind: row ids are uint32 (n < 2^32)");
+        eng->n_rows = total;
+        eng->xsplit_valid = false;
+        if (flags & TSOM_BIND_STREAMED) {
+            eng->streamed = true;
+            eng->x.release();
+            return;
+        }
+        // resident: stream the files once into HBM through the pinned staging
+        eng->streamed = false;
+        CU(eng->x.ensure(total * eng->D * sizeof(float) + tsom::kRowSlack));
+        eng->x_slack = true;
+        const uint64_t C = eng->stream_chunk_rows;
+        for (uint64_t r0 = 0, c = 0; r0 < total; r0 += C, ++c) {
+            const uint64_t r1 = std::min(total, r0 + C);
+            const int s = (int)(c & 1);
+            const float* src = host_chunk_source(eng, r0, r1, s);
+            CU(cudaMemcpyAsync(eng->x.as<float>() + r0 * eng->D, src,
+                               (r1 - r0) * eng->D * sizeof(float), cudaMemcpyHostToDevice,
+                               eng->copy_stream));
+            note_pinned_copy(eng, s);
+        }
+        CU(cudaStreamSynchronize(eng->copy_stream));
+        close_shards(eng);
+        tsom::launch_row_norm_max(eng->x.as<float>(), total, eng->D, eng->x2max.as<float>(),
                                   eng->stream);
         CU(cudaGetLastError());
         CU(cudaStreamSynchronize(eng->stream));

@@ -70,10 +70,7 @@ const char* tsom_dropin_last_error() { return g_err.c_str(); }
 std::size_t tsom_dropin_config_sizeof() { return sizeof(dropin_config); }
 
 // flags: bit0 streamed, bits1-2 bmu kernel (0 auto, 1 simt, 2 tc), bit3 force distances
-int tsom_dropin_train(const dropin_config* rc, const float* data, std::size_t n, std::size_t d,
-                      float* weights_out, double* qe_log, std::uint8_t* refresh_log, int device,
-                      unsigned flags, double* seconds_out) {
-    return guarded([&] {
+static SomConfig make_config(const dropin_config* rc) {
         SomConfig c;
         const auto kind = static_cast<TopologyKind>(rc->topology);
         c.topology = is_lattice(kind) ? TopologySpec::lattice(kind, rc->grid_w, rc->grid_h)
@@ -94,13 +91,23 @@ int tsom_dropin_train(const dropin_config* rc, const float* data, std::size_t n,
         c.refresh.max_interval = rc->refresh_max_interval;
         c.n_chunks = rc->n_chunks;
         c.seed = rc->seed;
+        return c;
+}
+
+static Sampler make_sampler(const dropin_config* rc, std::size_t n, std::uint64_t seed) {
         SamplingBudget b;
         b.mode = rc->budget_fixed ? BudgetMode::fixed : BudgetMode::proportional;
         b.m0 = rc->m0;
         b.rho = rc->rho;
-        Sampler sampler(static_cast<SamplingKind>(rc->sampling), b, n, c.seed, rc->alpha, rc->beta);
-        // DataMatrix over the caller's rows (one host copy, as DataSourceRef needs a matrix)
-        DataMatrix mat(n, d, std::vector<float>(data, data + n * d));
+        return Sampler(static_cast<SamplingKind>(rc->sampling), b, n, seed, rc->alpha, rc->beta);
+}
+
+// train_with_executor + CudaExecutor over any DataSourceRef (in-memory or ShardSet)
+static void run_train(const dropin_config* rc, const DataSourceRef& src, float* weights_out,
+                      double* qe_log, std::uint8_t* refresh_log, int device, unsigned flags,
+                      double* seconds_out) {
+        SomConfig c = make_config(rc);
+        Sampler sampler = make_sampler(rc, src.rows(), c.seed);
         toposom_b200::CudaOptions opts;
         opts.device = device;
         opts.streamed = (flags & 1u) != 0;
@@ -111,10 +118,10 @@ int tsom_dropin_train(const dropin_config* rc, const float* data, std::size_t n,
         std::pair<SomModel, RunLog> result;
         if (flags & 8u) {
             opts.distances = toposom_b200::Distances::always;
-            toposom_b200::CudaExecutor ex(mat, c.nodes(), opts);
-            result = train_with_executor(c, mat, sampler, ex, to);
+            toposom_b200::CudaExecutor ex(src, c.nodes(), opts);
+            result = train_with_executor(c, src, sampler, ex, to);
         } else {
-            result = toposom_b200::train_cuda(c, mat, sampler, opts, to);
+            result = toposom_b200::train_cuda(c, src, sampler, opts, to);
         }
         const std::chrono::duration<double> dt = std::chrono::steady_clock::now() - t0;
         if (seconds_out) *seconds_out = dt.count();
@@ -124,6 +131,35 @@ int tsom_dropin_train(const dropin_config* rc, const float* data, std::size_t n,
             if (qe_log) qe_log[t] = *result.second.iterations[t].qe_train;
             if (refresh_log) refresh_log[t] = result.second.iterations[t].refreshed ? 1 : 0;
         }
+}
+
+int tsom_dropin_train(const dropin_config* rc, const float* data, std::size_t n, std::size_t d,
+                      float* weights_out, double* qe_log, std::uint8_t* refresh_log, int device,
+                      unsigned flags, double* seconds_out) {
+    return guarded([&] {
+        // DataMatrix over the caller's rows (one host copy, as DataSourceRef needs a matrix)
+        DataMatrix mat(n, d, std::vector<float>(data, data + n * d));
+        run_train(rc, mat, weights_out, qe_log, refresh_log, device, flags, seconds_out);
+    });
+}
+
+// Same loop over a directory of part-*.shard files (open_shards, dataset.hpp:277-302)
+int tsom_dropin_train_shards(const dropin_config* rc, const char* shard_dir, std::size_t chunk_rows,
+                             float* weights_out, double* qe_log, std::uint8_t* refresh_log,
+                             int device, unsigned flags, double* seconds_out) {
+    return guarded([&] {
+        ShardSet set = open_shards(shard_dir, chunk_rows);
+        DataSourceRef src(set);
+        run_train(rc, src, weights_out, qe_log, refresh_log, device, flags, seconds_out);
+    });
+}
+
+// write_shards (dataset.hpp:252-275), for tests and benches that need shard files
+int tsom_dropin_write_shards(const float* data, std::size_t n, std::size_t d, const char* out_dir,
+                             std::size_t n_shards) {
+    return guarded([&] {
+        DataMatrix mat(n, d, std::vector<float>(data, data + n * d));
+        write_shards(mat, out_dir, n_shards, 4096);
     });
 }
 

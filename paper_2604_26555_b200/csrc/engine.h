@@ -151,7 +151,17 @@ struct Engine {
     DevBuf smooth_scratch;   // saug + split-b GEMM partials
     DevBuf status;         // device error word(s)
     DevBuf stage[2];       // streamed-mode device chunks
-    float* pinned[2] = {nullptr, nullptr};
+    float* pinned[2] = {nullptr, nullptr};  // host staging for shard / pageable sources
+    size_t pinned_rows = 0;
+    cudaEvent_t ev_pin[2] = {nullptr, nullptr};  // H2D from pinned[s] finished
+    bool pin_busy[2] = {false, false};
+    bool host_register = true;  // TSOM_OPT_HOST_REGISTER
+    struct ShardFile {
+        std::string path;
+        int fd = -1;
+        uint64_t row0 = 0, rows = 0;
+    };
+    std::vector<ShardFile> shards;  // FSOMSHRD files (dataset.hpp:171-344)
     cudaEvent_t ev[12] = {};  // 0 start, 1 bmu end, 6 accum end, 7 smooth end, 8/9 K1 kernel, 10 update end
     uint64_t last_recheck = 0;
     std::vector<uint32_t> chunk_counts;  // per-chunk re-check counts (async D2H targets)

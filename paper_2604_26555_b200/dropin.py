@@ -98,6 +98,11 @@ def load():
                                         C.POINTER(C.c_double)]
         L.tsom_dropin_find_bmus.argtypes = [C.c_void_p, C.c_size_t, C.c_void_p, C.c_size_t,
                                             C.c_size_t, C.c_void_p, C.c_void_p, C.c_int]
+        L.tsom_dropin_train_shards.argtypes = [C.POINTER(_Cfg), C.c_char_p, C.c_size_t,
+                                               C.c_void_p, C.c_void_p, C.c_void_p, C.c_int,
+                                               C.c_uint, C.POINTER(C.c_double)]
+        L.tsom_dropin_write_shards.argtypes = [C.c_void_p, C.c_size_t, C.c_size_t, C.c_char_p,
+                                               C.c_size_t]
         _dl = L
     return _dl
 
@@ -123,3 +128,31 @@ def train_cuda(cfg, data: np.ndarray, device: int = 0, log_qe: bool = False,
     if st:
         _lib._raise(st, L.tsom_dropin_last_error().decode())
     return w, qe, ref, secs.value
+
+
+def train_cuda_shards(cfg, shard_dir: str, d: int, device: int = 0, log_qe: bool = False,
+                      streamed: bool = True, bmu_kernel: int = 0, chunk_rows: int = 65536):
+    """Reference train_with_executor over open_shards(shard_dir) (dataset.hpp:277-302)
+    with the CudaExecutor reading the shard files itself."""
+    L = load()
+    w = np.empty((cfg.nodes, d), np.float32)
+    qe = np.zeros(cfg.n_iters) if log_qe else None
+    ref = np.zeros(cfg.n_iters, np.uint8)
+    secs = C.c_double()
+    flags = (1 if streamed else 0) | ((bmu_kernel & 3) << 1)
+    st = L.tsom_dropin_train_shards(C.byref(_cfg(cfg)), os.fsencode(shard_dir), chunk_rows,
+                                    w.ctypes.data, qe.ctypes.data if log_qe else None,
+                                    ref.ctypes.data, device, flags, C.byref(secs))
+    if st:
+        _lib._raise(st, L.tsom_dropin_last_error().decode())
+    return w, qe, ref, secs.value
+
+
+def write_shards(data: np.ndarray, out_dir: str, n_shards: int):
+    """The reference's own write_shards (dataset.hpp:252-275)."""
+    L = load()
+    data = np.ascontiguousarray(data, np.float32)
+    st = L.tsom_dropin_write_shards(data.ctypes.data, data.shape[0], data.shape[1],
+                                    os.fsencode(out_dir), n_shards)
+    if st:
+        _lib._raise(st, L.tsom_dropin_last_error().decode())

@@ -316,3 +316,27 @@ def test_full_size_properties(pkg, oracle_port):
     assert counts.sum() == n
     np.testing.assert_allclose(h, infl.T @ counts, rtol=1e-12)
     np.testing.assert_allclose(h.sum(), (infl.sum(1) * counts).sum(), rtol=1e-12)
+
+
+def test_nccl_world1_allreduce_path(pkg, oracle_port):
+    """The multi-GPU code path (dlopen NCCL, unique id, ncclCommInitRank, one
+    allreduce per epoch) on a world-size-1 communicator: results must equal the
+    communicator-free epoch."""
+    n, p = 20000, 256
+    x = oracle_port.synth_gmm(n, 50, 2670)
+    w = x[:p].copy()
+    infl = oracle_port.influence_from_dist(oracle_port.lattice_dist("hex", 16, 16), 3.0)
+    out = []
+    for comm in (False, True):
+        e = pkg.Engine(p, 50)
+        e.bind(x)
+        if comm:
+            e.comm_init(e.comm_unique_id(), 0, 1)
+        e.set_codebook(w)
+        e.set_influence(infl)
+        out.append(e.epoch(0.4))
+        e.set_topology_distance(oracle_port.lattice_dist("hex", 16, 16))
+        e.train_epoch(0.4, 3.0)
+        out.append((e.get_codebook(),))
+    assert (out[0][0] == out[2][0]).all() and (out[0][1] == out[2][1]).all()
+    assert (out[1][0] == out[3][0]).all()
