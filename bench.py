@@ -281,22 +281,26 @@ def run_gpu_arm(args):
             e.bind(host)
             e.set_codebook(w0)
             e.set_topology_distance(lattice_dist("hex", *P_GRID))
+            t1 = time.perf_counter()
             for t in range(epochs):
                 eta = schedule_value(0.5, "linear", t, epochs, 1e-4)
                 sigma = schedule_value(sigma0, "linear", t, epochs, 0.3)
                 e.train_epoch(eta, sigma)
             wf = e.get_codebook()
+            t2 = time.perf_counter()
             e.close()
-            return time.perf_counter() - t0, wf
+            t3 = time.perf_counter()
+            return t3 - t0, {"setup_s": t1 - t0, "epochs_s": t2 - t1, "close_s": t3 - t2}
         cabi_run(1)  # warm-up (allocations, module load)
-        secs, _ = cabi_run(EPOCHS)
+        secs, split = min((cabi_run(EPOCHS) for _ in range(3)), key=lambda r: r[0])
         h2d = n * D * 4 + P * D * 4 + P * P * 8
         d2h = P * D * 4
         e2e = {"value": n * EPOCHS / secs, "unit": UNIT,
                "h2d_bytes_per_step": int(h2d / EPOCHS), "d2h_bytes_per_step": int(d2h / EPOCHS),
                "path": "C-ABI tsom_bind_host_data + 10 x tsom_train_epoch + tsom_get_codebook "
                        "from pinned host rows, wall clock incl. engine creation",
-               "seconds_per_call": secs, "epochs_per_call": EPOCHS}
+               "seconds_per_call": secs, "epochs_per_call": EPOCHS, "best_of": 3,
+               "split_s": split}
         from paper_2604_26555_b200 import dropin
         if dropin.available():
             cfg = dropin.TrainConfig(topology="hex", grid_w=P_GRID[0], grid_h=P_GRID[1],

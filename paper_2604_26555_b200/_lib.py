@@ -29,6 +29,7 @@ TSOM_OPT_BMU_KERNEL = 1
 TSOM_OPT_TIE_TAU = 2
 TSOM_OPT_STREAM_CHUNK = 3
 TSOM_OPT_HOST_REGISTER = 5
+TSOM_OPT_STAGING_THREADS = 6
 
 # Every symbol include/tsom_b200.h declares (checked by tests/test_abi.py).
 EXPORTS = [

@@ -7,6 +7,7 @@
 #include <cuda_runtime.h>
 #include <dlfcn.h>
 #include <fcntl.h>
+#include <thread>
 #include <unistd.h>
 #include <nccl.h>
 
@@ -189,31 +190,28 @@ void run_bmu(Engine* eng, const float* x, const uint32_t* sel, uint64_t n, const
                                 eng->bmu.as<uint32_t>(), eng->ties.as<uint32_t>(),
                                 eng->tmask.as<uint32_t>(), eng->stream);
         CU(cudaGetLastError());
-        // near-tie rows (~1%): same tensor-core kernel in enumerate mode on just
-        // those rows, then exact FP64 over their few candidates
-        uint32_t nt = 0;
-        CU(cudaMemcpyAsync(&nt, eng->ties.p, sizeof(uint32_t), cudaMemcpyDeviceToHost, eng->stream));
-        CU(cudaStreamSynchronize(eng->stream));
-        const uint64_t chunk = 1ull << 20;
-        const uint32_t* tpos = eng->ties.as<uint32_t>() + 1;
-        for (uint64_t f0 = 0; f0 < nt; f0 += chunk) {
-            const uint64_t m = std::min<uint64_t>(chunk, nt - f0);
-            const uint64_t mt = (m + tsom::kTcTileM - 1) / tsom::kTcTileM;
-            CU(eng->tsplit.ensure(mt * tile_bytes));
-            CU(eng->part2.ensure((size_t)groups * 4 * m * sizeof(float)));
-            CU(eng->txn2.ensure(m * sizeof(float)));
-            tsom::launch_split_rows(x, sel, tpos + f0, m, eng->D, eng->tsplit.as<float>(),
-                                    eng->txn2.as<float>(), eng->stream);
-            CU(tsom::launch_bmu_tc(eng->tsplit.as<float>(), m, nullptr, true, eng->P,
-                                   eng->wsplit.as<float>(), eng->txn2.as<float>(), w2, tau,
-                                   eng->tmask.as<uint32_t>() + f0, eng->part2.as<float>(),
-                                   eng->sm_count, eng->stream));
-            tsom::launch_merge_partials(eng->part2.as<float>(), tpos + f0, m, groups, gn,
-                                        eng->txn2.as<float>(), w2, tau, x, sel,
-                                        eng->w.as<float>(), eng->D,
-                                        eng->bmu.as<uint32_t>(), eng->flags.as<uint32_t>(),
-                                        eng->stream);
-        }
+        // near-tie rows (~1-3%): same tensor-core kernel in enumerate mode on just
+        // those rows, then exact FP64 over their few candidates.  The list length
+        // stays on the device (kernels grid-stride over it), so the epoch needs
+        // no host round trip; rows beyond the enumerate capacity get the full
+        // exact re-scan.
+        const uint64_t cap = std::min<uint64_t>(n, std::max<uint64_t>(1ull << 20, n / 8));
+        const uint64_t mt = (cap + tsom::kTcTileM - 1) / tsom::kTcTileM;
+        CU(eng->tsplit.ensure(mt * tile_bytes));
+        CU(eng->part2.ensure((size_t)groups * 4 * cap * sizeof(float)));
+        CU(eng->txn2.ensure(cap * sizeof(float)));
+        const uint32_t* tcount = eng->ties.as<uint32_t>();
+        const uint32_t* tpos = tcount + 1;
+        tsom::launch_split_rows(x, sel, tpos, cap, eng->D, eng->tsplit.as<float>(),
+                                eng->txn2.as<float>(), eng->stream, tcount);
+        CU(tsom::launch_bmu_tc(eng->tsplit.as<float>(), cap, tcount, true, eng->P,
+                               eng->wsplit.as<float>(), eng->txn2.as<float>(), w2, tau,
+                               eng->tmask.as<uint32_t>(), eng->part2.as<float>(),
+                               eng->sm_count, eng->stream));
+        tsom::launch_merge_partials(eng->part2.as<float>(), tpos, tcount, cap, n, groups, gn,
+                                    eng->txn2.as<float>(), w2, tau, x, sel, eng->w.as<float>(),
+                                    eng->D, eng->bmu.as<uint32_t>(), eng->flags.as<uint32_t>(),
+                                    eng->stream);
     } else {
         CU(cudaEventRecord(eng->ev[8], eng->stream));
         // the FP32 accumulation bound grows with the d+1 terms of each dot product
@@ -270,7 +268,8 @@ void ensure_pinned(Engine* eng, uint64_t rows) {
     eng->pinned_rows = rows;
 }
 
-void read_shard_rows(Engine* eng, uint64_t r0, uint64_t r1, float* dst) {
+// returns "" or the failing shard's error message (called from staging threads)
+std::string read_shard_rows(const Engine* eng, uint64_t r0, uint64_t r1, float* dst) {
     const size_t rowb = (size_t)eng->D * sizeof(float);
     for (const auto& f : eng->shards) {
         const uint64_t a = std::max(r0, f.row0), b = std::min(r1, f.row0 + f.rows);
@@ -280,28 +279,50 @@ void read_shard_rows(Engine* eng, uint64_t r0, uint64_t r1, float* dst) {
         off_t off = (off_t)(24 + (a - f.row0) * rowb);
         while (left) {
             const ssize_t got = ::pread(f.fd, out, left, off);
-            REQUIRE(got > 0, TSOM_ERR_NUMERICAL, "shard read failed: " + f.path);
+            if (got <= 0) return "shard read failed: " + f.path;
             out += got;
             off += got;
             left -= (size_t)got;
         }
     }
+    return std::string();
 }
 
 const float* host_chunk_source(Engine* eng, uint64_t r0, uint64_t r1, int s) {
-    if (eng->shards.empty() && eng->host_registered) return eng->host_rows + r0 * eng->D;
+    if (eng->shards.empty() && eng->host_direct) return eng->host_rows + r0 * eng->D;
     ensure_pinned(eng, eng->stream_chunk_rows);
     if (eng->pin_busy[s]) CU(cudaEventSynchronize(eng->ev_pin[s]));
-    if (!eng->shards.empty())
-        read_shard_rows(eng, r0, r1, eng->pinned[s]);
-    else
-        std::memcpy(eng->pinned[s], eng->host_rows + r0 * eng->D,
-                    (r1 - r0) * eng->D * sizeof(float));
-    return eng->pinned[s];
+    float* dst = eng->pinned[s];
+    // one host thread streams ~10 GB/s; split the fill so staging keeps up
+    // with the PCIe copy engine
+    auto fill = [&](uint64_t a, uint64_t b) -> std::string {
+        if (!eng->shards.empty()) return read_shard_rows(eng, a, b, dst + (a - r0) * eng->D);
+        std::memcpy(dst + (a - r0) * eng->D, eng->host_rows + a * eng->D,
+                    (b - a) * eng->D * sizeof(float));
+        return std::string();
+    };
+    const uint64_t bytes = (r1 - r0) * eng->D * sizeof(float);
+    const uint32_t T = (uint32_t)std::min<uint64_t>(eng->staging_threads,
+                                                    std::max<uint64_t>(1, bytes >> 22));
+    if (T <= 1) {
+        const std::string e = fill(r0, r1);
+        REQUIRE(e.empty(), TSOM_ERR_NUMERICAL, e);
+    } else {
+        std::vector<std::thread> pool;
+        std::vector<std::string> errs(T);
+        const uint64_t per = (r1 - r0 + T - 1) / T;
+        for (uint32_t t = 0; t < T; ++t) {
+            const uint64_t a = std::min(r1, r0 + t * per), b = std::min(r1, a + per);
+            pool.emplace_back([&, a, b, t] { errs[t] = fill(a, b); });
+        }
+        for (auto& th : pool) th.join();
+        for (const auto& e : errs) REQUIRE(e.empty(), TSOM_ERR_NUMERICAL, e);
+    }
+    return dst;
 }
 
 void note_pinned_copy(Engine* eng, int s) {
-    if (eng->shards.empty() && eng->host_registered) return;
+    if (eng->shards.empty() && eng->host_direct) return;
     CU(cudaEventRecord(eng->ev_pin[s], eng->copy_stream));
     eng->pin_busy[s] = true;
 }
@@ -379,43 +400,54 @@ void accumulate_epoch(Engine* eng, const uint32_t* sel_host, uint64_t n_sel, boo
         CU(eng->stage[1].ensure(C * eng->D * sizeof(float) + tsom::kRowSlack));
         CU(eng->x2max.ensure(2 * sizeof(float)));
         ensure_accum(eng, C);
-        uint64_t pos0 = 0;  // selection cursor
-        bool first = true;
         const uint64_t nchunks = (eng->n_rows + C - 1) / C;
-        eng->chunk_counts.assign(2 * nchunks, 0u);
-        // events: ev[2+s] = stage s filled, ev[4+s] = stage s consumed.  No host
-        // sync inside the loop: the copy stream runs ahead into the free stage
-        // while the compute stream works on the other one.
-        uint64_t issued = 0;
-        for (uint64_t c = 0; c < nchunks; ++c) {
+        // chunk list (chunks holding no selected row are skipped)
+        struct Job { uint64_t c, r0, r1, p0, p1; };
+        std::vector<Job> jobs;
+        for (uint64_t c = 0, pos0 = 0; c < nchunks; ++c) {
             const uint64_t r0 = c * C, r1 = std::min(eng->n_rows, r0 + C);
-            uint64_t p0 = pos0, p1 = pos0;
+            uint64_t p1 = pos0;
             if (sel) {
-                p1 = (uint64_t)(std::lower_bound(sel + p0, sel + n, (uint32_t)r1) - sel);
-                if (p1 == p0) continue;  // nothing selected in this chunk
+                p1 = (uint64_t)(std::lower_bound(sel + pos0, sel + n, (uint32_t)r1) - sel);
+                if (p1 == pos0) continue;
             }
-            const int s = (int)(issued & 1);
-            // host read of this chunk overlaps the GPU work already queued
-            const float* src = host_chunk_source(eng, r0, r1, s);
-            if (issued >= 2) CU(cudaStreamWaitEvent(eng->copy_stream, eng->ev[4 + s], 0));
-            CU(cudaMemcpyAsync(eng->stage[s].p, src, (r1 - r0) * eng->D * sizeof(float),
+            jobs.push_back({c, r0, r1, pos0, p1});
+            pos0 = p1;
+        }
+        // events: ev[2+s] = stage s filled, ev[4+s] = stage s consumed.  Two
+        // chunks are in flight ahead of the compute stream: while chunk k is
+        // computed, chunk k+1 is on the copy engine and the host stages k+2.
+        auto issue = [&](size_t k) {
+            const Job& j = jobs[k];
+            const int s = (int)(k & 1);
+            const float* src = host_chunk_source(eng, j.r0, j.r1, s);
+            if (k >= 2) CU(cudaStreamWaitEvent(eng->copy_stream, eng->ev[4 + s], 0));
+            CU(cudaMemcpyAsync(eng->stage[s].p, src, (j.r1 - j.r0) * eng->D * sizeof(float),
                                cudaMemcpyHostToDevice, eng->copy_stream));
             note_pinned_copy(eng, s);
             CU(cudaEventRecord(eng->ev[2 + s], eng->copy_stream));
+        };
+        CU(eng->chunk_flags.ensure(std::max<size_t>(1, 2 * jobs.size()) * sizeof(uint32_t)));
+        for (size_t k = 0; k < std::min<size_t>(2, jobs.size()); ++k) issue(k);
+        bool first = true;
+        for (size_t k = 0; k < jobs.size(); ++k) {
+            const Job& j = jobs[k];
+            const int s = (int)(k & 1);
             CU(cudaStreamWaitEvent(eng->stream, eng->ev[2 + s], 0));
-            ++issued;
             const float* xs = eng->stage[s].as<float>();
             float* xmax = eng->x2max.as<float>() + 1;
-            tsom::launch_row_norm_max(xs, r1 - r0, eng->D, xmax, eng->stream);
+            tsom::launch_row_norm_max(xs, j.r1 - j.r0, eng->D, xmax, eng->stream);
             tsom::launch_fold_max(eng->x2max.as<float>(), eng->stream);
             // selected rows of this chunk are addressed as (row - r0): shift the base
-            const float* xbase = xs - (ptrdiff_t)(r0 * eng->D);
-            const uint64_t cn = sel ? (p1 - p0) : (r1 - r0);
-            const uint32_t* csel = sel ? dsel + p0 : nullptr;
-            const uint64_t out0 = sel ? p0 : r0;
+            const float* xbase = xs - (ptrdiff_t)(j.r0 * eng->D);
+            const uint64_t cn = sel ? (j.p1 - j.p0) : (j.r1 - j.r0);
+            const uint32_t* csel = sel ? dsel + j.p0 : nullptr;
+            const uint64_t out0 = sel ? j.p0 : j.r0;
             run_bmu(eng, sel ? xbase : xs, csel, cn, xmax, nullptr, nullptr);
-            CU(cudaMemcpyAsync(&eng->chunk_counts[2 * c], eng->flags.p, 2 * sizeof(uint32_t),
-                               cudaMemcpyDeviceToHost, eng->stream));
+            // re-check counters per chunk, kept on the device (a D2H into pageable
+            // memory here would block the host and stall the look-ahead)
+            CU(cudaMemcpyAsync(eng->chunk_flags.as<uint32_t>() + 2 * k, eng->flags.p,
+                               2 * sizeof(uint32_t), cudaMemcpyDeviceToDevice, eng->stream));
             tsom::launch_accumulate(sel ? xbase : xs, csel, cn, eng->D, eng->w.as<float>(), eng->P,
                                     eng->bmu.as<uint32_t>(),
                                     want_dist ? eng->dist.as<double>() + out0 : nullptr, want_dsum,
@@ -424,9 +456,14 @@ void accumulate_epoch(Engine* eng, const uint32_t* sel_host, uint64_t n_sel, boo
             CU(cudaGetLastError());
             CU(cudaEventRecord(eng->ev[4 + s], eng->stream));
             first = false;
-            pos0 = p1;
+            if (k + 2 < jobs.size()) issue(k + 2);
         }
         if (first) CU(cudaMemsetAsync(eng->sums.p, 0, slot_len(eng) * sizeof(double), eng->stream));
+        eng->chunk_counts.assign(std::max<size_t>(2, 2 * jobs.size()), 0u);
+        if (!jobs.empty())
+            CU(cudaMemcpyAsync(eng->chunk_counts.data(), eng->chunk_flags.p,
+                               2 * jobs.size() * sizeof(uint32_t), cudaMemcpyDeviceToHost,
+                               eng->stream));
         eng->recheck_from_chunks = true;
         CU(cudaEventRecord(eng->ev[1], eng->stream));
     }
@@ -550,7 +587,7 @@ int tsom_destroy(tsom_engine* eng) {
                       &eng->w2max, &eng->prev, &eng->infl, &eng->topo_dist, &eng->sel,
                       &eng->rows_scratch, &eng->gsplit, &eng->bmu, &eng->dist, &eng->part,
                       &eng->flags, &eng->ties, &eng->tmask, &eng->part2, &eng->tsplit, &eng->acc_buf[0], &eng->acc_buf[1], &eng->acc_buf[2], &eng->acc_buf[3],
-                      &eng->acc_buf[4], &eng->acc_buf[5], &eng->acc_buf[6], &eng->sums,
+                      &eng->acc_buf[4], &eng->acc_buf[5], &eng->acc_buf[6], &eng->sums, &eng->chunk_flags,
                       &eng->topo_buf[0], &eng->topo_buf[1], &eng->topo_buf[2], &eng->topo_buf[3],
                       &eng->topo_buf[4], &eng->topo_buf[5], &eng->topo_buf[6], &eng->topo_buf[7],
                       &eng->topo_buf[8], &eng->topo_buf[9], &eng->topo_buf[10], &eng->topo_buf[11],
@@ -590,6 +627,11 @@ int tsom_set_option(tsom_engine* eng, int key, int64_t value) {
             case TSOM_OPT_HOST_REGISTER:
                 eng->host_register = value != 0;
                 break;
+            case TSOM_OPT_STAGING_THREADS:
+                REQUIRE(value >= 1 && value <= 64, TSOM_ERR_INVALID,
+                        "option: staging threads in [1, 64]");
+                eng->staging_threads = (uint32_t)value;
+                break;
             default:
                 REQUIRE(false, TSOM_ERR_INVALID, "option: unknown key");
         }
@@ -605,6 +647,7 @@ int tsom_bind_host_data(tsom_engine* eng, const float* rows, uint64_t n_rows, ui
             cudaHostUnregister(const_cast<float*>(eng->host_rows));
             eng->host_registered = false;
         }
+        eng->host_direct = false;
         close_shards(eng);
         eng->xsplit_valid = false;
         eng->n_rows = n_rows;
@@ -612,12 +655,21 @@ int tsom_bind_host_data(tsom_engine* eng, const float* rows, uint64_t n_rows, ui
             eng->streamed = true;
             eng->host_rows = rows;
             eng->x.release();
-            // pin in place for async DMA; pageable memory still works (slower)
-            if (n_rows && eng->host_register && cudaHostRegister(const_cast<float*>(rows), n_rows * eng->D * sizeof(float),
-                                           cudaHostRegisterReadOnly) == cudaSuccess)
-                eng->host_registered = true;
-            else
+            // DMA straight from the caller's rows when they are page-locked
+            // already or can be pinned in place; otherwise pinned staging
+            cudaPointerAttributes pa{};
+            if (n_rows && cudaPointerGetAttributes(&pa, rows) == cudaSuccess &&
+                pa.type == cudaMemoryTypeHost) {
+                eng->host_direct = true;
+            } else {
                 cudaGetLastError();
+                if (n_rows && eng->host_register &&
+                    cudaHostRegister(const_cast<float*>(rows), n_rows * eng->D * sizeof(float),
+                                     cudaHostRegisterReadOnly) == cudaSuccess)
+                    eng->host_registered = eng->host_direct = true;
+                else
+                    cudaGetLastError();
+            }
             return;
         }
         eng->streamed = false;
@@ -642,6 +694,7 @@ int tsom_bind_shards(tsom_engine* eng, const char* const* paths, uint32_t n_path
             cudaHostUnregister(const_cast<float*>(eng->host_rows));
             eng->host_registered = false;
         }
+        eng->host_direct = false;
         close_shards(eng);
         eng->host_rows = nullptr;
         uint64_t total = 0;

@@ -151,11 +151,14 @@ struct Engine {
     DevBuf smooth_scratch;   // saug + split-b GEMM partials
     DevBuf status;         // device error word(s)
     DevBuf stage[2];       // streamed-mode device chunks
+    DevBuf chunk_flags;    // streamed mode: re-check counters per chunk
     float* pinned[2] = {nullptr, nullptr};  // host staging for shard / pageable sources
     size_t pinned_rows = 0;
     cudaEvent_t ev_pin[2] = {nullptr, nullptr};  // H2D from pinned[s] finished
     bool pin_busy[2] = {false, false};
     bool host_register = true;  // TSOM_OPT_HOST_REGISTER
+    bool host_direct = false;   // streamed host rows are DMA-able (pinned)
+    uint32_t staging_threads = 8;  // TSOM_OPT_STAGING_THREADS
     struct ShardFile {
         std::string path;
         int fd = -1;
@@ -189,7 +192,8 @@ void launch_fold_max(float* a, cudaStream_t st);
 // split rows (optionally gathered through sel, and/or through a position list
 // idx: split row f = position idx[f]) into tcgen05 tiles
 void launch_split_rows(const float* x, const uint32_t* sel, const uint32_t* idx, uint64_t n,
-                       uint32_t D, float* tiles, float* xn2, cudaStream_t st);
+                       uint32_t D, float* tiles, float* xn2, cudaStream_t st,
+                       const uint32_t* dev_n = nullptr);
 bool tc_supported(uint32_t P, uint32_t D);
 // nodes per CTA-resident codebook group (multiple of 16, <= 256)
 __host__ __device__ inline uint32_t tc_group_width(uint32_t P) {
@@ -212,10 +216,13 @@ void launch_merge_fast(const float* part, uint64_t n, uint32_t groups, uint32_t 
                        uint32_t* ties, uint32_t* tmask, cudaStream_t st);
 // enumerate-pass merge over the near-tie rows: candidates -> exact FP64 -> bmu;
 // overflow -> flags list for the full re-scan.
-void launch_merge_partials(const float* part, const uint32_t* ties, uint64_t n, uint32_t groups,
-                           uint32_t gn, const float* xn2, const float* w2max, float tau,
-                           const float* x, const uint32_t* sel, const float* w, uint32_t D,
-                           uint32_t* bmu, uint32_t* flags, cudaStream_t st);
+// ties: near-tie positions, dev_count: their number (device); rows past `cap`
+// are sent to the full re-scan; n_max bounds the count (grid sizing)
+void launch_merge_partials(const float* part, const uint32_t* ties, const uint32_t* dev_count,
+                           uint64_t cap, uint64_t n_max, uint32_t groups, uint32_t gn,
+                           const float* xn2, const float* w2max, float tau, const float* x,
+                           const uint32_t* sel, const float* w, uint32_t D, uint32_t* bmu,
+                           uint32_t* flags, cudaStream_t st);
 // exact FP64 re-scan of flagged rows (reference loop order)
 void launch_rescan(const float* x, const uint32_t* sel, const float* w, uint32_t P, uint32_t D,
                    const uint32_t* flags, uint64_t n, uint32_t* bmu, cudaStream_t st);

@@ -184,7 +184,7 @@ __global__ void __launch_bounds__(kThreads, 1)
               const float* __restrict__ xn2, const float* __restrict__ w2max, float tau,
               const uint32_t* __restrict__ rmask, float* __restrict__ part) {
     extern __shared__ __align__(1024) uint8_t smem[];
-    const uint64_t n = dev_n ? (uint64_t)*dev_n : n_host;
+    const uint64_t n = dev_n ? min((uint64_t)*dev_n, n_host) : n_host;  // n_host caps dev_n
     const uint32_t ntiles = (uint32_t)((n + kTcTileM - 1) / kTcTileM);
     const uint32_t w_bytes = 2u * kTcKPad * gn * 4u;  // hi + lo of this CTA's group
     uint8_t* sW = smem;

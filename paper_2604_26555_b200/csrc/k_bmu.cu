@@ -346,15 +346,25 @@ void launch_merge_fast(const float* part, uint64_t n, uint32_t groups, uint32_t 
 // ascending node order with strict < (lowest index wins), as find_bmus
 // (trainer.hpp:293-304); > 8 candidates in a group -> full exact re-scan list.
 __global__ void k_merge_partials(const float* __restrict__ part, const uint32_t* __restrict__ ties,
-                                 uint64_t n, uint32_t groups, uint32_t gn,
+                                 const uint32_t* __restrict__ dev_count, uint64_t cap,
+                                 uint32_t groups, uint32_t gn,
                                  const float* __restrict__ xn2, const float* __restrict__ w2max,
                                  float tau, const float* __restrict__ x,
                                  const uint32_t* __restrict__ sel, const float* __restrict__ w,
                                  uint32_t D, uint32_t* __restrict__ bmu,
                                  uint32_t* __restrict__ flags) {
-    for (uint64_t f = blockIdx.x * (uint64_t)blockDim.x + threadIdx.x; f < n;
+    // the near-tie list length is read on the device (no host round trip);
+    // rows past the enumerate capacity fall back to the full exact re-scan
+    const uint64_t count = *dev_count;
+    const uint64_t n = count < cap ? count : cap;
+    for (uint64_t f = blockIdx.x * (uint64_t)blockDim.x + threadIdx.x; f < count;
          f += (uint64_t)gridDim.x * blockDim.x) {
         const uint32_t pos = ties[f];
+        if (f >= cap) {
+            const uint32_t slot = atomicAdd(&flags[0], 1u);
+            flags[2 + slot] = pos;
+            continue;
+        }
         const float thr = tau * (__ldg(xn2 + f) + __ldg(w2max));
         float B1 = CUDART_INF_F;
         for (uint32_t g = 0; g < groups; ++g) B1 = fminf(B1, part[(size_t)g * 4 * n + f]);
@@ -402,13 +412,17 @@ __global__ void k_merge_partials(const float* __restrict__ part, const uint32_t*
     }
 }
 
-void launch_merge_partials(const float* part, const uint32_t* ties, uint64_t n, uint32_t groups,
-                           uint32_t gn, const float* xn2, const float* w2max, float tau,
-                           const float* x, const uint32_t* sel, const float* w, uint32_t D,
-                           uint32_t* bmu, uint32_t* flags, cudaStream_t st) {
-    if (n == 0) return;
-    TSOM_LAUNCH(k_merge_partials<<<(unsigned)((n + 255) / 256), 256, 0, st>>>(
-        part, ties, n, groups, gn, xn2, w2max, tau, x, sel, w, D, bmu, flags));
+void launch_merge_partials(const float* part, const uint32_t* ties, const uint32_t* dev_count,
+                           uint64_t cap, uint64_t n_max, uint32_t groups, uint32_t gn,
+                           const float* xn2, const float* w2max, float tau, const float* x,
+                           const uint32_t* sel, const float* w, uint32_t D, uint32_t* bmu,
+                           uint32_t* flags, cudaStream_t st) {
+    if (n_max == 0) return;
+    // grid-strides over the device count; sized for the enumerate capacity
+    uint64_t blocks = (std::min(cap, n_max) + 255) / 256;
+    blocks = std::max<uint64_t>(1, std::min<uint64_t>(blocks, 148ull * 16));
+    TSOM_LAUNCH(k_merge_partials<<<(unsigned)blocks, 256, 0, st>>>(
+        part, ties, dev_count, cap, groups, gn, xn2, w2max, tau, x, sel, w, D, bmu, flags));
 }
 
 // ---------------------------------------------------------------------------
@@ -474,9 +488,12 @@ void launch_rescan(const float* x, const uint32_t* sel, const float* w, uint32_t
 // pieces), else 0.  Rows past n are zero (their results are ignored).
 
 __global__ void k_split_rows(const float* __restrict__ x, const uint32_t* __restrict__ sel,
-                             const uint32_t* __restrict__ idx, uint64_t n, uint32_t D,
-                             float* __restrict__ tiles, float* __restrict__ xn2) {
+                             const uint32_t* __restrict__ idx, const uint32_t* __restrict__ dev_n,
+                             uint64_t n_host, uint32_t D, float* __restrict__ tiles,
+                             float* __restrict__ xn2) {
     // idx (optional): positions; split row f is then position idx[f]
+    // dev_n (optional): row count read on the device, capped at n_host
+    const uint64_t n = dev_n ? min((uint64_t)*dev_n, n_host) : n_host;
     const uint64_t ntiles = (n + kTcTileM - 1) / kTcTileM;
     const int r = threadIdx.x;  // 128 threads, one row each
     for (uint64_t tile = blockIdx.x; tile < ntiles; tile += gridDim.x) {
@@ -518,11 +535,13 @@ __global__ void k_split_rows(const float* __restrict__ x, const uint32_t* __rest
 }
 
 void launch_split_rows(const float* x, const uint32_t* sel, const uint32_t* idx, uint64_t n,
-                       uint32_t D, float* tiles, float* xn2, cudaStream_t st) {
+                       uint32_t D, float* tiles, float* xn2, cudaStream_t st,
+                       const uint32_t* dev_n) {
     if (n == 0) return;
     uint64_t tiles_n = (n + kTcTileM - 1) / kTcTileM;
     if (tiles_n > 148ull * 64) tiles_n = 148ull * 64;
-    TSOM_LAUNCH(k_split_rows<<<(unsigned)tiles_n, kTcTileM, 0, st>>>(x, sel, idx, n, D, tiles, xn2));
+    TSOM_LAUNCH(k_split_rows<<<(unsigned)tiles_n, kTcTileM, 0, st>>>(x, sel, idx, dev_n, n, D,
+                                                                       tiles, xn2));
 }
 
 }  // namespace tsom
