@@ -217,6 +217,7 @@ def run_gpu_arm(args):
     if args.kernel:
         eng.set_option(_lib.TSOM_OPT_BMU_KERNEL, args.kernel)
     eng.bind(host)
+    active_kernel = eng.active_bmu_kernel
     if world > 1:
         uid = [eng.comm_unique_id() if rank == 0 else None]
         dist.broadcast_object_list(uid, src=0)
@@ -317,21 +318,23 @@ def run_gpu_arm(args):
     pk, pk_kind = peaks()
     k1 = statistics.mean(k1_ms) if k1_ms else float("nan")
     flops = 2.0 * P * D * n
-    tf32_peak = pk["bf16_tflops"] / 2.0
     achieved = flops / (k1 / 1e3) / 1e12 if k1 > 0 else 0.0
-    roof = {"bound": "tensor", "kernel": "k1 BMU (" + ("tcgen05 3xTF32" if args.kernel != 1 and
-                                                      tsom_tc_active() else "SIMT FP32") + ")",
-            "achieved": achieved, "peak": tf32_peak / 3.0, "unit": "TFLOP/s",
-            "frac": achieved / (tf32_peak / 3.0),
-            "traffic": None,
+    kname, peak, pnote = roofline_peak(active_kernel, pk)
+    roof = {"bound": "tensor", "kernel": "k1 BMU (" + kname + ")",
+            "achieved": achieved, "peak": peak, "unit": "TFLOP/s",
+            "frac": achieved / peak,
+            "traffic": K1_TRAFFIC.get(active_kernel),
             "note": (f"achieved = 2*K*D*N useful flop per launch / mean K1 event time; peak = "
-                     f"{pk_kind} bf16 {pk['bf16_tflops']} TF/s / 2 (TF32) / 3 (3xTF32 split)"),
+                     f"{pk_kind} bf16 {pk['bf16_tflops']} TF/s {pnote}; traffic = ncu "
+                     f"dram__bytes_read+write per launch ({K1_TRAFFIC_SRC})"),
             "k1_ms": k1, "epoch_ms": statistics.mean(total_ms) if total_ms else None,
             "phase_ms": {k: statistics.mean(p[k] for p in phases) for k in phases[0]} if phases else None}
     line = {
         "metric": METRIC, "value": value, "unit": UNIT, "n_gpus": world, "steps": args.steps,
         "warmup": args.warmup, "ms_per_step": ms, "higher_is_better": True, "scaling": "weak",
-        "vs_baseline": None, "dtype": "f32 (3xTF32 BMU) + f64 accumulate/update",
+        "vs_baseline": None,
+        "dtype": {3: "f32 via 3xFP16 split", 2: "f32 via 3xTF32 split", 1: "f32"}[active_kernel]
+                 + " BMU (exact FP64 re-check) + f64 accumulate/update",
         "data": "synthetic Gaussian mixture (16 comps, U[-4,4] centres, unit noise), random-init "
                 "codebook by sample_draw",
         "config": {"workload": "c2: 32x32 hex SOM (1024 nodes), 1e7 x 50 rows per GPU, full "
@@ -357,22 +360,19 @@ def run_gpu_arm(args):
     return 0
 
 
-def tsom_tc_active():
-    from paper_2604_26555_b200 import _lib
-    L = _lib.load()
-    return b"tcgen05" in L.tsom_version() and _tc_probe()
+def roofline_peak(kernel, pk):
+    """Dense tensor peak the K1 kernel is bounded by, in useful-flop terms."""
+    if kernel == 3:  # kind::f16 runs at the bf16 rate; 3 split products per useful MAC
+        return "tcgen05 3xFP16", pk["bf16_tflops"] / 3.0, "/ 3 (3xFP16 split)"
+    if kernel == 2:  # kind::tf32 runs at half the bf16 rate
+        return "tcgen05 3xTF32", pk["bf16_tflops"] / 2.0 / 3.0, "/ 2 (TF32) / 3 (3xTF32 split)"
+    return "SIMT FP32", pk.get("fp32_tflops", 75.0), "(FP32 SIMT, nominal)"
 
 
-def _tc_probe():
-    import paper_2604_26555_b200 as tsom
-    from paper_2604_26555_b200 import _lib
-    try:
-        e = tsom.Engine(256, D)
-        e.set_option(_lib.TSOM_OPT_BMU_KERNEL, 2)
-        e.close()
-        return True
-    except Exception:
-        return False
+# ncu --set full, one launch of K1 at the bench shape (1e7 x 50, K=1024):
+# dram__bytes_read.sum + dram__bytes_write.sum, bytes per launch.
+K1_TRAFFIC = {}
+K1_TRAFFIC_SRC = "profiles/ (not captured for this kernel yet)"
 
 
 def main():
@@ -381,7 +381,7 @@ def main():
     ap.add_argument("--steps", type=int, default=50)
     ap.add_argument("--warmup", type=int, default=5)
     ap.add_argument("--impl", default="b200", choices=["b200", "reference"])
-    ap.add_argument("--kernel", type=int, default=0, help="0 auto, 1 SIMT, 2 tcgen05")
+    ap.add_argument("--kernel", type=int, default=0, help="0 auto, 1 SIMT, 2 tcgen05 3xTF32, 3 tcgen05 3xFP16")
     ap.add_argument("--no-e2e", action="store_true")
     ap.add_argument("--no-cpu", action="store_true")
     args = ap.parse_args()

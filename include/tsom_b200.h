@@ -53,7 +53,8 @@ extern "C" {
                                   streams them through double-buffered chunks */
 
 /* tsom_set_option keys */
-#define TSOM_OPT_BMU_KERNEL 1      /* 0 = auto (tcgen05 when supported), 1 = SIMT, 2 = tcgen05 */
+#define TSOM_OPT_BMU_KERNEL 1      /* 0 = auto, 1 = SIMT, 2 = tcgen05 3xTF32 (d <= 53),
+                                      3 = tcgen05 3xFP16 (d <= 62); auto = 3, else 2, else 1 */
 #define TSOM_OPT_TIE_TAU 2         /* value*2^-30: relative tie window for the exact re-check */
 #define TSOM_OPT_STREAM_CHUNK 3    /* rows per streamed chunk */
 #define TSOM_OPT_DETERMINISTIC 4   /* reserved */
@@ -66,7 +67,7 @@ typedef struct tsom_engine tsom_engine;
 /* Engine lifetime ---------------------------------------------------------- */
 
 /* Create an engine for a P-node, d-dimensional codebook on CUDA `device`
- * (1 <= d <= 256; the tensor-core BMU kernel covers d <= 54, larger d uses the
+ * (1 <= d <= 256; the tensor-core BMU kernels cover d <= 62, larger d uses the
  * SIMT kernel). */
 int tsom_create(int device, uint32_t nodes, uint32_t dims, tsom_engine** out);
 int tsom_destroy(tsom_engine* eng);
@@ -161,6 +162,9 @@ int tsom_pairwise_sq_dists(tsom_engine* eng, double* out);
 /* Rows of the last BMU pass whose winner was decided in exact FP64 (several
  * candidates inside the FP32 error window, or a full re-scan). */
 uint64_t tsom_last_recheck_count(const tsom_engine* eng);
+/* The BMU kernel the engine runs for its shape and options: 1 = SIMT FP32,
+ * 2 = tcgen05 3xTF32, 3 = tcgen05 3xFP16 (TSOM_OPT_BMU_KERNEL values). */
+int tsom_active_bmu_kernel(const tsom_engine* eng);
 
 /* Multi-GPU (one process per GPU) ---------------------------------------- */
 

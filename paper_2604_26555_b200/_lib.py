@@ -39,7 +39,7 @@ EXPORTS = [
     "tsom_bmu_bound", "tsom_qe", "tsom_set_topology_distance", "tsom_train_epoch",
     "tsom_last_recheck_count", "tsom_comm_unique_id", "tsom_comm_init", "tsom_last_timing",
     "tsom_stream", "tsom_last_timing_detail", "tsom_kernel_launches", "tsom_refresh_topology",
-    "tsom_pairwise_sq_dists", "tsom_bind_shards",
+    "tsom_pairwise_sq_dists", "tsom_bind_shards", "tsom_active_bmu_kernel",
 ]
 
 
@@ -105,6 +105,8 @@ def load():
     L.tsom_train_epoch.argtypes = [_vp, C.c_double, C.c_double, C.c_double, u32]
     L.tsom_last_recheck_count.argtypes = [_vp]
     L.tsom_last_recheck_count.restype = u64
+    L.tsom_active_bmu_kernel.argtypes = [_vp]
+    L.tsom_active_bmu_kernel.restype = C.c_int
     L.tsom_comm_unique_id.argtypes = [_vp, C.c_char_p]
     L.tsom_comm_init.argtypes = [_vp, C.c_char_p, i32, i32]
     L.tsom_last_timing.argtypes = [_vp] + [C.POINTER(C.c_float)] * 4
@@ -255,6 +257,11 @@ class Engine:
                     use_momentum: bool = False):
         self._check(self.L.tsom_train_epoch(self.h, float(eta), float(sigma), float(momentum),
                                             1 if use_momentum else 0))
+
+    @property
+    def active_bmu_kernel(self) -> int:
+        """1 SIMT, 2 tcgen05 3xTF32, 3 tcgen05 3xFP16."""
+        return int(self.L.tsom_active_bmu_kernel(self.h))
 
     @property
     def last_recheck_count(self) -> int:

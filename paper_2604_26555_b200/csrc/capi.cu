@@ -130,9 +130,23 @@ size_t slot_len(const Engine* e) { return (size_t)e->P * e->D + e->P + 2; }
 
 uint32_t ppad(const Engine* e) { return (e->P + 63) / 64 * 64; }
 
-bool use_tc(const Engine* e) {
-    if (e->bmu_kernel == 1) return false;
-    return tsom::tc_supported(e->P, e->D);
+// Tensor-core operand encoding for this engine: option 2 = 3xTF32, 3 = 3xFP16,
+// 0 (auto) = 3xFP16 when d fits (d <= 62), else 3xTF32 (d <= 53), else SIMT.
+int tc_kind(const Engine* e) {
+    if (e->bmu_kernel == 1) return tsom::kTcNone;
+    if (e->bmu_kernel == 2) return tsom::kTcTf32;
+    if (e->bmu_kernel == 3) return tsom::kTcF16;
+    if (tsom::tc_supported(tsom::kTcF16, e->P, e->D)) return tsom::kTcF16;
+    if (tsom::tc_supported(tsom::kTcTf32, e->P, e->D)) return tsom::kTcTf32;
+    return tsom::kTcNone;
+}
+
+tsom::TieWin tie_window(const Engine* e, int kind) {
+    tsom::TieWin w;
+    w.tau = (float)e->tau_tc;
+    w.abs_coef = kind == tsom::kTcF16 ? (float)(std::ldexp(1.0, -24) * std::sqrt((double)e->D)) : 0.0f;
+    w.quant = (float)std::ldexp(1.0, -14);
+    return w;
 }
 
 void ensure_rows(Engine* eng, uint64_t n) {
@@ -144,34 +158,39 @@ void ensure_rows(Engine* eng, uint64_t n) {
 void prep_codebook(Engine* eng) {
     REQUIRE(eng->codebook_set, TSOM_ERR_INVALID, "engine: codebook not set (tsom_set_codebook)");
     if (eng->codebook_prepped) return;
-    const bool tc = use_tc(eng);
-    const uint32_t gn = tsom::tc_group_width(eng->P);
-    const uint32_t groups = (eng->P + gn - 1) / gn;
-    if (tc) CU(eng->wsplit.ensure((size_t)groups * 2 * gn * tsom::kTcKPad * sizeof(float)));
     tsom::launch_prep_codebook(eng->w.as<float>(), eng->P, eng->D, eng->w2.as<double>(),
-                               eng->w2max.as<float>(), eng->wt.as<float>(), ppad(eng),
-                               tc ? eng->wsplit.as<float>() : nullptr, eng->stream);
+                               eng->w2max.as<float>(), eng->wt.as<float>(), ppad(eng), eng->stream);
     CU(cudaGetLastError());
     eng->codebook_prepped = true;
 }
 
 // K1 + exact re-check over rows `x` (selection `sel` of length n, or first n rows).
-// `tiles` = pre-split tcgen05 operand for exactly these n rows (or nullptr to build).
+// x2max: max ||x||^2 over these rows (device; picks the FP16 operand scale).
+// `tiles` = pre-split tcgen05 A tiles for exactly these n rows, built with the
+// scale of this same x2max (or nullptr to build them here).
 void run_bmu(Engine* eng, const float* x, const uint32_t* sel, uint64_t n, const float* x2max,
-             const float* tiles, const float* tiles_xn2) {
+             const void* tiles, const float* tiles_xn2) {
     CU(cudaMemsetAsync(eng->flags.p, 0, 2 * sizeof(uint32_t), eng->stream));
     if (n == 0) return;
-    if (use_tc(eng)) {
+    const int kind = tc_kind(eng);
+    if (kind != tsom::kTcNone) {
+        const tsom::TcGeom geo = tsom::tc_geom(kind, eng->D);
         const uint32_t gn = tsom::tc_group_width(eng->P);
         const uint32_t groups = (eng->P + gn - 1) / gn;
-        const size_t tile_bytes = 2ull * tsom::kTcTileM * tsom::kTcKPad * sizeof(float);
+        const float* scale = eng->scale.as<float>();
+        const tsom::TieWin win = tie_window(eng, kind);
+        // operand scale + codebook B operand for these rows (a few microseconds)
+        tsom::launch_set_scale(kind, x2max, eng->scale.as<float>(), eng->stream);
+        CU(eng->wsplit.ensure(tsom::tc_wsplit_bytes(kind, eng->P, eng->D)));
+        tsom::launch_prep_wsplit(kind, eng->w.as<float>(), eng->P, eng->D, scale, eng->wsplit.p,
+                                 eng->stream);
         if (!tiles) {
             const uint64_t ntiles = (n + tsom::kTcTileM - 1) / tsom::kTcTileM;
-            CU(eng->gsplit.ensure(ntiles * tile_bytes));
+            CU(eng->gsplit.ensure(ntiles * geo.tile_bytes));
             CU(eng->gxn2.ensure(n * sizeof(float)));
-            tsom::launch_split_rows(x, sel, nullptr, n, eng->D, eng->gsplit.as<float>(),
+            tsom::launch_split_rows(kind, x, sel, nullptr, n, eng->D, scale, eng->gsplit.p,
                                     eng->gxn2.as<float>(), eng->stream);
-            tiles = eng->gsplit.as<float>();
+            tiles = eng->gsplit.p;
             tiles_xn2 = eng->gxn2.as<float>();
         }
         CU(eng->part.ensure((size_t)groups * 3 * n * sizeof(float)));
@@ -179,16 +198,15 @@ void run_bmu(Engine* eng, const float* x, const uint32_t* sel, uint64_t n, const
         CU(eng->tmask.ensure(std::max<uint64_t>(n, 1) * sizeof(uint32_t)));
         CU(cudaMemsetAsync(eng->ties.p, 0, sizeof(uint32_t), eng->stream));
         const float* w2 = eng->w2max.as<float>();
-        const float tau = (float)eng->tau_tc;
         CU(cudaEventRecord(eng->ev[8], eng->stream));
-        CU(tsom::launch_bmu_tc(tiles, n, nullptr, false, eng->P, eng->wsplit.as<float>(),
-                               tiles_xn2, w2, tau, nullptr, eng->part.as<float>(),
-                               eng->sm_count, eng->stream));
+        CU(tsom::launch_bmu_tc(kind, tiles, n, nullptr, false, eng->P, eng->D, eng->wsplit.p,
+                               tiles_xn2, w2, scale, win, nullptr, eng->part.as<float>(),
+                               eng->sm_count, eng->smem_optin, eng->stream));
         CU(cudaEventRecord(eng->ev[9], eng->stream));
         eng->k1_timed = true;
-        tsom::launch_merge_fast(eng->part.as<float>(), n, groups, gn, tiles_xn2, w2, tau,
+        tsom::launch_merge_fast(eng->part.as<float>(), n, groups, gn, tiles_xn2, w2, scale, win,
                                 eng->bmu.as<uint32_t>(), eng->ties.as<uint32_t>(),
-                                eng->tmask.as<uint32_t>(), eng->stream);
+                                eng->tmask.as<uint32_t>(), eng->flags.as<uint32_t>(), eng->stream);
         CU(cudaGetLastError());
         // near-tie rows (~1-3%): same tensor-core kernel in enumerate mode on just
         // those rows, then exact FP64 over their few candidates.  The list length
@@ -197,21 +215,21 @@ void run_bmu(Engine* eng, const float* x, const uint32_t* sel, uint64_t n, const
         // exact re-scan.
         const uint64_t cap = std::min<uint64_t>(n, std::max<uint64_t>(1ull << 20, n / 8));
         const uint64_t mt = (cap + tsom::kTcTileM - 1) / tsom::kTcTileM;
-        CU(eng->tsplit.ensure(mt * tile_bytes));
+        CU(eng->tsplit.ensure(mt * geo.tile_bytes));
         CU(eng->part2.ensure((size_t)groups * 4 * cap * sizeof(float)));
         CU(eng->txn2.ensure(cap * sizeof(float)));
         const uint32_t* tcount = eng->ties.as<uint32_t>();
         const uint32_t* tpos = tcount + 1;
-        tsom::launch_split_rows(x, sel, tpos, cap, eng->D, eng->tsplit.as<float>(),
+        tsom::launch_split_rows(kind, x, sel, tpos, cap, eng->D, scale, eng->tsplit.p,
                                 eng->txn2.as<float>(), eng->stream, tcount);
-        CU(tsom::launch_bmu_tc(eng->tsplit.as<float>(), cap, tcount, true, eng->P,
-                               eng->wsplit.as<float>(), eng->txn2.as<float>(), w2, tau,
-                               eng->tmask.as<uint32_t>(), eng->part2.as<float>(),
-                               eng->sm_count, eng->stream));
+        CU(tsom::launch_bmu_tc(kind, eng->tsplit.p, cap, tcount, true, eng->P, eng->D,
+                               eng->wsplit.p, eng->txn2.as<float>(), w2, scale, win,
+                               eng->tmask.as<uint32_t>(), eng->part2.as<float>(), eng->sm_count,
+                               eng->smem_optin, eng->stream));
         tsom::launch_merge_partials(eng->part2.as<float>(), tpos, tcount, cap, n, groups, gn,
-                                    eng->txn2.as<float>(), w2, tau, x, sel, eng->w.as<float>(),
-                                    eng->D, eng->bmu.as<uint32_t>(), eng->flags.as<uint32_t>(),
-                                    eng->stream);
+                                    eng->txn2.as<float>(), w2, scale, win, x, sel,
+                                    eng->w.as<float>(), eng->D, eng->bmu.as<uint32_t>(),
+                                    eng->flags.as<uint32_t>(), eng->stream);
     } else {
         CU(cudaEventRecord(eng->ev[8], eng->stream));
         // the FP32 accumulation bound grows with the d+1 terms of each dot product
@@ -365,18 +383,24 @@ void accumulate_epoch(Engine* eng, const uint32_t* sel_host, uint64_t n_sel, boo
     eng->update_timed = false;
     CU(cudaEventRecord(eng->ev[0], eng->stream));
     if (!eng->streamed) {
-        const float* tiles = nullptr;
+        const void* tiles = nullptr;
         const float* tiles_xn2 = nullptr;
-        if (use_tc(eng) && !sel) {
-            if (!eng->xsplit_valid) {
+        const int kind = tc_kind(eng);
+        if (kind != tsom::kTcNone && !sel) {
+            if (!eng->xsplit_valid || eng->xsplit_kind != kind) {
+                // split once per bound dataset (the rows do not change across epochs)
                 const uint64_t ntiles = (eng->n_rows + tsom::kTcTileM - 1) / tsom::kTcTileM;
-                CU(eng->xsplit.ensure(ntiles * 2 * tsom::kTcTileM * tsom::kTcKPad * sizeof(float)));
+                CU(eng->xsplit.ensure(ntiles * tsom::tc_geom(kind, eng->D).tile_bytes));
                 CU(eng->xn2.ensure(std::max<uint64_t>(eng->n_rows, 1) * sizeof(float)));
-                tsom::launch_split_rows(eng->x.as<float>(), nullptr, nullptr, eng->n_rows, eng->D,
-                                        eng->xsplit.as<float>(), eng->xn2.as<float>(), eng->stream);
+                tsom::launch_set_scale(kind, eng->x2max.as<float>(), eng->scale.as<float>(),
+                                       eng->stream);
+                tsom::launch_split_rows(kind, eng->x.as<float>(), nullptr, nullptr, eng->n_rows,
+                                        eng->D, eng->scale.as<float>(), eng->xsplit.p,
+                                        eng->xn2.as<float>(), eng->stream);
                 eng->xsplit_valid = true;
+                eng->xsplit_kind = kind;
             }
-            tiles = eng->xsplit.as<float>();
+            tiles = eng->xsplit.p;
             tiles_xn2 = eng->xn2.as<float>();
         }
         run_bmu(eng, eng->x.as<float>(), dsel, n, eng->x2max.as<float>(), tiles, tiles_xn2);
@@ -557,6 +581,8 @@ int tsom_create(int device, uint32_t nodes, uint32_t dims, tsom_engine** out) {
         CU(eng->w2max.ensure(sizeof(float)));
         CU(eng->x2max.ensure(2 * sizeof(float)));
         CU(cudaMemset(eng->x2max.p, 0, 2 * sizeof(float)));
+        CU(eng->scale.ensure(4 * sizeof(float)));
+        CU(cudaMemset(eng->scale.p, 0, 4 * sizeof(float)));
         CU(eng->infl.ensure(P * P * sizeof(double)));
         CU(eng->U.ensure(P * D * sizeof(double)));
         CU(eng->H.ensure(P * sizeof(double)));
@@ -584,7 +610,7 @@ int tsom_destroy(tsom_engine* eng) {
         if (eng->ev_pin[s2]) cudaEventDestroy(eng->ev_pin[s2]);
     }
     for (DevBuf* b : {&eng->x, &eng->xsplit, &eng->xn2, &eng->gxn2, &eng->txn2, &eng->x2max, &eng->w, &eng->wt, &eng->wsplit, &eng->w2,
-                      &eng->w2max, &eng->prev, &eng->infl, &eng->topo_dist, &eng->sel,
+                      &eng->w2max, &eng->scale, &eng->prev, &eng->infl, &eng->topo_dist, &eng->sel,
                       &eng->rows_scratch, &eng->gsplit, &eng->bmu, &eng->dist, &eng->part,
                       &eng->flags, &eng->ties, &eng->tmask, &eng->part2, &eng->tsplit, &eng->acc_buf[0], &eng->acc_buf[1], &eng->acc_buf[2], &eng->acc_buf[3],
                       &eng->acc_buf[4], &eng->acc_buf[5], &eng->acc_buf[6], &eng->sums, &eng->chunk_flags,
@@ -610,9 +636,11 @@ int tsom_set_option(tsom_engine* eng, int key, int64_t value) {
     return guarded(eng, [&] {
         switch (key) {
             case TSOM_OPT_BMU_KERNEL:
-                REQUIRE(value >= 0 && value <= 2, TSOM_ERR_INVALID, "option: bmu kernel 0..2");
-                REQUIRE(value != 2 || tsom::tc_supported(eng->P, eng->D), TSOM_ERR_INVALID,
-                        "option: tcgen05 BMU kernel needs d <= 54");
+                REQUIRE(value >= 0 && value <= 3, TSOM_ERR_INVALID, "option: bmu kernel 0..3");
+                REQUIRE(value != 2 || tsom::tc_supported(tsom::kTcTf32, eng->P, eng->D),
+                        TSOM_ERR_INVALID, "option: 3xTF32 tcgen05 BMU kernel needs d <= 53");
+                REQUIRE(value != 3 || tsom::tc_supported(tsom::kTcF16, eng->P, eng->D),
+                        TSOM_ERR_INVALID, "option: 3xFP16 tcgen05 BMU kernel needs d <= 62");
                 eng->bmu_kernel = (int)value;
                 eng->codebook_prepped = false;
                 break;
@@ -623,6 +651,9 @@ int tsom_set_option(tsom_engine* eng, int key, int64_t value) {
             case TSOM_OPT_STREAM_CHUNK:
                 REQUIRE(value >= 128, TSOM_ERR_INVALID, "option: stream chunk >= 128 rows");
                 eng->stream_chunk_rows = (uint64_t)value;
+                break;
+            case 99:  // diagnostics (not in the public header): K1 stage isolation
+                tsom::g_k1_debug = (uint32_t)value;
                 break;
             case TSOM_OPT_HOST_REGISTER:
                 eng->host_register = value != 0;
@@ -1091,6 +1122,12 @@ int tsom_train_epoch(tsom_engine* eng, double eta, double sigma, double momentum
 }
 
 uint64_t tsom_last_recheck_count(const tsom_engine* eng) { return eng ? eng->last_recheck : 0; }
+
+int tsom_active_bmu_kernel(const tsom_engine* eng) {
+    if (!eng) return 0;
+    const int k = tc_kind(eng);
+    return k == tsom::kTcF16 ? 3 : (k == tsom::kTcTf32 ? 2 : 1);
+}
 
 int tsom_comm_unique_id(tsom_engine* eng, uint8_t id_out[128]) {
     return guarded(eng, [&] {

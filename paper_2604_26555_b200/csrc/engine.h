@@ -54,7 +54,48 @@ constexpr double kDefaultTauTc = 1.0 / 16384.0;     // 2^-14 (3xTF32 error is la
 
 constexpr int kTcTileM = 128;   // samples per tcgen05 tile (TMEM lanes)
 constexpr int kTcGroupN = 256;  // nodes per CTA-resident codebook group
-constexpr int kTcKPad = 56;     // d + 1 (norm column) padded to 7 tf32 k-steps
+constexpr int kTcKPad = 56;     // tf32 operand: d + 3 augmented columns padded to 7 k-steps
+constexpr uint32_t kTcF16MaxK = 192;  // f16 operand: 3d + 5 columns padded to 16 (d <= 62)
+constexpr uint32_t kCandOverflow = 15u;  // enumerate pass: > 8 candidates in a group
+
+// Tensor-core operand encodings of K1 (k1_bmu_tc.cu)
+enum TcKind : int { kTcNone = 0, kTcTf32 = 1, kTcF16 = 2 };
+struct TcGeom {
+    int kind;
+    uint32_t kpad;        // K elements per row (tf32: per half)
+    uint32_t ksteps;      // MMA k-steps (tf32: x3 products each)
+    uint32_t tile_bytes;  // one 128-row A tile
+    uint32_t row_bytes;   // one node row of the B operand
+};
+__host__ __device__ inline TcGeom tc_geom(int kind, uint32_t D) {
+    TcGeom g{kind, 0, 0, 0, 0};
+    if (kind == kTcTf32) {
+        g.kpad = kTcKPad;
+        g.ksteps = kTcKPad / 8;
+        g.tile_bytes = 2u * kTcTileM * kTcKPad * 4u;
+        g.row_bytes = 2u * kTcKPad * 4u;
+    } else if (kind == kTcF16) {
+        g.kpad = (3u * D + 5u + 15u) / 16u * 16u;
+        g.ksteps = g.kpad / 16u;
+        g.tile_bytes = kTcTileM * g.kpad * 2u;
+        g.row_bytes = g.kpad * 2u;
+    }
+    return g;
+}
+
+// Error window of the tensor-core BMU values (scaled units, S = s^2): a row whose
+// computed top-2 gap exceeds
+//   tau S (||x||^2 + max||w||^2) + abs_coef (sqrt(S ||x||^2) + 2 sqrt(S max||w||^2))
+//   [+ quant (|B1| + |B2|) for packed keys]
+// has a unique exact argmin equal to the computed one.
+struct TieWin {
+    float tau;       // relative bound of the split-precision products + FP32 accumulation
+    float abs_coef;  // absolute floor (FP16 subnormal spacing): 2^-24 sqrt(d), 0 for tf32
+    float quant;     // packed-key truncation: 2^-14
+};
+__host__ __device__ inline float tie_thr(float xn2, float w2max, float S, TieWin w) {
+    return w.tau * S * (xn2 + w2max) + w.abs_coef * (sqrtf(S * xn2) + 2.0f * sqrtf(S * w2max));
+}
 
 // K2: counting sort by BMU + per-piece FP64 gather accumulation (k_accum.cu).
 struct AccumScratch {
@@ -111,7 +152,9 @@ struct Engine {
     bool streamed = false;
     const float* host_rows = nullptr;  // streamed mode source
     bool host_registered = false;
-    DevBuf xsplit;      // pre-split tf32 tiles for the tensor-core kernel (all rows)
+    DevBuf xsplit;      // pre-split tcgen05 A tiles of all rows (encoding xsplit_kind)
+    int xsplit_kind = 0;
+    DevBuf scale;       // {s, s^2, overflow} of the operands currently in wsplit
     DevBuf xn2, gxn2, txn2;  // per-row ||x||^2 for xsplit / gsplit / tsplit rows
     bool xsplit_valid = false;
     DevBuf x2max;       // float: max ||x||^2 over bound rows
@@ -182,20 +225,26 @@ struct Engine {
 // Kernel launchers (all asynchronous on `st`)
 // ---------------------------------------------------------------------------
 
-// codebook prep: w2 (f64 ||w_j||^2), w2max, SIMT operand wt, tcgen05 operand wsplit
+// codebook prep: w2 (f64 ||w_j||^2), w2max, SIMT operand wt
 void launch_prep_codebook(const float* w, uint32_t P, uint32_t D, double* w2, float* w2max,
-                          float* wt, uint32_t Ppad, float* wsplit, cudaStream_t st);
+                          float* wt, uint32_t Ppad, cudaStream_t st);
 // max ||x||^2 over rows (f32 atomic max on non-negative floats)
 void launch_row_norm_max(const float* x, uint64_t n, uint32_t D, float* out, cudaStream_t st);
 // a[0] = max(a[0], a[1])
 void launch_fold_max(float* a, cudaStream_t st);
 // split rows (optionally gathered through sel, and/or through a position list
-// idx: split row f = position idx[f]) into tcgen05 tiles
-void launch_split_rows(const float* x, const uint32_t* sel, const uint32_t* idx, uint64_t n,
-                       uint32_t D, float* tiles, float* xn2, cudaStream_t st,
-                       const uint32_t* dev_n = nullptr);
-bool tc_supported(uint32_t P, uint32_t D);
-// nodes per CTA-resident codebook group (multiple of 16, <= 256)
+// idx: split row f = position idx[f]) into tcgen05 A tiles of encoding `kind`
+void launch_split_rows(int kind, const float* x, const uint32_t* sel, const uint32_t* idx,
+                       uint64_t n, uint32_t D, const float* scale, void* tiles, float* xn2,
+                       cudaStream_t st, const uint32_t* dev_n = nullptr);
+bool tc_supported(int kind, uint32_t P, uint32_t D);
+size_t tc_wsplit_bytes(int kind, uint32_t P, uint32_t D);
+// scale = {s, s^2, overflow flag}: kTcF16 picks s = 2^e from max ||x||^2 (x2max[0])
+void launch_set_scale(int kind, const float* x2max, float* scale, cudaStream_t st);
+// tcgen05 B operand of the codebook (per group, core-matrix order)
+void launch_prep_wsplit(int kind, const float* w, uint32_t P, uint32_t D, const float* scale,
+                        void* wsplit, cudaStream_t st);
+// nodes per CTA-resident codebook group (multiple of 32, <= 256)
 __host__ __device__ inline uint32_t tc_group_width(uint32_t P) {
     return P >= (uint32_t)kTcGroupN ? (uint32_t)kTcGroupN : (P + 31u) / 32u * 32u;
 }
@@ -206,23 +255,26 @@ void launch_bmu_simt(const float* x, const uint32_t* sel, uint64_t n, uint32_t D
                      uint32_t* bmu, uint32_t* flags, int sm_count, cudaStream_t st);
 // tcgen05 variant: per-group partials (enumerate = candidate lists; dev_n =
 // optional device row count).
-cudaError_t launch_bmu_tc(const float* tiles, uint64_t n, const uint32_t* dev_n, bool enumerate,
-                          uint32_t P, const float* wsplit, const float* xn2,
-                          const float* w2max, float tau, const uint32_t* rmask, float* part,
-                          int sm_count, cudaStream_t st);
+cudaError_t launch_bmu_tc(int kind, const void* tiles, uint64_t n, const uint32_t* dev_n,
+                          bool enumerate, uint32_t P, uint32_t D, const void* wsplit,
+                          const float* xn2, const float* w2max, const float* scale, TieWin win,
+                          const uint32_t* rmask, float* part, int sm_count, size_t smem_optin,
+                          cudaStream_t st);
+extern uint32_t g_k1_debug;  // diagnostics: bit0 skip epilogue math, bit1 skip MMAs
 // main-pass merge: bmu for rows with a clear winner, near-tie positions -> ties
 void launch_merge_fast(const float* part, uint64_t n, uint32_t groups, uint32_t gn,
-                       const float* xn2, const float* w2max, float tau, uint32_t* bmu,
-                       uint32_t* ties, uint32_t* tmask, cudaStream_t st);
+                       const float* xn2, const float* w2max, const float* scale, TieWin win,
+                       uint32_t* bmu, uint32_t* ties, uint32_t* tmask, uint32_t* flags,
+                       cudaStream_t st);
 // enumerate-pass merge over the near-tie rows: candidates -> exact FP64 -> bmu;
 // overflow -> flags list for the full re-scan.
 // ties: near-tie positions, dev_count: their number (device); rows past `cap`
 // are sent to the full re-scan; n_max bounds the count (grid sizing)
 void launch_merge_partials(const float* part, const uint32_t* ties, const uint32_t* dev_count,
                            uint64_t cap, uint64_t n_max, uint32_t groups, uint32_t gn,
-                           const float* xn2, const float* w2max, float tau, const float* x,
-                           const uint32_t* sel, const float* w, uint32_t D, uint32_t* bmu,
-                           uint32_t* flags, cudaStream_t st);
+                           const float* xn2, const float* w2max, const float* scale, TieWin win,
+                           const float* x, const uint32_t* sel, const float* w, uint32_t D,
+                           uint32_t* bmu, uint32_t* flags, cudaStream_t st);
 // exact FP64 re-scan of flagged rows (reference loop order)
 void launch_rescan(const float* x, const uint32_t* sel, const float* w, uint32_t P, uint32_t D,
                    const uint32_t* flags, uint64_t n, uint32_t* bmu, cudaStream_t st);

@@ -1,201 +1,364 @@
-// k1_bmu_tc.cu — K1: BMU search as a tcgen05 3xTF32 tile GEMM with a fused
-// top-2 epilogue (the samples x codebook distance matrix never reaches HBM).
+// k1_bmu_tc.cu — K1: BMU search as a tcgen05 tile GEMM with split-precision
+// operands and a fused top-2 epilogue (the samples x codebook distance matrix
+// never reaches HBM).  Reference: find_bmus, trainer.hpp:282-308.
 //
-// For every row x and node j the kernel evaluates  v_j = ||w_j||^2 - 2 x.w_j
-// (trainer.hpp:282-308 without the row-constant ||x||^2) as one augmented dot
-// product  x'.w'  with  x' = [x, 1, 1, 0..]  and  w' = [-2w, p1+p2, p3, 0..]
-// (k_bmu.cu: k_prep_codebook, k_split_rows), K padded to 56 = 7 tf32 k-steps.
-// 3xTF32: x' = xh + xl, w' = wh + wl (xh, wh exact tf32), and
-//   x'.w' ~= xh.wh + xl.wh + xh.wl          (xl.wl ~ 2^-22 relative, dropped)
-// accumulated in FP32 in TMEM.  Rows whose best/second-best gap falls inside
-// the error window are re-checked in exact FP64 (k_rescan), so BMU indices are
-// bit-identical to the reference.
+// For row x and node j the kernel evaluates one augmented dot product whose
+// value is (up to FP32 rounding and a power-of-two scale S = s^2)
+//     v_j = ||x||^2 + ||w_j||^2 - 2 x.w_j  = d^2(x, w_j).
+// Two operand encodings (TcKind), both "3-split" so FP32-level accuracy holds:
+//   * kTcTf32 (3xTF32, kind::tf32): x' = [x, 1, 1, ||x||^2, 0..] and
+//     w' = [-2w, p1+p2, p3, 1, 0..] (K = 56 = 7 k-steps of 8), split into
+//     hi/lo halves; per k-step  xh.wh + xl.wh + xh.wl  (21 MMAs per tile).
+//   * kTcF16 (3xFP16, kind::f16, 2x the TF32 rate): the three products are
+//     concatenated along K instead of issued separately,
+//         A = [xh | xl | xh | n_hi, n_lo, 1, 1, 1]   (x scaled by s)
+//         B = [wh | wh | wl | 1,    1,    p1, p2, p3] (w' = -2 w s)
+//     so one K = 16*ceil((3d+5)/16) pass (10 MMAs of K=16 at d = 50) yields
+//     xh.wh + xl.wh + xh.wl + ||x s||^2 + ||w s||^2.  s = 2^e is chosen from
+//     max ||x||^2 so every |x s| <= 16 (FP16 range; k_set_scale).
+// Rows whose best/second-best gap falls inside the error window (tie_thr) are
+// re-checked exactly in FP64 (k_bmu.cu), so BMU indices are bit-identical to
+// the reference.
+//
+// Epilogue: thread = row (TMEM lane), 256 node values per group.  Each value is
+// packed with its local node id in the low 8 mantissa bits (one LOP3) and the
+// packed keys go through a pairwise top-2 network (FMNMX / 3-input FMNMX3):
+// 3.5 ALU ops per value instead of 5 for a compare/select top-2 with a
+// separate index register.  Packing truncates the value by < 2^-15 relative;
+// the merge widens the window by 2^-14 (|B1| + |B2|) to stay exact.
 //
 // Work split: the codebook is cut into groups of gn <= 256 nodes.  A CTA keeps
-// one group resident in shared memory (hi|lo, 2 * 14 * gn * 16 B) for its
-// whole life and streams 128-row sample tiles (hi|lo, 57,344 B) through a
-// 2-stage cp.async.bulk pipeline.  Warp roles (256 threads):
+// one group resident in shared memory for its whole life and streams 128-row
+// sample tiles through a cp.async.bulk pipeline.  Warp roles (384 threads):
 //   warp 0      : producer — bulk copies (mbarrier complete_tx)
-//   warp 1      : MMA issuer — one elected thread, 21 tcgen05.mma per tile
-//                 (M=128 rows x N=gn nodes x K=8, three products x 7 k-steps)
+//   warp 1      : MMA issuer — one elected thread
 //   warp 2      : TMEM allocator (2 accumulator buffers x gn columns)
-//   warps 4..7  : epilogue — warp q+4 owns TMEM lanes 32q.. (tile rows) and all
-//                 columns; pipelined tcgen05.ld x32, eight independent top-2
-//                 streams per thread, candidate enumeration for near-ties
-// Samples sit on the TMEM lane axis, so no cross-lane reduction is needed.
+//   warps 4..11 : two sets of 4 epilogue warps, draining the two accumulator
+//                 buffers alternately (warp q of a set owns TMEM lanes 32q..)
+#include <cuda_fp16.h>
 #include <cuda_runtime.h>
 #include <math_constants.h>
 
 #include <cstdint>
 
 #include "engine.h"
+#include "tc_ptx.cuh"
 
 namespace tsom {
 
+using namespace ptx;
+
 namespace {
 
-constexpr int kThreads = 384;          // 4 role warps + 2 sets x 4 epilogue warps
-constexpr uint32_t kEpiThreads = 128;   // arrivals per accumulator buffer (one set)
-constexpr int kStages = 2;
-constexpr uint32_t kTileBytes = 2u * kTcTileM * kTcKPad * 4u;  // 57,344 (hi + lo)
-constexpr uint32_t kHalfTile = kTcTileM * kTcKPad * 4u;         // 28,672
-constexpr int kKSteps = kTcKPad / 8;                             // 7
+constexpr int kSets = 2;                // epilogue warp sets (4 warps each, one per TMEM lane quarter)
+constexpr int kThreads = 128 + kSets * 128;  // 4 role warps + the epilogue sets
+constexpr uint32_t kEpiThreads = 128;   // threads per epilogue set
+constexpr int kMaxStages = 4;
 
-__device__ __forceinline__ uint32_t smem_u32(const void* p) {
-    return static_cast<uint32_t>(__cvta_generic_to_shared(p));
-}
-
-__device__ __forceinline__ void mbar_init(uint64_t* bar, uint32_t count) {
-    asm volatile("mbarrier.init.shared::cta.b64 [%0], %1;" ::"r"(smem_u32(bar)), "r"(count));
-}
-
-__device__ __forceinline__ void mbar_expect_tx(uint64_t* bar, uint32_t bytes) {
-    asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;" ::"r"(smem_u32(bar)),
-                 "r"(bytes)
-                 : "memory");
-}
-
-__device__ __forceinline__ void mbar_arrive(uint64_t* bar) {
-    asm volatile("mbarrier.arrive.shared::cta.b64 _, [%0];" ::"r"(smem_u32(bar)) : "memory");
-}
-
-__device__ __forceinline__ void mbar_wait(uint64_t* bar, uint32_t parity) {
-    asm volatile(
-        "{\n\t"
-        ".reg .pred P1;\n\t"
-        "WAIT_%=:\n\t"
-        "mbarrier.try_wait.parity.shared::cta.b64 P1, [%0], %1, %2;\n\t"
-        "@!P1 bra WAIT_%=;\n\t"
-        "}" ::"r"(smem_u32(bar)),
-        "r"(parity), "r"(0x989680u)
-        : "memory");
-}
-
-__device__ __forceinline__ void bulk_g2s(void* dst, const void* src, uint32_t bytes, uint64_t* bar) {
-    asm volatile(
-        "cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1], %2, [%3];" ::"r"(
-            smem_u32(dst)),
-        "l"(src), "r"(bytes), "r"(smem_u32(bar))
-        : "memory");
-}
-
-// UMMA shared-memory descriptor, K-major, no swizzle (cute::UMMA::SmemDescriptor):
-// [0,14) start>>4, [16,30) LBO>>4 (k-core stride), [32,46) SBO>>4 (8-row stride),
-// [46,48) version = 1, [61,64) layout = SWIZZLE_NONE.
-__device__ __forceinline__ uint64_t umma_desc(uint32_t saddr, uint32_t lbo, uint32_t sbo) {
-    uint64_t d = 0;
-    d |= (uint64_t)((saddr >> 4) & 0x3FFFu);
-    d |= (uint64_t)((lbo >> 4) & 0x3FFFu) << 16;
-    d |= (uint64_t)((sbo >> 4) & 0x3FFFu) << 32;
-    d |= (uint64_t)1u << 46;
-    return d;
-}
-
-// Instruction descriptor for kind::tf32: D = F32, A = B = TF32, both K-major.
-__host__ __device__ constexpr uint32_t idesc_tf32(uint32_t M, uint32_t N) {
-    return (1u << 4) | (2u << 7) | (2u << 10) | ((N >> 3) << 17) | ((M >> 4) << 24);
-}
-
-__device__ __forceinline__ void mma_tf32(uint32_t d_tmem, uint64_t a, uint64_t b, uint32_t idesc,
-                                         uint32_t accumulate) {
-    asm volatile(
-        "{\n\t"
-        ".reg .pred p;\n\t"
-        "setp.ne.b32 p, %4, 0;\n\t"
-        "tcgen05.mma.cta_group::1.kind::tf32 [%0], %1, %2, %3, p;\n\t"
-        "}" ::"r"(d_tmem),
-        "l"(a), "l"(b), "r"(idesc), "r"(accumulate));
-}
-
-__device__ __forceinline__ void mma_commit(uint64_t* bar) {
-    asm volatile("tcgen05.commit.cta_group::1.mbarrier::arrive::one.shared::cluster.b64 [%0];" ::"r"(
-                     smem_u32(bar))
-                 : "memory");
-}
-
-__device__ __forceinline__ void tc_fence_before() {
-    asm volatile("tcgen05.fence::before_thread_sync;" ::: "memory");
-}
-__device__ __forceinline__ void tc_fence_after() {
-    asm volatile("tcgen05.fence::after_thread_sync;" ::: "memory");
-}
-
-#define TMEM_LD32(taddr, r)                                                                      \
-    asm volatile(                                                                                \
-        "tcgen05.ld.sync.aligned.32x32b.x32.b32 {%0,%1,%2,%3,%4,%5,%6,%7,%8,%9,%10,%11,%12,%13," \
-        "%14,%15,%16,%17,%18,%19,%20,%21,%22,%23,%24,%25,%26,%27,%28,%29,%30,%31}, [%32];"       \
-        : "=r"(r[0]), "=r"(r[1]), "=r"(r[2]), "=r"(r[3]), "=r"(r[4]), "=r"(r[5]), "=r"(r[6]),    \
-          "=r"(r[7]), "=r"(r[8]), "=r"(r[9]), "=r"(r[10]), "=r"(r[11]), "=r"(r[12]),            \
-          "=r"(r[13]), "=r"(r[14]), "=r"(r[15]), "=r"(r[16]), "=r"(r[17]), "=r"(r[18]),         \
-          "=r"(r[19]), "=r"(r[20]), "=r"(r[21]), "=r"(r[22]), "=r"(r[23]), "=r"(r[24]),         \
-          "=r"(r[25]), "=r"(r[26]), "=r"(r[27]), "=r"(r[28]), "=r"(r[29]), "=r"(r[30]),         \
-          "=r"(r[31])                                                                            \
-        : "r"(taddr))
-
-#define TMEM_LD16(taddr, r)                                                                      \
-    asm volatile(                                                                                \
-        "tcgen05.ld.sync.aligned.32x32b.x16.b32 {%0,%1,%2,%3,%4,%5,%6,%7,%8,%9,%10,%11,%12,%13," \
-        "%14,%15}, [%16];"                                                                       \
-        : "=r"(r[0]), "=r"(r[1]), "=r"(r[2]), "=r"(r[3]), "=r"(r[4]), "=r"(r[5]), "=r"(r[6]),    \
-          "=r"(r[7]), "=r"(r[8]), "=r"(r[9]), "=r"(r[10]), "=r"(r[11]), "=r"(r[12]),            \
-          "=r"(r[13]), "=r"(r[14]), "=r"(r[15])                                                  \
-        : "r"(taddr))
-
-__device__ __forceinline__ void tmem_wait_ld() {
-    asm volatile("tcgen05.wait::ld.sync.aligned;" ::: "memory");
+__device__ __forceinline__ float fmin3f(float a, float b, float c) {
+    float r;
+    asm("min.f32 %0, %1, %2, %3;" : "=f"(r) : "f"(a), "f"(b), "f"(c));
+    return r;
 }
 
 }  // namespace
 
-// branch-free top-2 step: strict < keeps the earliest j on ties, an exact tie
-// lands in b2 (gap 0 => candidate enumeration)
-__device__ __forceinline__ void top2_step(float v, uint32_t j, float& b1, uint32_t& i1,
-                                          float& b2) {
-    const float nb1 = fminf(b1, v);
-    b2 = fminf(b2, fmaxf(b1, v));
-    i1 = v < b1 ? j : i1;
-    b1 = nb1;
+// ---------------------------------------------------------------------------
+// Geometry of the two operand encodings
+// ---------------------------------------------------------------------------
+
+size_t tc_wsplit_bytes(int kind, uint32_t P, uint32_t D) {
+    const uint32_t gn = tc_group_width(P);
+    const uint32_t groups = (P + gn - 1) / gn;
+    const TcGeom g = tc_geom(kind, D);
+    return (size_t)groups * gn * g.row_bytes;
 }
 
-__device__ __forceinline__ void top2_merge_dev(float& b1, uint32_t& i1, float& b2, float ob1,
-                                               uint32_t oi1, float ob2) {
-    if (ob1 < b1 || (ob1 == b1 && oi1 < i1)) {
-        b2 = fminf(b1, ob2);
-        b1 = ob1;
-        i1 = oi1;
+bool tc_supported(int kind, uint32_t P, uint32_t D) {
+    if (P < 1) return false;
+    if (kind == kTcTf32) return D + 3 <= (uint32_t)kTcKPad;
+    if (kind == kTcF16) return 3u * D + 5u <= kTcF16MaxK;
+    return false;
+}
+
+// ---------------------------------------------------------------------------
+// Scale (kTcF16) and codebook operand
+// ---------------------------------------------------------------------------
+
+// scale[0] = s, scale[1] = s^2, scale[2] = overflow flag (bits), from max ||x||^2:
+// the largest power of two with max||x|| * s <= 16 (so |x_k s| <= 16 and
+// ||x s||^2 <= 256 fit FP16 with a 256x margin for ||w s||^2).
+__global__ void k_set_scale(int kind, const float* __restrict__ x2max, float* __restrict__ scale) {
+    float s = 1.0f;
+    if (kind == kTcF16) {
+        const float m = *x2max;
+        if (m > 0.0f && isfinite(m)) {
+            int e = ilogbf(16.0f / sqrtf(m));
+            e = max(-100, min(60, e));
+            s = ldexpf(1.0f, e);
+            while (m * s * s > 256.0f) s *= 0.5f;
+        }
+    }
+    scale[0] = s;
+    scale[1] = s * s;
+    scale[2] = 0.0f;
+}
+
+void launch_set_scale(int kind, const float* x2max, float* scale, cudaStream_t st) {
+    TSOM_LAUNCH(k_set_scale<<<1, 1, 0, st>>>(kind, x2max, scale));
+}
+
+__device__ __forceinline__ float tf32_trunc(float v) {
+    return __uint_as_float(__float_as_uint(v) & 0xFFFFE000u);
+}
+
+// One thread per (node, 16-byte K core).  Group g = j / gn holds gn nodes in
+// UMMA K-major core-matrix order: node r, core c at byte ((c * gn) + r) * 16
+// (kTcTf32: hi half then lo half; kTcF16: one concatenated operand).
+template <int kKind>
+__global__ void k_prep_wsplit(const float* __restrict__ w, uint32_t P, uint32_t D, uint32_t gn,
+                              uint32_t groups, const float* __restrict__ scale,
+                              uint8_t* __restrict__ wsplit) {
+    const uint32_t cores = kKind == kTcTf32 ? kTcKPad / 4 : tc_geom(kKind, D).kpad / 8;
+    const uint64_t tid = blockIdx.x * (uint64_t)blockDim.x + threadIdx.x;
+    const uint64_t total = (uint64_t)groups * gn * cores;
+    if (tid >= total) return;
+    const uint32_t j = (uint32_t)(tid / cores), c = (uint32_t)(tid % cores);
+    const uint32_t g = j / gn, r = j % gn;
+    const bool pad = j >= P;
+    const float* wj = w + (size_t)(pad ? 0 : j) * D;
+    if (kKind == kTcTf32) {
+        // w' = [-2w | p1 (hi) + p2 (lo) | p3 | 1 | 0..]; padding: 3e38 norm
+        double s2 = 0.0;
+        if (!pad)
+            for (uint32_t k = 0; k < D; ++k)
+                s2 = __dadd_rn(s2, __dmul_rn((double)wj[k], (double)wj[k]));
+        const float p1 = tf32_trunc((float)s2);
+        const float p2 = tf32_trunc((float)(s2 - (double)p1));
+        const float p3 = tf32_trunc((float)(s2 - (double)p1 - (double)p2));
+        float hi[4], lo[4];
+#pragma unroll
+        for (int q = 0; q < 4; ++q) {
+            const uint32_t k = c * 4 + q;
+            float h = 0.0f, l = 0.0f;
+            if (pad) {
+                if (k == D) h = tf32_trunc(3.0e38f);
+            } else if (k < D) {
+                const float v = -2.0f * wj[k];
+                h = tf32_trunc(v);
+                l = v - h;
+            } else if (k == D) {
+                h = p1;
+                l = p2;
+            } else if (k == D + 1) {
+                h = p3;
+            } else if (k == D + 2) {
+                h = 1.0f;
+            }
+            hi[q] = h;
+            lo[q] = l;
+        }
+        float* base = reinterpret_cast<float*>(wsplit) + (size_t)g * 2 * gn * kTcKPad;
+        const size_t off = ((size_t)c * gn + r) * 4;
+        *reinterpret_cast<float4*>(base + off) = make_float4(hi[0], hi[1], hi[2], hi[3]);
+        *reinterpret_cast<float4*>(base + (size_t)gn * kTcKPad + off) =
+            make_float4(lo[0], lo[1], lo[2], lo[3]);
     } else {
-        b2 = fminf(b2, ob1);
+        // B = [wh | wh | wl | 1, 1, p1, p2, p3 | 0..], w' = -2 w s; padding:
+        // p1 = p2 = p3 = 65504 (never wins: real values are < 2^17)
+        const float s = scale[0];
+        double n2 = 0.0;
+        if (!pad)
+            for (uint32_t k = 0; k < D; ++k) {
+                const double v = (double)(wj[k] * s);
+                n2 += v * v;
+            }
+        const __half q1 = __double2half(n2);
+        const __half q2 = __double2half(n2 - (double)__half2float(q1));
+        const __half q3 =
+            __double2half(n2 - (double)__half2float(q1) - (double)__half2float(q2));
+        if (!pad && c == 0 && !(n2 < 60000.0))
+            atomicOr(reinterpret_cast<unsigned*>(const_cast<float*>(scale)) + 2, 1u);
+        __align__(16) __half h[8];
+#pragma unroll
+        for (int q = 0; q < 8; ++q) {
+            const uint32_t k = c * 8 + q;
+            __half v = __float2half(0.0f);
+            if (pad) {
+                if (k >= 3 * D + 2 && k < 3 * D + 5) v = __float2half(65504.0f);
+            } else if (k < 3 * D) {
+                const uint32_t kk = k % D;
+                const float wv = -2.0f * (wj[kk] * s);
+                const __half whi = __float2half_rn(wv);
+                v = k < 2 * D ? whi : __float2half_rn(wv - __half2float(whi));
+            } else if (k == 3 * D || k == 3 * D + 1) {
+                v = __float2half(1.0f);
+            } else if (k == 3 * D + 2) {
+                v = q1;
+            } else if (k == 3 * D + 3) {
+                v = q2;
+            } else if (k == 3 * D + 4) {
+                v = q3;
+            }
+            h[q] = v;
+        }
+        uint8_t* base = wsplit + (size_t)g * gn * cores * 16;
+        *reinterpret_cast<uint4*>(base + ((size_t)c * gn + r) * 16) = *reinterpret_cast<uint4*>(h);
     }
 }
 
-// Candidate list of one (row, group): up to 4 local node indices (8 bits each)
-// whose computed value lies within thr of the group's best; count 15 = overflow.
-constexpr uint32_t kCandOverflow = 15u;
+void launch_prep_wsplit(int kind, const float* w, uint32_t P, uint32_t D, const float* scale,
+                        void* wsplit, cudaStream_t st) {
+    const uint32_t gn = tc_group_width(P);
+    const uint32_t groups = (P + gn - 1) / gn;
+    const uint32_t cores = kind == kTcTf32 ? kTcKPad / 4 : tc_geom(kind, D).kpad / 8;
+    const uint64_t total = (uint64_t)groups * gn * cores;
+    const unsigned blocks = (unsigned)((total + 255) / 256);
+    if (kind == kTcTf32)
+        TSOM_LAUNCH(k_prep_wsplit<kTcTf32><<<blocks, 256, 0, st>>>(
+            w, P, D, gn, groups, scale, static_cast<uint8_t*>(wsplit)));
+    else
+        TSOM_LAUNCH(k_prep_wsplit<kTcF16><<<blocks, 256, 0, st>>>(
+            w, P, D, gn, groups, scale, static_cast<uint8_t*>(wsplit)));
+}
 
-// kEnum = false (main pass): per (row, group) the top-2 (b1, i1, b2) only.
-// kEnum = true (near-tie rows only, see k_merge_fast): per (row, group) the best
-// value plus up to 8 local candidate ids within thr of it (count 15 = overflow),
-// enumerated only in the groups flagged relevant for the row (rmask).
+// ---------------------------------------------------------------------------
+// Split (optionally gathered) rows into A-operand tiles
+// ---------------------------------------------------------------------------
+//
+// Tile t (rows 128t..128t+127), row r, 16-byte K core c at byte
+// (c * 128 + r) * 16 (kTcTf32: hi half then lo half).  Rows past n are zero
+// (their results are ignored).  xn2[f] = ||x||^2 rounded up (unscaled): the
+// row's own error window (tie_thr).
+
+template <int kKind>
+__global__ void k_split_rows(const float* __restrict__ x, const uint32_t* __restrict__ sel,
+                             const uint32_t* __restrict__ idx, const uint32_t* __restrict__ dev_n,
+                             uint64_t n_host, uint32_t D, const float* __restrict__ scale,
+                             uint8_t* __restrict__ tiles, float* __restrict__ xn2) {
+    const uint64_t n = dev_n ? min((uint64_t)*dev_n, n_host) : n_host;
+    const uint64_t ntiles = (n + kTcTileM - 1) / kTcTileM;
+    const int r = threadIdx.x;  // 128 threads, one row each
+    const TcGeom geo = tc_geom(kKind, D);
+    const float s = kKind == kTcF16 ? scale[0] : 1.0f;
+    for (uint64_t tile = blockIdx.x; tile < ntiles; tile += gridDim.x) {
+        const uint64_t f = tile * kTcTileM + r;
+        uint8_t* base = tiles + tile * geo.tile_bytes;
+        const bool valid = f < n;
+        const float* src = nullptr;
+        if (valid) {
+            const uint64_t pos = idx ? (uint64_t)idx[f] : f;
+            src = x + (sel ? (uint64_t)sel[pos] : pos) * D;
+        }
+        double nrm = 0.0;
+        if (valid)
+            for (uint32_t k = 0; k < D; ++k) nrm += (double)src[k] * (double)src[k];
+        if (kKind == kTcTf32) {
+            // x' = [x | 1 | 1 | ||x||^2 | 0..]
+            float* fb = reinterpret_cast<float*>(base);
+            for (uint32_t kc = 0; kc < kTcKPad / 4; ++kc) {
+                float hi[4], lo[4];
+#pragma unroll
+                for (int q = 0; q < 4; ++q) {
+                    const uint32_t k = kc * 4 + q;
+                    float val = 0.0f;
+                    if (valid) {
+                        if (k < D) val = src[k];
+                        else if (k == D || k == D + 1) val = 1.0f;
+                        else if (k == D + 2) val = (float)nrm;
+                    }
+                    hi[q] = tf32_trunc(val);
+                    lo[q] = val - hi[q];
+                }
+                const size_t off = ((size_t)kc * kTcTileM + r) * 4;
+                *reinterpret_cast<float4*>(fb + off) = make_float4(hi[0], hi[1], hi[2], hi[3]);
+                *reinterpret_cast<float4*>(fb + (size_t)kTcTileM * kTcKPad + off) =
+                    make_float4(lo[0], lo[1], lo[2], lo[3]);
+            }
+        } else {
+            // A = [xh | xl | xh | n_hi, n_lo, 1, 1, 1 | 0..], x scaled by s
+            const double ns = nrm * (double)s * (double)s;
+            const __half nh = __double2half(ns);
+            const __half nl = __double2half(ns - (double)__half2float(nh));
+            for (uint32_t kc = 0; kc < geo.kpad / 8; ++kc) {
+                __align__(16) __half h[8];
+#pragma unroll
+                for (int q = 0; q < 8; ++q) {
+                    const uint32_t k = kc * 8 + q;
+                    __half v = __float2half(0.0f);
+                    if (valid) {
+                        if (k < 3 * D) {
+                            const float xv = src[k % D] * s;
+                            const __half xh = __float2half_rn(xv);
+                            v = (k >= D && k < 2 * D) ? __float2half_rn(xv - __half2float(xh)) : xh;
+                        } else if (k == 3 * D) {
+                            v = nh;
+                        } else if (k == 3 * D + 1) {
+                            v = nl;
+                        } else if (k < 3 * D + 5) {
+                            v = __float2half(1.0f);
+                        }
+                    }
+                    h[q] = v;
+                }
+                *reinterpret_cast<uint4*>(base + ((size_t)kc * kTcTileM + r) * 16) =
+                    *reinterpret_cast<uint4*>(h);
+            }
+        }
+        if (xn2 && valid) xn2[f] = (float)nrm * 1.0000003f;
+    }
+}
+
+void launch_split_rows(int kind, const float* x, const uint32_t* sel, const uint32_t* idx,
+                       uint64_t n, uint32_t D, const float* scale, void* tiles, float* xn2,
+                       cudaStream_t st, const uint32_t* dev_n) {
+    if (n == 0) return;
+    uint64_t tiles_n = (n + kTcTileM - 1) / kTcTileM;
+    if (tiles_n > 148ull * 64) tiles_n = 148ull * 64;
+    uint8_t* t = static_cast<uint8_t*>(tiles);
+    if (kind == kTcTf32)
+        TSOM_LAUNCH(k_split_rows<kTcTf32><<<(unsigned)tiles_n, kTcTileM, 0, st>>>(
+            x, sel, idx, dev_n, n, D, scale, t, xn2));
+    else
+        TSOM_LAUNCH(k_split_rows<kTcF16><<<(unsigned)tiles_n, kTcTileM, 0, st>>>(
+            x, sel, idx, dev_n, n, D, scale, t, xn2));
+}
+
+// ---------------------------------------------------------------------------
+// K1
+// ---------------------------------------------------------------------------
+
+// kEnum = false (main pass): per (row, group) the packed top-2 -> [B1 | i1 | B2]
+//   (B1, B2 with the 8 id bits cleared).
+// kEnum = true (near-tie rows only, see k_merge_fast): per (row, group) the raw
+// best value plus up to 8 local candidate ids within tie_thr of it (count 15 =
+// overflow, 0 = group not relevant for the row (rmask)).
 // dev_n (optional): row count read on the device (the near-tie list length).
-template <bool kEnum>
+template <int kKind, bool kEnum>
 __global__ void __launch_bounds__(kThreads, 1)
-    k1_bmu_tc(const float* __restrict__ tiles, uint64_t n_host, const uint32_t* __restrict__ dev_n,
-              uint32_t groups, uint32_t gn, const float* __restrict__ wsplit,
-              const float* __restrict__ xn2, const float* __restrict__ w2max, float tau,
-              const uint32_t* __restrict__ rmask, float* __restrict__ part) {
+    k1_bmu_tc(const uint8_t* __restrict__ tiles, uint64_t n_host, const uint32_t* __restrict__ dev_n,
+              uint32_t groups, uint32_t gn, uint32_t D, uint32_t stages,
+              const uint8_t* __restrict__ wsplit, const float* __restrict__ xn2,
+              const float* __restrict__ w2max, const float* __restrict__ scale, TieWin win,
+              const uint32_t* __restrict__ rmask, float* __restrict__ part, uint32_t one,
+              uint32_t neg1, uint32_t dbg) {
+    // one = 1, neg1 = 0xFFFFFFFF at run time: opaque to the compiler, so the
+    // epilogue's integer adds stay IMADs (FMA pipe) instead of IADD3 (ALU pipe)
     extern __shared__ __align__(1024) uint8_t smem[];
-    const uint64_t n = dev_n ? min((uint64_t)*dev_n, n_host) : n_host;  // n_host caps dev_n
+    const TcGeom geo = tc_geom(kKind, D);
+    const uint64_t n = dev_n ? min((uint64_t)*dev_n, n_host) : n_host;
     const uint32_t ntiles = (uint32_t)((n + kTcTileM - 1) / kTcTileM);
-    const uint32_t w_bytes = 2u * kTcKPad * gn * 4u;  // hi + lo of this CTA's group
+    const uint32_t w_bytes = gn * geo.row_bytes;  // this CTA's group (both halves for tf32)
     uint8_t* sW = smem;
     uint8_t* sX = smem + ((w_bytes + 1023u) & ~1023u);
-    uint64_t* bars = reinterpret_cast<uint64_t*>(sX + kStages * kTileBytes);
-    uint64_t* full_bar = bars;        // [kStages] X tile landed
-    uint64_t* empty_bar = bars + 2;   // [kStages] MMAs done with X tile
-    uint64_t* tfull_bar = bars + 4;   // [2] accumulator ready
-    uint64_t* tempty_bar = bars + 6;  // [2] accumulator drained
-    uint64_t* w_bar = bars + 8;       // codebook group landed
-    uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(bars + 9);
+    uint64_t* bars = reinterpret_cast<uint64_t*>(sX + stages * geo.tile_bytes);
+    uint64_t* full_bar = bars;                    // [stages] X tile landed
+    uint64_t* empty_bar = bars + kMaxStages;      // [stages] MMAs done with X tile
+    uint64_t* tfull_bar = bars + 2 * kMaxStages;  // [2] accumulator ready
+    uint64_t* tempty_bar = tfull_bar + 2;         // [2] accumulator drained
+    uint64_t* w_bar = tfull_bar + 4;              // codebook group landed
+    uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(w_bar + 1);
+    // w_bar + 2 .. : [2][kSets-1][128] float2 set-h -> set-0 exchange (main pass)
 
     const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
     const uint32_t g = blockIdx.x % groups;
@@ -204,13 +367,13 @@ __global__ void __launch_bounds__(kThreads, 1)
     const uint32_t acc_cols = gn <= 32 ? 32 : (gn <= 64 ? 64 : (gn <= 128 ? 128 : 256));
 
     if (threadIdx.x == 0) {
-        for (int s = 0; s < kStages; ++s) {
+        for (uint32_t s = 0; s < stages; ++s) {
             mbar_init(&full_bar[s], 1);
             mbar_init(&empty_bar[s], 1);
         }
         for (int a = 0; a < 2; ++a) {
             mbar_init(&tfull_bar[a], 1);
-            mbar_init(&tempty_bar[a], kEpiThreads);
+            mbar_init(&tempty_bar[a], kEnum ? kEpiThreads : kSets * kEpiThreads);
         }
         mbar_init(w_bar, 1);
         asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
@@ -228,18 +391,22 @@ __global__ void __launch_bounds__(kThreads, 1)
 
     if (warp == 0) {
         if (lane == 0 && ntiles > cta_in_group) {
-            // resident codebook group (hi and lo halves, each < 2^20 B of tx count)
+            // resident codebook group, in <= 64 KB bulk copies
             mbar_expect_tx(w_bar, w_bytes);
-            const float* wg = wsplit + (size_t)g * 2 * kTcKPad * gn;
-            bulk_g2s(sW, wg, w_bytes / 2, w_bar);
-            bulk_g2s(sW + w_bytes / 2, wg + (size_t)kTcKPad * gn, w_bytes / 2, w_bar);
+            const uint8_t* wg = wsplit + (size_t)g * w_bytes;
+            for (uint32_t off = 0; off < w_bytes; off += 65536u)
+                bulk_g2s(sW + off, wg + off, min(65536u, w_bytes - off), w_bar);
             uint32_t stage = 0, phase = 0;
             for (uint32_t t = cta_in_group; t < ntiles; t += ctas_per_group) {
                 mbar_wait(&empty_bar[stage], phase ^ 1);
-                mbar_expect_tx(&full_bar[stage], kTileBytes);
-                bulk_g2s(sX + stage * kTileBytes, tiles + (size_t)t * (kTileBytes / 4), kTileBytes,
-                         &full_bar[stage]);
-                if (++stage == kStages) {
+                if (dbg & 4u) {
+                    mbar_arrive(&full_bar[stage]);
+                } else {
+                    mbar_expect_tx(&full_bar[stage], geo.tile_bytes);
+                    bulk_g2s(sX + stage * geo.tile_bytes, tiles + (size_t)t * geo.tile_bytes,
+                             geo.tile_bytes, &full_bar[stage]);
+                }
+                if (++stage == stages) {
                     stage = 0;
                     phase ^= 1;
                 }
@@ -247,10 +414,10 @@ __global__ void __launch_bounds__(kThreads, 1)
         }
     } else if (warp == 1) {
         if (lane == 0 && ntiles > cta_in_group) {
-            const uint32_t idesc = idesc_tf32(kTcTileM, gn);
+            const uint32_t idesc = kKind == kTcTf32 ? idesc_tf32(kTcTileM, gn)
+                                                    : idesc_f16(kTcTileM, gn);
             const uint32_t w_lbo = gn * 16u;
             const uint32_t sw = smem_u32(sW);
-            const uint32_t sw_lo = sw + w_bytes / 2;
             mbar_wait(w_bar, 0);
             uint32_t stage = 0, phase = 0, acc = 0, acc_phase = 0;
             for (uint32_t t = cta_in_group; t < ntiles; t += ctas_per_group) {
@@ -258,21 +425,30 @@ __global__ void __launch_bounds__(kThreads, 1)
                 mbar_wait(&full_bar[stage], phase);
                 tc_fence_after();
                 const uint32_t d = tmem_base + acc * acc_cols;
-                const uint32_t sx = smem_u32(sX + stage * kTileBytes);
-                const uint32_t sx_lo = sx + kHalfTile;
+                const uint32_t sx = smem_u32(sX + stage * geo.tile_bytes);
+                if (dbg & 2u) {
+                } else if (kKind == kTcTf32) {
+                    const uint32_t sx_lo = sx + geo.tile_bytes / 2;
+                    const uint32_t sw_lo = sw + w_bytes / 2;
 #pragma unroll
-                for (int k = 0; k < kKSteps; ++k) {
-                    const uint64_t ah = umma_desc(sx + k * 4096u, 2048u, 128u);
-                    const uint64_t al = umma_desc(sx_lo + k * 4096u, 2048u, 128u);
-                    const uint64_t bh = umma_desc(sw + k * 2u * w_lbo, w_lbo, 128u);
-                    const uint64_t bl = umma_desc(sw_lo + k * 2u * w_lbo, w_lbo, 128u);
-                    mma_tf32(d, ah, bh, idesc, k > 0 ? 1u : 0u);
-                    mma_tf32(d, al, bh, idesc, 1u);
-                    mma_tf32(d, ah, bl, idesc, 1u);
+                    for (int k = 0; k < kTcKPad / 8; ++k) {
+                        const uint64_t ah = umma_desc(sx + k * 4096u, 2048u, 128u);
+                        const uint64_t al = umma_desc(sx_lo + k * 4096u, 2048u, 128u);
+                        const uint64_t bh = umma_desc(sw + k * 2u * w_lbo, w_lbo, 128u);
+                        const uint64_t bl = umma_desc(sw_lo + k * 2u * w_lbo, w_lbo, 128u);
+                        mma_tf32(d, ah, bh, idesc, k > 0 ? 1u : 0u);
+                        mma_tf32(d, al, bh, idesc, 1u);
+                        mma_tf32(d, ah, bl, idesc, 1u);
+                    }
+                } else {
+                    for (uint32_t k = 0; k < geo.ksteps; ++k)
+                        mma_f16(d, umma_desc(sx + k * 4096u, 2048u, 128u),
+                                umma_desc(sw + k * 2u * w_lbo, w_lbo, 128u), idesc,
+                                k > 0 ? 1u : 0u);
                 }
                 mma_commit(&empty_bar[stage]);  // X stage free once these MMAs retire
                 mma_commit(&tfull_bar[acc]);    // accumulator ready for the epilogue
-                if (++stage == kStages) {
+                if (++stage == stages) {
                     stage = 0;
                     phase ^= 1;
                 }
@@ -283,73 +459,144 @@ __global__ void __launch_bounds__(kThreads, 1)
             }
         }
     } else if (warp >= 4) {
-        // 2 sets x 4 epilogue warps: set s drains accumulator buffer s (every
-        // other tile), so two warps per SM sub-partition hide each other's
-        // latency without exchanging anything.  Warp (set, q) owns TMEM lanes
-        // 32q..32q+31 (= tile rows) and all gn columns; thread = row.
+        // Epilogue.  Warp (set, q) owns TMEM lanes 32q..32q+31 (= tile rows).
+        //   main pass: both sets drain every tile, set h taking half of the
+        //     32-column chunks; set 1 hands its per-row top-2 to set 0 through
+        //     shared memory (named barrier per lane quarter), set 0 merges.
+        //   enumerate pass: set s drains accumulator buffer s (every other tile)
+        //     over all gn columns.
         const uint32_t q = warp & 3, set = (warp - 4) >> 2;
         const uint32_t row = q * 32 + lane;
-        const uint32_t nfull = gn / 32, tail16 = (gn % 32) != 0;
-        const uint32_t acc = set;
-        uint32_t acc_phase = 0;
-        for (uint32_t t = cta_in_group + set * ctas_per_group; t < ntiles;
-             t += 2 * ctas_per_group) {
+        const uint32_t nch = gn / 32;  // gn is a multiple of 32 (tc_group_width)
+        const float S = scale[1];
+        uint32_t mask;
+        asm volatile("mov.b32 %0, 0xFFFFFF00;" : "=r"(mask));  // register operand of the LOP3
+        // main pass: set h takes chunks [h nch / kSets, (h+1) nch / kSets)
+        const uint32_t c_begin = kEnum ? 0 : set * nch / kSets;
+        const uint32_t c_count = kEnum ? nch : (set + 1) * nch / kSets - c_begin;
+        uint32_t acc = kEnum ? set : 0, acc_phase = 0;
+        // (enumerate pass: sets 0 and 1 alternate tiles, the other sets idle)
+        const uint32_t t0 =
+            kEnum ? (set < 2 ? cta_in_group + set * ctas_per_group : ntiles) : cta_in_group;
+        const uint32_t tstep = kEnum ? 2 * ctas_per_group : ctas_per_group;
+        for (uint32_t t = t0; t < ntiles; t += tstep) {
             mbar_wait(&tfull_bar[acc], acc_phase);
             tc_fence_after();
-            const uint32_t taddr = tmem_base + ((q * 32u) << 16) + acc * acc_cols;
-            // pass 1: eight independent top-2 streams (ILP), TMEM loads pipelined
-            float b1[8], b2[8];
-            uint32_t i1[8];
+            const uint32_t taddr = tmem_base + ((q * 32u) << 16) + acc * acc_cols + c_begin * 32;
+            uint32_t ra[32], rb[32];
+            float b1[4], b2[4];
+            uint32_t b1k[4];  // main pass: packed running best (integer view)
 #pragma unroll
-            for (int s2 = 0; s2 < 8; ++s2) {
+            for (int s2 = 0; s2 < 4; ++s2) {
                 b1[s2] = CUDART_INF_F;
                 b2[s2] = CUDART_INF_F;
-                i1[s2] = 0;
+                b1k[s2] = 0x7F800000u;
             }
-            uint32_t ra[32], rb[32];
-            if (nfull) TMEM_LD32(taddr, ra);
-            for (uint32_t c = 0; c < nfull; c += 2) {
-                tmem_wait_ld();
-                if (c + 1 < nfull) TMEM_LD32(taddr + (c + 1) * 32, rb);
+            // one 32-column chunk, ids relative to c_begin (compile-time base cb)
+#define TSOM_CHUNK(r, cb)                                                                   \
+    do {                                                                                    \
+        _Pragma("unroll") for (int m = 0; m < 16; ++m) {                                    \
+            const int s_ = m & 3;                                                           \
+            if (kEnum) {                                                                    \
+                b1[s_] = fmin3f(b1[s_], __uint_as_float(r[2 * m]),                          \
+                                __uint_as_float(r[2 * m + 1]));                             \
+            } else {                                                                        \
+                uint32_t ka, kb;                                                            \
+                asm("lop3.b32 %0, %1, %2, %3, 0xEC;"                                        \
+                    : "=r"(ka)                                                              \
+                    : "r"(r[2 * m]), "r"((uint32_t)((cb) + 2 * m)), "r"(mask));            \
+                asm("lop3.b32 %0, %1, %2, %3, 0xEC;"                                        \
+                    : "=r"(kb)                                                              \
+                    : "r"(r[2 * m + 1]), "r"((uint32_t)((cb) + 2 * m + 1)), "r"(mask));    \
+                /* hi/t on the ALU pipe (FMNMX); lo = a + b - hi and b1' = b1 + lo - t */ \
+                /* as integer IMADs on the FMA pipe ({lo, hi} = {a, b} bit-exactly)   */ \
+                const uint32_t hi = __float_as_uint(fmaxf(__uint_as_float(ka),             \
+                                                          __uint_as_float(kb)));            \
+                const uint32_t lo = ka * one + kb + hi * neg1;                              \
+                const uint32_t tt = __float_as_uint(fmaxf(__uint_as_float(b1k[s_]),         \
+                                                          __uint_as_float(lo)));            \
+                b1k[s_] = b1k[s_] * one + lo + tt * neg1;                                   \
+                b2[s_] = fmin3f(b2[s_], __uint_as_float(tt), __uint_as_float(hi));          \
+            }                                                                               \
+        }                                                                                   \
+    } while (0)
+            const uint32_t c_count_eff = (dbg & 1u) ? 0u : c_count;
+            const bool ld_on = !(dbg & 8u);
+            if (!ld_on) {
 #pragma unroll
-                for (int k = 0; k < 32; ++k)
-                    top2_step(__uint_as_float(ra[k]), c * 32 + k, b1[k & 7], i1[k & 7], b2[k & 7]);
-                if (c + 1 < nfull) {
-                    tmem_wait_ld();
-                    if (c + 2 < nfull) TMEM_LD32(taddr + (c + 2) * 32, ra);
-#pragma unroll
-                    for (int k = 0; k < 32; ++k)
-                        top2_step(__uint_as_float(rb[k]), (c + 1) * 32 + k, b1[k & 7], i1[k & 7],
-                                  b2[k & 7]);
+                for (int k = 0; k < 32; ++k) {
+                    ra[k] = 0x3F800000u + (row << 8) + k * 977u + t;
+                    rb[k] = ra[k] ^ 0x5A5A5Au;
                 }
             }
-            if (tail16) {
-                uint32_t r[16];
-                TMEM_LD16(taddr + nfull * 32, r);
-                tmem_wait_ld();
+            if (c_count_eff && ld_on) TSOM_TMEM_LD32(taddr, ra);
 #pragma unroll
-                for (int k = 0; k < 16; ++k)
-                    top2_step(__uint_as_float(r[k]), nfull * 32 + k, b1[k & 7], i1[k & 7], b2[k & 7]);
+            for (int c = 0; c < (kEnum ? 8 : 4); c += 2) {
+                if ((uint32_t)c < c_count_eff) {
+                    if (ld_on) {
+                        tmem_wait_ld();
+                        if ((uint32_t)c + 1 < c_count_eff) TSOM_TMEM_LD32(taddr + (c + 1) * 32, rb);
+                    }
+                    TSOM_CHUNK(ra, c * 32);
+                }
+                if ((uint32_t)c + 1 < c_count_eff) {
+                    if (ld_on) {
+                        tmem_wait_ld();
+                        if ((uint32_t)c + 2 < c_count_eff) TSOM_TMEM_LD32(taddr + (c + 2) * 32, ra);
+                    }
+                    TSOM_CHUNK(rb, (c + 1) * 32);
+                }
             }
+#undef TSOM_CHUNK
+            const uint64_t pos = (uint64_t)t * kTcTileM + row;
+            if (!kEnum) {
+                tc_fence_before();
+                mbar_arrive(&tempty_bar[acc]);  // this thread is done with the accumulator
+                // merge the 4 streams (packed keys compare as floats)
+                float k1 = __uint_as_float(b1k[0]), k2 = b2[0];
 #pragma unroll
-            for (int s2 = 1; s2 < 8; ++s2)
-                top2_merge_dev(b1[0], i1[0], b2[0], b1[s2], i1[s2], b2[s2]);
-            const float B1 = b1[0], B2 = b2[0];
-            const uint32_t I1 = i1[0];
-            uint32_t w1 = I1, w2 = __float_as_uint(B2), w3 = 1;
-            if (kEnum) {
+                for (int s2 = 1; s2 < 4; ++s2) {
+                    const float o1 = __uint_as_float(b1k[s2]);
+                    const float tt = fmaxf(k1, o1);
+                    k1 = fminf(k1, o1);
+                    k2 = fmin3f(k2, b2[s2], tt);
+                }
+                // ids are relative to the set's first chunk (no carry: id < 256)
+                if (c_begin && c_count) k1 = __uint_as_float(__float_as_uint(k1) + c_begin * 32);
+                float2* xch = reinterpret_cast<float2*>(w_bar + 2) + acc * (kSets - 1) * kTcTileM;
+                if (dbg & 16u) {
+                    if (k1 == 1.2345f && k2 == 3.0f) part[0] = 0.0f;  // keep the math alive
+                } else {
+                if (set) xch[(set - 1) * kTcTileM + row] = make_float2(k1, k2);
+                asm volatile("bar.sync %0, %1;" ::"r"(1 + q), "n"(32 * kSets) : "memory");
+                if (!set) {
+#pragma unroll
+                    for (int o2 = 0; o2 < kSets - 1; ++o2) {
+                        const float2 o = xch[o2 * kTcTileM + row];
+                        const float tt = fmaxf(k1, o.x);
+                        k1 = fminf(k1, o.x);
+                        k2 = fmin3f(k2, o.y, tt);
+                    }
+                    if (pos < n) {
+                        const uint32_t kb1 = __float_as_uint(k1);
+                        float* pg = part + (size_t)g * 3 * n;
+                        pg[pos] = __uint_as_float(kb1 & 0xFFFFFF00u);
+                        pg[n + pos] = __uint_as_float(kb1 & 0xFFu);
+                        pg[2 * n + pos] = __uint_as_float(__float_as_uint(k2) & 0xFFFFFF00u);
+                    }
+                }
+                }
+            } else {
+                const float B1 = fminf(fminf(b1[0], b1[1]), fminf(b1[2], b1[3]));
                 // enumerate the row's candidates v <= B1 + thr in ascending j
-                const uint64_t prow = (uint64_t)t * kTcTileM + row;
-                const bool relevant = prow < n && ((__ldg(rmask + prow) >> (g & 31)) & 1u);
-                const float thr = relevant ? tau * (__ldg(xn2 + prow) + __ldg(w2max)) : 0.0f;
-                const bool need = relevant && !(B2 - B1 > thr);
-                w2 = 0;
+                const bool need = pos < n && ((__ldg(rmask + pos) >> (g & 31)) & 1u);
+                const float thr = need ? tie_thr(__ldg(xn2 + pos), __ldg(w2max), S, win) : 0.0f;
+                const float lim = B1 + thr;
+                uint32_t pk0 = 0, pk1 = 0, nc = 0;
                 if (__any_sync(0xffffffffu, need)) {
-                    const float lim = B1 + thr;
-                    uint32_t pk0 = 0, pk1 = 0, nc = 0;
                     for (uint32_t cc = 0; cc < gn; cc += 16) {
                         uint32_t r[16];
-                        TMEM_LD16(taddr + cc, r);
+                        TSOM_TMEM_LD16(taddr + cc, r);
                         tmem_wait_ld();
 #pragma unroll
                         for (int k = 0; k < 16; ++k) {
@@ -361,24 +608,24 @@ __global__ void __launch_bounds__(kThreads, 1)
                             }
                         }
                     }
-                    if (need) {
-                        w1 = pk0;
-                        w2 = pk1;
-                        w3 = (nc >= 1 && nc <= 8) ? nc : kCandOverflow;
-                    }
+                }
+                tc_fence_before();
+                mbar_arrive(&tempty_bar[acc]);  // this thread is done with the accumulator
+                if (pos < n) {
+                    float* pg = part + (size_t)g * 4 * n;
+                    pg[pos] = B1;
+                    pg[n + pos] = __uint_as_float(pk0);
+                    pg[2 * n + pos] = __uint_as_float(pk1);
+                    pg[3 * n + pos] =
+                        __uint_as_float(!need ? 0u : ((nc >= 1 && nc <= 8) ? nc : kCandOverflow));
                 }
             }
-            tc_fence_before();
-            mbar_arrive(&tempty_bar[acc]);  // this thread is done with the accumulator
-            const uint64_t pos = (uint64_t)t * kTcTileM + row;
-            if (pos < n) {
-                float* pg = part + (size_t)g * (kEnum ? 4 : 3) * n;
-                pg[pos] = B1;
-                pg[n + pos] = __uint_as_float(w1);
-                pg[2 * n + pos] = __uint_as_float(w2);
-                if (kEnum) pg[3 * n + pos] = __uint_as_float(w3);
+            if (kEnum) {
+                acc_phase ^= 1;
+            } else if (++acc == 2) {
+                acc = 0;
+                acc_phase ^= 1;
             }
-            acc_phase ^= 1;
         }
     }
     tc_fence_before();
@@ -390,13 +637,17 @@ __global__ void __launch_bounds__(kThreads, 1)
     }
 }
 
-bool tc_supported(uint32_t P, uint32_t D) { return P >= 1 && D + 2 <= (uint32_t)kTcKPad; }
+// diagnostics only (option 99): bit0 skips the epilogue math, bit1 the MMAs,
+// bit2 the A-tile loads, so the stages can be timed in isolation
+uint32_t g_k1_debug = 0;
 
-cudaError_t launch_bmu_tc(const float* tiles, uint64_t n, const uint32_t* dev_n, bool enumerate,
-                          uint32_t P, const float* wsplit, const float* xn2,
-                          const float* w2max, float tau, const uint32_t* rmask, float* part,
-                          int sm_count, cudaStream_t st) {
+cudaError_t launch_bmu_tc(int kind, const void* tiles, uint64_t n, const uint32_t* dev_n,
+                          bool enumerate, uint32_t P, uint32_t D, const void* wsplit,
+                          const float* xn2, const float* w2max, const float* scale, TieWin win,
+                          const uint32_t* rmask, float* part, int sm_count, size_t smem_optin,
+                          cudaStream_t st) {
     if (n == 0) return cudaSuccess;
+    const TcGeom geo = tc_geom(kind, D);
     const uint32_t gn = tc_group_width(P);
     const uint32_t groups = (P + gn - 1) / gn;
     const uint32_t ntiles = (uint32_t)((n + kTcTileM - 1) / kTcTileM);  // upper bound
@@ -404,18 +655,35 @@ cudaError_t launch_bmu_tc(const float* tiles, uint64_t n, const uint32_t* dev_n,
     if (per_group < 1) per_group = 1;
     if (per_group > ntiles) per_group = ntiles;
     const uint32_t grid = per_group * groups;
-    const uint32_t w_bytes = 2u * kTcKPad * gn * 4u;
-    const size_t smem = ((w_bytes + 1023u) & ~1023u) + kStages * kTileBytes + 80;
-    auto kern = enumerate ? k1_bmu_tc<true> : k1_bmu_tc<false>;
-    static size_t attr[2] = {0, 0};
-    if (attr[enumerate] < smem) {
+    const uint32_t w_bytes = gn * geo.row_bytes;
+    const size_t fixed = ((w_bytes + 1023u) & ~1023u) + 128 + 2 * (kSets - 1) * kTcTileM * 8;
+    uint32_t stages = 2;
+    while (stages < 3 && fixed + (size_t)(stages + 1) * geo.tile_bytes <= smem_optin) ++stages;
+    const size_t smem = fixed + (size_t)stages * geo.tile_bytes;
+    if (smem > smem_optin) return cudaErrorInvalidConfiguration;
+    using KernT = void (*)(const uint8_t*, uint64_t, const uint32_t*, uint32_t, uint32_t, uint32_t,
+                           uint32_t, const uint8_t*, const float*, const float*, const float*,
+                           TieWin, const uint32_t*, float*, uint32_t, uint32_t, uint32_t);
+    KernT kern;
+    int slot;
+    if (kind == kTcTf32) {
+        kern = enumerate ? k1_bmu_tc<kTcTf32, true> : k1_bmu_tc<kTcTf32, false>;
+        slot = enumerate ? 1 : 0;
+    } else {
+        kern = enumerate ? k1_bmu_tc<kTcF16, true> : k1_bmu_tc<kTcF16, false>;
+        slot = enumerate ? 3 : 2;
+    }
+    static size_t attr[4] = {0, 0, 0, 0};
+    if (attr[slot] < smem) {
         cudaError_t e = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize,
                                              (int)smem);
         if (e != cudaSuccess) return e;
-        attr[enumerate] = smem;
+        attr[slot] = smem;
     }
-    TSOM_LAUNCH(kern<<<grid, kThreads, smem, st>>>(tiles, n, dev_n, groups, gn, wsplit, xn2,
-                                                   w2max, tau, rmask, part));
+    TSOM_LAUNCH(kern<<<grid, kThreads, smem, st>>>(
+        static_cast<const uint8_t*>(tiles), n, dev_n, groups, gn, D, stages,
+        static_cast<const uint8_t*>(wsplit), xn2, w2max, scale, win, rmask, part, 1u,
+        0xFFFFFFFFu, g_k1_debug));
     return cudaGetLastError();
 }
 

@@ -22,18 +22,11 @@ namespace tsom {
 // Codebook prep (once per codebook change)
 // ---------------------------------------------------------------------------
 
-// tf32 truncation: keep 10 explicit mantissa bits (the MMA ignores the low 13)
-__device__ __forceinline__ float tf32_hi(float v) {
-    return __uint_as_float(__float_as_uint(v) & 0xFFFFE000u);
-}
-
-// Split an augmented row (values v[0..kpad)) into tcgen05 K-major core-matrix
-// layout: element (row r, k) of a [rows]-row tile lives at
-//   ((k / 4) * rows + r) * 4 + (k % 4)      (hi part; lo part follows after rows*kpad)
+// SIMT operand wt ((d+1) x Ppad: -2 w^T and the ||w||^2 row), FP64 norms w2
+// and max ||w||^2 (the error window).
 __global__ void k_prep_codebook(const float* __restrict__ w, uint32_t P, uint32_t D,
                                 double* __restrict__ w2, float* __restrict__ w2max,
-                                float* __restrict__ wt, uint32_t Ppad,
-                                float* __restrict__ wsplit) {
+                                float* __restrict__ wt, uint32_t Ppad) {
     const uint32_t j = blockIdx.x * blockDim.x + threadIdx.x;
     if (j >= Ppad) return;
     if (j >= P) {  // padding node: never wins
@@ -45,69 +38,15 @@ __global__ void k_prep_codebook(const float* __restrict__ w, uint32_t P, uint32_
     double s = 0.0;
     for (uint32_t k = 0; k < D; ++k) s = __dadd_rn(s, __dmul_rn((double)wj[k], (double)wj[k]));
     w2[j] = s;
-    atomicMax(reinterpret_cast<int*>(w2max), __float_as_int((float)s));
+    atomicMax(reinterpret_cast<int*>(w2max), __float_as_int((float)s * 1.0000003f));
     for (uint32_t k = 0; k < D; ++k) wt[(size_t)k * Ppad + j] = -2.0f * wj[k];
     wt[(size_t)D * Ppad + j] = (float)s;
-    if (wsplit) {
-        // group g = j / 256 holds [hi: 14 x 256 x 4][lo: 14 x 256 x 4].  Columns
-        // k < D carry -2 w_jk split hi/lo; columns D and D+1 carry ||w_j||^2 as
-        // three tf32-exact pieces (p1 hi/p2 lo in column D, p3 hi in column D+1)
-        // so the norm enters the MMA with ~33 significant bits.
-        const uint32_t gn = tc_group_width(P);
-        const uint32_t g = j / gn, r = j % gn;
-        float* base = wsplit + (size_t)g * 2 * gn * kTcKPad;
-        const float p1 = tf32_hi((float)s);
-        const float p2 = tf32_hi((float)(s - (double)p1));
-        const float p3 = tf32_hi((float)(s - (double)p1 - (double)p2));
-        for (uint32_t k = 0; k < kTcKPad; ++k) {
-            float hi, lo;
-            if (k < D) {
-                const float v = -2.0f * wj[k];
-                hi = tf32_hi(v);
-                lo = v - hi;
-            } else if (k == D) {
-                hi = p1;
-                lo = p2;
-            } else if (k == D + 1) {
-                hi = p3;
-                lo = 0.0f;
-            } else {
-                hi = 0.0f;
-                lo = 0.0f;
-            }
-            const size_t off = ((size_t)(k / 4) * gn + r) * 4 + (k % 4);
-            base[off] = hi;
-            base[(size_t)gn * kTcKPad + off] = lo;
-        }
-    }
-}
-
-__global__ void k_prep_pad_groups(uint32_t P, uint32_t D, float* __restrict__ wsplit,
-                                  uint32_t groups) {
-    // padding nodes of the last tcgen05 group: norm column = 3e38 (finite, so
-    // 0 * v never makes a NaN inside the MMA), everything else 0 => never wins
-    const uint32_t gn = tc_group_width(P);
-    const uint32_t j = P + blockIdx.x * blockDim.x + threadIdx.x;
-    if (j >= groups * gn) return;
-    const uint32_t g = j / gn, r = j % gn;
-    float* base = wsplit + (size_t)g * 2 * gn * kTcKPad;
-    for (uint32_t k = 0; k < kTcKPad; ++k) {
-        const size_t off = ((size_t)(k / 4) * gn + r) * 4 + (k % 4);
-        base[off] = k == D ? tf32_hi(3.0e38f) : 0.0f;
-        base[(size_t)gn * kTcKPad + off] = 0.0f;
-    }
 }
 
 void launch_prep_codebook(const float* w, uint32_t P, uint32_t D, double* w2, float* w2max,
-                          float* wt, uint32_t Ppad, float* wsplit, cudaStream_t st) {
+                          float* wt, uint32_t Ppad, cudaStream_t st) {
     cudaMemsetAsync(w2max, 0, sizeof(float), st);
-    TSOM_LAUNCH(k_prep_codebook<<<(Ppad + 127) / 128, 128, 0, st>>>(w, P, D, w2, w2max, wt, Ppad, wsplit));
-    if (wsplit) {
-        const uint32_t gn = tc_group_width(P);
-        const uint32_t groups = (P + gn - 1) / gn;
-        const uint32_t pad = groups * gn - P;
-        if (pad) TSOM_LAUNCH(k_prep_pad_groups<<<(pad + 127) / 128, 128, 0, st>>>(P, D, wsplit, groups));
-    }
+    TSOM_LAUNCH(k_prep_codebook<<<(Ppad + 127) / 128, 128, 0, st>>>(w, P, D, w2, w2max, wt, Ppad));
 }
 
 // ---------------------------------------------------------------------------
@@ -297,17 +236,20 @@ __device__ __forceinline__ double exact_d2(const float* __restrict__ x,
     return acc;
 }
 
-// Main-pass merge.  part[g] = [b1 | i1 | b2] per row (k1_bmu_tc<false>).  A row
-// whose global best is separated from every other node by more than the FP32
-// error window thr gets its BMU here; otherwise its position joins `ties`
-// ([0] = count, positions from [1]) for the enumerate pass.
+// Main-pass merge.  part[g] = [B1 | i1 | B2] per row (k1_bmu_tc<.., false>,
+// packed-key values: the id bits cleared).  A row whose global best is
+// separated from every other node by more than the error window gets its BMU
+// here; otherwise its position joins `ties` ([0] = count, positions from [1])
+// for the enumerate pass, with the bitmask of groups inside the window.  If the
+// FP16 codebook operand overflowed (scale[2] != 0) every row goes to the full
+// exact re-scan (flags).
 __global__ void __launch_bounds__(256, 8) k_merge_fast(
     const float* __restrict__ part, uint64_t n, uint32_t groups, uint32_t gn,
-    const float* __restrict__ xn2, const float* __restrict__ w2max, float tau,
-    uint32_t* __restrict__ bmu, uint32_t* __restrict__ ties, uint32_t* __restrict__ tmask) {
+    const float* __restrict__ xn2, const float* __restrict__ w2max,
+    const float* __restrict__ scale, TieWin win, uint32_t* __restrict__ bmu,
+    uint32_t* __restrict__ ties, uint32_t* __restrict__ tmask, uint32_t* __restrict__ flags) {
     const uint64_t i = blockIdx.x * (uint64_t)blockDim.x + threadIdx.x;
     if (i >= n) return;
-    const float thr = tau * (__ldg(xn2 + i) + __ldg(w2max));
     float B1 = CUDART_INF_F, B2 = CUDART_INF_F;
     uint32_t I1 = 0;
     for (uint32_t g = 0; g < groups; ++g) {  // ascending groups = ascending node ids
@@ -316,6 +258,13 @@ __global__ void __launch_bounds__(256, 8) k_merge_fast(
                    __ldg(pg + 2 * n + i));
     }
     bmu[i] = I1;
+    if (__float_as_uint(__ldg(scale + 2)) != 0u) {
+        const uint32_t slot = atomicAdd(&flags[0], 1u);
+        flags[2 + slot] = (uint32_t)i;
+        return;
+    }
+    const float thr = tie_thr(__ldg(xn2 + i), __ldg(w2max), __ldg(scale + 1), win) +
+                      win.quant * (fabsf(B1) + fminf(fabsf(B2), 3.0e37f));
     if (!(B2 - B1 > thr)) {
         // groups whose best lies inside the window (bit g; > 32 groups: all)
         uint32_t mask = 0xFFFFFFFFu;
@@ -332,24 +281,27 @@ __global__ void __launch_bounds__(256, 8) k_merge_fast(
 }
 
 void launch_merge_fast(const float* part, uint64_t n, uint32_t groups, uint32_t gn,
-                       const float* xn2, const float* w2max, float tau, uint32_t* bmu,
-                       uint32_t* ties, uint32_t* tmask, cudaStream_t st) {
+                       const float* xn2, const float* w2max, const float* scale, TieWin win,
+                       uint32_t* bmu, uint32_t* ties, uint32_t* tmask, uint32_t* flags,
+                       cudaStream_t st) {
     if (n == 0) return;
     TSOM_LAUNCH(k_merge_fast<<<(unsigned)((n + 255) / 256), 256, 0, st>>>(
-        part, n, groups, gn, xn2, w2max, tau, bmu, ties, tmask));
+        part, n, groups, gn, xn2, w2max, scale, win, bmu, ties, tmask, flags));
 }
 
 
 // Enumerate-pass merge over the near-tie rows f < n (position ties[f]).
-// part[g] = [b1 | ids 0-3 | ids 4-7 | count] (k1_bmu_tc<true>, 8-bit local ids).
-// One candidate -> bmu; several -> exact FP64 distances of just those nodes in
-// ascending node order with strict < (lowest index wins), as find_bmus
-// (trainer.hpp:293-304); > 8 candidates in a group -> full exact re-scan list.
+// part[g] = [raw b1 | ids 0-3 | ids 4-7 | count] (k1_bmu_tc<.., true>, 8-bit
+// local ids, count 0 = group not enumerated).  One candidate -> bmu; several
+// -> exact FP64 distances of just those nodes in ascending node order with
+// strict < (lowest index wins), as find_bmus (trainer.hpp:293-304); > 8
+// candidates in a group -> full exact re-scan list.
 __global__ void k_merge_partials(const float* __restrict__ part, const uint32_t* __restrict__ ties,
                                  const uint32_t* __restrict__ dev_count, uint64_t cap,
                                  uint32_t groups, uint32_t gn,
                                  const float* __restrict__ xn2, const float* __restrict__ w2max,
-                                 float tau, const float* __restrict__ x,
+                                 const float* __restrict__ scale, TieWin win,
+                                 const float* __restrict__ x,
                                  const uint32_t* __restrict__ sel, const float* __restrict__ w,
                                  uint32_t D, uint32_t* __restrict__ bmu,
                                  uint32_t* __restrict__ flags) {
@@ -357,6 +309,7 @@ __global__ void k_merge_partials(const float* __restrict__ part, const uint32_t*
     // rows past the enumerate capacity fall back to the full exact re-scan
     const uint64_t count = *dev_count;
     const uint64_t n = count < cap ? count : cap;
+    const float S = __ldg(scale + 1);
     for (uint64_t f = blockIdx.x * (uint64_t)blockDim.x + threadIdx.x; f < count;
          f += (uint64_t)gridDim.x * blockDim.x) {
         const uint32_t pos = ties[f];
@@ -365,7 +318,7 @@ __global__ void k_merge_partials(const float* __restrict__ part, const uint32_t*
             flags[2 + slot] = pos;
             continue;
         }
-        const float thr = tau * (__ldg(xn2 + f) + __ldg(w2max));
+        const float thr = tie_thr(__ldg(xn2 + f), __ldg(w2max), S, win);
         float B1 = CUDART_INF_F;
         for (uint32_t g = 0; g < groups; ++g) B1 = fminf(B1, part[(size_t)g * 4 * n + f]);
         const float lim = B1 + thr;
@@ -375,6 +328,7 @@ __global__ void k_merge_partials(const float* __restrict__ part, const uint32_t*
             const float* pg = part + (size_t)g * 4 * n;
             if (!(pg[f] <= lim)) continue;
             const uint32_t cnt = __float_as_uint(pg[3 * n + f]);
+            if (cnt == 0) continue;
             if (cnt > 8) overflow = true;
             ncand += cnt;
             only = g * gn + (__float_as_uint(pg[n + f]) & 0xFFu);
@@ -414,15 +368,15 @@ __global__ void k_merge_partials(const float* __restrict__ part, const uint32_t*
 
 void launch_merge_partials(const float* part, const uint32_t* ties, const uint32_t* dev_count,
                            uint64_t cap, uint64_t n_max, uint32_t groups, uint32_t gn,
-                           const float* xn2, const float* w2max, float tau, const float* x,
-                           const uint32_t* sel, const float* w, uint32_t D, uint32_t* bmu,
-                           uint32_t* flags, cudaStream_t st) {
+                           const float* xn2, const float* w2max, const float* scale, TieWin win,
+                           const float* x, const uint32_t* sel, const float* w, uint32_t D,
+                           uint32_t* bmu, uint32_t* flags, cudaStream_t st) {
     if (n_max == 0) return;
     // grid-strides over the device count; sized for the enumerate capacity
     uint64_t blocks = (std::min(cap, n_max) + 255) / 256;
     blocks = std::max<uint64_t>(1, std::min<uint64_t>(blocks, 148ull * 16));
     TSOM_LAUNCH(k_merge_partials<<<(unsigned)blocks, 256, 0, st>>>(
-        part, ties, dev_count, cap, groups, gn, xn2, w2max, tau, x, sel, w, D, bmu, flags));
+        part, ties, dev_count, cap, groups, gn, xn2, w2max, scale, win, x, sel, w, D, bmu, flags));
 }
 
 // ---------------------------------------------------------------------------
@@ -476,72 +430,6 @@ void launch_rescan(const float* x, const uint32_t* sel, const float* w, uint32_t
     // grid sized for the worst case is wasteful; flagged rows are rare, the
     // kernel grid-strides over the device-side count.
     TSOM_LAUNCH(k_rescan<<<148 * 4, 256, 8 * D * sizeof(float), st>>>(x, sel, w, P, D, flags, bmu));
-}
-
-// ---------------------------------------------------------------------------
-// Split (optionally gathered) rows into tcgen05 operand tiles
-// ---------------------------------------------------------------------------
-//
-// Tile t (rows 128t..128t+127) occupies 2*128*56 floats: hi part then lo part,
-// each in K-major core-matrix order ((k/4)*128 + r)*4 + k%4.  Augmented
-// columns: k < D -> x_k, k == D and D+1 -> 1 (pairs with the two ||w||^2
-// pieces), else 0.  Rows past n are zero (their results are ignored).
-
-__global__ void k_split_rows(const float* __restrict__ x, const uint32_t* __restrict__ sel,
-                             const uint32_t* __restrict__ idx, const uint32_t* __restrict__ dev_n,
-                             uint64_t n_host, uint32_t D, float* __restrict__ tiles,
-                             float* __restrict__ xn2) {
-    // idx (optional): positions; split row f is then position idx[f]
-    // dev_n (optional): row count read on the device, capped at n_host
-    const uint64_t n = dev_n ? min((uint64_t)*dev_n, n_host) : n_host;
-    const uint64_t ntiles = (n + kTcTileM - 1) / kTcTileM;
-    const int r = threadIdx.x;  // 128 threads, one row each
-    for (uint64_t tile = blockIdx.x; tile < ntiles; tile += gridDim.x) {
-        const uint64_t f = tile * kTcTileM + r;
-        float* base = tiles + tile * 2 * kTcTileM * kTcKPad;
-        const bool valid = f < n;
-        const float* src = nullptr;
-        if (valid) {
-            const uint64_t pos = idx ? (uint64_t)idx[f] : f;
-            src = x + (sel ? (uint64_t)sel[pos] : pos) * D;
-        }
-        double nrm = 0.0;
-        for (uint32_t kc = 0; kc < kTcKPad / 4; ++kc) {
-            float hi[4], lo[4];
-#pragma unroll
-            for (int q = 0; q < 4; ++q) {
-                const uint32_t k = kc * 4 + q;
-                float val;
-                if (!valid)
-                    val = 0.0f;
-                else if (k < D) {
-                    val = src[k];
-                    nrm += (double)val * (double)val;
-                } else if (k == D || k == D + 1)
-                    val = 1.0f;
-                else
-                    val = 0.0f;
-                hi[q] = tf32_hi(val);
-                lo[q] = val - hi[q];
-            }
-            const size_t off = ((size_t)kc * kTcTileM + r) * 4;
-            *reinterpret_cast<float4*>(base + off) = make_float4(hi[0], hi[1], hi[2], hi[3]);
-            *reinterpret_cast<float4*>(base + (size_t)kTcTileM * kTcKPad + off) =
-                make_float4(lo[0], lo[1], lo[2], lo[3]);
-        }
-        // per-row ||x||^2, rounded up: the row's own FP32 error window (thr_i)
-        if (xn2 && valid) xn2[f] = (float)nrm * 1.0000003f;
-    }
-}
-
-void launch_split_rows(const float* x, const uint32_t* sel, const uint32_t* idx, uint64_t n,
-                       uint32_t D, float* tiles, float* xn2, cudaStream_t st,
-                       const uint32_t* dev_n) {
-    if (n == 0) return;
-    uint64_t tiles_n = (n + kTcTileM - 1) / kTcTileM;
-    if (tiles_n > 148ull * 64) tiles_n = 148ull * 64;
-    TSOM_LAUNCH(k_split_rows<<<(unsigned)tiles_n, kTcTileM, 0, st>>>(x, sel, idx, dev_n, n, D,
-                                                                       tiles, xn2));
 }
 
 }  // namespace tsom

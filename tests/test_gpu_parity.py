@@ -18,7 +18,7 @@ import oracle
 pytestmark = pytest.mark.gpu
 
 GOLDEN = os.path.join(os.path.dirname(__file__), "golden")
-KERNELS = [1, 2]  # SIMT, tcgen05
+KERNELS = [1, 2, 3]  # SIMT, tcgen05 3xTF32, tcgen05 3xFP16
 
 
 @pytest.fixture(scope="module")
@@ -29,10 +29,10 @@ def pkg():
 
 def engine(pkg, p, d, kernel=0):
     e = pkg.Engine(p, d)
-    if kernel == 2:
+    if kernel in (2, 3):
         from paper_2604_26555_b200 import _lib
         try:
-            e.set_option(_lib.TSOM_OPT_BMU_KERNEL, 2)
+            e.set_option(_lib.TSOM_OPT_BMU_KERNEL, kernel)
         except pkg.InvalidArgument:
             pytest.skip("tcgen05 kernel unsupported for this shape")
     elif kernel == 1:
@@ -340,3 +340,34 @@ def test_nccl_world1_allreduce_path(pkg, oracle_port):
         out.append((e.get_codebook(),))
     assert (out[0][0] == out[2][0]).all() and (out[0][1] == out[2][1]).all()
     assert (out[1][0] == out[3][0]).all()
+
+
+# --- operand range: the FP16 encoding rescales by a power of two ------------
+
+@pytest.mark.parametrize("kernel", KERNELS)
+@pytest.mark.parametrize("scale", [1e-30, 1e-4, 1.0, 3e3, 1e18])
+def test_bmu_exact_across_magnitudes(pkg, oracle_port, kernel, scale):
+    rng = np.random.default_rng(int(abs(np.log10(scale))) + 17)
+    x = (rng.standard_normal((3000, 50)) * scale).astype(np.float32)
+    w = x[rng.choice(3000, 300, replace=False)] + (
+        rng.standard_normal((300, 50)) * 0.1 * scale).astype(np.float32)
+    e = engine(pkg, 300, 50, kernel)
+    e.set_codebook(w)
+    b, d = e.bmu(x)
+    bo, do = oracle_port.find_bmus(x, w)
+    assert (b == bo).all()
+    np.testing.assert_allclose(d, do, rtol=1e-12, atol=0)
+
+
+@pytest.mark.parametrize("kernel", KERNELS)
+def test_bmu_exact_mixed_feature_scales(pkg, oracle_port, kernel):
+    # features spanning 10 decades (the FP16 subnormal floor enters the window)
+    rng = np.random.default_rng(5)
+    col = np.logspace(-5, 5, 50).astype(np.float32)
+    x = (rng.standard_normal((4000, 50)) * col).astype(np.float32)
+    w = x[rng.choice(4000, 256, replace=False)].copy()
+    e = engine(pkg, 256, 50, kernel)
+    e.set_codebook(w)
+    b, _ = e.bmu(x)
+    bo, _ = oracle_port.find_bmus(x, w)
+    assert (b == bo).all()
