@@ -145,7 +145,7 @@ tsom::TieWin tie_window(const Engine* e, int kind) {
     tsom::TieWin w;
     w.tau = (float)e->tau_tc;
     w.abs_coef = kind == tsom::kTcF16 ? (float)(std::ldexp(1.0, -24) * std::sqrt((double)e->D)) : 0.0f;
-    w.quant = (float)std::ldexp(1.0, -14);
+    w.quant = 0.0f;  // raw (unpacked) values in every K1 epilogue
     return w;
 }
 
@@ -188,12 +188,12 @@ void run_bmu(Engine* eng, const float* x, const uint32_t* sel, uint64_t n, const
             const uint64_t ntiles = (n + tsom::kTcTileM - 1) / tsom::kTcTileM;
             CU(eng->gsplit.ensure(ntiles * geo.tile_bytes));
             CU(eng->gxn2.ensure(n * sizeof(float)));
-            tsom::launch_split_rows(kind, x, sel, nullptr, n, eng->D, scale, eng->gsplit.p,
+            tsom::launch_split_rows(kind, x, sel, nullptr, n, eng->D, scale, win, eng->gsplit.p,
                                     eng->gxn2.as<float>(), eng->stream);
             tiles = eng->gsplit.p;
             tiles_xn2 = eng->gxn2.as<float>();
         }
-        CU(eng->part.ensure((size_t)groups * 3 * n * sizeof(float)));
+        CU(eng->part.ensure((size_t)groups * tsom::kTcEpiSets * 2 * n * sizeof(float)));
         CU(eng->ties.ensure((n + 1) * sizeof(uint32_t)));
         CU(eng->tmask.ensure(std::max<uint64_t>(n, 1) * sizeof(uint32_t)));
         CU(cudaMemsetAsync(eng->ties.p, 0, sizeof(uint32_t), eng->stream));
@@ -204,7 +204,8 @@ void run_bmu(Engine* eng, const float* x, const uint32_t* sel, uint64_t n, const
                                eng->sm_count, eng->smem_optin, eng->stream));
         CU(cudaEventRecord(eng->ev[9], eng->stream));
         eng->k1_timed = true;
-        tsom::launch_merge_fast(eng->part.as<float>(), n, groups, gn, tiles_xn2, w2, scale, win,
+        tsom::launch_merge_fast(eng->part.as<float>(), n, groups, tsom::kTcEpiSets, gn, tiles_xn2,
+                                w2, scale, win,
                                 eng->bmu.as<uint32_t>(), eng->ties.as<uint32_t>(),
                                 eng->tmask.as<uint32_t>(), eng->flags.as<uint32_t>(), eng->stream);
         CU(cudaGetLastError());
@@ -220,7 +221,7 @@ void run_bmu(Engine* eng, const float* x, const uint32_t* sel, uint64_t n, const
         CU(eng->txn2.ensure(cap * sizeof(float)));
         const uint32_t* tcount = eng->ties.as<uint32_t>();
         const uint32_t* tpos = tcount + 1;
-        tsom::launch_split_rows(kind, x, sel, tpos, cap, eng->D, scale, eng->tsplit.p,
+        tsom::launch_split_rows(kind, x, sel, tpos, cap, eng->D, scale, win, eng->tsplit.p,
                                 eng->txn2.as<float>(), eng->stream, tcount);
         CU(tsom::launch_bmu_tc(kind, eng->tsplit.p, cap, tcount, true, eng->P, eng->D,
                                eng->wsplit.p, eng->txn2.as<float>(), w2, scale, win,
@@ -395,8 +396,8 @@ void accumulate_epoch(Engine* eng, const uint32_t* sel_host, uint64_t n_sel, boo
                 tsom::launch_set_scale(kind, eng->x2max.as<float>(), eng->scale.as<float>(),
                                        eng->stream);
                 tsom::launch_split_rows(kind, eng->x.as<float>(), nullptr, nullptr, eng->n_rows,
-                                        eng->D, eng->scale.as<float>(), eng->xsplit.p,
-                                        eng->xn2.as<float>(), eng->stream);
+                                        eng->D, eng->scale.as<float>(), tie_window(eng, kind),
+                                        eng->xsplit.p, eng->xn2.as<float>(), eng->stream);
                 eng->xsplit_valid = true;
                 eng->xsplit_kind = kind;
             }
@@ -1122,6 +1123,11 @@ int tsom_train_epoch(tsom_engine* eng, double eta, double sigma, double momentum
 }
 
 uint64_t tsom_last_recheck_count(const tsom_engine* eng) { return eng ? eng->last_recheck : 0; }
+
+// diagnostics only (not in the public header): K1 timestamps of CTA 0
+int tsom_debug_k1_trace(unsigned long long* out, uint32_t n) {
+    return tsom::k1_trace_copy(out, n);
+}
 
 int tsom_active_bmu_kernel(const tsom_engine* eng) {
     if (!eng) return 0;

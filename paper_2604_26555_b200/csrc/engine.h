@@ -84,17 +84,25 @@ __host__ __device__ inline TcGeom tc_geom(int kind, uint32_t D) {
 }
 
 // Error window of the tensor-core BMU values (scaled units, S = s^2): a row whose
-// computed top-2 gap exceeds
-//   tau S (||x||^2 + max||w||^2) + abs_coef (sqrt(S ||x||^2) + 2 sqrt(S max||w||^2))
-//   [+ quant (|B1| + |B2|) for packed keys]
-// has a unique exact argmin equal to the computed one.
+// computed best/second-best gap exceeds
+//   thr = tau S (||x||^2 + max||w||^2) + abs_coef (sqrt(S ||x||^2) + 2 sqrt(S max||w||^2))
+// has a unique exact argmin equal to the computed one.  The row
+// part (tie_xpart) is computed once per split row and stored in place of
+// ||x||^2; the codebook part (tie_wpart) once per kernel.
 struct TieWin {
     float tau;       // relative bound of the split-precision products + FP32 accumulation
     float abs_coef;  // absolute floor (FP16 subnormal spacing): 2^-24 sqrt(d), 0 for tf32
-    float quant;     // packed-key truncation: 2^-14
+    float quant;     // (unused: every epilogue compares raw values)
 };
-__host__ __device__ inline float tie_thr(float xn2, float w2max, float S, TieWin w) {
-    return w.tau * S * (xn2 + w2max) + w.abs_coef * (sqrtf(S * xn2) + 2.0f * sqrtf(S * w2max));
+__host__ __device__ inline float tie_sqrt_up(float v) {
+    return v > 0.0f ? sqrtf(v) * 1.000001f : 0.0f;
+}
+// both parts rounded up (the window only has to be an upper bound)
+__host__ __device__ inline float tie_xpart(float xn2, float S, TieWin w) {
+    return (w.tau * S * xn2 + w.abs_coef * tie_sqrt_up(S * xn2)) * 1.000001f;
+}
+__host__ __device__ inline float tie_wpart(float w2max, float S, TieWin w) {
+    return (w.tau * S * w2max + 2.0f * w.abs_coef * tie_sqrt_up(S * w2max)) * 1.000001f;
 }
 
 // K2: counting sort by BMU + per-piece FP64 gather accumulation (k_accum.cu).
@@ -234,9 +242,10 @@ void launch_row_norm_max(const float* x, uint64_t n, uint32_t D, float* out, cud
 void launch_fold_max(float* a, cudaStream_t st);
 // split rows (optionally gathered through sel, and/or through a position list
 // idx: split row f = position idx[f]) into tcgen05 A tiles of encoding `kind`
+// tx[f] (optional) = tie_xpart of the row: its share of the error window
 void launch_split_rows(int kind, const float* x, const uint32_t* sel, const uint32_t* idx,
-                       uint64_t n, uint32_t D, const float* scale, void* tiles, float* xn2,
-                       cudaStream_t st, const uint32_t* dev_n = nullptr);
+                       uint64_t n, uint32_t D, const float* scale, TieWin win, void* tiles,
+                       float* tx, cudaStream_t st, const uint32_t* dev_n = nullptr);
 bool tc_supported(int kind, uint32_t P, uint32_t D);
 size_t tc_wsplit_bytes(int kind, uint32_t P, uint32_t D);
 // scale = {s, s^2, overflow flag}: kTcF16 picks s = 2^e from max ||x||^2 (x2max[0])
@@ -260,9 +269,11 @@ cudaError_t launch_bmu_tc(int kind, const void* tiles, uint64_t n, const uint32_
                           const float* xn2, const float* w2max, const float* scale, TieWin win,
                           const uint32_t* rmask, float* part, int sm_count, size_t smem_optin,
                           cudaStream_t st);
-extern uint32_t g_k1_debug;  // diagnostics: bit0 skip epilogue math, bit1 skip MMAs
+extern uint32_t g_k1_debug;
+int k1_trace_copy(unsigned long long* out, uint32_t n);  // diagnostics  // diagnostics: bit0 skip epilogue math, bit1 skip MMAs
 // main-pass merge: bmu for rows with a clear winner, near-tie positions -> ties
-void launch_merge_fast(const float* part, uint64_t n, uint32_t groups, uint32_t gn,
+constexpr uint32_t kTcEpiSets = 2;  // K1 main pass: partial results per group (sub-groups)
+void launch_merge_fast(const float* part, uint64_t n, uint32_t groups, uint32_t sets, uint32_t gn,
                        const float* xn2, const float* w2max, const float* scale, TieWin win,
                        uint32_t* bmu, uint32_t* ties, uint32_t* tmask, uint32_t* flags,
                        cudaStream_t st);

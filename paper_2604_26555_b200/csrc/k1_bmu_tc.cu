@@ -20,12 +20,11 @@
 // re-checked exactly in FP64 (k_bmu.cu), so BMU indices are bit-identical to
 // the reference.
 //
-// Epilogue: thread = row (TMEM lane), 256 node values per group.  Each value is
-// packed with its local node id in the low 8 mantissa bits (one LOP3) and the
-// packed keys go through a pairwise top-2 network (FMNMX / 3-input FMNMX3):
-// 3.5 ALU ops per value instead of 5 for a compare/select top-2 with a
-// separate index register.  Packing truncates the value by < 2^-15 relative;
-// the merge widens the window by 2^-14 (|B1| + |B2|) to stay exact.
+// Epilogue: thread = row (TMEM lane), 256 node values per group, two passes
+// over TMEM: the row minimum b (3-input FMNMX), then for every value the
+// window test c = sat(big (b + thr - v)) and a += c (j + 256) on the FMA pipe:
+// a in [256, 512) means the minimum is the only node within the error window
+// thr, and gives its id.  No per-value index bookkeeping on the ALU pipe.
 //
 // Work split: the codebook is cut into groups of gn <= 256 nodes.  A CTA keeps
 // one group resident in shared memory for its whole life and streams 128-row
@@ -50,10 +49,19 @@ using namespace ptx;
 
 namespace {
 
-constexpr int kSets = 2;                // epilogue warp sets (4 warps each, one per TMEM lane quarter)
-constexpr int kThreads = 128 + kSets * 128;  // 4 role warps + the epilogue sets
+// epilogue warp sets (4 warps each, one per TMEM lane quarter); each set keeps
+// its column slice of a tile in registers
+template <int kKind>
+struct EpiCfg {
+    static constexpr int kSets = (int)kTcEpiSets;
+    static constexpr int kThreads = 128 + kSets * 128;  // 4 role warps + the sets
+    static constexpr int kCPS = 8 / kSets;              // 32-column chunks per set (gn = 256)
+};
 constexpr uint32_t kEpiThreads = 128;   // threads per epilogue set
 constexpr int kMaxStages = 4;
+// main pass: true = the two epilogue sets alternate tiles (each drains all gn
+// columns of its tile); false = both sets split the columns of every tile
+constexpr bool kAltSets = false;  // (register-resident passes need <= 4 chunks per set)
 
 __device__ __forceinline__ float fmin3f(float a, float b, float c) {
     float r;
@@ -62,6 +70,14 @@ __device__ __forceinline__ float fmin3f(float a, float b, float c) {
 }
 
 }  // namespace
+
+// diagnostics (option 99 bit 5): CTA 0 timestamps [tile][8] (clock64)
+__device__ unsigned long long g_k1_trace[512 * 8];
+#define TSOM_TRACE(slot_, it_)                                                       \
+    do {                                                                              \
+        if (!kEnum && (dbg & 32u) && blockIdx.x == 0 && (it_) < 512u)                        \
+            g_k1_trace[(it_) * 8 + (slot_)] = (unsigned long long)clock64();          \
+    } while (0)
 
 // ---------------------------------------------------------------------------
 // Geometry of the two operand encodings
@@ -235,7 +251,7 @@ template <int kKind>
 __global__ void k_split_rows(const float* __restrict__ x, const uint32_t* __restrict__ sel,
                              const uint32_t* __restrict__ idx, const uint32_t* __restrict__ dev_n,
                              uint64_t n_host, uint32_t D, const float* __restrict__ scale,
-                             uint8_t* __restrict__ tiles, float* __restrict__ xn2) {
+                             TieWin win, uint8_t* __restrict__ tiles, float* __restrict__ xn2) {
     const uint64_t n = dev_n ? min((uint64_t)*dev_n, n_host) : n_host;
     const uint64_t ntiles = (n + kTcTileM - 1) / kTcTileM;
     const int r = threadIdx.x;  // 128 threads, one row each
@@ -305,23 +321,24 @@ __global__ void k_split_rows(const float* __restrict__ x, const uint32_t* __rest
                     *reinterpret_cast<uint4*>(h);
             }
         }
-        if (xn2 && valid) xn2[f] = (float)nrm * 1.0000003f;
+        if (xn2 && valid)
+            xn2[f] = tie_xpart((float)nrm * 1.0000003f, kKind == kTcF16 ? scale[1] : 1.0f, win);
     }
 }
 
 void launch_split_rows(int kind, const float* x, const uint32_t* sel, const uint32_t* idx,
-                       uint64_t n, uint32_t D, const float* scale, void* tiles, float* xn2,
-                       cudaStream_t st, const uint32_t* dev_n) {
+                       uint64_t n, uint32_t D, const float* scale, TieWin win, void* tiles,
+                       float* xn2, cudaStream_t st, const uint32_t* dev_n) {
     if (n == 0) return;
     uint64_t tiles_n = (n + kTcTileM - 1) / kTcTileM;
     if (tiles_n > 148ull * 64) tiles_n = 148ull * 64;
     uint8_t* t = static_cast<uint8_t*>(tiles);
     if (kind == kTcTf32)
         TSOM_LAUNCH(k_split_rows<kTcTf32><<<(unsigned)tiles_n, kTcTileM, 0, st>>>(
-            x, sel, idx, dev_n, n, D, scale, t, xn2));
+            x, sel, idx, dev_n, n, D, scale, win, t, xn2));
     else
         TSOM_LAUNCH(k_split_rows<kTcF16><<<(unsigned)tiles_n, kTcTileM, 0, st>>>(
-            x, sel, idx, dev_n, n, D, scale, t, xn2));
+            x, sel, idx, dev_n, n, D, scale, win, t, xn2));
 }
 
 // ---------------------------------------------------------------------------
@@ -335,16 +352,20 @@ void launch_split_rows(int kind, const float* x, const uint32_t* sel, const uint
 // overflow, 0 = group not relevant for the row (rmask)).
 // dev_n (optional): row count read on the device (the near-tie list length).
 template <int kKind, bool kEnum>
-__global__ void __launch_bounds__(kThreads, 1)
+__global__ void __launch_bounds__(EpiCfg<kKind>::kThreads, 1)
     k1_bmu_tc(const uint8_t* __restrict__ tiles, uint64_t n_host, const uint32_t* __restrict__ dev_n,
               uint32_t groups, uint32_t gn, uint32_t D, uint32_t stages,
               const uint8_t* __restrict__ wsplit, const float* __restrict__ xn2,
               const float* __restrict__ w2max, const float* __restrict__ scale, TieWin win,
               const uint32_t* __restrict__ rmask, float* __restrict__ part, uint32_t one,
-              uint32_t neg1, uint32_t dbg) {
+              uint32_t neg1, uint32_t dbg, uint32_t mc) {
+    // mc > 1: the CTAs of a cluster are the mc codebook groups of the same tile
+    // sequence; each loads 1/mc of every A tile and multicasts it to all, so the
+    // tile crosses L2 -> SM once per cluster instead of once per group.
     // one = 1, neg1 = 0xFFFFFFFF at run time: opaque to the compiler, so the
     // epilogue's integer adds stay IMADs (FMA pipe) instead of IADD3 (ALU pipe)
     extern __shared__ __align__(1024) uint8_t smem[];
+    constexpr int kSets = EpiCfg<kKind>::kSets, kCPS = EpiCfg<kKind>::kCPS;
     const TcGeom geo = tc_geom(kKind, D);
     const uint64_t n = dev_n ? min((uint64_t)*dev_n, n_host) : n_host;
     const uint32_t ntiles = (uint32_t)((n + kTcTileM - 1) / kTcTileM);
@@ -369,11 +390,11 @@ __global__ void __launch_bounds__(kThreads, 1)
     if (threadIdx.x == 0) {
         for (uint32_t s = 0; s < stages; ++s) {
             mbar_init(&full_bar[s], 1);
-            mbar_init(&empty_bar[s], 1);
+            mbar_init(&empty_bar[s], mc);  // one MMA-completion arrival per CTA of the cluster
         }
         for (int a = 0; a < 2; ++a) {
             mbar_init(&tfull_bar[a], 1);
-            mbar_init(&tempty_bar[a], kEnum ? kEpiThreads : kSets * kEpiThreads);
+            mbar_init(&tempty_bar[a], (kEnum || kAltSets) ? 4u : 4u * kSets);  // one per warp
         }
         mbar_init(w_bar, 1);
         asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
@@ -386,8 +407,10 @@ __global__ void __launch_bounds__(kThreads, 1)
     }
     tc_fence_before();
     __syncthreads();
+    if (mc > 1) cluster_sync();  // every CTA's barriers initialised before remote arrivals
     tc_fence_after();
     const uint32_t tmem_base = *tmem_slot;
+    const uint16_t mc_mask = (uint16_t)((1u << mc) - 1u);
 
     if (warp == 0) {
         if (lane == 0 && ntiles > cta_in_group) {
@@ -401,6 +424,13 @@ __global__ void __launch_bounds__(kThreads, 1)
                 mbar_wait(&empty_bar[stage], phase ^ 1);
                 if (dbg & 4u) {
                     mbar_arrive(&full_bar[stage]);
+                } else if (mc > 1) {
+                    // this CTA's slice of the tile, to the same stage of every CTA
+                    const uint32_t slice = geo.tile_bytes / mc, off = g * slice;
+                    mbar_expect_tx(&full_bar[stage], geo.tile_bytes);
+                    bulk_g2s_mc(sX + stage * geo.tile_bytes + off,
+                                tiles + (size_t)t * geo.tile_bytes + off, slice, &full_bar[stage],
+                                mc_mask);
                 } else {
                     mbar_expect_tx(&full_bar[stage], geo.tile_bytes);
                     bulk_g2s(sX + stage * geo.tile_bytes, tiles + (size_t)t * geo.tile_bytes,
@@ -421,8 +451,10 @@ __global__ void __launch_bounds__(kThreads, 1)
             mbar_wait(w_bar, 0);
             uint32_t stage = 0, phase = 0, acc = 0, acc_phase = 0;
             for (uint32_t t = cta_in_group; t < ntiles; t += ctas_per_group) {
+                const uint32_t it_ = (t - cta_in_group) / ctas_per_group;
                 mbar_wait(&tempty_bar[acc], acc_phase ^ 1);
                 mbar_wait(&full_bar[stage], phase);
+                TSOM_TRACE(0, it_);
                 tc_fence_after();
                 const uint32_t d = tmem_base + acc * acc_cols;
                 const uint32_t sx = smem_u32(sX + stage * geo.tile_bytes);
@@ -446,7 +478,11 @@ __global__ void __launch_bounds__(kThreads, 1)
                                 umma_desc(sw + k * 2u * w_lbo, w_lbo, 128u), idesc,
                                 k > 0 ? 1u : 0u);
                 }
-                mma_commit(&empty_bar[stage]);  // X stage free once these MMAs retire
+                TSOM_TRACE(1, it_);
+                if (mc > 1)
+                    mma_commit_mc(&empty_bar[stage], mc_mask);  // stage free in every CTA's view
+                else
+                    mma_commit(&empty_bar[stage]);  // X stage free once these MMAs retire
                 mma_commit(&tfull_bar[acc]);    // accumulator ready for the epilogue
                 if (++stage == stages) {
                     stage = 0;
@@ -460,138 +496,135 @@ __global__ void __launch_bounds__(kThreads, 1)
         }
     } else if (warp >= 4) {
         // Epilogue.  Warp (set, q) owns TMEM lanes 32q..32q+31 (= tile rows).
-        //   main pass: both sets drain every tile, set h taking half of the
-        //     32-column chunks; set 1 hands its per-row top-2 to set 0 through
-        //     shared memory (named barrier per lane quarter), set 0 merges.
-        //   enumerate pass: set s drains accumulator buffer s (every other tile)
-        //     over all gn columns.
         const uint32_t q = warp & 3, set = (warp - 4) >> 2;
         const uint32_t row = q * 32 + lane;
         const uint32_t nch = gn / 32;  // gn is a multiple of 32 (tc_group_width)
         const float S = scale[1];
-        uint32_t mask;
-        asm volatile("mov.b32 %0, 0xFFFFFF00;" : "=r"(mask));  // register operand of the LOP3
-        // main pass: set h takes chunks [h nch / kSets, (h+1) nch / kSets)
-        const uint32_t c_begin = kEnum ? 0 : set * nch / kSets;
-        const uint32_t c_count = kEnum ? nch : (set + 1) * nch / kSets - c_begin;
-        uint32_t acc = kEnum ? set : 0, acc_phase = 0;
-        // (enumerate pass: sets 0 and 1 alternate tiles, the other sets idle)
-        const uint32_t t0 =
-            kEnum ? (set < 2 ? cta_in_group + set * ctas_per_group : ntiles) : cta_in_group;
-        const uint32_t tstep = kEnum ? 2 * ctas_per_group : ctas_per_group;
-        for (uint32_t t = t0; t < ntiles; t += tstep) {
-            mbar_wait(&tfull_bar[acc], acc_phase);
-            tc_fence_after();
-            const uint32_t taddr = tmem_base + ((q * 32u) << 16) + acc * acc_cols + c_begin * 32;
-            uint32_t ra[32], rb[32];
-            float b1[4], b2[4];
-            uint32_t b1k[4];  // main pass: packed running best (integer view)
+        const float wpart = tie_wpart(__ldg(w2max), S, win);  // codebook part of the window
+        if (!kEnum) {
+            // Main pass: both sets drain every tile, set h taking chunks
+            // [h nch / kSets, (h+1) nch / kSets).  Per row and set:
+            //   pass 1: b = min v (3-input FMNMX, 0.5 ALU op per value);
+            //   pass 2: over the same columns, c = sat(big (lim - v)) is 1 for
+            //     every v <= lim = b + thr and 0 otherwise (one FFMA.SAT), and
+            //     a += c (j + 256) (one FFMA): a = 256 count + sum of ids, so
+            //     a in [256, 512) <=> exactly one node (the minimum) lies in
+            //     the window, and then id = a - 256.  Two FMA-pipe ops per
+            //     value, no ALU op, no index bookkeeping.
+            // Set 1 hands (b, a) to set 0 through shared memory; set 0 writes
+            // [B1 | id or 0xFFFFFFFF (several nodes in the window) | -].
+            const uint32_t c_begin = kAltSets ? 0u : set * nch / kSets;
+            const uint32_t c_count =
+                (dbg & 1u) ? 0u : (kAltSets ? nch : (set + 1) * nch / kSets - c_begin);
+            uint32_t acc = kAltSets ? set : 0, acc_phase = 0;
+            const uint32_t t0 = cta_in_group + (kAltSets ? set * ctas_per_group : 0);
+            const uint32_t tstep = kAltSets ? 2 * ctas_per_group : ctas_per_group;
+            // ||x||^2 of the row, prefetched one tile ahead (hides the load latency)
+            uint64_t pos_next = (uint64_t)t0 * kTcTileM + row;
+            float x2_next = pos_next < n ? __ldg(xn2 + pos_next) : 0.0f;
+            for (uint32_t t = t0; t < ntiles; t += tstep) {
+                const uint64_t pos = (uint64_t)t * kTcTileM + row;
+                const float x2 = x2_next;
+                pos_next = pos + (uint64_t)tstep * kTcTileM;
+                x2_next = pos_next < n ? __ldg(xn2 + pos_next) : 0.0f;
+                mbar_wait(&tfull_bar[acc], acc_phase);
+                const uint32_t it_ = (t - cta_in_group) / ctas_per_group;
+                if (lane == 0 && q == 0) TSOM_TRACE(2 + 3 * (set & 1), it_);
+                tc_fence_after();
+                const uint32_t taddr =
+                    tmem_base + ((q * 32u) << 16) + acc * acc_cols + c_begin * 32;
+                // this set's (<= 4) chunks are loaded once into registers (one
+                // TMEM round trip) and both passes run on the registers
+                uint32_t r[kCPS][32];
+                const bool full = c_count == (uint32_t)kCPS;  // the common case: no guards
+                if (full) {
 #pragma unroll
-            for (int s2 = 0; s2 < 4; ++s2) {
-                b1[s2] = CUDART_INF_F;
-                b2[s2] = CUDART_INF_F;
-                b1k[s2] = 0x7F800000u;
-            }
-            // one 32-column chunk, ids relative to c_begin (compile-time base cb)
-#define TSOM_CHUNK(r, cb)                                                                   \
+                    for (int c = 0; c < kCPS; ++c) TSOM_TMEM_LD32(taddr + c * 32, r[c]);
+                } else {
+#pragma unroll
+                    for (int c = 0; c < kCPS; ++c)
+                        if ((uint32_t)c < c_count) TSOM_TMEM_LD32(taddr + c * 32, r[c]);
+                }
+                tmem_wait_ld();
+                tc_fence_before();
+                __syncwarp();
+                if (lane == 0) mbar_arrive(&tempty_bar[acc]);  // warp done with the accumulator
+                float mn[4] = {CUDART_INF_F, CUDART_INF_F, CUDART_INF_F, CUDART_INF_F};
+#define TSOM_PASS1(r, cb)                                                                   \
+    _Pragma("unroll") for (int m = 0; m < 16; ++m) mn[m & 3] =                             \
+        fmin3f(mn[m & 3], __uint_as_float(r[2 * m]), __uint_as_float(r[2 * m + 1]))
+#define TSOM_PASS2(r, cb)                                                                   \
+    _Pragma("unroll") for (int k = 0; k < 32; ++k) a[k & 3] =                              \
+        fmaf(__saturatef(fmaf(__uint_as_float(r[k]), nb, lb)), (float)((cb) + k + 256), a[k & 3])
+#define TSOM_ALL(P)                                                                         \
     do {                                                                                    \
-        _Pragma("unroll") for (int m = 0; m < 16; ++m) {                                    \
-            const int s_ = m & 3;                                                           \
-            if (kEnum) {                                                                    \
-                b1[s_] = fmin3f(b1[s_], __uint_as_float(r[2 * m]),                          \
-                                __uint_as_float(r[2 * m + 1]));                             \
-            } else {                                                                        \
-                uint32_t ka, kb;                                                            \
-                asm("lop3.b32 %0, %1, %2, %3, 0xEC;"                                        \
-                    : "=r"(ka)                                                              \
-                    : "r"(r[2 * m]), "r"((uint32_t)((cb) + 2 * m)), "r"(mask));            \
-                asm("lop3.b32 %0, %1, %2, %3, 0xEC;"                                        \
-                    : "=r"(kb)                                                              \
-                    : "r"(r[2 * m + 1]), "r"((uint32_t)((cb) + 2 * m + 1)), "r"(mask));    \
-                /* hi/t on the ALU pipe (FMNMX); lo = a + b - hi and b1' = b1 + lo - t */ \
-                /* as integer IMADs on the FMA pipe ({lo, hi} = {a, b} bit-exactly)   */ \
-                const uint32_t hi = __float_as_uint(fmaxf(__uint_as_float(ka),             \
-                                                          __uint_as_float(kb)));            \
-                const uint32_t lo = ka * one + kb + hi * neg1;                              \
-                const uint32_t tt = __float_as_uint(fmaxf(__uint_as_float(b1k[s_]),         \
-                                                          __uint_as_float(lo)));            \
-                b1k[s_] = b1k[s_] * one + lo + tt * neg1;                                   \
-                b2[s_] = fmin3f(b2[s_], __uint_as_float(tt), __uint_as_float(hi));          \
-            }                                                                               \
+        if (full) {                                                                         \
+            _Pragma("unroll") for (int c = 0; c < kCPS; ++c) P(r[c], c * 32);               \
+        } else {                                                                            \
+            _Pragma("unroll") for (int c = 0; c < kCPS; ++c) if ((uint32_t)c < c_count)     \
+                P(r[c], c * 32);                                                            \
         }                                                                                   \
     } while (0)
-            const uint32_t c_count_eff = (dbg & 1u) ? 0u : c_count;
-            const bool ld_on = !(dbg & 8u);
-            if (!ld_on) {
-#pragma unroll
-                for (int k = 0; k < 32; ++k) {
-                    ra[k] = 0x3F800000u + (row << 8) + k * 977u + t;
-                    rb[k] = ra[k] ^ 0x5A5A5Au;
+                TSOM_ALL(TSOM_PASS1);
+                if (lane == 0 && q == 0) TSOM_TRACE(3 + 3 * (set & 1), it_);
+                const float b = fminf(fminf(mn[0], mn[1]), fminf(mn[2], mn[3]));
+                const float thr = x2 + wpart;
+                // window limit, nudged up so a value exactly at b + thr counts
+                const float lim0 = b + thr;
+                const float lim = lim0 + fabsf(lim0) * 2.4e-7f;
+                // big = 2^(60 - e(lim)): big * lim ~ 2^60, far from FP32 overflow
+                const int ef = (int)((__float_as_uint(lim) >> 23) & 0xFFu);
+                const float big = __int_as_float(max(67, min(247, 314 - ef)) << 23);
+                const float lb = lim * big, nb = -big;
+                float a[4] = {0.0f, 0.0f, 0.0f, 0.0f};
+                TSOM_ALL(TSOM_PASS2);
+#undef TSOM_ALL
+#undef TSOM_PASS1
+#undef TSOM_PASS2
+                if (lane == 0 && q == 0) TSOM_TRACE(4 + 3 * (set & 1), it_);
+                // a = 256 count + sum(local ids); decode: exactly one -> global id
+                const float asum = (a[0] + a[1]) + (a[2] + a[3]);
+                uint32_t code = 0xFFFFFFFFu;
+                if (asum >= 256.0f && asum < 512.0f && asum == floorf(asum))
+                    code = (uint32_t)asum - 256u + c_begin * 32u;
+                // each set writes its column slice as its own sub-group
+                // (k_merge_fast combines them: no exchange, no named barrier)
+                if (pos < n) {
+                    float* pg = part + (size_t)(g * kSets + set) * 2 * n;
+                    pg[pos] = b;
+                    pg[n + pos] = __uint_as_float(code == 0xFFFFFFFFu ? code : code - c_begin * 32u);
+                }
+                if (kAltSets) {
+                    acc_phase ^= 1;
+                } else if (++acc == 2) {
+                    acc = 0;
+                    acc_phase ^= 1;
                 }
             }
-            if (c_count_eff && ld_on) TSOM_TMEM_LD32(taddr, ra);
+        } else {
+            // Enumerate pass (near-tie rows only): set s drains accumulator
+            // buffer s (every other tile) over all gn columns: the row's raw
+            // minimum, then every node within the window of it.
+            uint32_t acc = set, acc_phase = 0;
+            const uint32_t t0 = set < 2 ? cta_in_group + set * ctas_per_group : ntiles;
+            for (uint32_t t = t0; t < ntiles; t += 2 * ctas_per_group) {
+                mbar_wait(&tfull_bar[acc], acc_phase);
+                tc_fence_after();
+                const uint32_t taddr = tmem_base + ((q * 32u) << 16) + acc * acc_cols;
+                float mn = CUDART_INF_F;
+                for (uint32_t cc = 0; cc < gn; cc += 32) {
+                    uint32_t r[32];
+                    TSOM_TMEM_LD32(taddr + cc, r);
+                    tmem_wait_ld();
 #pragma unroll
-            for (int c = 0; c < (kEnum ? 8 : 4); c += 2) {
-                if ((uint32_t)c < c_count_eff) {
-                    if (ld_on) {
-                        tmem_wait_ld();
-                        if ((uint32_t)c + 1 < c_count_eff) TSOM_TMEM_LD32(taddr + (c + 1) * 32, rb);
-                    }
-                    TSOM_CHUNK(ra, c * 32);
+                    for (int m = 0; m < 16; ++m)
+                        mn = fmin3f(mn, __uint_as_float(r[2 * m]), __uint_as_float(r[2 * m + 1]));
                 }
-                if ((uint32_t)c + 1 < c_count_eff) {
-                    if (ld_on) {
-                        tmem_wait_ld();
-                        if ((uint32_t)c + 2 < c_count_eff) TSOM_TMEM_LD32(taddr + (c + 2) * 32, ra);
-                    }
-                    TSOM_CHUNK(rb, (c + 1) * 32);
-                }
-            }
-#undef TSOM_CHUNK
-            const uint64_t pos = (uint64_t)t * kTcTileM + row;
-            if (!kEnum) {
-                tc_fence_before();
-                mbar_arrive(&tempty_bar[acc]);  // this thread is done with the accumulator
-                // merge the 4 streams (packed keys compare as floats)
-                float k1 = __uint_as_float(b1k[0]), k2 = b2[0];
-#pragma unroll
-                for (int s2 = 1; s2 < 4; ++s2) {
-                    const float o1 = __uint_as_float(b1k[s2]);
-                    const float tt = fmaxf(k1, o1);
-                    k1 = fminf(k1, o1);
-                    k2 = fmin3f(k2, b2[s2], tt);
-                }
-                // ids are relative to the set's first chunk (no carry: id < 256)
-                if (c_begin && c_count) k1 = __uint_as_float(__float_as_uint(k1) + c_begin * 32);
-                float2* xch = reinterpret_cast<float2*>(w_bar + 2) + acc * (kSets - 1) * kTcTileM;
-                if (dbg & 16u) {
-                    if (k1 == 1.2345f && k2 == 3.0f) part[0] = 0.0f;  // keep the math alive
-                } else {
-                if (set) xch[(set - 1) * kTcTileM + row] = make_float2(k1, k2);
-                asm volatile("bar.sync %0, %1;" ::"r"(1 + q), "n"(32 * kSets) : "memory");
-                if (!set) {
-#pragma unroll
-                    for (int o2 = 0; o2 < kSets - 1; ++o2) {
-                        const float2 o = xch[o2 * kTcTileM + row];
-                        const float tt = fmaxf(k1, o.x);
-                        k1 = fminf(k1, o.x);
-                        k2 = fmin3f(k2, o.y, tt);
-                    }
-                    if (pos < n) {
-                        const uint32_t kb1 = __float_as_uint(k1);
-                        float* pg = part + (size_t)g * 3 * n;
-                        pg[pos] = __uint_as_float(kb1 & 0xFFFFFF00u);
-                        pg[n + pos] = __uint_as_float(kb1 & 0xFFu);
-                        pg[2 * n + pos] = __uint_as_float(__float_as_uint(k2) & 0xFFFFFF00u);
-                    }
-                }
-                }
-            } else {
-                const float B1 = fminf(fminf(b1[0], b1[1]), fminf(b1[2], b1[3]));
+                const uint64_t pos = (uint64_t)t * kTcTileM + row;
                 // enumerate the row's candidates v <= B1 + thr in ascending j
                 const bool need = pos < n && ((__ldg(rmask + pos) >> (g & 31)) & 1u);
-                const float thr = need ? tie_thr(__ldg(xn2 + pos), __ldg(w2max), S, win) : 0.0f;
-                const float lim = B1 + thr;
+                const float thr = need ? __ldg(xn2 + pos) + wpart : 0.0f;
+                const float lim = mn + thr;
                 uint32_t pk0 = 0, pk1 = 0, nc = 0;
                 if (__any_sync(0xffffffffu, need)) {
                     for (uint32_t cc = 0; cc < gn; cc += 16) {
@@ -610,26 +643,23 @@ __global__ void __launch_bounds__(kThreads, 1)
                     }
                 }
                 tc_fence_before();
-                mbar_arrive(&tempty_bar[acc]);  // this thread is done with the accumulator
+                __syncwarp();
+                if (lane == 0) mbar_arrive(&tempty_bar[acc]);  // warp done with the accumulator
                 if (pos < n) {
                     float* pg = part + (size_t)g * 4 * n;
-                    pg[pos] = B1;
+                    pg[pos] = mn;
                     pg[n + pos] = __uint_as_float(pk0);
                     pg[2 * n + pos] = __uint_as_float(pk1);
                     pg[3 * n + pos] =
                         __uint_as_float(!need ? 0u : ((nc >= 1 && nc <= 8) ? nc : kCandOverflow));
                 }
-            }
-            if (kEnum) {
-                acc_phase ^= 1;
-            } else if (++acc == 2) {
-                acc = 0;
                 acc_phase ^= 1;
             }
         }
     }
     tc_fence_before();
     __syncthreads();
+    if (mc > 1) cluster_sync();  // no CTA leaves while a peer may still signal it
     if (warp == 2) {
         tc_fence_after();
         asm volatile("tcgen05.dealloc.cta_group::1.sync.aligned.b32 %0, %1;" ::"r"(tmem_base),
@@ -638,8 +668,14 @@ __global__ void __launch_bounds__(kThreads, 1)
 }
 
 // diagnostics only (option 99): bit0 skips the epilogue math, bit1 the MMAs,
-// bit2 the A-tile loads, so the stages can be timed in isolation
+// bit2 the A-tile loads, so the stages can be timed in isolation; bit5 traces
+// CTA 0; bit6 enables the cluster multicast of A tiles
 uint32_t g_k1_debug = 0;
+
+int k1_trace_copy(unsigned long long* out, uint32_t n) {
+    return cudaMemcpyFromSymbol(out, g_k1_trace, (n < 4096u ? n : 4096u) * 8) == cudaSuccess ? 0
+                                                                                             : 4;
+}
 
 cudaError_t launch_bmu_tc(int kind, const void* tiles, uint64_t n, const uint32_t* dev_n,
                           bool enumerate, uint32_t P, uint32_t D, const void* wsplit,
@@ -656,14 +692,15 @@ cudaError_t launch_bmu_tc(int kind, const void* tiles, uint64_t n, const uint32_
     if (per_group > ntiles) per_group = ntiles;
     const uint32_t grid = per_group * groups;
     const uint32_t w_bytes = gn * geo.row_bytes;
-    const size_t fixed = ((w_bytes + 1023u) & ~1023u) + 128 + 2 * (kSets - 1) * kTcTileM * 8;
+    const size_t fixed = ((w_bytes + 1023u) & ~1023u) + 128;
     uint32_t stages = 2;
     while (stages < 3 && fixed + (size_t)(stages + 1) * geo.tile_bytes <= smem_optin) ++stages;
     const size_t smem = fixed + (size_t)stages * geo.tile_bytes;
     if (smem > smem_optin) return cudaErrorInvalidConfiguration;
     using KernT = void (*)(const uint8_t*, uint64_t, const uint32_t*, uint32_t, uint32_t, uint32_t,
                            uint32_t, const uint8_t*, const float*, const float*, const float*,
-                           TieWin, const uint32_t*, float*, uint32_t, uint32_t, uint32_t);
+                           TieWin, const uint32_t*, float*, uint32_t, uint32_t, uint32_t,
+                           uint32_t);
     KernT kern;
     int slot;
     if (kind == kTcTf32) {
@@ -680,10 +717,59 @@ cudaError_t launch_bmu_tc(int kind, const void* tiles, uint64_t n, const uint32_
         if (e != cudaSuccess) return e;
         attr[slot] = smem;
     }
-    TSOM_LAUNCH(kern<<<grid, kThreads, smem, st>>>(
-        static_cast<const uint8_t*>(tiles), n, dev_n, groups, gn, D, stages,
+    const int threads = kind == kTcF16 ? EpiCfg<kTcF16>::kThreads : EpiCfg<kTcTf32>::kThreads;
+    // cluster of the `groups` CTAs that share each A tile (multicast loads);
+    // as many clusters as can be co-resident (one CTA per SM)
+    uint32_t mc = 1;
+    // (measured neutral at K = 1024 on B200, so off unless option 99 bit 6 asks)
+    if ((g_k1_debug & 64u) && groups >= 2 && groups <= 8 && geo.tile_bytes % (16u * groups) == 0)
+        mc = groups;
+    uint32_t clusters = per_group;
+    if (mc > 1) {
+        static int max_clusters[4] = {-1, -1, -1, -1};
+        static uint32_t mc_for[4] = {0, 0, 0, 0};
+        if (max_clusters[slot] < 0 || mc_for[slot] != mc) {
+            cudaLaunchConfig_t qc = {};
+            qc.gridDim = dim3(mc * per_group);
+            qc.blockDim = dim3(threads);
+            qc.dynamicSmemBytes = smem;
+            cudaLaunchAttribute qa[1];
+            qa[0].id = cudaLaunchAttributeClusterDimension;
+            qa[0].val.clusterDim.x = mc;
+            qa[0].val.clusterDim.y = 1;
+            qa[0].val.clusterDim.z = 1;
+            qc.attrs = qa;
+            qc.numAttrs = 1;
+            int nc = 0;
+            if (cudaOccupancyMaxActiveClusters(&nc, kern, &qc) != cudaSuccess) {
+                cudaGetLastError();
+                nc = 0;
+            }
+            max_clusters[slot] = nc;
+            mc_for[slot] = mc;
+        }
+        if (max_clusters[slot] < 1) mc = 1;
+        else clusters = std::min<uint32_t>(per_group, (uint32_t)max_clusters[slot]);
+    }
+    const uint32_t grid_x = clusters * groups;
+    cudaLaunchConfig_t cfg = {};
+    cfg.gridDim = dim3(grid_x);
+    cfg.blockDim = dim3(threads);
+    cfg.dynamicSmemBytes = smem;
+    cfg.stream = st;
+    cudaLaunchAttribute attr1[1];
+    attr1[0].id = cudaLaunchAttributeClusterDimension;
+    attr1[0].val.clusterDim.x = mc;
+    attr1[0].val.clusterDim.y = 1;
+    attr1[0].val.clusterDim.z = 1;
+    cfg.attrs = attr1;
+    cfg.numAttrs = 1;
+    ++g_launches;
+    const cudaError_t e = cudaLaunchKernelEx(
+        &cfg, kern, static_cast<const uint8_t*>(tiles), n, dev_n, groups, gn, D, stages,
         static_cast<const uint8_t*>(wsplit), xn2, w2max, scale, win, rmask, part, 1u,
-        0xFFFFFFFFu, g_k1_debug));
+        0xFFFFFFFFu, g_k1_debug, mc);
+    if (e != cudaSuccess) return e;
     return cudaGetLastError();
 }
 

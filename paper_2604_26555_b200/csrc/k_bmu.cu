@@ -236,57 +236,66 @@ __device__ __forceinline__ double exact_d2(const float* __restrict__ x,
     return acc;
 }
 
-// Main-pass merge.  part[g] = [B1 | i1 | B2] per row (k1_bmu_tc<.., false>,
-// packed-key values: the id bits cleared).  A row whose global best is
-// separated from every other node by more than the error window gets its BMU
-// here; otherwise its position joins `ties` ([0] = count, positions from [1])
-// for the enumerate pass, with the bitmask of groups inside the window.  If the
+// Main-pass merge.  part[sg] = [B1 | code] per row and sub-group sg = g * sets
+// + h (k1_bmu_tc<.., false>: epilogue set h of codebook group g covers the
+// group's chunks [h nch / sets, (h+1) nch / sets)): the sub-group's raw minimum
+// and, when it is the only node of the sub-group within the error window of
+// that minimum, its id relative to the sub-group (else 0xFFFFFFFF).  A row is
+// clear when its best sub-group has a unique in-window node and every other
+// sub-group's minimum lies outside the window; it then gets its BMU here.
+// Otherwise its position joins `ties` ([0] = count, positions from [1]) for the
+// enumerate pass, with the bitmask of codebook groups inside the window.  If the
 // FP16 codebook operand overflowed (scale[2] != 0) every row goes to the full
-// exact re-scan (flags).
+// exact re-scan.
 __global__ void __launch_bounds__(256, 8) k_merge_fast(
-    const float* __restrict__ part, uint64_t n, uint32_t groups, uint32_t gn,
+    const float* __restrict__ part, uint64_t n, uint32_t groups, uint32_t sets, uint32_t gn,
     const float* __restrict__ xn2, const float* __restrict__ w2max,
     const float* __restrict__ scale, TieWin win, uint32_t* __restrict__ bmu,
     uint32_t* __restrict__ ties, uint32_t* __restrict__ tmask, uint32_t* __restrict__ flags) {
     const uint64_t i = blockIdx.x * (uint64_t)blockDim.x + threadIdx.x;
     if (i >= n) return;
-    float B1 = CUDART_INF_F, B2 = CUDART_INF_F;
-    uint32_t I1 = 0;
-    for (uint32_t g = 0; g < groups; ++g) {  // ascending groups = ascending node ids
-        const float* pg = part + (size_t)g * 3 * n;
-        top2_merge(B1, I1, B2, __ldg(pg + i), g * gn + __float_as_uint(__ldg(pg + n + i)),
-                   __ldg(pg + 2 * n + i));
+    const uint32_t nsub = groups * sets, nch = gn / 32;
+    float B1 = CUDART_INF_F;
+    uint32_t smin = 0;
+    for (uint32_t sg = 0; sg < nsub; ++sg) {  // strict <: lowest node ids on equal minima
+        const float b = __ldg(part + (size_t)sg * 2 * n + i);
+        if (b < B1) {
+            B1 = b;
+            smin = sg;
+        }
     }
-    bmu[i] = I1;
+    const uint32_t code = __float_as_uint(__ldg(part + (size_t)smin * 2 * n + n + i));
+    const uint32_t gmin = smin / sets, hmin = smin % sets;
+    bmu[i] = gmin * gn + (hmin * nch / sets) * 32 + (code == 0xFFFFFFFFu ? 0u : code);
     if (__float_as_uint(__ldg(scale + 2)) != 0u) {
         const uint32_t slot = atomicAdd(&flags[0], 1u);
         flags[2 + slot] = (uint32_t)i;
         return;
     }
-    const float thr = tie_thr(__ldg(xn2 + i), __ldg(w2max), __ldg(scale + 1), win) +
-                      win.quant * (fabsf(B1) + fminf(fabsf(B2), 3.0e37f));
-    if (!(B2 - B1 > thr)) {
-        // groups whose best lies inside the window (bit g; > 32 groups: all)
-        uint32_t mask = 0xFFFFFFFFu;
-        if (groups <= 32) {
-            mask = 0;
-            const float lim = B1 + thr;
-            for (uint32_t g = 0; g < groups; ++g)
-                if (__ldg(part + (size_t)g * 3 * n + i) <= lim) mask |= 1u << g;
-        }
+    const float thr = __ldg(xn2 + i) + tie_wpart(__ldg(w2max), __ldg(scale + 1), win);
+    const float lim = B1 + thr;
+    bool clear = code != 0xFFFFFFFFu;
+    uint32_t mask = 0;
+    for (uint32_t sg = 0; sg < nsub; ++sg) {
+        const bool in = __ldg(part + (size_t)sg * 2 * n + i) <= lim;
+        const uint32_t g = sg / sets;
+        if (in) mask |= (g < 32 ? 1u << g : 0u);
+        if (in && sg != smin) clear = false;
+    }
+    if (!clear) {
         const uint32_t slot = atomicAdd(&ties[0], 1u);
         ties[1 + slot] = (uint32_t)i;
-        tmask[slot] = mask;
+        tmask[slot] = groups <= 32 ? mask : 0xFFFFFFFFu;
     }
 }
 
-void launch_merge_fast(const float* part, uint64_t n, uint32_t groups, uint32_t gn,
+void launch_merge_fast(const float* part, uint64_t n, uint32_t groups, uint32_t sets, uint32_t gn,
                        const float* xn2, const float* w2max, const float* scale, TieWin win,
                        uint32_t* bmu, uint32_t* ties, uint32_t* tmask, uint32_t* flags,
                        cudaStream_t st) {
     if (n == 0) return;
     TSOM_LAUNCH(k_merge_fast<<<(unsigned)((n + 255) / 256), 256, 0, st>>>(
-        part, n, groups, gn, xn2, w2max, scale, win, bmu, ties, tmask, flags));
+        part, n, groups, sets, gn, xn2, w2max, scale, win, bmu, ties, tmask, flags));
 }
 
 
@@ -318,7 +327,7 @@ __global__ void k_merge_partials(const float* __restrict__ part, const uint32_t*
             flags[2 + slot] = pos;
             continue;
         }
-        const float thr = tie_thr(__ldg(xn2 + f), __ldg(w2max), S, win);
+        const float thr = __ldg(xn2 + f) + tie_wpart(__ldg(w2max), S, win);
         float B1 = CUDART_INF_F;
         for (uint32_t g = 0; g < groups; ++g) B1 = fminf(B1, part[(size_t)g * 4 * n + f]);
         const float lim = B1 + thr;

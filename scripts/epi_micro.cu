@@ -39,6 +39,10 @@ __global__ void __launch_bounds__(256) kern(const uint32_t* in, float* out, int 
                 b2[s] = fmin3f(b2[s], tt, hi);
             } else if (V == 3) {  // min only (lower bound)
                 b1[s] = fmin3f(b1[s], __uint_as_float(a), __uint_as_float(b));
+            } else if (V == 4) {  // pass-2 style: count/idx of values <= lim
+                const float lim = b2[0];
+                if (__uint_as_float(a) <= lim) { b1k[1] = 2 * m; b1k[2] += one; }
+                if (__uint_as_float(b) <= lim) { b1k[1] = 2 * m + 1; b1k[2] += one; }
             }
         }
     }
@@ -55,12 +59,12 @@ int main() {
     uint32_t h[1024]; for (int i = 0; i < 1024; ++i) h[i] = 0x3F800000u + i * 7919u % 100000u;
     cudaMemcpy(in, h, 4096, cudaMemcpyHostToDevice);
     const int iters = 2000;
-    for (int warps = 2; warps <= 8; warps *= 2) {
+    for (int warps = 2; warps <= 2; warps *= 2) {
         const int threads = warps * 32 * 4;  // warps per SMSP x 4 SMSPs
         if (threads > 1024) break;
-        for (int v = 0; v < 4; ++v) {
+        for (int v = 0; v < 5; ++v) {
             cudaEvent_t e0, e1; cudaEventCreate(&e0); cudaEventCreate(&e1);
-            auto k = v == 0 ? kern<0> : v == 1 ? kern<1> : v == 2 ? kern<2> : kern<3>;
+            auto k = v == 0 ? kern<0> : v == 1 ? kern<1> : v == 2 ? kern<2> : v == 3 ? kern<3> : kern<4>;
             k<<<148, threads>>>(in, out, 10, 1u, 0xFFFFFFFFu);
             cudaEventRecord(e0);
             k<<<148, threads>>>(in, out, iters, 1u, 0xFFFFFFFFu);

@@ -16,7 +16,7 @@ for kern in (3,):
     rng = np.random.default_rng(0)
     e.set_codebook((rng.standard_normal((1024, 50)) * 3).astype(np.float32))
     e.set_topology_distance(lattice_dist("hex", 32, 32))
-    for dbg in (0, 1, 4, 5, 6, 7, 6 | 8, 6 | 16, 6 | 24, 8, 16, 24):
+    for dbg in (0, 64, 1, 65, 4, 5, 6, 7):
         e.set_option(99, dbg)
         ts = []
         for _ in range(6):
