@@ -145,7 +145,9 @@ int tsom_set_topology_distance(tsom_engine* eng, const double* dist);
 /* One full epoch on the device: influence(sigma) -> BMU -> accumulate ->
  * (allreduce) -> smoothing -> apply_update (trainer.hpp:341-369) with the
  * reference's H floor, momentum and non-finite guards.  flags bit0 = momentum
- * on.  Weights stay on the device (read with tsom_get_codebook). */
+ * on; bit1 = rows picked by the device sampler (tsom_sampler_init), which then
+ * observes their distances (trainer.hpp:495, 511).  Weights stay on the device
+ * (read with tsom_get_codebook). */
 int tsom_train_epoch(tsom_engine* eng, double eta, double sigma, double momentum,
                      uint32_t flags);
 /* Topology refresh on the device (refresh_topology topology.hpp:439-451) from
@@ -165,6 +167,31 @@ uint64_t tsom_last_recheck_count(const tsom_engine* eng);
 /* The BMU kernel the engine runs for its shape and options: 1 = SIMT FP32,
  * 2 = tcgen05 3xTF32, 3 = tcgen05 3xFP16 (TSOM_OPT_BMU_KERNEL values). */
 int tsom_active_bmu_kernel(const tsom_engine* eng);
+
+/* Device samplers (Sampler, sampling.hpp:183-221) ------------------------ */
+
+/* Per-epoch row selection on the device, identical to toposom::Sampler(kind,
+ * budget, N = tsom_rows(), seed, alpha, beta) for the same seed: kind 0 = full
+ * (select_full :46-51), 1 = random (Floyd, select_random :56-73), 2 = adaptive
+ * (select_adaptive :101-139 with update_adaptive :143-157).  m = the resolved
+ * budget (resolve_budget :30-40).  The random stream is the reference's
+ * mt19937_64 (Rng(seed, SeedStream::sampler), rng.hpp:21-37), produced by many
+ * device generators started with jump-ahead polynomials.  Errors:
+ * "select_random: m must be >= 1". */
+int tsom_sampler_init(tsom_engine* eng, int kind, uint64_t m, uint64_t seed, double alpha,
+                      double beta);
+/* Sampler::select(): the next sorted selection (kept on the device for the
+ * next sampled epoch); sel_out (optional) receives m_out row ids. */
+int tsom_sampler_select(tsom_engine* eng, uint32_t* sel_out, uint64_t* m_out);
+/* Sampler::observe(selected, distances) for the last selection: dist = one
+ * distance per selected row in selection order, or NULL for the distances of
+ * the last sampled tsom_train_epoch.  No-op unless adaptive. */
+int tsom_sampler_observe(tsom_engine* eng, const double* dist);
+/* AdaptiveSamplerState (sampling.hpp:83-92): last_error (N f64) and age (N u32). */
+int tsom_sampler_state(tsom_engine* eng, double* last_error, uint32_t* age);
+/* Host-only check of the jump-ahead (no GPU): 0 when the state jumped by `jump`
+ * draws from mt19937_64(seed) equals sequential generation. */
+int tsom_mt_selftest(uint64_t seed, uint64_t jump);
 
 /* Multi-GPU (one process per GPU) ---------------------------------------- */
 

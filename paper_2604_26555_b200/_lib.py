@@ -40,7 +40,11 @@ EXPORTS = [
     "tsom_last_recheck_count", "tsom_comm_unique_id", "tsom_comm_init", "tsom_last_timing",
     "tsom_stream", "tsom_last_timing_detail", "tsom_kernel_launches", "tsom_refresh_topology",
     "tsom_pairwise_sq_dists", "tsom_bind_shards", "tsom_active_bmu_kernel",
+    "tsom_sampler_init", "tsom_sampler_select", "tsom_sampler_observe", "tsom_sampler_state",
+    "tsom_mt_selftest",
 ]
+
+SAMPLER_KINDS = {"full": 0, "random": 1, "adaptive": 2}  # SamplingKind, sampling.hpp:163
 
 
 class TsomError(RuntimeError):
@@ -103,6 +107,12 @@ def load():
     L.tsom_qe.argtypes = [_vp, _vp, u64, C.POINTER(C.c_double), C.POINTER(u64)]
     L.tsom_set_topology_distance.argtypes = [_vp, _vp]
     L.tsom_train_epoch.argtypes = [_vp, C.c_double, C.c_double, C.c_double, u32]
+    L.tsom_sampler_init.argtypes = [_vp, i32, u64, u64, C.c_double, C.c_double]
+    L.tsom_sampler_select.argtypes = [_vp, _vp, C.POINTER(u64)]
+    L.tsom_sampler_observe.argtypes = [_vp, _vp]
+    L.tsom_sampler_state.argtypes = [_vp, _vp, _vp]
+    L.tsom_mt_selftest.argtypes = [u64, u64]
+    L.tsom_mt_selftest.restype = i32
     L.tsom_last_recheck_count.argtypes = [_vp]
     L.tsom_last_recheck_count.restype = u64
     L.tsom_active_bmu_kernel.argtypes = [_vp]
@@ -125,6 +135,12 @@ def load():
 
 def kernel_launches() -> int:
     return int(load().tsom_kernel_launches())
+
+
+def mt_selftest(seed: int, jump: int) -> int:
+    """Host-side check of the MT19937-64 jump-ahead (0 = jumped state and
+    outputs equal sequential generation); needs no GPU."""
+    return int(load().tsom_mt_selftest(int(seed), int(jump)))
 
 
 def version() -> str:
@@ -254,9 +270,36 @@ class Engine:
         return s.value, c.value
 
     def train_epoch(self, eta: float, sigma: float, momentum: float = 0.0,
-                    use_momentum: bool = False):
+                    use_momentum: bool = False, sampled: bool = False):
+        """One device-resident epoch; sampled=True lets the device sampler
+        (sampler_init) pick the rows and, if adaptive, observe their distances."""
         self._check(self.L.tsom_train_epoch(self.h, float(eta), float(sigma), float(momentum),
-                                            1 if use_momentum else 0))
+                                            (1 if use_momentum else 0) | (2 if sampled else 0)))
+
+    # --- device sampler (sampling.hpp:183-221) -------------------------------
+    def sampler_init(self, kind, m: int, seed: int, alpha: float = 1.0, beta: float = 1.0):
+        k = SAMPLER_KINDS[kind] if isinstance(kind, str) else int(kind)
+        self._check(self.L.tsom_sampler_init(self.h, k, int(m), int(seed) & (2**64 - 1),
+                                             float(alpha), float(beta)))
+
+    def sampler_select(self) -> np.ndarray:
+        """Sampler::select() on the device: sorted uint32 row ids."""
+        out = np.empty(self.rows, np.uint32)
+        m = C.c_uint64()
+        self._check(self.L.tsom_sampler_select(self.h, _ptr(out), C.byref(m)))
+        return out[: m.value].copy()
+
+    def sampler_observe(self, distances=None):
+        """Sampler::observe for the last selection (distances in selection order;
+        None = those of the last sampled epoch)."""
+        d = None if distances is None else np.ascontiguousarray(distances, np.float64)
+        self._check(self.L.tsom_sampler_observe(self.h, _ptr(d)))
+
+    def sampler_state(self):
+        e = np.empty(self.rows, np.float64)
+        a = np.empty(self.rows, np.uint32)
+        self._check(self.L.tsom_sampler_state(self.h, _ptr(e), _ptr(a)))
+        return e, a
 
     @property
     def active_bmu_kernel(self) -> int:

@@ -118,7 +118,8 @@ class CudaExecutor:
 @dataclass
 class ResidentConfig:
     """Subset of SomConfig (trainer.hpp:58-99) the device-resident loop supports
-    (full sampling; lattices, or MST/RNG graphs refreshed on the device)."""
+    (lattices, or MST/RNG graphs refreshed on the device; full, random or
+    adaptive sampling by the device sampler, sampling.hpp:183-221)."""
 
     topology: str = "hex"       # "rect" | "hex" | "mst" | "rng"
     grid_w: int = 32
@@ -136,6 +137,12 @@ class ResidentConfig:
     use_momentum: bool = False
     momentum: float = 0.5
     seed: int = 0
+    sampling: str = "full"      # "full" | "random" | "adaptive"
+    rho: float = 1.0            # proportional budget (resolve_budget, sampling.hpp:30-40)
+    m0: int = 0                 # fixed budget when budget_fixed
+    budget_fixed: bool = False
+    alpha: float = 1.0          # adaptive difficulty / staleness exponents
+    beta: float = 1.0
 
     @property
     def lattice(self) -> bool:
@@ -144,6 +151,19 @@ class ResidentConfig:
     @property
     def nodes(self) -> int:
         return self.grid_w * self.grid_h if self.lattice else self.graph_nodes
+
+
+def resolve_budget(cfg, n: int) -> int:
+    """resolve_budget (sampling.hpp:30-40)."""
+    if n < 1:
+        raise InvalidArgument(1, "resolve_budget: N must be >= 1")
+    if cfg.budget_fixed:
+        if cfg.m0 == 0:
+            raise InvalidArgument(1, "resolve_budget: fixed budget m0 must be >= 1")
+        return int(cfg.m0)
+    if not (0.0 < cfg.rho <= 1.0):
+        raise InvalidArgument(1, "resolve_budget: rho must be in (0, 1]")
+    return max(1, int(math.floor(n * cfg.rho)))
 
 
 def train_resident(cfg: ResidentConfig, engine: Engine, init_weights=None, log_qe=False):
@@ -163,6 +183,10 @@ def train_resident(cfg: ResidentConfig, engine: Engine, init_weights=None, log_q
     else:
         raise InvalidArgument(1, f"unknown topology kind: '{cfg.topology}'")
     sigma0 = resolved_sigma0(cfg.topology, cfg.grid_w, cfg.grid_h, cfg.sigma0)
+    sampled = cfg.sampling != "full"
+    if sampled:
+        engine.sampler_init(cfg.sampling, resolve_budget(cfg, engine.rows), cfg.seed, cfg.alpha,
+                            cfg.beta)
     log = []
     for t in range(cfg.n_iters):
         refreshed = False
@@ -172,7 +196,7 @@ def train_resident(cfg: ResidentConfig, engine: Engine, init_weights=None, log_q
             refreshed = True
         eta = schedule_value(cfg.eta0, cfg.lr_decay, t, cfg.n_iters, 1e-4)
         sigma = schedule_value(sigma0, cfg.radius_decay, t, cfg.n_iters, cfg.sigma_min)
-        engine.train_epoch(eta, sigma, cfg.momentum, cfg.use_momentum)
+        engine.train_epoch(eta, sigma, cfg.momentum, cfg.use_momentum, sampled=sampled)
         entry = {"iter": t, "eta": eta, "sigma": sigma, "refreshed": refreshed}
         if log_qe:
             s, c = engine.qe()
@@ -184,4 +208,4 @@ def train_resident(cfg: ResidentConfig, engine: Engine, init_weights=None, log_q
 __all__ = ["find_bmus", "map_samples", "mean_bmu_distance", "quantization_error",
            "CudaExecutor", "Accumulators", "ResidentConfig", "train_resident", "Engine",
            "NumericalFault", "InvalidArgument", "OutOfRange", "Rng", "init_sample_draw",
-           "schedule_value", "lattice_dist", "math"]
+           "schedule_value", "lattice_dist", "resolve_budget", "math"]

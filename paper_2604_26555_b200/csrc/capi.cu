@@ -21,6 +21,7 @@
 #include <vector>
 
 #include "engine.h"
+#include "mt_jump.h"
 
 using tsom::DevBuf;
 using tsom::Engine;
@@ -365,18 +366,20 @@ void ensure_accum(Engine* eng, uint64_t rows) {
 // One pass over the bound rows (resident or streamed): BMU search, then K2
 // into sums = [R | c | sum dist | rows] (+ allreduce).  want_dist: per-row
 // distances into eng->dist; want_dsum: distance sum; accumulate: R and c.
+// dev_sel (optional, resident data only): a sorted selection of n_sel rows
+// already in device memory (the device sampler's), used instead of sel_host.
 void accumulate_epoch(Engine* eng, const uint32_t* sel_host, uint64_t n_sel, bool want_dist,
-                      bool want_dsum, bool accumulate) {
+                      bool want_dsum, bool accumulate, const uint32_t* dev_sel = nullptr) {
     CU(eng->sums.ensure(slot_len(eng) * sizeof(double)));
-    const uint32_t* sel = normalise_selection(eng, sel_host, n_sel);
+    const uint32_t* sel = dev_sel ? dev_sel : normalise_selection(eng, sel_host, n_sel);
     const uint64_t n = sel ? n_sel : eng->n_rows;
     ensure_rows(eng, n);
-    if (sel) {
+    if (sel && !dev_sel) {
         CU(eng->sel.ensure(std::max<uint64_t>(n, 1) * sizeof(uint32_t)));
         CU(cudaMemcpyAsync(eng->sel.p, sel, n * sizeof(uint32_t), cudaMemcpyHostToDevice,
                            eng->stream));
     }
-    const uint32_t* dsel = sel ? eng->sel.as<uint32_t>() : nullptr;
+    const uint32_t* dsel = dev_sel ? dev_sel : (sel ? eng->sel.as<uint32_t>() : nullptr);
     prep_codebook(eng);
     eng->last_recheck = 0;
     eng->recheck_from_chunks = false;
@@ -1080,6 +1083,106 @@ int tsom_pairwise_sq_dists(tsom_engine* eng, double* out) {
     });
 }
 
+}  // extern "C"
+
+namespace {
+// run the device sampler; true = identity selection (all rows), else the
+// selection is in eng->sampler.sel (device), m rows
+bool sampler_pick(Engine* eng, uint64_t* m) {
+    tsom::SamplerState& smp = eng->sampler;
+    REQUIRE(smp.n == eng->n_rows, TSOM_ERR_INVALID,
+            "sampler: bound data changed since tsom_sampler_init");
+    CU(smp.sel.ensure(std::max<uint64_t>(smp.n, 1) * sizeof(uint32_t)));
+    const int rc = tsom::sampler_select(smp, smp.sel.as<uint32_t>(), m, eng->sm_count, eng->stream);
+    CU(cudaGetLastError());
+    REQUIRE(rc == 0 || rc == -1, TSOM_ERR_CUDA, "sampler: device allocation failed");
+    smp.identity = rc == -1;
+    smp.last_m = *m;
+    return smp.identity;
+}
+
+__global__ void k_iota(uint32_t* out, uint64_t n) {
+    for (uint64_t i = blockIdx.x * (uint64_t)blockDim.x + threadIdx.x; i < n;
+         i += (uint64_t)gridDim.x * blockDim.x)
+        out[i] = (uint32_t)i;
+}
+
+void fill_identity(Engine* eng, uint64_t n) {
+    tsom::SamplerState& smp = eng->sampler;
+    CU(smp.sel.ensure(std::max<uint64_t>(n, 1) * sizeof(uint32_t)));
+    TSOM_LAUNCH(k_iota<<<(unsigned)std::min<uint64_t>((n + 255) / 256, 4096), 256, 0, eng->stream>>>(
+        smp.sel.as<uint32_t>(), n));
+}
+}  // namespace
+
+extern "C" {
+
+int tsom_sampler_init(tsom_engine* eng, int kind, uint64_t m, uint64_t seed, double alpha,
+                      double beta) {
+    return guarded(eng, [&] {
+        CU(cudaSetDevice(eng->device));
+        REQUIRE(kind >= 0 && kind <= 2, TSOM_ERR_INVALID, "unknown sampling kind");
+        REQUIRE(eng->n_rows >= 1, TSOM_ERR_INVALID, "sampler: N must be >= 1 (bind data first)");
+        REQUIRE(kind == 0 || m >= 1, TSOM_ERR_INVALID, "select_random: m must be >= 1");
+        REQUIRE(eng->n_rows < (1ull << 31), TSOM_ERR_INVALID, "sampler: N < 2^31");
+        const int rc = tsom::sampler_setup(eng->sampler, kind, eng->n_rows, m, seed, alpha, beta,
+                                           eng->sm_count);
+        REQUIRE(rc == 0, TSOM_ERR_CUDA, "sampler: device allocation failed");
+        CU(cudaDeviceSynchronize());
+    });
+}
+
+int tsom_sampler_select(tsom_engine* eng, uint32_t* sel_out, uint64_t* m_out) {
+    return guarded(eng, [&] {
+        CU(cudaSetDevice(eng->device));
+        REQUIRE(eng->sampler.kind >= 0, TSOM_ERR_INVALID, "sampler: not initialised");
+        uint64_t m = 0;
+        const bool ident = sampler_pick(eng, &m);
+        if (ident) fill_identity(eng, m);
+        uint32_t status = 0;
+        CU(cudaMemcpyAsync(&status, eng->sampler.misc.as<uint64_t>() + 1, 4, cudaMemcpyDeviceToHost,
+                           eng->stream));
+        if (sel_out && m)
+            CU(cudaMemcpyAsync(sel_out, eng->sampler.sel.p, m * sizeof(uint32_t),
+                               cudaMemcpyDeviceToHost, eng->stream));
+        CU(cudaStreamSynchronize(eng->stream));
+        REQUIRE(!(status & 4u), TSOM_ERR_NUMERICAL, "sampler: random stream slack exceeded");
+        if (m_out) *m_out = m;
+    });
+}
+
+int tsom_sampler_observe(tsom_engine* eng, const double* dist) {
+    return guarded(eng, [&] {
+        CU(cudaSetDevice(eng->device));
+        tsom::SamplerState& smp = eng->sampler;
+        REQUIRE(smp.kind >= 0, TSOM_ERR_INVALID, "sampler: not initialised");
+        if (smp.kind != 2) return;
+        const uint64_t m = smp.last_m;
+        const double* d = eng->dist.as<double>();
+        if (dist) {
+            CU(eng->dist.ensure(std::max<uint64_t>(m, 1) * sizeof(double)));
+            CU(cudaMemcpyAsync(eng->dist.p, dist, m * sizeof(double), cudaMemcpyHostToDevice,
+                               eng->stream));
+            d = eng->dist.as<double>();
+        }
+        tsom::sampler_observe(smp, smp.sel.as<uint32_t>(), m, d, eng->sm_count, eng->stream);
+        CU(cudaStreamSynchronize(eng->stream));
+    });
+}
+
+int tsom_sampler_state(tsom_engine* eng, double* last_error, uint32_t* age) {
+    return guarded(eng, [&] {
+        CU(cudaSetDevice(eng->device));
+        tsom::SamplerState& smp = eng->sampler;
+        REQUIRE(smp.kind == 2, TSOM_ERR_INVALID, "sampler: no adaptive state");
+        if (last_error)
+            CU(cudaMemcpy(last_error, smp.err.p, smp.n * sizeof(double), cudaMemcpyDeviceToHost));
+        if (age) CU(cudaMemcpy(age, smp.age.p, smp.n * sizeof(uint32_t), cudaMemcpyDeviceToHost));
+    });
+}
+
+int tsom_mt_selftest(uint64_t seed, uint64_t jump) { return tsom::mt::selftest(seed, jump); }
+
 int tsom_train_epoch(tsom_engine* eng, double eta, double sigma, double momentum, uint32_t flags) {
     return guarded(eng, [&] {
         CU(cudaSetDevice(eng->device));
@@ -1099,7 +1202,36 @@ int tsom_train_epoch(tsom_engine* eng, double eta, double sigma, double momentum
             eng->max_h = 1.0;
         }
         prep_codebook(eng);
-        accumulate_epoch(eng, nullptr, eng->n_rows, false, false, true);
+        // flags bit 1: the device sampler picks this epoch's rows (select ->
+        // epoch over them -> observe), sampling.hpp:197-211
+        tsom::SamplerState& smp = eng->sampler;
+        const bool sampled = (flags & 2u) != 0;
+        REQUIRE(!sampled || smp.kind >= 0, TSOM_ERR_INVALID,
+                "train_epoch: no device sampler (tsom_sampler_init)");
+        uint64_t m = eng->n_rows;
+        bool ident = true;
+        std::vector<uint32_t> host_sel;
+        if (sampled) {
+            ident = sampler_pick(eng, &m);
+            if (!ident && eng->streamed) {
+                host_sel.resize(m);
+                CU(cudaMemcpyAsync(host_sel.data(), smp.sel.p, m * sizeof(uint32_t),
+                                   cudaMemcpyDeviceToHost, eng->stream));
+                CU(cudaStreamSynchronize(eng->stream));
+            }
+        }
+        const bool want_dist = sampled && smp.kind == 2;
+        if (ident)
+            accumulate_epoch(eng, nullptr, eng->n_rows, want_dist, false, true);
+        else if (eng->streamed)
+            accumulate_epoch(eng, host_sel.data(), m, want_dist, false, true);
+        else
+            accumulate_epoch(eng, nullptr, m, want_dist, false, true, smp.sel.as<uint32_t>());
+        if (want_dist) {
+            if (ident) fill_identity(eng, eng->n_rows);
+            tsom::sampler_observe(smp, ident ? smp.sel.as<uint32_t>() : smp.sel.as<uint32_t>(), m,
+                                  eng->dist.as<double>(), eng->sm_count, eng->stream);
+        }
         smooth(eng, eta);
         int ok = INT_MAX;
         CU(cudaMemcpyAsync(eng->status.p, &ok, sizeof(int), cudaMemcpyHostToDevice, eng->stream));

@@ -138,6 +138,30 @@ int launch_refresh_topology(const float* w, uint32_t P, uint32_t D, int kind, To
                             cudaStream_t st);
 void launch_gram_only(const float* w, uint32_t P, uint32_t D, TopoScratch& s, cudaStream_t st);
 
+// Device sampler (k_sampler.cu, sampling.hpp:183-221)
+struct SamplerState {
+    int kind = -1;  // -1 none, 0 full, 1 random, 2 adaptive
+    uint64_t n = 0, m = 0;
+    double alpha = 1.0, beta = 1.0;
+    uint64_t draws_per_epoch = 0;  // nominal draws (m random, n adaptive)
+    uint32_t G = 0;                // generators per epoch
+    uint64_t L = 0;                // draws per generator
+    uint64_t tail0 = 0;
+    uint32_t tail_len = 0;
+    uint64_t last_m = 0;           // size of the last selection
+    bool identity = false;         // last selection = all rows
+    DevBuf window, jp, seq, draws, tail, misc;  // stream
+    DevBuf err, age, keys, hist;                // adaptive
+    DevBuf first, tidx;                         // random
+    DevBuf bitmap, bcount, sel;                 // selection
+};
+int sampler_setup(SamplerState& s, int kind, uint64_t n, uint64_t m, uint64_t seed, double alpha,
+                  double beta, int sm_count);
+// 0: selection written to `out` (device), -1: identity (all rows), else error
+int sampler_select(SamplerState& s, uint32_t* out, uint64_t* m_out, int sm_count, cudaStream_t st);
+void sampler_observe(SamplerState& s, const uint32_t* sel, uint64_t m, const double* dist,
+                     int sm_count, cudaStream_t st);
+
 struct Engine {
     int device = 0;
     uint32_t P = 0, D = 0;
@@ -223,6 +247,9 @@ struct Engine {
     double max_h = 1.0;                  // max |influence| of the bound matrix
     float t_bmu = 0, t_accum = 0, t_smooth = 0, t_total = 0, t_k1 = 0, t_update = 0;
     bool k1_timed = false, update_timed = false;
+
+    // device sampler
+    SamplerState sampler;
 
     // multi-GPU
     void* nccl_comm = nullptr;

@@ -1,0 +1,586 @@
+// k_sampler.cu — the reference's per-epoch samplers on the device
+// (sampling.hpp:46-157, rng.hpp:33-91), producing the same selections as
+// toposom::Sampler for the same seed.
+//
+// Random stream: the sampler's Rng is std::mt19937_64 seeded with
+// mix_seed(seed, SeedStream::sampler).  An epoch's draws are produced by G
+// generators at once: generator g starts at draw g*L of the epoch, its state
+// obtained from the epoch's start state with the jump polynomial t^(gL) mod
+// phi (mt_jump.cpp): the start window is extended by 19937 + 311 words
+// (k_mt_extend, one CTA), then every generator CTA computes its window as an
+// XOR of shifted copies of that sequence held in shared memory, and twists /
+// tempers its L outputs (k_mt_generate).  The state after the epoch's draws is
+// read from the recorded untempered "tail" words, at the device-side draw count.
+//
+// select_random (sampling.hpp:56-73, Floyd): draw t_k = index(j + 1) for
+// j = n - m + k (rejection sampling, rng.hpp:42-51 — rejections are detected
+// and replayed sequentially); pick_j = t_k unless t_k was picked before, then
+// j.  "Picked before" is decided without the hash set: t_k collides iff an
+// earlier draw equals t_k (first-occurrence table) or t_k is an earlier j that
+// itself collided — a chain through strictly smaller j.
+//
+// select_adaptive (sampling.hpp:101-139): key_i = -log(1 - real01) / w_i with
+// w_i = (e_i/max e)^alpha + (a_i/max a)^beta, unseen rows first; the m
+// smallest (seen, key) pairs win (radix select on 64-bit sortable keys), then
+// the sorted index list.  update_adaptive (:143-157) on the device.
+#include <cuda_runtime.h>
+#include <math_constants.h>
+
+#include <cstdint>
+
+#include "engine.h"
+#include "mt_jump.h"
+
+namespace tsom {
+
+namespace {
+
+constexpr uint64_t kA = 0xB5026F5AA96619E9ULL, kUM = 0xFFFFFFFF80000000ULL,
+                   kLM = 0x7FFFFFFFULL;
+
+__device__ __forceinline__ uint64_t mt_step(uint64_t x0, uint64_t x1, uint64_t xm) {
+    const uint64_t y = (x0 & kUM) | (x1 & kLM);
+    return xm ^ (y >> 1) ^ ((y & 1ULL) ? kA : 0ULL);
+}
+
+__device__ __forceinline__ uint64_t mt_temper(uint64_t x) {
+    x ^= (x >> 29) & 0x5555555555555555ULL;
+    x ^= (x << 17) & 0x71D67FFFEDA60000ULL;
+    x ^= (x << 37) & 0xFFF7EEE000000000ULL;
+    x ^= (x >> 43);
+    return x;
+}
+
+constexpr int kT = 320;  // threads per MT CTA (>= 312)
+
+// one twist of the 312-word window `cur` into `nxt` (both shared), by kT threads
+__device__ __forceinline__ void twist(const uint64_t* cur, uint64_t* nxt) {
+    const int k = threadIdx.x;
+    if (k < 156) nxt[k] = mt_step(cur[k], cur[k + 1], cur[k + 156]);
+    __syncthreads();
+    if (k >= 156 && k < 311) nxt[k] = mt_step(cur[k], cur[k + 1], nxt[k - 156]);
+    if (k == 311) nxt[311] = mt_step(cur[311], nxt[0], nxt[155]);
+    __syncthreads();
+}
+
+}  // namespace
+
+// seq[0..312) = window, seq[312 .. 312 + 312 * twists) = the next untempered words
+__global__ void __launch_bounds__(kT) k_mt_extend(const uint64_t* __restrict__ window,
+                                                  uint32_t twists, uint64_t* __restrict__ seq) {
+    __shared__ uint64_t buf[2][312];
+    const int k = threadIdx.x;
+    if (k < 312) {
+        buf[0][k] = window[k];
+        seq[k] = window[k];
+    }
+    __syncthreads();
+    for (uint32_t t = 0; t < twists; ++t) {
+        twist(buf[t & 1], buf[(t + 1) & 1]);
+        if (k < 312) seq[312 + (size_t)t * 312 + k] = buf[(t + 1) & 1][k];
+    }
+}
+
+// Generator g: window at draw g*L (jump polynomial jp[g], g = 0 -> seq itself),
+// then `L` tempered outputs into draws[g*L ..) (bounded by total).  Untempered
+// words at positions [tail0, tail0 + tail_len) (window coordinates of the epoch
+// start: output q = temper(X[q + 312])) are copied to tail[].
+__global__ void __launch_bounds__(kT) k_mt_generate(const uint64_t* __restrict__ seq,
+                                                    const uint64_t* __restrict__ jp, uint64_t L,
+                                                    uint64_t total, uint64_t* __restrict__ draws,
+                                                    uint64_t tail0, uint32_t tail_len,
+                                                    uint64_t* __restrict__ tail) {
+    extern __shared__ uint64_t sm[];
+    uint64_t* s_seq = sm;                 // [mt::kSeq]
+    uint64_t* s_j = sm + mt::kSeq;        // [312]
+    uint64_t* s_w = s_j + 312;            // [2][312]
+    const int k = threadIdx.x;
+    const uint64_t g = blockIdx.x;
+    const uint64_t q0 = g * L;
+    if (q0 >= total) return;
+    if (g == 0) {
+        if (k < 312) s_w[k] = seq[k];
+    } else {
+        for (int i = k; i < mt::kSeq; i += kT) s_seq[i] = seq[i];
+        if (k < 312) s_j[k] = jp[(size_t)g * 312 + k];
+        __syncthreads();
+        uint64_t acc = 0;
+        if (k < 312) {
+            for (int w = 0; w < 312; ++w) {
+                uint64_t bits = s_j[w];
+                while (bits) {
+                    const int b = __ffsll((long long)bits) - 1;
+                    bits &= bits - 1;
+                    acc ^= s_seq[64 * w + b + k];
+                }
+            }
+            s_w[k] = acc;
+        }
+    }
+    __syncthreads();
+    const uint64_t q1 = min(q0 + L, total);
+    int cur = 0;
+    for (uint64_t q = q0; q < q1; q += 312) {
+        twist(s_w + cur * 312, s_w + (cur ^ 1) * 312);
+        cur ^= 1;
+        if (k < 312) {
+            const uint64_t x = s_w[cur * 312 + k];
+            const uint64_t qq = q + k;  // output index; x = X[qq + 312]
+            if (qq < q1) draws[qq] = mt_temper(x);
+            const uint64_t pos = qq + 312;
+            if (pos >= tail0 && pos < tail0 + tail_len) tail[pos - tail0] = x;
+        }
+    }
+}
+
+// new window = X[delta .. delta + 312): from seq (delta + 312 <= kSeq) or tail
+__global__ void k_mt_advance(const uint64_t* __restrict__ seq, const uint64_t* __restrict__ tail,
+                             uint64_t tail0, uint32_t tail_len, const uint64_t* __restrict__ delta,
+                             uint64_t* __restrict__ window, uint32_t* __restrict__ status) {
+    const uint64_t d = *delta;
+    const int k = threadIdx.x;
+    if (k >= 312) return;
+    const uint64_t pos = d + k;
+    if (pos < (uint64_t)mt::kSeq) {
+        window[k] = seq[pos];
+    } else if (pos >= tail0 && pos < tail0 + tail_len) {
+        window[k] = tail[pos - tail0];
+    } else if (k == 0) {
+        atomicOr(status, 4u);  // draws beyond the generated slack
+    }
+}
+
+// ---------------------------------------------------------------------------
+// select_random
+// ---------------------------------------------------------------------------
+
+// t_k = index(j + 1), j = n - m + k; flags rejections (x >= limit)
+__global__ void k_rand_index(const uint64_t* __restrict__ draws, uint64_t n, uint64_t m,
+                             uint32_t* __restrict__ t, uint32_t* __restrict__ first,
+                             uint32_t* __restrict__ status) {
+    for (uint64_t k = blockIdx.x * (uint64_t)blockDim.x + threadIdx.x; k < m;
+         k += (uint64_t)gridDim.x * blockDim.x) {
+        const uint64_t bound = n - m + k + 1;
+        const uint64_t limit = UINT64_MAX - UINT64_MAX % bound;
+        const uint64_t x = draws[k];
+        if (x >= limit) atomicOr(status, 1u);
+        const uint32_t tk = (uint32_t)(x % bound);
+        t[k] = tk;
+        atomicMin(&first[tk], (uint32_t)k);
+    }
+}
+
+// exact sequential replay when a rejection occurred (rng.hpp:42-51): every
+// index() call consumes draws until one is below its limit
+__global__ void k_rand_replay(const uint64_t* __restrict__ draws, uint64_t avail, uint64_t n,
+                              uint64_t m, uint32_t* __restrict__ t, uint32_t* __restrict__ first,
+                              uint64_t* __restrict__ delta, uint32_t* __restrict__ status) {
+    if (!(*status & 1u)) return;
+    uint64_t r = 0;
+    for (uint64_t k = 0; k < m; ++k) {
+        const uint64_t bound = n - m + k + 1;
+        const uint64_t limit = UINT64_MAX - UINT64_MAX % bound;
+        uint64_t x;
+        do {
+            if (r >= avail) {
+                atomicOr(status, 4u);
+                return;
+            }
+            x = draws[r++];
+        } while (x >= limit);
+        t[k] = (uint32_t)(x % bound);
+    }
+    for (uint64_t k = 0; k < m; ++k) first[t[k]] = 0xFFFFFFFFu;
+    for (uint64_t k = 0; k < m; ++k)
+        if (first[t[k]] == 0xFFFFFFFFu) first[t[k]] = (uint32_t)k;
+    *delta = r;
+}
+
+// Floyd's pick for every k (sampling.hpp:64-70), into the row bitmap
+__global__ void k_rand_pick(const uint32_t* __restrict__ t, const uint32_t* __restrict__ first,
+                            uint64_t n, uint64_t m, uint32_t* __restrict__ bitmap) {
+    const uint64_t j0 = n - m;
+    for (uint64_t k = blockIdx.x * (uint64_t)blockDim.x + threadIdx.x; k < m;
+         k += (uint64_t)gridDim.x * blockDim.x) {
+        // collided(k) = dup(k) || (t_k in [j0, j0 + k) && collided(t_k - j0))
+        uint64_t c = k;
+        bool coll;
+        while (true) {
+            const uint32_t tc = t[c];
+            if (first[tc] < (uint32_t)c) {
+                coll = true;
+                break;
+            }
+            if (tc >= j0 && tc < j0 + c) {
+                c = tc - j0;
+                continue;
+            }
+            coll = false;
+            break;
+        }
+        const uint64_t pick = coll ? j0 + k : (uint64_t)t[k];
+        atomicOr(&bitmap[pick >> 5], 1u << (pick & 31));
+    }
+}
+
+// ---------------------------------------------------------------------------
+// select_adaptive
+// ---------------------------------------------------------------------------
+
+__global__ void k_adapt_max(const double* __restrict__ err, const uint32_t* __restrict__ age,
+                            uint64_t n, unsigned long long* __restrict__ mx) {
+    double me = 0.0;
+    uint32_t ma = 0;
+    for (uint64_t i = blockIdx.x * (uint64_t)blockDim.x + threadIdx.x; i < n;
+         i += (uint64_t)gridDim.x * blockDim.x) {
+        me = fmax(me, err[i]);
+        ma = max(ma, age[i]);
+    }
+    for (int o = 16; o; o >>= 1) {
+        me = fmax(me, __shfl_xor_sync(0xffffffffu, me, o));
+        ma = max(ma, __shfl_xor_sync(0xffffffffu, ma, o));
+    }
+    if ((threadIdx.x & 31) == 0) {
+        atomicMax(&mx[0], (unsigned long long)__double_as_longlong(me));  // errors >= 0
+        atomicMax(&mx[1], (unsigned long long)ma);
+    }
+}
+
+__device__ __forceinline__ double pow_ref(double x, double e) {
+    // pow(x, 1) and pow(x, 2) are exact in the reference's libm as well
+    if (e == 1.0) return x;
+    if (e == 2.0) return x * x;
+    return pow(x, e);
+}
+
+// sortable 64-bit key: (seen << 63) | bits(key), key >= 0 (sampling.hpp:116-133)
+__global__ void k_adapt_keys(const double* __restrict__ err, const uint32_t* __restrict__ age,
+                             const uint64_t* __restrict__ draws, uint64_t n, double alpha,
+                             double beta, const unsigned long long* __restrict__ mx,
+                             unsigned long long* __restrict__ keys) {
+    const double max_err = fmax(__longlong_as_double((long long)mx[0]), 1e-12);
+    const double max_age = fmax((double)mx[1], 1e-12);
+    for (uint64_t i = blockIdx.x * (uint64_t)blockDim.x + threadIdx.x; i < n;
+         i += (uint64_t)gridDim.x * blockDim.x) {
+        const double e = err[i];
+        const double w = pow_ref(e / max_err, alpha) + pow_ref((double)age[i] / max_age, beta);
+        const double u = 1.0 - (double)(draws[i] >> 11) * 0x1.0p-53;
+        double key = w > 0.0 ? -log(u) / w : CUDART_INF;
+        key = fmax(key, 0.0);  // -log(1) = -0
+        const unsigned long long seen = e != 1e30 ? 1ULL : 0ULL;
+        keys[i] = (seen << 63) | (unsigned long long)__double_as_longlong(key);
+    }
+}
+
+// one radix-select digit (`width` <= 12 bits at `shift`) over keys matching
+// the prefix fixed so far above it
+__global__ void k_adapt_hist(const unsigned long long* __restrict__ keys, uint64_t n,
+                             const unsigned long long* __restrict__ sel_state, int shift,
+                             int width, uint32_t* __restrict__ hist) {
+    __shared__ uint32_t h[4096];
+    for (int i = threadIdx.x; i < 4096; i += blockDim.x) h[i] = 0;
+    __syncthreads();
+    const unsigned long long prefix = sel_state[0];
+    const unsigned long long hi_mask = shift + width >= 64 ? 0ULL : (~0ULL << (shift + width));
+    const unsigned long long dmask = (1ULL << width) - 1ULL;
+    for (uint64_t i = blockIdx.x * (uint64_t)blockDim.x + threadIdx.x; i < n;
+         i += (uint64_t)gridDim.x * blockDim.x) {
+        const unsigned long long k = keys[i];
+        if ((k & hi_mask) == prefix) atomicAdd(&h[(k >> shift) & dmask], 1u);
+    }
+    __syncthreads();
+    for (int i = threadIdx.x; i < 4096; i += blockDim.x)
+        if (h[i]) atomicAdd(&hist[i], h[i]);
+}
+
+// sel_state = [prefix, need]: pick the digit where the running count reaches need
+__global__ void k_adapt_digit(uint32_t* __restrict__ hist, int shift,
+                              unsigned long long* __restrict__ sel_state) {
+    if (threadIdx.x != 0) return;
+    unsigned long long need = sel_state[1];
+    unsigned long long cum = 0;
+    int d = 0;
+    for (; d < 4096; ++d) {
+        if (cum + hist[d] >= need) break;
+        cum += hist[d];
+    }
+    if (d == 4096) d = 4095;
+    sel_state[0] |= (unsigned long long)d << shift;
+    sel_state[1] = need - cum;
+    for (int i = 0; i < 4096; ++i) hist[i] = 0;
+}
+
+// rows with key < T, plus the first `need` rows with key == T (ties at the
+// boundary are implementation-defined in the reference; counted in status)
+__global__ void k_adapt_mark(const unsigned long long* __restrict__ keys, uint64_t n,
+                             const unsigned long long* __restrict__ sel_state,
+                             uint32_t* __restrict__ bitmap, unsigned long long* __restrict__ eq) {
+    const unsigned long long T = sel_state[0], need = sel_state[1];
+    for (uint64_t i = blockIdx.x * (uint64_t)blockDim.x + threadIdx.x; i < n;
+         i += (uint64_t)gridDim.x * blockDim.x) {
+        const unsigned long long k = keys[i];
+        bool take = k < T;
+        if (k == T) take = atomicAdd(eq, 1ULL) < need;
+        if (take) atomicOr(&bitmap[i >> 5], 1u << (i & 31));
+    }
+}
+
+// update_adaptive: every age + 1, then selected rows get their distance, age 0
+__global__ void k_adapt_age(uint32_t* __restrict__ age, uint64_t n) {
+    for (uint64_t i = blockIdx.x * (uint64_t)blockDim.x + threadIdx.x; i < n;
+         i += (uint64_t)gridDim.x * blockDim.x)
+        age[i] += 1u;
+}
+__global__ void k_adapt_observe(const uint32_t* __restrict__ sel, uint64_t m,
+                                const double* __restrict__ dist, double* __restrict__ err,
+                                uint32_t* __restrict__ age) {
+    for (uint64_t k = blockIdx.x * (uint64_t)blockDim.x + threadIdx.x; k < m;
+         k += (uint64_t)gridDim.x * blockDim.x) {
+        const uint32_t i = sel[k];
+        err[i] = dist[k];
+        age[i] = 0u;
+    }
+}
+
+// ---------------------------------------------------------------------------
+// bitmap -> sorted index list
+// ---------------------------------------------------------------------------
+
+__global__ void k_bitmap_count(const uint32_t* __restrict__ bitmap, uint64_t words,
+                               uint32_t* __restrict__ bcount) {
+    // one block = 1024 words
+    __shared__ uint32_t s[32];
+    const uint64_t w = blockIdx.x * 1024ull + threadIdx.x;
+    uint32_t c = w < words ? __popc(bitmap[w]) : 0u;
+    for (int o = 16; o; o >>= 1) c += __shfl_xor_sync(0xffffffffu, c, o);
+    if ((threadIdx.x & 31) == 0) s[threadIdx.x >> 5] = c;
+    __syncthreads();
+    if (threadIdx.x < 32) {
+        uint32_t v = s[threadIdx.x];
+        for (int o = 16; o; o >>= 1) v += __shfl_xor_sync(0xffffffffu, v, o);
+        if (threadIdx.x == 0) bcount[blockIdx.x] = v;
+    }
+}
+
+__global__ void k_block_scan(uint32_t* __restrict__ bcount, uint64_t nb,
+                             unsigned long long* __restrict__ total) {
+    if (threadIdx.x != 0) return;
+    unsigned long long run = 0;
+    for (uint64_t b = 0; b < nb; ++b) {
+        const uint32_t c = bcount[b];
+        bcount[b] = (uint32_t)run;
+        run += c;
+    }
+    *total = run;
+}
+
+__global__ void k_bitmap_write(const uint32_t* __restrict__ bitmap, uint64_t words,
+                               const uint32_t* __restrict__ boff, uint32_t* __restrict__ out) {
+    __shared__ uint32_t wsum[32];
+    const uint64_t w = blockIdx.x * 1024ull + threadIdx.x;
+    const uint32_t bits = w < words ? bitmap[w] : 0u;
+    const uint32_t c = __popc(bits);
+    // exclusive scan of c over the block
+    uint32_t inc = c;
+    const int lane = threadIdx.x & 31, wid = threadIdx.x >> 5;
+    for (int o = 1; o < 32; o <<= 1) {
+        const uint32_t v = __shfl_up_sync(0xffffffffu, inc, o);
+        if (lane >= o) inc += v;
+    }
+    if (lane == 31) wsum[wid] = inc;
+    __syncthreads();
+    if (wid == 0) {
+        uint32_t v = wsum[lane];
+        for (int o = 1; o < 32; o <<= 1) {
+            const uint32_t u = __shfl_up_sync(0xffffffffu, v, o);
+            if (lane >= o) v += u;
+        }
+        wsum[lane] = v;
+    }
+    __syncthreads();
+    uint32_t pos = boff[blockIdx.x] + inc - c + (wid ? wsum[wid - 1] : 0u);
+    uint32_t b = bits;
+    while (b) {
+        const int i = __ffs(b) - 1;
+        b &= b - 1;
+        out[pos++] = (uint32_t)(w * 32 + i);
+    }
+}
+
+// ---------------------------------------------------------------------------
+// host orchestration
+// ---------------------------------------------------------------------------
+
+namespace {
+constexpr uint32_t kSlack = 4096;  // extra draws for rejection replays
+}
+
+int sampler_setup(SamplerState& s, int kind, uint64_t n, uint64_t m, uint64_t seed, double alpha,
+                  double beta, int sm_count) {
+    s.kind = kind;
+    s.n = n;
+    s.m = m;
+    s.alpha = alpha;
+    s.beta = beta;
+    s.draws_per_epoch = 0;
+    if (kind == 1 && m < n) s.draws_per_epoch = m;
+    if (kind == 2) s.draws_per_epoch = n;
+    // Rng(seed, SeedStream::sampler): mt19937_64(mix_seed(seed, 3)) (rng.hpp:12-37)
+    uint64_t z = seed + 0x9e3779b97f4a7c15ULL * (3 + 1);
+    z = (z ^ (z >> 30)) * 0xbf58476d1ce4e5b9ULL;
+    z = (z ^ (z >> 27)) * 0x94d049bb133111ebULL;
+    uint64_t w[312];
+    mt::seed_window(z ^ (z >> 31), w);
+    if (s.window.ensure(312 * 8) != cudaSuccess) return 4;
+    if (cudaMemcpy(s.window.p, w, 312 * 8, cudaMemcpyHostToDevice) != cudaSuccess) return 4;
+    if (s.misc.ensure(64) != cudaSuccess) return 4;
+    if (!s.draws_per_epoch) return 0;
+    const uint64_t total = s.draws_per_epoch + kSlack;
+    uint64_t G = (total + 65535) / 65536;
+    G = std::max<uint64_t>(1, std::min<uint64_t>(G, 2ull * (uint64_t)sm_count));
+    const uint64_t L = (total + G - 1) / G;
+    s.G = (uint32_t)G;
+    s.L = L;
+    // jump polynomials t^(gL) mod phi, g = 1..G-1 (host, once per configuration)
+    std::vector<uint64_t> jp(G * 312, 0);
+    if (G > 1) {
+        const std::vector<uint64_t> J = mt::jump_poly(L);
+        std::vector<uint64_t> cur = J;
+        for (uint64_t g = 1; g < G; ++g) {
+            std::copy(cur.begin(), cur.end(), jp.begin() + g * 312);
+            if (g + 1 < G) cur = mt::mul_poly(cur, J);
+        }
+    }
+    if (s.jp.ensure(jp.size() * 8) != cudaSuccess) return 4;
+    if (cudaMemcpy(s.jp.p, jp.data(), jp.size() * 8, cudaMemcpyHostToDevice) != cudaSuccess) return 4;
+    const uint32_t twists = (mt::kSeq - 312 + 311) / 312;
+    if (s.seq.ensure((312 + (size_t)twists * 312) * 8) != cudaSuccess) return 4;
+    if (s.draws.ensure(total * 8) != cudaSuccess) return 4;
+    s.tail0 = s.draws_per_epoch;
+    s.tail_len = 312 + kSlack;
+    if (s.tail.ensure((size_t)s.tail_len * 8) != cudaSuccess) return 4;
+    if (s.misc.ensure(64) != cudaSuccess) return 4;
+    if (kind == 2) {
+        if (s.err.ensure(n * 8) != cudaSuccess || s.age.ensure(n * 4) != cudaSuccess ||
+            s.keys.ensure(n * 8) != cudaSuccess || s.hist.ensure(4096 * 4) != cudaSuccess)
+            return 4;
+        std::vector<double> e(1, 1e30);
+        // last_error = kUnseenError (sampling.hpp:81, 91), age = 0
+        const size_t chunk = 1 << 20;
+        std::vector<double> init(std::min<uint64_t>(n, chunk), 1e30);
+        for (uint64_t i = 0; i < n; i += chunk)
+            if (cudaMemcpy(s.err.as<double>() + i, init.data(), std::min<uint64_t>(chunk, n - i) * 8,
+                           cudaMemcpyHostToDevice) != cudaSuccess)
+                return 4;
+        if (cudaMemset(s.age.p, 0, n * 4) != cudaSuccess) return 4;
+        if (cudaMemset(s.hist.p, 0, 4096 * 4) != cudaSuccess) return 4;
+    }
+    if (kind == 1) {
+        if (s.first.ensure(n * 4) != cudaSuccess || s.tidx.ensure(m * 4) != cudaSuccess) return 4;
+    }
+    return 0;
+}
+
+// the epoch's draws (k_mt_extend + k_mt_generate); delta (device) = draws used
+static void generate_draws(SamplerState& s, cudaStream_t st) {
+    const uint32_t twists = (mt::kSeq - 312 + 311) / 312;
+    TSOM_LAUNCH(k_mt_extend<<<1, kT, 0, st>>>(s.window.as<uint64_t>(), twists, s.seq.as<uint64_t>()));
+    const size_t smem = (mt::kSeq + 312 + 2 * 312) * 8;
+    static bool attr = false;
+    if (!attr) {
+        cudaFuncSetAttribute(k_mt_generate, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+        attr = true;
+    }
+    const uint64_t total = s.draws_per_epoch + kSlack;
+    TSOM_LAUNCH(k_mt_generate<<<s.G, kT, smem, st>>>(s.seq.as<uint64_t>(), s.jp.as<uint64_t>(), s.L,
+                                                     total, s.draws.as<uint64_t>(), s.tail0,
+                                                     s.tail_len, s.tail.as<uint64_t>()));
+}
+
+static void bitmap_to_list(SamplerState& s, uint64_t n, uint32_t* out, cudaStream_t st) {
+    const uint64_t words = (n + 31) / 32;
+    const uint64_t nb = (words + 1023) / 1024;
+    TSOM_LAUNCH(k_bitmap_count<<<(unsigned)nb, 1024, 0, st>>>(s.bitmap.as<uint32_t>(), words,
+                                                               s.bcount.as<uint32_t>()));
+    TSOM_LAUNCH(k_block_scan<<<1, 32, 0, st>>>(s.bcount.as<uint32_t>(), nb,
+                                               reinterpret_cast<unsigned long long*>(
+                                                   s.misc.as<uint64_t>() + 3)));
+    TSOM_LAUNCH(k_bitmap_write<<<(unsigned)nb, 1024, 0, st>>>(s.bitmap.as<uint32_t>(), words,
+                                                               s.bcount.as<uint32_t>(), out));
+}
+
+// misc: [0] delta (draws used), [1] status (u32: 1 rejection, 2 boundary tie,
+// 4 slack exceeded), [2] tie count, [3] selected count, [4..5] adaptive max,
+// [6..7] radix state
+int sampler_select(SamplerState& s, uint32_t* out, uint64_t* m_out, int sm_count, cudaStream_t st) {
+    const uint64_t n = s.n;
+    uint64_t* misc = s.misc.as<uint64_t>();
+    cudaMemsetAsync(misc, 0, 64, st);
+    if (s.kind == 0 || (s.kind == 1 && s.m >= n)) {
+        *m_out = n;
+        return -1;  // identity selection: the caller uses "all rows"
+    }
+    const uint64_t words = (n + 31) / 32;
+    const uint64_t nb = (words + 1023) / 1024;
+    if (s.bitmap.ensure(words * 4) != cudaSuccess || s.bcount.ensure(nb * 4 + 4) != cudaSuccess)
+        return 4;
+    cudaMemsetAsync(s.bitmap.p, 0, words * 4, st);
+    generate_draws(s, st);
+    const unsigned grid = (unsigned)std::max<uint64_t>(
+        1, std::min<uint64_t>((std::max(s.m, n) + 255) / 256, (uint64_t)sm_count * 16));
+    uint32_t* status = reinterpret_cast<uint32_t*>(misc + 1);
+    if (s.kind == 1) {
+        const uint64_t m = s.m;
+        cudaMemsetAsync(s.first.p, 0xFF, n * 4, st);
+        cudaMemcpyAsync(misc, &m, 8, cudaMemcpyHostToDevice, st);  // delta = m (no rejection)
+        TSOM_LAUNCH(k_rand_index<<<grid, 256, 0, st>>>(s.draws.as<uint64_t>(), n, m,
+                                                       s.tidx.as<uint32_t>(), s.first.as<uint32_t>(),
+                                                       status));
+        TSOM_LAUNCH(k_rand_replay<<<1, 1, 0, st>>>(s.draws.as<uint64_t>(), s.draws_per_epoch + kSlack,
+                                                   n, m, s.tidx.as<uint32_t>(),
+                                                   s.first.as<uint32_t>(), misc, status));
+        TSOM_LAUNCH(k_rand_pick<<<grid, 256, 0, st>>>(s.tidx.as<uint32_t>(), s.first.as<uint32_t>(), n,
+                                                      m, s.bitmap.as<uint32_t>()));
+    } else {
+        const uint64_t m = std::min(s.m, n);
+        cudaMemcpyAsync(misc, &n, 8, cudaMemcpyHostToDevice, st);  // delta = n draws
+        auto* mx = reinterpret_cast<unsigned long long*>(misc + 4);
+        TSOM_LAUNCH(k_adapt_max<<<grid, 256, 0, st>>>(s.err.as<double>(), s.age.as<uint32_t>(), n, mx));
+        TSOM_LAUNCH(k_adapt_keys<<<grid, 256, 0, st>>>(
+            s.err.as<double>(), s.age.as<uint32_t>(), s.draws.as<uint64_t>(), n, s.alpha, s.beta, mx,
+            reinterpret_cast<unsigned long long*>(s.keys.p)));
+        auto* rs = reinterpret_cast<unsigned long long*>(misc + 6);
+        const unsigned long long st0[2] = {0ULL, (unsigned long long)m};
+        cudaMemcpyAsync(rs, st0, 16, cudaMemcpyHostToDevice, st);
+        // digits of the 64-bit key: bits 52-63, 40-51, 28-39, 16-27, 4-15, 0-3
+        const int shifts[6] = {52, 40, 28, 16, 4, 0}, widths[6] = {12, 12, 12, 12, 12, 4};
+        for (int d = 0; d < 6; ++d) {
+            TSOM_LAUNCH(k_adapt_hist<<<grid, 256, 0, st>>>(
+                reinterpret_cast<const unsigned long long*>(s.keys.p), n, rs, shifts[d], widths[d],
+                s.hist.as<uint32_t>()));
+            TSOM_LAUNCH(k_adapt_digit<<<1, 32, 0, st>>>(s.hist.as<uint32_t>(), shifts[d], rs));
+        }
+        TSOM_LAUNCH(k_adapt_mark<<<grid, 256, 0, st>>>(
+            reinterpret_cast<const unsigned long long*>(s.keys.p), n, rs, s.bitmap.as<uint32_t>(),
+            reinterpret_cast<unsigned long long*>(misc + 2)));
+    }
+    bitmap_to_list(s, n, out, st);
+    // the stream continues after the draws actually used
+    TSOM_LAUNCH(k_mt_advance<<<1, 320, 0, st>>>(s.seq.as<uint64_t>(), s.tail.as<uint64_t>(), s.tail0,
+                                                s.tail_len, misc, s.window.as<uint64_t>(), status));
+    *m_out = s.kind == 1 ? s.m : std::min(s.m, n);
+    return 0;
+}
+
+void sampler_observe(SamplerState& s, const uint32_t* sel, uint64_t m, const double* dist,
+                     int sm_count, cudaStream_t st) {
+    if (s.kind != 2) return;
+    const unsigned grid = (unsigned)std::max<uint64_t>(
+        1, std::min<uint64_t>((s.n + 255) / 256, (uint64_t)sm_count * 16));
+    TSOM_LAUNCH(k_adapt_age<<<grid, 256, 0, st>>>(s.age.as<uint32_t>(), s.n));
+    if (m)
+        TSOM_LAUNCH(k_adapt_observe<<<grid, 256, 0, st>>>(sel, m, dist, s.err.as<double>(),
+                                                          s.age.as<uint32_t>()));
+}
+
+}  // namespace tsom
