@@ -293,21 +293,59 @@ __global__ void k_adapt_hist(const unsigned long long* __restrict__ keys, uint64
         if (h[i]) atomicAdd(&hist[i], h[i]);
 }
 
-// sel_state = [prefix, need]: pick the digit where the running count reaches need
-__global__ void k_adapt_digit(uint32_t* __restrict__ hist, int shift,
-                              unsigned long long* __restrict__ sel_state) {
-    if (threadIdx.x != 0) return;
-    unsigned long long need = sel_state[1];
-    unsigned long long cum = 0;
-    int d = 0;
-    for (; d < 4096; ++d) {
-        if (cum + hist[d] >= need) break;
-        cum += hist[d];
+// sel_state = [prefix, need]: pick the digit where the running count reaches
+// need (one block of 1024 threads, 4 bins each, block-wide inclusive scan)
+__global__ void __launch_bounds__(1024) k_adapt_digit(uint32_t* __restrict__ hist, int shift,
+                                                      unsigned long long* __restrict__ sel_state) {
+    __shared__ unsigned long long wsum[32];
+    __shared__ int found;
+    const int t = threadIdx.x, lane = t & 31, wid = t >> 5;
+    const unsigned long long need = sel_state[1];
+    uint32_t h[4];
+    unsigned long long loc = 0;
+#pragma unroll
+    for (int i = 0; i < 4; ++i) {
+        h[i] = hist[4 * t + i];
+        loc += h[i];
     }
-    if (d == 4096) d = 4095;
-    sel_state[0] |= (unsigned long long)d << shift;
-    sel_state[1] = need - cum;
-    for (int i = 0; i < 4096; ++i) hist[i] = 0;
+    unsigned long long inc = loc;
+    for (int o = 1; o < 32; o <<= 1) {
+        const unsigned long long v = __shfl_up_sync(0xffffffffu, inc, o);
+        if (lane >= o) inc += v;
+    }
+    if (lane == 31) wsum[wid] = inc;
+    if (t == 0) found = 4095;
+    __syncthreads();
+    if (wid == 0) {
+        unsigned long long v = wsum[lane];
+        for (int o = 1; o < 32; o <<= 1) {
+            const unsigned long long u = __shfl_up_sync(0xffffffffu, v, o);
+            if (lane >= o) v += u;
+        }
+        wsum[lane] = v;
+    }
+    __syncthreads();
+    // exclusive prefix before this thread's 4 bins
+    unsigned long long cum = inc - loc + (wid ? wsum[wid - 1] : 0ULL);
+    int d = -1;
+    unsigned long long before = 0;
+#pragma unroll
+    for (int i = 0; i < 4; ++i) {
+        if (d < 0 && cum + h[i] >= need) {
+            d = 4 * t + i;
+            before = cum;
+        }
+        cum += h[i];
+    }
+    if (d >= 0) atomicMin(&found, d);
+    __syncthreads();
+    if (d >= 0 && d == found) {
+        sel_state[0] |= (unsigned long long)d << shift;
+        sel_state[1] = need - before;
+    }
+    __syncthreads();
+#pragma unroll
+    for (int i = 0; i < 4; ++i) hist[4 * t + i] = 0;
 }
 
 // rows with key < T, plus the first `need` rows with key == T (ties at the
@@ -558,7 +596,7 @@ int sampler_select(SamplerState& s, uint32_t* out, uint64_t* m_out, int sm_count
             TSOM_LAUNCH(k_adapt_hist<<<grid, 256, 0, st>>>(
                 reinterpret_cast<const unsigned long long*>(s.keys.p), n, rs, shifts[d], widths[d],
                 s.hist.as<uint32_t>()));
-            TSOM_LAUNCH(k_adapt_digit<<<1, 32, 0, st>>>(s.hist.as<uint32_t>(), shifts[d], rs));
+            TSOM_LAUNCH(k_adapt_digit<<<1, 1024, 0, st>>>(s.hist.as<uint32_t>(), shifts[d], rs));
         }
         TSOM_LAUNCH(k_adapt_mark<<<grid, 256, 0, st>>>(
             reinterpret_cast<const unsigned long long*>(s.keys.p), n, rs, s.bitmap.as<uint32_t>(),
