@@ -349,6 +349,11 @@ def run_gpu_arm(args):
     }
     if e2e:
         line["e2e"] = e2e
+    if rank == 0 and world == 1 and not args.no_c4:
+        if eng is not None:
+            eng.close()
+        torch.cuda.empty_cache()
+        line["c4"] = run_c4_leg(local)
     if rank == 0 and world == 1 and not args.no_cpu:
         v, cores, kind, sample, _ = cpu_reference(step_seconds=6.0)
         line["cpu_baseline"] = {"value": v, "unit": UNIT, "cores": cores, "kind": kind,
@@ -358,6 +363,74 @@ def run_gpu_arm(args):
     if world > 1:
         dist.destroy_process_group()
     return 0
+
+
+def run_c4_leg(local, n=100_000_000, rho=0.1, epochs=EPOCHS, warm=2):
+    """Config c4 on one GPU: 1024-node RNG-topology SOM, 1e8 x 50
+    GMM rows resident in HBM, adaptive sampler with rho = 0.1 on the device
+    (select -> epoch over the selected rows -> observe), RNG graph refreshed on
+    the device on the reference schedule.  Every per-epoch step is on the GPU;
+    timed with CUDA events on the engine stream."""
+    import numpy as np
+    import torch
+
+    import paper_2604_26555_b200 as tsom
+    from paper_2604_26555_b200.hostref import (RefreshState, Rng, init_sample_draw,
+                                               resolved_sigma0, schedule_value)
+    seed = 2608
+    r = Rng(seed, "synth")
+    centres = np.array([[-4.0 + 8.0 * r.real01() for _ in range(D)] for _ in range(16)],
+                       np.float32)
+    g = torch.Generator(device=f"cuda:{local}").manual_seed(seed)
+    x = torch.randn((n, D), device=f"cuda:{local}", generator=g, dtype=torch.float32)
+    comp = torch.randint(0, 16, (n,), device=f"cuda:{local}", generator=g)
+    x += torch.from_numpy(centres).to(x.device)[comp]
+    del comp
+
+    class _Rows:  # init_sample_draw over device rows: only the picked rows come back
+        shape = (n, D)
+
+        def __getitem__(self, idx):
+            return x[torch.from_numpy(np.asarray(idx)).to(x.device)].cpu().numpy()
+
+    e = tsom.Engine(P, D, device=local)
+    e.bind_device(x.data_ptr(), n)
+    e.set_codebook(init_sample_draw(_Rows(), P, seed))
+    m = max(1, int(np.floor(n * rho)))
+    e.sampler_init("adaptive", m, seed)
+    sigma0 = resolved_sigma0("rng", 0, 0, 0.0)
+    refresh = RefreshState(max(1, epochs // 10), 1.5, 25)
+    stream = torch.cuda.ExternalStream(e.stream, device=f"cuda:{local}")
+    ev0, ev1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+
+    def epoch(t):
+        tt = t % epochs
+        if refresh.should_refresh(tt):
+            e.refresh_topology("rng")
+            refresh.mark(tt)
+        eta = schedule_value(0.5, "linear", tt, epochs, 1e-4)
+        sigma = schedule_value(sigma0, "linear", tt, epochs, 0.3)
+        e.train_epoch(eta, sigma, sampled=True)
+
+    for t in range(warm):
+        epoch(t)
+    refresh = RefreshState(max(1, epochs // 10), 1.5, 25)
+    torch.cuda.synchronize()
+    ev0.record(stream)
+    for t in range(epochs):
+        epoch(t)
+    ev1.record(stream)
+    torch.cuda.synchronize()
+    secs = ev0.elapsed_time(ev1) / 1e3
+    s, c = e.qe()
+    e.close()
+    del x
+    torch.cuda.empty_cache()
+    return {"workload": "c4: 1024-node RNG-topology SOM (device refresh), 1e8 x 50 GMM rows "
+                        "resident, adaptive sampler rho=0.1 on the device, 10 epochs",
+            "value": m * epochs / secs, "unit": "selected samples*epochs/s",
+            "rows_considered_per_s": n * epochs / secs, "ms_per_epoch": secs * 1e3 / epochs,
+            "qe_after": s / c}
 
 
 def roofline_peak(kernel, pk):
@@ -385,6 +458,7 @@ def main():
     ap.add_argument("--kernel", type=int, default=0, help="0 auto, 1 SIMT, 2 tcgen05 3xTF32, 3 tcgen05 3xFP16")
     ap.add_argument("--no-e2e", action="store_true")
     ap.add_argument("--no-cpu", action="store_true")
+    ap.add_argument("--no-c4", action="store_true", help="skip the c4 (1e8 rows, adaptive) leg")
     args = ap.parse_args()
     if args.impl == "reference":
         return run_reference_arm(args)
