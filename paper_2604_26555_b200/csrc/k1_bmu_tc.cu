@@ -32,8 +32,9 @@
 //   warp 0      : producer — bulk copies (mbarrier complete_tx)
 //   warp 1      : MMA issuer — one elected thread
 //   warp 2      : TMEM allocator (2 accumulator buffers x gn columns)
-//   warps 4..11 : two sets of 4 epilogue warps, draining the two accumulator
-//                 buffers alternately (warp q of a set owns TMEM lanes 32q..)
+//   warps 4..11 : two sets of 4 epilogue warps; both drain every tile, set h
+//                 taking node columns [128h, 128h + 128) (warp q of a set owns
+//                 TMEM lanes 32q.., i.e. tile rows 32q..32q+31)
 #include <cuda_fp16.h>
 #include <cuda_runtime.h>
 #include <math_constants.h>
@@ -57,11 +58,7 @@ struct EpiCfg {
     static constexpr int kThreads = 128 + kSets * 128;  // 4 role warps + the sets
     static constexpr int kCPS = 8 / kSets;              // 32-column chunks per set (gn = 256)
 };
-constexpr uint32_t kEpiThreads = 128;   // threads per epilogue set
 constexpr int kMaxStages = 4;
-// main pass: true = the two epilogue sets alternate tiles (each drains all gn
-// columns of its tile); false = both sets split the columns of every tile
-constexpr bool kAltSets = false;  // (register-resident passes need <= 4 chunks per set)
 
 __device__ __forceinline__ float fmin3f(float a, float b, float c) {
     float r;
@@ -357,13 +354,11 @@ __global__ void __launch_bounds__(EpiCfg<kKind>::kThreads, 1)
               uint32_t groups, uint32_t gn, uint32_t D, uint32_t stages,
               const uint8_t* __restrict__ wsplit, const float* __restrict__ xn2,
               const float* __restrict__ w2max, const float* __restrict__ scale, TieWin win,
-              const uint32_t* __restrict__ rmask, float* __restrict__ part, uint32_t one,
-              uint32_t neg1, uint32_t dbg, uint32_t mc) {
+              const uint32_t* __restrict__ rmask, float* __restrict__ part, uint32_t dbg,
+              uint32_t mc) {
     // mc > 1: the CTAs of a cluster are the mc codebook groups of the same tile
     // sequence; each loads 1/mc of every A tile and multicasts it to all, so the
     // tile crosses L2 -> SM once per cluster instead of once per group.
-    // one = 1, neg1 = 0xFFFFFFFF at run time: opaque to the compiler, so the
-    // epilogue's integer adds stay IMADs (FMA pipe) instead of IADD3 (ALU pipe)
     extern __shared__ __align__(1024) uint8_t smem[];
     constexpr int kSets = EpiCfg<kKind>::kSets, kCPS = EpiCfg<kKind>::kCPS;
     const TcGeom geo = tc_geom(kKind, D);
@@ -379,7 +374,6 @@ __global__ void __launch_bounds__(EpiCfg<kKind>::kThreads, 1)
     uint64_t* tempty_bar = tfull_bar + 2;         // [2] accumulator drained
     uint64_t* w_bar = tfull_bar + 4;              // codebook group landed
     uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(w_bar + 1);
-    // w_bar + 2 .. : [2][kSets-1][128] float2 set-h -> set-0 exchange (main pass)
 
     const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
     const uint32_t g = blockIdx.x % groups;
@@ -394,7 +388,7 @@ __global__ void __launch_bounds__(EpiCfg<kKind>::kThreads, 1)
         }
         for (int a = 0; a < 2; ++a) {
             mbar_init(&tfull_bar[a], 1);
-            mbar_init(&tempty_bar[a], (kEnum || kAltSets) ? 4u : 4u * kSets);  // one per warp
+            mbar_init(&tempty_bar[a], kEnum ? 4u : 4u * kSets);  // one arrival per warp
         }
         mbar_init(w_bar, 1);
         asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
@@ -511,14 +505,14 @@ __global__ void __launch_bounds__(EpiCfg<kKind>::kThreads, 1)
             //     a in [256, 512) <=> exactly one node (the minimum) lies in
             //     the window, and then id = a - 256.  Two FMA-pipe ops per
             //     value, no ALU op, no index bookkeeping.
-            // Set 1 hands (b, a) to set 0 through shared memory; set 0 writes
-            // [B1 | id or 0xFFFFFFFF (several nodes in the window) | -].
-            const uint32_t c_begin = kAltSets ? 0u : set * nch / kSets;
-            const uint32_t c_count =
-                (dbg & 1u) ? 0u : (kAltSets ? nch : (set + 1) * nch / kSets - c_begin);
-            uint32_t acc = kAltSets ? set : 0, acc_phase = 0;
-            const uint32_t t0 = cta_in_group + (kAltSets ? set * ctas_per_group : 0);
-            const uint32_t tstep = kAltSets ? 2 * ctas_per_group : ctas_per_group;
+            // The set's slice is loaded into registers once (the accumulator
+            // is released right after), and the set writes [b | id within the
+            // slice, or 0xFFFFFFFF when several nodes lie in the window] as
+            // sub-group g * kSets + set for k_merge_fast.
+            const uint32_t c_begin = set * nch / kSets;
+            const uint32_t c_count = (dbg & 1u) ? 0u : (set + 1) * nch / kSets - c_begin;
+            uint32_t acc = 0, acc_phase = 0;
+            const uint32_t t0 = cta_in_group, tstep = ctas_per_group;
             // ||x||^2 of the row, prefetched one tile ahead (hides the load latency)
             uint64_t pos_next = (uint64_t)t0 * kTcTileM + row;
             float x2_next = pos_next < n ? __ldg(xn2 + pos_next) : 0.0f;
@@ -584,19 +578,17 @@ __global__ void __launch_bounds__(EpiCfg<kKind>::kThreads, 1)
                 if (lane == 0 && q == 0) TSOM_TRACE(4 + 3 * (set & 1), it_);
                 // a = 256 count + sum(local ids); decode: exactly one -> global id
                 const float asum = (a[0] + a[1]) + (a[2] + a[3]);
-                uint32_t code = 0xFFFFFFFFu;
+                uint32_t code = 0xFFFFFFFFu;  // id relative to the set's first column
                 if (asum >= 256.0f && asum < 512.0f && asum == floorf(asum))
-                    code = (uint32_t)asum - 256u + c_begin * 32u;
+                    code = (uint32_t)asum - 256u;
                 // each set writes its column slice as its own sub-group
                 // (k_merge_fast combines them: no exchange, no named barrier)
                 if (pos < n) {
                     float* pg = part + (size_t)(g * kSets + set) * 2 * n;
                     pg[pos] = b;
-                    pg[n + pos] = __uint_as_float(code == 0xFFFFFFFFu ? code : code - c_begin * 32u);
+                    pg[n + pos] = __uint_as_float(code);
                 }
-                if (kAltSets) {
-                    acc_phase ^= 1;
-                } else if (++acc == 2) {
+                if (++acc == 2) {
                     acc = 0;
                     acc_phase ^= 1;
                 }
@@ -699,8 +691,7 @@ cudaError_t launch_bmu_tc(int kind, const void* tiles, uint64_t n, const uint32_
     if (smem > smem_optin) return cudaErrorInvalidConfiguration;
     using KernT = void (*)(const uint8_t*, uint64_t, const uint32_t*, uint32_t, uint32_t, uint32_t,
                            uint32_t, const uint8_t*, const float*, const float*, const float*,
-                           TieWin, const uint32_t*, float*, uint32_t, uint32_t, uint32_t,
-                           uint32_t);
+                           TieWin, const uint32_t*, float*, uint32_t, uint32_t);
     KernT kern;
     int slot;
     if (kind == kTcTf32) {
@@ -767,8 +758,7 @@ cudaError_t launch_bmu_tc(int kind, const void* tiles, uint64_t n, const uint32_
     ++g_launches;
     const cudaError_t e = cudaLaunchKernelEx(
         &cfg, kern, static_cast<const uint8_t*>(tiles), n, dev_n, groups, gn, D, stages,
-        static_cast<const uint8_t*>(wsplit), xn2, w2max, scale, win, rmask, part, 1u,
-        0xFFFFFFFFu, g_k1_debug, mc);
+        static_cast<const uint8_t*>(wsplit), xn2, w2max, scale, win, rmask, part, g_k1_debug, mc);
     if (e != cudaSuccess) return e;
     return cudaGetLastError();
 }
