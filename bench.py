@@ -416,9 +416,11 @@ def run_c4_leg(local, n=100_000_000, rho=0.1, epochs=EPOCHS, warm=2):
         epoch(t)
     refresh = RefreshState(max(1, epochs // 10), 1.5, 25)
     torch.cuda.synchronize()
+    phases = []
     ev0.record(stream)
     for t in range(epochs):
         epoch(t)
+        phases.append(e.timing_detail())
     ev1.record(stream)
     torch.cuda.synchronize()
     secs = ev0.elapsed_time(ev1) / 1e3
@@ -430,6 +432,7 @@ def run_c4_leg(local, n=100_000_000, rho=0.1, epochs=EPOCHS, warm=2):
                         "resident, adaptive sampler rho=0.1 on the device, 10 epochs",
             "value": m * epochs / secs, "unit": "selected samples*epochs/s",
             "rows_considered_per_s": n * epochs / secs, "ms_per_epoch": secs * 1e3 / epochs,
+            "phase_ms": {k: round(statistics.mean(p[k] for p in phases), 3) for k in phases[0]},
             "qe_after": s / c}
 
 
@@ -459,9 +462,16 @@ def main():
     ap.add_argument("--no-e2e", action="store_true")
     ap.add_argument("--no-cpu", action="store_true")
     ap.add_argument("--no-c4", action="store_true", help="skip the c4 (1e8 rows, adaptive) leg")
+    ap.add_argument("--only-c4", action="store_true", help=argparse.SUPPRESS)
     args = ap.parse_args()
     if args.impl == "reference":
         return run_reference_arm(args)
+    if args.only_c4:  # diagnostics: the c4 leg alone
+        import torch
+        torch.cuda.set_device(0)
+        print(json.dumps(run_c4_leg(0, epochs=args.steps if args.steps < 50 else EPOCHS)),
+              flush=True)
+        return 0
     return run_gpu_arm(args)
 
 

@@ -207,7 +207,8 @@ int tsom_last_timing(const tsom_engine* eng, float* bmu_ms, float* accum_ms, flo
                      float* total_ms);
 /* Detail of the last epoch (ms): [0] BMU kernel (K1) alone, [1] BMU phase incl.
  * merge + exact re-check, [2] accumulation + reduce (+ allreduce), [3] smoothing,
- * [4] device update (tsom_train_epoch), [5] total. */
+ * [4] device update (tsom_train_epoch), [5] total (sampler excluded), [6] device sampler
+ * (sampled tsom_train_epoch). */
 int tsom_last_timing_detail(const tsom_engine* eng, float out[8]);
 /* Number of CUDA kernels this library has launched in this process. */
 uint64_t tsom_kernel_launches(void);

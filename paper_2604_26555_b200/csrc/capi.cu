@@ -542,6 +542,8 @@ void record_timing(Engine* eng) {
     eng->t_update = 0.0f;
     if (eng->k1_timed) cudaEventElapsedTime(&eng->t_k1, eng->ev[8], eng->ev[9]);
     if (eng->update_timed) cudaEventElapsedTime(&eng->t_update, eng->ev[7], eng->ev[10]);
+    eng->t_sample = 0.0f;
+    if (eng->sample_timed) cudaEventElapsedTime(&eng->t_sample, eng->ev[11], eng->ev[0]);
     cudaEventElapsedTime(&eng->t_bmu, eng->ev[0], eng->ev[1]);
     cudaEventElapsedTime(&eng->t_accum, eng->ev[1], eng->ev[6]);
     cudaEventElapsedTime(&eng->t_smooth, eng->ev[6], eng->ev[7]);
@@ -1211,7 +1213,9 @@ int tsom_train_epoch(tsom_engine* eng, double eta, double sigma, double momentum
         uint64_t m = eng->n_rows;
         bool ident = true;
         std::vector<uint32_t> host_sel;
+        eng->sample_timed = sampled;
         if (sampled) {
+            CU(cudaEventRecord(eng->ev[11], eng->stream));
             ident = sampler_pick(eng, &m);
             if (!ident && eng->streamed) {
                 host_sel.resize(m);
@@ -1309,8 +1313,8 @@ int tsom_last_timing(const tsom_engine* eng, float* bmu_ms, float* accum_ms, flo
 
 int tsom_last_timing_detail(const tsom_engine* eng, float out[8]) {
     if (!eng || !out) return TSOM_ERR_INVALID;
-    const float v[8] = {eng->t_k1,    eng->t_bmu,    eng->t_accum, eng->t_smooth,
-                        eng->t_update, eng->t_total, 0.0f,         0.0f};
+    const float v[8] = {eng->t_k1,    eng->t_bmu,    eng->t_accum,  eng->t_smooth,
+                        eng->t_update, eng->t_total, eng->t_sample, 0.0f};
     std::memcpy(out, v, sizeof(v));
     return TSOM_OK;
 }

@@ -246,7 +246,8 @@ struct Engine {
     bool recheck_from_chunks = false;
     double max_h = 1.0;                  // max |influence| of the bound matrix
     float t_bmu = 0, t_accum = 0, t_smooth = 0, t_total = 0, t_k1 = 0, t_update = 0;
-    bool k1_timed = false, update_timed = false;
+    float t_sample = 0;  // device sampler before the epoch (sampled tsom_train_epoch)
+    bool k1_timed = false, update_timed = false, sample_timed = false;
 
     // device sampler
     SamplerState sampler;

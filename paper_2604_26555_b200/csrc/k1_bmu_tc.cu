@@ -244,41 +244,71 @@ void launch_prep_wsplit(int kind, const float* w, uint32_t P, uint32_t D, const 
 // (their results are ignored).  xn2[f] = ||x||^2 rounded up (unscaled): the
 // row's own error window (tie_thr).
 
+// One block (256 threads) per 128-row tile: the tile's rows are gathered into
+// shared memory with coalesced loads (consecutive threads read consecutive
+// floats of a row), row norms come from shared memory, and every 16-byte K
+// core of the tile is written by one thread (consecutive threads = consecutive
+// rows of a core: coalesced stores).
+constexpr int kSplitThreads = 256;
+
 template <int kKind>
-__global__ void k_split_rows(const float* __restrict__ x, const uint32_t* __restrict__ sel,
-                             const uint32_t* __restrict__ idx, const uint32_t* __restrict__ dev_n,
-                             uint64_t n_host, uint32_t D, const float* __restrict__ scale,
-                             TieWin win, uint8_t* __restrict__ tiles, float* __restrict__ xn2) {
+__global__ void __launch_bounds__(kSplitThreads) k_split_rows(
+    const float* __restrict__ x, const uint32_t* __restrict__ sel,
+    const uint32_t* __restrict__ idx, const uint32_t* __restrict__ dev_n, uint64_t n_host,
+    uint32_t D, const float* __restrict__ scale, TieWin win, uint8_t* __restrict__ tiles,
+    float* __restrict__ xn2) {
+    extern __shared__ float srow[];                 // [128][D + 1]
+    __shared__ uint64_t rbase[kTcTileM];            // row offsets (floats)
+    __shared__ float snorm[kTcTileM];
     const uint64_t n = dev_n ? min((uint64_t)*dev_n, n_host) : n_host;
     const uint64_t ntiles = (n + kTcTileM - 1) / kTcTileM;
-    const int r = threadIdx.x;  // 128 threads, one row each
     const TcGeom geo = tc_geom(kKind, D);
     const float s = kKind == kTcF16 ? scale[0] : 1.0f;
+    const float S = kKind == kTcF16 ? scale[1] : 1.0f;
+    const uint32_t ld = D + 1;
+    const int t = threadIdx.x;
     for (uint64_t tile = blockIdx.x; tile < ntiles; tile += gridDim.x) {
-        const uint64_t f = tile * kTcTileM + r;
-        uint8_t* base = tiles + tile * geo.tile_bytes;
-        const bool valid = f < n;
-        const float* src = nullptr;
-        if (valid) {
-            const uint64_t pos = idx ? (uint64_t)idx[f] : f;
-            src = x + (sel ? (uint64_t)sel[pos] : pos) * D;
+        const uint64_t f0 = tile * kTcTileM;
+        const uint32_t rows = (uint32_t)(n - f0 < (uint64_t)kTcTileM ? n - f0 : (uint64_t)kTcTileM);
+        __syncthreads();  // previous tile's shared memory fully consumed
+        if (t < kTcTileM && (uint32_t)t < rows) {
+            const uint64_t pos = idx ? (uint64_t)idx[f0 + t] : f0 + t;
+            rbase[t] = (sel ? (uint64_t)sel[pos] : pos) * D;
         }
-        double nrm = 0.0;
-        if (valid)
-            for (uint32_t k = 0; k < D; ++k) nrm += (double)src[k] * (double)src[k];
+        __syncthreads();
+        for (uint32_t e = t; e < rows * D; e += kSplitThreads) {
+            const uint32_t r = e / D, k = e - r * D;
+            srow[r * ld + k] = x[rbase[r] + k];
+        }
+        __syncthreads();
+        if (t < kTcTileM) {
+            double nrm = 0.0;
+            if ((uint32_t)t < rows)
+                for (uint32_t k = 0; k < D; ++k) {
+                    const double v = (double)srow[t * ld + k];
+                    nrm += v * v;
+                }
+            snorm[t] = (float)nrm;
+            if (xn2 && (uint32_t)t < rows)
+                xn2[f0 + t] = tie_xpart((float)nrm * 1.0000003f, S, win);
+        }
+        __syncthreads();
+        uint8_t* base = tiles + tile * geo.tile_bytes;
         if (kKind == kTcTf32) {
-            // x' = [x | 1 | 1 | ||x||^2 | 0..]
+            // x' = [x | 1 | 1 | ||x||^2 | 0..], hi half then lo half
             float* fb = reinterpret_cast<float*>(base);
-            for (uint32_t kc = 0; kc < kTcKPad / 4; ++kc) {
+            for (uint32_t e = t; e < (uint32_t)(kTcKPad / 4) * kTcTileM; e += kSplitThreads) {
+                const uint32_t kc = e / kTcTileM, r = e % kTcTileM;
+                const bool valid = r < rows;
                 float hi[4], lo[4];
 #pragma unroll
                 for (int q = 0; q < 4; ++q) {
                     const uint32_t k = kc * 4 + q;
                     float val = 0.0f;
                     if (valid) {
-                        if (k < D) val = src[k];
+                        if (k < D) val = srow[r * ld + k];
                         else if (k == D || k == D + 1) val = 1.0f;
-                        else if (k == D + 2) val = (float)nrm;
+                        else if (k == D + 2) val = snorm[r];
                     }
                     hi[q] = tf32_trunc(val);
                     lo[q] = val - hi[q];
@@ -290,18 +320,24 @@ __global__ void k_split_rows(const float* __restrict__ x, const uint32_t* __rest
             }
         } else {
             // A = [xh | xl | xh | n_hi, n_lo, 1, 1, 1 | 0..], x scaled by s
-            const double ns = nrm * (double)s * (double)s;
-            const __half nh = __double2half(ns);
-            const __half nl = __double2half(ns - (double)__half2float(nh));
-            for (uint32_t kc = 0; kc < geo.kpad / 8; ++kc) {
+            for (uint32_t e = t; e < (geo.kpad / 8) * kTcTileM; e += kSplitThreads) {
+                const uint32_t kc = e / kTcTileM, r = e % kTcTileM;
+                const bool valid = r < rows;
                 __align__(16) __half h[8];
+                __half nh = __float2half(0.0f), nl = nh;
+                if (valid && kc * 8 + 8 > 3 * D) {
+                    const double ns = (double)snorm[r] * (double)s * (double)s;
+                    nh = __double2half(ns);
+                    nl = __double2half(ns - (double)__half2float(nh));
+                }
 #pragma unroll
                 for (int q = 0; q < 8; ++q) {
                     const uint32_t k = kc * 8 + q;
                     __half v = __float2half(0.0f);
                     if (valid) {
                         if (k < 3 * D) {
-                            const float xv = src[k % D] * s;
+                            const uint32_t kk = k < D ? k : (k < 2 * D ? k - D : k - 2 * D);
+                            const float xv = srow[r * ld + kk] * s;
                             const __half xh = __float2half_rn(xv);
                             v = (k >= D && k < 2 * D) ? __float2half_rn(xv - __half2float(xh)) : xh;
                         } else if (k == 3 * D) {
@@ -318,8 +354,6 @@ __global__ void k_split_rows(const float* __restrict__ x, const uint32_t* __rest
                     *reinterpret_cast<uint4*>(h);
             }
         }
-        if (xn2 && valid)
-            xn2[f] = tie_xpart((float)nrm * 1.0000003f, kKind == kTcF16 ? scale[1] : 1.0f, win);
     }
 }
 
@@ -328,13 +362,14 @@ void launch_split_rows(int kind, const float* x, const uint32_t* sel, const uint
                        float* xn2, cudaStream_t st, const uint32_t* dev_n) {
     if (n == 0) return;
     uint64_t tiles_n = (n + kTcTileM - 1) / kTcTileM;
-    if (tiles_n > 148ull * 64) tiles_n = 148ull * 64;
+    if (tiles_n > 148ull * 16) tiles_n = 148ull * 16;
     uint8_t* t = static_cast<uint8_t*>(tiles);
+    const size_t smem = (size_t)kTcTileM * (D + 1) * sizeof(float);
     if (kind == kTcTf32)
-        TSOM_LAUNCH(k_split_rows<kTcTf32><<<(unsigned)tiles_n, kTcTileM, 0, st>>>(
+        TSOM_LAUNCH(k_split_rows<kTcTf32><<<(unsigned)tiles_n, kSplitThreads, smem, st>>>(
             x, sel, idx, dev_n, n, D, scale, win, t, xn2));
     else
-        TSOM_LAUNCH(k_split_rows<kTcF16><<<(unsigned)tiles_n, kTcTileM, 0, st>>>(
+        TSOM_LAUNCH(k_split_rows<kTcF16><<<(unsigned)tiles_n, kSplitThreads, smem, st>>>(
             x, sel, idx, dev_n, n, D, scale, win, t, xn2));
 }
 
