@@ -218,12 +218,21 @@ def run_gpu_arm(args):
         eng.set_option(_lib.TSOM_OPT_BMU_KERNEL, args.kernel)
     eng.bind(host)
     active_kernel = eng.active_bmu_kernel
-    if world > 1:
-        uid = [eng.comm_unique_id() if rank == 0 else None]
-        dist.broadcast_object_list(uid, src=0)
-        eng.comm_init(uid[0], rank, world)
+
+    def attach_comm(e):
+        # one NCCL communicator per engine: rank 0's unique id over the gloo group
+        if world > 1 or args.force_comm:
+            uid = [e.comm_unique_id() if rank == 0 else None]
+            if world > 1:
+                dist.broadcast_object_list(uid, src=0)
+            e.comm_init(uid[0], rank, world)
+
+    attach_comm(eng)
     # init_weights(sample_draw) (trainer.hpp:192-211) over rank 0's rows, same on every rank
-    w0 = init_sample_draw(host_gmm_rows(n, SEED) if rank else host, P, SEED)
+    w0 = [init_sample_draw(host, P, SEED) if rank == 0 else None]
+    if world > 1:
+        dist.broadcast_object_list(w0, src=0)
+    w0 = w0[0]
     eng.set_codebook(w0)
     eng.set_topology_distance(lattice_dist("hex", *P_GRID))
     sigma0 = resolved_sigma0("hex", *P_GRID)
@@ -273,13 +282,16 @@ def run_gpu_arm(args):
     # wall-clock region; then the same workload through the reference's own
     # training loop with the CudaExecutor plugin (libtsom_dropin.so).
     e2e = None
-    if rank == 0 and world == 1 and not args.no_e2e:
+    if not args.no_e2e:
         def cabi_run(epochs):
+            if world > 1:
+                dist.barrier()
             t0 = time.perf_counter()
             e = tsom.Engine(P, D, device=local)
             if args.kernel:
                 e.set_option(_lib.TSOM_OPT_BMU_KERNEL, args.kernel)
             e.bind(host)
+            attach_comm(e)
             e.set_codebook(w0)
             e.set_topology_distance(lattice_dist("hex", *P_GRID))
             t1 = time.perf_counter()
@@ -293,17 +305,26 @@ def run_gpu_arm(args):
             t3 = time.perf_counter()
             return t3 - t0, {"setup_s": t1 - t0, "epochs_s": t2 - t1, "close_s": t3 - t2}
         cabi_run(1)  # warm-up (allocations, module load)
-        secs, split = min((cabi_run(EPOCHS) for _ in range(3)), key=lambda r: r[0])
+        runs = []
+        for _ in range(3):
+            secs_r, split_r = cabi_run(EPOCHS)
+            if world > 1:  # the job ends when the slowest rank ends
+                tm = torch.tensor([secs_r], dtype=torch.float64)
+                dist.all_reduce(tm, op=dist.ReduceOp.MAX)
+                secs_r = float(tm.item())
+            runs.append((secs_r, split_r))
+        secs, split = min(runs, key=lambda r: r[0])
         h2d = n * D * 4 + P * D * 4 + P * P * 8
         d2h = P * D * 4
-        e2e = {"value": n * EPOCHS / secs, "unit": UNIT,
+        e2e = {"value": n * world * EPOCHS / secs, "unit": UNIT,
                "h2d_bytes_per_step": int(h2d / EPOCHS), "d2h_bytes_per_step": int(d2h / EPOCHS),
                "path": "C-ABI tsom_bind_host_data + 10 x tsom_train_epoch + tsom_get_codebook "
-                       "from pinned host rows, wall clock incl. engine creation",
+                       "from pinned host rows, wall clock incl. engine creation (and the "
+                       "NCCL communicator when N > 1), max over ranks",
                "seconds_per_call": secs, "epochs_per_call": EPOCHS, "best_of": 3,
                "split_s": split}
         from paper_2604_26555_b200 import dropin
-        if dropin.available():
+        if world == 1 and dropin.available():
             cfg = dropin.TrainConfig(topology="hex", grid_w=P_GRID[0], grid_h=P_GRID[1],
                                      n_iters=EPOCHS, seed=SEED)
             warm = dropin.TrainConfig(topology="hex", grid_w=P_GRID[0], grid_h=P_GRID[1],
@@ -463,6 +484,7 @@ def main():
     ap.add_argument("--no-cpu", action="store_true")
     ap.add_argument("--no-c4", action="store_true", help="skip the c4 (1e8 rows, adaptive) leg")
     ap.add_argument("--only-c4", action="store_true", help=argparse.SUPPRESS)
+    ap.add_argument("--force-comm", action="store_true", help=argparse.SUPPRESS)  # NCCL at N=1
     args = ap.parse_args()
     if args.impl == "reference":
         return run_reference_arm(args)
