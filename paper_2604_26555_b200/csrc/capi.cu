@@ -205,6 +205,7 @@ void run_bmu(Engine* eng, const float* x, const uint32_t* sel, uint64_t n, const
                                eng->sm_count, eng->smem_optin, eng->stream));
         CU(cudaEventRecord(eng->ev[9], eng->stream));
         eng->k1_timed = true;
+        tsom::sampler_pregenerate(eng->sampler, eng->ev[9]);
         tsom::launch_merge_fast(eng->part.as<float>(), n, groups, tsom::kTcEpiSets, gn, tiles_xn2,
                                 w2, scale, win,
                                 eng->bmu.as<uint32_t>(), eng->ties.as<uint32_t>(),
@@ -241,6 +242,7 @@ void run_bmu(Engine* eng, const float* x, const uint32_t* sel, uint64_t n, const
                               eng->flags.as<uint32_t>(), eng->sm_count, eng->stream);
         CU(cudaEventRecord(eng->ev[9], eng->stream));
         eng->k1_timed = true;
+        tsom::sampler_pregenerate(eng->sampler, eng->ev[9]);
     }
     CU(cudaGetLastError());
     tsom::launch_rescan(x, sel, eng->w.as<float>(), eng->P, eng->D, eng->flags.as<uint32_t>(), n,
@@ -611,6 +613,7 @@ int tsom_destroy(tsom_engine* eng) {
     if (eng->nccl_comm && g_nccl.commDestroy) g_nccl.commDestroy((ncclComm_t)eng->nccl_comm);
     if (eng->host_registered) cudaHostUnregister(const_cast<float*>(eng->host_rows));
     close_shards(eng);
+    tsom::sampler_release(eng->sampler);
     for (int s2 = 0; s2 < 2; ++s2) {
         if (eng->pinned[s2]) cudaFreeHost(eng->pinned[s2]);
         if (eng->ev_pin[s2]) cudaEventDestroy(eng->ev_pin[s2]);

@@ -150,7 +150,15 @@ struct SamplerState {
     uint32_t tail_len = 0;
     uint64_t last_m = 0;           // size of the last selection
     bool identity = false;         // last selection = all rows
-    DevBuf window, jp, seq, draws, tail, misc;  // stream
+    DevBuf window, jp, misc;                    // stream state, jump polynomials
+    // draws are double-buffered: while an epoch trains on buffer `cur`, the
+    // next epoch's draws are generated into the other one on `side`
+    DevBuf seqb[2], drawsb[2], tailb[2];
+    int cur = 0;
+    bool pre = false;       // buffer `cur` already holds (or is receiving) this epoch's draws
+    bool want_gen = false;  // buffer `cur` still to be generated (after the next BMU kernel)
+    cudaStream_t side = nullptr;
+    cudaEvent_t ev_adv = nullptr, ev_gen = nullptr;
     DevBuf err, age, keys, hist;                // adaptive
     DevBuf first, tidx;                         // random
     DevBuf bitmap, bcount, sel;                 // selection
@@ -161,6 +169,10 @@ int sampler_setup(SamplerState& s, int kind, uint64_t n, uint64_t m, uint64_t se
 int sampler_select(SamplerState& s, uint32_t* out, uint64_t* m_out, int sm_count, cudaStream_t st);
 void sampler_observe(SamplerState& s, const uint32_t* sel, uint64_t m, const double* dist,
                      int sm_count, cudaStream_t st);
+void sampler_release(SamplerState& s);
+// start generating the next epoch's draws on the sampler's side stream once
+// `after` (recorded on the engine stream) completes
+void sampler_pregenerate(SamplerState& s, cudaEvent_t after);
 
 struct Engine {
     int device = 0;

@@ -455,6 +455,9 @@ constexpr uint32_t kSlack = 4096;  // extra draws for rejection replays
 
 int sampler_setup(SamplerState& s, int kind, uint64_t n, uint64_t m, uint64_t seed, double alpha,
                   double beta, int sm_count) {
+    if (s.side) cudaStreamSynchronize(s.side);  // no generation of a previous setup in flight
+    s.pre = false;
+    s.want_gen = false;
     s.kind = kind;
     s.n = n;
     s.m = m;
@@ -492,12 +495,20 @@ int sampler_setup(SamplerState& s, int kind, uint64_t n, uint64_t m, uint64_t se
     if (s.jp.ensure(jp.size() * 8) != cudaSuccess) return 4;
     if (cudaMemcpy(s.jp.p, jp.data(), jp.size() * 8, cudaMemcpyHostToDevice) != cudaSuccess) return 4;
     const uint32_t twists = (mt::kSeq - 312 + 311) / 312;
-    if (s.seq.ensure((312 + (size_t)twists * 312) * 8) != cudaSuccess) return 4;
-    if (s.draws.ensure(total * 8) != cudaSuccess) return 4;
     s.tail0 = s.draws_per_epoch;
     s.tail_len = 312 + kSlack;
-    if (s.tail.ensure((size_t)s.tail_len * 8) != cudaSuccess) return 4;
-    if (s.misc.ensure(64) != cudaSuccess) return 4;
+    for (int b = 0; b < 2; ++b) {
+        if (s.seqb[b].ensure((312 + (size_t)twists * 312) * 8) != cudaSuccess) return 4;
+        if (s.drawsb[b].ensure(total * 8) != cudaSuccess) return 4;
+        if (s.tailb[b].ensure((size_t)s.tail_len * 8) != cudaSuccess) return 4;
+    }
+    s.cur = 0;
+    s.pre = false;
+    if (!s.side && cudaStreamCreateWithFlags(&s.side, cudaStreamNonBlocking) != cudaSuccess) return 4;
+    if (!s.ev_adv && cudaEventCreateWithFlags(&s.ev_adv, cudaEventDisableTiming) != cudaSuccess)
+        return 4;
+    if (!s.ev_gen && cudaEventCreateWithFlags(&s.ev_gen, cudaEventDisableTiming) != cudaSuccess)
+        return 4;
     if (kind == 2) {
         if (s.err.ensure(n * 8) != cudaSuccess || s.age.ensure(n * 4) != cudaSuccess ||
             s.keys.ensure(n * 8) != cudaSuccess || s.hist.ensure(4096 * 4) != cudaSuccess)
@@ -520,9 +531,10 @@ int sampler_setup(SamplerState& s, int kind, uint64_t n, uint64_t m, uint64_t se
 }
 
 // the epoch's draws (k_mt_extend + k_mt_generate); delta (device) = draws used
-static void generate_draws(SamplerState& s, cudaStream_t st) {
+static void generate_draws(SamplerState& s, int b, cudaStream_t st) {
     const uint32_t twists = (mt::kSeq - 312 + 311) / 312;
-    TSOM_LAUNCH(k_mt_extend<<<1, kT, 0, st>>>(s.window.as<uint64_t>(), twists, s.seq.as<uint64_t>()));
+    TSOM_LAUNCH(k_mt_extend<<<1, kT, 0, st>>>(s.window.as<uint64_t>(), twists,
+                                              s.seqb[b].as<uint64_t>()));
     const size_t smem = (mt::kSeq + 312 + 2 * 312) * 8;
     static bool attr = false;
     if (!attr) {
@@ -530,9 +542,10 @@ static void generate_draws(SamplerState& s, cudaStream_t st) {
         attr = true;
     }
     const uint64_t total = s.draws_per_epoch + kSlack;
-    TSOM_LAUNCH(k_mt_generate<<<s.G, kT, smem, st>>>(s.seq.as<uint64_t>(), s.jp.as<uint64_t>(), s.L,
-                                                     total, s.draws.as<uint64_t>(), s.tail0,
-                                                     s.tail_len, s.tail.as<uint64_t>()));
+    TSOM_LAUNCH(k_mt_generate<<<s.G, kT, smem, st>>>(s.seqb[b].as<uint64_t>(), s.jp.as<uint64_t>(),
+                                                     s.L, total, s.drawsb[b].as<uint64_t>(),
+                                                     s.tail0, s.tail_len,
+                                                     s.tailb[b].as<uint64_t>()));
 }
 
 static void bitmap_to_list(SamplerState& s, uint64_t n, uint32_t* out, cudaStream_t st) {
@@ -563,7 +576,14 @@ int sampler_select(SamplerState& s, uint32_t* out, uint64_t* m_out, int sm_count
     if (s.bitmap.ensure(words * 4) != cudaSuccess || s.bcount.ensure(nb * 4 + 4) != cudaSuccess)
         return 4;
     cudaMemsetAsync(s.bitmap.p, 0, words * 4, st);
-    generate_draws(s, st);
+    const int b = s.cur;
+    if (s.pre)
+        cudaStreamWaitEvent(st, s.ev_gen, 0);  // generated during the previous epoch
+    else
+        generate_draws(s, b, st);
+    s.pre = false;
+    s.want_gen = false;
+    const uint64_t* draws = s.drawsb[b].as<uint64_t>();
     const unsigned grid = (unsigned)std::max<uint64_t>(
         1, std::min<uint64_t>((std::max(s.m, n) + 255) / 256, (uint64_t)sm_count * 16));
     uint32_t* status = reinterpret_cast<uint32_t*>(misc + 1);
@@ -571,10 +591,10 @@ int sampler_select(SamplerState& s, uint32_t* out, uint64_t* m_out, int sm_count
         const uint64_t m = s.m;
         cudaMemsetAsync(s.first.p, 0xFF, n * 4, st);
         cudaMemcpyAsync(misc, &m, 8, cudaMemcpyHostToDevice, st);  // delta = m (no rejection)
-        TSOM_LAUNCH(k_rand_index<<<grid, 256, 0, st>>>(s.draws.as<uint64_t>(), n, m,
+        TSOM_LAUNCH(k_rand_index<<<grid, 256, 0, st>>>(draws, n, m,
                                                        s.tidx.as<uint32_t>(), s.first.as<uint32_t>(),
                                                        status));
-        TSOM_LAUNCH(k_rand_replay<<<1, 1, 0, st>>>(s.draws.as<uint64_t>(), s.draws_per_epoch + kSlack,
+        TSOM_LAUNCH(k_rand_replay<<<1, 1, 0, st>>>(draws, s.draws_per_epoch + kSlack,
                                                    n, m, s.tidx.as<uint32_t>(),
                                                    s.first.as<uint32_t>(), misc, status));
         TSOM_LAUNCH(k_rand_pick<<<grid, 256, 0, st>>>(s.tidx.as<uint32_t>(), s.first.as<uint32_t>(), n,
@@ -585,7 +605,7 @@ int sampler_select(SamplerState& s, uint32_t* out, uint64_t* m_out, int sm_count
         auto* mx = reinterpret_cast<unsigned long long*>(misc + 4);
         TSOM_LAUNCH(k_adapt_max<<<grid, 256, 0, st>>>(s.err.as<double>(), s.age.as<uint32_t>(), n, mx));
         TSOM_LAUNCH(k_adapt_keys<<<grid, 256, 0, st>>>(
-            s.err.as<double>(), s.age.as<uint32_t>(), s.draws.as<uint64_t>(), n, s.alpha, s.beta, mx,
+            s.err.as<double>(), s.age.as<uint32_t>(), draws, n, s.alpha, s.beta, mx,
             reinterpret_cast<unsigned long long*>(s.keys.p)));
         auto* rs = reinterpret_cast<unsigned long long*>(misc + 6);
         const unsigned long long st0[2] = {0ULL, (unsigned long long)m};
@@ -604,10 +624,37 @@ int sampler_select(SamplerState& s, uint32_t* out, uint64_t* m_out, int sm_count
     }
     bitmap_to_list(s, n, out, st);
     // the stream continues after the draws actually used
-    TSOM_LAUNCH(k_mt_advance<<<1, 320, 0, st>>>(s.seq.as<uint64_t>(), s.tail.as<uint64_t>(), s.tail0,
-                                                s.tail_len, misc, s.window.as<uint64_t>(), status));
+    TSOM_LAUNCH(k_mt_advance<<<1, 320, 0, st>>>(s.seqb[b].as<uint64_t>(), s.tailb[b].as<uint64_t>(),
+                                                s.tail0, s.tail_len, misc,
+                                                s.window.as<uint64_t>(), status));
+    // the next epoch's draws depend only on the advanced stream state; they are
+    // generated on the side stream while this epoch trains (sampler_pregenerate,
+    // started once the BMU kernel has finished so it does not compete with it)
+    s.cur = b ^ 1;
+    s.want_gen = true;
     *m_out = s.kind == 1 ? s.m : std::min(s.m, n);
     return 0;
+}
+
+void sampler_pregenerate(SamplerState& s, cudaEvent_t after) {
+    if (!s.want_gen) return;
+    s.want_gen = false;
+    cudaStreamWaitEvent(s.side, after, 0);
+    generate_draws(s, s.cur, s.side);
+    cudaEventRecord(s.ev_gen, s.side);
+    s.pre = true;
+}
+
+void sampler_release(SamplerState& s) {
+    if (s.side) cudaStreamSynchronize(s.side);
+    for (DevBuf* d : {&s.window, &s.jp, &s.misc, &s.seqb[0], &s.seqb[1], &s.drawsb[0],
+                      &s.drawsb[1], &s.tailb[0], &s.tailb[1], &s.err, &s.age, &s.keys, &s.hist,
+                      &s.first, &s.tidx, &s.bitmap, &s.bcount, &s.sel})
+        d->release();
+    if (s.ev_adv) cudaEventDestroy(s.ev_adv);
+    if (s.ev_gen) cudaEventDestroy(s.ev_gen);
+    if (s.side) cudaStreamDestroy(s.side);
+    s = SamplerState();
 }
 
 void sampler_observe(SamplerState& s, const uint32_t* sel, uint64_t m, const double* dist,
