@@ -16,15 +16,20 @@
 // keep the reference's types and message prefixes.
 #pragma once
 
+#include <algorithm>
+#include <atomic>
 #include <cmath>
 #include <cstdint>
+#include <limits>
 #include <memory>
 #include <stdexcept>
 #include <string>
+#include <thread>
 #include <vector>
 
 #include "toposom/metrics.hpp"
 #include "toposom/trainer.hpp"
+#include "toposom/tune.hpp"
 #include "tsom_b200.h"
 
 namespace toposom_b200 {
@@ -181,6 +186,58 @@ inline double quantization_error_cuda(const toposom::SomModel& model, const Data
     uint64_t count = 0;
     eng.check(tsom_qe(eng.h, nullptr, 0, &sum, &count));
     return sum / static_cast<double>(count);
+}
+
+/// run_study (tune.hpp:125-159) with every trial trained by the GPU executor
+/// and scored by the GPU QE.  Trials are the reference's (sample_trial with
+/// Rng(mix_seed(seed, trial), SeedStream::trial), tune.hpp:77-93, 140-143) and
+/// come back in the reference's order (seed-major); up to `concurrency` trials
+/// run at once, each on its own engine and CUDA stream, so the many small
+/// trainings of a search overlap on the device.  A failing trial records the
+/// +infinity sentinel and the study continues, as in the reference.
+inline std::vector<toposom::TrialRecord> run_study_cuda(
+    const toposom::SearchSpace& space, const toposom::StudySpec& spec,
+    const DataMatrix& train_data, const DataMatrix& holdout_data, unsigned concurrency = 4,
+    CudaOptions opts = {}) {
+    using Record = toposom::TrialRecord;
+    if (spec.n_trials < 1) throw std::invalid_argument("run_study: n_trials must be >= 1");
+    if (spec.seeds.empty()) throw std::invalid_argument("run_study: need at least one seed");
+    space.validate();
+    std::vector<Record> records;
+    for (const std::uint64_t seed : spec.seeds)
+        for (std::size_t trial = 0; trial < spec.n_trials; ++trial) {
+            toposom::Rng trial_rng(toposom::mix_seed(seed, trial), toposom::SeedStream::trial);
+            Record rec;
+            rec.seed = seed;
+            rec.trial_index = trial;
+            rec.config = toposom::sample_trial(space, spec.base_config, trial_rng);
+            rec.config.seed = seed;
+            records.push_back(std::move(rec));
+        }
+    std::atomic<std::size_t> next{0};
+    auto worker = [&] {
+        for (std::size_t i = next++; i < records.size(); i = next++) {
+            Record& rec = records[i];
+            try {
+                toposom::Sampler sampler(spec.sampling, spec.budget, train_data.rows, rec.seed,
+                                         spec.sampler_alpha, spec.sampler_beta);
+                auto result = train_cuda(rec.config, train_data, sampler, opts);
+                rec.qe_train = quantization_error_cuda(result.first, train_data, opts.device);
+                rec.qe_holdout = quantization_error_cuda(result.first, holdout_data, opts.device);
+            } catch (const std::exception& e) {
+                rec.failed = true;
+                rec.failure = e.what();
+                rec.qe_train = std::numeric_limits<double>::infinity();
+                rec.qe_holdout = std::numeric_limits<double>::infinity();
+            }
+        }
+    };
+    std::vector<std::thread> pool;
+    const unsigned T = std::max(1u, std::min<unsigned>(concurrency, (unsigned)records.size()));
+    for (unsigned t = 1; t < T; ++t) pool.emplace_back(worker);
+    worker();
+    for (auto& th : pool) th.join();
+    return records;
 }
 
 }  // namespace toposom_b200

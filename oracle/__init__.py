@@ -375,6 +375,9 @@ class RefChecker(PortChecker):
                                       C.c_double, C.c_double, sz, C.c_void_p, _u32p,
                                       np.ctypeslib.ndpointer(np.uintp)]
         L.ref_train.argtypes = [C.POINTER(_Cfg), _f32p, sz, sz, _f32p, C.c_void_p, C.c_void_p]
+        L.ref_run_study.argtypes = [C.POINTER(_Cfg), sz, np.ctypeslib.ndpointer(np.uint64), sz,
+                                    _f32p, sz, _f32p, sz, sz, _f64p, _f64p,
+                                    np.ctypeslib.ndpointer(np.uint8)]
 
     def _check(self, st):
         if st:
@@ -487,6 +490,18 @@ class RefChecker(PortChecker):
             res.append(out[off: off + int(ms[t])].copy())
             off += int(ms[t])
         return res
+
+    def run_study(self, base: SomConfig, n_trials, seeds, train, holdout):
+        """run_study (tune.hpp:125-159) with the default SearchSpace: per trial
+        (seed-major) qe_train, qe_holdout, failed."""
+        train, holdout = _f32(train), _f32(holdout)
+        seeds = np.ascontiguousarray(seeds, np.uint64)
+        k = n_trials * len(seeds)
+        qt, qh, fl = np.empty(k), np.empty(k), np.zeros(k, np.uint8)
+        self._check(self.lib.ref_run_study(C.byref(_to_cfg(base)), n_trials, seeds, len(seeds),
+                                           train, train.shape[0], holdout, holdout.shape[0],
+                                           train.shape[1], qt, qh, fl))
+        return qt, qh, fl.astype(bool)
 
     def train(self, cfg: SomConfig, data, log_qe=False):
         data = _f32(data)

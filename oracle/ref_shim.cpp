@@ -15,6 +15,7 @@
 #include "toposom/metrics.hpp"
 #include "toposom/parallel.hpp"
 #include "toposom/trainer.hpp"
+#include "toposom/tune.hpp"
 
 using namespace toposom;
 
@@ -279,30 +280,63 @@ int ref_sampler_run(int kind, int budget_fixed, std::uint64_t m0, double rho, st
     });
 }
 
+// SomConfig (trainer.hpp:58-99) from the flat config
+static SomConfig to_config(const ref_config* rc) {
+    SomConfig c;
+    const auto kind = static_cast<TopologyKind>(rc->topology);
+    c.topology = is_lattice(kind) ? TopologySpec::lattice(kind, rc->grid_w, rc->grid_h)
+                      : TopologySpec::graph(kind, rc->nodes);
+    c.n_iters = rc->n_iters;
+    c.eta0 = rc->eta0;
+    c.lr_decay = rc->lr_exponential ? DecayKind::exponential : DecayKind::linear;
+    c.sigma0 = rc->sigma0;
+    c.radius_decay = rc->radius_exponential ? DecayKind::exponential : DecayKind::linear;
+    c.sigma_min = rc->sigma_min;
+    c.init_method = rc->init_method == 1 ? InitMethod::uniform_box
+            : rc->init_method == 2 ? InitMethod::pca_plane
+                           : InitMethod::sample_draw;
+    c.use_momentum = rc->use_momentum != 0;
+    c.momentum = rc->momentum;
+    c.refresh.warmup_iters = rc->refresh_warmup;
+    c.refresh.growth = rc->refresh_growth;
+    c.refresh.max_interval = rc->refresh_max_interval;
+    c.n_chunks = rc->n_chunks;
+    c.seed = rc->seed;
+    return c;
+}
+
+// run_study (tune.hpp:125-159), default SearchSpace, serial trials.
+int ref_run_study(const ref_config* rc, std::size_t n_trials, const std::uint64_t* seeds,
+                  std::size_t n_seeds, const float* train, std::size_t n, const float* holdout,
+                  std::size_t nh, std::size_t d, double* qe_train, double* qe_holdout,
+                  std::uint8_t* failed) {
+    return guarded([&] {
+        const auto tm = make_matrix(train, n, d);
+        const auto hm = make_matrix(holdout, nh, d);
+        StudySpec spec;
+        spec.base_config = to_config(rc);
+        spec.sampling = static_cast<SamplingKind>(rc->sampling);
+        spec.budget.mode = rc->budget_fixed ? BudgetMode::fixed : BudgetMode::proportional;
+        spec.budget.m0 = rc->m0;
+        spec.budget.rho = rc->rho;
+        spec.sampler_alpha = rc->alpha;
+        spec.sampler_beta = rc->beta;
+        spec.n_trials = n_trials;
+        spec.seeds.assign(seeds, seeds + n_seeds);
+        const auto recs = run_study(SearchSpace{}, spec, tm, hm);
+        for (std::size_t i = 0; i < recs.size(); ++i) {
+            qe_train[i] = recs[i].qe_train;
+            qe_holdout[i] = recs[i].qe_holdout;
+            failed[i] = recs[i].failed ? 1 : 0;
+        }
+    });
+}
+
 // Whole training run: train() for n_threads<=1, else train_parallel().
 int ref_train(const ref_config* rc, const float* data, std::size_t n, std::size_t d,
               float* weights_out, double* qe_log, std::uint8_t* refresh_log) {
     return guarded([&] {
-        SomConfig c;
-        const auto kind = static_cast<TopologyKind>(rc->topology);
-        c.topology = is_lattice(kind) ? TopologySpec::lattice(kind, rc->grid_w, rc->grid_h)
-                                      : TopologySpec::graph(kind, rc->nodes);
-        c.n_iters = rc->n_iters;
-        c.eta0 = rc->eta0;
-        c.lr_decay = rc->lr_exponential ? DecayKind::exponential : DecayKind::linear;
-        c.sigma0 = rc->sigma0;
-        c.radius_decay = rc->radius_exponential ? DecayKind::exponential : DecayKind::linear;
-        c.sigma_min = rc->sigma_min;
-        c.init_method = rc->init_method == 1 ? InitMethod::uniform_box
-                        : rc->init_method == 2 ? InitMethod::pca_plane
-                                               : InitMethod::sample_draw;
-        c.use_momentum = rc->use_momentum != 0;
-        c.momentum = rc->momentum;
-        c.refresh.warmup_iters = rc->refresh_warmup;
-        c.refresh.growth = rc->refresh_growth;
-        c.refresh.max_interval = rc->refresh_max_interval;
-        c.n_chunks = rc->n_chunks;
-        c.seed = rc->seed;
+        SomConfig c = to_config(rc);
         SamplingBudget b;
         b.mode = rc->budget_fixed ? BudgetMode::fixed : BudgetMode::proportional;
         b.m0 = rc->m0;

@@ -154,6 +154,40 @@ int tsom_dropin_train_shards(const dropin_config* rc, const char* shard_dir, std
     });
 }
 
+// run_study (tune.hpp:125-159) with GPU trials: default SearchSpace, the base
+// config and sampler from rc; records in the reference's order.
+int tsom_dropin_run_study(const dropin_config* rc, std::size_t n_trials, const std::uint64_t* seeds,
+                          std::size_t n_seeds, const float* train, std::size_t n,
+                          const float* holdout, std::size_t nh, std::size_t d, int device,
+                          unsigned concurrency, double* qe_train, double* qe_holdout,
+                          std::uint8_t* failed, double* seconds_out) {
+    return guarded([&] {
+        DataMatrix tm(n, d, std::vector<float>(train, train + n * d));
+        DataMatrix hm(nh, d, std::vector<float>(holdout, holdout + nh * d));
+        StudySpec spec;
+        spec.base_config = make_config(rc);
+        spec.sampling = static_cast<SamplingKind>(rc->sampling);
+        spec.budget.mode = rc->budget_fixed ? BudgetMode::fixed : BudgetMode::proportional;
+        spec.budget.m0 = rc->m0;
+        spec.budget.rho = rc->rho;
+        spec.sampler_alpha = rc->alpha;
+        spec.sampler_beta = rc->beta;
+        spec.n_trials = n_trials;
+        spec.seeds.assign(seeds, seeds + n_seeds);
+        toposom_b200::CudaOptions opts;
+        opts.device = device;
+        const auto t0 = std::chrono::steady_clock::now();
+        const auto recs = toposom_b200::run_study_cuda(SearchSpace{}, spec, tm, hm, concurrency, opts);
+        const std::chrono::duration<double> dt = std::chrono::steady_clock::now() - t0;
+        if (seconds_out) *seconds_out = dt.count();
+        for (std::size_t i = 0; i < recs.size(); ++i) {
+            qe_train[i] = recs[i].qe_train;
+            qe_holdout[i] = recs[i].qe_holdout;
+            failed[i] = recs[i].failed ? 1 : 0;
+        }
+    });
+}
+
 // write_shards (dataset.hpp:252-275), for tests and benches that need shard files
 int tsom_dropin_write_shards(const float* data, std::size_t n, std::size_t d, const char* out_dir,
                              std::size_t n_shards) {

@@ -96,6 +96,10 @@ def load():
         L.tsom_dropin_train.argtypes = [C.POINTER(_Cfg), C.c_void_p, C.c_size_t, C.c_size_t,
                                         C.c_void_p, C.c_void_p, C.c_void_p, C.c_int, C.c_uint,
                                         C.POINTER(C.c_double)]
+        L.tsom_dropin_run_study.argtypes = [C.POINTER(_Cfg), C.c_size_t, C.c_void_p, C.c_size_t,
+                                            C.c_void_p, C.c_size_t, C.c_void_p, C.c_size_t,
+                                            C.c_size_t, C.c_int, C.c_uint, C.c_void_p, C.c_void_p,
+                                            C.c_void_p, C.POINTER(C.c_double)]
         L.tsom_dropin_find_bmus.argtypes = [C.c_void_p, C.c_size_t, C.c_void_p, C.c_size_t,
                                             C.c_size_t, C.c_void_p, C.c_void_p, C.c_int]
         L.tsom_dropin_train_shards.argtypes = [C.POINTER(_Cfg), C.c_char_p, C.c_size_t,
@@ -109,6 +113,27 @@ def load():
 
 def available() -> bool:
     return os.path.exists(DROPIN_PATH)
+
+
+def run_study_cuda(base, n_trials: int, seeds, train: np.ndarray, holdout: np.ndarray,
+                   device: int = 0, concurrency: int = 4):
+    """run_study (tune.hpp:125-159, default SearchSpace) with every trial trained
+    and scored on the GPU (toposom_b200::run_study_cuda), up to `concurrency`
+    trials at once.  Returns (qe_train, qe_holdout, failed, seconds), seed-major."""
+    L = load()
+    train = np.ascontiguousarray(train, np.float32)
+    holdout = np.ascontiguousarray(holdout, np.float32)
+    seeds = np.ascontiguousarray(seeds, np.uint64)
+    k = n_trials * len(seeds)
+    qt, qh, fl = np.empty(k), np.empty(k), np.zeros(k, np.uint8)
+    secs = C.c_double()
+    st = L.tsom_dropin_run_study(C.byref(_cfg(base)), n_trials, seeds.ctypes.data, len(seeds),
+                                 train.ctypes.data, train.shape[0], holdout.ctypes.data,
+                                 holdout.shape[0], train.shape[1], device, concurrency,
+                                 qt.ctypes.data, qh.ctypes.data, fl.ctypes.data, C.byref(secs))
+    if st:
+        _lib._raise(st, L.tsom_dropin_last_error().decode())
+    return qt, qh, fl.astype(bool), secs.value
 
 
 def train_cuda(cfg, data: np.ndarray, device: int = 0, log_qe: bool = False,

@@ -371,3 +371,22 @@ def test_bmu_exact_mixed_feature_scales(pkg, oracle_port, kernel):
     b, _ = e.bmu(x)
     bo, _ = oracle_port.find_bmus(x, w)
     assert (b == bo).all()
+
+
+# --- tuning: run_study with GPU trials (tune.hpp:125-159) ---------------------
+
+def test_run_study_cuda_matches_reference(pkg, oracle_port, oracle_ref):
+    import oracle
+    from paper_2604_26555_b200 import dropin
+    if not dropin.available():
+        pytest.skip("drop-in library not built")
+    x = oracle_port.synth_gmm(3000, 8, 41)
+    train, holdout = x[:2400], x[2400:]
+    base = oracle.SomConfig(topology="hex", grid_w=5, grid_h=4, n_iters=10, seed=0)
+    seeds = [1, 2]
+    rt, rh, rf = oracle_ref.run_study(base, 4, seeds, train, holdout)
+    gt, gh, gf, _ = dropin.run_study_cuda(base, 4, seeds, train, holdout, concurrency=4)
+    assert (gf == rf).all()
+    ok = ~rf
+    np.testing.assert_allclose(gt[ok], rt[ok], rtol=1e-5)
+    np.testing.assert_allclose(gh[ok], rh[ok], rtol=1e-5)
