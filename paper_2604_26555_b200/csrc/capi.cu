@@ -11,6 +11,9 @@
 #include <unistd.h>
 #include <nccl.h>
 
+#include <condition_variable>
+#include <mutex>
+
 #include <algorithm>
 #include <climits>
 #include <cmath>
@@ -1100,6 +1103,7 @@ bool sampler_pick(Engine* eng, uint64_t* m) {
     CU(smp.sel.ensure(std::max<uint64_t>(smp.n, 1) * sizeof(uint32_t)));
     const int rc = tsom::sampler_select(smp, smp.sel.as<uint32_t>(), m, eng->sm_count, eng->stream);
     CU(cudaGetLastError());
+    REQUIRE(rc != 5, TSOM_ERR_NCCL, "nccl: allreduce failed (sampler)");
     REQUIRE(rc == 0 || rc == -1, TSOM_ERR_CUDA, "sampler: device allocation failed");
     smp.identity = rc == -1;
     smp.last_m = *m;
@@ -1120,7 +1124,74 @@ void fill_identity(Engine* eng, uint64_t n) {
 }
 }  // namespace
 
+// In-process stand-in for a communicator (tests only): ranks are engines driven
+// from separate host threads; allreduce goes through host memory with a
+// generation barrier.  Lets the sharded sampler be checked on one GPU.
+struct LoopbackGroup {
+    int world;
+    std::mutex mu;
+    std::condition_variable cv;
+    std::vector<uint64_t> acc;
+    int arrived = 0, leaving = 0;
+    uint64_t gen = 0;
+    explicit LoopbackGroup(int w) : world(w) {}
+    // element-wise reduce of `v` (u32 or u64 as u64 lanes) over the ranks
+    void reduce(std::vector<uint64_t>& v, bool is_max) {
+        std::unique_lock<std::mutex> lk(mu);
+        cv.wait(lk, [&] { return leaving == 0; });  // previous round fully drained
+        if (arrived == 0) acc.assign(v.size(), 0);
+        for (size_t i = 0; i < v.size(); ++i) acc[i] = is_max ? std::max(acc[i], v[i]) : acc[i] + v[i];
+        const uint64_t my_gen = gen;
+        if (++arrived == world) {
+            arrived = 0;
+            leaving = world;
+            ++gen;
+            cv.notify_all();
+        } else {
+            cv.wait(lk, [&] { return gen != my_gen; });
+        }
+        v = acc;
+        if (--leaving == 0) cv.notify_all();
+    }
+};
+
+namespace {
+void attach_loopback(Engine* eng, LoopbackGroup* g, int rank) {
+    tsom::SamplerState& smp = eng->sampler;
+    cudaStream_t st = eng->stream;
+    smp.loopback = true;
+    smp.world = g->world;
+    smp.rank = rank;
+    smp.allreduce = [g, st](void* buf, size_t count, int op) {
+        const size_t esz = op == 0 ? 4 : 8;
+        std::vector<uint8_t> raw(count * esz);
+        if (cudaMemcpyAsync(raw.data(), buf, raw.size(), cudaMemcpyDeviceToHost, st) != cudaSuccess ||
+            cudaStreamSynchronize(st) != cudaSuccess)
+            return false;
+        std::vector<uint64_t> v(count);
+        for (size_t i = 0; i < count; ++i)
+            v[i] = esz == 4 ? (uint64_t)reinterpret_cast<uint32_t*>(raw.data())[i]
+                            : reinterpret_cast<uint64_t*>(raw.data())[i];
+        g->reduce(v, op == 1);
+        for (size_t i = 0; i < count; ++i) {
+            if (esz == 4) reinterpret_cast<uint32_t*>(raw.data())[i] = (uint32_t)v[i];
+            else reinterpret_cast<uint64_t*>(raw.data())[i] = v[i];
+        }
+        return cudaMemcpyAsync(buf, raw.data(), raw.size(), cudaMemcpyHostToDevice, st) ==
+                   cudaSuccess &&
+               cudaStreamSynchronize(st) == cudaSuccess;
+    };
+}
+}  // namespace
+
 extern "C" {
+
+// diagnostics / tests only (not in the public header)
+void* tsom_debug_loopback_group(int world) { return new LoopbackGroup(world); }
+void tsom_debug_loopback_free(void* g) { delete static_cast<LoopbackGroup*>(g); }
+int tsom_debug_loopback_attach(tsom_engine* eng, void* g, int rank) {
+    return guarded(eng, [&] { attach_loopback(eng, static_cast<LoopbackGroup*>(g), rank); });
+}
 
 int tsom_sampler_init(tsom_engine* eng, int kind, uint64_t m, uint64_t seed, double alpha,
                       double beta) {
@@ -1130,7 +1201,39 @@ int tsom_sampler_init(tsom_engine* eng, int kind, uint64_t m, uint64_t seed, dou
         REQUIRE(eng->n_rows >= 1, TSOM_ERR_INVALID, "sampler: N must be >= 1 (bind data first)");
         REQUIRE(kind == 0 || m >= 1, TSOM_ERR_INVALID, "select_random: m must be >= 1");
         REQUIRE(eng->n_rows < (1ull << 31), TSOM_ERR_INVALID, "sampler: N < 2^31");
-        const int rc = tsom::sampler_setup(eng->sampler, kind, eng->n_rows, m, seed, alpha, beta,
+        tsom::SamplerState& smp = eng->sampler;
+        smp.sharded = eng->nccl_comm != nullptr || smp.loopback;
+        if (smp.sharded) {
+            // one Sampler over the ranks' rows in rank order: global N and this
+            // rank's first row from an allreduce of the per-rank row counts
+            cudaStream_t st = eng->stream;
+            if (!smp.loopback) {
+                ncclComm_t comm = (ncclComm_t)eng->nccl_comm;
+                smp.world = eng->world;
+                smp.rank = eng->rank;
+                smp.allreduce = [comm, st](void* buf, size_t count, int op) {
+                    const ncclDataType_t t = op == 0 ? ncclUint32 : ncclUint64;
+                    const ncclRedOp_t o = op == 1 ? ncclMax : ncclSum;
+                    return g_nccl.allReduce(buf, buf, count, t, o, comm, st) == ncclSuccess;
+                };
+            }
+            std::vector<uint64_t> cnt(smp.world, 0);
+            cnt[smp.rank] = eng->n_rows;
+            CU(smp.slots.ensure((size_t)smp.world * 8));
+            CU(cudaMemcpyAsync(smp.slots.p, cnt.data(), cnt.size() * 8, cudaMemcpyHostToDevice, st));
+            REQUIRE(smp.allreduce(smp.slots.p, cnt.size(), 2), TSOM_ERR_NCCL,
+                    "nccl: allreduce failed (sampler row counts)");
+            CU(cudaMemcpyAsync(cnt.data(), smp.slots.p, cnt.size() * 8, cudaMemcpyDeviceToHost, st));
+            CU(cudaStreamSynchronize(st));
+            smp.gN = 0;
+            smp.off = 0;
+            for (int r = 0; r < smp.world; ++r) {
+                if (r < smp.rank) smp.off += cnt[r];
+                smp.gN += cnt[r];
+            }
+            REQUIRE(smp.gN < (1ull << 32), TSOM_ERR_INVALID, "sampler: global N < 2^32");
+        }
+        const int rc = tsom::sampler_setup(smp, kind, eng->n_rows, m, seed, alpha, beta,
                                            eng->sm_count);
         REQUIRE(rc == 0, TSOM_ERR_CUDA, "sampler: device allocation failed");
         CU(cudaDeviceSynchronize());

@@ -20,6 +20,7 @@
 
 #include <atomic>
 #include <cstdint>
+#include <functional>
 #include <string>
 #include <vector>
 
@@ -162,6 +163,16 @@ struct SamplerState {
     DevBuf err, age, keys, hist;                // adaptive
     DevBuf first, tidx;                         // random
     DevBuf bitmap, bcount, sel;                 // selection
+    // Sharded (a communicator attached): this rank holds rows [off, off + n) of
+    // the gN rows the one reference Sampler covers; allreduce(buf, count, op)
+    // runs on the engine stream, op 0 = u32 sum, 1 = u64 max, 2 = u64 sum.
+    bool sharded = false;
+    bool loopback = false;         // tests: in-process rank group instead of NCCL
+    uint64_t gN = 0, off = 0;
+    int world = 1, rank = 0;
+    int jump0 = 0;                 // generator 0 starts at a jumped offset (off > 0)
+    std::function<bool(void*, size_t, int)> allreduce;
+    DevBuf jN, glist, slots;       // jump by gN (adaptive), global selection, per-rank counts
 };
 int sampler_setup(SamplerState& s, int kind, uint64_t n, uint64_t m, uint64_t seed, double alpha,
                   double beta, int sm_count);

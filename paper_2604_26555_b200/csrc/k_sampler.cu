@@ -89,7 +89,7 @@ __global__ void __launch_bounds__(kT) k_mt_generate(const uint64_t* __restrict__
                                                     const uint64_t* __restrict__ jp, uint64_t L,
                                                     uint64_t total, uint64_t* __restrict__ draws,
                                                     uint64_t tail0, uint32_t tail_len,
-                                                    uint64_t* __restrict__ tail) {
+                                                    uint64_t* __restrict__ tail, int jump0) {
     extern __shared__ uint64_t sm[];
     uint64_t* s_seq = sm;                 // [mt::kSeq]
     uint64_t* s_j = sm + mt::kSeq;        // [312]
@@ -98,7 +98,7 @@ __global__ void __launch_bounds__(kT) k_mt_generate(const uint64_t* __restrict__
     const uint64_t g = blockIdx.x;
     const uint64_t q0 = g * L;
     if (q0 >= total) return;
-    if (g == 0) {
+    if (g == 0 && !jump0) {
         if (k < 312) s_w[k] = seq[k];
     } else {
         for (int i = k; i < mt::kSeq; i += kT) s_seq[i] = seq[i];
@@ -147,6 +147,32 @@ __global__ void k_mt_advance(const uint64_t* __restrict__ seq, const uint64_t* _
         window[k] = tail[pos - tail0];
     } else if (k == 0) {
         atomicOr(status, 4u);  // draws beyond the generated slack
+    }
+}
+
+// window <- X[J .. J + 312) from the epoch-start sequence and jp = t^J mod phi
+// (sharded adaptive: every rank skips the whole epoch's N draws at once)
+__global__ void __launch_bounds__(kT) k_mt_jump_window(const uint64_t* __restrict__ seq,
+                                                       const uint64_t* __restrict__ jp,
+                                                       uint64_t* __restrict__ window) {
+    extern __shared__ uint64_t sm2[];
+    uint64_t* s_seq = sm2;
+    uint64_t* s_j = sm2 + mt::kSeq;
+    const int k = threadIdx.x;
+    for (int i = k; i < mt::kSeq; i += kT) s_seq[i] = seq[i];
+    if (k < 312) s_j[k] = jp[k];
+    __syncthreads();
+    if (k < 312) {
+        uint64_t acc = 0;
+        for (int w = 0; w < 312; ++w) {
+            uint64_t bits = s_j[w];
+            while (bits) {
+                const int b = __ffsll((long long)bits) - 1;
+                bits &= bits - 1;
+                acc ^= s_seq[64 * w + b + k];
+            }
+        }
+        window[k] = acc;
     }
 }
 
@@ -380,6 +406,51 @@ __global__ void k_adapt_observe(const uint32_t* __restrict__ sel, uint64_t m,
     }
 }
 
+// sharded random: the rows of a sorted global selection that fall in this
+// rank's range [off, off + n), as local ids; count -> *m_local
+__global__ void k_local_slice(const uint32_t* __restrict__ glist, const unsigned long long* total,
+                              uint64_t off, uint64_t n, uint32_t* __restrict__ out,
+                              unsigned long long* __restrict__ m_local) {
+    const uint64_t m = *total;
+    // lower bounds by binary search (one thread), then a strided copy
+    __shared__ uint64_t lo_hi[2];
+    if (threadIdx.x < 2) {
+        const uint64_t key = off + (threadIdx.x ? n : 0);
+        uint64_t lo = 0, hi = m;
+        while (lo < hi) {
+            const uint64_t mid = (lo + hi) / 2;
+            if ((uint64_t)glist[mid] < key) lo = mid + 1;
+            else hi = mid;
+        }
+        lo_hi[threadIdx.x] = lo;
+    }
+    __syncthreads();
+    const uint64_t a = lo_hi[0], b = lo_hi[1];
+    for (uint64_t i = a + threadIdx.x; i < b; i += blockDim.x) out[i - a] = (uint32_t)(glist[i] - off);
+    if (threadIdx.x == 0) *m_local = b - a;
+}
+
+// equal-to-threshold keys of this rank -> eq slot; then this rank's share of
+// the boundary ties in rank order (sel_state[1] = local need)
+__global__ void k_adapt_eq(const unsigned long long* __restrict__ keys, uint64_t n,
+                           const unsigned long long* __restrict__ sel_state,
+                           unsigned long long* __restrict__ slot) {
+    const unsigned long long T = sel_state[0];
+    unsigned long long c = 0;
+    for (uint64_t i = blockIdx.x * (uint64_t)blockDim.x + threadIdx.x; i < n;
+         i += (uint64_t)gridDim.x * blockDim.x)
+        c += keys[i] == T;
+    for (int o = 16; o; o >>= 1) c += __shfl_xor_sync(0xffffffffu, c, o);
+    if ((threadIdx.x & 31) == 0 && c) atomicAdd(slot, c);
+}
+__global__ void k_tie_quota(const unsigned long long* __restrict__ eq, int world, int rank,
+                            unsigned long long* __restrict__ sel_state) {
+    unsigned long long need = sel_state[1], before = 0;
+    for (int r = 0; r < rank; ++r) before += eq[r];
+    const unsigned long long mine = eq[rank];
+    sel_state[1] = need > before ? (need - before < mine ? need - before : mine) : 0ULL;
+}
+
 // ---------------------------------------------------------------------------
 // bitmap -> sorted index list
 // ---------------------------------------------------------------------------
@@ -463,9 +534,18 @@ int sampler_setup(SamplerState& s, int kind, uint64_t n, uint64_t m, uint64_t se
     s.m = m;
     s.alpha = alpha;
     s.beta = beta;
+    if (!s.sharded) {
+        s.gN = n;
+        s.off = 0;
+    }
+    const uint64_t gN = s.gN;
     s.draws_per_epoch = 0;
-    if (kind == 1 && m < n) s.draws_per_epoch = m;
+    // random: every rank draws the whole epoch's m indices (Floyd is global);
+    // adaptive: each rank draws for its own rows, at its offset of the stream
+    if (kind == 1 && m < gN) s.draws_per_epoch = m;
     if (kind == 2) s.draws_per_epoch = n;
+    const uint64_t stream_off = kind == 2 ? s.off : 0;
+    s.jump0 = stream_off > 0;
     // Rng(seed, SeedStream::sampler): mt19937_64(mix_seed(seed, 3)) (rng.hpp:12-37)
     uint64_t z = seed + 0x9e3779b97f4a7c15ULL * (3 + 1);
     z = (z ^ (z >> 30)) * 0xbf58476d1ce4e5b9ULL;
@@ -475,6 +555,13 @@ int sampler_setup(SamplerState& s, int kind, uint64_t n, uint64_t m, uint64_t se
     if (s.window.ensure(312 * 8) != cudaSuccess) return 4;
     if (cudaMemcpy(s.window.p, w, 312 * 8, cudaMemcpyHostToDevice) != cudaSuccess) return 4;
     if (s.misc.ensure(64) != cudaSuccess) return 4;
+    if (s.sharded && s.slots.ensure((size_t)std::max(1, s.world) * 8) != cudaSuccess) return 4;
+    if (kind == 2 && s.sharded) {
+        // the stream advances by gN draws per epoch, whatever this rank's share
+        const std::vector<uint64_t> JN = mt::jump_poly(gN);
+        if (s.jN.ensure(312 * 8) != cudaSuccess) return 4;
+        if (cudaMemcpy(s.jN.p, JN.data(), 312 * 8, cudaMemcpyHostToDevice) != cudaSuccess) return 4;
+    }
     if (!s.draws_per_epoch) return 0;
     const uint64_t total = s.draws_per_epoch + kSlack;
     uint64_t G = (total + 65535) / 65536;
@@ -482,12 +569,12 @@ int sampler_setup(SamplerState& s, int kind, uint64_t n, uint64_t m, uint64_t se
     const uint64_t L = (total + G - 1) / G;
     s.G = (uint32_t)G;
     s.L = L;
-    // jump polynomials t^(gL) mod phi, g = 1..G-1 (host, once per configuration)
+    // jump polynomials t^(stream_off + gL) mod phi (host, once per configuration)
     std::vector<uint64_t> jp(G * 312, 0);
-    if (G > 1) {
+    if (G > 1 || stream_off > 0) {
         const std::vector<uint64_t> J = mt::jump_poly(L);
-        std::vector<uint64_t> cur = J;
-        for (uint64_t g = 1; g < G; ++g) {
+        std::vector<uint64_t> cur = stream_off > 0 ? mt::jump_poly(stream_off) : J;
+        for (uint64_t g = stream_off > 0 ? 0 : 1; g < G; ++g) {
             std::copy(cur.begin(), cur.end(), jp.begin() + g * 312);
             if (g + 1 < G) cur = mt::mul_poly(cur, J);
         }
@@ -513,7 +600,6 @@ int sampler_setup(SamplerState& s, int kind, uint64_t n, uint64_t m, uint64_t se
         if (s.err.ensure(n * 8) != cudaSuccess || s.age.ensure(n * 4) != cudaSuccess ||
             s.keys.ensure(n * 8) != cudaSuccess || s.hist.ensure(4096 * 4) != cudaSuccess)
             return 4;
-        std::vector<double> e(1, 1e30);
         // last_error = kUnseenError (sampling.hpp:81, 91), age = 0
         const size_t chunk = 1 << 20;
         std::vector<double> init(std::min<uint64_t>(n, chunk), 1e30);
@@ -525,12 +611,13 @@ int sampler_setup(SamplerState& s, int kind, uint64_t n, uint64_t m, uint64_t se
         if (cudaMemset(s.hist.p, 0, 4096 * 4) != cudaSuccess) return 4;
     }
     if (kind == 1) {
-        if (s.first.ensure(n * 4) != cudaSuccess || s.tidx.ensure(m * 4) != cudaSuccess) return 4;
+        if (s.first.ensure(gN * 4) != cudaSuccess || s.tidx.ensure(m * 4) != cudaSuccess) return 4;
+        if (s.sharded && s.glist.ensure(m * 4) != cudaSuccess) return 4;
     }
     return 0;
 }
 
-// the epoch's draws (k_mt_extend + k_mt_generate); delta (device) = draws used
+// the epoch's draws (k_mt_extend + k_mt_generate) into buffer b
 static void generate_draws(SamplerState& s, int b, cudaStream_t st) {
     const uint32_t twists = (mt::kSeq - 312 + 311) / 312;
     TSOM_LAUNCH(k_mt_extend<<<1, kT, 0, st>>>(s.window.as<uint64_t>(), twists,
@@ -539,15 +626,18 @@ static void generate_draws(SamplerState& s, int b, cudaStream_t st) {
     static bool attr = false;
     if (!attr) {
         cudaFuncSetAttribute(k_mt_generate, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+        cudaFuncSetAttribute(k_mt_jump_window, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                             (int)((mt::kSeq + 312) * 8));
         attr = true;
     }
     const uint64_t total = s.draws_per_epoch + kSlack;
     TSOM_LAUNCH(k_mt_generate<<<s.G, kT, smem, st>>>(s.seqb[b].as<uint64_t>(), s.jp.as<uint64_t>(),
                                                      s.L, total, s.drawsb[b].as<uint64_t>(),
                                                      s.tail0, s.tail_len,
-                                                     s.tailb[b].as<uint64_t>()));
+                                                     s.tailb[b].as<uint64_t>(), s.jump0));
 }
 
+// bitmap of `n` rows -> sorted ids in `out`; total count -> misc[3]
 static void bitmap_to_list(SamplerState& s, uint64_t n, uint32_t* out, cudaStream_t st) {
     const uint64_t words = (n + 31) / 32;
     const uint64_t nb = (words + 1023) / 1024;
@@ -564,14 +654,16 @@ static void bitmap_to_list(SamplerState& s, uint64_t n, uint32_t* out, cudaStrea
 // 4 slack exceeded), [2] tie count, [3] selected count, [4..5] adaptive max,
 // [6..7] radix state
 int sampler_select(SamplerState& s, uint32_t* out, uint64_t* m_out, int sm_count, cudaStream_t st) {
-    const uint64_t n = s.n;
+    const uint64_t n = s.n, gN = s.gN;
     uint64_t* misc = s.misc.as<uint64_t>();
     cudaMemsetAsync(misc, 0, 64, st);
-    if (s.kind == 0 || (s.kind == 1 && s.m >= n)) {
+    if (s.kind == 0 || (s.kind == 1 && s.m >= gN)) {
         *m_out = n;
         return -1;  // identity selection: the caller uses "all rows"
     }
-    const uint64_t words = (n + 31) / 32;
+    // random sharded: the whole gN-row bitmap (Floyd is global)
+    const uint64_t bits = s.kind == 1 ? gN : n;
+    const uint64_t words = (bits + 31) / 32;
     const uint64_t nb = (words + 1023) / 1024;
     if (s.bitmap.ensure(words * 4) != cudaSuccess || s.bcount.ensure(nb * 4 + 4) != cudaSuccess)
         return 4;
@@ -585,54 +677,86 @@ int sampler_select(SamplerState& s, uint32_t* out, uint64_t* m_out, int sm_count
     s.want_gen = false;
     const uint64_t* draws = s.drawsb[b].as<uint64_t>();
     const unsigned grid = (unsigned)std::max<uint64_t>(
-        1, std::min<uint64_t>((std::max(s.m, n) + 255) / 256, (uint64_t)sm_count * 16));
+        1, std::min<uint64_t>((std::max(s.m, bits) + 255) / 256, (uint64_t)sm_count * 16));
     uint32_t* status = reinterpret_cast<uint32_t*>(misc + 1);
+    auto* total = reinterpret_cast<unsigned long long*>(misc + 3);
+    bool ok = true;
     if (s.kind == 1) {
         const uint64_t m = s.m;
-        cudaMemsetAsync(s.first.p, 0xFF, n * 4, st);
+        cudaMemsetAsync(s.first.p, 0xFF, gN * 4, st);
         cudaMemcpyAsync(misc, &m, 8, cudaMemcpyHostToDevice, st);  // delta = m (no rejection)
-        TSOM_LAUNCH(k_rand_index<<<grid, 256, 0, st>>>(draws, n, m,
-                                                       s.tidx.as<uint32_t>(), s.first.as<uint32_t>(),
-                                                       status));
-        TSOM_LAUNCH(k_rand_replay<<<1, 1, 0, st>>>(draws, s.draws_per_epoch + kSlack,
-                                                   n, m, s.tidx.as<uint32_t>(),
-                                                   s.first.as<uint32_t>(), misc, status));
-        TSOM_LAUNCH(k_rand_pick<<<grid, 256, 0, st>>>(s.tidx.as<uint32_t>(), s.first.as<uint32_t>(), n,
-                                                      m, s.bitmap.as<uint32_t>()));
+        TSOM_LAUNCH(k_rand_index<<<grid, 256, 0, st>>>(draws, gN, m, s.tidx.as<uint32_t>(),
+                                                       s.first.as<uint32_t>(), status));
+        TSOM_LAUNCH(k_rand_replay<<<1, 1, 0, st>>>(draws, s.draws_per_epoch + kSlack, gN, m,
+                                                   s.tidx.as<uint32_t>(), s.first.as<uint32_t>(),
+                                                   misc, status));
+        TSOM_LAUNCH(k_rand_pick<<<grid, 256, 0, st>>>(s.tidx.as<uint32_t>(), s.first.as<uint32_t>(),
+                                                      gN, m, s.bitmap.as<uint32_t>()));
+        if (s.sharded) {
+            bitmap_to_list(s, gN, s.glist.as<uint32_t>(), st);
+            TSOM_LAUNCH(k_local_slice<<<1, 1024, 0, st>>>(s.glist.as<uint32_t>(), total, s.off, n, out,
+                                                          total));
+        } else {
+            bitmap_to_list(s, n, out, st);
+        }
     } else {
-        const uint64_t m = std::min(s.m, n);
-        cudaMemcpyAsync(misc, &n, 8, cudaMemcpyHostToDevice, st);  // delta = n draws
+        const uint64_t m = std::min(s.m, gN);
+        cudaMemcpyAsync(misc, &gN, 8, cudaMemcpyHostToDevice, st);  // delta = gN draws
         auto* mx = reinterpret_cast<unsigned long long*>(misc + 4);
         TSOM_LAUNCH(k_adapt_max<<<grid, 256, 0, st>>>(s.err.as<double>(), s.age.as<uint32_t>(), n, mx));
+        if (s.sharded) ok &= s.allreduce(mx, 2, 1);  // the maxima over all rows
         TSOM_LAUNCH(k_adapt_keys<<<grid, 256, 0, st>>>(
             s.err.as<double>(), s.age.as<uint32_t>(), draws, n, s.alpha, s.beta, mx,
             reinterpret_cast<unsigned long long*>(s.keys.p)));
         auto* rs = reinterpret_cast<unsigned long long*>(misc + 6);
         const unsigned long long st0[2] = {0ULL, (unsigned long long)m};
         cudaMemcpyAsync(rs, st0, 16, cudaMemcpyHostToDevice, st);
-        // digits of the 64-bit key: bits 52-63, 40-51, 28-39, 16-27, 4-15, 0-3
+        // digits of the 64-bit key: bits 52-63, 40-51, 28-39, 16-27, 4-15, 0-3;
+        // sharded: each digit histogram summed over the ranks (the same digit
+        // is then picked everywhere: one global threshold)
         const int shifts[6] = {52, 40, 28, 16, 4, 0}, widths[6] = {12, 12, 12, 12, 12, 4};
         for (int d = 0; d < 6; ++d) {
             TSOM_LAUNCH(k_adapt_hist<<<grid, 256, 0, st>>>(
                 reinterpret_cast<const unsigned long long*>(s.keys.p), n, rs, shifts[d], widths[d],
                 s.hist.as<uint32_t>()));
+            if (s.sharded) ok &= s.allreduce(s.hist.p, 4096, 0);
             TSOM_LAUNCH(k_adapt_digit<<<1, 1024, 0, st>>>(s.hist.as<uint32_t>(), shifts[d], rs));
+        }
+        if (s.sharded) {  // boundary ties: taken in rank order
+            auto* eq = reinterpret_cast<unsigned long long*>(s.slots.p);
+            cudaMemsetAsync(eq, 0, (size_t)s.world * 8, st);
+            TSOM_LAUNCH(k_adapt_eq<<<grid, 256, 0, st>>>(
+                reinterpret_cast<const unsigned long long*>(s.keys.p), n, rs, eq + s.rank));
+            ok &= s.allreduce(eq, (size_t)s.world, 2);
+            TSOM_LAUNCH(k_tie_quota<<<1, 1, 0, st>>>(eq, s.world, s.rank, rs));
         }
         TSOM_LAUNCH(k_adapt_mark<<<grid, 256, 0, st>>>(
             reinterpret_cast<const unsigned long long*>(s.keys.p), n, rs, s.bitmap.as<uint32_t>(),
             reinterpret_cast<unsigned long long*>(misc + 2)));
+        bitmap_to_list(s, n, out, st);
     }
-    bitmap_to_list(s, n, out, st);
+    if (!ok) return 5;
     // the stream continues after the draws actually used
-    TSOM_LAUNCH(k_mt_advance<<<1, 320, 0, st>>>(s.seqb[b].as<uint64_t>(), s.tailb[b].as<uint64_t>(),
-                                                s.tail0, s.tail_len, misc,
-                                                s.window.as<uint64_t>(), status));
+    if (s.kind == 2 && s.sharded)
+        TSOM_LAUNCH(k_mt_jump_window<<<1, kT, (mt::kSeq + 312) * 8, st>>>(
+            s.seqb[b].as<uint64_t>(), s.jN.as<uint64_t>(), s.window.as<uint64_t>()));
+    else
+        TSOM_LAUNCH(k_mt_advance<<<1, 320, 0, st>>>(s.seqb[b].as<uint64_t>(),
+                                                    s.tailb[b].as<uint64_t>(), s.tail0, s.tail_len,
+                                                    misc, s.window.as<uint64_t>(), status));
     // the next epoch's draws depend only on the advanced stream state; they are
     // generated on the side stream while this epoch trains (sampler_pregenerate,
     // started once the BMU kernel has finished so it does not compete with it)
     s.cur = b ^ 1;
     s.want_gen = true;
-    *m_out = s.kind == 1 ? s.m : std::min(s.m, n);
+    if (s.sharded) {  // this rank's share is only known on the device
+        unsigned long long mloc = 0;
+        cudaMemcpyAsync(&mloc, total, 8, cudaMemcpyDeviceToHost, st);
+        cudaStreamSynchronize(st);
+        *m_out = mloc;
+    } else {
+        *m_out = s.kind == 1 ? s.m : std::min(s.m, n);
+    }
     return 0;
 }
 

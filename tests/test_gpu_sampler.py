@@ -94,3 +94,100 @@ def test_sampled_resident_training_vs_reference(pkg, oracle_port, oracle_ref, sa
     assert rel <= 1e-4
     qe = np.array([r["qe_train"] for r in log])
     np.testing.assert_allclose(qe, qe_ref, rtol=1e-5)
+
+
+# --- sharded sampler: one reference Sampler over the ranks' rows --------------
+#
+# Ranks are engines on the same GPU driven from separate threads, joined by an
+# in-process loopback group standing in for the NCCL communicator (the sampler
+# calls the same allreduce hook either way): the concatenation of the ranks'
+# selections must be the reference Sampler's selection over all rows.
+
+def _run_sharded(pkg, sizes, kind, m, seed, iters, alpha=1.0, beta=1.0, dist=None):
+    import ctypes as C
+    import threading
+
+    from paper_2604_26555_b200 import _lib
+    L = _lib.load()
+    L.tsom_debug_loopback_group.restype = C.c_void_p
+    L.tsom_debug_loopback_group.argtypes = [C.c_int]
+    L.tsom_debug_loopback_attach.argtypes = [C.c_void_p, C.c_void_p, C.c_int]
+    L.tsom_debug_loopback_free.argtypes = [C.c_void_p]
+    world = len(sizes)
+    g = L.tsom_debug_loopback_group(world)
+    offs = np.concatenate([[0], np.cumsum(sizes)[:-1]]).astype(np.int64)
+    engines = [engine_with_rows(pkg, s) for s in sizes]
+    for r, e in enumerate(engines):
+        assert L.tsom_debug_loopback_attach(e.h, g, r) == 0
+    out = [[None] * iters for _ in range(world)]
+    errors = []
+
+    def rank_main(r):
+        try:
+            e = engines[r]
+            e.sampler_init(kind, m, seed, alpha, beta)
+            for t in range(iters):
+                sel = e.sampler_select()
+                out[r][t] = sel.astype(np.int64) + offs[r]
+                if dist is not None:
+                    e.sampler_observe(dist[out[r][t]])
+        except Exception as ex:  # pragma: no cover - reported below
+            errors.append(ex)
+
+    th = [threading.Thread(target=rank_main, args=(r,)) for r in range(world)]
+    for t in th:
+        t.start()
+    for t in th:
+        t.join(timeout=600)
+    L.tsom_debug_loopback_free(g)
+    assert not errors, errors
+    return [np.concatenate([out[r][t] for r in range(world)]) for t in range(iters)], engines
+
+
+@pytest.mark.parametrize("sizes", [[12000, 9000, 9001], [1, 29999], [15000, 15000, 3]])
+def test_sharded_random_sampler_matches_reference(pkg, oracle_ref, sizes):
+    n, m, seed = sum(sizes), 3000, 29
+    ref = oracle_ref.sampler_run("random", n, seed, 4, m0=m, budget_fixed=True)
+    got, _ = _run_sharded(pkg, [s for s in sizes if s > 0], "random", m, seed, 4)
+    for t in range(4):
+        assert (got[t] == ref[t]).all(), f"epoch {t}"
+
+
+@pytest.mark.parametrize("sizes,alpha,beta", [([12000, 9000, 9001], 1.0, 1.0),
+                                              ([20000, 10000], 0.5, 2.0), ([7, 29993], 1.0, 1.0)])
+def test_sharded_adaptive_sampler_matches_reference(pkg, oracle_ref, sizes, alpha, beta):
+    n, seed, iters = sum(sizes), 37, 5
+    rho = 0.1
+    m = max(1, int(np.floor(n * rho)))
+    dist = np.random.default_rng(seed).random(n) * 10.0
+    ref = oracle_ref.sampler_run("adaptive", n, seed, iters, rho=rho, alpha=alpha, beta=beta,
+                                 dist_by_row=dist)
+    got, engines = _run_sharded(pkg, sizes, "adaptive", m, seed, iters, alpha, beta, dist)
+    for t in range(iters):
+        assert (got[t] == ref[t]).all(), f"epoch {t}: {len(got[t])} vs {len(ref[t])}"
+    # the per-rank adaptive state is the reference's, sliced
+    err = np.full(n, 1e30)
+    age = np.zeros(n, np.uint32)
+    for t in range(iters):
+        age += 1
+        err[ref[t]] = dist[ref[t]]
+        age[ref[t]] = 0
+    off = 0
+    for e, s in zip(engines, sizes):
+        ge, ga = e.sampler_state()
+        assert (ge == err[off:off + s]).all() and (ga == age[off:off + s]).all()
+        off += s
+
+
+def test_sampler_with_nccl_communicator_world1(pkg, oracle_ref):
+    # the NCCL allreduce hook of the sharded sampler (one rank)
+    n, seed = 20000, 43
+    dist = np.random.default_rng(seed).random(n)
+    ref = oracle_ref.sampler_run("adaptive", n, seed, 3, rho=0.2, dist_by_row=dist)
+    e = engine_with_rows(pkg, n)
+    e.comm_init(e.comm_unique_id(), 0, 1)
+    e.sampler_init("adaptive", int(n * 0.2), seed)
+    for t in range(3):
+        sel = e.sampler_select()
+        assert (sel == ref[t]).all()
+        e.sampler_observe(dist[sel])
