@@ -370,11 +370,18 @@ def run_gpu_arm(args):
     }
     if e2e:
         line["e2e"] = e2e
-    if rank == 0 and world == 1 and not args.no_c4:
+    if not args.no_c4:
         if eng is not None:
             eng.close()
         torch.cuda.empty_cache()
-        line["c4"] = run_c4_leg(local)
+        c4 = run_c4_leg(local, world=world, rank=rank, attach=attach_comm,
+                        bcast=(lambda o: (dist.broadcast_object_list(o, src=0), o)[1])
+                        if world > 1 else None,
+                        tmax=(lambda v: (lambda tm: (dist.all_reduce(tm, op=dist.ReduceOp.MAX),
+                                                     float(tm.item()))[1])(
+                            torch.tensor([v], dtype=torch.float64))) if world > 1 else None)
+        if rank == 0:
+            line["c4"] = c4
     if rank == 0 and world == 1 and not args.no_cpu:
         v, cores, kind, sample, _ = cpu_reference(step_seconds=6.0)
         line["cpu_baseline"] = {"value": v, "unit": UNIT, "cores": cores, "kind": kind,
@@ -386,12 +393,15 @@ def run_gpu_arm(args):
     return 0
 
 
-def run_c4_leg(local, n=100_000_000, rho=0.1, epochs=EPOCHS, warm=2):
-    """Config c4 on one GPU: 1024-node RNG-topology SOM, 1e8 x 50
-    GMM rows resident in HBM, adaptive sampler with rho = 0.1 on the device
-    (select -> epoch over the selected rows -> observe), RNG graph refreshed on
-    the device on the reference schedule.  Every per-epoch step is on the GPU;
-    timed with CUDA events on the engine stream."""
+def run_c4_leg(local, n=100_000_000, rho=0.1, epochs=EPOCHS, warm=2, world=1, rank=0,
+               attach=None, bcast=None, tmax=None):
+    """Config c4: 1024-node RNG-topology SOM, 1e8 x 50 GMM rows
+    resident in HBM (split over the ranks: n / world rows each), adaptive
+    sampler with rho = 0.1 on the device (select -> epoch over the selected rows
+    -> observe; with N > 1 one sharded sampler over all rows, its digit
+    histograms allreduced over NCCL), RNG graph refreshed on the device on the
+    reference schedule.  Every per-epoch step is on the GPU; timed with CUDA
+    events on the engine stream, max over ranks."""
     import numpy as np
     import torch
 
@@ -399,10 +409,12 @@ def run_c4_leg(local, n=100_000_000, rho=0.1, epochs=EPOCHS, warm=2):
     from paper_2604_26555_b200.hostref import (RefreshState, Rng, init_sample_draw,
                                                resolved_sigma0, schedule_value)
     seed = 2608
+    n_total = n
+    n = n_total // world + (1 if rank < n_total % world else 0)
     r = Rng(seed, "synth")
     centres = np.array([[-4.0 + 8.0 * r.real01() for _ in range(D)] for _ in range(16)],
                        np.float32)
-    g = torch.Generator(device=f"cuda:{local}").manual_seed(seed)
+    g = torch.Generator(device=f"cuda:{local}").manual_seed(seed + rank)
     x = torch.randn((n, D), device=f"cuda:{local}", generator=g, dtype=torch.float32)
     comp = torch.randint(0, 16, (n,), device=f"cuda:{local}", generator=g)
     x += torch.from_numpy(centres).to(x.device)[comp]
@@ -416,8 +428,13 @@ def run_c4_leg(local, n=100_000_000, rho=0.1, epochs=EPOCHS, warm=2):
 
     e = tsom.Engine(P, D, device=local)
     e.bind_device(x.data_ptr(), n)
-    e.set_codebook(init_sample_draw(_Rows(), P, seed))
-    m = max(1, int(np.floor(n * rho)))
+    if attach is not None:
+        attach(e)
+    w0 = [init_sample_draw(_Rows(), P, seed) if rank == 0 else None]
+    if bcast is not None:
+        w0 = bcast(w0)
+    e.set_codebook(w0[0])
+    m = max(1, int(np.floor(n_total * rho)))
     e.sampler_init("adaptive", m, seed)
     sigma0 = resolved_sigma0("rng", 0, 0, 0.0)
     refresh = RefreshState(max(1, epochs // 10), 1.5, 25)
@@ -445,14 +462,17 @@ def run_c4_leg(local, n=100_000_000, rho=0.1, epochs=EPOCHS, warm=2):
     ev1.record(stream)
     torch.cuda.synchronize()
     secs = ev0.elapsed_time(ev1) / 1e3
+    if tmax is not None:
+        secs = tmax(secs)
     s, c = e.qe()
     e.close()
     del x
     torch.cuda.empty_cache()
     return {"workload": "c4: 1024-node RNG-topology SOM (device refresh), 1e8 x 50 GMM rows "
-                        "resident, adaptive sampler rho=0.1 on the device, 10 epochs",
-            "value": m * epochs / secs, "unit": "selected samples*epochs/s",
-            "rows_considered_per_s": n * epochs / secs, "ms_per_epoch": secs * 1e3 / epochs,
+                        "resident (split over the GPUs), adaptive sampler rho=0.1 on the device "
+                        "(one sharded sampler), 10 epochs",
+            "value": m * epochs / secs, "unit": "selected samples*epochs/s", "n_gpus": world,
+            "rows_considered_per_s": n_total * epochs / secs, "ms_per_epoch": secs * 1e3 / epochs,
             "phase_ms": {k: round(statistics.mean(p[k] for p in phases), 3) for k in phases[0]},
             "qe_after": s / c}
 
