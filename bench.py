@@ -454,11 +454,12 @@ def run_c4_leg(local, n=100_000_000, rho=0.1, epochs=EPOCHS, warm=2, world=1, ra
         epoch(t)
     refresh = RefreshState(max(1, epochs // 10), 1.5, 25)
     torch.cuda.synchronize()
-    phases = []
+    phases, rechecks = [], []
     ev0.record(stream)
     for t in range(epochs):
         epoch(t)
         phases.append(e.timing_detail())
+        rechecks.append(e.last_recheck_count)
     ev1.record(stream)
     torch.cuda.synchronize()
     secs = ev0.elapsed_time(ev1) / 1e3
@@ -474,6 +475,7 @@ def run_c4_leg(local, n=100_000_000, rho=0.1, epochs=EPOCHS, warm=2, world=1, ra
             "value": m * epochs / secs, "unit": "selected samples*epochs/s", "n_gpus": world,
             "rows_considered_per_s": n_total * epochs / secs, "ms_per_epoch": secs * 1e3 / epochs,
             "phase_ms": {k: round(statistics.mean(p[k] for p in phases), 3) for k in phases[0]},
+            "rechecked_rows_per_epoch": statistics.mean(rechecks),
             "qe_after": s / c}
 
 
