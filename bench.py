@@ -113,6 +113,18 @@ def dist_env():
 # CPU reference (oracle/_ref: the reference headers compiled) on a bounded sample
 # ---------------------------------------------------------------------------
 
+def cpu_model():
+    """Host CPU model name (from /proc/cpuinfo) for the cpu_baseline record."""
+    try:
+        with open("/proc/cpuinfo") as f:
+            for ln in f:
+                if ln.startswith("model name"):
+                    return ln.split(":", 1)[1].strip()
+    except OSError:
+        pass
+    return None
+
+
 def cpu_reference(step_seconds=6.0, steps=1, warmup=0):
     """Time the reference's train_parallel (all host cores) on a bounded sample
     of the headline workload: 32x32 hex, D=50, full sampling; each step = one
@@ -161,7 +173,7 @@ def run_reference_arm(args):
         "config": {"workload": "c2: 32x32 hex SOM (1024 nodes), D=50, GMM rows, full sampling "
                                "(bounded CPU sample)", "model": "batch-SOM"},
         "cpu_baseline": {"value": value, "unit": UNIT, "cores": cores, "kind": kind,
-                         "sample": sample},
+                         "sample": sample, "cpu_model": cpu_model()},
         "e2e": {"value": value, "unit": UNIT, "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0},
     }
     print(json.dumps(line), flush=True)
@@ -320,7 +332,8 @@ def run_gpu_arm(args):
                "h2d_bytes_per_step": int(h2d / EPOCHS), "d2h_bytes_per_step": int(d2h / EPOCHS),
                "path": "C-ABI tsom_bind_host_data + 10 x tsom_train_epoch + tsom_get_codebook "
                        "from pinned host rows, wall clock incl. engine creation (and the "
-                       "NCCL communicator when N > 1), max over ranks",
+                       "NCCL communicator when N > 1), max over ranks; device buffers come "
+                       "from the engines' per-device caching pool, warm after the warm-up call",
                "seconds_per_call": secs, "epochs_per_call": EPOCHS, "best_of": 3,
                "split_s": split}
         from paper_2604_26555_b200 import dropin
@@ -385,7 +398,7 @@ def run_gpu_arm(args):
     if rank == 0 and world == 1 and not args.no_cpu:
         v, cores, kind, sample, _ = cpu_reference(step_seconds=6.0)
         line["cpu_baseline"] = {"value": v, "unit": UNIT, "cores": cores, "kind": kind,
-                                "sample": sample}
+                                "sample": sample, "cpu_model": cpu_model()}
     if rank == 0:
         print(json.dumps(line), flush=True)
     if world > 1:

@@ -192,6 +192,9 @@ int tsom_sampler_state(tsom_engine* eng, double* last_error, uint32_t* age);
 /* Host-only check of the jump-ahead (no GPU): 0 when the state jumped by `jump`
  * draws from mt19937_64(seed) equals sequential generation. */
 int tsom_mt_selftest(uint64_t seed, uint64_t jump);
+/* Return the device memory cached by destroyed engines to the driver (engines
+ * allocate from a per-device caching pool; cf. torch.cuda.empty_cache). */
+int tsom_release_cached_memory(int device);
 
 /* Multi-GPU (one process per GPU) ---------------------------------------- */
 

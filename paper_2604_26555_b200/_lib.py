@@ -41,7 +41,7 @@ EXPORTS = [
     "tsom_stream", "tsom_last_timing_detail", "tsom_kernel_launches", "tsom_refresh_topology",
     "tsom_pairwise_sq_dists", "tsom_bind_shards", "tsom_active_bmu_kernel",
     "tsom_sampler_init", "tsom_sampler_select", "tsom_sampler_observe", "tsom_sampler_state",
-    "tsom_mt_selftest",
+    "tsom_mt_selftest", "tsom_release_cached_memory",
 ]
 
 SAMPLER_KINDS = {"full": 0, "random": 1, "adaptive": 2}  # SamplingKind, sampling.hpp:163
@@ -113,6 +113,7 @@ def load():
     L.tsom_sampler_state.argtypes = [_vp, _vp, _vp]
     L.tsom_mt_selftest.argtypes = [u64, u64]
     L.tsom_mt_selftest.restype = i32
+    L.tsom_release_cached_memory.argtypes = [i32]
     L.tsom_last_recheck_count.argtypes = [_vp]
     L.tsom_last_recheck_count.restype = u64
     L.tsom_active_bmu_kernel.argtypes = [_vp]
@@ -135,6 +136,13 @@ def load():
 
 def kernel_launches() -> int:
     return int(load().tsom_kernel_launches())
+
+
+def release_cached_memory(device: int = 0) -> None:
+    """Trim the per-device pool engines allocate from (cf. torch.cuda.empty_cache)."""
+    st = load().tsom_release_cached_memory(int(device))
+    if st:
+        raise RuntimeError(f"tsom_release_cached_memory failed ({st})")
 
 
 def mt_selftest(seed: int, jump: int) -> int:

@@ -35,11 +35,72 @@ namespace tsom {
 
 std::atomic<uint64_t> g_launches{0};
 
+// Device memory comes from one stream-ordered pool per device that keeps freed
+// blocks cached (like torch's caching allocator): an engine created after
+// another one reuses its memory instead of paying cudaMalloc/cudaFree (tens to
+// hundreds of ms for GB-sized buffers).  Allocations are made on a private,
+// otherwise idle stream and synchronised, so a block is usable from every
+// stream on return; frees follow a device synchronisation (cudaFree's own
+// semantics), so no queued work can still touch a block the pool hands out
+// again.  tsom_release_cached_memory() trims the pool.
+struct DevicePool {
+    cudaMemPool_t pool = nullptr;
+    cudaStream_t st = nullptr;
+};
+
+static std::mutex g_pool_mu;
+static DevicePool g_pools[64];
+
+static cudaError_t device_pool(DevicePool** out) {
+    int dev = 0;
+    cudaError_t e = cudaGetDevice(&dev);
+    if (e != cudaSuccess) return e;
+    if (dev < 0 || dev >= 64) return cudaErrorInvalidDevice;
+    std::lock_guard<std::mutex> lk(g_pool_mu);
+    DevicePool& dp = g_pools[dev];
+    if (!dp.pool) {
+        cudaMemPoolProps props{};
+        props.allocType = cudaMemAllocationTypePinned;
+        props.location.type = cudaMemLocationTypeDevice;
+        props.location.id = dev;
+        if ((e = cudaMemPoolCreate(&dp.pool, &props)) != cudaSuccess) return e;
+        uint64_t keep = UINT64_MAX;
+        cudaMemPoolSetAttribute(dp.pool, cudaMemPoolAttrReleaseThreshold, &keep);
+        if ((e = cudaStreamCreateWithFlags(&dp.st, cudaStreamNonBlocking)) != cudaSuccess) {
+            cudaMemPoolDestroy(dp.pool);
+            dp.pool = nullptr;
+            return e;
+        }
+    }
+    *out = &dp;
+    return cudaSuccess;
+}
+
+void release_cached_memory() {
+    int dev = 0;
+    if (cudaGetDevice(&dev) != cudaSuccess || dev < 0 || dev >= 64) return;
+    std::lock_guard<std::mutex> lk(g_pool_mu);
+    if (g_pools[dev].pool) {
+        cudaStreamSynchronize(g_pools[dev].st);
+        cudaMemPoolTrimTo(g_pools[dev].pool, 0);
+    }
+}
+
 cudaError_t DevBuf::ensure(size_t need) {
     if (need <= bytes && p) return cudaSuccess;
     release();
     if (need == 0) return cudaSuccess;
-    cudaError_t e = cudaMalloc(&p, need);
+    DevicePool* dp = nullptr;
+    cudaError_t e = device_pool(&dp);
+    if (e == cudaSuccess) {
+        e = cudaMallocFromPoolAsync(&p, need, dp->pool, dp->st);
+        if (e == cudaErrorMemoryAllocation) {  // cached blocks may be in the way
+            cudaGetLastError();
+            release_cached_memory();
+            e = cudaMallocFromPoolAsync(&p, need, dp->pool, dp->st);
+        }
+        if (e == cudaSuccess) e = cudaStreamSynchronize(dp->st);
+    }
     if (e != cudaSuccess) {
         p = nullptr;
         bytes = 0;
@@ -50,8 +111,12 @@ cudaError_t DevBuf::ensure(size_t need) {
     return cudaSuccess;
 }
 
-void DevBuf::release() {
-    if (p && owned) cudaFree(p);
+void DevBuf::release(bool synced) {
+    if (p && owned) {
+        DevicePool* dp = nullptr;
+        if (!synced) cudaDeviceSynchronize();
+        if (device_pool(&dp) == cudaSuccess) cudaFreeAsync(p, dp->st);
+    }
     p = nullptr;
     bytes = 0;
     owned = true;
@@ -315,7 +380,7 @@ std::string read_shard_rows(const Engine* eng, uint64_t r0, uint64_t r1, float* 
 
 const float* host_chunk_source(Engine* eng, uint64_t r0, uint64_t r1, int s) {
     if (eng->shards.empty() && eng->host_direct) return eng->host_rows + r0 * eng->D;
-    ensure_pinned(eng, eng->stream_chunk_rows);
+    ensure_pinned(eng, std::max<uint64_t>(r1 - r0, eng->pinned_rows));
     if (eng->pin_busy[s]) CU(cudaEventSynchronize(eng->ev_pin[s]));
     float* dst = eng->pinned[s];
     // one host thread streams ~10 GB/s; split the fill so staging keeps up
@@ -350,6 +415,22 @@ void note_pinned_copy(Engine* eng, int s) {
     if (eng->shards.empty() && eng->host_direct) return;
     CU(cudaEventRecord(eng->ev_pin[s], eng->copy_stream));
     eng->pin_busy[s] = true;
+}
+
+// Copy rows [0, total) of the bound host source (shard files or caller rows)
+// into eng->x: staging threads fill one pinned slot while the copy engine
+// drains the other.
+void upload_rows(Engine* eng, uint64_t total, uint64_t C) {
+    for (uint64_t r0 = 0, c = 0; r0 < total; r0 += C, ++c) {
+        const uint64_t r1 = std::min(total, r0 + C);
+        const int s = (int)(c & 1);
+        const float* src = host_chunk_source(eng, r0, r1, s);
+        CU(cudaMemcpyAsync(eng->x.as<float>() + r0 * eng->D, src,
+                           (r1 - r0) * eng->D * sizeof(float), cudaMemcpyHostToDevice,
+                           eng->copy_stream));
+        note_pinned_copy(eng, s);
+    }
+    CU(cudaStreamSynchronize(eng->copy_stream));
 }
 
 // K2 scratch (counting sort + piece partials) sized for `rows` rows per launch.
@@ -612,7 +693,7 @@ int tsom_create(int device, uint32_t nodes, uint32_t dims, tsom_engine** out) {
 int tsom_destroy(tsom_engine* eng) {
     if (!eng) return TSOM_OK;
     cudaSetDevice(eng->device);
-    if (eng->stream) cudaStreamSynchronize(eng->stream);
+    cudaDeviceSynchronize();  // every stream of this engine idle before its blocks return
     if (eng->nccl_comm && g_nccl.commDestroy) g_nccl.commDestroy((ncclComm_t)eng->nccl_comm);
     if (eng->host_registered) cudaHostUnregister(const_cast<float*>(eng->host_rows));
     close_shards(eng);
@@ -631,7 +712,7 @@ int tsom_destroy(tsom_engine* eng) {
                       &eng->topo_buf[8], &eng->topo_buf[9], &eng->topo_buf[10], &eng->topo_buf[11],
                       &eng->topo_buf[12], &eng->topo_buf[13], &eng->topo_buf[14], &eng->U, &eng->H, &eng->status, &eng->smooth_scratch,
                       &eng->stage[0], &eng->stage[1]})
-        b->release();
+        b->release(true);
     for (auto& ev : eng->ev)
         if (ev) cudaEventDestroy(ev);
     if (eng->stream) cudaStreamDestroy(eng->stream);
@@ -720,7 +801,22 @@ int tsom_bind_host_data(tsom_engine* eng, const float* rows, uint64_t n_rows, ui
         const size_t bytes = n_rows * eng->D * sizeof(float);
         CU(eng->x.ensure(bytes + tsom::kRowSlack));
         eng->x_slack = true;
-        if (bytes) CU(cudaMemcpy(eng->x.p, rows, bytes, cudaMemcpyHostToDevice));
+        cudaPointerAttributes pa{};
+        const bool pinned = n_rows && cudaPointerGetAttributes(&pa, rows) == cudaSuccess &&
+                            pa.type == cudaMemoryTypeHost;
+        cudaGetLastError();
+        if (pinned || bytes < ((size_t)64 << 20)) {
+            if (bytes) CU(cudaMemcpy(eng->x.p, rows, bytes, cudaMemcpyHostToDevice));
+        } else {
+            // pageable rows: the driver's own staging runs at ~11 GB/s and
+            // pinning in place (cudaHostRegister) at ~21 GB/s; the
+            // multi-threaded pinned staging reaches ~22 GB/s (B200 box,
+            // scripts/bind_breakdown.py)
+            eng->host_rows = rows;
+            const uint64_t rowb = (uint64_t)eng->D * sizeof(float);
+            upload_rows(eng, n_rows, std::max<uint64_t>(1, ((uint64_t)32 << 20) / rowb));
+            eng->host_rows = nullptr;
+        }
         tsom::launch_row_norm_max(eng->x.as<float>(), n_rows, eng->D, eng->x2max.as<float>(),
                                   eng->stream);
         CU(cudaGetLastError());
@@ -783,17 +879,7 @@ int tsom_bind_shards(tsom_engine* eng, const char* const* paths, uint32_t n_path
         eng->streamed = false;
         CU(eng->x.ensure(total * eng->D * sizeof(float) + tsom::kRowSlack));
         eng->x_slack = true;
-        const uint64_t C = eng->stream_chunk_rows;
-        for (uint64_t r0 = 0, c = 0; r0 < total; r0 += C, ++c) {
-            const uint64_t r1 = std::min(total, r0 + C);
-            const int s = (int)(c & 1);
-            const float* src = host_chunk_source(eng, r0, r1, s);
-            CU(cudaMemcpyAsync(eng->x.as<float>() + r0 * eng->D, src,
-                               (r1 - r0) * eng->D * sizeof(float), cudaMemcpyHostToDevice,
-                               eng->copy_stream));
-            note_pinned_copy(eng, s);
-        }
-        CU(cudaStreamSynchronize(eng->copy_stream));
+        upload_rows(eng, total, eng->stream_chunk_rows);
         close_shards(eng);
         tsom::launch_row_norm_max(eng->x.as<float>(), total, eng->D, eng->x2max.as<float>(),
                                   eng->stream);
@@ -1290,6 +1376,16 @@ int tsom_sampler_state(tsom_engine* eng, double* last_error, uint32_t* age) {
 }
 
 int tsom_mt_selftest(uint64_t seed, uint64_t jump) { return tsom::mt::selftest(seed, jump); }
+
+int tsom_release_cached_memory(int device) {
+    if (cudaSetDevice(device) != cudaSuccess) {
+        cudaGetLastError();
+        return TSOM_ERR_CUDA;
+    }
+    cudaDeviceSynchronize();
+    tsom::release_cached_memory();
+    return TSOM_OK;
+}
 
 int tsom_train_epoch(tsom_engine* eng, double eta, double sigma, double momentum, uint32_t flags) {
     return guarded(eng, [&] {

@@ -6,6 +6,7 @@
 // exports a flat C entry with the same config layout as oracle/_ref's
 // ref_train, so tests and bench.py can run the identical reference loop with
 // the GPU executor swapped in.  No kernel code lives here.
+#include <chrono>
 #include <cstdint>
 #include <cstring>
 #include <stdexcept>
@@ -102,6 +103,23 @@ static Sampler make_sampler(const dropin_config* rc, std::size_t n, std::uint64_
         return Sampler(static_cast<SamplingKind>(rc->sampling), b, n, seed, rc->alpha, rc->beta);
 }
 
+// Executor wrapper that times run_iteration (flags bit 4: profile breakdown)
+struct TimedExecutor {
+    toposom_b200::CudaExecutor& ex;
+    double iter_s = 0.0;
+    IterationAccumulators run_iteration(const std::vector<std::uint32_t>& selected,
+                                        const DataMatrix& weights, const std::vector<double>& infl,
+                                        double eta, std::size_t n_chunks,
+                                        std::vector<double>& distances) {
+        const auto t0 = std::chrono::steady_clock::now();
+        auto acc = ex.run_iteration(selected, weights, infl, eta, n_chunks, distances);
+        iter_s += std::chrono::duration<double>(std::chrono::steady_clock::now() - t0).count();
+        return acc;
+    }
+    std::size_t workers() const { return ex.workers(); }
+    double barrier_wait_s() const { return ex.barrier_wait_s(); }
+};
+
 // train_with_executor + CudaExecutor over any DataSourceRef (in-memory or ShardSet)
 static void run_train(const dropin_config* rc, const DataSourceRef& src, float* weights_out,
                       double* qe_log, std::uint8_t* refresh_log, int device, unsigned flags,
@@ -116,7 +134,19 @@ static void run_train(const dropin_config* rc, const DataSourceRef& src, float* 
         to.log_qe = qe_log != nullptr;
         const auto t0 = std::chrono::steady_clock::now();
         std::pair<SomModel, RunLog> result;
-        if (flags & 8u) {
+        if (flags & 16u) {
+            // profile: seconds_out[1] = executor construction (bind), [2] = run_iteration
+            if (sampler.kind() != SamplingKind::adaptive && !(flags & 8u))
+                opts.distances = toposom_b200::Distances::never;
+            toposom_b200::CudaExecutor ex(src, c.nodes(), opts);
+            const auto t1 = std::chrono::steady_clock::now();
+            TimedExecutor tex{ex};
+            result = train_with_executor(c, src, sampler, tex, to);
+            if (seconds_out) {
+                seconds_out[1] = std::chrono::duration<double>(t1 - t0).count();
+                seconds_out[2] = tex.iter_s;
+            }
+        } else if (flags & 8u) {
             opts.distances = toposom_b200::Distances::always;
             toposom_b200::CudaExecutor ex(src, c.nodes(), opts);
             result = train_with_executor(c, src, sampler, ex, to);

@@ -38,10 +38,12 @@ struct DevBuf {
     size_t bytes = 0;
     bool owned = true;
     cudaError_t ensure(size_t need);
-    void release();
+    void release(bool synced = false);  // synced: the device is known idle
     template <typename T>
     T* as() const { return static_cast<T*>(p); }
 };
+
+void release_cached_memory();  // trim the device pool DevBuf allocates from
 
 struct Error {
     int code;

@@ -276,9 +276,31 @@ __global__ void __launch_bounds__(kSplitThreads) k_split_rows(
             rbase[t] = (sel ? (uint64_t)sel[pos] : pos) * D;
         }
         __syncthreads();
-        for (uint32_t e = t; e < rows * D; e += kSplitThreads) {
-            const uint32_t r = e / D, k = e - r * D;
-            srow[r * ld + k] = x[rbase[r] + k];
+        {
+            // one warp per row (rows w, w+8, ...), lanes along K (D <= 64):
+            // all of a warp's loads are issued before its stores so the
+            // gathered rows' latencies overlap
+            const uint32_t w = t >> 5, lane = t & 31;
+            constexpr int kRowsPerWarp = kTcTileM / (kSplitThreads / 32);
+            float v[kRowsPerWarp][2];
+#pragma unroll
+            for (int i = 0; i < kRowsPerWarp; ++i) {
+                const uint32_t r = w + 8u * i;
+#pragma unroll
+                for (int h = 0; h < 2; ++h) {
+                    const uint32_t k = lane + 32u * h;
+                    v[i][h] = (r < rows && k < D) ? __ldg(x + rbase[r] + k) : 0.0f;
+                }
+            }
+#pragma unroll
+            for (int i = 0; i < kRowsPerWarp; ++i) {
+                const uint32_t r = w + 8u * i;
+#pragma unroll
+                for (int h = 0; h < 2; ++h) {
+                    const uint32_t k = lane + 32u * h;
+                    if (r < rows && k < D) srow[r * ld + k] = v[i][h];
+                }
+            }
         }
         __syncthreads();
         if (t < kTcTileM) {

@@ -137,22 +137,25 @@ def run_study_cuda(base, n_trials: int, seeds, train: np.ndarray, holdout: np.nd
 
 
 def train_cuda(cfg, data: np.ndarray, device: int = 0, log_qe: bool = False,
-               streamed: bool = False, bmu_kernel: int = 0, force_distances: bool = False):
-    """Reference train_with_executor + CudaExecutor.  Returns (weights, qe_log, refresh_log, s)."""
+               streamed: bool = False, bmu_kernel: int = 0, force_distances: bool = False,
+               profile: bool = False):
+    """Reference train_with_executor + CudaExecutor.  Returns (weights, qe_log, refresh_log, s);
+    with profile=True, s = (total, executor construction incl. bind, sum of run_iteration)."""
     L = load()
     data = np.ascontiguousarray(data, np.float32)
     n, d = data.shape
     w = np.empty((cfg.nodes, d), np.float32)
     qe = np.zeros(cfg.n_iters) if log_qe else None
     ref = np.zeros(cfg.n_iters, np.uint8)
-    secs = C.c_double()
-    flags = (1 if streamed else 0) | ((bmu_kernel & 3) << 1) | (8 if force_distances else 0)
+    secs = (C.c_double * 3)()
+    flags = ((1 if streamed else 0) | ((bmu_kernel & 3) << 1) | (8 if force_distances else 0)
+             | (16 if profile else 0))
     st = L.tsom_dropin_train(C.byref(_cfg(cfg)), data.ctypes.data, n, d, w.ctypes.data,
                              qe.ctypes.data if log_qe else None, ref.ctypes.data, device, flags,
-                             C.byref(secs))
+                             secs)
     if st:
         _lib._raise(st, L.tsom_dropin_last_error().decode())
-    return w, qe, ref, secs.value
+    return w, qe, ref, (tuple(secs) if profile else secs[0])
 
 
 def train_cuda_shards(cfg, shard_dir: str, d: int, device: int = 0, log_qe: bool = False,
