@@ -99,6 +99,15 @@ cudaError_t DevBuf::ensure(size_t need) {
             release_cached_memory();
             e = cudaMallocFromPoolAsync(&p, need, dp->pool, dp->st);
         }
+        if (e == cudaSuccess) {
+            // debug: TSOM_POISON_ALLOC=<hex byte> fills new blocks with it so a
+            // kernel that relies on zeroed memory fails deterministically
+            static const int poison = [] {
+                const char* v = getenv("TSOM_POISON_ALLOC");
+                return v && v[0] ? (int)strtol(v, nullptr, 16) : -1;
+            }();
+            if (poison >= 0) e = cudaMemsetAsync(p, poison & 0xFF, need, dp->st);
+        }
         if (e == cudaSuccess) e = cudaStreamSynchronize(dp->st);
     }
     if (e != cudaSuccess) {
@@ -680,6 +689,7 @@ int tsom_create(int device, uint32_t nodes, uint32_t dims, tsom_engine** out) {
         CU(eng->H.ensure(P * sizeof(double)));
         CU(eng->status.ensure(4 * sizeof(int)));
         ensure_rows(eng, 1);
+        CU(cudaStreamSynchronize(0));  // the legacy-stream memsets above have landed
     });
     if (rc != TSOM_OK) {
         std::fprintf(stderr, "tsom_create: %s\n", eng->last_error.c_str());
@@ -748,6 +758,9 @@ int tsom_set_option(tsom_engine* eng, int key, int64_t value) {
             case 99:  // diagnostics (not in the public header): K1 stage isolation
                 tsom::g_k1_debug = (uint32_t)value;
                 break;
+            case 98:  // diagnostics: element-wise 3xFP16 split (k_split_rows<kTcF16>)
+                tsom::g_split_v1 = (int)value;
+                break;
             case TSOM_OPT_HOST_REGISTER:
                 eng->host_register = value != 0;
                 break;
@@ -806,7 +819,10 @@ int tsom_bind_host_data(tsom_engine* eng, const float* rows, uint64_t n_rows, ui
                             pa.type == cudaMemoryTypeHost;
         cudaGetLastError();
         if (pinned || bytes < ((size_t)64 << 20)) {
-            if (bytes) CU(cudaMemcpy(eng->x.p, rows, bytes, cudaMemcpyHostToDevice));
+            // on the stream the norm kernel below runs on (a plain cudaMemcpy
+            // from pageable memory may return before its DMA lands)
+            if (bytes)
+                CU(cudaMemcpyAsync(eng->x.p, rows, bytes, cudaMemcpyHostToDevice, eng->stream));
         } else {
             // pageable rows: the driver's own staging runs at ~11 GB/s and
             // pinning in place (cudaHostRegister) at ~21 GB/s; the
@@ -922,7 +938,7 @@ int tsom_bind_synthetic_gmm(tsom_engine* eng, uint64_t n_rows, uint64_t seed, ui
         for (auto& c : centres) c = (float)(-4.0 + 8.0 * ((double)(gen() >> 11) * 0x1.0p-53));
         DevBuf dc;
         CU(dc.ensure(centres.size() * sizeof(float)));
-        CU(cudaMemcpy(dc.p, centres.data(), centres.size() * sizeof(float), cudaMemcpyHostToDevice));
+        CU(tsom::h2d_blocking(dc.p, centres.data(), centres.size() * sizeof(float)));
         const size_t bytes = n_rows * eng->D * sizeof(float);
         CU(eng->x.ensure(bytes + tsom::kRowSlack));
         eng->x_slack = true;
@@ -1465,6 +1481,21 @@ uint64_t tsom_last_recheck_count(const tsom_engine* eng) { return eng ? eng->las
 // diagnostics only (not in the public header): K1 timestamps of CTA 0
 int tsom_debug_k1_trace(unsigned long long* out, uint32_t n) {
     return tsom::k1_trace_copy(out, n);
+}
+
+// diagnostics only (not in the public header): copy an internal device buffer
+// (0 xsplit, 1 xn2, 2 wsplit, 3 scale, 4 part, 5 gsplit, 6 gxn2, 7 w2max,
+// 8 x2max, 9 ties) to the host; returns the bytes copied
+int64_t tsom_debug_read(tsom_engine* eng, int which, void* out, uint64_t bytes) {
+    if (!eng) return -1;
+    cudaSetDevice(eng->device);
+    tsom::DevBuf* bufs[] = {&eng->xsplit, &eng->xn2, &eng->wsplit, &eng->scale, &eng->part,
+                            &eng->gsplit, &eng->gxn2, &eng->w2max, &eng->x2max, &eng->ties};
+    if (which < 0 || which >= (int)(sizeof(bufs) / sizeof(bufs[0]))) return -1;
+    const uint64_t nb = std::min<uint64_t>(bytes, bufs[which]->bytes);
+    cudaStreamSynchronize(eng->stream);
+    if (nb && cudaMemcpy(out, bufs[which]->p, nb, cudaMemcpyDeviceToHost) != cudaSuccess) return -1;
+    return (int64_t)nb;
 }
 
 int tsom_active_bmu_kernel(const tsom_engine* eng) {

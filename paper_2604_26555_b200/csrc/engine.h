@@ -45,6 +45,15 @@ struct DevBuf {
 
 void release_cached_memory();  // trim the device pool DevBuf allocates from
 
+// Host-to-device copy that is complete on return.  cudaMemcpy from pageable
+// memory may return once the data is staged, before the DMA lands; kernels on
+// the engine's non-blocking streams are not ordered after it.
+inline cudaError_t h2d_blocking(void* dst, const void* src, size_t bytes) {
+    cudaError_t e = cudaMemcpy(dst, src, bytes, cudaMemcpyHostToDevice);
+    if (e == cudaSuccess) e = cudaStreamSynchronize(0);
+    return e;
+}
+
 struct Error {
     int code;
     std::string msg;
@@ -323,6 +332,7 @@ cudaError_t launch_bmu_tc(int kind, const void* tiles, uint64_t n, const uint32_
                           const uint32_t* rmask, float* part, int sm_count, size_t smem_optin,
                           cudaStream_t st);
 extern uint32_t g_k1_debug;
+extern int g_split_v1;
 int k1_trace_copy(unsigned long long* out, uint32_t n);  // diagnostics  // diagnostics: bit0 skip epilogue math, bit1 skip MMAs
 // main-pass merge: bmu for rows with a clear winner, near-tie positions -> ties
 constexpr uint32_t kTcEpiSets = 2;  // K1 main pass: partial results per group (sub-groups)

@@ -379,6 +379,105 @@ __global__ void __launch_bounds__(kSplitThreads) k_split_rows(
     }
 }
 
+// 3xFP16 split, warp-synchronous: a warp owns 32 consecutive tile rows (a
+// quarter tile).  It stages them in its own shared-memory slice with
+// coalesced row loads (lanes along K, 16 rows in flight), then every lane
+// converts its own row — the FP64 norm in the same sequential order as
+// k_split_rows<kTcF16>, so the output is bit-identical — and writes the row's
+// 16-byte cores; for a fixed core the 32 lanes write 512 contiguous bytes.
+// No block-wide barriers: warps stream independently.
+constexpr int kSplitWarpRows = 32;
+
+__global__ void __launch_bounds__(kSplitThreads) k_split_rows_f16(
+    const float* __restrict__ x, const uint32_t* __restrict__ sel,
+    const uint32_t* __restrict__ idx, const uint32_t* __restrict__ dev_n, uint64_t n_host,
+    uint32_t D, const float* __restrict__ scale, TieWin win, uint8_t* __restrict__ tiles,
+    float* __restrict__ xn2) {
+    extern __shared__ float split_wsm[];
+    const uint64_t n = dev_n ? min((uint64_t)*dev_n, n_host) : n_host;
+    const uint64_t nchunks = (n + kTcTileM - 1) / kTcTileM * (kTcTileM / kSplitWarpRows);
+    const TcGeom geo = tc_geom(kTcF16, D);
+    const uint32_t ld = (D + 1) | 1u;  // odd stride: lane-per-row reads conflict free
+    const float s = scale[0];
+    const float S = scale[1];
+    const uint32_t w = threadIdx.x >> 5, lane = threadIdx.x & 31;
+    float* my = split_wsm + w * kSplitWarpRows * ld;
+    const __half one = __float2half(1.0f), zero = __float2half(0.0f);
+    const uint64_t nwarps = (uint64_t)gridDim.x * (kSplitThreads / 32);
+    for (uint64_t c = blockIdx.x * (uint64_t)(kSplitThreads / 32) + w; c < nchunks; c += nwarps) {
+        const uint64_t r0 = c * kSplitWarpRows;
+        const uint32_t rows =
+            r0 >= n ? 0u : (n - r0 < (uint64_t)kSplitWarpRows ? (uint32_t)(n - r0) : kSplitWarpRows);
+        uint64_t myrow = 0;
+        if (lane < rows) {
+            const uint64_t pos = idx ? (uint64_t)idx[r0 + lane] : r0 + lane;
+            myrow = sel ? (uint64_t)sel[pos] : pos;
+        }
+#pragma unroll
+        for (int half = 0; half < 2; ++half) {
+            float v[16][2];
+#pragma unroll
+            for (int i = 0; i < 16; ++i) {
+                const uint32_t r = half * 16 + i;
+                const uint64_t rb = __shfl_sync(0xffffffffu, myrow, r) * D;
+                v[i][0] = (r < rows && lane < D) ? __ldg(x + rb + lane) : 0.0f;
+                v[i][1] = (r < rows && lane + 32u < D) ? __ldg(x + rb + lane + 32u) : 0.0f;
+            }
+#pragma unroll
+            for (int i = 0; i < 16; ++i) {
+                float* dst = my + (half * 16 + i) * ld;
+                if (lane < D) dst[lane] = v[i][0];
+                if (lane + 32u < D) dst[lane + 32u] = v[i][1];
+            }
+        }
+        __syncwarp();
+        const bool valid = lane < rows;
+        const float* xr = my + lane * ld;
+        double nrm = 0.0;
+        if (valid)
+            for (uint32_t k = 0; k < D; ++k) {
+                const double t = (double)xr[k];
+                nrm += t * t;
+            }
+        const float nf = (float)nrm;
+        __half nh = zero, nl = zero;
+        if (valid) {
+            const double ns = (double)nf * (double)s * (double)s;
+            nh = __double2half(ns);
+            nl = __double2half(ns - (double)__half2float(nh));
+            if (xn2) xn2[r0 + lane] = tie_xpart(nf * 1.0000003f, S, win);
+        }
+        uint8_t* out = tiles + (c >> 2) * (uint64_t)geo.tile_bytes +
+                       (size_t)((c & 3) * kSplitWarpRows + lane) * 16;
+        for (uint32_t kc = 0; kc < geo.kpad / 8; ++kc) {
+            uint32_t pk[4] = {0u, 0u, 0u, 0u};
+#pragma unroll
+            for (int q = 0; q < 8; ++q) {
+                const uint32_t k = kc * 8 + q;
+                __half val = zero;
+                if (k < 3 * D) {
+                    const uint32_t seg = k < D ? 0u : (k < 2 * D ? 1u : 2u);
+                    const float xv = xr[k - seg * D] * s;
+                    const __half xh = __float2half_rn(xv);
+                    val = seg == 1 ? __float2half_rn(xv - __half2float(xh)) : xh;
+                } else if (k == 3 * D) {
+                    val = nh;
+                } else if (k == 3 * D + 1) {
+                    val = nl;
+                } else if (k < 3 * D + 5) {
+                    val = one;
+                }
+                pk[q >> 1] |= (uint32_t)__half_as_ushort(valid ? val : zero) << (16 * (q & 1));
+            }
+            *reinterpret_cast<uint4*>(out + (size_t)kc * kTcTileM * 16) =
+                make_uint4(pk[0], pk[1], pk[2], pk[3]);
+        }
+        __syncwarp();  // slice reused by the next chunk
+    }
+}
+
+int g_split_v1 = 0;  // debug: the element-wise split (TSOM option 98)
+
 void launch_split_rows(int kind, const float* x, const uint32_t* sel, const uint32_t* idx,
                        uint64_t n, uint32_t D, const float* scale, TieWin win, void* tiles,
                        float* xn2, cudaStream_t st, const uint32_t* dev_n) {
@@ -390,9 +489,25 @@ void launch_split_rows(int kind, const float* x, const uint32_t* sel, const uint
     if (kind == kTcTf32)
         TSOM_LAUNCH(k_split_rows<kTcTf32><<<(unsigned)tiles_n, kSplitThreads, smem, st>>>(
             x, sel, idx, dev_n, n, D, scale, win, t, xn2));
-    else
+    else if (g_split_v1)
         TSOM_LAUNCH(k_split_rows<kTcF16><<<(unsigned)tiles_n, kSplitThreads, smem, st>>>(
             x, sel, idx, dev_n, n, D, scale, win, t, xn2));
+    else {
+        const size_t wsmem = (size_t)(kSplitThreads / 32) * kSplitWarpRows * ((D + 1) | 1u) *
+                             sizeof(float);
+        static bool attr_set = false;
+        if (!attr_set) {
+            cudaFuncSetAttribute(k_split_rows_f16, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                 (int)(kSplitWarpRows * 8 * 64 * sizeof(float)));
+            cudaFuncSetAttribute(k_split_rows_f16,
+                                 cudaFuncAttributePreferredSharedMemoryCarveout, 100);
+            attr_set = true;
+        }
+        uint64_t blocks = ((n + kTcTileM - 1) / kTcTileM + 1) / 2;  // 4 warps per tile
+        if (blocks > 148ull * 8) blocks = 148ull * 8;
+        TSOM_LAUNCH(k_split_rows_f16<<<(unsigned)blocks, kSplitThreads, wsmem, st>>>(
+            x, sel, idx, dev_n, n, D, scale, win, t, xn2));
+    }
 }
 
 // ---------------------------------------------------------------------------

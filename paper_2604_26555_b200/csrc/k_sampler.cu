@@ -553,14 +553,14 @@ int sampler_setup(SamplerState& s, int kind, uint64_t n, uint64_t m, uint64_t se
     uint64_t w[312];
     mt::seed_window(z ^ (z >> 31), w);
     if (s.window.ensure(312 * 8) != cudaSuccess) return 4;
-    if (cudaMemcpy(s.window.p, w, 312 * 8, cudaMemcpyHostToDevice) != cudaSuccess) return 4;
+    if (h2d_blocking(s.window.p, w, 312 * 8) != cudaSuccess) return 4;
     if (s.misc.ensure(64) != cudaSuccess) return 4;
     if (s.sharded && s.slots.ensure((size_t)std::max(1, s.world) * 8) != cudaSuccess) return 4;
     if (kind == 2 && s.sharded) {
         // the stream advances by gN draws per epoch, whatever this rank's share
         const std::vector<uint64_t> JN = mt::jump_poly(gN);
         if (s.jN.ensure(312 * 8) != cudaSuccess) return 4;
-        if (cudaMemcpy(s.jN.p, JN.data(), 312 * 8, cudaMemcpyHostToDevice) != cudaSuccess) return 4;
+        if (h2d_blocking(s.jN.p, JN.data(), 312 * 8) != cudaSuccess) return 4;
     }
     if (!s.draws_per_epoch) return 0;
     const uint64_t total = s.draws_per_epoch + kSlack;
@@ -580,7 +580,7 @@ int sampler_setup(SamplerState& s, int kind, uint64_t n, uint64_t m, uint64_t se
         }
     }
     if (s.jp.ensure(jp.size() * 8) != cudaSuccess) return 4;
-    if (cudaMemcpy(s.jp.p, jp.data(), jp.size() * 8, cudaMemcpyHostToDevice) != cudaSuccess) return 4;
+    if (h2d_blocking(s.jp.p, jp.data(), jp.size() * 8) != cudaSuccess) return 4;
     const uint32_t twists = (mt::kSeq - 312 + 311) / 312;
     s.tail0 = s.draws_per_epoch;
     s.tail_len = 312 + kSlack;
@@ -604,11 +604,13 @@ int sampler_setup(SamplerState& s, int kind, uint64_t n, uint64_t m, uint64_t se
         const size_t chunk = 1 << 20;
         std::vector<double> init(std::min<uint64_t>(n, chunk), 1e30);
         for (uint64_t i = 0; i < n; i += chunk)
-            if (cudaMemcpy(s.err.as<double>() + i, init.data(), std::min<uint64_t>(chunk, n - i) * 8,
-                           cudaMemcpyHostToDevice) != cudaSuccess)
+            if (h2d_blocking(s.err.as<double>() + i, init.data(),
+                             std::min<uint64_t>(chunk, n - i) * 8) != cudaSuccess)
                 return 4;
         if (cudaMemset(s.age.p, 0, n * 4) != cudaSuccess) return 4;
         if (cudaMemset(s.hist.p, 0, 4096 * 4) != cudaSuccess) return 4;
+        // legacy-stream memsets: complete before the sampler's own streams use them
+        if (cudaStreamSynchronize(0) != cudaSuccess) return 4;
     }
     if (kind == 1) {
         if (s.first.ensure(gN * 4) != cudaSuccess || s.tidx.ensure(m * 4) != cudaSuccess) return 4;

@@ -390,3 +390,64 @@ def test_run_study_cuda_matches_reference(pkg, oracle_port, oracle_ref):
     ok = ~rf
     np.testing.assert_allclose(gt[ok], rt[ok], rtol=1e-5)
     np.testing.assert_allclose(gh[ok], rh[ok], rtol=1e-5)
+
+
+@pytest.mark.parametrize("d", [1, 2, 17, 50, 62])
+def test_split_row_image_equals_elementwise_split(pkg, oracle_port, d):
+    # the row-image 3xFP16 split (k_split_rows_f16) against the element-wise
+    # one (option 98): identical BMUs/distances, and both exact vs the oracle,
+    # on resident (tiles split once) and gathered (sampled selection) rows
+    from paper_2604_26555_b200 import _lib
+    rng = np.random.default_rng(40 + d)
+    n, p = 5000 + 37, 300
+    x = (rng.normal(size=(n, d)) * rng.uniform(0.1, 10.0, size=d)).astype(np.float32)
+    w = x[rng.choice(n, p, replace=False)].copy()
+    sel = np.sort(rng.choice(n, n // 3, replace=False)).astype(np.uint32)
+    out = {}
+    for v1 in (0, 1):
+        e = engine(pkg, p, d, 3)
+        try:
+            e.set_option(98, v1)
+            e.set_codebook(w)
+            b, dist = e.bmu(x)
+            e.bind(x)
+            e.set_influence(np.eye(p))
+            u, h, _ = e.epoch(0.5, selected=sel)
+            ua, ha, _ = e.epoch(0.5)
+            out[v1] = (b, dist, u, h, ua, ha)
+        finally:
+            e.set_option(98, 0)
+            e.close()
+    ob, od = oracle_port.find_bmus(x, w)
+    for v1 in (0, 1):
+        assert np.array_equal(out[v1][0], ob)
+        np.testing.assert_allclose(out[v1][1], od, rtol=1e-12)
+    for a, b in zip(out[0], out[1]):
+        assert np.array_equal(a, b)
+
+
+def test_bind_reuses_pool_blocks_exactly(pkg, oracle_port):
+    # engines reuse the device pool's blocks; a bind from pageable rows must be
+    # complete before the engine's own stream reads them (regression: the
+    # row-norm max once raced a plain cudaMemcpy and saw the previous engine's
+    # data, shrinking the FP16 scale below the error model)
+    def data(d, seed):
+        rng = np.random.default_rng(seed)
+        x = (rng.normal(size=(5037, d)) * rng.uniform(0.1, 10.0, size=d)).astype(np.float32)
+        return x, x[rng.choice(5037, 300, replace=False)].copy()
+    x0, w0 = data(60, 150)
+    e = engine(pkg, 300, 60, 3)
+    e.set_codebook(w0)
+    e.bmu(x0)
+    e.bind(x0)
+    e.bmu_bound()
+    e.close()
+    x, w = data(62, 102)
+    e = engine(pkg, 300, 62, 3)
+    e.set_codebook(w)
+    e.bmu(x)
+    e.bind(x)
+    b, _ = e.bmu_bound()
+    e.close()
+    ob, _ = oracle_port.find_bmus(x, w)
+    assert np.array_equal(b, ob)
