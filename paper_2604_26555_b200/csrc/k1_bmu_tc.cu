@@ -379,29 +379,40 @@ __global__ void __launch_bounds__(kSplitThreads) k_split_rows(
     }
 }
 
-// 3xFP16 split, warp-synchronous: a warp owns 32 consecutive tile rows (a
-// quarter tile).  It stages them in its own shared-memory slice with
-// coalesced row loads (lanes along K, 16 rows in flight), then every lane
-// converts its own row — the FP64 norm in the same sequential order as
-// k_split_rows<kTcF16>, so the output is bit-identical — and writes the row's
-// 16-byte cores; for a fixed core the 32 lanes write 512 contiguous bytes.
-// No block-wide barriers: warps stream independently.
-constexpr int kSplitWarpRows = 32;
+// 3xFP16 split, warp-synchronous: a warp owns 16 consecutive tile rows (an
+// eighth of a tile) and no block-wide barrier is involved.
+//   1. row loads are coalesced (lanes along K, 16 rows in flight);
+//   2. lane k converts element k of each row once (xh, xl) and stores the
+//      halves at K positions k, D + k, 2D + k of the row in the warp's
+//      half-precision row image (consecutive lanes -> consecutive halves);
+//   3. the FP64 row norms are reduced across lanes with a transposing
+//      butterfly (16 rows in 16 double shuffles), lane 2r ends with row r's
+//      norm and writes the row's augmented columns and its window term;
+//   4. lanes copy the image out in 16-byte cores (lanes 0-15: rows 0-15 of
+//      the first half of the cores, lanes 16-31: the second half), 256
+//      contiguous bytes per half-warp store.  The image's row stride is an odd
+//      number of 16-byte units, so those reads are bank-conflict free.
+// Matches k_split_rows<kTcF16> except for the summation order of the FP64 norm
+// (enters only the approximate distances and the error window, whose 1.0000003
+// factor covers it; decisions inside the window are re-checked in FP64).
+constexpr int kSplitWarpRows = 16;
 
-__global__ void __launch_bounds__(kSplitThreads) k_split_rows_f16(
+__global__ void __launch_bounds__(kSplitThreads, 4) k_split_rows_f16(
     const float* __restrict__ x, const uint32_t* __restrict__ sel,
     const uint32_t* __restrict__ idx, const uint32_t* __restrict__ dev_n, uint64_t n_host,
     uint32_t D, const float* __restrict__ scale, TieWin win, uint8_t* __restrict__ tiles,
     float* __restrict__ xn2) {
-    extern __shared__ float split_wsm[];
+    extern __shared__ __align__(16) uint8_t split_wsm[];
     const uint64_t n = dev_n ? min((uint64_t)*dev_n, n_host) : n_host;
-    const uint64_t nchunks = (n + kTcTileM - 1) / kTcTileM * (kTcTileM / kSplitWarpRows);
+    constexpr uint32_t kChunksPerTile = kTcTileM / kSplitWarpRows;
+    const uint64_t nchunks = (n + kTcTileM - 1) / kTcTileM * kChunksPerTile;
     const TcGeom geo = tc_geom(kTcF16, D);
-    const uint32_t ld = (D + 1) | 1u;  // odd stride: lane-per-row reads conflict free
+    const uint32_t hs = geo.kpad + 8;  // halves per image row: odd number of 16-byte units
+    const uint32_t ncores = geo.kpad / 8;
     const float s = scale[0];
     const float S = scale[1];
     const uint32_t w = threadIdx.x >> 5, lane = threadIdx.x & 31;
-    float* my = split_wsm + w * kSplitWarpRows * ld;
+    __half* img = reinterpret_cast<__half*>(split_wsm) + (size_t)w * kSplitWarpRows * hs;
     const __half one = __float2half(1.0f), zero = __float2half(0.0f);
     const uint64_t nwarps = (uint64_t)gridDim.x * (kSplitThreads / 32);
     for (uint64_t c = blockIdx.x * (uint64_t)(kSplitThreads / 32) + w; c < nchunks; c += nwarps) {
@@ -413,66 +424,73 @@ __global__ void __launch_bounds__(kSplitThreads) k_split_rows_f16(
             const uint64_t pos = idx ? (uint64_t)idx[r0 + lane] : r0 + lane;
             myrow = sel ? (uint64_t)sel[pos] : pos;
         }
+        float v[kSplitWarpRows][2];
 #pragma unroll
-        for (int half = 0; half < 2; ++half) {
-            float v[16][2];
+        for (int i = 0; i < kSplitWarpRows; ++i) {
+            const uint64_t rb = __shfl_sync(0xffffffffu, myrow, i) * D;
+            v[i][0] = ((uint32_t)i < rows && lane < D) ? __ldg(x + rb + lane) : 0.0f;
+            v[i][1] = ((uint32_t)i < rows && lane + 32u < D) ? __ldg(x + rb + lane + 32u) : 0.0f;
+        }
+        double p[kSplitWarpRows];
 #pragma unroll
-            for (int i = 0; i < 16; ++i) {
-                const uint32_t r = half * 16 + i;
-                const uint64_t rb = __shfl_sync(0xffffffffu, myrow, r) * D;
-                v[i][0] = (r < rows && lane < D) ? __ldg(x + rb + lane) : 0.0f;
-                v[i][1] = (r < rows && lane + 32u < D) ? __ldg(x + rb + lane + 32u) : 0.0f;
+        for (int i = 0; i < kSplitWarpRows; ++i) {
+            __half* row = img + i * hs;
+#pragma unroll
+            for (int h = 0; h < 2; ++h) {
+                const uint32_t k = lane + 32u * h;
+                if (k < D) {
+                    const float xv = v[i][h] * s;
+                    const __half xh = __float2half_rn(xv);
+                    row[k] = xh;
+                    row[D + k] = __float2half_rn(xv - __half2float(xh));
+                    row[2 * D + k] = xh;
+                }
             }
+            p[i] = (double)v[i][0] * (double)v[i][0] + (double)v[i][1] * (double)v[i][1];
+        }
+        // transposing butterfly: after the level with offset o, lanes with bit
+        // o set hold the upper half of the remaining rows
 #pragma unroll
-            for (int i = 0; i < 16; ++i) {
-                float* dst = my + (half * 16 + i) * ld;
-                if (lane < D) dst[lane] = v[i][0];
-                if (lane + 32u < D) dst[lane + 32u] = v[i][1];
+        for (int lvl = 0; lvl < 4; ++lvl) {
+            const int half = 8 >> lvl;
+            const uint32_t o = 16u >> lvl;
+            const bool up = (lane & o) != 0;
+#pragma unroll
+            for (int i = 0; i < half; ++i) {
+                const double keep = up ? p[i + half] : p[i];
+                const double send = up ? p[i] : p[i + half];
+                p[i] = keep + __shfl_xor_sync(0xffffffffu, send, o);
             }
+        }
+        p[0] += __shfl_xor_sync(0xffffffffu, p[0], 1);
+        const uint32_t rr = (lane >> 1) & 15u;  // the row whose norm this lane holds
+        const uint32_t ka = 3 * D + (lane & 1u) * 16u;
+        {
+            // lanes 2r, 2r+1 write row r's augmented columns [3D, kpad)
+            const bool valid = rr < rows;
+            const float nf = (float)p[0];
+            const double ns = (double)nf * (double)s * (double)s;
+            const __half nh = __double2half(ns);
+            const __half nl = __double2half(ns - (double)__half2float(nh));
+            __half* row = img + rr * hs;
+            for (uint32_t k = ka; k < geo.kpad && k < ka + 16u; ++k) {
+                const uint32_t a = k - 3 * D;
+                row[k] = !valid ? zero : a == 0 ? nh : a == 1 ? nl : a < 5 ? one : zero;
+            }
+            if (!(lane & 1u) && valid && xn2) xn2[r0 + rr] = tie_xpart(nf * 1.0000003f, S, win);
         }
         __syncwarp();
-        const bool valid = lane < rows;
-        const float* xr = my + lane * ld;
-        double nrm = 0.0;
-        if (valid)
-            for (uint32_t k = 0; k < D; ++k) {
-                const double t = (double)xr[k];
-                nrm += t * t;
-            }
-        const float nf = (float)nrm;
-        __half nh = zero, nl = zero;
-        if (valid) {
-            const double ns = (double)nf * (double)s * (double)s;
-            nh = __double2half(ns);
-            nl = __double2half(ns - (double)__half2float(nh));
-            if (xn2) xn2[r0 + lane] = tie_xpart(nf * 1.0000003f, S, win);
+        const uint32_t lr = lane & 15u, kc0 = (lane >> 4) * (ncores / 2);
+        uint8_t* out = tiles + (c / kChunksPerTile) * (uint64_t)geo.tile_bytes +
+                       (size_t)((c % kChunksPerTile) * kSplitWarpRows + lr) * 16;
+        const __half* src = img + lr * hs;
+        const bool valid = lr < rows;
+        for (uint32_t q = 0; q < ncores / 2; ++q) {
+            const uint32_t kc = kc0 + q;
+            uint4 val = valid ? *reinterpret_cast<const uint4*>(src + kc * 8) : make_uint4(0, 0, 0, 0);
+            *reinterpret_cast<uint4*>(out + (size_t)kc * kTcTileM * 16) = val;
         }
-        uint8_t* out = tiles + (c >> 2) * (uint64_t)geo.tile_bytes +
-                       (size_t)((c & 3) * kSplitWarpRows + lane) * 16;
-        for (uint32_t kc = 0; kc < geo.kpad / 8; ++kc) {
-            uint32_t pk[4] = {0u, 0u, 0u, 0u};
-#pragma unroll
-            for (int q = 0; q < 8; ++q) {
-                const uint32_t k = kc * 8 + q;
-                __half val = zero;
-                if (k < 3 * D) {
-                    const uint32_t seg = k < D ? 0u : (k < 2 * D ? 1u : 2u);
-                    const float xv = xr[k - seg * D] * s;
-                    const __half xh = __float2half_rn(xv);
-                    val = seg == 1 ? __float2half_rn(xv - __half2float(xh)) : xh;
-                } else if (k == 3 * D) {
-                    val = nh;
-                } else if (k == 3 * D + 1) {
-                    val = nl;
-                } else if (k < 3 * D + 5) {
-                    val = one;
-                }
-                pk[q >> 1] |= (uint32_t)__half_as_ushort(valid ? val : zero) << (16 * (q & 1));
-            }
-            *reinterpret_cast<uint4*>(out + (size_t)kc * kTcTileM * 16) =
-                make_uint4(pk[0], pk[1], pk[2], pk[3]);
-        }
-        __syncwarp();  // slice reused by the next chunk
+        __syncwarp();  // image reused by the next chunk
     }
 }
 
@@ -493,17 +511,18 @@ void launch_split_rows(int kind, const float* x, const uint32_t* sel, const uint
         TSOM_LAUNCH(k_split_rows<kTcF16><<<(unsigned)tiles_n, kSplitThreads, smem, st>>>(
             x, sel, idx, dev_n, n, D, scale, win, t, xn2));
     else {
-        const size_t wsmem = (size_t)(kSplitThreads / 32) * kSplitWarpRows * ((D + 1) | 1u) *
-                             sizeof(float);
+        const size_t wsmem = (size_t)(kSplitThreads / 32) * kSplitWarpRows *
+                             (tc_geom(kTcF16, D).kpad + 8) * sizeof(__half);
         static bool attr_set = false;
         if (!attr_set) {
             cudaFuncSetAttribute(k_split_rows_f16, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                                 (int)(kSplitWarpRows * 8 * 64 * sizeof(float)));
+                                 (int)((kSplitThreads / 32) * kSplitWarpRows *
+                                       (kTcF16MaxK + 8) * sizeof(__half)));
             cudaFuncSetAttribute(k_split_rows_f16,
                                  cudaFuncAttributePreferredSharedMemoryCarveout, 100);
             attr_set = true;
         }
-        uint64_t blocks = ((n + kTcTileM - 1) / kTcTileM + 1) / 2;  // 4 warps per tile
+        uint64_t blocks = (n + kTcTileM - 1) / kTcTileM;  // 8 warps x 16 rows per tile
         if (blocks > 148ull * 8) blocks = 148ull * 8;
         TSOM_LAUNCH(k_split_rows_f16<<<(unsigned)blocks, kSplitThreads, wsmem, st>>>(
             x, sel, idx, dev_n, n, D, scale, win, t, xn2));
