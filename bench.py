@@ -295,6 +295,8 @@ def run_gpu_arm(args):
     # training loop with the CudaExecutor plugin (libtsom_dropin.so).
     e2e = None
     if not args.no_e2e:
+        topo_d = lattice_dist("hex", *P_GRID)  # host input, like the rows
+
         def cabi_run(epochs):
             if world > 1:
                 dist.barrier()
@@ -302,10 +304,12 @@ def run_gpu_arm(args):
             e = tsom.Engine(P, D, device=local)
             if args.kernel:
                 e.set_option(_lib.TSOM_OPT_BMU_KERNEL, args.kernel)
+            ta = time.perf_counter()
             e.bind(host)
+            tb = time.perf_counter()
             attach_comm(e)
             e.set_codebook(w0)
-            e.set_topology_distance(lattice_dist("hex", *P_GRID))
+            e.set_topology_distance(topo_d)
             t1 = time.perf_counter()
             for t in range(epochs):
                 eta = schedule_value(0.5, "linear", t, epochs, 1e-4)
@@ -315,7 +319,8 @@ def run_gpu_arm(args):
             t2 = time.perf_counter()
             e.close()
             t3 = time.perf_counter()
-            return t3 - t0, {"setup_s": t1 - t0, "epochs_s": t2 - t1, "close_s": t3 - t2}
+            return t3 - t0, {"setup_s": t1 - t0, "epochs_s": t2 - t1, "close_s": t3 - t2,
+                             "create_s": ta - t0, "bind_s": tb - ta, "config_s": t1 - tb}
         cabi_run(1)  # warm-up (allocations, module load)
         runs = []
         for _ in range(3):

@@ -12,6 +12,7 @@
 #include <nccl.h>
 
 #include <condition_variable>
+#include <chrono>
 #include <mutex>
 
 #include <algorithm>
@@ -664,32 +665,39 @@ int tsom_create(int device, uint32_t nodes, uint32_t dims, tsom_engine** out) {
         CU(cudaGetDeviceCount(&ndev));
         REQUIRE(device >= 0 && device < ndev, TSOM_ERR_CUDA, "cuda: no such device");
         CU(cudaSetDevice(device));
-        cudaDeviceProp prop;
-        CU(cudaGetDeviceProperties(&prop, device));
-        REQUIRE(prop.major >= 10, TSOM_ERR_CUDA,
-                std::string("cuda: device ") + prop.name + " is not sm_100 (B200) class");
-        eng->sm_count = prop.multiProcessorCount;
-        eng->smem_optin = prop.sharedMemPerBlockOptin;
+        // single attributes (cudaGetDeviceProperties costs milliseconds per call)
+        int major = 0, sms = 0, smem = 0;
+        CU(cudaDeviceGetAttribute(&major, cudaDevAttrComputeCapabilityMajor, device));
+        CU(cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, device));
+        CU(cudaDeviceGetAttribute(&smem, cudaDevAttrMaxSharedMemoryPerBlockOptin, device));
+        if (major < 10) {
+            cudaDeviceProp prop;
+            CU(cudaGetDeviceProperties(&prop, device));
+            REQUIRE(false, TSOM_ERR_CUDA,
+                    std::string("cuda: device ") + prop.name + " is not sm_100 (B200) class");
+        }
+        eng->sm_count = sms;
+        eng->smem_optin = (size_t)smem;
         CU(cudaStreamCreateWithFlags(&eng->stream, cudaStreamNonBlocking));
         CU(cudaStreamCreateWithFlags(&eng->copy_stream, cudaStreamNonBlocking));
         for (auto& ev : eng->ev) CU(cudaEventCreate(&ev));
         const size_t P = nodes, D = dims;
         CU(eng->w.ensure(P * D * sizeof(float)));
         CU(eng->prev.ensure(P * D * sizeof(float)));
-        CU(cudaMemset(eng->prev.p, 0, P * D * sizeof(float)));
+        CU(cudaMemsetAsync(eng->prev.p, 0, P * D * sizeof(float), eng->stream));
         CU(eng->wt.ensure((size_t)(D + 1) * ppad(eng) * sizeof(float)));
         CU(eng->w2.ensure(P * sizeof(double)));
         CU(eng->w2max.ensure(sizeof(float)));
         CU(eng->x2max.ensure(2 * sizeof(float)));
-        CU(cudaMemset(eng->x2max.p, 0, 2 * sizeof(float)));
+        CU(cudaMemsetAsync(eng->x2max.p, 0, 2 * sizeof(float), eng->stream));
         CU(eng->scale.ensure(4 * sizeof(float)));
-        CU(cudaMemset(eng->scale.p, 0, 4 * sizeof(float)));
+        CU(cudaMemsetAsync(eng->scale.p, 0, 4 * sizeof(float), eng->stream));
         CU(eng->infl.ensure(P * P * sizeof(double)));
         CU(eng->U.ensure(P * D * sizeof(double)));
         CU(eng->H.ensure(P * sizeof(double)));
         CU(eng->status.ensure(4 * sizeof(int)));
         ensure_rows(eng, 1);
-        CU(cudaStreamSynchronize(0));  // the legacy-stream memsets above have landed
+        CU(cudaStreamSynchronize(eng->stream));
     });
     if (rc != TSOM_OK) {
         std::fprintf(stderr, "tsom_create: %s\n", eng->last_error.c_str());
@@ -812,7 +820,10 @@ int tsom_bind_host_data(tsom_engine* eng, const float* rows, uint64_t n_rows, ui
         eng->streamed = false;
         eng->host_rows = nullptr;
         const size_t bytes = n_rows * eng->D * sizeof(float);
+        const char* tr = getenv("TSOM_TRACE_BIND");
+        const auto tb0 = std::chrono::steady_clock::now();
         CU(eng->x.ensure(bytes + tsom::kRowSlack));
+        const auto tb1 = std::chrono::steady_clock::now();
         eng->x_slack = true;
         cudaPointerAttributes pa{};
         const bool pinned = n_rows && cudaPointerGetAttributes(&pa, rows) == cudaSuccess &&
@@ -832,6 +843,14 @@ int tsom_bind_host_data(tsom_engine* eng, const float* rows, uint64_t n_rows, ui
             const uint64_t rowb = (uint64_t)eng->D * sizeof(float);
             upload_rows(eng, n_rows, std::max<uint64_t>(1, ((uint64_t)32 << 20) / rowb));
             eng->host_rows = nullptr;
+        }
+        if (tr && tr[0] == '1') {
+            CU(cudaStreamSynchronize(eng->stream));
+            const auto tb2 = std::chrono::steady_clock::now();
+            fprintf(stderr, "[tsom bind] %s rows=%llu alloc %.2f ms copy %.2f ms\n",
+                    pinned ? "pinned" : "pageable", (unsigned long long)n_rows,
+                    std::chrono::duration<double, std::milli>(tb1 - tb0).count(),
+                    std::chrono::duration<double, std::milli>(tb2 - tb1).count());
         }
         tsom::launch_row_norm_max(eng->x.as<float>(), n_rows, eng->D, eng->x2max.as<float>(),
                                   eng->stream);
