@@ -201,6 +201,33 @@ def test_epoch_accumulators_vs_oracle(pkg, oracle_port, kernel, sampling):
     np.testing.assert_allclose(dist, do, rtol=1e-12)
 
 
+@pytest.mark.parametrize("d", [50, 13])
+@pytest.mark.parametrize("sampling", ["full", "random"])
+def test_epoch_accumulators_multi_chunk(pkg, oracle_port, d, sampling):
+    # K2 sorts rows by (chunk of 131072 rows, BMU): several chunks and a
+    # ragged last one, async (even d) and generic (odd d) gathers
+    n, p = 400_000 + 77, 256
+    x = oracle_port.synth_gmm(n, d, 2612)
+    w = x[np.linspace(0, n - 1, p).astype(int)].copy()
+    infl = oracle_port.influence_from_dist(oracle_port.lattice_dist("hex", 16, 16), 4.0)
+    if sampling == "full":
+        sel = np.arange(n, dtype=np.uint32)
+    else:
+        sel = np.sort(np.random.default_rng(2).choice(n, 300_001, replace=False)).astype(np.uint32)
+    e = engine(pkg, p, d, 0)
+    e.bind(x)
+    e.set_codebook(w)
+    e.set_influence(infl)
+    u, h, dist = e.epoch(0.45, sel, want_dist=True)
+    uo, ho, _, _, do = oracle_port.run_iteration(x, sel, w, infl, 0.45, 1, 8)
+    assert np.max(np.abs(u - uo)) <= 1e-9 * np.max(np.abs(uo))
+    np.testing.assert_allclose(h, ho, rtol=1e-9)
+    np.testing.assert_allclose(dist, do, rtol=1e-12)
+    qs, qc = e.qe(sel)
+    assert qc == len(sel)
+    assert qs == pytest.approx(float(np.sum(do)), rel=1e-12)
+
+
 def test_streamed_equals_resident(pkg, oracle_port):
     n, p = 50000, 128
     x = oracle_port.synth_gmm(n, 50, 2612)
