@@ -87,10 +87,29 @@ void release_cached_memory() {
     }
 }
 
+static bool pool_disabled() {  // TSOM_NO_POOL=1: plain cudaMalloc/cudaFree (diagnostics)
+    static const bool off = [] {
+        const char* v = getenv("TSOM_NO_POOL");
+        return v && v[0] == '1';
+    }();
+    return off;
+}
+
 cudaError_t DevBuf::ensure(size_t need) {
     if (need <= bytes && p) return cudaSuccess;
     release();
     if (need == 0) return cudaSuccess;
+    if (pool_disabled()) {
+        cudaError_t e = cudaMalloc(&p, need);
+        if (e != cudaSuccess) {
+            p = nullptr;
+            bytes = 0;
+            return e;
+        }
+        bytes = need;
+        owned = true;
+        return cudaSuccess;
+    }
     DevicePool* dp = nullptr;
     cudaError_t e = device_pool(&dp);
     if (e == cudaSuccess) {
@@ -124,8 +143,12 @@ cudaError_t DevBuf::ensure(size_t need) {
 void DevBuf::release(bool synced) {
     if (p && owned) {
         DevicePool* dp = nullptr;
-        if (!synced) cudaDeviceSynchronize();
-        if (device_pool(&dp) == cudaSuccess) cudaFreeAsync(p, dp->st);
+        if (pool_disabled()) {
+            cudaFree(p);
+        } else {
+            if (!synced) cudaDeviceSynchronize();
+            if (device_pool(&dp) == cudaSuccess) cudaFreeAsync(p, dp->st);
+        }
     }
     p = nullptr;
     bytes = 0;
