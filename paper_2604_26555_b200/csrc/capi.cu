@@ -792,6 +792,9 @@ int tsom_set_option(tsom_engine* eng, int key, int64_t value) {
             case 98:  // diagnostics: element-wise 3xFP16 split (k_split_rows<kTcF16>)
                 tsom::g_split_v1 = (int)value;
                 break;
+            case 97:  // diagnostics: 1 = cp.async K2 gather instead of the TMA gather
+                tsom::g_gather_kind = (int)value;
+                break;
             case TSOM_OPT_HOST_REGISTER:
                 eng->host_register = value != 0;
                 break;

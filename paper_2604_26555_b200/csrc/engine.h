@@ -333,6 +333,7 @@ cudaError_t launch_bmu_tc(int kind, const void* tiles, uint64_t n, const uint32_
                           cudaStream_t st);
 extern uint32_t g_k1_debug;
 extern int g_split_v1;
+extern int g_gather_kind;
 int k1_trace_copy(unsigned long long* out, uint32_t n);  // diagnostics  // diagnostics: bit0 skip epilogue math, bit1 skip MMAs
 // main-pass merge: bmu for rows with a clear winner, near-tie positions -> ties
 constexpr uint32_t kTcEpiSets = 2;  // K1 main pass: partial results per group (sub-groups)

@@ -24,6 +24,7 @@
 #include <cstdint>
 
 #include "engine.h"
+#include "tc_ptx.cuh"
 
 namespace tsom {
 
@@ -385,6 +386,139 @@ __global__ void __launch_bounds__(kAsyncWarps * 32, 2) k_gather_async(
     }
 }
 
+// TMA gather: lane l of a warp moves row l of a 32-row batch with one 1-D bulk
+// copy (`cp.async.bulk`, the 16-byte-aligned window around the 8-byte-aligned
+// row, into a 16-byte-aligned slot) completing on the batch's mbarrier; two
+// batches in flight per warp.  One instruction moves 32 rows (the cp.async
+// variant needs one per row plus the address shuffles), so the accumulation —
+// four independent FP64 chains per lane — is what the warp spends its issue
+// slots on.  Needs d even and readable slack after the last row (the window
+// may extend up to 8 bytes past it).
+constexpr int kTmaWarps = 8;
+
+__global__ void __launch_bounds__(kTmaWarps * 32, 2) k_gather_tma(
+    const float* __restrict__ x, const uint32_t* __restrict__ sel, const float* __restrict__ w,
+    uint32_t P, uint32_t D, uint32_t slot, const uint32_t* __restrict__ sorted,
+    const uint32_t* __restrict__ node_start, const uint32_t* __restrict__ piece_start,
+    const uint32_t* __restrict__ piece_node, double* __restrict__ partial,
+    double* __restrict__ dist_out, int want_dist, int accumulate) {
+    extern __shared__ __align__(128) uint8_t tsm[];
+    __shared__ __align__(8) uint64_t bars[kTmaWarps][2];
+    const uint32_t lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+    uint8_t* buf = tsm + (size_t)warp * 2 * 32 * slot;
+    if (lane == 0) {
+        ptx::mbar_init(&bars[warp][0], 1);
+        ptx::mbar_init(&bars[warp][1], 1);
+        asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
+    }
+    __syncwarp();
+    uint32_t phase = 0;  // bit s = parity to wait for on buffer s
+    const uint32_t npieces = piece_start[P];
+    const uint32_t Dp = D + 1;
+    const uint32_t ka = 2 * lane, kb = 2 * lane + 1;
+    const bool oka = ka < D, okb = kb < D;
+    const uint32_t rowb = D * 4;
+
+    // copy window of this lane's row; returns the bytes it will deliver
+    auto issue = [&](uint64_t row, uint32_t nrows, int s, uint32_t& offmask) {
+        const uint64_t a = reinterpret_cast<uint64_t>(x) + row * rowb;
+        const uint64_t a0 = a & ~15ull;
+        const uint32_t len = (uint32_t)(((a + rowb + 15) & ~15ull) - a0);
+        const bool mine = lane < nrows;
+        offmask = __ballot_sync(0xffffffffu, mine && (a & 15));
+        const uint32_t total = __reduce_add_sync(0xffffffffu, mine ? len : 0u);
+        asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
+        if (lane == 0) ptx::mbar_expect_tx(&bars[warp][s], total);
+        __syncwarp();
+        if (mine)
+            ptx::bulk_g2s(buf + ((size_t)s * 32 + lane) * slot, reinterpret_cast<const void*>(a0),
+                          len, &bars[warp][s]);
+    };
+
+    for (uint32_t p = blockIdx.x * kTmaWarps + warp; p < npieces; p += gridDim.x * kTmaWarps) {
+        const uint32_t b = piece_node[p];
+        const uint32_t r0 = node_start[b] + (p - piece_start[b]) * kPieceRows;
+        const uint32_t r1 = min(r0 + kPieceRows, node_start[b + 1]);
+        const uint32_t nb = (r1 - r0 + 31) / 32;  // batches of 32 rows (<= 8)
+        uint32_t pos[8];
+#pragma unroll
+        for (int m = 0; m < 8; ++m) {
+            const uint32_t r = r0 + 32 * m + lane;
+            pos[m] = r < r1 ? sorted[r] : 0u;
+        }
+        uint64_t rowid[8];
+#pragma unroll
+        for (int m = 0; m < 8; ++m) rowid[m] = sel ? (uint64_t)sel[pos[m]] : (uint64_t)pos[m];
+        double w0 = 0.0, w1 = 0.0;
+        if (want_dist) {
+            const float* wb = w + (size_t)b * D;
+            w0 = oka ? (double)wb[ka] : 0.0;
+            w1 = okb ? (double)wb[kb] : 0.0;
+        }
+        double a0 = 0.0, a1 = 0.0, c0 = 0.0, c1 = 0.0, ds = 0.0;
+        uint32_t offm[2];
+        issue(rowid[0], min(32u, r1 - r0), 0, offm[0]);
+#pragma unroll
+        for (int m = 0; m < 8; ++m) {
+            if (m < (int)nb) {
+                const uint32_t rows_m = min(32u, r1 - (r0 + 32 * m));
+                const int s = m & 1;
+                if (m + 1 < (int)nb)
+                    issue(rowid[m + 1], min(32u, r1 - (r0 + 32 * (m + 1))), s ^ 1, offm[s ^ 1]);
+                ptx::mbar_wait(&bars[warp][s], (phase >> s) & 1u);
+                phase ^= 1u << s;
+                const uint8_t* bm = buf + (size_t)s * 32 * slot + 8 * lane;
+                const uint32_t om = offm[s];
+                if (!want_dist) {
+                    uint32_t j = 0;
+                    for (; j + 2 <= rows_m; j += 2) {
+                        float2 u = make_float2(0.0f, 0.0f), v = u;
+                        if (okb) {
+                            u = *reinterpret_cast<const float2*>(bm + j * slot + ((om >> j) & 1u) * 8);
+                            v = *reinterpret_cast<const float2*>(bm + (j + 1) * slot +
+                                                                 ((om >> (j + 1)) & 1u) * 8);
+                        }
+                        a0 += (double)u.x;
+                        a1 += (double)u.y;
+                        c0 += (double)v.x;
+                        c1 += (double)v.y;
+                    }
+                    if (j < rows_m && okb) {
+                        const float2 u =
+                            *reinterpret_cast<const float2*>(bm + j * slot + ((om >> j) & 1u) * 8);
+                        a0 += (double)u.x;
+                        a1 += (double)u.y;
+                    }
+                } else {
+                    for (uint32_t j = 0; j < rows_m; ++j) {
+                        float2 v = make_float2(0.0f, 0.0f);
+                        if (okb)
+                            v = *reinterpret_cast<const float2*>(bm + j * slot + ((om >> j) & 1u) * 8);
+                        a0 += (double)v.x;
+                        a1 += (double)v.y;
+                        const double d0 = oka ? (double)v.x - w0 : 0.0;
+                        const double d1 = okb ? (double)v.y - w1 : 0.0;
+                        double d2 = fma(d0, d0, d1 * d1);
+#pragma unroll
+                        for (int o = 16; o; o >>= 1) d2 += __shfl_xor_sync(0xffffffffu, d2, o);
+                        const double dist = sqrt(d2 > 0.0 ? d2 : 0.0);
+                        const uint32_t pp = __shfl_sync(0xffffffffu, pos[m], j);
+                        if (dist_out && lane == 0) dist_out[pp] = dist;
+                        ds += dist;
+                    }
+                }
+                __syncwarp();  // buffer s is refilled by the issue of batch m + 2
+            }
+        }
+        double* out = partial + (size_t)p * Dp;
+        if (accumulate) {
+            if (oka) out[ka] = a0 + c0;
+            if (okb) out[kb] = a1 + c1;
+        }
+        if (lane == 0) out[D] = ds;
+    }
+}
+
 // sums[b][k] (+)= sum over the pieces of node b: one warp per (b, k), lanes
 // stride the node's pieces, fixed xor tree (deterministic, skew-proof)
 __global__ void k_piece_reduce(const double* __restrict__ partial,
@@ -438,6 +572,8 @@ __global__ void k_add_rowcount(double* __restrict__ sums, uint32_t P, uint32_t D
 
 // ---------------------------------------------------------------------------
 
+int g_gather_kind = 0;  // diagnostics (TSOM option 97): 1 = cp.async gather
+
 void launch_accumulate(const float* x, const uint32_t* sel, uint64_t n, uint32_t D,
                        const float* w, uint32_t P, const uint32_t* bmu, double* dist_out,
                        bool want_dist_sum, bool accumulate, bool first, const AccumScratch& s,
@@ -473,7 +609,22 @@ void launch_accumulate(const float* x, const uint32_t* sel, uint64_t n, uint32_t
     const unsigned gblocks = (unsigned)((warps * 32 + 255) / 256);
     const bool v2 = (D % 2 == 0) && D <= 64 && ((reinterpret_cast<uintptr_t>(x) & 7u) == 0);
     const size_t asmem = (size_t)kAsyncWarps * 2 * 32 * D * sizeof(float);
-    if (v2 && D <= 64 && asmem <= 110 * 1024) {
+    const uint32_t slot = (D * 4 + 8 + 15) / 16 * 16;  // longest 16-B window of a row
+    const size_t tsmem = (size_t)kTmaWarps * 2 * 32 * slot;
+    if (v2 && x_slack && g_gather_kind == 0 && ((reinterpret_cast<uintptr_t>(x) & 15u) == 0) &&
+        tsmem <= 110 * 1024) {
+        static size_t tattr = 0;
+        if (tattr < tsmem) {
+            cudaFuncSetAttribute(k_gather_tma, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                 (int)tsmem);
+            tattr = tsmem;
+        }
+        const uint64_t tblocks = (pieces + kTmaWarps - 1) / kTmaWarps;
+        const unsigned tb = (unsigned)(tblocks < (uint64_t)sm_count * 2 ? tblocks : sm_count * 2);
+        TSOM_LAUNCH(k_gather_tma<<<tb, kTmaWarps * 32, tsmem, st>>>(
+            x, sel, w, P, D, slot, s.sorted, s.node_start, s.piece_start, s.piece_node, s.partial,
+            dist_out, want_dist ? 1 : 0, accumulate ? 1 : 0));
+    } else if (v2 && D <= 64 && asmem <= 110 * 1024) {
         static size_t aattr = 0;
         if (aattr < asmem) {
             cudaFuncSetAttribute(k_gather_async, cudaFuncAttributeMaxDynamicSharedMemorySize,

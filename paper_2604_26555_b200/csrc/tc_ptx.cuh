@@ -1,6 +1,7 @@
 // tc_ptx.cuh — thin inline-PTX wrappers for the sm_100a features K1 uses:
 // mbarriers, 1-D bulk copies (cp.async.bulk), UMMA descriptors, tcgen05.mma /
-// commit / ld and the tcgen05 fences.  Only included by k1_bmu_tc.cu.
+// commit / ld and the tcgen05 fences (K1; the K2 gather uses the mbarrier and
+// bulk-copy wrappers).
 #pragma once
 
 #include <cstdint>
