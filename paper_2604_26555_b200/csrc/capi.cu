@@ -4,6 +4,7 @@
 // caller's point of view (it returns after its results are in the caller's
 // buffers), all device work is issued on the engine stream.  There is no CPU
 // fallback: if a kernel cannot run, the call fails with TSOM_ERR_CUDA.
+#include <cuda.h>
 #include <cuda_runtime.h>
 #include <dlfcn.h>
 #include <fcntl.h>
@@ -949,6 +950,30 @@ int tsom_bind_shards(tsom_engine* eng, const char* const* paths, uint32_t n_path
     });
 }
 
+// Whether kRowSlack bytes after [p, p + bytes) lie inside the same device
+// allocation (cuMemGetAddressRange through the runtime's driver entry point):
+// the row-window kernels may then read a few bytes past the last row of a
+// caller-owned buffer.
+static bool device_slack_after(const void* p, size_t bytes) {
+    using GetRange = CUresult (*)(CUdeviceptr*, size_t*, CUdeviceptr);
+    static GetRange fn = [] {
+        void* f = nullptr;
+        cudaDriverEntryPointQueryResult q{};
+        if (cudaGetDriverEntryPoint("cuMemGetAddressRange", &f, cudaEnableDefault, &q) !=
+                cudaSuccess ||
+            q != cudaDriverEntryPointSuccess) {
+            cudaGetLastError();
+            return (GetRange) nullptr;
+        }
+        return reinterpret_cast<GetRange>(f);
+    }();
+    if (!fn || !p) return false;
+    CUdeviceptr base = 0;
+    size_t size = 0;
+    if (fn(&base, &size, reinterpret_cast<CUdeviceptr>(p)) != CUDA_SUCCESS) return false;
+    return reinterpret_cast<uintptr_t>(p) + bytes + tsom::kRowSlack <= (uintptr_t)base + size;
+}
+
 int tsom_bind_device_data(tsom_engine* eng, const float* d_rows, uint64_t n_rows) {
     return guarded(eng, [&] {
         CU(cudaSetDevice(eng->device));
@@ -957,7 +982,7 @@ int tsom_bind_device_data(tsom_engine* eng, const float* d_rows, uint64_t n_rows
         eng->x.p = const_cast<float*>(d_rows);
         eng->x.bytes = n_rows * eng->D * sizeof(float);
         eng->x.owned = false;
-        eng->x_slack = false;
+        eng->x_slack = device_slack_after(d_rows, (size_t)n_rows * eng->D * sizeof(float));
         eng->n_rows = n_rows;
         eng->streamed = false;
         eng->xsplit_valid = false;

@@ -404,6 +404,7 @@ __global__ void __launch_bounds__(kTmaWarps * 32, 2) k_gather_tma(
     double* __restrict__ dist_out, int want_dist, int accumulate) {
     extern __shared__ __align__(128) uint8_t tsm[];
     __shared__ __align__(8) uint64_t bars[kTmaWarps][2];
+    __shared__ double wsm[kTmaWarps][64];  // w_b in FP64 for the distance pass (d <= 64)
     const uint32_t lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
     uint8_t* buf = tsm + (size_t)warp * 2 * 32 * slot;
     if (lane == 0) {
@@ -449,11 +450,11 @@ __global__ void __launch_bounds__(kTmaWarps * 32, 2) k_gather_tma(
         uint64_t rowid[8];
 #pragma unroll
         for (int m = 0; m < 8; ++m) rowid[m] = sel ? (uint64_t)sel[pos[m]] : (uint64_t)pos[m];
-        double w0 = 0.0, w1 = 0.0;
         if (want_dist) {
             const float* wb = w + (size_t)b * D;
-            w0 = oka ? (double)wb[ka] : 0.0;
-            w1 = okb ? (double)wb[kb] : 0.0;
+            __syncwarp();  // previous piece's distance pass done with wsm
+            for (uint32_t k = lane; k < D; k += 32) wsm[warp][k] = (double)wb[k];
+            __syncwarp();
         }
         double a0 = 0.0, a1 = 0.0, c0 = 0.0, c1 = 0.0, ds = 0.0;
         uint32_t offm[2];
@@ -467,45 +468,40 @@ __global__ void __launch_bounds__(kTmaWarps * 32, 2) k_gather_tma(
                     issue(rowid[m + 1], min(32u, r1 - (r0 + 32 * (m + 1))), s ^ 1, offm[s ^ 1]);
                 ptx::mbar_wait(&bars[warp][s], (phase >> s) & 1u);
                 phase ^= 1u << s;
-                const uint8_t* bm = buf + (size_t)s * 32 * slot + 8 * lane;
+                const uint8_t* bs = buf + (size_t)s * 32 * slot;
+                const uint8_t* bm = bs + 8 * lane;
                 const uint32_t om = offm[s];
-                if (!want_dist) {
-                    uint32_t j = 0;
-                    for (; j + 2 <= rows_m; j += 2) {
-                        float2 u = make_float2(0.0f, 0.0f), v = u;
-                        if (okb) {
-                            u = *reinterpret_cast<const float2*>(bm + j * slot + ((om >> j) & 1u) * 8);
-                            v = *reinterpret_cast<const float2*>(bm + (j + 1) * slot +
-                                                                 ((om >> (j + 1)) & 1u) * 8);
-                        }
-                        a0 += (double)u.x;
-                        a1 += (double)u.y;
-                        c0 += (double)v.x;
-                        c1 += (double)v.y;
+                uint32_t j = 0;
+                for (; j + 2 <= rows_m; j += 2) {
+                    float2 u = make_float2(0.0f, 0.0f), v = u;
+                    if (okb) {
+                        u = *reinterpret_cast<const float2*>(bm + j * slot + ((om >> j) & 1u) * 8);
+                        v = *reinterpret_cast<const float2*>(bm + (j + 1) * slot +
+                                                             ((om >> (j + 1)) & 1u) * 8);
                     }
-                    if (j < rows_m && okb) {
-                        const float2 u =
-                            *reinterpret_cast<const float2*>(bm + j * slot + ((om >> j) & 1u) * 8);
-                        a0 += (double)u.x;
-                        a1 += (double)u.y;
+                    a0 += (double)u.x;
+                    a1 += (double)u.y;
+                    c0 += (double)v.x;
+                    c1 += (double)v.y;
+                }
+                if (j < rows_m && okb) {
+                    const float2 u =
+                        *reinterpret_cast<const float2*>(bm + j * slot + ((om >> j) & 1u) * 8);
+                    a0 += (double)u.x;
+                    a1 += (double)u.y;
+                }
+                if (want_dist && lane < rows_m) {
+                    // lane = row: exact FP64 distance to w_b, features in order
+                    const float* xr =
+                        reinterpret_cast<const float*>(bs + lane * slot + ((om >> lane) & 1u) * 8);
+                    double d2 = 0.0;
+                    for (uint32_t k = 0; k < D; ++k) {
+                        const double dd = (double)xr[k] - wsm[warp][k];
+                        d2 = fma(dd, dd, d2);
                     }
-                } else {
-                    for (uint32_t j = 0; j < rows_m; ++j) {
-                        float2 v = make_float2(0.0f, 0.0f);
-                        if (okb)
-                            v = *reinterpret_cast<const float2*>(bm + j * slot + ((om >> j) & 1u) * 8);
-                        a0 += (double)v.x;
-                        a1 += (double)v.y;
-                        const double d0 = oka ? (double)v.x - w0 : 0.0;
-                        const double d1 = okb ? (double)v.y - w1 : 0.0;
-                        double d2 = fma(d0, d0, d1 * d1);
-#pragma unroll
-                        for (int o = 16; o; o >>= 1) d2 += __shfl_xor_sync(0xffffffffu, d2, o);
-                        const double dist = sqrt(d2 > 0.0 ? d2 : 0.0);
-                        const uint32_t pp = __shfl_sync(0xffffffffu, pos[m], j);
-                        if (dist_out && lane == 0) dist_out[pp] = dist;
-                        ds += dist;
-                    }
+                    const double dist = sqrt(d2);
+                    if (dist_out) dist_out[pos[m]] = dist;
+                    ds += dist;
                 }
                 __syncwarp();  // buffer s is refilled by the issue of batch m + 2
             }
@@ -514,6 +510,10 @@ __global__ void __launch_bounds__(kTmaWarps * 32, 2) k_gather_tma(
         if (accumulate) {
             if (oka) out[ka] = a0 + c0;
             if (okb) out[kb] = a1 + c1;
+        }
+        if (want_dist) {
+#pragma unroll
+            for (int o = 16; o; o >>= 1) ds += __shfl_xor_sync(0xffffffffu, ds, o);
         }
         if (lane == 0) out[D] = ds;
     }

@@ -478,3 +478,43 @@ def test_bind_reuses_pool_blocks_exactly(pkg, oracle_port):
     e.close()
     ob, _ = oracle_port.find_bmus(x, w)
     assert np.array_equal(b, ob)
+
+
+@pytest.mark.parametrize("owner", ["cudaMalloc", "torch"])
+def test_bind_device_rows_exact(pkg, oracle_port, owner):
+    # caller-owned device rows (tsom_bind_device_data): the K2 row windows may
+    # read past the last row only when the allocation has room for it
+    # (cuMemGetAddressRange); an exact-size cudaMalloc block and a torch
+    # tensor, both against the oracle
+    import torch
+    n, p, d = 70_001, 256, 50
+    x = oracle_port.synth_gmm(n, d, 2613)
+    w = x[np.linspace(0, n - 1, p).astype(int)].copy()
+    infl = oracle_port.influence_from_dist(oracle_port.lattice_dist("hex", 16, 16), 4.0)
+    torch.cuda.init()
+    free = None
+    if owner == "torch":
+        keep = torch.from_numpy(x).cuda()
+        ptr = keep.data_ptr()
+    else:
+        from cuda.bindings import runtime as rt
+        err, ptr = rt.cudaMalloc(x.nbytes)
+        assert err == rt.cudaError_t.cudaSuccess
+        (err,) = rt.cudaMemcpy(ptr, x.ctypes.data, x.nbytes, rt.cudaMemcpyKind.cudaMemcpyHostToDevice)
+        assert err == rt.cudaError_t.cudaSuccess
+        free = (rt, ptr)
+    try:
+        e = engine(pkg, p, d, 0)
+        e.bind_device(ptr, n)
+        e.set_codebook(w)
+        e.set_influence(infl)
+        u, h, dist = e.epoch(0.45, None, want_dist=True)
+        e.close()
+    finally:
+        if free:
+            free[0].cudaFree(free[1])
+    sel = np.arange(n, dtype=np.uint32)
+    uo, ho, _, _, do = oracle_port.run_iteration(x, sel, w, infl, 0.45, 1, 8)
+    assert np.max(np.abs(u - uo)) <= 1e-9 * np.max(np.abs(uo))
+    np.testing.assert_allclose(h, ho, rtol=1e-9)
+    np.testing.assert_allclose(dist, do, rtol=1e-12)
