@@ -63,6 +63,47 @@ __device__ __forceinline__ void twist(const uint64_t* cur, uint64_t* nxt) {
     __syncthreads();
 }
 
+// window[k] = XOR over the set bits i of the jump polynomial (s_j, 312
+// words) of s_seq[i + k], k < 312.  The set-bit indices are first listed in
+// s_idx (a block-wide scan of the words' popcounts), so the XOR loop is one
+// broadcast index load and one sequence load per term.  All kT threads call.
+__device__ __forceinline__ uint64_t jump_apply(const uint64_t* s_seq, const uint64_t* s_j,
+                                               uint16_t* s_idx, uint32_t* s_wsum) {
+    const int k = threadIdx.x, lane = k & 31, wid = k >> 5;
+    const uint64_t bits0 = k < 312 ? s_j[k] : 0ull;
+    const uint32_t c = __popcll(bits0);
+    uint32_t incl = c;
+#pragma unroll
+    for (int o = 1; o < 32; o <<= 1) {
+        const uint32_t v = __shfl_up_sync(0xffffffffu, incl, o);
+        if (lane >= o) incl += v;
+    }
+    if (lane == 31) s_wsum[wid] = incl;
+    __syncthreads();
+    uint32_t base = 0, nt = 0;
+    for (int w = 0; w < kT / 32; ++w) {
+        const uint32_t v = s_wsum[w];
+        if (w < wid) base += v;
+        nt += v;
+    }
+    uint32_t pos = base + incl - c;
+    for (uint64_t bits = bits0; bits; bits &= bits - 1)
+        s_idx[pos++] = (uint16_t)(64 * k + __ffsll((long long)bits) - 1);
+    __syncthreads();
+    uint64_t a0 = 0, a1 = 0;
+    if (k < 312) {
+        uint32_t t = 0;
+        for (; t + 4 <= nt; t += 4) {
+            a0 ^= s_seq[s_idx[t] + k] ^ s_seq[s_idx[t + 1] + k];
+            a1 ^= s_seq[s_idx[t + 2] + k] ^ s_seq[s_idx[t + 3] + k];
+        }
+        for (; t < nt; ++t) a0 ^= s_seq[s_idx[t] + k];
+    }
+    return a0 ^ a1;
+}
+
+constexpr size_t kJumpIdxBytes = (19937 + 64) * sizeof(uint16_t);
+
 }  // namespace
 
 // seq[0..312) = window, seq[312 .. 312 + 312 * twists) = the next untempered words
@@ -94,6 +135,8 @@ __global__ void __launch_bounds__(kT) k_mt_generate(const uint64_t* __restrict__
     uint64_t* s_seq = sm;                 // [mt::kSeq]
     uint64_t* s_j = sm + mt::kSeq;        // [312]
     uint64_t* s_w = s_j + 312;            // [2][312]
+    uint16_t* s_idx = reinterpret_cast<uint16_t*>(s_w + 2 * 312);
+    __shared__ uint32_t s_wsum[kT / 32];
     const int k = threadIdx.x;
     const uint64_t g = blockIdx.x;
     const uint64_t q0 = g * L;
@@ -104,18 +147,8 @@ __global__ void __launch_bounds__(kT) k_mt_generate(const uint64_t* __restrict__
         for (int i = k; i < mt::kSeq; i += kT) s_seq[i] = seq[i];
         if (k < 312) s_j[k] = jp[(size_t)g * 312 + k];
         __syncthreads();
-        uint64_t acc = 0;
-        if (k < 312) {
-            for (int w = 0; w < 312; ++w) {
-                uint64_t bits = s_j[w];
-                while (bits) {
-                    const int b = __ffsll((long long)bits) - 1;
-                    bits &= bits - 1;
-                    acc ^= s_seq[64 * w + b + k];
-                }
-            }
-            s_w[k] = acc;
-        }
+        const uint64_t acc = jump_apply(s_seq, s_j, s_idx, s_wsum);
+        if (k < 312) s_w[k] = acc;
     }
     __syncthreads();
     const uint64_t q1 = min(q0 + L, total);
@@ -158,22 +191,14 @@ __global__ void __launch_bounds__(kT) k_mt_jump_window(const uint64_t* __restric
     extern __shared__ uint64_t sm2[];
     uint64_t* s_seq = sm2;
     uint64_t* s_j = sm2 + mt::kSeq;
+    uint16_t* s_idx = reinterpret_cast<uint16_t*>(s_j + 312);
+    __shared__ uint32_t s_wsum[kT / 32];
     const int k = threadIdx.x;
     for (int i = k; i < mt::kSeq; i += kT) s_seq[i] = seq[i];
     if (k < 312) s_j[k] = jp[k];
     __syncthreads();
-    if (k < 312) {
-        uint64_t acc = 0;
-        for (int w = 0; w < 312; ++w) {
-            uint64_t bits = s_j[w];
-            while (bits) {
-                const int b = __ffsll((long long)bits) - 1;
-                bits &= bits - 1;
-                acc ^= s_seq[64 * w + b + k];
-            }
-        }
-        window[k] = acc;
-    }
+    const uint64_t acc = jump_apply(s_seq, s_j, s_idx, s_wsum);
+    if (k < 312) window[k] = acc;
 }
 
 // ---------------------------------------------------------------------------
@@ -565,7 +590,9 @@ int sampler_setup(SamplerState& s, int kind, uint64_t n, uint64_t m, uint64_t se
     if (!s.draws_per_epoch) return 0;
     const uint64_t total = s.draws_per_epoch + kSlack;
     uint64_t G = (total + 65535) / 65536;
-    G = std::max<uint64_t>(1, std::min<uint64_t>(G, 2ull * (uint64_t)sm_count));
+    // one generator CTA per SM (its jump window needs ~210 KB of shared memory):
+    // a second wave would repeat the jump for half the SMs
+    G = std::max<uint64_t>(1, std::min<uint64_t>(G, (uint64_t)sm_count));
     const uint64_t L = (total + G - 1) / G;
     s.G = (uint32_t)G;
     s.L = L;
@@ -624,12 +651,12 @@ static void generate_draws(SamplerState& s, int b, cudaStream_t st) {
     const uint32_t twists = (mt::kSeq - 312 + 311) / 312;
     TSOM_LAUNCH(k_mt_extend<<<1, kT, 0, st>>>(s.window.as<uint64_t>(), twists,
                                               s.seqb[b].as<uint64_t>()));
-    const size_t smem = (mt::kSeq + 312 + 2 * 312) * 8;
+    const size_t smem = (mt::kSeq + 312 + 2 * 312) * 8 + kJumpIdxBytes;
     static bool attr = false;
     if (!attr) {
         cudaFuncSetAttribute(k_mt_generate, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
         cudaFuncSetAttribute(k_mt_jump_window, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                             (int)((mt::kSeq + 312) * 8));
+                             (int)((mt::kSeq + 312) * 8 + kJumpIdxBytes));
         attr = true;
     }
     const uint64_t total = s.draws_per_epoch + kSlack;
@@ -740,7 +767,7 @@ int sampler_select(SamplerState& s, uint32_t* out, uint64_t* m_out, int sm_count
     if (!ok) return 5;
     // the stream continues after the draws actually used
     if (s.kind == 2 && s.sharded)
-        TSOM_LAUNCH(k_mt_jump_window<<<1, kT, (mt::kSeq + 312) * 8, st>>>(
+        TSOM_LAUNCH(k_mt_jump_window<<<1, kT, (mt::kSeq + 312) * 8 + kJumpIdxBytes, st>>>(
             s.seqb[b].as<uint64_t>(), s.jN.as<uint64_t>(), s.window.as<uint64_t>()));
     else
         TSOM_LAUNCH(k_mt_advance<<<1, 320, 0, st>>>(s.seqb[b].as<uint64_t>(),
