@@ -171,7 +171,7 @@ struct SamplerState {
     bool want_gen = false;  // buffer `cur` still to be generated (after the next BMU kernel)
     cudaStream_t side = nullptr;
     cudaEvent_t ev_adv = nullptr, ev_gen = nullptr;
-    DevBuf err, age, keys, hist;                // adaptive
+    DevBuf err, age, keys, hist, cand, ccnt;    // adaptive (cand: first-digit bucket)
     DevBuf first, tidx;                         // random
     DevBuf bitmap, bcount, sel;                 // selection
     // Sharded (a communicator attached): this rank holds rows [off, off + n) of

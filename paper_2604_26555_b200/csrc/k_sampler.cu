@@ -52,6 +52,7 @@ __device__ __forceinline__ uint64_t mt_temper(uint64_t x) {
 }
 
 constexpr int kT = 320;  // threads per MT CTA (>= 312)
+constexpr uint32_t kCompactBlocks = 1184;  // segments of the first-digit compaction
 
 // one twist of the 312-word window `cur` into `nxt` (both shared), by kT threads
 __device__ __forceinline__ void twist(const uint64_t* cur, uint64_t* nxt) {
@@ -304,6 +305,15 @@ __device__ __forceinline__ double pow_ref(double x, double e) {
     return pow(x, e);
 }
 
+// warp-aggregated shared-memory histogram increment: lanes with the same bin
+// add once (the radix digits of the keys concentrate on few bins)
+__device__ __forceinline__ void hist_add(uint32_t* h, uint32_t bin, bool active) {
+    const uint32_t key = active ? bin : 0xFFFFFFFFu;
+    const uint32_t peers = __match_any_sync(0xffffffffu, key);
+    const uint32_t lane = threadIdx.x & 31;
+    if (active && (__ffs(peers) - 1) == (int)lane) atomicAdd(&h[bin], (uint32_t)__popc(peers));
+}
+
 // sortable 64-bit key: (seen << 63) | bits(key), key >= 0 (sampling.hpp:116-133)
 __global__ void k_adapt_keys(const double* __restrict__ err, const uint32_t* __restrict__ age,
                              const uint64_t* __restrict__ draws, uint64_t n, double alpha,
@@ -323,6 +333,65 @@ __global__ void k_adapt_keys(const double* __restrict__ err, const uint32_t* __r
     }
 }
 
+// Keys in the first digit's chosen bucket -> cand[] with the histogram of
+// the second digit (bits 40-51); the later digits then scan only these.
+// Block b compacts keys [b*chunk, (b+1)*chunk) into its own segment of cand
+// starting at b*chunk (no global counter); cnt[b] = its candidates.
+__global__ void k_adapt_compact(const unsigned long long* __restrict__ keys, uint64_t n,
+                                uint64_t chunk, const unsigned long long* __restrict__ sel_state,
+                                unsigned long long* __restrict__ cand, uint32_t* __restrict__ cnt,
+                                uint32_t* __restrict__ hist) {
+    __shared__ uint32_t h[4096];
+    __shared__ uint32_t fill;
+    for (int i = threadIdx.x; i < 4096; i += blockDim.x) h[i] = 0;
+    if (threadIdx.x == 0) fill = 0;
+    __syncthreads();
+    const unsigned long long top = sel_state[0] >> 52;
+    const uint32_t lane = threadIdx.x & 31;
+    const uint64_t c0 = blockIdx.x * chunk, c1 = min(n, c0 + chunk);
+    unsigned long long* out = cand + c0;
+    for (uint64_t i0 = c0; i0 < c1; i0 += blockDim.x) {
+        const uint64_t i = i0 + threadIdx.x;
+        const unsigned long long k = i < c1 ? keys[i] : ~0ULL;
+        const bool in = i < c1 && (k >> 52) == top;
+        const uint32_t ballot = __ballot_sync(0xffffffffu, in);
+        if (ballot) {
+            uint32_t base = 0;
+            if (lane == 0) base = atomicAdd(&fill, (uint32_t)__popc(ballot));
+            base = __shfl_sync(0xffffffffu, base, 0);
+            if (in) out[base + __popc(ballot & ((1u << lane) - 1u))] = k;
+            hist_add(h, (uint32_t)((k >> 40) & 4095ULL), in);
+        }
+    }
+    __syncthreads();
+    if (threadIdx.x == 0) cnt[blockIdx.x] = fill;
+    for (int i = threadIdx.x; i < 4096; i += blockDim.x)
+        if (h[i]) atomicAdd(&hist[i], h[i]);
+}
+
+// radix digit histogram over the compacted segments of k_adapt_compact
+__global__ void k_adapt_hist_cand(const unsigned long long* __restrict__ cand, uint64_t chunk,
+                                  const uint32_t* __restrict__ cnt,
+                                  const unsigned long long* __restrict__ sel_state, int shift,
+                                  int width, uint32_t* __restrict__ hist) {
+    __shared__ uint32_t h[4096];
+    for (int i = threadIdx.x; i < 4096; i += blockDim.x) h[i] = 0;
+    __syncthreads();
+    const unsigned long long prefix = sel_state[0];
+    const unsigned long long hi_mask = ~0ULL << (shift + width);
+    const unsigned long long dmask = (1ULL << width) - 1ULL;
+    const unsigned long long* seg = cand + blockIdx.x * chunk;
+    const uint32_t m = cnt[blockIdx.x];
+    for (uint32_t i0 = 0; i0 < m; i0 += blockDim.x) {
+        const uint32_t i = i0 + threadIdx.x;
+        const unsigned long long k = i < m ? seg[i] : 0ULL;
+        hist_add(h, (uint32_t)((k >> shift) & dmask), i < m && (k & hi_mask) == prefix);
+    }
+    __syncthreads();
+    for (int i = threadIdx.x; i < 4096; i += blockDim.x)
+        if (h[i]) atomicAdd(&hist[i], h[i]);
+}
+
 // one radix-select digit (`width` <= 12 bits at `shift`) over keys matching
 // the prefix fixed so far above it
 __global__ void k_adapt_hist(const unsigned long long* __restrict__ keys, uint64_t n,
@@ -334,10 +403,12 @@ __global__ void k_adapt_hist(const unsigned long long* __restrict__ keys, uint64
     const unsigned long long prefix = sel_state[0];
     const unsigned long long hi_mask = shift + width >= 64 ? 0ULL : (~0ULL << (shift + width));
     const unsigned long long dmask = (1ULL << width) - 1ULL;
-    for (uint64_t i = blockIdx.x * (uint64_t)blockDim.x + threadIdx.x; i < n;
-         i += (uint64_t)gridDim.x * blockDim.x) {
-        const unsigned long long k = keys[i];
-        if ((k & hi_mask) == prefix) atomicAdd(&h[(k >> shift) & dmask], 1u);
+    const uint64_t stride = (uint64_t)gridDim.x * blockDim.x;
+    for (uint64_t i0 = blockIdx.x * (uint64_t)blockDim.x; i0 < n; i0 += stride) {
+        const uint64_t i = i0 + threadIdx.x;
+        const unsigned long long k = i < n ? keys[i] : 0ULL;
+        const bool in = i < n && (k & hi_mask) == prefix;
+        hist_add(h, (uint32_t)((k >> shift) & dmask), in);
     }
     __syncthreads();
     for (int i = threadIdx.x; i < 4096; i += blockDim.x)
@@ -579,7 +650,7 @@ int sampler_setup(SamplerState& s, int kind, uint64_t n, uint64_t m, uint64_t se
     mt::seed_window(z ^ (z >> 31), w);
     if (s.window.ensure(312 * 8) != cudaSuccess) return 4;
     if (h2d_blocking(s.window.p, w, 312 * 8) != cudaSuccess) return 4;
-    if (s.misc.ensure(64) != cudaSuccess) return 4;
+    if (s.misc.ensure(128) != cudaSuccess) return 4;
     if (s.sharded && s.slots.ensure((size_t)std::max(1, s.world) * 8) != cudaSuccess) return 4;
     if (kind == 2 && s.sharded) {
         // the stream advances by gN draws per epoch, whatever this rank's share
@@ -625,7 +696,8 @@ int sampler_setup(SamplerState& s, int kind, uint64_t n, uint64_t m, uint64_t se
         return 4;
     if (kind == 2) {
         if (s.err.ensure(n * 8) != cudaSuccess || s.age.ensure(n * 4) != cudaSuccess ||
-            s.keys.ensure(n * 8) != cudaSuccess || s.hist.ensure(4096 * 4) != cudaSuccess)
+            s.keys.ensure(n * 8) != cudaSuccess || s.hist.ensure(4096 * 4) != cudaSuccess ||
+            s.cand.ensure(n * 8) != cudaSuccess || s.ccnt.ensure(kCompactBlocks * 4) != cudaSuccess)
             return 4;
         // last_error = kUnseenError (sampling.hpp:81, 91), age = 0
         const size_t chunk = 1 << 20;
@@ -734,20 +806,31 @@ int sampler_select(SamplerState& s, uint32_t* out, uint64_t* m_out, int sm_count
         auto* mx = reinterpret_cast<unsigned long long*>(misc + 4);
         TSOM_LAUNCH(k_adapt_max<<<grid, 256, 0, st>>>(s.err.as<double>(), s.age.as<uint32_t>(), n, mx));
         if (s.sharded) ok &= s.allreduce(mx, 2, 1);  // the maxima over all rows
-        TSOM_LAUNCH(k_adapt_keys<<<grid, 256, 0, st>>>(
-            s.err.as<double>(), s.age.as<uint32_t>(), draws, n, s.alpha, s.beta, mx,
-            reinterpret_cast<unsigned long long*>(s.keys.p)));
         auto* rs = reinterpret_cast<unsigned long long*>(misc + 6);
         const unsigned long long st0[2] = {0ULL, (unsigned long long)m};
         cudaMemcpyAsync(rs, st0, 16, cudaMemcpyHostToDevice, st);
-        // digits of the 64-bit key: bits 52-63, 40-51, 28-39, 16-27, 4-15, 0-3;
-        // sharded: each digit histogram summed over the ranks (the same digit
-        // is then picked everywhere: one global threshold)
+        auto* keys = reinterpret_cast<unsigned long long*>(s.keys.p);
+        auto* cand = reinterpret_cast<unsigned long long*>(s.cand.p);
+        uint32_t* ccnt = s.ccnt.as<uint32_t>();
+        const uint64_t chunk = (n + kCompactBlocks - 1) / kCompactBlocks;
+        TSOM_LAUNCH(k_adapt_keys<<<grid, 256, 0, st>>>(s.err.as<double>(), s.age.as<uint32_t>(),
+                                                       draws, n, s.alpha, s.beta, mx, keys));
+        // digits of the 64-bit key: bits 52-63, 40-51, 28-39, 16-27, 4-15, 0-3.
+        // Digit 0 scans every key, digit 1 comes with the compaction of digit
+        // 0's bucket, digits 2-5 scan only that bucket.  Sharded: each digit
+        // histogram summed over the ranks (the same digit is then picked
+        // everywhere: one global threshold).
         const int shifts[6] = {52, 40, 28, 16, 4, 0}, widths[6] = {12, 12, 12, 12, 12, 4};
         for (int d = 0; d < 6; ++d) {
-            TSOM_LAUNCH(k_adapt_hist<<<grid, 256, 0, st>>>(
-                reinterpret_cast<const unsigned long long*>(s.keys.p), n, rs, shifts[d], widths[d],
-                s.hist.as<uint32_t>()));
+            if (d == 0)
+                TSOM_LAUNCH(k_adapt_hist<<<grid, 256, 0, st>>>(keys, n, rs, shifts[d], widths[d],
+                                                               s.hist.as<uint32_t>()));
+            else if (d == 1)
+                TSOM_LAUNCH(k_adapt_compact<<<kCompactBlocks, 256, 0, st>>>(
+                    keys, n, chunk, rs, cand, ccnt, s.hist.as<uint32_t>()));
+            else
+                TSOM_LAUNCH(k_adapt_hist_cand<<<kCompactBlocks, 256, 0, st>>>(
+                    cand, chunk, ccnt, rs, shifts[d], widths[d], s.hist.as<uint32_t>()));
             if (s.sharded) ok &= s.allreduce(s.hist.p, 4096, 0);
             TSOM_LAUNCH(k_adapt_digit<<<1, 1024, 0, st>>>(s.hist.as<uint32_t>(), shifts[d], rs));
         }
@@ -801,7 +884,7 @@ void sampler_pregenerate(SamplerState& s, cudaEvent_t after) {
 void sampler_release(SamplerState& s) {
     if (s.side) cudaStreamSynchronize(s.side);
     for (DevBuf* d : {&s.window, &s.jp, &s.misc, &s.seqb[0], &s.seqb[1], &s.drawsb[0],
-                      &s.drawsb[1], &s.tailb[0], &s.tailb[1], &s.err, &s.age, &s.keys, &s.hist,
+                      &s.drawsb[1], &s.tailb[0], &s.tailb[1], &s.err, &s.age, &s.keys, &s.hist, &s.cand, &s.ccnt,
                       &s.first, &s.tidx, &s.bitmap, &s.bcount, &s.sel})
         d->release();
     if (s.ev_adv) cudaEventDestroy(s.ev_adv);
