@@ -536,10 +536,11 @@ void accumulate_epoch(Engine* eng, const uint32_t* sel_host, uint64_t n_sel, boo
                                 accumulate, true, eng->acc, eng->sums.as<double>(), eng->sm_count,
                                 eng->stream, eng->x_slack);
         CU(cudaGetLastError());
-        eng->chunk_counts.assign(2, 0u);
+        eng->chunk_counts.clear();
         eng->recheck_from_chunks = true;
-        CU(cudaMemcpyAsync(&eng->chunk_counts[0], eng->flags.p, 2 * sizeof(uint32_t),
-                           cudaMemcpyDeviceToHost, eng->stream));
+        eng->hstat_counts = true;
+        CU(cudaMemcpyAsync(eng->hstat, eng->flags.p, 2 * sizeof(uint32_t), cudaMemcpyDeviceToHost,
+                           eng->stream));
     } else {
         // Streamed: rows live in host memory; chunks of stream_chunk_rows rows
         // are copied on copy_stream into two device stages, compute on stream.
@@ -607,6 +608,7 @@ void accumulate_epoch(Engine* eng, const uint32_t* sel_host, uint64_t n_sel, boo
             if (k + 2 < jobs.size()) issue(k + 2);
         }
         if (first) CU(cudaMemsetAsync(eng->sums.p, 0, slot_len(eng) * sizeof(double), eng->stream));
+        eng->hstat_counts = false;
         eng->chunk_counts.assign(std::max<size_t>(2, 2 * jobs.size()), 0u);
         if (!jobs.empty())
             CU(cudaMemcpyAsync(eng->chunk_counts.data(), eng->chunk_flags.p,
@@ -630,10 +632,18 @@ void accumulate_epoch(Engine* eng, const uint32_t* sel_host, uint64_t n_sel, boo
 // Guard of quantize_term (accum.hpp:34-38): every term eta*h*(x - w) must stay
 // below 2^22.  Conservative bound |eta*h*(x - w)| <= eta*max|h|*(max||x|| + max||w||),
 // evaluated after the pass (streamed mode learns max||x|| while streaming).
+// the term guard's inputs, read back with the epoch's other status words
+void enqueue_guard_read(Engine* eng) {
+    CU(cudaMemcpyAsync(eng->hstat + 3, eng->x2max.p, sizeof(float), cudaMemcpyDeviceToHost,
+                       eng->stream));
+    CU(cudaMemcpyAsync(eng->hstat + 4, eng->w2max.p, sizeof(float), cudaMemcpyDeviceToHost,
+                       eng->stream));
+}
+
+// after the end-of-epoch synchronisation
 void check_term_guard(Engine* eng, double eta) {
-    float hx[2] = {0, 0};
-    CU(cudaMemcpy(&hx[0], eng->x2max.p, sizeof(float), cudaMemcpyDeviceToHost));
-    CU(cudaMemcpy(&hx[1], eng->w2max.p, sizeof(float), cudaMemcpyDeviceToHost));
+    float hx[2];
+    std::memcpy(hx, eng->hstat + 3, sizeof(hx));
     const double bound =
         std::fabs(eta) * eng->max_h * (std::sqrt((double)hx[0]) + std::sqrt((double)hx[1]));
     REQUIRE(eng->max_h < 4194304.0 && bound < 4194304.0, TSOM_ERR_NUMERICAL,
@@ -643,7 +653,10 @@ void check_term_guard(Engine* eng, double eta) {
 void finish_recheck(Engine* eng) {
     if (eng->recheck_from_chunks) {
         uint64_t t = 0;
-        for (uint32_t c : eng->chunk_counts) t += c;
+        if (eng->hstat_counts)
+            t = (uint64_t)eng->hstat[0] + eng->hstat[1];
+        else
+            for (uint32_t c : eng->chunk_counts) t += c;
         eng->last_recheck = t;
     }
 }
@@ -720,6 +733,8 @@ int tsom_create(int device, uint32_t nodes, uint32_t dims, tsom_engine** out) {
         CU(eng->U.ensure(P * D * sizeof(double)));
         CU(eng->H.ensure(P * sizeof(double)));
         CU(eng->status.ensure(4 * sizeof(int)));
+        CU(cudaMallocHost(&eng->hstat, 16 * sizeof(uint32_t)));
+        std::memset(eng->hstat, 0, 16 * sizeof(uint32_t));
         ensure_rows(eng, 1);
         CU(cudaStreamSynchronize(eng->stream));
     });
@@ -757,6 +772,7 @@ int tsom_destroy(tsom_engine* eng) {
         b->release(true);
     for (auto& ev : eng->ev)
         if (ev) cudaEventDestroy(ev);
+    if (eng->hstat) cudaFreeHost(eng->hstat);
     if (eng->stream) cudaStreamDestroy(eng->stream);
     if (eng->copy_stream) cudaStreamDestroy(eng->copy_stream);
     delete eng;
@@ -1088,6 +1104,7 @@ int tsom_epoch(tsom_engine* eng, const uint32_t* selected, uint64_t n_sel, doubl
         if (dist_out && n)
             CU(cudaMemcpyAsync(dist_out, eng->dist.p, n * sizeof(double), cudaMemcpyDeviceToHost,
                                eng->stream));
+        enqueue_guard_read(eng);
         CU(cudaStreamSynchronize(eng->stream));
         finish_recheck(eng);
         record_timing(eng);
@@ -1525,8 +1542,7 @@ int tsom_train_epoch(tsom_engine* eng, double eta, double sigma, double momentum
                                   eng->dist.as<double>(), eng->sm_count, eng->stream);
         }
         smooth(eng, eta);
-        int ok = INT_MAX;
-        CU(cudaMemcpyAsync(eng->status.p, &ok, sizeof(int), cudaMemcpyHostToDevice, eng->stream));
+        tsom::launch_status_reset(eng->status.as<int>(), eng->stream);
         tsom::launch_apply_update(eng->w.as<float>(), eng->prev.as<float>(), eng->P, eng->D,
                                   eng->U.as<double>(), eng->H.as<double>(), momentum_on, momentum,
                                   eng->status.as<int>(), eng->stream);
@@ -1535,9 +1551,12 @@ int tsom_train_epoch(tsom_engine* eng, double eta, double sigma, double momentum
         eng->update_timed = true;
         eng->codebook_prepped = false;
         prep_codebook(eng);
-        int st = INT_MAX;
-        CU(cudaMemcpyAsync(&st, eng->status.p, sizeof(int), cudaMemcpyDeviceToHost, eng->stream));
+        CU(cudaMemcpyAsync(eng->hstat + 2, eng->status.p, sizeof(int), cudaMemcpyDeviceToHost,
+                           eng->stream));
+        enqueue_guard_read(eng);
         CU(cudaStreamSynchronize(eng->stream));
+        int st;
+        std::memcpy(&st, eng->hstat + 2, sizeof(int));
         finish_recheck(eng);
         record_timing(eng);
         check_term_guard(eng, eta);

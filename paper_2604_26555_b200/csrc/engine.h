@@ -276,7 +276,12 @@ struct Engine {
     std::vector<ShardFile> shards;  // FSOMSHRD files (dataset.hpp:171-344)
     cudaEvent_t ev[12] = {};  // 0 start, 1 bmu end, 6 accum end, 7 smooth end, 8/9 K1 kernel, 10 update end
     uint64_t last_recheck = 0;
-    std::vector<uint32_t> chunk_counts;  // per-chunk re-check counts (async D2H targets)
+    std::vector<uint32_t> chunk_counts;  // per-chunk re-check counts (streamed epochs)
+    // pinned per-epoch status words, read back asynchronously before the one
+    // end-of-epoch synchronisation: [0..1] re-check counts (resident epochs),
+    // [2] update status, [3] max ||x||^2 and [4] max ||w||^2 (term guard)
+    uint32_t* hstat = nullptr;
+    bool hstat_counts = false;  // [0..1] hold this epoch's re-check counts
     bool recheck_from_chunks = false;
     double max_h = 1.0;                  // max |influence| of the bound matrix
     float t_bmu = 0, t_accum = 0, t_smooth = 0, t_total = 0, t_k1 = 0, t_update = 0;
@@ -373,6 +378,8 @@ size_t smooth_scratch_doubles(uint32_t P, uint32_t D);
 void launch_apply_update(float* w, float* prev, uint32_t P, uint32_t D, const double* U,
                          const double* H, bool use_momentum, double momentum, int* status,
                          cudaStream_t st);
+// status[0] = INT_MAX (no failing node) before launch_apply_update
+void launch_status_reset(int* status, cudaStream_t st);
 // influence_matrix (topology.hpp:342-364) from a P x P distance matrix
 void launch_influence(const double* dist, size_t n, double inv_two_sigma_sq, double* out,
                       cudaStream_t st);

@@ -8,6 +8,7 @@
 #include <cuda_runtime.h>
 #include <math_constants.h>
 
+#include <climits>
 #include <cstdint>
 
 #include "engine.h"
@@ -151,6 +152,12 @@ void launch_apply_update(float* w, float* prev, uint32_t P, uint32_t D, const do
     TSOM_LAUNCH(k_apply_update<<<(unsigned)((n + 255) / 256), 256, 0, st>>>(w, prev, P, D, U, H,
                                                                 use_momentum ? 1 : 0, momentum,
                                                                 status));
+}
+
+__global__ void k_status_reset(int* status) { *status = INT_MAX; }
+
+void launch_status_reset(int* status, cudaStream_t st) {
+    TSOM_LAUNCH(k_status_reset<<<1, 1, 0, st>>>(status));
 }
 
 // influence_matrix (topology.hpp:342-364): z = (d*d)*inv, h = z > 57.6 ? 0 : exp(-z)
