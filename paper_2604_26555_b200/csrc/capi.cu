@@ -379,13 +379,50 @@ void close_shards(Engine* eng) {
     eng->shards.clear();
 }
 
+// Pinned staging blocks are cached process-wide (cudaMallocHost of tens of MB
+// costs tens of ms): engines take a block at least as large as they need and
+// return it on destroy.
+struct PinnedBlock {
+    void* p;
+    size_t bytes;
+};
+static std::mutex g_pinned_mu;
+static std::vector<PinnedBlock> g_pinned_free;
+
+static cudaError_t pinned_take(size_t bytes, void** out, size_t* got) {
+    {
+        std::lock_guard<std::mutex> lk(g_pinned_mu);
+        for (size_t i = 0; i < g_pinned_free.size(); ++i)
+            if (g_pinned_free[i].bytes >= bytes) {
+                *out = g_pinned_free[i].p;
+                *got = g_pinned_free[i].bytes;
+                g_pinned_free.erase(g_pinned_free.begin() + (std::ptrdiff_t)i);
+                return cudaSuccess;
+            }
+    }
+    *got = bytes;
+    return cudaMallocHost(out, bytes);
+}
+
+static void pinned_give(void* p, size_t bytes) {
+    if (!p) return;
+    std::lock_guard<std::mutex> lk(g_pinned_mu);
+    g_pinned_free.push_back({p, bytes});
+    if (g_pinned_free.size() > 8) {  // bound the cache: drop the oldest
+        cudaFreeHost(g_pinned_free.front().p);
+        g_pinned_free.erase(g_pinned_free.begin());
+    }
+}
+
 void ensure_pinned(Engine* eng, uint64_t rows) {
     if (eng->pinned_rows >= rows && eng->pinned[0]) return;
     for (int s = 0; s < 2; ++s) {
         if (eng->pin_busy[s]) CU(cudaEventSynchronize(eng->ev_pin[s]));
-        if (eng->pinned[s]) cudaFreeHost(eng->pinned[s]);
+        pinned_give(eng->pinned[s], eng->pinned_bytes[s]);
         eng->pinned[s] = nullptr;
-        CU(cudaMallocHost(&eng->pinned[s], rows * eng->D * sizeof(float)));
+        void* p = nullptr;
+        CU(pinned_take(rows * eng->D * sizeof(float), &p, &eng->pinned_bytes[s]));
+        eng->pinned[s] = static_cast<float*>(p);
         if (!eng->ev_pin[s]) CU(cudaEventCreateWithFlags(&eng->ev_pin[s], cudaEventDisableTiming));
         eng->pin_busy[s] = false;
     }
@@ -756,7 +793,7 @@ int tsom_destroy(tsom_engine* eng) {
     close_shards(eng);
     tsom::sampler_release(eng->sampler);
     for (int s2 = 0; s2 < 2; ++s2) {
-        if (eng->pinned[s2]) cudaFreeHost(eng->pinned[s2]);
+        pinned_give(eng->pinned[s2], eng->pinned_bytes[s2]);
         if (eng->ev_pin[s2]) cudaEventDestroy(eng->ev_pin[s2]);
     }
     for (DevBuf* b : {&eng->x, &eng->xsplit, &eng->xn2, &eng->gxn2, &eng->txn2, &eng->x2max, &eng->w, &eng->wt, &eng->wsplit, &eng->w2,

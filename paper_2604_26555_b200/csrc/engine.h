@@ -263,6 +263,7 @@ struct Engine {
     DevBuf chunk_flags;    // streamed mode: re-check counters per chunk
     float* pinned[2] = {nullptr, nullptr};  // host staging for shard / pageable sources
     size_t pinned_rows = 0;
+    size_t pinned_bytes[2] = {0, 0};  // sizes of the (possibly larger) cached blocks
     cudaEvent_t ev_pin[2] = {nullptr, nullptr};  // H2D from pinned[s] finished
     bool pin_busy[2] = {false, false};
     bool host_register = true;  // TSOM_OPT_HOST_REGISTER

@@ -518,3 +518,32 @@ def test_bind_device_rows_exact(pkg, oracle_port, owner):
     assert np.max(np.abs(u - uo)) <= 1e-9 * np.max(np.abs(uo))
     np.testing.assert_allclose(h, ho, rtol=1e-9)
     np.testing.assert_allclose(dist, do, rtol=1e-12)
+
+
+def test_pageable_bind_staging_and_gather_variants(pkg, oracle_port):
+    # an 80 MB pageable bind goes through the multi-threaded pinned staging
+    # (>= 64 MB); the epoch then runs with the TMA gather and with the cp.async
+    # gather (option 97), both against the oracle
+    from paper_2604_26555_b200 import _lib
+    n, p, d = 400_000, 256, 50
+    x = oracle_port.synth_gmm(n, d, 2614)
+    assert x.nbytes >= 64 << 20
+    w = x[np.linspace(0, n - 1, p).astype(int)].copy()
+    infl = oracle_port.influence_from_dist(oracle_port.lattice_dist("hex", 16, 16), 4.0)
+    sel = np.sort(np.random.default_rng(3).choice(n, 150_001, replace=False)).astype(np.uint32)
+    uo, ho, _, _, do = oracle_port.run_iteration(x, sel, w, infl, 0.45, 1, 8)
+    e = engine(pkg, p, d, 0)
+    try:
+        e.bind(x)
+        e.set_codebook(w)
+        e.set_influence(infl)
+        for kind in (0, 1):
+            e.set_option(97, kind)
+            u, h, dist = e.epoch(0.45, sel, want_dist=True)
+            assert np.max(np.abs(u - uo)) <= 1e-9 * np.max(np.abs(uo))
+            np.testing.assert_allclose(h, ho, rtol=1e-9)
+            np.testing.assert_allclose(dist, do, rtol=1e-12)
+    finally:
+        e.set_option(97, 0)
+        e.close()
+    _lib.release_cached_memory(0)
