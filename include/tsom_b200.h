@@ -60,7 +60,7 @@ extern "C" {
 #define TSOM_OPT_DETERMINISTIC 4   /* reserved */
 #define TSOM_OPT_HOST_REGISTER 5   /* streamed host rows: 1 (default) page-lock the caller's
                                       buffer for direct DMA, 0 copy through pinned staging */
-#define TSOM_OPT_STAGING_THREADS 6 /* host threads filling the pinned staging (default 8) */
+#define TSOM_OPT_STAGING_THREADS 6 /* host threads filling the pinned staging (default: min(16, cores)) */
 
 typedef struct tsom_engine tsom_engine;
 

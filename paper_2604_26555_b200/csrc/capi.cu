@@ -15,6 +15,7 @@
 #include <condition_variable>
 #include <chrono>
 #include <mutex>
+#include <functional>
 
 #include <algorithm>
 #include <climits>
@@ -449,6 +450,67 @@ std::string read_shard_rows(const Engine* eng, uint64_t r0, uint64_t r1, float* 
     return std::string();
 }
 
+// Persistent host workers for the staging fills (a fork-join per chunk;
+// spawning threads per chunk cost ~1 ms of every 32-MB chunk).  The calling
+// thread works too; concurrent callers (engines on several threads) take
+// turns.  Workers only copy host memory / read files.
+class StagingPool {
+public:
+    explicit StagingPool(unsigned n) {
+        for (unsigned i = 0; i < n; ++i) workers_.emplace_back([this] { loop(); });
+    }
+    void run(uint32_t n, const std::function<void(uint32_t)>& fn) {
+        std::lock_guard<std::mutex> turn(run_mu_);
+        std::unique_lock<std::mutex> lk(mu_);
+        job_ = &fn;
+        njobs_ = n;
+        next_ = 0;
+        finished_ = 0;
+        ++gen_;
+        cv_.notify_all();
+        while (next_ < njobs_) {
+            const uint32_t i = next_++;
+            lk.unlock();
+            fn(i);
+            lk.lock();
+            ++finished_;
+        }
+        done_.wait(lk, [&] { return finished_ == njobs_; });
+        job_ = nullptr;
+    }
+
+private:
+    void loop() {
+        std::unique_lock<std::mutex> lk(mu_);
+        uint64_t seen = 0;
+        for (;;) {
+            cv_.wait(lk, [&] { return gen_ != seen && job_ && next_ < njobs_; });
+            seen = gen_;
+            while (job_ && next_ < njobs_) {
+                const uint32_t i = next_++;
+                const std::function<void(uint32_t)>* fn = job_;
+                lk.unlock();
+                (*fn)(i);
+                lk.lock();
+                if (++finished_ == njobs_) done_.notify_all();
+            }
+        }
+    }
+    std::mutex run_mu_, mu_;
+    std::condition_variable cv_, done_;
+    std::vector<std::thread> workers_;
+    const std::function<void(uint32_t)>* job_ = nullptr;
+    uint32_t njobs_ = 0, next_ = 0, finished_ = 0;
+    uint64_t gen_ = 0;
+};
+
+StagingPool& staging_pool() {
+    // leaked on purpose: blocked workers need no joining at process exit
+    static StagingPool* pool =
+        new StagingPool(std::max(1u, std::min(16u, std::thread::hardware_concurrency())) - 1);
+    return *pool;
+}
+
 const float* host_chunk_source(Engine* eng, uint64_t r0, uint64_t r1, int s) {
     if (eng->shards.empty() && eng->host_direct) return eng->host_rows + r0 * eng->D;
     ensure_pinned(eng, std::max<uint64_t>(r1 - r0, eng->pinned_rows));
@@ -463,20 +525,20 @@ const float* host_chunk_source(Engine* eng, uint64_t r0, uint64_t r1, int s) {
         return std::string();
     };
     const uint64_t bytes = (r1 - r0) * eng->D * sizeof(float);
-    const uint32_t T = (uint32_t)std::min<uint64_t>(eng->staging_threads,
+    static const uint32_t host_threads = std::max(1u, std::min(16u, std::thread::hardware_concurrency()));
+    const uint32_t T = (uint32_t)std::min<uint64_t>(eng->staging_threads ? eng->staging_threads
+                                                                         : host_threads,
                                                     std::max<uint64_t>(1, bytes >> 22));
     if (T <= 1) {
         const std::string e = fill(r0, r1);
         REQUIRE(e.empty(), TSOM_ERR_NUMERICAL, e);
     } else {
-        std::vector<std::thread> pool;
         std::vector<std::string> errs(T);
         const uint64_t per = (r1 - r0 + T - 1) / T;
-        for (uint32_t t = 0; t < T; ++t) {
+        staging_pool().run(T, [&](uint32_t t) {
             const uint64_t a = std::min(r1, r0 + t * per), b = std::min(r1, a + per);
-            pool.emplace_back([&, a, b, t] { errs[t] = fill(a, b); });
-        }
-        for (auto& th : pool) th.join();
+            errs[t] = fill(a, b);
+        });
         for (const auto& e : errs) REQUIRE(e.empty(), TSOM_ERR_NUMERICAL, e);
     }
     return dst;

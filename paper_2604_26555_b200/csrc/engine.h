@@ -268,7 +268,7 @@ struct Engine {
     bool pin_busy[2] = {false, false};
     bool host_register = true;  // TSOM_OPT_HOST_REGISTER
     bool host_direct = false;   // streamed host rows are DMA-able (pinned)
-    uint32_t staging_threads = 8;  // TSOM_OPT_STAGING_THREADS
+    uint32_t staging_threads = 0;  // TSOM_OPT_STAGING_THREADS (0: min(16, host cores))
     struct ShardFile {
         std::string path;
         int fd = -1;

@@ -25,6 +25,7 @@ def main():
     ap.add_argument("--chunk", type=int, default=1 << 20)
     ap.add_argument("--shard-dir", default="/tmp/tsom_stream_shards")
     ap.add_argument("--modes", default="resident,pinned,pageable,shards")
+    ap.add_argument("--staging-threads", type=int, default=0, help="0: engine default")
     args = ap.parse_args()
 
     import numpy as np
@@ -68,6 +69,8 @@ def main():
     for mode in modes:
         e = tsom.Engine(P, D)
         e.set_option(_lib.TSOM_OPT_STREAM_CHUNK, args.chunk)
+        if args.staging_threads:
+            e.set_option(_lib.TSOM_OPT_STAGING_THREADS, args.staging_threads)
         t0 = time.perf_counter()
         if mode == "resident":
             e.bind(host)
