@@ -1,5 +1,5 @@
 """Profile target for the row split kernels: one gathered split with the
-element-wise kernel (option 98 = 1) and one with the row-image kernel, on the
+element-wise kernel (option 98 = 1) and one with the warp-synchronous kernel, on the
 c2 row shape.  Run under ncu -k regex:k_split_rows."""
 import os
 import sys
