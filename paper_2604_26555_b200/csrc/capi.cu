@@ -309,7 +309,7 @@ void run_bmu(Engine* eng, const float* x, const uint32_t* sel, uint64_t n, const
         CU(cudaEventRecord(eng->ev[9], eng->stream));
         eng->k1_timed = true;
         tsom::sampler_pregenerate(eng->sampler, eng->ev[9]);
-        tsom::launch_merge_fast(eng->part.as<float>(), n, groups, tsom::kTcEpiSets, gn, tiles_xn2,
+        tsom::launch_merge_fast(eng->part.as<float>(), n, groups, 1, gn, tiles_xn2,
                                 w2, scale, win,
                                 eng->bmu.as<uint32_t>(), eng->ties.as<uint32_t>(),
                                 eng->tmask.as<uint32_t>(), eng->flags.as<uint32_t>(), eng->stream);

@@ -565,6 +565,9 @@ __global__ void __launch_bounds__(EpiCfg<kKind>::kThreads, 1)
     uint64_t* tempty_bar = tfull_bar + 2;         // [2] accumulator drained
     uint64_t* w_bar = tfull_bar + 4;              // codebook group landed
     uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(w_bar + 1);
+    // [2 tiles][128 rows] (b, code) of epilogue set 1, merged into set 0's
+    float* xch_b = reinterpret_cast<float*>(bars + 16);
+    uint32_t* xch_c = reinterpret_cast<uint32_t*>(xch_b + 2 * kTcTileM);
 
     const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
     const uint32_t g = blockIdx.x % groups;
@@ -772,12 +775,31 @@ __global__ void __launch_bounds__(EpiCfg<kKind>::kThreads, 1)
                 uint32_t code = 0xFFFFFFFFu;  // id relative to the set's first column
                 if (asum >= 256.0f && asum < 512.0f && asum == floorf(asum))
                     code = (uint32_t)asum - 256u;
-                // each set writes its column slice as its own sub-group
-                // (k_merge_fast combines them: no exchange, no named barrier)
-                if (pos < n) {
-                    float* pg = part + (size_t)(g * kSets + set) * 2 * n;
-                    pg[pos] = b;
-                    pg[n + pos] = __uint_as_float(code);
+                // the sets' results for the group are merged here, exactly as
+                // k_merge_fast would merge them (set 0 wins equal minima; the
+                // group's id is ambiguous when the other set's minimum lies in
+                // the window of the group's), so one record per (row, group)
+                // leaves the CTA
+                static_assert(kSets == 2, "set merge assumes two epilogue sets");
+                if (set == 1) {
+                    xch_b[acc * kTcTileM + row] = b;
+                    xch_c[acc * kTcTileM + row] = code;
+                }
+                asm volatile("bar.sync 1, %0;" ::"n"(kSets * 128) : "memory");
+                if (set == 0 && pos < n) {
+                    const float b1 = xch_b[acc * kTcTileM + row];
+                    const uint32_t c1 = xch_c[acc * kTcTileM + row];
+                    float bg = b, other = b1;
+                    uint32_t cg = code;
+                    if (b1 < b) {
+                        bg = b1;
+                        other = b;
+                        cg = c1 == 0xFFFFFFFFu ? c1 : c1 + (nch / kSets) * 32u;
+                    }
+                    if (other <= bg + thr) cg = 0xFFFFFFFFu;
+                    float* pg = part + (size_t)g * 2 * n;
+                    pg[pos] = bg;
+                    pg[n + pos] = __uint_as_float(cg);
                 }
                 if (++acc == 2) {
                     acc = 0;
@@ -875,7 +897,7 @@ cudaError_t launch_bmu_tc(int kind, const void* tiles, uint64_t n, const uint32_
     if (per_group > ntiles) per_group = ntiles;
     const uint32_t grid = per_group * groups;
     const uint32_t w_bytes = gn * geo.row_bytes;
-    const size_t fixed = ((w_bytes + 1023u) & ~1023u) + 128;
+    const size_t fixed = ((w_bytes + 1023u) & ~1023u) + 128 + 2 * kTcTileM * 8;  // + set exchange
     uint32_t stages = 2;
     while (stages < 3 && fixed + (size_t)(stages + 1) * geo.tile_bytes <= smem_optin) ++stages;
     const size_t smem = fixed + (size_t)stages * geo.tile_bytes;
