@@ -237,8 +237,8 @@ __device__ __forceinline__ double exact_d2(const float* __restrict__ x,
 }
 
 // Main-pass merge.  part[sg] = [B1 | code] per row and sub-group sg = g * sets
-// + h (k1_bmu_tc<.., false>: epilogue set h of codebook group g covers the
-// group's chunks [h nch / sets, (h+1) nch / sets)): the sub-group's raw minimum
+// + h, the group's chunks [h nch / sets, (h+1) nch / sets) (k1_bmu_tc merges
+// its two epilogue sets in the CTA and passes sets = 1): the sub-group's raw minimum
 // and, when it is the only node of the sub-group within the error window of
 // that minimum, its id relative to the sub-group (else 0xFFFFFFFF).  A row is
 // clear when its best sub-group has a unique in-window node and every other
