@@ -21,6 +21,7 @@
 // 200 B row => ~212 B/row (204 B algorithmic).
 #include <cuda_runtime.h>
 
+#include <algorithm>
 #include <cstdint>
 
 #include "engine.h"
@@ -136,7 +137,6 @@ __global__ void __launch_bounds__(1024) k_nodescan(const uint32_t* __restrict__ 
         if (b < P) {
             node_start[b] = ns;
             piece_start[b] = ps;
-            for (uint32_t k = 0; k < pc; ++k) piece_node[ps + k] = b;
             double* cb = sums + (size_t)P * D + b;
             *cb = add_counts ? *cb + (double)t : (double)t;
         }
@@ -153,23 +153,40 @@ __global__ void __launch_bounds__(1024) k_nodescan(const uint32_t* __restrict__ 
     }
 }
 
+// piece -> node table: thread per piece, binary search in piece_start (a node
+// with many rows would otherwise write its hundreds of entries serially)
+__global__ void k_piece_nodes(const uint32_t* __restrict__ piece_start, uint32_t P,
+                              uint32_t max_pieces, uint32_t* __restrict__ piece_node) {
+    const uint32_t np = piece_start[P];
+    for (uint32_t p = blockIdx.x * blockDim.x + threadIdx.x; p < np && p < max_pieces;
+         p += gridDim.x * blockDim.x) {
+        uint32_t lo = 0, hi = P;  // last b with piece_start[b] <= p
+        while (hi - lo > 1) {
+            const uint32_t mid = (lo + hi) / 2;
+            if (piece_start[mid] <= p) lo = mid;
+            else hi = mid;
+        }
+        piece_node[p] = lo;
+    }
+}
+
 // Stable scatter of positions into BMU order (ties in position order).
 __global__ void __launch_bounds__(kScatterWarps * 32) k_scatter(
     const uint32_t* __restrict__ bmu, uint64_t n, uint32_t P, const uint32_t* __restrict__ offs,
     const uint32_t* __restrict__ node_start, uint32_t* __restrict__ sorted) {
-    extern __shared__ uint32_t whist[];  // [kScatterWarps][P] then the block's BMUs
-    uint32_t* sb = whist + (size_t)kScatterWarps * P;
+    // only the per-warp histograms live in shared memory (32 KB at P = 1024),
+    // so ~7 blocks fit an SM and the whole grid runs in one wave; the block's
+    // BMUs are read twice from global memory (the second time from L1/L2)
+    extern __shared__ uint32_t whist[];  // [kScatterWarps][P]
     const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
     const uint64_t r0 = (uint64_t)blockIdx.x * kHistRows;
     for (uint32_t e = threadIdx.x; e < kScatterWarps * P; e += blockDim.x) whist[e] = 0;
-    for (uint32_t e = threadIdx.x; e < kHistRows; e += blockDim.x)
-        sb[e] = r0 + e < n ? bmu[r0 + e] : 0u;  // one coalesced pass over the block's BMUs
     __syncthreads();
     const uint32_t sub = kHistRows / kScatterWarps;
     const uint64_t w0 = r0 + (uint64_t)warp * sub;
     const uint64_t w1 = (w0 + sub < n) ? w0 + sub : n;
     uint32_t* mine = whist + (size_t)warp * P;
-    for (uint64_t i = w0 + lane; i < w1; i += 32) atomicAdd(&mine[sb[i - r0]], 1u);
+    for (uint64_t i = w0 + lane; i < w1; i += 32) atomicAdd(&mine[__ldg(bmu + i)], 1u);
     __syncthreads();
     const uint32_t* boff = offs + (size_t)blockIdx.x * P;
     for (uint32_t b = threadIdx.x; b < P; b += blockDim.x) {
@@ -184,7 +201,7 @@ __global__ void __launch_bounds__(kScatterWarps * 32) k_scatter(
     for (uint64_t base = w0; base < w1; base += 32) {
         const uint64_t i = base + lane;
         const bool valid = i < w1;
-        const uint32_t b = valid ? sb[i - r0] : 0xFFFFFFFFu;
+        const uint32_t b = valid ? __ldg(bmu + i) : 0xFFFFFFFFu;
         const uint32_t peers = __match_any_sync(0xffffffffu, b);
         const uint32_t rank = __popc(peers & ((1u << lane) - 1u));
         if (valid) sorted[mine[b] + rank] = (uint32_t)i;
@@ -594,15 +611,20 @@ void launch_accumulate(const float* x, const uint32_t* sel, uint64_t n, uint32_t
     if (P > attr_p) {  // dynamic smem beyond 48 KB (P up to ~7000 nodes)
         cudaFuncSetAttribute(k_hist, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)(P * 4));
         cudaFuncSetAttribute(k_scatter, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                             (int)((kScatterWarps * P + kHistRows) * 4));
+                             (int)(kScatterWarps * P * 4));
         attr_p = P;
     }
     TSOM_LAUNCH(k_hist<<<nblk, 512, P * sizeof(uint32_t), st>>>(bmu, n, P, s.counts));
     TSOM_LAUNCH(k_colscan<<<(P + 31) / 32, 256, 0, st>>>(s.counts, nblk, P, s.totals));
     TSOM_LAUNCH(k_nodescan<<<1, 1024, 0, st>>>(s.totals, P, D, s.node_start, s.piece_start,
                                                s.piece_node, sums, add));
-    TSOM_LAUNCH(k_scatter<<<nblk, kScatterWarps * 32,
-                            ((size_t)kScatterWarps * P + kHistRows) * sizeof(uint32_t),
+    {
+        const uint64_t pmax = accum_pieces_max(n, P);
+        const unsigned pb = (unsigned)std::min<uint64_t>((pmax + 255) / 256, (uint64_t)sm_count * 4);
+        TSOM_LAUNCH(k_piece_nodes<<<pb, 256, 0, st>>>(s.piece_start, P, (uint32_t)pmax,
+                                                      s.piece_node));
+    }
+    TSOM_LAUNCH(k_scatter<<<nblk, kScatterWarps * 32, (size_t)kScatterWarps * P * sizeof(uint32_t),
                             st>>>(bmu, n, P, s.counts, s.node_start, s.sorted));
     const uint64_t pieces = accum_pieces_max(n, P);
     const uint64_t warps = pieces < (uint64_t)sm_count * 32 ? pieces : (uint64_t)sm_count * 32;
