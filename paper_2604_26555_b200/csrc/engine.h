@@ -162,7 +162,7 @@ struct SamplerState {
     uint32_t tail_len = 0;
     uint64_t last_m = 0;           // size of the last selection
     bool identity = false;         // last selection = all rows
-    DevBuf window, jp, misc;                    // stream state, jump polynomials
+    DevBuf window, jp, gwin, misc;              // stream state, jump polynomials, generator windows
     // draws are double-buffered: while an epoch trains on buffer `cur`, the
     // next epoch's draws are generated into the other one on `side`
     DevBuf seqb[2], drawsb[2], tailb[2];

@@ -123,34 +123,47 @@ __global__ void __launch_bounds__(kT) k_mt_extend(const uint64_t* __restrict__ w
     }
 }
 
-// Generator g: window at draw g*L (jump polynomial jp[g], g = 0 -> seq itself),
-// then `L` tempered outputs into draws[g*L ..) (bounded by total).  Untempered
-// words at positions [tail0, tail0 + tail_len) (window coordinates of the epoch
-// start: output q = temper(X[q + 312])) are copied to tail[].
-__global__ void __launch_bounds__(kT) k_mt_generate(const uint64_t* __restrict__ seq,
+// Generator g's start window (draw g*L): X[gL .. gL + 312) from the epoch's
+// extended sequence and the jump polynomial jp[g] (g = 0 without jump0: the
+// sequence itself).  One CTA per generator; ~210 KB of shared memory.
+__global__ void __launch_bounds__(kT) k_mt_jump_all(const uint64_t* __restrict__ seq,
                                                     const uint64_t* __restrict__ jp, uint64_t L,
-                                                    uint64_t total, uint64_t* __restrict__ draws,
-                                                    uint64_t tail0, uint32_t tail_len,
-                                                    uint64_t* __restrict__ tail, int jump0) {
+                                                    uint64_t total, uint64_t* __restrict__ wins,
+                                                    int jump0) {
     extern __shared__ uint64_t sm[];
     uint64_t* s_seq = sm;                 // [mt::kSeq]
     uint64_t* s_j = sm + mt::kSeq;        // [312]
-    uint64_t* s_w = s_j + 312;            // [2][312]
-    uint16_t* s_idx = reinterpret_cast<uint16_t*>(s_w + 2 * 312);
+    uint16_t* s_idx = reinterpret_cast<uint16_t*>(s_j + 312);
     __shared__ uint32_t s_wsum[kT / 32];
+    const int k = threadIdx.x;
+    const uint64_t g = blockIdx.x;
+    if (g * L >= total) return;
+    if (g == 0 && !jump0) {
+        if (k < 312) wins[k] = seq[k];
+        return;
+    }
+    for (int i = k; i < mt::kSeq; i += kT) s_seq[i] = seq[i];
+    if (k < 312) s_j[k] = jp[g * 312 + k];
+    __syncthreads();
+    const uint64_t acc = jump_apply(s_seq, s_j, s_idx, s_wsum);
+    if (k < 312) wins[g * 312 + k] = acc;
+}
+
+// Generator g: from its start window, `L` tempered outputs into draws[g*L ..)
+// (bounded by total).  Untempered words at positions [tail0, tail0 + tail_len)
+// (window coordinates of the epoch start: output q = temper(X[q + 312])) are
+// copied to tail[].  5 KB of shared memory: several generator CTAs share an
+// SM with the epoch's other kernels (the draws are made on a side stream).
+__global__ void __launch_bounds__(kT) k_mt_generate(const uint64_t* __restrict__ wins, uint64_t L,
+                                                    uint64_t total, uint64_t* __restrict__ draws,
+                                                    uint64_t tail0, uint32_t tail_len,
+                                                    uint64_t* __restrict__ tail) {
+    __shared__ uint64_t s_w[2 * 312];
     const int k = threadIdx.x;
     const uint64_t g = blockIdx.x;
     const uint64_t q0 = g * L;
     if (q0 >= total) return;
-    if (g == 0 && !jump0) {
-        if (k < 312) s_w[k] = seq[k];
-    } else {
-        for (int i = k; i < mt::kSeq; i += kT) s_seq[i] = seq[i];
-        if (k < 312) s_j[k] = jp[(size_t)g * 312 + k];
-        __syncthreads();
-        const uint64_t acc = jump_apply(s_seq, s_j, s_idx, s_wsum);
-        if (k < 312) s_w[k] = acc;
-    }
+    if (k < 312) s_w[k] = wins[g * 312 + k];
     __syncthreads();
     const uint64_t q1 = min(q0 + L, total);
     int cur = 0;
@@ -661,9 +674,10 @@ int sampler_setup(SamplerState& s, int kind, uint64_t n, uint64_t m, uint64_t se
     if (!s.draws_per_epoch) return 0;
     const uint64_t total = s.draws_per_epoch + kSlack;
     uint64_t G = (total + 65535) / 65536;
-    // one generator CTA per SM (its jump window needs ~210 KB of shared memory):
-    // a second wave would repeat the jump for half the SMs
-    G = std::max<uint64_t>(1, std::min<uint64_t>(G, (uint64_t)sm_count));
+    // two generators per SM: the jumps (one ~210-KB CTA each) run in two
+    // waves, the generation itself in small CTAs that halve the sequential
+    // twist rounds per generator
+    G = std::max<uint64_t>(1, std::min<uint64_t>(G, 2ull * (uint64_t)sm_count));
     const uint64_t L = (total + G - 1) / G;
     s.G = (uint32_t)G;
     s.L = L;
@@ -678,6 +692,7 @@ int sampler_setup(SamplerState& s, int kind, uint64_t n, uint64_t m, uint64_t se
         }
     }
     if (s.jp.ensure(jp.size() * 8) != cudaSuccess) return 4;
+    if (s.gwin.ensure(G * 312 * 8) != cudaSuccess) return 4;
     if (h2d_blocking(s.jp.p, jp.data(), jp.size() * 8) != cudaSuccess) return 4;
     const uint32_t twists = (mt::kSeq - 312 + 311) / 312;
     s.tail0 = s.draws_per_epoch;
@@ -723,19 +738,20 @@ static void generate_draws(SamplerState& s, int b, cudaStream_t st) {
     const uint32_t twists = (mt::kSeq - 312 + 311) / 312;
     TSOM_LAUNCH(k_mt_extend<<<1, kT, 0, st>>>(s.window.as<uint64_t>(), twists,
                                               s.seqb[b].as<uint64_t>()));
-    const size_t smem = (mt::kSeq + 312 + 2 * 312) * 8 + kJumpIdxBytes;
+    const size_t smem = (mt::kSeq + 312) * 8 + kJumpIdxBytes;
     static bool attr = false;
     if (!attr) {
-        cudaFuncSetAttribute(k_mt_generate, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+        cudaFuncSetAttribute(k_mt_jump_all, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
         cudaFuncSetAttribute(k_mt_jump_window, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                             (int)((mt::kSeq + 312) * 8 + kJumpIdxBytes));
+                             (int)smem);
         attr = true;
     }
     const uint64_t total = s.draws_per_epoch + kSlack;
-    TSOM_LAUNCH(k_mt_generate<<<s.G, kT, smem, st>>>(s.seqb[b].as<uint64_t>(), s.jp.as<uint64_t>(),
-                                                     s.L, total, s.drawsb[b].as<uint64_t>(),
-                                                     s.tail0, s.tail_len,
-                                                     s.tailb[b].as<uint64_t>(), s.jump0));
+    TSOM_LAUNCH(k_mt_jump_all<<<s.G, kT, smem, st>>>(s.seqb[b].as<uint64_t>(), s.jp.as<uint64_t>(),
+                                                     s.L, total, s.gwin.as<uint64_t>(), s.jump0));
+    TSOM_LAUNCH(k_mt_generate<<<s.G, kT, 0, st>>>(s.gwin.as<uint64_t>(), s.L, total,
+                                                  s.drawsb[b].as<uint64_t>(), s.tail0, s.tail_len,
+                                                  s.tailb[b].as<uint64_t>()));
 }
 
 // bitmap of `n` rows -> sorted ids in `out`; total count -> misc[3]
@@ -883,7 +899,7 @@ void sampler_pregenerate(SamplerState& s, cudaEvent_t after) {
 
 void sampler_release(SamplerState& s) {
     if (s.side) cudaStreamSynchronize(s.side);
-    for (DevBuf* d : {&s.window, &s.jp, &s.misc, &s.seqb[0], &s.seqb[1], &s.drawsb[0],
+    for (DevBuf* d : {&s.window, &s.jp, &s.gwin, &s.misc, &s.seqb[0], &s.seqb[1], &s.drawsb[0],
                       &s.drawsb[1], &s.tailb[0], &s.tailb[1], &s.err, &s.age, &s.keys, &s.hist, &s.cand, &s.ccnt,
                       &s.first, &s.tidx, &s.bitmap, &s.bcount, &s.sel})
         d->release();
