@@ -1571,9 +1571,14 @@ int tsom_sampler_state(tsom_engine* eng, double* last_error, uint32_t* age) {
         CU(cudaSetDevice(eng->device));
         tsom::SamplerState& smp = eng->sampler;
         REQUIRE(smp.kind == 2, TSOM_ERR_INVALID, "sampler: no adaptive state");
+        tsom::sampler_materialize_ages(smp, eng->sm_count, eng->stream);
         if (last_error)
-            CU(cudaMemcpy(last_error, smp.err.p, smp.n * sizeof(double), cudaMemcpyDeviceToHost));
-        if (age) CU(cudaMemcpy(age, smp.age.p, smp.n * sizeof(uint32_t), cudaMemcpyDeviceToHost));
+            CU(cudaMemcpyAsync(last_error, smp.err.p, smp.n * sizeof(double),
+                               cudaMemcpyDeviceToHost, eng->stream));
+        if (age)
+            CU(cudaMemcpyAsync(age, smp.age.p, smp.n * sizeof(uint32_t), cudaMemcpyDeviceToHost,
+                               eng->stream));
+        CU(cudaStreamSynchronize(eng->stream));
     });
 }
 

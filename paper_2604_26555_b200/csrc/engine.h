@@ -172,6 +172,7 @@ struct SamplerState {
     cudaStream_t side = nullptr;
     cudaEvent_t ev_adv = nullptr, ev_gen = nullptr;
     DevBuf err, age, keys, hist, cand, ccnt;    // adaptive (cand: first-digit bucket)
+    bool age_pending = false;  // observe marked rows; +1 / 0 applied at the next select
     DevBuf first, tidx;                         // random
     DevBuf bitmap, bcount, sel;                 // selection
     // Sharded (a communicator attached): this rank holds rows [off, off + n) of
@@ -191,6 +192,8 @@ int sampler_setup(SamplerState& s, int kind, uint64_t n, uint64_t m, uint64_t se
 int sampler_select(SamplerState& s, uint32_t* out, uint64_t* m_out, int sm_count, cudaStream_t st);
 void sampler_observe(SamplerState& s, const uint32_t* sel, uint64_t m, const double* dist,
                      int sm_count, cudaStream_t st);
+// apply the pending "+1 / observed rows 0" age update (before reading ages)
+void sampler_materialize_ages(SamplerState& s, int sm_count, cudaStream_t st);
 void sampler_release(SamplerState& s);
 // start generating the next epoch's draws on the sampler's side stream once
 // `after` (recorded on the engine stream) completes

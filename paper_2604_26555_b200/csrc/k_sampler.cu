@@ -292,14 +292,23 @@ __global__ void k_rand_pick(const uint32_t* __restrict__ t, const uint32_t* __re
 // select_adaptive
 // ---------------------------------------------------------------------------
 
+// update_adaptive's "every age + 1, the observed rows 0" (sampling.hpp:143-157)
+// is applied lazily: observe only marks its rows (kAgeMark), and the next
+// select reads every age through age_now() and writes the result back while
+// computing the keys, so no separate pass over the N ages is made.
+constexpr uint32_t kAgeMark = 0xFFFFFFFFu;
+__device__ __forceinline__ uint32_t age_now(uint32_t a, int pending) {
+    return pending ? (a == kAgeMark ? 0u : a + 1u) : a;
+}
+
 __global__ void k_adapt_max(const double* __restrict__ err, const uint32_t* __restrict__ age,
-                            uint64_t n, unsigned long long* __restrict__ mx) {
+                            uint64_t n, int pending, unsigned long long* __restrict__ mx) {
     double me = 0.0;
     uint32_t ma = 0;
     for (uint64_t i = blockIdx.x * (uint64_t)blockDim.x + threadIdx.x; i < n;
          i += (uint64_t)gridDim.x * blockDim.x) {
         me = fmax(me, err[i]);
-        ma = max(ma, age[i]);
+        ma = max(ma, age_now(age[i], pending));
     }
     for (int o = 16; o; o >>= 1) {
         me = fmax(me, __shfl_xor_sync(0xffffffffu, me, o));
@@ -328,16 +337,18 @@ __device__ __forceinline__ void hist_add(uint32_t* h, uint32_t bin, bool active)
 }
 
 // sortable 64-bit key: (seen << 63) | bits(key), key >= 0 (sampling.hpp:116-133)
-__global__ void k_adapt_keys(const double* __restrict__ err, const uint32_t* __restrict__ age,
+__global__ void k_adapt_keys(const double* __restrict__ err, uint32_t* __restrict__ age,
                              const uint64_t* __restrict__ draws, uint64_t n, double alpha,
-                             double beta, const unsigned long long* __restrict__ mx,
+                             double beta, int pending, const unsigned long long* __restrict__ mx,
                              unsigned long long* __restrict__ keys) {
     const double max_err = fmax(__longlong_as_double((long long)mx[0]), 1e-12);
     const double max_age = fmax((double)mx[1], 1e-12);
     for (uint64_t i = blockIdx.x * (uint64_t)blockDim.x + threadIdx.x; i < n;
          i += (uint64_t)gridDim.x * blockDim.x) {
         const double e = err[i];
-        const double w = pow_ref(e / max_err, alpha) + pow_ref((double)age[i] / max_age, beta);
+        const uint32_t a = age_now(age[i], pending);
+        if (pending) age[i] = a;
+        const double w = pow_ref(e / max_err, alpha) + pow_ref((double)a / max_age, beta);
         const double u = 1.0 - (double)(draws[i] >> 11) * 0x1.0p-53;
         double key = w > 0.0 ? -log(u) / w : CUDART_INF;
         key = fmax(key, 0.0);  // -log(1) = -0
@@ -499,10 +510,10 @@ __global__ void k_adapt_mark(const unsigned long long* __restrict__ keys, uint64
 }
 
 // update_adaptive: every age + 1, then selected rows get their distance, age 0
-__global__ void k_adapt_age(uint32_t* __restrict__ age, uint64_t n) {
+__global__ void k_adapt_age(uint32_t* __restrict__ age, uint64_t n) {  // materialise
     for (uint64_t i = blockIdx.x * (uint64_t)blockDim.x + threadIdx.x; i < n;
          i += (uint64_t)gridDim.x * blockDim.x)
-        age[i] += 1u;
+        age[i] = age_now(age[i], 1);
 }
 __global__ void k_adapt_observe(const uint32_t* __restrict__ sel, uint64_t m,
                                 const double* __restrict__ dist, double* __restrict__ err,
@@ -511,7 +522,7 @@ __global__ void k_adapt_observe(const uint32_t* __restrict__ sel, uint64_t m,
          k += (uint64_t)gridDim.x * blockDim.x) {
         const uint32_t i = sel[k];
         err[i] = dist[k];
-        age[i] = 0u;
+        age[i] = kAgeMark;  // -> 0 at the next select (age_now)
     }
 }
 
@@ -820,7 +831,9 @@ int sampler_select(SamplerState& s, uint32_t* out, uint64_t* m_out, int sm_count
         const uint64_t m = std::min(s.m, gN);
         cudaMemcpyAsync(misc, &gN, 8, cudaMemcpyHostToDevice, st);  // delta = gN draws
         auto* mx = reinterpret_cast<unsigned long long*>(misc + 4);
-        TSOM_LAUNCH(k_adapt_max<<<grid, 256, 0, st>>>(s.err.as<double>(), s.age.as<uint32_t>(), n, mx));
+        const int pending = s.age_pending ? 1 : 0;
+        TSOM_LAUNCH(k_adapt_max<<<grid, 256, 0, st>>>(s.err.as<double>(), s.age.as<uint32_t>(), n,
+                                                      pending, mx));
         if (s.sharded) ok &= s.allreduce(mx, 2, 1);  // the maxima over all rows
         auto* rs = reinterpret_cast<unsigned long long*>(misc + 6);
         const unsigned long long st0[2] = {0ULL, (unsigned long long)m};
@@ -830,7 +843,8 @@ int sampler_select(SamplerState& s, uint32_t* out, uint64_t* m_out, int sm_count
         uint32_t* ccnt = s.ccnt.as<uint32_t>();
         const uint64_t chunk = (n + kCompactBlocks - 1) / kCompactBlocks;
         TSOM_LAUNCH(k_adapt_keys<<<grid, 256, 0, st>>>(s.err.as<double>(), s.age.as<uint32_t>(),
-                                                       draws, n, s.alpha, s.beta, mx, keys));
+                                                       draws, n, s.alpha, s.beta, pending, mx, keys));
+        s.age_pending = false;  // the keys pass wrote the ages back
         // digits of the 64-bit key: bits 52-63, 40-51, 28-39, 16-27, 4-15, 0-3.
         // Digit 0 scans every key, digit 1 comes with the compaction of digit
         // 0's bucket, digits 2-5 scan only that bucket.  Sharded: each digit
@@ -914,10 +928,20 @@ void sampler_observe(SamplerState& s, const uint32_t* sel, uint64_t m, const dou
     if (s.kind != 2) return;
     const unsigned grid = (unsigned)std::max<uint64_t>(
         1, std::min<uint64_t>((s.n + 255) / 256, (uint64_t)sm_count * 16));
-    TSOM_LAUNCH(k_adapt_age<<<grid, 256, 0, st>>>(s.age.as<uint32_t>(), s.n));
+    if (s.age_pending)  // two observes without a select in between
+        TSOM_LAUNCH(k_adapt_age<<<grid, 256, 0, st>>>(s.age.as<uint32_t>(), s.n));
     if (m)
         TSOM_LAUNCH(k_adapt_observe<<<grid, 256, 0, st>>>(sel, m, dist, s.err.as<double>(),
                                                           s.age.as<uint32_t>()));
+    s.age_pending = true;
+}
+
+void sampler_materialize_ages(SamplerState& s, int sm_count, cudaStream_t st) {
+    if (s.kind != 2 || !s.age_pending) return;
+    const unsigned grid = (unsigned)std::max<uint64_t>(
+        1, std::min<uint64_t>((s.n + 255) / 256, (uint64_t)sm_count * 16));
+    TSOM_LAUNCH(k_adapt_age<<<grid, 256, 0, st>>>(s.age.as<uint32_t>(), s.n));
+    s.age_pending = false;
 }
 
 }  // namespace tsom
