@@ -1485,6 +1485,7 @@ int tsom_sampler_init(tsom_engine* eng, int kind, uint64_t m, uint64_t seed, dou
                       double beta) {
     return guarded(eng, [&] {
         CU(cudaSetDevice(eng->device));
+        CU(cudaStreamSynchronize(eng->stream));  // no queued epoch still uses the old state
         REQUIRE(kind >= 0 && kind <= 2, TSOM_ERR_INVALID, "unknown sampling kind");
         REQUIRE(eng->n_rows >= 1, TSOM_ERR_INVALID, "sampler: N must be >= 1 (bind data first)");
         REQUIRE(kind == 0 || m >= 1, TSOM_ERR_INVALID, "select_random: m must be >= 1");

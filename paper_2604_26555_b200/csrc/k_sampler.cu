@@ -648,6 +648,7 @@ int sampler_setup(SamplerState& s, int kind, uint64_t n, uint64_t m, uint64_t se
                   double beta, int sm_count) {
     if (s.side) cudaStreamSynchronize(s.side);  // no generation of a previous setup in flight
     s.pre = false;
+    s.age_pending = false;
     s.want_gen = false;
     s.kind = kind;
     s.n = n;
