@@ -509,12 +509,17 @@ __global__ void __launch_bounds__(kTmaWarps * 32, 2) k_gather_tma(
                 }
                 if (want_dist && lane < rows_m) {
                     // lane = row: exact FP64 distance to w_b, features in order
-                    const float* xr =
-                        reinterpret_cast<const float*>(bs + lane * slot + ((om >> lane) & 1u) * 8);
+                    // 8-byte reads (d is even): the 208-B slot stride then costs a
+                    // 2-way bank conflict instead of the 4-way of 4-byte reads
+                    const float2* xr = reinterpret_cast<const float2*>(
+                        bs + lane * slot + ((om >> lane) & 1u) * 8);
                     double d2 = 0.0;
-                    for (uint32_t k = 0; k < D; ++k) {
-                        const double dd = (double)xr[k] - wsm[warp][k];
-                        d2 = fma(dd, dd, d2);
+                    for (uint32_t k2 = 0; k2 < D / 2; ++k2) {
+                        const float2 v = xr[k2];
+                        const double d0 = (double)v.x - wsm[warp][2 * k2];
+                        d2 = fma(d0, d0, d2);
+                        const double d1 = (double)v.y - wsm[warp][2 * k2 + 1];
+                        d2 = fma(d1, d1, d2);
                     }
                     const double dist = sqrt(d2);
                     if (dist_out) dist_out[pos[m]] = dist;
