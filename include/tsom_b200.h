@@ -150,6 +150,17 @@ int tsom_set_topology_distance(tsom_engine* eng, const double* dist);
  * (read with tsom_get_codebook). */
 int tsom_train_epoch(tsom_engine* eng, double eta, double sigma, double momentum,
                      uint32_t flags);
+/* n_epochs consecutive tsom_train_epoch calls (the epoch loop of
+ * train_with_executor, trainer.hpp:486-520, with the schedules eta[t], sigma[t]
+ * precomputed by the caller) enqueued back to back with no host round trip
+ * between epochs.  The per-epoch checks run on the device: after a failing
+ * epoch the later ones leave the weights unchanged, and the call returns
+ * TSOM_ERR_NUMERICAL with *failed_epoch (optional) = the failing epoch.
+ * tsom_last_timing_detail then reports the last epoch's phases and the mean
+ * K1 time of the call. */
+int tsom_train_epochs(tsom_engine* eng, uint32_t n_epochs, const double* eta,
+                      const double* sigma, double momentum, uint32_t flags,
+                      uint32_t* failed_epoch);
 /* Topology refresh on the device (refresh_topology topology.hpp:439-451) from
  * the engine's current codebook: FP64 Gram (pairwise_sq_dists :81-108), then
  * kind 2 = MST (build_mst :192-220) or 3 = RNG (build_rng_graph :229-258), then

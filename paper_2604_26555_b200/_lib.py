@@ -41,7 +41,7 @@ EXPORTS = [
     "tsom_stream", "tsom_last_timing_detail", "tsom_kernel_launches", "tsom_refresh_topology",
     "tsom_pairwise_sq_dists", "tsom_bind_shards", "tsom_active_bmu_kernel",
     "tsom_sampler_init", "tsom_sampler_select", "tsom_sampler_observe", "tsom_sampler_state",
-    "tsom_mt_selftest", "tsom_release_cached_memory",
+    "tsom_mt_selftest", "tsom_release_cached_memory", "tsom_train_epochs",
 ]
 
 SAMPLER_KINDS = {"full": 0, "random": 1, "adaptive": 2}  # SamplingKind, sampling.hpp:163
@@ -107,6 +107,7 @@ def load():
     L.tsom_qe.argtypes = [_vp, _vp, u64, C.POINTER(C.c_double), C.POINTER(u64)]
     L.tsom_set_topology_distance.argtypes = [_vp, _vp]
     L.tsom_train_epoch.argtypes = [_vp, C.c_double, C.c_double, C.c_double, u32]
+    L.tsom_train_epochs.argtypes = [_vp, u32, _vp, _vp, C.c_double, u32, C.POINTER(u32)]
     L.tsom_sampler_init.argtypes = [_vp, i32, u64, u64, C.c_double, C.c_double]
     L.tsom_sampler_select.argtypes = [_vp, _vp, C.POINTER(u64)]
     L.tsom_sampler_observe.argtypes = [_vp, _vp]
@@ -283,6 +284,19 @@ class Engine:
         (sampler_init) pick the rows and, if adaptive, observe their distances."""
         self._check(self.L.tsom_train_epoch(self.h, float(eta), float(sigma), float(momentum),
                                             (1 if use_momentum else 0) | (2 if sampled else 0)))
+
+    def train_epochs(self, etas, sigmas, momentum: float = 0.0, use_momentum: bool = False,
+                     sampled: bool = False):
+        """len(etas) device-resident epochs back to back (no host round trip
+        between them); a numerical fault names the failing epoch."""
+        eta = np.ascontiguousarray(etas, np.float64)
+        sig = np.ascontiguousarray(sigmas, np.float64)
+        assert eta.shape == sig.shape and eta.ndim == 1 and len(eta) >= 1
+        failed = C.c_uint32()
+        self._check(self.L.tsom_train_epochs(self.h, len(eta), _ptr(eta), _ptr(sig),
+                                             float(momentum),
+                                             (1 if use_momentum else 0) | (2 if sampled else 0),
+                                             C.byref(failed)))
 
     # --- device sampler (sampling.hpp:183-221) -------------------------------
     def sampler_init(self, kind, m: int, seed: int, alpha: float = 1.0, beta: float = 1.0):

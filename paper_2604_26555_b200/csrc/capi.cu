@@ -268,6 +268,13 @@ void prep_codebook(Engine* eng) {
     eng->codebook_prepped = true;
 }
 
+// the K1 main-pass events of the current epoch (per-epoch pairs during
+// tsom_train_epochs, else ev[8] / ev[9])
+cudaEvent_t k1_event(Engine* eng, int end) {
+    if (eng->k1_slot >= 0) return eng->k1_ev[2 * (size_t)eng->k1_slot + end];
+    return eng->ev[8 + end];
+}
+
 // K1 + exact re-check over rows `x` (selection `sel` of length n, or first n rows).
 // x2max: max ||x||^2 over these rows (device; picks the FP16 operand scale).
 // `tiles` = pre-split tcgen05 A tiles for exactly these n rows, built with the
@@ -302,13 +309,13 @@ void run_bmu(Engine* eng, const float* x, const uint32_t* sel, uint64_t n, const
         CU(eng->tmask.ensure(std::max<uint64_t>(n, 1) * sizeof(uint32_t)));
         CU(cudaMemsetAsync(eng->ties.p, 0, sizeof(uint32_t), eng->stream));
         const float* w2 = eng->w2max.as<float>();
-        CU(cudaEventRecord(eng->ev[8], eng->stream));
+        CU(cudaEventRecord(k1_event(eng, 0), eng->stream));
         CU(tsom::launch_bmu_tc(kind, tiles, n, nullptr, false, eng->P, eng->D, eng->wsplit.p,
                                tiles_xn2, w2, scale, win, nullptr, eng->part.as<float>(),
                                eng->sm_count, eng->smem_optin, eng->stream));
-        CU(cudaEventRecord(eng->ev[9], eng->stream));
+        CU(cudaEventRecord(k1_event(eng, 1), eng->stream));
         eng->k1_timed = true;
-        tsom::sampler_pregenerate(eng->sampler, eng->ev[9]);
+        tsom::sampler_pregenerate(eng->sampler, k1_event(eng, 1));
         tsom::launch_merge_fast(eng->part.as<float>(), n, groups, 1, gn, tiles_xn2,
                                 w2, scale, win,
                                 eng->bmu.as<uint32_t>(), eng->ties.as<uint32_t>(),
@@ -337,15 +344,15 @@ void run_bmu(Engine* eng, const float* x, const uint32_t* sel, uint64_t n, const
                                     eng->w.as<float>(), eng->D, eng->bmu.as<uint32_t>(),
                                     eng->flags.as<uint32_t>(), eng->stream);
     } else {
-        CU(cudaEventRecord(eng->ev[8], eng->stream));
+        CU(cudaEventRecord(k1_event(eng, 0), eng->stream));
         // the FP32 accumulation bound grows with the d+1 terms of each dot product
         const double tau_s = eng->tau_simt * std::max(1.0, (eng->D + 1) / 51.0);
         tsom::launch_bmu_simt(x, sel, n, eng->D, eng->wt.as<float>(), eng->P, ppad(eng), x2max,
                               eng->w2max.as<float>(), (float)tau_s, eng->bmu.as<uint32_t>(),
                               eng->flags.as<uint32_t>(), eng->sm_count, eng->stream);
-        CU(cudaEventRecord(eng->ev[9], eng->stream));
+        CU(cudaEventRecord(k1_event(eng, 1), eng->stream));
         eng->k1_timed = true;
-        tsom::sampler_pregenerate(eng->sampler, eng->ev[9]);
+        tsom::sampler_pregenerate(eng->sampler, k1_event(eng, 1));
     }
     CU(cudaGetLastError());
     tsom::launch_rescan(x, sel, eng->w.as<float>(), eng->P, eng->D, eng->flags.as<uint32_t>(), n,
@@ -867,11 +874,12 @@ int tsom_destroy(tsom_engine* eng) {
                       &eng->topo_buf[4], &eng->topo_buf[5], &eng->topo_buf[6], &eng->topo_buf[7],
                       &eng->topo_buf[8], &eng->topo_buf[9], &eng->topo_buf[10], &eng->topo_buf[11],
                       &eng->topo_buf[12], &eng->topo_buf[13], &eng->topo_buf[14], &eng->U, &eng->H, &eng->status, &eng->smooth_scratch,
-                      &eng->stage[0], &eng->stage[1]})
+                      &eng->stage[0], &eng->stage[1], &eng->dead})
         b->release(true);
     for (auto& ev : eng->ev)
         if (ev) cudaEventDestroy(ev);
     if (eng->hstat) cudaFreeHost(eng->hstat);
+    for (cudaEvent_t e : eng->k1_ev) cudaEventDestroy(e);
     if (eng->stream) cudaStreamDestroy(eng->stream);
     if (eng->copy_stream) cudaStreamDestroy(eng->copy_stream);
     delete eng;
@@ -1595,67 +1603,75 @@ int tsom_release_cached_memory(int device) {
     return TSOM_OK;
 }
 
+// One device-resident epoch (tsom_train_epoch), enqueued on the engine stream
+// without waiting for it; dead (optional): the multi-epoch failure record.
+static void train_epoch_enqueue(Engine* eng, double eta, double sigma, double momentum, uint32_t flags,
+                         const int* dead) {
+    CU(cudaSetDevice(eng->device));
+    REQUIRE(eng->topo_set, TSOM_ERR_INVALID, "train_epoch: topology distance not set");
+    REQUIRE(sigma > 0.0, TSOM_ERR_INVALID, "influence_matrix: sigma must be > 0");
+    const bool momentum_on = (flags & 1u) != 0;
+    // influence(sigma) on the device (topology.hpp:342-364); the device
+    // path keys its cache on sigma exactly like influence_cache_key (:399-401)
+    const int64_t key = (int64_t)std::llround(sigma * 1e6);
+    if (!(eng->infl_set && eng->infl_key == key)) {
+        const double inv = 1.0 / (2.0 * sigma * sigma);
+        tsom::launch_influence(eng->topo_dist.as<double>(), (size_t)eng->P * eng->P, inv,
+                               eng->infl.as<double>(), eng->stream);
+        CU(cudaGetLastError());
+        eng->infl_key = key;
+        eng->infl_set = true;
+        eng->max_h = 1.0;
+    }
+    prep_codebook(eng);
+    // flags bit 1: the device sampler picks this epoch's rows (select ->
+    // epoch over them -> observe), sampling.hpp:197-211
+    tsom::SamplerState& smp = eng->sampler;
+    const bool sampled = (flags & 2u) != 0;
+    REQUIRE(!sampled || smp.kind >= 0, TSOM_ERR_INVALID,
+            "train_epoch: no device sampler (tsom_sampler_init)");
+    uint64_t m = eng->n_rows;
+    bool ident = true;
+    std::vector<uint32_t> host_sel;
+    eng->sample_timed = sampled;
+    if (sampled) {
+        CU(cudaEventRecord(eng->ev[11], eng->stream));
+        ident = sampler_pick(eng, &m);
+        if (!ident && eng->streamed) {
+            host_sel.resize(m);
+            CU(cudaMemcpyAsync(host_sel.data(), smp.sel.p, m * sizeof(uint32_t),
+                               cudaMemcpyDeviceToHost, eng->stream));
+            CU(cudaStreamSynchronize(eng->stream));
+        }
+    }
+    const bool want_dist = sampled && smp.kind == 2;
+    if (ident)
+        accumulate_epoch(eng, nullptr, eng->n_rows, want_dist, false, true);
+    else if (eng->streamed)
+        accumulate_epoch(eng, host_sel.data(), m, want_dist, false, true);
+    else
+        accumulate_epoch(eng, nullptr, m, want_dist, false, true, smp.sel.as<uint32_t>());
+    if (want_dist) {
+        if (ident) fill_identity(eng, eng->n_rows);
+        tsom::sampler_observe(smp, ident ? smp.sel.as<uint32_t>() : smp.sel.as<uint32_t>(), m,
+                              eng->dist.as<double>(), eng->sm_count, eng->stream);
+    }
+    smooth(eng, eta);
+    tsom::launch_status_reset(eng->status.as<int>(), eng->stream);
+    tsom::launch_apply_update_guarded(eng->w.as<float>(), eng->prev.as<float>(), eng->P,
+                                      eng->D, eng->U.as<double>(), eng->H.as<double>(),
+                                      momentum_on, momentum, eng->status.as<int>(), dead,
+                                      eng->stream);
+    CU(cudaGetLastError());
+    CU(cudaEventRecord(eng->ev[10], eng->stream));
+    eng->update_timed = true;
+    eng->codebook_prepped = false;
+    prep_codebook(eng);
+}
+
 int tsom_train_epoch(tsom_engine* eng, double eta, double sigma, double momentum, uint32_t flags) {
     return guarded(eng, [&] {
-        CU(cudaSetDevice(eng->device));
-        REQUIRE(eng->topo_set, TSOM_ERR_INVALID, "train_epoch: topology distance not set");
-        REQUIRE(sigma > 0.0, TSOM_ERR_INVALID, "influence_matrix: sigma must be > 0");
-        const bool momentum_on = (flags & 1u) != 0;
-        // influence(sigma) on the device (topology.hpp:342-364); the device
-        // path keys its cache on sigma exactly like influence_cache_key (:399-401)
-        const int64_t key = (int64_t)std::llround(sigma * 1e6);
-        if (!(eng->infl_set && eng->infl_key == key)) {
-            const double inv = 1.0 / (2.0 * sigma * sigma);
-            tsom::launch_influence(eng->topo_dist.as<double>(), (size_t)eng->P * eng->P, inv,
-                                   eng->infl.as<double>(), eng->stream);
-            CU(cudaGetLastError());
-            eng->infl_key = key;
-            eng->infl_set = true;
-            eng->max_h = 1.0;
-        }
-        prep_codebook(eng);
-        // flags bit 1: the device sampler picks this epoch's rows (select ->
-        // epoch over them -> observe), sampling.hpp:197-211
-        tsom::SamplerState& smp = eng->sampler;
-        const bool sampled = (flags & 2u) != 0;
-        REQUIRE(!sampled || smp.kind >= 0, TSOM_ERR_INVALID,
-                "train_epoch: no device sampler (tsom_sampler_init)");
-        uint64_t m = eng->n_rows;
-        bool ident = true;
-        std::vector<uint32_t> host_sel;
-        eng->sample_timed = sampled;
-        if (sampled) {
-            CU(cudaEventRecord(eng->ev[11], eng->stream));
-            ident = sampler_pick(eng, &m);
-            if (!ident && eng->streamed) {
-                host_sel.resize(m);
-                CU(cudaMemcpyAsync(host_sel.data(), smp.sel.p, m * sizeof(uint32_t),
-                                   cudaMemcpyDeviceToHost, eng->stream));
-                CU(cudaStreamSynchronize(eng->stream));
-            }
-        }
-        const bool want_dist = sampled && smp.kind == 2;
-        if (ident)
-            accumulate_epoch(eng, nullptr, eng->n_rows, want_dist, false, true);
-        else if (eng->streamed)
-            accumulate_epoch(eng, host_sel.data(), m, want_dist, false, true);
-        else
-            accumulate_epoch(eng, nullptr, m, want_dist, false, true, smp.sel.as<uint32_t>());
-        if (want_dist) {
-            if (ident) fill_identity(eng, eng->n_rows);
-            tsom::sampler_observe(smp, ident ? smp.sel.as<uint32_t>() : smp.sel.as<uint32_t>(), m,
-                                  eng->dist.as<double>(), eng->sm_count, eng->stream);
-        }
-        smooth(eng, eta);
-        tsom::launch_status_reset(eng->status.as<int>(), eng->stream);
-        tsom::launch_apply_update(eng->w.as<float>(), eng->prev.as<float>(), eng->P, eng->D,
-                                  eng->U.as<double>(), eng->H.as<double>(), momentum_on, momentum,
-                                  eng->status.as<int>(), eng->stream);
-        CU(cudaGetLastError());
-        CU(cudaEventRecord(eng->ev[10], eng->stream));
-        eng->update_timed = true;
-        eng->codebook_prepped = false;
-        prep_codebook(eng);
+        train_epoch_enqueue(eng, eta, sigma, momentum, flags, nullptr);
         CU(cudaMemcpyAsync(eng->hstat + 2, eng->status.p, sizeof(int), cudaMemcpyDeviceToHost,
                            eng->stream));
         enqueue_guard_read(eng);
@@ -1667,6 +1683,66 @@ int tsom_train_epoch(tsom_engine* eng, double eta, double sigma, double momentum
         check_term_guard(eng, eta);
         REQUIRE(st == INT_MAX, TSOM_ERR_NUMERICAL,
                 "numerical fault: non-finite weight update at node " + std::to_string(st));
+    });
+}
+
+int tsom_train_epochs(tsom_engine* eng, uint32_t n_epochs, const double* eta,
+                      const double* sigma, double momentum, uint32_t flags,
+                      uint32_t* failed_epoch) {
+    return guarded(eng, [&] {
+        CU(cudaSetDevice(eng->device));
+        REQUIRE(n_epochs >= 1 && eta && sigma, TSOM_ERR_INVALID,
+                "train_epochs: need n >= 1 and eta / sigma arrays");
+        if (failed_epoch) *failed_epoch = UINT32_MAX;
+        CU(eng->dead.ensure(4 * sizeof(int)));
+        CU(cudaMemsetAsync(eng->dead.p, 0, 4 * sizeof(int), eng->stream));
+        while (eng->k1_ev.size() < 2 * (size_t)n_epochs) {
+            cudaEvent_t ev;
+            CU(cudaEventCreate(&ev));
+            eng->k1_ev.push_back(ev);
+        }
+        int* dead = eng->dead.as<int>();
+        struct SlotReset {
+            Engine* e;
+            ~SlotReset() { e->k1_slot = -1; }
+        } reset{eng};
+        for (uint32_t t = 0; t < n_epochs; ++t) {
+            eng->k1_slot = (int)t;
+            eng->k1_timed = false;
+            train_epoch_enqueue(eng, eta[t], sigma[t], momentum, flags, dead);
+            tsom::launch_epoch_guard(eng->status.as<int>(), eng->x2max.as<float>(),
+                                     eng->w2max.as<float>(), eta[t], eng->max_h, t, dead,
+                                     eng->stream);
+            CU(cudaGetLastError());
+        }
+        const bool k1_all = eng->k1_timed;  // every epoch ran the tcgen05 main pass
+        eng->k1_slot = -1;
+        CU(cudaMemcpyAsync(eng->hstat + 5, dead, 3 * sizeof(int), cudaMemcpyDeviceToHost,
+                           eng->stream));
+        CU(cudaStreamSynchronize(eng->stream));
+        finish_recheck(eng);
+        record_timing(eng);  // phases of the last epoch
+        eng->t_k1 = 0.0f;
+        if (k1_all) {
+            float sum = 0.0f;
+            for (uint32_t t = 0; t < n_epochs; ++t) {
+                float ms = 0.0f;
+                cudaEventElapsedTime(&ms, eng->k1_ev[2 * (size_t)t], eng->k1_ev[2 * (size_t)t + 1]);
+                sum += ms;
+            }
+            eng->t_k1 = sum / (float)n_epochs;  // mean main-pass K1 time of the call
+        }
+        int rec[3];
+        std::memcpy(rec, eng->hstat + 5, sizeof(rec));
+        if (rec[0]) {
+            if (failed_epoch) *failed_epoch = (uint32_t)(rec[0] - 1);
+            REQUIRE(rec[1] != 1, TSOM_ERR_NUMERICAL,
+                    "numerical fault: non-finite weight update at node " + std::to_string(rec[2]) +
+                        " (epoch " + std::to_string(rec[0] - 1) + ")");
+            REQUIRE(false, TSOM_ERR_NUMERICAL,
+                    "numerical fault: accumulation term out of range (|term| >= 2^22) (epoch " +
+                        std::to_string(rec[0] - 1) + ")");
+        }
     });
 }
 

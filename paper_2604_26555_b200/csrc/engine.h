@@ -279,6 +279,12 @@ struct Engine {
     };
     std::vector<ShardFile> shards;  // FSOMSHRD files (dataset.hpp:171-344)
     cudaEvent_t ev[12] = {};  // 0 start, 1 bmu end, 6 accum end, 7 smooth end, 8/9 K1 kernel, 10 update end
+    // tsom_train_epochs: per-epoch K1 start/end events (the main pass of epoch t
+    // records k1_ev[2t], k1_ev[2t+1] instead of ev[8], ev[9]) and the device
+    // failure record [epoch + 1, kind (1 non-finite update, 2 term guard), node]
+    std::vector<cudaEvent_t> k1_ev;
+    int k1_slot = -1;
+    DevBuf dead;
     uint64_t last_recheck = 0;
     std::vector<uint32_t> chunk_counts;  // per-chunk re-check counts (streamed epochs)
     // pinned per-epoch status words, read back asynchronously before the one
@@ -384,6 +390,13 @@ void launch_apply_update(float* w, float* prev, uint32_t P, uint32_t D, const do
                          cudaStream_t st);
 // status[0] = INT_MAX (no failing node) before launch_apply_update
 void launch_status_reset(int* status, cudaStream_t st);
+// multi-epoch runs: skip the update once dead[0] != 0; after an epoch, record
+// a failed update (status) or a violated term guard in dead[]
+void launch_apply_update_guarded(float* w, float* prev, uint32_t P, uint32_t D, const double* U,
+                                 const double* H, bool use_momentum, double momentum, int* status,
+                                 const int* dead, cudaStream_t st);
+void launch_epoch_guard(const int* status, const float* x2max, const float* w2max, double eta,
+                        double max_h, uint32_t epoch, int* dead, cudaStream_t st);
 // influence_matrix (topology.hpp:342-364) from a P x P distance matrix
 void launch_influence(const double* dist, size_t n, double inv_two_sigma_sq, double* out,
                       cudaStream_t st);

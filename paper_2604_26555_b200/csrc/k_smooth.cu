@@ -125,9 +125,10 @@ size_t smooth_scratch_doubles(uint32_t P, uint32_t D) {
 __global__ void k_apply_update(float* __restrict__ w, float* __restrict__ prev, uint32_t P,
                                uint32_t D, const double* __restrict__ U,
                                const double* __restrict__ H, int use_momentum, double momentum,
-                               int* __restrict__ status) {
+                               int* __restrict__ status, const int* __restrict__ dead) {
     const size_t e = blockIdx.x * (size_t)blockDim.x + threadIdx.x;
     if (e >= (size_t)P * D) return;
+    if (dead && *dead) return;  // an earlier epoch of this multi-epoch run failed
     const uint32_t j = (uint32_t)(e / D);
     const double h = H[j];
     if (h < 1e-12) {
@@ -151,7 +152,40 @@ void launch_apply_update(float* w, float* prev, uint32_t P, uint32_t D, const do
     const size_t n = (size_t)P * D;
     TSOM_LAUNCH(k_apply_update<<<(unsigned)((n + 255) / 256), 256, 0, st>>>(w, prev, P, D, U, H,
                                                                 use_momentum ? 1 : 0, momentum,
-                                                                status));
+                                                                status, nullptr));
+}
+
+void launch_apply_update_guarded(float* w, float* prev, uint32_t P, uint32_t D, const double* U,
+                                 const double* H, bool use_momentum, double momentum, int* status,
+                                 const int* dead, cudaStream_t st) {
+    const size_t n = (size_t)P * D;
+    TSOM_LAUNCH(k_apply_update<<<(unsigned)((n + 255) / 256), 256, 0, st>>>(w, prev, P, D, U, H,
+                                                                use_momentum ? 1 : 0, momentum,
+                                                                status, dead));
+}
+
+// the host checks of tsom_train_epoch (non-finite update; |term| bound of
+// accum.hpp:35: |eta| max_h (||x|| + ||w||) < 2^22), evaluated on the device
+__global__ void k_epoch_guard(const int* __restrict__ status, const float* __restrict__ x2max,
+                              const float* __restrict__ w2max, double eta, double max_h,
+                              uint32_t epoch, int* __restrict__ dead) {
+    if (dead[0]) return;
+    if (*status != INT_MAX) {
+        dead[0] = (int)epoch + 1;
+        dead[1] = 1;
+        dead[2] = *status;
+        return;
+    }
+    const double bound = fabs(eta) * max_h * (sqrt((double)*x2max) + sqrt((double)*w2max));
+    if (!(max_h < 4194304.0 && bound < 4194304.0)) {
+        dead[0] = (int)epoch + 1;
+        dead[1] = 2;
+    }
+}
+
+void launch_epoch_guard(const int* status, const float* x2max, const float* w2max, double eta,
+                        double max_h, uint32_t epoch, int* dead, cudaStream_t st) {
+    TSOM_LAUNCH(k_epoch_guard<<<1, 1, 0, st>>>(status, x2max, w2max, eta, max_h, epoch, dead));
 }
 
 __global__ void k_status_reset(int* status) { *status = INT_MAX; }

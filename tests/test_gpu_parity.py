@@ -547,3 +547,59 @@ def test_pageable_bind_staging_and_gather_variants(pkg, oracle_port):
         e.set_option(97, 0)
         e.close()
     _lib.release_cached_memory(0)
+
+
+@pytest.mark.parametrize("sampled", [False, True])
+def test_train_epochs_equals_epoch_loop(pkg, oracle_port, sampled):
+    # tsom_train_epochs (no host round trip between epochs) against the same
+    # schedule through tsom_train_epoch one call at a time: identical codebooks
+    n, p, d = 60_000, 64, 20
+    x = oracle_port.synth_gmm(n, d, 2615)
+    w0 = x[np.linspace(0, n - 1, p).astype(int)].copy()
+    dist = oracle_port.lattice_dist("hex", 8, 8)
+    etas = [0.5 - 0.04 * t for t in range(8)]
+    sigmas = [3.0 - 0.3 * t for t in range(8)]
+    out = []
+    for multi in (False, True):
+        e = pkg.Engine(p, d)
+        e.bind(x)
+        e.set_codebook(w0)
+        e.set_topology_distance(dist)
+        if sampled:
+            e.sampler_init("adaptive", n // 10, 77)
+        if multi:
+            e.train_epochs(etas, sigmas, sampled=sampled)
+        else:
+            for eta, sig in zip(etas, sigmas):
+                e.train_epoch(eta, sig, sampled=sampled)
+        out.append(e.get_codebook())
+        e.close()
+    assert np.array_equal(out[0], out[1])
+
+
+def test_train_epochs_reports_the_failing_epoch(pkg, oracle_port):
+    # a schedule whose third epoch violates the accumulation-term guard: the
+    # multi-epoch call names epoch 2, and the codebook is the one the
+    # per-epoch loop leaves when it raises at the same epoch
+    n, p, d = 20_000, 16, 8
+    x = oracle_port.synth_gmm(n, d, 2616)
+    w0 = x[np.linspace(0, n - 1, p).astype(int)].copy()
+    dist = oracle_port.lattice_dist("rect", 4, 4)
+    etas, sigmas = [0.5, 0.4, 1e7, 0.3], [2.0, 1.8, 1.6, 1.4]
+    books = []
+    for multi in (False, True):
+        e = pkg.Engine(p, d)
+        e.bind(x)
+        e.set_codebook(w0)
+        e.set_topology_distance(dist)
+        if multi:
+            with pytest.raises(pkg.NumericalFault, match=r"term out of range.*\(epoch 2\)"):
+                e.train_epochs(etas, sigmas)
+        else:
+            e.train_epoch(etas[0], sigmas[0])
+            e.train_epoch(etas[1], sigmas[1])
+            with pytest.raises(pkg.NumericalFault, match="term out of range"):
+                e.train_epoch(etas[2], sigmas[2])
+        books.append(e.get_codebook())
+        e.close()
+    assert np.array_equal(books[0], books[1])
