@@ -187,21 +187,33 @@ def train_resident(cfg: ResidentConfig, engine: Engine, init_weights=None, log_q
     if sampled:
         engine.sampler_init(cfg.sampling, resolve_budget(cfg, engine.rows), cfg.seed, cfg.alpha,
                             cfg.beta)
+    # the schedules and the refresh points depend only on t, so the epochs
+    # between two refreshes (all of them for lattices) go to the device in one
+    # tsom_train_epochs call; with log_qe every epoch is its own call
     log = []
     for t in range(cfg.n_iters):
-        refreshed = False
-        if refresh is not None and refresh.should_refresh(t):
-            engine.refresh_topology(cfg.topology)  # from the current device codebook
+        refreshed = refresh is not None and refresh.should_refresh(t)
+        if refreshed:
             refresh.mark(t)
-            refreshed = True
-        eta = schedule_value(cfg.eta0, cfg.lr_decay, t, cfg.n_iters, 1e-4)
-        sigma = schedule_value(sigma0, cfg.radius_decay, t, cfg.n_iters, cfg.sigma_min)
-        engine.train_epoch(eta, sigma, cfg.momentum, cfg.use_momentum, sampled=sampled)
-        entry = {"iter": t, "eta": eta, "sigma": sigma, "refreshed": refreshed}
+        log.append({"iter": t, "refreshed": refreshed,
+                    "eta": schedule_value(cfg.eta0, cfg.lr_decay, t, cfg.n_iters, 1e-4),
+                    "sigma": schedule_value(sigma0, cfg.radius_decay, t, cfg.n_iters,
+                                            cfg.sigma_min)})
+    t = 0
+    while t < cfg.n_iters:
+        if log[t]["refreshed"]:
+            engine.refresh_topology(cfg.topology)  # from the current device codebook
+        t1 = t + 1
+        if not log_qe:
+            while t1 < cfg.n_iters and not log[t1]["refreshed"]:
+                t1 += 1
+        seg = log[t:t1]
+        engine.train_epochs([e["eta"] for e in seg], [e["sigma"] for e in seg], cfg.momentum,
+                            cfg.use_momentum, sampled=sampled)
         if log_qe:
             s, c = engine.qe()
-            entry["qe_train"] = s / c
-        log.append(entry)
+            log[t]["qe_train"] = s / c
+        t = t1
     return log
 
 

@@ -787,6 +787,7 @@ void record_timing(Engine* eng) {
     cudaEventElapsedTime(&eng->t_accum, eng->ev[1], eng->ev[6]);
     cudaEventElapsedTime(&eng->t_smooth, eng->ev[6], eng->ev[7]);
     cudaEventElapsedTime(&eng->t_total, eng->ev[0], eng->ev[7]);
+    cudaGetLastError();  // an event pair that was not recorded must not poison later calls
 }
 
 }  // namespace
@@ -1721,7 +1722,8 @@ int tsom_train_epochs(tsom_engine* eng, uint32_t n_epochs, const double* eta,
                            eng->stream));
         CU(cudaStreamSynchronize(eng->stream));
         finish_recheck(eng);
-        record_timing(eng);  // phases of the last epoch
+        eng->k1_timed = false;  // ev[8] / ev[9] were not recorded: per-epoch events below
+        record_timing(eng);     // phases of the last epoch
         eng->t_k1 = 0.0f;
         if (k1_all) {
             float sum = 0.0f;
@@ -1731,6 +1733,7 @@ int tsom_train_epochs(tsom_engine* eng, uint32_t n_epochs, const double* eta,
                 sum += ms;
             }
             eng->t_k1 = sum / (float)n_epochs;  // mean main-pass K1 time of the call
+            cudaGetLastError();  // a timing query is never an error of the epochs
         }
         int rec[3];
         std::memcpy(rec, eng->hstat + 5, sizeof(rec));
