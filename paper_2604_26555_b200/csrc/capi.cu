@@ -324,7 +324,7 @@ void run_bmu(Engine* eng, const float* x, const uint32_t* sel, uint64_t n, const
         // near-tie rows (~1-3%): same tensor-core kernel in enumerate mode on just
         // those rows, then exact FP64 over their few candidates.  The list length
         // stays on the device (kernels grid-stride over it), so the epoch needs
-        // no host round trip; rows beyond the enumerate capacity get the full
+        // no host round trip; rows with > 8 candidates in a group get the full
         // exact re-scan.
         // capacity = every row: a collapsed map (large sigma, early epochs) can put
         // a large share of the rows in the window, and rows past the capacity
