@@ -389,39 +389,65 @@ void launch_merge_partials(const float* part, const uint32_t* ties, const uint32
 }
 
 // ---------------------------------------------------------------------------
-// Exact re-scan (one warp per flagged row), reference order and rounding
+// Exact re-scan of flagged rows, reference order and rounding
 // ---------------------------------------------------------------------------
+
+// A block takes 32 flagged rows; the codebook streams through shared memory in
+// chunks of 64 nodes, so each node row is read once per 32 rows.  Thread
+// (r, q) = (tid / 8, tid % 8) evaluates row r against nodes q, q + 8, ... of a
+// chunk in FP64 with the reference's operation order (sub, mul, add per
+// feature, strict < over ascending j), then the 8 threads of a row reduce
+// with ties to the lowest j.
+constexpr int kRescanRows = 32, kRescanNodes = 64;
 
 __global__ void __launch_bounds__(256) k_rescan(const float* __restrict__ x,
                                                 const uint32_t* __restrict__ sel,
                                                 const float* __restrict__ w, uint32_t P,
                                                 uint32_t D, const uint32_t* __restrict__ flags,
                                                 uint32_t* __restrict__ bmu) {
-    extern __shared__ float xrow_all[];
+    extern __shared__ float rs_smem[];
+    float* xs = rs_smem;                          // [32][D]
+    float* ws = rs_smem + kRescanRows * D;        // [64][D + 1]
+    const uint32_t ldw = D + 1;
     const uint32_t count = flags[0];
-    const int lane = threadIdx.x & 31, wib = threadIdx.x >> 5;
-    float* xrow = xrow_all + wib * D;
-    for (uint32_t f = blockIdx.x * 8 + wib; f < count; f += gridDim.x * 8) {
-        const uint32_t pos = flags[2 + f];
-        const uint64_t row = sel ? (uint64_t)sel[pos] : pos;
-        __syncwarp();
-        for (uint32_t k = lane; k < D; k += 32) xrow[k] = x[row * D + k];
-        __syncwarp();
+    const uint32_t t = threadIdx.x, r = t >> 3, q = t & 7;
+    for (uint32_t f0 = blockIdx.x * kRescanRows; f0 < count; f0 += gridDim.x * kRescanRows) {
+        const uint32_t nr = min((uint32_t)kRescanRows, count - f0);
+        __syncthreads();  // previous rows' shared data consumed
+        for (uint32_t e = t; e < nr * D; e += blockDim.x) {
+            const uint32_t rr = e / D, k = e - rr * D;
+            const uint32_t pos = flags[2 + f0 + rr];
+            const uint64_t row = sel ? (uint64_t)sel[pos] : pos;
+            xs[rr * D + k] = x[row * D + k];
+        }
         double best = CUDART_INF;
         uint32_t best_j = 0xFFFFFFFFu;
-        for (uint32_t j = lane; j < P; j += 32) {
-            const float* wj = w + (size_t)j * D;
-            double acc = 0.0;
-            for (uint32_t k = 0; k < D; ++k) {
-                const double diff = __dsub_rn((double)xrow[k], (double)wj[k]);
-                acc = __dadd_rn(acc, __dmul_rn(diff, diff));
+        const float* xr = xs + r * D;
+        for (uint32_t c0 = 0; c0 < P; c0 += kRescanNodes) {
+            const uint32_t nc = min((uint32_t)kRescanNodes, P - c0);
+            __syncthreads();  // (first chunk: x rows staged; later: chunk consumed)
+            for (uint32_t e = t; e < nc * D; e += blockDim.x) {
+                const uint32_t jj = e / D, k = e - jj * D;
+                ws[jj * ldw + k] = w[(size_t)(c0 + jj) * D + k];
             }
-            if (acc < best) {  // ascending j within a lane: strict < keeps lowest
-                best = acc;
-                best_j = j;
+            __syncthreads();
+            if (r < nr) {
+                for (uint32_t jj = q; jj < nc; jj += 8) {
+                    const float* wj = ws + jj * ldw;
+                    double acc = 0.0;
+                    for (uint32_t k = 0; k < D; ++k) {
+                        const double diff = __dsub_rn((double)xr[k], (double)wj[k]);
+                        acc = __dadd_rn(acc, __dmul_rn(diff, diff));
+                    }
+                    if (acc < best) {  // ascending j per thread: strict < keeps the lowest
+                        best = acc;
+                        best_j = c0 + jj;
+                    }
+                }
             }
         }
-        for (int o = 16; o; o >>= 1) {
+#pragma unroll
+        for (int o = 4; o; o >>= 1) {  // the row's 8 threads (lanes 8r' .. 8r' + 7)
             const double ob = __shfl_xor_sync(0xffffffffu, best, o);
             const uint32_t oj = __shfl_xor_sync(0xffffffffu, best_j, o);
             if (ob < best || (ob == best && oj < best_j)) {
@@ -429,16 +455,21 @@ __global__ void __launch_bounds__(256) k_rescan(const float* __restrict__ x,
                 best_j = oj;
             }
         }
-        if (lane == 0) bmu[pos] = best_j == 0xFFFFFFFFu ? 0u : best_j;
+        if (q == 0 && r < nr) bmu[flags[2 + f0 + r]] = best_j == 0xFFFFFFFFu ? 0u : best_j;
     }
 }
 
 void launch_rescan(const float* x, const uint32_t* sel, const float* w, uint32_t P, uint32_t D,
                    const uint32_t* flags, uint64_t n, uint32_t* bmu, cudaStream_t st) {
     if (n == 0) return;
-    // grid sized for the worst case is wasteful; flagged rows are rare, the
-    // kernel grid-strides over the device-side count.
-    TSOM_LAUNCH(k_rescan<<<148 * 4, 256, 8 * D * sizeof(float), st>>>(x, sel, w, P, D, flags, bmu));
+    // flagged rows are usually few: the kernel grid-strides over the device count
+    const size_t smem = ((size_t)kRescanRows * D + (size_t)kRescanNodes * (D + 1)) * sizeof(float);
+    static size_t attr = 0;
+    if (smem > attr) {
+        cudaFuncSetAttribute(k_rescan, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+        attr = smem;
+    }
+    TSOM_LAUNCH(k_rescan<<<148 * 2, 256, smem, st>>>(x, sel, w, P, D, flags, bmu));
 }
 
 }  // namespace tsom
