@@ -125,15 +125,16 @@ def cpu_model():
     return None
 
 
-def cpu_reference(step_seconds=6.0, steps=1, warmup=0):
-    """Time the reference's train_parallel (all host cores) on a bounded sample
-    of the headline workload: 32x32 hex, D=50, full sampling; each step = one
-    epoch.  Returns (samples·epochs/s, cores, kind, sample description)."""
+def cpu_reference(step_seconds=6.0, steps=1, warmup=0, threads=None):
+    """Time the reference's train_parallel (all host cores, or `threads`) on a
+    bounded sample of the headline workload: 32x32 hex, D=50, full sampling;
+    each step = one epoch.  Returns (samples·epochs/s, cores, kind, sample
+    description, seconds per step)."""
     import numpy as np
 
     import oracle
     chk = oracle.best()
-    cores = os.cpu_count() or 1
+    cores = threads or os.cpu_count() or 1
     # calibrate rows so one epoch takes ~step_seconds
     probe_rows = 256 * cores
     x = chk.synth_gmm(probe_rows, D, SEED)
@@ -411,8 +412,10 @@ def run_gpu_arm(args):
             line["c4"] = c4
     if rank == 0 and world == 1 and not args.no_cpu:
         v, cores, kind, sample, _ = cpu_reference(step_seconds=6.0)
+        v1, _, _, sample1, _ = cpu_reference(step_seconds=3.0, threads=1)
         line["cpu_baseline"] = {"value": v, "unit": UNIT, "cores": cores, "kind": kind,
-                                "sample": sample, "cpu_model": cpu_model()}
+                                "sample": sample, "cpu_model": cpu_model(),
+                                "single_thread": {"value": v1, "sample": sample1}}
     if rank == 0:
         print(json.dumps(line), flush=True)
     if world > 1:
