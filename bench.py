@@ -378,6 +378,16 @@ def run_gpu_arm(args):
                      f"dram__bytes_read+write per launch ({K1_TRAFFIC_SRC})"),
             "k1_ms": k1, "epoch_ms": statistics.mean(total_ms) if total_ms else None,
             "phase_ms": {k: statistics.mean(p[k] for p in phases) for k in phases[0]} if phases else None}
+    # K2 (accumulation) against HBM: 204 algorithmic bytes per row (the row
+    # and its BMU) over the accumulate phase's event time
+    acc_ms = statistics.mean(p["accum_ms"] for p in phases) if phases else float("nan")
+    k2_gbs = n * 204 / (acc_ms / 1e3) / 1e9 if acc_ms > 0 else 0.0
+    k2_roof = {"bound": "hbm", "kernel": "k2 sort + TMA gather + piece reduce",
+               "achieved": k2_gbs, "peak": pk["hbm_gbs"], "unit": "GB/s",
+               "frac": k2_gbs / pk["hbm_gbs"], "accum_ms": acc_ms,
+               "note": "achieved = 204 B/row x rows / accumulate-phase event time (3 untimed "
+                       "epochs); the gather reads ~1.6x that from DRAM (200-B rows at random "
+                       "positions touch 2-3 128-B lines)"}
     line = {
         "metric": METRIC, "value": value, "unit": UNIT, "n_gpus": world, "steps": args.steps,
         "warmup": args.warmup, "ms_per_step": ms, "higher_is_better": True, "scaling": "weak",
@@ -391,6 +401,7 @@ def run_gpu_arm(args):
                    "nodes": P, "dims": D, "rows_per_gpu": n, "global_rows": n * world,
                    "parallelism": f"dp{world}", "l2": "inputs (2 GB/GPU) > L2 (126 MB); no flush"},
         "roofline": roof,
+        "roofline_k2": k2_roof,
         "clocks": clk.summary(),
         "gpu_launches": int(launches),
         "qe_gpu_after": qe_gpu,
