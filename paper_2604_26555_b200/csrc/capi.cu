@@ -639,11 +639,23 @@ void accumulate_epoch(Engine* eng, const uint32_t* sel_host, uint64_t n_sel, boo
         run_bmu(eng, eng->x.as<float>(), dsel, n, eng->x2max.as<float>(), tiles, tiles_xn2);
         CU(cudaEventRecord(eng->ev[1], eng->stream));
         ensure_accum(eng, n);
+        // a 256-B-stride copy of the rows for the K2 gather (built once per bind)
+        const float* xpad = nullptr;
+        if (eng->D % 2 == 0 && eng->D <= tsom::kPadFloats - 2 &&
+            eng->n_rows * (uint64_t)tsom::kPadFloats * 4 <= (32ull << 30)) {
+            if (!eng->xpad_valid) {
+                CU(eng->xpad.ensure(eng->n_rows * (uint64_t)tsom::kPadFloats * sizeof(float)));
+                tsom::launch_pad_rows(eng->x.as<float>(), eng->n_rows, eng->D,
+                                      eng->xpad.as<float>(), eng->stream);
+                eng->xpad_valid = true;
+            }
+            xpad = eng->xpad.as<float>();
+        }
         tsom::launch_accumulate(eng->x.as<float>(), dsel, n, eng->D, eng->w.as<float>(), eng->P,
                                 eng->bmu.as<uint32_t>(),
                                 want_dist ? eng->dist.as<double>() : nullptr, want_dsum,
                                 accumulate, true, eng->acc, eng->sums.as<double>(), eng->sm_count,
-                                eng->stream, eng->x_slack);
+                                eng->stream, eng->x_slack, xpad);
         CU(cudaGetLastError());
         eng->chunk_counts.clear();
         eng->recheck_from_chunks = true;
@@ -878,7 +890,7 @@ int tsom_destroy(tsom_engine* eng) {
                       &eng->topo_buf[4], &eng->topo_buf[5], &eng->topo_buf[6], &eng->topo_buf[7],
                       &eng->topo_buf[8], &eng->topo_buf[9], &eng->topo_buf[10], &eng->topo_buf[11],
                       &eng->topo_buf[12], &eng->topo_buf[13], &eng->topo_buf[14], &eng->U, &eng->H, &eng->status, &eng->smooth_scratch,
-                      &eng->stage[0], &eng->stage[1], &eng->dead})
+                      &eng->stage[0], &eng->stage[1], &eng->dead, &eng->xpad})
         b->release(true);
     for (auto& ev : eng->ev)
         if (ev) cudaEventDestroy(ev);
@@ -949,6 +961,7 @@ int tsom_bind_host_data(tsom_engine* eng, const float* rows, uint64_t n_rows, ui
         eng->host_direct = false;
         close_shards(eng);
         eng->xsplit_valid = false;
+        eng->xpad_valid = false;
         eng->n_rows = n_rows;
         if (flags & TSOM_BIND_STREAMED) {
             eng->streamed = true;
@@ -1059,6 +1072,7 @@ int tsom_bind_shards(tsom_engine* eng, const char* const* paths, uint32_t n_path
         REQUIRE(total < (1ull << 32), TSOM_ERR_INVALID, "bind: row ids are uint32 (n < 2^32)");
         eng->n_rows = total;
         eng->xsplit_valid = false;
+        eng->xpad_valid = false;
         if (flags & TSOM_BIND_STREAMED) {
             eng->streamed = true;
             eng->x.release();
@@ -1113,6 +1127,7 @@ int tsom_bind_device_data(tsom_engine* eng, const float* d_rows, uint64_t n_rows
         eng->n_rows = n_rows;
         eng->streamed = false;
         eng->xsplit_valid = false;
+        eng->xpad_valid = false;
         tsom::launch_row_norm_max(d_rows, n_rows, eng->D, eng->x2max.as<float>(), eng->stream);
         CU(cudaGetLastError());
         CU(cudaStreamSynchronize(eng->stream));
@@ -1145,6 +1160,7 @@ int tsom_bind_synthetic_gmm(tsom_engine* eng, uint64_t n_rows, uint64_t seed, ui
         eng->n_rows = n_rows;
         eng->streamed = false;
         eng->xsplit_valid = false;
+        eng->xpad_valid = false;
         tsom::launch_row_norm_max(eng->x.as<float>(), n_rows, eng->D, eng->x2max.as<float>(),
                                   eng->stream);
         CU(cudaStreamSynchronize(eng->stream));

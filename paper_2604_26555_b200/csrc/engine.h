@@ -285,6 +285,8 @@ struct Engine {
     std::vector<cudaEvent_t> k1_ev;
     int k1_slot = -1;
     DevBuf dead;
+    DevBuf xpad;              // resident rows at a 256-B stride for the K2 gather
+    bool xpad_valid = false;
     uint64_t last_recheck = 0;
     std::vector<uint32_t> chunk_counts;  // per-chunk re-check counts (streamed epochs)
     // pinned per-epoch status words, read back asynchronously before the one
@@ -375,7 +377,12 @@ void accum_scratch_bytes(uint64_t n, uint32_t P, uint32_t D, size_t out[7]);
 void launch_accumulate(const float* x, const uint32_t* sel, uint64_t n, uint32_t D,
                        const float* w, uint32_t P, const uint32_t* bmu, double* dist_out,
                        bool want_dist_sum, bool accumulate, bool first, const AccumScratch& s,
-                       double* sums, int sm_count, cudaStream_t st, bool x_slack = false);
+                       double* sums, int sm_count, cudaStream_t st, bool x_slack = false,
+                       const float* xpad = nullptr);
+// the resident rows copied at a 256-byte stride (kPadFloats floats per row;
+// the K2 gather's rows are then exactly two 128-byte lines)
+constexpr uint32_t kPadFloats = 64;
+void launch_pad_rows(const float* x, uint64_t n, uint32_t D, float* xpad, cudaStream_t st);
 // bytes of slack the engine allocates after resident rows (TMA row gathers read
 // up to 16 bytes past a row)
 constexpr size_t kRowSlack = 64;

@@ -414,8 +414,9 @@ __global__ void __launch_bounds__(kAsyncWarps * 32, 2) k_gather_async(
 constexpr int kTmaWarps = 8;
 
 __global__ void __launch_bounds__(kTmaWarps * 32, 2) k_gather_tma(
-    const float* __restrict__ x, const uint32_t* __restrict__ sel, const float* __restrict__ w,
-    uint32_t P, uint32_t D, uint32_t slot, const uint32_t* __restrict__ sorted,
+    const float* __restrict__ x, uint32_t ldx, const uint32_t* __restrict__ sel,
+    const float* __restrict__ w, uint32_t P, uint32_t D, uint32_t slot,
+    const uint32_t* __restrict__ sorted,
     const uint32_t* __restrict__ node_start, const uint32_t* __restrict__ piece_start,
     const uint32_t* __restrict__ piece_node, double* __restrict__ partial,
     double* __restrict__ dist_out, int want_dist, int accumulate) {
@@ -435,11 +436,12 @@ __global__ void __launch_bounds__(kTmaWarps * 32, 2) k_gather_tma(
     const uint32_t Dp = D + 1;
     const uint32_t ka = 2 * lane, kb = 2 * lane + 1;
     const bool oka = ka < D, okb = kb < D;
-    const uint32_t rowb = D * 4;
+    const uint32_t rowb = D * 4;                 // bytes of a row
+    const uint64_t strideb = (uint64_t)ldx * 4;  // bytes between rows (D, or 64 padded)
 
     // copy window of this lane's row; returns the bytes it will deliver
     auto issue = [&](uint64_t row, uint32_t nrows, int s, uint32_t& offmask) {
-        const uint64_t a = reinterpret_cast<uint64_t>(x) + row * rowb;
+        const uint64_t a = reinterpret_cast<uint64_t>(x) + row * strideb;
         const uint64_t a0 = a & ~15ull;
         const uint32_t len = (uint32_t)(((a + rowb + 15) & ~15ull) - a0);
         const bool mine = lane < nrows;
@@ -596,10 +598,27 @@ __global__ void k_add_rowcount(double* __restrict__ sums, uint32_t P, uint32_t D
 
 int g_gather_kind = 0;  // diagnostics (TSOM option 97): 1 = cp.async gather
 
+__global__ void k_pad_rows(const float* __restrict__ x, uint64_t n, uint32_t D,
+                           float* __restrict__ xpad) {
+    const uint64_t total = n * kPadFloats;
+    for (uint64_t e = blockIdx.x * (uint64_t)blockDim.x + threadIdx.x; e < total;
+         e += (uint64_t)gridDim.x * blockDim.x) {
+        const uint64_t r = e / kPadFloats;
+        const uint32_t k = (uint32_t)(e % kPadFloats);
+        xpad[e] = k < D ? x[r * D + k] : 0.0f;
+    }
+}
+
+void launch_pad_rows(const float* x, uint64_t n, uint32_t D, float* xpad, cudaStream_t st) {
+    if (n == 0) return;
+    TSOM_LAUNCH(k_pad_rows<<<148 * 16, 256, 0, st>>>(x, n, D, xpad));
+}
+
 void launch_accumulate(const float* x, const uint32_t* sel, uint64_t n, uint32_t D,
                        const float* w, uint32_t P, const uint32_t* bmu, double* dist_out,
                        bool want_dist_sum, bool accumulate, bool first, const AccumScratch& s,
-                       double* sums, int sm_count, cudaStream_t st, bool x_slack) {
+                       double* sums, int sm_count, cudaStream_t st, bool x_slack,
+                       const float* xpad) {
     const int add = first ? 0 : 1;
     if (n == 0) {
         if (first) cudaMemsetAsync(sums, 0, ((size_t)P * D + P + 2) * sizeof(double), st);
@@ -638,8 +657,13 @@ void launch_accumulate(const float* x, const uint32_t* sel, uint64_t n, uint32_t
     const size_t asmem = (size_t)kAsyncWarps * 2 * 32 * D * sizeof(float);
     const uint32_t slot = (D * 4 + 8 + 15) / 16 * 16;  // longest 16-B window of a row
     const size_t tsmem = (size_t)kTmaWarps * 2 * 32 * slot;
-    if (v2 && x_slack && g_gather_kind == 0 && ((reinterpret_cast<uintptr_t>(x) & 15u) == 0) &&
-        tsmem <= 110 * 1024) {
+    // padded copy (rows at a 256-B stride, line aligned): a row is exactly two
+    // 128-B lines instead of two or three
+    const bool use_pad = xpad && v2 && D <= kPadFloats - 2 && g_gather_kind == 0 &&
+                         tsmem <= 110 * 1024;
+    if (use_pad ||
+        (v2 && x_slack && g_gather_kind == 0 && ((reinterpret_cast<uintptr_t>(x) & 15u) == 0) &&
+         tsmem <= 110 * 1024)) {
         static size_t tattr = 0;
         if (tattr < tsmem) {
             cudaFuncSetAttribute(k_gather_tma, cudaFuncAttributeMaxDynamicSharedMemorySize,
@@ -649,8 +673,9 @@ void launch_accumulate(const float* x, const uint32_t* sel, uint64_t n, uint32_t
         const uint64_t tblocks = (pieces + kTmaWarps - 1) / kTmaWarps;
         const unsigned tb = (unsigned)(tblocks < (uint64_t)sm_count * 2 ? tblocks : sm_count * 2);
         TSOM_LAUNCH(k_gather_tma<<<tb, kTmaWarps * 32, tsmem, st>>>(
-            x, sel, w, P, D, slot, s.sorted, s.node_start, s.piece_start, s.piece_node, s.partial,
-            dist_out, want_dist ? 1 : 0, accumulate ? 1 : 0));
+            use_pad ? xpad : x, use_pad ? (uint32_t)kPadFloats : D, sel, w, P, D, slot, s.sorted,
+            s.node_start, s.piece_start, s.piece_node, s.partial, dist_out, want_dist ? 1 : 0,
+            accumulate ? 1 : 0));
     } else if (v2 && D <= 64 && asmem <= 110 * 1024) {
         static size_t aattr = 0;
         if (aattr < asmem) {
