@@ -280,7 +280,10 @@ cudaEvent_t k1_event(Engine* eng, int end) {
 // `tiles` = pre-split tcgen05 A tiles for exactly these n rows, built with the
 // scale of this same x2max (or nullptr to build them here).
 void run_bmu(Engine* eng, const float* x, const uint32_t* sel, uint64_t n, const float* x2max,
-             const void* tiles, const float* tiles_xn2) {
+             const void* tiles, const float* tiles_xn2, const float* xpad = nullptr) {
+    // the splits read rows from the 256-B-stride copy when there is one
+    const float* xsrc = xpad ? xpad : x;
+    const uint32_t ldx = xpad ? tsom::kPadFloats : eng->D;
     CU(cudaMemsetAsync(eng->flags.p, 0, 2 * sizeof(uint32_t), eng->stream));
     if (n == 0) return;
     const int kind = tc_kind(eng);
@@ -299,8 +302,9 @@ void run_bmu(Engine* eng, const float* x, const uint32_t* sel, uint64_t n, const
             const uint64_t ntiles = (n + tsom::kTcTileM - 1) / tsom::kTcTileM;
             CU(eng->gsplit.ensure(ntiles * geo.tile_bytes));
             CU(eng->gxn2.ensure(n * sizeof(float)));
-            tsom::launch_split_rows(kind, x, sel, nullptr, n, eng->D, scale, win, eng->gsplit.p,
-                                    eng->gxn2.as<float>(), eng->stream);
+            tsom::launch_split_rows(kind, xsrc, sel, nullptr, n, eng->D, scale, win,
+                                    eng->gsplit.p, eng->gxn2.as<float>(), eng->stream, nullptr,
+                                    ldx);
             tiles = eng->gsplit.p;
             tiles_xn2 = eng->gxn2.as<float>();
         }
@@ -336,8 +340,8 @@ void run_bmu(Engine* eng, const float* x, const uint32_t* sel, uint64_t n, const
         CU(eng->txn2.ensure(cap * sizeof(float)));
         const uint32_t* tcount = eng->ties.as<uint32_t>();
         const uint32_t* tpos = tcount + 1;
-        tsom::launch_split_rows(kind, x, sel, tpos, cap, eng->D, scale, win, eng->tsplit.p,
-                                eng->txn2.as<float>(), eng->stream, tcount);
+        tsom::launch_split_rows(kind, xsrc, sel, tpos, cap, eng->D, scale, win, eng->tsplit.p,
+                                eng->txn2.as<float>(), eng->stream, tcount, ldx);
         CU(tsom::launch_bmu_tc(kind, eng->tsplit.p, cap, tcount, true, eng->P, eng->D,
                                eng->wsplit.p, eng->txn2.as<float>(), w2, scale, win,
                                eng->tmask.as<uint32_t>(), eng->part2.as<float>(), eng->sm_count,
@@ -636,10 +640,8 @@ void accumulate_epoch(Engine* eng, const uint32_t* sel_host, uint64_t n_sel, boo
             tiles = eng->xsplit.p;
             tiles_xn2 = eng->xn2.as<float>();
         }
-        run_bmu(eng, eng->x.as<float>(), dsel, n, eng->x2max.as<float>(), tiles, tiles_xn2);
-        CU(cudaEventRecord(eng->ev[1], eng->stream));
-        ensure_accum(eng, n);
-        // a 256-B-stride copy of the rows for the K2 gather (built once per bind)
+        // a 256-B-stride copy of the rows for the gathered splits and the K2
+        // gather (built once per bind)
         const float* xpad = nullptr;
         if (eng->D % 2 == 0 && eng->D <= tsom::kPadFloats - 2 &&
             eng->n_rows * (uint64_t)tsom::kPadFloats * 4 <= (32ull << 30)) {
@@ -651,6 +653,9 @@ void accumulate_epoch(Engine* eng, const uint32_t* sel_host, uint64_t n_sel, boo
             }
             xpad = eng->xpad.as<float>();
         }
+        run_bmu(eng, eng->x.as<float>(), dsel, n, eng->x2max.as<float>(), tiles, tiles_xn2, xpad);
+        CU(cudaEventRecord(eng->ev[1], eng->stream));
+        ensure_accum(eng, n);
         tsom::launch_accumulate(eng->x.as<float>(), dsel, n, eng->D, eng->w.as<float>(), eng->P,
                                 eng->bmu.as<uint32_t>(),
                                 want_dist ? eng->dist.as<double>() : nullptr, want_dsum,

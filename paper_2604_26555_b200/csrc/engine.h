@@ -324,7 +324,8 @@ void launch_fold_max(float* a, cudaStream_t st);
 // tx[f] (optional) = tie_xpart of the row: its share of the error window
 void launch_split_rows(int kind, const float* x, const uint32_t* sel, const uint32_t* idx,
                        uint64_t n, uint32_t D, const float* scale, TieWin win, void* tiles,
-                       float* tx, cudaStream_t st, const uint32_t* dev_n = nullptr);
+                       float* tx, cudaStream_t st, const uint32_t* dev_n = nullptr,
+                       uint32_t ldx = 0);  // row stride in floats (0: D)
 bool tc_supported(int kind, uint32_t P, uint32_t D);
 size_t tc_wsplit_bytes(int kind, uint32_t P, uint32_t D);
 // scale = {s, s^2, overflow flag}: kTcF16 picks s = 2^e from max ||x||^2 (x2max[0])

@@ -253,7 +253,7 @@ constexpr int kSplitThreads = 256;
 
 template <int kKind>
 __global__ void __launch_bounds__(kSplitThreads) k_split_rows(
-    const float* __restrict__ x, const uint32_t* __restrict__ sel,
+    const float* __restrict__ x, uint32_t ldx, const uint32_t* __restrict__ sel,
     const uint32_t* __restrict__ idx, const uint32_t* __restrict__ dev_n, uint64_t n_host,
     uint32_t D, const float* __restrict__ scale, TieWin win, uint8_t* __restrict__ tiles,
     float* __restrict__ xn2) {
@@ -273,7 +273,7 @@ __global__ void __launch_bounds__(kSplitThreads) k_split_rows(
         __syncthreads();  // previous tile's shared memory fully consumed
         if (t < kTcTileM && (uint32_t)t < rows) {
             const uint64_t pos = idx ? (uint64_t)idx[f0 + t] : f0 + t;
-            rbase[t] = (sel ? (uint64_t)sel[pos] : pos) * D;
+            rbase[t] = (sel ? (uint64_t)sel[pos] : pos) * ldx;
         }
         __syncthreads();
         {
@@ -398,7 +398,7 @@ __global__ void __launch_bounds__(kSplitThreads) k_split_rows(
 constexpr int kSplitWarpRows = 16;
 
 __global__ void __launch_bounds__(kSplitThreads, 4) k_split_rows_f16(
-    const float* __restrict__ x, const uint32_t* __restrict__ sel,
+    const float* __restrict__ x, uint32_t ldx, const uint32_t* __restrict__ sel,
     const uint32_t* __restrict__ idx, const uint32_t* __restrict__ dev_n, uint64_t n_host,
     uint32_t D, const float* __restrict__ scale, TieWin win, uint8_t* __restrict__ tiles,
     float* __restrict__ xn2) {
@@ -427,7 +427,7 @@ __global__ void __launch_bounds__(kSplitThreads, 4) k_split_rows_f16(
         float v[kSplitWarpRows][2];
 #pragma unroll
         for (int i = 0; i < kSplitWarpRows; ++i) {
-            const uint64_t rb = __shfl_sync(0xffffffffu, myrow, i) * D;
+            const uint64_t rb = __shfl_sync(0xffffffffu, myrow, i) * ldx;
             v[i][0] = ((uint32_t)i < rows && lane < D) ? __ldg(x + rb + lane) : 0.0f;
             v[i][1] = ((uint32_t)i < rows && lane + 32u < D) ? __ldg(x + rb + lane + 32u) : 0.0f;
         }
@@ -498,18 +498,19 @@ int g_split_v1 = 0;  // debug: the element-wise split (TSOM option 98)
 
 void launch_split_rows(int kind, const float* x, const uint32_t* sel, const uint32_t* idx,
                        uint64_t n, uint32_t D, const float* scale, TieWin win, void* tiles,
-                       float* xn2, cudaStream_t st, const uint32_t* dev_n) {
+                       float* xn2, cudaStream_t st, const uint32_t* dev_n, uint32_t ldx) {
     if (n == 0) return;
+    if (ldx == 0) ldx = D;
     uint64_t tiles_n = (n + kTcTileM - 1) / kTcTileM;
     if (tiles_n > 148ull * 16) tiles_n = 148ull * 16;
     uint8_t* t = static_cast<uint8_t*>(tiles);
     const size_t smem = (size_t)kTcTileM * (D + 1) * sizeof(float);
     if (kind == kTcTf32)
         TSOM_LAUNCH(k_split_rows<kTcTf32><<<(unsigned)tiles_n, kSplitThreads, smem, st>>>(
-            x, sel, idx, dev_n, n, D, scale, win, t, xn2));
+            x, ldx, sel, idx, dev_n, n, D, scale, win, t, xn2));
     else if (g_split_v1)
         TSOM_LAUNCH(k_split_rows<kTcF16><<<(unsigned)tiles_n, kSplitThreads, smem, st>>>(
-            x, sel, idx, dev_n, n, D, scale, win, t, xn2));
+            x, ldx, sel, idx, dev_n, n, D, scale, win, t, xn2));
     else {
         const size_t wsmem = (size_t)(kSplitThreads / 32) * kSplitWarpRows *
                              (tc_geom(kTcF16, D).kpad + 8) * sizeof(__half);
@@ -525,7 +526,7 @@ void launch_split_rows(int kind, const float* x, const uint32_t* sel, const uint
         uint64_t blocks = (n + kTcTileM - 1) / kTcTileM;  // 8 warps x 16 rows per tile
         if (blocks > 148ull * 8) blocks = 148ull * 8;
         TSOM_LAUNCH(k_split_rows_f16<<<(unsigned)blocks, kSplitThreads, wsmem, st>>>(
-            x, sel, idx, dev_n, n, D, scale, win, t, xn2));
+            x, ldx, sel, idx, dev_n, n, D, scale, win, t, xn2));
     }
 }
 
