@@ -252,40 +252,69 @@ __global__ void __launch_bounds__(256, 8) k_merge_fast(
     const float* __restrict__ xn2, const float* __restrict__ w2max,
     const float* __restrict__ scale, TieWin win, uint32_t* __restrict__ bmu,
     uint32_t* __restrict__ ties, uint32_t* __restrict__ tmask, uint32_t* __restrict__ flags) {
+    constexpr uint32_t kCache = 8;  // sub-group minima kept in registers (K <= 2048 at sets 1)
     const uint64_t i = blockIdx.x * (uint64_t)blockDim.x + threadIdx.x;
-    if (i >= n) return;
+    const bool valid = i < n;
+    const uint32_t lane = threadIdx.x & 31;
     const uint32_t nsub = groups * sets, nch = gn / 32;
-    float B1 = CUDART_INF_F;
-    uint32_t smin = 0;
-    for (uint32_t sg = 0; sg < nsub; ++sg) {  // strict <: lowest node ids on equal minima
-        const float b = __ldg(part + (size_t)sg * 2 * n + i);
-        if (b < B1) {
-            B1 = b;
-            smin = sg;
+    bool need_tie = false;
+    uint32_t mask = 0;
+    if (valid) {
+        float bc[kCache];
+        float B1 = CUDART_INF_F;
+        uint32_t smin = 0;
+#pragma unroll
+        for (uint32_t sg = 0; sg < kCache; ++sg) {  // strict <: lowest node ids on equal minima
+            bc[sg] = sg < nsub ? __ldg(part + (size_t)sg * 2 * n + i) : CUDART_INF_F;
+            if (bc[sg] < B1) {
+                B1 = bc[sg];
+                smin = sg;
+            }
+        }
+        for (uint32_t sg = kCache; sg < nsub; ++sg) {
+            const float b = __ldg(part + (size_t)sg * 2 * n + i);
+            if (b < B1) {
+                B1 = b;
+                smin = sg;
+            }
+        }
+        const uint32_t code = __float_as_uint(__ldg(part + (size_t)smin * 2 * n + n + i));
+        const uint32_t gmin = smin / sets, hmin = smin % sets;
+        bmu[i] = gmin * gn + (hmin * nch / sets) * 32 + (code == 0xFFFFFFFFu ? 0u : code);
+        if (__float_as_uint(__ldg(scale + 2)) != 0u) {
+            const uint32_t slot = atomicAdd(&flags[0], 1u);
+            flags[2 + slot] = (uint32_t)i;
+        } else {
+            const float thr = __ldg(xn2 + i) + tie_wpart(__ldg(w2max), __ldg(scale + 1), win);
+            const float lim = B1 + thr;
+            bool clear = code != 0xFFFFFFFFu;
+#pragma unroll
+            for (uint32_t sg = 0; sg < kCache; ++sg) {
+                const bool in = sg < nsub && bc[sg] <= lim;
+                const uint32_t g = sg / sets;
+                if (in) mask |= (g < 32 ? 1u << g : 0u);
+                if (in && sg != smin) clear = false;
+            }
+            for (uint32_t sg = kCache; sg < nsub; ++sg) {
+                const bool in = __ldg(part + (size_t)sg * 2 * n + i) <= lim;
+                const uint32_t g = sg / sets;
+                if (in) mask |= (g < 32 ? 1u << g : 0u);
+                if (in && sg != smin) clear = false;
+            }
+            need_tie = !clear;
         }
     }
-    const uint32_t code = __float_as_uint(__ldg(part + (size_t)smin * 2 * n + n + i));
-    const uint32_t gmin = smin / sets, hmin = smin % sets;
-    bmu[i] = gmin * gn + (hmin * nch / sets) * 32 + (code == 0xFFFFFFFFu ? 0u : code);
-    if (__float_as_uint(__ldg(scale + 2)) != 0u) {
-        const uint32_t slot = atomicAdd(&flags[0], 1u);
-        flags[2 + slot] = (uint32_t)i;
-        return;
-    }
-    const float thr = __ldg(xn2 + i) + tie_wpart(__ldg(w2max), __ldg(scale + 1), win);
-    const float lim = B1 + thr;
-    bool clear = code != 0xFFFFFFFFu;
-    uint32_t mask = 0;
-    for (uint32_t sg = 0; sg < nsub; ++sg) {
-        const bool in = __ldg(part + (size_t)sg * 2 * n + i) <= lim;
-        const uint32_t g = sg / sets;
-        if (in) mask |= (g < 32 ? 1u << g : 0u);
-        if (in && sg != smin) clear = false;
-    }
-    if (!clear) {
-        const uint32_t slot = atomicAdd(&ties[0], 1u);
-        ties[1 + slot] = (uint32_t)i;
-        tmask[slot] = groups <= 32 ? mask : 0xFFFFFFFFu;
+    // warp-aggregated append to the near-tie list (one atomic per warp)
+    const uint32_t ballot = __ballot_sync(0xffffffffu, need_tie);
+    if (ballot) {
+        uint32_t base = 0;
+        if (lane == (uint32_t)(__ffs(ballot) - 1)) base = atomicAdd(&ties[0], (uint32_t)__popc(ballot));
+        base = __shfl_sync(0xffffffffu, base, __ffs(ballot) - 1);
+        if (need_tie) {
+            const uint32_t slot = base + __popc(ballot & ((1u << lane) - 1u));
+            ties[1 + slot] = (uint32_t)i;
+            tmask[slot] = groups <= 32 ? mask : 0xFFFFFFFFu;
+        }
     }
 }
 
