@@ -1,0 +1,52 @@
+// capi_internal.h — shared by the engine's host translation units (capi.cu,
+// host_staging.cu): the error plumbing of the guarded C-ABI calls and the
+// host-side row staging.
+#pragma once
+
+#include <cuda_runtime.h>
+
+#include <cstdint>
+#include <string>
+
+#include "engine.h"
+#include "tsom_b200.h"
+
+namespace tsom {
+
+// a failed CU / REQUIRE inside a guarded call: the status it returns
+struct Fail {
+    int code;
+};
+
+#define CU(expr)                                                                          \
+    do {                                                                                  \
+        cudaError_t _e = (expr);                                                          \
+        if (_e != cudaSuccess) {                                                          \
+            eng->last_error = std::string("cuda: ") + cudaGetErrorString(_e) + " at " #expr; \
+            throw ::tsom::Fail{TSOM_ERR_CUDA};                                            \
+        }                                                                                 \
+    } while (0)
+
+#define REQUIRE(cond, code, msg)        \
+    do {                                \
+        if (!(cond)) {                  \
+            eng->last_error = (msg);    \
+            throw ::tsom::Fail{code};   \
+        }                               \
+    } while (0)
+
+namespace host {
+
+// FSOMSHRD files of a shard bind
+void close_shards(Engine* eng);
+// two pinned staging slots of at least `rows` rows (blocks cached process-wide)
+void ensure_pinned(Engine* eng, uint64_t rows);
+void pinned_give(void* p, size_t bytes);
+// host pointer of rows [r0, r1) the copy engine can read (slot s when staged)
+const float* host_chunk_source(Engine* eng, uint64_t r0, uint64_t r1, int s);
+void note_pinned_copy(Engine* eng, int s);
+// rows [0, total) of the bound host source into eng->x, C rows per chunk
+void upload_rows(Engine* eng, uint64_t total, uint64_t C);
+
+}  // namespace host
+}  // namespace tsom
