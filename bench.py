@@ -357,6 +357,13 @@ def run_gpu_arm(args):
                                       n_iters=1, seed=SEED)
             dropin.train_cuda(warm, host[:200_000], device=local)
             _, _, _, dsecs = dropin.train_cuda(cfg, host, device=local)
+            dropin.train_device(warm, host[:200_000], device=local)
+            _, _, _, vsecs = dropin.train_device(cfg, host, device=local)
+            e2e["dropin_device_loop"] = {
+                "value": n * EPOCHS / vsecs, "seconds_per_call": vsecs,
+                "path": "toposom_b200::train_device (C++ drop-in: init_weights and lattice "
+                        "distances as the reference builds them, then every epoch step on the "
+                        "device; host DataMatrix bound through the pinned staging)"}
             e2e["dropin_reference_loop"] = {
                 "value": n * EPOCHS / dsecs, "seconds_per_call": dsecs,
                 "path": "toposom::train_with_executor + toposom_b200::CudaExecutor "

@@ -18,6 +18,7 @@
 
 #include <algorithm>
 #include <atomic>
+#include <chrono>
 #include <cmath>
 #include <cstdint>
 #include <limits>
@@ -158,6 +159,120 @@ inline std::pair<toposom::SomModel, toposom::RunLog> train_cuda(
     if (data.rows() < 1) throw std::invalid_argument("train: empty training data");
     CudaExecutor executor(data, config.nodes(), opts);
     return toposom::train_with_executor(config, data, sampler, executor, options);
+}
+
+/// The sampler of a device-resident run: the arguments of toposom::Sampler
+/// (sampling.hpp:185-191) except n (the data's rows) and the seed (the
+/// config's, as train_with_executor's callers use it).
+struct DeviceSampling {
+    toposom::SamplingKind kind = toposom::SamplingKind::full;
+    toposom::SamplingBudget budget{};
+    double alpha = 1.0;
+    double beta = 1.0;
+};
+
+/// train_with_executor (trainer.hpp:466-523) with every step of every epoch
+/// on the device: init_weights and the lattice distances on the host as the
+/// reference builds them, then selection (device sampler), topology refresh
+/// on the reference's schedule (device MST / RNG graph and hop counts),
+/// influence, BMU, accumulation, smoothing and apply_update.  The epochs
+/// between two refreshes go to the engine as one tsom_train_epochs call (no
+/// host round trip between them); with options.log_qe each epoch is its own
+/// call followed by the device QE.  options.timeout_s is checked between
+/// calls.  Returns the reference's (SomModel, RunLog): weights, momentum
+/// memory, topology state (edges, hop counts and refresh counters of the last
+/// refresh for graphs) and one log entry per epoch.
+inline std::pair<toposom::SomModel, toposom::RunLog> train_device(
+    const toposom::SomConfig& config, const DataSourceRef& data, DeviceSampling sampling = {},
+    CudaOptions opts = {}, const toposom::TrainOptions& options = {}) {
+    config.validate();
+    if (data.rows() < 1) throw std::invalid_argument("train: empty training data");
+    toposom::SomModel model;
+    model.weights = toposom::init_weights(config, data);
+    model.prev_update = DataMatrix(config.nodes(), data.cols());
+    model.topology_state = toposom::build_topology(config.topology);
+    opts.distances = Distances::never;
+    CudaExecutor ex(data, config.nodes(), opts);  // engine + rows (resident or streamed)
+    tsom_engine* h = ex.engine();
+    auto check = [h](int st) { throw_status(st, tsom_last_error(h)); };
+    check(tsom_set_codebook(h, model.weights.values.data()));
+    toposom::TopologyState& ts = model.topology_state;
+    const bool lattice = toposom::is_lattice(config.topology.kind);
+    if (lattice) check(tsom_set_topology_distance(h, ts.lattice_distances.data()));
+    const bool sampled = sampling.kind != toposom::SamplingKind::full;
+    if (sampled)
+        check(tsom_sampler_init(h, static_cast<int>(sampling.kind),
+                                toposom::resolve_budget(sampling.budget, data.rows()), config.seed,
+                                sampling.alpha, sampling.beta));
+    // schedules and refresh points depend only on t; the refresh counters are
+    // advanced exactly as refresh_topology does (topology.hpp:442-451)
+    const toposom::RefreshPolicy policy = config.resolved_refresh();
+    const double sigma0 = config.resolved_sigma0();
+    const std::size_t total = config.n_iters;
+    std::vector<double> etas(total), sigmas(total);
+    std::vector<char> refresh(total, 0);
+    for (std::size_t t = 0; t < total; ++t) {
+        etas[t] = toposom::schedule_value(config.eta0, config.lr_decay, t, total,
+                                          toposom::kEtaFloor);
+        sigmas[t] = toposom::schedule_value(sigma0, config.radius_decay, t, total,
+                                            config.sigma_min);
+        if (toposom::should_refresh(policy, t, ts)) {
+            refresh[t] = 1;
+            ts.last_refresh_iter = static_cast<std::int64_t>(t);
+            ++ts.refresh_count;
+            if (t >= policy.warmup_iters) ++ts.post_warmup_refreshes;
+        }
+    }
+    const std::size_t P = config.nodes();
+    std::vector<std::uint32_t> edges(lattice ? 0 : P * (P - 1));
+    std::vector<std::uint16_t> hops(lattice ? 0 : P * P);
+    std::uint64_t n_edges = 0;
+    const std::uint32_t flags = (config.use_momentum ? 1u : 0u) | (sampled ? 2u : 0u);
+    toposom::RunLog log;
+    const auto run_start = std::chrono::steady_clock::now();
+    for (std::size_t t = 0; t < total;) {
+        if (options.timeout_s > 0.0) {
+            const std::chrono::duration<double> el = std::chrono::steady_clock::now() - run_start;
+            if (el.count() > options.timeout_s)
+                throw toposom::TrainTimeoutError("training run exceeded timeout of " +
+                                                 std::to_string(options.timeout_s) +
+                                                 " s at iteration " + std::to_string(t));
+        }
+        if (refresh[t])
+            check(tsom_refresh_topology(h, static_cast<int>(config.topology.kind), edges.data(),
+                                        edges.size() / 2, &n_edges, hops.data()));
+        std::size_t t1 = t + 1;
+        if (!options.log_qe)
+            while (t1 < total && !refresh[t1]) ++t1;
+        std::uint32_t failed = 0;
+        check(tsom_train_epochs(h, static_cast<std::uint32_t>(t1 - t), etas.data() + t,
+                                sigmas.data() + t, config.momentum, flags, &failed));
+        for (std::size_t u = t; u < t1; ++u) {
+            toposom::IterationLogEntry e;
+            e.iter = u;
+            e.eta = etas[u];
+            e.sigma = sigmas[u];
+            e.refreshed = refresh[u] != 0;
+            log.iterations.push_back(e);
+        }
+        if (options.log_qe) {
+            double sum = 0.0;
+            std::uint64_t count = 0;
+            check(tsom_qe(h, nullptr, 0, &sum, &count));
+            log.iterations.back().qe_train = sum / static_cast<double>(count);
+        }
+        t = t1;
+    }
+    log.reduce_count = total;
+    check(tsom_get_codebook(h, model.weights.values.data()));
+    check(tsom_get_prev_update(h, model.prev_update.values.data()));
+    if (!lattice) {
+        ts.edges.clear();
+        for (std::uint64_t k = 0; k < n_edges; ++k) ts.edges.emplace_back(edges[2 * k], edges[2 * k + 1]);
+        ts.hop_dist = std::move(hops);
+    }
+    model.iter = total;
+    return {std::move(model), std::move(log)};
 }
 
 /// find_bmus (trainer.hpp:282-308) on the GPU; bit-identical BMU indices.

@@ -107,6 +107,9 @@ uint64_t tsom_rows(const tsom_engine* eng);
 /* Codebook P x d (SomModel::weights, trainer.hpp:106). */
 int tsom_set_codebook(tsom_engine* eng, const float* weights);
 int tsom_get_codebook(tsom_engine* eng, float* weights);
+/* SomModel::prev_update (trainer.hpp:108): the momentum memory the device
+ * update keeps (all zero when momentum is off), P x d f32. */
+int tsom_get_prev_update(tsom_engine* eng, float* prev);
 /* Influence P x P float64 (cached_influence, topology.hpp:406-418).  key is the
  * caller's cache key (e.g. influence_cache_key(sigma) mixed with the topology
  * refresh count); an unchanged non-negative key skips the upload. */

@@ -42,6 +42,7 @@ EXPORTS = [
     "tsom_pairwise_sq_dists", "tsom_bind_shards", "tsom_active_bmu_kernel",
     "tsom_sampler_init", "tsom_sampler_select", "tsom_sampler_observe", "tsom_sampler_state",
     "tsom_mt_selftest", "tsom_release_cached_memory", "tsom_train_epochs",
+    "tsom_get_prev_update",
 ]
 
 SAMPLER_KINDS = {"full": 0, "random": 1, "adaptive": 2}  # SamplingKind, sampling.hpp:163
@@ -100,6 +101,7 @@ def load():
     L.tsom_rows.restype = u64
     L.tsom_set_codebook.argtypes = [_vp, _vp]
     L.tsom_get_codebook.argtypes = [_vp, _vp]
+    L.tsom_get_prev_update.argtypes = [_vp, _vp]
     L.tsom_set_influence.argtypes = [_vp, _vp, i64]
     L.tsom_epoch.argtypes = [_vp, _vp, u64, C.c_double, _vp, _vp, _vp]
     L.tsom_bmu.argtypes = [_vp, _vp, u64, _vp, _vp]

@@ -870,6 +870,16 @@ int tsom_get_codebook(tsom_engine* eng, float* weights) {
     });
 }
 
+int tsom_get_prev_update(tsom_engine* eng, float* prev) {
+    return guarded(eng, [&] {
+        CU(cudaSetDevice(eng->device));
+        REQUIRE(prev, TSOM_ERR_INVALID, "get_prev_update: null buffer");
+        CU(cudaMemcpyAsync(prev, eng->prev.p, (size_t)eng->P * eng->D * sizeof(float),
+                           cudaMemcpyDeviceToHost, eng->stream));
+        CU(cudaStreamSynchronize(eng->stream));
+    });
+}
+
 int tsom_set_influence(tsom_engine* eng, const double* influence, int64_t key) {
     return guarded(eng, [&] {
         CU(cudaSetDevice(eng->device));

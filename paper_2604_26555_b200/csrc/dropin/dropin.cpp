@@ -134,7 +134,17 @@ static void run_train(const dropin_config* rc, const DataSourceRef& src, float* 
         to.log_qe = qe_log != nullptr;
         const auto t0 = std::chrono::steady_clock::now();
         std::pair<SomModel, RunLog> result;
-        if (flags & 16u) {
+        if (flags & 32u) {
+            // every step on the device (toposom_b200::train_device)
+            toposom_b200::DeviceSampling ds;
+            ds.kind = static_cast<SamplingKind>(rc->sampling);
+            ds.budget.mode = rc->budget_fixed ? BudgetMode::fixed : BudgetMode::proportional;
+            ds.budget.m0 = rc->m0;
+            ds.budget.rho = rc->rho;
+            ds.alpha = rc->alpha;
+            ds.beta = rc->beta;
+            result = toposom_b200::train_device(c, src, ds, opts, to);
+        } else if (flags & 16u) {
             // profile: seconds_out[1] = executor construction (bind), [2] = run_iteration
             if (sampler.kind() != SamplingKind::adaptive && !(flags & 8u))
                 opts.distances = toposom_b200::Distances::never;

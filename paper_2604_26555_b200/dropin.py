@@ -136,6 +136,27 @@ def run_study_cuda(base, n_trials: int, seeds, train: np.ndarray, holdout: np.nd
     return qt, qh, fl.astype(bool), secs.value
 
 
+def train_device(cfg, data: np.ndarray, device: int = 0, log_qe: bool = False,
+                 streamed: bool = False):
+    """toposom_b200::train_device: the reference's epoch loop with every step on
+    the device (sampler, refresh, influence, BMU, accumulate, update).
+    Returns (weights, qe_log, refresh_log, seconds)."""
+    L = load()
+    data = np.ascontiguousarray(data, np.float32)
+    n, d = data.shape
+    w = np.empty((cfg.nodes, d), np.float32)
+    qe = np.zeros(cfg.n_iters) if log_qe else None
+    ref = np.zeros(cfg.n_iters, np.uint8)
+    secs = (C.c_double * 3)()
+    flags = (1 if streamed else 0) | 32
+    st = L.tsom_dropin_train(C.byref(_cfg(cfg)), data.ctypes.data, n, d, w.ctypes.data,
+                             qe.ctypes.data if log_qe else None, ref.ctypes.data, device, flags,
+                             secs)
+    if st:
+        _lib._raise(st, L.tsom_dropin_last_error().decode())
+    return w, qe, ref, secs[0]
+
+
 def train_cuda(cfg, data: np.ndarray, device: int = 0, log_qe: bool = False,
                streamed: bool = False, bmu_kernel: int = 0, force_distances: bool = False,
                profile: bool = False):

@@ -603,3 +603,33 @@ def test_train_epochs_reports_the_failing_epoch(pkg, oracle_port):
         books.append(e.get_codebook())
         e.close()
     assert np.array_equal(books[0], books[1])
+
+
+@pytest.mark.parametrize("kw", DROPIN_CONFIGS, ids=lambda k: f"{k['topology']}")
+def test_train_device_vs_golden(pkg, kw):
+    """toposom_b200::train_device (every step on the device) vs the reference loop +
+    SerialExecutor: same bars as the drop-in loop."""
+    from paper_2604_26555_b200 import dropin
+    if not dropin.available():
+        pytest.skip("libtsom_dropin.so not built")
+    g = np.load(os.path.join(GOLDEN, "train_runs.npz"))
+    i = DROPIN_CONFIGS.index(kw)
+    cfg = dropin.TrainConfig(**kw)
+    w, qe, ref, _ = dropin.train_device(cfg, g["x"], log_qe=True)
+    assert rel_maxnorm(w, g[f"w{i}"]) <= 1e-4
+    np.testing.assert_allclose(qe, g[f"qe{i}"], rtol=1e-5)
+    # the refresh schedule is the reference's
+    w2, _, ref2, _ = dropin.train_cuda(cfg, g["x"])
+    assert np.array_equal(ref, ref2)
+
+
+def test_train_device_config1(pkg, oracle_port):
+    from paper_2604_26555_b200 import dropin
+    if not dropin.available():
+        pytest.skip("libtsom_dropin.so not built")
+    g = np.load(os.path.join(GOLDEN, "config1_20k.npz"))
+    x = oracle_port.synth_gmm(int(g["n"]), 50, int(g["seed"]))
+    cfg = dropin.TrainConfig(topology="rect", grid_w=10, grid_h=10, n_iters=10,
+                             seed=int(g["seed"]))
+    w, _, _, _ = dropin.train_device(cfg, x)
+    assert rel_maxnorm(w, g["w"]) <= 1e-4
