@@ -743,8 +743,8 @@ __global__ void __launch_bounds__(EpiCfg<kKind>::kThreads, 1)
     _Pragma("unroll") for (int m = 0; m < 16; ++m) mn[m & 3] =                             \
         fmin3f(mn[m & 3], __uint_as_float(r[2 * m]), __uint_as_float(r[2 * m + 1]))
 #define TSOM_PASS2(r, cb)                                                                   \
-    _Pragma("unroll") for (int k = 0; k < 32; ++k) a[k & 3] =                              \
-        fmaf(__saturatef(fmaf(__uint_as_float(r[k]), nb, lb)), (float)((cb) + k + 256), a[k & 3])
+    _Pragma("unroll") for (int k = 0; k < 32; ++k) a[k & 7] =                              \
+        fmaf(__saturatef(fmaf(__uint_as_float(r[k]), nb, lb)), (float)((cb) + k + 256), a[k & 7])
 #define TSOM_ALL(P)                                                                         \
     do {                                                                                    \
         if (full) {                                                                         \
@@ -765,14 +765,14 @@ __global__ void __launch_bounds__(EpiCfg<kKind>::kThreads, 1)
                 const int ef = (int)((__float_as_uint(lim) >> 23) & 0xFFu);
                 const float big = __int_as_float(max(67, min(247, 314 - ef)) << 23);
                 const float lb = lim * big, nb = -big;
-                float a[4] = {0.0f, 0.0f, 0.0f, 0.0f};
+                float a[8] = {0.0f, 0.0f, 0.0f, 0.0f, 0.0f, 0.0f, 0.0f, 0.0f};
                 TSOM_ALL(TSOM_PASS2);
 #undef TSOM_ALL
 #undef TSOM_PASS1
 #undef TSOM_PASS2
                 if (lane == 0 && q == 0) TSOM_TRACE(4 + 3 * (set & 1), it_);
                 // a = 256 count + sum(local ids); decode: exactly one -> global id
-                const float asum = (a[0] + a[1]) + (a[2] + a[3]);
+                const float asum = ((a[0] + a[1]) + (a[2] + a[3])) + ((a[4] + a[5]) + (a[6] + a[7]));
                 uint32_t code = 0xFFFFFFFFu;  // id relative to the set's first column
                 if (asum >= 256.0f && asum < 512.0f && asum == floorf(asum))
                     code = (uint32_t)asum - 256u;
