@@ -633,3 +633,17 @@ def test_train_device_config1(pkg, oracle_port):
                              seed=int(g["seed"]))
     w, _, _, _ = dropin.train_device(cfg, x)
     assert rel_maxnorm(w, g["w"]) <= 1e-4
+
+
+def test_train_device_streamed_equals_resident(pkg):
+    # the device loop over rows streamed from host memory every epoch gives the
+    # codebook of the resident run
+    from paper_2604_26555_b200 import dropin
+    if not dropin.available():
+        pytest.skip("libtsom_dropin.so not built")
+    g = np.load(os.path.join(GOLDEN, "train_runs.npz"))
+    cfg = dropin.TrainConfig(**DROPIN_CONFIGS[1])  # MST: refreshes on the device
+    w_res, _, ref_res, _ = dropin.train_device(cfg, g["x"])
+    w_str, _, ref_str, _ = dropin.train_device(cfg, g["x"], streamed=True)
+    assert np.array_equal(ref_res, ref_str)
+    assert rel_maxnorm(w_str, w_res.astype(np.float64)) <= 1e-6
