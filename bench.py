@@ -295,6 +295,18 @@ def run_gpu_arm(args):
         rechecks.append(eng.last_recheck_count)
     s, c = eng.qe()
     qe_gpu = s / c
+    # QE vs the CPU oracle: the trained codebook's mean BMU distance over a
+    # 20,000-row sample, GPU (tsom_bmu) against the oracle's find_bmus
+    qe_check = None
+    if rank == 0 and not args.no_cpu:
+        import oracle
+        w_fin = eng.get_codebook()
+        sample = np.ascontiguousarray(host[:20_000])
+        _, d_gpu = eng.bmu(sample)
+        _, d_cpu = oracle.port.find_bmus(sample, w_fin)
+        qe_check = {"rows": len(sample), "qe_gpu": float(np.mean(d_gpu)),
+                    "qe_cpu_oracle": float(np.mean(d_cpu)),
+                    "rel_diff": float(abs(np.mean(d_gpu) - np.mean(d_cpu)) / np.mean(d_cpu))}
 
     eng.close()
     eng = None
@@ -412,6 +424,7 @@ def run_gpu_arm(args):
         "clocks": clk.summary(),
         "gpu_launches": int(launches),
         "qe_gpu_after": qe_gpu,
+        "qe_vs_cpu": qe_check,
         "rechecked_rows_per_epoch": statistics.mean(rechecks) if rechecks else None,
     }
     if e2e:
