@@ -252,6 +252,12 @@ const uint32_t* normalise_selection(Engine* eng, const uint32_t* sel, uint64_t n
     return sel;
 }
 
+// the rows get a 256-B-stride copy for the gathers (d even, <= 62; <= 32 GB)
+bool pad_eligible(const Engine* eng) {
+    return eng->D % 2 == 0 && eng->D <= tsom::kPadFloats - 2 &&
+           eng->n_rows * (uint64_t)tsom::kPadFloats * 4 <= (32ull << 30);
+}
+
 // K2 scratch (counting sort + piece partials) sized for `rows` rows per launch.
 void ensure_accum(Engine* eng, uint64_t rows) {
     if (rows <= eng->acc_rows && eng->acc.counts) return;
@@ -315,8 +321,7 @@ void accumulate_epoch(Engine* eng, const uint32_t* sel_host, uint64_t n_sel, boo
         // a 256-B-stride copy of the rows for the gathered splits and the K2
         // gather (built once per bind)
         const float* xpad = nullptr;
-        if (eng->D % 2 == 0 && eng->D <= tsom::kPadFloats - 2 &&
-            eng->n_rows * (uint64_t)tsom::kPadFloats * 4 <= (32ull << 30)) {
+        if (pad_eligible(eng)) {
             if (!eng->xpad_valid) {
                 CU(eng->xpad.ensure(eng->n_rows * (uint64_t)tsom::kPadFloats * sizeof(float)));
                 tsom::launch_pad_rows(eng->x.as<float>(), eng->n_rows, eng->D,
@@ -673,7 +678,35 @@ int tsom_bind_host_data(tsom_engine* eng, const float* rows, uint64_t n_rows, ui
         const bool pinned = n_rows && cudaPointerGetAttributes(&pa, rows) == cudaSuccess &&
                             pa.type == cudaMemoryTypeHost;
         cudaGetLastError();
-        if (pinned || bytes < ((size_t)64 << 20)) {
+        bool norms_done = false;
+        if (pinned && bytes >= ((size_t)256 << 20)) {
+            // page-locked rows in 8 chunks on the copy stream; the row-norm
+            // maximum and the 256-B-stride copy of each chunk run on the
+            // engine stream while the next chunk is in flight
+            const bool pad = pad_eligible(eng);
+            if (pad) CU(eng->xpad.ensure(n_rows * (uint64_t)tsom::kPadFloats * sizeof(float)));
+            CU(cudaMemsetAsync(eng->x2max.p, 0, sizeof(float), eng->stream));
+            const uint64_t C = (n_rows + 7) / 8;
+            for (uint64_t r0 = 0; r0 < n_rows; r0 += C) {
+                const uint64_t nr = std::min(C, n_rows - r0);
+                CU(cudaMemcpyAsync(eng->x.as<float>() + r0 * eng->D, rows + r0 * eng->D,
+                                   nr * eng->D * sizeof(float), cudaMemcpyHostToDevice,
+                                   eng->copy_stream));
+                cudaEvent_t ev;
+                CU(cudaEventCreateWithFlags(&ev, cudaEventDisableTiming));
+                CU(cudaEventRecord(ev, eng->copy_stream));
+                CU(cudaStreamWaitEvent(eng->stream, ev, 0));
+                cudaEventDestroy(ev);  // released once the wait has been satisfied
+                tsom::launch_row_norm_max(eng->x.as<float>() + r0 * eng->D, nr, eng->D,
+                                          eng->x2max.as<float>(), eng->stream, false);
+                if (pad)
+                    tsom::launch_pad_rows(eng->x.as<float>() + r0 * eng->D, nr, eng->D,
+                                          eng->xpad.as<float>() + r0 * tsom::kPadFloats,
+                                          eng->stream);
+            }
+            eng->xpad_valid = pad;
+            norms_done = true;
+        } else if (pinned || bytes < ((size_t)64 << 20)) {
             // on the stream the norm kernel below runs on (a plain cudaMemcpy
             // from pageable memory may return before its DMA lands)
             if (bytes)
@@ -696,8 +729,9 @@ int tsom_bind_host_data(tsom_engine* eng, const float* rows, uint64_t n_rows, ui
                     std::chrono::duration<double, std::milli>(tb1 - tb0).count(),
                     std::chrono::duration<double, std::milli>(tb2 - tb1).count());
         }
-        tsom::launch_row_norm_max(eng->x.as<float>(), n_rows, eng->D, eng->x2max.as<float>(),
-                                  eng->stream);
+        if (!norms_done)
+            tsom::launch_row_norm_max(eng->x.as<float>(), n_rows, eng->D,
+                                      eng->x2max.as<float>(), eng->stream);
         CU(cudaGetLastError());
         CU(cudaStreamSynchronize(eng->stream));
     });

@@ -316,7 +316,8 @@ struct Engine {
 void launch_prep_codebook(const float* w, uint32_t P, uint32_t D, double* w2, float* w2max,
                           float* wt, uint32_t Ppad, cudaStream_t st);
 // max ||x||^2 over rows (f32 atomic max on non-negative floats)
-void launch_row_norm_max(const float* x, uint64_t n, uint32_t D, float* out, cudaStream_t st);
+void launch_row_norm_max(const float* x, uint64_t n, uint32_t D, float* out, cudaStream_t st,
+                         bool reset = true);  // reset = false: fold into *out (atomicMax)
 // a[0] = max(a[0], a[1])
 void launch_fold_max(float* a, cudaStream_t st);
 // split rows (optionally gathered through sel, and/or through a position list

@@ -67,8 +67,9 @@ __global__ void k_row_norm_max(const float* __restrict__ x, uint64_t n, uint32_t
     if ((threadIdx.x & 31) == 0) atomicMax(reinterpret_cast<int*>(out), __float_as_int(best));
 }
 
-void launch_row_norm_max(const float* x, uint64_t n, uint32_t D, float* out, cudaStream_t st) {
-    cudaMemsetAsync(out, 0, sizeof(float), st);
+void launch_row_norm_max(const float* x, uint64_t n, uint32_t D, float* out, cudaStream_t st,
+                         bool reset) {
+    if (reset) cudaMemsetAsync(out, 0, sizeof(float), st);
     if (n == 0) return;
     uint64_t blocks = (n + 255) / 256;
     if (blocks > 148 * 16) blocks = 148 * 16;
