@@ -21,6 +21,8 @@
 #include <chrono>
 #include <cmath>
 #include <cstdint>
+#include <cstring>
+#include <future>
 #include <limits>
 #include <memory>
 #include <stdexcept>
@@ -29,6 +31,7 @@
 #include <vector>
 
 #include "toposom/metrics.hpp"
+#include "toposom/parallel.hpp"
 #include "toposom/trainer.hpp"
 #include "toposom/tune.hpp"
 #include "tsom_b200.h"
@@ -47,6 +50,7 @@ inline void throw_status(int status, const char* msg) {
         case TSOM_ERR_INVALID: throw std::invalid_argument(m);
         case TSOM_ERR_RANGE: throw std::out_of_range(m);
         case TSOM_ERR_NUMERICAL: throw std::runtime_error(m);
+        case TSOM_ERR_TIMEOUT: throw std::runtime_error(m);  // collect_with_barrier's error
         default: throw std::runtime_error("toposom_b200: " + m);
     }
 }
@@ -69,9 +73,107 @@ enum class Distances { always, never };
 
 struct CudaOptions {
     int device = 0;
+    // more than one entry: one engine per entry, each owning a contiguous
+    // slice of the rows (assign_shards, parallel.hpp:28-41), joined by an
+    // in-process rank group with one ordered reduce per epoch — the
+    // ThreadedExecutor shape (parallel.hpp:99-140) with GPUs as workers.  The
+    // same device may repeat (several engines on one GPU).
+    std::vector<int> devices;
     bool streamed = false;            // keep rows in host memory, stream every epoch
     Distances distances = Distances::always;
     int bmu_kernel = 0;               // 0 auto (tcgen05), 1 SIMT, 2 tcgen05
+    double barrier_timeout_s = toposom::kDefaultBarrierTimeoutS;  // parallel.hpp:24
+};
+
+/// G engines joined by an in-process rank group (tsom_group_*): each owns
+/// rows [slice.first, slice.second) of the data.  for_each runs a step on
+/// every engine from its own thread and rethrows the first failure in engine
+/// order, like collect_with_barrier (parallel.hpp:67-86); a rank that misses
+/// the reduce deadline fails its peers' reduce with TSOM_ERR_TIMEOUT.
+class EngineSet {
+public:
+    EngineSet(const DataSourceRef& data, std::size_t nodes, const CudaOptions& opts) {
+        std::vector<int> devs = opts.devices;
+        if (devs.empty()) devs.push_back(opts.device);
+        const std::size_t G = devs.size();
+        if (G > 1 && !data.in_memory())
+            throw std::invalid_argument(
+                "CudaExecutor: several devices need an in-memory DataMatrix (shard sources bind "
+                "to one engine)");
+        slices_ = toposom::assign_shards(data.rows(), G);
+        if (G > 1) {
+            const int st = tsom_group_create(static_cast<int>(G), &group_);
+            if (st) throw_status(st, "tsom_group_create failed");
+        }
+        for (std::size_t g = 0; g < G; ++g) {
+            engines_.push_back(std::make_unique<Engine>(devs[g], nodes, data.cols()));
+            Engine& e = *engines_.back();
+            if (opts.bmu_kernel)
+                e.check(tsom_set_option(e.h, TSOM_OPT_BMU_KERNEL, opts.bmu_kernel));
+            e.check(tsom_set_option(e.h, TSOM_OPT_BARRIER_TIMEOUT_MS,
+                                    std::max<std::int64_t>(1, std::llround(opts.barrier_timeout_s * 1e3))));
+            if (group_) e.check(tsom_group_join(e.h, group_, static_cast<int>(g)));
+        }
+        const std::uint32_t flags = opts.streamed ? TSOM_BIND_STREAMED : TSOM_BIND_COPY;
+        if (data.in_memory()) {
+            const DataMatrix* rows = data.matrix();
+            for_each([&](std::size_t g, tsom_engine* h) {
+                const auto& sl = slices_[g];
+                return tsom_bind_host_data(h, rows->values.data() + sl.first * rows->cols,
+                                           sl.second - sl.first, flags);
+            });
+        } else {
+            // Shard-backed source: the engine reads the FSOMSHRD files itself
+            // (copied once into HBM, or streamed from disk every epoch through
+            // pinned staging), replacing the per-epoch rescans of
+            // DataSourceRef::fetch_rows (dataset.hpp:400-415).
+            std::vector<std::string> names;
+            for (const auto& p : data.shards()->shard_paths) names.push_back(p.string());
+            std::vector<const char*> cpaths;
+            for (const auto& n : names) cpaths.push_back(n.c_str());
+            engines_[0]->check(tsom_bind_shards(engines_[0]->h, cpaths.data(),
+                                                (std::uint32_t)cpaths.size(), flags));
+        }
+    }
+    ~EngineSet() {
+        engines_.clear();
+        if (group_) tsom_group_destroy(group_);
+    }
+    EngineSet(const EngineSet&) = delete;
+    EngineSet& operator=(const EngineSet&) = delete;
+
+    std::size_t size() const { return engines_.size(); }
+    tsom_engine* handle(std::size_t g) const { return engines_[g]->h; }
+    const std::pair<std::size_t, std::size_t>& slice(std::size_t g) const { return slices_[g]; }
+
+    /// f(g, engine) -> C-ABI status, on every engine concurrently (inline when G = 1)
+    template <typename F>
+    void for_each(F&& f) {
+        const std::size_t G = engines_.size();
+        if (G == 1) {
+            engines_[0]->check(f(std::size_t{0}, engines_[0]->h));
+            return;
+        }
+        std::vector<std::future<int>> fut;
+        fut.reserve(G);
+        for (std::size_t g = 0; g < G; ++g)
+            fut.push_back(std::async(std::launch::async, [&f, g, this] { return f(g, engines_[g]->h); }));
+        std::vector<int> st(G);
+        for (std::size_t g = 0; g < G; ++g) st[g] = fut[g].get();
+        // the first failure in worker order; a peer's "aborted" follows a timeout
+        for (int pass = 0; pass < 2; ++pass)
+            for (std::size_t g = 0; g < G; ++g)
+                if (st[g] != TSOM_OK) {
+                    const char* m = tsom_last_error(engines_[g]->h);
+                    if (pass == 0 && std::strncmp(m, "reduce barrier aborted", 22) == 0) continue;
+                    throw_status(st[g], m);
+                }
+    }
+
+private:
+    std::vector<std::pair<std::size_t, std::size_t>> slices_;
+    tsom_group* group_ = nullptr;
+    std::vector<std::unique_ptr<Engine>> engines_;
 };
 
 /// Convert the engine's float64 U/H into the reference's fixed-point
@@ -86,30 +188,15 @@ inline toposom::AccumInt to_fixed(double v) {
 class CudaExecutor {
 public:
     CudaExecutor(const DataSourceRef& data, std::size_t nodes, const CudaOptions& opts = {})
-        : opts_(opts), eng_(std::make_unique<Engine>(opts.device, nodes, data.cols())),
-          nodes_(nodes), dims_(data.cols()) {
-        if (opts.bmu_kernel) eng_->check(tsom_set_option(eng_->h, TSOM_OPT_BMU_KERNEL, opts.bmu_kernel));
-        if (data.in_memory()) {
-            rows_ = data.matrix();
-            eng_->check(tsom_bind_host_data(eng_->h, rows_->values.data(), rows_->rows,
-                                            opts.streamed ? TSOM_BIND_STREAMED : TSOM_BIND_COPY));
-        } else {
-            // Shard-backed source: the engine reads the FSOMSHRD files itself
-            // (copied once into HBM, or streamed from disk every epoch through
-            // pinned staging), replacing the per-epoch rescans of
-            // DataSourceRef::fetch_rows (dataset.hpp:400-415).
-            std::vector<std::string> names;
-            for (const auto& p : data.shards()->shard_paths) names.push_back(p.string());
-            std::vector<const char*> cpaths;
-            for (const auto& n : names) cpaths.push_back(n.c_str());
-            eng_->check(tsom_bind_shards(eng_->h, cpaths.data(), (std::uint32_t)cpaths.size(),
-                                         opts.streamed ? TSOM_BIND_STREAMED : TSOM_BIND_COPY));
-        }
-    }
+        : opts_(opts), set_(data, nodes, opts), nodes_(nodes), dims_(data.cols()) {}
 
     /// Executor::run_iteration (trainer.hpp:446-453): one accumulation pass
     /// plus the single reduce.  n_chunks is result-invariant by contract
-    /// (test_trainer.cpp:315-333) and therefore not used.
+    /// (test_trainer.cpp:315-333) and therefore not used.  With several
+    /// engines the sorted selection is split by row owner (each engine gets
+    /// the ids in its slice, made local), every engine runs its pass from its
+    /// own thread, the ranks' sums meet in one ordered reduce, and the
+    /// distances land in selection order (the slices are contiguous).
     IterationAccumulators run_iteration(const std::vector<std::uint32_t>& selected,
                                         const DataMatrix& weights,
                                         const std::vector<double>& influence, double eta,
@@ -118,35 +205,65 @@ public:
             throw std::invalid_argument("accumulate: accumulator shape mismatch");
         if (influence.size() != nodes_ * nodes_)
             throw std::invalid_argument("accumulate: influence shape mismatch");
-        eng_->check(tsom_set_codebook(eng_->h, weights.values.data()));
-        eng_->check(tsom_set_influence(eng_->h, influence.data(), -1));
+        const std::size_t G = set_.size();
+        // the reference's loop hands in cached_influence(...) (topology.hpp:406-418):
+        // upload only when its content changed (compared, not keyed by address)
+        const bool new_infl = influence != infl_;
+        if (new_infl) infl_ = influence;
+        for (std::uint32_t id : selected)
+            if (id >= set_.slice(G - 1).second)
+                throw std::out_of_range("fetch_rows: row index beyond data size");
         u_.resize(nodes_ * dims_);
         h_.resize(nodes_);
         distances.clear();
-        double* dist_out = nullptr;
-        if (opts_.distances == Distances::always) {
-            distances.resize(selected.size());
-            dist_out = distances.data();
-        }
-        static const std::uint32_t kNone = 0;  // non-null + n_sel 0 = empty selection
-        const std::uint32_t* sel = selected.empty() ? &kNone : selected.data();
-        eng_->check(tsom_epoch(eng_->h, sel, selected.size(), eta, u_.data(), h_.data(), dist_out));
+        const bool want_dist = opts_.distances == Distances::always;
+        if (want_dist) distances.resize(selected.size());
+        // selection split by owner (sorted ids: one lower_bound per slice)
+        std::vector<std::size_t> p(G + 1, selected.size());
+        p[0] = 0;
+        for (std::size_t g = 1; g < G; ++g)
+            p[g] = static_cast<std::size_t>(
+                std::lower_bound(selected.begin(), selected.end(),
+                                 static_cast<std::uint32_t>(set_.slice(g).first)) -
+                selected.begin());
+        local_.resize(G);
+        set_.for_each([&](std::size_t g, tsom_engine* h) {
+            int st = tsom_set_codebook(h, weights.values.data());
+            if (!st && new_infl) st = tsom_set_influence(h, influence.data(), -1);
+            if (st) return st;
+            static const std::uint32_t kNone = 0;  // non-null + n_sel 0 = empty selection
+            const std::uint32_t* sel = &kNone;
+            const std::size_t n = p[g + 1] - p[g];
+            if (G == 1) {
+                if (n) sel = selected.data();
+            } else if (n) {
+                const std::uint32_t o = static_cast<std::uint32_t>(set_.slice(g).first);
+                local_[g].assign(selected.begin() + p[g], selected.begin() + p[g + 1]);
+                for (auto& v : local_[g]) v -= o;
+                sel = local_[g].data();
+            }
+            return tsom_epoch(h, sel, n, eta, g == 0 ? u_.data() : nullptr,
+                              g == 0 ? h_.data() : nullptr,
+                              want_dist ? distances.data() + p[g] : nullptr);
+        });
         IterationAccumulators acc(nodes_, dims_);
         for (std::size_t i = 0; i < u_.size(); ++i) acc.u[i] = to_fixed(u_[i]);
         for (std::size_t j = 0; j < nodes_; ++j) acc.h[j] = to_fixed(h_[j]);
         return acc;
     }
 
-    std::size_t workers() const { return 1; }
-    double barrier_wait_s() const { return 0.0; }
-    tsom_engine* engine() const { return eng_->h; }
+    std::size_t workers() const { return set_.size(); }
+    /// seconds rank 0 spent waiting in the reduce (ThreadedExecutor::barrier_wait_s)
+    double barrier_wait_s() const { return tsom_barrier_wait_s(set_.handle(0)); }
+    tsom_engine* engine() const { return set_.handle(0); }
+    EngineSet& engines() { return set_; }
 
 private:
     CudaOptions opts_;
-    std::unique_ptr<Engine> eng_;
+    EngineSet set_;
     std::size_t nodes_, dims_;
-    const DataMatrix* rows_ = nullptr;
-    std::vector<double> u_, h_;
+    std::vector<double> u_, h_, infl_;
+    std::vector<std::vector<std::uint32_t>> local_;
 };
 
 /// GPU analogue of toposom::train / train_parallel (trainer.hpp:526-530,
@@ -181,7 +298,11 @@ struct DeviceSampling {
 /// call followed by the device QE.  options.timeout_s is checked between
 /// calls.  Returns the reference's (SomModel, RunLog): weights, momentum
 /// memory, topology state (edges, hop counts and refresh counters of the last
-/// refresh for graphs) and one log entry per epoch.
+/// refresh for graphs) and one log entry per epoch.  With opts.devices the
+/// rows are split over several engines (EngineSet) that run every step in
+/// lockstep from their own threads: one ordered reduce per epoch, one sharded
+/// device sampler over all rows, identical refreshes and updates on every
+/// engine (the multi-GPU epoch of SURVEY.md §8(e)).
 inline std::pair<toposom::SomModel, toposom::RunLog> train_device(
     const toposom::SomConfig& config, const DataSourceRef& data, DeviceSampling sampling = {},
     CudaOptions opts = {}, const toposom::TrainOptions& options = {}) {
@@ -192,18 +313,22 @@ inline std::pair<toposom::SomModel, toposom::RunLog> train_device(
     model.prev_update = DataMatrix(config.nodes(), data.cols());
     model.topology_state = toposom::build_topology(config.topology);
     opts.distances = Distances::never;
-    CudaExecutor ex(data, config.nodes(), opts);  // engine + rows (resident or streamed)
-    tsom_engine* h = ex.engine();
+    EngineSet es(data, config.nodes(), opts);  // engines + their rows (resident or streamed)
+    tsom_engine* h = es.handle(0);
     auto check = [h](int st) { throw_status(st, tsom_last_error(h)); };
-    check(tsom_set_codebook(h, model.weights.values.data()));
     toposom::TopologyState& ts = model.topology_state;
     const bool lattice = toposom::is_lattice(config.topology.kind);
-    if (lattice) check(tsom_set_topology_distance(h, ts.lattice_distances.data()));
     const bool sampled = sampling.kind != toposom::SamplingKind::full;
-    if (sampled)
-        check(tsom_sampler_init(h, static_cast<int>(sampling.kind),
-                                toposom::resolve_budget(sampling.budget, data.rows()), config.seed,
-                                sampling.alpha, sampling.beta));
+    const std::uint64_t m_sel = sampled ? toposom::resolve_budget(sampling.budget, data.rows()) : 0;
+    es.for_each([&](std::size_t, tsom_engine* e) {
+        int st = tsom_set_codebook(e, model.weights.values.data());
+        if (!st && lattice) st = tsom_set_topology_distance(e, ts.lattice_distances.data());
+        // one Sampler over all rows; with several engines it is sharded over them
+        if (!st && sampled)
+            st = tsom_sampler_init(e, static_cast<int>(sampling.kind), m_sel, config.seed,
+                                   sampling.alpha, sampling.beta);
+        return st;
+    });
     // schedules and refresh points depend only on t; the refresh counters are
     // advanced exactly as refresh_topology does (topology.hpp:442-451)
     const toposom::RefreshPolicy policy = config.resolved_refresh();
@@ -239,14 +364,21 @@ inline std::pair<toposom::SomModel, toposom::RunLog> train_device(
                                                  " s at iteration " + std::to_string(t));
         }
         if (refresh[t])
-            check(tsom_refresh_topology(h, static_cast<int>(config.topology.kind), edges.data(),
-                                        edges.size() / 2, &n_edges, hops.data()));
+            es.for_each([&](std::size_t g, tsom_engine* e) {
+                return g == 0 ? tsom_refresh_topology(e, static_cast<int>(config.topology.kind),
+                                                      edges.data(), edges.size() / 2, &n_edges,
+                                                      hops.data())
+                              : tsom_refresh_topology(e, static_cast<int>(config.topology.kind),
+                                                      nullptr, 0, nullptr, nullptr);
+            });
         std::size_t t1 = t + 1;
         if (!options.log_qe)
             while (t1 < total && !refresh[t1]) ++t1;
-        std::uint32_t failed = 0;
-        check(tsom_train_epochs(h, static_cast<std::uint32_t>(t1 - t), etas.data() + t,
-                                sigmas.data() + t, config.momentum, flags, &failed));
+        es.for_each([&](std::size_t, tsom_engine* e) {
+            std::uint32_t failed = 0;
+            return tsom_train_epochs(e, static_cast<std::uint32_t>(t1 - t), etas.data() + t,
+                                     sigmas.data() + t, config.momentum, flags, &failed);
+        });
         for (std::size_t u = t; u < t1; ++u) {
             toposom::IterationLogEntry e;
             e.iter = u;
@@ -258,7 +390,11 @@ inline std::pair<toposom::SomModel, toposom::RunLog> train_device(
         if (options.log_qe) {
             double sum = 0.0;
             std::uint64_t count = 0;
-            check(tsom_qe(h, nullptr, 0, &sum, &count));
+            es.for_each([&](std::size_t g, tsom_engine* e) {
+                double s2 = 0.0;
+                std::uint64_t c2 = 0;
+                return g == 0 ? tsom_qe(e, nullptr, 0, &sum, &count) : tsom_qe(e, nullptr, 0, &s2, &c2);
+            });
             log.iterations.back().qe_train = sum / static_cast<double>(count);
         }
         t = t1;

@@ -61,8 +61,14 @@ extern "C" {
 #define TSOM_OPT_HOST_REGISTER 5   /* streamed host rows: 1 (default) page-lock the caller's
                                       buffer for direct DMA, 0 copy through pinned staging */
 #define TSOM_OPT_STAGING_THREADS 6 /* host threads filling the pinned staging (default: min(16, cores)) */
+#define TSOM_OPT_BARRIER_TIMEOUT_MS 7 /* reduce-barrier deadline, ms (default 60000 =
+                                         kDefaultBarrierTimeoutS, parallel.hpp:24); a rank that
+                                         misses it fails the call with TSOM_ERR_TIMEOUT
+                                         "reduce barrier timed out after X s waiting for worker g"
+                                         (collect_with_barrier, parallel.hpp:67-86) */
 
 typedef struct tsom_engine tsom_engine;
+typedef struct tsom_group tsom_group;
 
 /* Engine lifetime ---------------------------------------------------------- */
 
@@ -214,10 +220,26 @@ int tsom_release_cached_memory(int device);
 
 /* 128-byte ncclUniqueId produced by rank 0 and broadcast by the caller. */
 int tsom_comm_unique_id(tsom_engine* eng, uint8_t id_out[128]);
-/* Attach an NCCL communicator; every epoch then ends with exactly one
- * ncclAllReduce(sum, float64) of the packed [S | c | sum dist | count] buffer
- * (parallel.hpp:90-95 reduce). */
+/* Attach an NCCL communicator (non-blocking: initialisation and every reduce
+ * are polled against TSOM_OPT_BARRIER_TIMEOUT_MS and aborted with
+ * ncclCommAbort -> TSOM_ERR_TIMEOUT when a peer never arrives); every epoch then
+ * ends with exactly one ncclAllReduce(sum, float64) of the packed
+ * [S | c | sum dist | count] buffer (parallel.hpp:90-95 reduce). */
 int tsom_comm_init(tsom_engine* eng, const uint8_t id[128], int rank, int world);
+/* In-process rank group: `world` engines driven from separate threads of one
+ * process (one per GPU, the ThreadedExecutor shape of parallel.hpp:99-140, or
+ * several on one GPU) joined by a host-memory reduce instead of NCCL.  Each
+ * rank's contribution is kept and the reduce is evaluated in rank order
+ * (parallel.hpp:90-95), so every rank gets the same sums; a rank that misses
+ * the barrier deadline is named ("reduce barrier timed out after X s waiting
+ * for worker g", TSOM_ERR_TIMEOUT).  The sharded device sampler uses the same
+ * group.  Destroy the group after its engines. */
+int tsom_group_create(int world, tsom_group** out);
+int tsom_group_join(tsom_engine* eng, tsom_group* group, int rank);
+int tsom_group_destroy(tsom_group* group);
+/* Seconds this engine has spent in reduce barriers
+ * (ThreadedExecutor::barrier_wait_s, parallel.hpp:136). */
+double tsom_barrier_wait_s(const tsom_engine* eng);
 
 /* Timing of the last epoch (device events), milliseconds. */
 int tsom_last_timing(const tsom_engine* eng, float* bmu_ms, float* accum_ms, float* smooth_ms,

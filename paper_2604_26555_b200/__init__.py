@@ -6,8 +6,8 @@ in ``include/tsom_b200.h``) and the C++ drop-in executor in
 binding plus a reference-shaped API; importing it loads the CUDA library and
 fails loudly if it is missing (there is no CPU fallback).
 """
-from ._lib import (Engine, InvalidArgument, NumericalFault, OutOfRange, TsomError,  # noqa: F401
-                   load, version)
+from ._lib import (BarrierTimeout, Engine, InvalidArgument, RankGroup,  # noqa: F401
+                   NumericalFault, OutOfRange, TsomError, load, version)
 from .api import (Accumulators, CudaExecutor, ResidentConfig, find_bmus,  # noqa: F401
                   map_samples, mean_bmu_distance, quantization_error, train_resident)
 

@@ -30,6 +30,7 @@ TSOM_OPT_TIE_TAU = 2
 TSOM_OPT_STREAM_CHUNK = 3
 TSOM_OPT_HOST_REGISTER = 5
 TSOM_OPT_STAGING_THREADS = 6
+TSOM_OPT_BARRIER_TIMEOUT_MS = 7
 
 # Every symbol include/tsom_b200.h declares (checked by tests/test_abi.py).
 EXPORTS = [
@@ -42,7 +43,8 @@ EXPORTS = [
     "tsom_pairwise_sq_dists", "tsom_bind_shards", "tsom_active_bmu_kernel",
     "tsom_sampler_init", "tsom_sampler_select", "tsom_sampler_observe", "tsom_sampler_state",
     "tsom_mt_selftest", "tsom_release_cached_memory", "tsom_train_epochs",
-    "tsom_get_prev_update",
+    "tsom_get_prev_update", "tsom_barrier_wait_s", "tsom_group_create", "tsom_group_join",
+    "tsom_group_destroy",
 ]
 
 SAMPLER_KINDS = {"full": 0, "random": 1, "adaptive": 2}  # SamplingKind, sampling.hpp:163
@@ -68,9 +70,14 @@ class OutOfRange(TsomError, IndexError):
     pass
 
 
+class BarrierTimeout(TsomError):
+    """A rank missed the reduce barrier's deadline (collect_with_barrier,
+    parallel.hpp:67-86: std::runtime_error "reduce barrier timed out ...")."""
+
+
 def _raise(status: int, msg: str):
     cls = {TSOM_ERR_INVALID: InvalidArgument, TSOM_ERR_NUMERICAL: NumericalFault,
-           TSOM_ERR_RANGE: OutOfRange}.get(status, TsomError)
+           TSOM_ERR_RANGE: OutOfRange, TSOM_ERR_TIMEOUT: BarrierTimeout}.get(status, TsomError)
     raise cls(status, msg)
 
 
@@ -131,6 +138,11 @@ def load():
     L.tsom_bind_shards.argtypes = [_vp, C.POINTER(C.c_char_p), u32, u32]
     L.tsom_stream.argtypes = [_vp]
     L.tsom_stream.restype = _vp
+    L.tsom_barrier_wait_s.argtypes = [_vp]
+    L.tsom_barrier_wait_s.restype = C.c_double
+    L.tsom_group_create.argtypes = [i32, C.POINTER(_vp)]
+    L.tsom_group_join.argtypes = [_vp, _vp, i32]
+    L.tsom_group_destroy.argtypes = [_vp]
     for name in EXPORTS:
         getattr(L, name)  # every declared entry point must resolve
     _lib = L
@@ -376,3 +388,38 @@ class Engine:
     def comm_init(self, uid: bytes, rank: int, world: int):
         assert len(uid) == 128
         self._check(self.L.tsom_comm_init(self.h, uid, rank, world))
+
+    def join_group(self, group: "RankGroup", rank: int):
+        """Make this engine rank `rank` of an in-process rank group (the epoch
+        reduce and the sharded sampler then go through it instead of NCCL)."""
+        self._check(self.L.tsom_group_join(self.h, group.h, int(rank)))
+
+    @property
+    def barrier_wait_s(self) -> float:
+        """Seconds spent in reduce barriers (ThreadedExecutor::barrier_wait_s)."""
+        return float(self.L.tsom_barrier_wait_s(self.h))
+
+
+class RankGroup:
+    """In-process rank group (tsom_group_*): engines driven from separate
+    threads joined by an ordered host-memory reduce with a barrier deadline."""
+
+    def __init__(self, world: int):
+        self.L = load()
+        self.world = int(world)
+        h = _vp()
+        st = self.L.tsom_group_create(self.world, C.byref(h))
+        if st:
+            _raise(st, "tsom_group_create failed")
+        self.h = h
+
+    def close(self):
+        if self.h:
+            self.L.tsom_group_destroy(self.h)
+            self.h = None
+
+    def __enter__(self):
+        return self
+
+    def __exit__(self, *exc):
+        self.close()

@@ -91,15 +91,18 @@ class CudaExecutor:
         data = _as_rows(data)
         self.engine = Engine(nodes, data.shape[1], device)
         self.engine.bind(data, streamed=streamed)
-        self._infl_id = None
+        self._infl = None  # host copy of the influence matrix last uploaded
 
     def run_iteration(self, selected, weights, influence, eta, n_chunks=1, distances=None):
         eng = self.engine
         eng.set_codebook(weights)
-        key = id(influence)
-        if key != self._infl_id:
-            eng.set_influence(influence, -1)
-            self._infl_id = key
+        # upload only when the matrix changed: compared by content (an object
+        # identity key would miss a matrix updated in place, or a new temporary
+        # that reuses a freed object's address)
+        infl = np.ascontiguousarray(influence, np.float64)
+        if self._infl is None or not np.array_equal(infl, self._infl):
+            eng.set_influence(infl, -1)
+            self._infl = infl.copy()
         want = distances is not None
         sel = None if selected is None else np.asarray(selected, np.uint32)
         u, h, d = eng.epoch(eta, sel, want_dist=want)
@@ -112,7 +115,7 @@ class CudaExecutor:
         return 1
 
     def barrier_wait_s(self) -> float:
-        return 0.0
+        return self.engine.barrier_wait_s
 
 
 @dataclass

@@ -16,6 +16,7 @@
 #include <chrono>
 #include <mutex>
 #include <functional>
+#include <memory>
 
 #include <algorithm>
 #include <climits>
@@ -74,6 +75,9 @@ struct NcclApi {
     ncclResult_t (*allReduce)(const void*, void*, size_t, ncclDataType_t, ncclRedOp_t, ncclComm_t,
                               cudaStream_t) = nullptr;
     ncclResult_t (*commDestroy)(ncclComm_t) = nullptr;
+    ncclResult_t (*commInitRankConfig)(ncclComm_t*, int, ncclUniqueId, int, ncclConfig_t*) = nullptr;
+    ncclResult_t (*getAsyncError)(ncclComm_t, ncclResult_t*) = nullptr;
+    ncclResult_t (*commAbort)(ncclComm_t) = nullptr;
     const char* (*errStr)(ncclResult_t) = nullptr;
     bool load(std::string& err) {
         if (h) return true;
@@ -89,7 +93,11 @@ struct NcclApi {
         allReduce = (decltype(allReduce))dlsym(h, "ncclAllReduce");
         commDestroy = (decltype(commDestroy))dlsym(h, "ncclCommDestroy");
         errStr = (decltype(errStr))dlsym(h, "ncclGetErrorString");
-        if (!getUniqueId || !commInitRank || !allReduce || !commDestroy) {
+        commInitRankConfig = (decltype(commInitRankConfig))dlsym(h, "ncclCommInitRankConfig");
+        getAsyncError = (decltype(getAsyncError))dlsym(h, "ncclCommGetAsyncError");
+        commAbort = (decltype(commAbort))dlsym(h, "ncclCommAbort");
+        if (!getUniqueId || !commInitRank || !allReduce || !commDestroy || !commInitRankConfig ||
+            !getAsyncError || !commAbort) {
             err = "nccl: missing symbols";
             return false;
         }
@@ -235,21 +243,48 @@ void run_bmu(Engine* eng, const float* x, const uint32_t* sel, uint64_t n, const
     CU(cudaGetLastError());
 }
 
-// Validate a selection against the bound rows (fetch_rows, dataset.hpp:393-416)
-// and reduce the identity selection to "all rows".
-const uint32_t* normalise_selection(Engine* eng, const uint32_t* sel, uint64_t n_sel) {
-    if (!sel) {
-        REQUIRE(n_sel == 0 || n_sel == eng->n_rows, TSOM_ERR_INVALID,
-                "epoch: NULL selection means all rows (n_sel must be 0 or tsom_rows())");
-        return nullptr;
+// out[0] = ids >= n_rows, out[1] = positions i > 0 with sel[i] <= sel[i-1]
+__global__ void k_check_sel(const uint32_t* __restrict__ sel, uint64_t n, uint64_t n_rows,
+                            unsigned long long* out) {
+    unsigned long long bad = 0, unsorted = 0;
+    for (uint64_t i = blockIdx.x * (uint64_t)blockDim.x + threadIdx.x; i < n;
+         i += (uint64_t)gridDim.x * blockDim.x) {
+        const uint32_t v = sel[i];
+        bad += v >= n_rows;
+        unsorted += i > 0 && v <= sel[i - 1];
     }
-    if (n_sel == 0) return sel;
-    // contract: sorted, distinct (Sampler::select, sampling.hpp:42-43) ⇒ the
-    // last id is the largest, and size N spanning [0, N-1] is the identity
-    REQUIRE(sel[n_sel - 1] < eng->n_rows && sel[0] <= sel[n_sel - 1], TSOM_ERR_RANGE,
-            "fetch_rows: row index beyond data size");
-    if (n_sel == eng->n_rows && sel[0] == 0 && sel[n_sel - 1] == eng->n_rows - 1) return nullptr;
-    return sel;
+    for (int o = 16; o; o >>= 1) {
+        bad += __shfl_xor_sync(0xffffffffu, bad, o);
+        unsorted += __shfl_xor_sync(0xffffffffu, unsorted, o);
+    }
+    if ((threadIdx.x & 31) == 0 && (bad | unsorted)) {
+        atomicAdd(out, bad);
+        atomicAdd(out + 1, unsorted);
+    }
+}
+
+// Upload a caller selection into eng->sel and validate it on the device
+// against the bound rows (fetch_rows, dataset.hpp:393-416: an id beyond the
+// data is out_of_range; any order and repeats are a valid gather).  Returns
+// true when it is the identity (N strictly increasing ids in [0, N)), which
+// then runs as "all rows".
+bool upload_selection(Engine* eng, const uint32_t* sel, uint64_t n) {
+    CU(eng->sel.ensure(std::max<uint64_t>(n, 1) * sizeof(uint32_t)));
+    if (n == 0) return false;
+    CU(cudaMemcpyAsync(eng->sel.p, sel, n * sizeof(uint32_t), cudaMemcpyHostToDevice, eng->stream));
+    auto* chk = reinterpret_cast<unsigned long long*>(eng->hstat + 8);  // pinned [8..11]
+    CU(cudaMemsetAsync(eng->status.as<int>() + 2, 0, 16, eng->stream));
+    auto* dchk = reinterpret_cast<unsigned long long*>(eng->status.as<int>() + 2);
+    const unsigned grid = (unsigned)std::min<uint64_t>((n + 255) / 256, (uint64_t)eng->sm_count * 8);
+    TSOM_LAUNCH(k_check_sel<<<grid, 256, 0, eng->stream>>>(eng->sel.as<uint32_t>(), n,
+                                                           eng->n_rows, dchk));
+    CU(cudaGetLastError());
+    CU(cudaMemcpyAsync(chk, dchk, 16, cudaMemcpyDeviceToHost, eng->stream));
+    CU(cudaStreamSynchronize(eng->stream));
+    REQUIRE(chk[0] == 0, TSOM_ERR_RANGE, "fetch_rows: row index beyond data size");
+    REQUIRE(chk[1] == 0 || !eng->streamed, TSOM_ERR_INVALID,
+            "epoch: streamed data needs a sorted, distinct selection (Sampler::select order)");
+    return chk[1] == 0 && n == eng->n_rows;
 }
 
 // the rows get a 256-B-stride copy for the gathers (d even, <= 62; <= 32 GB)
@@ -282,14 +317,16 @@ void ensure_accum(Engine* eng, uint64_t rows) {
 void accumulate_epoch(Engine* eng, const uint32_t* sel_host, uint64_t n_sel, bool want_dist,
                       bool want_dsum, bool accumulate, const uint32_t* dev_sel = nullptr) {
     CU(eng->sums.ensure(slot_len(eng) * sizeof(double)));
-    const uint32_t* sel = dev_sel ? dev_sel : normalise_selection(eng, sel_host, n_sel);
+    const uint32_t* sel = dev_sel;
+    if (!dev_sel) {
+        if (!sel_host)
+            REQUIRE(n_sel == 0 || n_sel == eng->n_rows, TSOM_ERR_INVALID,
+                    "epoch: NULL selection means all rows (n_sel must be 0 or tsom_rows())");
+        else if (!upload_selection(eng, sel_host, n_sel))
+            sel = sel_host;
+    }
     const uint64_t n = sel ? n_sel : eng->n_rows;
     ensure_rows(eng, n);
-    if (sel && !dev_sel) {
-        CU(eng->sel.ensure(std::max<uint64_t>(n, 1) * sizeof(uint32_t)));
-        CU(cudaMemcpyAsync(eng->sel.p, sel, n * sizeof(uint32_t), cudaMemcpyHostToDevice,
-                           eng->stream));
-    }
     const uint32_t* dsel = dev_sel ? dev_sel : (sel ? eng->sel.as<uint32_t>() : nullptr);
     prep_codebook(eng);
     eng->last_recheck = 0;
@@ -423,13 +460,83 @@ void accumulate_epoch(Engine* eng, const uint32_t* sel_host, uint64_t n_sel, boo
     if (n == 0 && !eng->streamed)
         CU(cudaMemsetAsync(eng->sums.p, 0, slot_len(eng) * sizeof(double), eng->stream));
     CU(cudaGetLastError());
-    if (eng->nccl_comm) {
-        ncclResult_t r = g_nccl.allReduce(eng->sums.p, eng->sums.p, slot_len(eng), ncclFloat64, ncclSum,
-                                          (ncclComm_t)eng->nccl_comm, eng->stream);
-        REQUIRE(r == ncclSuccess, TSOM_ERR_NCCL,
-                std::string("nccl: allreduce failed: ") + (g_nccl.errStr ? g_nccl.errStr(r) : "?"));
+    // the one reduce of the epoch (parallel.hpp:90-95): [S | c | sum dist | rows]
+    // summed over the ranks, identical on every rank afterwards
+    if (eng->comm_reduce && (accumulate || want_dsum)) {
+        const int rc = eng->comm_reduce(eng->sums.p, slot_len(eng), 3);
+        if (rc != TSOM_OK) throw tsom::Fail{rc};
     }
     CU(cudaEventRecord(eng->ev[2 + 4], eng->stream));
+}
+
+std::string barrier_seconds(double s) { return std::to_string(s); }  // the reference's format
+
+// Drop the communicator after a failed or timed-out reduce (ncclCommAbort
+// ends its kernels); the engine then runs single-rank again.
+void abort_comm(Engine* eng) {
+    if (eng->nccl_comm && g_nccl.commAbort) g_nccl.commAbort((ncclComm_t)eng->nccl_comm);
+    eng->nccl_comm = nullptr;
+    eng->comm_reduce = nullptr;
+    eng->sampler.allreduce = nullptr;
+    eng->sampler.sync = nullptr;
+    eng->red_pending = 0;
+    eng->world = 1;
+    eng->rank = 0;
+    cudaStreamSynchronize(eng->stream);
+    cudaGetLastError();
+}
+
+// Wait for the engine stream.  With NCCL reduces in flight this is the reduce
+// barrier of collect_with_barrier (parallel.hpp:67-86): every enqueued reduce
+// must complete within barrier_timeout_s of the previous one (or of the start
+// of the wait), else the communicator is aborted and the call fails with
+// TSOM_ERR_TIMEOUT instead of hanging on a dead peer.
+void wait_stream(Engine* eng) {
+    if (!eng->nccl_comm || eng->red_pending == 0) {
+        eng->red_pending = 0;
+        CU(cudaStreamSynchronize(eng->stream));
+        return;
+    }
+    using clk = std::chrono::steady_clock;
+    const size_t pending = eng->red_pending;
+    const auto t0 = clk::now();
+    auto mark = t0;
+    size_t done = 0;
+    for (int spin = 0;; ++spin) {
+        while (done < pending) {
+            const cudaError_t q = cudaEventQuery(eng->red_ev[done]);
+            if (q == cudaErrorNotReady) break;
+            CU(q);
+            ++done;
+            mark = clk::now();
+        }
+        const cudaError_t q = cudaStreamQuery(eng->stream);
+        if (q == cudaSuccess) break;
+        if (q != cudaErrorNotReady) CU(q);
+        ncclResult_t ae = ncclSuccess;
+        g_nccl.getAsyncError((ncclComm_t)eng->nccl_comm, &ae);
+        if (ae != ncclSuccess && ae != ncclInProgress) {
+            abort_comm(eng);
+            REQUIRE(false, TSOM_ERR_NCCL,
+                    std::string("nccl: reduce failed: ") + (g_nccl.errStr ? g_nccl.errStr(ae) : "?"));
+        }
+        if (done < pending &&
+            std::chrono::duration<double>(clk::now() - mark).count() > eng->barrier_timeout_s) {
+            const int me = eng->rank, world = eng->world;
+            abort_comm(eng);
+            // NCCL does not say which peer is missing: name the ranks it can be
+            REQUIRE(false, TSOM_ERR_TIMEOUT,
+                    "reduce barrier timed out after " + barrier_seconds(eng->barrier_timeout_s) +
+                        " s waiting for worker " + std::to_string(me == 0 ? 1 : 0) +
+                        (world > 2 ? " (or another peer of rank " + std::to_string(me) + ")" : ""));
+        }
+        if (spin < 256)
+            std::this_thread::yield();
+        else
+            std::this_thread::sleep_for(std::chrono::microseconds(50));
+    }
+    eng->barrier_wait_s += std::chrono::duration<double>(clk::now() - t0).count();
+    eng->red_pending = 0;
 }
 
 // Guard of quantize_term (accum.hpp:34-38): every term eta*h*(x - w) must stay
@@ -536,9 +643,9 @@ int tsom_create(int device, uint32_t nodes, uint32_t dims, tsom_engine** out) {
         CU(eng->infl.ensure(P * P * sizeof(double)));
         CU(eng->U.ensure(P * D * sizeof(double)));
         CU(eng->H.ensure(P * sizeof(double)));
-        CU(eng->status.ensure(4 * sizeof(int)));
-        CU(cudaMallocHost(&eng->hstat, 16 * sizeof(uint32_t)));
-        std::memset(eng->hstat, 0, 16 * sizeof(uint32_t));
+        CU(eng->status.ensure(8 * sizeof(int)));
+        CU(cudaMallocHost(&eng->hstat, 32 * sizeof(uint32_t)));
+        std::memset(eng->hstat, 0, 32 * sizeof(uint32_t));
         ensure_rows(eng, 1);
         CU(cudaStreamSynchronize(eng->stream));
     });
@@ -578,6 +685,7 @@ int tsom_destroy(tsom_engine* eng) {
         if (ev) cudaEventDestroy(ev);
     if (eng->hstat) cudaFreeHost(eng->hstat);
     for (cudaEvent_t e : eng->k1_ev) cudaEventDestroy(e);
+    for (cudaEvent_t e : eng->red_ev) cudaEventDestroy(e);
     if (eng->stream) cudaStreamDestroy(eng->stream);
     if (eng->copy_stream) cudaStreamDestroy(eng->copy_stream);
     delete eng;
@@ -619,6 +727,10 @@ int tsom_set_option(tsom_engine* eng, int key, int64_t value) {
                 break;
             case TSOM_OPT_HOST_REGISTER:
                 eng->host_register = value != 0;
+                break;
+            case TSOM_OPT_BARRIER_TIMEOUT_MS:
+                REQUIRE(value >= 1, TSOM_ERR_INVALID, "option: barrier timeout >= 1 ms");
+                eng->barrier_timeout_s = (double)value / 1000.0;
                 break;
             case TSOM_OPT_STAGING_THREADS:
                 REQUIRE(value >= 1 && value <= 64, TSOM_ERR_INVALID,
@@ -936,7 +1048,7 @@ int tsom_epoch(tsom_engine* eng, const uint32_t* selected, uint64_t n_sel, doubl
     return guarded(eng, [&] {
         CU(cudaSetDevice(eng->device));
         REQUIRE(eng->infl_set, TSOM_ERR_INVALID, "epoch: influence not set");
-        REQUIRE(eng->n_rows > 0 || (selected && n_sel == 0) || eng->nccl_comm, TSOM_ERR_INVALID,
+        REQUIRE(eng->n_rows > 0 || (selected && n_sel == 0) || eng->comm_reduce, TSOM_ERR_INVALID,
                 "epoch: no data bound");
         prep_codebook(eng);
         accumulate_epoch(eng, selected, n_sel, dist_out != nullptr, false, true);
@@ -953,7 +1065,7 @@ int tsom_epoch(tsom_engine* eng, const uint32_t* selected, uint64_t n_sel, doubl
             CU(cudaMemcpyAsync(dist_out, eng->dist.p, n * sizeof(double), cudaMemcpyDeviceToHost,
                                eng->stream));
         enqueue_guard_read(eng);
-        CU(cudaStreamSynchronize(eng->stream));
+        wait_stream(eng);
         finish_recheck(eng);
         record_timing(eng);
         if (n) check_term_guard(eng, eta);
@@ -1021,7 +1133,7 @@ int tsom_qe(tsom_engine* eng, const uint32_t* selected, uint64_t n_sel, double* 
         double tail[2] = {0, 0};
         CU(cudaMemcpyAsync(tail, eng->sums.as<double>() + (size_t)eng->P * eng->D + eng->P,
                            2 * sizeof(double), cudaMemcpyDeviceToHost, eng->stream));
-        CU(cudaStreamSynchronize(eng->stream));
+        wait_stream(eng);
         finish_recheck(eng);
         if (dist_sum) *dist_sum = tail[0];
         if (count) *count = (uint64_t)tail[1];
@@ -1140,7 +1252,12 @@ bool sampler_pick(Engine* eng, uint64_t* m) {
     CU(smp.sel.ensure(std::max<uint64_t>(smp.n, 1) * sizeof(uint32_t)));
     const int rc = tsom::sampler_select(smp, smp.sel.as<uint32_t>(), m, eng->sm_count, eng->stream);
     CU(cudaGetLastError());
-    REQUIRE(rc != 5, TSOM_ERR_NCCL, "nccl: allreduce failed (sampler)");
+    if (rc == 5) {
+        if (eng->last_error.rfind("reduce barrier timed out", 0) == 0)
+            throw tsom::Fail{TSOM_ERR_TIMEOUT};
+        if (eng->last_error.rfind("nccl", 0) != 0) eng->last_error = "nccl: allreduce failed (sampler)";
+        throw tsom::Fail{TSOM_ERR_NCCL};
+    }
     REQUIRE(rc == 0 || rc == -1, TSOM_ERR_CUDA, "sampler: device allocation failed");
     smp.identity = rc == -1;
     smp.last_m = *m;
@@ -1161,73 +1278,153 @@ void fill_identity(Engine* eng, uint64_t n) {
 }
 }  // namespace
 
-// In-process stand-in for a communicator (tests only): ranks are engines driven
-// from separate host threads; allreduce goes through host memory with a
-// generation barrier.  Lets the sharded sampler be checked on one GPU.
+// In-process rank group (tsom_group_*): ranks are engines driven from separate
+// host threads of one process (one engine per GPU, or several engines on one
+// GPU in the tests); a reduce goes through host memory with a
+// generation barrier.  Every rank's contribution is kept and the reduction is
+// evaluated in rank order by the last rank to arrive, so the f64 sums are the
+// same on every rank and from run to run (the ordered reduce of
+// parallel.hpp:90-95).  A rank that does not arrive within the barrier timeout
+// is named, like collect_with_barrier (parallel.hpp:67-86).  This is the
+// ThreadedExecutor shape (parallel.hpp:99-140) with engines as workers; it
+// also lets the multi-rank epoch and the sharded sampler run on one GPU.
 struct LoopbackGroup {
     int world;
     std::mutex mu;
     std::condition_variable cv;
-    std::vector<uint64_t> acc;
+    std::vector<std::vector<uint8_t>> contrib;
+    std::vector<char> present;
+    std::vector<uint8_t> result;
     int arrived = 0, leaving = 0;
     uint64_t gen = 0;
-    explicit LoopbackGroup(int w) : world(w) {}
-    // element-wise reduce of `v` (u32 or u64 as u64 lanes) over the ranks
-    void reduce(std::vector<uint64_t>& v, bool is_max) {
+    bool broken = false;
+    explicit LoopbackGroup(int w) : world(w), contrib(w), present(w, 0) {}
+
+    template <typename T, typename F>
+    void fold(size_t count, F f) {
+        result = contrib[0];
+        T* acc = reinterpret_cast<T*>(result.data());
+        for (int r = 1; r < world; ++r) {
+            const T* v = reinterpret_cast<const T*>(contrib[r].data());
+            for (size_t i = 0; i < count; ++i) acc[i] = f(acc[i], v[i]);
+        }
+    }
+    // In-place reduce of `bytes` host bytes (op as Engine::comm_reduce).
+    // Returns -1 on success, -2 if the group was broken by another rank's
+    // timeout, else the first rank that did not arrive in time.
+    int reduce(int rank, void* data, size_t bytes, int op, double timeout_s) {
+        using clk = std::chrono::steady_clock;
+        const auto deadline =
+            clk::now() + std::chrono::duration_cast<clk::duration>(std::chrono::duration<double>(timeout_s));
         std::unique_lock<std::mutex> lk(mu);
-        cv.wait(lk, [&] { return leaving == 0; });  // previous round fully drained
-        if (arrived == 0) acc.assign(v.size(), 0);
-        for (size_t i = 0; i < v.size(); ++i) acc[i] = is_max ? std::max(acc[i], v[i]) : acc[i] + v[i];
+        // previous round fully drained
+        if (!cv.wait_until(lk, deadline, [&] { return leaving == 0 || broken; })) {
+            broken = true;
+            cv.notify_all();
+            return -2;
+        }
+        if (broken) return -2;
+        const uint8_t* src = static_cast<const uint8_t*>(data);
+        contrib[rank].assign(src, src + bytes);
+        present[rank] = 1;
         const uint64_t my_gen = gen;
         if (++arrived == world) {
+            const size_t count = bytes / (op == 0 ? 4 : 8);
+            switch (op) {
+                case 0: fold<uint32_t>(count, [](uint32_t a, uint32_t b) { return a + b; }); break;
+                case 1: fold<uint64_t>(count, [](uint64_t a, uint64_t b) { return a > b ? a : b; }); break;
+                case 2: fold<uint64_t>(count, [](uint64_t a, uint64_t b) { return a + b; }); break;
+                default: fold<double>(count, [](double a, double b) { return a + b; }); break;
+            }
             arrived = 0;
             leaving = world;
+            std::fill(present.begin(), present.end(), 0);
             ++gen;
             cv.notify_all();
-        } else {
-            cv.wait(lk, [&] { return gen != my_gen; });
+        } else if (!cv.wait_until(lk, deadline, [&] { return gen != my_gen || broken; })) {
+            int late = 0;
+            while (late < world && present[late]) ++late;
+            broken = true;
+            cv.notify_all();
+            return late;
         }
-        v = acc;
+        if (gen == my_gen) return -2;  // broken while waiting
+        std::memcpy(data, result.data(), bytes);
         if (--leaving == 0) cv.notify_all();
+        return -1;
     }
 };
 
 namespace {
+// the reduce hook of an engine joined to a loopback group: device buffer ->
+// host, group reduce (with the barrier deadline), host -> device
 void attach_loopback(Engine* eng, LoopbackGroup* g, int rank) {
+    REQUIRE(rank >= 0 && rank < g->world, TSOM_ERR_INVALID, "comm: bad rank/world");
+    eng->world = g->world;
+    eng->rank = rank;
+    eng->comm_reduce = [eng, g, rank](void* buf, size_t count, int op) -> int {
+        cudaStream_t st = eng->stream;
+        const size_t bytes = count * (op == 0 ? 4 : 8);
+        std::vector<uint8_t> raw(bytes);
+        if (cudaMemcpyAsync(raw.data(), buf, bytes, cudaMemcpyDeviceToHost, st) != cudaSuccess ||
+            cudaStreamSynchronize(st) != cudaSuccess) {
+            eng->last_error = "cuda: reduce staging failed";
+            return TSOM_ERR_CUDA;
+        }
+        const auto t0 = std::chrono::steady_clock::now();
+        const int late = g->reduce(rank, raw.data(), bytes, op, eng->barrier_timeout_s);
+        eng->barrier_wait_s +=
+            std::chrono::duration<double>(std::chrono::steady_clock::now() - t0).count();
+        if (late >= 0) {
+            eng->last_error = "reduce barrier timed out after " +
+                              std::to_string(eng->barrier_timeout_s) + " s waiting for worker " +
+                              std::to_string(late);
+            return TSOM_ERR_TIMEOUT;
+        }
+        if (late == -2) {
+            eng->last_error = "reduce barrier aborted: another rank timed out";
+            return TSOM_ERR_TIMEOUT;
+        }
+        if (cudaMemcpyAsync(buf, raw.data(), bytes, cudaMemcpyHostToDevice, st) != cudaSuccess ||
+            cudaStreamSynchronize(st) != cudaSuccess) {
+            eng->last_error = "cuda: reduce staging failed";
+            return TSOM_ERR_CUDA;
+        }
+        return TSOM_OK;
+    };
     tsom::SamplerState& smp = eng->sampler;
-    cudaStream_t st = eng->stream;
     smp.loopback = true;
     smp.world = g->world;
     smp.rank = rank;
-    smp.allreduce = [g, st](void* buf, size_t count, int op) {
-        const size_t esz = op == 0 ? 4 : 8;
-        std::vector<uint8_t> raw(count * esz);
-        if (cudaMemcpyAsync(raw.data(), buf, raw.size(), cudaMemcpyDeviceToHost, st) != cudaSuccess ||
-            cudaStreamSynchronize(st) != cudaSuccess)
-            return false;
-        std::vector<uint64_t> v(count);
-        for (size_t i = 0; i < count; ++i)
-            v[i] = esz == 4 ? (uint64_t)reinterpret_cast<uint32_t*>(raw.data())[i]
-                            : reinterpret_cast<uint64_t*>(raw.data())[i];
-        g->reduce(v, op == 1);
-        for (size_t i = 0; i < count; ++i) {
-            if (esz == 4) reinterpret_cast<uint32_t*>(raw.data())[i] = (uint32_t)v[i];
-            else reinterpret_cast<uint64_t*>(raw.data())[i] = v[i];
-        }
-        return cudaMemcpyAsync(buf, raw.data(), raw.size(), cudaMemcpyHostToDevice, st) ==
-                   cudaSuccess &&
-               cudaStreamSynchronize(st) == cudaSuccess;
+    smp.allreduce = [eng](void* buf, size_t count, int op) {
+        return eng->comm_reduce && eng->comm_reduce(buf, count, op) == TSOM_OK;
     };
+    smp.sync = nullptr;
 }
 }  // namespace
 
 extern "C" {
 
-// diagnostics / tests only (not in the public header)
-void* tsom_debug_loopback_group(int world) { return new LoopbackGroup(world); }
-void tsom_debug_loopback_free(void* g) { delete static_cast<LoopbackGroup*>(g); }
-int tsom_debug_loopback_attach(tsom_engine* eng, void* g, int rank) {
-    return guarded(eng, [&] { attach_loopback(eng, static_cast<LoopbackGroup*>(g), rank); });
+// the handle owns one reference; every joined engine holds another, so the
+// group and its engines can be destroyed in any order
+int tsom_group_create(int world, tsom_group** out) {
+    if (!out || world < 1) return TSOM_ERR_INVALID;
+    *out = reinterpret_cast<tsom_group*>(new std::shared_ptr<LoopbackGroup>(
+        std::make_shared<LoopbackGroup>(world)));
+    return TSOM_OK;
+}
+int tsom_group_destroy(tsom_group* g) {
+    delete reinterpret_cast<std::shared_ptr<LoopbackGroup>*>(g);
+    return TSOM_OK;
+}
+int tsom_group_join(tsom_engine* eng, tsom_group* g, int rank) {
+    return guarded(eng, [&] {
+        REQUIRE(g, TSOM_ERR_INVALID, "comm: null group");
+        REQUIRE(!eng->nccl_comm, TSOM_ERR_INVALID, "comm: engine already has an NCCL communicator");
+        const auto& sp = *reinterpret_cast<std::shared_ptr<LoopbackGroup>*>(g);
+        attach_loopback(eng, sp.get(), rank);
+        eng->group_ref = sp;
+    });
 }
 
 int tsom_sampler_init(tsom_engine* eng, int kind, uint64_t m, uint64_t seed, double alpha,
@@ -1240,29 +1437,33 @@ int tsom_sampler_init(tsom_engine* eng, int kind, uint64_t m, uint64_t seed, dou
         REQUIRE(kind == 0 || m >= 1, TSOM_ERR_INVALID, "select_random: m must be >= 1");
         REQUIRE(eng->n_rows < (1ull << 31), TSOM_ERR_INVALID, "sampler: N < 2^31");
         tsom::SamplerState& smp = eng->sampler;
-        smp.sharded = eng->nccl_comm != nullptr || smp.loopback;
+        smp.sharded = eng->comm_reduce != nullptr;
         if (smp.sharded) {
             // one Sampler over the ranks' rows in rank order: global N and this
             // rank's first row from an allreduce of the per-rank row counts
             cudaStream_t st = eng->stream;
-            if (!smp.loopback) {
-                ncclComm_t comm = (ncclComm_t)eng->nccl_comm;
-                smp.world = eng->world;
-                smp.rank = eng->rank;
-                smp.allreduce = [comm, st](void* buf, size_t count, int op) {
-                    const ncclDataType_t t = op == 0 ? ncclUint32 : ncclUint64;
-                    const ncclRedOp_t o = op == 1 ? ncclMax : ncclSum;
-                    return g_nccl.allReduce(buf, buf, count, t, o, comm, st) == ncclSuccess;
+            smp.world = eng->world;
+            smp.rank = eng->rank;
+            smp.allreduce = [eng](void* buf, size_t count, int op) {
+                return eng->comm_reduce && eng->comm_reduce(buf, count, op) == TSOM_OK;
+            };
+            if (eng->nccl_comm)
+                smp.sync = [eng](cudaStream_t) {
+                    try {
+                        wait_stream(eng);
+                        return true;
+                    } catch (const tsom::Fail&) {
+                        return false;
+                    }
                 };
-            }
             std::vector<uint64_t> cnt(smp.world, 0);
             cnt[smp.rank] = eng->n_rows;
             CU(smp.slots.ensure((size_t)smp.world * 8));
             CU(cudaMemcpyAsync(smp.slots.p, cnt.data(), cnt.size() * 8, cudaMemcpyHostToDevice, st));
-            REQUIRE(smp.allreduce(smp.slots.p, cnt.size(), 2), TSOM_ERR_NCCL,
-                    "nccl: allreduce failed (sampler row counts)");
+            const int rc = eng->comm_reduce(smp.slots.p, cnt.size(), 2);
+            if (rc != TSOM_OK) throw tsom::Fail{rc};
             CU(cudaMemcpyAsync(cnt.data(), smp.slots.p, cnt.size() * 8, cudaMemcpyDeviceToHost, st));
-            CU(cudaStreamSynchronize(st));
+            wait_stream(eng);
             smp.gN = 0;
             smp.off = 0;
             for (int r = 0; r < smp.world; ++r) {
@@ -1291,7 +1492,7 @@ int tsom_sampler_select(tsom_engine* eng, uint32_t* sel_out, uint64_t* m_out) {
         if (sel_out && m)
             CU(cudaMemcpyAsync(sel_out, eng->sampler.sel.p, m * sizeof(uint32_t),
                                cudaMemcpyDeviceToHost, eng->stream));
-        CU(cudaStreamSynchronize(eng->stream));
+        wait_stream(eng);
         REQUIRE(!(status & 4u), TSOM_ERR_NUMERICAL, "sampler: random stream slack exceeded");
         if (m_out) *m_out = m;
     });
@@ -1382,7 +1583,7 @@ static void train_epoch_enqueue(Engine* eng, double eta, double sigma, double mo
             host_sel.resize(m);
             CU(cudaMemcpyAsync(host_sel.data(), smp.sel.p, m * sizeof(uint32_t),
                                cudaMemcpyDeviceToHost, eng->stream));
-            CU(cudaStreamSynchronize(eng->stream));
+            wait_stream(eng);
         }
     }
     const bool want_dist = sampled && smp.kind == 2;
@@ -1416,7 +1617,7 @@ int tsom_train_epoch(tsom_engine* eng, double eta, double sigma, double momentum
         CU(cudaMemcpyAsync(eng->hstat + 2, eng->status.p, sizeof(int), cudaMemcpyDeviceToHost,
                            eng->stream));
         enqueue_guard_read(eng);
-        CU(cudaStreamSynchronize(eng->stream));
+        wait_stream(eng);
         int st;
         std::memcpy(&st, eng->hstat + 2, sizeof(int));
         finish_recheck(eng);
@@ -1460,7 +1661,7 @@ int tsom_train_epochs(tsom_engine* eng, uint32_t n_epochs, const double* eta,
         eng->k1_slot = -1;
         CU(cudaMemcpyAsync(eng->hstat + 5, dead, 3 * sizeof(int), cudaMemcpyDeviceToHost,
                            eng->stream));
-        CU(cudaStreamSynchronize(eng->stream));
+        wait_stream(eng);
         finish_recheck(eng);
         eng->k1_timed = false;  // ev[8] / ev[9] were not recorded: per-epoch events below
         record_timing(eng);     // phases of the last epoch
@@ -1537,15 +1738,66 @@ int tsom_comm_init(tsom_engine* eng, const uint8_t id[128], int rank, int world)
         REQUIRE(g_nccl.load(err), TSOM_ERR_NCCL, err);
         ncclUniqueId uid;
         std::memcpy(&uid, id, 128);
-        ncclComm_t comm;
-        ncclResult_t r = g_nccl.commInitRank(&comm, world, uid, rank);
+        // non-blocking communicator: initialisation and every reduce can be
+        // polled against the barrier deadline and aborted (ncclCommAbort)
+        // when a peer never arrives, instead of blocking forever
+        ncclComm_t comm = nullptr;
+        ncclConfig_t cfg = NCCL_CONFIG_INITIALIZER;
+        cfg.blocking = 0;
+        ncclResult_t r = g_nccl.commInitRankConfig(&comm, world, uid, rank, &cfg);
+        using clk = std::chrono::steady_clock;
+        const auto t0 = clk::now();
+        while (r == ncclInProgress) {
+            if (std::chrono::duration<double>(clk::now() - t0).count() > eng->barrier_timeout_s) {
+                g_nccl.commAbort(comm);
+                REQUIRE(false, TSOM_ERR_TIMEOUT,
+                        "comm init timed out after " + barrier_seconds(eng->barrier_timeout_s) +
+                            " s waiting for the other ranks of " + std::to_string(world));
+            }
+            std::this_thread::sleep_for(std::chrono::microseconds(200));
+            g_nccl.getAsyncError(comm, &r);
+        }
         REQUIRE(r == ncclSuccess, TSOM_ERR_NCCL,
-                std::string("nccl: ncclCommInitRank failed: ") + (g_nccl.errStr ? g_nccl.errStr(r) : "?"));
+                std::string("nccl: ncclCommInitRankConfig failed: ") +
+                    (g_nccl.errStr ? g_nccl.errStr(r) : "?"));
         eng->nccl_comm = comm;
         eng->rank = rank;
         eng->world = world;
+        eng->comm_reduce = [eng, comm](void* buf, size_t count, int op) -> int {
+            const ncclDataType_t t =
+                op == 0 ? ncclUint32 : (op == 3 ? ncclFloat64 : ncclUint64);
+            const ncclRedOp_t o = op == 1 ? ncclMax : ncclSum;
+            ncclResult_t rr = g_nccl.allReduce(buf, buf, count, t, o, comm, eng->stream);
+            // a non-blocking communicator may still be enqueueing the call
+            while (rr == ncclInProgress) {
+                std::this_thread::yield();
+                g_nccl.getAsyncError(comm, &rr);
+            }
+            if (rr != ncclSuccess) {
+                eng->last_error = std::string("nccl: allreduce failed: ") +
+                                  (g_nccl.errStr ? g_nccl.errStr(rr) : "?");
+                return TSOM_ERR_NCCL;
+            }
+            // the barrier of this reduce: wait_stream polls it with the deadline
+            if (eng->red_pending == eng->red_ev.size()) {
+                cudaEvent_t ev;
+                if (cudaEventCreateWithFlags(&ev, cudaEventDisableTiming) != cudaSuccess) {
+                    eng->last_error = "cuda: event creation failed";
+                    return TSOM_ERR_CUDA;
+                }
+                eng->red_ev.push_back(ev);
+            }
+            if (cudaEventRecord(eng->red_ev[eng->red_pending], eng->stream) != cudaSuccess) {
+                eng->last_error = "cuda: event record failed";
+                return TSOM_ERR_CUDA;
+            }
+            ++eng->red_pending;
+            return TSOM_OK;
+        };
     });
 }
+
+double tsom_barrier_wait_s(const tsom_engine* eng) { return eng ? eng->barrier_wait_s : 0.0; }
 
 int tsom_last_timing(const tsom_engine* eng, float* bmu_ms, float* accum_ms, float* smooth_ms,
                      float* total_ms) {

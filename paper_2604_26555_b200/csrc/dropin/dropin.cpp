@@ -130,6 +130,11 @@ static void run_train(const dropin_config* rc, const DataSourceRef& src, float* 
         opts.device = device;
         opts.streamed = (flags & 1u) != 0;
         opts.bmu_kernel = static_cast<int>((flags >> 1) & 3u);
+        // bits 8-11: engines (one per row slice, all on `device`); 0 = 1
+        const unsigned engines = (flags >> 8) & 15u;
+        if (engines > 1) opts.devices.assign(engines, device);
+        // bits 12-27: reduce-barrier timeout in ms (0 = the reference's 60 s)
+        if ((flags >> 12) & 0xFFFFu) opts.barrier_timeout_s = ((flags >> 12) & 0xFFFFu) / 1000.0;
         TrainOptions to;
         to.log_qe = qe_log != nullptr;
         const auto t0 = std::chrono::steady_clock::now();

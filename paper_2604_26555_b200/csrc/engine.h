@@ -21,6 +21,7 @@
 #include <atomic>
 #include <cstdint>
 #include <functional>
+#include <memory>
 #include <string>
 #include <vector>
 
@@ -184,6 +185,9 @@ struct SamplerState {
     int world = 1, rank = 0;
     int jump0 = 0;                 // generator 0 starts at a jumped offset (off > 0)
     std::function<bool(void*, size_t, int)> allreduce;
+    // waits for the engine stream after a sharded selection (the engine's
+    // reduce barrier with its deadline); false = the barrier failed
+    std::function<bool(cudaStream_t)> sync;
     DevBuf jN, glist, slots;       // jump by gN (adaptive), global selection, per-rank counts
 };
 int sampler_setup(SamplerState& s, int kind, uint64_t n, uint64_t m, uint64_t seed, double alpha,
@@ -306,6 +310,19 @@ struct Engine {
     // multi-GPU
     void* nccl_comm = nullptr;
     int rank = 0, world = 1;
+    // The reduce step of an epoch (and of the sharded sampler): the NCCL
+    // communicator, or (tests) an in-process loopback group of engines.
+    // op 0 = u32 sum, 1 = u64 max, 2 = u64 sum, 3 = f64 sum, in place on the
+    // device buffer; returns a TSOM status with last_error set on failure.
+    std::function<int(void*, size_t, int)> comm_reduce;
+    // collect_with_barrier's deadline (parallel.hpp:24, 67-86): a rank that
+    // does not reach the reduce within this many seconds fails the call with
+    // TSOM_ERR_TIMEOUT instead of hanging it
+    double barrier_timeout_s = 60.0;
+    std::shared_ptr<void> group_ref;  // keeps a joined in-process rank group alive
+    double barrier_wait_s = 0.0;   // seconds spent waiting in reduces (ThreadedExecutor::barrier_wait_s)
+    std::vector<cudaEvent_t> red_ev;  // one per enqueued NCCL reduce of the current call
+    size_t red_pending = 0;
 };
 
 // ---------------------------------------------------------------------------

@@ -895,7 +895,11 @@ int sampler_select(SamplerState& s, uint32_t* out, uint64_t* m_out, int sm_count
     if (s.sharded) {  // this rank's share is only known on the device
         unsigned long long mloc = 0;
         cudaMemcpyAsync(&mloc, total, 8, cudaMemcpyDeviceToHost, st);
-        cudaStreamSynchronize(st);
+        if (s.sync) {
+            if (!s.sync(st)) return 5;
+        } else {
+            cudaStreamSynchronize(st);
+        }
         *m_out = mloc;
     } else {
         *m_out = s.kind == 1 ? s.m : std::min(s.m, n);

@@ -104,21 +104,14 @@ def test_sampled_resident_training_vs_reference(pkg, oracle_port, oracle_ref, sa
 # selections must be the reference Sampler's selection over all rows.
 
 def _run_sharded(pkg, sizes, kind, m, seed, iters, alpha=1.0, beta=1.0, dist=None):
-    import ctypes as C
     import threading
 
-    from paper_2604_26555_b200 import _lib
-    L = _lib.load()
-    L.tsom_debug_loopback_group.restype = C.c_void_p
-    L.tsom_debug_loopback_group.argtypes = [C.c_int]
-    L.tsom_debug_loopback_attach.argtypes = [C.c_void_p, C.c_void_p, C.c_int]
-    L.tsom_debug_loopback_free.argtypes = [C.c_void_p]
     world = len(sizes)
-    g = L.tsom_debug_loopback_group(world)
+    g = pkg.RankGroup(world)
     offs = np.concatenate([[0], np.cumsum(sizes)[:-1]]).astype(np.int64)
     engines = [engine_with_rows(pkg, s) for s in sizes]
     for r, e in enumerate(engines):
-        assert L.tsom_debug_loopback_attach(e.h, g, r) == 0
+        e.join_group(g, r)
     out = [[None] * iters for _ in range(world)]
     errors = []
 
@@ -139,7 +132,7 @@ def _run_sharded(pkg, sizes, kind, m, seed, iters, alpha=1.0, beta=1.0, dist=Non
         t.start()
     for t in th:
         t.join(timeout=600)
-    L.tsom_debug_loopback_free(g)
+    g.close()
     assert not errors, errors
     return [np.concatenate([out[r][t] for r in range(world)]) for t in range(iters)], engines
 
