@@ -85,6 +85,23 @@ _lib = None
 _vp = C.c_void_p
 
 
+def _point_at_nccl_wheel():
+    """The engine dlopens NCCL lazily; prefer the NCCL wheel torch is linked
+    against, so one process never holds two different libnccl.so.2."""
+    if os.environ.get("TSOM_NCCL_LIB"):
+        return
+    try:
+        import importlib.util
+        spec = importlib.util.find_spec("nvidia.nccl")
+    except (ImportError, ValueError):
+        return
+    for base in (spec.submodule_search_locations or []) if spec else []:
+        cand = os.path.join(base, "lib", "libnccl.so.2")
+        if os.path.exists(cand):
+            os.environ["TSOM_NCCL_LIB"] = cand
+            return
+
+
 def load():
     """Load libtsom_b200.so (built by ``__graft_entry__.build()``)."""
     global _lib
@@ -93,6 +110,7 @@ def load():
     if not os.path.exists(LIB_PATH):
         raise ImportError(f"{LIB_PATH} is missing: run `python -c 'import __graft_entry__ as g; "
                           "g.build()'` (there is no CPU fallback)")
+    _point_at_nccl_wheel()
     L = C.CDLL(LIB_PATH)
     u32, u64, i64, i32 = C.c_uint32, C.c_uint64, C.c_int64, C.c_int
     L.tsom_create.argtypes = [i32, u32, u32, C.POINTER(_vp)]

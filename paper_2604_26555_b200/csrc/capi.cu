@@ -81,9 +81,16 @@ struct NcclApi {
     const char* (*errStr)(ncclResult_t) = nullptr;
     bool load(std::string& err) {
         if (h) return true;
+        // a NCCL the process already loaded (e.g. by torch) first, then
+        // TSOM_NCCL_LIB (the Python binding points it at the NCCL wheel torch
+        // links against), then the loader's search path: two different
+        // libnccl.so.2 in one process would break whichever loads second
+        h = dlopen("libnccl.so.2", RTLD_NOW | RTLD_GLOBAL | RTLD_NOLOAD);
+        const char* env = getenv("TSOM_NCCL_LIB");
+        if (!h && env && *env) h = dlopen(env, RTLD_NOW | RTLD_GLOBAL);
         const char* names[] = {"libnccl.so.2", "libnccl.so"};
         for (const char* n : names)
-            if ((h = dlopen(n, RTLD_NOW | RTLD_GLOBAL))) break;
+            if (!h && (h = dlopen(n, RTLD_NOW | RTLD_GLOBAL))) break;
         if (!h) {
             err = std::string("nccl: cannot load libnccl.so.2: ") + dlerror();
             return false;
@@ -1417,6 +1424,16 @@ int tsom_group_destroy(tsom_group* g) {
     delete reinterpret_cast<std::shared_ptr<LoopbackGroup>*>(g);
     return TSOM_OK;
 }
+// tests only (not in the public header): one rank's host-side reduce through
+// the group, no engine or GPU involved; returns -1 ok, -2 aborted, else the
+// late rank
+int tsom_debug_group_reduce(tsom_group* g, int rank, void* data, uint64_t bytes, int op,
+                            double timeout_s) {
+    if (!g) return -3;
+    return (*reinterpret_cast<std::shared_ptr<LoopbackGroup>*>(g))->reduce(rank, data, bytes, op,
+                                                                           timeout_s);
+}
+
 int tsom_group_join(tsom_engine* eng, tsom_group* g, int rank) {
     return guarded(eng, [&] {
         REQUIRE(g, TSOM_ERR_INVALID, "comm: null group");

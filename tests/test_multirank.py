@@ -1,11 +1,15 @@
-"""Multi-rank (data-parallel) host logic on CPU with gloo, world size 2.
+"""Multi-rank (data-parallel) host logic on CPU (no GPU in this container).
 
 The engine's N>1 path: each rank reduces its own row shard to
 the packed sums [S_b | c_b | sum dist | rows], one allreduce(sum) combines
-them, and every rank runs the identical FP64 smoothing.  Here the per-rank K2
-sums are restated in numpy from the oracle's BMUs, combined with a real gloo
-allreduce, smoothed with the K3 algebra, and compared with the single-process
-reference accumulators.
+them, and every rank runs the identical FP64 smoothing.  The engine itself
+runs that path with 2/3/4 ranks on the GPU (tests/test_gpu_multirank.py).
+Here, on CPU: (1) the decomposition with a real gloo allreduce at world size
+2 — per-rank K2 sums restated in numpy from the oracle's BMUs, smoothed with
+the K3 algebra, against the single-process reference accumulators; (2) the
+engine library's in-process rank group (the reduce the multi-rank epoch
+calls), driven from threads without an engine: rank-ordered f64 sums and the
+barrier deadline.
 """
 import os
 import socket
@@ -89,3 +93,85 @@ def test_sharded_epoch_equals_single_process(tmp_path, world):
         assert np.max(np.abs(o["U"] - uo)) <= 1e-9 * np.max(np.abs(uo))
         np.testing.assert_allclose(o["H"], ho, rtol=1e-9)
     assert (outs[0]["U"] == outs[1]["U"]).all()
+
+
+# --- the in-process rank group's reduce (host logic, no GPU) ------------------
+#
+# tsom_group_* is the reduce the engine's multi-rank epoch uses when its ranks
+# are threads of one process (tests/test_gpu_multirank.py drives it through
+# the engines on a GPU).  Its host side is checked here directly: the reduce
+# is evaluated in rank order whatever the arrival order (parallel.hpp:90-95,
+# so every rank and every run gets the same f64 sums), and a rank that misses
+# the deadline is named (collect_with_barrier, parallel.hpp:67-86).
+
+def _group_lib():
+    import ctypes as C
+
+    from paper_2604_26555_b200 import _lib
+    L = _lib.load()
+    L.tsom_debug_group_reduce.argtypes = [C.c_void_p, C.c_int, C.c_void_p, C.c_uint64, C.c_int,
+                                          C.c_double]
+    L.tsom_debug_group_reduce.restype = C.c_int
+    return L
+
+
+def _reduce_on_threads(world, bufs, op, timeout_s=10.0, skip=(), delays=None):
+    import threading
+    import time
+
+    from paper_2604_26555_b200 import RankGroup
+    L = _group_lib()
+    g = RankGroup(world)
+    rc = [None] * world
+
+    def rank(r):
+        if delays:
+            time.sleep(delays[r])
+        rc[r] = L.tsom_debug_group_reduce(g.h, r, bufs[r].ctypes.data, bufs[r].nbytes, op,
+                                          timeout_s)
+
+    th = [threading.Thread(target=rank, args=(r,)) for r in range(world) if r not in skip]
+    for t in th:
+        t.start()
+    for t in th:
+        t.join(timeout=60)
+    g.close()
+    return rc
+
+
+@pytest.mark.parametrize("world", [2, 3, 4])
+def test_group_f64_reduce_is_rank_ordered(world):
+    rng = np.random.default_rng(world)
+    vals = [rng.standard_normal(4099) * 10.0 ** rng.integers(-8, 8, 4099) for _ in range(world)]
+    want = vals[0].copy()
+    for r in range(1, world):
+        want = want + vals[r]  # left fold in rank order
+    for delays in ([0.0] * world, [0.02 * (world - r) for r in range(world)]):
+        bufs = [v.copy() for v in vals]
+        rc = _reduce_on_threads(world, bufs, 3, delays=delays)
+        assert rc == [-1] * world
+        for b in bufs:
+            assert (b == want).all()  # bit-identical on every rank, any arrival order
+
+
+def test_group_integer_reduces():
+    a = [np.array([1, 2, 3, 2**31], np.uint32), np.array([5, 6, 7, 2**31 - 1], np.uint32)]
+    rc = _reduce_on_threads(2, a, 0)
+    assert rc == [-1, -1] and a[0].tolist() == [6, 8, 10, 2**32 - 1] and (a[0] == a[1]).all()
+    m = [np.array([3, 9, 2**63], np.uint64), np.array([7, 1, 5], np.uint64),
+         np.array([0, 4, 6], np.uint64)]
+    rc = _reduce_on_threads(3, m, 1)
+    assert rc == [-1] * 3 and m[2].tolist() == [7, 9, 2**63]
+    s = [np.array([2**40, 1], np.uint64), np.array([2**40, 2], np.uint64)]
+    _reduce_on_threads(2, s, 2)
+    assert s[1].tolist() == [2**41, 3]
+
+
+def test_group_deadline_names_the_late_rank():
+    import time
+    bufs = [np.zeros(8) for _ in range(3)]
+    t0 = time.perf_counter()
+    rc = _reduce_on_threads(3, bufs, 3, timeout_s=0.2, skip=(1,))
+    assert time.perf_counter() - t0 < 5.0
+    # one waiting rank names worker 1, the other sees the broken barrier
+    assert sorted(rc[r] for r in (0, 2)) == [-2, 1]
