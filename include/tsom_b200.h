@@ -61,6 +61,8 @@ extern "C" {
 #define TSOM_OPT_HOST_REGISTER 5   /* streamed host rows: 1 (default) page-lock the caller's
                                       buffer for direct DMA, 0 copy through pinned staging */
 #define TSOM_OPT_STAGING_THREADS 6 /* host threads filling the pinned staging (default: min(16, cores)) */
+#define TSOM_OPT_PAD_ROWS 8          /* resident rows at a 256-B stride (d even, <= 62):
+                                        1 (default) or 0 = packed d-float rows */
 #define TSOM_OPT_BARRIER_TIMEOUT_MS 7 /* reduce-barrier deadline, ms (default 60000 =
                                          kDefaultBarrierTimeoutS, parallel.hpp:24); a rank that
                                          misses it fails the call with TSOM_ERR_TIMEOUT
@@ -249,6 +251,8 @@ int tsom_last_timing(const tsom_engine* eng, float* bmu_ms, float* accum_ms, flo
  * [4] device update (tsom_train_epoch), [5] total (sampler excluded), [6] device sampler
  * (sampled tsom_train_epoch). */
 int tsom_last_timing_detail(const tsom_engine* eng, float out[8]);
+/* Device memory this engine holds (bytes of its buffers, sampler included). */
+uint64_t tsom_device_bytes(const tsom_engine* eng);
 /* Number of CUDA kernels this library has launched in this process. */
 uint64_t tsom_kernel_launches(void);
 /* The CUDA stream all engine work is issued on (cudaStream_t as void*). */

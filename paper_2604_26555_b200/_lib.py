@@ -44,7 +44,7 @@ EXPORTS = [
     "tsom_sampler_init", "tsom_sampler_select", "tsom_sampler_observe", "tsom_sampler_state",
     "tsom_mt_selftest", "tsom_release_cached_memory", "tsom_train_epochs",
     "tsom_get_prev_update", "tsom_barrier_wait_s", "tsom_group_create", "tsom_group_join",
-    "tsom_group_destroy",
+    "tsom_group_destroy", "tsom_device_bytes",
 ]
 
 SAMPLER_KINDS = {"full": 0, "random": 1, "adaptive": 2}  # SamplingKind, sampling.hpp:163
@@ -156,6 +156,8 @@ def load():
     L.tsom_bind_shards.argtypes = [_vp, C.POINTER(C.c_char_p), u32, u32]
     L.tsom_stream.argtypes = [_vp]
     L.tsom_stream.restype = _vp
+    L.tsom_device_bytes.argtypes = [_vp]
+    L.tsom_device_bytes.restype = u64
     L.tsom_barrier_wait_s.argtypes = [_vp]
     L.tsom_barrier_wait_s.restype = C.c_double
     L.tsom_group_create.argtypes = [i32, C.POINTER(_vp)]
@@ -411,6 +413,11 @@ class Engine:
         """Make this engine rank `rank` of an in-process rank group (the epoch
         reduce and the sharded sampler then go through it instead of NCCL)."""
         self._check(self.L.tsom_group_join(self.h, group.h, int(rank)))
+
+    @property
+    def device_bytes(self) -> int:
+        """Device memory held by this engine's buffers."""
+        return int(self.L.tsom_device_bytes(self.h))
 
     @property
     def barrier_wait_s(self) -> float:

@@ -49,7 +49,6 @@ using tsom::host::ensure_pinned;
 using tsom::host::host_chunk_source;
 using tsom::host::note_pinned_copy;
 using tsom::host::pinned_give;
-using tsom::host::upload_rows;
 
 const char* kVersion = "toposom-b200 0.2 (sm_100a; tcgen05 3xFP16 BMU with exact FP64 near-tie resolution, TMA row gathers)";
 
@@ -136,9 +135,10 @@ tsom::TieWin tie_window(const Engine* e, int kind) {
     return w;
 }
 
-void ensure_rows(Engine* eng, uint64_t n) {
+// per-row scratch of a pass over n rows (distances only when asked for)
+void ensure_rows(Engine* eng, uint64_t n, bool want_dist = false) {
     CU(eng->bmu.ensure(std::max<uint64_t>(n, 1) * sizeof(uint32_t)));
-    CU(eng->dist.ensure(std::max<uint64_t>(n, 1) * sizeof(double)));
+    if (want_dist) CU(eng->dist.ensure(std::max<uint64_t>(n, 1) * sizeof(double)));
     CU(eng->flags.ensure((std::max<uint64_t>(n, 1) + 2) * sizeof(uint32_t)));
 }
 
@@ -158,15 +158,23 @@ cudaEvent_t k1_event(Engine* eng, int end) {
     return eng->ev[8 + end];
 }
 
+// near-tie list passes: pcount[p] = clamp(count - p * cap, 0, cap)
+constexpr uint32_t kTiePasses = 4;
+__global__ void k_tie_pass_counts(const uint32_t* __restrict__ count, uint64_t cap,
+                                  uint32_t passes, uint32_t* __restrict__ pcount) {
+    const uint32_t p = threadIdx.x;
+    if (p >= passes) return;
+    const uint64_t c = *count, o = (uint64_t)p * cap;
+    pcount[p] = (uint32_t)(c <= o ? 0 : (c - o < cap ? c - o : cap));
+}
+
 // K1 + exact re-check over rows `x` (selection `sel` of length n, or first n rows).
 // x2max: max ||x||^2 over these rows (device; picks the FP16 operand scale).
 // `tiles` = pre-split tcgen05 A tiles for exactly these n rows, built with the
 // scale of this same x2max (or nullptr to build them here).
-void run_bmu(Engine* eng, const float* x, const uint32_t* sel, uint64_t n, const float* x2max,
-             const void* tiles, const float* tiles_xn2, const float* xpad = nullptr) {
-    // the splits read rows from the 256-B-stride copy when there is one
-    const float* xsrc = xpad ? xpad : x;
-    const uint32_t ldx = xpad ? tsom::kPadFloats : eng->D;
+void run_bmu(Engine* eng, const float* x, uint32_t ldx, const uint32_t* sel, uint64_t n,
+             const float* x2max, const void* tiles, const float* tiles_xn2) {
+    const float* xsrc = x;
     CU(cudaMemsetAsync(eng->flags.p, 0, 2 * sizeof(uint32_t), eng->stream));
     if (n == 0) return;
     const int kind = tc_kind(eng);
@@ -191,7 +199,7 @@ void run_bmu(Engine* eng, const float* x, const uint32_t* sel, uint64_t n, const
             tiles = eng->gsplit.p;
             tiles_xn2 = eng->gxn2.as<float>();
         }
-        CU(eng->part.ensure((size_t)groups * tsom::kTcEpiSets * 2 * n * sizeof(float)));
+        CU(eng->part.ensure((size_t)groups * 2 * n * sizeof(float)));
         CU(eng->ties.ensure((n + 1) * sizeof(uint32_t)));
         CU(eng->tmask.ensure(std::max<uint64_t>(n, 1) * sizeof(uint32_t)));
         CU(cudaMemsetAsync(eng->ties.p, 0, sizeof(uint32_t), eng->stream));
@@ -212,32 +220,42 @@ void run_bmu(Engine* eng, const float* x, const uint32_t* sel, uint64_t n, const
         // those rows, then exact FP64 over their few candidates.  The list length
         // stays on the device (kernels grid-stride over it), so the epoch needs
         // no host round trip; rows with > 8 candidates in a group get the full
-        // exact re-scan.
-        // capacity = every row: a collapsed map (large sigma, early epochs) can put
-        // a large share of the rows in the window, and rows past the capacity
-        // would take the full exact re-scan (~60 us per 1e3 rows at K = 1024)
-        const uint64_t cap = n;
+        // exact re-scan.  A collapsed map (large sigma, early epochs) can put a
+        // large share of the rows in the window, so the list is worked through
+        // in up to kTiePasses passes of `cap` slots each: the enumerate scratch
+        // is bounded at ~n / kTiePasses rows, pass p reads its
+        // slot count (clamped to [0, cap]) on the device, and passes past the
+        // actual count exit at once.
+        const uint32_t passes = n > (1u << 20) ? kTiePasses : 1u;
+        const uint64_t cap = (n + passes - 1) / passes;
         const uint64_t mt = (cap + tsom::kTcTileM - 1) / tsom::kTcTileM;
         CU(eng->tsplit.ensure(mt * geo.tile_bytes));
         CU(eng->part2.ensure((size_t)groups * 4 * cap * sizeof(float)));
         CU(eng->txn2.ensure(cap * sizeof(float)));
+        CU(eng->tcnt.ensure(kTiePasses * sizeof(uint32_t)));
         const uint32_t* tcount = eng->ties.as<uint32_t>();
         const uint32_t* tpos = tcount + 1;
-        tsom::launch_split_rows(kind, xsrc, sel, tpos, cap, eng->D, scale, win, eng->tsplit.p,
-                                eng->txn2.as<float>(), eng->stream, tcount, ldx);
-        CU(tsom::launch_bmu_tc(kind, eng->tsplit.p, cap, tcount, true, eng->P, eng->D,
-                               eng->wsplit.p, eng->txn2.as<float>(), w2, scale, win,
-                               eng->tmask.as<uint32_t>(), eng->part2.as<float>(), eng->sm_count,
-                               eng->smem_optin, eng->stream));
-        tsom::launch_merge_partials(eng->part2.as<float>(), tpos, tcount, cap, n, groups, gn,
-                                    eng->txn2.as<float>(), w2, scale, win, x, sel,
-                                    eng->w.as<float>(), eng->D, eng->bmu.as<uint32_t>(),
-                                    eng->flags.as<uint32_t>(), eng->stream);
+        uint32_t* pcount = eng->tcnt.as<uint32_t>();
+        TSOM_LAUNCH(k_tie_pass_counts<<<1, 32, 0, eng->stream>>>(tcount, cap, passes, pcount));
+        for (uint32_t pz = 0; pz < passes; ++pz) {
+            const uint64_t o = (uint64_t)pz * cap;
+            tsom::launch_split_rows(kind, xsrc, sel, tpos + o, cap, eng->D, scale, win,
+                                    eng->tsplit.p, eng->txn2.as<float>(), eng->stream, pcount + pz,
+                                    ldx);
+            CU(tsom::launch_bmu_tc(kind, eng->tsplit.p, cap, pcount + pz, true, eng->P, eng->D,
+                                   eng->wsplit.p, eng->txn2.as<float>(), w2, scale, win,
+                                   eng->tmask.as<uint32_t>() + o, eng->part2.as<float>(),
+                                   eng->sm_count, eng->smem_optin, eng->stream));
+            tsom::launch_merge_partials(eng->part2.as<float>(), tpos + o, pcount + pz, cap, cap,
+                                        groups, gn, eng->txn2.as<float>(), w2, scale, win, x, ldx,
+                                        sel, eng->w.as<float>(), eng->D, eng->bmu.as<uint32_t>(),
+                                        eng->flags.as<uint32_t>(), eng->stream);
+        }
     } else {
         CU(cudaEventRecord(k1_event(eng, 0), eng->stream));
         // the FP32 accumulation bound grows with the d+1 terms of each dot product
         const double tau_s = eng->tau_simt * std::max(1.0, (eng->D + 1) / 51.0);
-        tsom::launch_bmu_simt(x, sel, n, eng->D, eng->wt.as<float>(), eng->P, ppad(eng), x2max,
+        tsom::launch_bmu_simt(x, ldx, sel, n, eng->D, eng->wt.as<float>(), eng->P, ppad(eng), x2max,
                               eng->w2max.as<float>(), (float)tau_s, eng->bmu.as<uint32_t>(),
                               eng->flags.as<uint32_t>(), eng->sm_count, eng->stream);
         CU(cudaEventRecord(k1_event(eng, 1), eng->stream));
@@ -245,8 +263,8 @@ void run_bmu(Engine* eng, const float* x, const uint32_t* sel, uint64_t n, const
         tsom::sampler_pregenerate(eng->sampler, k1_event(eng, 1));
     }
     CU(cudaGetLastError());
-    tsom::launch_rescan(x, sel, eng->w.as<float>(), eng->P, eng->D, eng->flags.as<uint32_t>(), n,
-                        eng->bmu.as<uint32_t>(), eng->stream);
+    tsom::launch_rescan(x, ldx, sel, eng->w.as<float>(), eng->P, eng->D,
+                        eng->flags.as<uint32_t>(), n, eng->bmu.as<uint32_t>(), eng->stream);
     CU(cudaGetLastError());
 }
 
@@ -294,10 +312,58 @@ bool upload_selection(Engine* eng, const uint32_t* sel, uint64_t n) {
     return chk[1] == 0 && n == eng->n_rows;
 }
 
-// the rows get a 256-B-stride copy for the gathers (d even, <= 62; <= 32 GB)
+// resident rows are kept at a 256-B stride (each row exactly two 128-B lines
+// for the K2 gather) when d is even and <= 62 (TSOM_OPT_PAD_ROWS, default on)
 bool pad_eligible(const Engine* eng) {
-    return eng->D % 2 == 0 && eng->D <= tsom::kPadFloats - 2 &&
-           eng->n_rows * (uint64_t)tsom::kPadFloats * 4 <= (32ull << 30);
+    return eng->pad_rows && eng->D % 2 == 0 && eng->D <= tsom::kPadFloats - 2;
+}
+
+// The one resident copy of the bound rows: n_rows at stride ldx (+ slack for
+// the row-window gathers).
+void alloc_resident(Engine* eng, uint64_t n_rows) {
+    eng->ldx = pad_eligible(eng) ? tsom::kPadFloats : eng->D;
+    CU(eng->x.ensure(std::max<uint64_t>(n_rows, 1) * eng->ldx * sizeof(float) + tsom::kRowSlack));
+    eng->x_slack = true;
+}
+
+// Rows [0, total) of the bound host source (caller rows, or shard files read
+// into pinned staging) into the resident copy, C rows per chunk on the copy
+// stream.  Each chunk's row-norm maximum (and, for padded rows, its placement
+// at the 256-B stride from a packed device stage) runs on the engine stream
+// while the next chunk is in flight.
+void upload_resident(Engine* eng, uint64_t total, uint64_t C) {
+    alloc_resident(eng, total);
+    const bool pad = eng->ldx != eng->D;
+    const uint64_t rowb = (uint64_t)eng->D * sizeof(float);
+    C = std::max<uint64_t>(1, std::min<uint64_t>(C, std::max<uint64_t>(total, 1)));
+    if (pad) {
+        CU(eng->stage[0].ensure(C * rowb + tsom::kRowSlack));
+        CU(eng->stage[1].ensure(C * rowb + tsom::kRowSlack));
+    }
+    CU(cudaMemsetAsync(eng->x2max.p, 0, sizeof(float), eng->stream));
+    for (uint64_t r0 = 0, c = 0; r0 < total; r0 += C, ++c) {
+        const uint64_t r1 = std::min(total, r0 + C), nr = r1 - r0;
+        const int s = (int)(c & 1);
+        const float* src = host_chunk_source(eng, r0, r1, s);
+        float* dst = pad ? eng->stage[s].as<float>() : eng->x.as<float>() + r0 * eng->D;
+        if (pad && c >= 2) CU(cudaStreamWaitEvent(eng->copy_stream, eng->ev[4 + s], 0));
+        CU(cudaMemcpyAsync(dst, src, nr * rowb, cudaMemcpyHostToDevice, eng->copy_stream));
+        note_pinned_copy(eng, s);
+        CU(cudaEventRecord(eng->ev[2 + s], eng->copy_stream));
+        CU(cudaStreamWaitEvent(eng->stream, eng->ev[2 + s], 0));
+        tsom::launch_row_norm_max(dst, nr, eng->D, eng->x2max.as<float>(), eng->stream, false);
+        if (pad) {
+            tsom::launch_pad_rows(dst, nr, eng->D, eng->x.as<float>() + r0 * tsom::kPadFloats,
+                                  eng->stream);
+            CU(cudaEventRecord(eng->ev[4 + s], eng->stream));
+        }
+    }
+    CU(cudaGetLastError());
+    CU(cudaStreamSynchronize(eng->stream));
+    if (pad) {
+        eng->stage[0].release(true);
+        eng->stage[1].release(true);
+    }
 }
 
 // K2 scratch (counting sort + piece partials) sized for `rows` rows per launch.
@@ -333,7 +399,7 @@ void accumulate_epoch(Engine* eng, const uint32_t* sel_host, uint64_t n_sel, boo
             sel = sel_host;
     }
     const uint64_t n = sel ? n_sel : eng->n_rows;
-    ensure_rows(eng, n);
+    ensure_rows(eng, n, want_dist);
     const uint32_t* dsel = dev_sel ? dev_sel : (sel ? eng->sel.as<uint32_t>() : nullptr);
     prep_codebook(eng);
     eng->last_recheck = 0;
@@ -355,33 +421,23 @@ void accumulate_epoch(Engine* eng, const uint32_t* sel_host, uint64_t n_sel, boo
                                        eng->stream);
                 tsom::launch_split_rows(kind, eng->x.as<float>(), nullptr, nullptr, eng->n_rows,
                                         eng->D, eng->scale.as<float>(), tie_window(eng, kind),
-                                        eng->xsplit.p, eng->xn2.as<float>(), eng->stream);
+                                        eng->xsplit.p, eng->xn2.as<float>(), eng->stream, nullptr,
+                                        eng->ldx);
                 eng->xsplit_valid = true;
                 eng->xsplit_kind = kind;
             }
             tiles = eng->xsplit.p;
             tiles_xn2 = eng->xn2.as<float>();
         }
-        // a 256-B-stride copy of the rows for the gathered splits and the K2
-        // gather (built once per bind)
-        const float* xpad = nullptr;
-        if (pad_eligible(eng)) {
-            if (!eng->xpad_valid) {
-                CU(eng->xpad.ensure(eng->n_rows * (uint64_t)tsom::kPadFloats * sizeof(float)));
-                tsom::launch_pad_rows(eng->x.as<float>(), eng->n_rows, eng->D,
-                                      eng->xpad.as<float>(), eng->stream);
-                eng->xpad_valid = true;
-            }
-            xpad = eng->xpad.as<float>();
-        }
-        run_bmu(eng, eng->x.as<float>(), dsel, n, eng->x2max.as<float>(), tiles, tiles_xn2, xpad);
+        run_bmu(eng, eng->x.as<float>(), eng->ldx, dsel, n, eng->x2max.as<float>(), tiles,
+                tiles_xn2);
         CU(cudaEventRecord(eng->ev[1], eng->stream));
         ensure_accum(eng, n);
         tsom::launch_accumulate(eng->x.as<float>(), dsel, n, eng->D, eng->w.as<float>(), eng->P,
                                 eng->bmu.as<uint32_t>(),
                                 want_dist ? eng->dist.as<double>() : nullptr, want_dsum,
                                 accumulate, true, eng->acc, eng->sums.as<double>(), eng->sm_count,
-                                eng->stream, eng->x_slack, xpad);
+                                eng->stream, eng->x_slack, eng->ldx);
         CU(cudaGetLastError());
         eng->chunk_counts.clear();
         eng->recheck_from_chunks = true;
@@ -439,7 +495,7 @@ void accumulate_epoch(Engine* eng, const uint32_t* sel_host, uint64_t n_sel, boo
             const uint64_t cn = sel ? (j.p1 - j.p0) : (j.r1 - j.r0);
             const uint32_t* csel = sel ? dsel + j.p0 : nullptr;
             const uint64_t out0 = sel ? j.p0 : j.r0;
-            run_bmu(eng, sel ? xbase : xs, csel, cn, xmax, nullptr, nullptr);
+            run_bmu(eng, sel ? xbase : xs, eng->D, csel, cn, xmax, nullptr, nullptr);
             // re-check counters per chunk, kept on the device (a D2H into pageable
             // memory here would block the host and stall the look-ahead)
             CU(cudaMemcpyAsync(eng->chunk_flags.as<uint32_t>() + 2 * k, eng->flags.p,
@@ -601,6 +657,20 @@ void record_timing(Engine* eng) {
     cudaGetLastError();  // an event pair that was not recorded must not poison later calls
 }
 
+// every device buffer an engine owns (the sampler's are released separately)
+std::vector<DevBuf*> all_buffers(Engine* eng) {
+    return std::vector<DevBuf*>({&eng->x, &eng->xsplit, &eng->xn2, &eng->gxn2, &eng->txn2, &eng->x2max, &eng->w, &eng->wt, &eng->wsplit, &eng->w2,
+                      &eng->w2max, &eng->scale, &eng->prev, &eng->infl, &eng->topo_dist, &eng->sel,
+                      &eng->rows_scratch, &eng->gsplit, &eng->bmu, &eng->dist, &eng->part,
+                      &eng->flags, &eng->ties, &eng->tmask, &eng->part2, &eng->tsplit, &eng->tcnt, &eng->acc_buf[0], &eng->acc_buf[1], &eng->acc_buf[2], &eng->acc_buf[3],
+                      &eng->acc_buf[4], &eng->acc_buf[5], &eng->acc_buf[6], &eng->sums, &eng->chunk_flags,
+                      &eng->topo_buf[0], &eng->topo_buf[1], &eng->topo_buf[2], &eng->topo_buf[3],
+                      &eng->topo_buf[4], &eng->topo_buf[5], &eng->topo_buf[6], &eng->topo_buf[7],
+                      &eng->topo_buf[8], &eng->topo_buf[9], &eng->topo_buf[10], &eng->topo_buf[11],
+                      &eng->topo_buf[12], &eng->topo_buf[13], &eng->topo_buf[14], &eng->U, &eng->H, &eng->status, &eng->smooth_scratch,
+                      &eng->stage[0], &eng->stage[1], &eng->dead});
+}
+
 }  // namespace
 
 extern "C" {
@@ -677,16 +747,7 @@ int tsom_destroy(tsom_engine* eng) {
         pinned_give(eng->pinned[s2], eng->pinned_bytes[s2]);
         if (eng->ev_pin[s2]) cudaEventDestroy(eng->ev_pin[s2]);
     }
-    for (DevBuf* b : {&eng->x, &eng->xsplit, &eng->xn2, &eng->gxn2, &eng->txn2, &eng->x2max, &eng->w, &eng->wt, &eng->wsplit, &eng->w2,
-                      &eng->w2max, &eng->scale, &eng->prev, &eng->infl, &eng->topo_dist, &eng->sel,
-                      &eng->rows_scratch, &eng->gsplit, &eng->bmu, &eng->dist, &eng->part,
-                      &eng->flags, &eng->ties, &eng->tmask, &eng->part2, &eng->tsplit, &eng->acc_buf[0], &eng->acc_buf[1], &eng->acc_buf[2], &eng->acc_buf[3],
-                      &eng->acc_buf[4], &eng->acc_buf[5], &eng->acc_buf[6], &eng->sums, &eng->chunk_flags,
-                      &eng->topo_buf[0], &eng->topo_buf[1], &eng->topo_buf[2], &eng->topo_buf[3],
-                      &eng->topo_buf[4], &eng->topo_buf[5], &eng->topo_buf[6], &eng->topo_buf[7],
-                      &eng->topo_buf[8], &eng->topo_buf[9], &eng->topo_buf[10], &eng->topo_buf[11],
-                      &eng->topo_buf[12], &eng->topo_buf[13], &eng->topo_buf[14], &eng->U, &eng->H, &eng->status, &eng->smooth_scratch,
-                      &eng->stage[0], &eng->stage[1], &eng->dead, &eng->xpad})
+    for (DevBuf* b : all_buffers(eng))
         b->release(true);
     for (auto& ev : eng->ev)
         if (ev) cudaEventDestroy(ev);
@@ -739,6 +800,9 @@ int tsom_set_option(tsom_engine* eng, int key, int64_t value) {
                 REQUIRE(value >= 1, TSOM_ERR_INVALID, "option: barrier timeout >= 1 ms");
                 eng->barrier_timeout_s = (double)value / 1000.0;
                 break;
+            case TSOM_OPT_PAD_ROWS:
+                eng->pad_rows = value != 0;
+                break;
             case TSOM_OPT_STAGING_THREADS:
                 REQUIRE(value >= 1 && value <= 64, TSOM_ERR_INVALID,
                         "option: staging threads in [1, 64]");
@@ -762,97 +826,49 @@ int tsom_bind_host_data(tsom_engine* eng, const float* rows, uint64_t n_rows, ui
         eng->host_direct = false;
         close_shards(eng);
         eng->xsplit_valid = false;
-        eng->xpad_valid = false;
         eng->n_rows = n_rows;
-        if (flags & TSOM_BIND_STREAMED) {
-            eng->streamed = true;
-            eng->host_rows = rows;
-            eng->x.release();
-            // DMA straight from the caller's rows when they are page-locked
-            // already or can be pinned in place; otherwise pinned staging
-            cudaPointerAttributes pa{};
-            if (n_rows && cudaPointerGetAttributes(&pa, rows) == cudaSuccess &&
-                pa.type == cudaMemoryTypeHost) {
-                eng->host_direct = true;
-            } else {
-                cudaGetLastError();
-                if (n_rows && eng->host_register &&
-                    cudaHostRegister(const_cast<float*>(rows), n_rows * eng->D * sizeof(float),
-                                     cudaHostRegisterReadOnly) == cudaSuccess)
-                    eng->host_registered = eng->host_direct = true;
-                else
-                    cudaGetLastError();
-            }
-            return;
-        }
-        eng->streamed = false;
-        eng->host_rows = nullptr;
-        const size_t bytes = n_rows * eng->D * sizeof(float);
-        const char* tr = getenv("TSOM_TRACE_BIND");
-        const auto tb0 = std::chrono::steady_clock::now();
-        CU(eng->x.ensure(bytes + tsom::kRowSlack));
-        const auto tb1 = std::chrono::steady_clock::now();
-        eng->x_slack = true;
         cudaPointerAttributes pa{};
         const bool pinned = n_rows && cudaPointerGetAttributes(&pa, rows) == cudaSuccess &&
                             pa.type == cudaMemoryTypeHost;
         cudaGetLastError();
-        bool norms_done = false;
-        if (pinned && bytes >= ((size_t)256 << 20)) {
-            // page-locked rows in 8 chunks on the copy stream; the row-norm
-            // maximum and the 256-B-stride copy of each chunk run on the
-            // engine stream while the next chunk is in flight
-            const bool pad = pad_eligible(eng);
-            if (pad) CU(eng->xpad.ensure(n_rows * (uint64_t)tsom::kPadFloats * sizeof(float)));
-            CU(cudaMemsetAsync(eng->x2max.p, 0, sizeof(float), eng->stream));
-            const uint64_t C = (n_rows + 7) / 8;
-            for (uint64_t r0 = 0; r0 < n_rows; r0 += C) {
-                const uint64_t nr = std::min(C, n_rows - r0);
-                CU(cudaMemcpyAsync(eng->x.as<float>() + r0 * eng->D, rows + r0 * eng->D,
-                                   nr * eng->D * sizeof(float), cudaMemcpyHostToDevice,
-                                   eng->copy_stream));
-                cudaEvent_t ev;
-                CU(cudaEventCreateWithFlags(&ev, cudaEventDisableTiming));
-                CU(cudaEventRecord(ev, eng->copy_stream));
-                CU(cudaStreamWaitEvent(eng->stream, ev, 0));
-                cudaEventDestroy(ev);  // released once the wait has been satisfied
-                tsom::launch_row_norm_max(eng->x.as<float>() + r0 * eng->D, nr, eng->D,
-                                          eng->x2max.as<float>(), eng->stream, false);
-                if (pad)
-                    tsom::launch_pad_rows(eng->x.as<float>() + r0 * eng->D, nr, eng->D,
-                                          eng->xpad.as<float>() + r0 * tsom::kPadFloats,
-                                          eng->stream);
+        eng->host_rows = rows;
+        if (flags & TSOM_BIND_STREAMED) {
+            eng->streamed = true;
+            eng->x.release();
+            eng->ldx = eng->D;
+            // DMA straight from the caller's rows when they are page-locked
+            // already or can be pinned in place; otherwise pinned staging
+            if (pinned) {
+                eng->host_direct = true;
+            } else if (n_rows && eng->host_register &&
+                       cudaHostRegister(const_cast<float*>(rows), n_rows * eng->D * sizeof(float),
+                                        cudaHostRegisterReadOnly) == cudaSuccess) {
+                eng->host_registered = eng->host_direct = true;
+            } else {
+                cudaGetLastError();
             }
-            eng->xpad_valid = pad;
-            norms_done = true;
-        } else if (pinned || bytes < ((size_t)64 << 20)) {
-            // on the stream the norm kernel below runs on (a plain cudaMemcpy
-            // from pageable memory may return before its DMA lands)
-            if (bytes)
-                CU(cudaMemcpyAsync(eng->x.p, rows, bytes, cudaMemcpyHostToDevice, eng->stream));
-        } else {
-            // pageable rows: the driver's own staging runs at ~11 GB/s and
-            // pinning in place (cudaHostRegister) at ~21 GB/s; the
-            // multi-threaded pinned staging reaches ~22 GB/s (B200 box,
-            // scripts/bind_breakdown.py)
-            eng->host_rows = rows;
-            const uint64_t rowb = (uint64_t)eng->D * sizeof(float);
-            upload_rows(eng, n_rows, std::max<uint64_t>(1, ((uint64_t)32 << 20) / rowb));
-            eng->host_rows = nullptr;
+            return;
         }
-        if (tr && tr[0] == '1') {
-            CU(cudaStreamSynchronize(eng->stream));
-            const auto tb2 = std::chrono::steady_clock::now();
-            fprintf(stderr, "[tsom bind] %s rows=%llu alloc %.2f ms copy %.2f ms\n",
-                    pinned ? "pinned" : "pageable", (unsigned long long)n_rows,
-                    std::chrono::duration<double, std::milli>(tb1 - tb0).count(),
-                    std::chrono::duration<double, std::milli>(tb2 - tb1).count());
-        }
-        if (!norms_done)
-            tsom::launch_row_norm_max(eng->x.as<float>(), n_rows, eng->D,
-                                      eng->x2max.as<float>(), eng->stream);
-        CU(cudaGetLastError());
-        CU(cudaStreamSynchronize(eng->stream));
+        eng->streamed = false;
+        eng->host_direct = pinned;
+        const char* tr = getenv("TSOM_TRACE_BIND");
+        const auto tb0 = std::chrono::steady_clock::now();
+        // page-locked rows: 8 chunks straight from the caller's buffer, each
+        // chunk's norms / 256-B-stride placement overlapped with the next DMA;
+        // pageable rows: 32-MB chunks through the multi-threaded pinned staging
+        // (~22 GB/s, vs ~11 GB/s for the driver's own staging; B200 box,
+        // scripts/bind_breakdown.py)
+        const uint64_t rowb = (uint64_t)eng->D * sizeof(float);
+        const uint64_t C = pinned ? std::max<uint64_t>((n_rows + 7) / 8, 4096)
+                                  : std::max<uint64_t>(1, ((uint64_t)32 << 20) / rowb);
+        upload_resident(eng, n_rows, C);
+        eng->host_rows = nullptr;
+        eng->host_direct = false;
+        if (tr && tr[0] == '1')
+            fprintf(stderr, "[tsom bind] %s rows=%llu ldx=%u %.2f ms\n",
+                    pinned ? "pinned" : "pageable", (unsigned long long)n_rows, eng->ldx,
+                    std::chrono::duration<double, std::milli>(std::chrono::steady_clock::now() -
+                                                              tb0).count());
     });
 }
 
@@ -902,22 +918,16 @@ int tsom_bind_shards(tsom_engine* eng, const char* const* paths, uint32_t n_path
         REQUIRE(total < (1ull << 32), TSOM_ERR_INVALID, "bind: row ids are uint32 (n < 2^32)");
         eng->n_rows = total;
         eng->xsplit_valid = false;
-        eng->xpad_valid = false;
         if (flags & TSOM_BIND_STREAMED) {
             eng->streamed = true;
             eng->x.release();
+            eng->ldx = eng->D;
             return;
         }
         // resident: stream the files once into HBM through the pinned staging
         eng->streamed = false;
-        CU(eng->x.ensure(total * eng->D * sizeof(float) + tsom::kRowSlack));
-        eng->x_slack = true;
-        upload_rows(eng, total, eng->stream_chunk_rows);
+        upload_resident(eng, total, eng->stream_chunk_rows);
         close_shards(eng);
-        tsom::launch_row_norm_max(eng->x.as<float>(), total, eng->D, eng->x2max.as<float>(),
-                                  eng->stream);
-        CU(cudaGetLastError());
-        CU(cudaStreamSynchronize(eng->stream));
     });
 }
 
@@ -950,14 +960,15 @@ int tsom_bind_device_data(tsom_engine* eng, const float* d_rows, uint64_t n_rows
         CU(cudaSetDevice(eng->device));
         REQUIRE(n_rows < (1ull << 32), TSOM_ERR_INVALID, "bind: row ids are uint32 (n < 2^32)");
         eng->x.release();
+        // borrowed rows keep the caller's packed layout (no second copy)
         eng->x.p = const_cast<float*>(d_rows);
         eng->x.bytes = n_rows * eng->D * sizeof(float);
         eng->x.owned = false;
+        eng->ldx = eng->D;
         eng->x_slack = device_slack_after(d_rows, (size_t)n_rows * eng->D * sizeof(float));
         eng->n_rows = n_rows;
         eng->streamed = false;
         eng->xsplit_valid = false;
-        eng->xpad_valid = false;
         tsom::launch_row_norm_max(d_rows, n_rows, eng->D, eng->x2max.as<float>(), eng->stream);
         CU(cudaGetLastError());
         CU(cudaStreamSynchronize(eng->stream));
@@ -981,18 +992,15 @@ int tsom_bind_synthetic_gmm(tsom_engine* eng, uint64_t n_rows, uint64_t seed, ui
         DevBuf dc;
         CU(dc.ensure(centres.size() * sizeof(float)));
         CU(tsom::h2d_blocking(dc.p, centres.data(), centres.size() * sizeof(float)));
-        const size_t bytes = n_rows * eng->D * sizeof(float);
-        CU(eng->x.ensure(bytes + tsom::kRowSlack));
-        eng->x_slack = true;
-        tsom::launch_synth_gmm(eng->x.as<float>(), n_rows, eng->D, dc.as<float>(), n_comp, seed,
-                               row_offset, eng->stream);
-        CU(cudaGetLastError());
         eng->n_rows = n_rows;
+        alloc_resident(eng, n_rows);
+        tsom::launch_synth_gmm(eng->x.as<float>(), n_rows, eng->D, dc.as<float>(), n_comp, seed,
+                               row_offset, eng->stream, eng->ldx);
+        CU(cudaGetLastError());
         eng->streamed = false;
         eng->xsplit_valid = false;
-        eng->xpad_valid = false;
         tsom::launch_row_norm_max(eng->x.as<float>(), n_rows, eng->D, eng->x2max.as<float>(),
-                                  eng->stream);
+                                  eng->stream, true, eng->ldx);
         CU(cudaStreamSynchronize(eng->stream));
         dc.release();
     });
@@ -1088,11 +1096,11 @@ int tsom_bmu(tsom_engine* eng, const float* rows, uint64_t n, uint32_t* bmu, dou
         CU(eng->rows_scratch.ensure(n * eng->D * sizeof(float) + tsom::kRowSlack));
         CU(cudaMemcpyAsync(eng->rows_scratch.p, rows, n * eng->D * sizeof(float),
                            cudaMemcpyHostToDevice, eng->stream));
-        ensure_rows(eng, n);
+        ensure_rows(eng, n, dist != nullptr);
         CU(eng->sums.ensure(slot_len(eng) * sizeof(double)));
         float* xm = eng->x2max.as<float>() + 1;
         tsom::launch_row_norm_max(eng->rows_scratch.as<float>(), n, eng->D, xm, eng->stream);
-        run_bmu(eng, eng->rows_scratch.as<float>(), nullptr, n, xm, nullptr, nullptr);
+        run_bmu(eng, eng->rows_scratch.as<float>(), eng->D, nullptr, n, xm, nullptr, nullptr);
         if (dist) {
             ensure_accum(eng, n);
             tsom::launch_accumulate(eng->rows_scratch.as<float>(), nullptr, n, eng->D,
@@ -1523,6 +1531,8 @@ int tsom_sampler_observe(tsom_engine* eng, const double* dist) {
         if (smp.kind != 2) return;
         const uint64_t m = smp.last_m;
         const double* d = eng->dist.as<double>();
+        REQUIRE(dist || d || m == 0, TSOM_ERR_INVALID,
+                "sampler: no distances to observe (no sampled epoch produced them)");
         if (dist) {
             CU(eng->dist.ensure(std::max<uint64_t>(m, 1) * sizeof(double)));
             CU(cudaMemcpyAsync(eng->dist.p, dist, m * sizeof(double), cudaMemcpyHostToDevice,
@@ -1835,6 +1845,21 @@ int tsom_last_timing_detail(const tsom_engine* eng, float out[8]) {
 }
 
 uint64_t tsom_kernel_launches(void) { return tsom::g_launches.load(); }
+
+uint64_t tsom_device_bytes(const tsom_engine* e) {
+    if (!e) return 0;
+    Engine* eng = const_cast<tsom_engine*>(e);
+    uint64_t total = 0;
+    for (const DevBuf* b : all_buffers(eng))
+        if (b->owned) total += b->bytes;
+    const tsom::SamplerState& s = eng->sampler;
+    for (const DevBuf* b : {&s.window, &s.jp, &s.gwin, &s.misc, &s.seqb[0], &s.seqb[1],
+                            &s.drawsb[0], &s.drawsb[1], &s.tailb[0], &s.tailb[1], &s.err, &s.age,
+                            &s.keys, &s.hist, &s.cand, &s.ccnt, &s.first, &s.tidx, &s.bitmap,
+                            &s.bcount, &s.sel, &s.jN, &s.glist, &s.slots})
+        total += b->bytes;
+    return total;
+}
 
 void* tsom_stream(tsom_engine* eng) { return eng ? (void*)eng->stream : nullptr; }
 

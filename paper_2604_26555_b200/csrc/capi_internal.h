@@ -45,8 +45,6 @@ void pinned_give(void* p, size_t bytes);
 // host pointer of rows [r0, r1) the copy engine can read (slot s when staged)
 const float* host_chunk_source(Engine* eng, uint64_t r0, uint64_t r1, int s);
 void note_pinned_copy(Engine* eng, int s);
-// rows [0, total) of the bound host source into eng->x, C rows per chunk
-void upload_rows(Engine* eng, uint64_t total, uint64_t C);
 
 }  // namespace host
 }  // namespace tsom

@@ -45,6 +45,9 @@ struct DevBuf {
 };
 
 void release_cached_memory();  // trim the device pool DevBuf allocates from
+// cudaFuncSetAttribute(MaxDynamicSharedMemorySize, >= bytes) once per (kernel, device)
+// (newly_set: true when this call set it, i.e. first use on this device)
+cudaError_t ensure_smem_attr(const void* func, size_t bytes, bool* newly_set = nullptr);
 
 // Host-to-device copy that is complete on return.  cudaMemcpy from pageable
 // memory may return once the data is staged, before the DMA lands; kernels on
@@ -219,7 +222,9 @@ struct Engine {
     uint64_t stream_chunk_rows = 1u << 20;
 
     // bound data
-    DevBuf x;           // resident rows
+    DevBuf x;           // resident rows, row stride ldx floats
+    uint32_t ldx = 0;   // D (packed), or kPadFloats: each row on its own two 128-B lines
+    bool pad_rows = true;  // TSOM_OPT_PAD_ROWS
     uint64_t n_rows = 0;
     bool x_slack = false;  // kRowSlack bytes readable after the last resident row
     bool streamed = false;
@@ -258,7 +263,8 @@ struct Engine {
     DevBuf ties;           // [0] near-tie count, then positions (enumerate pass input)
     DevBuf tmask;          // per near-tie row: bitmask of groups inside the window
     DevBuf part2;          // enumerate-pass partials
-    DevBuf tsplit;         // split tiles of the near-tie rows
+    DevBuf tsplit;         // split tiles of the near-tie rows (one pass of them)
+    DevBuf tcnt;           // per-pass near-tie counts
     DevBuf acc_buf[7];     // AccumScratch arrays
     tsom::AccumScratch acc;
     uint64_t acc_rows = 0; // capacity the scratch was sized for
@@ -289,8 +295,6 @@ struct Engine {
     std::vector<cudaEvent_t> k1_ev;
     int k1_slot = -1;
     DevBuf dead;
-    DevBuf xpad;              // resident rows at a 256-B stride for the K2 gather
-    bool xpad_valid = false;
     uint64_t last_recheck = 0;
     std::vector<uint32_t> chunk_counts;  // per-chunk re-check counts (streamed epochs)
     // pinned per-epoch status words, read back asynchronously before the one
@@ -334,7 +338,8 @@ void launch_prep_codebook(const float* w, uint32_t P, uint32_t D, double* w2, fl
                           float* wt, uint32_t Ppad, cudaStream_t st);
 // max ||x||^2 over rows (f32 atomic max on non-negative floats)
 void launch_row_norm_max(const float* x, uint64_t n, uint32_t D, float* out, cudaStream_t st,
-                         bool reset = true);  // reset = false: fold into *out (atomicMax)
+                         bool reset = true,  // reset = false: fold into *out (atomicMax)
+                         uint32_t ldx = 0);  // row stride in floats (0: D)
 // a[0] = max(a[0], a[1])
 void launch_fold_max(float* a, cudaStream_t st);
 // split rows (optionally gathered through sel, and/or through a position list
@@ -357,9 +362,10 @@ __host__ __device__ inline uint32_t tc_group_width(uint32_t P) {
 }
 
 // K1: BMU candidates.  SIMT variant writes final bmu + flags directly.
-void launch_bmu_simt(const float* x, const uint32_t* sel, uint64_t n, uint32_t D, const float* wt,
-                     uint32_t P, uint32_t Ppad, const float* x2max, const float* w2max, float tau,
-                     uint32_t* bmu, uint32_t* flags, int sm_count, cudaStream_t st);
+void launch_bmu_simt(const float* x, uint32_t ldx, const uint32_t* sel, uint64_t n, uint32_t D,
+                     const float* wt, uint32_t P, uint32_t Ppad, const float* x2max,
+                     const float* w2max, float tau, uint32_t* bmu, uint32_t* flags, int sm_count,
+                     cudaStream_t st);
 // tcgen05 variant: per-group partials (enumerate = candidate lists; dev_n =
 // optional device row count).
 cudaError_t launch_bmu_tc(int kind, const void* tiles, uint64_t n, const uint32_t* dev_n,
@@ -384,11 +390,11 @@ void launch_merge_fast(const float* part, uint64_t n, uint32_t groups, uint32_t 
 void launch_merge_partials(const float* part, const uint32_t* ties, const uint32_t* dev_count,
                            uint64_t cap, uint64_t n_max, uint32_t groups, uint32_t gn,
                            const float* xn2, const float* w2max, const float* scale, TieWin win,
-                           const float* x, const uint32_t* sel, const float* w, uint32_t D,
-                           uint32_t* bmu, uint32_t* flags, cudaStream_t st);
+                           const float* x, uint32_t ldx, const uint32_t* sel, const float* w,
+                           uint32_t D, uint32_t* bmu, uint32_t* flags, cudaStream_t st);
 // exact FP64 re-scan of flagged rows (reference loop order)
-void launch_rescan(const float* x, const uint32_t* sel, const float* w, uint32_t P, uint32_t D,
-                   const uint32_t* flags, uint64_t n, uint32_t* bmu, cudaStream_t st);
+void launch_rescan(const float* x, uint32_t ldx, const uint32_t* sel, const float* w, uint32_t P,
+                   uint32_t D, const uint32_t* flags, uint64_t n, uint32_t* bmu, cudaStream_t st);
 
 void accum_scratch_bytes(uint64_t n, uint32_t P, uint32_t D, size_t out[7]);
 // sums = [R (P*d) | c (P) | sum dist | rows]; first=false adds to it (streamed chunks).
@@ -397,9 +403,9 @@ void launch_accumulate(const float* x, const uint32_t* sel, uint64_t n, uint32_t
                        const float* w, uint32_t P, const uint32_t* bmu, double* dist_out,
                        bool want_dist_sum, bool accumulate, bool first, const AccumScratch& s,
                        double* sums, int sm_count, cudaStream_t st, bool x_slack = false,
-                       const float* xpad = nullptr);
-// the resident rows copied at a 256-byte stride (kPadFloats floats per row;
-// the K2 gather's rows are then exactly two 128-byte lines)
+                       uint32_t ldx = 0);  // row stride in floats (0: D; kPadFloats: padded rows)
+// resident rows at a 256-byte stride (kPadFloats floats per row, zero tail):
+// the K2 gather's rows are then exactly two 128-byte lines
 constexpr uint32_t kPadFloats = 64;
 void launch_pad_rows(const float* x, uint64_t n, uint32_t D, float* xpad, cudaStream_t st);
 // bytes of slack the engine allocates after resident rows (TMA row gathers read
@@ -428,6 +434,6 @@ void launch_influence(const double* dist, size_t n, double inv_two_sigma_sq, dou
                       cudaStream_t st);
 // synthetic Gaussian mixture rows
 void launch_synth_gmm(float* x, uint64_t n, uint32_t D, const float* centres, uint32_t n_comp,
-                      uint64_t seed, uint64_t row_offset, cudaStream_t st);
+                      uint64_t seed, uint64_t row_offset, cudaStream_t st, uint32_t ldx = 0);
 
 }  // namespace tsom

@@ -205,18 +205,5 @@ void note_pinned_copy(Engine* eng, int s) {
 // Copy rows [0, total) of the bound host source (shard files or caller rows)
 // into eng->x: staging threads fill one pinned slot while the copy engine
 // drains the other.
-void upload_rows(Engine* eng, uint64_t total, uint64_t C) {
-    for (uint64_t r0 = 0, c = 0; r0 < total; r0 += C, ++c) {
-        const uint64_t r1 = std::min(total, r0 + C);
-        const int s = (int)(c & 1);
-        const float* src = host_chunk_source(eng, r0, r1, s);
-        CU(cudaMemcpyAsync(eng->x.as<float>() + r0 * eng->D, src,
-                           (r1 - r0) * eng->D * sizeof(float), cudaMemcpyHostToDevice,
-                           eng->copy_stream));
-        note_pinned_copy(eng, s);
-    }
-    CU(cudaStreamSynchronize(eng->copy_stream));
-}
-
 }  // namespace host
 }  // namespace tsom

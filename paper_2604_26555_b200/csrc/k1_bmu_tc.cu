@@ -514,15 +514,13 @@ void launch_split_rows(int kind, const float* x, const uint32_t* sel, const uint
     else {
         const size_t wsmem = (size_t)(kSplitThreads / 32) * kSplitWarpRows *
                              (tc_geom(kTcF16, D).kpad + 8) * sizeof(__half);
-        static bool attr_set = false;
-        if (!attr_set) {
-            cudaFuncSetAttribute(k_split_rows_f16, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                                 (int)((kSplitThreads / 32) * kSplitWarpRows *
-                                       (kTcF16MaxK + 8) * sizeof(__half)));
-            cudaFuncSetAttribute(k_split_rows_f16,
-                                 cudaFuncAttributePreferredSharedMemoryCarveout, 100);
-            attr_set = true;
-        }
+        bool first = false;
+        ensure_smem_attr((const void*)k_split_rows_f16,
+                         (kSplitThreads / 32) * kSplitWarpRows * (kTcF16MaxK + 8) * sizeof(__half),
+                         &first);
+        if (first)
+            cudaFuncSetAttribute(k_split_rows_f16, cudaFuncAttributePreferredSharedMemoryCarveout,
+                                 100);
         uint64_t blocks = (n + kTcTileM - 1) / kTcTileM;  // 8 warps x 16 rows per tile
         if (blocks > 148ull * 8) blocks = 148ull * 8;
         TSOM_LAUNCH(k_split_rows_f16<<<(unsigned)blocks, kSplitThreads, wsmem, st>>>(
@@ -555,6 +553,7 @@ __global__ void __launch_bounds__(EpiCfg<kKind>::kThreads, 1)
     constexpr int kSets = EpiCfg<kKind>::kSets, kCPS = EpiCfg<kKind>::kCPS;
     const TcGeom geo = tc_geom(kKind, D);
     const uint64_t n = dev_n ? min((uint64_t)*dev_n, n_host) : n_host;
+    if (n == 0) return;  // an empty near-tie pass (uniform over the grid and its clusters)
     const uint32_t ntiles = (uint32_t)((n + kTcTileM - 1) / kTcTileM);
     const uint32_t w_bytes = gn * geo.row_bytes;  // this CTA's group (both halves for tf32)
     uint8_t* sW = smem;
@@ -915,12 +914,9 @@ cudaError_t launch_bmu_tc(int kind, const void* tiles, uint64_t n, const uint32_
         kern = enumerate ? k1_bmu_tc<kTcF16, true> : k1_bmu_tc<kTcF16, false>;
         slot = enumerate ? 3 : 2;
     }
-    static size_t attr[4] = {0, 0, 0, 0};
-    if (attr[slot] < smem) {
-        cudaError_t e = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                                             (int)smem);
+    {
+        const cudaError_t e = ensure_smem_attr((const void*)kern, smem);
         if (e != cudaSuccess) return e;
-        attr[slot] = smem;
     }
     const int threads = kind == kTcF16 ? EpiCfg<kTcF16>::kThreads : EpiCfg<kTcTf32>::kThreads;
     // cluster of the `groups` CTAs that share each A tile (multicast loads);

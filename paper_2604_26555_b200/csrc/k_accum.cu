@@ -618,7 +618,8 @@ void launch_accumulate(const float* x, const uint32_t* sel, uint64_t n, uint32_t
                        const float* w, uint32_t P, const uint32_t* bmu, double* dist_out,
                        bool want_dist_sum, bool accumulate, bool first, const AccumScratch& s,
                        double* sums, int sm_count, cudaStream_t st, bool x_slack,
-                       const float* xpad) {
+                       uint32_t ldx) {
+    if (ldx == 0) ldx = D;
     const int add = first ? 0 : 1;
     if (n == 0) {
         if (first) cudaMemsetAsync(sums, 0, ((size_t)P * D + P + 2) * sizeof(double), st);
@@ -631,13 +632,9 @@ void launch_accumulate(const float* x, const uint32_t* sel, uint64_t n, uint32_t
         return;
     }
     const uint32_t nblk = (uint32_t)accum_blocks(n);
-    static uint32_t attr_p = 0;
-    if (P > attr_p) {  // dynamic smem beyond 48 KB (P up to ~7000 nodes)
-        cudaFuncSetAttribute(k_hist, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)(P * 4));
-        cudaFuncSetAttribute(k_scatter, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                             (int)(kScatterWarps * P * 4));
-        attr_p = P;
-    }
+    // dynamic smem beyond 48 KB (P up to ~7000 nodes)
+    ensure_smem_attr((const void*)k_hist, (size_t)P * 4);
+    ensure_smem_attr((const void*)k_scatter, (size_t)kScatterWarps * P * 4);
     TSOM_LAUNCH(k_hist<<<nblk, 512, P * sizeof(uint32_t), st>>>(bmu, n, P, s.counts));
     TSOM_LAUNCH(k_colscan<<<(P + 31) / 32, 256, 0, st>>>(s.counts, nblk, P, s.totals));
     TSOM_LAUNCH(k_nodescan<<<1, 1024, 0, st>>>(s.totals, P, D, s.node_start, s.piece_start,
@@ -657,32 +654,21 @@ void launch_accumulate(const float* x, const uint32_t* sel, uint64_t n, uint32_t
     const size_t asmem = (size_t)kAsyncWarps * 2 * 32 * D * sizeof(float);
     const uint32_t slot = (D * 4 + 8 + 15) / 16 * 16;  // longest 16-B window of a row
     const size_t tsmem = (size_t)kTmaWarps * 2 * 32 * slot;
-    // padded copy (rows at a 256-B stride, line aligned): a row is exactly two
-    // 128-B lines instead of two or three
-    const bool use_pad = xpad && v2 && D <= kPadFloats - 2 && g_gather_kind == 0 &&
-                         tsmem <= 110 * 1024;
+    // padded rows (a 256-B stride, line aligned): a row is exactly two 128-B
+    // lines instead of two or three; only the TMA gather reads strided rows
+    const bool use_pad = ldx != D;
     if (use_pad ||
         (v2 && x_slack && g_gather_kind == 0 && ((reinterpret_cast<uintptr_t>(x) & 15u) == 0) &&
          tsmem <= 110 * 1024)) {
-        static size_t tattr = 0;
-        if (tattr < tsmem) {
-            cudaFuncSetAttribute(k_gather_tma, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                                 (int)tsmem);
-            tattr = tsmem;
-        }
+        ensure_smem_attr((const void*)k_gather_tma, tsmem);
         const uint64_t tblocks = (pieces + kTmaWarps - 1) / kTmaWarps;
         const unsigned tb = (unsigned)(tblocks < (uint64_t)sm_count * 2 ? tblocks : sm_count * 2);
         TSOM_LAUNCH(k_gather_tma<<<tb, kTmaWarps * 32, tsmem, st>>>(
-            use_pad ? xpad : x, use_pad ? (uint32_t)kPadFloats : D, sel, w, P, D, slot, s.sorted,
+            x, ldx, sel, w, P, D, slot, s.sorted,
             s.node_start, s.piece_start, s.piece_node, s.partial, dist_out, want_dist ? 1 : 0,
             accumulate ? 1 : 0));
     } else if (v2 && D <= 64 && asmem <= 110 * 1024) {
-        static size_t aattr = 0;
-        if (aattr < asmem) {
-            cudaFuncSetAttribute(k_gather_async, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                                 (int)asmem);
-            aattr = asmem;
-        }
+        ensure_smem_attr((const void*)k_gather_async, asmem);
         const uint64_t ablocks = (pieces + kAsyncWarps - 1) / kAsyncWarps;
         const unsigned ab = (unsigned)(ablocks < (uint64_t)sm_count * 2 ? ablocks : sm_count * 2);
         TSOM_LAUNCH(k_gather_async<<<ab, kAsyncWarps * 32, asmem, st>>>(

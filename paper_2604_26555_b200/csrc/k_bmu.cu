@@ -53,12 +53,12 @@ void launch_prep_codebook(const float* w, uint32_t P, uint32_t D, double* w2, fl
 // max ||x||^2 (bound once per dataset)
 // ---------------------------------------------------------------------------
 
-__global__ void k_row_norm_max(const float* __restrict__ x, uint64_t n, uint32_t D,
+__global__ void k_row_norm_max(const float* __restrict__ x, uint64_t n, uint32_t D, uint32_t ldx,
                                float* __restrict__ out) {
     float best = 0.0f;
     for (uint64_t i = blockIdx.x * (uint64_t)blockDim.x + threadIdx.x; i < n;
          i += (uint64_t)gridDim.x * blockDim.x) {
-        const float* r = x + i * D;
+        const float* r = x + i * ldx;
         double s = 0.0;
         for (uint32_t k = 0; k < D; ++k) s += (double)r[k] * (double)r[k];
         best = fmaxf(best, (float)s * 1.0000002f);
@@ -68,12 +68,12 @@ __global__ void k_row_norm_max(const float* __restrict__ x, uint64_t n, uint32_t
 }
 
 void launch_row_norm_max(const float* x, uint64_t n, uint32_t D, float* out, cudaStream_t st,
-                         bool reset) {
+                         bool reset, uint32_t ldx) {
     if (reset) cudaMemsetAsync(out, 0, sizeof(float), st);
     if (n == 0) return;
     uint64_t blocks = (n + 255) / 256;
     if (blocks > 148 * 16) blocks = 148 * 16;
-    TSOM_LAUNCH(k_row_norm_max<<<(unsigned)blocks, 256, 0, st>>>(x, n, D, out));
+    TSOM_LAUNCH(k_row_norm_max<<<(unsigned)blocks, 256, 0, st>>>(x, n, D, ldx ? ldx : D, out));
 }
 
 __global__ void k_fold_max(float* a) { a[0] = fmaxf(a[0], a[1]); }
@@ -104,7 +104,7 @@ __device__ __forceinline__ void top2_merge(float& b1, uint32_t& i1, float& b2, f
 }
 
 __global__ void __launch_bounds__(256) k1_bmu_simt(
-    const float* __restrict__ x, const uint32_t* __restrict__ sel, uint64_t n, uint32_t D,
+    const float* __restrict__ x, uint32_t ldx, const uint32_t* __restrict__ sel, uint64_t n, uint32_t D,
     const float* __restrict__ wt, uint32_t P, uint32_t Ppad, const float* __restrict__ x2max,
     const float* __restrict__ w2max, float tau, uint32_t* __restrict__ bmu,
     uint32_t* __restrict__ flags) {
@@ -125,7 +125,7 @@ __global__ void __launch_bounds__(256) k1_bmu_simt(
             float v = 0.0f;
             if (pos < n) {
                 const uint64_t row = sel ? (uint64_t)sel[pos] : pos;
-                v = x[row * D + k];
+                v = x[row * ldx + k];
             }
             xs[k * SIMT_XS + r] = v;
         }
@@ -205,20 +205,17 @@ __global__ void __launch_bounds__(256) k1_bmu_simt(
     }
 }
 
-void launch_bmu_simt(const float* x, const uint32_t* sel, uint64_t n, uint32_t D, const float* wt,
-                     uint32_t P, uint32_t Ppad, const float* x2max, const float* w2max, float tau,
-                     uint32_t* bmu, uint32_t* flags, int sm_count, cudaStream_t st) {
+void launch_bmu_simt(const float* x, uint32_t ldx, const uint32_t* sel, uint64_t n, uint32_t D,
+                     const float* wt, uint32_t P, uint32_t Ppad, const float* x2max,
+                     const float* w2max, float tau, uint32_t* bmu, uint32_t* flags, int sm_count,
+                     cudaStream_t st) {
     if (n == 0) return;
     const size_t smem = (size_t)(D + 1) * (SIMT_XS + SIMT_TN) * sizeof(float);
-    static bool attr_set = false;
-    if (!attr_set) {
-        cudaFuncSetAttribute(k1_bmu_simt, cudaFuncAttributeMaxDynamicSharedMemorySize, 200 * 1024);
-        attr_set = true;
-    }
+    ensure_smem_attr((const void*)k1_bmu_simt, 200 * 1024);
     uint64_t tiles = (n + SIMT_TM - 1) / SIMT_TM;
     uint64_t grid = (uint64_t)sm_count * 8;
     if (grid > tiles) grid = tiles;
-    TSOM_LAUNCH(k1_bmu_simt<<<(unsigned)grid, 256, smem, st>>>(x, sel, n, D, wt, P, Ppad, x2max, w2max, tau, bmu,
+    TSOM_LAUNCH(k1_bmu_simt<<<(unsigned)grid, 256, smem, st>>>(x, ldx, sel, n, D, wt, P, Ppad, x2max, w2max, tau, bmu,
                                                    flags));
 }
 
@@ -340,7 +337,7 @@ __global__ void k_merge_partials(const float* __restrict__ part, const uint32_t*
                                  uint32_t groups, uint32_t gn,
                                  const float* __restrict__ xn2, const float* __restrict__ w2max,
                                  const float* __restrict__ scale, TieWin win,
-                                 const float* __restrict__ x,
+                                 const float* __restrict__ x, uint32_t ldx,
                                  const uint32_t* __restrict__ sel, const float* __restrict__ w,
                                  uint32_t D, uint32_t* __restrict__ bmu,
                                  uint32_t* __restrict__ flags) {
@@ -383,7 +380,7 @@ __global__ void k_merge_partials(const float* __restrict__ part, const uint32_t*
             continue;
         }
         atomicAdd(&flags[1], 1u);
-        const float* xr = x + (sel ? (uint64_t)sel[pos] : (uint64_t)pos) * D;
+        const float* xr = x + (sel ? (uint64_t)sel[pos] : (uint64_t)pos) * ldx;
         double best = CUDART_INF;
         uint32_t best_j = 0;
         for (uint32_t g = 0; g < groups; ++g) {
@@ -408,14 +405,15 @@ __global__ void k_merge_partials(const float* __restrict__ part, const uint32_t*
 void launch_merge_partials(const float* part, const uint32_t* ties, const uint32_t* dev_count,
                            uint64_t cap, uint64_t n_max, uint32_t groups, uint32_t gn,
                            const float* xn2, const float* w2max, const float* scale, TieWin win,
-                           const float* x, const uint32_t* sel, const float* w, uint32_t D,
-                           uint32_t* bmu, uint32_t* flags, cudaStream_t st) {
+                           const float* x, uint32_t ldx, const uint32_t* sel, const float* w,
+                           uint32_t D, uint32_t* bmu, uint32_t* flags, cudaStream_t st) {
     if (n_max == 0) return;
     // grid-strides over the device count; sized for the enumerate capacity
     uint64_t blocks = (std::min(cap, n_max) + 255) / 256;
     blocks = std::max<uint64_t>(1, std::min<uint64_t>(blocks, 148ull * 16));
     TSOM_LAUNCH(k_merge_partials<<<(unsigned)blocks, 256, 0, st>>>(
-        part, ties, dev_count, cap, groups, gn, xn2, w2max, scale, win, x, sel, w, D, bmu, flags));
+        part, ties, dev_count, cap, groups, gn, xn2, w2max, scale, win, x, ldx, sel, w, D, bmu,
+        flags));
 }
 
 // ---------------------------------------------------------------------------
@@ -430,7 +428,7 @@ void launch_merge_partials(const float* part, const uint32_t* ties, const uint32
 // with ties to the lowest j.
 constexpr int kRescanRows = 32, kRescanNodes = 64;
 
-__global__ void __launch_bounds__(256) k_rescan(const float* __restrict__ x,
+__global__ void __launch_bounds__(256) k_rescan(const float* __restrict__ x, uint32_t ldx,
                                                 const uint32_t* __restrict__ sel,
                                                 const float* __restrict__ w, uint32_t P,
                                                 uint32_t D, const uint32_t* __restrict__ flags,
@@ -448,7 +446,7 @@ __global__ void __launch_bounds__(256) k_rescan(const float* __restrict__ x,
             const uint32_t rr = e / D, k = e - rr * D;
             const uint32_t pos = flags[2 + f0 + rr];
             const uint64_t row = sel ? (uint64_t)sel[pos] : pos;
-            xs[rr * D + k] = x[row * D + k];
+            xs[rr * D + k] = x[row * ldx + k];
         }
         double best = CUDART_INF;
         uint32_t best_j = 0xFFFFFFFFu;
@@ -489,17 +487,13 @@ __global__ void __launch_bounds__(256) k_rescan(const float* __restrict__ x,
     }
 }
 
-void launch_rescan(const float* x, const uint32_t* sel, const float* w, uint32_t P, uint32_t D,
-                   const uint32_t* flags, uint64_t n, uint32_t* bmu, cudaStream_t st) {
+void launch_rescan(const float* x, uint32_t ldx, const uint32_t* sel, const float* w, uint32_t P,
+                   uint32_t D, const uint32_t* flags, uint64_t n, uint32_t* bmu, cudaStream_t st) {
     if (n == 0) return;
     // flagged rows are usually few: the kernel grid-strides over the device count
     const size_t smem = ((size_t)kRescanRows * D + (size_t)kRescanNodes * (D + 1)) * sizeof(float);
-    static size_t attr = 0;
-    if (smem > attr) {
-        cudaFuncSetAttribute(k_rescan, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
-        attr = smem;
-    }
-    TSOM_LAUNCH(k_rescan<<<148 * 2, 256, smem, st>>>(x, sel, w, P, D, flags, bmu));
+    ensure_smem_attr((const void*)k_rescan, smem);
+    TSOM_LAUNCH(k_rescan<<<148 * 2, 256, smem, st>>>(x, ldx, sel, w, P, D, flags, bmu));
 }
 
 }  // namespace tsom

@@ -751,13 +751,8 @@ static void generate_draws(SamplerState& s, int b, cudaStream_t st) {
     TSOM_LAUNCH(k_mt_extend<<<1, kT, 0, st>>>(s.window.as<uint64_t>(), twists,
                                               s.seqb[b].as<uint64_t>()));
     const size_t smem = (mt::kSeq + 312) * 8 + kJumpIdxBytes;
-    static bool attr = false;
-    if (!attr) {
-        cudaFuncSetAttribute(k_mt_jump_all, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
-        cudaFuncSetAttribute(k_mt_jump_window, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                             (int)smem);
-        attr = true;
-    }
+    ensure_smem_attr((const void*)k_mt_jump_all, smem);
+    ensure_smem_attr((const void*)k_mt_jump_window, smem);
     const uint64_t total = s.draws_per_epoch + kSlack;
     TSOM_LAUNCH(k_mt_jump_all<<<s.G, kT, smem, st>>>(s.seqb[b].as<uint64_t>(), s.jp.as<uint64_t>(),
                                                      s.L, total, s.gwin.as<uint64_t>(), s.jump0));

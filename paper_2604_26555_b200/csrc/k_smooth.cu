@@ -218,7 +218,7 @@ __device__ __forceinline__ uint64_t smix(uint64_t z) {
     return z ^ (z >> 31);
 }
 
-__global__ void k_synth_gmm(float* __restrict__ x, uint64_t n, uint32_t D,
+__global__ void k_synth_gmm(float* __restrict__ x, uint64_t n, uint32_t D, uint32_t ldx,
                             const float* __restrict__ centres, uint32_t n_comp, uint64_t seed,
                             uint64_t row_offset) {
     const uint64_t i = blockIdx.x * (uint64_t)blockDim.x + threadIdx.x;
@@ -226,7 +226,8 @@ __global__ void k_synth_gmm(float* __restrict__ x, uint64_t n, uint32_t D,
     const uint64_t g = row_offset + i;
     const uint64_t base = smix(seed ^ smix(g));
     const uint32_t m = (uint32_t)(base % n_comp);
-    float* row = x + i * D;
+    float* row = x + i * ldx;
+    for (uint32_t k = D; k < ldx; ++k) row[k] = 0.0f;  // padded rows: zero tail
     for (uint32_t k = 0; k < D; k += 2) {
         const uint64_t h = smix(base + k);
         const float u1 = 1.0f - (float)(h >> 40) * 0x1.0p-24f;  // (0, 1]
@@ -240,10 +241,10 @@ __global__ void k_synth_gmm(float* __restrict__ x, uint64_t n, uint32_t D,
 }
 
 void launch_synth_gmm(float* x, uint64_t n, uint32_t D, const float* centres, uint32_t n_comp,
-                      uint64_t seed, uint64_t row_offset, cudaStream_t st) {
+                      uint64_t seed, uint64_t row_offset, cudaStream_t st, uint32_t ldx) {
     if (n == 0) return;
-    TSOM_LAUNCH(k_synth_gmm<<<(unsigned)((n + 255) / 256), 256, 0, st>>>(x, n, D, centres, n_comp, seed,
-                                                            row_offset));
+    TSOM_LAUNCH(k_synth_gmm<<<(unsigned)((n + 255) / 256), 256, 0, st>>>(
+        x, n, D, ldx ? ldx : D, centres, n_comp, seed, row_offset));
 }
 
 }  // namespace tsom

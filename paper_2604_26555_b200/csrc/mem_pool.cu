@@ -4,7 +4,9 @@
 
 #include <cstdint>
 #include <cstdlib>
+#include <map>
 #include <mutex>
+#include <utility>
 
 #include "engine.h"
 
@@ -127,6 +129,27 @@ void DevBuf::release(bool synced) {
     p = nullptr;
     bytes = 0;
     owned = true;
+}
+
+// Kernel attributes are per device (context): one cache entry per
+// (kernel, device), so a second engine on another GPU of the same process
+// sets them for its own device too.
+cudaError_t ensure_smem_attr(const void* func, size_t bytes, bool* newly_set) {
+    if (newly_set) *newly_set = false;
+    static std::mutex mu;
+    static std::map<std::pair<const void*, int>, size_t> done;
+    int dev = 0;
+    cudaError_t e = cudaGetDevice(&dev);
+    if (e != cudaSuccess) return e;
+    std::lock_guard<std::mutex> lk(mu);
+    size_t& have = done[{func, dev}];
+    if (have >= bytes) return cudaSuccess;
+    e = cudaFuncSetAttribute(func, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)bytes);
+    if (e == cudaSuccess) {
+        have = bytes;
+        if (newly_set) *newly_set = true;
+    }
+    return e;
 }
 
 }  // namespace tsom
