@@ -158,14 +158,17 @@ cudaEvent_t k1_event(Engine* eng, int end) {
     return eng->ev[8 + end];
 }
 
-// near-tie list passes: pcount[p] = clamp(count - p * cap, 0, cap)
+// near-tie list passes: pcount[p] = clamp(count - p * cap, 0, cap); the last
+// pass keeps the whole remainder (its slots past cap take the full re-scan)
 constexpr uint32_t kTiePasses = 4;
+constexpr uint32_t kTieCapDiv = 16;  // enumerate scratch: n / 16 rows (4 passes cover 25 %)
 __global__ void k_tie_pass_counts(const uint32_t* __restrict__ count, uint64_t cap,
                                   uint32_t passes, uint32_t* __restrict__ pcount) {
     const uint32_t p = threadIdx.x;
     if (p >= passes) return;
     const uint64_t c = *count, o = (uint64_t)p * cap;
-    pcount[p] = (uint32_t)(c <= o ? 0 : (c - o < cap ? c - o : cap));
+    const uint64_t rest = c <= o ? 0 : c - o;
+    pcount[p] = (uint32_t)(p + 1 == passes ? rest : (rest < cap ? rest : cap));
 }
 
 // K1 + exact re-check over rows `x` (selection `sel` of length n, or first n rows).
@@ -221,13 +224,14 @@ void run_bmu(Engine* eng, const float* x, uint32_t ldx, const uint32_t* sel, uin
         // stays on the device (kernels grid-stride over it), so the epoch needs
         // no host round trip; rows with > 8 candidates in a group get the full
         // exact re-scan.  A collapsed map (large sigma, early epochs) can put a
-        // large share of the rows in the window, so the list is worked through
-        // in up to kTiePasses passes of `cap` slots each: the enumerate scratch
-        // is bounded at ~n / kTiePasses rows, pass p reads its
-        // slot count (clamped to [0, cap]) on the device, and passes past the
-        // actual count exit at once.
+        // large share of the rows in the window (measured up to 18 %), so the
+        // list is worked through in kTiePasses passes of `cap` slots each: the
+        // enumerate scratch is bounded at n / 16 rows, pass p
+        // reads its slot count on the device, passes past the actual count
+        // exit at once, and slots past 4 cap (> 25 % of the rows) take the
+        // full exact re-scan.
         const uint32_t passes = n > (1u << 20) ? kTiePasses : 1u;
-        const uint64_t cap = (n + passes - 1) / passes;
+        const uint64_t cap = passes > 1 ? (n + kTieCapDiv - 1) / kTieCapDiv : n;
         const uint64_t mt = (cap + tsom::kTcTileM - 1) / tsom::kTcTileM;
         CU(eng->tsplit.ensure(mt * geo.tile_bytes));
         CU(eng->part2.ensure((size_t)groups * 4 * cap * sizeof(float)));
@@ -1137,6 +1141,7 @@ int tsom_bmu_bound(tsom_engine* eng, const uint32_t* selected, uint64_t n_sel, u
                                    eng->stream));
         }
         CU(cudaStreamSynchronize(eng->stream));
+        finish_recheck(eng);
     });
 }
 

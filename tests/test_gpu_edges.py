@@ -78,3 +78,31 @@ def test_simt_and_tc_agree_on_many_groups(pkg, oracle_port):
         outs.append(e.bmu(x)[0])
     bo, _ = oracle_port.find_bmus(x, w)
     assert (outs[0] == bo).all() and (outs[1] == bo).all()
+
+
+@pytest.mark.parametrize("dup_every", [2, 16])
+def test_near_tie_passes_and_overflow(pkg, oracle_port, dup_every):
+    """More rows than one near-tie pass holds (n > 2^20: the enumerate scratch
+    is n / 16 rows, 4 passes): with every node duplicated, every row is an
+    exact tie, so the 4 passes fill and the remaining 75 % of the rows take
+    the full exact re-scan.  Every BMU must still be the reference's
+    (ties to the lowest index, trainer.hpp:293-304), and U / H match."""
+    n, p, d = 1_200_000, 64, 50
+    x = oracle_port.synth_gmm(n, d, 2730)
+    base = x[np.linspace(0, n - 1, p // dup_every).astype(int)]
+    w = np.repeat(base, dup_every, axis=0).copy()
+    e = pkg.Engine(p, d)
+    e.bind(x)
+    e.set_codebook(w)
+    b, dist = e.bmu_bound(None, want_dist=True)
+    assert e.last_recheck_count > n // 2
+    bo, do = oracle_port.find_bmus(x, w)
+    assert (b == bo).all()
+    np.testing.assert_allclose(dist, do, rtol=1e-12)
+    infl = oracle_port.influence_from_dist(oracle_port.lattice_dist("rect", 8, 8), 2.0)
+    e.set_influence(infl)
+    u, h, _ = e.epoch(0.3)
+    sel = np.arange(n, dtype=np.uint32)
+    uo, ho, _, _, _ = oracle_port.run_iteration(x, sel, w, infl, 0.3, 1, 8)
+    assert np.max(np.abs(u - uo)) <= 1e-9 * np.max(np.abs(uo))
+    np.testing.assert_allclose(h, ho, rtol=1e-9)
