@@ -211,6 +211,14 @@ int tsom_sampler_select(tsom_engine* eng, uint32_t* sel_out, uint64_t* m_out);
 int tsom_sampler_observe(tsom_engine* eng, const double* dist);
 /* AdaptiveSamplerState (sampling.hpp:83-92): last_error (N f64) and age (N u32). */
 int tsom_sampler_state(tsom_engine* eng, double* last_error, uint32_t* age);
+/* The SURVEY.md §8(d) synthetic rows on the host (no GPU), value-identical to
+ * the reference's generator: Rng(seed, SeedStream::synth) (rng.hpp:21-37),
+ * n_comp x d centres real(-4, 4), then per row m = index(n_comp) and
+ * x_k = f32(mu[m][k] + gaussian()) (rng.hpp:64-76).  `threads` host threads
+ * (0 = all cores), each jumping the mt19937_64 stream to its first row.
+ * out: n x d row-major f32. */
+int tsom_synth_gmm_host(float* out, uint64_t n, uint32_t d, uint64_t seed, uint32_t n_comp,
+                        uint32_t threads);
 /* Host-only check of the jump-ahead (no GPU): 0 when the state jumped by `jump`
  * draws from mt19937_64(seed) equals sequential generation. */
 int tsom_mt_selftest(uint64_t seed, uint64_t jump);

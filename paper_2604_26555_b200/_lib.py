@@ -44,7 +44,7 @@ EXPORTS = [
     "tsom_sampler_init", "tsom_sampler_select", "tsom_sampler_observe", "tsom_sampler_state",
     "tsom_mt_selftest", "tsom_release_cached_memory", "tsom_train_epochs",
     "tsom_get_prev_update", "tsom_barrier_wait_s", "tsom_group_create", "tsom_group_join",
-    "tsom_group_destroy", "tsom_device_bytes",
+    "tsom_group_destroy", "tsom_device_bytes", "tsom_synth_gmm_host",
 ]
 
 SAMPLER_KINDS = {"full": 0, "random": 1, "adaptive": 2}  # SamplingKind, sampling.hpp:163
@@ -156,6 +156,7 @@ def load():
     L.tsom_bind_shards.argtypes = [_vp, C.POINTER(C.c_char_p), u32, u32]
     L.tsom_stream.argtypes = [_vp]
     L.tsom_stream.restype = _vp
+    L.tsom_synth_gmm_host.argtypes = [_vp, u64, u32, u64, u32, u32]
     L.tsom_device_bytes.argtypes = [_vp]
     L.tsom_device_bytes.restype = u64
     L.tsom_barrier_wait_s.argtypes = [_vp]
@@ -178,6 +179,20 @@ def release_cached_memory(device: int = 0) -> None:
     st = load().tsom_release_cached_memory(int(device))
     if st:
         raise RuntimeError(f"tsom_release_cached_memory failed ({st})")
+
+
+def synth_gmm_host(n: int, d: int = 50, seed: int = 2604, n_comp: int = 16,
+                   threads: int = 0, out=None) -> np.ndarray:
+    """The reference's Gaussian-mixture rows, generated on all
+    host cores (no GPU); value-identical to Rng(seed, synth) in sequence."""
+    L = load()
+    if out is None:
+        out = np.empty((n, d), np.float32)
+    assert out.shape == (n, d) and out.dtype == np.float32 and out.flags.c_contiguous
+    st = L.tsom_synth_gmm_host(out.ctypes.data if n else None, n, d, seed, n_comp, threads)
+    if st:
+        _raise(st, "tsom_synth_gmm_host: bad arguments")
+    return out
 
 
 def mt_selftest(seed: int, jump: int) -> int:
