@@ -109,6 +109,9 @@ int tsom_bind_device_data(tsom_engine* eng, const float* d_rows, uint64_t n_rows
 int tsom_bind_synthetic_gmm(tsom_engine* eng, uint64_t n_rows, uint64_t seed, uint32_t n_comp,
                             uint64_t row_offset);
 uint64_t tsom_rows(const tsom_engine* eng);
+/* Copy resident rows [row0, row0 + n) back to the host as n x d row-major
+ * f32 (DataSourceRef::fetch_rows of a contiguous range, dataset.hpp:393-399). */
+int tsom_get_rows(tsom_engine* eng, uint64_t row0, uint64_t n, float* out);
 
 /* Per-epoch state ---------------------------------------------------------- */
 
@@ -216,9 +219,10 @@ int tsom_sampler_state(tsom_engine* eng, double* last_error, uint32_t* age);
  * n_comp x d centres real(-4, 4), then per row m = index(n_comp) and
  * x_k = f32(mu[m][k] + gaussian()) (rng.hpp:64-76).  `threads` host threads
  * (0 = all cores), each jumping the mt19937_64 stream to its first row.
- * out: n x d row-major f32. */
-int tsom_synth_gmm_host(float* out, uint64_t n, uint32_t d, uint64_t seed, uint32_t n_comp,
-                        uint32_t threads);
+ * out: rows [row0, row0 + n) of the stream, n x d row-major f32 (a rank's
+ * contiguous share of a dataset generated once). */
+int tsom_synth_gmm_host(float* out, uint64_t row0, uint64_t n, uint32_t d, uint64_t seed,
+                        uint32_t n_comp, uint32_t threads);
 /* Host-only check of the jump-ahead (no GPU): 0 when the state jumped by `jump`
  * draws from mt19937_64(seed) equals sequential generation. */
 int tsom_mt_selftest(uint64_t seed, uint64_t jump);

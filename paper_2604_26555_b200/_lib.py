@@ -44,7 +44,7 @@ EXPORTS = [
     "tsom_sampler_init", "tsom_sampler_select", "tsom_sampler_observe", "tsom_sampler_state",
     "tsom_mt_selftest", "tsom_release_cached_memory", "tsom_train_epochs",
     "tsom_get_prev_update", "tsom_barrier_wait_s", "tsom_group_create", "tsom_group_join",
-    "tsom_group_destroy", "tsom_device_bytes", "tsom_synth_gmm_host",
+    "tsom_group_destroy", "tsom_device_bytes", "tsom_synth_gmm_host", "tsom_get_rows",
 ]
 
 SAMPLER_KINDS = {"full": 0, "random": 1, "adaptive": 2}  # SamplingKind, sampling.hpp:163
@@ -156,7 +156,8 @@ def load():
     L.tsom_bind_shards.argtypes = [_vp, C.POINTER(C.c_char_p), u32, u32]
     L.tsom_stream.argtypes = [_vp]
     L.tsom_stream.restype = _vp
-    L.tsom_synth_gmm_host.argtypes = [_vp, u64, u32, u64, u32, u32]
+    L.tsom_synth_gmm_host.argtypes = [_vp, u64, u64, u32, u64, u32, u32]
+    L.tsom_get_rows.argtypes = [_vp, u64, u64, _vp]
     L.tsom_device_bytes.argtypes = [_vp]
     L.tsom_device_bytes.restype = u64
     L.tsom_barrier_wait_s.argtypes = [_vp]
@@ -182,14 +183,15 @@ def release_cached_memory(device: int = 0) -> None:
 
 
 def synth_gmm_host(n: int, d: int = 50, seed: int = 2604, n_comp: int = 16,
-                   threads: int = 0, out=None) -> np.ndarray:
+                   threads: int = 0, out=None, row0: int = 0) -> np.ndarray:
     """The reference's Gaussian-mixture rows, generated on all
-    host cores (no GPU); value-identical to Rng(seed, synth) in sequence."""
+    host cores (no GPU); value-identical to Rng(seed, synth) in sequence.
+    row0: first row of the stream (a rank's slice of one dataset)."""
     L = load()
     if out is None:
         out = np.empty((n, d), np.float32)
     assert out.shape == (n, d) and out.dtype == np.float32 and out.flags.c_contiguous
-    st = L.tsom_synth_gmm_host(out.ctypes.data if n else None, n, d, seed, n_comp, threads)
+    st = L.tsom_synth_gmm_host(out.ctypes.data if n else None, row0, n, d, seed, n_comp, threads)
     if st:
         _raise(st, "tsom_synth_gmm_host: bad arguments")
     return out
@@ -269,6 +271,15 @@ class Engine:
     @property
     def rows(self) -> int:
         return int(self.L.tsom_rows(self.h))
+
+    def get_rows(self, row0: int = 0, n=None, out=None) -> np.ndarray:
+        """Resident rows [row0, row0 + n) back on the host (n x d f32)."""
+        n = self.rows - row0 if n is None else int(n)
+        if out is None:
+            out = np.empty((n, self.dims), np.float32)
+        assert out.shape == (n, self.dims) and out.dtype == np.float32 and out.flags.c_contiguous
+        self._check(self.L.tsom_get_rows(self.h, int(row0), n, _ptr(out) if n else None))
+        return out
 
     def set_codebook(self, w: np.ndarray):
         w = np.ascontiguousarray(w, np.float32)

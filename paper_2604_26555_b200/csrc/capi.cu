@@ -1012,6 +1012,21 @@ int tsom_bind_synthetic_gmm(tsom_engine* eng, uint64_t n_rows, uint64_t seed, ui
 
 uint64_t tsom_rows(const tsom_engine* eng) { return eng ? eng->n_rows : 0; }
 
+int tsom_get_rows(tsom_engine* eng, uint64_t row0, uint64_t n, float* out) {
+    return guarded(eng, [&] {
+        CU(cudaSetDevice(eng->device));
+        REQUIRE(!eng->streamed && eng->x.p, TSOM_ERR_INVALID, "get_rows: no resident rows bound");
+        REQUIRE(row0 + n <= eng->n_rows && row0 + n >= row0, TSOM_ERR_RANGE,
+                "fetch_rows: row index beyond data size");
+        REQUIRE(out || n == 0, TSOM_ERR_INVALID, "get_rows: null buffer");
+        if (n == 0) return;
+        const size_t rowb = (size_t)eng->D * sizeof(float), pitch = (size_t)eng->ldx * sizeof(float);
+        CU(cudaMemcpy2DAsync(out, rowb, eng->x.as<float>() + row0 * eng->ldx, pitch, rowb, n,
+                             cudaMemcpyDeviceToHost, eng->stream));
+        CU(cudaStreamSynchronize(eng->stream));
+    });
+}
+
 int tsom_set_codebook(tsom_engine* eng, const float* weights) {
     return guarded(eng, [&] {
         CU(cudaSetDevice(eng->device));

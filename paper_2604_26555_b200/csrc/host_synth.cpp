@@ -75,7 +75,8 @@ uint64_t synth_seed(uint64_t seed) {  // mix_seed(seed, SeedStream::synth = 4), 
     return z ^ (z >> 31);
 }
 
-// rows [r0, r1) from a generator positioned at row r0; false on a rejection
+// rows [r0, r1) (into out + r * d) from a generator positioned at row r0;
+// false on a rejection
 bool gen_rows(Draws& rg, const std::vector<double>& mu, float* out, uint64_t r0, uint64_t r1,
               uint32_t d, uint32_t n_comp) {
     const uint64_t un = n_comp, limit = UINT64_MAX - UINT64_MAX % un;
@@ -93,8 +94,8 @@ bool gen_rows(Draws& rg, const std::vector<double>& mu, float* out, uint64_t r0,
 }  // namespace
 }  // namespace tsom
 
-extern "C" int tsom_synth_gmm_host(float* out, uint64_t n, uint32_t d, uint64_t seed,
-                                   uint32_t n_comp, uint32_t threads) {
+extern "C" int tsom_synth_gmm_host(float* out, uint64_t row0, uint64_t n, uint32_t d,
+                                   uint64_t seed, uint32_t n_comp, uint32_t threads) {
     using namespace tsom;
     if ((!out && n) || d < 1 || n_comp < 1) return 1;  // TSOM_ERR_INVALID
     uint64_t window[312];
@@ -105,23 +106,27 @@ extern "C" int tsom_synth_gmm_host(float* out, uint64_t n, uint32_t d, uint64_t 
     if (threads == 0) threads = std::max(1u, std::thread::hardware_concurrency());
     const uint64_t min_rows = 65536;  // below this the jumps cost more than they save
     uint64_t T = std::min<uint64_t>(threads, std::max<uint64_t>(1, n / min_rows));
-    // the reference order, one generator (rejections redrawn as index() does)
+    if (row0 > 0) T = std::max<uint64_t>(T, 1);
+    // the reference order, one generator from row 0 (rejections redrawn as
+    // index() does); rows before row0 are drawn and dropped
     auto sequential = [&] {
         Draws rg(window);
         for (uint64_t i = 0; i < (uint64_t)n_comp * d; ++i) rg.real01();
         const uint64_t un = n_comp, limit = UINT64_MAX - UINT64_MAX % un;
-        for (uint64_t r = 0; r < n; ++r) {
+        for (uint64_t r = 0; r < row0 + n; ++r) {
             uint64_t x;
             do {
                 x = rg.g();
             } while (x >= limit);
             const size_t m = static_cast<size_t>(x % un);
-            for (uint32_t k = 0; k < d; ++k)
-                out[r * d + k] = static_cast<float>(mu[m * d + k] + rg.gaussian());
+            for (uint32_t k = 0; k < d; ++k) {
+                const double g = rg.gaussian();
+                if (r >= row0) out[(r - row0) * d + k] = static_cast<float>(mu[m * d + k] + g);
+            }
         }
         return 0;
     };
-    if (T <= 1) return sequential();
+    if (T <= 1 && row0 == 0) return sequential();
     // untempered words from the seed window, the input of every jump
     std::vector<uint64_t> seq(mt::kSeq + 1);
     mt::extend(window, seq.size() - 312, seq.data());
@@ -130,7 +135,8 @@ extern "C" int tsom_synth_gmm_host(float* out, uint64_t n, uint32_t d, uint64_t 
     std::vector<std::thread> pool;
     for (uint64_t t = 0; t < T; ++t)
         pool.emplace_back([&, t] {
-            const uint64_t r0 = std::min(n, t * per), r1 = std::min(n, r0 + per);
+            // rows [r0, r1) of the stream, written from out[(r0 - row0) * d]
+            const uint64_t r0 = row0 + std::min(n, t * per), r1 = row0 + std::min(n, t * per + per);
             if (r0 >= r1) return;
             // a pending cached gaussian at row r0 (r0 d odd) is the second half
             // of the pair drawn just before its index draw: start 2 draws early
@@ -143,7 +149,7 @@ extern "C" int tsom_synth_gmm_host(float* out, uint64_t n, uint32_t d, uint64_t 
                 rg.has_cached = false;
                 rg.gaussian();  // recompute the pair; its sin half is now cached
             }
-            ok[t] = gen_rows(rg, mu, out, r0, r1, d, n_comp);
+            ok[t] = gen_rows(rg, mu, out - row0 * d, r0, r1, d, n_comp);
         });
     for (auto& th : pool) th.join();
     for (char o : ok)

@@ -22,6 +22,15 @@ def test_host_synth_matches_reference_generator(oracle_port, n, d, seed, n_comp,
     assert np.array_equal(got.view(np.uint32), np.asarray(want, np.float32).view(np.uint32))
 
 
+@pytest.mark.parametrize("d", [50, 7])
+def test_host_synth_row_slices(oracle_port, d):
+    """A rank's slice [row0, row0 + n) equals the same rows of the whole set."""
+    whole = _lib.synth_gmm_host(300_000, d, 77, 16, 8)
+    for row0, n in [(0, 1000), (123_457, 100_000), (299_999, 1), (150_000, 150_000)]:
+        part = _lib.synth_gmm_host(n, d, 77, 16, 8, row0=row0)
+        assert np.array_equal(part, whole[row0:row0 + n])
+
+
 def test_host_synth_rejects_bad_arguments():
     with pytest.raises(_lib.InvalidArgument):
         _lib.synth_gmm_host(10, 0)
