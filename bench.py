@@ -621,7 +621,7 @@ def leg_c4(args, ctx):
     e.set_codebook(w0)
     m = max(1, int(np.floor(n_total * rho)))
     e.sampler_init("adaptive", m, seed)
-    graph_epochs(e, "rng", 2)  # warm-up
+    graph_epochs(e, "rng", 2, sampled=True)  # warm-up (allocations of the sampled epochs)
     e.set_codebook(w0)
     e.sampler_init("adaptive", m, seed)
     secs, _ = timed(lambda: graph_epochs(e, "rng", epochs, sampled=True), ctx, e)
@@ -633,6 +633,7 @@ def leg_c4(args, ctx):
         rechecks.append(e.last_recheck_count)
     s, c = e.qe()
     dev_bytes, used = e.device_bytes, hbm_used_gb(local)
+    refresh_s, _ = timed(lambda: e.refresh_topology("rng"), ctx, e)
     close_engine(e)
     pk, _ = peaks()
     k1 = statistics.mean(p["k1_ms"] for p in phases)
@@ -646,6 +647,7 @@ def leg_c4(args, ctx):
            "rows_considered_per_s": n_total * epochs / secs, "ms_per_epoch": secs * 1e3 / epochs,
            "phase_ms": {k: round(statistics.mean(p[k] for p in phases), 3) for k in phases[0]},
            "rechecked_rows_per_epoch": statistics.mean(rechecks), "qe_after": s / c,
+           "refresh_ms": refresh_s * 1e3,
            "roofline": {"bound": "tensor", "kernel": "k1 BMU (" + kname + ") over the selected rows",
                         "achieved": 2.0 * P * D * m_rank / (k1 / 1e3) / 1e12, "peak": peak,
                         "unit": "TFLOP/s",
@@ -679,7 +681,9 @@ def leg_c3(args, ctx):
         e.set_codebook(w0)
         secs, marks = timed(lambda: graph_epochs(e, "mst", epochs), ctx, e)
         s, c = e.qe()
+        rs, _ = timed(lambda: e.refresh_topology("mst"), ctx, e)
         return secs, {"ms_per_epoch": secs * 1e3 / epochs, "refresh_epochs": marks,
+                      "refresh_ms": rs * 1e3,
                       "qe_after": s / c, "engine_bytes": e.device_bytes,
                       "device_used_gb": hbm_used_gb(local)}
 
