@@ -1739,6 +1739,11 @@ int tsom_train_epochs(tsom_engine* eng, uint32_t n_epochs, const double* eta,
 
 uint64_t tsom_last_recheck_count(const tsom_engine* eng) { return eng ? eng->last_recheck : 0; }
 
+// diagnostics only (not in the public header): the device buffer (bound rows x
+// groups * group width floats) K1's main pass writes its raw values into
+// while option 99 bit 7 is set
+int tsom_debug_k1_dump(float* d_buf) { return tsom::k1_set_dump(d_buf); }
+
 // diagnostics only (not in the public header): K1 timestamps of CTA 0
 int tsom_debug_k1_trace(unsigned long long* out, uint32_t n) {
     return tsom::k1_trace_copy(out, n);

@@ -376,7 +376,8 @@ cudaError_t launch_bmu_tc(int kind, const void* tiles, uint64_t n, const uint32_
 extern uint32_t g_k1_debug;
 extern int g_split_v1;
 extern int g_gather_kind;
-int k1_trace_copy(unsigned long long* out, uint32_t n);  // diagnostics  // diagnostics: bit0 skip epilogue math, bit1 skip MMAs
+int k1_trace_copy(unsigned long long* out, uint32_t n);
+int k1_set_dump(float* d_buf);  // diagnostics: option 99 bit 7 target (rows x groups*gn floats)  // diagnostics  // diagnostics: bit0 skip epilogue math, bit1 skip MMAs
 // main-pass merge: bmu for rows with a clear winner, near-tie positions -> ties
 constexpr uint32_t kTcEpiSets = 2;  // K1 main pass: partial results per group (sub-groups)
 void launch_merge_fast(const float* part, uint64_t n, uint32_t groups, uint32_t sets, uint32_t gn,

@@ -70,6 +70,10 @@ __device__ __forceinline__ float fmin3f(float a, float b, float c) {
 
 // diagnostics (option 99 bit 5): CTA 0 timestamps [tile][8] (clock64)
 __device__ unsigned long long g_k1_trace[512 * 8];
+// diagnostics (option 99 bit 7): every raw main-pass value v[row][group * gn + col]
+// (scaled units) to this buffer, to measure the split-product error against
+// the window (scripts/k1_window_error.py)
+__device__ float* g_k1_dump = nullptr;
 #define TSOM_TRACE(slot_, it_)                                                       \
     do {                                                                              \
         if (!kEnum && (dbg & 32u) && blockIdx.x == 0 && (it_) < 512u)                        \
@@ -737,6 +741,14 @@ __global__ void __launch_bounds__(EpiCfg<kKind>::kThreads, 1)
                 tc_fence_before();
                 __syncwarp();
                 if (lane == 0) mbar_arrive(&tempty_bar[acc]);  // warp done with the accumulator
+                if ((dbg & 128u) && pos < n) {
+                    float* dp = g_k1_dump + pos * (uint64_t)(groups * gn) + g * gn + c_begin * 32;
+#pragma unroll
+                    for (int c = 0; c < kCPS; ++c)
+                        if ((uint32_t)c < c_count)
+#pragma unroll
+                            for (int k = 0; k < 32; ++k) dp[c * 32 + k] = __uint_as_float(r[c][k]);
+                }
                 float mn[4] = {CUDART_INF_F, CUDART_INF_F, CUDART_INF_F, CUDART_INF_F};
 #define TSOM_PASS1(r, cb)                                                                   \
     _Pragma("unroll") for (int m = 0; m < 16; ++m) mn[m & 3] =                             \
@@ -876,6 +888,10 @@ __global__ void __launch_bounds__(EpiCfg<kKind>::kThreads, 1)
 // bit2 the A-tile loads, so the stages can be timed in isolation; bit5 traces
 // CTA 0; bit6 enables the cluster multicast of A tiles
 uint32_t g_k1_debug = 0;
+
+int k1_set_dump(float* d_buf) {
+    return cudaMemcpyToSymbol(g_k1_dump, &d_buf, sizeof(d_buf)) == cudaSuccess ? 0 : 4;
+}
 
 int k1_trace_copy(unsigned long long* out, uint32_t n) {
     return cudaMemcpyFromSymbol(out, g_k1_trace, (n < 4096u ? n : 4096u) * 8) == cudaSuccess ? 0

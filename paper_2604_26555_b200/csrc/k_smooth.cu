@@ -26,23 +26,45 @@ __global__ void k_build_saug(const double* __restrict__ sums, const float* __res
     saug[e] = k < D ? sums[(size_t)b * D + k] : c;
 }
 
-// H_j = sum_b infl[b][j] c_b: block = 32 nodes x 8 b-slices, fixed-order fold
+// H_j = sum_b infl[b][j] c_b: block = 32 nodes x 8 b-slices, fixed-order fold.
+// Two values per node:
+//   Hx[j] — in FP64, the denominator's exact value, for U's  - w_j H_j  term;
+//   H[j]  — the reference's H: every term h[b][j] is quantised to the 2^-40
+//           grid (quantize_term, accum.hpp:34-38) and the c_b copies of it are
+//           summed exactly, H = (double)(sum_b c_b llrint(h 2^40)) 2^-40
+//           (dequantize, accum.hpp:40-42): bit-identical to the reference,
+//           so its H < 1e-12 freeze rule (trainer.hpp:350) fires on the same
+//           nodes (terms below 2^-41 vanish there too).
 __global__ void __launch_bounds__(256) k_smooth_den(const double* __restrict__ infl,
                                                     const double* __restrict__ sums, uint32_t P,
-                                                    uint32_t D, double* __restrict__ H) {
+                                                    uint32_t D, double* __restrict__ H,
+                                                    double* __restrict__ Hx) {
     __shared__ double part[8][33];
+    __shared__ __int128 qpart[8][33];
     const uint32_t tj = threadIdx.x & 31, sl = threadIdx.x >> 5;
     const uint32_t j = blockIdx.x * 32 + tj;
     const double* c = sums + (size_t)P * D;
     double acc = 0.0;
+    __int128 qacc = 0;
     if (j < P)
-        for (uint32_t b = sl; b < P; b += 8) acc = fma(infl[(size_t)b * P + j], c[b], acc);
+        for (uint32_t b = sl; b < P; b += 8) {
+            const double h = infl[(size_t)b * P + j];
+            acc = fma(h, c[b], acc);
+            const long long q = __double2ll_rn(h * 1099511627776.0);  // llrint(h 2^40)
+            qacc += (__int128)q * (__int128)(unsigned long long)c[b];
+        }
     part[sl][tj] = acc;
+    qpart[sl][tj] = qacc;
     __syncthreads();
     if (sl == 0 && j < P) {
         double v = 0.0;
-        for (int k = 0; k < 8; ++k) v += part[k][tj];
-        H[j] = v;
+        __int128 qv = 0;
+        for (int k = 0; k < 8; ++k) {
+            v += part[k][tj];
+            qv += qpart[k][tj];
+        }
+        Hx[j] = v;
+        H[j] = (double)qv * (1.0 / 1099511627776.0);
     }
 }
 
@@ -90,7 +112,7 @@ __global__ void __launch_bounds__(256) k_smooth_gemm(const double* __restrict__ 
     }
 }
 
-// U = eta * (sum_z partial[z] - w * H), fixed slice order (deterministic)
+// U = eta * (sum_z partial[z] - w * Hx), fixed slice order (deterministic)
 __global__ void k_smooth_finish(const double* __restrict__ partial, const float* __restrict__ w,
                                 const double* __restrict__ H, uint32_t P, uint32_t D, double eta,
                                 double* __restrict__ U) {
@@ -103,21 +125,22 @@ __global__ void k_smooth_finish(const double* __restrict__ partial, const float*
 
 void launch_smooth(const double* infl, const double* sums, const float* w, uint32_t P, uint32_t D,
                    double eta, double* U, double* H, double* scratch, cudaStream_t st) {
-    // scratch: P*(d+1) (saug) + SM_SPLIT*P*d (slice partials) doubles
+    // scratch: P*(d+1) (saug) + SM_SPLIT*P*d (slice partials) + P (Hx) doubles
     double* saug = scratch;
     double* partial = scratch + (size_t)P * (D + 1);
+    double* Hx = partial + (size_t)SM_SPLIT * P * D;
     const size_t n = (size_t)P * (D + 1);
     TSOM_LAUNCH(k_build_saug<<<(unsigned)((n + 255) / 256), 256, 0, st>>>(sums, w, P, D, saug));
-    TSOM_LAUNCH(k_smooth_den<<<(P + 31) / 32, 256, 0, st>>>(infl, sums, P, D, H));
+    TSOM_LAUNCH(k_smooth_den<<<(P + 31) / 32, 256, 0, st>>>(infl, sums, P, D, H, Hx));
     dim3 grid((P + SM_TJ - 1) / SM_TJ, (D + SM_KC - 1) / SM_KC, SM_SPLIT);
     TSOM_LAUNCH(k_smooth_gemm<<<grid, 256, 0, st>>>(infl, saug, P, D, partial));
     const size_t pd = (size_t)P * D;
-    TSOM_LAUNCH(k_smooth_finish<<<(unsigned)((pd + 255) / 256), 256, 0, st>>>(partial, w, H, P, D,
-                                                                            eta, U));
+    TSOM_LAUNCH(k_smooth_finish<<<(unsigned)((pd + 255) / 256), 256, 0, st>>>(partial, w, Hx, P,
+                                                                            D, eta, U));
 }
 
 size_t smooth_scratch_doubles(uint32_t P, uint32_t D) {
-    return (size_t)P * (D + 1) + (size_t)SM_SPLIT * P * D;
+    return (size_t)P * (D + 1) + (size_t)SM_SPLIT * P * D + P;
 }
 
 // apply_update (trainer.hpp:341-369): H < 1e-12 → node frozen (momentum memory

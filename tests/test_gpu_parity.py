@@ -284,6 +284,16 @@ def test_resident_training_config1_shape(pkg, oracle_port):
     np.testing.assert_allclose(qe, g["qe"], rtol=1e-5)
 
 
+def gpu_qe(pkg, x, w):
+    """quantization_error (metrics.hpp:28-30) of codebook w on rows x, on the GPU."""
+    e = pkg.Engine(w.shape[0], w.shape[1])
+    e.bind(x)
+    e.set_codebook(w)
+    s, c = e.qe()
+    e.close()
+    return s / c
+
+
 DROPIN_CONFIGS = [
     dict(topology="hex", grid_w=4, grid_h=4, n_iters=8, seed=17),
     dict(topology="mst", nodes=16, n_iters=8, seed=17),
@@ -304,7 +314,10 @@ def test_dropin_train_vs_golden(pkg, kw):
     cfg = dropin.TrainConfig(**kw)
     w, qe, _, _ = dropin.train_cuda(cfg, g["x"], log_qe=True)
     assert rel_maxnorm(w, g[f"w{i}"]) <= 1e-4
+    # the per-epoch QE above is the reference loop's own (host) mean_bmu_distance
+    # (trainer.hpp:518); the trained codebook's QE on the GPU (tsom_qe):
     np.testing.assert_allclose(qe, g[f"qe{i}"], rtol=1e-5)
+    np.testing.assert_allclose(gpu_qe(pkg, g["x"], w), g[f"qe{i}"][-1], rtol=1e-5)
 
 
 def test_dropin_config1_run(pkg, oracle_port):
@@ -318,6 +331,7 @@ def test_dropin_config1_run(pkg, oracle_port):
     w, qe, _, _ = dropin.train_cuda(cfg, x, log_qe=True)
     assert rel_maxnorm(w, g["w"]) <= 1e-4
     np.testing.assert_allclose(qe, g["qe"], rtol=1e-5)
+    np.testing.assert_allclose(gpu_qe(pkg, x, w), g["qe"][-1], rtol=1e-5)
 
 
 # --- BASELINE-size properties (1e7 x 50, K = 1024) --------------------------
@@ -341,8 +355,14 @@ def test_full_size_properties(pkg, oracle_port):
     b, _ = e.bmu_bound(None, want_dist=False)
     counts = np.bincount(b, minlength=p).astype(np.float64)
     assert counts.sum() == n
-    np.testing.assert_allclose(h, infl.T @ counts, rtol=1e-12)
-    np.testing.assert_allclose(h.sum(), (infl.sum(1) * counts).sum(), rtol=1e-12)
+    np.testing.assert_allclose(h, infl.T @ counts, rtol=1e-9)
+    np.testing.assert_allclose(h.sum(), (infl.sum(1) * counts).sum(), rtol=1e-9)
+    # and H is the reference's quantised sum exactly: every term h[b][j] on the
+    # 2^-40 grid (accum.hpp:34-42), c_b copies of it, summed in integers
+    q = np.rint(infl * 2.0**40).astype(np.int64).astype(object)
+    cb = counts.astype(np.int64).astype(object)
+    hq = np.array([float(sum(cb[i] * q[i, j] for i in range(p) if cb[i])) for j in range(p)])
+    assert np.array_equal(h, hq / 2.0**40)
 
 
 def test_nccl_world1_allreduce_path(pkg, oracle_port):
@@ -647,3 +667,30 @@ def test_train_device_streamed_equals_resident(pkg):
     w_str, _, ref_str, _ = dropin.train_device(cfg, g["x"], streamed=True)
     assert np.array_equal(ref_res, ref_str)
     assert rel_maxnorm(w_str, w_res.astype(np.float64)) <= 1e-6
+
+
+@pytest.mark.parametrize("sampling", ["full", "random"])
+def test_h_bit_identical_to_reference(pkg, oracle_port, sampling):
+    """H is the reference's exactly: each term h[b][j] quantised to the 2^-40
+    grid (quantize_term, accum.hpp:34-38), c_b copies summed in integers,
+    dequantised once (accum.hpp:40-42) — so the H < 1e-12 freeze rule of
+    apply_update (trainer.hpp:350) fires on the same nodes, including nodes
+    whose every influence term is below 2^-41 (sigma at its 0.3 floor)."""
+    n, p = 30000, 256
+    x = oracle_port.synth_gmm(n, 50, 2740)
+    w = x[np.linspace(0, n - 1, p).astype(int)].copy()
+    dist = oracle_port.lattice_dist("hex", 16, 16)
+    sel = None if sampling == "full" else np.sort(
+        np.random.default_rng(1).choice(n, 7000, replace=False)).astype(np.uint32)
+    ids = np.arange(n, dtype=np.uint32) if sel is None else sel
+    for sigma in (4.0, 0.3):
+        infl = oracle_port.influence_from_dist(dist, sigma)
+        e = pkg.Engine(p, 50)
+        e.bind(x)
+        e.set_codebook(w)
+        e.set_influence(infl)
+        u, h, _ = e.epoch(0.4, sel)
+        uo, ho, _, _, _ = oracle_port.run_iteration(x, ids, w, infl, 0.4, 1, 4)
+        assert np.array_equal(h, ho), f"sigma {sigma}: {np.sum(h != ho)} H values differ"
+        assert np.array_equal(h < 1e-12, ho < 1e-12)
+        assert np.max(np.abs(u - uo)) <= 1e-9 * np.max(np.abs(uo))

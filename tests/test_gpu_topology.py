@@ -47,6 +47,36 @@ def test_gram_graphs_hops_bit_exact(pkg, oracle_port, name, w):
         assert (hops == oracle_port.hop_distances(eref, P)).all(), kind
 
 
+def k1024_codebooks():
+    yield "gmm", oracle.port.synth_gmm(1024, 50, 2651)
+    # a 32 x 32 integer grid in 2 of 50 dims: massive exact distance ties
+    g = np.stack(np.meshgrid(np.arange(32), np.arange(32)), -1).reshape(-1, 2).astype(np.float32)
+    yield "grid", np.concatenate([g, np.zeros((1024, 48), np.float32)], 1)
+    # a trained-looking codebook: GMM rows pulled towards their component centres
+    x = oracle.port.synth_gmm(1024, 50, 2652)
+    c = oracle.port.synth_gmm(16, 50, 2652)
+    yield "clustered", (0.9 * c[np.arange(1024) % 16] + 0.1 * x).astype(np.float32)
+
+
+@pytest.mark.parametrize("name,w", list(k1024_codebooks()),
+                         ids=lambda v: v if isinstance(v, str) else "")
+def test_graphs_bit_exact_k1024(pkg, oracle_port, name, w):
+    """The BASELINE topology size (1024 nodes): Gram, MST and RNG edge lists and
+    hop counts bit-identical to the reference's (topology.hpp:81-325)."""
+    import oracle as orc
+    chk = orc.ref if orc.ref.available else oracle_port
+    e = pkg.Engine(1024, 50)
+    e.set_codebook(w)
+    sq = e.pairwise_sq_dists()
+    sq_ref = chk.pairwise_sq_dists(w)
+    assert (sq == sq_ref).all()
+    for kind in ("mst", "rng"):
+        edges, hops = e.refresh_topology(kind, want_hops=True)
+        eref = chk.build_graph(kind, sq_ref)
+        assert edges.shape == eref.shape and (edges == eref).all(), kind
+        assert (hops == chk.hop_distances(eref, 1024)).all(), kind
+
+
 def test_refresh_timing_k1024(pkg, oracle_port):
     w = oracle_port.synth_gmm(1024, 50, 2651)
     e = pkg.Engine(1024, 50)
