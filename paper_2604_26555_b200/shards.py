@@ -23,7 +23,7 @@ def write_one_shard(path: str, rows: np.ndarray) -> None:
     rows = np.ascontiguousarray(rows, np.float32)
     with open(path, "wb") as f:
         f.write(HEADER.pack(MAGIC, VERSION, rows.shape[0], rows.shape[1]))
-        f.write(memoryview(rows).cast("B"))  # no host copy of the rows
+        rows.tofile(f)  # no host copy of the rows
 
 
 def write_shards(data: np.ndarray, out_dir: str, n_shards: int) -> list[str]:
