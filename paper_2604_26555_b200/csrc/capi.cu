@@ -435,6 +435,10 @@ void accumulate_epoch(Engine* eng, const uint32_t* sel_host, uint64_t n_sel, boo
         }
         run_bmu(eng, eng->x.as<float>(), eng->ldx, dsel, n, eng->x2max.as<float>(), tiles,
                 tiles_xn2);
+        eng->pass_x = eng->x.as<float>();
+        eng->pass_ldx = eng->ldx;
+        eng->pass_sel = dsel;
+        eng->pass_n = n;
         CU(cudaEventRecord(eng->ev[1], eng->stream));
         ensure_accum(eng, n);
         tsom::launch_accumulate(eng->x.as<float>(), dsel, n, eng->D, eng->w.as<float>(), eng->P,
@@ -451,6 +455,9 @@ void accumulate_epoch(Engine* eng, const uint32_t* sel_host, uint64_t n_sel, boo
     } else {
         // Streamed: rows live in host memory; chunks of stream_chunk_rows rows
         // are copied on copy_stream into two device stages, compute on stream.
+        eng->pass_x = nullptr;
+        eng->pass_sel = nullptr;
+        eng->pass_n = 0;
         const uint64_t C = eng->stream_chunk_rows;
         CU(eng->stage[0].ensure(C * eng->D * sizeof(float) + tsom::kRowSlack));
         CU(eng->stage[1].ensure(C * eng->D * sizeof(float) + tsom::kRowSlack));
@@ -606,24 +613,37 @@ void wait_stream(Engine* eng) {
     eng->red_pending = 0;
 }
 
-// Guard of quantize_term (accum.hpp:34-38): every term eta*h*(x - w) must stay
-// below 2^22.  Conservative bound |eta*h*(x - w)| <= eta*max|h|*(max||x|| + max||w||),
-// evaluated after the pass (streamed mode learns max||x|| while streaming).
-// the term guard's inputs, read back with the epoch's other status words
+// Guard of quantize_term (accum.hpp:34-38) for the last accumulation pass,
+// with the epoch's (pre-update) codebook: exact on resident rows (k_guard.cu:
+// a cheap bound, and only when it fails the per-node extremes test);
+// streamed rows are not kept, so there the bound decides alone.
+// dead (optional): the multi-epoch failure record, set before the update.
+uint32_t enqueue_term_guard(Engine* eng, double eta, int* dead = nullptr, uint32_t epoch = 0) {
+    const size_t words = tsom::guard_scratch_words(eng->P, eng->D);
+    if (eng->guard_buf.bytes < words * sizeof(uint32_t)) {
+        CU(eng->guard_buf.ensure(words * sizeof(uint32_t)));
+        CU(cudaMemsetAsync(eng->guard_buf.p, 0, words * sizeof(uint32_t), eng->stream));
+    }
+    const uint32_t tag = ++eng->guard_tag ? eng->guard_tag : ++eng->guard_tag;  // never 0
+    tsom::launch_term_guard(eng->pass_x, eng->pass_ldx, eng->pass_sel, eng->pass_n,
+                            eng->bmu.as<uint32_t>(), eng->w.as<float>(), eng->infl.as<double>(),
+                            eng->P, eng->D, eta, eng->x2max.as<float>(), eng->w2max.as<float>(),
+                            eng->hmax.as<double>(), tag,
+                            tsom::guard_scratch(eng->guard_buf.as<uint32_t>(), eng->P, eng->D),
+                            eng->sm_count, eng->stream, dead, epoch);
+    CU(cudaGetLastError());
+    return tag;
+}
+
+// the guard's verdict, read back with the epoch's other status words
 void enqueue_guard_read(Engine* eng) {
-    CU(cudaMemcpyAsync(eng->hstat + 3, eng->x2max.p, sizeof(float), cudaMemcpyDeviceToHost,
-                       eng->stream));
-    CU(cudaMemcpyAsync(eng->hstat + 4, eng->w2max.p, sizeof(float), cudaMemcpyDeviceToHost,
-                       eng->stream));
+    CU(cudaMemcpyAsync(eng->hstat + 3, eng->guard_buf.as<uint32_t>() + 1, sizeof(uint32_t),
+                       cudaMemcpyDeviceToHost, eng->stream));
 }
 
 // after the end-of-epoch synchronisation
-void check_term_guard(Engine* eng, double eta) {
-    float hx[2];
-    std::memcpy(hx, eng->hstat + 3, sizeof(hx));
-    const double bound =
-        std::fabs(eta) * eng->max_h * (std::sqrt((double)hx[0]) + std::sqrt((double)hx[1]));
-    REQUIRE(eng->max_h < 4194304.0 && bound < 4194304.0, TSOM_ERR_NUMERICAL,
+void check_term_guard(Engine* eng, uint32_t tag) {
+    REQUIRE(eng->hstat[3] != tag, TSOM_ERR_NUMERICAL,
             "numerical fault: accumulation term out of range (|term| >= 2^22)");
 }
 
@@ -672,7 +692,7 @@ std::vector<DevBuf*> all_buffers(Engine* eng) {
                       &eng->topo_buf[4], &eng->topo_buf[5], &eng->topo_buf[6], &eng->topo_buf[7],
                       &eng->topo_buf[8], &eng->topo_buf[9], &eng->topo_buf[10], &eng->topo_buf[11],
                       &eng->topo_buf[12], &eng->topo_buf[13], &eng->topo_buf[14], &eng->U, &eng->H, &eng->status, &eng->smooth_scratch,
-                      &eng->stage[0], &eng->stage[1], &eng->dead});
+                      &eng->stage[0], &eng->stage[1], &eng->dead, &eng->hmax, &eng->guard_buf});
 }
 
 }  // namespace
@@ -725,6 +745,8 @@ int tsom_create(int device, uint32_t nodes, uint32_t dims, tsom_engine** out) {
         CU(eng->U.ensure(P * D * sizeof(double)));
         CU(eng->H.ensure(P * sizeof(double)));
         CU(eng->status.ensure(8 * sizeof(int)));
+        CU(eng->hmax.ensure(sizeof(double)));
+        CU(cudaMemsetAsync(eng->hmax.p, 0, sizeof(double), eng->stream));
         CU(cudaMallocHost(&eng->hstat, 32 * sizeof(uint32_t)));
         std::memset(eng->hstat, 0, 32 * sizeof(uint32_t));
         ensure_rows(eng, 1);
@@ -1066,11 +1088,10 @@ int tsom_set_influence(tsom_engine* eng, const double* influence, int64_t key) {
         REQUIRE(influence, TSOM_ERR_INVALID, "set_influence: null matrix");
         if (key >= 0 && eng->infl_set && key == eng->infl_key) return;
         const size_t n = (size_t)eng->P * eng->P;
-        double mh = 0.0;
-        for (size_t i = 0; i < n; ++i) mh = std::max(mh, std::fabs(influence[i]));
-        eng->max_h = mh;
         CU(cudaMemcpyAsync(eng->infl.p, influence, n * sizeof(double), cudaMemcpyHostToDevice,
                            eng->stream));
+        tsom::launch_infl_absmax(eng->infl.as<double>(), n, eng->hmax.as<double>(), eng->stream);
+        CU(cudaGetLastError());
         CU(cudaStreamSynchronize(eng->stream));
         eng->infl_key = key;
         eng->infl_set = true;
@@ -1087,6 +1108,7 @@ int tsom_epoch(tsom_engine* eng, const uint32_t* selected, uint64_t n_sel, doubl
         prep_codebook(eng);
         accumulate_epoch(eng, selected, n_sel, dist_out != nullptr, false, true);
         smooth(eng, eta);
+        const uint32_t tag = enqueue_term_guard(eng, eta);
         const size_t P = eng->P, D = eng->D;
         if (u_out)
             CU(cudaMemcpyAsync(u_out, eng->U.p, P * D * sizeof(double), cudaMemcpyDeviceToHost,
@@ -1102,7 +1124,7 @@ int tsom_epoch(tsom_engine* eng, const uint32_t* selected, uint64_t n_sel, doubl
         wait_stream(eng);
         finish_recheck(eng);
         record_timing(eng);
-        if (n) check_term_guard(eng, eta);
+        if (n) check_term_guard(eng, tag);
     });
 }
 
@@ -1595,7 +1617,7 @@ int tsom_release_cached_memory(int device) {
 // One device-resident epoch (tsom_train_epoch), enqueued on the engine stream
 // without waiting for it; dead (optional): the multi-epoch failure record.
 static void train_epoch_enqueue(Engine* eng, double eta, double sigma, double momentum, uint32_t flags,
-                         const int* dead) {
+                         int* dead, uint32_t epoch) {
     CU(cudaSetDevice(eng->device));
     REQUIRE(eng->topo_set, TSOM_ERR_INVALID, "train_epoch: topology distance not set");
     REQUIRE(sigma > 0.0, TSOM_ERR_INVALID, "influence_matrix: sigma must be > 0");
@@ -1607,10 +1629,11 @@ static void train_epoch_enqueue(Engine* eng, double eta, double sigma, double mo
         const double inv = 1.0 / (2.0 * sigma * sigma);
         tsom::launch_influence(eng->topo_dist.as<double>(), (size_t)eng->P * eng->P, inv,
                                eng->infl.as<double>(), eng->stream);
+        tsom::launch_infl_absmax(eng->infl.as<double>(), (size_t)eng->P * eng->P,
+                                 eng->hmax.as<double>(), eng->stream);
         CU(cudaGetLastError());
         eng->infl_key = key;
         eng->infl_set = true;
-        eng->max_h = 1.0;
     }
     prep_codebook(eng);
     // flags bit 1: the device sampler picks this epoch's rows (select ->
@@ -1646,6 +1669,10 @@ static void train_epoch_enqueue(Engine* eng, double eta, double sigma, double mo
                               eng->dist.as<double>(), eng->sm_count, eng->stream);
     }
     smooth(eng, eta);
+    // the term guard on this epoch's rows and codebook; a violation records
+    // the failure before the update, which then leaves the weights as they
+    // were (the reference throws out of run_iteration, trainer.hpp:506)
+    eng->last_guard_tag = enqueue_term_guard(eng, eta, dead, epoch);
     tsom::launch_status_reset(eng->status.as<int>(), eng->stream);
     tsom::launch_apply_update_guarded(eng->w.as<float>(), eng->prev.as<float>(), eng->P,
                                       eng->D, eng->U.as<double>(), eng->H.as<double>(),
@@ -1660,7 +1687,10 @@ static void train_epoch_enqueue(Engine* eng, double eta, double sigma, double mo
 
 int tsom_train_epoch(tsom_engine* eng, double eta, double sigma, double momentum, uint32_t flags) {
     return guarded(eng, [&] {
-        train_epoch_enqueue(eng, eta, sigma, momentum, flags, nullptr);
+        CU(cudaSetDevice(eng->device));
+        CU(eng->dead.ensure(4 * sizeof(int)));
+        CU(cudaMemsetAsync(eng->dead.p, 0, 4 * sizeof(int), eng->stream));
+        train_epoch_enqueue(eng, eta, sigma, momentum, flags, eng->dead.as<int>(), 0);
         CU(cudaMemcpyAsync(eng->hstat + 2, eng->status.p, sizeof(int), cudaMemcpyDeviceToHost,
                            eng->stream));
         enqueue_guard_read(eng);
@@ -1669,7 +1699,7 @@ int tsom_train_epoch(tsom_engine* eng, double eta, double sigma, double momentum
         std::memcpy(&st, eng->hstat + 2, sizeof(int));
         finish_recheck(eng);
         record_timing(eng);
-        check_term_guard(eng, eta);
+        check_term_guard(eng, eng->last_guard_tag);  // the update was skipped
         REQUIRE(st == INT_MAX, TSOM_ERR_NUMERICAL,
                 "numerical fault: non-finite weight update at node " + std::to_string(st));
     });
@@ -1698,10 +1728,8 @@ int tsom_train_epochs(tsom_engine* eng, uint32_t n_epochs, const double* eta,
         for (uint32_t t = 0; t < n_epochs; ++t) {
             eng->k1_slot = (int)t;
             eng->k1_timed = false;
-            train_epoch_enqueue(eng, eta[t], sigma[t], momentum, flags, dead);
-            tsom::launch_epoch_guard(eng->status.as<int>(), eng->x2max.as<float>(),
-                                     eng->w2max.as<float>(), eta[t], eng->max_h, t, dead,
-                                     eng->stream);
+            train_epoch_enqueue(eng, eta[t], sigma[t], momentum, flags, dead, t);
+            tsom::launch_epoch_guard(eng->status.as<int>(), t, dead, eng->stream);
             CU(cudaGetLastError());
         }
         const bool k1_all = eng->k1_timed;  // every epoch ran the tcgen05 main pass

@@ -303,7 +303,15 @@ struct Engine {
     uint32_t* hstat = nullptr;
     bool hstat_counts = false;  // [0..1] hold this epoch's re-check counts
     bool recheck_from_chunks = false;
-    double max_h = 1.0;                  // max |influence| of the bound matrix
+    // term guard (k_guard.cu): max |h| of the influence (device double), the
+    // zero-initialised extremes scratch, the invocation tag, and the row set
+    // of the last accumulation pass (x == nullptr: streamed, bound only)
+    DevBuf hmax, guard_buf;
+    uint32_t guard_tag = 0, last_guard_tag = 0;
+    const float* pass_x = nullptr;
+    uint32_t pass_ldx = 0;
+    const uint32_t* pass_sel = nullptr;
+    uint64_t pass_n = 0;
     float t_bmu = 0, t_accum = 0, t_smooth = 0, t_total = 0, t_k1 = 0, t_update = 0;
     float t_sample = 0;  // device sampler before the epoch (sampled tsom_train_epoch)
     bool k1_timed = false, update_timed = false, sample_timed = false;
@@ -428,8 +436,27 @@ void launch_status_reset(int* status, cudaStream_t st);
 void launch_apply_update_guarded(float* w, float* prev, uint32_t P, uint32_t D, const double* U,
                                  const double* H, bool use_momentum, double momentum, int* status,
                                  const int* dead, cudaStream_t st);
-void launch_epoch_guard(const int* status, const float* x2max, const float* w2max, double eta,
-                        double max_h, uint32_t epoch, int* dead, cudaStream_t st);
+// after an epoch's update: a non-finite update recorded in dead[]
+void launch_epoch_guard(const int* status, uint32_t epoch, int* dead, cudaStream_t st);
+// The accumulation-term guard of quantize_term (accum.hpp:34-38), exact
+// (k_guard.cu): flag[1] == tag iff the reference would throw for this epoch's
+// rows, BMUs and (pre-update) codebook.  Zero-initialised scratch of
+// guard_scratch_words() u32; dead (optional): multi-epoch failure record.
+struct GuardScratch {
+    uint32_t* flag = nullptr;  // [2]
+    uint32_t* seen = nullptr;  // [P]
+    uint32_t* mn = nullptr;    // [P * D]
+    uint32_t* mx = nullptr;    // [P * D]
+};
+size_t guard_scratch_words(uint32_t P, uint32_t D);
+GuardScratch guard_scratch(uint32_t* base, uint32_t P, uint32_t D);
+void launch_term_guard(const float* x, uint32_t ldx, const uint32_t* sel, uint64_t n,
+                       const uint32_t* bmu, const float* w, const double* infl, uint32_t P,
+                       uint32_t D, double eta, const float* x2max, const float* w2max,
+                       const double* hmax, uint32_t tag, GuardScratch g, int sm_count,
+                       cudaStream_t st, int* dead = nullptr, uint32_t epoch = 0);
+// max |h| of an influence matrix into *hmax (device double)
+void launch_infl_absmax(const double* infl, size_t n, double* hmax, cudaStream_t st);
 // influence_matrix (topology.hpp:342-364) from a P x P distance matrix
 void launch_influence(const double* dist, size_t n, double inv_two_sigma_sq, double* out,
                       cudaStream_t st);

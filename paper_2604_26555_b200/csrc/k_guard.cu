@@ -1,0 +1,178 @@
+// k_guard.cu — the accumulation-term guard of the reference, exactly.
+//
+// The reference quantises every term of an epoch (accumulate,
+// trainer.hpp:318-336; quantize_term, accum.hpp:34-38) and throws
+// "numerical fault: accumulation term out of range (|term| >= 2^22)" when
+//     |h[b][j]|  >= 2^22        (add_h)   or
+//     |fl(fl(eta h[b][j]) fl(x_ik - w_jk))| >= 2^22   (add_u)
+// for any row i (BMU b) of the selection, node j and feature k.  The engine
+// never forms those N K d terms.  It checks, on the device:
+//   1. a cheap bound: |eta| max|h| (max||x|| + max||w||) < 2^22 and
+//      max|h| < 2^22 — true for any sane data, and then nothing else runs;
+//   2. only when the bound fails, the exact test: per BMU node b and feature
+//      k the smallest and largest x_ik over its rows (one pass over the
+//      rows), then for every (b, j, k) the reference's term at both extremes.
+//      Every operation is monotone in x (IEEE rounding is), so the largest
+//      |term| over a node's rows is attained at one of them: the test fires
+//      exactly when the reference would throw, and for h only over the rows
+//      b some row maps to.
+// The codebook is the epoch's own (before apply_update), like the reference's.
+#include <cuda_runtime.h>
+
+#include <cstdint>
+
+#include "engine.h"
+
+namespace tsom {
+
+namespace {
+
+constexpr double kTermLimit = 4194304.0;  // 2^22, accum.hpp:30
+
+// float -> uint32 whose unsigned order is the float order
+__device__ __forceinline__ uint32_t f2ord(float f) {
+    const uint32_t u = __float_as_uint(f);
+    return (u & 0x80000000u) ? ~u : (u | 0x80000000u);
+}
+__device__ __forceinline__ float ord2f(uint32_t o) {
+    return __uint_as_float((o & 0x80000000u) ? (o & 0x7FFFFFFFu) : ~o);
+}
+
+__device__ __forceinline__ bool cheap_bound_over(const float* x2max, const float* w2max,
+                                                 const double* hmax, double eta) {
+    const double h = *hmax;
+    const double bound = fabs(eta) * h * (sqrt((double)*x2max) + sqrt((double)*w2max));
+    return !(h < kTermLimit && bound < kTermLimit);
+}
+
+__global__ void k_infl_absmax(const double* __restrict__ infl, size_t n,
+                              unsigned long long* __restrict__ out) {
+    double m = 0.0;
+    for (size_t i = blockIdx.x * (size_t)blockDim.x + threadIdx.x; i < n;
+         i += (size_t)gridDim.x * blockDim.x) {
+        const double a = fabs(infl[i]);
+        m = a > m || a != a ? a : m;  // NaN wins (it fails every comparison the guard makes)
+    }
+    for (int o = 16; o; o >>= 1) {
+        const double v = __shfl_xor_sync(0xffffffffu, m, o);
+        m = v > m || v != v ? v : m;
+    }
+    // non-negative doubles (and +NaN) order like their bit patterns
+    if ((threadIdx.x & 31) == 0) atomicMax(out, (unsigned long long)__double_as_longlong(m));
+}
+
+// The flags carry the invocation's tag (a counter the host passes) instead of
+// a boolean, so no launch is spent clearing them: flag[0] == tag: the cheap
+// bound failed this time; flag[1] == tag: a term the reference would reject.
+// mn / mx / seen are all zero between invocations (k_guard_clear restores
+// that after a use), so the common case costs three launches that return at
+// once.
+
+// flag[0] = tag when the cheap bound is over; then per-node feature extremes
+__global__ void k_guard_minmax(const float* __restrict__ x, uint32_t ldx,
+                               const uint32_t* __restrict__ sel, uint64_t n,
+                               const uint32_t* __restrict__ bmu, uint32_t D,
+                               const float* __restrict__ x2max, const float* __restrict__ w2max,
+                               const double* __restrict__ hmax, double eta, uint32_t tag,
+                               uint32_t* __restrict__ flag, uint32_t* __restrict__ mn,
+                               uint32_t* __restrict__ mx, uint32_t* __restrict__ seen) {
+    if (!cheap_bound_over(x2max, w2max, hmax, eta)) return;
+    if (blockIdx.x == 0 && threadIdx.x == 0) flag[0] = tag;
+    if (!x) return;  // no resident rows (streamed): the bound decides alone
+    for (uint64_t e = blockIdx.x * (uint64_t)blockDim.x + threadIdx.x; e < n * D;
+         e += (uint64_t)gridDim.x * blockDim.x) {
+        const uint64_t i = e / D;
+        const uint32_t k = (uint32_t)(e - i * D);
+        const uint32_t b = bmu[i];
+        const float v = x[(sel ? (uint64_t)sel[i] : i) * ldx + k];
+        // min as the max of the complemented order key (both arrays start at 0)
+        atomicMax(mx + (size_t)b * D + k, f2ord(v));
+        atomicMax(mn + (size_t)b * D + k, ~f2ord(v));
+        if (k == 0) seen[b] = 1u;
+    }
+}
+
+// flag[1] = a term the reference would reject (flag[0] set, or streamed rows)
+__global__ void k_guard_exact(const float* __restrict__ w, const double* __restrict__ infl,
+                              uint32_t P, uint32_t D, double eta, int has_rows, uint32_t tag,
+                              uint32_t* __restrict__ flag, const uint32_t* __restrict__ mn,
+                              const uint32_t* __restrict__ mx, const uint32_t* __restrict__ seen) {
+    if (flag[0] != tag) return;
+    if (!has_rows) {
+        if (blockIdx.x == 0 && threadIdx.x == 0) flag[1] = tag;
+        return;
+    }
+    for (uint64_t e = blockIdx.x * (uint64_t)blockDim.x + threadIdx.x; e < (uint64_t)P * P;
+         e += (uint64_t)gridDim.x * blockDim.x) {
+        const uint32_t b = (uint32_t)(e / P), j = (uint32_t)(e - (uint64_t)b * P);
+        if (!seen[b]) continue;
+        const double h = infl[(size_t)b * P + j];
+        bool bad = !(fabs(h) < kTermLimit);
+        const double eh = __dmul_rn(eta, h);
+        for (uint32_t k = 0; k < D && !bad; ++k) {
+            const double wk = (double)w[(size_t)j * D + k];
+            const double t1 = __dmul_rn(eh, __dsub_rn((double)ord2f(mx[(size_t)b * D + k]), wk));
+            const double t2 = __dmul_rn(eh, __dsub_rn((double)ord2f(~mn[(size_t)b * D + k]), wk));
+            bad = !(fabs(t1) < kTermLimit) || !(fabs(t2) < kTermLimit);
+        }
+        if (bad) flag[1] = tag;
+    }
+}
+
+// back to all-zero extremes after an invocation that used them
+__global__ void k_guard_clear(uint32_t P, uint32_t D, uint32_t tag,
+                              const uint32_t* __restrict__ flag, uint32_t* __restrict__ mn,
+                              uint32_t* __restrict__ mx, uint32_t* __restrict__ seen) {
+    if (flag[0] != tag) return;
+    for (uint64_t e = blockIdx.x * (uint64_t)blockDim.x + threadIdx.x; e < (uint64_t)P * D;
+         e += (uint64_t)gridDim.x * blockDim.x) {
+        mn[e] = 0u;
+        mx[e] = 0u;
+        if (e < P) seen[e] = 0u;
+    }
+}
+
+// a term-guard violation of this epoch fails a multi-epoch run before its update
+__global__ void k_guard_dead(const uint32_t* __restrict__ flag, uint32_t tag, uint32_t epoch,
+                             int* __restrict__ dead) {
+    if (dead[0] == 0 && flag[1] == tag) {
+        dead[0] = (int)epoch + 1;
+        dead[1] = 2;
+    }
+}
+
+}  // namespace
+
+void launch_infl_absmax(const double* infl, size_t n, double* hmax, cudaStream_t st) {
+    cudaMemsetAsync(hmax, 0, sizeof(double), st);
+    const unsigned blocks = (unsigned)std::min<size_t>((n + 255) / 256, 148 * 4);
+    TSOM_LAUNCH(k_infl_absmax<<<blocks, 256, 0, st>>>(
+        infl, n, reinterpret_cast<unsigned long long*>(hmax)));
+}
+
+void launch_term_guard(const float* x, uint32_t ldx, const uint32_t* sel, uint64_t n,
+                       const uint32_t* bmu, const float* w, const double* infl, uint32_t P,
+                       uint32_t D, double eta, const float* x2max, const float* w2max,
+                       const double* hmax, uint32_t tag, GuardScratch g, int sm_count,
+                       cudaStream_t st, int* dead, uint32_t epoch) {
+    TSOM_LAUNCH(k_guard_minmax<<<(unsigned)sm_count * 4, 256, 0, st>>>(
+        x, ldx, sel, n, bmu, D, x2max, w2max, hmax, eta, tag, g.flag, g.mn, g.mx, g.seen));
+    TSOM_LAUNCH(k_guard_exact<<<(unsigned)sm_count * 2, 256, 0, st>>>(
+        w, infl, P, D, eta, x ? 1 : 0, tag, g.flag, g.mn, g.mx, g.seen));
+    TSOM_LAUNCH(k_guard_clear<<<(unsigned)sm_count, 256, 0, st>>>(P, D, tag, g.flag, g.mn, g.mx,
+                                                                  g.seen));
+    if (dead) TSOM_LAUNCH(k_guard_dead<<<1, 1, 0, st>>>(g.flag, tag, epoch, dead));
+}
+
+size_t guard_scratch_words(uint32_t P, uint32_t D) { return 2 + (size_t)P + 2 * (size_t)P * D; }
+
+GuardScratch guard_scratch(uint32_t* base, uint32_t P, uint32_t D) {
+    GuardScratch g;
+    g.flag = base;
+    g.seen = base + 2;
+    g.mn = g.seen + P;
+    g.mx = g.mn + (size_t)P * D;
+    return g;
+}
+
+}  // namespace tsom

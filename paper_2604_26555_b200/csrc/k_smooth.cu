@@ -189,26 +189,18 @@ void launch_apply_update_guarded(float* w, float* prev, uint32_t P, uint32_t D, 
 
 // the host checks of tsom_train_epoch (non-finite update; |term| bound of
 // accum.hpp:35: |eta| max_h (||x|| + ||w||) < 2^22), evaluated on the device
-__global__ void k_epoch_guard(const int* __restrict__ status, const float* __restrict__ x2max,
-                              const float* __restrict__ w2max, double eta, double max_h,
-                              uint32_t epoch, int* __restrict__ dead) {
+__global__ void k_epoch_guard(const int* __restrict__ status, uint32_t epoch,
+                              int* __restrict__ dead) {
     if (dead[0]) return;
     if (*status != INT_MAX) {
         dead[0] = (int)epoch + 1;
         dead[1] = 1;
         dead[2] = *status;
-        return;
-    }
-    const double bound = fabs(eta) * max_h * (sqrt((double)*x2max) + sqrt((double)*w2max));
-    if (!(max_h < 4194304.0 && bound < 4194304.0)) {
-        dead[0] = (int)epoch + 1;
-        dead[1] = 2;
     }
 }
 
-void launch_epoch_guard(const int* status, const float* x2max, const float* w2max, double eta,
-                        double max_h, uint32_t epoch, int* dead, cudaStream_t st) {
-    TSOM_LAUNCH(k_epoch_guard<<<1, 1, 0, st>>>(status, x2max, w2max, eta, max_h, epoch, dead));
+void launch_epoch_guard(const int* status, uint32_t epoch, int* dead, cudaStream_t st) {
+    TSOM_LAUNCH(k_epoch_guard<<<1, 1, 0, st>>>(status, epoch, dead));
 }
 
 __global__ void k_status_reset(int* status) { *status = INT_MAX; }

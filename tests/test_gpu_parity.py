@@ -694,3 +694,69 @@ def test_h_bit_identical_to_reference(pkg, oracle_port, sampling):
         assert np.array_equal(h, ho), f"sigma {sigma}: {np.sum(h != ho)} H values differ"
         assert np.array_equal(h < 1e-12, ho < 1e-12)
         assert np.max(np.abs(u - uo)) <= 1e-9 * np.max(np.abs(uo))
+
+
+@pytest.mark.parametrize("big,fails", [(2.0**23, True), (2.0**23 - 1.0, False)])
+def test_term_guard_is_exact_at_the_boundary(pkg, oracle_port, big, fails):
+    """quantize_term (accum.hpp:34-38) rejects |eta h (x - w)| >= 2^22.  Rows at
+    0 with BMU node 0 and full influence on node 1 at `big` give the term
+    -0.5 * big: exactly 2^22 (the reference throws) or 2^22 - 0.5 (it does
+    not).  The engine's cheap norm bound (8.4e6) fails for both, so the exact
+    per-node extremes test decides — the same way as the reference, for the
+    accumulation pass (tsom_epoch) and for the device epoch, whose update a
+    failure skips (the reference throws before apply_update)."""
+    rng = np.random.default_rng(0)
+    x = (rng.standard_normal((64, 4)) * 1e-3).astype(np.float32)
+    w = np.array([[0.0] * 4, [big] * 4], np.float32)
+    infl = np.ones((2, 2))
+    ref_fails = False
+    try:
+        oracle_port.run_iteration(x, np.arange(64, dtype=np.uint32), w, infl, 0.5, 1, 1)
+    except oracle.OracleError as ex:
+        ref_fails = ex.status == 2
+    assert ref_fails == fails
+    e = pkg.Engine(2, 4)
+    e.bind(x)
+    e.set_codebook(w)
+    e.set_influence(infl)
+    if fails:
+        with pytest.raises(pkg.NumericalFault, match=r"accumulation term out of range"):
+            e.epoch(0.5)
+    else:
+        e.epoch(0.5)
+    e.set_topology_distance(np.zeros((2, 2)))  # influence exp(0) = 1 everywhere
+    if fails:
+        with pytest.raises(pkg.NumericalFault, match=r"accumulation term out of range"):
+            e.train_epoch(0.5, 1.0)
+        assert np.array_equal(e.get_codebook(), w)  # no update
+        # a legal first epoch (node 1 at 2^21 moves to ~2^20), then eta = 8
+        # makes the second epoch's terms ~2^23: the failure names epoch 1 and
+        # leaves the weights after epoch 0
+        e.set_codebook(w * 0.25)
+        e.train_epoch(0.5, 1.0)
+        w1 = e.get_codebook()
+        e.set_codebook(w * 0.25)
+        with pytest.raises(pkg.NumericalFault, match=r"\(epoch 1\)"):
+            e.train_epochs([0.5, 8.0], [1.0, 1.0])
+        assert np.array_equal(e.get_codebook(), w1)
+    else:
+        e.train_epoch(0.5, 1.0)
+        assert not np.array_equal(e.get_codebook(), w)
+
+
+def test_term_guard_cheap_bound_over_but_terms_small(pkg, oracle_port):
+    """Large values close to each other: the norm bound (|eta| (||x|| + ||w||)
+    = 7e6) exceeds 2^22 but every term is tiny — the reference accepts, and so
+    must the engine (it used to raise here)."""
+    rng = np.random.default_rng(1)
+    x = (1e6 + rng.standard_normal((200, 50))).astype(np.float32)
+    w = (1e6 + rng.standard_normal((16, 50))).astype(np.float32)
+    infl = oracle_port.influence_from_dist(oracle_port.lattice_dist("rect", 4, 4), 2.0)
+    uo, ho, _, _, _ = oracle_port.run_iteration(x, np.arange(200, dtype=np.uint32), w, infl,
+                                                0.5, 1, 1)
+    e = pkg.Engine(16, 50)
+    e.bind(x)
+    e.set_codebook(w)
+    e.set_influence(infl)
+    u, h, _ = e.epoch(0.5)
+    assert np.array_equal(h, ho)
