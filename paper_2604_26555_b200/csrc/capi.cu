@@ -625,13 +625,17 @@ uint32_t enqueue_term_guard(Engine* eng, double eta, int* dead = nullptr, uint32
         CU(cudaMemsetAsync(eng->guard_buf.p, 0, words * sizeof(uint32_t), eng->stream));
     }
     const uint32_t tag = ++eng->guard_tag ? eng->guard_tag : ++eng->guard_tag;  // never 0
-    tsom::launch_term_guard(eng->pass_x, eng->pass_ldx, eng->pass_sel, eng->pass_n,
+    static const int mode = [] {  // diagnostics: TSOM_GUARD=1 plain launch, 2 skip (A/B)
+        const char* v = getenv("TSOM_GUARD");
+        return v ? atoi(v) : 0;
+    }();
+    if (mode == 2) return tag;
+    CU(tsom::launch_term_guard(eng->pass_x, eng->pass_ldx, eng->pass_sel, eng->pass_n,
                             eng->bmu.as<uint32_t>(), eng->w.as<float>(), eng->infl.as<double>(),
                             eng->P, eng->D, eta, eng->x2max.as<float>(), eng->w2max.as<float>(),
                             eng->hmax.as<double>(), tag,
                             tsom::guard_scratch(eng->guard_buf.as<uint32_t>(), eng->P, eng->D),
-                            eng->sm_count, eng->stream, dead, epoch);
-    CU(cudaGetLastError());
+                            eng->sm_count, eng->stream, dead, epoch));
     return tag;
 }
 

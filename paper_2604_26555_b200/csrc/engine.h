@@ -450,7 +450,7 @@ struct GuardScratch {
 };
 size_t guard_scratch_words(uint32_t P, uint32_t D);
 GuardScratch guard_scratch(uint32_t* base, uint32_t P, uint32_t D);
-void launch_term_guard(const float* x, uint32_t ldx, const uint32_t* sel, uint64_t n,
+cudaError_t launch_term_guard(const float* x, uint32_t ldx, const uint32_t* sel, uint64_t n,
                        const uint32_t* bmu, const float* w, const double* infl, uint32_t P,
                        uint32_t D, double eta, const float* x2max, const float* w2max,
                        const double* hmax, uint32_t tag, GuardScratch g, int sm_count,

@@ -542,7 +542,8 @@ void launch_split_rows(int kind, const float* x, const uint32_t* sel, const uint
 // best value plus up to 8 local candidate ids within tie_thr of it (count 15 =
 // overflow, 0 = group not relevant for the row (rmask)).
 // dev_n (optional): row count read on the device (the near-tie list length).
-template <int kKind, bool kEnum>
+// kDump (diagnostics, option 99 bit 7): the main pass also stores every raw value
+template <int kKind, bool kEnum, bool kDump = false>
 __global__ void __launch_bounds__(EpiCfg<kKind>::kThreads, 1)
     k1_bmu_tc(const uint8_t* __restrict__ tiles, uint64_t n_host, const uint32_t* __restrict__ dev_n,
               uint32_t groups, uint32_t gn, uint32_t D, uint32_t stages,
@@ -741,7 +742,7 @@ __global__ void __launch_bounds__(EpiCfg<kKind>::kThreads, 1)
                 tc_fence_before();
                 __syncwarp();
                 if (lane == 0) mbar_arrive(&tempty_bar[acc]);  // warp done with the accumulator
-                if ((dbg & 128u) && pos < n) {
+                if (kDump && pos < n) {
                     float* dp = g_k1_dump + pos * (uint64_t)(groups * gn) + g * gn + c_begin * 32;
 #pragma unroll
                     for (int c = 0; c < kCPS; ++c)
@@ -924,10 +925,14 @@ cudaError_t launch_bmu_tc(int kind, const void* tiles, uint64_t n, const uint32_
     KernT kern;
     int slot;
     if (kind == kTcTf32) {
-        kern = enumerate ? k1_bmu_tc<kTcTf32, true> : k1_bmu_tc<kTcTf32, false>;
+        kern = enumerate ? k1_bmu_tc<kTcTf32, true>
+                         : ((g_k1_debug & 128u) ? k1_bmu_tc<kTcTf32, false, true>
+                                                : k1_bmu_tc<kTcTf32, false>);
         slot = enumerate ? 1 : 0;
     } else {
-        kern = enumerate ? k1_bmu_tc<kTcF16, true> : k1_bmu_tc<kTcF16, false>;
+        kern = enumerate ? k1_bmu_tc<kTcF16, true>
+                         : ((g_k1_debug & 128u) ? k1_bmu_tc<kTcF16, false, true>
+                                                : k1_bmu_tc<kTcF16, false>);
         slot = enumerate ? 3 : 2;
     }
     {

@@ -17,11 +17,14 @@
 //      exactly when the reference would throw, and for h only over the rows
 //      b some row maps to.
 // The codebook is the epoch's own (before apply_update), like the reference's.
+#include <cooperative_groups.h>
 #include <cuda_runtime.h>
 
 #include <cstdint>
 
 #include "engine.h"
+
+namespace cg = cooperative_groups;
 
 namespace tsom {
 
@@ -62,82 +65,72 @@ __global__ void k_infl_absmax(const double* __restrict__ infl, size_t n,
 }
 
 // The flags carry the invocation's tag (a counter the host passes) instead of
-// a boolean, so no launch is spent clearing them: flag[0] == tag: the cheap
+// a boolean, so nothing is spent clearing them: flag[0] == tag: the cheap
 // bound failed this time; flag[1] == tag: a term the reference would reject.
-// mn / mx / seen are all zero between invocations (k_guard_clear restores
-// that after a use), so the common case costs three launches that return at
-// once.
-
-// flag[0] = tag when the cheap bound is over; then per-node feature extremes
-__global__ void k_guard_minmax(const float* __restrict__ x, uint32_t ldx,
-                               const uint32_t* __restrict__ sel, uint64_t n,
-                               const uint32_t* __restrict__ bmu, uint32_t D,
-                               const float* __restrict__ x2max, const float* __restrict__ w2max,
-                               const double* __restrict__ hmax, double eta, uint32_t tag,
-                               uint32_t* __restrict__ flag, uint32_t* __restrict__ mn,
-                               uint32_t* __restrict__ mx, uint32_t* __restrict__ seen) {
+// mn / mx / seen are all zero between invocations (phase 3 restores that
+// after a use).  One cooperative launch: every block evaluates the cheap
+// bound first and, in the common case, returns at once (uniformly, so the
+// grid barriers are never reached).
+__global__ void __launch_bounds__(256) k_term_guard(
+    const float* __restrict__ x, uint32_t ldx, const uint32_t* __restrict__ sel, uint64_t n,
+    const uint32_t* __restrict__ bmu, const float* __restrict__ w,
+    const double* __restrict__ infl, uint32_t P, uint32_t D, double eta,
+    const float* __restrict__ x2max, const float* __restrict__ w2max,
+    const double* __restrict__ hmax, uint32_t tag, uint32_t* __restrict__ flag,
+    uint32_t* __restrict__ mn, uint32_t* __restrict__ mx, uint32_t* __restrict__ seen,
+    int* __restrict__ dead, uint32_t epoch) {
     if (!cheap_bound_over(x2max, w2max, hmax, eta)) return;
-    if (blockIdx.x == 0 && threadIdx.x == 0) flag[0] = tag;
-    if (!x) return;  // no resident rows (streamed): the bound decides alone
-    for (uint64_t e = blockIdx.x * (uint64_t)blockDim.x + threadIdx.x; e < n * D;
-         e += (uint64_t)gridDim.x * blockDim.x) {
-        const uint64_t i = e / D;
-        const uint32_t k = (uint32_t)(e - i * D);
-        const uint32_t b = bmu[i];
-        const float v = x[(sel ? (uint64_t)sel[i] : i) * ldx + k];
-        // min as the max of the complemented order key (both arrays start at 0)
-        atomicMax(mx + (size_t)b * D + k, f2ord(v));
-        atomicMax(mn + (size_t)b * D + k, ~f2ord(v));
-        if (k == 0) seen[b] = 1u;
-    }
-}
-
-// flag[1] = a term the reference would reject (flag[0] set, or streamed rows)
-__global__ void k_guard_exact(const float* __restrict__ w, const double* __restrict__ infl,
-                              uint32_t P, uint32_t D, double eta, int has_rows, uint32_t tag,
-                              uint32_t* __restrict__ flag, const uint32_t* __restrict__ mn,
-                              const uint32_t* __restrict__ mx, const uint32_t* __restrict__ seen) {
-    if (flag[0] != tag) return;
-    if (!has_rows) {
-        if (blockIdx.x == 0 && threadIdx.x == 0) flag[1] = tag;
-        return;
-    }
-    for (uint64_t e = blockIdx.x * (uint64_t)blockDim.x + threadIdx.x; e < (uint64_t)P * P;
-         e += (uint64_t)gridDim.x * blockDim.x) {
-        const uint32_t b = (uint32_t)(e / P), j = (uint32_t)(e - (uint64_t)b * P);
-        if (!seen[b]) continue;
-        const double h = infl[(size_t)b * P + j];
-        bool bad = !(fabs(h) < kTermLimit);
-        const double eh = __dmul_rn(eta, h);
-        for (uint32_t k = 0; k < D && !bad; ++k) {
-            const double wk = (double)w[(size_t)j * D + k];
-            const double t1 = __dmul_rn(eh, __dsub_rn((double)ord2f(mx[(size_t)b * D + k]), wk));
-            const double t2 = __dmul_rn(eh, __dsub_rn((double)ord2f(~mn[(size_t)b * D + k]), wk));
-            bad = !(fabs(t1) < kTermLimit) || !(fabs(t2) < kTermLimit);
+    cg::grid_group grid = cg::this_grid();
+    const uint64_t t0 = blockIdx.x * (uint64_t)blockDim.x + threadIdx.x;
+    const uint64_t ts = (uint64_t)gridDim.x * blockDim.x;
+    if (t0 == 0) flag[0] = tag;
+    bool bad_all = false;
+    if (!x) {
+        bad_all = true;  // no resident rows (streamed): the bound decides alone
+    } else {
+        // phase 1: per BMU node and feature, the extremes of the rows
+        for (uint64_t e = t0; e < n * D; e += ts) {
+            const uint64_t i = e / D;
+            const uint32_t k = (uint32_t)(e - i * D);
+            const uint32_t b = bmu[i];
+            const float v = x[(sel ? (uint64_t)sel[i] : i) * ldx + k];
+            // min as the max of the complemented order key (both start at 0)
+            atomicMax(mx + (size_t)b * D + k, f2ord(v));
+            atomicMax(mn + (size_t)b * D + k, ~f2ord(v));
+            if (k == 0) seen[b] = 1u;
         }
-        if (bad) flag[1] = tag;
+        grid.sync();
+        // phase 2: the reference's term at both extremes, every (b, j, k)
+        for (uint64_t e = t0; e < (uint64_t)P * P; e += ts) {
+            const uint32_t b = (uint32_t)(e / P), j = (uint32_t)(e - (uint64_t)b * P);
+            if (!seen[b]) continue;
+            const double h = infl[(size_t)b * P + j];
+            bool bad = !(fabs(h) < kTermLimit);
+            const double eh = __dmul_rn(eta, h);
+            for (uint32_t k = 0; k < D && !bad; ++k) {
+                const double wk = (double)w[(size_t)j * D + k];
+                const double t1 = __dmul_rn(eh, __dsub_rn((double)ord2f(mx[(size_t)b * D + k]), wk));
+                const double t2 = __dmul_rn(eh, __dsub_rn((double)ord2f(~mn[(size_t)b * D + k]), wk));
+                bad = !(fabs(t1) < kTermLimit) || !(fabs(t2) < kTermLimit);
+            }
+            if (bad) flag[1] = tag;
+        }
+        grid.sync();
+        // phase 3: back to all-zero extremes
+        for (uint64_t e = t0; e < (uint64_t)P * D; e += ts) {
+            mn[e] = 0u;
+            mx[e] = 0u;
+            if (e < P) seen[e] = 0u;
+        }
     }
-}
-
-// back to all-zero extremes after an invocation that used them
-__global__ void k_guard_clear(uint32_t P, uint32_t D, uint32_t tag,
-                              const uint32_t* __restrict__ flag, uint32_t* __restrict__ mn,
-                              uint32_t* __restrict__ mx, uint32_t* __restrict__ seen) {
-    if (flag[0] != tag) return;
-    for (uint64_t e = blockIdx.x * (uint64_t)blockDim.x + threadIdx.x; e < (uint64_t)P * D;
-         e += (uint64_t)gridDim.x * blockDim.x) {
-        mn[e] = 0u;
-        mx[e] = 0u;
-        if (e < P) seen[e] = 0u;
-    }
-}
-
-// a term-guard violation of this epoch fails a multi-epoch run before its update
-__global__ void k_guard_dead(const uint32_t* __restrict__ flag, uint32_t tag, uint32_t epoch,
-                             int* __restrict__ dead) {
-    if (dead[0] == 0 && flag[1] == tag) {
-        dead[0] = (int)epoch + 1;
-        dead[1] = 2;
+    if (bad_all && t0 == 0) flag[1] = tag;
+    // a violation of this epoch fails a multi-epoch run before its update
+    if (dead && t0 == 0) {
+        __threadfence();
+        if (dead[0] == 0 && (bad_all || flag[1] == tag)) {
+            dead[0] = (int)epoch + 1;
+            dead[1] = 2;
+        }
     }
 }
 
@@ -150,18 +143,18 @@ void launch_infl_absmax(const double* infl, size_t n, double* hmax, cudaStream_t
         infl, n, reinterpret_cast<unsigned long long*>(hmax)));
 }
 
-void launch_term_guard(const float* x, uint32_t ldx, const uint32_t* sel, uint64_t n,
+cudaError_t launch_term_guard(const float* x, uint32_t ldx, const uint32_t* sel, uint64_t n,
                        const uint32_t* bmu, const float* w, const double* infl, uint32_t P,
                        uint32_t D, double eta, const float* x2max, const float* w2max,
                        const double* hmax, uint32_t tag, GuardScratch g, int sm_count,
                        cudaStream_t st, int* dead, uint32_t epoch) {
-    TSOM_LAUNCH(k_guard_minmax<<<(unsigned)sm_count * 4, 256, 0, st>>>(
-        x, ldx, sel, n, bmu, D, x2max, w2max, hmax, eta, tag, g.flag, g.mn, g.mx, g.seen));
-    TSOM_LAUNCH(k_guard_exact<<<(unsigned)sm_count * 2, 256, 0, st>>>(
-        w, infl, P, D, eta, x ? 1 : 0, tag, g.flag, g.mn, g.mx, g.seen));
-    TSOM_LAUNCH(k_guard_clear<<<(unsigned)sm_count, 256, 0, st>>>(P, D, tag, g.flag, g.mn, g.mx,
-                                                                  g.seen));
-    if (dead) TSOM_LAUNCH(k_guard_dead<<<1, 1, 0, st>>>(g.flag, tag, epoch, dead));
+    void* args[] = {(void*)&x,     (void*)&ldx,   (void*)&sel,   (void*)&n,    (void*)&bmu,
+                    (void*)&w,     (void*)&infl,  (void*)&P,     (void*)&D,    (void*)&eta,
+                    (void*)&x2max, (void*)&w2max, (void*)&hmax,  (void*)&tag,  (void*)&g.flag,
+                    (void*)&g.mn,  (void*)&g.mx,  (void*)&g.seen, (void*)&dead, (void*)&epoch};
+    ++g_launches;
+    return cudaLaunchCooperativeKernel((const void*)k_term_guard, dim3((unsigned)sm_count * 2),
+                                       dim3(256), args, 0, st);
 }
 
 size_t guard_scratch_words(uint32_t P, uint32_t D) { return 2 + (size_t)P + 2 * (size_t)P * D; }

@@ -35,19 +35,20 @@ __global__ void k_build_saug(const double* __restrict__ sums, const float* __res
 //           (dequantize, accum.hpp:40-42): bit-identical to the reference,
 //           so its H < 1e-12 freeze rule (trainer.hpp:350) fires on the same
 //           nodes (terms below 2^-41 vanish there too).
-__global__ void __launch_bounds__(256) k_smooth_den(const double* __restrict__ infl,
-                                                    const double* __restrict__ sums, uint32_t P,
-                                                    uint32_t D, double* __restrict__ H,
-                                                    double* __restrict__ Hx) {
-    __shared__ double part[8][33];
-    __shared__ __int128 qpart[8][33];
+constexpr int kDenSlices = 32;  // b-slices per block (32 nodes x 32 slices = 1024 threads)
+__global__ void __launch_bounds__(1024) k_smooth_den(const double* __restrict__ infl,
+                                                     const double* __restrict__ sums, uint32_t P,
+                                                     uint32_t D, double* __restrict__ H,
+                                                     double* __restrict__ Hx) {
+    __shared__ double part[kDenSlices][33];
+    __shared__ __int128 qpart[kDenSlices][33];
     const uint32_t tj = threadIdx.x & 31, sl = threadIdx.x >> 5;
     const uint32_t j = blockIdx.x * 32 + tj;
     const double* c = sums + (size_t)P * D;
     double acc = 0.0;
     __int128 qacc = 0;
     if (j < P)
-        for (uint32_t b = sl; b < P; b += 8) {
+        for (uint32_t b = sl; b < P; b += kDenSlices) {
             const double h = infl[(size_t)b * P + j];
             acc = fma(h, c[b], acc);
             const long long q = __double2ll_rn(h * 1099511627776.0);  // llrint(h 2^40)
@@ -59,7 +60,7 @@ __global__ void __launch_bounds__(256) k_smooth_den(const double* __restrict__ i
     if (sl == 0 && j < P) {
         double v = 0.0;
         __int128 qv = 0;
-        for (int k = 0; k < 8; ++k) {
+        for (int k = 0; k < kDenSlices; ++k) {
             v += part[k][tj];
             qv += qpart[k][tj];
         }
@@ -131,7 +132,7 @@ void launch_smooth(const double* infl, const double* sums, const float* w, uint3
     double* Hx = partial + (size_t)SM_SPLIT * P * D;
     const size_t n = (size_t)P * (D + 1);
     TSOM_LAUNCH(k_build_saug<<<(unsigned)((n + 255) / 256), 256, 0, st>>>(sums, w, P, D, saug));
-    TSOM_LAUNCH(k_smooth_den<<<(P + 31) / 32, 256, 0, st>>>(infl, sums, P, D, H, Hx));
+    TSOM_LAUNCH(k_smooth_den<<<(P + 31) / 32, 32 * kDenSlices, 0, st>>>(infl, sums, P, D, H, Hx));
     dim3 grid((P + SM_TJ - 1) / SM_TJ, (D + SM_KC - 1) / SM_KC, SM_SPLIT);
     TSOM_LAUNCH(k_smooth_gemm<<<grid, 256, 0, st>>>(infl, saug, P, D, partial));
     const size_t pd = (size_t)P * D;
