@@ -158,6 +158,17 @@ cudaEvent_t k1_event(Engine* eng, int end) {
     return eng->ev[8 + end];
 }
 
+constexpr uint32_t kTieLogCap = 1024;  // tie_log entries between two syncs
+
+// the near-tie fractions logged since the last sync (called after it)
+void fold_tie_log(Engine* eng) {
+    for (uint32_t i = 0; i < eng->tie_log_n; ++i)
+        if (eng->tie_log[2 * i + 1])
+            eng->tie_frac_max = std::max(eng->tie_frac_max, (double)eng->tie_log[2 * i] /
+                                                                (double)eng->tie_log[2 * i + 1]);
+    eng->tie_log_n = 0;
+}
+
 // near-tie list passes: pcount[p] = clamp(count - p * cap, 0, cap); the last
 // pass keeps the whole remainder (its slots past cap take the full re-scan)
 constexpr uint32_t kTiePasses = 4;
@@ -219,6 +230,12 @@ void run_bmu(Engine* eng, const float* x, uint32_t ldx, const uint32_t* sel, uin
                                 eng->bmu.as<uint32_t>(), eng->ties.as<uint32_t>(),
                                 eng->tmask.as<uint32_t>(), eng->flags.as<uint32_t>(), eng->stream);
         CU(cudaGetLastError());
+        if (eng->tie_log_n < kTieLogCap) {
+            eng->tie_log[2 * eng->tie_log_n + 1] = (uint32_t)std::min<uint64_t>(n, UINT32_MAX);
+            CU(cudaMemcpyAsync(eng->tie_log + 2 * eng->tie_log_n, eng->ties.p, sizeof(uint32_t),
+                               cudaMemcpyDeviceToHost, eng->stream));
+            ++eng->tie_log_n;
+        }
         // near-tie rows (~1-3%): same tensor-core kernel in enumerate mode on just
         // those rows, then exact FP64 over their few candidates.  The list length
         // stays on the device (kernels grid-stride over it), so the epoch needs
@@ -230,8 +247,16 @@ void run_bmu(Engine* eng, const float* x, uint32_t ldx, const uint32_t* sel, uin
         // reads its slot count on the device, passes past the actual count
         // exit at once, and slots past 4 cap (> 25 % of the rows) take the
         // full exact re-scan.
-        const uint32_t passes = n > (1u << 20) ? kTiePasses : 1u;
+        // passes launched: all kTiePasses until near-ties have been observed,
+        // then twice the largest fraction seen so far plus one spare pass
+        // (never fewer than the data need: the last pass's overflow takes the
+        // exact re-scan, so a short count costs time, not correctness)
+        uint32_t passes = n > (1u << 20) ? kTiePasses : 1u;
         const uint64_t cap = passes > 1 ? (n + kTieCapDiv - 1) / kTieCapDiv : n;
+        if (passes > 1 && eng->tie_frac_max >= 0.0) {
+            const double need = 2.0 * eng->tie_frac_max * (double)n / (double)cap;
+            passes = std::min<uint32_t>(kTiePasses, (uint32_t)std::ceil(need) + 1u);
+        }
         const uint64_t mt = (cap + tsom::kTcTileM - 1) / tsom::kTcTileM;
         CU(eng->tsplit.ensure(mt * geo.tile_bytes));
         CU(eng->part2.ensure((size_t)groups * 4 * cap * sizeof(float)));
@@ -652,6 +677,7 @@ void check_term_guard(Engine* eng, uint32_t tag) {
 }
 
 void finish_recheck(Engine* eng) {
+    fold_tie_log(eng);
     if (eng->recheck_from_chunks) {
         uint64_t t = 0;
         if (eng->hstat_counts)
@@ -752,6 +778,7 @@ int tsom_create(int device, uint32_t nodes, uint32_t dims, tsom_engine** out) {
         CU(eng->hmax.ensure(sizeof(double)));
         CU(cudaMemsetAsync(eng->hmax.p, 0, sizeof(double), eng->stream));
         CU(cudaMallocHost(&eng->hstat, 32 * sizeof(uint32_t)));
+        CU(cudaMallocHost(&eng->tie_log, 2 * kTieLogCap * sizeof(uint32_t)));
         std::memset(eng->hstat, 0, 32 * sizeof(uint32_t));
         ensure_rows(eng, 1);
         CU(cudaStreamSynchronize(eng->stream));
@@ -782,6 +809,7 @@ int tsom_destroy(tsom_engine* eng) {
     for (auto& ev : eng->ev)
         if (ev) cudaEventDestroy(ev);
     if (eng->hstat) cudaFreeHost(eng->hstat);
+    if (eng->tie_log) cudaFreeHost(eng->tie_log);
     for (cudaEvent_t e : eng->k1_ev) cudaEventDestroy(e);
     for (cudaEvent_t e : eng->red_ev) cudaEventDestroy(e);
     if (eng->stream) cudaStreamDestroy(eng->stream);
@@ -819,6 +847,9 @@ int tsom_set_option(tsom_engine* eng, int key, int64_t value) {
                 break;
             case 98:  // diagnostics: element-wise 3xFP16 split (k_split_rows<kTcF16>)
                 tsom::g_split_v1 = (int)value;
+                break;
+            case 96:  // diagnostics: 1 = the per-row main-pass merge (k_merge_fast)
+                tsom::g_merge_v1 = (int)value;
                 break;
             case 97:  // diagnostics: 1 = cp.async K2 gather instead of the TMA gather
                 tsom::g_gather_kind = (int)value;

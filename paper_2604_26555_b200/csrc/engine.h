@@ -301,6 +301,12 @@ struct Engine {
     // end-of-epoch synchronisation: [0..1] re-check counts (resident epochs),
     // [2] update status, [3] max ||x||^2 and [4] max ||w||^2 (term guard)
     uint32_t* hstat = nullptr;
+    // near-tie list lengths of the main passes since the last sync ([count,
+    // rows] pairs, pinned, read back asynchronously); their largest fraction
+    // sizes the enumerate passes of later epochs (run_bmu)
+    uint32_t* tie_log = nullptr;
+    uint32_t tie_log_n = 0;
+    double tie_frac_max = -1.0;  // < 0: nothing observed yet
     bool hstat_counts = false;  // [0..1] hold this epoch's re-check counts
     bool recheck_from_chunks = false;
     // term guard (k_guard.cu): max |h| of the influence (device double), the
@@ -384,6 +390,7 @@ cudaError_t launch_bmu_tc(int kind, const void* tiles, uint64_t n, const uint32_
 extern uint32_t g_k1_debug;
 extern int g_split_v1;
 extern int g_gather_kind;
+extern int g_merge_v1;
 int k1_trace_copy(unsigned long long* out, uint32_t n);
 int k1_set_dump(float* d_buf);  // diagnostics: option 99 bit 7 target (rows x groups*gn floats)  // diagnostics  // diagnostics: bit0 skip epilogue math, bit1 skip MMAs
 // main-pass merge: bmu for rows with a clear winner, near-tie positions -> ties

@@ -316,14 +316,115 @@ __global__ void __launch_bounds__(256, 8) k_merge_fast(
     }
 }
 
+// The same merge, four consecutive rows per thread (one sub-group record per
+// codebook group, groups <= 8, n % 4 == 0): every load of a thread — the
+// minima and codes of all groups and the row windows, 16 B each — is
+// independent and issued at once, so a warp pays one memory latency instead of
+// the two of the per-row kernel (the code of the winning group is read
+// without knowing the winner).  Rows, BMUs, the near-tie list order and the
+// masks are those of k_merge_fast.
+template <int kG>
+__global__ void __launch_bounds__(256) k_merge_fast4(
+    const float* __restrict__ part, uint64_t n, uint32_t gn, const float* __restrict__ xn2,
+    const float* __restrict__ w2max, const float* __restrict__ scale, TieWin win,
+    uint32_t* __restrict__ bmu, uint32_t* __restrict__ ties, uint32_t* __restrict__ tmask,
+    uint32_t* __restrict__ flags) {
+    const uint64_t q = blockIdx.x * (uint64_t)blockDim.x + threadIdx.x;  // row quad
+    const uint64_t i0 = q * 4;
+    const bool valid = i0 < n;
+    const uint32_t lane = threadIdx.x & 31;
+    float4 mn[kG];
+    uint4 cd[kG];
+    float4 xw = make_float4(0.f, 0.f, 0.f, 0.f);
+    if (valid) {
+#pragma unroll
+        for (int g = 0; g < kG; ++g) {
+            mn[g] = __ldg(reinterpret_cast<const float4*>(part + (size_t)g * 2 * n + i0));
+            cd[g] = __ldg(reinterpret_cast<const uint4*>(part + (size_t)g * 2 * n + n + i0));
+        }
+        xw = __ldg(reinterpret_cast<const float4*>(xn2 + i0));
+    }
+    const bool overflow = __float_as_uint(__ldg(scale + 2)) != 0u;
+    const float wpart = tie_wpart(__ldg(w2max), __ldg(scale + 1), win);
+    uint32_t out[4];
+#pragma unroll
+    for (int r = 0; r < 4; ++r) {
+        float b[kG];
+        uint32_t c[kG];
+#pragma unroll
+        for (int g = 0; g < kG; ++g) {
+            b[g] = r == 0 ? mn[g].x : r == 1 ? mn[g].y : r == 2 ? mn[g].z : mn[g].w;
+            c[g] = r == 0 ? cd[g].x : r == 1 ? cd[g].y : r == 2 ? cd[g].z : cd[g].w;
+        }
+        float B1 = CUDART_INF_F;
+        uint32_t gmin = 0, code = 0;
+#pragma unroll
+        for (int g = 0; g < kG; ++g)  // strict <: lowest node ids on equal minima
+            if (b[g] < B1) {
+                B1 = b[g];
+                gmin = g;
+                code = c[g];
+            }
+        out[r] = gmin * gn + (code == 0xFFFFFFFFu ? 0u : code);
+        bool need_tie = false;
+        uint32_t mask = 0;
+        if (valid) {
+            if (overflow) {
+                const uint32_t slot = atomicAdd(&flags[0], 1u);
+                flags[2 + slot] = (uint32_t)(i0 + r);
+            } else {
+                const float x2 = r == 0 ? xw.x : r == 1 ? xw.y : r == 2 ? xw.z : xw.w;
+                const float lim = B1 + (x2 + wpart);
+                bool clear = code != 0xFFFFFFFFu;
+#pragma unroll
+                for (int g = 0; g < kG; ++g) {
+                    const bool in = b[g] <= lim;
+                    if (in) mask |= 1u << g;
+                    if (in && (uint32_t)g != gmin) clear = false;
+                }
+                need_tie = !clear;
+            }
+        }
+        // warp-aggregated append to the near-tie list (one atomic per warp)
+        const uint32_t ballot = __ballot_sync(0xffffffffu, need_tie);
+        if (ballot) {
+            uint32_t base = 0;
+            if (lane == (uint32_t)(__ffs(ballot) - 1))
+                base = atomicAdd(&ties[0], (uint32_t)__popc(ballot));
+            base = __shfl_sync(0xffffffffu, base, __ffs(ballot) - 1);
+            if (need_tie) {
+                const uint32_t slot = base + __popc(ballot & ((1u << lane) - 1u));
+                ties[1 + slot] = (uint32_t)(i0 + r);
+                tmask[slot] = mask;
+            }
+        }
+    }
+    if (valid) *reinterpret_cast<uint4*>(bmu + i0) = make_uint4(out[0], out[1], out[2], out[3]);
+}
+
 void launch_merge_fast(const float* part, uint64_t n, uint32_t groups, uint32_t sets, uint32_t gn,
                        const float* xn2, const float* w2max, const float* scale, TieWin win,
                        uint32_t* bmu, uint32_t* ties, uint32_t* tmask, uint32_t* flags,
                        cudaStream_t st) {
     if (n == 0) return;
+    if (sets == 1 && n % 4 == 0 && groups <= 8 && !g_merge_v1) {
+        const unsigned blocks = (unsigned)((n / 4 + 255) / 256);
+#define TSOM_MERGE4(G)                                                                       \
+    case G:                                                                                  \
+        TSOM_LAUNCH(k_merge_fast4<G><<<blocks, 256, 0, st>>>(part, n, gn, xn2, w2max, scale, \
+                                                             win, bmu, ties, tmask, flags)); \
+        return;
+        switch (groups) {
+            TSOM_MERGE4(1) TSOM_MERGE4(2) TSOM_MERGE4(3) TSOM_MERGE4(4)
+            TSOM_MERGE4(5) TSOM_MERGE4(6) TSOM_MERGE4(7) TSOM_MERGE4(8)
+        }
+#undef TSOM_MERGE4
+    }
     TSOM_LAUNCH(k_merge_fast<<<(unsigned)((n + 255) / 256), 256, 0, st>>>(
         part, n, groups, sets, gn, xn2, w2max, scale, win, bmu, ties, tmask, flags));
 }
+
+int g_merge_v1 = 0;  // diagnostics (TSOM option 96): 1 = the per-row merge
 
 
 // Enumerate-pass merge over the near-tie rows f < n (position ties[f]).
