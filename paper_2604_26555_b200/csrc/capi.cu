@@ -162,6 +162,15 @@ constexpr uint32_t kTieLogCap = 1024;  // tie_log entries between two syncs
 
 // the near-tie fractions logged since the last sync (called after it)
 void fold_tie_log(Engine* eng) {
+    if (eng->tie_log_n == 0) return;
+    std::vector<uint32_t> cnt(eng->tie_log_n);
+    if (cudaMemcpy(cnt.data(), eng->tie_dev.p, cnt.size() * sizeof(uint32_t),
+                   cudaMemcpyDeviceToHost) != cudaSuccess) {
+        cudaGetLastError();
+        eng->tie_log_n = 0;
+        return;
+    }
+    for (uint32_t i = 0; i < eng->tie_log_n; ++i) eng->tie_log[2 * i] = cnt[i];
     for (uint32_t i = 0; i < eng->tie_log_n; ++i)
         if (eng->tie_log[2 * i + 1])
             eng->tie_frac_max = std::max(eng->tie_frac_max, (double)eng->tie_log[2 * i] /
@@ -174,8 +183,10 @@ void fold_tie_log(Engine* eng) {
 constexpr uint32_t kTiePasses = 4;
 constexpr uint32_t kTieCapDiv = 16;  // enumerate scratch: n / 16 rows (4 passes cover 25 %)
 __global__ void k_tie_pass_counts(const uint32_t* __restrict__ count, uint64_t cap,
-                                  uint32_t passes, uint32_t* __restrict__ pcount) {
+                                  uint32_t passes, uint32_t* __restrict__ pcount,
+                                  uint32_t* __restrict__ log_slot) {
     const uint32_t p = threadIdx.x;
+    if (p == 0 && log_slot) *log_slot = *count;  // the near-tie count, for later pass sizing
     if (p >= passes) return;
     const uint64_t c = *count, o = (uint64_t)p * cap;
     const uint64_t rest = c <= o ? 0 : c - o;
@@ -189,17 +200,21 @@ __global__ void k_tie_pass_counts(const uint32_t* __restrict__ count, uint64_t c
 void run_bmu(Engine* eng, const float* x, uint32_t ldx, const uint32_t* sel, uint64_t n,
              const float* x2max, const void* tiles, const float* tiles_xn2) {
     const float* xsrc = x;
-    CU(cudaMemsetAsync(eng->flags.p, 0, 2 * sizeof(uint32_t), eng->stream));
-    if (n == 0) return;
     const int kind = tc_kind(eng);
+    if (n == 0 || kind == tsom::kTcNone)
+        CU(cudaMemsetAsync(eng->flags.p, 0, 2 * sizeof(uint32_t), eng->stream));
+    if (n == 0) return;
     if (kind != tsom::kTcNone) {
         const tsom::TcGeom geo = tsom::tc_geom(kind, eng->D);
         const uint32_t gn = tsom::tc_group_width(eng->P);
         const uint32_t groups = (eng->P + gn - 1) / gn;
         const float* scale = eng->scale.as<float>();
         const tsom::TieWin win = tie_window(eng, kind);
-        // operand scale + codebook B operand for these rows (a few microseconds)
-        tsom::launch_set_scale(kind, x2max, eng->scale.as<float>(), eng->stream);
+        CU(eng->ties.ensure((n + 1) * sizeof(uint32_t)));
+        // operand scale + codebook B operand for these rows (a few microseconds);
+        // the re-check counters and the near-tie count start at zero
+        tsom::launch_set_scale(kind, x2max, eng->scale.as<float>(), eng->stream,
+                               eng->flags.as<uint32_t>(), 2, eng->ties.as<uint32_t>());
         CU(eng->wsplit.ensure(tsom::tc_wsplit_bytes(kind, eng->P, eng->D)));
         tsom::launch_prep_wsplit(kind, eng->w.as<float>(), eng->P, eng->D, scale, eng->wsplit.p,
                                  eng->stream);
@@ -214,9 +229,7 @@ void run_bmu(Engine* eng, const float* x, uint32_t ldx, const uint32_t* sel, uin
             tiles_xn2 = eng->gxn2.as<float>();
         }
         CU(eng->part.ensure((size_t)groups * 2 * n * sizeof(float)));
-        CU(eng->ties.ensure((n + 1) * sizeof(uint32_t)));
         CU(eng->tmask.ensure(std::max<uint64_t>(n, 1) * sizeof(uint32_t)));
-        CU(cudaMemsetAsync(eng->ties.p, 0, sizeof(uint32_t), eng->stream));
         const float* w2 = eng->w2max.as<float>();
         CU(cudaEventRecord(k1_event(eng, 0), eng->stream));
         CU(tsom::launch_bmu_tc(kind, tiles, n, nullptr, false, eng->P, eng->D, eng->wsplit.p,
@@ -230,11 +243,10 @@ void run_bmu(Engine* eng, const float* x, uint32_t ldx, const uint32_t* sel, uin
                                 eng->bmu.as<uint32_t>(), eng->ties.as<uint32_t>(),
                                 eng->tmask.as<uint32_t>(), eng->flags.as<uint32_t>(), eng->stream);
         CU(cudaGetLastError());
+        uint32_t* log_slot = nullptr;  // the count goes to a device log, read after the sync
         if (eng->tie_log_n < kTieLogCap) {
             eng->tie_log[2 * eng->tie_log_n + 1] = (uint32_t)std::min<uint64_t>(n, UINT32_MAX);
-            CU(cudaMemcpyAsync(eng->tie_log + 2 * eng->tie_log_n, eng->ties.p, sizeof(uint32_t),
-                               cudaMemcpyDeviceToHost, eng->stream));
-            ++eng->tie_log_n;
+            log_slot = eng->tie_dev.as<uint32_t>() + eng->tie_log_n++;
         }
         // near-tie rows (~1-3%): same tensor-core kernel in enumerate mode on just
         // those rows, then exact FP64 over their few candidates.  The list length
@@ -265,7 +277,8 @@ void run_bmu(Engine* eng, const float* x, uint32_t ldx, const uint32_t* sel, uin
         const uint32_t* tcount = eng->ties.as<uint32_t>();
         const uint32_t* tpos = tcount + 1;
         uint32_t* pcount = eng->tcnt.as<uint32_t>();
-        TSOM_LAUNCH(k_tie_pass_counts<<<1, 32, 0, eng->stream>>>(tcount, cap, passes, pcount));
+        TSOM_LAUNCH(k_tie_pass_counts<<<1, 32, 0, eng->stream>>>(tcount, cap, passes, pcount,
+                                                                  log_slot));
         for (uint32_t pz = 0; pz < passes; ++pz) {
             const uint64_t o = (uint64_t)pz * cap;
             tsom::launch_split_rows(kind, xsrc, sel, tpos + o, cap, eng->D, scale, win,
@@ -722,7 +735,8 @@ std::vector<DevBuf*> all_buffers(Engine* eng) {
                       &eng->topo_buf[4], &eng->topo_buf[5], &eng->topo_buf[6], &eng->topo_buf[7],
                       &eng->topo_buf[8], &eng->topo_buf[9], &eng->topo_buf[10], &eng->topo_buf[11],
                       &eng->topo_buf[12], &eng->topo_buf[13], &eng->topo_buf[14], &eng->U, &eng->H, &eng->status, &eng->smooth_scratch,
-                      &eng->stage[0], &eng->stage[1], &eng->dead, &eng->hmax, &eng->guard_buf});
+                      &eng->stage[0], &eng->stage[1], &eng->dead, &eng->hmax, &eng->guard_buf,
+                      &eng->tie_dev});
 }
 
 }  // namespace
@@ -775,10 +789,11 @@ int tsom_create(int device, uint32_t nodes, uint32_t dims, tsom_engine** out) {
         CU(eng->U.ensure(P * D * sizeof(double)));
         CU(eng->H.ensure(P * sizeof(double)));
         CU(eng->status.ensure(8 * sizeof(int)));
-        CU(eng->hmax.ensure(sizeof(double)));
-        CU(cudaMemsetAsync(eng->hmax.p, 0, sizeof(double), eng->stream));
+        CU(eng->hmax.ensure(tsom::kHmaxParts * sizeof(double)));
+        CU(cudaMemsetAsync(eng->hmax.p, 0, tsom::kHmaxParts * sizeof(double), eng->stream));
         CU(cudaMallocHost(&eng->hstat, 32 * sizeof(uint32_t)));
         CU(cudaMallocHost(&eng->tie_log, 2 * kTieLogCap * sizeof(uint32_t)));
+        CU(eng->tie_dev.ensure(kTieLogCap * sizeof(uint32_t)));
         std::memset(eng->hstat, 0, 32 * sizeof(uint32_t));
         ensure_rows(eng, 1);
         CU(cudaStreamSynchronize(eng->stream));
@@ -1663,9 +1678,7 @@ static void train_epoch_enqueue(Engine* eng, double eta, double sigma, double mo
     if (!(eng->infl_set && eng->infl_key == key)) {
         const double inv = 1.0 / (2.0 * sigma * sigma);
         tsom::launch_influence(eng->topo_dist.as<double>(), (size_t)eng->P * eng->P, inv,
-                               eng->infl.as<double>(), eng->stream);
-        tsom::launch_infl_absmax(eng->infl.as<double>(), (size_t)eng->P * eng->P,
-                                 eng->hmax.as<double>(), eng->stream);
+                               eng->infl.as<double>(), eng->stream, eng->hmax.as<double>());
         CU(cudaGetLastError());
         eng->infl_key = key;
         eng->infl_set = true;

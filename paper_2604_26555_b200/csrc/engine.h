@@ -305,6 +305,7 @@ struct Engine {
     // rows] pairs, pinned, read back asynchronously); their largest fraction
     // sizes the enumerate passes of later epochs (run_bmu)
     uint32_t* tie_log = nullptr;
+    DevBuf tie_dev;  // the counts themselves, written by k_tie_pass_counts
     uint32_t tie_log_n = 0;
     double tie_frac_max = -1.0;  // < 0: nothing observed yet
     bool hstat_counts = false;  // [0..1] hold this epoch's re-check counts
@@ -366,7 +367,9 @@ void launch_split_rows(int kind, const float* x, const uint32_t* sel, const uint
 bool tc_supported(int kind, uint32_t P, uint32_t D);
 size_t tc_wsplit_bytes(int kind, uint32_t P, uint32_t D);
 // scale = {s, s^2, overflow flag}: kTcF16 picks s = 2^e from max ||x||^2 (x2max[0])
-void launch_set_scale(int kind, const float* x2max, float* scale, cudaStream_t st);
+// zero[0..nzero) and *zero2 (optional) are cleared first: the counters of the pass
+void launch_set_scale(int kind, const float* x2max, float* scale, cudaStream_t st,
+                      uint32_t* zero = nullptr, uint32_t nzero = 0, uint32_t* zero2 = nullptr);
 // tcgen05 B operand of the codebook (per group, core-matrix order)
 void launch_prep_wsplit(int kind, const float* w, uint32_t P, uint32_t D, const float* scale,
                         void* wsplit, cudaStream_t st);
@@ -462,11 +465,29 @@ cudaError_t launch_term_guard(const float* x, uint32_t ldx, const uint32_t* sel,
                        uint32_t D, double eta, const float* x2max, const float* w2max,
                        const double* hmax, uint32_t tag, GuardScratch g, int sm_count,
                        cudaStream_t st, int* dead = nullptr, uint32_t epoch = 0);
-// max |h| of an influence matrix into *hmax (device double)
-void launch_infl_absmax(const double* infl, size_t n, double* hmax, cudaStream_t st);
+// max |h| of an influence matrix as kHmaxParts per-block maxima (no reset
+// needed: every block writes its slot; the guard folds them)
+constexpr unsigned kHmaxParts = 592;
+void launch_infl_absmax(const double* infl, size_t n, double* hpart, cudaStream_t st);
+// block-wide max of a non-negative double (NaN wins) into out[blockIdx.x]
+__device__ __forceinline__ void block_max_to(double m, double* out) {
+    __shared__ double s_bm[32];
+    for (int o = 16; o; o >>= 1) {
+        const double v = __shfl_xor_sync(0xffffffffu, m, o);
+        m = v > m || v != v ? v : m;
+    }
+    if ((threadIdx.x & 31) == 0) s_bm[threadIdx.x >> 5] = m;
+    __syncthreads();
+    if (threadIdx.x == 0) {
+        for (unsigned w = 1; w < (blockDim.x + 31) / 32; ++w)
+            m = s_bm[w] > m || s_bm[w] != s_bm[w] ? s_bm[w] : m;
+        out[blockIdx.x] = m;
+    }
+}
 // influence_matrix (topology.hpp:342-364) from a P x P distance matrix
+// (hpart: kHmaxParts per-block maxima of |h| for the term guard)
 void launch_influence(const double* dist, size_t n, double inv_two_sigma_sq, double* out,
-                      cudaStream_t st);
+                      cudaStream_t st, double* hpart);
 // synthetic Gaussian mixture rows
 void launch_synth_gmm(float* x, uint64_t n, uint32_t D, const float* centres, uint32_t n_comp,
                       uint64_t seed, uint64_t row_offset, cudaStream_t st, uint32_t ldx = 0);

@@ -105,7 +105,11 @@ bool tc_supported(int kind, uint32_t P, uint32_t D) {
 // scale[0] = s, scale[1] = s^2, scale[2] = overflow flag (bits), from max ||x||^2:
 // the largest power of two with max||x|| * s <= 16 (so |x_k s| <= 16 and
 // ||x s||^2 <= 256 fit FP16 with a 256x margin for ||w s||^2).
-__global__ void k_set_scale(int kind, const float* __restrict__ x2max, float* __restrict__ scale) {
+__global__ void k_set_scale(int kind, const float* __restrict__ x2max, float* __restrict__ scale,
+                            uint32_t* __restrict__ zero, uint32_t nzero, uint32_t* __restrict__ zero2) {
+    // the pass's counters start at zero (no separate memset launches)
+    for (uint32_t k = 0; k < nzero; ++k) zero[k] = 0u;
+    if (zero2) *zero2 = 0u;
     float s = 1.0f;
     if (kind == kTcF16) {
         const float m = *x2max;
@@ -121,8 +125,9 @@ __global__ void k_set_scale(int kind, const float* __restrict__ x2max, float* __
     scale[2] = 0.0f;
 }
 
-void launch_set_scale(int kind, const float* x2max, float* scale, cudaStream_t st) {
-    TSOM_LAUNCH(k_set_scale<<<1, 1, 0, st>>>(kind, x2max, scale));
+void launch_set_scale(int kind, const float* x2max, float* scale, cudaStream_t st, uint32_t* zero,
+                      uint32_t nzero, uint32_t* zero2) {
+    TSOM_LAUNCH(k_set_scale<<<1, 1, 0, st>>>(kind, x2max, scale, zero, nzero, zero2));
 }
 
 __device__ __forceinline__ float tf32_trunc(float v) {

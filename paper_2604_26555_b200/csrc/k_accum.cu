@@ -106,12 +106,14 @@ __global__ void __launch_bounds__(1024) k_nodescan(const uint32_t* __restrict__ 
                                                    uint32_t D, uint32_t* __restrict__ node_start,
                                                    uint32_t* __restrict__ piece_start,
                                                    uint32_t* __restrict__ piece_node,
-                                                   double* __restrict__ sums, int add_counts) {
+                                                   double* __restrict__ sums, int add_counts,
+                                                   int zero_dsum) {
     __shared__ uint32_t s_rows[1024], s_pcs[1024];
     __shared__ uint32_t carry_rows, carry_pcs;
     if (threadIdx.x == 0) {
         carry_rows = 0;
         carry_pcs = 0;
+        if (zero_dsum) sums[(size_t)P * D + P] = 0.0;  // no distances this pass
     }
     __syncthreads();
     for (uint32_t base = 0; base < P; base += 1024) {
@@ -171,6 +173,9 @@ __global__ void k_piece_nodes(const uint32_t* __restrict__ piece_start, uint32_t
 }
 
 // Stable scatter of positions into BMU order (ties in position order).
+// (Measured and reverted: ordering a block's 16384 positions by node in shared
+// memory first and writing node runs out whole — 125 us vs 79 us at 1e7 rows:
+// the larger block footprint halves the resident blocks.)
 __global__ void __launch_bounds__(kScatterWarps * 32) k_scatter(
     const uint32_t* __restrict__ bmu, uint64_t n, uint32_t P, const uint32_t* __restrict__ offs,
     const uint32_t* __restrict__ node_start, uint32_t* __restrict__ sorted) {
@@ -638,7 +643,8 @@ void launch_accumulate(const float* x, const uint32_t* sel, uint64_t n, uint32_t
     TSOM_LAUNCH(k_hist<<<nblk, 512, P * sizeof(uint32_t), st>>>(bmu, n, P, s.counts));
     TSOM_LAUNCH(k_colscan<<<(P + 31) / 32, 256, 0, st>>>(s.counts, nblk, P, s.totals));
     TSOM_LAUNCH(k_nodescan<<<1, 1024, 0, st>>>(s.totals, P, D, s.node_start, s.piece_start,
-                                               s.piece_node, sums, add));
+                                               s.piece_node, sums, add,
+                                               (!want_dist && first) ? 1 : 0));
     {
         const uint64_t pmax = accum_pieces_max(n, P);
         const unsigned pb = (unsigned)std::min<uint64_t>((pmax + 255) / 256, (uint64_t)sm_count * 4);
@@ -698,8 +704,6 @@ void launch_accumulate(const float* x, const uint32_t* sel, uint64_t n, uint32_t
             s.partial, s.piece_start, P, D, sums, add));
     if (want_dist)
         TSOM_LAUNCH(k_dist_reduce<<<1, 1024, 0, st>>>(s.partial, s.piece_start, P, D, sums, add));
-    else if (first)
-        cudaMemsetAsync(sums + (size_t)P * D + P, 0, sizeof(double), st);
     TSOM_LAUNCH(k_add_rowcount<<<1, 1, 0, st>>>(sums, P, D, (double)n, add));
 }
 

@@ -41,27 +41,38 @@ __device__ __forceinline__ float ord2f(uint32_t o) {
     return __uint_as_float((o & 0x80000000u) ? (o & 0x7FFFFFFFu) : ~o);
 }
 
+// the cheap bound, with max|h| folded from the kHmaxParts block maxima
+// (every block of the caller evaluates it identically)
 __device__ __forceinline__ bool cheap_bound_over(const float* x2max, const float* w2max,
-                                                 const double* hmax, double eta) {
-    const double h = *hmax;
+                                                 const double* hpart, double eta) {
+    __shared__ double s_h[32];
+    double h = 0.0;
+    for (unsigned k = threadIdx.x; k < kHmaxParts; k += blockDim.x) {
+        const double v = hpart[k];
+        h = v > h || v != v ? v : h;
+    }
+    for (int o = 16; o; o >>= 1) {
+        const double v = __shfl_xor_sync(0xffffffffu, h, o);
+        h = v > h || v != v ? v : h;
+    }
+    if ((threadIdx.x & 31) == 0) s_h[threadIdx.x >> 5] = h;
+    __syncthreads();
+    h = 0.0;
+    for (unsigned w = 0; w < (blockDim.x + 31) / 32; ++w) h = s_h[w] > h || s_h[w] != s_h[w] ? s_h[w] : h;
+    __syncthreads();
     const double bound = fabs(eta) * h * (sqrt((double)*x2max) + sqrt((double)*w2max));
-    return !(h < kTermLimit && bound < kTermLimit);
+    return !(h < kTermLimit && bound < kTermLimit);  // NaN anywhere: over
 }
 
-__global__ void k_infl_absmax(const double* __restrict__ infl, size_t n,
-                              unsigned long long* __restrict__ out) {
+__global__ void __launch_bounds__(256) k_infl_absmax(const double* __restrict__ infl, size_t n,
+                                                     double* __restrict__ hpart) {
     double m = 0.0;
     for (size_t i = blockIdx.x * (size_t)blockDim.x + threadIdx.x; i < n;
          i += (size_t)gridDim.x * blockDim.x) {
         const double a = fabs(infl[i]);
         m = a > m || a != a ? a : m;  // NaN wins (it fails every comparison the guard makes)
     }
-    for (int o = 16; o; o >>= 1) {
-        const double v = __shfl_xor_sync(0xffffffffu, m, o);
-        m = v > m || v != v ? v : m;
-    }
-    // non-negative doubles (and +NaN) order like their bit patterns
-    if ((threadIdx.x & 31) == 0) atomicMax(out, (unsigned long long)__double_as_longlong(m));
+    block_max_to(m, hpart);
 }
 
 // The flags carry the invocation's tag (a counter the host passes) instead of
@@ -136,11 +147,8 @@ __global__ void __launch_bounds__(256) k_term_guard(
 
 }  // namespace
 
-void launch_infl_absmax(const double* infl, size_t n, double* hmax, cudaStream_t st) {
-    cudaMemsetAsync(hmax, 0, sizeof(double), st);
-    const unsigned blocks = (unsigned)std::min<size_t>((n + 255) / 256, 148 * 4);
-    TSOM_LAUNCH(k_infl_absmax<<<blocks, 256, 0, st>>>(
-        infl, n, reinterpret_cast<unsigned long long*>(hmax)));
+void launch_infl_absmax(const double* infl, size_t n, double* hpart, cudaStream_t st) {
+    TSOM_LAUNCH(k_infl_absmax<<<kHmaxParts, 256, 0, st>>>(infl, n, hpart));
 }
 
 cudaError_t launch_term_guard(const float* x, uint32_t ldx, const uint32_t* sel, uint64_t n,

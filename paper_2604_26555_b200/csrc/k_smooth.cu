@@ -211,18 +211,25 @@ void launch_status_reset(int* status, cudaStream_t st) {
 }
 
 // influence_matrix (topology.hpp:342-364): z = (d*d)*inv, h = z > 57.6 ? 0 : exp(-z)
-__global__ void k_influence(const double* __restrict__ dist, size_t n, double inv,
-                            double* __restrict__ out) {
-    const size_t i = blockIdx.x * (size_t)blockDim.x + threadIdx.x;
-    if (i >= n) return;
-    const double d = dist[i];
-    const double z = __dmul_rn(__dmul_rn(d, d), inv);
-    out[i] = z > 57.6 ? 0.0 : exp(-z);
+// (also the per-block maxima of |h| the term guard reduces: hpart[kHmaxParts])
+__global__ void __launch_bounds__(256) k_influence(const double* __restrict__ dist, size_t n,
+                                                   double inv, double* __restrict__ out,
+                                                   double* __restrict__ hpart) {
+    double m = 0.0;
+    for (size_t i = blockIdx.x * (size_t)blockDim.x + threadIdx.x; i < n;
+         i += (size_t)gridDim.x * blockDim.x) {
+        const double d = dist[i];
+        const double z = __dmul_rn(__dmul_rn(d, d), inv);
+        const double h = z > 57.6 ? 0.0 : exp(-z);
+        out[i] = h;
+        m = h > m || h != h ? h : m;
+    }
+    block_max_to(m, hpart);
 }
 
 void launch_influence(const double* dist, size_t n, double inv_two_sigma_sq, double* out,
-                      cudaStream_t st) {
-    TSOM_LAUNCH(k_influence<<<(unsigned)((n + 255) / 256), 256, 0, st>>>(dist, n, inv_two_sigma_sq, out));
+                      cudaStream_t st, double* hpart) {
+    TSOM_LAUNCH(k_influence<<<kHmaxParts, 256, 0, st>>>(dist, n, inv_two_sigma_sq, out, hpart));
 }
 
 // Synthetic Gaussian mixture: component and unit normal noise
