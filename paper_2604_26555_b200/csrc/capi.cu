@@ -199,6 +199,7 @@ __global__ void k_tie_pass_counts(const uint32_t* __restrict__ count, uint64_t c
 // scale of this same x2max (or nullptr to build them here).
 void run_bmu(Engine* eng, const float* x, uint32_t ldx, const uint32_t* sel, uint64_t n,
              const float* x2max, const void* tiles, const float* tiles_xn2) {
+    tsom::NvtxRange nv("tsom.bmu");
     const float* xsrc = x;
     const int kind = tc_kind(eng);
     if (n == 0 || kind == tsom::kTcNone)
@@ -374,6 +375,7 @@ void alloc_resident(Engine* eng, uint64_t n_rows) {
 // at the 256-B stride from a packed device stage) runs on the engine stream
 // while the next chunk is in flight.
 void upload_resident(Engine* eng, uint64_t total, uint64_t C) {
+    tsom::NvtxRange nv("tsom.bind_upload");
     alloc_resident(eng, total);
     const bool pad = eng->ldx != eng->D;
     const uint64_t rowb = (uint64_t)eng->D * sizeof(float);
@@ -431,6 +433,7 @@ void ensure_accum(Engine* eng, uint64_t rows) {
 // already in device memory (the device sampler's), used instead of sel_host.
 void accumulate_epoch(Engine* eng, const uint32_t* sel_host, uint64_t n_sel, bool want_dist,
                       bool want_dsum, bool accumulate, const uint32_t* dev_sel = nullptr) {
+    tsom::NvtxRange nv("tsom.pass");
     CU(eng->sums.ensure(slot_len(eng) * sizeof(double)));
     const uint32_t* sel = dev_sel;
     if (!dev_sel) {
@@ -575,6 +578,7 @@ void accumulate_epoch(Engine* eng, const uint32_t* sel_host, uint64_t n_sel, boo
     // the one reduce of the epoch (parallel.hpp:90-95): [S | c | sum dist | rows]
     // summed over the ranks, identical on every rank afterwards
     if (eng->comm_reduce && (accumulate || want_dsum)) {
+        tsom::NvtxRange nvr("tsom.reduce");
         const int rc = eng->comm_reduce(eng->sums.p, slot_len(eng), 3);
         if (rc != TSOM_OK) throw tsom::Fail{rc};
     }
@@ -604,6 +608,7 @@ void abort_comm(Engine* eng) {
 // of the wait), else the communicator is aborted and the call fails with
 // TSOM_ERR_TIMEOUT instead of hanging on a dead peer.
 void wait_stream(Engine* eng) {
+    tsom::NvtxRange nv("tsom.wait");
     if (!eng->nccl_comm || eng->red_pending == 0) {
         eng->red_pending = 0;
         CU(cudaStreamSynchronize(eng->stream));
@@ -702,6 +707,7 @@ void finish_recheck(Engine* eng) {
 }
 
 void smooth(Engine* eng, double eta) {
+    tsom::NvtxRange nv("tsom.smooth");
     CU(eng->smooth_scratch.ensure(tsom::smooth_scratch_doubles(eng->P, eng->D) * sizeof(double)));
     tsom::launch_smooth(eng->infl.as<double>(), eng->sums.as<double>(), eng->w.as<float>(), eng->P,
                         eng->D, eta, eng->U.as<double>(), eng->H.as<double>(),
@@ -1298,6 +1304,7 @@ int tsom_refresh_topology(tsom_engine* eng, int kind, uint32_t* edges_out, uint6
                           uint64_t* n_edges, uint16_t* hops_out) {
     return guarded(eng, [&] {
         CU(cudaSetDevice(eng->device));
+        tsom::NvtxRange nv("tsom.refresh_topology");
         REQUIRE(kind == 2 || kind == 3, TSOM_ERR_INVALID,
                 "refresh_topology: kind must be 2 (mst) or 3 (rng)");
         REQUIRE(eng->codebook_set, TSOM_ERR_INVALID, "engine: codebook not set (tsom_set_codebook)");
@@ -1353,6 +1360,7 @@ namespace {
 // run the device sampler; true = identity selection (all rows), else the
 // selection is in eng->sampler.sel (device), m rows
 bool sampler_pick(Engine* eng, uint64_t* m) {
+    tsom::NvtxRange nv("tsom.sampler_select");
     tsom::SamplerState& smp = eng->sampler;
     REQUIRE(smp.n == eng->n_rows, TSOM_ERR_INVALID,
             "sampler: bound data changed since tsom_sampler_init");
@@ -1668,6 +1676,7 @@ int tsom_release_cached_memory(int device) {
 // without waiting for it; dead (optional): the multi-epoch failure record.
 static void train_epoch_enqueue(Engine* eng, double eta, double sigma, double momentum, uint32_t flags,
                          int* dead, uint32_t epoch) {
+    tsom::NvtxRange nv("tsom.train_epoch");
     CU(cudaSetDevice(eng->device));
     REQUIRE(eng->topo_set, TSOM_ERR_INVALID, "train_epoch: topology distance not set");
     REQUIRE(sigma > 0.0, TSOM_ERR_INVALID, "influence_matrix: sigma must be > 0");

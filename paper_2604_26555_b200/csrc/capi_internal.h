@@ -4,6 +4,7 @@
 #pragma once
 
 #include <cuda_runtime.h>
+#include <nvtx3/nvToolsExt.h>
 
 #include <cstdint>
 #include <string>
@@ -12,6 +13,15 @@
 #include "tsom_b200.h"
 
 namespace tsom {
+
+// NVTX range over a host-side phase (enqueue of an epoch's steps, binds,
+// refreshes); header-only NVTX 3, free when no tool is attached
+struct NvtxRange {
+    explicit NvtxRange(const char* name) { nvtxRangePushA(name); }
+    ~NvtxRange() { nvtxRangePop(); }
+    NvtxRange(const NvtxRange&) = delete;
+    NvtxRange& operator=(const NvtxRange&) = delete;
+};
 
 // a failed CU / REQUIRE inside a guarded call: the status it returns
 struct Fail {

@@ -271,29 +271,40 @@ __global__ void __launch_bounds__(256) k_bfs_all(const uint32_t* __restrict__ de
                                                  uint16_t* __restrict__ hops,
                                                  double* __restrict__ hopd,
                                                  uint32_t* __restrict__ status) {
-    extern __shared__ uint16_t dist_s[];  // [P]
-    __shared__ int grew;
+    // dist_s[P] (u16), then the next-frontier bitmap mark_s[ceil(P/32)] (u32).
+    // Level-synchronous: phase A only reads distances and sets bits of the
+    // unvisited neighbours (atomicOr), phase B lets the owner thread of each
+    // bitmap word assign level + 1 and clear the word — no shared location is
+    // written by two threads without an atomic (racecheck-clean).
+    extern __shared__ uint16_t dist_s[];
+    uint32_t* mark_s = reinterpret_cast<uint32_t*>(dist_s + ((P + 1) & ~1u));
+    const uint32_t words = (P + 31) / 32;
     const uint32_t src = blockIdx.x;
-    for (uint32_t i = threadIdx.x; i < P; i += blockDim.x) dist_s[i] = 0xFFFFu;
-    __syncthreads();
-    if (threadIdx.x == 0) dist_s[src] = 0;
+    for (uint32_t i = threadIdx.x; i < P; i += blockDim.x) dist_s[i] = i == src ? 0 : 0xFFFFu;
+    for (uint32_t i = threadIdx.x; i < words; i += blockDim.x) mark_s[i] = 0u;
     __syncthreads();
     for (uint32_t level = 0;; ++level) {
-        if (threadIdx.x == 0) grew = 0;
-        __syncthreads();
         for (uint32_t v = threadIdx.x; v < P; v += blockDim.x) {
             if (dist_s[v] != level) continue;
             for (uint32_t e = deg[v]; e < deg[v + 1]; ++e) {
                 const uint32_t u = adj[e];
-                if (dist_s[u] == 0xFFFFu) {
-                    dist_s[u] = (uint16_t)(level + 1);  // benign race: same value
-                    grew = 1;
-                }
+                if (dist_s[u] == 0xFFFFu) atomicOr(&mark_s[u >> 5], 1u << (u & 31));
             }
         }
         __syncthreads();
-        if (!grew) break;
-        __syncthreads();
+        int grew = 0;
+        for (uint32_t wd = threadIdx.x; wd < words; wd += blockDim.x) {
+            uint32_t m = mark_s[wd];
+            if (!m) continue;
+            mark_s[wd] = 0u;
+            grew = 1;
+            while (m) {
+                const uint32_t bit = __ffs(m) - 1;
+                m &= m - 1;
+                dist_s[wd * 32 + bit] = (uint16_t)(level + 1);
+            }
+        }
+        if (!__syncthreads_or(grew)) break;
     }
     for (uint32_t i = threadIdx.x; i < P; i += blockDim.x) {
         const uint16_t h = dist_s[i];
@@ -331,7 +342,7 @@ int launch_refresh_topology(const float* w, uint32_t P, uint32_t D, int kind, To
     TSOM_LAUNCH(k_rng_rowcount<<<(P + 255) / 256, 256, 0, st>>>(s.keep, P, s.rowcnt));
     TSOM_LAUNCH(k_rng_emit<<<1, 1024, 0, st>>>(s.keep, P, s.rowcnt, s.edges, s.ne));
     TSOM_LAUNCH(k_build_csr<<<1, 1024, 0, st>>>(s.edges, s.ne, P, s.deg, s.adj, s.status));
-    const size_t bsm = (size_t)P * sizeof(uint16_t);
+    const size_t bsm = (size_t)((P + 1) & ~1u) * sizeof(uint16_t) + (size_t)(P + 31) / 32 * 4;
     if (bsm > 48 * 1024) cudaFuncSetAttribute(k_bfs_all, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)bsm);
     TSOM_LAUNCH(k_bfs_all<<<P, 256, bsm, st>>>(s.deg, s.adj, P, s.hops, s.hopd, s.status));
     return 0;
