@@ -679,10 +679,12 @@ def leg_c3(args, ctx):
         e.set_codebook(w0)
         graph_epochs(e, "mst", 2)  # warm-up
         e.set_codebook(w0)
-        secs, marks = timed(lambda: graph_epochs(e, "mst", epochs), ctx, e)
+        with ClockSampler(ctx["local"]) as clk:
+            secs, marks = timed(lambda: graph_epochs(e, "mst", epochs), ctx, e)
         s, c = e.qe()
         rs, _ = timed(lambda: e.refresh_topology("mst"), ctx, e)
         return secs, {"ms_per_epoch": secs * 1e3 / epochs, "refresh_epochs": marks,
+                      "clocks": clk.summary(),
                       "refresh_ms": rs * 1e3,
                       "qe_after": s / c, "engine_bytes": e.device_bytes,
                       "device_used_gb": hbm_used_gb(local)}
@@ -748,8 +750,10 @@ def leg_c5(args, ctx):
     e.set_topology_distance(topo)
     e.train_epochs(etas[:2], sigmas[:2])
     e.set_codebook(w0)
-    secs, _ = timed(lambda: e.train_epochs(etas, sigmas), ctx, e)
+    with ClockSampler(local) as clk:
+        secs, _ = timed(lambda: e.train_epochs(etas, sigmas), ctx, e)
     out["resident"] = {"value": n * epochs / secs, "ms_per_epoch": secs * 1e3 / epochs,
+                       "clocks": clk.summary(),
                        "engine_bytes": e.device_bytes,
                        "bytes_per_row": round(e.device_bytes / n, 1),
                        "device_used_gb": hbm_used_gb(local)}
