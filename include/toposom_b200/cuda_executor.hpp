@@ -83,6 +83,9 @@ struct CudaOptions {
     Distances distances = Distances::always;
     int bmu_kernel = 0;               // 0 auto (tcgen05), 1 SIMT, 2 tcgen05
     double barrier_timeout_s = toposom::kDefaultBarrierTimeoutS;  // parallel.hpp:24
+    // exact sums (TSOM_OPT_DETERMINISTIC): results bit-identical for any number
+    // of engines, like the reference's for any worker count (parallel.hpp:17-21)
+    bool exact = false;
 };
 
 /// G engines joined by an in-process rank group (tsom_group_*): each owns
@@ -112,6 +115,7 @@ public:
                 e.check(tsom_set_option(e.h, TSOM_OPT_BMU_KERNEL, opts.bmu_kernel));
             e.check(tsom_set_option(e.h, TSOM_OPT_BARRIER_TIMEOUT_MS,
                                     std::max<std::int64_t>(1, std::llround(opts.barrier_timeout_s * 1e3))));
+            if (opts.exact) e.check(tsom_set_option(e.h, TSOM_OPT_DETERMINISTIC, 1));
             if (group_) e.check(tsom_group_join(e.h, group_, static_cast<int>(g)));
         }
         const std::uint32_t flags = opts.streamed ? TSOM_BIND_STREAMED : TSOM_BIND_COPY;

@@ -57,7 +57,14 @@ extern "C" {
                                       3 = tcgen05 3xFP16 (d <= 62); auto = 3, else 2, else 1 */
 #define TSOM_OPT_TIE_TAU 2         /* value*2^-30: relative tie window for the exact re-check */
 #define TSOM_OPT_STREAM_CHUNK 3    /* rows per streamed chunk */
-#define TSOM_OPT_DETERMINISTIC 4   /* reserved */
+#define TSOM_OPT_DETERMINISTIC 4   /* 1 = exact sums: every row's features and distance on
+                                      fixed-point grids set by the data's global bounds, summed
+                                      in int64 limbs and reduced as integers, so an epoch's
+                                      results are bit-identical for any rank count, chunking or
+                                      selection order (the reference's guarantee,
+                                      accum.hpp:12-20; parallel.hpp:17-21).  Resident rows,
+                                      d even and <= 62.  Default 0: FP64 sums (they agree to
+                                      summation order) */
 #define TSOM_OPT_HOST_REGISTER 5   /* streamed host rows: 1 (default) page-lock the caller's
                                       buffer for direct DMA, 0 copy through pinned staging */
 #define TSOM_OPT_STAGING_THREADS 6 /* host threads filling the pinned staging (default: min(16, cores)) */

@@ -28,6 +28,7 @@ TSOM_BIND_STREAMED = 1
 TSOM_OPT_BMU_KERNEL = 1
 TSOM_OPT_TIE_TAU = 2
 TSOM_OPT_STREAM_CHUNK = 3
+TSOM_OPT_DETERMINISTIC = 4
 TSOM_OPT_HOST_REGISTER = 5
 TSOM_OPT_STAGING_THREADS = 6
 TSOM_OPT_BARRIER_TIMEOUT_MS = 7

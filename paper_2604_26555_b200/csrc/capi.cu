@@ -426,6 +426,31 @@ void ensure_accum(Engine* eng, uint64_t rows) {
     eng->acc_rows = rows;
 }
 
+// Exact mode: the global max ||x||^2 (once per bind; a u64 max over the ranks
+// of the float's bits — non-negative floats order like their bits) and the
+// limb buffer; returns the ExactSums of this engine.
+tsom::ExactSums exact_setup(Engine* eng) {
+    REQUIRE(!eng->streamed, TSOM_ERR_INVALID,
+            "exact mode (TSOM_OPT_DETERMINISTIC) needs resident rows");
+    CU(eng->xsums.ensure(tsom::exact_sums_words(eng->P, eng->D) * sizeof(long long)));
+    CU(eng->xmax_g.ensure(sizeof(uint64_t)));
+    if (!eng->xmax_g_ready) {
+        CU(cudaMemsetAsync(eng->xmax_g.p, 0, sizeof(uint64_t), eng->stream));
+        CU(cudaMemcpyAsync(eng->xmax_g.p, eng->x2max.p, sizeof(float), cudaMemcpyDeviceToDevice,
+                           eng->stream));
+        if (eng->comm_reduce) {
+            const int rc = eng->comm_reduce(eng->xmax_g.p, 1, 1);
+            if (rc != TSOM_OK) throw tsom::Fail{rc};
+        }
+        eng->xmax_g_ready = true;
+    }
+    tsom::ExactSums ex;
+    ex.xs = eng->xsums.as<long long>();
+    ex.xmax2 = eng->xmax_g.as<float>();
+    ex.w2max = eng->w2max.as<float>();
+    return ex;
+}
+
 // One pass over the bound rows (resident or streamed): BMU search, then K2
 // into sums = [R | c | sum dist | rows] (+ allreduce).  want_dist: per-row
 // distances into eng->dist; want_dsum: distance sum; accumulate: R and c.
@@ -474,6 +499,8 @@ void accumulate_epoch(Engine* eng, const uint32_t* sel_host, uint64_t n_sel, boo
             tiles = eng->xsplit.p;
             tiles_xn2 = eng->xn2.as<float>();
         }
+        tsom::ExactSums ex;
+        if (eng->exact) ex = exact_setup(eng);
         run_bmu(eng, eng->x.as<float>(), eng->ldx, dsel, n, eng->x2max.as<float>(), tiles,
                 tiles_xn2);
         eng->pass_x = eng->x.as<float>();
@@ -482,11 +509,13 @@ void accumulate_epoch(Engine* eng, const uint32_t* sel_host, uint64_t n_sel, boo
         eng->pass_n = n;
         CU(cudaEventRecord(eng->ev[1], eng->stream));
         ensure_accum(eng, n);
-        tsom::launch_accumulate(eng->x.as<float>(), dsel, n, eng->D, eng->w.as<float>(), eng->P,
-                                eng->bmu.as<uint32_t>(),
-                                want_dist ? eng->dist.as<double>() : nullptr, want_dsum,
-                                accumulate, true, eng->acc, eng->sums.as<double>(), eng->sm_count,
-                                eng->stream, eng->x_slack, eng->ldx);
+        const int arc = tsom::launch_accumulate(
+            eng->x.as<float>(), dsel, n, eng->D, eng->w.as<float>(), eng->P,
+            eng->bmu.as<uint32_t>(), want_dist ? eng->dist.as<double>() : nullptr, want_dsum,
+            accumulate, true, eng->acc, eng->sums.as<double>(), eng->sm_count, eng->stream,
+            eng->x_slack, eng->ldx, eng->exact ? &ex : nullptr);
+        REQUIRE(arc == 0, TSOM_ERR_INVALID,
+                "exact mode (TSOM_OPT_DETERMINISTIC) needs d even and <= 62 with resident rows");
         CU(cudaGetLastError());
         eng->chunk_counts.clear();
         eng->recheck_from_chunks = true;
@@ -499,6 +528,8 @@ void accumulate_epoch(Engine* eng, const uint32_t* sel_host, uint64_t n_sel, boo
         eng->pass_x = nullptr;
         eng->pass_sel = nullptr;
         eng->pass_n = 0;
+        REQUIRE(!eng->exact, TSOM_ERR_INVALID,
+                "exact mode (TSOM_OPT_DETERMINISTIC) needs resident rows");
         const uint64_t C = eng->stream_chunk_rows;
         CU(eng->stage[0].ensure(C * eng->D * sizeof(float) + tsom::kRowSlack));
         CU(eng->stage[1].ensure(C * eng->D * sizeof(float) + tsom::kRowSlack));
@@ -577,7 +608,21 @@ void accumulate_epoch(Engine* eng, const uint32_t* sel_host, uint64_t n_sel, boo
     CU(cudaGetLastError());
     // the one reduce of the epoch (parallel.hpp:90-95): [S | c | sum dist | rows]
     // summed over the ranks, identical on every rank afterwards
-    if (eng->comm_reduce && (accumulate || want_dsum)) {
+    if (eng->exact && !eng->streamed) {
+        // exact sums: the one reduce is an int64 sum of the limb buffer, then
+        // the f64 sums are rebuilt from it (the same on every rank)
+        if (eng->comm_reduce && (accumulate || want_dsum)) {
+            tsom::NvtxRange nvr("tsom.reduce");
+            const int rc = eng->comm_reduce(eng->xsums.p, tsom::exact_sums_words(eng->P, eng->D), 4);
+            if (rc != TSOM_OK) throw tsom::Fail{rc};
+        }
+        tsom::ExactSums ex;
+        ex.xs = eng->xsums.as<long long>();
+        ex.xmax2 = eng->xmax_g.as<float>();
+        ex.w2max = eng->w2max.as<float>();
+        tsom::launch_exact_unpack(ex, eng->P, eng->D, eng->sums.as<double>(), eng->stream);
+        CU(cudaGetLastError());
+    } else if (eng->comm_reduce && (accumulate || want_dsum)) {
         tsom::NvtxRange nvr("tsom.reduce");
         const int rc = eng->comm_reduce(eng->sums.p, slot_len(eng), 3);
         if (rc != TSOM_OK) throw tsom::Fail{rc};
@@ -742,7 +787,7 @@ std::vector<DevBuf*> all_buffers(Engine* eng) {
                       &eng->topo_buf[8], &eng->topo_buf[9], &eng->topo_buf[10], &eng->topo_buf[11],
                       &eng->topo_buf[12], &eng->topo_buf[13], &eng->topo_buf[14], &eng->U, &eng->H, &eng->status, &eng->smooth_scratch,
                       &eng->stage[0], &eng->stage[1], &eng->dead, &eng->hmax, &eng->guard_buf,
-                      &eng->tie_dev});
+                      &eng->tie_dev, &eng->xsums, &eng->xmax_g});
 }
 
 }  // namespace
@@ -882,6 +927,10 @@ int tsom_set_option(tsom_engine* eng, int key, int64_t value) {
                 REQUIRE(value >= 1, TSOM_ERR_INVALID, "option: barrier timeout >= 1 ms");
                 eng->barrier_timeout_s = (double)value / 1000.0;
                 break;
+            case TSOM_OPT_DETERMINISTIC:
+                eng->exact = value != 0;
+                eng->xmax_g_ready = false;
+                break;
             case TSOM_OPT_PAD_ROWS:
                 eng->pad_rows = value != 0;
                 break;
@@ -908,6 +957,7 @@ int tsom_bind_host_data(tsom_engine* eng, const float* rows, uint64_t n_rows, ui
         eng->host_direct = false;
         close_shards(eng);
         eng->xsplit_valid = false;
+        eng->xmax_g_ready = false;
         eng->n_rows = n_rows;
         cudaPointerAttributes pa{};
         const bool pinned = n_rows && cudaPointerGetAttributes(&pa, rows) == cudaSuccess &&
@@ -1000,6 +1050,7 @@ int tsom_bind_shards(tsom_engine* eng, const char* const* paths, uint32_t n_path
         REQUIRE(total < (1ull << 32), TSOM_ERR_INVALID, "bind: row ids are uint32 (n < 2^32)");
         eng->n_rows = total;
         eng->xsplit_valid = false;
+        eng->xmax_g_ready = false;
         if (flags & TSOM_BIND_STREAMED) {
             eng->streamed = true;
             eng->x.release();
@@ -1051,6 +1102,7 @@ int tsom_bind_device_data(tsom_engine* eng, const float* d_rows, uint64_t n_rows
         eng->n_rows = n_rows;
         eng->streamed = false;
         eng->xsplit_valid = false;
+        eng->xmax_g_ready = false;
         tsom::launch_row_norm_max(d_rows, n_rows, eng->D, eng->x2max.as<float>(), eng->stream);
         CU(cudaGetLastError());
         CU(cudaStreamSynchronize(eng->stream));
@@ -1081,6 +1133,7 @@ int tsom_bind_synthetic_gmm(tsom_engine* eng, uint64_t n_rows, uint64_t seed, ui
         CU(cudaGetLastError());
         eng->streamed = false;
         eng->xsplit_valid = false;
+        eng->xmax_g_ready = false;
         tsom::launch_row_norm_max(eng->x.as<float>(), n_rows, eng->D, eng->x2max.as<float>(),
                                   eng->stream, true, eng->ldx);
         CU(cudaStreamSynchronize(eng->stream));
@@ -1449,6 +1502,7 @@ struct LoopbackGroup {
                 case 0: fold<uint32_t>(count, [](uint32_t a, uint32_t b) { return a + b; }); break;
                 case 1: fold<uint64_t>(count, [](uint64_t a, uint64_t b) { return a > b ? a : b; }); break;
                 case 2: fold<uint64_t>(count, [](uint64_t a, uint64_t b) { return a + b; }); break;
+                case 4: fold<int64_t>(count, [](int64_t a, int64_t b) { return a + b; }); break;
                 default: fold<double>(count, [](double a, double b) { return a + b; }); break;
             }
             arrived = 0;
@@ -1902,7 +1956,7 @@ int tsom_comm_init(tsom_engine* eng, const uint8_t id[128], int rank, int world)
         eng->world = world;
         eng->comm_reduce = [eng, comm](void* buf, size_t count, int op) -> int {
             const ncclDataType_t t =
-                op == 0 ? ncclUint32 : (op == 3 ? ncclFloat64 : ncclUint64);
+                op == 0 ? ncclUint32 : (op == 3 ? ncclFloat64 : (op == 4 ? ncclInt64 : ncclUint64));
             const ncclRedOp_t o = op == 1 ? ncclMax : ncclSum;
             ncclResult_t rr = g_nccl.allReduce(buf, buf, count, t, o, comm, eng->stream);
             // a non-blocking communicator may still be enqueueing the call

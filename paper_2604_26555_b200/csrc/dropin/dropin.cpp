@@ -135,6 +135,7 @@ static void run_train(const dropin_config* rc, const DataSourceRef& src, float* 
         if (engines > 1) opts.devices.assign(engines, device);
         // bits 12-27: reduce-barrier timeout in ms (0 = the reference's 60 s)
         if ((flags >> 12) & 0xFFFFu) opts.barrier_timeout_s = ((flags >> 12) & 0xFFFFu) / 1000.0;
+        opts.exact = (flags >> 28) & 1u;  // bit 28: exact sums
         TrainOptions to;
         to.log_qe = qe_log != nullptr;
         const auto t0 = std::chrono::steady_clock::now();

@@ -225,6 +225,11 @@ struct Engine {
     DevBuf x;           // resident rows, row stride ldx floats
     uint32_t ldx = 0;   // D (packed), or kPadFloats: each row on its own two 128-B lines
     bool pad_rows = true;  // TSOM_OPT_PAD_ROWS
+    // TSOM_OPT_DETERMINISTIC: exact (order-independent) sums, k_accum.cu
+    bool exact = false;
+    DevBuf xsums;         // exact_sums_words int64: the epoch's reduce buffer in exact mode
+    DevBuf xmax_g;        // max ||x||^2 over all ranks' rows (float; u64 slot for the reduce)
+    bool xmax_g_ready = false;
     uint64_t n_rows = 0;
     bool x_slack = false;  // kRowSlack bytes readable after the last resident row
     bool streamed = false;
@@ -331,7 +336,7 @@ struct Engine {
     int rank = 0, world = 1;
     // The reduce step of an epoch (and of the sharded sampler): the NCCL
     // communicator, or (tests) an in-process loopback group of engines.
-    // op 0 = u32 sum, 1 = u64 max, 2 = u64 sum, 3 = f64 sum, in place on the
+    // op 0 = u32 sum, 1 = u64 max, 2 = u64 sum, 3 = f64 sum, 4 = i64 sum, in place on the
     // device buffer; returns a TSOM status with last_error set on failure.
     std::function<int(void*, size_t, int)> comm_reduce;
     // collect_with_barrier's deadline (parallel.hpp:24, 67-86): a rank that
@@ -418,11 +423,36 @@ void launch_rescan(const float* x, uint32_t ldx, const uint32_t* sel, const floa
 void accum_scratch_bytes(uint64_t n, uint32_t P, uint32_t D, size_t out[7]);
 // sums = [R (P*d) | c (P) | sum dist | rows]; first=false adds to it (streamed chunks).
 // accumulate=false -> distances / distance sum only (QE, find_bmus).
-void launch_accumulate(const float* x, const uint32_t* sel, uint64_t n, uint32_t D,
+// Exact mode (TSOM_OPT_DETERMINISTIC): the epoch's sums on fixed-point grids
+// given by the data's global bounds, in int64 limbs — independent of chunks,
+// pieces and ranks (k_accum.cu).  xs: exact_sums_words(P, D) int64 =
+// [S limbs (3 P d) | sum-dist limbs (3) | counts (P) | rows (1)]; the one
+// reduce is an int64 sum of it; launch_exact_unpack writes the f64 sums.
+struct ExactSums {
+    long long* xs = nullptr;
+    const float* xmax2 = nullptr;  // max ||x||^2 over every rank's rows
+    const float* w2max = nullptr;  // max ||w||^2 of the epoch's codebook
+};
+// the grids: x values at 2^L with max|x| 2^L <= 2^53 (<= 256 rows a piece stay
+// below 2^61), distances at the scale of max||x|| + max||w|| the same way
+__host__ __device__ inline void exact_scales(const float* xmax2, const float* w2max, double* sx,
+                                             double* sd) {
+    const double xm = sqrt((double)*xmax2), dm = xm + sqrt((double)*w2max);
+    const int ex = xm > 0.0 ? ilogb(xm) + 1 : 0;
+    const int ed = dm > 0.0 ? ilogb(dm) + 1 : 0;
+    *sx = ldexp(1.0, 53 - (ex < -900 ? -900 : ex));
+    *sd = ldexp(1.0, 53 - (ed < -900 ? -900 : ed));
+}
+size_t exact_sums_words(uint32_t P, uint32_t D);
+void launch_exact_unpack(const ExactSums& ex, uint32_t P, uint32_t D, double* sums,
+                         cudaStream_t st);
+// returns 1 when `exact` is asked for on a path without the TMA gather, else 0
+int launch_accumulate(const float* x, const uint32_t* sel, uint64_t n, uint32_t D,
                        const float* w, uint32_t P, const uint32_t* bmu, double* dist_out,
                        bool want_dist_sum, bool accumulate, bool first, const AccumScratch& s,
                        double* sums, int sm_count, cudaStream_t st, bool x_slack = false,
-                       uint32_t ldx = 0);  // row stride in floats (0: D; kPadFloats: padded rows)
+                       uint32_t ldx = 0,  // row stride in floats (0: D; kPadFloats: padded rows)
+                       const ExactSums* exact = nullptr);
 // resident rows at a 256-byte stride (kPadFloats floats per row, zero tail):
 // the K2 gather's rows are then exactly two 128-byte lines
 constexpr uint32_t kPadFloats = 64;

@@ -418,13 +418,18 @@ __global__ void __launch_bounds__(kAsyncWarps * 32, 2) k_gather_async(
 // may extend up to 8 bytes past it).
 constexpr int kTmaWarps = 8;
 
+// kExact: every feature value and distance is put on a fixed-point grid fixed
+// by the data's global bounds (exact_scales) and summed in int64 — exact and so
+// order-independent: the sums do not depend on pieces, chunks or ranks.
+template <bool kExact>
 __global__ void __launch_bounds__(kTmaWarps * 32, 2) k_gather_tma(
     const float* __restrict__ x, uint32_t ldx, const uint32_t* __restrict__ sel,
     const float* __restrict__ w, uint32_t P, uint32_t D, uint32_t slot,
     const uint32_t* __restrict__ sorted,
     const uint32_t* __restrict__ node_start, const uint32_t* __restrict__ piece_start,
     const uint32_t* __restrict__ piece_node, double* __restrict__ partial,
-    double* __restrict__ dist_out, int want_dist, int accumulate) {
+    double* __restrict__ dist_out, int want_dist, int accumulate,
+    const float* __restrict__ xmax2, const float* __restrict__ w2max) {
     extern __shared__ __align__(128) uint8_t tsm[];
     __shared__ __align__(8) uint64_t bars[kTmaWarps][2];
     __shared__ double wsm[kTmaWarps][64];  // w_b in FP64 for the distance pass (d <= 64)
@@ -443,6 +448,8 @@ __global__ void __launch_bounds__(kTmaWarps * 32, 2) k_gather_tma(
     const bool oka = ka < D, okb = kb < D;
     const uint32_t rowb = D * 4;                 // bytes of a row
     const uint64_t strideb = (uint64_t)ldx * 4;  // bytes between rows (D, or 64 padded)
+    double sx = 0.0, sd = 0.0;
+    if (kExact) exact_scales(xmax2, w2max, &sx, &sd);
 
     // copy window of this lane's row; returns the bytes it will deliver
     auto issue = [&](uint64_t row, uint32_t nrows, int s, uint32_t& offmask) {
@@ -481,6 +488,7 @@ __global__ void __launch_bounds__(kTmaWarps * 32, 2) k_gather_tma(
             __syncwarp();
         }
         double a0 = 0.0, a1 = 0.0, c0 = 0.0, c1 = 0.0, ds = 0.0;
+        long long qa0 = 0, qa1 = 0, qc0 = 0, qc1 = 0, qds = 0;
         uint32_t offm[2];
         issue(rowid[0], min(32u, r1 - r0), 0, offm[0]);
 #pragma unroll
@@ -503,16 +511,28 @@ __global__ void __launch_bounds__(kTmaWarps * 32, 2) k_gather_tma(
                         v = *reinterpret_cast<const float2*>(bm + (j + 1) * slot +
                                                              ((om >> (j + 1)) & 1u) * 8);
                     }
-                    a0 += (double)u.x;
-                    a1 += (double)u.y;
-                    c0 += (double)v.x;
-                    c1 += (double)v.y;
+                    if (kExact) {
+                        qa0 += __double2ll_rn((double)u.x * sx);
+                        qa1 += __double2ll_rn((double)u.y * sx);
+                        qc0 += __double2ll_rn((double)v.x * sx);
+                        qc1 += __double2ll_rn((double)v.y * sx);
+                    } else {
+                        a0 += (double)u.x;
+                        a1 += (double)u.y;
+                        c0 += (double)v.x;
+                        c1 += (double)v.y;
+                    }
                 }
                 if (j < rows_m && okb) {
                     const float2 u =
                         *reinterpret_cast<const float2*>(bm + j * slot + ((om >> j) & 1u) * 8);
-                    a0 += (double)u.x;
-                    a1 += (double)u.y;
+                    if (kExact) {
+                        qa0 += __double2ll_rn((double)u.x * sx);
+                        qa1 += __double2ll_rn((double)u.y * sx);
+                    } else {
+                        a0 += (double)u.x;
+                        a1 += (double)u.y;
+                    }
                 }
                 if (want_dist && lane < rows_m) {
                     // lane = row: exact FP64 distance to w_b, features in order
@@ -530,21 +550,34 @@ __global__ void __launch_bounds__(kTmaWarps * 32, 2) k_gather_tma(
                     }
                     const double dist = sqrt(d2);
                     if (dist_out) dist_out[pos[m]] = dist;
-                    ds += dist;
+                    if (kExact) qds += __double2ll_rn(dist * sd);
+                    else ds += dist;
                 }
                 __syncwarp();  // buffer s is refilled by the issue of batch m + 2
             }
         }
         double* out = partial + (size_t)p * Dp;
-        if (accumulate) {
-            if (oka) out[ka] = a0 + c0;
-            if (okb) out[kb] = a1 + c1;
-        }
-        if (want_dist) {
+        if (kExact) {  // int64 partials (<= 256 rows x 2^54) in the double slots
+            if (accumulate) {
+                if (oka) out[ka] = __longlong_as_double(qa0 + qc0);
+                if (okb) out[kb] = __longlong_as_double(qa1 + qc1);
+            }
+            if (want_dist) {
 #pragma unroll
-            for (int o = 16; o; o >>= 1) ds += __shfl_xor_sync(0xffffffffu, ds, o);
+                for (int o = 16; o; o >>= 1) qds += __shfl_xor_sync(0xffffffffu, qds, o);
+            }
+            if (lane == 0) out[D] = __longlong_as_double(qds);
+        } else {
+            if (accumulate) {
+                if (oka) out[ka] = a0 + c0;
+                if (okb) out[kb] = a1 + c1;
+            }
+            if (want_dist) {
+#pragma unroll
+                for (int o = 16; o; o >>= 1) ds += __shfl_xor_sync(0xffffffffu, ds, o);
+            }
+            if (lane == 0) out[D] = ds;
         }
-        if (lane == 0) out[D] = ds;
     }
 }
 
@@ -599,6 +632,109 @@ __global__ void k_add_rowcount(double* __restrict__ sums, uint32_t P, uint32_t D
     *t = add ? *t + rows : rows;
 }
 
+// ---- exact mode: int128 sums as three int64 limbs of 42 / 42 / 44 bits ------
+// (limbs of up to 2^20 ranks or chunks add in int64 without overflow; the
+// reduce step is a plain int64 sum, then exact_unpack recombines)
+
+__device__ __forceinline__ void to_limbs(__int128 v, long long* l) {
+    const long long m = (1ll << 42) - 1;
+    l[0] = (long long)(v & m);
+    l[1] = (long long)((v >> 42) & m);
+    l[2] = (long long)(v >> 84);
+}
+__device__ __forceinline__ __int128 from_limbs(const long long* l) {
+    return ((__int128)l[2] << 84) + ((__int128)l[1] << 42) + (__int128)l[0];
+}
+__device__ __forceinline__ __int128 warp_sum_i128(__int128 v) {
+#pragma unroll
+    for (int o = 16; o; o >>= 1) {
+        const unsigned long long lo = __shfl_xor_sync(0xffffffffu, (unsigned long long)v, o);
+        const long long hi = __shfl_xor_sync(0xffffffffu, (long long)(v >> 64), o);
+        v += ((__int128)hi << 64) | (__int128)lo;
+    }
+    return v;
+}
+
+// xs[e] limbs (+)= sum over node b's pieces of the int64 partials, e = b*D + k
+__global__ void k_piece_reduce_exact(const double* __restrict__ partial,
+                                     const uint32_t* __restrict__ piece_start, uint32_t P,
+                                     uint32_t D, long long* __restrict__ xs, int add) {
+    const size_t e = (blockIdx.x * (size_t)blockDim.x + threadIdx.x) >> 5;
+    const int lane = threadIdx.x & 31;
+    if (e >= (size_t)P * D) return;
+    const uint32_t Dp = D + 1;
+    const uint32_t b = (uint32_t)(e / D), k = (uint32_t)(e % D);
+    const uint32_t p0 = piece_start[b], p1 = piece_start[b + 1];
+    __int128 v = 0;
+    for (uint32_t p = p0 + lane; p < p1; p += 32)
+        v += (__int128)__double_as_longlong(partial[(size_t)p * Dp + k]);
+    v = warp_sum_i128(v);
+    if (lane == 0) {
+        long long l[3];
+        to_limbs(v, l);
+        long long* o = xs + 3 * e;
+        for (int i = 0; i < 3; ++i) o[i] = add ? o[i] + l[i] : l[i];
+    }
+}
+
+__global__ void __launch_bounds__(1024) k_dist_reduce_exact(const double* __restrict__ partial,
+                                                            const uint32_t* __restrict__ piece_start,
+                                                            uint32_t P, uint32_t D,
+                                                            long long* __restrict__ xs, int add) {
+    __shared__ long long red[32][2];
+    const uint32_t np = piece_start[P], Dp = D + 1;
+    __int128 v = 0;
+    for (uint32_t p = threadIdx.x; p < np; p += 1024)
+        v += (__int128)__double_as_longlong(partial[(size_t)p * Dp + D]);
+    v = warp_sum_i128(v);
+    if ((threadIdx.x & 31) == 0) {
+        red[threadIdx.x >> 5][0] = (long long)(unsigned long long)v;
+        red[threadIdx.x >> 5][1] = (long long)(v >> 64);
+    }
+    __syncthreads();
+    if (threadIdx.x == 0) {
+        __int128 t = 0;
+        for (int w = 0; w < 32; ++w)
+            t += ((__int128)red[w][1] << 64) | (__int128)(unsigned long long)red[w][0];
+        long long l[3];
+        to_limbs(t, l);
+        long long* o = xs + 3 * (size_t)P * D;
+        for (int i = 0; i < 3; ++i) o[i] = add ? o[i] + l[i] : l[i];
+    }
+}
+
+// the counts and the row total (exact f64 integers) join the int64 buffer, so
+// the epoch's one reduce is a single int64 sum
+__global__ void k_exact_pack(const double* __restrict__ sums, uint32_t P, uint32_t D,
+                             long long* __restrict__ xs) {
+    const uint32_t b = blockIdx.x * blockDim.x + threadIdx.x;
+    long long* t = xs + 3 * ((size_t)P * D + 1);
+    if (b < P) t[b] = (long long)sums[(size_t)P * D + b];
+    if (b == 0) t[P] = (long long)sums[(size_t)P * D + P + 1];
+}
+
+// back to the f64 sums layout [S | c | sum dist | rows] for K3: each exact sum
+// converted once (round to nearest) and scaled back by a power of two
+__global__ void k_exact_unpack(const long long* __restrict__ xs, uint32_t P, uint32_t D,
+                               const float* __restrict__ xmax2, const float* __restrict__ w2max,
+                               double* __restrict__ sums) {
+    double sx, sd;
+    exact_scales(xmax2, w2max, &sx, &sd);
+    const size_t n = (size_t)P * D;
+    for (size_t e = blockIdx.x * (size_t)blockDim.x + threadIdx.x; e < n + P + 2;
+         e += (size_t)gridDim.x * blockDim.x) {
+        if (e < n) {
+            sums[e] = (double)from_limbs(xs + 3 * e) / sx;
+        } else if (e < n + P) {
+            sums[e] = (double)xs[3 * (n + 1) + (e - n)];
+        } else if (e == n + P) {
+            sums[e] = (double)from_limbs(xs + 3 * n) / sd;
+        } else {
+            sums[e] = (double)xs[3 * (n + 1) + P];
+        }
+    }
+}
+
 // ---------------------------------------------------------------------------
 
 int g_gather_kind = 0;  // diagnostics (TSOM option 97): 1 = cp.async gather
@@ -619,22 +755,29 @@ void launch_pad_rows(const float* x, uint64_t n, uint32_t D, float* xpad, cudaSt
     TSOM_LAUNCH(k_pad_rows<<<148 * 16, 256, 0, st>>>(x, n, D, xpad));
 }
 
-void launch_accumulate(const float* x, const uint32_t* sel, uint64_t n, uint32_t D,
+int launch_accumulate(const float* x, const uint32_t* sel, uint64_t n, uint32_t D,
                        const float* w, uint32_t P, const uint32_t* bmu, double* dist_out,
                        bool want_dist_sum, bool accumulate, bool first, const AccumScratch& s,
                        double* sums, int sm_count, cudaStream_t st, bool x_slack,
-                       uint32_t ldx) {
+                       uint32_t ldx, const ExactSums* exact) {
     if (ldx == 0) ldx = D;
     const int add = first ? 0 : 1;
     if (n == 0) {
         if (first) cudaMemsetAsync(sums, 0, ((size_t)P * D + P + 2) * sizeof(double), st);
-        return;
+        if (exact && first) {
+            cudaMemsetAsync(exact->xs, 0, exact_sums_words(P, D) * sizeof(long long), st);
+        }
+        return 0;
     }
     const bool want_dist = dist_out != nullptr || want_dist_sum;
     if (!accumulate && !want_dist) {  // BMU only: nothing to gather
         if (first) cudaMemsetAsync(sums, 0, ((size_t)P * D + P + 2) * sizeof(double), st);
         TSOM_LAUNCH(k_add_rowcount<<<1, 1, 0, st>>>(sums, P, D, (double)n, add));
-        return;
+        if (exact) {
+            if (!add) cudaMemsetAsync(exact->xs, 0, 3 * ((size_t)P * D + 1) * sizeof(long long), st);
+            TSOM_LAUNCH(k_exact_pack<<<(P + 255) / 256, 256, 0, st>>>(sums, P, D, exact->xs));
+        }
+        return 0;
     }
     const uint32_t nblk = (uint32_t)accum_blocks(n);
     // dynamic smem beyond 48 KB (P up to ~7000 nodes)
@@ -663,16 +806,25 @@ void launch_accumulate(const float* x, const uint32_t* sel, uint64_t n, uint32_t
     // padded rows (a 256-B stride, line aligned): a row is exactly two 128-B
     // lines instead of two or three; only the TMA gather reads strided rows
     const bool use_pad = ldx != D;
-    if (use_pad ||
+    const bool tma = use_pad ||
         (v2 && x_slack && g_gather_kind == 0 && ((reinterpret_cast<uintptr_t>(x) & 15u) == 0) &&
-         tsmem <= 110 * 1024)) {
-        ensure_smem_attr((const void*)k_gather_tma, tsmem);
+         tsmem <= 110 * 1024);
+    if (exact && !tma) return 1;  // exact sums need the TMA row gather (d even, <= 62)
+    if (tma) {
         const uint64_t tblocks = (pieces + kTmaWarps - 1) / kTmaWarps;
         const unsigned tb = (unsigned)(tblocks < (uint64_t)sm_count * 2 ? tblocks : sm_count * 2);
-        TSOM_LAUNCH(k_gather_tma<<<tb, kTmaWarps * 32, tsmem, st>>>(
-            x, ldx, sel, w, P, D, slot, s.sorted,
-            s.node_start, s.piece_start, s.piece_node, s.partial, dist_out, want_dist ? 1 : 0,
-            accumulate ? 1 : 0));
+        if (exact) {
+            ensure_smem_attr((const void*)k_gather_tma<true>, tsmem);
+            TSOM_LAUNCH(k_gather_tma<true><<<tb, kTmaWarps * 32, tsmem, st>>>(
+                x, ldx, sel, w, P, D, slot, s.sorted, s.node_start, s.piece_start, s.piece_node,
+                s.partial, dist_out, want_dist ? 1 : 0, accumulate ? 1 : 0, exact->xmax2,
+                exact->w2max));
+        } else {
+            ensure_smem_attr((const void*)k_gather_tma<false>, tsmem);
+            TSOM_LAUNCH(k_gather_tma<false><<<tb, kTmaWarps * 32, tsmem, st>>>(
+                x, ldx, sel, w, P, D, slot, s.sorted, s.node_start, s.piece_start, s.piece_node,
+                s.partial, dist_out, want_dist ? 1 : 0, accumulate ? 1 : 0, nullptr, nullptr));
+        }
     } else if (v2 && D <= 64 && asmem <= 110 * 1024) {
         ensure_smem_attr((const void*)k_gather_async, asmem);
         const uint64_t ablocks = (pieces + kAsyncWarps - 1) / kAsyncWarps;
@@ -699,13 +851,38 @@ void launch_accumulate(const float* x, const uint32_t* sel, uint64_t n, uint32_t
 #undef TSOM_GATHER_ANY
     }
     const size_t m = (size_t)P * D;
+    if (exact) {
+        // S and the distance sum exact in the int64 limb buffer (zero when not
+        // produced), then counts and rows joined: the one reduce is on exact->xs
+        if (accumulate)
+            TSOM_LAUNCH(k_piece_reduce_exact<<<(unsigned)((m * 32 + 255) / 256), 256, 0, st>>>(
+                s.partial, s.piece_start, P, D, exact->xs, add));
+        else if (!add)
+            cudaMemsetAsync(exact->xs, 0, 3 * m * sizeof(long long), st);
+        if (want_dist)
+            TSOM_LAUNCH(k_dist_reduce_exact<<<1, 1024, 0, st>>>(s.partial, s.piece_start, P, D,
+                                                                 exact->xs, add));
+        else if (!add)
+            cudaMemsetAsync(exact->xs + 3 * m, 0, 3 * sizeof(long long), st);
+        TSOM_LAUNCH(k_add_rowcount<<<1, 1, 0, st>>>(sums, P, D, (double)n, add));
+        TSOM_LAUNCH(k_exact_pack<<<(P + 255) / 256, 256, 0, st>>>(sums, P, D, exact->xs));
+        return 0;
+    }
     if (accumulate)
         TSOM_LAUNCH(k_piece_reduce<<<(unsigned)((m * 32 + 255) / 256), 256, 0, st>>>(
             s.partial, s.piece_start, P, D, sums, add));
     if (want_dist)
         TSOM_LAUNCH(k_dist_reduce<<<1, 1024, 0, st>>>(s.partial, s.piece_start, P, D, sums, add));
     TSOM_LAUNCH(k_add_rowcount<<<1, 1, 0, st>>>(sums, P, D, (double)n, add));
+    return 0;
 }
+
+void launch_exact_unpack(const ExactSums& ex, uint32_t P, uint32_t D, double* sums,
+                         cudaStream_t st) {
+    TSOM_LAUNCH(k_exact_unpack<<<148, 256, 0, st>>>(ex.xs, P, D, ex.xmax2, ex.w2max, sums));
+}
+
+size_t exact_sums_words(uint32_t P, uint32_t D) { return 3 * ((size_t)P * D + 1) + P + 1; }
 
 void accum_scratch_bytes(uint64_t n, uint32_t P, uint32_t D, size_t out[7]) {
     const uint64_t nblk = accum_blocks(n), pieces = accum_pieces_max(n, P);

@@ -136,13 +136,13 @@ def run_study_cuda(base, n_trials: int, seeds, train: np.ndarray, holdout: np.nd
     return qt, qh, fl.astype(bool), secs.value
 
 
-def _engine_flags(engines: int) -> int:
+def _engine_flags(engines: int, exact: bool = False) -> int:
     assert 1 <= engines <= 15
-    return (engines if engines > 1 else 0) << 8
+    return ((engines if engines > 1 else 0) << 8) | ((1 if exact else 0) << 28)
 
 
 def train_device(cfg, data: np.ndarray, device: int = 0, log_qe: bool = False,
-                 streamed: bool = False, engines: int = 1):
+                 streamed: bool = False, engines: int = 1, exact: bool = False):
     """toposom_b200::train_device: the reference's epoch loop with every step on
     the device (sampler, refresh, influence, BMU, accumulate, update).  engines
     > 1 splits the rows over that many engines on `device` joined by an
@@ -155,7 +155,7 @@ def train_device(cfg, data: np.ndarray, device: int = 0, log_qe: bool = False,
     qe = np.zeros(cfg.n_iters) if log_qe else None
     ref = np.zeros(cfg.n_iters, np.uint8)
     secs = (C.c_double * 3)()
-    flags = (1 if streamed else 0) | 32 | _engine_flags(engines)
+    flags = (1 if streamed else 0) | 32 | _engine_flags(engines, exact)
     st = L.tsom_dropin_train(C.byref(_cfg(cfg)), data.ctypes.data, n, d, w.ctypes.data,
                              qe.ctypes.data if log_qe else None, ref.ctypes.data, device, flags,
                              secs)
@@ -166,7 +166,7 @@ def train_device(cfg, data: np.ndarray, device: int = 0, log_qe: bool = False,
 
 def train_cuda(cfg, data: np.ndarray, device: int = 0, log_qe: bool = False,
                streamed: bool = False, bmu_kernel: int = 0, force_distances: bool = False,
-               profile: bool = False, engines: int = 1):
+               profile: bool = False, engines: int = 1, exact: bool = False):
     """Reference train_with_executor + CudaExecutor.  Returns (weights, qe_log, refresh_log, s);
     with profile=True, s = (total, executor construction incl. bind, sum of run_iteration).
     engines > 1: the executor splits the rows over that many engines (the
@@ -179,7 +179,7 @@ def train_cuda(cfg, data: np.ndarray, device: int = 0, log_qe: bool = False,
     ref = np.zeros(cfg.n_iters, np.uint8)
     secs = (C.c_double * 3)()
     flags = ((1 if streamed else 0) | ((bmu_kernel & 3) << 1) | (8 if force_distances else 0)
-             | (16 if profile else 0) | _engine_flags(engines))
+             | (16 if profile else 0) | _engine_flags(engines, exact))
     st = L.tsom_dropin_train(C.byref(_cfg(cfg)), data.ctypes.data, n, d, w.ctypes.data,
                              qe.ctypes.data if log_qe else None, ref.ctypes.data, device, flags,
                              secs)

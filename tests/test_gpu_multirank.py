@@ -427,3 +427,123 @@ def test_selection_validation(pkg, oracle_port):
     uo2, ho2, _, _, _ = oracle_port.run_iteration(x, dup, w, infl, 0.5, 1, 1)
     np.testing.assert_allclose(h2, ho2, rtol=1e-9)
     assert np.max(np.abs(u2 - uo2)) <= 1e-9 * np.max(np.abs(uo2))
+
+
+# --- exact mode: bit-identical for any rank count ------------------------------
+#
+# TSOM_OPT_DETERMINISTIC puts every feature value and distance on a fixed-point
+# grid set by the data's global bounds and sums them in int64 limbs, reduced as
+# integers: the reference's guarantee (accum.hpp:12-20, parallel.hpp:17-21 —
+# "any G produces bit-identical final weights"; test_parallel.cpp:144-162).
+
+def exact_engine(pkg, rows, p, configure):
+    from paper_2604_26555_b200 import _lib
+    e = pkg.Engine(p, rows.shape[1])
+    e.set_option(_lib.TSOM_OPT_DETERMINISTIC, 1)
+    e.bind(rows)
+    configure(e)
+    return e
+
+
+@pytest.mark.parametrize("world", [2, 3, 4])
+def test_exact_epoch_bit_identical_across_ranks(pkg, oracle_port, world):
+    from paper_2604_26555_b200 import _lib
+    n, p = 30011, 256
+    x = oracle_port.synth_gmm(n, 50, 2750 + world)
+    w = x[np.linspace(0, n - 1, p).astype(int)].copy()
+    infl = oracle_port.influence_from_dist(oracle_port.lattice_dist("hex", 16, 16), 4.0)
+
+    def configure(e):
+        e.set_codebook(w)
+        e.set_influence(infl)
+
+    single = exact_engine(pkg, x, p, configure)
+    u1, h1, d1 = single.epoch(0.45, want_dist=True)
+    s1, c1 = single.qe()
+    plain = pkg.Engine(p, 50)
+    plain.bind(x)
+    configure(plain)
+    u0, h0, _ = plain.epoch(0.45)
+    assert np.max(np.abs(u1 - u0)) <= 1e-12 * np.max(np.abs(u0))  # the grid costs nothing
+    assert np.array_equal(h1, h0)
+    g = pkg.RankGroup(world)
+    sl = assign_shards(n, world)
+    engines = []
+    for r, (a, b) in enumerate(sl):
+        e = exact_engine(pkg, x[a:b], p, configure)
+        e.join_group(g, r)
+        engines.append(e)
+    res = run_ranks(world, lambda r: engines[r].epoch(0.45, want_dist=True))
+    for r in range(world):
+        assert np.array_equal(res[r][0], u1), f"rank {r}: U not bit-identical"
+        assert np.array_equal(res[r][1], h1)
+    assert np.array_equal(np.concatenate([res[r][2] for r in range(world)]), d1)
+    q = run_ranks(world, lambda r: engines[r].qe())
+    assert all(s == s1 and c == c1 for s, c in q)
+    g.close()
+
+
+def test_exact_sums_ignore_selection_order(pkg, oracle_port):
+    """The same multiset of rows in any order gives bit-identical sums."""
+    n, p = 20000, 128
+    x = oracle_port.synth_gmm(n, 50, 2760)
+    w = x[:p].copy()
+    infl = oracle_port.influence_from_dist(oracle_port.lattice_dist("rect", 16, 8), 3.0)
+
+    def configure(e):
+        e.set_codebook(w)
+        e.set_influence(infl)
+
+    e = exact_engine(pkg, x, p, configure)
+    sel = np.sort(np.random.default_rng(4).choice(n, 9000, replace=False)).astype(np.uint32)
+    u1, h1, _ = e.epoch(0.5, sel)
+    u2, h2, _ = e.epoch(0.5, np.random.default_rng(5).permutation(sel))
+    assert np.array_equal(u1, u2) and np.array_equal(h1, h2)
+
+
+@pytest.mark.parametrize("world", [2, 4])
+def test_exact_training_bit_identical_across_ranks(pkg, oracle_port, world):
+    """tsom_train_epochs at the c2 shape: every rank's final codebook equals the
+    single engine's bit for bit."""
+    from paper_2604_26555_b200.hostref import init_sample_draw, lattice_dist, resolved_sigma0
+    n, p = 40000, 1024
+    x = oracle_port.synth_gmm(n, 50, 2606)
+    w0 = init_sample_draw(x, p, 2606)
+    dist = lattice_dist("hex", 32, 32)
+    etas, sigmas = _schedules(10, resolved_sigma0("hex", 32, 32))
+
+    def configure(e):
+        e.set_codebook(w0)
+        e.set_topology_distance(dist)
+
+    single = exact_engine(pkg, x, p, configure)
+    single.train_epochs(etas, sigmas)
+    w1 = single.get_codebook()
+    g = pkg.RankGroup(world)
+    engines = []
+    for r, (a, b) in enumerate(assign_shards(n, world)):
+        e = exact_engine(pkg, x[a:b], p, configure)
+        e.join_group(g, r)
+        engines.append(e)
+    run_ranks(world, lambda r: engines[r].train_epochs(etas, sigmas))
+    for r in range(world):
+        assert np.array_equal(engines[r].get_codebook(), w1), f"rank {r}"
+    g.close()
+
+
+@pytest.mark.parametrize("kw", [dict(topology="rng", nodes=12, n_iters=6, seed=4,
+                                     sampling="adaptive", rho=0.3),
+                                dict(topology="hex", grid_w=4, grid_h=4, n_iters=8, seed=17)],
+                         ids=["rng-adaptive", "hex"])
+def test_exact_dropin_bit_identical_across_engines(pkg, kw):
+    """The C++ drop-ins with CudaOptions::exact: 1, 2 and 3 engines give the same
+    weights bit for bit (the reference's train_parallel guarantee)."""
+    from paper_2604_26555_b200 import dropin
+    if not dropin.available():
+        pytest.skip("libtsom_dropin.so not built")
+    g = np.load(os.path.join(GOLDEN, "train_runs.npz"))
+    cfg = dropin.TrainConfig(**kw)
+    ws = [dropin.train_device(cfg, g["x"], engines=k, exact=True)[0] for k in (1, 2, 3)]
+    assert np.array_equal(ws[0], ws[1]) and np.array_equal(ws[0], ws[2])
+    wc = [dropin.train_cuda(cfg, g["x"], engines=k, exact=True)[0] for k in (1, 3)]
+    assert np.array_equal(wc[0], wc[1])
