@@ -81,3 +81,29 @@ def test_c5_shape_streamed_from_shards(pkg, golden, oracle_port, tmp_path):
         e.bind_shards(write_shards(x, str(tmp_path), 7), streamed=True)
 
     run(pkg, golden, oracle_port, "c2", bind)
+
+
+def test_c1_in_full(pkg):
+    """BASELINE config c1 in full (10x10 rect, 1e5 x 50 rows, 10 epochs): the
+    device loop (C++ train_device) and the Python device loop against the
+    reference's own run (tests/golden/config1_1e5.npz, make_golden_c1.py).
+    Rows from the product's host generator (tsom_synth_gmm_host, value-identical
+    to the reference's Rng stream)."""
+    from paper_2604_26555_b200 import _lib, dropin
+    path = os.path.join(os.path.dirname(GOLDEN), "config1_1e5.npz")
+    g = np.load(path)
+    seed, n = int(g["seed"]), int(g["n"])
+    x = _lib.synth_gmm_host(n, 50, seed)
+    rc = pkg.ResidentConfig(topology="rect", grid_w=10, grid_h=10, n_iters=10, seed=seed)
+    e = pkg.Engine(100, 50)
+    e.bind(x)
+    log = pkg.train_resident(rc, e, pkg.api.init_sample_draw(x, 100, seed), log_qe=True)
+    w = e.get_codebook()
+    rel = np.max(np.abs(w.astype(np.float64) - g["w"])) / np.max(np.abs(g["w"]))
+    assert rel <= 1e-6, f"codebook rel max-norm {rel:.2e}"
+    np.testing.assert_allclose([r["qe_train"] for r in log], g["qe"], rtol=1e-9)
+    if dropin.available():
+        cfg = dropin.TrainConfig(topology="rect", grid_w=10, grid_h=10, n_iters=10, seed=seed)
+        wd, qd, _, _ = dropin.train_device(cfg, x, log_qe=True)
+        assert np.max(np.abs(wd.astype(np.float64) - g["w"])) / np.max(np.abs(g["w"])) <= 1e-6
+        np.testing.assert_allclose(qd, g["qe"], rtol=1e-9)
