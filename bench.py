@@ -875,14 +875,14 @@ def roofline_peak(kernel, pk):
 
 
 # ncu --set full, one launch of K1 at the bench shape (1e7 x 50, K=1024):
-# dram__bytes_read.sum + dram__bytes_write.sum, bytes per launch.  Captures
-# (profiles/r01_ncu_full_summary*.json) saw 3.74, 6.61, 5.82 and 5.17 GB read:
-# the A tiles (3.2 GB) are read by the 4 codebook-group CTAs and L2 catches a
-# run-dependent part of the repeats; the latest capture is reported.
-K1_TRAFFIC = {3: 5.170710e9 + 0.319864e9}
-K1_TRAFFIC_SRC = "profiles/r01_ncu_full_summary_d.json, k1_bmu_tc<2, 0>: 5.17 GB read (split A " \
-                 "tiles 3.2 GB, each read by the 4 node-group CTAs, partly from L2; earlier " \
-                 "captures 3.74-6.61 GB) + 0.32 GB per-group partial-result writes"
+# dram__bytes_read.sum + dram__bytes_write.sum, bytes per launch
+# (profiles/r02_ncu_full_summary.json, scripts/ncu_round2.sh).  The split A
+# tiles are 3.2 GB; the 4 codebook-group CTAs each stream them and L2 catches
+# part of the repeats (earlier captures: 3.74-6.61 GB read).
+K1_TRAFFIC = {3: 4.049247e9 + 0.3195904e9}
+K1_TRAFFIC_SRC = "profiles/r02_ncu_full_summary.json, k1_bmu_tc<2, 0, 0>: 4.05 GB read (split A " \
+                 "tiles 3.2 GB, each streamed by the 4 node-group CTAs, L2 hit rate 54 %) + " \
+                 "0.32 GB per-group partial-result writes"
 
 
 def main():

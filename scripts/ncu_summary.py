@@ -17,6 +17,7 @@ KEEP = [
     "lts__t_sectors_srcunit_tex.sum", "sm__warps_active.avg.pct_of_peak_sustained_active",
     "launch__registers_per_thread", "launch__grid_size", "launch__block_size",
     "launch__cluster_dim_x", "smsp__inst_executed.sum",
+    "sm__mem_tensor_cycles_active.avg.pct_of_peak_sustained_elapsed", "lts__t_sector_hit_rate.pct",
 ]
 
 
