@@ -82,8 +82,8 @@ typedef struct tsom_group tsom_group;
 /* Engine lifetime ---------------------------------------------------------- */
 
 /* Create an engine for a P-node, d-dimensional codebook on CUDA `device`
- * (1 <= d <= 256; the tensor-core BMU kernels cover d <= 62, larger d uses the
- * SIMT kernel). */
+ * (1 <= P <= 65536, 1 <= d <= 256; the tensor-core BMU kernels cover d <= 62,
+ * larger d uses the SIMT kernel). */
 int tsom_create(int device, uint32_t nodes, uint32_t dims, tsom_engine** out);
 int tsom_destroy(tsom_engine* eng);
 const char* tsom_last_error(const tsom_engine* eng);

@@ -261,14 +261,15 @@ void run_bmu(Engine* eng, const float* x, uint32_t ldx, const uint32_t* sel, uin
         // exit at once, and slots past 4 cap (> 25 % of the rows) take the
         // full exact re-scan.
         // passes launched: all kTiePasses until near-ties have been observed,
-        // then twice the largest fraction seen so far plus one spare pass
-        // (never fewer than the data need: the last pass's overflow takes the
-        // exact re-scan, so a short count costs time, not correctness)
+        // then enough for 1.25 x the largest fraction seen so far (at least
+        // one).  An empty pass still costs three launches (~12 us), and a
+        // count past the last pass only costs time (its overflow takes the
+        // exact re-scan), not correctness.
         uint32_t passes = n > (1u << 20) ? kTiePasses : 1u;
         const uint64_t cap = passes > 1 ? (n + kTieCapDiv - 1) / kTieCapDiv : n;
         if (passes > 1 && eng->tie_frac_max >= 0.0) {
-            const double need = 2.0 * eng->tie_frac_max * (double)n / (double)cap;
-            passes = std::min<uint32_t>(kTiePasses, (uint32_t)std::ceil(need) + 1u);
+            const double need = 1.25 * eng->tie_frac_max * (double)n / (double)cap;
+            passes = std::min<uint32_t>(kTiePasses, std::max<uint32_t>(1u, (uint32_t)std::ceil(need)));
         }
         const uint64_t mt = (cap + tsom::kTcTileM - 1) / tsom::kTcTileM;
         CU(eng->tsplit.ensure(mt * geo.tile_bytes));
@@ -799,7 +800,9 @@ const char* tsom_version(void) { return kVersion; }
 int tsom_create(int device, uint32_t nodes, uint32_t dims, tsom_engine** out) {
     if (!out) return TSOM_ERR_INVALID;
     *out = nullptr;
-    if (nodes < 1 || dims < 1 || dims > 256) return TSOM_ERR_INVALID;  // d <= 256 (K2 lanes)
+    // d <= 256 (K2 lanes); K <= 65536 (16-bit node ids in the near-tie merge;
+    // the K x K FP64 influence matrix alone is 34 GB there)
+    if (nodes < 1 || nodes > 65536 || dims < 1 || dims > 256) return TSOM_ERR_INVALID;
     auto* eng = new tsom_engine();
     eng->device = device;
     eng->P = nodes;

@@ -592,7 +592,7 @@ __global__ void __launch_bounds__(EpiCfg<kKind>::kThreads, 1)
         }
         for (int a = 0; a < 2; ++a) {
             mbar_init(&tfull_bar[a], 1);
-            mbar_init(&tempty_bar[a], kEnum ? 4u : 4u * kSets);  // one arrival per warp
+            mbar_init(&tempty_bar[a], 4u * kSets);  // one arrival per epilogue warp
         }
         mbar_init(w_bar, 1);
         asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
@@ -825,58 +825,106 @@ __global__ void __launch_bounds__(EpiCfg<kKind>::kThreads, 1)
                 }
             }
         } else {
-            // Enumerate pass (near-tie rows only): set s drains accumulator
-            // buffer s (every other tile) over all gn columns: the row's raw
-            // minimum, then every node within the window of it.
-            uint32_t acc = set, acc_phase = 0;
-            const uint32_t t0 = set < 2 ? cta_in_group + set * ctas_per_group : ntiles;
-            for (uint32_t t = t0; t < ntiles; t += 2 * ctas_per_group) {
-                mbar_wait(&tfull_bar[acc], acc_phase);
-                tc_fence_after();
-                const uint32_t taddr = tmem_base + ((q * 32u) << 16) + acc * acc_cols;
-                float mn = CUDART_INF_F;
-                for (uint32_t cc = 0; cc < gn; cc += 32) {
-                    uint32_t r[32];
-                    TSOM_TMEM_LD32(taddr + cc, r);
-                    tmem_wait_ld();
-#pragma unroll
-                    for (int m = 0; m < 16; ++m)
-                        mn = fmin3f(mn, __uint_as_float(r[2 * m]), __uint_as_float(r[2 * m + 1]));
-                }
+            // Enumerate pass (near-tie rows only), laid out like the main pass:
+            // both sets drain every tile, set h loading its chunks [h nch /
+            // kSets, (h+1) nch / kSets) into registers with one TMEM round trip
+            // (the accumulator is released at once).  The sets swap their
+            // minima through shared memory, so each enumerates its columns
+            // against the group's raw minimum B1: a 32-bit mask of v <= B1 +
+            // thr per chunk, then the set bits in ascending order.  Set 1
+            // hands its candidates to set 0, which appends them after its own
+            // (set 1's ids are the higher ones: ascending node order) and
+            // writes [B1 | ids 0-3 | ids 4-7 | count] (count 0: group not
+            // relevant for the row, kCandOverflow: > 8 candidates).
+            static_assert(kSets == 2, "set exchange assumes two epilogue sets");
+            // single-buffered: a set rewrites its slots for the next tile only
+            // after the second barrier of this one, which the reader has passed
+            float* xmin = xch_b;                                                  // [2 set][128]
+            uint32_t* xlist = reinterpret_cast<uint32_t*>(xch_b + 2 * kTcTileM);  // [3][128]
+            const uint32_t c_begin = set * nch / kSets;
+            const uint32_t c_count = (set + 1) * nch / kSets - c_begin;
+            uint32_t acc = 0, acc_phase = 0;
+            for (uint32_t t = cta_in_group; t < ntiles; t += ctas_per_group) {
                 const uint64_t pos = (uint64_t)t * kTcTileM + row;
-                // enumerate the row's candidates v <= B1 + thr in ascending j
                 const bool need = pos < n && ((__ldg(rmask + pos) >> (g & 31)) & 1u);
                 const float thr = need ? __ldg(xn2 + pos) + wpart : 0.0f;
-                const float lim = mn + thr;
-                uint32_t pk0 = 0, pk1 = 0, nc = 0;
-                if (__any_sync(0xffffffffu, need)) {
-                    for (uint32_t cc = 0; cc < gn; cc += 16) {
-                        uint32_t r[16];
-                        TSOM_TMEM_LD16(taddr + cc, r);
-                        tmem_wait_ld();
+                mbar_wait(&tfull_bar[acc], acc_phase);
+                tc_fence_after();
+                const uint32_t taddr =
+                    tmem_base + ((q * 32u) << 16) + acc * acc_cols + c_begin * 32;
+                uint32_t r[kCPS][32];
 #pragma unroll
-                        for (int k = 0; k < 16; ++k) {
-                            if (need && __uint_as_float(r[k]) <= lim) {
-                                const uint32_t id = (cc + k) << (8 * (nc & 3));
-                                if (nc < 4) pk0 |= id;
-                                else if (nc < 8) pk1 |= id;
-                                ++nc;
-                            }
-                        }
-                    }
-                }
+                for (int c = 0; c < kCPS; ++c)
+                    if ((uint32_t)c < c_count) TSOM_TMEM_LD32(taddr + c * 32, r[c]);
+                tmem_wait_ld();
                 tc_fence_before();
                 __syncwarp();
                 if (lane == 0) mbar_arrive(&tempty_bar[acc]);  // warp done with the accumulator
-                if (pos < n) {
+                float mn[2] = {CUDART_INF_F, CUDART_INF_F};
+#pragma unroll
+                for (int c = 0; c < kCPS; ++c)
+                    if ((uint32_t)c < c_count) {
+#pragma unroll
+                        for (int m = 0; m < 16; ++m)
+                            mn[m & 1] = fmin3f(mn[m & 1], __uint_as_float(r[c][2 * m]),
+                                               __uint_as_float(r[c][2 * m + 1]));
+                    }
+                const float bs = fminf(mn[0], mn[1]);
+                xmin[set * kTcTileM + row] = bs;
+                asm volatile("bar.sync 1, %0;" ::"n"(kSets * 128) : "memory");
+                const float B1 = fminf(bs, xmin[(set ^ 1) * kTcTileM + row]);
+                const float lim = B1 + thr;
+                uint32_t pk0 = 0, pk1 = 0, nc = 0;
+                if (__any_sync(0xffffffffu, need)) {
+#pragma unroll
+                    for (int c = 0; c < kCPS; ++c)
+                        if ((uint32_t)c < c_count) {
+                            uint32_t m = 0;
+#pragma unroll
+                            for (int k = 0; k < 32; ++k)
+                                m |= (__uint_as_float(r[c][k]) <= lim ? 1u : 0u) << k;
+                            if (!need) m = 0;
+                            while (m && nc <= 8) {
+                                const uint32_t id = (c_begin + c) * 32u + (__ffs(m) - 1);
+                                m &= m - 1;
+                                if (nc < 4) pk0 |= id << (8 * nc);
+                                else if (nc < 8) pk1 |= id << (8 * (nc - 4));
+                                ++nc;
+                            }
+                        }
+                }
+                if (set == 1) {
+                    uint32_t* xl = xlist;
+                    xl[row] = nc;
+                    xl[kTcTileM + row] = pk0;
+                    xl[2 * kTcTileM + row] = pk1;
+                }
+                asm volatile("bar.sync 1, %0;" ::"n"(kSets * 128) : "memory");
+                if (set == 0 && pos < n) {
+                    const uint32_t* xl = xlist;
+                    const uint32_t n1 = xl[row];
+                    uint32_t cnt = nc + n1;
+                    if (need && nc <= 8 && cnt <= 8) {
+                        const uint32_t q0 = xl[kTcTileM + row], q1 = xl[2 * kTcTileM + row];
+                        for (uint32_t i = 0; i < n1; ++i) {
+                            const uint32_t id = ((i < 4 ? q0 : q1) >> (8 * (i & 3))) & 0xFFu;
+                            const uint32_t p = nc + i;
+                            if (p < 4) pk0 |= id << (8 * p);
+                            else pk1 |= id << (8 * (p - 4));
+                        }
+                    } else if (need) {
+                        cnt = kCandOverflow;
+                    }
                     float* pg = part + (size_t)g * 4 * n;
-                    pg[pos] = mn;
+                    pg[pos] = B1;
                     pg[n + pos] = __uint_as_float(pk0);
                     pg[2 * n + pos] = __uint_as_float(pk1);
-                    pg[3 * n + pos] =
-                        __uint_as_float(!need ? 0u : ((nc >= 1 && nc <= 8) ? nc : kCandOverflow));
+                    pg[3 * n + pos] = __uint_as_float(!need ? 0u : cnt);
                 }
-                acc_phase ^= 1;
+                if (++acc == 2) {
+                    acc = 0;
+                    acc_phase ^= 1;
+                }
             }
         }
     }
@@ -919,7 +967,7 @@ cudaError_t launch_bmu_tc(int kind, const void* tiles, uint64_t n, const uint32_
     if (per_group > ntiles) per_group = ntiles;
     const uint32_t grid = per_group * groups;
     const uint32_t w_bytes = gn * geo.row_bytes;
-    const size_t fixed = ((w_bytes + 1023u) & ~1023u) + 128 + 2 * kTcTileM * 8;  // + set exchange
+    const size_t fixed = ((w_bytes + 1023u) & ~1023u) + 128 + 2 * kTcTileM * 10;  // + set exchange
     uint32_t stages = 2;
     while (stages < 3 && fixed + (size_t)(stages + 1) * geo.tile_bytes <= smem_optin) ++stages;
     const size_t smem = fixed + (size_t)stages * geo.tile_bytes;

@@ -321,8 +321,9 @@ __global__ void __launch_bounds__(256, 8) k_merge_fast(
 // minima and codes of all groups and the row windows, 16 B each — is
 // independent and issued at once, so a warp pays one memory latency instead of
 // the two of the per-row kernel (the code of the winning group is read
-// without knowing the winner).  Rows, BMUs, the near-tie list order and the
-// masks are those of k_merge_fast.
+// without knowing the winner).  BMUs, the near-tie rows and their masks are
+// those of k_merge_fast; the list is appended to once per block (its order,
+// which no result depends on, is by block).
 template <int kG>
 __global__ void __launch_bounds__(256) k_merge_fast4(
     const float* __restrict__ part, uint64_t n, uint32_t gn, const float* __restrict__ xn2,
@@ -346,7 +347,7 @@ __global__ void __launch_bounds__(256) k_merge_fast4(
     }
     const bool overflow = __float_as_uint(__ldg(scale + 2)) != 0u;
     const float wpart = tie_wpart(__ldg(w2max), __ldg(scale + 1), win);
-    uint32_t out[4];
+    uint32_t out[4], masks[4], ballots[4];
 #pragma unroll
     for (int r = 0; r < 4; ++r) {
         float b[kG];
@@ -385,19 +386,39 @@ __global__ void __launch_bounds__(256) k_merge_fast4(
                 need_tie = !clear;
             }
         }
-        // warp-aggregated append to the near-tie list (one atomic per warp)
-        const uint32_t ballot = __ballot_sync(0xffffffffu, need_tie);
-        if (ballot) {
-            uint32_t base = 0;
-            if (lane == (uint32_t)(__ffs(ballot) - 1))
-                base = atomicAdd(&ties[0], (uint32_t)__popc(ballot));
-            base = __shfl_sync(0xffffffffu, base, __ffs(ballot) - 1);
-            if (need_tie) {
-                const uint32_t slot = base + __popc(ballot & ((1u << lane) - 1u));
-                ties[1 + slot] = (uint32_t)(i0 + r);
-                tmask[slot] = mask;
-            }
+        masks[r] = mask;
+        ballots[r] = __ballot_sync(0xffffffffu, need_tie);
+    }
+    // block-aggregated append to the near-tie list: one atomic per block of
+    // 1024 rows (a per-warp atomic on the one counter serialises ~2e5 atomics
+    // per epoch at a 3 % near-tie rate); slots within the block in (warp, r,
+    // lane) order
+    __shared__ uint32_t wtot[8], blk_base;
+    const uint32_t warp = threadIdx.x >> 5;
+    uint32_t wcount = 0;
+#pragma unroll
+    for (int r = 0; r < 4; ++r) wcount += __popc(ballots[r]);
+    if (lane == 0) wtot[warp] = wcount;
+    __syncthreads();
+    if (threadIdx.x == 0) {
+        uint32_t t = 0;
+        for (uint32_t k = 0; k < blockDim.x / 32; ++k) {
+            const uint32_t v = wtot[k];
+            wtot[k] = t;
+            t += v;
         }
+        blk_base = t ? atomicAdd(&ties[0], t) : 0u;
+    }
+    __syncthreads();
+    uint32_t base = blk_base + wtot[warp];
+#pragma unroll
+    for (int r = 0; r < 4; ++r) {
+        if ((ballots[r] >> lane) & 1u) {
+            const uint32_t slot = base + __popc(ballots[r] & ((1u << lane) - 1u));
+            ties[1 + slot] = (uint32_t)(i0 + r);
+            tmask[slot] = masks[r];
+        }
+        base += __popc(ballots[r]);
     }
     if (valid) *reinterpret_cast<uint4*>(bmu + i0) = make_uint4(out[0], out[1], out[2], out[3]);
 }
@@ -432,74 +453,116 @@ int g_merge_v1 = 0;  // diagnostics (TSOM option 96): 1 = the per-row merge
 // local ids, count 0 = group not enumerated).  One candidate -> bmu; several
 // -> exact FP64 distances of just those nodes in ascending node order with
 // strict < (lowest index wins), as find_bmus (trainer.hpp:293-304); > 8
-// candidates in a group -> full exact re-scan list.
-__global__ void k_merge_partials(const float* __restrict__ part, const uint32_t* __restrict__ ties,
-                                 const uint32_t* __restrict__ dev_count, uint64_t cap,
-                                 uint32_t groups, uint32_t gn,
-                                 const float* __restrict__ xn2, const float* __restrict__ w2max,
-                                 const float* __restrict__ scale, TieWin win,
-                                 const float* __restrict__ x, uint32_t ldx,
-                                 const uint32_t* __restrict__ sel, const float* __restrict__ w,
-                                 uint32_t D, uint32_t* __restrict__ bmu,
-                                 uint32_t* __restrict__ flags) {
+// candidates in a group (or > kMaxCand in all) -> full exact re-scan list.
+//
+// A warp takes 32 near-tie rows (lane = row) and flattens their (row,
+// candidate) pairs into a warp-private shared-memory list, so each exact
+// distance — 50 dependent FP64 adds in the reference's feature order — runs on
+// its own lane instead of one row's candidates running one after another on
+// the row's lane; then every row picks its best pair in ascending node order.
+// The re-check count is added once per warp (a per-row atomic on the one
+// counter serialises ~3e5 atomics per epoch).
+constexpr uint32_t kMaxCand = 16;  // candidates per row evaluated here
+constexpr int kMpWarps = 8;
+
+__global__ void __launch_bounds__(kMpWarps * 32) k_merge_partials(
+    const float* __restrict__ part, const uint32_t* __restrict__ ties,
+    const uint32_t* __restrict__ dev_count, uint64_t cap, uint32_t groups, uint32_t gn,
+    const float* __restrict__ xn2, const float* __restrict__ w2max,
+    const float* __restrict__ scale, TieWin win, const float* __restrict__ x, uint32_t ldx,
+    const uint32_t* __restrict__ sel, const float* __restrict__ w, uint32_t D,
+    uint32_t* __restrict__ bmu, uint32_t* __restrict__ flags) {
+    __shared__ uint16_t pj[kMpWarps][32 * kMaxCand];  // candidate node of pair p
+    __shared__ uint8_t prow[kMpWarps][32 * kMaxCand]; // owning lane of pair p
+    __shared__ double pd[kMpWarps][32 * kMaxCand];    // exact squared distance
+    __shared__ const float* xrow[kMpWarps][32];
     // the near-tie list length is read on the device (no host round trip);
     // rows past the enumerate capacity fall back to the full exact re-scan
     const uint64_t count = *dev_count;
     const uint64_t n = count < cap ? count : cap;
     const float S = __ldg(scale + 1);
-    for (uint64_t f = blockIdx.x * (uint64_t)blockDim.x + threadIdx.x; f < count;
-         f += (uint64_t)gridDim.x * blockDim.x) {
-        const uint32_t pos = ties[f];
-        if (f >= cap) {
-            const uint32_t slot = atomicAdd(&flags[0], 1u);
-            flags[2 + slot] = pos;
-            continue;
+    const uint32_t lane = threadIdx.x & 31, wp = threadIdx.x >> 5;
+    const uint64_t wstride = (uint64_t)gridDim.x * kMpWarps * 32;
+    for (uint64_t f0 = (blockIdx.x * (uint64_t)kMpWarps + wp) * 32; f0 < count; f0 += wstride) {
+        const uint64_t f = f0 + lane;
+        uint32_t pos = 0, ncand = 0, only = 0;
+        bool rescan = false;
+        float lim = 0.0f;
+        if (f < count) {
+            pos = ties[f];
+            if (f >= cap) {
+                rescan = true;
+            } else {
+                const float thr = __ldg(xn2 + f) + tie_wpart(__ldg(w2max), S, win);
+                float B1 = CUDART_INF_F;
+                for (uint32_t g = 0; g < groups; ++g) B1 = fminf(B1, part[(size_t)g * 4 * n + f]);
+                lim = B1 + thr;
+                bool overflow = false;
+                for (uint32_t g = 0; g < groups; ++g) {
+                    const float* pg = part + (size_t)g * 4 * n;
+                    if (!(pg[f] <= lim)) continue;
+                    const uint32_t cnt = __float_as_uint(pg[3 * n + f]);
+                    if (cnt == 0) continue;
+                    if (cnt > 8) overflow = true;
+                    ncand += cnt;
+                    only = g * gn + (__float_as_uint(pg[n + f]) & 0xFFu);
+                }
+                if (overflow || ncand == 0 || ncand > kMaxCand) rescan = true;
+                else if (ncand == 1) bmu[pos] = only;
+            }
         }
-        const float thr = __ldg(xn2 + f) + tie_wpart(__ldg(w2max), S, win);
-        float B1 = CUDART_INF_F;
-        for (uint32_t g = 0; g < groups; ++g) B1 = fminf(B1, part[(size_t)g * 4 * n + f]);
-        const float lim = B1 + thr;
-        uint32_t ncand = 0, only = 0;
-        bool overflow = false;
-        for (uint32_t g = 0; g < groups; ++g) {
-            const float* pg = part + (size_t)g * 4 * n;
-            if (!(pg[f] <= lim)) continue;
-            const uint32_t cnt = __float_as_uint(pg[3 * n + f]);
-            if (cnt == 0) continue;
-            if (cnt > 8) overflow = true;
-            ncand += cnt;
-            only = g * gn + (__float_as_uint(pg[n + f]) & 0xFFu);
-        }
-        if (overflow || ncand == 0) {
+        if (rescan) {
             const uint32_t slot = atomicAdd(&flags[0], 1u);
             flags[2 + slot] = pos;
             bmu[pos] = only;
-            continue;
         }
-        if (ncand == 1) {
-            bmu[pos] = only;
-            continue;
+        const bool multi = !rescan && ncand >= 2;
+        const uint32_t mball = __ballot_sync(0xffffffffu, multi);
+        if (!mball) continue;
+        if (lane == 0) atomicAdd(&flags[1], (uint32_t)__popc(mball));
+        // exclusive scan of the pair counts over the warp
+        uint32_t mine = multi ? ncand : 0u, off = mine;
+#pragma unroll
+        for (int o = 1; o < 32; o <<= 1) {
+            const uint32_t v = __shfl_up_sync(0xffffffffu, off, o);
+            if ((int)lane >= o) off += v;
         }
-        atomicAdd(&flags[1], 1u);
-        const float* xr = x + (sel ? (uint64_t)sel[pos] : (uint64_t)pos) * ldx;
-        double best = CUDART_INF;
-        uint32_t best_j = 0;
-        for (uint32_t g = 0; g < groups; ++g) {
-            const float* pg = part + (size_t)g * 4 * n;
-            if (!(pg[f] <= lim)) continue;
-            const uint32_t cnt = __float_as_uint(pg[3 * n + f]);
-            const uint32_t pk0 = __float_as_uint(pg[n + f]), pk1 = __float_as_uint(pg[2 * n + f]);
-            for (uint32_t c = 0; c < cnt; ++c) {
-                const uint32_t pk = c < 4 ? pk0 : pk1;
-                const uint32_t j = g * gn + ((pk >> (8 * (c & 3))) & 0xFFu);
-                const double d2 = exact_d2(xr, w + (size_t)j * D, D);
-                if (d2 < best) {
-                    best = d2;
-                    best_j = j;
+        const uint32_t total = __shfl_sync(0xffffffffu, off, 31);
+        off -= mine;
+        if (multi) {
+            xrow[wp][lane] = x + (sel ? (uint64_t)sel[pos] : (uint64_t)pos) * ldx;
+            uint32_t c = 0;
+            for (uint32_t g = 0; g < groups; ++g) {
+                const float* pg = part + (size_t)g * 4 * n;
+                if (!(pg[f] <= lim)) continue;
+                const uint32_t cnt = __float_as_uint(pg[3 * n + f]);
+                const uint32_t pk0 = __float_as_uint(pg[n + f]), pk1 = __float_as_uint(pg[2 * n + f]);
+                for (uint32_t k = 0; k < cnt; ++k, ++c) {
+                    const uint32_t pk = k < 4 ? pk0 : pk1;
+                    pj[wp][off + c] = (uint16_t)(g * gn + ((pk >> (8 * (k & 3))) & 0xFFu));
+                    prow[wp][off + c] = (uint8_t)lane;
                 }
             }
         }
-        bmu[pos] = best_j;
+        __syncwarp();
+        for (uint32_t p = lane; p < total; p += 32) {
+            const uint32_t j = pj[wp][p];
+            pd[wp][p] = exact_d2(xrow[wp][prow[wp][p]], w + (size_t)j * D, D);
+        }
+        __syncwarp();
+        if (multi) {
+            double best = CUDART_INF;
+            uint32_t best_j = 0;
+            for (uint32_t c = 0; c < ncand; ++c) {  // ascending node order, strict <
+                const double d2 = pd[wp][off + c];
+                if (d2 < best) {
+                    best = d2;
+                    best_j = pj[wp][off + c];
+                }
+            }
+            bmu[pos] = best_j;
+        }
+        __syncwarp();  // pair lists rewritten by the next round
     }
 }
 
@@ -510,9 +573,9 @@ void launch_merge_partials(const float* part, const uint32_t* ties, const uint32
                            uint32_t D, uint32_t* bmu, uint32_t* flags, cudaStream_t st) {
     if (n_max == 0) return;
     // grid-strides over the device count; sized for the enumerate capacity
-    uint64_t blocks = (std::min(cap, n_max) + 255) / 256;
-    blocks = std::max<uint64_t>(1, std::min<uint64_t>(blocks, 148ull * 16));
-    TSOM_LAUNCH(k_merge_partials<<<(unsigned)blocks, 256, 0, st>>>(
+    uint64_t blocks = (std::min(cap, n_max) + kMpWarps * 32 - 1) / (kMpWarps * 32);
+    blocks = std::max<uint64_t>(1, std::min<uint64_t>(blocks, 148ull * 8));
+    TSOM_LAUNCH(k_merge_partials<<<(unsigned)blocks, kMpWarps * 32, 0, st>>>(
         part, ties, dev_count, cap, groups, gn, xn2, w2max, scale, win, x, ldx, sel, w, D, bmu,
         flags));
 }
