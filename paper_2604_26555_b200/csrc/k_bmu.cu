@@ -234,6 +234,35 @@ __device__ __forceinline__ double exact_d2(const float* __restrict__ x,
     return acc;
 }
 
+// exact_d2 for d even, d <= 64 and 8-byte aligned rows: all loads of both rows
+// are issued before the first add (the scalar loop waits on a load per
+// feature); the arithmetic and its order are exact_d2's
+__device__ __forceinline__ double exact_d2_v2(const float* __restrict__ x,
+                                              const float* __restrict__ wj, uint32_t D) {
+    double acc = 0.0;
+#pragma unroll
+    for (int h = 0; h < 2; ++h) {  // two halves of 32 features: 64 data registers
+        float2 xv[16], wv[16];
+#pragma unroll
+        for (int q = 0; q < 16; ++q) {
+            if (2u * (16 * h + q) < D) {
+                xv[q] = __ldg(reinterpret_cast<const float2*>(x) + 16 * h + q);
+                wv[q] = __ldg(reinterpret_cast<const float2*>(wj) + 16 * h + q);
+            }
+        }
+#pragma unroll
+        for (int q = 0; q < 16; ++q) {
+            if (2u * (16 * h + q) < D) {
+                const double d0 = __dsub_rn((double)xv[q].x, (double)wv[q].x);
+                acc = __dadd_rn(acc, __dmul_rn(d0, d0));
+                const double d1 = __dsub_rn((double)xv[q].y, (double)wv[q].y);
+                acc = __dadd_rn(acc, __dmul_rn(d1, d1));
+            }
+        }
+    }
+    return acc;
+}
+
 // Main-pass merge.  part[sg] = [B1 | code] per row and sub-group sg = g * sets
 // + h, the group's chunks [h nch / sets, (h+1) nch / sets) (k1_bmu_tc merges
 // its two epilogue sets in the CTA and passes sets = 1): the sub-group's raw minimum
@@ -465,7 +494,7 @@ int g_merge_v1 = 0;  // diagnostics (TSOM option 96): 1 = the per-row merge
 constexpr uint32_t kMaxCand = 16;  // candidates per row evaluated here
 constexpr int kMpWarps = 8;
 
-__global__ void __launch_bounds__(kMpWarps * 32) k_merge_partials(
+__global__ void __launch_bounds__(kMpWarps * 32, 2) k_merge_partials(
     const float* __restrict__ part, const uint32_t* __restrict__ ties,
     const uint32_t* __restrict__ dev_count, uint64_t cap, uint32_t groups, uint32_t gn,
     const float* __restrict__ xn2, const float* __restrict__ w2max,
@@ -483,6 +512,9 @@ __global__ void __launch_bounds__(kMpWarps * 32) k_merge_partials(
     const float S = __ldg(scale + 1);
     const uint32_t lane = threadIdx.x & 31, wp = threadIdx.x >> 5;
     const uint64_t wstride = (uint64_t)gridDim.x * kMpWarps * 32;
+    // 8-byte rows (d even): both rows loaded up front, one latency per pair
+    const bool pairs_v2 = (D % 2) == 0 && D <= 64 && (ldx % 2) == 0 &&
+                          ((reinterpret_cast<uintptr_t>(x) | reinterpret_cast<uintptr_t>(w)) & 7u) == 0;
     for (uint64_t f0 = (blockIdx.x * (uint64_t)kMpWarps + wp) * 32; f0 < count; f0 += wstride) {
         const uint64_t f = f0 + lane;
         uint32_t pos = 0, ncand = 0, only = 0;
@@ -547,7 +579,9 @@ __global__ void __launch_bounds__(kMpWarps * 32) k_merge_partials(
         __syncwarp();
         for (uint32_t p = lane; p < total; p += 32) {
             const uint32_t j = pj[wp][p];
-            pd[wp][p] = exact_d2(xrow[wp][prow[wp][p]], w + (size_t)j * D, D);
+            const float* xr = xrow[wp][prow[wp][p]];
+            const float* wj = w + (size_t)j * D;
+            pd[wp][p] = pairs_v2 ? exact_d2_v2(xr, wj, D) : exact_d2(xr, wj, D);
         }
         __syncwarp();
         if (multi) {
