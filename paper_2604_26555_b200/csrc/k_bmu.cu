@@ -241,18 +241,18 @@ __device__ __forceinline__ double exact_d2_v2(const float* __restrict__ x,
                                               const float* __restrict__ wj, uint32_t D) {
     double acc = 0.0;
 #pragma unroll
-    for (int h = 0; h < 2; ++h) {  // two halves of 32 features: 64 data registers
-        float2 xv[16], wv[16];
+    for (int h = 0; h < 4; ++h) {  // four chunks of 16 features: 32 data registers
+        float2 xv[8], wv[8];
 #pragma unroll
-        for (int q = 0; q < 16; ++q) {
-            if (2u * (16 * h + q) < D) {
-                xv[q] = __ldg(reinterpret_cast<const float2*>(x) + 16 * h + q);
-                wv[q] = __ldg(reinterpret_cast<const float2*>(wj) + 16 * h + q);
+        for (int q = 0; q < 8; ++q) {
+            if (2u * (8 * h + q) < D) {
+                xv[q] = __ldg(reinterpret_cast<const float2*>(x) + 8 * h + q);
+                wv[q] = __ldg(reinterpret_cast<const float2*>(wj) + 8 * h + q);
             }
         }
 #pragma unroll
-        for (int q = 0; q < 16; ++q) {
-            if (2u * (16 * h + q) < D) {
+        for (int q = 0; q < 8; ++q) {
+            if (2u * (8 * h + q) < D) {
                 const double d0 = __dsub_rn((double)xv[q].x, (double)wv[q].x);
                 acc = __dadd_rn(acc, __dmul_rn(d0, d0));
                 const double d1 = __dsub_rn((double)xv[q].y, (double)wv[q].y);
@@ -494,7 +494,7 @@ int g_merge_v1 = 0;  // diagnostics (TSOM option 96): 1 = the per-row merge
 constexpr uint32_t kMaxCand = 16;  // candidates per row evaluated here
 constexpr int kMpWarps = 8;
 
-__global__ void __launch_bounds__(kMpWarps * 32, 2) k_merge_partials(
+__global__ void __launch_bounds__(kMpWarps * 32, 3) k_merge_partials(
     const float* __restrict__ part, const uint32_t* __restrict__ ties,
     const uint32_t* __restrict__ dev_count, uint64_t cap, uint32_t groups, uint32_t gn,
     const float* __restrict__ xn2, const float* __restrict__ w2max,
@@ -525,6 +525,11 @@ __global__ void __launch_bounds__(kMpWarps * 32, 2) k_merge_partials(
             if (f >= cap) {
                 rescan = true;
             } else {
+                // the row's lines start towards L2 now (a DRAM round trip, hidden
+                // behind the candidate records) for the distance pass below
+                const float* xr = x + (sel ? (uint64_t)sel[pos] : (uint64_t)pos) * ldx;
+                asm volatile("prefetch.global.L2 [%0];" ::"l"(xr));
+                asm volatile("prefetch.global.L2 [%0];" ::"l"(xr + D - 1));
                 const float thr = __ldg(xn2 + f) + tie_wpart(__ldg(w2max), S, win);
                 float B1 = CUDART_INF_F;
                 for (uint32_t g = 0; g < groups; ++g) B1 = fminf(B1, part[(size_t)g * 4 * n + f]);

@@ -3,7 +3,7 @@
 # candidate merge and the near-tie row split
 ncu --set full --import-source on --clock-control none --kernel-name-base demangled \
     --profile-from-start off \
-    -k regex:"k1_bmu_tc<.int.2, .bool.1|k_merge_partials|k_split_rows|k_scatter|k_merge_fast4" \
+    -k regex:"${NCU_K:-k1_bmu_tc<.int.2, .bool.1|k_merge_partials|k_split_rows|k_scatter|k_merge_fast4}" \
     -o gpurun_out/neartie -f \
     python scripts/neartie_target.py 10000000 6 > gpurun_out/neartie.log 2>&1
 python scripts/ncu_summary.py gpurun_out/neartie.ncu-rep > gpurun_out/neartie_summary.json
