@@ -521,8 +521,11 @@ void accumulate_epoch(Engine* eng, const uint32_t* sel_host, uint64_t n_sel, boo
         eng->chunk_counts.clear();
         eng->recheck_from_chunks = true;
         eng->hstat_counts = true;
-        CU(cudaMemcpyAsync(eng->hstat, eng->flags.p, 2 * sizeof(uint32_t), cudaMemcpyDeviceToHost,
-                           eng->stream));
+        // (a multi-epoch call reads only its last epoch's counts: a D2H copy
+        // in the middle of the stream costs ~15 us of device time per epoch)
+        if (!eng->defer_hstat)
+            CU(cudaMemcpyAsync(eng->hstat, eng->flags.p, 2 * sizeof(uint32_t),
+                               cudaMemcpyDeviceToHost, eng->stream));
     } else {
         // Streamed: rows live in host memory; chunks of stream_chunk_rows rows
         // are copied on copy_stream into two device stages, compute on stream.
@@ -757,7 +760,7 @@ void smooth(Engine* eng, double eta) {
     CU(eng->smooth_scratch.ensure(tsom::smooth_scratch_doubles(eng->P, eng->D) * sizeof(double)));
     tsom::launch_smooth(eng->infl.as<double>(), eng->sums.as<double>(), eng->w.as<float>(), eng->P,
                         eng->D, eta, eng->U.as<double>(), eng->H.as<double>(),
-                        eng->smooth_scratch.as<double>(), eng->stream);
+                        eng->smooth_scratch.as<double>(), eng->stream, eng->status.as<int>());
     CU(cudaGetLastError());
     CU(cudaEventRecord(eng->ev[7], eng->stream));
 }
@@ -1786,8 +1789,8 @@ static void train_epoch_enqueue(Engine* eng, double eta, double sigma, double mo
     // the term guard on this epoch's rows and codebook; a violation records
     // the failure before the update, which then leaves the weights as they
     // were (the reference throws out of run_iteration, trainer.hpp:506)
+    // (apply_update's fault slot was reset by the smoothing's last kernel)
     eng->last_guard_tag = enqueue_term_guard(eng, eta, dead, epoch);
-    tsom::launch_status_reset(eng->status.as<int>(), eng->stream);
     tsom::launch_apply_update_guarded(eng->w.as<float>(), eng->prev.as<float>(), eng->P,
                                       eng->D, eng->U.as<double>(), eng->H.as<double>(),
                                       momentum_on, momentum, eng->status.as<int>(), dead,
@@ -1837,11 +1840,15 @@ int tsom_train_epochs(tsom_engine* eng, uint32_t n_epochs, const double* eta,
         int* dead = eng->dead.as<int>();
         struct SlotReset {
             Engine* e;
-            ~SlotReset() { e->k1_slot = -1; }
+            ~SlotReset() {
+                e->k1_slot = -1;
+                e->defer_hstat = false;
+            }
         } reset{eng};
         for (uint32_t t = 0; t < n_epochs; ++t) {
             eng->k1_slot = (int)t;
             eng->k1_timed = false;
+            eng->defer_hstat = t + 1 < n_epochs;
             train_epoch_enqueue(eng, eta[t], sigma[t], momentum, flags, dead, t);
             tsom::launch_epoch_guard(eng->status.as<int>(), t, dead, eng->stream);
             CU(cudaGetLastError());

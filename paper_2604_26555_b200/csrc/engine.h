@@ -313,6 +313,7 @@ struct Engine {
     DevBuf tie_dev;  // the counts themselves, written by k_tie_pass_counts
     uint32_t tie_log_n = 0;
     double tie_frac_max = -1.0;  // < 0: nothing observed yet
+    bool defer_hstat = false;  // tsom_train_epochs: skip the count copy but for the last epoch
     bool hstat_counts = false;  // [0..1] hold this epoch's re-check counts
     bool recheck_from_chunks = false;
     // term guard (k_guard.cu): max |h| of the influence (device double), the
@@ -462,8 +463,10 @@ void launch_pad_rows(const float* x, uint64_t n, uint32_t D, float* xpad, cudaSt
 constexpr size_t kRowSlack = 64;
 
 // K3: smoothing num = H^T S, den = H^T c; U = eta (num - w den), H = den
+// status (optional): apply_update's fault slot, reset to INT_MAX here
 void launch_smooth(const double* infl, const double* sums, const float* w, uint32_t P, uint32_t D,
-                   double eta, double* U, double* H, double* scratch, cudaStream_t st);
+                   double eta, double* U, double* H, double* scratch, cudaStream_t st,
+                   int* status = nullptr);
 size_t smooth_scratch_doubles(uint32_t P, uint32_t D);
 // apply_update on device (trainer.hpp:341-369); status[0] = first bad node + 1
 void launch_apply_update(float* w, float* prev, uint32_t P, uint32_t D, const double* U,

@@ -596,9 +596,13 @@ __global__ void __launch_bounds__(kTmaWarps * 32, 2) k_gather_tma(
 // stride the node's pieces, fixed xor tree (deterministic, skew-proof)
 __global__ void k_piece_reduce(const double* __restrict__ partial,
                                const uint32_t* __restrict__ piece_start, uint32_t P, uint32_t D,
-                               double* __restrict__ sums, int add) {
+                               double* __restrict__ sums, int add, double rows) {
     const size_t e = (blockIdx.x * (size_t)blockDim.x + threadIdx.x) >> 5;
     const int lane = threadIdx.x & 31;
+    if (blockIdx.x == 0 && threadIdx.x == 0) {  // the pass's row count (k_add_rowcount)
+        double* t = sums + (size_t)P * D + P + 1;
+        *t = add ? *t + rows : rows;
+    }
     if (e >= (size_t)P * D) return;
     const uint32_t Dp = D + 1;
     const uint32_t b = (uint32_t)(e / D), k = (uint32_t)(e % D);
@@ -881,10 +885,10 @@ int launch_accumulate(const float* x, const uint32_t* sel, uint64_t n, uint32_t 
     }
     if (accumulate)
         TSOM_LAUNCH(k_piece_reduce<<<(unsigned)((m * 32 + 255) / 256), 256, 0, st>>>(
-            s.partial, s.piece_start, P, D, sums, add));
+            s.partial, s.piece_start, P, D, sums, add, (double)n));
     if (want_dist)
         TSOM_LAUNCH(k_dist_reduce<<<1, 1024, 0, st>>>(s.partial, s.piece_start, P, D, sums, add));
-    TSOM_LAUNCH(k_add_rowcount<<<1, 1, 0, st>>>(sums, P, D, (double)n, add));
+    if (!accumulate) TSOM_LAUNCH(k_add_rowcount<<<1, 1, 0, st>>>(sums, P, D, (double)n, add));
     return 0;
 }
 

@@ -116,8 +116,9 @@ __global__ void __launch_bounds__(256) k_smooth_gemm(const double* __restrict__ 
 // U = eta * (sum_z partial[z] - w * Hx), fixed slice order (deterministic)
 __global__ void k_smooth_finish(const double* __restrict__ partial, const float* __restrict__ w,
                                 const double* __restrict__ H, uint32_t P, uint32_t D, double eta,
-                                double* __restrict__ U) {
+                                double* __restrict__ U, int* __restrict__ status) {
     const size_t e = blockIdx.x * (size_t)blockDim.x + threadIdx.x;
+    if (status && e == 0) *status = INT_MAX;  // apply_update's fault slot (k_status_reset)
     if (e >= (size_t)P * D) return;
     double s = 0.0;
     for (int z = 0; z < SM_SPLIT; ++z) s += partial[(size_t)z * P * D + e];
@@ -125,7 +126,8 @@ __global__ void k_smooth_finish(const double* __restrict__ partial, const float*
 }
 
 void launch_smooth(const double* infl, const double* sums, const float* w, uint32_t P, uint32_t D,
-                   double eta, double* U, double* H, double* scratch, cudaStream_t st) {
+                   double eta, double* U, double* H, double* scratch, cudaStream_t st,
+                   int* status) {
     // scratch: P*(d+1) (saug) + SM_SPLIT*P*d (slice partials) + P (Hx) doubles
     double* saug = scratch;
     double* partial = scratch + (size_t)P * (D + 1);
@@ -137,7 +139,7 @@ void launch_smooth(const double* infl, const double* sums, const float* w, uint3
     TSOM_LAUNCH(k_smooth_gemm<<<grid, 256, 0, st>>>(infl, saug, P, D, partial));
     const size_t pd = (size_t)P * D;
     TSOM_LAUNCH(k_smooth_finish<<<(unsigned)((pd + 255) / 256), 256, 0, st>>>(partial, w, Hx, P,
-                                                                            D, eta, U));
+                                                                            D, eta, U, status));
 }
 
 size_t smooth_scratch_doubles(uint32_t P, uint32_t D) {
