@@ -336,25 +336,61 @@ __device__ __forceinline__ void hist_add(uint32_t* h, uint32_t bin, bool active)
     if (active && (__ffs(peers) - 1) == (int)lane) atomicAdd(&h[bin], (uint32_t)__popc(peers));
 }
 
-// sortable 64-bit key: (seen << 63) | bits(key), key >= 0 (sampling.hpp:116-133)
-__global__ void k_adapt_keys(const double* __restrict__ err, uint32_t* __restrict__ age,
-                             const uint64_t* __restrict__ draws, uint64_t n, double alpha,
-                             double beta, int pending, const unsigned long long* __restrict__ mx,
-                             unsigned long long* __restrict__ keys) {
+// sortable 64-bit key: (seen << 63) | bits(key), key >= 0 (sampling.hpp:116-133),
+// and the histogram of the keys' first radix digit (bits 52-63, over every key,
+// so no second pass over the N keys is made for it).  The age term
+// a / max_age takes few values (ages count epochs): it comes from a per-block
+// table of the same IEEE quotients for a < kAgeTab.
+constexpr uint32_t kAgeTab = 1024;
+__global__ void __launch_bounds__(256) k_adapt_keys(
+    const double* __restrict__ err, uint32_t* __restrict__ age, const uint64_t* __restrict__ draws,
+    uint64_t n, double alpha, double beta, int pending, const unsigned long long* __restrict__ mx,
+    unsigned long long* __restrict__ keys, uint32_t* __restrict__ hist) {
+    __shared__ uint32_t h[4096];
+    __shared__ double agetab[kAgeTab];
     const double max_err = fmax(__longlong_as_double((long long)mx[0]), 1e-12);
     const double max_age = fmax((double)mx[1], 1e-12);
-    for (uint64_t i = blockIdx.x * (uint64_t)blockDim.x + threadIdx.x; i < n;
-         i += (uint64_t)gridDim.x * blockDim.x) {
-        const double e = err[i];
-        const uint32_t a = age_now(age[i], pending);
-        if (pending) age[i] = a;
-        const double w = pow_ref(e / max_err, alpha) + pow_ref((double)a / max_age, beta);
-        const double u = 1.0 - (double)(draws[i] >> 11) * 0x1.0p-53;
-        double key = w > 0.0 ? -log(u) / w : CUDART_INF;
-        key = fmax(key, 0.0);  // -log(1) = -0
-        const unsigned long long seen = e != 1e30 ? 1ULL : 0ULL;
-        keys[i] = (seen << 63) | (unsigned long long)__double_as_longlong(key);
+    for (int i = threadIdx.x; i < 4096; i += blockDim.x) h[i] = 0;
+    for (uint32_t a = threadIdx.x; a < kAgeTab; a += blockDim.x) agetab[a] = (double)a / max_age;
+    __syncthreads();
+    // kU elements per thread and step, all loads issued before the arithmetic
+    constexpr int kU = 4;
+    const uint64_t stride = (uint64_t)gridDim.x * blockDim.x * kU;
+    for (uint64_t i0 = blockIdx.x * (uint64_t)blockDim.x * kU; i0 < n; i0 += stride) {
+        double e[kU];
+        uint32_t a[kU];
+        uint64_t dr[kU];
+#pragma unroll
+        for (int q = 0; q < kU; ++q) {
+            const uint64_t i = i0 + (uint64_t)q * blockDim.x + threadIdx.x;
+            const bool in = i < n;
+            e[q] = in ? err[i] : 0.0;
+            a[q] = in ? age[i] : 0u;
+            dr[q] = in ? draws[i] : 0ull;
+        }
+#pragma unroll
+        for (int q = 0; q < kU; ++q) {
+            const uint64_t i = i0 + (uint64_t)q * blockDim.x + threadIdx.x;
+            const bool in = i < n;
+            unsigned long long kb = 0;
+            if (in) {
+                const uint32_t an = age_now(a[q], pending);
+                if (pending) age[i] = an;
+                const double ta = an < kAgeTab ? agetab[an] : (double)an / max_age;
+                const double w = pow_ref(e[q] / max_err, alpha) + pow_ref(ta, beta);
+                const double u = 1.0 - (double)(dr[q] >> 11) * 0x1.0p-53;
+                double key = w > 0.0 ? -log(u) / w : CUDART_INF;
+                key = fmax(key, 0.0);  // -log(1) = -0
+                const unsigned long long seen = e[q] != 1e30 ? 1ULL : 0ULL;
+                kb = (seen << 63) | (unsigned long long)__double_as_longlong(key);
+                keys[i] = kb;
+            }
+            hist_add(h, (uint32_t)(kb >> 52), in);
+        }
     }
+    __syncthreads();
+    for (int i = threadIdx.x; i < 4096; i += blockDim.x)
+        if (h[i]) atomicAdd(&hist[i], h[i]);
 }
 
 // Keys in the first digit's chosen bucket -> cand[] with the histogram of
@@ -410,29 +446,6 @@ __global__ void k_adapt_hist_cand(const unsigned long long* __restrict__ cand, u
         const uint32_t i = i0 + threadIdx.x;
         const unsigned long long k = i < m ? seg[i] : 0ULL;
         hist_add(h, (uint32_t)((k >> shift) & dmask), i < m && (k & hi_mask) == prefix);
-    }
-    __syncthreads();
-    for (int i = threadIdx.x; i < 4096; i += blockDim.x)
-        if (h[i]) atomicAdd(&hist[i], h[i]);
-}
-
-// one radix-select digit (`width` <= 12 bits at `shift`) over keys matching
-// the prefix fixed so far above it
-__global__ void k_adapt_hist(const unsigned long long* __restrict__ keys, uint64_t n,
-                             const unsigned long long* __restrict__ sel_state, int shift,
-                             int width, uint32_t* __restrict__ hist) {
-    __shared__ uint32_t h[4096];
-    for (int i = threadIdx.x; i < 4096; i += blockDim.x) h[i] = 0;
-    __syncthreads();
-    const unsigned long long prefix = sel_state[0];
-    const unsigned long long hi_mask = shift + width >= 64 ? 0ULL : (~0ULL << (shift + width));
-    const unsigned long long dmask = (1ULL << width) - 1ULL;
-    const uint64_t stride = (uint64_t)gridDim.x * blockDim.x;
-    for (uint64_t i0 = blockIdx.x * (uint64_t)blockDim.x; i0 < n; i0 += stride) {
-        const uint64_t i = i0 + threadIdx.x;
-        const unsigned long long k = i < n ? keys[i] : 0ULL;
-        const bool in = i < n && (k & hi_mask) == prefix;
-        hist_add(h, (uint32_t)((k >> shift) & dmask), in);
     }
     __syncthreads();
     for (int i = threadIdx.x; i < 4096; i += blockDim.x)
@@ -839,7 +852,8 @@ int sampler_select(SamplerState& s, uint32_t* out, uint64_t* m_out, int sm_count
         uint32_t* ccnt = s.ccnt.as<uint32_t>();
         const uint64_t chunk = (n + kCompactBlocks - 1) / kCompactBlocks;
         TSOM_LAUNCH(k_adapt_keys<<<grid, 256, 0, st>>>(s.err.as<double>(), s.age.as<uint32_t>(),
-                                                       draws, n, s.alpha, s.beta, pending, mx, keys));
+                                                       draws, n, s.alpha, s.beta, pending, mx, keys,
+                                                       s.hist.as<uint32_t>()));
         s.age_pending = false;  // the keys pass wrote the ages back
         // digits of the 64-bit key: bits 52-63, 40-51, 28-39, 16-27, 4-15, 0-3.
         // Digit 0 scans every key, digit 1 comes with the compaction of digit
@@ -848,13 +862,11 @@ int sampler_select(SamplerState& s, uint32_t* out, uint64_t* m_out, int sm_count
         // everywhere: one global threshold).
         const int shifts[6] = {52, 40, 28, 16, 4, 0}, widths[6] = {12, 12, 12, 12, 12, 4};
         for (int d = 0; d < 6; ++d) {
-            if (d == 0)
-                TSOM_LAUNCH(k_adapt_hist<<<grid, 256, 0, st>>>(keys, n, rs, shifts[d], widths[d],
-                                                               s.hist.as<uint32_t>()));
-            else if (d == 1)
+            // (digit 0's histogram came with the keys, k_adapt_keys)
+            if (d == 1)
                 TSOM_LAUNCH(k_adapt_compact<<<kCompactBlocks, 256, 0, st>>>(
                     keys, n, chunk, rs, cand, ccnt, s.hist.as<uint32_t>()));
-            else
+            else if (d >= 2)
                 TSOM_LAUNCH(k_adapt_hist_cand<<<kCompactBlocks, 256, 0, st>>>(
                     cand, chunk, ccnt, rs, shifts[d], widths[d], s.hist.as<uint32_t>()));
             if (s.sharded) ok &= s.allreduce(s.hist.p, 4096, 0);
