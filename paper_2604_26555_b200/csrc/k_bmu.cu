@@ -24,42 +24,30 @@ namespace tsom {
 
 // SIMT operand wt ((d+1) x Ppad: -2 w^T and the ||w||^2 row), FP64 norms w2
 // and max ||w||^2 (the error window).
-__global__ void __launch_bounds__(1024) k_prep_codebook(const float* __restrict__ w, uint32_t P,
-                                                        uint32_t D, double* __restrict__ w2,
-                                                        float* __restrict__ w2max,
-                                                        float* __restrict__ wt, uint32_t Ppad) {
-    // one block: the max is reduced in the block (no memset + atomic pass)
-    // (the max is taken on the bit patterns, as the former atomicMax was: a NaN
-    // norm propagates into the window instead of being dropped)
-    __shared__ int red[32];
-    int mx = 0;
-    for (uint32_t j = threadIdx.x; j < Ppad; j += blockDim.x) {
-        if (j >= P) {  // padding node: never wins
-            for (uint32_t k = 0; k < D; ++k) wt[(size_t)k * Ppad + j] = 0.0f;
-            wt[(size_t)D * Ppad + j] = CUDART_INF_F;
-            continue;
-        }
-        const float* wj = w + (size_t)j * D;
-        double s = 0.0;
-        for (uint32_t k = 0; k < D; ++k) s = __dadd_rn(s, __dmul_rn((double)wj[k], (double)wj[k]));
-        w2[j] = s;
-        mx = max(mx, __float_as_int((float)s * 1.0000003f));
-        for (uint32_t k = 0; k < D; ++k) wt[(size_t)k * Ppad + j] = -2.0f * wj[k];
-        wt[(size_t)D * Ppad + j] = (float)s;
+__global__ void k_prep_codebook(const float* __restrict__ w, uint32_t P, uint32_t D,
+                                double* __restrict__ w2, float* __restrict__ w2max,
+                                float* __restrict__ wt, uint32_t Ppad) {
+    const uint32_t j = blockIdx.x * blockDim.x + threadIdx.x;
+    if (j >= Ppad) return;
+    if (j >= P) {  // padding node: never wins
+        for (uint32_t k = 0; k < D; ++k) wt[(size_t)k * Ppad + j] = 0.0f;
+        wt[(size_t)D * Ppad + j] = CUDART_INF_F;
+        return;
     }
-    for (int o = 16; o; o >>= 1) mx = max(mx, __shfl_xor_sync(0xffffffffu, mx, o));
-    if ((threadIdx.x & 31) == 0) red[threadIdx.x >> 5] = mx;
-    __syncthreads();
-    if (threadIdx.x < 32) {
-        mx = threadIdx.x < blockDim.x / 32 ? red[threadIdx.x] : 0;
-        for (int o = 16; o; o >>= 1) mx = max(mx, __shfl_xor_sync(0xffffffffu, mx, o));
-        if (threadIdx.x == 0) *w2max = __int_as_float(mx);
-    }
+    const float* wj = w + (size_t)j * D;
+    double s = 0.0;
+    for (uint32_t k = 0; k < D; ++k) s = __dadd_rn(s, __dmul_rn((double)wj[k], (double)wj[k]));
+    w2[j] = s;
+    atomicMax(reinterpret_cast<int*>(w2max), __float_as_int((float)s * 1.0000003f));
+    for (uint32_t k = 0; k < D; ++k) wt[(size_t)k * Ppad + j] = -2.0f * wj[k];
+    wt[(size_t)D * Ppad + j] = (float)s;
 }
 
 void launch_prep_codebook(const float* w, uint32_t P, uint32_t D, double* w2, float* w2max,
                           float* wt, uint32_t Ppad, cudaStream_t st) {
-    TSOM_LAUNCH(k_prep_codebook<<<1, 1024, 0, st>>>(w, P, D, w2, w2max, wt, Ppad));
+    // (one block reducing the maximum itself instead: 21 us vs 4.5 + 1.6 us)
+    cudaMemsetAsync(w2max, 0, sizeof(float), st);
+    TSOM_LAUNCH(k_prep_codebook<<<(Ppad + 127) / 128, 128, 0, st>>>(w, P, D, w2, w2max, wt, Ppad));
 }
 
 // ---------------------------------------------------------------------------
