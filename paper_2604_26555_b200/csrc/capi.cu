@@ -212,10 +212,13 @@ void run_bmu(Engine* eng, const float* x, uint32_t ldx, const uint32_t* sel, uin
         const float* scale = eng->scale.as<float>();
         const tsom::TieWin win = tie_window(eng, kind);
         CU(eng->ties.ensure((n + 1) * sizeof(uint32_t)));
+        CU(eng->tcls.ensure(2 * tsom::kTieClasses * sizeof(uint32_t)));
         // operand scale + codebook B operand for these rows (a few microseconds);
-        // the re-check counters and the near-tie count start at zero
+        // the re-check counters, the near-tie count and its class counters
+        // start at zero
         tsom::launch_set_scale(kind, x2max, eng->scale.as<float>(), eng->stream,
-                               eng->flags.as<uint32_t>(), 2, eng->ties.as<uint32_t>());
+                               eng->flags.as<uint32_t>(), 2, eng->ties.as<uint32_t>(),
+                               eng->tcls.as<uint32_t>(), 2 * tsom::kTieClasses);
         CU(eng->wsplit.ensure(tsom::tc_wsplit_bytes(kind, eng->P, eng->D)));
         tsom::launch_prep_wsplit(kind, eng->w.as<float>(), eng->P, eng->D, scale, eng->wsplit.p,
                                  eng->stream);
@@ -239,10 +242,17 @@ void run_bmu(Engine* eng, const float* x, uint32_t ldx, const uint32_t* sel, uin
         CU(cudaEventRecord(k1_event(eng, 1), eng->stream));
         eng->k1_timed = true;
         tsom::sampler_pregenerate(eng->sampler, k1_event(eng, 1));
-        tsom::launch_merge_fast(eng->part.as<float>(), n, groups, 1, gn, tiles_xn2,
-                                w2, scale, win,
-                                eng->bmu.as<uint32_t>(), eng->ties.as<uint32_t>(),
-                                eng->tmask.as<uint32_t>(), eng->flags.as<uint32_t>(), eng->stream);
+        // (the near-tie list's group classes are counted by the merge, and the
+        // class-sorted list's tile masks zeroed there: k_tie_classes below)
+        const uint64_t ntl = (n + tsom::kTcTileM - 1) / tsom::kTcTileM;
+        CU(eng->tsort.ensure((2 * (size_t)n + 1 + ntl + 8) * sizeof(uint32_t)));
+        uint32_t* ties_s = eng->tsort.as<uint32_t>();
+        uint32_t* tmask_s = ties_s + n + 1;
+        uint32_t* tile_mask = tmask_s + n;
+        const bool classed = tsom::launch_merge_fast(
+            eng->part.as<float>(), n, groups, 1, gn, tiles_xn2, w2, scale, win,
+            eng->bmu.as<uint32_t>(), eng->ties.as<uint32_t>(), eng->tmask.as<uint32_t>(),
+            eng->flags.as<uint32_t>(), eng->stream, eng->tcls.as<uint32_t>(), tile_mask);
         CU(cudaGetLastError());
         uint32_t* log_slot = nullptr;  // the count goes to a device log, read after the sync
         if (eng->tie_log_n < kTieLogCap) {
@@ -266,7 +276,10 @@ void run_bmu(Engine* eng, const float* x, uint32_t ldx, const uint32_t* sel, uin
         // count past the last pass only costs time (its overflow takes the
         // exact re-scan), not correctness.
         uint32_t passes = n > (1u << 20) ? kTiePasses : 1u;
-        const uint64_t cap = passes > 1 ? (n + kTieCapDiv - 1) / kTieCapDiv : n;
+        // (a multiple of the tile: pass p starts at tile p cap / 128 of the list)
+        const uint64_t cap = passes > 1
+            ? ((n + kTieCapDiv - 1) / kTieCapDiv + tsom::kTcTileM - 1) / tsom::kTcTileM * tsom::kTcTileM
+            : n;
         if (passes > 1 && eng->tie_frac_max >= 0.0) {
             const double need = 1.25 * eng->tie_frac_max * (double)n / (double)cap;
             passes = std::min<uint32_t>(kTiePasses, std::max<uint32_t>(1u, (uint32_t)std::ceil(need)));
@@ -276,7 +289,19 @@ void run_bmu(Engine* eng, const float* x, uint32_t ldx, const uint32_t* sel, uin
         CU(eng->part2.ensure((size_t)groups * 4 * cap * sizeof(float)));
         CU(eng->txn2.ensure(cap * sizeof(float)));
         CU(eng->tcnt.ensure(kTiePasses * sizeof(uint32_t)));
-        const uint32_t* tcount = eng->ties.as<uint32_t>();
+        // the near-tie list re-ordered by the groups its rows need (k_bmu.cu:
+        // k_tie_classes): the enumerate pass's tiles then each need few groups,
+        // and the CTAs of a group skip the tiles holding none of its rows
+        if (classed)
+            tsom::launch_tie_classes(eng->ties.as<uint32_t>(), eng->tmask.as<uint32_t>(), n,
+                                     eng->tcls.as<uint32_t>(), ties_s, tmask_s, tile_mask,
+                                     eng->stream);
+        else {  // (the per-row merge: the list as it is, every group every tile)
+            ties_s = eng->ties.as<uint32_t>();
+            tmask_s = eng->tmask.as<uint32_t>();
+            tile_mask = nullptr;
+        }
+        const uint32_t* tcount = ties_s;
         const uint32_t* tpos = tcount + 1;
         uint32_t* pcount = eng->tcnt.as<uint32_t>();
         TSOM_LAUNCH(k_tie_pass_counts<<<1, 32, 0, eng->stream>>>(tcount, cap, passes, pcount,
@@ -288,12 +313,13 @@ void run_bmu(Engine* eng, const float* x, uint32_t ldx, const uint32_t* sel, uin
                                     ldx);
             CU(tsom::launch_bmu_tc(kind, eng->tsplit.p, cap, pcount + pz, true, eng->P, eng->D,
                                    eng->wsplit.p, eng->txn2.as<float>(), w2, scale, win,
-                                   eng->tmask.as<uint32_t>() + o, eng->part2.as<float>(),
-                                   eng->sm_count, eng->smem_optin, eng->stream));
+                                   tmask_s + o, eng->part2.as<float>(), eng->sm_count,
+                                   eng->smem_optin, eng->stream,
+                                   tile_mask ? tile_mask + o / tsom::kTcTileM : nullptr));
             tsom::launch_merge_partials(eng->part2.as<float>(), tpos + o, pcount + pz, cap, cap,
                                         groups, gn, eng->txn2.as<float>(), w2, scale, win, x, ldx,
                                         sel, eng->w.as<float>(), eng->D, eng->bmu.as<uint32_t>(),
-                                        eng->flags.as<uint32_t>(), eng->stream);
+                                        eng->flags.as<uint32_t>(), eng->stream, tmask_s + o);
         }
     } else {
         CU(cudaEventRecord(k1_event(eng, 0), eng->stream));
@@ -783,7 +809,7 @@ void record_timing(Engine* eng) {
 std::vector<DevBuf*> all_buffers(Engine* eng) {
     return std::vector<DevBuf*>({&eng->x, &eng->xsplit, &eng->xn2, &eng->gxn2, &eng->txn2, &eng->x2max, &eng->w, &eng->wt, &eng->wsplit, &eng->w2,
                       &eng->w2max, &eng->scale, &eng->prev, &eng->infl, &eng->topo_dist, &eng->sel,
-                      &eng->rows_scratch, &eng->gsplit, &eng->bmu, &eng->dist, &eng->part,
+                      &eng->rows_scratch, &eng->gsplit, &eng->tsort, &eng->tcls, &eng->bmu, &eng->dist, &eng->part,
                       &eng->flags, &eng->ties, &eng->tmask, &eng->part2, &eng->tsplit, &eng->tcnt, &eng->acc_buf[0], &eng->acc_buf[1], &eng->acc_buf[2], &eng->acc_buf[3],
                       &eng->acc_buf[4], &eng->acc_buf[5], &eng->acc_buf[6], &eng->sums, &eng->chunk_flags,
                       &eng->topo_buf[0], &eng->topo_buf[1], &eng->topo_buf[2], &eng->topo_buf[3],

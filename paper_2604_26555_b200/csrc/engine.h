@@ -261,6 +261,7 @@ struct Engine {
     DevBuf sel;
     DevBuf rows_scratch;   // caller rows for tsom_bmu / gathered split tiles
     DevBuf gsplit;         // split tiles of a gathered selection
+    DevBuf tsort, tcls;    // near-tie list by group class + tile masks; class counters
     DevBuf bmu;
     DevBuf dist;
     DevBuf part;           // tcgen05 per-group partial top-2 [groups][n] (b1, i1, b2)
@@ -375,7 +376,8 @@ size_t tc_wsplit_bytes(int kind, uint32_t P, uint32_t D);
 // scale = {s, s^2, overflow flag}: kTcF16 picks s = 2^e from max ||x||^2 (x2max[0])
 // zero[0..nzero) and *zero2 (optional) are cleared first: the counters of the pass
 void launch_set_scale(int kind, const float* x2max, float* scale, cudaStream_t st,
-                      uint32_t* zero = nullptr, uint32_t nzero = 0, uint32_t* zero2 = nullptr);
+                      uint32_t* zero = nullptr, uint32_t nzero = 0, uint32_t* zero2 = nullptr,
+                      uint32_t* zero3 = nullptr, uint32_t nzero3 = 0);
 // tcgen05 B operand of the codebook (per group, core-matrix order)
 void launch_prep_wsplit(int kind, const float* w, uint32_t P, uint32_t D, const float* scale,
                         void* wsplit, cudaStream_t st);
@@ -395,7 +397,7 @@ cudaError_t launch_bmu_tc(int kind, const void* tiles, uint64_t n, const uint32_
                           bool enumerate, uint32_t P, uint32_t D, const void* wsplit,
                           const float* xn2, const float* w2max, const float* scale, TieWin win,
                           const uint32_t* rmask, float* part, int sm_count, size_t smem_optin,
-                          cudaStream_t st);
+                          cudaStream_t st, const uint32_t* tile_mask = nullptr);
 extern uint32_t g_k1_debug;
 extern int g_split_v1;
 extern int g_gather_kind;
@@ -404,19 +406,32 @@ int k1_trace_copy(unsigned long long* out, uint32_t n);
 int k1_set_dump(float* d_buf);  // diagnostics: option 99 bit 7 target (rows x groups*gn floats)  // diagnostics  // diagnostics: bit0 skip epilogue math, bit1 skip MMAs
 // main-pass merge: bmu for rows with a clear winner, near-tie positions -> ties
 constexpr uint32_t kTcEpiSets = 2;  // K1 main pass: partial results per group (sub-groups)
-void launch_merge_fast(const float* part, uint64_t n, uint32_t groups, uint32_t sets, uint32_t gn,
+// returns true when the near-tie rows' group classes were counted into cls
+bool launch_merge_fast(const float* part, uint64_t n, uint32_t groups, uint32_t sets, uint32_t gn,
                        const float* xn2, const float* w2max, const float* scale, TieWin win,
                        uint32_t* bmu, uint32_t* ties, uint32_t* tmask, uint32_t* flags,
-                       cudaStream_t st);
+                       cudaStream_t st, uint32_t* cls = nullptr, uint32_t* tile_mask = nullptr);
 // enumerate-pass merge over the near-tie rows: candidates -> exact FP64 -> bmu;
 // overflow -> flags list for the full re-scan.
 // ties: near-tie positions, dev_count: their number (device); rows past `cap`
 // are sent to the full re-scan; n_max bounds the count (grid sizing)
+// rmask (optional): per row the groups enumerated for it (the others skipped)
 void launch_merge_partials(const float* part, const uint32_t* ties, const uint32_t* dev_count,
                            uint64_t cap, uint64_t n_max, uint32_t groups, uint32_t gn,
                            const float* xn2, const float* w2max, const float* scale, TieWin win,
                            const float* x, uint32_t ldx, const uint32_t* sel, const float* w,
-                           uint32_t D, uint32_t* bmu, uint32_t* flags, cudaStream_t st);
+                           uint32_t D, uint32_t* bmu, uint32_t* flags, cudaStream_t st,
+                           const uint32_t* rmask = nullptr);
+// near-tie list re-ordered by the groups each row needs (k_bmu.cu)
+constexpr uint32_t kTieClasses = 9;
+#ifdef __CUDACC__
+__device__ inline uint32_t tie_class(uint32_t mask) {  // one group alone, or several
+    const uint32_t c = __popc(mask) == 1 ? (uint32_t)(__ffs(mask) - 1) : kTieClasses - 1;
+    return c < kTieClasses - 1 ? c : kTieClasses - 1;
+}
+#endif
+void launch_tie_classes(const uint32_t* ties, const uint32_t* tmask, uint64_t n_max, uint32_t* cls,
+                        uint32_t* ties_s, uint32_t* tmask_s, uint32_t* tile_mask, cudaStream_t st);
 // exact FP64 re-scan of flagged rows (reference loop order)
 void launch_rescan(const float* x, uint32_t ldx, const uint32_t* sel, const float* w, uint32_t P,
                    uint32_t D, const uint32_t* flags, uint64_t n, uint32_t* bmu, cudaStream_t st);

@@ -106,10 +106,12 @@ bool tc_supported(int kind, uint32_t P, uint32_t D) {
 // the largest power of two with max||x|| * s <= 16 (so |x_k s| <= 16 and
 // ||x s||^2 <= 256 fit FP16 with a 256x margin for ||w s||^2).
 __global__ void k_set_scale(int kind, const float* __restrict__ x2max, float* __restrict__ scale,
-                            uint32_t* __restrict__ zero, uint32_t nzero, uint32_t* __restrict__ zero2) {
+                            uint32_t* __restrict__ zero, uint32_t nzero, uint32_t* __restrict__ zero2,
+                            uint32_t* __restrict__ zero3, uint32_t nzero3) {
     // the pass's counters start at zero (no separate memset launches)
     for (uint32_t k = 0; k < nzero; ++k) zero[k] = 0u;
     if (zero2) *zero2 = 0u;
+    for (uint32_t k = 0; k < nzero3; ++k) zero3[k] = 0u;
     float s = 1.0f;
     if (kind == kTcF16) {
         const float m = *x2max;
@@ -126,8 +128,9 @@ __global__ void k_set_scale(int kind, const float* __restrict__ x2max, float* __
 }
 
 void launch_set_scale(int kind, const float* x2max, float* scale, cudaStream_t st, uint32_t* zero,
-                      uint32_t nzero, uint32_t* zero2) {
-    TSOM_LAUNCH(k_set_scale<<<1, 1, 0, st>>>(kind, x2max, scale, zero, nzero, zero2));
+                      uint32_t nzero, uint32_t* zero2, uint32_t* zero3, uint32_t nzero3) {
+    TSOM_LAUNCH(k_set_scale<<<1, 1, 0, st>>>(kind, x2max, scale, zero, nzero, zero2, zero3,
+                                             zero3 ? nzero3 : 0u));
 }
 
 __device__ __forceinline__ float tf32_trunc(float v) {
@@ -555,7 +558,7 @@ __global__ void __launch_bounds__(EpiCfg<kKind>::kThreads, 1)
               const uint8_t* __restrict__ wsplit, const float* __restrict__ xn2,
               const float* __restrict__ w2max, const float* __restrict__ scale, TieWin win,
               const uint32_t* __restrict__ rmask, float* __restrict__ part, uint32_t dbg,
-              uint32_t mc) {
+              uint32_t mc, const uint32_t* __restrict__ tile_mask) {
     // mc > 1: the CTAs of a cluster are the mc codebook groups of the same tile
     // sequence; each loads 1/mc of every A tile and multicasts it to all, so the
     // tile crosses L2 -> SM once per cluster instead of once per group.
@@ -619,6 +622,7 @@ __global__ void __launch_bounds__(EpiCfg<kKind>::kThreads, 1)
                 bulk_g2s(sW + off, wg + off, min(65536u, w_bytes - off), w_bar);
             uint32_t stage = 0, phase = 0;
             for (uint32_t t = cta_in_group; t < ntiles; t += ctas_per_group) {
+                if (kEnum && tile_mask && !((tile_mask[t] >> (g & 31)) & 1u)) continue;
                 mbar_wait(&empty_bar[stage], phase ^ 1);
                 if (dbg & 4u) {
                     mbar_arrive(&full_bar[stage]);
@@ -649,6 +653,7 @@ __global__ void __launch_bounds__(EpiCfg<kKind>::kThreads, 1)
             mbar_wait(w_bar, 0);
             uint32_t stage = 0, phase = 0, acc = 0, acc_phase = 0;
             for (uint32_t t = cta_in_group; t < ntiles; t += ctas_per_group) {
+                if (kEnum && tile_mask && !((tile_mask[t] >> (g & 31)) & 1u)) continue;
                 const uint32_t it_ = (t - cta_in_group) / ctas_per_group;
                 mbar_wait(&tempty_bar[acc], acc_phase ^ 1);
                 mbar_wait(&full_bar[stage], phase);
@@ -845,6 +850,9 @@ __global__ void __launch_bounds__(EpiCfg<kKind>::kThreads, 1)
             const uint32_t c_count = (set + 1) * nch / kSets - c_begin;
             uint32_t acc = 0, acc_phase = 0;
             for (uint32_t t = cta_in_group; t < ntiles; t += ctas_per_group) {
+                // (tiles without a row needing this group are skipped by all
+                // three roles alike; the merge ignores their records)
+                if (tile_mask && !((tile_mask[t] >> (g & 31)) & 1u)) continue;
                 const uint64_t pos = (uint64_t)t * kTcTileM + row;
                 const bool need = pos < n && ((__ldg(rmask + pos) >> (g & 31)) & 1u);
                 const float thr = need ? __ldg(xn2 + pos) + wpart : 0.0f;
@@ -956,7 +964,7 @@ cudaError_t launch_bmu_tc(int kind, const void* tiles, uint64_t n, const uint32_
                           bool enumerate, uint32_t P, uint32_t D, const void* wsplit,
                           const float* xn2, const float* w2max, const float* scale, TieWin win,
                           const uint32_t* rmask, float* part, int sm_count, size_t smem_optin,
-                          cudaStream_t st) {
+                          cudaStream_t st, const uint32_t* tile_mask) {
     if (n == 0) return cudaSuccess;
     const TcGeom geo = tc_geom(kind, D);
     const uint32_t gn = tc_group_width(P);
@@ -974,7 +982,7 @@ cudaError_t launch_bmu_tc(int kind, const void* tiles, uint64_t n, const uint32_
     if (smem > smem_optin) return cudaErrorInvalidConfiguration;
     using KernT = void (*)(const uint8_t*, uint64_t, const uint32_t*, uint32_t, uint32_t, uint32_t,
                            uint32_t, const uint8_t*, const float*, const float*, const float*,
-                           TieWin, const uint32_t*, float*, uint32_t, uint32_t);
+                           TieWin, const uint32_t*, float*, uint32_t, uint32_t, const uint32_t*);
     KernT kern;
     int slot;
     if (kind == kTcTf32) {
@@ -1042,7 +1050,8 @@ cudaError_t launch_bmu_tc(int kind, const void* tiles, uint64_t n, const uint32_
     ++g_launches;
     const cudaError_t e = cudaLaunchKernelEx(
         &cfg, kern, static_cast<const uint8_t*>(tiles), n, dev_n, groups, gn, D, stages,
-        static_cast<const uint8_t*>(wsplit), xn2, w2max, scale, win, rmask, part, g_k1_debug, mc);
+        static_cast<const uint8_t*>(wsplit), xn2, w2max, scale, win, rmask, part, g_k1_debug, mc,
+        (enumerate && mc == 1) ? tile_mask : nullptr);  // (multicast loads need every tile)
     if (e != cudaSuccess) return e;
     return cudaGetLastError();
 }

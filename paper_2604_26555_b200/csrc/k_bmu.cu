@@ -359,7 +359,7 @@ __global__ void __launch_bounds__(256) k_merge_fast4(
     const float* __restrict__ part, uint64_t n, uint32_t gn, const float* __restrict__ xn2,
     const float* __restrict__ w2max, const float* __restrict__ scale, TieWin win,
     uint32_t* __restrict__ bmu, uint32_t* __restrict__ ties, uint32_t* __restrict__ tmask,
-    uint32_t* __restrict__ flags) {
+    uint32_t* __restrict__ flags, uint32_t* __restrict__ cls, uint32_t* __restrict__ tile_mask) {
     const uint64_t q = blockIdx.x * (uint64_t)blockDim.x + threadIdx.x;  // row quad
     const uint64_t i0 = q * 4;
     const bool valid = i0 < n;
@@ -423,13 +423,25 @@ __global__ void __launch_bounds__(256) k_merge_fast4(
     // 1024 rows (a per-warp atomic on the one counter serialises ~2e5 atomics
     // per epoch at a 3 % near-tie rate); slots within the block in (warp, r,
     // lane) order
-    __shared__ uint32_t wtot[8], blk_base;
+    __shared__ uint32_t wtot[8], blk_base, ccount[kTieClasses];
     const uint32_t warp = threadIdx.x >> 5;
     uint32_t wcount = 0;
 #pragma unroll
     for (int r = 0; r < 4; ++r) wcount += __popc(ballots[r]);
     if (lane == 0) wtot[warp] = wcount;
+    if (cls && threadIdx.x < kTieClasses) ccount[threadIdx.x] = 0u;
+    // k_tie_classes' tile masks start at zero (this block: 1024 list slots)
+    if (tile_mask && threadIdx.x < 1024u / kTcTileM)
+        tile_mask[blockIdx.x * (1024u / kTcTileM) + threadIdx.x] = 0u;
     __syncthreads();
+    if (cls) {  // the near-tie rows' group classes (k_tie_classes), counted here
+#pragma unroll
+        for (int r = 0; r < 4; ++r)
+            if ((ballots[r] >> lane) & 1u) {
+                const uint32_t c = tie_class(masks[r]);
+                atomicAdd(&ccount[c], 1u);
+            }
+    }
     if (threadIdx.x == 0) {
         uint32_t t = 0;
         for (uint32_t k = 0; k < blockDim.x / 32; ++k) {
@@ -440,6 +452,8 @@ __global__ void __launch_bounds__(256) k_merge_fast4(
         blk_base = t ? atomicAdd(&ties[0], t) : 0u;
     }
     __syncthreads();
+    if (cls && threadIdx.x < kTieClasses && ccount[threadIdx.x])
+        atomicAdd(&cls[threadIdx.x], ccount[threadIdx.x]);
     uint32_t base = blk_base + wtot[warp];
 #pragma unroll
     for (int r = 0; r < 4; ++r) {
@@ -453,18 +467,19 @@ __global__ void __launch_bounds__(256) k_merge_fast4(
     if (valid) *reinterpret_cast<uint4*>(bmu + i0) = make_uint4(out[0], out[1], out[2], out[3]);
 }
 
-void launch_merge_fast(const float* part, uint64_t n, uint32_t groups, uint32_t sets, uint32_t gn,
+bool launch_merge_fast(const float* part, uint64_t n, uint32_t groups, uint32_t sets, uint32_t gn,
                        const float* xn2, const float* w2max, const float* scale, TieWin win,
                        uint32_t* bmu, uint32_t* ties, uint32_t* tmask, uint32_t* flags,
-                       cudaStream_t st) {
-    if (n == 0) return;
+                       cudaStream_t st, uint32_t* cls, uint32_t* tile_mask) {
+    if (n == 0) return false;
     if (sets == 1 && n % 4 == 0 && groups <= 8 && !g_merge_v1) {
         const unsigned blocks = (unsigned)((n / 4 + 255) / 256);
 #define TSOM_MERGE4(G)                                                                       \
     case G:                                                                                  \
         TSOM_LAUNCH(k_merge_fast4<G><<<blocks, 256, 0, st>>>(part, n, gn, xn2, w2max, scale, \
-                                                             win, bmu, ties, tmask, flags)); \
-        return;
+                                                             win, bmu, ties, tmask, flags,   \
+                                                             cls, tile_mask));               \
+        return cls != nullptr;
         switch (groups) {
             TSOM_MERGE4(1) TSOM_MERGE4(2) TSOM_MERGE4(3) TSOM_MERGE4(4)
             TSOM_MERGE4(5) TSOM_MERGE4(6) TSOM_MERGE4(7) TSOM_MERGE4(8)
@@ -473,10 +488,75 @@ void launch_merge_fast(const float* part, uint64_t n, uint32_t groups, uint32_t 
     }
     TSOM_LAUNCH(k_merge_fast<<<(unsigned)((n + 255) / 256), 256, 0, st>>>(
         part, n, groups, sets, gn, xn2, w2max, scale, win, bmu, ties, tmask, flags));
+    return false;  // (no group classes counted: the near-tie list stays as it is)
 }
 
 int g_merge_v1 = 0;  // diagnostics (TSOM option 96): 1 = the per-row merge
 
+
+// Near-tie rows by the codebook groups they need enumerated (their window
+// mask from k_merge_fast4): class g < kTieClasses - 1 = group g alone, the
+// last class = several (or a group past the classes).  The list is re-ordered
+// class by class, so the enumerate pass's 128-row tiles are (nearly all) of one
+// class, and tile_mask[t] = OR of the tile's row masks tells the CTAs of group
+// g which tiles hold any row of theirs: most near-ties need one group, which
+// then does all their enumerate work instead of every group.
+// In: the class counts cls[0, kTieClasses) and the zeroed tile masks (both from
+// k_merge_fast4).  Out: ties_s = [count | positions], tmask_s, tile_mask.  The
+// order within a class is arbitrary (no result depends on the list order).
+// cls[kTieClasses, 2 kTieClasses) = fill counters (zeroed by k_set_scale).
+__global__ void k_tie_classes(const uint32_t* __restrict__ ties, const uint32_t* __restrict__ tmask,
+                              uint32_t* __restrict__ cls, uint32_t* __restrict__ ties_s,
+                              uint32_t* __restrict__ tmask_s, uint32_t* __restrict__ tile_mask) {
+    const uint32_t count = ties[0];
+    const uint32_t lane = threadIdx.x & 31;
+    uint32_t off[kTieClasses];
+    uint32_t run = 0;
+#pragma unroll
+    for (int c = 0; c < (int)kTieClasses; ++c) {
+        off[c] = run;
+        run += cls[c];
+    }
+    const uint32_t stride = gridDim.x * blockDim.x;
+    for (uint32_t i0 = blockIdx.x * blockDim.x; i0 < count; i0 += stride) {
+        const uint32_t i = i0 + threadIdx.x;
+        const bool in = i < count;
+        const uint32_t m = in ? tmask[i] : 0u;
+        const uint32_t c = tie_class(m);
+        const uint32_t peers = __match_any_sync(0xffffffffu, in ? c : 0xFFFFFFFFu);
+        const uint32_t leader = __ffs(peers) - 1;
+        uint32_t base = 0;
+        if (in && lane == leader) base = atomicAdd(&cls[kTieClasses + c], (uint32_t)__popc(peers));
+        base = __shfl_sync(0xffffffffu, base, leader);
+        // the class group's slots are consecutive: its leader ORs the group's
+        // masks into the (at most two) tiles they fall in
+        uint32_t mor = 0;
+#pragma unroll 8
+        for (int l = 0; l < 32; ++l) {
+            const uint32_t v = __shfl_sync(0xffffffffu, m, l);
+            if ((peers >> l) & 1u) mor |= v;
+        }
+        if (in) {
+            const uint32_t idx = off[c] + base + __popc(peers & ((1u << lane) - 1u));
+            ties_s[1 + idx] = ties[1 + i];
+            tmask_s[idx] = m;
+            if (lane == leader) {
+                const uint32_t first = off[c] + base, last = first + __popc(peers) - 1;
+                atomicOr(&tile_mask[first / kTcTileM], mor);
+                if (last / kTcTileM != first / kTcTileM) atomicOr(&tile_mask[last / kTcTileM], mor);
+            }
+        }
+    }
+    if (blockIdx.x == 0 && threadIdx.x == 0) ties_s[0] = count;
+}
+
+void launch_tie_classes(const uint32_t* ties, const uint32_t* tmask, uint64_t n_max, uint32_t* cls,
+                        uint32_t* ties_s, uint32_t* tmask_s, uint32_t* tile_mask, cudaStream_t st) {
+    const unsigned blocks = (unsigned)std::max<uint64_t>(
+        1, std::min<uint64_t>((n_max + 255) / 256, 148ull * 8));
+    TSOM_LAUNCH(k_tie_classes<<<blocks, 256, 0, st>>>(ties, tmask, cls, ties_s, tmask_s,
+                                                      tile_mask));
+}
 
 // Enumerate-pass merge over the near-tie rows f < n (position ties[f]).
 // part[g] = [raw b1 | ids 0-3 | ids 4-7 | count] (k1_bmu_tc<.., true>, 8-bit
@@ -501,7 +581,7 @@ __global__ void __launch_bounds__(kMpWarps * 32, 3) k_merge_partials(
     const float* __restrict__ xn2, const float* __restrict__ w2max,
     const float* __restrict__ scale, TieWin win, const float* __restrict__ x, uint32_t ldx,
     const uint32_t* __restrict__ sel, const float* __restrict__ w, uint32_t D,
-    uint32_t* __restrict__ bmu, uint32_t* __restrict__ flags) {
+    uint32_t* __restrict__ bmu, uint32_t* __restrict__ flags, const uint32_t* __restrict__ rmask) {
     __shared__ uint16_t pj[kMpWarps][32 * kMaxCand];  // candidate node of pair p
     __shared__ uint8_t prow[kMpWarps][32 * kMaxCand]; // owning lane of pair p
     __shared__ double pd[kMpWarps][32 * kMaxCand];    // exact squared distance
@@ -518,7 +598,7 @@ __global__ void __launch_bounds__(kMpWarps * 32, 3) k_merge_partials(
                           ((reinterpret_cast<uintptr_t>(x) | reinterpret_cast<uintptr_t>(w)) & 7u) == 0;
     for (uint64_t f0 = (blockIdx.x * (uint64_t)kMpWarps + wp) * 32; f0 < count; f0 += wstride) {
         const uint64_t f = f0 + lane;
-        uint32_t pos = 0, ncand = 0, only = 0;
+        uint32_t pos = 0, ncand = 0, only = 0, gm = 0;
         bool rescan = false;
         float lim = 0.0f;
         if (f < count) {
@@ -532,13 +612,17 @@ __global__ void __launch_bounds__(kMpWarps * 32, 3) k_merge_partials(
                 asm volatile("prefetch.global.L2 [%0];" ::"l"(xr));
                 asm volatile("prefetch.global.L2 [%0];" ::"l"(xr + D - 1));
                 const float thr = __ldg(xn2 + f) + tie_wpart(__ldg(w2max), S, win);
+                // groups enumerated for this row (the others' records are not
+                // written when their CTAs skip the row's tile)
+                gm = rmask ? rmask[f] : 0xFFFFFFFFu;
                 float B1 = CUDART_INF_F;
-                for (uint32_t g = 0; g < groups; ++g) B1 = fminf(B1, part[(size_t)g * 4 * n + f]);
+                for (uint32_t g = 0; g < groups; ++g)
+                    if ((gm >> (g & 31)) & 1u) B1 = fminf(B1, part[(size_t)g * 4 * n + f]);
                 lim = B1 + thr;
                 bool overflow = false;
                 for (uint32_t g = 0; g < groups; ++g) {
                     const float* pg = part + (size_t)g * 4 * n;
-                    if (!(pg[f] <= lim)) continue;
+                    if (!((gm >> (g & 31)) & 1u) || !(pg[f] <= lim)) continue;
                     const uint32_t cnt = __float_as_uint(pg[3 * n + f]);
                     if (cnt == 0) continue;
                     if (cnt > 8) overflow = true;
@@ -572,7 +656,7 @@ __global__ void __launch_bounds__(kMpWarps * 32, 3) k_merge_partials(
             uint32_t c = 0;
             for (uint32_t g = 0; g < groups; ++g) {
                 const float* pg = part + (size_t)g * 4 * n;
-                if (!(pg[f] <= lim)) continue;
+                if (!((gm >> (g & 31)) & 1u) || !(pg[f] <= lim)) continue;
                 const uint32_t cnt = __float_as_uint(pg[3 * n + f]);
                 const uint32_t pk0 = __float_as_uint(pg[n + f]), pk1 = __float_as_uint(pg[2 * n + f]);
                 for (uint32_t k = 0; k < cnt; ++k, ++c) {
@@ -610,14 +694,15 @@ void launch_merge_partials(const float* part, const uint32_t* ties, const uint32
                            uint64_t cap, uint64_t n_max, uint32_t groups, uint32_t gn,
                            const float* xn2, const float* w2max, const float* scale, TieWin win,
                            const float* x, uint32_t ldx, const uint32_t* sel, const float* w,
-                           uint32_t D, uint32_t* bmu, uint32_t* flags, cudaStream_t st) {
+                           uint32_t D, uint32_t* bmu, uint32_t* flags, cudaStream_t st,
+                           const uint32_t* rmask) {
     if (n_max == 0) return;
     // grid-strides over the device count; sized for the enumerate capacity
     uint64_t blocks = (std::min(cap, n_max) + kMpWarps * 32 - 1) / (kMpWarps * 32);
     blocks = std::max<uint64_t>(1, std::min<uint64_t>(blocks, 148ull * 8));
     TSOM_LAUNCH(k_merge_partials<<<(unsigned)blocks, kMpWarps * 32, 0, st>>>(
         part, ties, dev_count, cap, groups, gn, xn2, w2max, scale, win, x, ldx, sel, w, D, bmu,
-        flags));
+        flags, rmask));
 }
 
 // ---------------------------------------------------------------------------
