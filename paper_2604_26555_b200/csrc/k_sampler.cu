@@ -399,8 +399,9 @@ __global__ void __launch_bounds__(256) k_adapt_keys(
 // starting at b*chunk (no global counter); cnt[b] = its candidates.
 __global__ void k_adapt_compact(const unsigned long long* __restrict__ keys, uint64_t n,
                                 uint64_t chunk, const unsigned long long* __restrict__ sel_state,
-                                unsigned long long* __restrict__ cand, uint32_t* __restrict__ cnt,
-                                uint32_t* __restrict__ hist) {
+                                unsigned long long* __restrict__ cand, uint32_t* __restrict__ cidx,
+                                uint32_t* __restrict__ cnt, uint32_t* __restrict__ hist,
+                                uint32_t* __restrict__ bitmap) {
     __shared__ uint32_t h[4096];
     __shared__ uint32_t fill;
     for (int i = threadIdx.x; i < 4096; i += blockDim.x) h[i] = 0;
@@ -410,16 +411,27 @@ __global__ void k_adapt_compact(const unsigned long long* __restrict__ keys, uin
     const uint32_t lane = threadIdx.x & 31;
     const uint64_t c0 = blockIdx.x * chunk, c1 = min(n, c0 + chunk);
     unsigned long long* out = cand + c0;
+    uint32_t* oidx = cidx + c0;
     for (uint64_t i0 = c0; i0 < c1; i0 += blockDim.x) {
         const uint64_t i = i0 + threadIdx.x;
         const unsigned long long k = i < c1 ? keys[i] : ~0ULL;
         const bool in = i < c1 && (k >> 52) == top;
+        // every key below the first digit's bucket is below the threshold: its
+        // row is selected here, one bitmap word per warp (chunk and the warp's
+        // rows are 32-aligned); the bucket's own rows are decided by
+        // k_adapt_mark_cand once the threshold is complete
+        const uint32_t take = __ballot_sync(0xffffffffu, i < c1 && (k >> 52) < top);
+        if (lane == 0 && i < c1) bitmap[i >> 5] = take;
         const uint32_t ballot = __ballot_sync(0xffffffffu, in);
         if (ballot) {
             uint32_t base = 0;
             if (lane == 0) base = atomicAdd(&fill, (uint32_t)__popc(ballot));
             base = __shfl_sync(0xffffffffu, base, 0);
-            if (in) out[base + __popc(ballot & ((1u << lane) - 1u))] = k;
+            if (in) {
+                const uint32_t slot = base + __popc(ballot & ((1u << lane) - 1u));
+                out[slot] = k;
+                oidx[slot] = (uint32_t)i;
+            }
             hist_add(h, (uint32_t)((k >> 40) & 4095ULL), in);
         }
     }
@@ -507,18 +519,27 @@ __global__ void __launch_bounds__(1024) k_adapt_digit(uint32_t* __restrict__ his
     for (int i = 0; i < 4; ++i) hist[4 * t + i] = 0;
 }
 
-// rows with key < T, plus the first `need` rows with key == T (ties at the
-// boundary are implementation-defined in the reference; counted in status)
-__global__ void k_adapt_mark(const unsigned long long* __restrict__ keys, uint64_t n,
-                             const unsigned long long* __restrict__ sel_state,
-                             uint32_t* __restrict__ bitmap, unsigned long long* __restrict__ eq) {
+// the first digit's bucket (k_adapt_compact's segments): rows with key < T,
+// plus the first `need` rows with key == T (ties at the boundary are
+// implementation-defined in the reference; counted in status).  The rows below
+// the bucket were selected by the compaction.
+__global__ void k_adapt_mark_cand(const unsigned long long* __restrict__ cand,
+                                  const uint32_t* __restrict__ cidx, uint64_t chunk,
+                                  const uint32_t* __restrict__ cnt,
+                                  const unsigned long long* __restrict__ sel_state,
+                                  uint32_t* __restrict__ bitmap, unsigned long long* __restrict__ eq) {
     const unsigned long long T = sel_state[0], need = sel_state[1];
-    for (uint64_t i = blockIdx.x * (uint64_t)blockDim.x + threadIdx.x; i < n;
-         i += (uint64_t)gridDim.x * blockDim.x) {
-        const unsigned long long k = keys[i];
+    const unsigned long long* seg = cand + blockIdx.x * chunk;
+    const uint32_t* sidx = cidx + blockIdx.x * chunk;
+    const uint32_t m = cnt[blockIdx.x];
+    for (uint32_t i = threadIdx.x; i < m; i += blockDim.x) {
+        const unsigned long long k = seg[i];
         bool take = k < T;
         if (k == T) take = atomicAdd(eq, 1ULL) < need;
-        if (take) atomicOr(&bitmap[i >> 5], 1u << (i & 31));
+        if (take) {
+            const uint32_t r = sidx[i];
+            atomicOr(&bitmap[r >> 5], 1u << (r & 31));
+        }
     }
 }
 
@@ -565,14 +586,16 @@ __global__ void k_local_slice(const uint32_t* __restrict__ glist, const unsigned
 
 // equal-to-threshold keys of this rank -> eq slot; then this rank's share of
 // the boundary ties in rank order (sel_state[1] = local need)
-__global__ void k_adapt_eq(const unsigned long long* __restrict__ keys, uint64_t n,
+__global__ void k_adapt_eq(const unsigned long long* __restrict__ cand, uint64_t chunk,
+                           const uint32_t* __restrict__ cnt,
                            const unsigned long long* __restrict__ sel_state,
                            unsigned long long* __restrict__ slot) {
+    // keys equal to T are in the first digit's bucket: its segments only
     const unsigned long long T = sel_state[0];
+    const unsigned long long* seg = cand + blockIdx.x * chunk;
+    const uint32_t m = cnt[blockIdx.x];
     unsigned long long c = 0;
-    for (uint64_t i = blockIdx.x * (uint64_t)blockDim.x + threadIdx.x; i < n;
-         i += (uint64_t)gridDim.x * blockDim.x)
-        c += keys[i] == T;
+    for (uint32_t i = threadIdx.x; i < m; i += blockDim.x) c += seg[i] == T;
     for (int o = 16; o; o >>= 1) c += __shfl_xor_sync(0xffffffffu, c, o);
     if ((threadIdx.x & 31) == 0 && c) atomicAdd(slot, c);
 }
@@ -737,7 +760,8 @@ int sampler_setup(SamplerState& s, int kind, uint64_t n, uint64_t m, uint64_t se
     if (kind == 2) {
         if (s.err.ensure(n * 8) != cudaSuccess || s.age.ensure(n * 4) != cudaSuccess ||
             s.keys.ensure(n * 8) != cudaSuccess || s.hist.ensure(4096 * 4) != cudaSuccess ||
-            s.cand.ensure(n * 8) != cudaSuccess || s.ccnt.ensure(kCompactBlocks * 4) != cudaSuccess)
+            s.cand.ensure(n * 8) != cudaSuccess || s.cidx.ensure(n * 4) != cudaSuccess ||
+            s.ccnt.ensure(kCompactBlocks * 4) != cudaSuccess)
             return 4;
         // last_error = kUnseenError (sampling.hpp:81, 91), age = 0
         const size_t chunk = 1 << 20;
@@ -850,7 +874,8 @@ int sampler_select(SamplerState& s, uint32_t* out, uint64_t* m_out, int sm_count
         auto* keys = reinterpret_cast<unsigned long long*>(s.keys.p);
         auto* cand = reinterpret_cast<unsigned long long*>(s.cand.p);
         uint32_t* ccnt = s.ccnt.as<uint32_t>();
-        const uint64_t chunk = (n + kCompactBlocks - 1) / kCompactBlocks;
+        // (a multiple of 32: a compaction warp's rows fill whole bitmap words)
+        const uint64_t chunk = ((n + kCompactBlocks - 1) / kCompactBlocks + 31) / 32 * 32;
         TSOM_LAUNCH(k_adapt_keys<<<grid, 256, 0, st>>>(s.err.as<double>(), s.age.as<uint32_t>(),
                                                        draws, n, s.alpha, s.beta, pending, mx, keys,
                                                        s.hist.as<uint32_t>()));
@@ -865,7 +890,8 @@ int sampler_select(SamplerState& s, uint32_t* out, uint64_t* m_out, int sm_count
             // (digit 0's histogram came with the keys, k_adapt_keys)
             if (d == 1)
                 TSOM_LAUNCH(k_adapt_compact<<<kCompactBlocks, 256, 0, st>>>(
-                    keys, n, chunk, rs, cand, ccnt, s.hist.as<uint32_t>()));
+                    keys, n, chunk, rs, cand, s.cidx.as<uint32_t>(), ccnt, s.hist.as<uint32_t>(),
+                    s.bitmap.as<uint32_t>()));
             else if (d >= 2)
                 TSOM_LAUNCH(k_adapt_hist_cand<<<kCompactBlocks, 256, 0, st>>>(
                     cand, chunk, ccnt, rs, shifts[d], widths[d], s.hist.as<uint32_t>()));
@@ -875,13 +901,13 @@ int sampler_select(SamplerState& s, uint32_t* out, uint64_t* m_out, int sm_count
         if (s.sharded) {  // boundary ties: taken in rank order
             auto* eq = reinterpret_cast<unsigned long long*>(s.slots.p);
             cudaMemsetAsync(eq, 0, (size_t)s.world * 8, st);
-            TSOM_LAUNCH(k_adapt_eq<<<grid, 256, 0, st>>>(
-                reinterpret_cast<const unsigned long long*>(s.keys.p), n, rs, eq + s.rank));
+            TSOM_LAUNCH(k_adapt_eq<<<kCompactBlocks, 256, 0, st>>>(cand, chunk, ccnt, rs,
+                                                                    eq + s.rank));
             ok &= s.allreduce(eq, (size_t)s.world, 2);
             TSOM_LAUNCH(k_tie_quota<<<1, 1, 0, st>>>(eq, s.world, s.rank, rs));
         }
-        TSOM_LAUNCH(k_adapt_mark<<<grid, 256, 0, st>>>(
-            reinterpret_cast<const unsigned long long*>(s.keys.p), n, rs, s.bitmap.as<uint32_t>(),
+        TSOM_LAUNCH(k_adapt_mark_cand<<<kCompactBlocks, 256, 0, st>>>(
+            cand, s.cidx.as<uint32_t>(), chunk, ccnt, rs, s.bitmap.as<uint32_t>(),
             reinterpret_cast<unsigned long long*>(misc + 2)));
         bitmap_to_list(s, n, out, st);
     }
@@ -926,7 +952,7 @@ void sampler_pregenerate(SamplerState& s, cudaEvent_t after) {
 void sampler_release(SamplerState& s) {
     if (s.side) cudaStreamSynchronize(s.side);
     for (DevBuf* d : {&s.window, &s.jp, &s.gwin, &s.misc, &s.seqb[0], &s.seqb[1], &s.drawsb[0],
-                      &s.drawsb[1], &s.tailb[0], &s.tailb[1], &s.err, &s.age, &s.keys, &s.hist, &s.cand, &s.ccnt,
+                      &s.drawsb[1], &s.tailb[0], &s.tailb[1], &s.err, &s.age, &s.keys, &s.hist, &s.cand, &s.cidx, &s.ccnt,
                       &s.first, &s.tidx, &s.bitmap, &s.bcount, &s.sel})
         d->release();
     if (s.ev_adv) cudaEventDestroy(s.ev_adv);
