@@ -175,7 +175,7 @@ struct SamplerState {
     bool want_gen = false;  // buffer `cur` still to be generated (after the next BMU kernel)
     cudaStream_t side = nullptr;
     cudaEvent_t ev_adv = nullptr, ev_gen = nullptr;
-    DevBuf err, age, keys, hist, cand, ccnt;    // adaptive (cand: first-digit bucket)
+    DevBuf err, age, keys, hist, cand, cidx, ccnt;  // adaptive (cand, cidx: first-digit bucket)
     bool age_pending = false;  // observe marked rows; +1 / 0 applied at the next select
     DevBuf first, tidx;                         // random
     DevBuf bitmap, bcount, sel;                 // selection
