@@ -312,6 +312,8 @@ def run_gpu_arm(args):
     eng = tsom.Engine(P, D, device=local)
     if args.kernel:
         eng.set_option(_lib.TSOM_OPT_BMU_KERNEL, args.kernel)
+    if args.row_order is not None:
+        eng.set_option(_lib.TSOM_OPT_ROW_ORDER, args.row_order)
     eng.bind(host)
     active_kernel = eng.active_bmu_kernel
     attach_comm(eng)
@@ -482,6 +484,8 @@ def leg_e2e(args, ctx, host, w0):
         e = tsom.Engine(P, D, device=local)
         if args.kernel:
             e.set_option(_lib.TSOM_OPT_BMU_KERNEL, args.kernel)
+        if args.row_order is not None:
+            e.set_option(_lib.TSOM_OPT_ROW_ORDER, args.row_order)
         ta = time.perf_counter()
         e.bind(rows)
         tb = time.perf_counter()
@@ -901,6 +905,8 @@ def main():
     ap.add_argument("--warmup", type=int, default=5)
     ap.add_argument("--impl", default="b200", choices=["b200", "reference"])
     ap.add_argument("--kernel", type=int, default=0, help="0 auto, 1 SIMT, 2 tcgen05 3xTF32, 3 tcgen05 3xFP16")
+    ap.add_argument("--row-order", type=int, default=None,
+                    help="TSOM_OPT_ROW_ORDER for the c2 engines (default: the engine's, 1)")
     ap.add_argument("--no-e2e", action="store_true")
     ap.add_argument("--no-cpu", action="store_true")
     ap.add_argument("--no-c4", action="store_true", help="skip the c4 (1e8 rows, adaptive) leg")

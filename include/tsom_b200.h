@@ -70,6 +70,13 @@ extern "C" {
 #define TSOM_OPT_STAGING_THREADS 6 /* host threads filling the pinned staging (default: min(16, cores)) */
 #define TSOM_OPT_PAD_ROWS 8          /* resident rows at a 256-B stride (d even, <= 62):
                                         1 (default) or 0 = packed d-float rows */
+#define TSOM_OPT_ROW_ORDER 9          /* resident rows kept in BMU order: 0 = bind order,
+                                         1 (default) = re-laid out (packed) once, in the BMU order
+                                         of the first full pass over them, R >= 2 = and again
+                                         every R full training passes.  Rows that share a BMU are
+                                         then adjacent: K1 skips the column chunks no row of a
+                                         warp needs, K2 gathers runs of rows in one copy.  Row
+                                         ids in every call stay the caller's */
 #define TSOM_OPT_BARRIER_TIMEOUT_MS 7 /* reduce-barrier deadline, ms (default 60000 =
                                          kDefaultBarrierTimeoutS, parallel.hpp:24); a rank that
                                          misses it fails the call with TSOM_ERR_TIMEOUT

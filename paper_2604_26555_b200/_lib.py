@@ -33,6 +33,7 @@ TSOM_OPT_HOST_REGISTER = 5
 TSOM_OPT_STAGING_THREADS = 6
 TSOM_OPT_BARRIER_TIMEOUT_MS = 7
 TSOM_OPT_PAD_ROWS = 8
+TSOM_OPT_ROW_ORDER = 9
 
 # Every symbol include/tsom_b200.h declares (checked by tests/test_abi.py).
 EXPORTS = [

@@ -197,8 +197,9 @@ __global__ void k_tie_pass_counts(const uint32_t* __restrict__ count, uint64_t c
 // x2max: max ||x||^2 over these rows (device; picks the FP16 operand scale).
 // `tiles` = pre-split tcgen05 A tiles for exactly these n rows, built with the
 // scale of this same x2max (or nullptr to build them here).
+// skip: the rows are the BMU-ordered bound rows (K1's chunk-skipping epilogue).
 void run_bmu(Engine* eng, const float* x, uint32_t ldx, const uint32_t* sel, uint64_t n,
-             const float* x2max, const void* tiles, const float* tiles_xn2) {
+             const float* x2max, const void* tiles, const float* tiles_xn2, bool skip = false) {
     tsom::NvtxRange nv("tsom.bmu");
     const float* xsrc = x;
     const int kind = tc_kind(eng);
@@ -238,7 +239,7 @@ void run_bmu(Engine* eng, const float* x, uint32_t ldx, const uint32_t* sel, uin
         CU(cudaEventRecord(k1_event(eng, 0), eng->stream));
         CU(tsom::launch_bmu_tc(kind, tiles, n, nullptr, false, eng->P, eng->D, eng->wsplit.p,
                                tiles_xn2, w2, scale, win, nullptr, eng->part.as<float>(),
-                               eng->sm_count, eng->smem_optin, eng->stream));
+                               eng->sm_count, eng->smem_optin, eng->stream, nullptr, skip));
         CU(cudaEventRecord(k1_event(eng, 1), eng->stream));
         eng->k1_timed = true;
         tsom::sampler_pregenerate(eng->sampler, k1_event(eng, 1));
@@ -453,6 +454,57 @@ void ensure_accum(Engine* eng, uint64_t rows) {
     eng->acc_rows = rows;
 }
 
+// TSOM_OPT_ROW_ORDER (k_order.cu).  A new bind drops the order.
+void reset_order(Engine* eng) {
+    eng->ordered = false;
+    eng->sorted_full = false;
+    eng->passes_since_order = 0;
+    eng->perm.release();
+    eng->pinv.release();
+    eng->idmap.release();
+    eng->unperm.release();
+}
+
+// Re-lay the rows out now?  Needs the engine's own resident copy and the
+// BMU-ordered positions of a full pass over them (acc.sorted): the first time
+// once one is there, then every row_order (>= 2) full training passes.
+bool order_due(const Engine* eng) {
+    if (!eng->row_order || eng->streamed || !eng->x.owned || !eng->x.p || !eng->sorted_full ||
+        eng->n_rows < 2)
+        return false;
+    if (!eng->ordered) return true;
+    return eng->row_order >= 2 && eng->passes_since_order >= eng->row_order;
+}
+
+// The resident rows re-laid out (packed: the gather then reads runs of rows in
+// one copy) in the BMU order of the last full pass; perm / pinv composed with
+// the previous order.  Costs one read + write of the rows; the split tiles are
+// rebuilt from the new layout by the pass that follows.
+void order_rows(Engine* eng) {
+    tsom::NvtxRange nv("tsom.order_rows");
+    const uint64_t n = eng->n_rows;
+    DevBuf nx, np;
+    CU(nx.ensure(n * eng->D * sizeof(float) + tsom::kRowSlack));
+    CU(np.ensure(n * sizeof(uint32_t)));
+    tsom::launch_permute_rows(eng->x.as<float>(), eng->ldx, eng->acc.sorted, n, eng->D,
+                              nx.as<float>(), eng->ordered ? eng->perm.as<uint32_t>() : nullptr,
+                              np.as<uint32_t>(), eng->stream);
+    CU(cudaGetLastError());
+    std::swap(eng->x, nx);
+    std::swap(eng->perm, np);
+    nx.release();  // (after a device synchronisation: the permute has read it)
+    np.release(true);
+    CU(eng->pinv.ensure(n * sizeof(uint32_t)));
+    tsom::launch_invert_perm(eng->perm.as<uint32_t>(), n, eng->pinv.as<uint32_t>(), eng->stream);
+    CU(cudaGetLastError());
+    eng->ldx = eng->D;
+    eng->x_slack = true;
+    eng->xsplit_valid = false;
+    eng->ordered = true;
+    eng->sorted_full = false;
+    eng->passes_since_order = 0;
+}
+
 // Exact mode: the global max ||x||^2 (once per bind; a u64 max over the ranks
 // of the float's bits — non-negative floats order like their bits) and the
 // limb buffer; returns the ExactSums of this engine.
@@ -496,8 +548,18 @@ void accumulate_epoch(Engine* eng, const uint32_t* sel_host, uint64_t n_sel, boo
             sel = sel_host;
     }
     const uint64_t n = sel ? n_sel : eng->n_rows;
-    ensure_rows(eng, n, want_dist);
     const uint32_t* dsel = dev_sel ? dev_sel : (sel ? eng->sel.as<uint32_t>() : nullptr);
+    if (!eng->streamed) {
+        if (!sel && order_due(eng)) order_rows(eng);
+        if (sel && eng->ordered && n) {  // caller row ids -> positions of the ordered rows
+            CU(eng->idmap.ensure(n * sizeof(uint32_t)));
+            tsom::launch_map_ids(dsel, n, eng->pinv.as<uint32_t>(), eng->idmap.as<uint32_t>(),
+                                 eng->stream);
+            CU(cudaGetLastError());
+            dsel = eng->idmap.as<uint32_t>();
+        }
+    }
+    ensure_rows(eng, n, want_dist);
     prep_codebook(eng);
     eng->last_recheck = 0;
     eng->recheck_from_chunks = false;
@@ -529,7 +591,7 @@ void accumulate_epoch(Engine* eng, const uint32_t* sel_host, uint64_t n_sel, boo
         tsom::ExactSums ex;
         if (eng->exact) ex = exact_setup(eng);
         run_bmu(eng, eng->x.as<float>(), eng->ldx, dsel, n, eng->x2max.as<float>(), tiles,
-                tiles_xn2);
+                tiles_xn2, eng->ordered && !sel);
         eng->pass_x = eng->x.as<float>();
         eng->pass_ldx = eng->ldx;
         eng->pass_sel = dsel;
@@ -544,6 +606,18 @@ void accumulate_epoch(Engine* eng, const uint32_t* sel_host, uint64_t n_sel, boo
         REQUIRE(arc == 0, TSOM_ERR_INVALID,
                 "exact mode (TSOM_OPT_DETERMINISTIC) needs d even and <= 62 with resident rows");
         CU(cudaGetLastError());
+        // a full pass leaves its BMU-ordered positions in acc.sorted (the
+        // next re-layout's order); per-row distances go back to caller order
+        eng->sorted_full = !sel && n == eng->n_rows && n > 0 &&
+                           (accumulate || want_dist || want_dsum);
+        if (eng->sorted_full && accumulate) ++eng->passes_since_order;
+        if (eng->ordered && !sel && want_dist && n) {
+            CU(eng->unperm.ensure(n * sizeof(double)));
+            tsom::launch_unpermute_f64(eng->dist.as<double>(), eng->perm.as<uint32_t>(), n,
+                                       eng->unperm.as<double>(), eng->stream);
+            CU(cudaGetLastError());
+            std::swap(eng->dist, eng->unperm);
+        }
         eng->chunk_counts.clear();
         eng->recheck_from_chunks = true;
         eng->hstat_counts = true;
@@ -555,6 +629,7 @@ void accumulate_epoch(Engine* eng, const uint32_t* sel_host, uint64_t n_sel, boo
     } else {
         // Streamed: rows live in host memory; chunks of stream_chunk_rows rows
         // are copied on copy_stream into two device stages, compute on stream.
+        eng->sorted_full = false;
         eng->pass_x = nullptr;
         eng->pass_sel = nullptr;
         eng->pass_n = 0;
@@ -817,7 +892,8 @@ std::vector<DevBuf*> all_buffers(Engine* eng) {
                       &eng->topo_buf[8], &eng->topo_buf[9], &eng->topo_buf[10], &eng->topo_buf[11],
                       &eng->topo_buf[12], &eng->topo_buf[13], &eng->topo_buf[14], &eng->U, &eng->H, &eng->status, &eng->smooth_scratch,
                       &eng->stage[0], &eng->stage[1], &eng->dead, &eng->hmax, &eng->guard_buf,
-                      &eng->tie_dev, &eng->xsums, &eng->xmax_g});
+                      &eng->tie_dev, &eng->xsums, &eng->xmax_g, &eng->perm, &eng->pinv,
+                      &eng->idmap, &eng->unperm});
 }
 
 }  // namespace
@@ -966,6 +1042,11 @@ int tsom_set_option(tsom_engine* eng, int key, int64_t value) {
             case TSOM_OPT_PAD_ROWS:
                 eng->pad_rows = value != 0;
                 break;
+            case TSOM_OPT_ROW_ORDER:
+                REQUIRE(value >= 0 && value <= (1 << 30), TSOM_ERR_INVALID,
+                        "option: row order 0, 1 or a re-layout period >= 2");
+                eng->row_order = (uint32_t)value;
+                break;
             case TSOM_OPT_STAGING_THREADS:
                 REQUIRE(value >= 1 && value <= 64, TSOM_ERR_INVALID,
                         "option: staging threads in [1, 64]");
@@ -989,6 +1070,7 @@ int tsom_bind_host_data(tsom_engine* eng, const float* rows, uint64_t n_rows, ui
         eng->host_direct = false;
         close_shards(eng);
         eng->xsplit_valid = false;
+        reset_order(eng);
         eng->xmax_g_ready = false;
         eng->n_rows = n_rows;
         cudaPointerAttributes pa{};
@@ -1082,6 +1164,7 @@ int tsom_bind_shards(tsom_engine* eng, const char* const* paths, uint32_t n_path
         REQUIRE(total < (1ull << 32), TSOM_ERR_INVALID, "bind: row ids are uint32 (n < 2^32)");
         eng->n_rows = total;
         eng->xsplit_valid = false;
+        reset_order(eng);
         eng->xmax_g_ready = false;
         if (flags & TSOM_BIND_STREAMED) {
             eng->streamed = true;
@@ -1134,6 +1217,7 @@ int tsom_bind_device_data(tsom_engine* eng, const float* d_rows, uint64_t n_rows
         eng->n_rows = n_rows;
         eng->streamed = false;
         eng->xsplit_valid = false;
+        reset_order(eng);
         eng->xmax_g_ready = false;
         tsom::launch_row_norm_max(d_rows, n_rows, eng->D, eng->x2max.as<float>(), eng->stream);
         CU(cudaGetLastError());
@@ -1165,6 +1249,7 @@ int tsom_bind_synthetic_gmm(tsom_engine* eng, uint64_t n_rows, uint64_t seed, ui
         CU(cudaGetLastError());
         eng->streamed = false;
         eng->xsplit_valid = false;
+        reset_order(eng);
         eng->xmax_g_ready = false;
         tsom::launch_row_norm_max(eng->x.as<float>(), n_rows, eng->D, eng->x2max.as<float>(),
                                   eng->stream, true, eng->ldx);
@@ -1184,8 +1269,18 @@ int tsom_get_rows(tsom_engine* eng, uint64_t row0, uint64_t n, float* out) {
         REQUIRE(out || n == 0, TSOM_ERR_INVALID, "get_rows: null buffer");
         if (n == 0) return;
         const size_t rowb = (size_t)eng->D * sizeof(float), pitch = (size_t)eng->ldx * sizeof(float);
-        CU(cudaMemcpy2DAsync(out, rowb, eng->x.as<float>() + row0 * eng->ldx, pitch, rowb, n,
-                             cudaMemcpyDeviceToHost, eng->stream));
+        if (eng->ordered) {  // caller rows [row0, row0 + n) sit at positions pinv[.]
+            CU(eng->rows_scratch.ensure(n * rowb));
+            tsom::launch_permute_rows(eng->x.as<float>(), eng->ldx, eng->pinv.as<uint32_t>() + row0,
+                                      n, eng->D, eng->rows_scratch.as<float>(), nullptr, nullptr,
+                                      eng->stream);
+            CU(cudaGetLastError());
+            CU(cudaMemcpyAsync(out, eng->rows_scratch.p, n * rowb, cudaMemcpyDeviceToHost,
+                               eng->stream));
+        } else {
+            CU(cudaMemcpy2DAsync(out, rowb, eng->x.as<float>() + row0 * eng->ldx, pitch, rowb, n,
+                                 cudaMemcpyDeviceToHost, eng->stream));
+        }
         CU(cudaStreamSynchronize(eng->stream));
     });
 }
@@ -1285,6 +1380,7 @@ int tsom_bmu(tsom_engine* eng, const float* rows, uint64_t n, uint32_t* bmu, dou
         run_bmu(eng, eng->rows_scratch.as<float>(), eng->D, nullptr, n, xm, nullptr, nullptr);
         if (dist) {
             ensure_accum(eng, n);
+            eng->sorted_full = false;  // acc.sorted now orders these rows
             tsom::launch_accumulate(eng->rows_scratch.as<float>(), nullptr, n, eng->D,
                                     eng->w.as<float>(), eng->P, eng->bmu.as<uint32_t>(),
                                     eng->dist.as<double>(), false, false, true, eng->acc,
@@ -1312,7 +1408,15 @@ int tsom_bmu_bound(tsom_engine* eng, const uint32_t* selected, uint64_t n_sel, u
         accumulate_epoch(eng, selected, n_sel, dist != nullptr, false, false);
         const uint64_t n = selected ? n_sel : eng->n_rows;
         if (n) {
-            CU(cudaMemcpyAsync(bmu, eng->bmu.p, n * sizeof(uint32_t), cudaMemcpyDeviceToHost,
+            const void* b = eng->bmu.p;
+            if (!selected && eng->ordered) {  // positions -> caller row order
+                CU(eng->unperm.ensure(n * sizeof(uint32_t)));
+                tsom::launch_unpermute_u32(eng->bmu.as<uint32_t>(), eng->perm.as<uint32_t>(), n,
+                                           eng->unperm.as<uint32_t>(), eng->stream);
+                CU(cudaGetLastError());
+                b = eng->unperm.p;
+            }
+            CU(cudaMemcpyAsync(bmu, b, n * sizeof(uint32_t), cudaMemcpyDeviceToHost,
                                eng->stream));
             if (dist)
                 CU(cudaMemcpyAsync(dist, eng->dist.p, n * sizeof(double), cudaMemcpyDeviceToHost,

@@ -241,6 +241,15 @@ struct Engine {
     DevBuf xn2, gxn2, txn2;  // per-row ||x||^2 for xsplit / gsplit / tsplit rows
     bool xsplit_valid = false;
     DevBuf x2max;       // float: max ||x||^2 over bound rows
+    // TSOM_OPT_ROW_ORDER (k_order.cu): the resident rows re-laid out in the BMU
+    // order of an earlier full pass — position q holds caller row perm[q],
+    // pinv is the inverse; every call still takes and returns caller row ids
+    uint32_t row_order = 1;     // 0 off, 1 once, R >= 2 also every R full passes
+    bool ordered = false;
+    DevBuf perm, pinv, idmap;   // idmap: a selection mapped to positions
+    DevBuf unperm;              // per-row outputs scattered back to caller order
+    bool sorted_full = false;   // acc.sorted = the last full pass's BMU-ordered positions
+    uint32_t passes_since_order = 0;
 
     // codebook
     DevBuf w, wt, wsplit, w2, w2max, prev;
@@ -392,12 +401,13 @@ void launch_bmu_simt(const float* x, uint32_t ldx, const uint32_t* sel, uint64_t
                      const float* w2max, float tau, uint32_t* bmu, uint32_t* flags, int sm_count,
                      cudaStream_t st);
 // tcgen05 variant: per-group partials (enumerate = candidate lists; dev_n =
-// optional device row count).
+// optional device row count; skip: the main pass over BMU-ordered rows, whose
+// epilogue skips the column chunks no row of a warp needs).
 cudaError_t launch_bmu_tc(int kind, const void* tiles, uint64_t n, const uint32_t* dev_n,
                           bool enumerate, uint32_t P, uint32_t D, const void* wsplit,
                           const float* xn2, const float* w2max, const float* scale, TieWin win,
                           const uint32_t* rmask, float* part, int sm_count, size_t smem_optin,
-                          cudaStream_t st, const uint32_t* tile_mask = nullptr);
+                          cudaStream_t st, const uint32_t* tile_mask = nullptr, bool skip = false);
 extern uint32_t g_k1_debug;
 extern int g_split_v1;
 extern int g_gather_kind;
@@ -473,6 +483,19 @@ int launch_accumulate(const float* x, const uint32_t* sel, uint64_t n, uint32_t 
 // the K2 gather's rows are then exactly two 128-byte lines
 constexpr uint32_t kPadFloats = 64;
 void launch_pad_rows(const float* x, uint64_t n, uint32_t D, float* xpad, cudaStream_t st);
+// BMU-ordered residency (k_order.cu): dst[q] = src[sorted[q]] packed, perm_out[q]
+// = perm_in[sorted[q]] (perm_in null: identity); pinv = perm^-1; out[i] =
+// pinv[sel[i]]; out[perm[q]] = v[q]
+void launch_permute_rows(const float* src, uint32_t ldx, const uint32_t* sorted, uint64_t n,
+                         uint32_t D, float* dst, const uint32_t* perm_in, uint32_t* perm_out,
+                         cudaStream_t st);
+void launch_invert_perm(const uint32_t* perm, uint64_t n, uint32_t* pinv, cudaStream_t st);
+void launch_map_ids(const uint32_t* sel, uint64_t n, const uint32_t* pinv, uint32_t* out,
+                    cudaStream_t st);
+void launch_unpermute_u32(const uint32_t* v, const uint32_t* perm, uint64_t n, uint32_t* out,
+                          cudaStream_t st);
+void launch_unpermute_f64(const double* v, const uint32_t* perm, uint64_t n, double* out,
+                          cudaStream_t st);
 // bytes of slack the engine allocates after resident rows (TMA row gathers read
 // up to 16 bytes past a row)
 constexpr size_t kRowSlack = 64;

@@ -551,7 +551,9 @@ void launch_split_rows(int kind, const float* x, const uint32_t* sel, const uint
 // overflow, 0 = group not relevant for the row (rmask)).
 // dev_n (optional): row count read on the device (the near-tie list length).
 // kDump (diagnostics, option 99 bit 7): the main pass also stores every raw value
-template <int kKind, bool kEnum, bool kDump = false>
+// kSkip (main pass over rows in BMU order): pass 2 skips the 32-column chunks
+//   no row of the warp needs (see below).
+template <int kKind, bool kEnum, bool kDump = false, bool kSkip = false>
 __global__ void __launch_bounds__(EpiCfg<kKind>::kThreads, 1)
     k1_bmu_tc(const uint8_t* __restrict__ tiles, uint64_t n_host, const uint32_t* __restrict__ dev_n,
               uint32_t groups, uint32_t gn, uint32_t D, uint32_t stages,
@@ -760,25 +762,54 @@ __global__ void __launch_bounds__(EpiCfg<kKind>::kThreads, 1)
 #pragma unroll
                             for (int k = 0; k < 32; ++k) dp[c * 32 + k] = __uint_as_float(r[c][k]);
                 }
-                float mn[4] = {CUDART_INF_F, CUDART_INF_F, CUDART_INF_F, CUDART_INF_F};
-#define TSOM_PASS1(r, cb)                                                                   \
-    _Pragma("unroll") for (int m = 0; m < 16; ++m) mn[m & 3] =                             \
-        fmin3f(mn[m & 3], __uint_as_float(r[2 * m]), __uint_as_float(r[2 * m + 1]))
-#define TSOM_PASS2(r, cb)                                                                   \
+                // pass 1 keeps one minimum per 32-column chunk (two chains
+                // each).  kSkip: pass 2 then skips every chunk whose minimum
+                // lies outside the window for all 32 rows of the warp — such
+                // a chunk adds exactly 0 to a (sat(big (lim - v)) = 0 for v >=
+                // lim), so the skip changes no result.  Rows whose values
+                // cluster (the BMU-ordered resident rows) need
+                // pass 2 on ~40 % of the chunks; on rows in random order the
+                // vote costs more than it saves, hence the template switch.
+                float mc[kCPS][2];
+#pragma unroll
+                for (int c = 0; c < kCPS; ++c) mc[c][0] = mc[c][1] = CUDART_INF_F;
+#define TSOM_PASS1(c)                                                                       \
+    _Pragma("unroll") for (int m = 0; m < 16; ++m) mc[c][m & 1] =                          \
+        fmin3f(mc[c][m & 1], __uint_as_float(r[c][2 * m]), __uint_as_float(r[c][2 * m + 1]))
+#define TSOM_PASS2(c)                                                                       \
+    if (!kSkip || __any_sync(0xffffffffu, cmin[c] < lim))                                  \
     _Pragma("unroll") for (int k = 0; k < 32; ++k) a[k & 7] =                              \
-        fmaf(__saturatef(fmaf(__uint_as_float(r[k]), nb, lb)), (float)((cb) + k + 256), a[k & 7])
+        fmaf(__saturatef(fmaf(__uint_as_float(r[c][k]), nb, lb)), (float)((c) * 32 + k + 256), \
+             a[k & 7])
 #define TSOM_ALL(P)                                                                         \
     do {                                                                                    \
         if (full) {                                                                         \
-            _Pragma("unroll") for (int c = 0; c < kCPS; ++c) P(r[c], c * 32);               \
+            _Pragma("unroll") for (int c = 0; c < kCPS; ++c) P(c);                          \
         } else {                                                                            \
             _Pragma("unroll") for (int c = 0; c < kCPS; ++c) if ((uint32_t)c < c_count)     \
-                P(r[c], c * 32);                                                            \
+                P(c);                                                                       \
         }                                                                                   \
     } while (0)
                 TSOM_ALL(TSOM_PASS1);
                 if (lane == 0 && q == 0) TSOM_TRACE(3 + 3 * (set & 1), it_);
-                const float b = fminf(fminf(mn[0], mn[1]), fminf(mn[2], mn[3]));
+                float cmin[kCPS];
+#pragma unroll
+                for (int c = 0; c < kCPS; ++c) cmin[c] = fminf(mc[c][0], mc[c][1]);
+                float b = cmin[0];
+#pragma unroll
+                for (int c = 1; c < kCPS; ++c) b = fminf(b, cmin[c]);
+                if (dbg & 512u) {  // diagnostics: pass-2 chunks run / chunks, trace slots 4094-4095
+                    const float l0 = b + (x2 + wpart);
+                    const float l1 = l0 + fabsf(l0) * 2.4e-7f;
+                    uint32_t run = 0;
+#pragma unroll
+                    for (int c = 0; c < kCPS; ++c)
+                        run += ((uint32_t)c < c_count) && __any_sync(0xffffffffu, cmin[c] < l1);
+                    if (lane == 0) {
+                        atomicAdd(&g_k1_trace[4094], (unsigned long long)run);
+                        atomicAdd(&g_k1_trace[4095], (unsigned long long)c_count);
+                    }
+                }
                 const float thr = x2 + wpart;
                 // window limit, nudged up so a value exactly at b + thr counts
                 const float lim0 = b + thr;
@@ -964,8 +995,9 @@ cudaError_t launch_bmu_tc(int kind, const void* tiles, uint64_t n, const uint32_
                           bool enumerate, uint32_t P, uint32_t D, const void* wsplit,
                           const float* xn2, const float* w2max, const float* scale, TieWin win,
                           const uint32_t* rmask, float* part, int sm_count, size_t smem_optin,
-                          cudaStream_t st, const uint32_t* tile_mask) {
+                          cudaStream_t st, const uint32_t* tile_mask, bool skip) {
     if (n == 0) return cudaSuccess;
+    skip = skip && !enumerate && !(g_k1_debug & (128u | 256u));  // (bit 8: A/B of the skip)
     const TcGeom geo = tc_geom(kind, D);
     const uint32_t gn = tc_group_width(P);
     const uint32_t groups = (P + gn - 1) / gn;
@@ -988,12 +1020,14 @@ cudaError_t launch_bmu_tc(int kind, const void* tiles, uint64_t n, const uint32_
     if (kind == kTcTf32) {
         kern = enumerate ? k1_bmu_tc<kTcTf32, true>
                          : ((g_k1_debug & 128u) ? k1_bmu_tc<kTcTf32, false, true>
-                                                : k1_bmu_tc<kTcTf32, false>);
+                                                : (skip ? k1_bmu_tc<kTcTf32, false, false, true>
+                                                        : k1_bmu_tc<kTcTf32, false>));
         slot = enumerate ? 1 : 0;
     } else {
         kern = enumerate ? k1_bmu_tc<kTcF16, true>
                          : ((g_k1_debug & 128u) ? k1_bmu_tc<kTcF16, false, true>
-                                                : k1_bmu_tc<kTcF16, false>);
+                                                : (skip ? k1_bmu_tc<kTcF16, false, false, true>
+                                                        : k1_bmu_tc<kTcF16, false>));
         slot = enumerate ? 3 : 2;
     }
     {

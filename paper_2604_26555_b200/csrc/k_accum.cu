@@ -462,20 +462,39 @@ __global__ void __launch_bounds__(kTmaWarps * 32, 2) k_gather_tma(
     double sx = 0.0, sd = 0.0;
     if (kExact) exact_scales(xmax2, w2max, &sx, &sd);
 
-    // copy window of this lane's row; returns the bytes it will deliver
-    auto issue = [&](uint64_t row, uint32_t nrows, int s, uint32_t& offmask) {
+    // copy window of this lane's row into its slot (offmask: rows whose window
+    // starts 8 bytes before them).  A batch of consecutive packed rows (rows
+    // kept in BMU order) is one bulk copy instead: rows at the
+    // row stride from byte `coff` of the buffer (returned; -1 = per-row slots).
+    auto issue = [&](uint64_t row, uint32_t nrows, int s, uint32_t& offmask) -> int {
+        const bool mine = lane < nrows;
+        const uint64_t row0 = __shfl_sync(0xffffffffu, row, 0);
+        const bool cont = strideb == rowb && __all_sync(0xffffffffu, !mine || row == row0 + lane);
+        asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
+        if (cont) {
+            const uint64_t b0 = reinterpret_cast<uint64_t>(x) + row0 * strideb;
+            const uint64_t c0 = b0 & ~15ull;
+            const uint32_t len = (uint32_t)(((b0 + (uint64_t)nrows * rowb + 15) & ~15ull) - c0);
+            offmask = 0;
+            if (lane == 0) {
+                ptx::mbar_expect_tx(&bars[warp][s], len);
+                ptx::bulk_g2s(buf + (size_t)s * 32 * slot, reinterpret_cast<const void*>(c0), len,
+                              &bars[warp][s]);
+            }
+            __syncwarp();
+            return (int)(b0 & 15);
+        }
         const uint64_t a = reinterpret_cast<uint64_t>(x) + row * strideb;
         const uint64_t a0 = a & ~15ull;
         const uint32_t len = (uint32_t)(((a + rowb + 15) & ~15ull) - a0);
-        const bool mine = lane < nrows;
         offmask = __ballot_sync(0xffffffffu, mine && (a & 15));
         const uint32_t total = __reduce_add_sync(0xffffffffu, mine ? len : 0u);
-        asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
         if (lane == 0) ptx::mbar_expect_tx(&bars[warp][s], total);
         __syncwarp();
         if (mine)
             ptx::bulk_g2s(buf + ((size_t)s * 32 + lane) * slot, reinterpret_cast<const void*>(a0),
                           len, &bars[warp][s]);
+        return -1;
     };
 
     for (uint32_t p = blockIdx.x * kTmaWarps + warp; p < npieces; p += gridDim.x * kTmaWarps) {
@@ -501,25 +520,29 @@ __global__ void __launch_bounds__(kTmaWarps * 32, 2) k_gather_tma(
         double a0 = 0.0, a1 = 0.0, c0 = 0.0, c1 = 0.0, ds = 0.0;
         long long qa0 = 0, qa1 = 0, qc0 = 0, qc1 = 0, qds = 0;
         uint32_t offm[2];
-        issue(rowid[0], min(32u, r1 - r0), 0, offm[0]);
+        int coff[2];
+        coff[0] = issue(rowid[0], min(32u, r1 - r0), 0, offm[0]);
 #pragma unroll
         for (int m = 0; m < 8; ++m) {
             if (m < (int)nb) {
                 const uint32_t rows_m = min(32u, r1 - (r0 + 32 * m));
                 const int s = m & 1;
                 if (m + 1 < (int)nb)
-                    issue(rowid[m + 1], min(32u, r1 - (r0 + 32 * (m + 1))), s ^ 1, offm[s ^ 1]);
+                    coff[s ^ 1] =
+                        issue(rowid[m + 1], min(32u, r1 - (r0 + 32 * (m + 1))), s ^ 1, offm[s ^ 1]);
                 ptx::mbar_wait(&bars[warp][s], (phase >> s) & 1u);
                 phase ^= 1u << s;
-                const uint8_t* bs = buf + (size_t)s * 32 * slot;
+                // row j of the batch at bs + j rs (+ 8 when bit j of om is set)
+                const uint8_t* bs = buf + (size_t)s * 32 * slot + (coff[s] < 0 ? 0 : coff[s]);
+                const uint32_t rs = coff[s] < 0 ? slot : rowb;
                 const uint8_t* bm = bs + 8 * lane;
                 const uint32_t om = offm[s];
                 uint32_t j = 0;
                 for (; j + 2 <= rows_m; j += 2) {
                     float2 u = make_float2(0.0f, 0.0f), v = u;
                     if (okb) {
-                        u = *reinterpret_cast<const float2*>(bm + j * slot + ((om >> j) & 1u) * 8);
-                        v = *reinterpret_cast<const float2*>(bm + (j + 1) * slot +
+                        u = *reinterpret_cast<const float2*>(bm + j * rs + ((om >> j) & 1u) * 8);
+                        v = *reinterpret_cast<const float2*>(bm + (j + 1) * rs +
                                                              ((om >> (j + 1)) & 1u) * 8);
                     }
                     if (kExact) {
@@ -536,7 +559,7 @@ __global__ void __launch_bounds__(kTmaWarps * 32, 2) k_gather_tma(
                 }
                 if (j < rows_m && okb) {
                     const float2 u =
-                        *reinterpret_cast<const float2*>(bm + j * slot + ((om >> j) & 1u) * 8);
+                        *reinterpret_cast<const float2*>(bm + j * rs + ((om >> j) & 1u) * 8);
                     if (kExact) {
                         qa0 += __double2ll_rn((double)u.x * sx);
                         qa1 += __double2ll_rn((double)u.y * sx);
@@ -550,7 +573,7 @@ __global__ void __launch_bounds__(kTmaWarps * 32, 2) k_gather_tma(
                     // 8-byte reads (d is even): the 208-B slot stride then costs a
                     // 2-way bank conflict instead of the 4-way of 4-byte reads
                     const float2* xr = reinterpret_cast<const float2*>(
-                        bs + lane * slot + ((om >> lane) & 1u) * 8);
+                        bs + lane * rs + ((om >> lane) & 1u) * 8);
                     double d2 = 0.0;
                     for (uint32_t k2 = 0; k2 < D / 2; ++k2) {
                         const float2 v = xr[k2];

@@ -91,6 +91,7 @@ def main():
     x = _lib.synth_gmm_host(args.rows, D, seed)
     e = tsom.Engine(P, D)
     e.set_option(_lib.TSOM_OPT_BMU_KERNEL, args.kernel)
+    e.set_option(_lib.TSOM_OPT_ROW_ORDER, 0)  # raw dump is in position order
     e.bind(x)
     e.set_codebook(init_sample_draw(x, P, seed))
     e.set_topology_distance(lattice_dist("hex", 32, 32))

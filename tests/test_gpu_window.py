@@ -59,6 +59,7 @@ def test_k1_error_is_far_inside_the_window(pkg, oracle_port, kernel):
     x = oracle_port.synth_gmm(n, D, 2606)
     e = pkg.Engine(P, D)
     e.set_option(_lib.TSOM_OPT_BMU_KERNEL, kernel)
+    e.set_option(_lib.TSOM_OPT_ROW_ORDER, 0)  # raw dump is in position order
     e.bind(x)
     e.set_codebook(init_sample_draw(x, P, 2606))
     e.set_topology_distance(lattice_dist("hex", 32, 32))
