@@ -627,6 +627,8 @@ def leg_c4(args, ctx):
     n = n_total // world + (1 if rank < n_total % world else 0)
     off = sum(n_total // world + (1 if r < n_total % world else 0) for r in range(rank))
     e = tsom.Engine(P, D, device=local)
+    if args.image is not None:
+        e.set_option(95, args.image)  # diagnostics: split image on / off
     # N >= 1e8: device-generated rows (SURVEY §8(d) allows it for throughput)
     e.bind_synthetic_gmm(n, seed, 16, off)
     ctx["attach"](e)
@@ -907,6 +909,7 @@ def main():
     ap.add_argument("--kernel", type=int, default=0, help="0 auto, 1 SIMT, 2 tcgen05 3xTF32, 3 tcgen05 3xFP16")
     ap.add_argument("--row-order", type=int, default=None,
                     help="TSOM_OPT_ROW_ORDER for the c2 engines (default: the engine's, 1)")
+    ap.add_argument("--image", type=int, default=None, help=argparse.SUPPRESS)  # c4: split image A/B
     ap.add_argument("--no-e2e", action="store_true")
     ap.add_argument("--no-cpu", action="store_true")
     ap.add_argument("--no-c4", action="store_true", help="skip the c4 (1e8 rows, adaptive) leg")

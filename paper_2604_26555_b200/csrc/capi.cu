@@ -193,6 +193,78 @@ __global__ void k_tie_pass_counts(const uint32_t* __restrict__ count, uint64_t c
     pcount[p] = (uint32_t)(p + 1 == passes ? rest : (rest < cap ? rest : cap));
 }
 
+// ids[i] = sel[pos[i]] (pos null: i) for i < count (count = *dev_n when given),
+// and their window terms from the split image
+__global__ void k_gather_ids(const uint32_t* __restrict__ sel, const uint32_t* __restrict__ pos,
+                             const uint32_t* __restrict__ dev_n, uint64_t n_host,
+                             const float* __restrict__ img_xn2, uint32_t* __restrict__ ids,
+                             float* __restrict__ xn2) {
+    const uint64_t n = dev_n ? min((uint64_t)*dev_n, n_host) : n_host;
+    for (uint64_t i = blockIdx.x * (uint64_t)blockDim.x + threadIdx.x; i < n;
+         i += (uint64_t)gridDim.x * blockDim.x) {
+        const uint32_t r = sel[pos ? pos[i] : i];
+        ids[i] = r;
+        xn2[i] = img_xn2[r];
+    }
+}
+
+using EncodeTiledFn = CUresult (*)(CUtensorMap*, CUtensorMapDataType, cuuint32_t, void*,
+                                   const cuuint64_t*, const cuuint64_t*, const cuuint32_t*,
+                                   const cuuint32_t*, CUtensorMapInterleave, CUtensorMapSwizzle,
+                                   CUtensorMapL2promotion, CUtensorMapFloatOOBfill);
+
+EncodeTiledFn encode_tiled() {
+    static EncodeTiledFn fn = [] {
+        void* f = nullptr;
+        cudaDriverEntryPointQueryResult q{};
+        if (cudaGetDriverEntryPoint("cuTensorMapEncodeTiled", &f, cudaEnableDefault, &q) !=
+                cudaSuccess ||
+            q != cudaDriverEntryPointSuccess) {
+            cudaGetLastError();
+            return (EncodeTiledFn) nullptr;
+        }
+        return reinterpret_cast<EncodeTiledFn>(f);
+    }();
+    return fn;
+}
+
+// Use (and if needed build) the split image for a 3xFP16 pass over the
+// selection `sel` (n rows) of the resident rows: false = pre-split tiles as
+// before (streamed or caller rows, small selections, image off or no room).
+bool use_image(Engine* eng, const float* x, const uint32_t* sel, uint64_t n, int kind) {
+    if (!sel || kind != tsom::kTcF16 || !eng->img_mode || eng->streamed || !eng->x.p ||
+        x != eng->x.as<float>() || n * 64 < eng->n_rows || !encode_tiled())
+        return false;
+    if (eng->img_valid) return true;
+    const tsom::TcGeom geo = tsom::tc_geom(kind, eng->D);
+    const uint32_t w = (geo.kpad + 63u) / 64u * 64u;
+    if (eng->ximg.ensure(eng->n_rows * w * 2) != cudaSuccess ||
+        eng->ximg_xn2.ensure(eng->n_rows * sizeof(float)) != cudaSuccess) {
+        cudaGetLastError();
+        eng->ximg.release();
+        eng->ximg_xn2.release();
+        eng->img_mode = 0;  // no room next to the rows: the per-pass split stays
+        return false;
+    }
+    tsom::launch_split_image(eng->x.as<float>(), eng->ldx, eng->n_rows, eng->D,
+                             eng->scale.as<float>(), tie_window(eng, kind), eng->ximg.p, w,
+                             eng->ximg_xn2.as<float>(), eng->stream);
+    CU(cudaGetLastError());
+    cuuint64_t gdim[2] = {(cuuint64_t)w, (cuuint64_t)eng->n_rows};
+    cuuint64_t gstr[1] = {(cuuint64_t)w * 2};
+    cuuint32_t box[2] = {64, 1};  // tile::gather4: one row per coordinate, a 128-B atom wide
+    cuuint32_t es[2] = {1, 1};
+    const CUresult cr = encode_tiled()(&eng->img_map, CU_TENSOR_MAP_DATA_TYPE_UINT16, 2,
+                                       eng->ximg.p, gdim, gstr, box, es,
+                                       CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_128B,
+                                       CU_TENSOR_MAP_L2_PROMOTION_L2_128B,
+                                       CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
+    REQUIRE(cr == CUDA_SUCCESS, TSOM_ERR_CUDA, "cuTensorMapEncodeTiled failed for the split image");
+    eng->img_w = w;
+    eng->img_valid = true;
+    return true;
+}
+
 // K1 + exact re-check over rows `x` (selection `sel` of length n, or first n rows).
 // x2max: max ||x||^2 over these rows (device; picks the FP16 operand scale).
 // `tiles` = pre-split tcgen05 A tiles for exactly these n rows, built with the
@@ -223,7 +295,19 @@ void run_bmu(Engine* eng, const float* x, uint32_t ldx, const uint32_t* sel, uin
         CU(eng->wsplit.ensure(tsom::tc_wsplit_bytes(kind, eng->P, eng->D)));
         tsom::launch_prep_wsplit(kind, eng->w.as<float>(), eng->P, eng->D, scale, eng->wsplit.p,
                                  eng->stream);
-        if (!tiles) {
+        // selections of the resident rows: K1 gathers them from the split image
+        const bool img = !tiles && use_image(eng, x, sel, n, kind);
+        const CUtensorMap* tmap = img ? &eng->img_map : nullptr;
+        if (img) {
+            CU(eng->gxn2.ensure(n * sizeof(float)));
+            CU(eng->gid.ensure(2 * n * sizeof(uint32_t)));  // [selection ids | near-tie ids]
+            TSOM_LAUNCH(k_gather_ids<<<(unsigned)std::min<uint64_t>((n + 255) / 256, 148 * 16), 256,
+                                       0, eng->stream>>>(sel, nullptr, nullptr, n,
+                                                         eng->ximg_xn2.as<float>(),
+                                                         eng->gid.as<uint32_t>(),
+                                                         eng->gxn2.as<float>()));
+            tiles_xn2 = eng->gxn2.as<float>();
+        } else if (!tiles) {
             const uint64_t ntiles = (n + tsom::kTcTileM - 1) / tsom::kTcTileM;
             CU(eng->gsplit.ensure(ntiles * geo.tile_bytes));
             CU(eng->gxn2.ensure(n * sizeof(float)));
@@ -239,7 +323,8 @@ void run_bmu(Engine* eng, const float* x, uint32_t ldx, const uint32_t* sel, uin
         CU(cudaEventRecord(k1_event(eng, 0), eng->stream));
         CU(tsom::launch_bmu_tc(kind, tiles, n, nullptr, false, eng->P, eng->D, eng->wsplit.p,
                                tiles_xn2, w2, scale, win, nullptr, eng->part.as<float>(),
-                               eng->sm_count, eng->smem_optin, eng->stream, nullptr, skip));
+                               eng->sm_count, eng->smem_optin, eng->stream, nullptr, skip, tmap,
+                               img ? eng->gid.as<uint32_t>() : nullptr));
         CU(cudaEventRecord(k1_event(eng, 1), eng->stream));
         eng->k1_timed = true;
         tsom::sampler_pregenerate(eng->sampler, k1_event(eng, 1));
@@ -286,7 +371,7 @@ void run_bmu(Engine* eng, const float* x, uint32_t ldx, const uint32_t* sel, uin
             passes = std::min<uint32_t>(kTiePasses, std::max<uint32_t>(1u, (uint32_t)std::ceil(need)));
         }
         const uint64_t mt = (cap + tsom::kTcTileM - 1) / tsom::kTcTileM;
-        CU(eng->tsplit.ensure(mt * geo.tile_bytes));
+        if (!img) CU(eng->tsplit.ensure(mt * geo.tile_bytes));
         CU(eng->part2.ensure((size_t)groups * 4 * cap * sizeof(float)));
         CU(eng->txn2.ensure(cap * sizeof(float)));
         CU(eng->tcnt.ensure(kTiePasses * sizeof(uint32_t)));
@@ -309,14 +394,23 @@ void run_bmu(Engine* eng, const float* x, uint32_t ldx, const uint32_t* sel, uin
                                                                   log_slot));
         for (uint32_t pz = 0; pz < passes; ++pz) {
             const uint64_t o = (uint64_t)pz * cap;
-            tsom::launch_split_rows(kind, xsrc, sel, tpos + o, cap, eng->D, scale, win,
-                                    eng->tsplit.p, eng->txn2.as<float>(), eng->stream, pcount + pz,
-                                    ldx);
-            CU(tsom::launch_bmu_tc(kind, eng->tsplit.p, cap, pcount + pz, true, eng->P, eng->D,
-                                   eng->wsplit.p, eng->txn2.as<float>(), w2, scale, win,
-                                   tmask_s + o, eng->part2.as<float>(), eng->sm_count,
+            // the pass's rows: split into tiles, or (image) their ids
+            uint32_t* tid = img ? eng->gid.as<uint32_t>() + n : nullptr;
+            if (img)
+                TSOM_LAUNCH(k_gather_ids<<<(unsigned)std::min<uint64_t>((cap + 255) / 256, 148 * 8),
+                                           256, 0, eng->stream>>>(
+                    sel, tpos + o, pcount + pz, cap, eng->ximg_xn2.as<float>(), tid,
+                    eng->txn2.as<float>()));
+            else
+                tsom::launch_split_rows(kind, xsrc, sel, tpos + o, cap, eng->D, scale, win,
+                                        eng->tsplit.p, eng->txn2.as<float>(), eng->stream,
+                                        pcount + pz, ldx);
+            CU(tsom::launch_bmu_tc(kind, img ? nullptr : eng->tsplit.p, cap, pcount + pz, true,
+                                   eng->P, eng->D, eng->wsplit.p, eng->txn2.as<float>(), w2, scale,
+                                   win, tmask_s + o, eng->part2.as<float>(), eng->sm_count,
                                    eng->smem_optin, eng->stream,
-                                   tile_mask ? tile_mask + o / tsom::kTcTileM : nullptr));
+                                   tile_mask ? tile_mask + o / tsom::kTcTileM : nullptr, false,
+                                   tmap, tid));
             tsom::launch_merge_partials(eng->part2.as<float>(), tpos + o, pcount + pz, cap, cap,
                                         groups, gn, eng->txn2.as<float>(), w2, scale, win, x, ldx,
                                         sel, eng->w.as<float>(), eng->D, eng->bmu.as<uint32_t>(),
@@ -463,6 +557,9 @@ void reset_order(Engine* eng) {
     eng->pinv.release();
     eng->idmap.release();
     eng->unperm.release();
+    eng->img_valid = false;  // (the split image follows the rows)
+    eng->ximg.release();
+    eng->ximg_xn2.release();
 }
 
 // Re-lay the rows out now?  Needs the engine's own resident copy and the
@@ -500,6 +597,7 @@ void order_rows(Engine* eng) {
     eng->ldx = eng->D;
     eng->x_slack = true;
     eng->xsplit_valid = false;
+    eng->img_valid = false;
     eng->ordered = true;
     eng->sorted_full = false;
     eng->passes_since_order = 0;
@@ -893,7 +991,7 @@ std::vector<DevBuf*> all_buffers(Engine* eng) {
                       &eng->topo_buf[12], &eng->topo_buf[13], &eng->topo_buf[14], &eng->U, &eng->H, &eng->status, &eng->smooth_scratch,
                       &eng->stage[0], &eng->stage[1], &eng->dead, &eng->hmax, &eng->guard_buf,
                       &eng->tie_dev, &eng->xsums, &eng->xmax_g, &eng->perm, &eng->pinv,
-                      &eng->idmap, &eng->unperm});
+                      &eng->idmap, &eng->unperm, &eng->ximg, &eng->ximg_xn2, &eng->gid});
 }
 
 }  // namespace
@@ -1011,6 +1109,7 @@ int tsom_set_option(tsom_engine* eng, int key, int64_t value) {
             case TSOM_OPT_TIE_TAU:
                 REQUIRE(value >= 0, TSOM_ERR_INVALID, "option: tau must be >= 0");
                 eng->tau_simt = eng->tau_tc = (double)value * std::ldexp(1.0, -30);
+                eng->xsplit_valid = eng->img_valid = false;  // their window terms change
                 break;
             case TSOM_OPT_STREAM_CHUNK:
                 REQUIRE(value >= 128, TSOM_ERR_INVALID, "option: stream chunk >= 128 rows");
@@ -1024,6 +1123,10 @@ int tsom_set_option(tsom_engine* eng, int key, int64_t value) {
                 break;
             case 96:  // diagnostics: 1 = the per-row main-pass merge (k_merge_fast)
                 tsom::g_merge_v1 = (int)value;
+                break;
+            case 95:  // diagnostics: 0 = no split image (selections split per pass)
+                eng->img_mode = (int)value;
+                eng->img_valid = false;
                 break;
             case 97:  // diagnostics: 1 = cp.async K2 gather instead of the TMA gather
                 tsom::g_gather_kind = (int)value;

@@ -16,6 +16,7 @@
 //   U, H     P*d, P       f64             smoothed accumulators (K3 output)
 #pragma once
 
+#include <cuda.h>
 #include <cuda_runtime.h>
 
 #include <atomic>
@@ -250,6 +251,17 @@ struct Engine {
     DevBuf unperm;              // per-row outputs scattered back to caller order
     bool sorted_full = false;   // acc.sorted = the last full pass's BMU-ordered positions
     uint32_t passes_since_order = 0;
+    // 3xFP16 split image of the resident rows (row-major, img_w halves per
+    // row) + per-row window terms: the gather source of K1 for selections
+    // (kGather), built on the first selection pass that covers >= 1/64 of
+    // the rows (launch_split_image).  Diagnostics option 95 = 1 turns it on;
+    // off by default: measured slower than splitting the selection per pass
+    // (TMA gather4 of 128-B row segments is op-rate bound)
+    DevBuf ximg, ximg_xn2, gid;
+    bool img_valid = false;
+    int img_mode = 0;
+    uint32_t img_w = 0;
+    alignas(64) CUtensorMap img_map{};
 
     // codebook
     DevBuf w, wt, wsplit, w2, w2max, prev;
@@ -379,7 +391,12 @@ void launch_fold_max(float* a, cudaStream_t st);
 void launch_split_rows(int kind, const float* x, const uint32_t* sel, const uint32_t* idx,
                        uint64_t n, uint32_t D, const float* scale, TieWin win, void* tiles,
                        float* tx, cudaStream_t st, const uint32_t* dev_n = nullptr,
-                       uint32_t ldx = 0);  // row stride in floats (0: D)
+                       uint32_t ldx = 0);
+// The 3xFP16 split of rows [0, n) as a row-major image: row r at img + r * img_w
+// halves (img_w = 64 * atoms >= kpad; columns past kpad are not written), the
+// gather source of K1's kGather mode; xn2[r] = the row's window term.
+void launch_split_image(const float* x, uint32_t ldx, uint64_t n, uint32_t D, const float* scale,
+                        TieWin win, void* img, uint32_t img_w, float* xn2, cudaStream_t st);  // row stride in floats (0: D)
 bool tc_supported(int kind, uint32_t P, uint32_t D);
 size_t tc_wsplit_bytes(int kind, uint32_t P, uint32_t D);
 // scale = {s, s^2, overflow flag}: kTcF16 picks s = 2^e from max ||x||^2 (x2max[0])
@@ -402,12 +419,14 @@ void launch_bmu_simt(const float* x, uint32_t ldx, const uint32_t* sel, uint64_t
                      cudaStream_t st);
 // tcgen05 variant: per-group partials (enumerate = candidate lists; dev_n =
 // optional device row count; skip: the main pass over BMU-ordered rows, whose
-// epilogue skips the column chunks no row of a warp needs).
+// epilogue skips the column chunks no row of a warp needs; tmap: 3xFP16 rows
+// gathered by id (grow[pos]) from the split image instead of tiles).
 cudaError_t launch_bmu_tc(int kind, const void* tiles, uint64_t n, const uint32_t* dev_n,
                           bool enumerate, uint32_t P, uint32_t D, const void* wsplit,
                           const float* xn2, const float* w2max, const float* scale, TieWin win,
                           const uint32_t* rmask, float* part, int sm_count, size_t smem_optin,
-                          cudaStream_t st, const uint32_t* tile_mask = nullptr, bool skip = false);
+                          cudaStream_t st, const uint32_t* tile_mask = nullptr, bool skip = false,
+                          const CUtensorMap* tmap = nullptr, const uint32_t* grow = nullptr);
 extern uint32_t g_k1_debug;
 extern int g_split_v1;
 extern int g_gather_kind;

@@ -35,11 +35,15 @@
 //   warps 4..11 : two sets of 4 epilogue warps; both drain every tile, set h
 //                 taking node columns [128h, 128h + 128) (warp q of a set owns
 //                 TMEM lanes 32q.., i.e. tile rows 32q..32q+31)
+#include <cuda.h>
 #include <cuda_fp16.h>
 #include <cuda_runtime.h>
 #include <math_constants.h>
 
 #include <cstdint>
+#include <map>
+#include <mutex>
+#include <tuple>
 
 #include "engine.h"
 #include "tc_ptx.cuh"
@@ -409,11 +413,13 @@ __global__ void __launch_bounds__(kSplitThreads) k_split_rows(
 // factor covers it; decisions inside the window are re-checked in FP64).
 constexpr int kSplitWarpRows = 16;
 
+// img_w > 0: the rows go to a row-major image instead (row r at tiles + r *
+// img_w halves, cores [0, kpad / 8) of it; launch_split_image).
 __global__ void __launch_bounds__(kSplitThreads, 4) k_split_rows_f16(
     const float* __restrict__ x, uint32_t ldx, const uint32_t* __restrict__ sel,
     const uint32_t* __restrict__ idx, const uint32_t* __restrict__ dev_n, uint64_t n_host,
     uint32_t D, const float* __restrict__ scale, TieWin win, uint8_t* __restrict__ tiles,
-    float* __restrict__ xn2) {
+    float* __restrict__ xn2, uint32_t img_w = 0) {
     extern __shared__ __align__(16) uint8_t split_wsm[];
     const uint64_t n = dev_n ? min((uint64_t)*dev_n, n_host) : n_host;
     constexpr uint32_t kChunksPerTile = kTcTileM / kSplitWarpRows;
@@ -492,6 +498,17 @@ __global__ void __launch_bounds__(kSplitThreads, 4) k_split_rows_f16(
             if (!(lane & 1u) && valid && xn2) xn2[r0 + rr] = tie_xpart(nf * 1.0000003f, S, win);
         }
         __syncwarp();
+        if (img_w) {
+            // row-major image: consecutive lanes store consecutive 16-B cores
+            // of a row (the warp's 16 rows x ncores cores in order)
+            for (uint32_t e = lane; e < rows * ncores; e += 32) {
+                const uint32_t r = e / ncores, kc = e - r * ncores;
+                *reinterpret_cast<uint4*>(tiles + ((r0 + r) * img_w + kc * 8) * sizeof(__half)) =
+                    *reinterpret_cast<const uint4*>(img + r * hs + kc * 8);
+            }
+            __syncwarp();  // image reused by the next chunk
+            continue;
+        }
         const uint32_t lr = lane & 15u, kc0 = (lane >> 4) * (ncores / 2);
         uint8_t* out = tiles + (c / kChunksPerTile) * (uint64_t)geo.tile_bytes +
                        (size_t)((c % kChunksPerTile) * kSplitWarpRows + lr) * 16;
@@ -540,6 +557,25 @@ void launch_split_rows(int kind, const float* x, const uint32_t* sel, const uint
     }
 }
 
+void launch_split_image(const float* x, uint32_t ldx, uint64_t n, uint32_t D, const float* scale,
+                        TieWin win, void* img, uint32_t img_w, float* xn2, cudaStream_t st) {
+    if (n == 0) return;
+    if (ldx == 0) ldx = D;
+    const size_t wsmem = (size_t)(kSplitThreads / 32) * kSplitWarpRows *
+                         (tc_geom(kTcF16, D).kpad + 8) * sizeof(__half);
+    bool first = false;
+    ensure_smem_attr((const void*)k_split_rows_f16,
+                     (kSplitThreads / 32) * kSplitWarpRows * (kTcF16MaxK + 8) * sizeof(__half),
+                     &first);
+    if (first)
+        cudaFuncSetAttribute(k_split_rows_f16, cudaFuncAttributePreferredSharedMemoryCarveout, 100);
+    uint64_t blocks = (n + kTcTileM - 1) / kTcTileM;
+    if (blocks > 148ull * 8) blocks = 148ull * 8;
+    TSOM_LAUNCH(k_split_rows_f16<<<(unsigned)blocks, kSplitThreads, wsmem, st>>>(
+        x, ldx, nullptr, nullptr, nullptr, n, D, scale, win, static_cast<uint8_t*>(img), xn2,
+        img_w));
+}
+
 // ---------------------------------------------------------------------------
 // K1
 // ---------------------------------------------------------------------------
@@ -553,14 +589,21 @@ void launch_split_rows(int kind, const float* x, const uint32_t* sel, const uint
 // kDump (diagnostics, option 99 bit 7): the main pass also stores every raw value
 // kSkip (main pass over rows in BMU order): pass 2 skips the 32-column chunks
 //   no row of the warp needs (see below).
-template <int kKind, bool kEnum, bool kDump = false, bool kSkip = false>
+// kGather (3xFP16, rows picked by id: selections, near-tie rows): instead of
+//   pre-split tiles, the producer warp gathers each tile's 128 rows straight
+//   from the row-major split image (one TMA tile::gather4 per 4 rows and
+//   64-column atom, 128-B swizzled; tensor map tmap, row ids grow[pos]), and
+//   the MMAs read the A operand through SWIZZLE_128B descriptors.
+template <int kKind, bool kEnum, bool kDump = false, bool kSkip = false, bool kGather = false>
 __global__ void __launch_bounds__(EpiCfg<kKind>::kThreads, 1)
     k1_bmu_tc(const uint8_t* __restrict__ tiles, uint64_t n_host, const uint32_t* __restrict__ dev_n,
               uint32_t groups, uint32_t gn, uint32_t D, uint32_t stages,
               const uint8_t* __restrict__ wsplit, const float* __restrict__ xn2,
               const float* __restrict__ w2max, const float* __restrict__ scale, TieWin win,
               const uint32_t* __restrict__ rmask, float* __restrict__ part, uint32_t dbg,
-              uint32_t mc, const uint32_t* __restrict__ tile_mask) {
+              uint32_t mc, const uint32_t* __restrict__ tile_mask,
+              const __grid_constant__ CUtensorMap tmap, const uint32_t* __restrict__ grow,
+              uint32_t natoms) {
     // mc > 1: the CTAs of a cluster are the mc codebook groups of the same tile
     // sequence; each loads 1/mc of every A tile and multicasts it to all, so the
     // tile crosses L2 -> SM once per cluster instead of once per group.
@@ -571,9 +614,12 @@ __global__ void __launch_bounds__(EpiCfg<kKind>::kThreads, 1)
     if (n == 0) return;  // an empty near-tie pass (uniform over the grid and its clusters)
     const uint32_t ntiles = (uint32_t)((n + kTcTileM - 1) / kTcTileM);
     const uint32_t w_bytes = gn * geo.row_bytes;  // this CTA's group (both halves for tf32)
+    // one A stage: a pre-split tile, or natoms 128-row x 128-B swizzle atoms
+    const uint32_t tbytes = kGather ? natoms * (kTcTileM * 128u) : geo.tile_bytes;
     uint8_t* sW = smem;
     uint8_t* sX = smem + ((w_bytes + 1023u) & ~1023u);
-    uint64_t* bars = reinterpret_cast<uint64_t*>(sX + stages * geo.tile_bytes);
+    if (kGather && (smem_u32(sX) & 1023u)) __trap();  // swizzle atoms need 1024-B alignment
+    uint64_t* bars = reinterpret_cast<uint64_t*>(sX + stages * tbytes);
     uint64_t* full_bar = bars;                    // [stages] X tile landed
     uint64_t* empty_bar = bars + kMaxStages;      // [stages] MMAs done with X tile
     uint64_t* tfull_bar = bars + 2 * kMaxStages;  // [2] accumulator ready
@@ -615,7 +661,50 @@ __global__ void __launch_bounds__(EpiCfg<kKind>::kThreads, 1)
     const uint32_t tmem_base = *tmem_slot;
     const uint16_t mc_mask = (uint16_t)((1u << mc) - 1u);
 
-    if (warp == 0) {
+    if (kGather && warp == 0) {
+        if (ntiles > cta_in_group) {
+            if (lane == 0) {  // resident codebook group, in <= 64 KB bulk copies
+                mbar_expect_tx(w_bar, w_bytes);
+                const uint8_t* wg = wsplit + (size_t)g * w_bytes;
+                for (uint32_t off = 0; off < w_bytes; off += 65536u)
+                    bulk_g2s(sW + off, wg + off, min(65536u, w_bytes - off), w_bar);
+            }
+            uint32_t stage = 0, phase = 0;
+            // mc > 1: the cluster's CTAs (the codebook groups, same tile
+            // sequence) each gather 128 / mc rows of the tile and multicast
+            // them to all, so every row is fetched once per cluster
+            const uint32_t rpc = kTcTileM / mc;
+            const uint32_t row = (mc > 1 ? g * rpc : 0u) + 4u * lane;
+            for (uint32_t t = cta_in_group; t < ntiles; t += ctas_per_group) {
+                if (kEnum && tile_mask && !((tile_mask[t] >> (g & 31)) & 1u)) continue;
+                mbar_wait(&empty_bar[stage], phase ^ 1);
+                if (lane == 0) mbar_expect_tx(&full_bar[stage], tbytes);
+                __syncwarp();
+                // lane l gathers rows row..row+3 of the tile (rows past n repeat a
+                // valid id; their results are never read) into every atom
+                if (4u * lane < rpc) {
+                    const uint64_t p0 = (uint64_t)t * kTcTileM + row;
+                    int id[4];
+#pragma unroll
+                    for (int j = 0; j < 4; ++j)
+                        id[j] = (int)__ldg(grow + (p0 + j < n ? p0 + j : n - 1));
+                    uint8_t* dst = sX + stage * tbytes + row * 128u;
+                    for (uint32_t a = 0; a < natoms; ++a) {
+                        if (mc > 1)
+                            tma_gather4_mc(dst + a * (kTcTileM * 128u), &tmap, (int)(a * 64u), id[0],
+                                           id[1], id[2], id[3], &full_bar[stage], mc_mask);
+                        else
+                            tma_gather4(dst + a * (kTcTileM * 128u), &tmap, (int)(a * 64u), id[0],
+                                        id[1], id[2], id[3], &full_bar[stage]);
+                    }
+                }
+                if (++stage == stages) {
+                    stage = 0;
+                    phase ^= 1;
+                }
+            }
+        }
+    } else if (warp == 0) {
         if (lane == 0 && ntiles > cta_in_group) {
             // resident codebook group, in <= 64 KB bulk copies
             mbar_expect_tx(w_bar, w_bytes);
@@ -662,8 +751,14 @@ __global__ void __launch_bounds__(EpiCfg<kKind>::kThreads, 1)
                 TSOM_TRACE(0, it_);
                 tc_fence_after();
                 const uint32_t d = tmem_base + acc * acc_cols;
-                const uint32_t sx = smem_u32(sX + stage * geo.tile_bytes);
+                const uint32_t sx = smem_u32(sX + stage * tbytes);
                 if (dbg & 2u) {
+                } else if (kGather) {
+                    // k-step k: atom k / 4, 32 B into its (swizzled) rows
+                    for (uint32_t k = 0; k < geo.ksteps; ++k)
+                        mma_f16(d, umma_desc_sw128(sx + (k >> 2) * (kTcTileM * 128u) + (k & 3u) * 32u),
+                                umma_desc(sw + k * 2u * w_lbo, w_lbo, 128u), idesc,
+                                k > 0 ? 1u : 0u);
                 } else if (kKind == kTcTf32) {
                     const uint32_t sx_lo = sx + geo.tile_bytes / 2;
                     const uint32_t sw_lo = sw + w_bytes / 2;
@@ -995,10 +1090,15 @@ cudaError_t launch_bmu_tc(int kind, const void* tiles, uint64_t n, const uint32_
                           bool enumerate, uint32_t P, uint32_t D, const void* wsplit,
                           const float* xn2, const float* w2max, const float* scale, TieWin win,
                           const uint32_t* rmask, float* part, int sm_count, size_t smem_optin,
-                          cudaStream_t st, const uint32_t* tile_mask, bool skip) {
+                          cudaStream_t st, const uint32_t* tile_mask, bool skip,
+                          const CUtensorMap* tmap, const uint32_t* grow) {
     if (n == 0) return cudaSuccess;
     skip = skip && !enumerate && !(g_k1_debug & (128u | 256u));  // (bit 8: A/B of the skip)
+    const bool gather = tmap != nullptr;
+    if (gather && kind != kTcF16) return cudaErrorInvalidValue;
     const TcGeom geo = tc_geom(kind, D);
+    const uint32_t natoms = (geo.kpad + 63u) / 64u;
+    const uint32_t tbytes = gather ? natoms * (kTcTileM * 128u) : geo.tile_bytes;
     const uint32_t gn = tc_group_width(P);
     const uint32_t groups = (P + gn - 1) / gn;
     const uint32_t ntiles = (uint32_t)((n + kTcTileM - 1) / kTcTileM);  // upper bound
@@ -1009,26 +1109,28 @@ cudaError_t launch_bmu_tc(int kind, const void* tiles, uint64_t n, const uint32_
     const uint32_t w_bytes = gn * geo.row_bytes;
     const size_t fixed = ((w_bytes + 1023u) & ~1023u) + 128 + 2 * kTcTileM * 10;  // + set exchange
     uint32_t stages = 2;
-    while (stages < 3 && fixed + (size_t)(stages + 1) * geo.tile_bytes <= smem_optin) ++stages;
-    const size_t smem = fixed + (size_t)stages * geo.tile_bytes;
+    while (stages < 3 && fixed + (size_t)(stages + 1) * tbytes <= smem_optin) ++stages;
+    const size_t smem = fixed + (size_t)stages * tbytes;
     if (smem > smem_optin) return cudaErrorInvalidConfiguration;
     using KernT = void (*)(const uint8_t*, uint64_t, const uint32_t*, uint32_t, uint32_t, uint32_t,
                            uint32_t, const uint8_t*, const float*, const float*, const float*,
-                           TieWin, const uint32_t*, float*, uint32_t, uint32_t, const uint32_t*);
+                           TieWin, const uint32_t*, float*, uint32_t, uint32_t, const uint32_t*,
+                           const CUtensorMap, const uint32_t*, uint32_t);
     KernT kern;
-    int slot;
-    if (kind == kTcTf32) {
+    if (gather) {
+        kern = enumerate ? k1_bmu_tc<kTcF16, true, false, false, true>
+                         : (skip ? k1_bmu_tc<kTcF16, false, false, true, true>
+                                 : k1_bmu_tc<kTcF16, false, false, false, true>);
+    } else if (kind == kTcTf32) {
         kern = enumerate ? k1_bmu_tc<kTcTf32, true>
                          : ((g_k1_debug & 128u) ? k1_bmu_tc<kTcTf32, false, true>
                                                 : (skip ? k1_bmu_tc<kTcTf32, false, false, true>
                                                         : k1_bmu_tc<kTcTf32, false>));
-        slot = enumerate ? 1 : 0;
     } else {
         kern = enumerate ? k1_bmu_tc<kTcF16, true>
                          : ((g_k1_debug & 128u) ? k1_bmu_tc<kTcF16, false, true>
                                                 : (skip ? k1_bmu_tc<kTcF16, false, false, true>
                                                         : k1_bmu_tc<kTcF16, false>));
-        slot = enumerate ? 3 : 2;
     }
     {
         const cudaError_t e = ensure_smem_attr((const void*)kern, smem);
@@ -1039,13 +1141,24 @@ cudaError_t launch_bmu_tc(int kind, const void* tiles, uint64_t n, const uint32_
     // as many clusters as can be co-resident (one CTA per SM)
     uint32_t mc = 1;
     // (measured neutral at K = 1024 on B200, so off unless option 99 bit 6 asks)
-    if ((g_k1_debug & 64u) && groups >= 2 && groups <= 8 && geo.tile_bytes % (16u * groups) == 0)
+    if (!gather && (g_k1_debug & 64u) && groups >= 2 && groups <= 8 &&
+        geo.tile_bytes % (16u * groups) == 0)
+        mc = groups;
+    // gathered rows: each row fetched once per cluster of the group CTAs
+    // (the per-CTA gather4 rate bounds the kernel otherwise; option 99 bit 10 off)
+    if (gather && groups >= 2 && groups <= 8 && kTcTileM % (4u * groups) == 0 &&
+        !(g_k1_debug & 1024u))
         mc = groups;
     uint32_t clusters = per_group;
     if (mc > 1) {
-        static int max_clusters[4] = {-1, -1, -1, -1};
-        static uint32_t mc_for[4] = {0, 0, 0, 0};
-        if (max_clusters[slot] < 0 || mc_for[slot] != mc) {
+        // max co-resident clusters, per (kernel, device, cluster size)
+        static std::mutex mu;
+        static std::map<std::tuple<const void*, int, uint32_t>, int> max_clusters;
+        int dev = 0;
+        cudaGetDevice(&dev);
+        std::lock_guard<std::mutex> lk(mu);
+        auto it = max_clusters.find({(const void*)kern, dev, mc});
+        if (it == max_clusters.end()) {
             cudaLaunchConfig_t qc = {};
             qc.gridDim = dim3(mc * per_group);
             qc.blockDim = dim3(threads);
@@ -1062,11 +1175,10 @@ cudaError_t launch_bmu_tc(int kind, const void* tiles, uint64_t n, const uint32_
                 cudaGetLastError();
                 nc = 0;
             }
-            max_clusters[slot] = nc;
-            mc_for[slot] = mc;
+            it = max_clusters.emplace(std::make_tuple((const void*)kern, dev, mc), nc).first;
         }
-        if (max_clusters[slot] < 1) mc = 1;
-        else clusters = std::min<uint32_t>(per_group, (uint32_t)max_clusters[slot]);
+        if (it->second < 1) mc = 1;
+        else clusters = std::min<uint32_t>(per_group, (uint32_t)it->second);
     }
     const uint32_t grid_x = clusters * groups;
     cudaLaunchConfig_t cfg = {};
@@ -1085,7 +1197,8 @@ cudaError_t launch_bmu_tc(int kind, const void* tiles, uint64_t n, const uint32_
     const cudaError_t e = cudaLaunchKernelEx(
         &cfg, kern, static_cast<const uint8_t*>(tiles), n, dev_n, groups, gn, D, stages,
         static_cast<const uint8_t*>(wsplit), xn2, w2max, scale, win, rmask, part, g_k1_debug, mc,
-        (enumerate && mc == 1) ? tile_mask : nullptr);  // (multicast loads need every tile)
+        (enumerate && mc == 1) ? tile_mask : nullptr,  // (multicast loads need every tile)
+        gather ? *tmap : CUtensorMap{}, grow, natoms);
     if (e != cudaSuccess) return e;
     return cudaGetLastError();
 }

@@ -74,6 +74,43 @@ __device__ __forceinline__ uint64_t umma_desc(uint32_t saddr, uint32_t lbo, uint
     return d;
 }
 
+// K-major, 128-B swizzled operand (the TMA SWIZZLE_128B layout: 8-row atoms of
+// 128 B per row, atoms 1024-B aligned): SBO = 1024 B between 8-row groups, LBO
+// unused, layout type 2 (SWIZZLE_128B) at bits 61-63.  A K = 16 step inside an
+// atom advances the start address by 32 B.
+__device__ __forceinline__ uint64_t umma_desc_sw128(uint32_t saddr) {
+    uint64_t d = 0;
+    d |= (uint64_t)((saddr >> 4) & 0x3FFFu);
+    d |= (uint64_t)1u << 16;
+    d |= (uint64_t)(1024u >> 4) << 32;
+    d |= (uint64_t)1u << 46;
+    d |= (uint64_t)2u << 61;
+    return d;
+}
+
+// TMA gather of 4 rows (ids r0..r3) x one box width starting at column c of a
+// 2-D tensor map (box height 1), into dst in the map's swizzle
+__device__ __forceinline__ void tma_gather4(void* dst, const void* tmap, int c, int r0, int r1,
+                                            int r2, int r3, uint64_t* bar) {
+    asm volatile(
+        "cp.async.bulk.tensor.2d.shared::cluster.global.tile::gather4.mbarrier::complete_tx::bytes"
+        " [%0], [%1, {%2, %3, %4, %5, %6}], [%7];" ::"r"(smem_u32(dst)),
+        "l"(reinterpret_cast<uint64_t>(tmap)), "r"(c), "r"(r0), "r"(r1), "r"(r2), "r"(r3),
+        "r"(smem_u32(bar))
+        : "memory");
+}
+
+// multicast variant: the 4 rows land at the same offset in every CTA of cta_mask
+__device__ __forceinline__ void tma_gather4_mc(void* dst, const void* tmap, int c, int r0, int r1,
+                                               int r2, int r3, uint64_t* bar, uint16_t cta_mask) {
+    asm volatile(
+        "cp.async.bulk.tensor.2d.shared::cluster.global.tile::gather4.mbarrier::complete_tx::bytes"
+        ".multicast::cluster [%0], [%1, {%2, %3, %4, %5, %6}], [%7], %8;" ::"r"(smem_u32(dst)),
+        "l"(reinterpret_cast<uint64_t>(tmap)), "r"(c), "r"(r0), "r"(r1), "r"(r2), "r"(r3),
+        "r"(smem_u32(bar)), "h"(cta_mask)
+        : "memory");
+}
+
 // Instruction descriptors (cute::UMMA::InstrDescriptor): D = F32 (bits 4-5 = 1),
 // A/B format at bits 7-9 / 10-12 (F16 = 0, TF32 = 2), both K-major, N>>3 at
 // bits 17-22, M>>4 at bits 24-28.
