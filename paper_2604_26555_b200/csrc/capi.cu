@@ -1124,6 +1124,10 @@ int tsom_set_option(tsom_engine* eng, int key, int64_t value) {
             case 96:  // diagnostics: 1 = the per-row main-pass merge (k_merge_fast)
                 tsom::g_merge_v1 = (int)value;
                 break;
+            case 94:  // diagnostics: pageable-bind staging chunk, bytes
+                REQUIRE(value >= (1 << 20), TSOM_ERR_INVALID, "option: chunk >= 1 MiB");
+                eng->pageable_chunk_bytes = (uint64_t)value;
+                break;
             case 95:  // diagnostics: 0 = no split image (selections split per pass)
                 eng->img_mode = (int)value;
                 eng->img_valid = false;
@@ -1204,12 +1208,12 @@ int tsom_bind_host_data(tsom_engine* eng, const float* rows, uint64_t n_rows, ui
         const auto tb0 = std::chrono::steady_clock::now();
         // page-locked rows: 8 chunks straight from the caller's buffer, each
         // chunk's norms / 256-B-stride placement overlapped with the next DMA;
-        // pageable rows: 32-MB chunks through the multi-threaded pinned staging
-        // (~22 GB/s, vs ~11 GB/s for the driver's own staging; B200 box,
-        // scripts/bind_breakdown.py)
+        // pageable rows: 128-MB chunks through the multi-threaded pinned
+        // staging (44 GB/s on 16 host threads; 32-MB chunks: 24.5 GB/s, the
+        // driver's own staging ~11 GB/s; scripts/pageable_bind_ab.py)
         const uint64_t rowb = (uint64_t)eng->D * sizeof(float);
         const uint64_t C = pinned ? std::max<uint64_t>((n_rows + 7) / 8, 4096)
-                                  : std::max<uint64_t>(1, ((uint64_t)32 << 20) / rowb);
+                                  : std::max<uint64_t>(1, eng->pageable_chunk_bytes / rowb);
         upload_resident(eng, n_rows, C);
         eng->host_rows = nullptr;
         eng->host_direct = false;

@@ -309,6 +309,7 @@ struct Engine {
     bool host_register = true;  // TSOM_OPT_HOST_REGISTER
     bool host_direct = false;   // streamed host rows are DMA-able (pinned)
     uint32_t staging_threads = 0;  // TSOM_OPT_STAGING_THREADS (0: min(16, host cores))
+    uint64_t pageable_chunk_bytes = (uint64_t)128 << 20;  // pageable bind staging chunk
     struct ShardFile {
         std::string path;
         int fd = -1;
