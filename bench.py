@@ -846,10 +846,13 @@ def leg_c1(args, ctx):
     cfg = dropin.TrainConfig(topology="rect", grid_w=10, grid_h=10, n_iters=EPOCHS, seed=seed)
     dropin.train_device(dropin.TrainConfig(topology="rect", grid_w=10, grid_h=10, n_iters=1,
                                            seed=seed), x, device=ctx["local"])
-    w_gpu, qe_gpu, _, secs = dropin.train_device(cfg, x, device=ctx["local"], log_qe=True)
+    # best of 3 whole runs (a 10-ms run: host-side jitter dominates one sample)
+    runs = [dropin.train_device(cfg, x, device=ctx["local"], log_qe=True) for _ in range(3)]
+    w_gpu, qe_gpu, _, secs = min(runs, key=lambda r: r[3])
     out = {"workload": "c1: 10x10 rect SOM, 1e5 x 50 GMM rows (reference generator), 10 epochs "
                        "(in full)", "unit": UNIT, "value": n * EPOCHS / secs,
-           "seconds": secs, "path": "toposom_b200::train_device, wall clock (host data)"}
+           "seconds": secs,
+           "path": "toposom_b200::train_device, wall clock (host data), best of 3 runs"}
     if args.no_cpu:
         return out
     chk = oracle.best()

@@ -567,7 +567,7 @@ void reset_order(Engine* eng) {
 // once one is there, then every row_order (>= 2) full training passes.
 bool order_due(const Engine* eng) {
     if (!eng->row_order || eng->streamed || !eng->x.owned || !eng->x.p || !eng->sorted_full ||
-        eng->n_rows < 2)
+        eng->n_rows < std::max<uint64_t>(2, eng->row_order_min))
         return false;
     if (!eng->ordered) return true;
     return eng->row_order >= 2 && eng->passes_since_order >= eng->row_order;
@@ -580,18 +580,20 @@ bool order_due(const Engine* eng) {
 void order_rows(Engine* eng) {
     tsom::NvtxRange nv("tsom.order_rows");
     const uint64_t n = eng->n_rows;
+    // stream-ordered: the new blocks and the frees of the old ones follow the
+    // engine stream (no device synchronisation in the middle of an epoch loop)
     DevBuf nx, np;
-    CU(nx.ensure(n * eng->D * sizeof(float) + tsom::kRowSlack));
-    CU(np.ensure(n * sizeof(uint32_t)));
+    CU(nx.ensure_on(n * eng->D * sizeof(float) + tsom::kRowSlack, eng->stream));
+    CU(np.ensure_on(n * sizeof(uint32_t), eng->stream));
     tsom::launch_permute_rows(eng->x.as<float>(), eng->ldx, eng->acc.sorted, n, eng->D,
                               nx.as<float>(), eng->ordered ? eng->perm.as<uint32_t>() : nullptr,
                               np.as<uint32_t>(), eng->stream);
     CU(cudaGetLastError());
     std::swap(eng->x, nx);
     std::swap(eng->perm, np);
-    nx.release();  // (after a device synchronisation: the permute has read it)
-    np.release(true);
-    CU(eng->pinv.ensure(n * sizeof(uint32_t)));
+    nx.release_on(eng->stream);
+    np.release_on(eng->stream);
+    CU(eng->pinv.ensure_on(n * sizeof(uint32_t), eng->stream));
     tsom::launch_invert_perm(eng->perm.as<uint32_t>(), n, eng->pinv.as<uint32_t>(), eng->stream);
     CU(cudaGetLastError());
     eng->ldx = eng->D;
@@ -1028,6 +1030,11 @@ int tsom_create(int device, uint32_t nodes, uint32_t dims, tsom_engine** out) {
         }
         eng->sm_count = sms;
         eng->smem_optin = (size_t)smem;
+        // diagnostics: defaults for engines built by code that sets no options
+        // (the C++ drop-ins), for A/B runs
+        if (const char* v = getenv("TSOM_ROW_ORDER")) eng->row_order = (uint32_t)atoi(v);
+        if (const char* v = getenv("TSOM_PAGEABLE_CHUNK_MB"))
+            eng->pageable_chunk_bytes = std::max<uint64_t>(1, (uint64_t)atoll(v)) << 20;
         CU(cudaStreamCreateWithFlags(&eng->stream, cudaStreamNonBlocking));
         CU(cudaStreamCreateWithFlags(&eng->copy_stream, cudaStreamNonBlocking));
         for (auto& ev : eng->ev) CU(cudaEventCreate(&ev));
@@ -1123,6 +1130,9 @@ int tsom_set_option(tsom_engine* eng, int key, int64_t value) {
                 break;
             case 96:  // diagnostics: 1 = the per-row main-pass merge (k_merge_fast)
                 tsom::g_merge_v1 = (int)value;
+                break;
+            case 93:  // diagnostics: fewest rows a BMU-order re-layout is made for
+                eng->row_order_min = (uint64_t)value;
                 break;
             case 94:  // diagnostics: pageable-bind staging chunk, bytes
                 REQUIRE(value >= (1 << 20), TSOM_ERR_INVALID, "option: chunk >= 1 MiB");

@@ -41,6 +41,10 @@ struct DevBuf {
     bool owned = true;
     cudaError_t ensure(size_t need);
     void release(bool synced = false);  // synced: the device is known idle
+    // stream-ordered variants (no synchronisation): the block is usable by
+    // work queued on st after the call / returned once st's queued work is done
+    cudaError_t ensure_on(size_t need, cudaStream_t st);
+    void release_on(cudaStream_t st);
     template <typename T>
     T* as() const { return static_cast<T*>(p); }
 };
@@ -246,6 +250,7 @@ struct Engine {
     // order of an earlier full pass — position q holds caller row perm[q],
     // pinv is the inverse; every call still takes and returns caller row ids
     uint32_t row_order = 1;     // 0 off, 1 once, R >= 2 also every R full passes
+    uint64_t row_order_min = 1u << 18;  // fewer rows: not worth a re-layout
     bool ordered = false;
     DevBuf perm, pinv, idmap;   // idmap: a selection mapped to positions
     DevBuf unperm;              // per-row outputs scattered back to caller order

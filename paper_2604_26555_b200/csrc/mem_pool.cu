@@ -116,6 +116,37 @@ cudaError_t DevBuf::ensure(size_t need) {
     return cudaSuccess;
 }
 
+cudaError_t DevBuf::ensure_on(size_t need, cudaStream_t st) {
+    if (need <= bytes && p) return cudaSuccess;
+    if (pool_disabled()) return ensure(need);
+    release_on(st);
+    DevicePool* dp = nullptr;
+    cudaError_t e = device_pool(&dp);
+    if (e == cudaSuccess) e = cudaMallocFromPoolAsync(&p, need, dp->pool, st);
+    if (e != cudaSuccess) {
+        p = nullptr;
+        bytes = 0;
+        return e;
+    }
+    bytes = need;
+    owned = true;
+    return cudaSuccess;
+}
+
+void DevBuf::release_on(cudaStream_t st) {
+    if (p && owned) {
+        if (pool_disabled()) {
+            cudaStreamSynchronize(st);
+            cudaFree(p);
+        } else {
+            cudaFreeAsync(p, st);
+        }
+    }
+    p = nullptr;
+    bytes = 0;
+    owned = true;
+}
+
 void DevBuf::release(bool synced) {
     if (p && owned) {
         DevicePool* dp = nullptr;

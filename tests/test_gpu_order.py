@@ -36,6 +36,7 @@ def make_pair(pkg, x, w, dist, order=1, exact=False):
     for ro in (0, order):
         e = pkg.Engine(w.shape[0], w.shape[1])
         e.set_option(_lib.TSOM_OPT_ROW_ORDER, ro)
+        e.set_option(93, 0)  # re-lay out even these 60k rows (default: >= 2^18 rows)
         if exact:
             e.set_option(_lib.TSOM_OPT_DETERMINISTIC, 1)
         e.bind(x)
