@@ -892,15 +892,15 @@ def roofline_peak(kernel, pk):
     return "SIMT FP32", pk.get("fp32_tflops", 75.0), "(FP32 SIMT, nominal)"
 
 
-# ncu --set full, one launch of K1 at the bench shape (1e7 x 50, K=1024):
-# dram__bytes_read.sum + dram__bytes_write.sum, bytes per launch
-# (profiles/r02b_ncu_full_summary.json, scripts/ncu_round2b.sh).  The split A
+# ncu --set full, one launch of K1 at the bench shape (1e7 x 50, K=1024, rows in
+# BMU order): dram__bytes_read.sum + dram__bytes_write.sum, bytes per launch
+# (profiles/r02c_ncu_full_summary.json, scripts/ncu_round2c.sh).  The split A
 # tiles are 3.2 GB; the 4 codebook-group CTAs each stream them and L2 catches
 # part of the repeats (earlier captures: 3.74-6.61 GB read).
-K1_TRAFFIC = {3: 5.024428e9 + 0.3197955e9}
-K1_TRAFFIC_SRC = "profiles/r02b_ncu_full_summary.json, k1_bmu_tc<2, 0, 0>: 5.02 GB read (split A " \
-                 "tiles 3.2 GB, each streamed by the 4 node-group CTAs, partly from L2) + " \
-                 "0.32 GB per-group partial-result writes"
+K1_TRAFFIC = {3: 6.139586e9 + 0.3201408e9}
+K1_TRAFFIC_SRC = "profiles/r02c_ncu_full_summary.json, k1_bmu_tc<2, 0, 0, 1>: 6.14 GB read " \
+                 "(split A tiles 3.2 GB, each streamed by the 4 node-group CTAs, partly from L2) " \
+                 "+ 0.32 GB per-group partial-result writes"
 
 
 def main():
