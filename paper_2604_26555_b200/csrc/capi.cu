@@ -160,6 +160,31 @@ cudaEvent_t k1_event(Engine* eng, int end) {
 
 constexpr uint32_t kTieLogCap = 1024;  // tie_log entries between two syncs
 
+// An engine's pinned host words (hstat: 32 status words, then tie_log) come
+// from a process-wide cache: cudaMallocHost / cudaFreeHost cost milliseconds
+// per call (a third of an engine's creation), and studies create many engines.
+constexpr size_t kHostWords = 32 + 2 * kTieLogCap;
+std::mutex g_host_words_mu;
+std::vector<uint32_t*> g_host_words_free;
+
+cudaError_t host_words_take(uint32_t** out) {
+    {
+        std::lock_guard<std::mutex> lk(g_host_words_mu);
+        if (!g_host_words_free.empty()) {
+            *out = g_host_words_free.back();
+            g_host_words_free.pop_back();
+            return cudaSuccess;
+        }
+    }
+    return cudaMallocHost(reinterpret_cast<void**>(out), kHostWords * sizeof(uint32_t));
+}
+
+void host_words_give(uint32_t* p) {
+    if (!p) return;
+    std::lock_guard<std::mutex> lk(g_host_words_mu);
+    g_host_words_free.push_back(p);
+}
+
 // the near-tie fractions logged since the last sync (called after it)
 void fold_tie_log(Engine* eng) {
     if (eng->tie_log_n == 0) return;
@@ -1055,8 +1080,8 @@ int tsom_create(int device, uint32_t nodes, uint32_t dims, tsom_engine** out) {
         CU(eng->status.ensure(8 * sizeof(int)));
         CU(eng->hmax.ensure(tsom::kHmaxParts * sizeof(double)));
         CU(cudaMemsetAsync(eng->hmax.p, 0, tsom::kHmaxParts * sizeof(double), eng->stream));
-        CU(cudaMallocHost(&eng->hstat, 32 * sizeof(uint32_t)));
-        CU(cudaMallocHost(&eng->tie_log, 2 * kTieLogCap * sizeof(uint32_t)));
+        CU(host_words_take(&eng->hstat));
+        eng->tie_log = eng->hstat + 32;
         CU(eng->tie_dev.ensure(kTieLogCap * sizeof(uint32_t)));
         std::memset(eng->hstat, 0, 32 * sizeof(uint32_t));
         ensure_rows(eng, 1);
@@ -1087,8 +1112,7 @@ int tsom_destroy(tsom_engine* eng) {
         b->release(true);
     for (auto& ev : eng->ev)
         if (ev) cudaEventDestroy(ev);
-    if (eng->hstat) cudaFreeHost(eng->hstat);
-    if (eng->tie_log) cudaFreeHost(eng->tie_log);
+    host_words_give(eng->hstat);  // (tie_log lives in the same block)
     for (cudaEvent_t e : eng->k1_ev) cudaEventDestroy(e);
     for (cudaEvent_t e : eng->red_ev) cudaEventDestroy(e);
     if (eng->stream) cudaStreamDestroy(eng->stream);
