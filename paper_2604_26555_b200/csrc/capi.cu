@@ -1155,6 +1155,9 @@ int tsom_set_option(tsom_engine* eng, int key, int64_t value) {
             case 96:  // diagnostics: 1 = the per-row main-pass merge (k_merge_fast)
                 tsom::g_merge_v1 = (int)value;
                 break;
+            case 92:  // diagnostics: gathered split L2 prefetch distance in chunks (0 = off)
+                tsom::g_split_prefetch = (int)value;
+                break;
             case 93:  // diagnostics: fewest rows a BMU-order re-layout is made for
                 eng->row_order_min = (uint64_t)value;
                 break;

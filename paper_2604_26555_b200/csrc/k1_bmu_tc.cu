@@ -419,7 +419,7 @@ __global__ void __launch_bounds__(kSplitThreads, 4) k_split_rows_f16(
     const float* __restrict__ x, uint32_t ldx, const uint32_t* __restrict__ sel,
     const uint32_t* __restrict__ idx, const uint32_t* __restrict__ dev_n, uint64_t n_host,
     uint32_t D, const float* __restrict__ scale, TieWin win, uint8_t* __restrict__ tiles,
-    float* __restrict__ xn2, uint32_t img_w = 0) {
+    float* __restrict__ xn2, uint32_t img_w = 0, int prefetch = 0) {
     extern __shared__ __align__(16) uint8_t split_wsm[];
     const uint64_t n = dev_n ? min((uint64_t)*dev_n, n_host) : n_host;
     constexpr uint32_t kChunksPerTile = kTcTileM / kSplitWarpRows;
@@ -441,6 +441,17 @@ __global__ void __launch_bounds__(kSplitThreads, 4) k_split_rows_f16(
         if (lane < rows) {
             const uint64_t pos = idx ? (uint64_t)idx[r0 + lane] : r0 + lane;
             myrow = sel ? (uint64_t)sel[pos] : pos;
+        }
+        if (sel && prefetch) {
+            // gathered rows: the warp's chunk `prefetch` iterations ahead into
+            // L2 while this one is loaded and converted (lane l < 16: row l,
+            // lane l + 16: its second 128-B line), raising the rows in flight
+            const uint64_t cn = c + (uint64_t)prefetch * nwarps, rn = cn * kSplitWarpRows + (lane & 15u);
+            if (rn < n && rn < nchunks * kSplitWarpRows) {
+                const uint64_t pos = idx ? (uint64_t)idx[rn] : rn;
+                const float* a = x + (uint64_t)sel[pos] * ldx + (lane >> 4) * 32u;
+                asm volatile("prefetch.global.L2 [%0];" ::"l"(a));
+            }
         }
         float v[kSplitWarpRows][2];
 #pragma unroll
@@ -524,6 +535,7 @@ __global__ void __launch_bounds__(kSplitThreads, 4) k_split_rows_f16(
 }
 
 int g_split_v1 = 0;  // debug: the element-wise split (TSOM option 98)
+int g_split_prefetch = 1;  // gathered split: L2 prefetch distance in chunks (option 92; 0 off)
 
 void launch_split_rows(int kind, const float* x, const uint32_t* sel, const uint32_t* idx,
                        uint64_t n, uint32_t D, const float* scale, TieWin win, void* tiles,
@@ -553,7 +565,7 @@ void launch_split_rows(int kind, const float* x, const uint32_t* sel, const uint
         uint64_t blocks = (n + kTcTileM - 1) / kTcTileM;  // 8 warps x 16 rows per tile
         if (blocks > 148ull * 8) blocks = 148ull * 8;
         TSOM_LAUNCH(k_split_rows_f16<<<(unsigned)blocks, kSplitThreads, wsmem, st>>>(
-            x, ldx, sel, idx, dev_n, n, D, scale, win, t, xn2));
+            x, ldx, sel, idx, dev_n, n, D, scale, win, t, xn2, 0u, g_split_prefetch));
     }
 }
 
