@@ -2174,12 +2174,14 @@ int tsom_debug_k1_trace(unsigned long long* out, uint32_t n) {
 
 // diagnostics only (not in the public header): copy an internal device buffer
 // (0 xsplit, 1 xn2, 2 wsplit, 3 scale, 4 part, 5 gsplit, 6 gxn2, 7 w2max,
-// 8 x2max, 9 ties) to the host; returns the bytes copied
+// 8 x2max, 9 ties, 10 bmu (per position), 11 perm) to the host; returns the
+// bytes copied
 int64_t tsom_debug_read(tsom_engine* eng, int which, void* out, uint64_t bytes) {
     if (!eng) return -1;
     cudaSetDevice(eng->device);
     tsom::DevBuf* bufs[] = {&eng->xsplit, &eng->xn2, &eng->wsplit, &eng->scale, &eng->part,
-                            &eng->gsplit, &eng->gxn2, &eng->w2max, &eng->x2max, &eng->ties};
+                            &eng->gsplit, &eng->gxn2, &eng->w2max, &eng->x2max, &eng->ties,
+                            &eng->bmu, &eng->perm};
     if (which < 0 || which >= (int)(sizeof(bufs) / sizeof(bufs[0]))) return -1;
     const uint64_t nb = std::min<uint64_t>(bytes, bufs[which]->bytes);
     cudaStreamSynchronize(eng->stream);
