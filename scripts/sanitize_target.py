@@ -7,7 +7,10 @@ compute-sanitizer (memcheck / racecheck / synccheck / initcheck):
   * K3 smoothing, apply_update, influence, the term guard (cheap path and the
     exact extremes path), the device sampler (random + adaptive, with
     observe), topology refresh (MST + RNG), a streamed epoch, a 2-rank group
-    epoch.
+    epoch;
+  * the BMU-order re-layout (k_order.cu: permute, inverse, id mapping,
+    scatter back), K1's chunk-skipping epilogue, K2's contiguous-batch copies,
+    and the split image with K1's gather4 mode (multicast over the cluster).
 
 Usage: compute-sanitizer --tool racecheck python scripts/sanitize_target.py
 """
@@ -41,6 +44,22 @@ for kernel in (3, 2, 1):
     e.epoch(0.3, sel, want_dist=True)
     e.qe()
     e.close()
+
+# BMU-ordered rows (re-layout forced at this size), then selections through
+# the mapping; the split image + gather4 K1 for a selection
+e = tsom.Engine(P, D)
+e.set_option(93, 0)
+e.bind(x)
+e.set_codebook(w)
+e.set_topology_distance(dist)
+e.train_epochs([0.5, 0.4, 0.3], [4.0, 3.0, 2.0])
+e.bmu_bound(None)
+e.get_rows(10, 100)
+e.set_influence(np.exp(-dist ** 2 / 8.0))
+e.epoch(0.3, np.arange(n - 1, 0, -2, dtype=np.uint32), want_dist=True)
+e.set_option(95, 1)
+e.epoch(0.3, np.arange(0, n, 2, dtype=np.uint32), want_dist=True)
+e.close()
 
 # packed rows (no 256-B stride), random + adaptive samplers, refresh, guard paths
 e = tsom.Engine(P, D)
