@@ -275,7 +275,8 @@ int tsom_last_timing(const tsom_engine* eng, float* bmu_ms, float* accum_ms, flo
 /* Detail of the last epoch (ms): [0] BMU kernel (K1) alone, [1] BMU phase incl.
  * merge + exact re-check, [2] accumulation + reduce (+ allreduce), [3] smoothing,
  * [4] device update (tsom_train_epoch), [5] total (sampler excluded), [6] device sampler
- * (sampled tsom_train_epoch). */
+ * (sampled tsom_train_epoch), [7] mean accumulation phase over the epochs of the last
+ * tsom_train_epochs call (resident rows; per-epoch events). */
 int tsom_last_timing_detail(const tsom_engine* eng, float out[8]);
 /* Device memory this engine holds (bytes of its buffers, sampler included). */
 uint64_t tsom_device_bytes(const tsom_engine* eng);

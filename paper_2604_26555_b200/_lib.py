@@ -421,8 +421,9 @@ class Engine:
     def timing_detail(self):
         v = (C.c_float * 8)()
         self._check(self.L.tsom_last_timing_detail(self.h, v))
-        keys = ["k1_ms", "bmu_ms", "accum_ms", "smooth_ms", "update_ms", "total_ms", "sample_ms"]
-        return dict(zip(keys, list(v)[:7]))
+        keys = ["k1_ms", "bmu_ms", "accum_ms", "smooth_ms", "update_ms", "total_ms", "sample_ms",
+                "accum_mean_ms"]
+        return dict(zip(keys, list(v)))
 
     @property
     def stream(self) -> int:

@@ -722,6 +722,8 @@ void accumulate_epoch(Engine* eng, const uint32_t* sel_host, uint64_t n_sel, boo
         eng->pass_sel = dsel;
         eng->pass_n = n;
         CU(cudaEventRecord(eng->ev[1], eng->stream));
+        if (eng->k1_slot >= 0)  // multi-epoch call: this epoch's accumulation phase
+            CU(cudaEventRecord(eng->acc_ev[2 * (size_t)eng->k1_slot], eng->stream));
         ensure_accum(eng, n);
         const int arc = tsom::launch_accumulate(
             eng->x.as<float>(), dsel, n, eng->D, eng->w.as<float>(), eng->P,
@@ -858,6 +860,8 @@ void accumulate_epoch(Engine* eng, const uint32_t* sel_host, uint64_t n_sel, boo
         if (rc != TSOM_OK) throw tsom::Fail{rc};
     }
     CU(cudaEventRecord(eng->ev[2 + 4], eng->stream));
+    if (eng->k1_slot >= 0 && !eng->streamed)
+        CU(cudaEventRecord(eng->acc_ev[2 * (size_t)eng->k1_slot + 1], eng->stream));
 }
 
 std::string barrier_seconds(double s) { return std::to_string(s); }  // the reference's format
@@ -1114,6 +1118,7 @@ int tsom_destroy(tsom_engine* eng) {
         if (ev) cudaEventDestroy(ev);
     host_words_give(eng->hstat);  // (tie_log lives in the same block)
     for (cudaEvent_t e : eng->k1_ev) cudaEventDestroy(e);
+    for (cudaEvent_t e : eng->acc_ev) cudaEventDestroy(e);
     for (cudaEvent_t e : eng->red_ev) cudaEventDestroy(e);
     if (eng->stream) cudaStreamDestroy(eng->stream);
     if (eng->copy_stream) cudaStreamDestroy(eng->copy_stream);
@@ -2111,6 +2116,11 @@ int tsom_train_epochs(tsom_engine* eng, uint32_t n_epochs, const double* eta,
             CU(cudaEventCreate(&ev));
             eng->k1_ev.push_back(ev);
         }
+        while (eng->acc_ev.size() < 2 * (size_t)n_epochs) {
+            cudaEvent_t ev;
+            CU(cudaEventCreate(&ev));
+            eng->acc_ev.push_back(ev);
+        }
         int* dead = eng->dead.as<int>();
         struct SlotReset {
             Engine* e;
@@ -2145,6 +2155,17 @@ int tsom_train_epochs(tsom_engine* eng, uint32_t n_epochs, const double* eta,
             }
             eng->t_k1 = sum / (float)n_epochs;  // mean main-pass K1 time of the call
             cudaGetLastError();  // a timing query is never an error of the epochs
+        }
+        eng->t_accum_mean = 0.0f;
+        if (!eng->streamed) {
+            float sum = 0.0f;
+            for (uint32_t t = 0; t < n_epochs; ++t) {
+                float ms = 0.0f;
+                cudaEventElapsedTime(&ms, eng->acc_ev[2 * (size_t)t], eng->acc_ev[2 * (size_t)t + 1]);
+                sum += ms;
+            }
+            eng->t_accum_mean = sum / (float)n_epochs;  // mean accumulation phase of the call
+            cudaGetLastError();
         }
         int rec[3];
         std::memcpy(rec, eng->hstat + 5, sizeof(rec));
@@ -2289,7 +2310,7 @@ int tsom_last_timing(const tsom_engine* eng, float* bmu_ms, float* accum_ms, flo
 int tsom_last_timing_detail(const tsom_engine* eng, float out[8]) {
     if (!eng || !out) return TSOM_ERR_INVALID;
     const float v[8] = {eng->t_k1,    eng->t_bmu,    eng->t_accum,  eng->t_smooth,
-                        eng->t_update, eng->t_total, eng->t_sample, 0.0f};
+                        eng->t_update, eng->t_total, eng->t_sample, eng->t_accum_mean};
     std::memcpy(out, v, sizeof(v));
     return TSOM_OK;
 }

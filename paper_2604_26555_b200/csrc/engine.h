@@ -326,6 +326,8 @@ struct Engine {
     // records k1_ev[2t], k1_ev[2t+1] instead of ev[8], ev[9]) and the device
     // failure record [epoch + 1, kind (1 non-finite update, 2 term guard), node]
     std::vector<cudaEvent_t> k1_ev;
+    std::vector<cudaEvent_t> acc_ev;  // the same for the accumulation phase (resident passes)
+    float t_accum_mean = 0.0f;        // mean accumulation phase of the last multi-epoch call
     int k1_slot = -1;
     DevBuf dead;
     uint64_t last_recheck = 0;
