@@ -442,14 +442,14 @@ __global__ void __launch_bounds__(kSplitThreads, 4) k_split_rows_f16(
             const uint64_t pos = idx ? (uint64_t)idx[r0 + lane] : r0 + lane;
             myrow = sel ? (uint64_t)sel[pos] : pos;
         }
-        if (sel && prefetch) {
+        if ((sel || idx) && prefetch) {
             // gathered rows: the warp's chunk `prefetch` iterations ahead into
             // L2 while this one is loaded and converted (lane l < 16: row l,
             // lane l + 16: its second 128-B line), raising the rows in flight
             const uint64_t cn = c + (uint64_t)prefetch * nwarps, rn = cn * kSplitWarpRows + (lane & 15u);
             if (rn < n && rn < nchunks * kSplitWarpRows) {
                 const uint64_t pos = idx ? (uint64_t)idx[rn] : rn;
-                const float* a = x + (uint64_t)sel[pos] * ldx + (lane >> 4) * 32u;
+                const float* a = x + (sel ? (uint64_t)sel[pos] : pos) * ldx + (lane >> 4) * 32u;
                 asm volatile("prefetch.global.L2 [%0];" ::"l"(a));
             }
         }
