@@ -608,8 +608,20 @@ void order_rows(Engine* eng) {
     // stream-ordered: the new blocks and the frees of the old ones follow the
     // engine stream (no device synchronisation in the middle of an epoch loop)
     DevBuf nx, np;
-    CU(nx.ensure_on(n * eng->D * sizeof(float) + tsom::kRowSlack, eng->stream));
-    CU(np.ensure_on(n * sizeof(uint32_t), eng->stream));
+    if (nx.ensure_on(n * eng->D * sizeof(float) + tsom::kRowSlack, eng->stream) != cudaSuccess ||
+        np.ensure_on(n * sizeof(uint32_t), eng->stream) != cudaSuccess ||
+        (!eng->ordered &&
+         eng->pinv.ensure_on(n * sizeof(uint32_t), eng->stream) != cudaSuccess)) {
+        // no room for a second copy of the rows: an optimisation, not a
+        // failure — the rows keep their layout and no re-layout is tried again
+        cudaGetLastError();
+        nx.release_on(eng->stream);
+        np.release_on(eng->stream);
+        if (!eng->ordered) eng->pinv.release_on(eng->stream);
+        eng->row_order = 0;
+        eng->sorted_full = false;
+        return;
+    }
     tsom::launch_permute_rows(eng->x.as<float>(), eng->ldx, eng->acc.sorted, n, eng->D,
                               nx.as<float>(), eng->ordered ? eng->perm.as<uint32_t>() : nullptr,
                               np.as<uint32_t>(), eng->stream);
@@ -618,7 +630,6 @@ void order_rows(Engine* eng) {
     std::swap(eng->perm, np);
     nx.release_on(eng->stream);
     np.release_on(eng->stream);
-    CU(eng->pinv.ensure_on(n * sizeof(uint32_t), eng->stream));
     tsom::launch_invert_perm(eng->perm.as<uint32_t>(), n, eng->pinv.as<uint32_t>(), eng->stream);
     CU(cudaGetLastError());
     eng->ldx = eng->D;

@@ -123,6 +123,11 @@ cudaError_t DevBuf::ensure_on(size_t need, cudaStream_t st) {
     DevicePool* dp = nullptr;
     cudaError_t e = device_pool(&dp);
     if (e == cudaSuccess) e = cudaMallocFromPoolAsync(&p, need, dp->pool, st);
+    if (e == cudaErrorMemoryAllocation) {  // cached blocks may be in the way
+        cudaGetLastError();
+        release_cached_memory();
+        e = cudaMallocFromPoolAsync(&p, need, dp->pool, st);
+    }
     if (e != cudaSuccess) {
         p = nullptr;
         bytes = 0;
