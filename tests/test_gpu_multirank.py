@@ -547,3 +547,47 @@ def test_exact_dropin_bit_identical_across_engines(pkg, kw):
     assert np.array_equal(ws[0], ws[1]) and np.array_equal(ws[0], ws[2])
     wc = [dropin.train_cuda(cfg, g["x"], engines=k, exact=True)[0] for k in (1, 3)]
     assert np.array_equal(wc[0], wc[1])
+
+
+@pytest.mark.parametrize("world", [1, 3])
+def test_exact_training_with_bmu_ordered_shards(pkg, oracle_port, world):
+    """Every rank re-lays its shard out in BMU order (TSOM_OPT_ROW_ORDER, forced
+    at this size) while the single reference engine keeps the bind order: in
+    exact mode the sums do not depend on the row order, so the codebooks are
+    identical bit for bit, and the per-row BMUs come back in caller order."""
+    from paper_2604_26555_b200 import _lib
+    from paper_2604_26555_b200.hostref import init_sample_draw, lattice_dist, resolved_sigma0
+    n, p = 40000, 1024
+    x = oracle_port.synth_gmm(n, 50, 2606)
+    w0 = init_sample_draw(x, p, 2606)
+    dist = lattice_dist("hex", 32, 32)
+    etas, sigmas = _schedules(10, resolved_sigma0("hex", 32, 32))
+
+    def configure(e):
+        e.set_codebook(w0)
+        e.set_topology_distance(dist)
+
+    single = exact_engine(pkg, x, p, configure)
+    single.set_option(_lib.TSOM_OPT_ROW_ORDER, 0)
+    single.train_epochs(etas, sigmas)
+    w1 = single.get_codebook()
+    b1, _ = single.bmu_bound(None, want_dist=False)
+    g = pkg.RankGroup(world)
+    engines = []
+    sl = assign_shards(n, world)
+    for r, (a, b) in enumerate(sl):
+        e = pkg.Engine(p, 50)
+        e.set_option(_lib.TSOM_OPT_DETERMINISTIC, 1)
+        e.set_option(93, 0)  # re-lay out even these shards
+        e.bind(x[a:b])
+        configure(e)
+        e.join_group(g, r)
+        engines.append(e)
+    run_ranks(world, lambda r: engines[r].train_epochs(etas, sigmas))
+    for r in range(world):
+        assert np.array_equal(engines[r].get_codebook(), w1), f"rank {r}"
+    bm = run_ranks(world, lambda r: engines[r].bmu_bound(None, want_dist=False)[0])
+    assert (np.concatenate(bm) == b1).all()
+    for r, (a, b) in enumerate(sl):
+        assert np.array_equal(engines[r].get_rows(), x[a:b])
+    g.close()
