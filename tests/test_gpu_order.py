@@ -30,11 +30,13 @@ def rel_maxnorm(a, b):
     return float(np.max(np.abs(np.asarray(a, np.float64) - b)) / max(np.max(np.abs(b)), 1e-300))
 
 
-def make_pair(pkg, x, w, dist, order=1, exact=False):
+def make_pair(pkg, x, w, dist, order=1, exact=False, kernel=0):
     from paper_2604_26555_b200 import _lib
     es = []
     for ro in (0, order):
         e = pkg.Engine(w.shape[0], w.shape[1])
+        if kernel:
+            e.set_option(_lib.TSOM_OPT_BMU_KERNEL, kernel)
         e.set_option(_lib.TSOM_OPT_ROW_ORDER, ro)
         e.set_option(93, 0)  # re-lay out even these 60k rows (default: >= 2^18 rows)
         if exact:
@@ -59,9 +61,10 @@ def influence(oracle_port, dist, sigma):
     return oracle_port.influence_from_dist(dist, sigma)
 
 
-def test_epoch_outputs_match_bind_order(pkg, data, oracle_port):
+@pytest.mark.parametrize("kernel", [3, 2, 1], ids=["3xFP16", "3xTF32", "SIMT"])
+def test_epoch_outputs_match_bind_order(pkg, data, oracle_port, kernel):
     x, w, dist = data
-    a, b = make_pair(pkg, x, w, dist)
+    a, b = make_pair(pkg, x, w, dist, kernel=kernel)
     try:
         infl = influence(oracle_port, dist, 6.0)
         for e in (a, b):
