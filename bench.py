@@ -314,6 +314,8 @@ def run_gpu_arm(args):
         eng.set_option(_lib.TSOM_OPT_BMU_KERNEL, args.kernel)
     if args.row_order is not None:
         eng.set_option(_lib.TSOM_OPT_ROW_ORDER, args.row_order)
+    if args.k1_debug is not None:
+        eng.set_option(99, args.k1_debug)  # diagnostics A/B (process-wide K1 variant bits)
     eng.bind(host)
     active_kernel = eng.active_bmu_kernel
     attach_comm(eng)
@@ -918,6 +920,7 @@ def main():
     ap.add_argument("--row-order", type=int, default=None,
                     help="TSOM_OPT_ROW_ORDER for the c2 engines (default: the engine's, 1)")
     ap.add_argument("--image", type=int, default=None, help=argparse.SUPPRESS)  # c4: split image A/B
+    ap.add_argument("--k1-debug", type=int, default=None, help=argparse.SUPPRESS)  # option 99 A/B
     ap.add_argument("--no-e2e", action="store_true")
     ap.add_argument("--no-cpu", action="store_true")
     ap.add_argument("--no-c4", action="store_true", help="skip the c4 (1e8 rows, adaptive) leg")

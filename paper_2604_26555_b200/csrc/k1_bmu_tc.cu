@@ -686,7 +686,7 @@ __global__ void __launch_bounds__(EpiCfg<kKind>::kThreads, 1)
             // sequence) each gather 128 / mc rows of the tile and multicast
             // them to all, so every row is fetched once per cluster
             const uint32_t rpc = kTcTileM / mc;
-            const uint32_t row = (mc > 1 ? g * rpc : 0u) + 4u * lane;
+            const uint32_t row = (mc > 1 ? (g % mc) * rpc : 0u) + 4u * lane;
             for (uint32_t t = cta_in_group; t < ntiles; t += ctas_per_group) {
                 if (kEnum && tile_mask && !((tile_mask[t] >> (g & 31)) & 1u)) continue;
                 mbar_wait(&empty_bar[stage], phase ^ 1);
@@ -731,7 +731,7 @@ __global__ void __launch_bounds__(EpiCfg<kKind>::kThreads, 1)
                     mbar_arrive(&full_bar[stage]);
                 } else if (mc > 1) {
                     // this CTA's slice of the tile, to the same stage of every CTA
-                    const uint32_t slice = geo.tile_bytes / mc, off = g * slice;
+                    const uint32_t slice = geo.tile_bytes / mc, off = (g % mc) * slice;
                     mbar_expect_tx(&full_bar[stage], geo.tile_bytes);
                     bulk_g2s_mc(sX + stage * geo.tile_bytes + off,
                                 tiles + (size_t)t * geo.tile_bytes + off, slice, &full_bar[stage],
@@ -1156,6 +1156,14 @@ cudaError_t launch_bmu_tc(int kind, const void* tiles, uint64_t n, const uint32_
     if (!gather && (g_k1_debug & 64u) && groups >= 2 && groups <= 8 &&
         geo.tile_bytes % (16u * groups) == 0)
         mc = groups;
+    // main pass: clusters of 2 group CTAs share each A tile (each CTA loads half
+    // and multicasts it), so a tile leaves HBM/L2 twice instead of four times at
+    // K = 1024: less DRAM power under the cap, K1 2.37 -> 2.30 ms (bench A/B,
+    // scripts/ab_mc2.sh; all four groups per cluster packs fewer clusters onto
+    // the GPCs and was slower).  Option 99 bit 12 turns it off.
+    if (!gather && !enumerate && mc == 1 && !(g_k1_debug & 4096u) && groups % 2 == 0 &&
+        geo.tile_bytes % 32u == 0)
+        mc = 2;
     // gathered rows: each row fetched once per cluster of the group CTAs
     // (the per-CTA gather4 rate bounds the kernel otherwise; option 99 bit 10 off)
     if (gather && groups >= 2 && groups <= 8 && kTcTileM % (4u * groups) == 0 &&
