@@ -900,14 +900,15 @@ def roofline_peak(kernel, pk):
 
 
 # ncu --set full, one launch of K1 at the bench shape (1e7 x 50, K=1024, rows in
-# BMU order): dram__bytes_read.sum + dram__bytes_write.sum, bytes per launch
+# BMU order, A tiles multicast over clusters of 2 group CTAs):
+# dram__bytes_read.sum + dram__bytes_write.sum, bytes per launch
 # (profiles/r02c_ncu_full_summary.json, scripts/ncu_round2c.sh).  The split A
-# tiles are 3.2 GB; the 4 codebook-group CTAs each stream them and L2 catches
-# part of the repeats (earlier captures: 3.74-6.61 GB read).
-K1_TRAFFIC = {3: 6.139586e9 + 0.3201408e9}
-K1_TRAFFIC_SRC = "profiles/r02c_ncu_full_summary.json, k1_bmu_tc<2, 0, 0, 1>: 6.14 GB read " \
-                 "(split A tiles 3.2 GB, each streamed by the 4 node-group CTAs, partly from L2) " \
-                 "+ 0.32 GB per-group partial-result writes"
+# tiles are 3.2 GB: each now leaves DRAM about once (6.1 GB without the
+# multicast, the 4 group CTAs streaming every tile and L2 catching part).
+K1_TRAFFIC = {3: 3.309947e9 + 0.322691e9}
+K1_TRAFFIC_SRC = "profiles/r02c_ncu_full_summary.json, k1_bmu_tc<2, 0, 0, 1> (clusters of 2): " \
+                 "3.31 GB read (the 3.2 GB of split A tiles about once; each cluster loads a " \
+                 "tile once and multicasts it) + 0.32 GB per-group partial-result writes"
 
 
 def main():
