@@ -70,13 +70,16 @@ extern "C" {
 #define TSOM_OPT_STAGING_THREADS 6 /* host threads filling the pinned staging (default: min(16, cores)) */
 #define TSOM_OPT_PAD_ROWS 8          /* resident rows at a 256-B stride (d even, <= 62):
                                         1 (default) or 0 = packed d-float rows */
-#define TSOM_OPT_ROW_ORDER 9          /* resident rows kept in BMU order: 0 = bind order,
-                                         1 (default) = re-laid out (packed) once, in the BMU order
-                                         of the first full pass over them, R >= 2 = and again
-                                         every R full training passes.  Rows that share a BMU are
-                                         then adjacent: K1 skips the column chunks no row of a
-                                         warp needs, K2 gathers runs of rows in one copy.  Row
-                                         ids in every call stay the caller's */
+#define TSOM_OPT_ROW_ORDER 9          /* resident rows kept in BMU order (rows that share a
+                                         BMU adjacent: K1 skips the column chunks no row of a warp
+                                         needs, K2 copies runs of rows): 0 = bind order; 1
+                                         (default, auto) = re-laid out (packed) once, in the BMU
+                                         order of the last full pass, at an epoch of a
+                                         tsom_train_epochs call with >= 20 epochs still to run (a
+                                         shorter run does not win back the re-layout); 2 = once, at
+                                         the first full pass after one; R >= 3 = that, then every R
+                                         full training passes.  Row ids in every call stay the
+                                         caller's */
 #define TSOM_OPT_BARRIER_TIMEOUT_MS 7 /* reduce-barrier deadline, ms (default 60000 =
                                          kDefaultBarrierTimeoutS, parallel.hpp:24); a rank that
                                          misses it fails the call with TSOM_ERR_TIMEOUT

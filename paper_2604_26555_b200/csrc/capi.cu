@@ -588,51 +588,58 @@ void reset_order(Engine* eng) {
 }
 
 // Re-lay the rows out now?  Needs the engine's own resident copy and the
-// BMU-ordered positions of a full pass over them (acc.sorted): the first time
-// once one is there, then every row_order (>= 2) full training passes.
+// BMU-ordered positions of a full pass over them (acc.sorted).  row_order 1
+// (auto): once, at an epoch of a tsom_train_epochs call with at least
+// kOrderMinEpochs epochs still to run — the re-layout costs about one to two
+// epochs' time and each later epoch saves ~5 %, so a shorter run would lose
+// (scripts/ab_relayout.sh, scripts/ab_relayout_large.py); 2: once, at the
+// first full pass that finds one; R >= 3: that, then every R full passes.
+constexpr uint32_t kOrderMinEpochs = 20;
 bool order_due(const Engine* eng) {
     if (!eng->row_order || eng->streamed || !eng->x.owned || !eng->x.p || !eng->sorted_full ||
         eng->n_rows < std::max<uint64_t>(2, eng->row_order_min))
         return false;
+    if (eng->row_order == 1) return !eng->ordered && eng->epochs_left >= kOrderMinEpochs;
     if (!eng->ordered) return true;
-    return eng->row_order >= 2 && eng->passes_since_order >= eng->row_order;
+    return eng->row_order >= 3 && eng->passes_since_order >= eng->row_order;
 }
 
 // The resident rows re-laid out (packed: the gather then reads runs of rows in
 // one copy) in the BMU order of the last full pass; perm / pinv composed with
-// the previous order.  Costs one read + write of the rows; the split tiles are
-// rebuilt from the new layout by the pass that follows.
+// the previous order.  No new block for the rows: the permuted rows go to the
+// split tiles' buffer (rebuilt from the new layout by the pass that follows
+// anyway) and are copied back into the rows' own buffer — a pool allocation
+// of a second copy costs tens of milliseconds once the pool has to map new
+// memory, more than the re-layout saves in a run.  ~2.3 ms at 1e7 rows.
 void order_rows(Engine* eng) {
     tsom::NvtxRange nv("tsom.order_rows");
     const uint64_t n = eng->n_rows;
-    // stream-ordered: the new blocks and the frees of the old ones follow the
-    // engine stream (no device synchronisation in the middle of an epoch loop)
-    DevBuf nx, np;
-    if (nx.ensure_on(n * eng->D * sizeof(float) + tsom::kRowSlack, eng->stream) != cudaSuccess ||
+    const size_t packed = n * eng->D * sizeof(float);
+    DevBuf np;
+    if (eng->xsplit.bytes < packed || packed > eng->x.bytes ||
         np.ensure_on(n * sizeof(uint32_t), eng->stream) != cudaSuccess ||
         (!eng->ordered &&
          eng->pinv.ensure_on(n * sizeof(uint32_t), eng->stream) != cudaSuccess)) {
-        // no room for a second copy of the rows: an optimisation, not a
-        // failure — the rows keep their layout and no re-layout is tried again
+        // no split tiles to borrow (SIMT kernel) or no room for the id maps:
+        // an optimisation, not a failure — the rows keep their layout
         cudaGetLastError();
-        nx.release_on(eng->stream);
         np.release_on(eng->stream);
         if (!eng->ordered) eng->pinv.release_on(eng->stream);
         eng->row_order = 0;
         eng->sorted_full = false;
         return;
     }
-    tsom::launch_permute_rows(eng->x.as<float>(), eng->ldx, eng->acc.sorted, n, eng->D,
-                              nx.as<float>(), eng->ordered ? eng->perm.as<uint32_t>() : nullptr,
+    float* tmp = eng->xsplit.as<float>();
+    tsom::launch_permute_rows(eng->x.as<float>(), eng->ldx, eng->acc.sorted, n, eng->D, tmp,
+                              eng->ordered ? eng->perm.as<uint32_t>() : nullptr,
                               np.as<uint32_t>(), eng->stream);
     CU(cudaGetLastError());
-    std::swap(eng->x, nx);
+    CU(cudaMemcpyAsync(eng->x.p, tmp, packed, cudaMemcpyDeviceToDevice, eng->stream));
     std::swap(eng->perm, np);
-    nx.release_on(eng->stream);
     np.release_on(eng->stream);
     tsom::launch_invert_perm(eng->perm.as<uint32_t>(), n, eng->pinv.as<uint32_t>(), eng->stream);
     CU(cudaGetLastError());
-    eng->ldx = eng->D;
+    eng->ldx = eng->D;  // (the buffer keeps its size; the tail past the packed rows is slack)
     eng->x_slack = true;
     eng->xsplit_valid = false;
     eng->img_valid = false;
@@ -1204,7 +1211,7 @@ int tsom_set_option(tsom_engine* eng, int key, int64_t value) {
                 break;
             case TSOM_OPT_ROW_ORDER:
                 REQUIRE(value >= 0 && value <= (1 << 30), TSOM_ERR_INVALID,
-                        "option: row order 0, 1 or a re-layout period >= 2");
+                        "option: row order 0, 1 (auto), 2 (once) or a re-layout period >= 3");
                 eng->row_order = (uint32_t)value;
                 break;
             case TSOM_OPT_STAGING_THREADS:
@@ -2138,12 +2145,14 @@ int tsom_train_epochs(tsom_engine* eng, uint32_t n_epochs, const double* eta,
             ~SlotReset() {
                 e->k1_slot = -1;
                 e->defer_hstat = false;
+                e->epochs_left = 0;
             }
         } reset{eng};
         for (uint32_t t = 0; t < n_epochs; ++t) {
             eng->k1_slot = (int)t;
             eng->k1_timed = false;
             eng->defer_hstat = t + 1 < n_epochs;
+            eng->epochs_left = n_epochs - t;
             train_epoch_enqueue(eng, eta[t], sigma[t], momentum, flags, dead, t);
             tsom::launch_epoch_guard(eng->status.as<int>(), t, dead, eng->stream);
             CU(cudaGetLastError());

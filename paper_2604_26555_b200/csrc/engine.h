@@ -249,7 +249,8 @@ struct Engine {
     // TSOM_OPT_ROW_ORDER (k_order.cu): the resident rows re-laid out in the BMU
     // order of an earlier full pass — position q holds caller row perm[q],
     // pinv is the inverse; every call still takes and returns caller row ids
-    uint32_t row_order = 1;     // 0 off, 1 once, R >= 2 also every R full passes
+    uint32_t row_order = 1;     // 0 off, 1 auto (long multi-epoch calls), 2 once, R >= 3 periodic
+    uint32_t epochs_left = 0;   // tsom_train_epochs: epochs of the call from this one on
     uint64_t row_order_min = 1u << 18;  // fewer rows: not worth a re-layout
     bool ordered = false;
     DevBuf perm, pinv, idmap;   // idmap: a selection mapped to positions

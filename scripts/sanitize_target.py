@@ -48,6 +48,7 @@ for kernel in (3, 2, 1):
 # BMU-ordered rows (re-layout forced at this size), then selections through
 # the mapping; the split image + gather4 K1 for a selection
 e = tsom.Engine(P, D)
+e.set_option(_lib.TSOM_OPT_ROW_ORDER, 2)
 e.set_option(93, 0)
 e.bind(x)
 e.set_codebook(w)

@@ -578,7 +578,8 @@ def test_exact_training_with_bmu_ordered_shards(pkg, oracle_port, world):
     for r, (a, b) in enumerate(sl):
         e = pkg.Engine(p, 50)
         e.set_option(_lib.TSOM_OPT_DETERMINISTIC, 1)
-        e.set_option(93, 0)  # re-lay out even these shards
+        e.set_option(_lib.TSOM_OPT_ROW_ORDER, 2)  # once, at the second full pass
+        e.set_option(93, 0)  # even for these shards
         e.bind(x[a:b])
         configure(e)
         e.join_group(g, r)

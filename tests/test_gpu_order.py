@@ -30,7 +30,7 @@ def rel_maxnorm(a, b):
     return float(np.max(np.abs(np.asarray(a, np.float64) - b)) / max(np.max(np.abs(b)), 1e-300))
 
 
-def make_pair(pkg, x, w, dist, order=1, exact=False, kernel=0):
+def make_pair(pkg, x, w, dist, order=2, exact=False, kernel=0):
     from paper_2604_26555_b200 import _lib
     es = []
     for ro in (0, order):
@@ -119,17 +119,29 @@ def test_exact_mode_bit_identical(pkg, data, oracle_port):
         b.close()
 
 
-@pytest.mark.parametrize("order", [1, 2])
+@pytest.mark.parametrize("order", [1, 2, 3])
 def test_training_runs_match(pkg, data, order):
+    """1 = auto (re-laid out in a call with >= 20 epochs left: here at the
+    second of 24), 2 = once, 3 = every 3 full passes."""
     from paper_2604_26555_b200.hostref import resolved_sigma0, schedule_value
     x, w, dist = data
     s0 = resolved_sigma0("hex", 32, 32)
-    etas = [schedule_value(0.5, "linear", t, 10, 1e-4) for t in range(10)]
-    sigmas = [schedule_value(s0, "linear", t, 10, 0.3) for t in range(10)]
+    etas = [schedule_value(0.5, "linear", t % 12, 12, 1e-4) for t in range(24)]
+    sigmas = [schedule_value(s0, "linear", t % 12, 12, 0.3) for t in range(24)]
     a, b = make_pair(pkg, x, w, dist, order=order)
     try:
         a.train_epochs(etas, sigmas)
         b.train_epochs(etas, sigmas)
+        if order == 1:
+            from paper_2604_26555_b200 import _lib
+            import ctypes as C
+            L = _lib.load()
+            L.tsom_debug_read.argtypes = [C.c_void_p, C.c_int, C.c_void_p, C.c_uint64]
+            L.tsom_debug_read.restype = C.c_int64
+            perm = np.empty(len(x), np.uint32)
+            assert L.tsom_debug_read(b.h, 11, perm.ctypes.data, perm.nbytes) == perm.nbytes, \
+                "auto mode did not re-lay out in a 24-epoch call"
+            assert not np.array_equal(perm, np.arange(len(x), dtype=np.uint32))
         assert rel_maxnorm(b.get_codebook(), a.get_codebook()) <= 1e-6
         assert np.array_equal(a.bmu_bound(None)[0], b.bmu_bound(None)[0])
     finally:
