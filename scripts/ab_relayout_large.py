@@ -1,4 +1,4 @@
-"""Diagnostics: 10-epoch runs at 1e8+ rows with (row order 1) and without (0)
+"""Diagnostics: 10-epoch runs at 1e8+ rows with (row order 2) and without (0)
 the one BMU-order re-layout — the c3 shape (MST refreshed on the reference
 schedule, 1e8 device-generated rows) and the c5 resident shape (32x32 hex,
 1.25e8 rows) — CUDA events around each whole run, alternating."""
@@ -43,6 +43,6 @@ def run(kind, n, ro):
 
 
 for kind, n in (("mst", 100_000_000), ("hex", 125_000_000)):
-    for ro in (0, 1, 0, 1):
+    for ro in (0, 2, 0, 2):
         print(f"{kind} n={n} row_order={ro}: ms/epoch {[round(v, 2) for v in run(kind, n, ro)]}",
               flush=True)
