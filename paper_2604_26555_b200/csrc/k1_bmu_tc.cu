@@ -1086,7 +1086,10 @@ __global__ void __launch_bounds__(EpiCfg<kKind>::kThreads, 1)
 
 // diagnostics only (option 99): bit0 skips the epilogue math, bit1 the MMAs,
 // bit2 the A-tile loads, so the stages can be timed in isolation; bit5 traces
-// CTA 0; bit6 enables the cluster multicast of A tiles
+// CTA 0; bit6 multicasts A tiles over clusters of all group CTAs; bit7 dumps
+// every raw main-pass value; bit8 turns the chunk skip off; bit9 counts the
+// pass-2 chunks run; bit10 unicasts the gather4 path; bit12 turns the
+// default cluster-of-2 multicast off
 uint32_t g_k1_debug = 0;
 
 int k1_set_dump(float* d_buf) {
