@@ -188,3 +188,40 @@ def test_rebind_drops_order(pkg, data, oracle_port):
         assert np.array_equal(bb, oracle_port.find_bmus(y, w)[0])
     finally:
         b.close()
+
+
+def test_row_order_option_validation(pkg):
+    from paper_2604_26555_b200 import _lib
+    e = pkg.Engine(16, 4)
+    try:
+        for v in (0, 1, 2, 3, 100):
+            e.set_option(_lib.TSOM_OPT_ROW_ORDER, v)
+        with pytest.raises(ValueError):
+            e.set_option(_lib.TSOM_OPT_ROW_ORDER, -1)
+    finally:
+        e.close()
+
+
+def test_short_runs_keep_the_bind_order(pkg, data):
+    """Auto mode (the default) re-lays out only in a tsom_train_epochs call
+    with >= 20 epochs left: a 10-epoch call and single-epoch calls leave the
+    rows in bind order."""
+    import ctypes as C
+    from paper_2604_26555_b200 import _lib
+    x, w, dist = data
+    e = pkg.Engine(w.shape[0], w.shape[1])
+    try:
+        e.set_option(93, 0)
+        e.bind(x)
+        e.set_codebook(w)
+        e.set_topology_distance(dist)
+        e.train_epochs([0.5] * 10, [4.0] * 10)
+        for _ in range(3):
+            e.train_epoch(0.3, 3.0)
+        L = _lib.load()
+        L.tsom_debug_read.argtypes = [C.c_void_p, C.c_int, C.c_void_p, C.c_uint64]
+        L.tsom_debug_read.restype = C.c_int64
+        buf = np.empty(len(x), np.uint32)
+        assert L.tsom_debug_read(e.h, 11, buf.ctypes.data, buf.nbytes) == 0  # no permutation
+    finally:
+        e.close()
