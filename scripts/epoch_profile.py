@@ -27,6 +27,9 @@ cycles = int(sys.argv[2]) if len(sys.argv) > 2 else 1
 P, D, seed, E = 1024, 50, 2606, 10
 x = _lib.synth_gmm_host(n, D, seed)
 e = tsom.Engine(P, D)
+# the bench's steady state: rows re-laid out in BMU order (its 50-epoch timed
+# call does it in auto mode; these per-epoch calls ask for it explicitly)
+e.set_option(_lib.TSOM_OPT_ROW_ORDER, 2)
 e.bind(x)
 e.set_codebook(init_sample_draw(x, P, seed))
 e.set_topology_distance(lattice_dist("hex", 32, 32))
