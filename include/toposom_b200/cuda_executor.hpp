@@ -86,6 +86,11 @@ struct CudaOptions {
     // exact sums (TSOM_OPT_DETERMINISTIC): results bit-identical for any number
     // of engines, like the reference's for any worker count (parallel.hpp:17-21)
     bool exact = false;
+    // TSOM_OPT_ROW_ORDER for the engines (-1: the engine's auto mode, which
+    // re-lays the rows out only in device calls of >= 20 epochs; train_cuda
+    // and train_device ask for 2 (once) when config.n_iters >= 20, since the
+    // reference loop calls the executor one epoch at a time)
+    int row_order = -1;
 };
 
 /// G engines joined by an in-process rank group (tsom_group_*): each owns
@@ -116,6 +121,7 @@ public:
             e.check(tsom_set_option(e.h, TSOM_OPT_BARRIER_TIMEOUT_MS,
                                     std::max<std::int64_t>(1, std::llround(opts.barrier_timeout_s * 1e3))));
             if (opts.exact) e.check(tsom_set_option(e.h, TSOM_OPT_DETERMINISTIC, 1));
+            if (opts.row_order >= 0) e.check(tsom_set_option(e.h, TSOM_OPT_ROW_ORDER, opts.row_order));
             if (group_) e.check(tsom_group_join(e.h, group_, static_cast<int>(g)));
         }
         const std::uint32_t flags = opts.streamed ? TSOM_BIND_STREAMED : TSOM_BIND_COPY;
@@ -278,6 +284,7 @@ inline std::pair<toposom::SomModel, toposom::RunLog> train_cuda(
     CudaOptions opts = {}, const toposom::TrainOptions& options = {}) {
     if (sampler.kind() != toposom::SamplingKind::adaptive) opts.distances = Distances::never;
     if (data.rows() < 1) throw std::invalid_argument("train: empty training data");
+    if (opts.row_order < 0 && config.n_iters >= 20) opts.row_order = 2;  // a long run
     CudaExecutor executor(data, config.nodes(), opts);
     return toposom::train_with_executor(config, data, sampler, executor, options);
 }
@@ -317,6 +324,7 @@ inline std::pair<toposom::SomModel, toposom::RunLog> train_device(
     model.prev_update = DataMatrix(config.nodes(), data.cols());
     model.topology_state = toposom::build_topology(config.topology);
     opts.distances = Distances::never;
+    if (opts.row_order < 0 && config.n_iters >= 20) opts.row_order = 2;  // a long run
     EngineSet es(data, config.nodes(), opts);  // engines + their rows (resident or streamed)
     tsom_engine* h = es.handle(0);
     auto check = [h](int st) { throw_status(st, tsom_last_error(h)); };
