@@ -17,11 +17,16 @@
 #include <cuda_runtime.h>
 #include <math_constants.h>
 
+#include <cooperative_groups.h>
+
+#include <algorithm>
 #include <cstdint>
 
 #include "engine.h"
 
 namespace tsom {
+
+namespace cg = cooperative_groups;
 
 // norms[i] = sum_k w_ik^2 (sequential, no FMA), topology.hpp:85-91
 __global__ void k_gram_norms(const float* __restrict__ w, uint32_t P, uint32_t D,
@@ -170,6 +175,113 @@ __global__ void __launch_bounds__(1024) k_mst_boruvka(const double* __restrict__
     }
 }
 
+// The same Boruvka over the whole GPU: one cooperative launch, the phases of
+// a round separated by grid-wide barriers — (1) a warp per vertex finds its
+// lightest edge leaving its component, (2) a warp per component root the
+// lightest over its members, (3) a thread per root records that edge (it is
+// in the MST: the unique minimum across the cut under the total order) and
+// hooks the component onto the other end's (a mutual pair keeps the smaller
+// root), (4) every vertex follows the hooks to its new root.  Each round at
+// least halves the components; a round with no edge found ends the loop.
+// scratch: bw/ba/bb [2P] (vertex minima, then component minima), parent [P],
+// cnt [2] (edges found per round, alternating), comp [P].
+__device__ __forceinline__ void warp_edge_min(double& w, uint32_t& a, uint32_t& b) {
+#pragma unroll
+    for (int o = 16; o; o >>= 1) {
+        const double ow = __shfl_xor_sync(0xffffffffu, w, o);
+        const uint32_t oa = __shfl_xor_sync(0xffffffffu, a, o);
+        const uint32_t ob = __shfl_xor_sync(0xffffffffu, b, o);
+        if (edge_less(ow, oa, ob, w, a, b)) {
+            w = ow;
+            a = oa;
+            b = ob;
+        }
+    }
+}
+
+__global__ void __launch_bounds__(256) k_mst_grid(const double* __restrict__ d2, uint32_t P,
+                                                  uint32_t* __restrict__ comp,
+                                                  double* __restrict__ bw, uint32_t* __restrict__ ba,
+                                                  uint32_t* __restrict__ bb,
+                                                  uint32_t* __restrict__ parent,
+                                                  uint32_t* __restrict__ cnt,
+                                                  uint8_t* __restrict__ keep) {
+    cg::grid_group grid = cg::this_grid();
+    const uint32_t tid = blockIdx.x * blockDim.x + threadIdx.x, nth = gridDim.x * blockDim.x;
+    const uint32_t lane = threadIdx.x & 31, gw = tid >> 5, nw = nth >> 5;
+    for (uint32_t i = tid; i < P; i += nth) comp[i] = i;
+    if (tid == 0) {
+        cnt[0] = 0;
+        cnt[1] = 0;
+    }
+    grid.sync();
+    for (uint32_t round = 0;; ++round) {
+        for (uint32_t i = gw; i < P; i += nw) {  // (1)
+            const uint32_t ci = comp[i];
+            double w = CUDART_INF;
+            uint32_t a = 0xFFFFFFFFu, b = 0xFFFFFFFFu;
+            for (uint32_t j = lane; j < P; j += 32) {
+                if (comp[j] == ci) continue;
+                const double wv = d2[(size_t)i * P + j];
+                const uint32_t aa = i < j ? i : j, bb2 = i < j ? j : i;
+                if (edge_less(wv, aa, bb2, w, a, b)) {
+                    w = wv;
+                    a = aa;
+                    b = bb2;
+                }
+            }
+            warp_edge_min(w, a, b);
+            if (lane == 0) {
+                bw[i] = w;
+                ba[i] = a;
+                bb[i] = b;
+            }
+        }
+        grid.sync();
+        for (uint32_t c = gw; c < P; c += nw) {  // (2)
+            if (comp[c] != c) continue;  // (warp-uniform)
+            double w = CUDART_INF;
+            uint32_t a = 0xFFFFFFFFu, b = 0xFFFFFFFFu;
+            for (uint32_t i = lane; i < P; i += 32)
+                if (comp[i] == c && edge_less(bw[i], ba[i], bb[i], w, a, b)) {
+                    w = bw[i];
+                    a = ba[i];
+                    b = bb[i];
+                }
+            warp_edge_min(w, a, b);
+            if (lane == 0) {
+                bw[P + c] = w;
+                ba[P + c] = a;
+                bb[P + c] = b;
+            }
+        }
+        grid.sync();
+        const uint32_t cur = round & 1u;
+        for (uint32_t c = tid; c < P; c += nth) {  // (3)
+            if (comp[c] != c) continue;
+            const uint32_t a = ba[P + c], b = bb[P + c];
+            if (a == 0xFFFFFFFFu) {
+                parent[c] = c;
+                continue;
+            }
+            keep[(size_t)a * P + b] = 1;
+            const uint32_t t = comp[a] == c ? comp[b] : comp[a];
+            const bool mutual = ba[P + t] == a && bb[P + t] == b;
+            parent[c] = (mutual && c < t) ? c : t;
+            atomicAdd(&cnt[cur], 1u);
+        }
+        grid.sync();
+        if (*reinterpret_cast<volatile uint32_t*>(&cnt[cur]) == 0) break;  // one component
+        for (uint32_t i = tid; i < P; i += nth) {  // (4)
+            uint32_t r = comp[i];
+            while (parent[r] != r) r = parent[r];
+            comp[i] = r;
+        }
+        if (tid == 0) cnt[cur ^ 1u] = 0;
+        grid.sync();
+    }
+}
+
 // ---------------------------------------------------------------------------
 // RNG: thread per candidate pair (a < b), witnesses r scanned with early exit.
 // Emits a P x P byte mask; compaction in (a, b) order keeps the reference's
@@ -199,50 +311,76 @@ __global__ void __launch_bounds__(256) k_rng_mask(const double* __restrict__ d2,
     }
 }
 
-// compaction of the keep mask into sorted (a, b) pairs: one thread per row a
-// counts, one CTA scans, rows write their edges in order.
+// compaction of the keep mask into sorted (a, b) pairs: a warp per row counts
+// its edges (ballots over 32 columns at a time), one CTA scans the counts into
+// row offsets, and a warp per row writes its edges in column order
 __global__ void k_rng_rowcount(const uint8_t* __restrict__ keep, uint32_t P,
                                uint32_t* __restrict__ rowcnt) {
-    const uint32_t a = blockIdx.x * blockDim.x + threadIdx.x;
-    if (a >= P) return;
-    uint32_t c = 0;
-    for (uint32_t b = a + 1; b < P; ++b) c += keep[(size_t)a * P + b];
-    rowcnt[a] = c;
+    const uint32_t lane = threadIdx.x & 31;
+    const uint32_t nw = (gridDim.x * blockDim.x) >> 5;
+    for (uint32_t a = (blockIdx.x * blockDim.x + threadIdx.x) >> 5; a < P; a += nw) {
+        uint32_t c = 0;
+        for (uint32_t b0 = 0; b0 < P; b0 += 32) {
+            const uint32_t b = b0 + lane;
+            c += __popc(__ballot_sync(0xffffffffu, b < P && b > a && keep[(size_t)a * P + b]));
+        }
+        if (lane == 0) rowcnt[a] = c;
+    }
+}
+
+__global__ void __launch_bounds__(1024) k_rng_scan(uint32_t P, const uint32_t* __restrict__ rowcnt,
+                                                   uint32_t* __restrict__ rowoff,
+                                                   uint32_t* __restrict__ ne) {
+    __shared__ uint32_t sc[1024];
+    __shared__ uint32_t carry;
+    if (threadIdx.x == 0) carry = 0;
+    __syncthreads();
+    for (uint32_t base = 0; base < P; base += 1024) {
+        const uint32_t a = base + threadIdx.x;
+        const uint32_t v = a < P ? rowcnt[a] : 0u;
+        sc[threadIdx.x] = v;
+        __syncthreads();
+        for (uint32_t off = 1; off < 1024; off <<= 1) {
+            const uint32_t add = threadIdx.x >= off ? sc[threadIdx.x - off] : 0u;
+            __syncthreads();
+            sc[threadIdx.x] += add;
+            __syncthreads();
+        }
+        if (a < P) rowoff[a] = carry + sc[threadIdx.x] - v;
+        __syncthreads();
+        if (threadIdx.x == 1023) carry += sc[1023];
+        __syncthreads();
+    }
+    if (threadIdx.x == 0) *ne = carry;
 }
 
 __global__ void k_rng_emit(const uint8_t* __restrict__ keep, uint32_t P,
-                           const uint32_t* __restrict__ rowcnt, uint32_t* __restrict__ edges,
-                           uint32_t* __restrict__ ne) {
-    // single CTA: exclusive scan of row counts, then each row writes its edges
-    if (threadIdx.x == 0) {
-        uint32_t run = 0;
-        for (uint32_t a = 0; a < P; ++a) run += rowcnt[a];
-        *ne = run;
-    }
-    for (uint32_t a = threadIdx.x; a < P; a += blockDim.x) {
-        uint32_t off = 0;
-        for (uint32_t q = 0; q < a; ++q) off += rowcnt[q];
-        for (uint32_t b = a + 1; b < P; ++b)
-            if (keep[(size_t)a * P + b]) {
-                edges[2 * off] = a;
-                edges[2 * off + 1] = b;
-                ++off;
+                           const uint32_t* __restrict__ rowoff, uint32_t* __restrict__ edges) {
+    const uint32_t lane = threadIdx.x & 31;
+    const uint32_t nw = (gridDim.x * blockDim.x) >> 5;
+    for (uint32_t a = (blockIdx.x * blockDim.x + threadIdx.x) >> 5; a < P; a += nw) {
+        uint32_t o = rowoff[a];
+        for (uint32_t b0 = 0; b0 < P; b0 += 32) {
+            const uint32_t b = b0 + lane;
+            const bool k = b < P && b > a && keep[(size_t)a * P + b];
+            const uint32_t m = __ballot_sync(0xffffffffu, k);
+            if (k) {
+                const uint32_t q = o + __popc(m & ((1u << lane) - 1u));
+                edges[2 * q] = a;
+                edges[2 * q + 1] = b;
             }
+            o += __popc(m);
+        }
     }
 }
 
-// ---------------------------------------------------------------------------
-// all-pairs hop counts: one CTA per BFS source, CSR adjacency, frontier in smem
-// ---------------------------------------------------------------------------
-
-__global__ void k_build_csr(const uint32_t* __restrict__ edges, const uint32_t* __restrict__ ne,
-                            uint32_t P, uint32_t* __restrict__ deg, uint32_t* __restrict__ adj,
-                            uint32_t* __restrict__ status) {
-    // single CTA; P and edge counts are O(1e4)
+// degrees (atomic counts), then offsets by one CTA's scan, then the fill with
+// an atomic cursor per node: the adjacency order within a node is arbitrary,
+// which BFS hop counts do not depend on
+__global__ void k_csr_degrees(const uint32_t* __restrict__ edges, const uint32_t* __restrict__ ne,
+                              uint32_t P, uint32_t* __restrict__ deg, uint32_t* __restrict__ status) {
     const uint32_t n = *ne;
-    for (uint32_t i = threadIdx.x; i <= P; i += blockDim.x) deg[i] = 0;
-    __syncthreads();
-    for (uint32_t e = threadIdx.x; e < n; e += blockDim.x) {
+    for (uint32_t e = blockIdx.x * blockDim.x + threadIdx.x; e < n; e += gridDim.x * blockDim.x) {
         const uint32_t a = edges[2 * e], b = edges[2 * e + 1];
         if (a >= P || b >= P) {
             atomicOr(status, 2u);  // edge index out of range
@@ -251,18 +389,43 @@ __global__ void k_build_csr(const uint32_t* __restrict__ edges, const uint32_t* 
         atomicAdd(&deg[a + 1], 1u);
         atomicAdd(&deg[b + 1], 1u);
     }
+}
+
+__global__ void __launch_bounds__(1024) k_csr_scan(uint32_t P, uint32_t* __restrict__ deg,
+                                                   uint32_t* __restrict__ cursor) {
+    __shared__ uint32_t sc[1024];
+    __shared__ uint32_t carry;
+    if (threadIdx.x == 0) carry = 0;
     __syncthreads();
-    if (threadIdx.x == 0)
-        for (uint32_t i = 0; i < P; ++i) deg[i + 1] += deg[i];
-    __syncthreads();
-    // fill: sequential per node for a deterministic adjacency order
-    for (uint32_t v = threadIdx.x; v < P; v += blockDim.x) {
-        uint32_t f = deg[v];
-        for (uint32_t e = 0; e < n; ++e) {
-            const uint32_t a = edges[2 * e], b = edges[2 * e + 1];
-            if (a == v) adj[f++] = b;
-            else if (b == v) adj[f++] = a;
+    for (uint32_t base = 0; base < P; base += 1024) {
+        const uint32_t i = base + threadIdx.x;
+        const uint32_t v = i < P ? deg[i + 1] : 0u;
+        sc[threadIdx.x] = v;
+        __syncthreads();
+        for (uint32_t off = 1; off < 1024; off <<= 1) {
+            const uint32_t add = threadIdx.x >= off ? sc[threadIdx.x - off] : 0u;
+            __syncthreads();
+            sc[threadIdx.x] += add;
+            __syncthreads();
         }
+        if (i < P) {
+            deg[i + 1] = carry + sc[threadIdx.x];
+            cursor[i] = carry + sc[threadIdx.x] - v;
+        }
+        __syncthreads();
+        if (threadIdx.x == 1023) carry += sc[1023];
+        __syncthreads();
+    }
+}
+
+__global__ void k_csr_fill(const uint32_t* __restrict__ edges, const uint32_t* __restrict__ ne,
+                           uint32_t P, uint32_t* __restrict__ cursor, uint32_t* __restrict__ adj) {
+    const uint32_t n = *ne;
+    for (uint32_t e = blockIdx.x * blockDim.x + threadIdx.x; e < n; e += gridDim.x * blockDim.x) {
+        const uint32_t a = edges[2 * e], b = edges[2 * e + 1];
+        if (a >= P || b >= P) continue;
+        adj[atomicAdd(&cursor[a], 1u)] = b;
+        adj[atomicAdd(&cursor[b], 1u)] = a;
     }
 }
 
@@ -332,16 +495,57 @@ int launch_refresh_topology(const float* w, uint32_t P, uint32_t D, int kind, To
     cudaMemsetAsync(s.status, 0, sizeof(uint32_t), st);
     if (kind == 2) {
         cudaMemsetAsync(s.keep, 0, (size_t)P * P, st);
-        if (P > 1)
-            TSOM_LAUNCH(k_mst_boruvka<<<1, 1024, 0, st>>>(s.d2, P, s.comp, s.bw, s.ba, s.bb,
-                                                          s.keep));
+        if (P > 1) {
+            // the grid-wide Boruvka (one cooperative launch); the one-CTA
+            // version if the cooperative launch is refused
+            // (scratch: parent = rowcnt, the round counters = deg[0..1], both
+            // rewritten by the compaction below)
+            static int blocks_per_sm = -1;
+            if (blocks_per_sm < 0 &&
+                cudaOccupancyMaxActiveBlocksPerMultiprocessor(&blocks_per_sm, k_mst_grid, 256, 0) !=
+                    cudaSuccess) {
+                cudaGetLastError();
+                blocks_per_sm = 0;
+            }
+            int dev = 0, sms = 0;
+            cudaGetDevice(&dev);
+            cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
+            const unsigned nb = (unsigned)std::min(std::max(blocks_per_sm, 0), 4) * (unsigned)sms;
+            cudaError_t e = cudaErrorInvalidConfiguration;
+            if (nb > 0) {
+                const double* d2 = s.d2;
+                uint32_t* comp = s.comp;
+                double* bw = s.bw;
+                uint32_t* ba = s.ba;
+                uint32_t* bb = s.bb;
+                uint32_t* parent = s.rowcnt;
+                uint32_t* cnt = s.deg;
+                uint8_t* keep = s.keep;
+                void* args[] = {(void*)&d2, (void*)&P, (void*)&comp, (void*)&bw, (void*)&ba,
+                                (void*)&bb, (void*)&parent, (void*)&cnt, (void*)&keep};
+                ++g_launches;
+                e = cudaLaunchCooperativeKernel((const void*)k_mst_grid, dim3(nb), dim3(256), args,
+                                                0, st);
+            }
+            if (e != cudaSuccess) {
+                cudaGetLastError();
+                TSOM_LAUNCH(k_mst_boruvka<<<1, 1024, 0, st>>>(s.d2, P, s.comp, s.bw, s.ba, s.bb,
+                                                              s.keep));
+            }
+        }
     } else {
         const dim3 rg((P + 255) / 256, P);
         TSOM_LAUNCH(k_rng_mask<<<rg, 256, 0, st>>>(s.d2, P, s.keep));
     }
-    TSOM_LAUNCH(k_rng_rowcount<<<(P + 255) / 256, 256, 0, st>>>(s.keep, P, s.rowcnt));
-    TSOM_LAUNCH(k_rng_emit<<<1, 1024, 0, st>>>(s.keep, P, s.rowcnt, s.edges, s.ne));
-    TSOM_LAUNCH(k_build_csr<<<1, 1024, 0, st>>>(s.edges, s.ne, P, s.deg, s.adj, s.status));
+    const unsigned wb = (P + 7) / 8;  // a warp per row, 8 warps per block
+    TSOM_LAUNCH(k_rng_rowcount<<<wb, 256, 0, st>>>(s.keep, P, s.rowcnt));
+    TSOM_LAUNCH(k_rng_scan<<<1, 1024, 0, st>>>(P, s.rowcnt, s.comp, s.ne));  // (comp: row offsets)
+    TSOM_LAUNCH(k_rng_emit<<<wb, 256, 0, st>>>(s.keep, P, s.comp, s.edges));
+    cudaMemsetAsync(s.deg, 0, (size_t)(P + 1) * sizeof(uint32_t), st);
+    TSOM_LAUNCH(k_csr_degrees<<<(P + 255) / 256 * 4, 256, 0, st>>>(s.edges, s.ne, P, s.deg,
+                                                                   s.status));
+    TSOM_LAUNCH(k_csr_scan<<<1, 1024, 0, st>>>(P, s.deg, s.rowcnt));  // (rowcnt: fill cursors)
+    TSOM_LAUNCH(k_csr_fill<<<(P + 255) / 256 * 4, 256, 0, st>>>(s.edges, s.ne, P, s.rowcnt, s.adj));
     const size_t bsm = (size_t)((P + 1) & ~1u) * sizeof(uint16_t) + (size_t)(P + 31) / 32 * 4;
     if (bsm > 48 * 1024) cudaFuncSetAttribute(k_bfs_all, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)bsm);
     TSOM_LAUNCH(k_bfs_all<<<P, 256, bsm, st>>>(s.deg, s.adj, P, s.hops, s.hopd, s.status));
