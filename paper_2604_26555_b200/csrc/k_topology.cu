@@ -311,6 +311,79 @@ __global__ void __launch_bounds__(256) k_rng_mask(const double* __restrict__ d2,
     }
 }
 
+// RNG with nearest-first witnesses: every row a's other nodes sorted by d2
+// (one CTA per row, bitonic sort in shared memory), then a thread per pair
+// (a, b > a) scans a's list only while d_ar < d_ab — a node at least as far
+// from a as b cannot block the pair (max(d_ar, d_br) < d_ab needs d_ar <
+// d_ab) — and stops at the first witness.  Same predicate, same mask as
+// k_rng_mask (an OR over the same witnesses); far pairs meet a witness among
+// a's first few neighbours instead of after a scan in index order.
+__global__ void __launch_bounds__(1024) k_rng_sort_rows(const double* __restrict__ d2, uint32_t P,
+                                                        uint32_t P2, double* __restrict__ skey,
+                                                        uint16_t* __restrict__ sidx) {
+    extern __shared__ uint8_t rsm[];
+    double* key = reinterpret_cast<double*>(rsm);
+    uint16_t* idx = reinterpret_cast<uint16_t*>(key + P2);
+    const uint32_t a = blockIdx.x;
+    for (uint32_t i = threadIdx.x; i < P2; i += blockDim.x) {
+        key[i] = (i < P && i != a) ? d2[(size_t)a * P + i] : CUDART_INF;
+        idx[i] = (uint16_t)(i < P ? i : 0);
+    }
+    __syncthreads();
+    for (uint32_t k = 2; k <= P2; k <<= 1)
+        for (uint32_t j = k >> 1; j > 0; j >>= 1) {
+            for (uint32_t i = threadIdx.x; i < P2; i += blockDim.x) {
+                const uint32_t l = i ^ j;
+                if (l > i) {
+                    const bool up = (i & k) == 0;
+                    const bool gt = key[i] > key[l] || (key[i] == key[l] && idx[i] > idx[l]);
+                    if (gt == up) {
+                        const double tk = key[i];
+                        key[i] = key[l];
+                        key[l] = tk;
+                        const uint16_t ti = idx[i];
+                        idx[i] = idx[l];
+                        idx[l] = ti;
+                    }
+                }
+            }
+            __syncthreads();
+        }
+    for (uint32_t i = threadIdx.x; i + 1 < P; i += blockDim.x) {  // (the INF self entry is last)
+        skey[(size_t)a * P + i] = key[i];
+        sidx[(size_t)a * P + i] = idx[i];
+    }
+}
+
+__global__ void __launch_bounds__(256) k_rng_mask_sorted(const double* __restrict__ d2, uint32_t P,
+                                                         const double* __restrict__ skey,
+                                                         const uint16_t* __restrict__ sidx,
+                                                         uint8_t* __restrict__ keep) {
+    const uint32_t a = blockIdx.y;
+    if (a >= P) return;
+    const double* ka = skey + (size_t)a * P;
+    const uint16_t* ia = sidx + (size_t)a * P;
+    for (uint32_t b = blockIdx.x * blockDim.x + threadIdx.x; b < P; b += gridDim.x * blockDim.x) {
+        if (b <= a) {
+            keep[(size_t)a * P + b] = 0;
+            continue;
+        }
+        const double dab = d2[(size_t)a * P + b];
+        bool blocked = false;
+        for (uint32_t q = 0; q + 1 < P; ++q) {
+            const double dar = ka[q];
+            if (!(dar < dab)) break;  // every later r is at least as far from a
+            const uint32_t r = ia[q];
+            if (r == b) continue;
+            if (d2[(size_t)r * P + b] < dab) {  // == max(d_ar, d_br) < d_ab here
+                blocked = true;
+                break;
+            }
+        }
+        keep[(size_t)a * P + b] = blocked ? 0 : 1;
+    }
+}
+
 // compaction of the keep mask into sorted (a, b) pairs: a warp per row counts
 // its edges (ballots over 32 columns at a time), one CTA scans the counts into
 // row offsets, and a warp per row writes its edges in column order
@@ -535,7 +608,20 @@ int launch_refresh_topology(const float* w, uint32_t P, uint32_t D, int kind, To
         }
     } else {
         const dim3 rg((P + 255) / 256, P);
-        TSOM_LAUNCH(k_rng_mask<<<rg, 256, 0, st>>>(s.d2, P, s.keep));
+        uint32_t P2 = 1;
+        while (P2 < P) P2 <<= 1;
+        const size_t ssm = (size_t)P2 * (sizeof(double) + sizeof(uint16_t));
+        if (P >= 64 && P2 <= 16384 && ssm <= 200 * 1024) {
+            // (scratch: the sorted keys in hopd, the indices in hops — both
+            // rewritten by the BFS below)
+            if (ssm > 48 * 1024)
+                cudaFuncSetAttribute(k_rng_sort_rows, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                     (int)ssm);
+            TSOM_LAUNCH(k_rng_sort_rows<<<P, 1024, ssm, st>>>(s.d2, P, P2, s.hopd, s.hops));
+            TSOM_LAUNCH(k_rng_mask_sorted<<<rg, 256, 0, st>>>(s.d2, P, s.hopd, s.hops, s.keep));
+        } else {
+            TSOM_LAUNCH(k_rng_mask<<<rg, 256, 0, st>>>(s.d2, P, s.keep));
+        }
     }
     const unsigned wb = (P + 7) / 8;  // a warp per row, 8 warps per block
     TSOM_LAUNCH(k_rng_rowcount<<<wb, 256, 0, st>>>(s.keep, P, s.rowcnt));
