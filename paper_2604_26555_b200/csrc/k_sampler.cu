@@ -627,16 +627,41 @@ __global__ void k_bitmap_count(const uint32_t* __restrict__ bitmap, uint64_t wor
     }
 }
 
-__global__ void k_block_scan(uint32_t* __restrict__ bcount, uint64_t nb,
-                             unsigned long long* __restrict__ total) {
-    if (threadIdx.x != 0) return;
-    unsigned long long run = 0;
-    for (uint64_t b = 0; b < nb; ++b) {
-        const uint32_t c = bcount[b];
-        bcount[b] = (uint32_t)run;
-        run += c;
+// exclusive scan of the per-block counts in place, 1024 at a time (warp
+// scans, then a scan of the warp sums); *total = the sum
+__global__ void __launch_bounds__(1024) k_block_scan(uint32_t* __restrict__ bcount, uint64_t nb,
+                                                     unsigned long long* __restrict__ total) {
+    __shared__ uint32_t wsum[32];
+    __shared__ unsigned long long carry;
+    const uint32_t lane = threadIdx.x & 31, wid = threadIdx.x >> 5;
+    if (threadIdx.x == 0) carry = 0;
+    __syncthreads();
+    for (uint64_t base = 0; base < nb; base += 1024) {
+        const uint64_t b = base + threadIdx.x;
+        const uint32_t c = b < nb ? bcount[b] : 0u;
+        uint32_t inc = c;
+        for (int o = 1; o < 32; o <<= 1) {
+            const uint32_t v = __shfl_up_sync(0xffffffffu, inc, o);
+            if ((int)lane >= o) inc += v;
+        }
+        if (lane == 31) wsum[wid] = inc;
+        __syncthreads();
+        if (wid == 0) {
+            uint32_t v = wsum[lane];
+            for (int o = 1; o < 32; o <<= 1) {
+                const uint32_t u = __shfl_up_sync(0xffffffffu, v, o);
+                if ((int)lane >= o) v += u;
+            }
+            wsum[lane] = v;  // inclusive over the warps
+        }
+        __syncthreads();
+        const uint32_t before = (wid ? wsum[wid - 1] : 0u) + inc - c;
+        if (b < nb) bcount[b] = (uint32_t)(carry + before);
+        __syncthreads();
+        if (threadIdx.x == 0) carry += wsum[31];
+        __syncthreads();
     }
-    *total = run;
+    if (threadIdx.x == 0) *total = carry;
 }
 
 __global__ void k_bitmap_write(const uint32_t* __restrict__ bitmap, uint64_t words,
@@ -804,7 +829,7 @@ static void bitmap_to_list(SamplerState& s, uint64_t n, uint32_t* out, cudaStrea
     const uint64_t nb = (words + 1023) / 1024;
     TSOM_LAUNCH(k_bitmap_count<<<(unsigned)nb, 1024, 0, st>>>(s.bitmap.as<uint32_t>(), words,
                                                                s.bcount.as<uint32_t>()));
-    TSOM_LAUNCH(k_block_scan<<<1, 32, 0, st>>>(s.bcount.as<uint32_t>(), nb,
+    TSOM_LAUNCH(k_block_scan<<<1, 1024, 0, st>>>(s.bcount.as<uint32_t>(), nb,
                                                reinterpret_cast<unsigned long long*>(
                                                    s.misc.as<uint64_t>() + 3)));
     TSOM_LAUNCH(k_bitmap_write<<<(unsigned)nb, 1024, 0, st>>>(s.bitmap.as<uint32_t>(), words,
