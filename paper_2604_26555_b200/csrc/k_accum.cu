@@ -535,16 +535,13 @@ __global__ void __launch_bounds__(kTmaWarps * 32, 2) k_gather_tma(
                 // row j of the batch at bs + j rs (+ 8 when bit j of om is set)
                 const uint8_t* bs = buf + (size_t)s * 32 * slot + (coff[s] < 0 ? 0 : coff[s]);
                 const uint32_t rs = coff[s] < 0 ? slot : rowb;
-                const uint8_t* bm = bs + 8 * lane;
+                // lanes past the row's features re-read feature pair 0 (their
+                // sums are never stored): no per-row branch; row j's offset
+                // walks the pointer; omv holds the window bits of the rows still to add
+                const uint8_t* bm = bs + (okb ? 8 * lane : 0u);
                 const uint32_t om = offm[s];
-                uint32_t j = 0;
-                for (; j + 2 <= rows_m; j += 2) {
-                    float2 u = make_float2(0.0f, 0.0f), v = u;
-                    if (okb) {
-                        u = *reinterpret_cast<const float2*>(bm + j * rs + ((om >> j) & 1u) * 8);
-                        v = *reinterpret_cast<const float2*>(bm + (j + 1) * rs +
-                                                             ((om >> (j + 1)) & 1u) * 8);
-                    }
+                uint32_t omv = om;
+                auto add2 = [&](float2 u, float2 v) {
                     if (kExact) {
                         qa0 += __double2ll_rn((double)u.x * sx);
                         qa1 += __double2ll_rn((double)u.y * sx);
@@ -556,10 +553,24 @@ __global__ void __launch_bounds__(kTmaWarps * 32, 2) k_gather_tma(
                         c0 += (double)v.x;
                         c1 += (double)v.y;
                     }
+                };
+                uint32_t j = 0;
+                if (om == 0) {  // contiguous batch or aligned rows: one add per row
+                    for (; j + 2 <= rows_m; j += 2) {
+                        add2(*reinterpret_cast<const float2*>(bm),
+                             *reinterpret_cast<const float2*>(bm + rs));
+                        bm += 2 * rs;
+                    }
+                } else {
+                    for (; j + 2 <= rows_m; j += 2) {
+                        add2(*reinterpret_cast<const float2*>(bm + ((omv << 3) & 8u)),
+                             *reinterpret_cast<const float2*>(bm + rs + ((omv << 2) & 8u)));
+                        bm += 2 * rs;
+                        omv >>= 2;
+                    }
                 }
-                if (j < rows_m && okb) {
-                    const float2 u =
-                        *reinterpret_cast<const float2*>(bm + j * rs + ((om >> j) & 1u) * 8);
+                if (j < rows_m) {
+                    const float2 u = *reinterpret_cast<const float2*>(bm + ((omv << 3) & 8u));
                     if (kExact) {
                         qa0 += __double2ll_rn((double)u.x * sx);
                         qa1 += __double2ll_rn((double)u.y * sx);

@@ -15,17 +15,6 @@
 
 namespace tsom {
 
-// S_aug[b][k] = S_b[k] (k < d), S_aug[b][d] = c_b   (sums = [S | c | ...])
-__global__ void k_build_saug(const double* __restrict__ sums, const float* __restrict__ w,
-                             uint32_t P, uint32_t D, double* __restrict__ saug) {
-    const size_t e = blockIdx.x * (size_t)blockDim.x + threadIdx.x;
-    const uint32_t Dp = D + 1;
-    if (e >= (size_t)P * Dp) return;
-    const uint32_t b = (uint32_t)(e / Dp), k = (uint32_t)(e % Dp);
-    const double c = sums[(size_t)P * D + b];
-    saug[e] = k < D ? sums[(size_t)b * D + k] : c;
-}
-
 // H_j = sum_b infl[b][j] c_b: block = 32 nodes x 8 b-slices, fixed-order fold.
 // Two values per node:
 //   Hx[j] — in FP64, the denominator's exact value, for U's  - w_j H_j  term;
@@ -69,15 +58,15 @@ __global__ void __launch_bounds__(1024) k_smooth_den(const double* __restrict__ 
     }
 }
 
-// partial[z][j][k] = sum_{b in slice z} infl[b][j] * saug[b][k], k < d.
+// partial[z][j][k] = sum_{b in slice z} infl[b][j] * S_b[k], k < d (S = the
+// first P d entries of the sums buffer, read in place).
 // Block: 32 nodes j x 64 columns k x one of SM_SPLIT b-slices (fills the GPU).
 constexpr int SM_TJ = 32, SM_TB = 32, SM_KG = 8, SM_KC = SM_KG * 8, SM_SPLIT = 8;
 __global__ void __launch_bounds__(256) k_smooth_gemm(const double* __restrict__ infl,
-                                                     const double* __restrict__ saug, uint32_t P,
+                                                     const double* __restrict__ sums, uint32_t P,
                                                      uint32_t D, double* __restrict__ partial) {
     __shared__ double hs[SM_TB * SM_TJ];
     __shared__ double ss[SM_TB * SM_KC];
-    const uint32_t Dp = D + 1;
     const int tj = threadIdx.x % SM_TJ, kg = threadIdx.x / SM_TJ;
     const uint32_t j0 = blockIdx.x * SM_TJ, j = j0 + tj;
     const uint32_t k0 = blockIdx.y * SM_KC;
@@ -94,7 +83,7 @@ __global__ void __launch_bounds__(256) k_smooth_gemm(const double* __restrict__ 
         }
         for (int e = threadIdx.x; e < SM_TB * SM_KC; e += 256) {
             const uint32_t bb = b0 + e / SM_KC, kk = k0 + e % SM_KC;
-            ss[e] = (bb < bz1 && kk < D) ? saug[(size_t)bb * Dp + kk] : 0.0;
+            ss[e] = (bb < bz1 && kk < D) ? sums[(size_t)bb * D + kk] : 0.0;
         }
         __syncthreads();
 #pragma unroll 4
@@ -128,15 +117,12 @@ __global__ void k_smooth_finish(const double* __restrict__ partial, const float*
 void launch_smooth(const double* infl, const double* sums, const float* w, uint32_t P, uint32_t D,
                    double eta, double* U, double* H, double* scratch, cudaStream_t st,
                    int* status) {
-    // scratch: P*(d+1) (saug) + SM_SPLIT*P*d (slice partials) + P (Hx) doubles
-    double* saug = scratch;
+    // scratch: P*(d+1) (unused) + SM_SPLIT*P*d (slice partials) + P (Hx) doubles
     double* partial = scratch + (size_t)P * (D + 1);
     double* Hx = partial + (size_t)SM_SPLIT * P * D;
-    const size_t n = (size_t)P * (D + 1);
-    TSOM_LAUNCH(k_build_saug<<<(unsigned)((n + 255) / 256), 256, 0, st>>>(sums, w, P, D, saug));
     TSOM_LAUNCH(k_smooth_den<<<(P + 31) / 32, 32 * kDenSlices, 0, st>>>(infl, sums, P, D, H, Hx));
     dim3 grid((P + SM_TJ - 1) / SM_TJ, (D + SM_KC - 1) / SM_KC, SM_SPLIT);
-    TSOM_LAUNCH(k_smooth_gemm<<<grid, 256, 0, st>>>(infl, saug, P, D, partial));
+    TSOM_LAUNCH(k_smooth_gemm<<<grid, 256, 0, st>>>(infl, sums, P, D, partial));
     const size_t pd = (size_t)P * D;
     TSOM_LAUNCH(k_smooth_finish<<<(unsigned)((pd + 255) / 256), 256, 0, st>>>(partial, w, Hx, P,
                                                                             D, eta, U, status));
