@@ -462,39 +462,34 @@ __global__ void __launch_bounds__(kTmaWarps * 32, 2) k_gather_tma(
     double sx = 0.0, sd = 0.0;
     if (kExact) exact_scales(xmax2, w2max, &sx, &sd);
 
-    // copy window of this lane's row into its slot (offmask: rows whose window
-    // starts 8 bytes before them).  A batch of consecutive packed rows (rows
-    // kept in BMU order) is one bulk copy instead: rows at the
-    // row stride from byte `coff` of the buffer (returned; -1 = per-row slots).
-    auto issue = [&](uint64_t row, uint32_t nrows, int s, uint32_t& offmask) -> int {
+    // Batch copy: every run of consecutive packed rows (rows kept in BMU order,
+    // DESIGN.md §4, keep most of a node's rows in runs) is one bulk copy of
+    // its 16-byte-aligned window, issued by the run's first lane into that
+    // lane's slot; a run of k rows fits the k slots it starts (window <= 4dk
+    // + 16 <= k slot for k >= 2).  Padded or scattered rows are runs of one.
+    // roff = this lane's row's byte offset in buffer s; returns true when the
+    // batch is a single run (rows at the row stride from lane 0's offset).
+    auto issue = [&](uint64_t row, uint32_t nrows, int s, uint32_t& roff) -> bool {
         const bool mine = lane < nrows;
-        const uint64_t row0 = __shfl_sync(0xffffffffu, row, 0);
-        const bool cont = strideb == rowb && __all_sync(0xffffffffu, !mine || row == row0 + lane);
-        asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
-        if (cont) {
-            const uint64_t b0 = reinterpret_cast<uint64_t>(x) + row0 * strideb;
-            const uint64_t c0 = b0 & ~15ull;
-            const uint32_t len = (uint32_t)(((b0 + (uint64_t)nrows * rowb + 15) & ~15ull) - c0);
-            offmask = 0;
-            if (lane == 0) {
-                ptx::mbar_expect_tx(&bars[warp][s], len);
-                ptx::bulk_g2s(buf + (size_t)s * 32 * slot, reinterpret_cast<const void*>(c0), len,
-                              &bars[warp][s]);
-            }
-            __syncwarp();
-            return (int)(b0 & 15);
-        }
         const uint64_t a = reinterpret_cast<uint64_t>(x) + row * strideb;
-        const uint64_t a0 = a & ~15ull;
-        const uint32_t len = (uint32_t)(((a + rowb + 15) & ~15ull) - a0);
-        offmask = __ballot_sync(0xffffffffu, mine && (a & 15));
-        const uint32_t total = __reduce_add_sync(0xffffffffu, mine ? len : 0u);
+        const uint64_t prev = __shfl_up_sync(0xffffffffu, row, 1);
+        const bool lead = mine && !(lane > 0 && strideb == rowb && row == prev + 1);
+        const uint32_t leads = __ballot_sync(0xffffffffu, lead);
+        const uint32_t below = leads & (0xffffffffu >> (31 - lane));  // leaders <= lane
+        const uint32_t l = 31 - __clz(below);                          // this row's run leader
+        const uint32_t above = leads & ~(0xffffffffu >> (31 - lane));
+        const uint32_t k = (above ? (uint32_t)__ffs(above) - 1 : nrows) - lane;  // run rows (leaders)
+        const uint64_t c0 = a & ~15ull;
+        const uint32_t len = lead ? (uint32_t)(((a + (uint64_t)k * rowb + 15) & ~15ull) - c0) : 0u;
+        roff = l * slot + __shfl_sync(0xffffffffu, (uint32_t)(a & 15), l) + (lane - l) * rowb;
+        const uint32_t total = __reduce_add_sync(0xffffffffu, len);
+        asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
         if (lane == 0) ptx::mbar_expect_tx(&bars[warp][s], total);
         __syncwarp();
-        if (mine)
-            ptx::bulk_g2s(buf + ((size_t)s * 32 + lane) * slot, reinterpret_cast<const void*>(a0),
+        if (lead)
+            ptx::bulk_g2s(buf + ((size_t)s * 32 + lane) * slot, reinterpret_cast<const void*>(c0),
                           len, &bars[warp][s]);
-        return -1;
+        return leads == 1u;
     };
 
     for (uint32_t p = blockIdx.x * kTmaWarps + warp; p < npieces; p += gridDim.x * kTmaWarps) {
@@ -519,28 +514,23 @@ __global__ void __launch_bounds__(kTmaWarps * 32, 2) k_gather_tma(
         }
         double a0 = 0.0, a1 = 0.0, c0 = 0.0, c1 = 0.0, ds = 0.0;
         long long qa0 = 0, qa1 = 0, qc0 = 0, qc1 = 0, qds = 0;
-        uint32_t offm[2];
-        int coff[2];
-        coff[0] = issue(rowid[0], min(32u, r1 - r0), 0, offm[0]);
+        uint32_t roff[2];
+        bool one[2];
+        one[0] = issue(rowid[0], min(32u, r1 - r0), 0, roff[0]);
 #pragma unroll
         for (int m = 0; m < 8; ++m) {
             if (m < (int)nb) {
                 const uint32_t rows_m = min(32u, r1 - (r0 + 32 * m));
                 const int s = m & 1;
                 if (m + 1 < (int)nb)
-                    coff[s ^ 1] =
-                        issue(rowid[m + 1], min(32u, r1 - (r0 + 32 * (m + 1))), s ^ 1, offm[s ^ 1]);
+                    one[s ^ 1] =
+                        issue(rowid[m + 1], min(32u, r1 - (r0 + 32 * (m + 1))), s ^ 1, roff[s ^ 1]);
                 ptx::mbar_wait(&bars[warp][s], (phase >> s) & 1u);
                 phase ^= 1u << s;
-                // row j of the batch at bs + j rs (+ 8 when bit j of om is set)
-                const uint8_t* bs = buf + (size_t)s * 32 * slot + (coff[s] < 0 ? 0 : coff[s]);
-                const uint32_t rs = coff[s] < 0 ? slot : rowb;
+                const uint8_t* bs = buf + (size_t)s * 32 * slot;
                 // lanes past the row's features re-read feature pair 0 (their
-                // sums are never stored): no per-row branch; row j's offset
-                // walks the pointer; omv holds the window bits of the rows still to add
-                const uint8_t* bm = bs + (okb ? 8 * lane : 0u);
-                const uint32_t om = offm[s];
-                uint32_t omv = om;
+                // sums are never stored): no per-row branch
+                const uint8_t* bl = bs + (okb ? 8 * lane : 0u);
                 auto add2 = [&](float2 u, float2 v) {
                     if (kExact) {
                         qa0 += __double2ll_rn((double)u.x * sx);
@@ -555,22 +545,22 @@ __global__ void __launch_bounds__(kTmaWarps * 32, 2) k_gather_tma(
                     }
                 };
                 uint32_t j = 0;
-                if (om == 0) {  // contiguous batch or aligned rows: one add per row
+                if (one[s]) {  // one run: row j at lane 0's offset + j rowb
+                    const uint8_t* bm = bl + __shfl_sync(0xffffffffu, roff[s], 0);
                     for (; j + 2 <= rows_m; j += 2) {
                         add2(*reinterpret_cast<const float2*>(bm),
-                             *reinterpret_cast<const float2*>(bm + rs));
-                        bm += 2 * rs;
+                             *reinterpret_cast<const float2*>(bm + rowb));
+                        bm += 2 * rowb;
                     }
                 } else {
-                    for (; j + 2 <= rows_m; j += 2) {
-                        add2(*reinterpret_cast<const float2*>(bm + ((omv << 3) & 8u)),
-                             *reinterpret_cast<const float2*>(bm + rs + ((omv << 2) & 8u)));
-                        bm += 2 * rs;
-                        omv >>= 2;
-                    }
+                    for (; j + 2 <= rows_m; j += 2)
+                        add2(*reinterpret_cast<const float2*>(bl + __shfl_sync(0xffffffffu, roff[s], j)),
+                             *reinterpret_cast<const float2*>(
+                                 bl + __shfl_sync(0xffffffffu, roff[s], j + 1)));
                 }
                 if (j < rows_m) {
-                    const float2 u = *reinterpret_cast<const float2*>(bm + ((omv << 3) & 8u));
+                    const float2 u =
+                        *reinterpret_cast<const float2*>(bl + __shfl_sync(0xffffffffu, roff[s], j));
                     if (kExact) {
                         qa0 += __double2ll_rn((double)u.x * sx);
                         qa1 += __double2ll_rn((double)u.y * sx);
@@ -583,8 +573,7 @@ __global__ void __launch_bounds__(kTmaWarps * 32, 2) k_gather_tma(
                     // lane = row: exact FP64 distance to w_b, features in order
                     // 8-byte reads (d is even): the 208-B slot stride then costs a
                     // 2-way bank conflict instead of the 4-way of 4-byte reads
-                    const float2* xr = reinterpret_cast<const float2*>(
-                        bs + lane * rs + ((om >> lane) & 1u) * 8);
+                    const float2* xr = reinterpret_cast<const float2*>(bs + roff[s]);
                     double d2 = 0.0;
                     for (uint32_t k2 = 0; k2 < D / 2; ++k2) {
                         const float2 v = xr[k2];
