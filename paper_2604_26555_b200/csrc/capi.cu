@@ -1181,6 +1181,9 @@ int tsom_set_option(tsom_engine* eng, int key, int64_t value) {
             case 92:  // diagnostics: gathered split L2 prefetch distance in chunks (0 = off)
                 tsom::g_split_prefetch = (int)value;
                 break;
+            case 91:  // diagnostics: gathered split rows staged by TMA (1, default) or loaded (0)
+                tsom::g_split_tma = (int)value;
+                break;
             case 93:  // diagnostics: fewest rows a BMU-order re-layout is made for
                 eng->row_order_min = (uint64_t)value;
                 break;

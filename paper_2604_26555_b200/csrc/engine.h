@@ -439,6 +439,7 @@ cudaError_t launch_bmu_tc(int kind, const void* tiles, uint64_t n, const uint32_
 extern uint32_t g_k1_debug;
 extern int g_split_v1;
 extern int g_split_prefetch;
+extern int g_split_tma;
 extern int g_gather_kind;
 extern int g_merge_v1;
 int k1_trace_copy(unsigned long long* out, uint32_t n);

@@ -415,12 +415,21 @@ constexpr int kSplitWarpRows = 16;
 
 // img_w > 0: the rows go to a row-major image instead (row r at tiles + r *
 // img_w halves, cores [0, kpad / 8) of it; launch_split_image).
-__global__ void __launch_bounds__(kSplitThreads, 4) k_split_rows_f16(
+//
+// kTma (gathered rows: a selection or the near-tie list, d even <= 64, rows
+// 8-byte aligned): the rows are not loaded through registers but staged by
+// TMA — lane l < 16 bulk-copies row l's 16-byte window into the warp's
+// staging buffer — double-buffered, so the next chunk's 16 rows are in flight
+// while this one is converted (the register loads keep only one chunk in
+// flight per warp at the 64 registers of 4 blocks per SM).
+template <bool kTma>
+__global__ void __launch_bounds__(kSplitThreads, kTma ? 2 : 4) k_split_rows_f16(
     const float* __restrict__ x, uint32_t ldx, const uint32_t* __restrict__ sel,
     const uint32_t* __restrict__ idx, const uint32_t* __restrict__ dev_n, uint64_t n_host,
     uint32_t D, const float* __restrict__ scale, TieWin win, uint8_t* __restrict__ tiles,
     float* __restrict__ xn2, uint32_t img_w = 0, int prefetch = 0) {
     extern __shared__ __align__(16) uint8_t split_wsm[];
+    __shared__ __align__(8) uint64_t sbars[kTma ? kSplitThreads / 32 : 1][2];
     const uint64_t n = dev_n ? min((uint64_t)*dev_n, n_host) : n_host;
     constexpr uint32_t kChunksPerTile = kTcTileM / kSplitWarpRows;
     const uint64_t nchunks = (n + kTcTileM - 1) / kTcTileM * kChunksPerTile;
@@ -433,16 +442,59 @@ __global__ void __launch_bounds__(kSplitThreads, 4) k_split_rows_f16(
     __half* img = reinterpret_cast<__half*>(split_wsm) + (size_t)w * kSplitWarpRows * hs;
     const __half one = __float2half(1.0f), zero = __float2half(0.0f);
     const uint64_t nwarps = (uint64_t)gridDim.x * (kSplitThreads / 32);
-    for (uint64_t c = blockIdx.x * (uint64_t)(kSplitThreads / 32) + w; c < nchunks; c += nwarps) {
+    // kTma: staging buffers [2][16 rows][slot] after the 8 warps' images
+    const uint32_t slot = (D * 4 + 8 + 15) / 16 * 16;
+    uint8_t* stage = split_wsm + (size_t)(kSplitThreads / 32) * kSplitWarpRows * hs * sizeof(__half) +
+                     (size_t)w * 2 * kSplitWarpRows * slot;
+    uint32_t phase = 0;
+    // issue chunk cc into buffer b: lane l < 16 copies row l's window; returns
+    // the row's byte offset in the buffer (lane l)
+    auto stage_issue = [&](uint64_t cc, int b) -> uint32_t {
+        const uint64_t q0 = cc * kSplitWarpRows;
+        const bool mine = lane < (uint32_t)kSplitWarpRows && cc < nchunks && q0 + lane < n;
+        uint64_t a = 0;
+        uint32_t len = 0;
+        if (mine) {
+            const uint64_t pos = idx ? (uint64_t)idx[q0 + lane] : q0 + lane;
+            a = reinterpret_cast<uint64_t>(x + (sel ? (uint64_t)sel[pos] : pos) * ldx);
+            len = (uint32_t)(((a + D * 4u + 15) & ~15ull) - (a & ~15ull));
+        }
+        const uint32_t total = __reduce_add_sync(0xffffffffu, len);
+        asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
+        if (lane == 0) ptx::mbar_expect_tx(&sbars[w][b], total);
+        __syncwarp();
+        if (mine)
+            ptx::bulk_g2s(stage + ((size_t)b * kSplitWarpRows + lane) * slot,
+                          reinterpret_cast<const void*>(a & ~15ull), len, &sbars[w][b]);
+        return ((size_t)b * kSplitWarpRows + (lane & 15u)) * slot + (uint32_t)(a & 15);
+    };
+    uint32_t soff[2] = {0u, 0u};
+    const uint64_t cfirst = blockIdx.x * (uint64_t)(kSplitThreads / 32) + w;
+    if (kTma) {
+        if (lane == 0) {
+            ptx::mbar_init(&sbars[w][0], 1);
+            ptx::mbar_init(&sbars[w][1], 1);
+            asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
+        }
+        __syncwarp();
+        soff[0] = stage_issue(cfirst, 0);
+    }
+    int sb = 0;
+    for (uint64_t c = cfirst; c < nchunks; c += nwarps, sb ^= 1) {
         const uint64_t r0 = c * kSplitWarpRows;
         const uint32_t rows =
             r0 >= n ? 0u : (n - r0 < (uint64_t)kSplitWarpRows ? (uint32_t)(n - r0) : kSplitWarpRows);
         uint64_t myrow = 0;
-        if (lane < rows) {
+        if (!kTma && lane < rows) {
             const uint64_t pos = idx ? (uint64_t)idx[r0 + lane] : r0 + lane;
             myrow = sel ? (uint64_t)sel[pos] : pos;
         }
-        if ((sel || idx) && prefetch) {
+        if (kTma) {
+            soff[sb ^ 1] = stage_issue(c + nwarps, sb ^ 1);
+            ptx::mbar_wait(&sbars[w][sb], (phase >> sb) & 1u);
+            phase ^= 1u << sb;
+        }
+        if (!kTma && (sel || idx) && prefetch) {
             // gathered rows: the warp's chunk `prefetch` iterations ahead into
             // L2 while this one is loaded and converted (lane l < 16: row l,
             // lane l + 16: its second 128-B line), raising the rows in flight
@@ -453,29 +505,55 @@ __global__ void __launch_bounds__(kSplitThreads, 4) k_split_rows_f16(
                 asm volatile("prefetch.global.L2 [%0];" ::"l"(a));
             }
         }
-        float v[kSplitWarpRows][2];
-#pragma unroll
-        for (int i = 0; i < kSplitWarpRows; ++i) {
-            const uint64_t rb = __shfl_sync(0xffffffffu, myrow, i) * ldx;
-            v[i][0] = ((uint32_t)i < rows && lane < D) ? __ldg(x + rb + lane) : 0.0f;
-            v[i][1] = ((uint32_t)i < rows && lane + 32u < D) ? __ldg(x + rb + lane + 32u) : 0.0f;
-        }
         double p[kSplitWarpRows];
+        if (kTma) {
+            // lane l: the adjacent elements 2l, 2l + 1 (d even): one packed
+            // conversion per half pair (F2FP) and 4-byte image stores; the
+            // halves are those of the element-wise path (both round to nearest)
+            const uint32_t so = soff[sb];
+            const bool on = 2u * lane < D;
 #pragma unroll
-        for (int i = 0; i < kSplitWarpRows; ++i) {
-            __half* row = img + i * hs;
-#pragma unroll
-            for (int h = 0; h < 2; ++h) {
-                const uint32_t k = lane + 32u * h;
-                if (k < D) {
-                    const float xv = v[i][h] * s;
-                    const __half xh = __float2half_rn(xv);
-                    row[k] = xh;
-                    row[D + k] = __float2half_rn(xv - __half2float(xh));
-                    row[2 * D + k] = xh;
+            for (int i = 0; i < kSplitWarpRows; ++i) {
+                const uint8_t* rs = stage + __shfl_sync(0xffffffffu, so, i);
+                const float2 v = ((uint32_t)i < rows && on)
+                                     ? *reinterpret_cast<const float2*>(rs + 8u * lane)
+                                     : make_float2(0.0f, 0.0f);
+                if (on) {
+                    __half* row = img + i * hs;
+                    const float x0 = v.x * s, x1 = v.y * s;
+                    const __half2 hh = __floats2half2_rn(x0, x1);
+                    const float2 hf = __half22float2(hh);
+                    const __half2 hl = __floats2half2_rn(x0 - hf.x, x1 - hf.y);
+                    *reinterpret_cast<__half2*>(row + 2u * lane) = hh;
+                    *reinterpret_cast<__half2*>(row + D + 2u * lane) = hl;
+                    *reinterpret_cast<__half2*>(row + 2u * D + 2u * lane) = hh;
                 }
+                p[i] = (double)v.x * (double)v.x + (double)v.y * (double)v.y;
             }
-            p[i] = (double)v[i][0] * (double)v[i][0] + (double)v[i][1] * (double)v[i][1];
+        } else {
+            float v[kSplitWarpRows][2];
+#pragma unroll
+            for (int i = 0; i < kSplitWarpRows; ++i) {
+                const uint64_t rb = __shfl_sync(0xffffffffu, myrow, i) * ldx;
+                v[i][0] = ((uint32_t)i < rows && lane < D) ? __ldg(x + rb + lane) : 0.0f;
+                v[i][1] = ((uint32_t)i < rows && lane + 32u < D) ? __ldg(x + rb + lane + 32u) : 0.0f;
+            }
+#pragma unroll
+            for (int i = 0; i < kSplitWarpRows; ++i) {
+                __half* row = img + i * hs;
+#pragma unroll
+                for (int h = 0; h < 2; ++h) {
+                    const uint32_t k = lane + 32u * h;
+                    if (k < D) {
+                        const float xv = v[i][h] * s;
+                        const __half xh = __float2half_rn(xv);
+                        row[k] = xh;
+                        row[D + k] = __float2half_rn(xv - __half2float(xh));
+                        row[2 * D + k] = xh;
+                    }
+                }
+                p[i] = (double)v[i][0] * (double)v[i][0] + (double)v[i][1] * (double)v[i][1];
+            }
         }
         // transposing butterfly: after the level with offset o, lanes with bit
         // o set hold the upper half of the remaining rows
@@ -536,6 +614,7 @@ __global__ void __launch_bounds__(kSplitThreads, 4) k_split_rows_f16(
 
 int g_split_v1 = 0;  // debug: the element-wise split (TSOM option 98)
 int g_split_prefetch = 1;  // gathered split: L2 prefetch distance in chunks (option 92; 0 off)
+int g_split_tma = 1;       // gathered split: rows staged by TMA (option 91; 0 = register loads)
 
 void launch_split_rows(int kind, const float* x, const uint32_t* sel, const uint32_t* idx,
                        uint64_t n, uint32_t D, const float* scale, TieWin win, void* tiles,
@@ -555,16 +634,28 @@ void launch_split_rows(int kind, const float* x, const uint32_t* sel, const uint
     else {
         const size_t wsmem = (size_t)(kSplitThreads / 32) * kSplitWarpRows *
                              (tc_geom(kTcF16, D).kpad + 8) * sizeof(__half);
+        uint64_t blocks = (n + kTcTileM - 1) / kTcTileM;  // 8 warps x 16 rows per tile
+        // gathered rows staged by TMA (needs d even <= 64, 8-byte aligned rows)
+        const bool tma = (sel || idx) && g_split_tma && D % 2 == 0 && D <= 64 && ldx % 2 == 0 &&
+                         (reinterpret_cast<uintptr_t>(x) & 15u) == 0;
+        if (tma) {
+            const size_t tsmem = wsmem + (size_t)(kSplitThreads / 32) * 2 * kSplitWarpRows *
+                                             ((D * 4 + 8 + 15) / 16 * 16);
+            ensure_smem_attr((const void*)k_split_rows_f16<true>, tsmem);
+            if (blocks > 148ull * 2) blocks = 148ull * 2;
+            TSOM_LAUNCH(k_split_rows_f16<true><<<(unsigned)blocks, kSplitThreads, tsmem, st>>>(
+                x, ldx, sel, idx, dev_n, n, D, scale, win, t, xn2, 0u, 0));
+            return;
+        }
         bool first = false;
-        ensure_smem_attr((const void*)k_split_rows_f16,
+        ensure_smem_attr((const void*)k_split_rows_f16<false>,
                          (kSplitThreads / 32) * kSplitWarpRows * (kTcF16MaxK + 8) * sizeof(__half),
                          &first);
         if (first)
-            cudaFuncSetAttribute(k_split_rows_f16, cudaFuncAttributePreferredSharedMemoryCarveout,
-                                 100);
-        uint64_t blocks = (n + kTcTileM - 1) / kTcTileM;  // 8 warps x 16 rows per tile
+            cudaFuncSetAttribute(k_split_rows_f16<false>,
+                                 cudaFuncAttributePreferredSharedMemoryCarveout, 100);
         if (blocks > 148ull * 8) blocks = 148ull * 8;
-        TSOM_LAUNCH(k_split_rows_f16<<<(unsigned)blocks, kSplitThreads, wsmem, st>>>(
+        TSOM_LAUNCH(k_split_rows_f16<false><<<(unsigned)blocks, kSplitThreads, wsmem, st>>>(
             x, ldx, sel, idx, dev_n, n, D, scale, win, t, xn2, 0u, g_split_prefetch));
     }
 }
@@ -576,14 +667,15 @@ void launch_split_image(const float* x, uint32_t ldx, uint64_t n, uint32_t D, co
     const size_t wsmem = (size_t)(kSplitThreads / 32) * kSplitWarpRows *
                          (tc_geom(kTcF16, D).kpad + 8) * sizeof(__half);
     bool first = false;
-    ensure_smem_attr((const void*)k_split_rows_f16,
+    ensure_smem_attr((const void*)k_split_rows_f16<false>,
                      (kSplitThreads / 32) * kSplitWarpRows * (kTcF16MaxK + 8) * sizeof(__half),
                      &first);
     if (first)
-        cudaFuncSetAttribute(k_split_rows_f16, cudaFuncAttributePreferredSharedMemoryCarveout, 100);
+        cudaFuncSetAttribute(k_split_rows_f16<false>, cudaFuncAttributePreferredSharedMemoryCarveout,
+                             100);
     uint64_t blocks = (n + kTcTileM - 1) / kTcTileM;
     if (blocks > 148ull * 8) blocks = 148ull * 8;
-    TSOM_LAUNCH(k_split_rows_f16<<<(unsigned)blocks, kSplitThreads, wsmem, st>>>(
+    TSOM_LAUNCH(k_split_rows_f16<false><<<(unsigned)blocks, kSplitThreads, wsmem, st>>>(
         x, ldx, nullptr, nullptr, nullptr, n, D, scale, win, static_cast<uint8_t*>(img), xn2,
         img_w));
 }
