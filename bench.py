@@ -904,12 +904,12 @@ def roofline_peak(kernel, pk):
 # ncu --set full, one launch of K1 at the bench shape (1e7 x 50, K=1024, rows in
 # BMU order, A tiles multicast over clusters of 2 group CTAs):
 # dram__bytes_read.sum + dram__bytes_write.sum, bytes per launch
-# (profiles/r02c_ncu_full_summary.json, scripts/ncu_round2c.sh).  The split A
-# tiles are 3.2 GB: each now leaves DRAM about once (6.1 GB without the
-# multicast, the 4 group CTAs streaming every tile and L2 catching part).
-K1_TRAFFIC = {3: 3.309947e9 + 0.322691e9}
+# (profiles/r02c_ncu_full_summary.json, scripts/round2d_profiles.sh).  The split A
+# tiles are 3.2 GB: each leaves DRAM 1.0-1.16 times over the captures (6.1 GB
+# without the multicast, the 4 group CTAs streaming every tile and L2 catching part).
+K1_TRAFFIC = {3: 3.721560e9 + 0.320970e9}
 K1_TRAFFIC_SRC = "profiles/r02c_ncu_full_summary.json, k1_bmu_tc<2, 0, 0, 1> (clusters of 2): " \
-                 "3.31 GB read (the 3.2 GB of split A tiles about once; each cluster loads a " \
+                 "3.72 GB read (the 3.2 GB of split A tiles 1.16 times; each cluster loads a " \
                  "tile once and multicasts it) + 0.32 GB per-group partial-result writes"
 
 
