@@ -13,9 +13,11 @@
 //   k_colscan   per-node exclusive scan over blocks   (in place) + node totals
 //   k_nodescan  node starts, counts c_b, piece table  (one block)
 //   k_scatter   stable counting sort of row positions by BMU
-//   k_gather    one warp per piece (<= 256 rows of one node): x rows gathered
-//               in batches of 8, FP64 register accumulation, optional exact
-//               distances; one partial row per piece
+//   k_gather_tma  one warp per piece (<= 256 rows of one node): 32-row
+//               batches staged by TMA bulk copies (one per run of consecutive
+//               rows), FP64 register accumulation, optional exact distances;
+//               one partial row per piece (k_gather_async / k_gather_any: the
+//               cp.async and register-load variants for other shapes)
 //   k_piece_reduce  sums the pieces of every node in order -> sums buffer
 // HBM traffic per row: ~4 B x 3 (bmu passes) + 8 B (sorted position) + the
 // 200 B row => ~212 B/row (204 B algorithmic).
@@ -462,8 +464,8 @@ __global__ void __launch_bounds__(kTmaWarps * 32, 2) k_gather_tma(
     double sx = 0.0, sd = 0.0;
     if (kExact) exact_scales(xmax2, w2max, &sx, &sd);
 
-    // Batch copy: every run of consecutive packed rows (rows kept in BMU order,
-    // DESIGN.md §4, keep most of a node's rows in runs) is one bulk copy of
+    // Batch copy: every run of consecutive packed rows (the BMU-ordered
+    // residency, keeps most of a node's rows in runs) is one bulk copy of
     // its 16-byte-aligned window, issued by the run's first lane into that
     // lane's slot; a run of k rows fits the k slots it starts (window <= 4dk
     // + 16 <= k slot for k >= 2).  Padded or scattered rows are runs of one.
